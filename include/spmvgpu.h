@@ -1,0 +1,191 @@
+/*
+ * spmvgpu.h -- C-ABI of the B200-native RNS-BFV backend for the CSSC
+ * encrypted-SpMV cloud phase.  Plain pointers and sizes only; no exceptions
+ * cross this boundary: every call returns SPMVGPU_OK or a negative status and
+ * leaves a thread-local message for spmvgpu_last_error().
+ *
+ * What each group replaces in the reference (/root/reference/proj):
+ *   context + keys     HeParams / SimBackend ctor      include/spmv/he.hpp:35-43, 119-139
+ *   ciphertext arena   Ciphertext value type           include/spmv/he.hpp:51-55
+ *   encrypt/decrypt    HeBackend::encode/encrypt/decrypt  include/spmv/he.hpp:95-100
+ *   add/mul/rotate     HeBackend::add/multiply/multiply_plain/rotate  he.hpp:102-110
+ *   cloud plan         the cloud loop of spmv()          src/protocol.cpp:121-140
+ *                      + intra_chunk_sum / inter_chunk_sum  src/aggregate.cpp:36-74
+ *   cssc_spmv_*        spmv / spmv_partitioned          include/spmv/protocol.hpp:62-71
+ *   cssc_pack_*        csr_to_cssc / generate_chunks / partition_rows / reorg_vector
+ *                      include/spmv/sparse.hpp:68, chunk.hpp:30-35, reorg.hpp:21
+ */
+#ifndef SPMVGPU_H
+#define SPMVGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes; the C++ adapter maps them back to the reference's exception
+ * types (include/spmv/errors.hpp:13-66) */
+enum {
+    SPMVGPU_OK = 0,
+    SPMVGPU_ERR_INVALID_ARGUMENT = -1,  /* std::invalid_argument */
+    SPMVGPU_ERR_OVER_LENGTH = -2,       /* OverLengthError */
+    SPMVGPU_ERR_NOISE_EXHAUSTED = -3,   /* NoiseExhaustedError */
+    SPMVGPU_ERR_DIMENSION = -4,         /* DimensionMismatchError */
+    SPMVGPU_ERR_COLUMN_TOO_TALL = -5,   /* ColumnTooTallError */
+    SPMVGPU_ERR_INDEX_RANGE = -6,       /* IndexOutOfRangeError */
+    SPMVGPU_ERR_DUPLICATE = -7,         /* DuplicateEntryError */
+    SPMVGPU_ERR_CUDA = -8,
+    SPMVGPU_ERR_INTERNAL = -9
+};
+
+typedef struct spmvgpu_ctx spmvgpu_ctx;
+typedef struct spmvgpu_plan spmvgpu_plan;
+typedef uint64_t spmvgpu_ct; /* opaque device ciphertext handle */
+
+typedef struct {
+    int logn;        /* ring degree N = 2^logn; slots per BFV row S = N/2 */
+    int L;           /* data primes (ciphertext modulus Q) */
+    int K;           /* special primes (key switching modulus P) */
+    int alpha;       /* primes per key-switching digit */
+    int qbits, pbits;
+    uint64_t t;      /* plaintext modulus, prime, t = 1 mod 2N */
+    uint64_t seed;   /* seeds every sampled polynomial (keys, encryptions) */
+    int device;
+    /* reference HeParams fields kept for API parity (he.hpp:24-43) */
+    double ciphertext_size_mb;
+    int noise_initial, noise_ct_ct, noise_ct_pt, noise_add, noise_rot;
+} spmvgpu_params;
+
+const char* spmvgpu_last_error(void);
+void spmvgpu_default_params(int logn, spmvgpu_params* out);
+
+int spmvgpu_ctx_create(const spmvgpu_params* p, spmvgpu_ctx** out);
+void spmvgpu_ctx_destroy(spmvgpu_ctx* c);
+/* primes (Q | P | B | t) and basic sizes */
+int spmvgpu_ctx_primes(const spmvgpu_ctx* c, uint64_t* primes, int cap, int* count);
+int spmvgpu_ctx_sizes(const spmvgpu_ctx* c, uint64_t* n, uint64_t* slots, uint64_t* ct_words,
+                      uint64_t* ksk_words, int* dnum);
+int spmvgpu_sync(spmvgpu_ctx* c);
+/* opaque CUDA stream the context works on (cudaStream_t) */
+void* spmvgpu_stream(spmvgpu_ctx* c);
+
+/* keys: generated on the device from the seed; download in canonical
+ * coefficient form for word-level parity checks */
+int spmvgpu_galois_keys(spmvgpu_ctx* c, const int64_t* steps, size_t n);
+uint32_t spmvgpu_galois_element(const spmvgpu_ctx* c, int64_t step);
+int spmvgpu_download_sk(spmvgpu_ctx* c, int64_t* out);
+int spmvgpu_download_pk(spmvgpu_ctx* c, uint64_t* out);
+int spmvgpu_download_ksk(spmvgpu_ctx* c, uint32_t which, uint64_t* out); /* 0 = relin */
+
+/* ciphertext arena: [2][L][N] uint64 words, coefficient form */
+int spmvgpu_ct_alloc(spmvgpu_ctx* c, size_t count, spmvgpu_ct* out);
+int spmvgpu_ct_free(spmvgpu_ctx* c, const spmvgpu_ct* cts, size_t count);
+int spmvgpu_ct_upload(spmvgpu_ctx* c, spmvgpu_ct ct, const uint64_t* words);
+int spmvgpu_ct_download(spmvgpu_ctx* c, spmvgpu_ct ct, uint64_t* words);
+
+/* batched encode+encrypt: item i encodes vals[offsets[i] .. offsets[i+1]) into
+ * row 0 of the slots with encryption stream streams[i] (0 = next fresh id;
+ * streams may be NULL) */
+int spmvgpu_encrypt(spmvgpu_ctx* c, const int64_t* vals, const uint64_t* offsets,
+                    const uint64_t* streams, const spmvgpu_ct* out, size_t n);
+/* batched decrypt+decode: slots is n x S residues mod t; budgets = measured
+ * invariant-noise budget (bits, saturates near 60) */
+int spmvgpu_decrypt(spmvgpu_ctx* c, const spmvgpu_ct* cts, size_t n, uint64_t* slots,
+                    int32_t* budgets);
+int spmvgpu_add(spmvgpu_ctx* c, const spmvgpu_ct* a, const spmvgpu_ct* b, const spmvgpu_ct* out,
+                size_t n);
+int spmvgpu_mul_relin(spmvgpu_ctx* c, const spmvgpu_ct* a, const spmvgpu_ct* b,
+                      const spmvgpu_ct* out, size_t n);
+/* out_i = rot(src_i, steps_i) (cyclic left over S slots, negative = right) */
+int spmvgpu_rotate(spmvgpu_ctx* c, const spmvgpu_ct* src, const int64_t* steps,
+                   const spmvgpu_ct* out, size_t n);
+/* out_i = acc_i + rot(src_i, steps_i): the fused rotate-and-add tree step */
+int spmvgpu_rotate_add(spmvgpu_ctx* c, const spmvgpu_ct* acc, const spmvgpu_ct* src,
+                       const int64_t* steps, const spmvgpu_ct* out, size_t n);
+/* out_i = a_i * encode(vals[offsets[i] .. offsets[i+1])) */
+int spmvgpu_mul_plain(spmvgpu_ctx* c, const spmvgpu_ct* a, const int64_t* vals,
+                      const uint64_t* offsets, const spmvgpu_ct* out, size_t n);
+/* KAT: in-place forward/inverse NTT of `limbs` host limbs modulo prime index */
+int spmvgpu_ntt(spmvgpu_ctx* c, int prime_index, uint64_t* data, size_t limbs, int inverse);
+
+/* ---- the batched cloud phase: every chunk of every slice in shared launches ----
+ * chunk i: product of a_cts[i] and b_cts[i], folded by rotation_schedule(r_i, c_i),
+ * masked to its first r_i slots and accumulated into out_cts[slice_i]. */
+int spmvgpu_plan_create(spmvgpu_ctx* c, size_t n_chunks, const uint64_t* r, const uint64_t* cols,
+                        const uint32_t* slice, size_t n_slices, const spmvgpu_ct* a_cts,
+                        const spmvgpu_ct* b_cts, const spmvgpu_ct* out_cts, spmvgpu_plan** out);
+int spmvgpu_plan_run(spmvgpu_plan* p);         /* enqueue on the context stream */
+int spmvgpu_plan_capture(spmvgpu_plan* p);     /* record a CUDA graph; later runs replay it */
+typedef struct {
+    uint64_t chunks, slices, levels, kernels_per_run, limb_ntts_per_run;
+    uint64_t rotations, distinct_keys;
+    uint64_t hbm_bytes_algorithmic; /* compulsory bytes per run (SURVEY 8(d) formulas) */
+    uint64_t key_bytes_per_run;
+} spmvgpu_plan_stats;
+int spmvgpu_plan_stats_get(const spmvgpu_plan* p, spmvgpu_plan_stats* out);
+void spmvgpu_plan_destroy(spmvgpu_plan* p);
+
+/* ---- protocol level (host C++ above the device ABI) ---- */
+typedef struct {
+    uint64_t n_mult_cc, n_mult_cp, n_rot, n_add, n_enc, n_dec;
+} cssc_ledger;
+typedef struct {
+    int64_t from, to, kind, payload_bytes, ciphertext_count;
+} cssc_message; /* roles A=0 B=1 Cloud=2; kinds per protocol.hpp:25-31 */
+typedef struct {
+    uint64_t rows, cols;
+    const int64_t* row_ptrs;    /* rows + 1 */
+    const int64_t* col_indices; /* nnz */
+    const int64_t* values;      /* nnz */
+} cssc_csr;
+typedef struct {
+    cssc_ledger ledger;
+    uint64_t n_ct;
+    int32_t noise_model_bits;     /* reference model counter (87 with >= 1 chunk) */
+    int32_t noise_measured_bits;  /* min measured BFV budget over slices */
+    uint64_t n_messages;
+} cssc_result;
+
+/* spmv_partitioned on the GPU backend: values (rows) in original row order */
+int cssc_spmv_partitioned(spmvgpu_ctx* c, const cssc_csr* m, const int64_t* v, uint64_t vlen,
+                          uint64_t chunk_size, int key_holder, int64_t* values,
+                          cssc_result* res, cssc_message* msgs, uint64_t msg_cap);
+/* several independent matrices in shared launches (BASELINE config 5) */
+int cssc_spmv_batch(spmvgpu_ctx* c, const cssc_csr* ms, const int64_t* const* vs, size_t nmat,
+                    uint64_t chunk_size, int key_holder, int64_t* const* values,
+                    cssc_result* res);
+
+/* staged form for benchmarking: pack + encrypt once, run the cloud phase many
+ * times from device-resident ciphertexts, then decrypt */
+typedef struct cssc_job cssc_job;
+int cssc_job_create(spmvgpu_ctx* c, const cssc_csr* ms, const int64_t* const* vs, size_t nmat,
+                    uint64_t chunk_size, cssc_job** out);
+int cssc_job_encrypt(cssc_job* j);            /* client phase: encode + encrypt on device */
+int cssc_job_cloud(cssc_job* j, int use_graph); /* cloud phase, enqueued (no sync) */
+int cssc_job_finish(cssc_job* j, int64_t* const* values, cssc_result* res); /* decrypt */
+int cssc_job_plan_stats(const cssc_job* j, spmvgpu_plan_stats* out);
+int cssc_job_input_bytes(const cssc_job* j, uint64_t* h2d, uint64_t* d2h);
+void cssc_job_destroy(cssc_job* j);
+
+/* host pack helpers (reference algorithms, exposed for parity tests) */
+int64_t cssc_pack_chunks(const cssc_csr* m, uint64_t budget, int64_t* r_list, int64_t* c_list,
+                         int64_t* vflat, int64_t* cflat, int64_t* row_map, uint64_t* flat_total);
+int cssc_rotation_schedule(uint64_t rows, uint64_t cols, uint64_t* offsets, int32_t* from_acc);
+/* synthetic generators matching the reference's (synthetic.cpp:32-86) plus the
+ * BASELINE config shapes */
+int64_t cssc_random_sparse_csr(uint64_t rows, uint64_t cols, uint64_t nnz, uint64_t seed,
+                               int64_t lo, int64_t hi, int64_t* rp, int64_t* ci, int64_t* va);
+void cssc_random_vector(uint64_t len, uint64_t seed, int64_t lo, int64_t hi, int64_t* out);
+void cssc_random_nonzero_vector(uint64_t len, uint64_t seed, int64_t lo, int64_t hi, int64_t* out);
+int64_t cssc_power_law_csr(uint64_t n, double mean_degree, double exponent, uint64_t seed,
+                           int64_t lo, int64_t hi, int64_t* rp, int64_t* ci, int64_t* va,
+                           uint64_t cap);
+int64_t cssc_stencil27_csr(uint64_t side, uint64_t seed, int64_t lo, int64_t hi, int64_t* rp,
+                           int64_t* ci, int64_t* va, uint64_t cap);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

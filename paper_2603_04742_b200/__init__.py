@@ -1,0 +1,518 @@
+"""B200-native RNS-BFV evaluation of the CSSC encrypted SpMV (arxiv 2603.04742).
+
+Thin ctypes layer over the in-tree native library ``lib/libcssc_he.so``
+(CUDA sm_100a kernels + C++ host, C-ABI in ``include/spmvgpu.h``).  There is
+no Python or CPU fallback: importing works without a GPU (so the C-ABI can be
+inspected), but every compute call goes through the native library and fails
+loudly when it is missing or when no CUDA device is present.
+
+Mirrors of the reference API (``/root/reference/proj/include/spmv``):
+  Context           ~ HeParams + SimBackend construction (he.hpp:35-43, 119-139)
+  Context.encrypt / decrypt / add / mul_relin / mul_plain / rotate
+                    ~ HeBackend virtuals (he.hpp:95-114)
+  spmv_partitioned  ~ spmv::spmv_partitioned (protocol.hpp:69-71)
+  spmv_batch        ~ several independent spmv_partitioned runs in shared launches
+  Job               staged pack/encrypt -> cloud -> decrypt, for benchmarking
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from pathlib import Path
+
+import numpy as np
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "lib" / "libcssc_he.so"
+
+u64p = C.POINTER(C.c_uint64)
+i64p = C.POINTER(C.c_int64)
+i32p = C.POINTER(C.c_int32)
+u32p = C.POINTER(C.c_uint32)
+
+
+class SpmvgpuParams(C.Structure):
+    _fields_ = [("logn", C.c_int), ("L", C.c_int), ("K", C.c_int), ("alpha", C.c_int),
+                ("qbits", C.c_int), ("pbits", C.c_int), ("t", C.c_uint64), ("seed", C.c_uint64),
+                ("device", C.c_int), ("ciphertext_size_mb", C.c_double),
+                ("noise_initial", C.c_int), ("noise_ct_ct", C.c_int), ("noise_ct_pt", C.c_int),
+                ("noise_add", C.c_int), ("noise_rot", C.c_int)]
+
+
+class PlanStats(C.Structure):
+    _fields_ = [(n, C.c_uint64) for n in (
+        "chunks", "slices", "levels", "kernels_per_run", "limb_ntts_per_run", "rotations",
+        "distinct_keys", "hbm_bytes_algorithmic", "key_bytes_per_run")]
+
+
+class Ledger(C.Structure):
+    _fields_ = [(n, C.c_uint64) for n in ("n_mult_cc", "n_mult_cp", "n_rot", "n_add", "n_enc", "n_dec")]
+
+
+class Message(C.Structure):
+    _fields_ = [(n, C.c_int64) for n in ("from_", "to", "kind", "payload_bytes", "ciphertext_count")]
+
+
+class CsrC(C.Structure):
+    _fields_ = [("rows", C.c_uint64), ("cols", C.c_uint64), ("row_ptrs", i64p),
+                ("col_indices", i64p), ("values", i64p)]
+
+
+class ResultC(C.Structure):
+    _fields_ = [("ledger", Ledger), ("n_ct", C.c_uint64), ("noise_model_bits", C.c_int32),
+                ("noise_measured_bits", C.c_int32), ("n_messages", C.c_uint64)]
+
+
+# C-ABI symbol table: name -> (restype, argtypes).  tests check every entry
+# against include/spmvgpu.h.
+_SIGS = {
+    "spmvgpu_last_error": (C.c_char_p, []),
+    "spmvgpu_default_params": (None, [C.c_int, C.POINTER(SpmvgpuParams)]),
+    "spmvgpu_ctx_create": (C.c_int, [C.POINTER(SpmvgpuParams), C.POINTER(C.c_void_p)]),
+    "spmvgpu_ctx_destroy": (None, [C.c_void_p]),
+    "spmvgpu_ctx_primes": (C.c_int, [C.c_void_p, u64p, C.c_int, C.POINTER(C.c_int)]),
+    "spmvgpu_ctx_sizes": (C.c_int, [C.c_void_p, u64p, u64p, u64p, u64p, C.POINTER(C.c_int)]),
+    "spmvgpu_sync": (C.c_int, [C.c_void_p]),
+    "spmvgpu_stream": (C.c_void_p, [C.c_void_p]),
+    "spmvgpu_galois_keys": (C.c_int, [C.c_void_p, i64p, C.c_size_t]),
+    "spmvgpu_galois_element": (C.c_uint32, [C.c_void_p, C.c_int64]),
+    "spmvgpu_download_sk": (C.c_int, [C.c_void_p, i64p]),
+    "spmvgpu_download_pk": (C.c_int, [C.c_void_p, u64p]),
+    "spmvgpu_download_ksk": (C.c_int, [C.c_void_p, C.c_uint32, u64p]),
+    "spmvgpu_ct_alloc": (C.c_int, [C.c_void_p, C.c_size_t, u64p]),
+    "spmvgpu_ct_free": (C.c_int, [C.c_void_p, u64p, C.c_size_t]),
+    "spmvgpu_ct_upload": (C.c_int, [C.c_void_p, C.c_uint64, u64p]),
+    "spmvgpu_ct_download": (C.c_int, [C.c_void_p, C.c_uint64, u64p]),
+    "spmvgpu_encrypt": (C.c_int, [C.c_void_p, i64p, u64p, u64p, u64p, C.c_size_t]),
+    "spmvgpu_decrypt": (C.c_int, [C.c_void_p, u64p, C.c_size_t, u64p, i32p]),
+    "spmvgpu_add": (C.c_int, [C.c_void_p, u64p, u64p, u64p, C.c_size_t]),
+    "spmvgpu_mul_relin": (C.c_int, [C.c_void_p, u64p, u64p, u64p, C.c_size_t]),
+    "spmvgpu_rotate": (C.c_int, [C.c_void_p, u64p, i64p, u64p, C.c_size_t]),
+    "spmvgpu_rotate_add": (C.c_int, [C.c_void_p, u64p, u64p, i64p, u64p, C.c_size_t]),
+    "spmvgpu_mul_plain": (C.c_int, [C.c_void_p, u64p, i64p, u64p, u64p, C.c_size_t]),
+    "spmvgpu_ntt": (C.c_int, [C.c_void_p, C.c_int, u64p, C.c_size_t, C.c_int]),
+    "spmvgpu_plan_create": (C.c_int, [C.c_void_p, C.c_size_t, u64p, u64p, u32p, C.c_size_t,
+                                      u64p, u64p, u64p, C.POINTER(C.c_void_p)]),
+    "spmvgpu_plan_run": (C.c_int, [C.c_void_p]),
+    "spmvgpu_plan_capture": (C.c_int, [C.c_void_p]),
+    "spmvgpu_plan_stats_get": (C.c_int, [C.c_void_p, C.POINTER(PlanStats)]),
+    "spmvgpu_plan_destroy": (None, [C.c_void_p]),
+    "cssc_spmv_partitioned": (C.c_int, [C.c_void_p, C.POINTER(CsrC), i64p, C.c_uint64, C.c_uint64,
+                                        C.c_int, i64p, C.POINTER(ResultC), C.POINTER(Message),
+                                        C.c_uint64]),
+    "cssc_spmv_batch": (C.c_int, [C.c_void_p, C.POINTER(CsrC), C.POINTER(i64p), C.c_size_t,
+                                  C.c_uint64, C.c_int, C.POINTER(i64p), C.POINTER(ResultC)]),
+    "cssc_job_create": (C.c_int, [C.c_void_p, C.POINTER(CsrC), C.POINTER(i64p), C.c_size_t,
+                                  C.c_uint64, C.POINTER(C.c_void_p)]),
+    "cssc_job_encrypt": (C.c_int, [C.c_void_p]),
+    "cssc_job_cloud": (C.c_int, [C.c_void_p, C.c_int]),
+    "cssc_job_finish": (C.c_int, [C.c_void_p, C.POINTER(i64p), C.POINTER(ResultC)]),
+    "cssc_job_plan_stats": (C.c_int, [C.c_void_p, C.POINTER(PlanStats)]),
+    "cssc_job_input_bytes": (C.c_int, [C.c_void_p, u64p, u64p]),
+    "cssc_job_destroy": (None, [C.c_void_p]),
+    "cssc_pack_chunks": (C.c_int64, [C.POINTER(CsrC), C.c_uint64, i64p, i64p, i64p, i64p, i64p, u64p]),
+    "cssc_rotation_schedule": (C.c_int, [C.c_uint64, C.c_uint64, u64p, i32p]),
+    "cssc_random_sparse_csr": (C.c_int64, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int64,
+                                           C.c_int64, i64p, i64p, i64p]),
+    "cssc_random_vector": (None, [C.c_uint64, C.c_uint64, C.c_int64, C.c_int64, i64p]),
+    "cssc_random_nonzero_vector": (None, [C.c_uint64, C.c_uint64, C.c_int64, C.c_int64, i64p]),
+    "cssc_power_law_csr": (C.c_int64, [C.c_uint64, C.c_double, C.c_double, C.c_uint64, C.c_int64,
+                                       C.c_int64, i64p, i64p, i64p, C.c_uint64]),
+    "cssc_stencil27_csr": (C.c_int64, [C.c_uint64, C.c_uint64, C.c_int64, C.c_int64, i64p, i64p,
+                                       i64p, C.c_uint64]),
+}
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load the native library (raises if it was not built: no fallback)."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise RuntimeError(f"native library missing: {LIB_PATH} (run __graft_entry__.build())")
+        L = C.CDLL(str(LIB_PATH))
+        for name, (res, args) in _SIGS.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+STATUS = {-1: ValueError, -2: "OverLengthError", -3: "NoiseExhaustedError", -4: "DimensionMismatchError",
+          -5: "ColumnTooTallError", -6: "IndexOutOfRangeError", -7: "DuplicateEntryError",
+          -8: RuntimeError, -9: RuntimeError}
+
+
+class SpmvError(RuntimeError):
+    def __init__(self, status: int, kind: str, msg: str):
+        super().__init__(f"{kind}: {msg}")
+        self.status, self.kind = status, kind
+
+
+def check(status: int) -> None:
+    if status != 0:
+        kind = STATUS.get(status, RuntimeError)
+        name = kind if isinstance(kind, str) else kind.__name__
+        raise SpmvError(status, name, lib().spmvgpu_last_error().decode())
+
+
+def _p(a: np.ndarray, t):
+    return a.ctypes.data_as(t)
+
+
+def _u64(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.uint64))
+
+
+def _i64(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.int64))
+
+
+def default_params(logn: int) -> SpmvgpuParams:
+    p = SpmvgpuParams()
+    lib().spmvgpu_default_params(logn, C.byref(p))
+    return p
+
+
+class Context:
+    """Device-resident RNS-BFV context (keys generated on the GPU from `seed`)."""
+
+    def __init__(self, logn: int = 14, seed: int = 1, device: int = 0, **overrides):
+        p = default_params(logn)
+        p.seed = seed
+        p.device = device
+        for k, v in overrides.items():
+            setattr(p, k, v)
+        self.params = p
+        h = C.c_void_p()
+        check(lib().spmvgpu_ctx_create(C.byref(p), C.byref(h)))
+        self.h = h
+        n, s, ctw, kw = (C.c_uint64() for _ in range(4))
+        dn = C.c_int()
+        check(lib().spmvgpu_ctx_sizes(h, C.byref(n), C.byref(s), C.byref(ctw), C.byref(kw), C.byref(dn)))
+        self.n, self.slots, self.ct_words, self.ksk_words, self.dnum = n.value, s.value, ctw.value, kw.value, dn.value
+        buf = np.zeros(64, np.uint64)
+        cnt = C.c_int()
+        check(lib().spmvgpu_ctx_primes(h, _p(buf, u64p), 64, C.byref(cnt)))
+        self.primes = [int(x) for x in buf[:cnt.value]]
+        self.L, self.K = p.L, p.K
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().spmvgpu_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- memory
+    def alloc(self, n: int) -> np.ndarray:
+        hs = np.zeros(n, np.uint64)
+        if n:
+            check(lib().spmvgpu_ct_alloc(self.h, n, _p(hs, u64p)))
+        return hs
+
+    def free(self, hs) -> None:
+        hs = _u64(hs)
+        if hs.size:
+            check(lib().spmvgpu_ct_free(self.h, _p(hs, u64p), hs.size))
+
+    def upload(self, ct: int, words: np.ndarray) -> None:
+        w = _u64(words)
+        assert w.size == self.ct_words
+        check(lib().spmvgpu_ct_upload(self.h, int(ct), _p(w, u64p)))
+
+    def download(self, ct: int) -> np.ndarray:
+        w = np.zeros(self.ct_words, np.uint64)
+        check(lib().spmvgpu_ct_download(self.h, int(ct), _p(w, u64p)))
+        return w
+
+    # ---- keys
+    def download_sk(self) -> np.ndarray:
+        s = np.zeros(self.n, np.int64)
+        check(lib().spmvgpu_download_sk(self.h, _p(s, i64p)))
+        return s
+
+    def download_pk(self) -> np.ndarray:
+        w = np.zeros(2 * self.L * self.n, np.uint64)
+        check(lib().spmvgpu_download_pk(self.h, _p(w, u64p)))
+        return w
+
+    def download_ksk(self, which: int) -> np.ndarray:
+        w = np.zeros(self.ksk_words, np.uint64)
+        check(lib().spmvgpu_download_ksk(self.h, which, _p(w, u64p)))
+        return w
+
+    def galois_element(self, step: int) -> int:
+        return int(lib().spmvgpu_galois_element(self.h, step))
+
+    # ---- batched ops
+    def encrypt(self, values, streams=None) -> np.ndarray:
+        vals = [_i64(v) for v in values]
+        offs = np.zeros(len(vals) + 1, np.uint64)
+        offs[1:] = np.cumsum([v.size for v in vals])
+        flat = _i64(np.concatenate(vals)) if vals and offs[-1] else np.zeros(1, np.int64)
+        out = self.alloc(len(vals))
+        st = _u64(streams) if streams is not None else None
+        check(lib().spmvgpu_encrypt(self.h, _p(flat, i64p), _p(offs, u64p),
+                                    _p(st, u64p) if st is not None else None, _p(out, u64p), len(vals)))
+        return out
+
+    def decrypt(self, cts):
+        cts = _u64(cts)
+        slots = np.zeros((cts.size, self.slots), np.uint64)
+        b = np.zeros(cts.size, np.int32)
+        check(lib().spmvgpu_decrypt(self.h, _p(cts, u64p), cts.size, _p(slots, u64p), _p(b, i32p)))
+        return slots, b
+
+    def add(self, a, b) -> np.ndarray:
+        a, b = _u64(a), _u64(b)
+        out = self.alloc(a.size)
+        check(lib().spmvgpu_add(self.h, _p(a, u64p), _p(b, u64p), _p(out, u64p), a.size))
+        return out
+
+    def mul_relin(self, a, b) -> np.ndarray:
+        a, b = _u64(a), _u64(b)
+        out = self.alloc(a.size)
+        check(lib().spmvgpu_mul_relin(self.h, _p(a, u64p), _p(b, u64p), _p(out, u64p), a.size))
+        return out
+
+    def rotate(self, a, steps) -> np.ndarray:
+        a, st = _u64(a), _i64(steps)
+        out = self.alloc(a.size)
+        check(lib().spmvgpu_rotate(self.h, _p(a, u64p), _p(st, i64p), _p(out, u64p), a.size))
+        return out
+
+    def rotate_add(self, acc, src, steps) -> np.ndarray:
+        acc, src, st = _u64(acc), _u64(src), _i64(steps)
+        out = self.alloc(acc.size)
+        check(lib().spmvgpu_rotate_add(self.h, _p(acc, u64p), _p(src, u64p), _p(st, i64p), _p(out, u64p),
+                                       acc.size))
+        return out
+
+    def mul_plain(self, a, values) -> np.ndarray:
+        a = _u64(a)
+        vals = [_i64(v) for v in values]
+        offs = np.zeros(len(vals) + 1, np.uint64)
+        offs[1:] = np.cumsum([v.size for v in vals])
+        flat = _i64(np.concatenate(vals)) if offs[-1] else np.zeros(1, np.int64)
+        out = self.alloc(a.size)
+        check(lib().spmvgpu_mul_plain(self.h, _p(a, u64p), _p(flat, i64p), _p(offs, u64p), _p(out, u64p),
+                                      a.size))
+        return out
+
+    def ntt(self, prime_index: int, data: np.ndarray, inverse: bool = False) -> np.ndarray:
+        d = _u64(data).copy()
+        limbs = d.size // self.n
+        check(lib().spmvgpu_ntt(self.h, prime_index, _p(d, u64p), limbs, int(inverse)))
+        return d
+
+    def sync(self):
+        check(lib().spmvgpu_sync(self.h))
+
+
+@dataclass
+class Csr:
+    rows: int
+    cols: int
+    row_ptrs: np.ndarray
+    col_indices: np.ndarray
+    values: np.ndarray
+    _keep: list = field(default_factory=list, repr=False)
+
+    @property
+    def nnz(self) -> int:
+        return int(self.row_ptrs[-1]) if self.rows else 0
+
+    def c(self) -> CsrC:
+        rp, ci, va = _i64(self.row_ptrs), _i64(self.col_indices), _i64(self.values)
+        if va.size == 0:
+            ci = va = np.zeros(1, np.int64)
+        self._keep = [rp, ci, va]
+        return CsrC(self.rows, self.cols, _p(rp, i64p), _p(ci, i64p), _p(va, i64p))
+
+    def dense(self) -> np.ndarray:
+        d = np.zeros((self.rows, self.cols), np.int64)
+        for i in range(self.rows):
+            for k in range(int(self.row_ptrs[i]), int(self.row_ptrs[i + 1])):
+                d[i, int(self.col_indices[k])] = int(self.values[k])
+        return d
+
+    @staticmethod
+    def from_dense(d) -> "Csr":
+        d = np.asarray(d, dtype=np.int64)
+        rows, cols = d.shape if d.ndim == 2 else (0, 0)
+        rp, ci, va = [0], [], []
+        for i in range(rows):
+            for j in range(cols):
+                if d[i, j]:
+                    ci.append(j)
+                    va.append(int(d[i, j]))
+            rp.append(len(va))
+        return Csr(rows, cols, _i64(rp), _i64(ci), _i64(va))
+
+
+def _result(r: ResultC, values: np.ndarray, msgs=None) -> dict:
+    led = r.ledger
+    out = {"values": values, "n_ct": int(r.n_ct), "noise": int(r.noise_model_bits),
+           "measured_noise": int(r.noise_measured_bits),
+           "ledger": {k: int(getattr(led, k)) for k, _ in Ledger._fields_}}
+    if msgs is not None:
+        out["messages"] = [(m.from_, m.to, m.kind, m.payload_bytes, m.ciphertext_count)
+                           for m in msgs[: int(r.n_messages)]]
+    return out
+
+
+def spmv_partitioned(ctx: Context, m: Csr, v, chunk_size: int | None = None, key_holder: int = 0) -> dict:
+    vv = _i64(v)
+    chunk = ctx.slots if chunk_size is None else chunk_size
+    vals = np.zeros(max(m.rows, 1), np.int64)
+    res = ResultC()
+    cap = 5 * (m.rows // max(chunk, 1) + 2)
+    msgs = (Message * cap)()
+    csr = m.c()
+    vp = vv if vv.size else np.zeros(1, np.int64)
+    check(lib().cssc_spmv_partitioned(ctx.h, C.byref(csr), _p(vp, i64p), vv.size, chunk, key_holder,
+                                      _p(vals, i64p), C.byref(res), msgs, cap))
+    return _result(res, vals[: m.rows], msgs)
+
+
+def spmv_batch(ctx: Context, ms, vs, chunk_size: int | None = None, key_holder: int = 0) -> list:
+    chunk = ctx.slots if chunk_size is None else chunk_size
+    n = len(ms)
+    csrs = (CsrC * n)(*[m.c() for m in ms])
+    vv = [_i64(v) for v in vs]
+    vptr = (i64p * n)(*[_p(v, i64p) for v in vv])
+    outs = [np.zeros(max(m.rows, 1), np.int64) for m in ms]
+    optr = (i64p * n)(*[_p(o, i64p) for o in outs])
+    res = (ResultC * n)()
+    check(lib().cssc_spmv_batch(ctx.h, csrs, vptr, n, chunk, key_holder, optr, res))
+    return [_result(res[i], outs[i][: ms[i].rows]) for i in range(n)]
+
+
+class Job:
+    """Staged evaluation: pack (host) -> encrypt (device) -> cloud (device, repeatable) -> finish."""
+
+    def __init__(self, ctx: Context, ms, vs, chunk_size: int | None = None):
+        self.ctx, self.ms = ctx, list(ms)
+        chunk = ctx.slots if chunk_size is None else chunk_size
+        n = len(self.ms)
+        self._csrs = (CsrC * n)(*[m.c() for m in self.ms])
+        self._vv = [_i64(v) for v in vs]
+        vptr = (i64p * n)(*[_p(v, i64p) for v in self._vv])
+        h = C.c_void_p()
+        check(lib().cssc_job_create(ctx.h, self._csrs, vptr, n, chunk, C.byref(h)))
+        self.h = h
+
+    def encrypt(self):
+        check(lib().cssc_job_encrypt(self.h))
+
+    def cloud(self, graph: bool = True):
+        check(lib().cssc_job_cloud(self.h, int(graph)))
+
+    def finish(self) -> list:
+        n = len(self.ms)
+        outs = [np.zeros(max(m.rows, 1), np.int64) for m in self.ms]
+        optr = (i64p * n)(*[_p(o, i64p) for o in outs])
+        res = (ResultC * n)()
+        check(lib().cssc_job_finish(self.h, optr, res))
+        return [_result(res[i], outs[i][: self.ms[i].rows]) for i in range(n)]
+
+    def stats(self) -> dict:
+        s = PlanStats()
+        check(lib().cssc_job_plan_stats(self.h, C.byref(s)))
+        return {k: int(getattr(s, k)) for k, _ in PlanStats._fields_}
+
+    def io_bytes(self):
+        a, b = C.c_uint64(), C.c_uint64()
+        check(lib().cssc_job_input_bytes(self.h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().cssc_job_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ---- generators (native, reference-identical streams) ----
+def random_sparse_csr(rows, cols, nnz, seed, lo=-100, hi=100) -> Csr:
+    rp = np.zeros(rows + 1, np.int64)
+    ci = np.zeros(max(nnz, 1), np.int64)
+    va = np.zeros(max(nnz, 1), np.int64)
+    r = lib().cssc_random_sparse_csr(rows, cols, nnz, seed, lo, hi, _p(rp, i64p), _p(ci, i64p), _p(va, i64p))
+    if r < 0:
+        check(int(r))
+    return Csr(rows, cols, rp, ci[:r], va[:r])
+
+
+def random_vector(n, seed, lo=-100, hi=100, nonzero=False) -> np.ndarray:
+    out = np.zeros(max(n, 1), np.int64)
+    f = lib().cssc_random_nonzero_vector if nonzero else lib().cssc_random_vector
+    f(n, seed, lo, hi, _p(out, i64p))
+    return out[:n]
+
+
+def _grow(call, rows):
+    cap = 1 << 16
+    while True:
+        rp = np.zeros(rows + 1, np.int64)
+        ci = np.zeros(cap, np.int64)
+        va = np.zeros(cap, np.int64)
+        r = call(rp, ci, va, cap)
+        if r >= 0:
+            return rp, ci[:r], va[:r]
+        if r <= -100:
+            cap = int(-r - 100) + 1
+            continue
+        check(int(r))
+
+
+def power_law_csr(n, mean_degree=12.0, exponent=2.0, seed=3, lo=-8, hi=8) -> Csr:
+    rp, ci, va = _grow(lambda rp, ci, va, cap: lib().cssc_power_law_csr(
+        n, mean_degree, exponent, seed, lo, hi, _p(rp, i64p), _p(ci, i64p), _p(va, i64p), cap), n)
+    return Csr(n, n, rp, ci, va)
+
+
+def stencil27_csr(side=32, seed=4, lo=-8, hi=8) -> Csr:
+    n = side ** 3
+    rp, ci, va = _grow(lambda rp, ci, va, cap: lib().cssc_stencil27_csr(
+        side, seed, lo, hi, _p(rp, i64p), _p(ci, i64p), _p(va, i64p), cap), n)
+    return Csr(n, n, rp, ci, va)
+
+
+def rotation_schedule(rows: int, cols: int):
+    off = np.zeros(128, np.uint64)
+    fa = np.zeros(128, np.int32)
+    n = lib().cssc_rotation_schedule(rows, cols, _p(off, u64p), _p(fa, i32p))
+    if n < 0:
+        check(int(n))
+    return [(int(off[i]), bool(fa[i])) for i in range(n)]
+
+
+def pack_chunks(m: Csr, budget: int) -> dict:
+    csr = m.c()
+    tot = C.c_uint64()
+    n = lib().cssc_pack_chunks(C.byref(csr), budget, None, None, None, None, None, C.byref(tot))
+    if n < 0:
+        check(int(n))
+    r = np.zeros(max(n, 1), np.int64)
+    c = np.zeros(max(n, 1), np.int64)
+    vf = np.zeros(max(tot.value, 1), np.int64)
+    cf = np.zeros(max(tot.value, 1), np.int64)
+    rm = np.zeros(max(m.rows, 1), np.int64)
+    lib().cssc_pack_chunks(C.byref(csr), budget, _p(r, i64p), _p(c, i64p), _p(vf, i64p), _p(cf, i64p),
+                           _p(rm, i64p), C.byref(tot))
+    return {"n_ct": int(n), "r": r[:n], "c": c[:n], "vflat": vf[: tot.value], "cflat": cf[: tot.value],
+            "row_map": rm[: m.rows]}

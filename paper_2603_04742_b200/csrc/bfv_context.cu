@@ -1,0 +1,468 @@
+// bfv_context.cu -- see bfv_context.hpp.
+#include "bfv_context.hpp"
+
+#include <algorithm>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+
+namespace cssc {
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// ------------------------------------------------------------------ pool
+DevicePool::~DevicePool() { trim(); }
+
+void* DevicePool::alloc(size_t bytes) {
+    {
+        std::lock_guard<std::mutex> g(mu_);
+        auto it = free_.find(bytes);
+        if (it != free_.end()) {
+            void* p = it->second;
+            free_.erase(it);
+            return p;
+        }
+    }
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        trim();
+        cuda_check(cudaMalloc(&p, bytes), "cudaMalloc");
+    }
+    return p;
+}
+
+void DevicePool::release(void* p, size_t bytes) {
+    std::lock_guard<std::mutex> g(mu_);
+    free_.emplace(bytes, p);
+}
+
+void DevicePool::trim() {
+    std::lock_guard<std::mutex> g(mu_);
+    for (auto& kv : free_) cudaFree(kv.second);
+    free_.clear();
+}
+
+DevBuf::DevBuf(DevicePool* pool, size_t bytes) : pool_(pool), bytes_(bytes) {
+    ptr_ = bytes ? pool->alloc(bytes) : nullptr;
+}
+DevBuf::~DevBuf() {
+    if (ptr_) pool_->release(ptr_, bytes_);
+}
+DevBuf::DevBuf(DevBuf&& o) noexcept : pool_(o.pool_), ptr_(o.ptr_), bytes_(o.bytes_) {
+    o.ptr_ = nullptr;
+    o.bytes_ = 0;
+}
+DevBuf& DevBuf::operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+        if (ptr_) pool_->release(ptr_, bytes_);
+        pool_ = o.pool_;
+        ptr_ = o.ptr_;
+        bytes_ = o.bytes_;
+        o.ptr_ = nullptr;
+        o.bytes_ = 0;
+    }
+    return *this;
+}
+void DevBuf::ensure(DevicePool* pool, size_t bytes) {
+    if (bytes <= bytes_) return;
+    // all work is ordered on the context stream, so releasing to the pool is safe
+    if (ptr_) pool_->release(ptr_, bytes_);
+    pool_ = pool;
+    ptr_ = pool->alloc(bytes);
+    bytes_ = bytes;
+}
+
+// ------------------------------------------------------------------ context
+GpuContext::GpuContext(const RnsConfig& cfg, int device) : P_(cfg), device_(device) {
+    if (cfg.logn > 14) throw std::invalid_argument("ring degree above 2^14 needs the clustered NTT (logn 15) which is not built yet");
+    cuda_check(cudaSetDevice(device), "cudaSetDevice");
+    cuda_check(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking), "stream");
+    DevConsts host = P_.host;
+    const size_t tw_bytes = sizeof(u64) * 2 * (size_t)P_.n;
+    for (int i = 0; i < P_.np; ++i) {
+        DevBuf f(&pool_, tw_bytes), v(&pool_, tw_bytes);
+        cuda_check(cudaMemcpy(f.words(), P_.tw_fwd[i].data(), tw_bytes, cudaMemcpyHostToDevice), "tw");
+        cuda_check(cudaMemcpy(v.words(), P_.tw_inv[i].data(), tw_bytes, cudaMemcpyHostToDevice), "tw");
+        host.tw[i].fwd = f.words();
+        host.tw[i].inv = v.words();
+        tables_.push_back(std::move(f));
+        tables_.push_back(std::move(v));
+    }
+    pos0_ = DevBuf(&pool_, sizeof(u32) * P_.S);
+    cuda_check(cudaMemcpy(pos0_.as<u32>(), P_.pos0.data(), sizeof(u32) * P_.S, cudaMemcpyHostToDevice),
+               "pos0");
+    host.pos0 = pos0_.as<u32>();
+    cuda_check(cudaMalloc(&dc_, sizeof(DevConsts)), "consts");
+    cuda_check(cudaMemcpy(dc_, &host, sizeof(DevConsts), cudaMemcpyHostToDevice), "consts");
+    keygen();
+    synchronize();
+}
+
+GpuContext::~GpuContext() {
+    if (st_) cudaStreamSynchronize(st_);
+    // buffers release into pool_; pool_ destructor frees device memory
+    gk_.clear();
+    if (dc_) cudaFree(dc_);
+    if (st_) cudaStreamDestroy(st_);
+}
+
+void GpuContext::synchronize() { cuda_check(cudaStreamSynchronize(st_), "stream sync"); }
+
+void* GpuContext::upload_bytes(const void* src, size_t bytes, int slot) {
+    ensure_ws(scratch_[slot], std::max<size_t>(bytes, 256));
+    if (bytes)
+        cuda_check(cudaMemcpyAsync(scratch_[slot].as<void>(), src, bytes, cudaMemcpyHostToDevice, st_),
+                   "upload");
+    return scratch_[slot].as<void>();
+}
+
+template <class T>
+T* GpuContext::upload_ptrs(const std::vector<T>& v, int slot) {
+    return static_cast<T*>(upload_bytes(v.data(), sizeof(T) * v.size(), slot));
+}
+
+NttJob GpuContext::job(const u64* src, u64* dst, int limbs, const std::vector<int>& pidx) const {
+    NttJob j;
+    j.src = src;
+    j.dst = dst;
+    j.limbs = limbs;
+    if (limbs > 64) throw std::invalid_argument("too many limbs in one NTT job");
+    for (int i = 0; i < limbs; ++i) j.pidx[i] = (signed char)pidx[i % pidx.size()];
+    return j;
+}
+
+static std::vector<int> range_idx(int lo, int hi) {
+    std::vector<int> v;
+    for (int i = lo; i < hi; ++i) v.push_back(i);
+    return v;
+}
+
+// ------------------------------------------------------------------ keys
+void GpuContext::keygen() {
+    const int n = P_.n, L = P_.cfg.L, LK = L + P_.cfg.K, logn = P_.cfg.logn;
+    const u64 seed = P_.cfg.seed;
+    s_small_ = DevBuf(&pool_, sizeof(int64_t) * n);
+    launch_sample_small(logn, seed, DOM_SK, 0, 0, s_small_.as<int64_t>(), st_);
+    s_ntt_ = DevBuf(&pool_, sizeof(u64) * (size_t)LK * n);
+    launch_lift_small(dc_, logn, s_small_.as<int64_t>(), LK, 0, s_ntt_.words(), st_);
+    launch_ntt(dc_, logn, false, job(s_ntt_.words(), s_ntt_.words(), LK, range_idx(0, LK)), 1, st_);
+
+    // public key over Q: pk1 = a, pk0 = -(a s + e)
+    pk_ = DevBuf(&pool_, sizeof(u64) * 2 * (size_t)L * n);
+    u64* pk0 = pk_.words();
+    u64* pk1 = pk_.words() + (size_t)L * n;
+    launch_sample_uniform(dc_, logn, seed, DOM_PK_A, 0, 0, L, 0, pk1, st_);
+    launch_ntt(dc_, logn, false, job(pk1, pk1, L, range_idx(0, L)), 1, st_);
+    DevBuf e_small(&pool_, sizeof(int64_t) * n), E(&pool_, sizeof(u64) * (size_t)L * n);
+    launch_sample_small(logn, seed, DOM_PK_E, 0, 1, e_small.as<int64_t>(), st_);
+    launch_lift_small(dc_, logn, e_small.as<int64_t>(), L, 0, E.words(), st_);
+    launch_ntt(dc_, logn, false, job(E.words(), E.words(), L, range_idx(0, L)), 1, st_);
+    launch_key_combine(dc_, logn, L, pk1, E.words(), s_ntt_.words(), nullptr, 0, 0, pk0, st_);
+
+    // relinearisation key: target s^2
+    DevBuf s2(&pool_, sizeof(u64) * (size_t)LK * n);
+    launch_square(dc_, logn, LK, s_ntt_.words(), s2.words(), st_);
+    rlk_ = gen_ksk(0, s2.words());
+    synchronize();
+}
+
+DevBuf GpuContext::gen_ksk(u64 keyid, const u64* sp_ntt) {
+    const int n = P_.n, L = P_.cfg.L, LK = L + P_.cfg.K, logn = P_.cfg.logn;
+    const u64 seed = P_.cfg.seed;
+    DevBuf key(&pool_, sizeof(u64) * ksk_words());
+    DevBuf e_small(&pool_, sizeof(int64_t) * n), E(&pool_, sizeof(u64) * (size_t)LK * n);
+    for (int d = 0; d < P_.dnum; ++d) {
+        u64* k0 = key.words() + ((size_t)d * 2 + 0) * LK * n;
+        u64* k1 = key.words() + ((size_t)d * 2 + 1) * LK * n;
+        launch_sample_uniform(dc_, logn, seed, DOM_KSK_A, d, keyid, LK, 0, k1, st_);
+        launch_ntt(dc_, logn, false, job(k1, k1, LK, range_idx(0, LK)), 1, st_);
+        launch_sample_small(logn, seed, DOM_KSK_E | ((u32)d << 16), keyid, 1, e_small.as<int64_t>(), st_);
+        launch_lift_small(dc_, logn, e_small.as<int64_t>(), LK, 0, E.words(), st_);
+        launch_ntt(dc_, logn, false, job(E.words(), E.words(), LK, range_idx(0, LK)), 1, st_);
+        const int lo = d * P_.cfg.alpha, hi = std::min(lo + P_.cfg.alpha, L);
+        launch_key_combine(dc_, logn, LK, k1, E.words(), s_ntt_.words(), sp_ntt, lo, hi, k0, st_);
+    }
+    return key;
+}
+
+const u64* GpuContext::galois_key(u32 g) {
+    std::lock_guard<std::mutex> lk(mu_);
+    auto it = gk_.find(g);
+    if (it != gk_.end()) return it->second.words();
+    const int n = P_.n, LK = P_.cfg.L + P_.cfg.K, logn = P_.cfg.logn;
+    DevBuf sg(&pool_, sizeof(int64_t) * n), sp(&pool_, sizeof(u64) * (size_t)LK * n);
+    launch_automorph_small(logn, g, s_small_.as<int64_t>(), sg.as<int64_t>(), st_);
+    launch_lift_small(dc_, logn, sg.as<int64_t>(), LK, 0, sp.words(), st_);
+    launch_ntt(dc_, logn, false, job(sp.words(), sp.words(), LK, range_idx(0, LK)), 1, st_);
+    DevBuf key = gen_ksk(g, sp.words());
+    const u64* p = key.words();
+    gk_.emplace(g, std::move(key));
+    return p;
+}
+
+void GpuContext::ensure_galois_keys(const std::vector<int64_t>& steps) {
+    for (int64_t k : steps) {
+        const u32 g = galois_element(k, P_.n);
+        if (g != 1) galois_key(g);
+    }
+}
+
+void GpuContext::download_sk(int64_t* out) {
+    synchronize();
+    cuda_check(cudaMemcpy(out, s_small_.as<int64_t>(), sizeof(int64_t) * P_.n, cudaMemcpyDeviceToHost), "sk");
+}
+
+void GpuContext::download_pk_coef(u64* out) {
+    const int L = P_.cfg.L;
+    DevBuf tmp(&pool_, sizeof(u64) * 2 * (size_t)L * P_.n);
+    launch_ntt(dc_, P_.cfg.logn, true, job(pk_.words(), tmp.words(), 2 * L, range_idx(0, L)), 1, st_);
+    synchronize();
+    cuda_check(cudaMemcpy(out, tmp.words(), tmp.bytes(), cudaMemcpyDeviceToHost), "pk");
+}
+
+void GpuContext::download_key_coef(u32 which, u64* out) {
+    const int LK = P_.cfg.L + P_.cfg.K;
+    const u64* key = which == 0 ? rlk_.words() : galois_key(which);
+    DevBuf tmp(&pool_, sizeof(u64) * ksk_words());
+    launch_ntt(dc_, P_.cfg.logn, true, job(key, tmp.words(), 2 * P_.dnum * LK, range_idx(0, LK)), 1,
+               st_);
+    synchronize();
+    cuda_check(cudaMemcpy(out, tmp.words(), tmp.bytes(), cudaMemcpyDeviceToHost), "ksk");
+}
+
+// ------------------------------------------------------------------ encrypt / decrypt
+void GpuContext::encrypt(const int64_t* vals, const u64* offs, const u64* streams,
+                         const std::vector<u64*>& out) {
+    const int items = (int)out.size();
+    if (!items) return;
+    for (int i = 0; i < items; ++i)
+        if (offs[i + 1] - offs[i] > (u64)P_.S) throw std::length_error("encode: values exceed slot count");
+    auto* dv = static_cast<int64_t*>(upload_bytes(vals, sizeof(int64_t) * offs[items], 0));
+    auto* doff = static_cast<u64*>(upload_bytes(offs, sizeof(u64) * (items + 1), 1));
+    auto* dst = static_cast<u64*>(upload_bytes(streams, sizeof(u64) * items, 2));
+    auto* dout = upload_ptrs(out, 3);
+    encrypt_dev(dv, doff, dst, dout, items);
+}
+
+void GpuContext::encrypt_dev(const int64_t* d_vals, const u64* d_offs, const u64* d_streams,
+                             u64* const* d_out, int items) {
+    const int n = P_.n, L = P_.cfg.L, logn = P_.cfg.logn;
+    ensure_ws(wsM_, sizeof(u64) * (size_t)items * n);
+    ensure_ws(wsU_, sizeof(u64) * (size_t)items * L * n);
+    ensure_ws(wsC_, sizeof(u64) * (size_t)items * 2 * L * n);
+    u64* M = wsM_.words();
+    launch_encode_scatter(dc_, P_, d_vals, d_offs, M, items, st_);
+    launch_ntt(dc_, logn, true, job(M, M, 1, {P_.t_index()}), items, st_);
+    launch_enc_sample_u(dc_, P_, P_.cfg.seed, d_streams, wsU_.words(), items, st_);
+    launch_ntt(dc_, logn, false, job(wsU_.words(), wsU_.words(), L, range_idx(0, L)), items, st_);
+    launch_enc_pk(dc_, P_, pk_.words(), wsU_.words(), wsC_.words(), items, st_);
+    launch_ntt(dc_, logn, true, job(wsC_.words(), wsC_.words(), 2 * L, range_idx(0, L)), items, st_);
+    launch_enc_finish(dc_, P_, P_.cfg.seed, d_streams, wsC_.words(), M, d_out, items, st_);
+    stats_.kernels += 7;
+    stats_.limb_ntts += (u64)items * (1 + 3 * L);
+}
+
+void GpuContext::decrypt(const std::vector<const u64*>& cts, u64* slots_host, int* budgets) {
+    const int items = (int)cts.size();
+    if (!items) return;
+    const int n = P_.n, L = P_.cfg.L, logn = P_.cfg.logn;
+    ensure_ws(wsX_, sizeof(u64) * (size_t)items * L * n);
+    ensure_ws(wsM_, sizeof(u64) * (size_t)items * n);
+    ensure_ws(wsU_, sizeof(u64) * (size_t)items * (n / 2) + 8 * (size_t)items + 64);
+    auto* dct = upload_ptrs(cts, 0);
+    NttJob j = job(nullptr, wsX_.words(), L, range_idx(0, L));
+    j.src_items = dct;
+    j.src_limb_offset = L;
+    launch_ntt(dc_, logn, false, j, items, st_);
+    launch_mul_s(dc_, P_, wsX_.words(), s_ntt_.words(), items, st_);
+    launch_ntt(dc_, logn, true, job(wsX_.words(), wsX_.words(), L, range_idx(0, L)), items, st_);
+    u64* slots_dev = wsU_.words();
+    auto* maxdev = reinterpret_cast<unsigned long long*>(wsU_.words() + (size_t)items * (n / 2));
+    launch_dec_scale(dc_, P_, dct, wsX_.words(), wsM_.words(), maxdev, items, st_);
+    launch_ntt(dc_, logn, false, job(wsM_.words(), wsM_.words(), 1, {P_.t_index()}), items, st_);
+    launch_decode_gather(dc_, P_, wsM_.words(), slots_dev, items, st_);
+    std::vector<unsigned long long> md(items);
+    cuda_check(cudaMemcpyAsync(slots_host, slots_dev, sizeof(u64) * (size_t)items * (n / 2),
+                               cudaMemcpyDeviceToHost, st_), "slots");
+    cuda_check(cudaMemcpyAsync(md.data(), maxdev, sizeof(unsigned long long) * items,
+                               cudaMemcpyDeviceToHost, st_), "dev");
+    synchronize();
+    for (int i = 0; i < items; ++i) {
+        const int bl = md[i] ? 64 - __builtin_clzll(md[i]) : 0;
+        if (budgets) budgets[i] = std::max(0, 63 - bl);
+    }
+    stats_.kernels += 7;
+    stats_.limb_ntts += (u64)items * (2 * L + 1);
+}
+
+// ------------------------------------------------------------------ ct ops
+void GpuContext::add(const std::vector<const u64*>& a, const std::vector<const u64*>& b,
+                     const std::vector<u64*>& out) {
+    const int items = (int)out.size();
+    if (!items) return;
+    launch_add(dc_, P_, upload_ptrs(a, 0), upload_ptrs(b, 1), upload_ptrs(out, 2), items, st_);
+    stats_.kernels += 1;
+}
+
+void GpuContext::mul_relin_dev(const u64* const* A, const u64* const* B, u64* const* OUT,
+                               int items, u64* T, u64* Z, u64* D2, u64* DX, u64* ACC,
+                               const u64* const* RLK) {
+    const int L = P_.cfg.L, K = P_.cfg.K, LK = L + K, M = L + P_.nB, logn = P_.cfg.logn;
+    std::vector<int> pm;
+    for (int j = 0; j < M; ++j) pm.push_back(j < L ? j : K + j);
+    launch_mul_extend(dc_, P_, A, B, T, items, st_);
+    launch_ntt(dc_, logn, false, job(T, T, 4 * M, pm), items, st_);
+    launch_mul_tensor(dc_, P_, T, Z, items, st_);
+    launch_ntt(dc_, logn, true, job(Z, Z, 3 * M, pm), items, st_);
+    launch_mul_scale(dc_, P_, Z, OUT, D2, items, st_);
+    launch_ks_modup_contig(dc_, P_, D2, DX, items, st_);
+    launch_ntt(dc_, logn, false, job(DX, DX, P_.dnum * LK, range_idx(0, LK)), items, st_);
+    launch_ks_inner(dc_, P_, DX, RLK, ACC, items, st_);
+    launch_ntt(dc_, logn, true, job(ACC, ACC, 2 * LK, range_idx(0, LK)), items, st_);
+    launch_ks_moddown(dc_, P_, ACC, reinterpret_cast<const u64* const*>(OUT), nullptr, nullptr, OUT,
+                      items, st_);
+    stats_.kernels += 10;
+    stats_.limb_ntts += (u64)items * (7 * M + P_.dnum * LK + 2 * LK);
+}
+
+void GpuContext::mul_relin(const std::vector<const u64*>& a, const std::vector<const u64*>& b,
+                           const std::vector<u64*>& out) {
+    const int items = (int)out.size();
+    if (!items) return;
+    ensure_ws(wsT_, sizeof(u64) * items * mul_T_words());
+    ensure_ws(wsZ_, sizeof(u64) * items * mul_Z_words());
+    ensure_ws(wsD2_, sizeof(u64) * items * poly_words());
+    ensure_ws(wsDX_, sizeof(u64) * items * dx_words());
+    ensure_ws(wsACC_, sizeof(u64) * items * ksacc_words());
+    std::vector<const u64*> rlk(items, rlk_.words());
+    mul_relin_dev(upload_ptrs(a, 0), upload_ptrs(b, 1), upload_ptrs(out, 2), items, wsT_.words(),
+                  wsZ_.words(), wsD2_.words(), wsDX_.words(), wsACC_.words(), upload_ptrs(rlk, 3));
+}
+
+void GpuContext::rotate_dev(const u64* const* SRC, const u32* ginv, const u64* const* KEY,
+                            const u64* const* BASE, u64* const* OUT, int items, u64* DX, u64* ACC) {
+    const int LK = P_.cfg.L + P_.cfg.K, logn = P_.cfg.logn;
+    launch_ks_modup(dc_, P_, SRC, 1, ginv, DX, items, st_);
+    launch_ntt(dc_, logn, false, job(DX, DX, P_.dnum * LK, range_idx(0, LK)), items, st_);
+    launch_ks_inner(dc_, P_, DX, KEY, ACC, items, st_);
+    launch_ntt(dc_, logn, true, job(ACC, ACC, 2 * LK, range_idx(0, LK)), items, st_);
+    launch_ks_moddown(dc_, P_, ACC, BASE, SRC, ginv, OUT, items, st_);
+    stats_.kernels += 5;
+    stats_.limb_ntts += (u64)items * (P_.dnum * LK + 2 * LK);
+}
+
+static u32 inverse_galois(u32 g, int n) {
+    const u64 two_n = 2 * (u64)n;
+    u64 r = 1, b = g;
+    for (u64 e = (u64)n - 1; e; e >>= 1) {
+        if (e & 1) r = r * b % two_n;
+        b = b * b % two_n;
+    }
+    return (u32)r;
+}
+
+void GpuContext::rotate(const std::vector<const u64*>& src, const std::vector<int64_t>& k,
+                        const std::vector<const u64*>& base, const std::vector<u64*>& out) {
+    const int items = (int)out.size();
+    std::vector<const u64*> rs, rb, keys, ia, ib;
+    std::vector<u64*> ro, io;
+    std::vector<u32> gi;
+    bool any_base = false;
+    for (int i = 0; i < items; ++i) any_base |= base[i] != nullptr;
+    for (int i = 0; i < items; ++i) {
+        const u32 g = galois_element(k[i], P_.n);
+        if (g == 1) {
+            if (base[i]) {
+                ia.push_back(base[i]);
+                ib.push_back(src[i]);
+                io.push_back(out[i]);
+            } else if (out[i] != src[i]) {
+                cuda_check(cudaMemcpyAsync(out[i], src[i], sizeof(u64) * ct_words(),
+                                           cudaMemcpyDeviceToDevice, st_), "copy");
+            }
+            continue;
+        }
+        rs.push_back(src[i]);
+        rb.push_back(base[i]);
+        keys.push_back(galois_key(g));
+        gi.push_back(inverse_galois(g, P_.n));
+        ro.push_back(out[i]);
+    }
+    const int r = (int)ro.size();
+    if (r) {
+        if (any_base)
+            for (auto& p : rb)
+                if (!p) throw std::invalid_argument("rotate: mixed base/no-base batch");
+        ensure_ws(wsDX_, sizeof(u64) * r * dx_words());
+        ensure_ws(wsACC_, sizeof(u64) * r * ksacc_words());
+        rotate_dev(upload_ptrs(rs, 0), upload_ptrs(gi, 1), upload_ptrs(keys, 2),
+                   any_base ? upload_ptrs(rb, 3) : nullptr, upload_ptrs(ro, 4), r, wsDX_.words(),
+                   wsACC_.words());
+    }
+    if (!io.empty()) add(ia, ib, io);
+}
+
+void GpuContext::mul_plain(const std::vector<const u64*>& a, const int64_t* vals,
+                           const u64* offs, const std::vector<u64*>& out) {
+    const int items = (int)out.size();
+    if (!items) return;
+    const int n = P_.n, L = P_.cfg.L, logn = P_.cfg.logn;
+    for (int i = 0; i < items; ++i)
+        if (offs[i + 1] - offs[i] > (u64)P_.S) throw std::length_error("encode: values exceed slot count");
+    ensure_ws(wsM_, sizeof(u64) * (size_t)items * n);
+    ensure_ws(wsPT_, sizeof(u64) * (size_t)items * L * n);
+    ensure_ws(wsX_, sizeof(u64) * (size_t)items * 2 * L * n);
+    auto* dv = static_cast<int64_t*>(upload_bytes(vals, sizeof(int64_t) * offs[items], 0));
+    auto* doff = static_cast<u64*>(upload_bytes(offs, sizeof(u64) * (items + 1), 1));
+    launch_encode_scatter(dc_, P_, dv, doff, wsM_.words(), items, st_);
+    launch_ntt(dc_, logn, true, job(wsM_.words(), wsM_.words(), 1, {P_.t_index()}), items, st_);
+    launch_plain_lift(dc_, P_, wsM_.words(), wsPT_.words(), items, st_);
+    launch_ntt(dc_, logn, false, job(wsPT_.words(), wsPT_.words(), L, range_idx(0, L)), items, st_);
+    NttJob j = job(nullptr, wsX_.words(), 2 * L, range_idx(0, L));
+    j.src_items = upload_ptrs(a, 2);
+    launch_ntt(dc_, logn, false, j, items, st_);
+    launch_pointwise_plain(dc_, P_, wsX_.words(), wsPT_.words(), items, 2, st_);
+    launch_ntt(dc_, logn, true, job(wsX_.words(), wsX_.words(), 2 * L, range_idx(0, L)), items, st_);
+    for (int i = 0; i < items; ++i)
+        cuda_check(cudaMemcpyAsync(out[i], wsX_.words() + (size_t)i * ct_words(), sizeof(u64) * ct_words(),
+                                   cudaMemcpyDeviceToDevice, st_), "copy");
+    stats_.kernels += 7;
+}
+
+void GpuContext::encode_masks(const std::vector<int>& ones_len, u64* MASKS) {
+    const int m = (int)ones_len.size();
+    if (!m) return;
+    const int n = P_.n, L = P_.cfg.L, logn = P_.cfg.logn;
+    std::vector<u64> offs(m + 1, 0);
+    for (int i = 0; i < m; ++i) {
+        if (ones_len[i] > P_.S) throw std::length_error("mask longer than slot count");
+        offs[i + 1] = offs[i] + (u64)ones_len[i];
+    }
+    std::vector<int64_t> vals(std::max<u64>(offs[m], 1), 1);
+    ensure_ws(wsM_, sizeof(u64) * (size_t)m * n);
+    auto* dv = static_cast<int64_t*>(upload_bytes(vals.data(), sizeof(int64_t) * vals.size(), 0));
+    auto* doff = static_cast<u64*>(upload_bytes(offs.data(), sizeof(u64) * offs.size(), 1));
+    launch_encode_scatter(dc_, P_, dv, doff, wsM_.words(), m, st_);
+    launch_ntt(dc_, logn, true, job(wsM_.words(), wsM_.words(), 1, {P_.t_index()}), m, st_);
+    launch_plain_lift(dc_, P_, wsM_.words(), MASKS, m, st_);
+    launch_ntt(dc_, logn, false, job(MASKS, MASKS, L, range_idx(0, L)), m, st_);
+}
+
+void GpuContext::ntt_host(int prime_index, u64* data, int limbs, bool inverse) {
+    const int n = P_.n;
+    DevBuf buf(&pool_, sizeof(u64) * (size_t)limbs * n);
+    cuda_check(cudaMemcpyAsync(buf.words(), data, buf.bytes(), cudaMemcpyHostToDevice, st_), "ntt in");
+    launch_ntt(dc_, P_.cfg.logn, inverse, job(buf.words(), buf.words(), 1, {prime_index}), limbs, st_);
+    cuda_check(cudaMemcpyAsync(data, buf.words(), buf.bytes(), cudaMemcpyDeviceToHost, st_), "ntt out");
+    synchronize();
+}
+
+template const u64** GpuContext::upload_ptrs<const u64*>(const std::vector<const u64*>&, int);
+template u64** GpuContext::upload_ptrs<u64*>(const std::vector<u64*>&, int);
+template u32* GpuContext::upload_ptrs<u32>(const std::vector<u32>&, int);
+
+}  // namespace cssc

@@ -1,0 +1,154 @@
+// bfv_context.hpp -- device-resident RNS-BFV context: parameters, keys,
+// ciphertext memory and the batched homomorphic operations.  Host C++ only
+// orchestrates; every arithmetic step is a kernel in bfv_kernels.cu.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <vector>
+
+#include "bfv_kernels.cuh"
+#include "rns_params.hpp"
+
+namespace cssc {
+
+void cuda_check(cudaError_t e, const char* what);
+
+// Size-bucketed caching allocator (all ciphertexts of a context share a size).
+class DevicePool {
+public:
+    ~DevicePool();
+    void* alloc(size_t bytes);
+    void release(void* p, size_t bytes);
+    void trim();
+
+private:
+    std::mutex mu_;
+    std::multimap<size_t, void*> free_;
+};
+
+// RAII device buffer backed by a pool
+class DevBuf {
+public:
+    DevBuf() = default;
+    DevBuf(DevicePool* pool, size_t bytes);
+    ~DevBuf();
+    DevBuf(DevBuf&& o) noexcept;
+    DevBuf& operator=(DevBuf&& o) noexcept;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    template <class T>
+    T* as() const { return static_cast<T*>(ptr_); }
+    u64* words() const { return static_cast<u64*>(ptr_); }
+    size_t bytes() const { return bytes_; }
+    bool empty() const { return ptr_ == nullptr; }
+    void ensure(DevicePool* pool, size_t bytes);  // grow (contents discarded)
+
+private:
+    DevicePool* pool_ = nullptr;
+    void* ptr_ = nullptr;
+    size_t bytes_ = 0;
+};
+
+// Counts what one batched call launched (for bench accounting).
+struct LaunchStats {
+    uint64_t kernels = 0;
+    uint64_t limb_ntts = 0;
+};
+
+class GpuContext {
+public:
+    explicit GpuContext(const RnsConfig& cfg, int device = 0);
+    ~GpuContext();
+
+    const RnsParams& params() const { return P_; }
+    const DevConsts* dconsts() const { return dc_; }
+    cudaStream_t stream() const { return st_; }
+    DevicePool& pool() { return pool_; }
+    int n() const { return P_.n; }
+    int L() const { return P_.cfg.L; }
+    size_t ct_words() const { return (size_t)2 * P_.cfg.L * P_.n; }
+    size_t ksk_words() const { return (size_t)P_.dnum * 2 * (P_.cfg.L + P_.cfg.K) * P_.n; }
+    uint64_t next_stream_id() { return stream_counter_.fetch_add(1); }
+    LaunchStats& stats() { return stats_; }
+
+    // keys (NTT form on device)
+    const u64* relin_key() const { return rlk_.words(); }
+    const u64* galois_key(u32 g);                 // generated on first use
+    void ensure_galois_keys(const std::vector<int64_t>& steps);
+    size_t galois_key_count() const { return gk_.size(); }
+    const u64* s_ntt() const { return s_ntt_.words(); }
+    const u64* pk() const { return pk_.words(); }
+    void download_sk(int64_t* out);
+    void download_pk_coef(u64* out);               // canonical coefficient form
+    void download_key_coef(u32 which, u64* out);   // 0 = relin, else Galois element
+
+    // ---- batched operations; all pointers are device pointers ----
+    // item i encodes vals[offs[i] .. offs[i+1]) (host arrays); streams: encryption stream ids
+    void encrypt(const int64_t* vals, const u64* offs, const u64* streams,
+                 const std::vector<u64*>& out);
+    // same with device-resident arrays
+    void encrypt_dev(const int64_t* d_vals, const u64* d_offs, const u64* d_streams,
+                     u64* const* d_out, int items);
+    void decrypt(const std::vector<const u64*>& cts, u64* slots_host, int* budgets);
+    void add(const std::vector<const u64*>& a, const std::vector<const u64*>& b,
+             const std::vector<u64*>& out);
+    void mul_relin(const std::vector<const u64*>& a, const std::vector<const u64*>& b,
+                   const std::vector<u64*>& out);
+    // out_i = (base_i ? base_i : 0) + rot(src_i, k_i)
+    void rotate(const std::vector<const u64*>& src, const std::vector<int64_t>& k,
+                const std::vector<const u64*>& base, const std::vector<u64*>& out);
+    // out_i = a_i * encode(vals_i)
+    void mul_plain(const std::vector<const u64*>& a, const int64_t* vals, const u64* offs,
+                   const std::vector<u64*>& out);
+    // KAT helpers
+    void ntt_host(int prime_index, u64* data, int limbs, bool inverse);
+    void synchronize();
+
+    // building blocks reused by the batched cloud plan (pointer arrays on device)
+    void mul_relin_dev(const u64* const* A, const u64* const* B, u64* const* OUT, int items,
+                       u64* T, u64* Z, u64* D2, u64* DX, u64* ACC, const u64* const* RLK);
+    void rotate_dev(const u64* const* SRC, const u32* ginv, const u64* const* KEY,
+                    const u64* const* BASE, u64* const* OUT, int items, u64* DX, u64* ACC);
+    void encode_masks(const std::vector<int>& ones_len, u64* MASKS);  // NTT form [m][L][N]
+    NttJob job(const u64* src, u64* dst, int limbs, const std::vector<int>& pidx) const;
+
+    // workspace sizing (words per item)
+    size_t mul_T_words() const { return (size_t)4 * (P_.cfg.L + P_.nB) * P_.n; }
+    size_t mul_Z_words() const { return (size_t)3 * (P_.cfg.L + P_.nB) * P_.n; }
+    size_t dx_words() const { return (size_t)P_.dnum * (P_.cfg.L + P_.cfg.K) * P_.n; }
+    size_t ksacc_words() const { return (size_t)2 * (P_.cfg.L + P_.cfg.K) * P_.n; }
+    size_t poly_words() const { return (size_t)P_.cfg.L * P_.n; }
+
+    // scratch pointer arrays (stream-ordered reuse)
+    template <class T>
+    T* upload_ptrs(const std::vector<T>& v, int slot);
+    void* upload_bytes(const void* src, size_t bytes, int slot);
+
+private:
+    void keygen();
+    DevBuf gen_ksk(u64 keyid, const u64* sp_ntt);
+    void ensure_ws(DevBuf& b, size_t bytes) { b.ensure(&pool_, bytes); }
+
+    RnsParams P_;
+    int device_ = 0;
+    cudaStream_t st_ = nullptr;
+    DevicePool pool_;
+    DevConsts* dc_ = nullptr;
+    std::vector<DevBuf> tables_;
+    DevBuf pos0_;
+    DevBuf s_small_, s_ntt_, pk_, rlk_;
+    std::map<u32, DevBuf> gk_;
+    std::atomic<uint64_t> stream_counter_{1};
+    LaunchStats stats_;
+    // workspaces for ad-hoc batched calls
+    DevBuf wsT_, wsZ_, wsD2_, wsDX_, wsACC_, wsM_, wsX_, wsU_, wsC_, wsPT_;
+    DevBuf scratch_[8];
+    std::mutex mu_;
+};
+
+}  // namespace cssc

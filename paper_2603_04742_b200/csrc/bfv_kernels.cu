@@ -1,0 +1,798 @@
+// bfv_kernels.cu -- sm_100a kernels for the batched RNS-BFV cloud phase.
+//
+// Every kernel covers all RNS limbs of all items of a batch in one launch:
+// elementwise kernels put one thread on one coefficient index k of one item
+// (coalesced over k for every limb), NTT kernels put one CTA on one limb.
+// Formulas E1..E5 refer to DESIGN.md "Arithmetic spec"; the CPU oracle
+// (oracle/bfv_oracle.c) states the same integer formulas.
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+
+#include "bfv_kernels.cuh"
+#include "ntt.cuh"
+
+namespace cssc {
+
+#define CSSC_CHECK_LAUNCH()                                                            \
+    do {                                                                               \
+        cudaError_t e_ = cudaGetLastError();                                           \
+        if (e_ != cudaSuccess)                                                         \
+            throw std::runtime_error(std::string("kernel launch: ") + cudaGetErrorString(e_)); \
+    } while (0)
+
+constexpr int EW_THREADS = 128;
+
+__device__ __forceinline__ void add128(u64& hi, u64& lo, u64 xhi, u64 xlo) {
+    lo += xlo;
+    hi += xhi + (lo < xlo);
+}
+
+// ---------------------------------------------------------------------------
+// ChaCha20 block (RFC 8439 2.3); key = (seed_lo, seed_hi, fixed words)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ u32 rotl32(u32 v, int n) { return __funnelshift_l(v, v, n); }
+
+#define CSSC_QR(a, b, c, d)                         \
+    a += b; d ^= a; d = rotl32(d, 16);              \
+    c += d; b ^= c; b = rotl32(b, 12);              \
+    a += b; d ^= a; d = rotl32(d, 8);               \
+    c += d; b ^= c; b = rotl32(b, 7);
+
+__device__ void chacha20_block(u64 seed, u32 ctr, u32 n0, u32 n1, u32 n2, u32 out[16]) {
+    const u32 s[16] = {0x61707865u, 0x3320646eu, 0x79622d32u, 0x6b206574u,
+                       (u32)seed,   (u32)(seed >> 32), 0x63737363u, 0x2d68652du,
+                       0x62323030u, 0x2d707267u, 0x6b657973u, 0x00000001u,
+                       ctr,         n0,          n1,          n2};
+    u32 x[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) x[i] = s[i];
+#pragma unroll 1
+    for (int i = 0; i < 10; ++i) {
+        CSSC_QR(x[0], x[4], x[8], x[12]);
+        CSSC_QR(x[1], x[5], x[9], x[13]);
+        CSSC_QR(x[2], x[6], x[10], x[14]);
+        CSSC_QR(x[3], x[7], x[11], x[15]);
+        CSSC_QR(x[0], x[5], x[10], x[15]);
+        CSSC_QR(x[1], x[6], x[11], x[12]);
+        CSSC_QR(x[2], x[7], x[8], x[13]);
+        CSSC_QR(x[3], x[4], x[9], x[14]);
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) out[i] = x[i] + s[i];
+}
+
+__device__ __forceinline__ u64 word64(const u32* blk, int w) {
+    return (u64)blk[2 * w] | ((u64)blk[2 * w + 1] << 32);
+}
+__device__ __forceinline__ int64_t ternary_of(u64 w) { return (int64_t)(w % 3) - 1; }
+__device__ __forceinline__ int64_t cbd_of(u64 w) {
+    return (int64_t)__popcll(w & 0x1FFFFFull) - (int64_t)__popcll((w >> 21) & 0x1FFFFFull);
+}
+__device__ __forceinline__ u64 lift_signed(int64_t v, u64 q) {
+    return v >= 0 ? (u64)v : q - (u64)(-v);
+}
+
+// ---------------------------------------------------------------------------
+// NTT
+// ---------------------------------------------------------------------------
+template <int LOGN, bool INV>
+__global__ void __launch_bounds__(NttGeom<LOGN>::THREADS)
+    k_ntt(const DevConsts* __restrict__ dc, NttJob job) {
+    extern __shared__ u64 smem[];
+    constexpr int N = 1 << LOGN;
+    const int item = blockIdx.x / job.limbs;
+    const int j = blockIdx.x - item * job.limbs;
+    const int prime = job.pidx[j];
+    const u64* src = job.src_items
+                         ? job.src_items[item] + (size_t)(job.src_limb_offset + j) * N
+                         : job.src + ((size_t)item * job.limbs + j) * N;
+    u64* dst = job.dst_items ? job.dst_items[item] + (size_t)j * N
+                             : job.dst + ((size_t)item * job.limbs + j) * N;
+    load_limb<LOGN>(smem, src);
+    __syncthreads();
+    const u64 q = dc->mod[prime].q;
+    if (!INV) {
+        ntt_fwd_smem<LOGN>(smem, dc, prime);
+        store_limb_fwd<LOGN>(dst, smem, q);
+    } else {
+        ntt_inv_smem<LOGN>(smem, dc, prime);
+        store_limb_inv<LOGN>(dst, smem, q, dc->ninv[prime], dc->ninv_sh[prime]);
+    }
+}
+
+size_t ntt_smem_bytes(int logn) { return (size_t)8 << logn; }
+
+template <int LOGN>
+static void launch_ntt_t(const DevConsts* dc, bool inv, const NttJob& job, int items,
+                         cudaStream_t st) {
+    static bool configured = false;
+    constexpr int SMEM = NttGeom<LOGN>::SMEM;
+    if (!configured) {
+        cudaFuncSetAttribute(k_ntt<LOGN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+        cudaFuncSetAttribute(k_ntt<LOGN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+        configured = true;
+    }
+    const int grid = items * job.limbs;
+    if (grid == 0) return;
+    if (inv)
+        k_ntt<LOGN, true><<<grid, NttGeom<LOGN>::THREADS, SMEM, st>>>(dc, job);
+    else
+        k_ntt<LOGN, false><<<grid, NttGeom<LOGN>::THREADS, SMEM, st>>>(dc, job);
+    CSSC_CHECK_LAUNCH();
+}
+
+void launch_ntt(const DevConsts* dc, int logn, bool inverse, const NttJob& job, int items,
+                cudaStream_t st) {
+    switch (logn) {
+        case 10: launch_ntt_t<10>(dc, inverse, job, items, st); break;
+        case 11: launch_ntt_t<11>(dc, inverse, job, items, st); break;
+        case 12: launch_ntt_t<12>(dc, inverse, job, items, st); break;
+        case 13: launch_ntt_t<13>(dc, inverse, job, items, st); break;
+        case 14: launch_ntt_t<14>(dc, inverse, job, items, st); break;
+        default: throw std::invalid_argument("NTT: unsupported logn " + std::to_string(logn));
+    }
+}
+
+static dim3 ew_grid(int n, int items) { return dim3((unsigned)(n / EW_THREADS), (unsigned)items); }
+
+// ---------------------------------------------------------------------------
+// E1: exact centred basis extension of one coefficient (X residues -> Y)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void extend_exact(const DevConsts* __restrict__ dc,
+                                             const ExtConsts& e, const u64* x, u64* out) {
+    u64 y[MAXB];
+    u64 shi = 0, slo = 0;
+    for (int i = 0; i < e.nx; ++i) {
+        const u64 qi = dc->mod[e.xi[i]].q;
+        y[i] = shoup(x[i], e.xhat_inv[i], e.xhat_inv_sh[i], qi);
+        add128(shi, slo, 0, frac64(y[i], e.R1[i], e.R0[i]));
+    }
+    const u64 v = shi + (slo >> 63);
+    for (int j = 0; j < e.ny; ++j) {
+        const u64 p = dc->mod[e.yi[j]].q;
+        u64 acc = 0;
+        for (int i = 0; i < e.nx; ++i) acc = add_mod(acc, shoup(y[i], e.xhat_y[i][j], e.xhat_y_sh[i][j], p), p);
+        out[j] = sub_mod(acc, shoup(v, e.X_y[j], e.X_y_sh[j], p), p);
+    }
+}
+
+// T[item][poly 0..3][M][N]: Q limbs copied, B limbs by E1.  polys: a0 a1 b0 b1
+__global__ void k_mul_extend(const DevConsts* __restrict__ dc, const u64* const* A,
+                             const u64* const* B, u64* T) {
+    const int n = dc->n, L = dc->L, nB = dc->nB, M = L + nB;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int item = blockIdx.y;
+    u64 x[MAXB], o[MAXB];
+    for (int p = 0; p < 4; ++p) {
+        const u64* src = (p < 2 ? A[item] : B[item]) + (size_t)(p & 1) * L * n;
+        u64* dst = T + ((size_t)item * 4 + p) * M * n;
+        for (int i = 0; i < L; ++i) {
+            x[i] = src[(size_t)i * n + k];
+            dst[(size_t)i * n + k] = x[i];
+        }
+        extend_exact(dc, dc->extQB, x, o);
+        for (int j = 0; j < nB; ++j) dst[(size_t)(L + j) * n + k] = o[j];
+    }
+}
+
+void launch_mul_extend(const DevConsts* dc, const RnsParams& P, const u64* const* A,
+                       const u64* const* B, u64* T, int items, cudaStream_t st) {
+    if (!items) return;
+    k_mul_extend<<<ew_grid(P.n, items), EW_THREADS, 0, st>>>(dc, A, B, T);
+    CSSC_CHECK_LAUNCH();
+}
+
+__global__ void k_mul_tensor(const DevConsts* __restrict__ dc, const u64* __restrict__ T,
+                             u64* __restrict__ Z) {
+    const int n = dc->n, L = dc->L, nB = dc->nB, M = L + nB;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int item = blockIdx.y;
+    const size_t P = (size_t)M * n;
+    const u64* t = T + (size_t)item * 4 * P;
+    u64* z = Z + (size_t)item * 3 * P;
+    for (int j = 0; j < M; ++j) {
+        const int pi = j < L ? j : dc->K + j;  // B limbs follow P in the prime table
+        const Modulus md = dc->mod[pi];
+        const size_t o = (size_t)j * n + k;
+        const u64 a0 = t[o], a1 = t[P + o], b0 = t[2 * P + o], b1 = t[3 * P + o];
+        z[o] = mul_mod(a0, b0, md);
+        z[P + o] = add_mod(mul_mod(a0, b1, md), mul_mod(a1, b0, md), md.q);
+        z[2 * P + o] = mul_mod(a1, b1, md);
+    }
+}
+
+void launch_mul_tensor(const DevConsts* dc, const RnsParams& P, const u64* T, u64* Z, int items,
+                       cudaStream_t st) {
+    if (!items) return;
+    k_mul_tensor<<<ew_grid(P.n, items), EW_THREADS, 0, st>>>(dc, T, Z);
+    CSSC_CHECK_LAUNCH();
+}
+
+// E2: w = round(t z / Q) in B, then E1 B -> Q.  r = 0,1 -> OUT ct, r = 2 -> D2
+__global__ void k_mul_scale(const DevConsts* __restrict__ dc, const u64* __restrict__ Z,
+                            u64* const* OUT, u64* __restrict__ D2) {
+    const int n = dc->n, L = dc->L, nB = dc->nB, K = dc->K, M = L + nB;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int item = blockIdx.y;
+    const size_t P = (size_t)M * n;
+    u64 xi[MAXL], w[MAXB], o[MAXB];
+    for (int r = 0; r < 3; ++r) {
+        const u64* z = Z + ((size_t)item * 3 + r) * P;
+        u64 shi = 0, slo = 0;
+        for (int i = 0; i < L; ++i) {
+            const u64 qi = dc->mod[i].q;
+            xi[i] = shoup(z[(size_t)i * n + k], dc->QhatInv[i], dc->QhatInv_sh[i], qi);
+            add128(shi, slo, umulhi(xi[i], dc->T1[i]), xi[i] * dc->T1[i]);
+            add128(shi, slo, 0, umulhi(xi[i], dc->T0[i]));
+        }
+        const u64 rr = shi + (slo >> 63);
+        for (int j = 0; j < nB; ++j) {
+            const u64 bj = dc->mod[L + K + j].q;
+            u64 acc = 0;
+            for (int i = 0; i < L; ++i)
+                acc = add_mod(acc, shoup(xi[i], dc->QhatB[i][j], dc->QhatB_sh[i][j], bj), bj);
+            const u64 alpha = shoup(sub_mod(acc, z[(size_t)(L + j) * n + k], bj), dc->QinvB[j],
+                                    dc->QinvB_sh[j], bj);
+            w[j] = sub_mod(rr, shoup(alpha, dc->tB[j], dc->tB_sh[j], bj), bj);
+        }
+        extend_exact(dc, dc->extBQ, w, o);
+        u64* dst = r < 2 ? OUT[item] + (size_t)r * L * n : D2 + (size_t)item * L * n;
+        for (int i = 0; i < L; ++i) dst[(size_t)i * n + k] = o[i];
+    }
+}
+
+void launch_mul_scale(const DevConsts* dc, const RnsParams& P, const u64* Z, u64* const* OUT,
+                      u64* D2, int items, cudaStream_t st) {
+    if (!items) return;
+    k_mul_scale<<<ew_grid(P.n, items), EW_THREADS, 0, st>>>(dc, Z, OUT, D2);
+    CSSC_CHECK_LAUNCH();
+}
+
+// ---------------------------------------------------------------------------
+// hybrid key switching
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int automorph_src(u32 ginv, int k, int n, bool& neg) {
+    if (ginv == 0) {
+        neg = false;
+        return k;
+    }
+    const u32 i0 = (u32)(((unsigned long long)ginv * (unsigned)k) & (unsigned long long)(2 * n - 1));
+    neg = i0 >= (u32)n;
+    return neg ? (int)(i0 - n) : (int)i0;
+}
+
+// E3: DX[item][digit][LK][N] = ModUp of SRC (optionally permuted by X -> X^g)
+__global__ void k_ks_modup(const DevConsts* __restrict__ dc, const u64* const* SRC,
+                           const u64* SRCC, int src_poly, const u32* ginv, u64* DX) {
+    const int n = dc->n, L = dc->L, LK = L + dc->K, alpha = dc->alpha;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int item = blockIdx.y;
+    const u64* src = SRC ? SRC[item] + (size_t)src_poly * L * n : SRCC + (size_t)item * L * n;
+    bool neg;
+    const int idx = automorph_src(ginv ? ginv[item] : 0u, k, n, neg);
+    u64 x[MAXL], y[MAXL];
+    for (int i = 0; i < L; ++i) {
+        const u64 v = src[(size_t)i * n + idx];
+        x[i] = neg ? neg_mod(v, dc->mod[i].q) : v;
+    }
+    for (int dg = 0; dg < dc->dnum; ++dg) {
+        const int lo = dg * alpha, hi = min(lo + alpha, L);
+        for (int i = lo; i < hi; ++i)
+            y[i] = shoup(x[i], dc->dig_hat_inv[i], dc->dig_hat_inv_sh[i], dc->mod[i].q);
+        u64* out = DX + ((size_t)item * dc->dnum + dg) * LK * n;
+        for (int j = 0; j < LK; ++j) {
+            u64 v;
+            if (j >= lo && j < hi) {
+                v = x[j];
+            } else {
+                const u64 m = dc->mod[j].q;
+                v = 0;
+                for (int i = lo; i < hi; ++i)
+                    v = add_mod(v, shoup(y[i], dc->dig_hat[i][j], dc->dig_hat_sh[i][j], m), m);
+            }
+            out[(size_t)j * n + k] = v;
+        }
+    }
+}
+
+void launch_ks_modup(const DevConsts* dc, const RnsParams& P, const u64* const* SRC, int src_poly,
+                     const u32* ginv, u64* DX, int items, cudaStream_t st) {
+    if (!items) return;
+    k_ks_modup<<<ew_grid(P.n, items), EW_THREADS, 0, st>>>(dc, SRC, nullptr, src_poly, ginv, DX);
+    CSSC_CHECK_LAUNCH();
+}
+
+void launch_ks_modup_contig(const DevConsts* dc, const RnsParams& P, const u64* SRC, u64* DX,
+                            int items, cudaStream_t st) {
+    if (!items) return;
+    k_ks_modup<<<ew_grid(P.n, items), EW_THREADS, 0, st>>>(dc, nullptr, SRC, 0, nullptr, DX);
+    CSSC_CHECK_LAUNCH();
+}
+
+// ACC[item][2][LK][N] = sum_digit DX (.) KEY  (NTT domain)
+__global__ void k_ks_inner(const DevConsts* __restrict__ dc, const u64* __restrict__ DX,
+                           const u64* const* KEY, u64* __restrict__ ACC) {
+    const int n = dc->n, LK = dc->L + dc->K, dnum = dc->dnum;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int item = blockIdx.y;
+    const u64* key = KEY[item];
+    const size_t PL = (size_t)LK * n;
+    for (int j = 0; j < LK; ++j) {
+        const Modulus md = dc->mod[j];
+        u64 a0 = 0, a1 = 0;
+        for (int dg = 0; dg < dnum; ++dg) {
+            const u64 d = DX[((size_t)item * dnum + dg) * PL + (size_t)j * n + k];
+            const u64 k0 = __ldg(key + ((size_t)dg * 2 + 0) * PL + (size_t)j * n + k);
+            const u64 k1 = __ldg(key + ((size_t)dg * 2 + 1) * PL + (size_t)j * n + k);
+            a0 = add_mod(a0, mul_mod(d, k0, md), md.q);
+            a1 = add_mod(a1, mul_mod(d, k1, md), md.q);
+        }
+        ACC[((size_t)item * 2 + 0) * PL + (size_t)j * n + k] = a0;
+        ACC[((size_t)item * 2 + 1) * PL + (size_t)j * n + k] = a1;
+    }
+}
+
+void launch_ks_inner(const DevConsts* dc, const RnsParams& P, const u64* DX,
+                     const u64* const* KEY, u64* ACC, int items, cudaStream_t st) {
+    if (!items) return;
+    k_ks_inner<<<ew_grid(P.n, items), EW_THREADS, 0, st>>>(dc, DX, KEY, ACC);
+    CSSC_CHECK_LAUNCH();
+}
+
+// E4 + fused adds
+__global__ void k_ks_moddown(const DevConsts* __restrict__ dc, const u64* __restrict__ ACC,
+                             const u64* const* BASE, const u64* const* RSRC, const u32* ginv,
+                             u64* const* OUT) {
+    const int n = dc->n, L = dc->L, K = dc->K, LK = L + K;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int item = blockIdx.y;
+    const size_t PL = (size_t)LK * n;
+    bool neg = false;
+    int ridx = k;
+    if (RSRC) ridx = automorph_src(ginv ? ginv[item] : 0u, k, n, neg);
+    u64 y[MAXL];
+    for (int p = 0; p < 2; ++p) {
+        const u64* acc = ACC + ((size_t)item * 2 + p) * PL;
+        for (int kk = 0; kk < K; ++kk) {
+            const u64 pk = dc->mod[L + kk].q;
+            y[kk] = shoup(acc[(size_t)(L + kk) * n + k], dc->phat_inv[kk], dc->phat_inv_sh[kk], pk);
+        }
+        u64* out = OUT[item] + (size_t)p * L * n;
+        const u64* base = BASE ? BASE[item] + (size_t)p * L * n : nullptr;
+        const u64* rs = (RSRC && p == 0) ? RSRC[item] : nullptr;
+        for (int j = 0; j < L; ++j) {
+            const u64 q = dc->mod[j].q;
+            u64 c = 0;
+            for (int kk = 0; kk < K; ++kk)
+                c = add_mod(c, shoup(y[kk], dc->phat_q[kk][j], dc->phat_q_sh[kk][j], q), q);
+            u64 v = shoup(sub_mod(acc[(size_t)j * n + k], c, q), dc->Pinv_q[j], dc->Pinv_q_sh[j], q);
+            if (base) v = add_mod(v, base[(size_t)j * n + k], q);
+            if (rs) {
+                const u64 r = rs[(size_t)j * n + ridx];
+                v = add_mod(v, neg ? neg_mod(r, q) : r, q);
+            }
+            out[(size_t)j * n + k] = v;
+        }
+    }
+}
+
+void launch_ks_moddown(const DevConsts* dc, const RnsParams& P, const u64* ACC,
+                       const u64* const* BASE, const u64* const* RSRC, const u32* ginv,
+                       u64* const* OUT, int items, cudaStream_t st) {
+    if (!items) return;
+    k_ks_moddown<<<ew_grid(P.n, items), EW_THREADS, 0, st>>>(dc, ACC, BASE, RSRC, ginv, OUT);
+    CSSC_CHECK_LAUNCH();
+}
+
+// ---------------------------------------------------------------------------
+// masks and plaintext products
+// ---------------------------------------------------------------------------
+__global__ void k_mask_accum(const DevConsts* __restrict__ dc, const u64* __restrict__ MT,
+                             const int* slice_off, const int* slice_items, const int* item_mask,
+                             const u64* __restrict__ MASKS, u64* __restrict__ RES) {
+    const int n = dc->n, L = dc->L;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int s = blockIdx.y;
+    const int b = slice_off[s], e = slice_off[s + 1];
+    const size_t CT = (size_t)2 * L * n;
+    for (int p = 0; p < 2; ++p)
+        for (int j = 0; j < L; ++j) {
+            const Modulus md = dc->mod[j];
+            u64 acc = 0;
+            for (int x = b; x < e; ++x) {
+                const int it = slice_items[x];
+                const u64 a = MT[(size_t)it * CT + ((size_t)p * L + j) * n + k];
+                const u64 m = MASKS[((size_t)item_mask[it] * L + j) * n + k];
+                acc = add_mod(acc, mul_mod(a, m, md), md.q);
+            }
+            RES[(size_t)s * CT + ((size_t)p * L + j) * n + k] = acc;
+        }
+}
+
+void launch_mask_accum(const DevConsts* dc, const RnsParams& P, const u64* MT,
+                       const int* slice_off, const int* slice_items, const int* item_mask,
+                       const u64* MASKS, u64* RES, int slices, cudaStream_t st) {
+    if (!slices) return;
+    k_mask_accum<<<ew_grid(P.n, slices), EW_THREADS, 0, st>>>(dc, MT, slice_off, slice_items,
+                                                              item_mask, MASKS, RES);
+    CSSC_CHECK_LAUNCH();
+}
+
+// X[item][poly][L][N] *= PT[item][L][N]
+__global__ void k_pointwise_plain(const DevConsts* __restrict__ dc, u64* X, const u64* PT,
+                                  int polys) {
+    const int n = dc->n, L = dc->L;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int item = blockIdx.y;
+    for (int p = 0; p < polys; ++p)
+        for (int j = 0; j < L; ++j) {
+            const size_t o = (((size_t)item * polys + p) * L + j) * n + k;
+            X[o] = mul_mod(X[o], PT[((size_t)item * L + j) * n + k], dc->mod[j]);
+        }
+}
+
+void launch_pointwise_plain(const DevConsts* dc, const RnsParams& P, u64* X, const u64* PT,
+                            int items, int polys, cudaStream_t st) {
+    if (!items) return;
+    k_pointwise_plain<<<ew_grid(P.n, items), EW_THREADS, 0, st>>>(dc, X, PT, polys);
+    CSSC_CHECK_LAUNCH();
+}
+
+// ---------------------------------------------------------------------------
+// encoding, encryption, decryption
+// ---------------------------------------------------------------------------
+__global__ void k_encode_scatter(const DevConsts* __restrict__ dc, const int64_t* vals,
+                                 const u64* offs, u64* M) {
+    const int S = dc->n / 2;
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const int item = blockIdx.y;
+    const u64 b = offs[item];
+    if (j >= S || (u64)j >= offs[item + 1] - b) return;
+    const int64_t t = (int64_t)dc->t;
+    int64_t v = vals[b + j] % t;
+    if (v < 0) v += t;
+    M[(size_t)item * dc->n + dc->pos0[j]] = (u64)v;
+}
+
+void launch_encode_scatter(const DevConsts* dc, const RnsParams& P, const int64_t* vals,
+                           const u64* offs, u64* M, int items, cudaStream_t st) {
+    if (!items) return;
+    cudaMemsetAsync(M, 0, sizeof(u64) * (size_t)P.n * items, st);
+    k_encode_scatter<<<dim3((unsigned)(P.S / EW_THREADS + 1), (unsigned)items), EW_THREADS, 0, st>>>(
+        dc, vals, offs, M);
+    CSSC_CHECK_LAUNCH();
+}
+
+// PT[item][L][N] = centred lift of M[item][N] (mod t) to each q_j (coef form)
+__global__ void k_plain_lift(const DevConsts* __restrict__ dc, const u64* M, u64* PT) {
+    const int n = dc->n, L = dc->L;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int item = blockIdx.y;
+    const u64 t = dc->t, m = M[(size_t)item * n + k];
+    for (int j = 0; j < L; ++j) {
+        const u64 q = dc->mod[j].q;
+        PT[((size_t)item * L + j) * n + k] = m <= t / 2 ? m : q - (t - m);
+    }
+}
+
+void launch_plain_lift(const DevConsts* dc, const RnsParams& P, const u64* M, u64* PT, int items,
+                       cudaStream_t st) {
+    if (!items) return;
+    k_plain_lift<<<ew_grid(P.n, items), EW_THREADS, 0, st>>>(dc, M, PT);
+    CSSC_CHECK_LAUNCH();
+}
+
+// one thread per ChaCha block = 8 coefficients of u; U[item][L][N]
+__global__ void k_enc_sample_u(const DevConsts* __restrict__ dc, u64 seed, const u64* streams,
+                               u64* U) {
+    const int n = dc->n, L = dc->L;
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    const int item = blockIdx.y;
+    if (b >= n / 8) return;
+    const u64 id = streams[item];
+    u32 blk[16];
+    chacha20_block(seed, (u32)b, DOM_ENC_U, (u32)id, (u32)(id >> 32), blk);
+    for (int w = 0; w < 8; ++w) {
+        const int64_t u = ternary_of(word64(blk, w));
+        const int k = 8 * b + w;
+        for (int j = 0; j < L; ++j) U[((size_t)item * L + j) * n + k] = lift_signed(u, dc->mod[j].q);
+    }
+}
+
+void launch_enc_sample_u(const DevConsts* dc, const RnsParams& P, u64 seed, const u64* streams,
+                         u64* U, int items, cudaStream_t st) {
+    if (!items) return;
+    k_enc_sample_u<<<dim3((unsigned)((P.n / 8 + 63) / 64), (unsigned)items), 64, 0, st>>>(dc, seed,
+                                                                                         streams, U);
+    CSSC_CHECK_LAUNCH();
+}
+
+// C[item][2][L][N] = PK[p] (.) U  (NTT domain)
+__global__ void k_enc_pk(const DevConsts* __restrict__ dc, const u64* PK, const u64* U, u64* C) {
+    const int n = dc->n, L = dc->L;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int item = blockIdx.y;
+    for (int j = 0; j < L; ++j) {
+        const Modulus md = dc->mod[j];
+        const u64 u = U[((size_t)item * L + j) * n + k];
+        for (int p = 0; p < 2; ++p)
+            C[(((size_t)item * 2 + p) * L + j) * n + k] =
+                mul_mod(__ldg(PK + ((size_t)p * L + j) * n + k), u, md);
+    }
+}
+
+void launch_enc_pk(const DevConsts* dc, const RnsParams& P, const u64* PK, const u64* U, u64* C,
+                   int items, cudaStream_t st) {
+    if (!items) return;
+    k_enc_pk<<<ew_grid(P.n, items), EW_THREADS, 0, st>>>(dc, PK, U, C);
+    CSSC_CHECK_LAUNCH();
+}
+
+// OUT = C + (e0 + Delta m, e1), thread per 8 coefficients
+__global__ void k_enc_finish(const DevConsts* __restrict__ dc, u64 seed, const u64* streams,
+                             const u64* C, const u64* M, u64* const* OUT) {
+    const int n = dc->n, L = dc->L;
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    const int item = blockIdx.y;
+    if (b >= n / 8) return;
+    const u64 id = streams[item];
+    u32 e0b[16], e1b[16];
+    chacha20_block(seed, (u32)b, DOM_ENC_E0, (u32)id, (u32)(id >> 32), e0b);
+    chacha20_block(seed, (u32)b, DOM_ENC_E1, (u32)id, (u32)(id >> 32), e1b);
+    u64* out = OUT[item];
+    for (int w = 0; w < 8; ++w) {
+        const int k = 8 * b + w;
+        const int64_t e0 = cbd_of(word64(e0b, w)), e1 = cbd_of(word64(e1b, w));
+        const u64 m = M[(size_t)item * n + k];
+        for (int j = 0; j < L; ++j) {
+            const u64 q = dc->mod[j].q;
+            const size_t o0 = (((size_t)item * 2 + 0) * L + j) * n + k;
+            const size_t o1 = (((size_t)item * 2 + 1) * L + j) * n + k;
+            u64 c0 = add_mod(C[o0], lift_signed(e0, q), q);
+            c0 = add_mod(c0, shoup(m, dc->delta[j], dc->delta_sh[j], q), q);
+            const u64 c1 = add_mod(C[o1], lift_signed(e1, q), q);
+            out[(size_t)j * n + k] = c0;
+            out[((size_t)L + j) * n + k] = c1;
+        }
+    }
+}
+
+void launch_enc_finish(const DevConsts* dc, const RnsParams& P, u64 seed, const u64* streams,
+                       const u64* C, const u64* M, u64* const* OUT, int items, cudaStream_t st) {
+    if (!items) return;
+    k_enc_finish<<<dim3((unsigned)((P.n / 8 + 63) / 64), (unsigned)items), 64, 0, st>>>(
+        dc, seed, streams, C, M, OUT);
+    CSSC_CHECK_LAUNCH();
+}
+
+__global__ void k_mul_s(const DevConsts* __restrict__ dc, u64* X, const u64* S_NTT) {
+    const int n = dc->n, L = dc->L;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int item = blockIdx.y;
+    for (int j = 0; j < L; ++j) {
+        const size_t o = ((size_t)item * L + j) * n + k;
+        X[o] = mul_mod(X[o], S_NTT[(size_t)j * n + k], dc->mod[j]);
+    }
+}
+
+void launch_mul_s(const DevConsts* dc, const RnsParams& P, u64* X, const u64* S_NTT, int items,
+                  cudaStream_t st) {
+    if (!items) return;
+    k_mul_s<<<ew_grid(P.n, items), EW_THREADS, 0, st>>>(dc, X, S_NTT);
+    CSSC_CHECK_LAUNCH();
+}
+
+// E5: m = round(t (c0 + c1 s) / Q) mod t; maxdev = max |fraction| (2^-64 units)
+__global__ void k_dec_scale(const DevConsts* __restrict__ dc, const u64* const* CT,
+                            const u64* X, u64* M, unsigned long long* maxdev) {
+    const int n = dc->n, L = dc->L;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int item = blockIdx.y;
+    const u64* c0 = CT[item];
+    u64 shi = 0, slo = 0;
+    for (int i = 0; i < L; ++i) {
+        const u64 q = dc->mod[i].q;
+        const u64 x = add_mod(c0[(size_t)i * n + k], X[((size_t)item * L + i) * n + k], q);
+        const u64 xi = shoup(x, dc->QhatInv[i], dc->QhatInv_sh[i], q);
+        add128(shi, slo, umulhi(xi, dc->T1[i]), xi * dc->T1[i]);
+        add128(shi, slo, 0, umulhi(xi, dc->T0[i]));
+    }
+    const u64 r = shi + (slo >> 63);
+    M[(size_t)item * n + k] = r % dc->t;
+    const int64_t d = (int64_t)slo;
+    unsigned long long ad = d < 0 ? (unsigned long long)0 - (unsigned long long)d : (unsigned long long)d;
+    for (int off = 16; off > 0; off >>= 1) {
+        const unsigned long long o = __shfl_xor_sync(0xffffffffu, ad, off);
+        ad = o > ad ? o : ad;
+    }
+    if ((threadIdx.x & 31) == 0) atomicMax(maxdev + item, ad);
+}
+
+void launch_dec_scale(const DevConsts* dc, const RnsParams& P, const u64* const* CT,
+                      const u64* X, u64* M, unsigned long long* maxdev, int items,
+                      cudaStream_t st) {
+    if (!items) return;
+    cudaMemsetAsync(maxdev, 0, sizeof(unsigned long long) * items, st);
+    k_dec_scale<<<ew_grid(P.n, items), EW_THREADS, 0, st>>>(dc, CT, X, M, maxdev);
+    CSSC_CHECK_LAUNCH();
+}
+
+__global__ void k_decode_gather(const DevConsts* __restrict__ dc, const u64* M, u64* slots) {
+    const int S = dc->n / 2;
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const int item = blockIdx.y;
+    if (j >= S) return;
+    slots[(size_t)item * S + j] = M[(size_t)item * dc->n + dc->pos0[j]];
+}
+
+void launch_decode_gather(const DevConsts* dc, const RnsParams& P, const u64* M, u64* slots,
+                          int items, cudaStream_t st) {
+    if (!items) return;
+    k_decode_gather<<<dim3((unsigned)(P.S / EW_THREADS + 1), (unsigned)items), EW_THREADS, 0, st>>>(
+        dc, M, slots);
+    CSSC_CHECK_LAUNCH();
+}
+
+// ---------------------------------------------------------------------------
+// key generation helpers
+// ---------------------------------------------------------------------------
+__global__ void k_sample_small(int n, u64 seed, u32 n0, u64 id, int kind, int64_t* out) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= n / 8) return;
+    u32 blk[16];
+    chacha20_block(seed, (u32)b, n0, (u32)id, (u32)(id >> 32), blk);
+    for (int w = 0; w < 8; ++w) {
+        const u64 x = word64(blk, w);
+        out[8 * b + w] = kind == 0 ? ternary_of(x) : cbd_of(x);
+    }
+}
+
+void launch_sample_small(int logn, u64 seed, u32 dom, u64 id, int kind, int64_t* out,
+                         cudaStream_t st) {
+    const int n = 1 << logn;
+    k_sample_small<<<(n / 8 + 63) / 64, 64, 0, st>>>(n, seed, dom, id, kind, out);
+    CSSC_CHECK_LAUNCH();
+}
+
+// uniform residues for limbs [limb0, limb0+limbs): coefficient k uses words 2k, 2k+1
+__global__ void k_sample_uniform(const DevConsts* __restrict__ dc, u64 seed, u32 dom, int digit,
+                                 u64 id, int limb0, u64* out) {
+    const int n = dc->n;
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    const int l = limb0 + blockIdx.y;
+    if (b >= n / 4) return;
+    const Modulus md = dc->mod[l];
+    u32 blk[16];
+    chacha20_block(seed, (u32)b, dom | ((u32)l << 8) | ((u32)digit << 16), (u32)id,
+                   (u32)(id >> 32), blk);
+    for (int w = 0; w < 4; ++w) {
+        const u64 hi = word64(blk, 2 * w), lo = word64(blk, 2 * w + 1);
+        const u64 h = reduce128(0, hi, md.q, md.mu1, md.mu0);
+        out[(size_t)blockIdx.y * n + 4 * b + w] = reduce128(h, lo, md.q, md.mu1, md.mu0);
+    }
+}
+
+void launch_sample_uniform(const DevConsts* dc, int logn, u64 seed, u32 dom, int digit, u64 id,
+                           int limbs, int limb0, u64* out, cudaStream_t st) {
+    const int n = 1 << logn;
+    k_sample_uniform<<<dim3((unsigned)((n / 4 + 63) / 64), (unsigned)limbs), 64, 0, st>>>(
+        dc, seed, dom, digit, id, limb0, out);
+    CSSC_CHECK_LAUNCH();
+}
+
+__global__ void k_lift_small(const DevConsts* __restrict__ dc, const int64_t* s, int limb0,
+                             u64* out) {
+    const int n = dc->n;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int l = blockIdx.y;
+    out[(size_t)l * n + k] = lift_signed(s[k], dc->mod[limb0 + l].q);
+}
+
+void launch_lift_small(const DevConsts* dc, int logn, const int64_t* s, int limbs, int limb0,
+                       u64* out, cudaStream_t st) {
+    k_lift_small<<<ew_grid(1 << logn, limbs), EW_THREADS, 0, st>>>(dc, s, limb0, out);
+    CSSC_CHECK_LAUNCH();
+}
+
+__global__ void k_automorph_small(int n, u32 ginv, const int64_t* in, int64_t* out) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    bool neg;
+    const int idx = automorph_src(ginv, k, n, neg);
+    out[k] = neg ? -in[idx] : in[idx];
+}
+
+void launch_automorph_small(int logn, u32 g, const int64_t* in, int64_t* out, cudaStream_t st) {
+    const int n = 1 << logn;
+    // inverse of g in (Z/2N)^*: g^(N-1)
+    const u64 two_n = 2 * (u64)n;
+    u64 ginv = 1, b = g;
+    for (u64 e = (u64)n - 1; e; e >>= 1) {
+        if (e & 1) ginv = ginv * b % two_n;
+        b = b * b % two_n;
+    }
+    k_automorph_small<<<(n + 127) / 128, 128, 0, st>>>(n, (u32)ginv, in, out);
+    CSSC_CHECK_LAUNCH();
+}
+
+__global__ void k_key_combine(const DevConsts* __restrict__ dc, const u64* A, const u64* E,
+                              const u64* S, const u64* SP, int dlo, int dhi, u64* out) {
+    const int n = dc->n;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = blockIdx.y;
+    const Modulus md = dc->mod[j];
+    const size_t o = (size_t)j * n + k;
+    u64 v = add_mod(mul_mod(A[o], S[o], md), E[o], md.q);
+    v = neg_mod(v, md.q);
+    if (SP && j >= dlo && j < dhi)
+        v = add_mod(v, mul_mod(dc->P_q[j], SP[o], md), md.q);
+    out[o] = v;
+}
+
+void launch_key_combine(const DevConsts* dc, int logn, int limbs, const u64* A, const u64* E,
+                        const u64* S, const u64* SP, int digit_lo, int digit_hi, u64* out,
+                        cudaStream_t st) {
+    k_key_combine<<<ew_grid(1 << logn, limbs), EW_THREADS, 0, st>>>(dc, A, E, S, SP, digit_lo,
+                                                                    digit_hi, out);
+    CSSC_CHECK_LAUNCH();
+}
+
+__global__ void k_square(const DevConsts* __restrict__ dc, const u64* S, u64* out) {
+    const int n = dc->n;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = blockIdx.y;
+    const size_t o = (size_t)j * n + k;
+    out[o] = mul_mod(S[o], S[o], dc->mod[j]);
+}
+
+void launch_square(const DevConsts* dc, int logn, int limbs, const u64* S, u64* out,
+                   cudaStream_t st) {
+    k_square<<<ew_grid(1 << logn, limbs), EW_THREADS, 0, st>>>(dc, S, out);
+    CSSC_CHECK_LAUNCH();
+}
+
+// ---------------------------------------------------------------------------
+// generic ciphertext ops
+// ---------------------------------------------------------------------------
+__global__ void k_add(const DevConsts* __restrict__ dc, const u64* const* A, const u64* const* B,
+                      u64* const* OUT) {
+    const int n = dc->n, L = dc->L;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int item = blockIdx.y;
+    for (int p = 0; p < 2; ++p)
+        for (int j = 0; j < L; ++j) {
+            const size_t o = ((size_t)p * L + j) * n + k;
+            OUT[item][o] = add_mod(A[item][o], B[item][o], dc->mod[j].q);
+        }
+}
+
+void launch_add(const DevConsts* dc, const RnsParams& P, const u64* const* A,
+                const u64* const* B, u64* const* OUT, int items, cudaStream_t st) {
+    if (!items) return;
+    k_add<<<ew_grid(P.n, items), EW_THREADS, 0, st>>>(dc, A, B, OUT);
+    CSSC_CHECK_LAUNCH();
+}
+
+__global__ void k_automorph_ct(const DevConsts* __restrict__ dc, const u64* const* A,
+                               const u32* ginv, u64* const* OUT) {
+    const int n = dc->n, L = dc->L;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int item = blockIdx.y;
+    bool neg;
+    const int idx = automorph_src(ginv[item], k, n, neg);
+    for (int p = 0; p < 2; ++p)
+        for (int j = 0; j < L; ++j) {
+            const u64 v = A[item][((size_t)p * L + j) * n + idx];
+            OUT[item][((size_t)p * L + j) * n + k] = neg ? neg_mod(v, dc->mod[j].q) : v;
+        }
+}
+
+void launch_automorph_ct(const DevConsts* dc, const RnsParams& P, const u64* const* A,
+                         const u32* ginv, u64* const* OUT, int items, cudaStream_t st) {
+    if (!items) return;
+    k_automorph_ct<<<ew_grid(P.n, items), EW_THREADS, 0, st>>>(dc, A, ginv, OUT);
+    CSSC_CHECK_LAUNCH();
+}
+
+}  // namespace cssc

@@ -1,0 +1,111 @@
+// bfv_kernels.cuh -- launch wrappers for the sm_100a RNS-BFV kernels.
+//
+// Every wrapper processes a whole batch (all chunks x all RNS limbs) in one
+// launch.  Per-item operands are passed as device arrays of pointers so that
+// ciphertexts can live anywhere in the context's arena; temporaries are
+// contiguous [item][poly][limb][N].
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "rns_params.hpp"
+
+namespace cssc {
+
+struct NttJob {
+    const u64* src = nullptr;               // contiguous [items][limbs][N] (if src_items null)
+    const u64* const* src_items = nullptr;  // per-item base pointers, each [limbs][N]
+    int src_limb_offset = 0;                // skip this many limbs of each src item
+    u64* dst = nullptr;                     // contiguous [items][limbs][N] (if dst_items null)
+    u64* const* dst_items = nullptr;        // per-item base pointers, each [limbs][N]
+    int limbs = 0;                          // limbs per item
+    signed char pidx[64];                   // global prime index of limb j
+};
+
+// sampler domains (nonce word 0 = dom | limb << 8 | digit << 16)
+enum SampleDomain : u32 {
+    DOM_SK = 1,
+    DOM_PK_A = 2,
+    DOM_PK_E = 3,
+    DOM_KSK_A = 4,
+    DOM_KSK_E = 5,
+    DOM_ENC_U = 6,
+    DOM_ENC_E0 = 7,
+    DOM_ENC_E1 = 8,
+};
+
+void launch_ntt(const DevConsts* dc, int logn, bool inverse, const NttJob& job, int items,
+                cudaStream_t st);
+size_t ntt_smem_bytes(int logn);
+
+// ct x ct
+void launch_mul_extend(const DevConsts* dc, const RnsParams& P, const u64* const* A,
+                       const u64* const* B, u64* T, int items, cudaStream_t st);
+void launch_mul_tensor(const DevConsts* dc, const RnsParams& P, const u64* T, u64* Z, int items,
+                       cudaStream_t st);
+void launch_mul_scale(const DevConsts* dc, const RnsParams& P, const u64* Z, u64* const* OUT,
+                      u64* D2, int items, cudaStream_t st);
+
+// hybrid key switching
+void launch_ks_modup(const DevConsts* dc, const RnsParams& P, const u64* const* SRC, int src_poly,
+                     const u32* ginv, u64* DX, int items, cudaStream_t st);
+void launch_ks_modup_contig(const DevConsts* dc, const RnsParams& P, const u64* SRC, u64* DX,
+                            int items, cudaStream_t st);
+void launch_ks_inner(const DevConsts* dc, const RnsParams& P, const u64* DX,
+                     const u64* const* KEY, u64* ACC, int items, cudaStream_t st);
+// OUT[p] = BASE[p] (same index, optional) + (p==0 ? phi_g(RSRC[0]) : 0) (optional)
+//          + ModDown(ACC[p])
+void launch_ks_moddown(const DevConsts* dc, const RnsParams& P, const u64* ACC,
+                       const u64* const* BASE, const u64* const* RSRC, const u32* ginv,
+                       u64* const* OUT, int items, cudaStream_t st);
+
+// masks / plaintext products
+void launch_mask_accum(const DevConsts* dc, const RnsParams& P, const u64* MT,
+                       const int* slice_off, const int* slice_items, const int* item_mask,
+                       const u64* MASKS, u64* RES, int slices, cudaStream_t st);
+void launch_pointwise_plain(const DevConsts* dc, const RnsParams& P, u64* X, const u64* PT,
+                            int items, int polys, cudaStream_t st);
+
+// encoding / encryption / decryption
+// item i encodes vals[offs[i] .. offs[i+1]) (at most S values)
+void launch_encode_scatter(const DevConsts* dc, const RnsParams& P, const int64_t* vals,
+                           const u64* offs, u64* M, int items, cudaStream_t st);
+void launch_plain_lift(const DevConsts* dc, const RnsParams& P, const u64* M, u64* PT, int items,
+                       cudaStream_t st);
+void launch_enc_sample_u(const DevConsts* dc, const RnsParams& P, u64 seed, const u64* streams,
+                         u64* U, int items, cudaStream_t st);
+void launch_enc_pk(const DevConsts* dc, const RnsParams& P, const u64* PK, const u64* U, u64* C,
+                   int items, cudaStream_t st);
+void launch_enc_finish(const DevConsts* dc, const RnsParams& P, u64 seed, const u64* streams,
+                       const u64* C, const u64* M, u64* const* OUT, int items, cudaStream_t st);
+void launch_mul_s(const DevConsts* dc, const RnsParams& P, u64* X, const u64* S_NTT, int items,
+                  cudaStream_t st);
+void launch_dec_scale(const DevConsts* dc, const RnsParams& P, const u64* const* CT,
+                      const u64* X, u64* M, unsigned long long* maxdev, int items,
+                      cudaStream_t st);
+void launch_decode_gather(const DevConsts* dc, const RnsParams& P, const u64* M, u64* slots,
+                          int items, cudaStream_t st);
+
+// keys
+void launch_sample_small(int logn, u64 seed, u32 dom, u64 id, int kind /*0 ternary,1 cbd*/,
+                         int64_t* out, cudaStream_t st);
+void launch_sample_uniform(const DevConsts* dc, int logn, u64 seed, u32 dom, int digit, u64 id,
+                           int limbs, int limb0, u64* out, cudaStream_t st);
+void launch_lift_small(const DevConsts* dc, int logn, const int64_t* s, int limbs, int limb0,
+                       u64* out, cudaStream_t st);
+void launch_automorph_small(int logn, u32 g, const int64_t* in, int64_t* out, cudaStream_t st);
+// out = -(A*S + E) [+ P_q * SP on the digit's limbs]; all NTT form over limbs [0, limbs)
+void launch_key_combine(const DevConsts* dc, int logn, int limbs, const u64* A, const u64* E,
+                        const u64* S, const u64* SP, int digit_lo, int digit_hi, u64* out,
+                        cudaStream_t st);
+void launch_square(const DevConsts* dc, int logn, int limbs, const u64* S, u64* out,
+                   cudaStream_t st);
+
+// generic ct ops
+void launch_add(const DevConsts* dc, const RnsParams& P, const u64* const* A,
+                const u64* const* B, u64* const* OUT, int items, cudaStream_t st);
+void launch_automorph_ct(const DevConsts* dc, const RnsParams& P, const u64* const* A,
+                         const u32* ginv, u64* const* OUT, int items, cudaStream_t st);
+
+}  // namespace cssc

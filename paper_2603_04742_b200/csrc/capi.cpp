@@ -1,0 +1,475 @@
+// capi.cpp -- the extern "C" boundary (include/spmvgpu.h).
+// Device-side entry points (spmvgpu_*) wrap GpuContext / CloudPlan; the
+// protocol front door (cssc_*) wraps the host C++ spmv layer, which itself
+// talks to the device only through spmvgpu_*.  No exception crosses the ABI.
+#include <cstring>
+#include <memory>
+#include <new>
+#include <stdexcept>
+#include <string>
+
+#include "bfv_context.hpp"
+#include "cloud_plan.hpp"
+#include "host/batched_spmv.hpp"
+#include "spmv/gpu_backend.hpp"
+#include "spmv/synthetic.hpp"
+#include "spmvgpu.h"
+
+struct spmvgpu_ctx {
+    std::unique_ptr<cssc::GpuContext> g;
+    spmvgpu_params p;
+    spmv::HeParams hp;
+};
+
+struct spmvgpu_plan {
+    spmvgpu_ctx* ctx;
+    std::unique_ptr<cssc::CloudPlan> plan;
+};
+
+struct cssc_job {
+    spmvgpu_ctx* ctx;
+    std::vector<spmv::CsrMatrix> ms;
+    std::vector<std::vector<std::int64_t>> vs;
+    std::unique_ptr<spmv::detail::BatchedSpmv> job;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return SPMVGPU_OK;
+    } catch (const spmv::OverLengthError& e) {
+        return fail(SPMVGPU_ERR_OVER_LENGTH, e.what());
+    } catch (const std::length_error& e) {
+        return fail(SPMVGPU_ERR_OVER_LENGTH, e.what());
+    } catch (const spmv::NoiseExhaustedError& e) {
+        return fail(SPMVGPU_ERR_NOISE_EXHAUSTED, e.what());
+    } catch (const spmv::DimensionMismatchError& e) {
+        return fail(SPMVGPU_ERR_DIMENSION, e.what());
+    } catch (const spmv::ColumnTooTallError& e) {
+        return fail(SPMVGPU_ERR_COLUMN_TOO_TALL, e.what());
+    } catch (const spmv::IndexOutOfRangeError& e) {
+        return fail(SPMVGPU_ERR_INDEX_RANGE, e.what());
+    } catch (const spmv::DuplicateEntryError& e) {
+        return fail(SPMVGPU_ERR_DUPLICATE, e.what());
+    } catch (const std::invalid_argument& e) {
+        return fail(SPMVGPU_ERR_INVALID_ARGUMENT, e.what());
+    } catch (const std::bad_alloc&) {
+        return fail(SPMVGPU_ERR_INTERNAL, "host allocation failed");
+    } catch (const std::exception& e) {
+        const std::string w = e.what();
+        return fail(w.find("cuda") != std::string::npos || w.find("CUDA") != std::string::npos ||
+                            w.find("kernel") != std::string::npos
+                        ? SPMVGPU_ERR_CUDA
+                        : SPMVGPU_ERR_INTERNAL,
+                    w);
+    }
+}
+
+cssc::GpuContext& G(spmvgpu_ctx* c) {
+    if (!c || !c->g) throw std::invalid_argument("null context");
+    return *c->g;
+}
+
+using cssc::u64;
+
+std::vector<const u64*> cptrs(const spmvgpu_ct* h, size_t n) {
+    std::vector<const u64*> v(n);
+    for (size_t i = 0; i < n; ++i) {
+        if (!h[i]) throw std::invalid_argument("null ciphertext handle");
+        v[i] = reinterpret_cast<const u64*>(h[i]);
+    }
+    return v;
+}
+std::vector<u64*> mptrs(const spmvgpu_ct* h, size_t n) {
+    std::vector<u64*> v(n);
+    for (size_t i = 0; i < n; ++i) {
+        if (!h[i]) throw std::invalid_argument("null ciphertext handle");
+        v[i] = reinterpret_cast<u64*>(h[i]);
+    }
+    return v;
+}
+
+spmv::CsrMatrix to_csr(const cssc_csr& m) {
+    spmv::CsrMatrix out;
+    out.rows = m.rows;
+    out.cols = m.cols;
+    out.row_ptrs.assign(m.row_ptrs, m.row_ptrs + m.rows + 1);
+    const size_t nnz = m.rows ? static_cast<size_t>(m.row_ptrs[m.rows]) : 0;
+    if (m.rows && m.row_ptrs[0] != 0) throw std::invalid_argument("csr: row_ptrs[0] must be 0");
+    out.col_indices.assign(m.col_indices, m.col_indices + nnz);
+    out.values.assign(m.values, m.values + nnz);
+    for (size_t c : out.col_indices)
+        if (c >= m.cols) throw spmv::IndexOutOfRangeError("csr: column index out of range");
+    return out;
+}
+
+void fill_result(const spmv::SpmvResult& r, int64_t* values, cssc_result* res, cssc_message* msgs,
+                 uint64_t cap) {
+    if (values && !r.values.empty()) std::memcpy(values, r.values.data(), sizeof(int64_t) * r.values.size());
+    if (res) {
+        res->ledger = {r.op_ledger.n_mult_cc, r.op_ledger.n_mult_cp, r.op_ledger.n_rot,
+                       r.op_ledger.n_add,     r.op_ledger.n_enc,     r.op_ledger.n_dec};
+        res->n_ct = r.n_ct;
+        res->noise_model_bits = r.noise_budget_remaining_bits;
+        res->noise_measured_bits = r.measured_noise_budget_bits;
+        res->n_messages = r.message_ledger.messages.size();
+    }
+    if (msgs)
+        for (size_t i = 0; i < r.message_ledger.messages.size() && i < cap; ++i) {
+            const auto& m = r.message_ledger.messages[i];
+            msgs[i] = {static_cast<int64_t>(m.from), static_cast<int64_t>(m.to), static_cast<int64_t>(m.kind),
+                       static_cast<int64_t>(m.payload_bytes), static_cast<int64_t>(m.ciphertext_count)};
+        }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* spmvgpu_last_error(void) { return g_err.c_str(); }
+
+void spmvgpu_default_params(int logn, spmvgpu_params* p) {
+    std::memset(p, 0, sizeof *p);
+    p->logn = logn;
+    if (logn <= 13) {  // N = 8192: Q 3 x 54 bits + P 54 bits = 216 <= 218 (128-bit security)
+        p->L = 3, p->K = 1, p->alpha = 1, p->qbits = 54, p->pbits = 54;
+    } else if (logn == 14) {  // N = 16384: 6 x 60 = 360 <= 438
+        p->L = 4, p->K = 2, p->alpha = 2, p->qbits = 60, p->pbits = 60;
+    } else {  // N = 32768: 12 x 60 = 720 <= 881
+        p->L = 8, p->K = 4, p->alpha = 4, p->qbits = 60, p->pbits = 60;
+    }
+    p->t = 65537;
+    p->seed = 1;
+    p->device = 0;
+    p->ciphertext_size_mb = 0.52;
+    p->noise_initial = 146;
+    p->noise_ct_ct = 33;
+    p->noise_ct_pt = 26;
+    p->noise_add = 0;
+    p->noise_rot = 0;
+}
+
+int spmvgpu_ctx_create(const spmvgpu_params* p, spmvgpu_ctx** out) {
+    return guard([&] {
+        if (!p || !out) throw std::invalid_argument("null argument");
+        cssc::RnsConfig cfg;
+        cfg.logn = p->logn;
+        cfg.L = p->L;
+        cfg.K = p->K;
+        cfg.alpha = p->alpha;
+        cfg.qbits = p->qbits;
+        cfg.pbits = p->pbits;
+        cfg.t = p->t;
+        cfg.seed = p->seed;
+        auto c = std::make_unique<spmvgpu_ctx>();
+        c->p = *p;
+        c->hp.slot_count = (size_t)1 << (p->logn - 1);
+        c->hp.plaintext_modulus = p->t;
+        c->hp.ciphertext_size_mb = p->ciphertext_size_mb > 0 ? p->ciphertext_size_mb : 0.52;
+        c->hp.noise = {p->noise_initial, p->noise_ct_ct, p->noise_ct_pt, p->noise_add, p->noise_rot};
+        c->hp.validate();
+        c->g = std::make_unique<cssc::GpuContext>(cfg, p->device);
+        *out = c.release();
+    });
+}
+
+void spmvgpu_ctx_destroy(spmvgpu_ctx* c) { delete c; }
+
+int spmvgpu_ctx_primes(const spmvgpu_ctx* c, uint64_t* primes, int cap, int* count) {
+    return guard([&] {
+        const auto& P = const_cast<spmvgpu_ctx*>(c)->g->params();
+        *count = P.np;
+        for (int i = 0; i < P.np && i < cap; ++i) primes[i] = P.primes[i];
+    });
+}
+
+int spmvgpu_ctx_sizes(const spmvgpu_ctx* c, uint64_t* n, uint64_t* slots, uint64_t* ct_words,
+                      uint64_t* ksk_words, int* dnum) {
+    return guard([&] {
+        auto& g = G(const_cast<spmvgpu_ctx*>(c));
+        if (n) *n = g.n();
+        if (slots) *slots = g.params().S;
+        if (ct_words) *ct_words = g.ct_words();
+        if (ksk_words) *ksk_words = g.ksk_words();
+        if (dnum) *dnum = g.params().dnum;
+    });
+}
+
+int spmvgpu_sync(spmvgpu_ctx* c) { return guard([&] { G(c).synchronize(); }); }
+void* spmvgpu_stream(spmvgpu_ctx* c) { return c && c->g ? (void*)c->g->stream() : nullptr; }
+
+int spmvgpu_galois_keys(spmvgpu_ctx* c, const int64_t* steps, size_t n) {
+    return guard([&] { G(c).ensure_galois_keys(std::vector<int64_t>(steps, steps + n)); });
+}
+uint32_t spmvgpu_galois_element(const spmvgpu_ctx* c, int64_t step) {
+    return cssc::galois_element(step, const_cast<spmvgpu_ctx*>(c)->g->n());
+}
+int spmvgpu_download_sk(spmvgpu_ctx* c, int64_t* out) { return guard([&] { G(c).download_sk(out); }); }
+int spmvgpu_download_pk(spmvgpu_ctx* c, uint64_t* out) { return guard([&] { G(c).download_pk_coef(out); }); }
+int spmvgpu_download_ksk(spmvgpu_ctx* c, uint32_t which, uint64_t* out) {
+    return guard([&] { G(c).download_key_coef(which, out); });
+}
+
+int spmvgpu_ct_alloc(spmvgpu_ctx* c, size_t count, spmvgpu_ct* out) {
+    return guard([&] {
+        auto& g = G(c);
+        for (size_t i = 0; i < count; ++i) out[i] = reinterpret_cast<spmvgpu_ct>(g.pool().alloc(sizeof(u64) * g.ct_words()));
+    });
+}
+int spmvgpu_ct_free(spmvgpu_ctx* c, const spmvgpu_ct* cts, size_t count) {
+    return guard([&] {
+        auto& g = G(c);
+        for (size_t i = 0; i < count; ++i)
+            if (cts[i]) g.pool().release(reinterpret_cast<void*>(cts[i]), sizeof(u64) * g.ct_words());
+    });
+}
+int spmvgpu_ct_upload(spmvgpu_ctx* c, spmvgpu_ct ct, const uint64_t* words) {
+    return guard([&] {
+        auto& g = G(c);
+        cssc::cuda_check(cudaMemcpyAsync(reinterpret_cast<void*>(ct), words, sizeof(u64) * g.ct_words(),
+                                         cudaMemcpyHostToDevice, g.stream()), "ct upload");
+        g.synchronize();
+    });
+}
+int spmvgpu_ct_download(spmvgpu_ctx* c, spmvgpu_ct ct, uint64_t* words) {
+    return guard([&] {
+        auto& g = G(c);
+        cssc::cuda_check(cudaMemcpyAsync(words, reinterpret_cast<void*>(ct), sizeof(u64) * g.ct_words(),
+                                         cudaMemcpyDeviceToHost, g.stream()), "ct download");
+        g.synchronize();
+    });
+}
+
+int spmvgpu_encrypt(spmvgpu_ctx* c, const int64_t* vals, const uint64_t* offsets, const uint64_t* streams,
+                    const spmvgpu_ct* out, size_t n) {
+    return guard([&] {
+        auto& g = G(c);
+        std::vector<u64> st(n);
+        for (size_t i = 0; i < n; ++i) st[i] = streams && streams[i] ? streams[i] : g.next_stream_id();
+        g.encrypt(vals, offsets, st.data(), mptrs(out, n));
+    });
+}
+int spmvgpu_decrypt(spmvgpu_ctx* c, const spmvgpu_ct* cts, size_t n, uint64_t* slots, int32_t* budgets) {
+    return guard([&] {
+        std::vector<int> b(n);
+        G(c).decrypt(cptrs(cts, n), slots, b.data());
+        if (budgets)
+            for (size_t i = 0; i < n; ++i) budgets[i] = b[i];
+    });
+}
+int spmvgpu_add(spmvgpu_ctx* c, const spmvgpu_ct* a, const spmvgpu_ct* b, const spmvgpu_ct* out, size_t n) {
+    return guard([&] { G(c).add(cptrs(a, n), cptrs(b, n), mptrs(out, n)); });
+}
+int spmvgpu_mul_relin(spmvgpu_ctx* c, const spmvgpu_ct* a, const spmvgpu_ct* b, const spmvgpu_ct* out,
+                      size_t n) {
+    return guard([&] { G(c).mul_relin(cptrs(a, n), cptrs(b, n), mptrs(out, n)); });
+}
+int spmvgpu_rotate(spmvgpu_ctx* c, const spmvgpu_ct* src, const int64_t* steps, const spmvgpu_ct* out,
+                   size_t n) {
+    return guard([&] {
+        G(c).rotate(cptrs(src, n), std::vector<int64_t>(steps, steps + n), std::vector<const u64*>(n, nullptr),
+                    mptrs(out, n));
+    });
+}
+int spmvgpu_rotate_add(spmvgpu_ctx* c, const spmvgpu_ct* acc, const spmvgpu_ct* src, const int64_t* steps,
+                       const spmvgpu_ct* out, size_t n) {
+    return guard([&] {
+        auto o = mptrs(out, n);
+        auto s = cptrs(src, n);
+        for (size_t i = 0; i < n; ++i)
+            if ((const u64*)o[i] == s[i]) throw std::invalid_argument("rotate_add: out must not alias src");
+        G(c).rotate(s, std::vector<int64_t>(steps, steps + n), cptrs(acc, n), o);
+    });
+}
+int spmvgpu_mul_plain(spmvgpu_ctx* c, const spmvgpu_ct* a, const int64_t* vals, const uint64_t* offsets,
+                      const spmvgpu_ct* out, size_t n) {
+    return guard([&] { G(c).mul_plain(cptrs(a, n), vals, offsets, mptrs(out, n)); });
+}
+int spmvgpu_ntt(spmvgpu_ctx* c, int prime_index, uint64_t* data, size_t limbs, int inverse) {
+    return guard([&] {
+        auto& g = G(c);
+        if (prime_index < 0 || prime_index >= g.params().np) throw std::invalid_argument("prime index");
+        g.ntt_host(prime_index, data, (int)limbs, inverse != 0);
+    });
+}
+
+int spmvgpu_plan_create(spmvgpu_ctx* c, size_t n_chunks, const uint64_t* r, const uint64_t* cols,
+                        const uint32_t* slice, size_t n_slices, const spmvgpu_ct* a_cts, const spmvgpu_ct* b_cts,
+                        const spmvgpu_ct* out_cts, spmvgpu_plan** out) {
+    return guard([&] {
+        auto p = std::make_unique<spmvgpu_plan>();
+        p->ctx = c;
+        p->plan = std::make_unique<cssc::CloudPlan>(
+            G(c), std::vector<uint64_t>(r, r + n_chunks), std::vector<uint64_t>(cols, cols + n_chunks),
+            std::vector<uint32_t>(slice, slice + n_chunks), (int)n_slices, cptrs(a_cts, n_chunks),
+            cptrs(b_cts, n_chunks), mptrs(out_cts, n_slices));
+        *out = p.release();
+    });
+}
+int spmvgpu_plan_run(spmvgpu_plan* p) { return guard([&] { p->plan->run(); }); }
+int spmvgpu_plan_capture(spmvgpu_plan* p) { return guard([&] { p->plan->capture(); }); }
+int spmvgpu_plan_stats_get(const spmvgpu_plan* p, spmvgpu_plan_stats* o) {
+    return guard([&] {
+        const auto& s = p->plan->stats();
+        o->chunks = s.chunks;
+        o->slices = s.slices;
+        o->levels = s.levels;
+        o->kernels_per_run = s.kernels;
+        o->limb_ntts_per_run = s.limb_ntts;
+        o->rotations = s.rotations;
+        o->distinct_keys = s.distinct_keys;
+        o->hbm_bytes_algorithmic = s.hbm_bytes;
+        o->key_bytes_per_run = s.key_bytes;
+    });
+}
+void spmvgpu_plan_destroy(spmvgpu_plan* p) { delete p; }
+
+// ---------------------------------------------------------------- protocol front door
+int cssc_spmv_partitioned(spmvgpu_ctx* c, const cssc_csr* m, const int64_t* v, uint64_t vlen,
+                          uint64_t chunk_size, int key_holder, int64_t* values, cssc_result* res,
+                          cssc_message* msgs, uint64_t msg_cap) {
+    return guard([&] {
+        spmv::GpuBfvBackend be(c->hp, c);
+        const spmv::CsrMatrix mm = to_csr(*m);
+        const std::vector<int64_t> vv(v, v + vlen);
+        const auto r = spmv::spmv_partitioned(be, mm, vv, chunk_size, static_cast<spmv::PartyRole>(key_holder));
+        fill_result(r, values, res, msgs, msg_cap);
+    });
+}
+
+int cssc_spmv_batch(spmvgpu_ctx* c, const cssc_csr* ms, const int64_t* const* vs, size_t nmat, uint64_t chunk_size,
+                    int key_holder, int64_t* const* values, cssc_result* res) {
+    return guard([&] {
+        spmv::GpuBfvBackend be(c->hp, c);
+        std::vector<spmv::CsrMatrix> mats;
+        std::vector<std::vector<int64_t>> vecs;
+        for (size_t i = 0; i < nmat; ++i) {
+            mats.push_back(to_csr(ms[i]));
+            vecs.emplace_back(vs[i], vs[i] + ms[i].cols);
+        }
+        const auto r = spmv::spmv_batch(be, mats, vecs, chunk_size, static_cast<spmv::PartyRole>(key_holder));
+        for (size_t i = 0; i < nmat; ++i) fill_result(r[i], values ? values[i] : nullptr, res ? res + i : nullptr, nullptr, 0);
+    });
+}
+
+int cssc_job_create(spmvgpu_ctx* c, const cssc_csr* ms, const int64_t* const* vs, size_t nmat,
+                    uint64_t chunk_size, cssc_job** out) {
+    return guard([&] {
+        auto j = std::make_unique<cssc_job>();
+        j->ctx = c;
+        for (size_t i = 0; i < nmat; ++i) {
+            j->ms.push_back(to_csr(ms[i]));
+            j->vs.emplace_back(vs[i], vs[i] + ms[i].cols);
+        }
+        j->job = std::make_unique<spmv::detail::BatchedSpmv>(c, c->hp, j->ms, j->vs, chunk_size,
+                                                             spmv::PartyRole::ClientA);
+        *out = j.release();
+    });
+}
+int cssc_job_encrypt(cssc_job* j) { return guard([&] { j->job->encrypt(); }); }
+int cssc_job_cloud(cssc_job* j, int use_graph) { return guard([&] { j->job->cloud(use_graph != 0); }); }
+int cssc_job_finish(cssc_job* j, int64_t* const* values, cssc_result* res) {
+    return guard([&] {
+        const auto r = j->job->finish();
+        for (size_t i = 0; i < r.size(); ++i) fill_result(r[i], values ? values[i] : nullptr, res ? res + i : nullptr, nullptr, 0);
+    });
+}
+int cssc_job_plan_stats(const cssc_job* j, spmvgpu_plan_stats* out) {
+    return guard([&] {
+        std::memset(out, 0, sizeof *out);
+        if (j->job->plan()) spmvgpu_plan_stats_get(j->job->plan(), out);
+    });
+}
+int cssc_job_input_bytes(const cssc_job* j, uint64_t* h2d, uint64_t* d2h) {
+    return guard([&] {
+        *h2d = j->job->h2d_bytes();
+        *d2h = j->job->d2h_bytes();
+    });
+}
+void cssc_job_destroy(cssc_job* j) { delete j; }
+
+int64_t cssc_pack_chunks(const cssc_csr* m, uint64_t budget, int64_t* r_list, int64_t* c_list, int64_t* vflat,
+                         int64_t* cflat, int64_t* row_map, uint64_t* flat_total) {
+    int64_t n = 0;
+    const int st = guard([&] {
+        const auto cs = spmv::generate_chunks(spmv::csr_to_cssc(to_csr(*m)), budget);
+        uint64_t tot = 0;
+        for (const auto& ch : cs.chunks) tot += ch.value_flat.size();
+        *flat_total = tot;
+        if (r_list) {
+            uint64_t off = 0;
+            for (size_t i = 0; i < cs.n_ct(); ++i) {
+                r_list[i] = (int64_t)cs.r_list[i];
+                c_list[i] = (int64_t)cs.c_list[i];
+                std::memcpy(vflat + off, cs.chunks[i].value_flat.data(), 8 * cs.chunks[i].value_flat.size());
+                std::memcpy(cflat + off, cs.chunks[i].colidx_flat.data(), 8 * cs.chunks[i].colidx_flat.size());
+                off += cs.chunks[i].value_flat.size();
+            }
+            for (size_t i = 0; i < cs.row_map.size(); ++i) row_map[i] = (int64_t)cs.row_map[i];
+        }
+        n = (int64_t)cs.n_ct();
+    });
+    return st == SPMVGPU_OK ? n : st;
+}
+
+int cssc_rotation_schedule(uint64_t rows, uint64_t cols, uint64_t* offsets, int32_t* from_acc) {
+    int n = 0;
+    const int st = guard([&] {
+        const auto s = spmv::rotation_schedule(rows, cols);
+        for (size_t i = 0; i < s.size(); ++i) {
+            if (offsets) offsets[i] = s[i].offset;
+            if (from_acc) from_acc[i] = s[i].from_accumulator ? 1 : 0;
+        }
+        n = (int)s.size();
+    });
+    return st == SPMVGPU_OK ? n : st;
+}
+
+static int64_t export_csr(const spmv::CsrMatrix& m, int64_t* rp, int64_t* ci, int64_t* va, uint64_t cap) {
+    if (m.nnz() > cap) return -(int64_t)m.nnz() - 100;  // caller retries with a larger buffer
+    for (size_t i = 0; i <= m.rows; ++i) rp[i] = (int64_t)m.row_ptrs[i];
+    for (size_t k = 0; k < m.nnz(); ++k) {
+        ci[k] = (int64_t)m.col_indices[k];
+        va[k] = m.values[k];
+    }
+    return (int64_t)m.nnz();
+}
+
+int64_t cssc_random_sparse_csr(uint64_t rows, uint64_t cols, uint64_t nnz, uint64_t seed, int64_t lo, int64_t hi,
+                               int64_t* rp, int64_t* ci, int64_t* va) {
+    int64_t r = 0;
+    const int st = guard([&] { r = export_csr(spmv::random_sparse_csr(rows, cols, nnz, seed, lo, hi), rp, ci, va, nnz); });
+    return st == SPMVGPU_OK ? r : st;
+}
+void cssc_random_vector(uint64_t len, uint64_t seed, int64_t lo, int64_t hi, int64_t* out) {
+    const auto v = spmv::random_vector(len, seed, lo, hi);
+    std::memcpy(out, v.data(), sizeof(int64_t) * len);
+}
+void cssc_random_nonzero_vector(uint64_t len, uint64_t seed, int64_t lo, int64_t hi, int64_t* out) {
+    const auto v = spmv::random_nonzero_vector(len, seed, lo, hi);
+    std::memcpy(out, v.data(), sizeof(int64_t) * len);
+}
+int64_t cssc_power_law_csr(uint64_t n, double mean_degree, double exponent, uint64_t seed, int64_t lo, int64_t hi,
+                           int64_t* rp, int64_t* ci, int64_t* va, uint64_t cap) {
+    int64_t r = 0;
+    const int st = guard([&] { r = export_csr(spmv::power_law_csr(n, mean_degree, exponent, seed, lo, hi), rp, ci, va, cap); });
+    return st == SPMVGPU_OK ? r : st;
+}
+int64_t cssc_stencil27_csr(uint64_t side, uint64_t seed, int64_t lo, int64_t hi, int64_t* rp, int64_t* ci,
+                           int64_t* va, uint64_t cap) {
+    int64_t r = 0;
+    const int st = guard([&] { r = export_csr(spmv::stencil27_csr(side, seed, lo, hi), rp, ci, va, cap); });
+    return st == SPMVGPU_OK ? r : st;
+}
+
+}  // extern "C"

@@ -1,0 +1,77 @@
+// cloud_plan.hpp -- the batched cloud phase of the encrypted CSSC SpMV.
+//
+// Lowers the reference's per-chunk loop (protocol.cpp:121-140:
+// multiply -> intra_chunk_sum -> inter_chunk_sum) over every chunk of every
+// slice (and every matrix of a batch) into a fixed launch sequence:
+//   1. one batched ct x ct multiply + relinearisation over all chunks;
+//   2. level l = 0..depth-1 of the rotate-and-add trees: every chunk whose
+//      rotation_schedule (aggregate.cpp:19-34) has > l steps does
+//      acc <- acc + rot(step.from_accumulator ? acc : product, offset)
+//      in one fused key-switch launch group (chunks are ordered by descending
+//      schedule length so level l is a prefix of the item list);
+//   3. one masked, segmented accumulation of all folded chunks into one
+//      result ciphertext per slice (inter_chunk_sum, aggregate.cpp:55-74).
+// The sequence is fixed at plan time and can be captured as a CUDA graph.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <vector>
+
+#include "bfv_context.hpp"
+
+namespace cssc {
+
+struct PlanStats {
+    uint64_t chunks = 0, slices = 0, levels = 0, kernels = 0, limb_ntts = 0;
+    uint64_t rotations = 0, distinct_keys = 0;
+    uint64_t hbm_bytes = 0, key_bytes = 0;
+};
+
+class CloudPlan {
+public:
+    // a/b: per-chunk input ciphertexts; out: one result ciphertext per slice
+    CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r, const std::vector<uint64_t>& c,
+              const std::vector<uint32_t>& slice, int n_slices, const std::vector<const u64*>& a,
+              const std::vector<const u64*>& b, const std::vector<u64*>& out);
+    ~CloudPlan();
+    void run();      // enqueue (graph replay when captured)
+    void capture();  // record a CUDA graph of run()
+    const PlanStats& stats() const { return stats_; }
+
+private:
+    void record();
+    template <class T>
+    T* put(const std::vector<T>& v);
+
+    GpuContext& ctx_;
+    int n_ = 0, ns_ = 0;
+    PlanStats stats_;
+    DevBuf prod_, acc0_, acc1_;
+    DevBuf T_, Z_, D2_, DX_, ACC_, MT_, MASKS_;
+    std::vector<DevBuf> arrays_;  // device pointer / index arrays
+    // device arrays
+    const u64* const* A_ = nullptr;
+    const u64* const* B_ = nullptr;
+    u64* const* PROD_ = nullptr;
+    const u64* const* RLK_ = nullptr;
+    struct Level {
+        int items;
+        const u64* const* src;
+        const u64* const* base;
+        u64* const* out;
+        const u64* const* key;
+        const u32* ginv;
+    };
+    std::vector<Level> levels_;
+    const u64* const* FINAL_ = nullptr;
+    u64* const* OUT_ = nullptr;
+    const int* slice_off_ = nullptr;
+    const int* slice_items_ = nullptr;
+    const int* item_mask_ = nullptr;
+    int n_masks_ = 0;
+    cudaGraph_t graph_ = nullptr;
+    cudaGraphExec_t exec_ = nullptr;
+};
+
+}  // namespace cssc

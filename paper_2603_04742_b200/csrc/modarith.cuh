@@ -1,0 +1,82 @@
+// modarith.cuh -- 64-bit modular arithmetic for the RNS-BFV kernels (sm_100a).
+//
+// All primes are < 2^62 so lazy values in [0, 4q) fit a u64.  Constant
+// multiplications (NTT twiddles, basis-conversion constants) use Shoup's
+// precomputed quotient (3 u64 multiplies); variable x variable products use a
+// Barrett reduction of the 128-bit product with mu = floor(2^128 / q).
+// Results are always canonical in [0, q) unless the name says "lazy", so the
+// outputs are independent of the reduction strategy.
+#pragma once
+#include <cstdint>
+
+#ifdef __CUDACC__
+#define CSSC_HD __host__ __device__ __forceinline__
+#else
+#define CSSC_HD inline
+#endif
+
+namespace cssc {
+
+using u64 = std::uint64_t;
+using u32 = std::uint32_t;
+
+CSSC_HD u64 umulhi(u64 a, u64 b) {
+#ifdef __CUDA_ARCH__
+    return __umul64hi(a, b);
+#else
+    return (u64)(((unsigned __int128)a * b) >> 64);
+#endif
+}
+
+CSSC_HD u64 add_mod(u64 a, u64 b, u64 q) {
+    u64 s = a + b;
+    return s >= q ? s - q : s;
+}
+CSSC_HD u64 sub_mod(u64 a, u64 b, u64 q) { return a >= b ? a - b : a + q - b; }
+CSSC_HD u64 neg_mod(u64 a, u64 q) { return a ? q - a : 0; }
+
+// a * w mod q in [0, 2q) for any a < 2^64, w < q, wsh = floor(w * 2^64 / q)
+CSSC_HD u64 shoup_lazy(u64 a, u64 w, u64 wsh, u64 q) {
+    u64 qh = umulhi(a, wsh);
+    return a * w - qh * q;
+}
+CSSC_HD u64 shoup(u64 a, u64 w, u64 wsh, u64 q) {
+    u64 r = shoup_lazy(a, w, wsh, q);
+    return r >= q ? r - q : r;
+}
+
+// (z1 * 2^64 + z0) mod q for z1 < q; mu = floor(2^128 / q) = mu1 * 2^64 + mu0.
+// The quotient estimate is at most 2 short, hence two conditional subtractions.
+CSSC_HD u64 reduce128(u64 z1, u64 z0, u64 q, u64 mu1, u64 mu0) {
+    u64 a_hi = umulhi(z0, mu0);
+    u64 b_lo = z0 * mu1, b_hi = umulhi(z0, mu1);
+    u64 c_lo = z1 * mu0, c_hi = umulhi(z1, mu0);
+    u64 s = a_hi + b_lo;
+    u64 carry = s < a_hi;
+    u64 s2 = s + c_lo;
+    carry += s2 < s;
+    u64 qhat = z1 * mu1 + b_hi + c_hi + carry;
+    u64 r = z0 - qhat * q;
+    if (r >= q) r -= q;
+    if (r >= q) r -= q;
+    return r;
+}
+
+CSSC_HD u64 mul_mod(u64 a, u64 b, u64 q, u64 mu1, u64 mu0) {
+    return reduce128(umulhi(a, b), a * b, q, mu1, mu0);
+}
+
+// Per-prime constants needed inside kernels.
+struct Modulus {
+    u64 q;
+    u64 mu1, mu0;  // floor(2^128 / q)
+};
+
+CSSC_HD u64 mul_mod(u64 a, u64 b, const Modulus& m) { return mul_mod(a, b, m.q, m.mu1, m.mu0); }
+CSSC_HD u64 reduce64(u64 a, const Modulus& m) { return reduce128(0, a, m.q, m.mu1, m.mu0); }
+
+// Fixed-point fraction floor(y * 2^64 / x) ~ y*R1 + hi(y*R0), R = floor(2^128/x):
+// the integer formula shared with the oracle (E1).
+CSSC_HD u64 frac64(u64 y, u64 R1, u64 R0) { return y * R1 + umulhi(y, R0); }
+
+}  // namespace cssc
