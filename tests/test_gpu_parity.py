@@ -1,0 +1,108 @@
+"""GPU parity: the sm_100a path against the CPU oracle, word for word (P5),
+and decryptions against the reference simulator slot for slot (P1).
+
+Keys and input ciphertexts come from the same seeds on both sides; every
+output polynomial is compared in canonical coefficient form."""
+import numpy as np
+import pytest
+
+import paper_2603_04742_b200 as pk
+from oracle_bindings import BfvOracle
+
+pytestmark = pytest.mark.gpu
+
+# (logn, overrides): small rings for speed plus the real C1/C2 parameter sets
+SETS = [
+    (10, {}),
+    (11, dict(L=4, K=2, alpha=2, qbits=60, pbits=60)),
+    (12, dict(L=5, K=2, alpha=2, qbits=58, pbits=58)),
+    (13, {}),
+]
+
+
+@pytest.fixture(scope="module", params=SETS, ids=lambda s: f"logn{s[0]}")
+def pair(request):
+    logn, ov = request.param
+    ctx = pk.Context(logn=logn, seed=7, **ov)
+    orc = BfvOracle.like(ctx)
+    return ctx, orc
+
+
+def rand_vals(n, seed, lo=-8, hi=8):
+    rng = np.random.default_rng(seed)
+    return rng.integers(lo, hi + 1, n)
+
+
+def test_primes_match(pair):
+    ctx, orc = pair
+    assert ctx.primes == orc.primes
+
+
+def test_ntt_matches_oracle(pair):
+    ctx, orc = pair
+    rng = np.random.default_rng(1)
+    for pi in (0, len(ctx.primes) - 1, len(ctx.primes) - 2):
+        q = ctx.primes[pi]
+        a = np.array([int(x) for x in rng.integers(0, q, ctx.n, dtype=np.uint64)], np.uint64) % np.uint64(q)
+        assert np.array_equal(ctx.ntt(pi, a), orc.ntt(pi, a))
+        assert np.array_equal(ctx.ntt(pi, a, inverse=True), orc.ntt(pi, a, inverse=True))
+
+
+def test_keys_match(pair):
+    ctx, orc = pair
+    assert np.array_equal(ctx.download_sk(), orc.sk())
+    assert np.array_equal(ctx.download_pk(), orc.pk())
+    assert np.array_equal(ctx.download_ksk(0), orc.ksk(0))
+    g = ctx.galois_element(3)
+    assert g == orc.galois_elt(3)
+    assert np.array_equal(ctx.download_ksk(g), orc.ksk(g))
+
+
+def test_encrypt_decrypt_match(pair):
+    ctx, orc = pair
+    S = ctx.slots
+    vals = [rand_vals(S, 1), rand_vals(S // 3, 2), rand_vals(0, 3)]
+    streams = [101, 102, 103]
+    hs = ctx.encrypt(vals, streams)
+    for h, v, s in zip(hs, vals, streams):
+        assert np.array_equal(ctx.download(int(h)), orc.encrypt(v, s))
+    slots, budgets = ctx.decrypt(hs)
+    for row, v in zip(slots, vals):
+        want = np.zeros(S, np.int64)
+        want[: len(v)] = np.mod(v, 65537)
+        assert np.array_equal(row.astype(np.int64), want)
+    assert (budgets > 0).all()
+    ctx.free(hs)
+
+
+def test_mul_relin_rotate_mask_match(pair):
+    ctx, orc = pair
+    S = ctx.slots
+    a, b = rand_vals(S, 11), rand_vals(S, 12)
+    ha, hb = ctx.encrypt([a, b], [201, 202])
+    ca, cb = orc.encrypt(a, 201), orc.encrypt(b, 202)
+    hp = ctx.mul_relin([ha], [hb])
+    cp = orc.mul_relin(ca, cb)
+    assert np.array_equal(ctx.download(int(hp[0])), cp)
+    prod = (a * b) % 65537
+    for k in (1, 5, S - 1, -3):
+        hr = ctx.rotate(hp, [k])
+        cr = orc.rotate(cp, k)
+        assert np.array_equal(ctx.download(int(hr[0])), cr), k
+        sl, bud = ctx.decrypt(hr)
+        assert np.array_equal(sl[0].astype(np.int64), np.roll(prod, -k))
+        assert bud[0] > 0
+        ctx.free(hr)
+    # fused rotate-and-add
+    hs = ctx.rotate_add(hp, hp, [7])
+    cs = orc.add(cp, orc.rotate(cp, 7))
+    assert np.array_equal(ctx.download(int(hs[0])), cs)
+    # plaintext mask
+    hm = ctx.mul_plain(hs, [np.ones(9, np.int64)])
+    cm = orc.mul_plain(cs, np.ones(9, np.int64))
+    assert np.array_equal(ctx.download(int(hm[0])), cm)
+    sl, _ = ctx.decrypt(hm)
+    want = (prod + np.roll(prod, -7)) % 65537
+    want[9:] = 0
+    assert np.array_equal(sl[0].astype(np.int64), want)
+    ctx.free(np.concatenate([ha[None], hb[None], hp, hs, hm]))

@@ -1,0 +1,113 @@
+"""End-to-end encrypted SpMV on the GPU backend vs the reference semantics (P1-P4).
+
+The checker is the reference library itself (oracle/_ref, compiled from
+/root/reference) when present, else the C restatement (oracle/sim_oracle.c);
+both run SimBackend with slot_count = S = N/2."""
+import numpy as np
+import pytest
+
+import paper_2603_04742_b200 as pk
+from oracle_bindings import ref_lib, sim_spmv_partitioned
+
+pytestmark = pytest.mark.gpu
+
+
+def checker(m, v, S, chunk):
+    lib = ref_lib()
+    return sim_spmv_partitioned(m, v, S, chunk, lib=lib)
+
+
+@pytest.fixture(scope="module")
+def ctx10():
+    return pk.Context(logn=10, seed=3)
+
+
+@pytest.fixture(scope="module")
+def ctx13():
+    return pk.Context(logn=13, seed=1)
+
+
+def assert_same(got, want):
+    assert np.array_equal(got["values"], want["values"])
+    assert got["ledger"] == want["ledger"]
+    assert got["n_ct"] == want["n_ct"]
+    assert got["noise"] == want["noise"]
+    if "messages" in got:
+        assert got["messages"] == want["messages"]
+
+
+@pytest.mark.parametrize("seed", range(900, 912))
+def test_random_small_instances(ctx10, seed):
+    rows, cols = 1 + seed % 17, 1 + (seed * 3) % 19
+    nnz = (rows * cols) // (1 + seed % 3)
+    m = pk.random_sparse_csr(rows, cols, nnz, seed)
+    v = pk.random_vector(cols, seed)
+    got = pk.spmv_partitioned(ctx10, m, v, ctx10.slots)
+    assert_same(got, checker(m, v, ctx10.slots, ctx10.slots))
+    assert got["measured_noise"] > 0 or got["n_ct"] == 0
+
+
+@pytest.mark.parametrize("seed", range(1200, 1206))
+def test_partitioned_small_budget(ctx10, seed):
+    rows, cols = 8 + seed % 70, 1 + (seed * 3) % 12
+    m = pk.random_sparse_csr(rows, cols, rows * cols // 4, seed)
+    v = pk.random_vector(cols, seed)
+    got = pk.spmv_partitioned(ctx10, m, v, 8)
+    assert_same(got, checker(m, v, ctx10.slots, 8))
+
+
+def test_edge_cases(ctx10):
+    S = ctx10.slots
+    zeros = pk.Csr.from_dense([[0, 0], [0, 0]])
+    r = pk.spmv_partitioned(ctx10, zeros, [3, 9], S)
+    assert list(r["values"]) == [0, 0] and r["n_ct"] == 0 and r["noise"] == 146
+    m = pk.Csr.from_dense([[0, 0], [7, 0], [0, 0]])
+    assert list(pk.spmv_partitioned(ctx10, m, [3, 9], S)["values"]) == [0, 21, 0]
+    ident = pk.Csr.from_dense([[1, 0], [0, 1]])
+    r = pk.spmv_partitioned(ctx10, ident, [5, -3], S)
+    assert list(r["values"]) == [5, -3] and r["noise"] == 87
+    empty = pk.Csr(0, 4, np.zeros(1, np.int64), np.zeros(0, np.int64), np.zeros(0, np.int64))
+    assert pk.spmv_partitioned(ctx10, empty, [1, 2, 3, 4], 8)["values"].size == 0
+    with pytest.raises(pk.SpmvError) as e:
+        pk.spmv_partitioned(ctx10, ident, [1, 2, 3], S)
+    assert e.value.kind == "DimensionMismatchError"
+    with pytest.raises(pk.SpmvError) as e:
+        pk.spmv_partitioned(ctx10, ident, [1, 2], S + 1)
+    assert e.value.kind == "ValueError"
+
+
+def test_config1_matches_reference(ctx13):
+    """BASELINE config 1: 256x256, 1% density, values in [-8,8]\\{0}, N=8192."""
+    m = pk.random_sparse_csr(256, 256, 655, 1, -8, 8)
+    v = pk.random_vector(256, 1, -8, 8, nonzero=True)
+    got = pk.spmv_partitioned(ctx13, m, v)
+    want = checker(m, v, ctx13.slots, ctx13.slots)
+    assert_same(got, want)
+    dense = m.dense()
+    exact = (dense @ v) % 65537
+    exact = np.where(exact > 32768, exact - 65537, exact)
+    assert np.array_equal(got["values"], exact)
+
+
+def test_batch_equals_individual_runs(ctx10):
+    ms = [pk.random_sparse_csr(40, 40, 120, s, -8, 8) for s in range(500, 506)]
+    vs = [pk.random_vector(40, s, -8, 8, nonzero=True) for s in range(500, 506)]
+    batch = pk.spmv_batch(ctx10, ms, vs, 32)
+    for m, v, b in zip(ms, vs, batch):
+        want = checker(m, v, ctx10.slots, 32)
+        assert np.array_equal(b["values"], want["values"])
+        assert b["ledger"] == want["ledger"]
+
+
+def test_job_graph_replay(ctx10):
+    ms = [pk.random_sparse_csr(60, 50, 300, s, -8, 8) for s in range(7, 10)]
+    vs = [pk.random_vector(50, s, -8, 8, nonzero=True) for s in range(7, 10)]
+    job = pk.Job(ctx10, ms, vs)
+    job.encrypt()
+    for _ in range(3):
+        job.cloud(graph=True)
+    res = job.finish()
+    for m, v, r in zip(ms, vs, res):
+        assert np.array_equal(r["values"], checker(m, v, ctx10.slots, ctx10.slots)["values"])
+    st = job.stats()
+    assert st["chunks"] > 0 and st["limb_ntts_per_run"] > 0
