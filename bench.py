@@ -1,0 +1,373 @@
+#!/usr/bin/env python
+"""Encrypted CSSC SpMV benchmark (B200, sm_100a RNS-BFV).
+
+One "step" = the cloud phase of one encrypted SpMV workload (BASELINE.json
+config; default config 2 = configs[1], 4096x4096 at 0.1%): batched ct x ct
+multiply + relinearisation, the rotate-and-add trees, and the masked per-slice
+accumulation, from device-resident input ciphertexts to result ciphertexts.
+  value  : ms per step on the device (CUDA events, L2 flushed before every step)
+  e2e    : the same workload through the public API (spmv_batch: host CSR +
+           vector in, decrypted values out; pack, H2D, encrypt, cloud,
+           decrypt, D2H all inside the timed region)
+  roofline: the dominant kernel (batched NTT) against the measured integer
+           butterfly peak, plus its HBM fraction of MEASURED_PEAKS.json
+  cpu_baseline: the unmodified reference (oracle/_ref, SimBackend) on 1 host core
+
+Multi-GPU (torchrun): every rank runs its own replica of the workload (weak
+scaling, no data-path collective); ms_per_step is the max over ranks and
+value = ms_per_step / world_size (amortised latency per workload).
+`--impl reference` times the reference's own CPU path instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "encrypted SpMV latency (ms) & key-switch/NTT GB/s vs HBM roofline, 1xB200"
+
+
+def make_config(cfg: int):
+    import paper_2603_04742_b200 as pk
+
+    if cfg == 1:
+        ms = [pk.random_sparse_csr(256, 256, 655, 1, -8, 8)]
+        vs = [pk.random_vector(256, 1, -8, 8, nonzero=True)]
+        return dict(name="C1 256x256 uniform 1% (655 nnz)", logn=13, ms=ms, vs=vs)
+    if cfg == 2:
+        ms = [pk.random_sparse_csr(4096, 4096, 16777, 2, -8, 8)]
+        vs = [pk.random_vector(4096, 2, -8, 8, nonzero=True)]
+        return dict(name="C2 4096x4096 uniform 0.1% (16777 nnz)", logn=14, ms=ms, vs=vs)
+    if cfg == 3:
+        ms = [pk.power_law_csr(16384, 12.0, 2.0, 3, -8, 8)]
+        vs = [pk.random_vector(16384, 3, -8, 8, nonzero=True)]
+        return dict(name="C3 16384x16384 power-law Zipf(2) mean 12", logn=14, ms=ms, vs=vs)
+    if cfg == 4:
+        ms = [pk.stencil27_csr(32, 4, -8, 8)]
+        vs = [pk.random_vector(32768, 4, -8, 8, nonzero=True)]
+        return dict(name="C4 32^3 grid 27-point stencil (830584 nnz)", logn=15, ms=ms, vs=vs)
+    if cfg == 5:
+        ms = [pk.random_sparse_csr(2048, 2048, 20972, 500 + k, -8, 8) for k in range(64)]
+        vs = [pk.random_vector(2048, 500 + k, -8, 8, nonzero=True) for k in range(64)]
+        return dict(name="C5 64 x 2048x2048 uniform 0.5% (20972 nnz each)", logn=14, ms=ms, vs=vs)
+    raise ValueError(cfg)
+
+
+def exact_values(m, v, t=65537):
+    """Plain matvec reduced to the centred residues the decryptor reports."""
+    rp, ci, va = m.row_ptrs, m.col_indices, m.values
+    rows = np.repeat(np.arange(m.rows), np.diff(rp))
+    acc = np.zeros(m.rows, np.int64)
+    np.add.at(acc, rows, va * v[ci])
+    r = np.mod(acc, t)
+    return np.where(r > t // 2, r - t, r)
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled while the GPU is under load."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 3 + i and r[3 + i] == "Active"})
+        loaded = [s for s in sm if s > 300] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+
+
+def cpu_reference_time(ms, vs, slot_count, budget_s=3.0):
+    """The unmodified reference SimBackend spmv_partitioned on 1 host core
+    (oracle/_ref); best-of-reps wall time of one whole workload, ms."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    from oracle_bindings import ref_lib, _i64, _p, i64p
+
+    L = ref_lib()
+    if L is None:
+        return None
+    keep = []
+
+    def one():
+        tot = 0.0
+        for m, v in zip(ms, vs):
+            rp, ci, va, vv = _i64(m.row_ptrs), _i64(m.col_indices), _i64(m.values), _i64(v)
+            keep.append((rp, ci, va, vv))
+            tot += L.ref_time_spmv_partitioned(slot_count, 65537, m.rows, m.cols, _p(rp, i64p), _p(ci, i64p),
+                                               _p(va, i64p), _p(vv, i64p), slot_count, 1)
+        return tot
+
+    first = one()
+    reps = max(1, min(200, int(budget_s * 1e3 / max(first, 1e-3))))
+    best = min([first] + [one() for _ in range(reps - 1)])
+    return best, reps
+
+
+def run_reference_arm(args, cfg):
+    """--impl reference: the reference's own CPU path on all host cores it can use
+    (independent matrices in parallel threads; the library itself is single-threaded)."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    from oracle_bindings import ref_lib, _i64, _p, i64p
+
+    L = ref_lib()
+    if L is None:
+        return {"impl": "reference", "unavailable": "oracle/_ref/libspmv_ref.so not built"}
+    S = 1 << (cfg["logn"] - 1)
+    ms, vs = cfg["ms"], cfg["vs"]
+    arrays = [(_i64(m.row_ptrs), _i64(m.col_indices), _i64(m.values), _i64(v)) for m, v in zip(ms, vs)]
+    threads = max(1, min(len(ms), os.cpu_count() or 1))
+
+    def work(idx):
+        for i in idx:
+            rp, ci, va, vv = arrays[i]
+            m = ms[i]
+            L.ref_time_spmv_partitioned(S, 65537, m.rows, m.cols, _p(rp, i64p), _p(ci, i64p), _p(va, i64p),
+                                        _p(vv, i64p), S, 1)
+
+    def step():
+        parts = [list(range(k, len(ms), threads)) for k in range(threads)]
+        ts = [threading.Thread(target=work, args=(p,)) for p in parts]
+        t0 = time.perf_counter()
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        return (time.perf_counter() - t0) * 1e3
+
+    for _ in range(args.warmup):
+        step()
+    times = [step() for _ in range(args.steps)]
+    v = statistics.mean(times)
+    sample = f"{cfg['name']}: full workload per step ({len(ms)} matrix/matrices), SimBackend slot_count={S}"
+    return {"metric": METRIC, "value": round(v, 4), "unit": "ms", "n_gpus": 0, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(v, 4), "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u64", "data": "synthetic (seeded, BASELINE.json shapes)",
+            "impl": "reference",
+            "config": {"workload": cfg["name"], "parallelism": f"{threads} host threads"},
+            "cpu_baseline": {"value": round(v, 4), "unit": "ms", "cores": threads, "kind": "reference",
+                             "sample": sample},
+            "e2e": {"value": round(v, 4), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def measure_config(pk, cfg, args, rank, world, device, full=True):
+    import torch
+
+    ctx = pk.Context(logn=cfg["logn"], seed=1, device=device)
+    ms, vs = cfg["ms"], cfg["vs"]
+    job = pk.Job(ctx, ms, vs)
+    job.encrypt()
+    job.cloud(graph=True)
+    res = job.finish()
+    verified = all(np.array_equal(r["values"], exact_values(m, v)) for m, v, r in zip(ms, vs, res))
+    st = job.stats()
+    stream = torch.cuda.ExternalStream(ctx.stream_ptr(), device=device)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
+
+    def step_timed():
+        with torch.cuda.stream(stream):
+            flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        job.cloud(graph=True)
+        b.record(stream)
+        return a, b
+
+    for _ in range(args.warmup):
+        step_timed()
+    torch.cuda.synchronize(device)
+    sampler = ClockSampler(device)
+    sampler.start()
+    # keep the GPU busy long enough for the clock sampler to see the loaded state
+    t_end = time.time() + (1.0 if full else 0.3)
+    while time.time() < t_end:
+        for _ in range(4):
+            job.cloud(graph=True)
+        torch.cuda.synchronize(device)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize(device)
+    evs = [step_timed() for _ in range(args.steps)]
+    torch.cuda.synchronize(device)
+    if world > 1:
+        torch.distributed.barrier()
+    clocks = sampler.stop()
+    times = [a.elapsed_time(b) for a, b in evs]
+    ms_step = statistics.mean(times)
+    if world > 1:
+        t = torch.tensor([ms_step], device=device)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms_step = float(t.item())
+    out = {"name": cfg["name"], "ms_per_step": ms_step, "median_ms": statistics.median(times),
+           "min_ms": min(times), "verified": verified, "plan": st, "clocks": clocks,
+           "measured_noise_bits": min(r["measured_noise"] for r in res if r["n_ct"] > 0)}
+    if not full:
+        job.close()
+        ctx.close()
+        return out
+
+    # e2e through the public API (host in, host out)
+    h2d, d2h = job.io_bytes()
+    e2e = []
+    for i in range(max(2, min(args.steps, 10)) + 1):
+        torch.cuda.synchronize(device)
+        t0 = time.perf_counter()
+        r = pk.spmv_batch(ctx, ms, vs)
+        e2e.append((time.perf_counter() - t0) * 1e3)
+        if i == 0:
+            verified = verified and all(np.array_equal(x["values"], exact_values(m, v)) for m, v, x in zip(ms, vs, r))
+    e2e = e2e[1:]
+    out["e2e"] = {"value": round(statistics.mean(e2e), 4), "unit": "ms", "h2d_bytes_per_step": int(h2d),
+                  "d2h_bytes_per_step": int(d2h)}
+    out["verified"] = verified
+    # roofline of the dominant kernel: the batched NTT (largest launch of the plan)
+    L, nB = ctx.params.L, ctx.params.L + 1
+    limbs = max(1, st["chunks"]) * 4 * (L + nB)
+    us = ctx.probe_ntt_us(limbs, inverse=False, reps=20)
+    n = ctx.n
+    logn = cfg["logn"]
+    bfly = limbs * (n // 2) * logn
+    peak = ctx.probe_butterfly_peak()
+    hbm_bytes = limbs * 2 * n * 8
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    out["roofline"] = {
+        "bound": "int", "kernel": "k_ntt (batched negacyclic NTT, one CTA per limb)",
+        "achieved": round(bfly / (us * 1e-6) / 1e9, 2), "peak": round(peak / 1e9, 2),
+        "unit": "Gbutterfly/s", "frac": round(bfly / (us * 1e-6) / peak, 4),
+        "traffic": None, "launch_us": round(us, 3), "limbs_per_launch": limbs,
+        "hbm_achieved_gbs": round(hbm_bytes / (us * 1e-6) / 1e9, 1), "hbm_peak_gbs": hbm_peak,
+        "hbm_frac": round(hbm_bytes / (us * 1e-6) / 1e9 / hbm_peak, 4),
+        "peak_source": "register-resident lazy-Shoup radix-16 butterfly probe (this run); HBM: MEASURED_PEAKS.json",
+    }
+    out["whole_plan_hbm_gbs"] = round(st["hbm_bytes_algorithmic"] / (ms_step * 1e-3) / 1e9, 1)
+    job.close()
+    ctx.close()
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--all-configs", dest="all_configs", action="store_true", default=True)
+    ap.add_argument("--only", dest="all_configs", action="store_false")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        if rank == 0:
+            cfg = make_config(args.config)
+            print(json.dumps(run_reference_arm(args, cfg)), flush=True)
+        return
+
+    import torch
+    import paper_2603_04742_b200 as pk
+
+    if world > 1:
+        torch.cuda.set_device(local)
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = make_config(args.config)
+    head = measure_config(pk, cfg, args, rank, world, local, full=True)
+    others = {}
+    if args.all_configs:
+        for c in (1, 2, 3, 4, 5):
+            if c == args.config:
+                continue
+            try:
+                o = measure_config(pk, make_config(c), args, rank, world, local, full=False)
+                others[f"C{c}"] = {"ms": round(o["ms_per_step"], 4), "verified": o["verified"],
+                                   "chunks": o["plan"]["chunks"], "rotations": o["plan"]["rotations"],
+                                   "limb_ntts": o["plan"]["limb_ntts_per_run"],
+                                   "whole_plan_hbm_gbs": round(o["plan"]["hbm_bytes_algorithmic"] /
+                                                               (o["ms_per_step"] * 1e-3) / 1e9, 1)}
+            except Exception as e:  # a failing side config must not hide the headline
+                others[f"C{c}"] = {"error": str(e)[:200]}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        r = cpu_reference_time(cfg["ms"], cfg["vs"], 1 << (cfg["logn"] - 1))
+        if r is not None:
+            best, reps = r
+            cpu = {"value": round(best, 4), "unit": "ms", "cores": 1, "kind": "reference",
+                   "sample": f"{cfg['name']}: whole workload, reference SimBackend spmv_partitioned "
+                             f"(plaintext slot simulator), best of {reps} runs, slot_count={1 << (cfg['logn'] - 1)}"}
+    if world > 1:
+        torch.distributed.barrier()
+    if rank == 0:
+        ms_step = head["ms_per_step"]
+        line = {
+            "metric": METRIC, "value": round(ms_step / world, 4), "unit": "ms", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+            "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic (seeded generators with BASELINE.json shapes; values in [-8,8]\\{0})",
+            "config": {"workload": head["name"], "ring_degree": 1 << cfg["logn"],
+                       "rns": f"L={ctx_desc(cfg['logn'])}", "chunks": head["plan"]["chunks"],
+                       "rotations": head["plan"]["rotations"], "levels": head["plan"]["levels"],
+                       "l2": "flushed (256 MiB write) before every timed step",
+                       "parallelism": f"replica per GPU x{world}"},
+            "clocks": head["clocks"], "e2e": head["e2e"], "gpu_launches": head["plan"]["kernels_per_run"],
+            "roofline": head["roofline"], "cpu_baseline": cpu, "verified_exact": head["verified"],
+            "measured_noise_bits_min": head["measured_noise_bits"],
+            "whole_plan_hbm_gbs": head["whole_plan_hbm_gbs"],
+            "limb_ntts_per_step": head["plan"]["limb_ntts_per_run"], "other_configs": others,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def ctx_desc(logn):
+    import paper_2603_04742_b200 as pk
+
+    p = pk.default_params(logn)
+    return f"{p.L}x{p.qbits}b,K={p.K}x{p.pbits}b,alpha={p.alpha}"
+
+
+if __name__ == "__main__":
+    main()

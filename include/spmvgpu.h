@@ -110,6 +110,13 @@ int spmvgpu_mul_plain(spmvgpu_ctx* c, const spmvgpu_ct* a, const int64_t* vals,
 /* KAT: in-place forward/inverse NTT of `limbs` host limbs modulo prime index */
 int spmvgpu_ntt(spmvgpu_ctx* c, int prime_index, uint64_t* data, size_t limbs, int inverse);
 
+/* roofline probes, timed with CUDA events on the context stream:
+ * average device time (us) of one batched NTT launch over `limbs` device limbs
+ * (the kernel the cloud plan launches), and the register-resident peak of the
+ * identical lazy Shoup butterfly sequence (butterflies per second). */
+int spmvgpu_probe_ntt(spmvgpu_ctx* c, size_t limbs, int inverse, int reps, double* us_per_launch);
+int spmvgpu_probe_butterfly_peak(spmvgpu_ctx* c, double* butterflies_per_s);
+
 /* ---- the batched cloud phase: every chunk of every slice in shared launches ----
  * chunk i: product of a_cts[i] and b_cts[i], folded by rotation_schedule(r_i, c_i),
  * masked to its first r_i slots and accumulated into out_cts[slice_i]. */

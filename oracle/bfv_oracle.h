@@ -48,6 +48,8 @@ uint64_t bfvo_psi(const bfvo_ctx* c, int prime_index); /* index L+K+L+1 = t */
  * (output position p holds a(psi^(2*bitrev(p)+1))). */
 void bfvo_ntt(const bfvo_ctx* c, int prime_index, uint64_t* a);
 void bfvo_intt(const bfvo_ctx* c, int prime_index, uint64_t* a);
+void bfvo_chacha_block_raw(const uint32_t key[8], uint32_t counter, const uint32_t nonce[3],
+                           uint32_t out[16]);
 uint64_t bfvo_chacha_word(uint64_t seed, uint32_t n0, uint32_t n1, uint32_t n2,
                           uint64_t index);
 

@@ -92,6 +92,8 @@ _SIGS = {
     "spmvgpu_rotate_add": (C.c_int, [C.c_void_p, u64p, u64p, i64p, u64p, C.c_size_t]),
     "spmvgpu_mul_plain": (C.c_int, [C.c_void_p, u64p, i64p, u64p, u64p, C.c_size_t]),
     "spmvgpu_ntt": (C.c_int, [C.c_void_p, C.c_int, u64p, C.c_size_t, C.c_int]),
+    "spmvgpu_probe_ntt": (C.c_int, [C.c_void_p, C.c_size_t, C.c_int, C.c_int, C.POINTER(C.c_double)]),
+    "spmvgpu_probe_butterfly_peak": (C.c_int, [C.c_void_p, C.POINTER(C.c_double)]),
     "spmvgpu_plan_create": (C.c_int, [C.c_void_p, C.c_size_t, u64p, u64p, u32p, C.c_size_t,
                                       u64p, u64p, u64p, C.POINTER(C.c_void_p)]),
     "spmvgpu_plan_run": (C.c_int, [C.c_void_p]),
@@ -315,6 +317,19 @@ class Context:
 
     def sync(self):
         check(lib().spmvgpu_sync(self.h))
+
+    def stream_ptr(self) -> int:
+        return int(lib().spmvgpu_stream(self.h) or 0)
+
+    def probe_ntt_us(self, limbs: int, inverse: bool = False, reps: int = 20) -> float:
+        us = C.c_double()
+        check(lib().spmvgpu_probe_ntt(self.h, limbs, int(inverse), reps, C.byref(us)))
+        return us.value
+
+    def probe_butterfly_peak(self) -> float:
+        bps = C.c_double()
+        check(lib().spmvgpu_probe_butterfly_peak(self.h, C.byref(bps)))
+        return bps.value
 
 
 @dataclass

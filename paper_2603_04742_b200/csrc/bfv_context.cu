@@ -78,7 +78,6 @@ void DevBuf::ensure(DevicePool* pool, size_t bytes) {
 
 // ------------------------------------------------------------------ context
 GpuContext::GpuContext(const RnsConfig& cfg, int device) : P_(cfg), device_(device) {
-    if (cfg.logn > 14) throw std::invalid_argument("ring degree above 2^14 needs the clustered NTT (logn 15) which is not built yet");
     cuda_check(cudaSetDevice(device), "cudaSetDevice");
     cuda_check(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking), "stream");
     DevConsts host = P_.host;
@@ -127,10 +126,13 @@ T* GpuContext::upload_ptrs(const std::vector<T>& v, int slot) {
 
 NttJob GpuContext::job(const u64* src, u64* dst, int limbs, const std::vector<int>& pidx) const {
     NttJob j;
+    std::memset(j.pidx, 0, sizeof j.pidx);
     j.src = src;
     j.dst = dst;
     j.limbs = limbs;
-    if (limbs > 64) throw std::invalid_argument("too many limbs in one NTT job");
+    if (limbs > MAX_JOB_LIMBS || limbs < 1) throw std::invalid_argument("NTT job limb count out of range");
+    for (int p : pidx)
+        if (p < 0 || p >= P_.np) throw std::invalid_argument("NTT job prime index out of range");
     for (int i = 0; i < limbs; ++i) j.pidx[i] = (signed char)pidx[i % pidx.size()];
     return j;
 }

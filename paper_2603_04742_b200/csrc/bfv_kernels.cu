@@ -2,10 +2,11 @@
 //
 // Every kernel covers all RNS limbs of all items of a batch in one launch:
 // elementwise kernels put one thread on one coefficient index k of one item
-// (coalesced over k for every limb), NTT kernels put one CTA on one limb.
+// (coalesced over k for every limb); NTTs run as two-phase tiled kernels.
 // Formulas E1..E5 refer to DESIGN.md "Arithmetic spec"; the CPU oracle
 // (oracle/bfv_oracle.c) states the same integer formulas.
 #include <cstdio>
+#include <type_traits>
 #include <stdexcept>
 #include <string>
 
@@ -74,30 +75,125 @@ __device__ __forceinline__ u64 lift_signed(int64_t v, u64 q) {
 }
 
 // ---------------------------------------------------------------------------
-// NTT
+// NTT: two-phase kernels (see ntt.cuh)
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ const u64* job_src(const NttJob& job, int item, int j, int n) {
+    return job.src_items ? job.src_items[item] + (size_t)(job.src_limb_offset + j) * n
+                         : job.src + ((size_t)item * job.limbs + j) * n;
+}
+__device__ __forceinline__ u64* job_dst(const NttJob& job, int item, int j, int n) {
+    return job.dst_items ? job.dst_items[item] + (size_t)j * n : job.dst + ((size_t)item * job.limbs + j) * n;
+}
+
+// Column phase: 16 strided columns of R1 elements.  Forward: first phase
+// (src -> dst).  Inverse: last phase (dst -> dst), applies N^-1, canonical.
 template <int LOGN, bool INV>
-__global__ void __launch_bounds__(NttGeom<LOGN>::THREADS)
-    k_ntt(const DevConsts* __restrict__ dc, NttJob job) {
+__global__ void __launch_bounds__(128) k_ntt_cols(const DevConsts* __restrict__ dc, NttJob job) {
+    using G = Ntt2<LOGN>;
     extern __shared__ u64 smem[];
-    constexpr int N = 1 << LOGN;
-    const int item = blockIdx.x / job.limbs;
-    const int j = blockIdx.x - item * job.limbs;
+    u64* tile = smem;                       // [R1][16]
+    u64* tws = smem + G::LINES * G::R1;     // [R1] pairs
+    const int tileid = blockIdx.x % G::CTAS_C;
+    const int lj = blockIdx.x / G::CTAS_C;
+    const int item = lj / job.limbs, j = lj - item * job.limbs;
     const int prime = job.pidx[j];
-    const u64* src = job.src_items
-                         ? job.src_items[item] + (size_t)(job.src_limb_offset + j) * N
-                         : job.src + ((size_t)item * job.limbs + j) * N;
-    u64* dst = job.dst_items ? job.dst_items[item] + (size_t)j * N
-                             : job.dst + ((size_t)item * job.limbs + j) * N;
-    load_limb<LOGN>(smem, src);
-    __syncthreads();
     const u64 q = dc->mod[prime].q;
-    if (!INV) {
-        ntt_fwd_smem<LOGN>(smem, dc, prime);
-        store_limb_fwd<LOGN>(dst, smem, q);
-    } else {
-        ntt_inv_smem<LOGN>(smem, dc, prime);
-        store_limb_inv<LOGN>(dst, smem, q, dc->ninv[prime], dc->ninv_sh[prime]);
+    const u64* tw = INV ? dc->tw[prime].inv : dc->tw[prime].fwd;
+    const u64* src = INV ? job_dst(job, item, j, G::N) : job_src(job, item, j, G::N);
+    u64* dst = job_dst(job, item, j, G::N);
+    const int col0 = tileid * G::LINES;
+    // twiddles W[0 .. R1) into smem
+    for (int i = threadIdx.x; i < G::R1; i += 128) {
+        const ulonglong2 w = __ldg(reinterpret_cast<const ulonglong2*>(tw) + i);
+        tws[2 * i] = w.x;
+        tws[2 * i + 1] = w.y;
+    }
+    // rows of 16 consecutive words: 8 threads x 16 B per row; every load of the
+    // tile is issued before the first smem store (R1/16 loads in flight)
+    {
+        constexpr int PER = G::R1 / 16;
+        ulonglong2 v[PER];
+#pragma unroll
+        for (int r = 0; r < PER; ++r) {
+            const int i = threadIdx.x + 128 * r, c = i >> 3, h = i & 7;
+            v[r] = __ldg(reinterpret_cast<const ulonglong2*>(src + (size_t)c * G::R2 + col0 + 2 * h));
+        }
+#pragma unroll
+        for (int r = 0; r < PER; ++r) {
+            const int i = threadIdx.x + 128 * r, c = i >> 3, h = i & 7;
+            tile[c * 16 + 2 * h] = v[r].x;
+            tile[c * 16 + 2 * h + 1] = v[r].y;
+        }
+    }
+    __syncthreads();
+    auto addr = [](int l, int pos) { return pos * 16 + l; };
+    auto twf = [&](int sl, int, int blk) {
+        const int k = (1 << sl) + blk;
+        return make_ulonglong2(tws[2 * k], tws[2 * k + 1]);
+    };
+    line_ntt<G::A, 0, INV>(tile, q, addr, twf);
+    const u64 ni = dc->ninv[prime], nish = dc->ninv_sh[prime];
+#pragma unroll
+    for (int r = 0; r < G::R1 / 16; ++r) {
+        const int i = threadIdx.x + 128 * r, c = i >> 3, h = i & 7;
+        u64 a0 = tile[c * 16 + 2 * h], a1 = tile[c * 16 + 2 * h + 1];
+        if (INV) {
+            a0 = shoup(a0, ni, nish, q);
+            a1 = shoup(a1, ni, nish, q);
+        }
+        *reinterpret_cast<ulonglong2*>(dst + (size_t)c * G::R2 + col0 + 2 * h) = make_ulonglong2(a0, a1);
+    }
+}
+
+// Block phase: 16 contiguous blocks of R2 elements.  Forward: last phase
+// (dst -> dst, canonical output).  Inverse: first phase (src -> dst).
+template <int LOGN, bool INV>
+__global__ void __launch_bounds__(128) k_ntt_blocks(const DevConsts* __restrict__ dc, NttJob job) {
+    using G = Ntt2<LOGN>;
+    extern __shared__ u64 smem[];
+    constexpr int PITCH = G::R2 + 1;
+    const int tileid = blockIdx.x % G::CTAS_B;
+    const int lj = blockIdx.x / G::CTAS_B;
+    const int item = lj / job.limbs, j = lj - item * job.limbs;
+    const int prime = job.pidx[j];
+    const u64 q = dc->mod[prime].q;
+    const u64* tw = INV ? dc->tw[prime].inv : dc->tw[prime].fwd;
+    const u64* src = INV ? job_src(job, item, j, G::N) : job_dst(job, item, j, G::N);
+    u64* dst = job_dst(job, item, j, G::N);
+    const int blk0 = tileid * G::LINES;
+    const size_t base = (size_t)blk0 * G::R2;
+    {
+        constexpr int PER = G::LINES * G::R2 / 256;
+        ulonglong2 v[PER];
+#pragma unroll
+        for (int r = 0; r < PER; ++r)
+            v[r] = __ldg(reinterpret_cast<const ulonglong2*>(src + base) + threadIdx.x + 128 * r);
+#pragma unroll
+        for (int r = 0; r < PER; ++r) {
+            const int x = 2 * (threadIdx.x + 128 * r), b = x >> G::B, c = x & (G::R2 - 1);
+            smem[b * PITCH + c] = v[r].x;
+            smem[b * PITCH + c + 1] = v[r].y;
+        }
+    }
+    __syncthreads();
+    auto addr = [](int l, int pos) { return l * PITCH + pos; };
+    auto twf = [&](int sl, int l, int blk) {
+        const int k = (1 << (G::A + sl)) + ((blk0 + l) << sl) + blk;
+        return __ldg(reinterpret_cast<const ulonglong2*>(tw) + k);
+    };
+    line_ntt<G::B, 0, INV>(smem, q, addr, twf);
+    const u64 two_q = 2 * q;
+#pragma unroll
+    for (int r = 0; r < G::LINES * G::R2 / 256; ++r) {
+        const int x = 2 * (threadIdx.x + 128 * r), b = x >> G::B, c = x & (G::R2 - 1);
+        u64 a0 = smem[b * PITCH + c], a1 = smem[b * PITCH + c + 1];
+        if (!INV) {
+            a0 = a0 >= two_q ? a0 - two_q : a0;
+            a0 = a0 >= q ? a0 - q : a0;
+            a1 = a1 >= two_q ? a1 - two_q : a1;
+            a1 = a1 >= q ? a1 - q : a1;
+        }
+        *reinterpret_cast<ulonglong2*>(dst + base + x) = make_ulonglong2(a0, a1);
     }
 }
 
@@ -106,19 +202,26 @@ size_t ntt_smem_bytes(int logn) { return (size_t)8 << logn; }
 template <int LOGN>
 static void launch_ntt_t(const DevConsts* dc, bool inv, const NttJob& job, int items,
                          cudaStream_t st) {
+    using G = Ntt2<LOGN>;
     static bool configured = false;
-    constexpr int SMEM = NttGeom<LOGN>::SMEM;
     if (!configured) {
-        cudaFuncSetAttribute(k_ntt<LOGN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-        cudaFuncSetAttribute(k_ntt<LOGN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+        cudaFuncSetAttribute(k_ntt_cols<LOGN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM_C);
+        cudaFuncSetAttribute(k_ntt_cols<LOGN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM_C);
+        cudaFuncSetAttribute(k_ntt_blocks<LOGN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM_B);
+        cudaFuncSetAttribute(k_ntt_blocks<LOGN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM_B);
         configured = true;
     }
-    const int grid = items * job.limbs;
-    if (grid == 0) return;
-    if (inv)
-        k_ntt<LOGN, true><<<grid, NttGeom<LOGN>::THREADS, SMEM, st>>>(dc, job);
-    else
-        k_ntt<LOGN, false><<<grid, NttGeom<LOGN>::THREADS, SMEM, st>>>(dc, job);
+    const int limbs = items * job.limbs;
+    if (limbs == 0) return;
+    if (!inv) {
+        k_ntt_cols<LOGN, false><<<limbs * G::CTAS_C, 128, G::SMEM_C, st>>>(dc, job);
+        CSSC_CHECK_LAUNCH();
+        k_ntt_blocks<LOGN, false><<<limbs * G::CTAS_B, 128, G::SMEM_B, st>>>(dc, job);
+    } else {
+        k_ntt_blocks<LOGN, true><<<limbs * G::CTAS_B, 128, G::SMEM_B, st>>>(dc, job);
+        CSSC_CHECK_LAUNCH();
+        k_ntt_cols<LOGN, true><<<limbs * G::CTAS_C, 128, G::SMEM_C, st>>>(dc, job);
+    }
     CSSC_CHECK_LAUNCH();
 }
 
@@ -130,48 +233,76 @@ void launch_ntt(const DevConsts* dc, int logn, bool inverse, const NttJob& job, 
         case 12: launch_ntt_t<12>(dc, inverse, job, items, st); break;
         case 13: launch_ntt_t<13>(dc, inverse, job, items, st); break;
         case 14: launch_ntt_t<14>(dc, inverse, job, items, st); break;
+        case 15: launch_ntt_t<15>(dc, inverse, job, items, st); break;
         default: throw std::invalid_argument("NTT: unsupported logn " + std::to_string(logn));
     }
 }
 
 static dim3 ew_grid(int n, int items) { return dim3((unsigned)(n / EW_THREADS), (unsigned)items); }
 
+// Compile-time RNS shapes (L data primes, K special primes, alpha primes per
+// digit) of the supported parameter sets; 0 = read from DevConsts at run time.
+// With a fixed shape every per-coefficient residue array lives in registers.
+template <class F>
+static void dispatch_shape(const RnsParams& P, F&& f) {
+    const auto& c = P.cfg;
+    using std::integral_constant;
+    if (c.L == 3 && c.K == 1 && c.alpha == 1)
+        f(integral_constant<int, 3>{}, integral_constant<int, 1>{}, integral_constant<int, 1>{});
+    else if (c.L == 4 && c.K == 2 && c.alpha == 2)
+        f(integral_constant<int, 4>{}, integral_constant<int, 2>{}, integral_constant<int, 2>{});
+    else if (c.L == 8 && c.K == 4 && c.alpha == 4)
+        f(integral_constant<int, 8>{}, integral_constant<int, 4>{}, integral_constant<int, 4>{});
+    else
+        f(integral_constant<int, 0>{}, integral_constant<int, 0>{}, integral_constant<int, 0>{});
+}
+#define SHAPE_ARGS decltype(l_)::value, decltype(k_)::value, decltype(a_)::value
+
 // ---------------------------------------------------------------------------
 // E1: exact centred basis extension of one coefficient (X residues -> Y)
 // ---------------------------------------------------------------------------
+template <int NXT, int NYT>
 __device__ __forceinline__ void extend_exact(const DevConsts* __restrict__ dc,
                                              const ExtConsts& e, const u64* x, u64* out) {
+    const int nx = NXT ? NXT : e.nx, ny = NYT ? NYT : e.ny;
     u64 y[MAXB];
     u64 shi = 0, slo = 0;
-    for (int i = 0; i < e.nx; ++i) {
+#pragma unroll
+    for (int i = 0; i < nx; ++i) {
         const u64 qi = dc->mod[e.xi[i]].q;
         y[i] = shoup(x[i], e.xhat_inv[i], e.xhat_inv_sh[i], qi);
         add128(shi, slo, 0, frac64(y[i], e.R1[i], e.R0[i]));
     }
     const u64 v = shi + (slo >> 63);
-    for (int j = 0; j < e.ny; ++j) {
+#pragma unroll
+    for (int j = 0; j < ny; ++j) {
         const u64 p = dc->mod[e.yi[j]].q;
         u64 acc = 0;
-        for (int i = 0; i < e.nx; ++i) acc = add_mod(acc, shoup(y[i], e.xhat_y[i][j], e.xhat_y_sh[i][j], p), p);
+#pragma unroll
+        for (int i = 0; i < nx; ++i) acc = add_mod(acc, shoup(y[i], e.xhat_y[i][j], e.xhat_y_sh[i][j], p), p);
         out[j] = sub_mod(acc, shoup(v, e.X_y[j], e.X_y_sh[j], p), p);
     }
 }
 
 // T[item][poly 0..3][M][N]: Q limbs copied, B limbs by E1.  polys: a0 a1 b0 b1
+template <int LT, int KT, int AT>
 __global__ void k_mul_extend(const DevConsts* __restrict__ dc, const u64* const* A,
                              const u64* const* B, u64* T) {
-    const int n = dc->n, L = dc->L, nB = dc->nB, M = L + nB;
+    const int n = dc->n, L = LT ? LT : dc->L, nB = L + 1, M = L + nB;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     const int item = blockIdx.y;
     u64 x[MAXB], o[MAXB];
+#pragma unroll 1
     for (int p = 0; p < 4; ++p) {
         const u64* src = (p < 2 ? A[item] : B[item]) + (size_t)(p & 1) * L * n;
         u64* dst = T + ((size_t)item * 4 + p) * M * n;
+#pragma unroll
         for (int i = 0; i < L; ++i) {
             x[i] = src[(size_t)i * n + k];
             dst[(size_t)i * n + k] = x[i];
         }
-        extend_exact(dc, dc->extQB, x, o);
+        extend_exact<LT, LT ? LT + 1 : 0>(dc, dc->extQB, x, o);
+#pragma unroll
         for (int j = 0; j < nB; ++j) dst[(size_t)(L + j) * n + k] = o[j];
     }
 }
@@ -179,20 +310,24 @@ __global__ void k_mul_extend(const DevConsts* __restrict__ dc, const u64* const*
 void launch_mul_extend(const DevConsts* dc, const RnsParams& P, const u64* const* A,
                        const u64* const* B, u64* T, int items, cudaStream_t st) {
     if (!items) return;
-    k_mul_extend<<<ew_grid(P.n, items), EW_THREADS, 0, st>>>(dc, A, B, T);
+    dispatch_shape(P, [&](auto l_, auto k_, auto a_) {
+        k_mul_extend<SHAPE_ARGS><<<ew_grid(P.n, items), EW_THREADS, 0, st>>>(dc, A, B, T);
+    });
     CSSC_CHECK_LAUNCH();
 }
 
+template <int LT, int KT, int AT>
 __global__ void k_mul_tensor(const DevConsts* __restrict__ dc, const u64* __restrict__ T,
                              u64* __restrict__ Z) {
-    const int n = dc->n, L = dc->L, nB = dc->nB, M = L + nB;
+    const int n = dc->n, L = LT ? LT : dc->L, K = KT ? KT : dc->K, M = 2 * L + 1;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     const int item = blockIdx.y;
     const size_t P = (size_t)M * n;
     const u64* t = T + (size_t)item * 4 * P;
     u64* z = Z + (size_t)item * 3 * P;
+#pragma unroll
     for (int j = 0; j < M; ++j) {
-        const int pi = j < L ? j : dc->K + j;  // B limbs follow P in the prime table
+        const int pi = j < L ? j : K + j;  // B limbs follow P in the prime table
         const Modulus md = dc->mod[pi];
         const size_t o = (size_t)j * n + k;
         const u64 a0 = t[o], a1 = t[P + o], b0 = t[2 * P + o], b1 = t[3 * P + o];
@@ -205,21 +340,26 @@ __global__ void k_mul_tensor(const DevConsts* __restrict__ dc, const u64* __rest
 void launch_mul_tensor(const DevConsts* dc, const RnsParams& P, const u64* T, u64* Z, int items,
                        cudaStream_t st) {
     if (!items) return;
-    k_mul_tensor<<<ew_grid(P.n, items), EW_THREADS, 0, st>>>(dc, T, Z);
+    dispatch_shape(P, [&](auto l_, auto k_, auto a_) {
+        k_mul_tensor<SHAPE_ARGS><<<ew_grid(P.n, items), EW_THREADS, 0, st>>>(dc, T, Z);
+    });
     CSSC_CHECK_LAUNCH();
 }
 
 // E2: w = round(t z / Q) in B, then E1 B -> Q.  r = 0,1 -> OUT ct, r = 2 -> D2
+template <int LT, int KT, int AT>
 __global__ void k_mul_scale(const DevConsts* __restrict__ dc, const u64* __restrict__ Z,
                             u64* const* OUT, u64* __restrict__ D2) {
-    const int n = dc->n, L = dc->L, nB = dc->nB, K = dc->K, M = L + nB;
+    const int n = dc->n, L = LT ? LT : dc->L, nB = L + 1, K = KT ? KT : dc->K, M = L + nB;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     const int item = blockIdx.y;
     const size_t P = (size_t)M * n;
     u64 xi[MAXL], w[MAXB], o[MAXB];
+#pragma unroll 1
     for (int r = 0; r < 3; ++r) {
         const u64* z = Z + ((size_t)item * 3 + r) * P;
         u64 shi = 0, slo = 0;
+#pragma unroll
         for (int i = 0; i < L; ++i) {
             const u64 qi = dc->mod[i].q;
             xi[i] = shoup(z[(size_t)i * n + k], dc->QhatInv[i], dc->QhatInv_sh[i], qi);
@@ -227,17 +367,20 @@ __global__ void k_mul_scale(const DevConsts* __restrict__ dc, const u64* __restr
             add128(shi, slo, 0, umulhi(xi[i], dc->T0[i]));
         }
         const u64 rr = shi + (slo >> 63);
+#pragma unroll
         for (int j = 0; j < nB; ++j) {
             const u64 bj = dc->mod[L + K + j].q;
             u64 acc = 0;
+#pragma unroll
             for (int i = 0; i < L; ++i)
                 acc = add_mod(acc, shoup(xi[i], dc->QhatB[i][j], dc->QhatB_sh[i][j], bj), bj);
             const u64 alpha = shoup(sub_mod(acc, z[(size_t)(L + j) * n + k], bj), dc->QinvB[j],
                                     dc->QinvB_sh[j], bj);
             w[j] = sub_mod(rr, shoup(alpha, dc->tB[j], dc->tB_sh[j], bj), bj);
         }
-        extend_exact(dc, dc->extBQ, w, o);
+        extend_exact<LT ? LT + 1 : 0, LT>(dc, dc->extBQ, w, o);
         u64* dst = r < 2 ? OUT[item] + (size_t)r * L * n : D2 + (size_t)item * L * n;
+#pragma unroll
         for (int i = 0; i < L; ++i) dst[(size_t)i * n + k] = o[i];
     }
 }
@@ -245,7 +388,9 @@ __global__ void k_mul_scale(const DevConsts* __restrict__ dc, const u64* __restr
 void launch_mul_scale(const DevConsts* dc, const RnsParams& P, const u64* Z, u64* const* OUT,
                       u64* D2, int items, cudaStream_t st) {
     if (!items) return;
-    k_mul_scale<<<ew_grid(P.n, items), EW_THREADS, 0, st>>>(dc, Z, OUT, D2);
+    dispatch_shape(P, [&](auto l_, auto k_, auto a_) {
+        k_mul_scale<SHAPE_ARGS><<<ew_grid(P.n, items), EW_THREADS, 0, st>>>(dc, Z, OUT, D2);
+    });
     CSSC_CHECK_LAUNCH();
 }
 
@@ -263,24 +408,29 @@ __device__ __forceinline__ int automorph_src(u32 ginv, int k, int n, bool& neg) 
 }
 
 // E3: DX[item][digit][LK][N] = ModUp of SRC (optionally permuted by X -> X^g)
+template <int LT, int KT, int AT>
 __global__ void k_ks_modup(const DevConsts* __restrict__ dc, const u64* const* SRC,
                            const u64* SRCC, int src_poly, const u32* ginv, u64* DX) {
-    const int n = dc->n, L = dc->L, LK = L + dc->K, alpha = dc->alpha;
+    const int n = dc->n, L = LT ? LT : dc->L, K = KT ? KT : dc->K, LK = L + K;
+    const int alpha = AT ? AT : dc->alpha, dnum = (L + alpha - 1) / alpha;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     const int item = blockIdx.y;
     const u64* src = SRC ? SRC[item] + (size_t)src_poly * L * n : SRCC + (size_t)item * L * n;
     bool neg;
     const int idx = automorph_src(ginv ? ginv[item] : 0u, k, n, neg);
     u64 x[MAXL], y[MAXL];
+#pragma unroll
     for (int i = 0; i < L; ++i) {
         const u64 v = src[(size_t)i * n + idx];
-        x[i] = neg ? neg_mod(v, dc->mod[i].q) : v;
+        const u64 q = dc->mod[i].q;
+        x[i] = neg ? neg_mod(v, q) : v;
+        y[i] = shoup(x[i], dc->dig_hat_inv[i], dc->dig_hat_inv_sh[i], q);
     }
-    for (int dg = 0; dg < dc->dnum; ++dg) {
+#pragma unroll
+    for (int dg = 0; dg < dnum; ++dg) {
         const int lo = dg * alpha, hi = min(lo + alpha, L);
-        for (int i = lo; i < hi; ++i)
-            y[i] = shoup(x[i], dc->dig_hat_inv[i], dc->dig_hat_inv_sh[i], dc->mod[i].q);
-        u64* out = DX + ((size_t)item * dc->dnum + dg) * LK * n;
+        u64* out = DX + ((size_t)item * dnum + dg) * LK * n;
+#pragma unroll
         for (int j = 0; j < LK; ++j) {
             u64 v;
             if (j >= lo && j < hi) {
@@ -288,6 +438,7 @@ __global__ void k_ks_modup(const DevConsts* __restrict__ dc, const u64* const* S
             } else {
                 const u64 m = dc->mod[j].q;
                 v = 0;
+#pragma unroll
                 for (int i = lo; i < hi; ++i)
                     v = add_mod(v, shoup(y[i], dc->dig_hat[i][j], dc->dig_hat_sh[i][j], m), m);
             }
@@ -299,28 +450,36 @@ __global__ void k_ks_modup(const DevConsts* __restrict__ dc, const u64* const* S
 void launch_ks_modup(const DevConsts* dc, const RnsParams& P, const u64* const* SRC, int src_poly,
                      const u32* ginv, u64* DX, int items, cudaStream_t st) {
     if (!items) return;
-    k_ks_modup<<<ew_grid(P.n, items), EW_THREADS, 0, st>>>(dc, SRC, nullptr, src_poly, ginv, DX);
+    dispatch_shape(P, [&](auto l_, auto k_, auto a_) {
+        k_ks_modup<SHAPE_ARGS><<<ew_grid(P.n, items), EW_THREADS, 0, st>>>(dc, SRC, nullptr, src_poly, ginv, DX);
+    });
     CSSC_CHECK_LAUNCH();
 }
 
 void launch_ks_modup_contig(const DevConsts* dc, const RnsParams& P, const u64* SRC, u64* DX,
                             int items, cudaStream_t st) {
     if (!items) return;
-    k_ks_modup<<<ew_grid(P.n, items), EW_THREADS, 0, st>>>(dc, nullptr, SRC, 0, nullptr, DX);
+    dispatch_shape(P, [&](auto l_, auto k_, auto a_) {
+        k_ks_modup<SHAPE_ARGS><<<ew_grid(P.n, items), EW_THREADS, 0, st>>>(dc, nullptr, SRC, 0, nullptr, DX);
+    });
     CSSC_CHECK_LAUNCH();
 }
 
 // ACC[item][2][LK][N] = sum_digit DX (.) KEY  (NTT domain)
+template <int LT, int KT, int AT>
 __global__ void k_ks_inner(const DevConsts* __restrict__ dc, const u64* __restrict__ DX,
                            const u64* const* KEY, u64* __restrict__ ACC) {
-    const int n = dc->n, LK = dc->L + dc->K, dnum = dc->dnum;
+    const int n = dc->n, L = LT ? LT : dc->L, K = KT ? KT : dc->K, LK = L + K;
+    const int alpha = AT ? AT : dc->alpha, dnum = (L + alpha - 1) / alpha;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     const int item = blockIdx.y;
     const u64* key = KEY[item];
     const size_t PL = (size_t)LK * n;
+#pragma unroll
     for (int j = 0; j < LK; ++j) {
         const Modulus md = dc->mod[j];
         u64 a0 = 0, a1 = 0;
+#pragma unroll
         for (int dg = 0; dg < dnum; ++dg) {
             const u64 d = DX[((size_t)item * dnum + dg) * PL + (size_t)j * n + k];
             const u64 k0 = __ldg(key + ((size_t)dg * 2 + 0) * PL + (size_t)j * n + k);
@@ -336,15 +495,18 @@ __global__ void k_ks_inner(const DevConsts* __restrict__ dc, const u64* __restri
 void launch_ks_inner(const DevConsts* dc, const RnsParams& P, const u64* DX,
                      const u64* const* KEY, u64* ACC, int items, cudaStream_t st) {
     if (!items) return;
-    k_ks_inner<<<ew_grid(P.n, items), EW_THREADS, 0, st>>>(dc, DX, KEY, ACC);
+    dispatch_shape(P, [&](auto l_, auto k_, auto a_) {
+        k_ks_inner<SHAPE_ARGS><<<ew_grid(P.n, items), EW_THREADS, 0, st>>>(dc, DX, KEY, ACC);
+    });
     CSSC_CHECK_LAUNCH();
 }
 
 // E4 + fused adds
+template <int LT, int KT, int AT>
 __global__ void k_ks_moddown(const DevConsts* __restrict__ dc, const u64* __restrict__ ACC,
                              const u64* const* BASE, const u64* const* RSRC, const u32* ginv,
                              u64* const* OUT) {
-    const int n = dc->n, L = dc->L, K = dc->K, LK = L + K;
+    const int n = dc->n, L = LT ? LT : dc->L, K = KT ? KT : dc->K, LK = L + K;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     const int item = blockIdx.y;
     const size_t PL = (size_t)LK * n;
@@ -352,8 +514,10 @@ __global__ void k_ks_moddown(const DevConsts* __restrict__ dc, const u64* __rest
     int ridx = k;
     if (RSRC) ridx = automorph_src(ginv ? ginv[item] : 0u, k, n, neg);
     u64 y[MAXL];
+#pragma unroll
     for (int p = 0; p < 2; ++p) {
         const u64* acc = ACC + ((size_t)item * 2 + p) * PL;
+#pragma unroll
         for (int kk = 0; kk < K; ++kk) {
             const u64 pk = dc->mod[L + kk].q;
             y[kk] = shoup(acc[(size_t)(L + kk) * n + k], dc->phat_inv[kk], dc->phat_inv_sh[kk], pk);
@@ -361,9 +525,11 @@ __global__ void k_ks_moddown(const DevConsts* __restrict__ dc, const u64* __rest
         u64* out = OUT[item] + (size_t)p * L * n;
         const u64* base = BASE ? BASE[item] + (size_t)p * L * n : nullptr;
         const u64* rs = (RSRC && p == 0) ? RSRC[item] : nullptr;
+#pragma unroll
         for (int j = 0; j < L; ++j) {
             const u64 q = dc->mod[j].q;
             u64 c = 0;
+#pragma unroll
             for (int kk = 0; kk < K; ++kk)
                 c = add_mod(c, shoup(y[kk], dc->phat_q[kk][j], dc->phat_q_sh[kk][j], q), q);
             u64 v = shoup(sub_mod(acc[(size_t)j * n + k], c, q), dc->Pinv_q[j], dc->Pinv_q_sh[j], q);
@@ -381,41 +547,51 @@ void launch_ks_moddown(const DevConsts* dc, const RnsParams& P, const u64* ACC,
                        const u64* const* BASE, const u64* const* RSRC, const u32* ginv,
                        u64* const* OUT, int items, cudaStream_t st) {
     if (!items) return;
-    k_ks_moddown<<<ew_grid(P.n, items), EW_THREADS, 0, st>>>(dc, ACC, BASE, RSRC, ginv, OUT);
+    dispatch_shape(P, [&](auto l_, auto k_, auto a_) {
+        k_ks_moddown<SHAPE_ARGS><<<ew_grid(P.n, items), EW_THREADS, 0, st>>>(dc, ACC, BASE, RSRC, ginv, OUT);
+    });
     CSSC_CHECK_LAUNCH();
 }
 
 // ---------------------------------------------------------------------------
 // masks and plaintext products
 // ---------------------------------------------------------------------------
+template <int LT, int KT, int AT>
 __global__ void k_mask_accum(const DevConsts* __restrict__ dc, const u64* __restrict__ MT,
                              const int* slice_off, const int* slice_items, const int* item_mask,
                              const u64* __restrict__ MASKS, u64* __restrict__ RES) {
-    const int n = dc->n, L = dc->L;
+    const int n = dc->n, L = LT ? LT : dc->L;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     const int s = blockIdx.y;
     const int b = slice_off[s], e = slice_off[s + 1];
     const size_t CT = (size_t)2 * L * n;
-    for (int p = 0; p < 2; ++p)
+    u64 acc[2 * MAXL];
+#pragma unroll
+    for (int x = 0; x < 2 * L; ++x) acc[x] = 0;
+    for (int x = b; x < e; ++x) {
+        const int it = slice_items[x];
+        const u64* mt = MT + (size_t)it * CT + k;
+        const u64* mk = MASKS + (size_t)item_mask[it] * L * n + k;
+#pragma unroll
         for (int j = 0; j < L; ++j) {
             const Modulus md = dc->mod[j];
-            u64 acc = 0;
-            for (int x = b; x < e; ++x) {
-                const int it = slice_items[x];
-                const u64 a = MT[(size_t)it * CT + ((size_t)p * L + j) * n + k];
-                const u64 m = MASKS[((size_t)item_mask[it] * L + j) * n + k];
-                acc = add_mod(acc, mul_mod(a, m, md), md.q);
-            }
-            RES[(size_t)s * CT + ((size_t)p * L + j) * n + k] = acc;
+            const u64 m = mk[(size_t)j * n];
+            acc[j] = add_mod(acc[j], mul_mod(mt[(size_t)j * n], m, md), md.q);
+            acc[L + j] = add_mod(acc[L + j], mul_mod(mt[(size_t)(L + j) * n], m, md), md.q);
         }
+    }
+#pragma unroll
+    for (int x = 0; x < 2 * L; ++x) RES[(size_t)s * CT + (size_t)x * n + k] = acc[x];
 }
 
 void launch_mask_accum(const DevConsts* dc, const RnsParams& P, const u64* MT,
                        const int* slice_off, const int* slice_items, const int* item_mask,
                        const u64* MASKS, u64* RES, int slices, cudaStream_t st) {
     if (!slices) return;
-    k_mask_accum<<<ew_grid(P.n, slices), EW_THREADS, 0, st>>>(dc, MT, slice_off, slice_items,
-                                                              item_mask, MASKS, RES);
+    dispatch_shape(P, [&](auto l_, auto k_, auto a_) {
+        k_mask_accum<SHAPE_ARGS><<<ew_grid(P.n, slices), EW_THREADS, 0, st>>>(dc, MT, slice_off, slice_items,
+                                                                              item_mask, MASKS, RES);
+    });
     CSSC_CHECK_LAUNCH();
 }
 
@@ -793,6 +969,73 @@ void launch_automorph_ct(const DevConsts* dc, const RnsParams& P, const u64* con
     if (!items) return;
     k_automorph_ct<<<ew_grid(P.n, items), EW_THREADS, 0, st>>>(dc, A, ginv, OUT);
     CSSC_CHECK_LAUNCH();
+}
+
+}  // namespace cssc
+
+namespace cssc {
+
+// ---------------------------------------------------------------------------
+// roofline probe: the radix-16 lazy-Shoup butterfly network of fwd_pass, fed
+// from registers only (no memory traffic), to measure the integer peak the
+// NTT can approach.  Each iteration = 4 stages x 8 butterflies.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_bfly_peak(u64 q, u64 w0, u64 w0sh, int iters, u64* sink) {
+    u64 v[16];
+    u64 w = w0, wsh = w0sh;
+#pragma unroll
+    for (int c = 0; c < 16; ++c) v[c] = (threadIdx.x * 16 + c + blockIdx.x) % q;
+    const u64 two_q = 2 * q;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int h = 1 << (3 - u);
+#pragma unroll
+            for (int c = 0; c < 16; ++c) {
+                if (c & h) continue;
+                u64 x = v[c];
+                x = x >= two_q ? x - two_q : x;
+                const u64 y = shoup_lazy(v[c + h], w, wsh, q);
+                v[c] = x + y;
+                v[c + h] = x - y + two_q;
+            }
+        }
+        w += 1;  // keep the twiddle live per iteration (as per-stage table loads would)
+    }
+    u64 s = 0;
+#pragma unroll
+    for (int c = 0; c < 16; ++c) s ^= v[c];
+    if (s == 0x1234567) sink[0] = s;
+}
+
+double probe_butterfly_peak(const DevConsts* dc_host_copy_q, u64 q, u64 w, u64 wsh, cudaStream_t st) {
+    (void)dc_host_copy_q;
+    auto ok = [](cudaError_t e, const char* what) {
+        if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+    };
+    u64* sink = nullptr;
+    ok(cudaMalloc(&sink, 8), "cudaMalloc");
+    int dev = 0, sms = 148;
+    ok(cudaGetDevice(&dev), "device");
+    ok(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "attr");
+    const int blocks = sms * 8, threads = 256, iters = 2048;
+    cudaEvent_t a = nullptr, b = nullptr;
+    ok(cudaEventCreate(&a), "event");
+    ok(cudaEventCreate(&b), "event");
+    k_bfly_peak<<<blocks, threads, 0, st>>>(q, w, wsh, 64, sink);  // warm
+    CSSC_CHECK_LAUNCH();
+    ok(cudaEventRecord(a, st), "record");
+    k_bfly_peak<<<blocks, threads, 0, st>>>(q, w, wsh, iters, sink);
+    ok(cudaEventRecord(b, st), "record");
+    ok(cudaEventSynchronize(b), "probe");
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(sink);
+    CSSC_CHECK_LAUNCH();
+    const double bfly = (double)blocks * threads * iters * 32.0;
+    return bfly / (ms * 1e-3);
 }
 
 }  // namespace cssc

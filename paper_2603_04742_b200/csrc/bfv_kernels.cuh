@@ -13,6 +13,8 @@
 
 namespace cssc {
 
+constexpr int MAX_JOB_LIMBS = 128;  // 4 * (2L + 1) = 68 at L = 8 (ring 2^15)
+
 struct NttJob {
     const u64* src = nullptr;               // contiguous [items][limbs][N] (if src_items null)
     const u64* const* src_items = nullptr;  // per-item base pointers, each [limbs][N]
@@ -20,7 +22,7 @@ struct NttJob {
     u64* dst = nullptr;                     // contiguous [items][limbs][N] (if dst_items null)
     u64* const* dst_items = nullptr;        // per-item base pointers, each [limbs][N]
     int limbs = 0;                          // limbs per item
-    signed char pidx[64];                   // global prime index of limb j
+    signed char pidx[MAX_JOB_LIMBS];        // global prime index of limb j
 };
 
 // sampler domains (nonce word 0 = dom | limb << 8 | digit << 16)
@@ -108,4 +110,9 @@ void launch_add(const DevConsts* dc, const RnsParams& P, const u64* const* A,
 void launch_automorph_ct(const DevConsts* dc, const RnsParams& P, const u64* const* A,
                          const u32* ginv, u64* const* OUT, int items, cudaStream_t st);
 
+}  // namespace cssc
+
+namespace cssc {
+// register-resident lazy-Shoup butterfly peak (butterflies / s)
+double probe_butterfly_peak(const DevConsts* unused, u64 q, u64 w, u64 wsh, cudaStream_t st);
 }  // namespace cssc

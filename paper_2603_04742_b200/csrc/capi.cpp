@@ -473,3 +473,44 @@ int64_t cssc_stencil27_csr(uint64_t side, uint64_t seed, int64_t lo, int64_t hi,
 }
 
 }  // extern "C"
+
+extern "C" {
+
+int spmvgpu_probe_ntt(spmvgpu_ctx* c, size_t limbs, int inverse, int reps, double* us_per_launch) {
+    return guard([&] {
+        auto& g = G(c);
+        const auto& P = g.params();
+        cssc::DevBuf buf(&g.pool(), sizeof(u64) * limbs * P.n);
+        cssc::cuda_check(cudaMemsetAsync(buf.words(), 0, buf.bytes(), g.stream()), "memset");
+        std::vector<int> pidx;
+        for (int j = 0; j < P.cfg.L; ++j) pidx.push_back(j);
+        // `limbs` CTAs as (limbs / L) items of L limbs, primes cycling over Q
+        const cssc::NttJob job = g.job(buf.words(), buf.words(), P.cfg.L, pidx);
+        const int items = (int)std::max<size_t>(1, limbs / P.cfg.L);
+        cssc::launch_ntt(g.dconsts(), P.cfg.logn, inverse != 0, job, items, g.stream());
+        g.synchronize();
+        cudaEvent_t a = nullptr, b = nullptr;
+        cssc::cuda_check(cudaEventCreate(&a), "event");
+        cssc::cuda_check(cudaEventCreate(&b), "event");
+        cssc::cuda_check(cudaEventRecord(a, g.stream()), "event record");
+        for (int r = 0; r < reps; ++r) cssc::launch_ntt(g.dconsts(), P.cfg.logn, inverse != 0, job, items, g.stream());
+        cssc::cuda_check(cudaEventRecord(b, g.stream()), "event record");
+        cssc::cuda_check(cudaEventSynchronize(b), "probe ntt");
+        float ms = 0;
+        cudaEventElapsedTime(&ms, a, b);
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        *us_per_launch = 1e3 * ms / reps;
+    });
+}
+
+int spmvgpu_probe_butterfly_peak(spmvgpu_ctx* c, double* bps) {
+    return guard([&] {
+        auto& g = G(c);
+        const auto& P = g.params();
+        const u64 q = P.primes[0], w = P.tw_fwd[0][2], wsh = P.tw_fwd[0][3];
+        *bps = cssc::probe_butterfly_peak(nullptr, q, w, wsh, g.stream());
+    });
+}
+
+}  // extern "C"
