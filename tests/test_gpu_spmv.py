@@ -111,3 +111,20 @@ def test_job_graph_replay(ctx10):
         assert np.array_equal(r["values"], checker(m, v, ctx10.slots, ctx10.slots)["values"])
     st = job.stats()
     assert st["chunks"] > 0 and st["limb_ntts_per_run"] > 0
+
+
+GOLDEN = __import__("json").loads(
+    (__import__("pathlib").Path(__file__).parent / "golden" / "ref_cases.json").read_text())["cases"]
+
+
+@pytest.mark.parametrize("case", GOLDEN, ids=[c["name"] for c in GOLDEN])
+def test_matches_reference_fixtures(ctx10, ctx13, case):
+    """Committed outputs of the compiled reference (tests/golden/make_golden.py);
+    values are independent of slot_count once chunk_size is fixed."""
+    ctx = ctx13 if case["chunk"] > ctx10.slots else ctx10
+    m = pk.Csr(case["rows"], case["cols"], np.array(case["row_ptrs"], np.int64),
+               np.array(case["col_indices"], np.int64), np.array(case["values_in"], np.int64))
+    got = pk.spmv_partitioned(ctx, m, np.array(case["v"], np.int64), case["chunk"])
+    assert [int(x) for x in got["values"]] == case["values"]
+    assert got["ledger"] == case["ledger"] and got["n_ct"] == case["n_ct"] and got["noise"] == case["noise"]
+    assert [list(x) for x in got["messages"]] == case["messages"]
