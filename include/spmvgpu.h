@@ -68,6 +68,9 @@ int spmvgpu_ctx_primes(const spmvgpu_ctx* c, uint64_t* primes, int cap, int* cou
 int spmvgpu_ctx_sizes(const spmvgpu_ctx* c, uint64_t* n, uint64_t* slots, uint64_t* ct_words,
                       uint64_t* ksk_words, int* dnum);
 int spmvgpu_sync(spmvgpu_ctx* c);
+/* tuning switches: "fused_key_switch" (1 = 3-kernel fused key switch, default;
+ * 0 = the 7-launch ModUp / NTT / inner product / INTT / ModDown pipeline) */
+int spmvgpu_set_option(spmvgpu_ctx* c, const char* name, int64_t value);
 /* opaque CUDA stream the context works on (cudaStream_t) */
 void* spmvgpu_stream(spmvgpu_ctx* c);
 

@@ -74,6 +74,7 @@ _SIGS = {
     "spmvgpu_ctx_primes": (C.c_int, [C.c_void_p, u64p, C.c_int, C.POINTER(C.c_int)]),
     "spmvgpu_ctx_sizes": (C.c_int, [C.c_void_p, u64p, u64p, u64p, u64p, C.POINTER(C.c_int)]),
     "spmvgpu_sync": (C.c_int, [C.c_void_p]),
+    "spmvgpu_set_option": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int64]),
     "spmvgpu_stream": (C.c_void_p, [C.c_void_p]),
     "spmvgpu_galois_keys": (C.c_int, [C.c_void_p, i64p, C.c_size_t]),
     "spmvgpu_galois_element": (C.c_uint32, [C.c_void_p, C.c_int64]),
@@ -317,6 +318,9 @@ class Context:
 
     def sync(self):
         check(lib().spmvgpu_sync(self.h))
+
+    def set_option(self, name: str, value: int) -> None:
+        check(lib().spmvgpu_set_option(self.h, name.encode(), int(value)))
 
     def stream_ptr(self) -> int:
         return int(lib().spmvgpu_stream(self.h) or 0)

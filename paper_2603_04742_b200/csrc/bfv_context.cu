@@ -321,13 +321,19 @@ void GpuContext::mul_relin_dev(const u64* const* A, const u64* const* B, u64* co
     launch_mul_tensor(dc_, P_, T, Z, items, st_);
     launch_ntt(dc_, logn, true, job(Z, Z, 3 * M, pm), items, st_);
     launch_mul_scale(dc_, P_, Z, OUT, D2, items, st_);
-    launch_ks_modup_contig(dc_, P_, D2, DX, items, st_);
-    launch_ntt(dc_, logn, false, job(DX, DX, P_.dnum * LK, range_idx(0, LK)), items, st_);
-    launch_ks_inner(dc_, P_, DX, RLK, ACC, items, st_);
-    launch_ntt(dc_, logn, true, job(ACC, ACC, 2 * LK, range_idx(0, LK)), items, st_);
-    launch_ks_moddown(dc_, P_, ACC, reinterpret_cast<const u64* const*>(OUT), nullptr, nullptr, OUT,
-                      items, st_);
-    stats_.kernels += 10;
+    if (fused_ks_) {
+        launch_ks_fused(dc_, P_, nullptr, D2, 0, nullptr, RLK, reinterpret_cast<const u64* const*>(OUT),
+                        nullptr, OUT, DX, ACC, items, st_);
+        stats_.kernels += 11;
+    } else {
+        launch_ks_modup_contig(dc_, P_, D2, DX, items, st_);
+        launch_ntt(dc_, logn, false, job(DX, DX, P_.dnum * LK, range_idx(0, LK)), items, st_);
+        launch_ks_inner(dc_, P_, DX, RLK, ACC, items, st_);
+        launch_ntt(dc_, logn, true, job(ACC, ACC, 2 * LK, range_idx(0, LK)), items, st_);
+        launch_ks_moddown(dc_, P_, ACC, reinterpret_cast<const u64* const*>(OUT), nullptr, nullptr, OUT,
+                          items, st_);
+        stats_.kernels += 10;
+    }
     stats_.limb_ntts += (u64)items * (7 * M + P_.dnum * LK + 2 * LK);
 }
 
@@ -348,12 +354,17 @@ void GpuContext::mul_relin(const std::vector<const u64*>& a, const std::vector<c
 void GpuContext::rotate_dev(const u64* const* SRC, const u32* ginv, const u64* const* KEY,
                             const u64* const* BASE, u64* const* OUT, int items, u64* DX, u64* ACC) {
     const int LK = P_.cfg.L + P_.cfg.K, logn = P_.cfg.logn;
-    launch_ks_modup(dc_, P_, SRC, 1, ginv, DX, items, st_);
-    launch_ntt(dc_, logn, false, job(DX, DX, P_.dnum * LK, range_idx(0, LK)), items, st_);
-    launch_ks_inner(dc_, P_, DX, KEY, ACC, items, st_);
-    launch_ntt(dc_, logn, true, job(ACC, ACC, 2 * LK, range_idx(0, LK)), items, st_);
-    launch_ks_moddown(dc_, P_, ACC, BASE, SRC, ginv, OUT, items, st_);
-    stats_.kernels += 5;
+    if (fused_ks_) {
+        launch_ks_fused(dc_, P_, SRC, nullptr, 1, ginv, KEY, BASE, SRC, OUT, DX, ACC, items, st_);
+        stats_.kernels += 4;
+    } else {
+        launch_ks_modup(dc_, P_, SRC, 1, ginv, DX, items, st_);
+        launch_ntt(dc_, logn, false, job(DX, DX, P_.dnum * LK, range_idx(0, LK)), items, st_);
+        launch_ks_inner(dc_, P_, DX, KEY, ACC, items, st_);
+        launch_ntt(dc_, logn, true, job(ACC, ACC, 2 * LK, range_idx(0, LK)), items, st_);
+        launch_ks_moddown(dc_, P_, ACC, BASE, SRC, ginv, OUT, items, st_);
+        stats_.kernels += 5;
+    }
     stats_.limb_ntts += (u64)items * (P_.dnum * LK + 2 * LK);
 }
 

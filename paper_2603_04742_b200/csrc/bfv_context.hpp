@@ -75,6 +75,9 @@ public:
     size_t ksk_words() const { return (size_t)P_.dnum * 2 * (P_.cfg.L + P_.cfg.K) * P_.n; }
     uint64_t next_stream_id() { return stream_counter_.fetch_add(1); }
     LaunchStats& stats() { return stats_; }
+    // fused 3-kernel key switch (default) or the 7-launch reference pipeline
+    void set_fused_key_switch(bool on) { fused_ks_ = on; }
+    bool fused_key_switch() const { return fused_ks_; }
 
     // keys (NTT form on device)
     const u64* relin_key() const { return rlk_.words(); }
@@ -145,6 +148,7 @@ private:
     std::map<u32, DevBuf> gk_;
     std::atomic<uint64_t> stream_counter_{1};
     LaunchStats stats_;
+    bool fused_ks_ = true;
     // workspaces for ad-hoc batched calls
     DevBuf wsT_, wsZ_, wsD2_, wsDX_, wsACC_, wsM_, wsX_, wsU_, wsC_, wsPT_;
     DevBuf scratch_[8];

@@ -102,29 +102,15 @@ __global__ void __launch_bounds__(128) k_ntt_cols(const DevConsts* __restrict__ 
     const u64* src = INV ? job_dst(job, item, j, G::N) : job_src(job, item, j, G::N);
     u64* dst = job_dst(job, item, j, G::N);
     const int col0 = tileid * G::LINES;
-    // twiddles W[0 .. R1) into smem
-    for (int i = threadIdx.x; i < G::R1; i += 128) {
-        const ulonglong2 w = __ldg(reinterpret_cast<const ulonglong2*>(tw) + i);
-        tws[2 * i] = w.x;
-        tws[2 * i + 1] = w.y;
-    }
-    // rows of 16 consecutive words: 8 threads x 16 B per row; every load of the
-    // tile is issued before the first smem store (R1/16 loads in flight)
-    {
-        constexpr int PER = G::R1 / 16;
-        ulonglong2 v[PER];
+    // twiddles W[0 .. R1) and the tile (rows of 16 consecutive words, 8 threads
+    // x 16 B per row) via async copies: every load of the CTA in flight at once
+    for (int i = threadIdx.x; i < G::R1; i += 128) cp_async16(tws + 2 * i, tw + 2 * i);
 #pragma unroll
-        for (int r = 0; r < PER; ++r) {
-            const int i = threadIdx.x + 128 * r, c = i >> 3, h = i & 7;
-            v[r] = __ldg(reinterpret_cast<const ulonglong2*>(src + (size_t)c * G::R2 + col0 + 2 * h));
-        }
-#pragma unroll
-        for (int r = 0; r < PER; ++r) {
-            const int i = threadIdx.x + 128 * r, c = i >> 3, h = i & 7;
-            tile[c * 16 + 2 * h] = v[r].x;
-            tile[c * 16 + 2 * h + 1] = v[r].y;
-        }
+    for (int r = 0; r < G::R1 / 16; ++r) {
+        const int i = threadIdx.x + 128 * r, c = i >> 3, h = i & 7;
+        cp_async16(tile + c * 16 + 2 * h, src + (size_t)c * G::R2 + col0 + 2 * h);
     }
+    cp_async_wait_all();
     __syncthreads();
     auto addr = [](int l, int pos) { return pos * 16 + l; };
     auto twf = [&](int sl, int, int blk) {
@@ -162,25 +148,17 @@ __global__ void __launch_bounds__(128) k_ntt_blocks(const DevConsts* __restrict_
     u64* dst = job_dst(job, item, j, G::N);
     const int blk0 = tileid * G::LINES;
     const size_t base = (size_t)blk0 * G::R2;
-    {
-        constexpr int PER = G::LINES * G::R2 / 256;
-        ulonglong2 v[PER];
+    u64* tws = smem + G::LINES * PITCH;
 #pragma unroll
-        for (int r = 0; r < PER; ++r)
-            v[r] = __ldg(reinterpret_cast<const ulonglong2*>(src + base) + threadIdx.x + 128 * r);
-#pragma unroll
-        for (int r = 0; r < PER; ++r) {
-            const int x = 2 * (threadIdx.x + 128 * r), b = x >> G::B, c = x & (G::R2 - 1);
-            smem[b * PITCH + c] = v[r].x;
-            smem[b * PITCH + c + 1] = v[r].y;
-        }
+    for (int r = 0; r < G::LINES * G::R2 / 128; ++r) {
+        const int x = threadIdx.x + 128 * r, b = x >> G::B, c = x & (G::R2 - 1);
+        cp_async8(smem + b * PITCH + c, src + base + x);
     }
+    load_block_twiddles<LOGN>(tws, tw, blk0);
+    cp_async_wait_all();
     __syncthreads();
     auto addr = [](int l, int pos) { return l * PITCH + pos; };
-    auto twf = [&](int sl, int l, int blk) {
-        const int k = (1 << (G::A + sl)) + ((blk0 + l) << sl) + blk;
-        return __ldg(reinterpret_cast<const ulonglong2*>(tw) + k);
-    };
+    auto twf = [&](int sl, int l, int blk) { return block_tw<LOGN>(tws, sl, l, blk); };
     line_ntt<G::B, 0, INV>(smem, q, addr, twf);
     const u64 two_q = 2 * q;
 #pragma unroll
@@ -223,6 +201,42 @@ static void launch_ntt_t(const DevConsts* dc, bool inv, const NttJob& job, int i
         k_ntt_cols<LOGN, true><<<limbs * G::CTAS_C, 128, G::SMEM_C, st>>>(dc, job);
     }
     CSSC_CHECK_LAUNCH();
+}
+
+template <int LOGN>
+static void launch_phase_t(const DevConsts* dc, bool inv, bool cols, const NttJob& job, int items,
+                           cudaStream_t st) {
+    using G = Ntt2<LOGN>;
+    const int limbs = items * job.limbs;
+    if (limbs == 0) return;
+    if (cols) {
+        if (inv)
+            k_ntt_cols<LOGN, true><<<limbs * G::CTAS_C, 128, G::SMEM_C, st>>>(dc, job);
+        else
+            k_ntt_cols<LOGN, false><<<limbs * G::CTAS_C, 128, G::SMEM_C, st>>>(dc, job);
+    } else {
+        if (inv)
+            k_ntt_blocks<LOGN, true><<<limbs * G::CTAS_B, 128, G::SMEM_B, st>>>(dc, job);
+        else
+            k_ntt_blocks<LOGN, false><<<limbs * G::CTAS_B, 128, G::SMEM_B, st>>>(dc, job);
+    }
+    CSSC_CHECK_LAUNCH();
+}
+
+// One phase only (used by fused pipelines).  Column phase of an inverse
+// transform reads and writes job.dst in place, like the second half of
+// launch_ntt.
+void launch_ntt_phase(const DevConsts* dc, int logn, bool inverse, bool cols, const NttJob& job,
+                      int items, cudaStream_t st) {
+    switch (logn) {
+        case 10: launch_ntt_t<10>(dc, inverse, job, 0, st); launch_phase_t<10>(dc, inverse, cols, job, items, st); break;
+        case 11: launch_ntt_t<11>(dc, inverse, job, 0, st); launch_phase_t<11>(dc, inverse, cols, job, items, st); break;
+        case 12: launch_ntt_t<12>(dc, inverse, job, 0, st); launch_phase_t<12>(dc, inverse, cols, job, items, st); break;
+        case 13: launch_ntt_t<13>(dc, inverse, job, 0, st); launch_phase_t<13>(dc, inverse, cols, job, items, st); break;
+        case 14: launch_ntt_t<14>(dc, inverse, job, 0, st); launch_phase_t<14>(dc, inverse, cols, job, items, st); break;
+        case 15: launch_ntt_t<15>(dc, inverse, job, 0, st); launch_phase_t<15>(dc, inverse, cols, job, items, st); break;
+        default: throw std::invalid_argument("NTT: unsupported logn " + std::to_string(logn));
+    }
 }
 
 void launch_ntt(const DevConsts* dc, int logn, bool inverse, const NttJob& job, int items,
@@ -292,8 +306,8 @@ __global__ void k_mul_extend(const DevConsts* __restrict__ dc, const u64* const*
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     const int item = blockIdx.y;
     u64 x[MAXB], o[MAXB];
-#pragma unroll 1
-    for (int p = 0; p < 4; ++p) {
+    {  // one polynomial per grid z-slice: keeps the E1 constants out of registers
+        const int p = blockIdx.z;
         const u64* src = (p < 2 ? A[item] : B[item]) + (size_t)(p & 1) * L * n;
         u64* dst = T + ((size_t)item * 4 + p) * M * n;
 #pragma unroll
@@ -311,7 +325,9 @@ void launch_mul_extend(const DevConsts* dc, const RnsParams& P, const u64* const
                        const u64* const* B, u64* T, int items, cudaStream_t st) {
     if (!items) return;
     dispatch_shape(P, [&](auto l_, auto k_, auto a_) {
-        k_mul_extend<SHAPE_ARGS><<<ew_grid(P.n, items), EW_THREADS, 0, st>>>(dc, A, B, T);
+        dim3 g = ew_grid(P.n, items);
+        g.z = 4;
+        k_mul_extend<SHAPE_ARGS><<<g, EW_THREADS, 0, st>>>(dc, A, B, T);
     });
     CSSC_CHECK_LAUNCH();
 }
@@ -355,8 +371,8 @@ __global__ void k_mul_scale(const DevConsts* __restrict__ dc, const u64* __restr
     const int item = blockIdx.y;
     const size_t P = (size_t)M * n;
     u64 xi[MAXL], w[MAXB], o[MAXB];
-#pragma unroll 1
-    for (int r = 0; r < 3; ++r) {
+    {  // one tensor component per grid z-slice
+        const int r = blockIdx.z;
         const u64* z = Z + ((size_t)item * 3 + r) * P;
         u64 shi = 0, slo = 0;
 #pragma unroll
@@ -389,7 +405,9 @@ void launch_mul_scale(const DevConsts* dc, const RnsParams& P, const u64* Z, u64
                       u64* D2, int items, cudaStream_t st) {
     if (!items) return;
     dispatch_shape(P, [&](auto l_, auto k_, auto a_) {
-        k_mul_scale<SHAPE_ARGS><<<ew_grid(P.n, items), EW_THREADS, 0, st>>>(dc, Z, OUT, D2);
+        dim3 g = ew_grid(P.n, items);
+        g.z = 3;
+        k_mul_scale<SHAPE_ARGS><<<g, EW_THREADS, 0, st>>>(dc, Z, OUT, D2);
     });
     CSSC_CHECK_LAUNCH();
 }

@@ -39,6 +39,9 @@ enum SampleDomain : u32 {
 
 void launch_ntt(const DevConsts* dc, int logn, bool inverse, const NttJob& job, int items,
                 cudaStream_t st);
+// a single phase of the two-phase NTT (cols = column phase, else block phase)
+void launch_ntt_phase(const DevConsts* dc, int logn, bool inverse, bool cols, const NttJob& job,
+                      int items, cudaStream_t st);
 size_t ntt_smem_bytes(int logn);
 
 // ct x ct
@@ -115,4 +118,13 @@ void launch_automorph_ct(const DevConsts* dc, const RnsParams& P, const u64* con
 namespace cssc {
 // register-resident lazy-Shoup butterfly peak (butterflies / s)
 double probe_butterfly_peak(const DevConsts* unused, u64 q, u64 w, u64 wsh, cudaStream_t st);
+}  // namespace cssc
+
+namespace cssc {
+// Fused hybrid key switch (ks_fused.cu): OUT[p] = BASE[p] + (p==0 ? phi_g(RSRC.c0) : 0)
+// + KeySwitch(phi_g(SRC poly src_poly)) with per-item keys; SRC == nullptr reads the
+// contiguous [item][L][N] polynomials at SRCC instead.  DX / ACC are workspaces.
+void launch_ks_fused(const DevConsts* dc, const RnsParams& P, const u64* const* SRC, const u64* SRCC,
+                     int src_poly, const u32* ginv, const u64* const* KEY, const u64* const* BASE,
+                     const u64* const* RSRC, u64* const* OUT, u64* DX, u64* ACC, int items, cudaStream_t st);
 }  // namespace cssc

@@ -206,6 +206,15 @@ int spmvgpu_ctx_sizes(const spmvgpu_ctx* c, uint64_t* n, uint64_t* slots, uint64
 }
 
 int spmvgpu_sync(spmvgpu_ctx* c) { return guard([&] { G(c).synchronize(); }); }
+int spmvgpu_set_option(spmvgpu_ctx* c, const char* name, int64_t value) {
+    return guard([&] {
+        const std::string n = name ? name : "";
+        if (n == "fused_key_switch")
+            G(c).set_fused_key_switch(value != 0);
+        else
+            throw std::invalid_argument("unknown option: " + n);
+    });
+}
 void* spmvgpu_stream(spmvgpu_ctx* c) { return c && c->g ? (void*)c->g->stream() : nullptr; }
 
 int spmvgpu_galois_keys(spmvgpu_ctx* c, const int64_t* steps, size_t n) {

@@ -85,7 +85,8 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
     stats_.levels = depth;
     stats_.hbm_bytes = n ? (u64)n * 3 * C + KEY : 0;
     stats_.key_bytes = n ? KEY : 0;
-    stats_.kernels = n ? 10 : 0;
+    const bool fused = ctx.fused_key_switch();
+    stats_.kernels = n ? (fused ? 11 : 14) : 0;  // each NTT is two kernels (column, block phase)
     stats_.limb_ntts = (u64)n * (7 * M + P.dnum * LK + 2 * LK);
 
     std::set<u32> all_keys;
@@ -126,7 +127,7 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
         stats_.rotations += items;
         stats_.hbm_bytes += (u64)items * 3 * C + lvl_keys.size() * KEY;
         stats_.key_bytes += lvl_keys.size() * KEY;
-        stats_.kernels += 5;
+        stats_.kernels += fused ? 4 : 7;
         stats_.limb_ntts += (u64)items * (P.dnum * LK + 2 * LK);
     }
     stats_.distinct_keys = all_keys.size();
@@ -163,7 +164,7 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
     slice_items_ = put(items_by_slice);
     item_mask_ = put(item_mask);
     stats_.hbm_bytes += (u64)n * 2 * C + (u64)n_masks_ * PT;
-    stats_.kernels += n ? 3 : 0;
+    stats_.kernels += n ? 5 : 0;
     stats_.limb_ntts += (u64)n * 2 * L + (u64)ns_ * 2 * L;
     ctx.synchronize();
 }

@@ -1,0 +1,278 @@
+// ks_fused.cu -- hybrid key switching fused around the two-phase NTT.
+//
+//   K1 k_ks_modup_cols   : automorphism gather + ModUp (E3) of one digit into
+//                          one target limb, then the NTT column phase, per
+//                          column tile                    -> DX (lazy, [0,4q))
+//   K2 k_ks_blocks_inner : for every digit: NTT block phase of DX, multiply by
+//                          the switching-key tiles and accumulate (both key
+//                          polynomials); then the INTT block phase of both
+//                          accumulators                    -> ACC (lazy, [0,2q))
+//   then the column-phase INTT of ACC (standard kernel, full occupancy) and
+//   the elementwise ModDown (E4) with the fused adds
+//                          out = base + phi_g(rsrc.c0) + ModDown(acc)
+// replacing ModUp, NTT x2, inner product, INTT x2 and ModDown (7 launches)
+// by 4 launches with two fewer full passes over the digit/accumulator
+// buffers.  Same integer formulas as bfv_kernels.cu / the oracle, so the
+// outputs are bit-identical.
+#include <stdexcept>
+#include <string>
+#include <type_traits>
+
+#include "bfv_kernels.cuh"
+#include "ntt.cuh"
+
+namespace cssc {
+
+#define KS_CHECK()                                                                              \
+    do {                                                                                        \
+        cudaError_t e_ = cudaGetLastError();                                                    \
+        if (e_ != cudaSuccess) throw std::runtime_error(std::string("ks launch: ") + cudaGetErrorString(e_)); \
+    } while (0)
+
+__device__ __forceinline__ int ks_automorph(u32 ginv, int k, int n, bool& neg) {
+    if (ginv == 0) {
+        neg = false;
+        return k;
+    }
+    const u32 i0 = (u32)(((unsigned long long)ginv * (unsigned)k) & (unsigned long long)(2 * n - 1));
+    neg = i0 >= (u32)n;
+    return neg ? (int)(i0 - n) : (int)i0;
+}
+
+template <int LOGN>
+__device__ __forceinline__ void load_col_twiddles(u64* tws, const u64* tw) {
+    using G = Ntt2<LOGN>;
+    for (int i = threadIdx.x; i < G::R1; i += 128) {
+        const ulonglong2 w = __ldg(reinterpret_cast<const ulonglong2*>(tw) + i);
+        tws[2 * i] = w.x;
+        tws[2 * i + 1] = w.y;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K1: ModUp + NTT column phase
+// ---------------------------------------------------------------------------
+template <int LOGN, int LT, int KT, int AT>
+__global__ void __launch_bounds__(128) k_ks_modup_cols(const DevConsts* __restrict__ dc, const u64* const* SRC,
+                                                       const u64* SRCC, int src_poly, const u32* ginv, u64* DX) {
+    using G = Ntt2<LOGN>;
+    extern __shared__ u64 smem[];
+    u64* tile = smem;
+    u64* tws = smem + G::LINES * G::R1;
+    const int L = LT ? LT : dc->L, K = KT ? KT : dc->K, LK = L + K;
+    const int alpha = AT ? AT : dc->alpha, dnum = (L + alpha - 1) / alpha;
+    int bid = blockIdx.x;
+    const int tileid = bid % G::CTAS_C;
+    bid /= G::CTAS_C;
+    const int j = bid % LK;
+    bid /= LK;
+    const int dg = bid % dnum;
+    const int item = bid / dnum;
+    const int lo = dg * alpha, hi = min(lo + alpha, L);
+    const u64* src = SRC ? SRC[item] + (size_t)src_poly * L * G::N : SRCC + (size_t)item * L * G::N;
+    const u32 gi = ginv ? ginv[item] : 0u;
+    const u64 m = dc->mod[j].q;
+    const bool own = j >= lo && j < hi;
+    const int col0 = tileid * G::LINES;
+    load_col_twiddles<LOGN>(tws, dc->tw[j].fwd);
+    constexpr int PER = G::R1 / 8;  // elements per thread (16 lines x R1 / 128)
+#pragma unroll 4
+    for (int r = 0; r < PER; ++r) {
+        const int e = threadIdx.x + 128 * r, c = e >> 4, jl = e & 15;
+        bool neg;
+        const int idx = ks_automorph(gi, col0 + jl + G::R2 * c, G::N, neg);
+        u64 v;
+        if (own) {
+            const u64 x = __ldg(src + (size_t)j * G::N + idx);
+            v = neg ? neg_mod(x, m) : x;
+        } else {
+            v = 0;
+#pragma unroll
+            for (int i = lo; i < (AT ? lo + AT : hi); ++i) {
+                if (AT && i >= hi) break;
+                const u64 qi = dc->mod[i].q;
+                u64 x = __ldg(src + (size_t)i * G::N + idx);
+                x = neg ? neg_mod(x, qi) : x;
+                const u64 y = shoup(x, dc->dig_hat_inv[i], dc->dig_hat_inv_sh[i], qi);
+                v = add_mod(v, shoup(y, dc->dig_hat[i][j], dc->dig_hat_sh[i][j], m), m);
+            }
+        }
+        tile[c * 16 + jl] = v;
+    }
+    __syncthreads();
+    auto addr = [](int l, int pos) { return pos * 16 + l; };
+    auto twf = [&](int sl, int, int blk) {
+        const int k = (1 << sl) + blk;
+        return make_ulonglong2(tws[2 * k], tws[2 * k + 1]);
+    };
+    line_ntt<G::A, 0, false>(tile, m, addr, twf);
+    u64* dst = DX + (((size_t)item * dnum + dg) * LK + j) * G::N;
+#pragma unroll
+    for (int r = 0; r < G::R1 / 16; ++r) {
+        const int i = threadIdx.x + 128 * r, c = i >> 3, h = i & 7;
+        *reinterpret_cast<ulonglong2*>(dst + (size_t)c * G::R2 + col0 + 2 * h) =
+            make_ulonglong2(tile[c * 16 + 2 * h], tile[c * 16 + 2 * h + 1]);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K2: NTT block phase + key inner product + INTT block phase
+// ---------------------------------------------------------------------------
+template <int LOGN, int LT, int KT, int AT>
+__global__ void __launch_bounds__(128) k_ks_blocks_inner(const DevConsts* __restrict__ dc, const u64* __restrict__ DX,
+                                                         const u64* const* KEY, u64* __restrict__ ACC) {
+    using G = Ntt2<LOGN>;
+    extern __shared__ u64 smem[];
+    constexpr int PITCH = G::PITCH;
+    constexpr int TW = G::LINES * PITCH;
+    u64* work = smem;
+    u64* acc0 = smem + TW;
+    u64* acc1 = smem + 2 * TW;
+    u64* tws = smem + 3 * TW;
+    const int L = LT ? LT : dc->L, K = KT ? KT : dc->K, LK = L + K;
+    const int alpha = AT ? AT : dc->alpha, dnum = (L + alpha - 1) / alpha;
+    int bid = blockIdx.x;
+    const int tileid = bid % G::CTAS_B;
+    bid /= G::CTAS_B;
+    const int j = bid % LK;
+    const int item = bid / LK;
+    const Modulus md = dc->mod[j];
+    const u64 q = md.q;
+    const int blk0 = tileid * G::LINES;
+    const size_t base = (size_t)blk0 * G::R2;
+    const u64* key = KEY[item];
+    const size_t PL = (size_t)LK * G::N;
+    constexpr int PER = G::LINES * G::R2 / 256;  // ulonglong2 per thread
+    auto addr = [](int l, int pos) { return l * PITCH + pos; };
+    auto twf = [&](int sl, int l, int blk) { return block_tw<LOGN>(tws, sl, l, blk); };
+    load_block_twiddles<LOGN>(tws, dc->tw[j].fwd, blk0);
+#pragma unroll 1
+    for (int dg = 0; dg < dnum; ++dg) {
+        const u64* d = DX + (((size_t)item * dnum + dg) * LK + j) * G::N + base;
+        ulonglong2 v[PER];
+#pragma unroll
+        for (int r = 0; r < PER; ++r) v[r] = __ldg(reinterpret_cast<const ulonglong2*>(d) + threadIdx.x + 128 * r);
+        if (dg) __syncthreads();  // previous digit's accumulate finished reading `work`
+#pragma unroll
+        for (int r = 0; r < PER; ++r) {
+            const int x = 2 * (threadIdx.x + 128 * r), b = x >> G::B, c = x & (G::R2 - 1);
+            work[b * PITCH + c] = v[r].x;
+            work[b * PITCH + c + 1] = v[r].y;
+        }
+        cp_async_wait_all();
+        __syncthreads();
+        line_ntt<G::B, 0, false>(work, q, addr, twf);
+        // accumulate work (.) key into acc0/acc1, key tiles streamed coalesced
+        const u64* k0 = key + ((size_t)dg * 2 + 0) * PL + (size_t)j * G::N + base;
+        const u64* k1 = key + ((size_t)dg * 2 + 1) * PL + (size_t)j * G::N + base;
+#pragma unroll
+        for (int r = 0; r < PER; ++r) {
+            const int i = threadIdx.x + 128 * r, x = 2 * i, b = x >> G::B, c = x & (G::R2 - 1);
+            const ulonglong2 a = __ldg(reinterpret_cast<const ulonglong2*>(k0) + i);
+            const ulonglong2 e = __ldg(reinterpret_cast<const ulonglong2*>(k1) + i);
+            const int s0 = b * PITCH + c;
+            const u64 w0 = work[s0], w1 = work[s0 + 1];
+            const u64 p00 = mul_mod(w0, a.x, md), p01 = mul_mod(w1, a.y, md);
+            const u64 p10 = mul_mod(w0, e.x, md), p11 = mul_mod(w1, e.y, md);
+            if (dg == 0) {
+                acc0[s0] = p00;
+                acc0[s0 + 1] = p01;
+                acc1[s0] = p10;
+                acc1[s0 + 1] = p11;
+            } else {
+                acc0[s0] = add_mod(acc0[s0], p00, q);
+                acc0[s0 + 1] = add_mod(acc0[s0 + 1], p01, q);
+                acc1[s0] = add_mod(acc1[s0], p10, q);
+                acc1[s0 + 1] = add_mod(acc1[s0 + 1], p11, q);
+            }
+        }
+    }
+    __syncthreads();
+    load_block_twiddles<LOGN>(tws, dc->tw[j].inv, blk0);
+    cp_async_wait_all();
+    __syncthreads();
+    line_ntt<G::B, 0, true>(acc0, q, addr, twf);
+    line_ntt<G::B, 0, true>(acc1, q, addr, twf);
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+        const u64* a = p ? acc1 : acc0;
+        u64* dst = ACC + (((size_t)item * 2 + p) * LK + j) * G::N + base;
+#pragma unroll
+        for (int r = 0; r < PER; ++r) {
+            const int i = threadIdx.x + 128 * r, x = 2 * i, b = x >> G::B, c = x & (G::R2 - 1);
+            reinterpret_cast<ulonglong2*>(dst)[i] = make_ulonglong2(a[b * PITCH + c], a[b * PITCH + c + 1]);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// launch
+// ---------------------------------------------------------------------------
+template <class F>
+static void ks_dispatch_shape(const RnsParams& P, F&& f) {
+    const auto& c = P.cfg;
+    using std::integral_constant;
+    if (c.L == 3 && c.K == 1 && c.alpha == 1)
+        f(integral_constant<int, 3>{}, integral_constant<int, 1>{}, integral_constant<int, 1>{});
+    else if (c.L == 4 && c.K == 2 && c.alpha == 2)
+        f(integral_constant<int, 4>{}, integral_constant<int, 2>{}, integral_constant<int, 2>{});
+    else if (c.L == 8 && c.K == 4 && c.alpha == 4)
+        f(integral_constant<int, 8>{}, integral_constant<int, 4>{}, integral_constant<int, 4>{});
+    else
+        f(integral_constant<int, 0>{}, integral_constant<int, 0>{}, integral_constant<int, 0>{});
+}
+
+template <int LOGN, int LT, int KT, int AT>
+static void ks_fused_t(const DevConsts* dc, const RnsParams& P, const u64* const* SRC, const u64* SRCC,
+                       int src_poly, const u32* ginv, const u64* const* KEY, const u64* const* BASE,
+                       const u64* const* RSRC, u64* const* OUT, u64* DX, u64* ACC, int items, cudaStream_t st) {
+    using G = Ntt2<LOGN>;
+    const int L = P.cfg.L, K = P.cfg.K, LK = L + K, dnum = P.dnum;
+    const int smem1 = G::SMEM_C;
+    const int smem2 = (3 * G::LINES * G::PITCH + 2 * G::TWB) * 8;
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(k_ks_modup_cols<LOGN, LT, KT, AT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem1);
+        cudaFuncSetAttribute(k_ks_blocks_inner<LOGN, LT, KT, AT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
+        configured = true;
+    }
+    k_ks_modup_cols<LOGN, LT, KT, AT><<<items * dnum * LK * G::CTAS_C, 128, smem1, st>>>(dc, SRC, SRCC, src_poly,
+                                                                                      ginv, DX);
+    KS_CHECK();
+    k_ks_blocks_inner<LOGN, LT, KT, AT><<<items * LK * G::CTAS_B, 128, smem2, st>>>(dc, DX, KEY, ACC);
+    KS_CHECK();
+    NttJob j;
+    for (int i = 0; i < MAX_JOB_LIMBS; ++i) j.pidx[i] = (signed char)(i % LK);
+    j.src = ACC;
+    j.dst = ACC;
+    j.limbs = 2 * LK;
+    launch_ntt_phase(dc, LOGN, /*inverse=*/true, /*cols=*/true, j, items, st);
+    launch_ks_moddown(dc, P, ACC, BASE, RSRC, ginv, OUT, items, st);
+}
+
+template <int LOGN>
+static void ks_fused_logn(const DevConsts* dc, const RnsParams& P, const u64* const* SRC, const u64* SRCC,
+                          int src_poly, const u32* ginv, const u64* const* KEY, const u64* const* BASE,
+                          const u64* const* RSRC, u64* const* OUT, u64* DX, u64* ACC, int items, cudaStream_t st) {
+    ks_dispatch_shape(P, [&](auto l_, auto k_, auto a_) {
+        ks_fused_t<LOGN, decltype(l_)::value, decltype(k_)::value, decltype(a_)::value>(
+            dc, P, SRC, SRCC, src_poly, ginv, KEY, BASE, RSRC, OUT, DX, ACC, items, st);
+    });
+}
+
+void launch_ks_fused(const DevConsts* dc, const RnsParams& P, const u64* const* SRC, const u64* SRCC,
+                     int src_poly, const u32* ginv, const u64* const* KEY, const u64* const* BASE,
+                     const u64* const* RSRC, u64* const* OUT, u64* DX, u64* ACC, int items, cudaStream_t st) {
+    if (!items) return;
+    switch (P.cfg.logn) {
+        case 10: ks_fused_logn<10>(dc, P, SRC, SRCC, src_poly, ginv, KEY, BASE, RSRC, OUT, DX, ACC, items, st); break;
+        case 11: ks_fused_logn<11>(dc, P, SRC, SRCC, src_poly, ginv, KEY, BASE, RSRC, OUT, DX, ACC, items, st); break;
+        case 12: ks_fused_logn<12>(dc, P, SRC, SRCC, src_poly, ginv, KEY, BASE, RSRC, OUT, DX, ACC, items, st); break;
+        case 13: ks_fused_logn<13>(dc, P, SRC, SRCC, src_poly, ginv, KEY, BASE, RSRC, OUT, DX, ACC, items, st); break;
+        case 14: ks_fused_logn<14>(dc, P, SRC, SRCC, src_poly, ginv, KEY, BASE, RSRC, OUT, DX, ACC, items, st); break;
+        case 15: ks_fused_logn<15>(dc, P, SRC, SRCC, src_poly, ginv, KEY, BASE, RSRC, OUT, DX, ACC, items, st); break;
+        default: throw std::invalid_argument("key switch: unsupported logn");
+    }
+}
+
+}  // namespace cssc

@@ -25,8 +25,9 @@ namespace cssc {
 
 template <int LOGN>
 struct Ntt2 {
-    static constexpr int A = (LOGN + 1) / 2;  // column-phase stages
-    static constexpr int B = LOGN - A;        // block-phase stages
+    // block phase: 6 stages (7 at 2^15) so its twiddles fit next to the tile
+    static constexpr int B = LOGN >= 15 ? 7 : (LOGN >= 12 ? 6 : LOGN / 2);
+    static constexpr int A = LOGN - B;        // column-phase stages
     static constexpr int R1 = 1 << A;         // column length
     static constexpr int R2 = 1 << B;         // block length / number of columns
     static constexpr int N = 1 << LOGN;
@@ -34,9 +35,51 @@ struct Ntt2 {
     static constexpr int LINES = 16;
     static constexpr int CTAS_C = R2 / LINES;  // column-phase CTAs per limb
     static constexpr int CTAS_B = R1 / LINES;  // block-phase CTAs per limb
+    static constexpr int PITCH = R2 + 1;       // odd block-tile pitch (conflict free)
+    // block-phase twiddles of one tile: stage s holds 16 lines x 2^s entries
+    // with an odd line stride (1 at s = 0, 2^s + 1 after) -> conflict-free LDS.128
+    __host__ __device__ static constexpr int tw_stride(int s) { return s == 0 ? 1 : (1 << s) + 1; }
+    __host__ __device__ static constexpr int tw_off(int s) { return s == 0 ? 0 : LINES * ((1 << s) + s - 2); }
+    static constexpr int TWB = LINES * ((1 << B) + B - 2);  // = tw_off(B) entries
     static constexpr int SMEM_C = (LINES * R1 + 2 * R1) * 8;
-    static constexpr int SMEM_B = (LINES * (R2 + 1)) * 8;
+    static constexpr int SMEM_B = (LINES * PITCH + 2 * TWB) * 8;
 };
+
+// Ampere-style async global->smem copies (LDGSTS): the tile and twiddle loads
+// of a CTA are all in flight at once without register staging.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// Stage the block-phase twiddles of blocks [blk0, blk0 + 16) into smem:
+// stage s needs W[2^(A+s) + (blk0 + l) * 2^s + blk], contiguous over (l, blk).
+template <int LOGN>
+__device__ __forceinline__ void load_block_twiddles(u64* tws, const u64* table, int blk0) {
+    using G = Ntt2<LOGN>;
+    const ulonglong2* t2 = reinterpret_cast<const ulonglong2*>(table);
+#pragma unroll
+    for (int s = 0; s < G::B; ++s) {
+        const int cnt = G::LINES << s;
+        const int gbase = (1 << (G::A + s)) + (blk0 << s);
+        for (int i = threadIdx.x; i < cnt; i += 128) {
+            const int l = i >> s, blk = i & ((1 << s) - 1);
+            const int e = G::tw_off(s) + l * G::tw_stride(s) + blk;
+            cp_async16(tws + 2 * e, t2 + gbase + i);
+        }
+    }
+}
+
+template <int LOGN>
+__device__ __forceinline__ ulonglong2 block_tw(const u64* tws, int s, int l, int blk) {
+    using G = Ntt2<LOGN>;
+    return *reinterpret_cast<const ulonglong2*>(tws + 2 * (G::tw_off(s) + l * G::tw_stride(s) + blk));
+}
 
 // One radix-2^R pass over local stages [S0L, S0L+R) of 16 lines of length 2^RB.
 // addr(l, pos): smem word of element pos of line l.  tw(sl, l, blk): twiddle
@@ -48,6 +91,7 @@ __device__ __forceinline__ void line_pass(u64* s, u64 q, Addr addr, Tw tw) {
     constexpr int LOG_TL = RB - S0L - R;
     constexpr int G = 16 * (1 << (RB - R));
     const u64 two_q = 2 * q;
+#pragma unroll 1
     for (int gi = threadIdx.x; gi < G; gi += 128) {
         const int l = gi & 15;
         const int g = gi >> 4;
@@ -98,7 +142,9 @@ __device__ __forceinline__ void line_pass(u64* s, u64 q, Addr addr, Tw tw) {
 template <int RB, int S0L, bool INV, class Addr, class Tw>
 __device__ __forceinline__ void line_ntt(u64* s, u64 q, Addr addr, Tw tw) {
     if constexpr (S0L < RB) {
-        constexpr int R = (RB - S0L) >= 4 ? 4 : (RB - S0L);
+        // pass radix: 6 -> 3+3, 9 -> 3+3+3, 5 -> 3+2, otherwise 4s then the rest
+        constexpr int REM = RB - S0L;
+        constexpr int R = (REM == 6 || REM == 9 || REM == 5) ? 3 : (REM >= 4 ? 4 : REM);
         if (!INV) {
             line_pass<RB, S0L, R, false>(s, q, addr, tw);
             __syncthreads();

@@ -106,3 +106,18 @@ def test_mul_relin_rotate_mask_match(pair):
     want[9:] = 0
     assert np.array_equal(sl[0].astype(np.int64), want)
     ctx.free(np.concatenate([ha[None], hb[None], hp, hs, hm]))
+
+
+def test_fused_and_unfused_key_switch_agree():
+    """The fused 3-kernel key switch and the 7-launch pipeline give the same words."""
+    ctx = pk.Context(logn=14, seed=5)
+    S = ctx.slots
+    a, b = rand_vals(S, 21), rand_vals(S, 22)
+    ha, hb = ctx.encrypt([a, b], [1, 2])
+    outs = {}
+    for fused in (1, 0):
+        ctx.set_option("fused_key_switch", fused)
+        hp = ctx.mul_relin([ha], [hb])
+        hr = ctx.rotate_add(hp, hp, [129])
+        outs[fused] = (ctx.download(int(hp[0])), ctx.download(int(hr[0])))
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
