@@ -88,8 +88,9 @@ __device__ __forceinline__ u64* job_dst(const NttJob& job, int item, int j, int 
 // Column phase: 16 strided columns of R1 elements.  Forward: first phase
 // (src -> dst).  Inverse: last phase (dst -> dst), applies N^-1, canonical.
 template <int LOGN, bool INV>
-__global__ void __launch_bounds__(128) k_ntt_cols(const DevConsts* __restrict__ dc, NttJob job) {
+__global__ void __launch_bounds__(Ntt2<LOGN>::TC, 256 / Ntt2<LOGN>::TC * 2) k_ntt_cols(const DevConsts* __restrict__ dc, NttJob job) {
     using G = Ntt2<LOGN>;
+    constexpr int T = G::TC;
     extern __shared__ u64 smem[];
     u64* tile = smem;                       // [R1][16]
     u64* tws = smem + G::LINES * G::R1;     // [R1] pairs
@@ -104,10 +105,10 @@ __global__ void __launch_bounds__(128) k_ntt_cols(const DevConsts* __restrict__ 
     const int col0 = tileid * G::LINES;
     // twiddles W[0 .. R1) and the tile (rows of 16 consecutive words, 8 threads
     // x 16 B per row) via async copies: every load of the CTA in flight at once
-    for (int i = threadIdx.x; i < G::R1; i += 128) cp_async16(tws + 2 * i, tw + 2 * i);
+    for (int i = threadIdx.x; i < G::R1; i += T) cp_async16(tws + 2 * i, tw + 2 * i);
 #pragma unroll
-    for (int r = 0; r < G::R1 / 16; ++r) {
-        const int i = threadIdx.x + 128 * r, c = i >> 3, h = i & 7;
+    for (int r = 0; r < G::R1 * 8 / T; ++r) {
+        const int i = threadIdx.x + T * r, c = i >> 3, h = i & 7;
         cp_async16(tile + c * 16 + 2 * h, src + (size_t)c * G::R2 + col0 + 2 * h);
     }
     cp_async_wait_all();
@@ -120,8 +121,8 @@ __global__ void __launch_bounds__(128) k_ntt_cols(const DevConsts* __restrict__ 
     line_ntt<G::A, 0, INV>(tile, q, addr, twf);
     const u64 ni = dc->ninv[prime], nish = dc->ninv_sh[prime];
 #pragma unroll
-    for (int r = 0; r < G::R1 / 16; ++r) {
-        const int i = threadIdx.x + 128 * r, c = i >> 3, h = i & 7;
+    for (int r = 0; r < G::R1 * 8 / T; ++r) {
+        const int i = threadIdx.x + T * r, c = i >> 3, h = i & 7;
         u64 a0 = tile[c * 16 + 2 * h], a1 = tile[c * 16 + 2 * h + 1];
         if (INV) {
             a0 = shoup(a0, ni, nish, q);
@@ -192,13 +193,13 @@ static void launch_ntt_t(const DevConsts* dc, bool inv, const NttJob& job, int i
     const int limbs = items * job.limbs;
     if (limbs == 0) return;
     if (!inv) {
-        k_ntt_cols<LOGN, false><<<limbs * G::CTAS_C, 128, G::SMEM_C, st>>>(dc, job);
+        k_ntt_cols<LOGN, false><<<limbs * G::CTAS_C, G::TC, G::SMEM_C, st>>>(dc, job);
         CSSC_CHECK_LAUNCH();
         k_ntt_blocks<LOGN, false><<<limbs * G::CTAS_B, 128, G::SMEM_B, st>>>(dc, job);
     } else {
         k_ntt_blocks<LOGN, true><<<limbs * G::CTAS_B, 128, G::SMEM_B, st>>>(dc, job);
         CSSC_CHECK_LAUNCH();
-        k_ntt_cols<LOGN, true><<<limbs * G::CTAS_C, 128, G::SMEM_C, st>>>(dc, job);
+        k_ntt_cols<LOGN, true><<<limbs * G::CTAS_C, G::TC, G::SMEM_C, st>>>(dc, job);
     }
     CSSC_CHECK_LAUNCH();
 }
@@ -211,9 +212,9 @@ static void launch_phase_t(const DevConsts* dc, bool inv, bool cols, const NttJo
     if (limbs == 0) return;
     if (cols) {
         if (inv)
-            k_ntt_cols<LOGN, true><<<limbs * G::CTAS_C, 128, G::SMEM_C, st>>>(dc, job);
+            k_ntt_cols<LOGN, true><<<limbs * G::CTAS_C, G::TC, G::SMEM_C, st>>>(dc, job);
         else
-            k_ntt_cols<LOGN, false><<<limbs * G::CTAS_C, 128, G::SMEM_C, st>>>(dc, job);
+            k_ntt_cols<LOGN, false><<<limbs * G::CTAS_C, G::TC, G::SMEM_C, st>>>(dc, job);
     } else {
         if (inv)
             k_ntt_blocks<LOGN, true><<<limbs * G::CTAS_B, 128, G::SMEM_B, st>>>(dc, job);

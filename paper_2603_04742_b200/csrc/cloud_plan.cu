@@ -2,6 +2,7 @@
 #include "cloud_plan.hpp"
 
 #include <algorithm>
+#include <cstring>
 #include <map>
 #include <numeric>
 #include <set>
@@ -11,15 +12,16 @@
 
 namespace cssc {
 
+// Plan arrays are staged on the host and uploaded with ONE copy at the end
+// of the constructor; put() hands out their future device addresses.
 template <class T>
 T* CloudPlan::put(const std::vector<T>& v) {
-    DevBuf b(&ctx_.pool(), std::max<size_t>(sizeof(T) * v.size(), 64));
-    if (!v.empty())
-        cuda_check(cudaMemcpy(b.as<void>(), v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice),
-                   "plan upload");
-    T* p = b.as<T>();
-    arrays_.push_back(std::move(b));
-    return p;
+    const size_t off = (stage_.size() + 15) & ~size_t(15);
+    const size_t bytes = sizeof(T) * v.size();
+    if (off + bytes > arena_.bytes()) throw std::logic_error("plan arena too small");
+    stage_.resize(off + bytes);
+    if (bytes) std::memcpy(stage_.data() + off, v.data(), bytes);
+    return reinterpret_cast<T*>(arena_.as<unsigned char>() + off);
 }
 
 CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
@@ -46,6 +48,9 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
     std::stable_sort(order.begin(), order.end(),
                      [&](int x, int y) { return steps[x].size() > steps[y].size(); });
     const int depth = n ? (int)steps[order[0]].size() : 0;
+    // upper bound of all plan arrays (8-byte entries) plus 16-byte alignment slack
+    arena_ = DevBuf(&ctx.pool(), 8 * ((size_t)(8 + 5 * depth) * std::max(n, 1) + 2 * (size_t)ns_ + 8) +
+                                     16 * (size_t)(5 * depth + 16));
 
     prod_ = DevBuf(&ctx.pool(), sizeof(u64) * ctw * std::max(n, 1));
     if (depth >= 1) acc0_ = DevBuf(&ctx.pool(), sizeof(u64) * ctw * n);
@@ -166,6 +171,10 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
     stats_.hbm_bytes += (u64)n * 2 * C + (u64)n_masks_ * PT;
     stats_.kernels += n ? 5 : 0;
     stats_.limb_ntts += (u64)n * 2 * L + (u64)ns_ * 2 * L;
+    if (!stage_.empty())
+        cuda_check(cudaMemcpyAsync(arena_.as<void>(), stage_.data(), stage_.size(), cudaMemcpyHostToDevice,
+                                   ctx.stream()),
+                   "plan upload");
     ctx.synchronize();
 }
 

@@ -49,7 +49,8 @@ private:
     PlanStats stats_;
     DevBuf prod_, acc0_, acc1_;
     DevBuf T_, Z_, D2_, DX_, ACC_, MT_, MASKS_;
-    std::vector<DevBuf> arrays_;  // device pointer / index arrays
+    DevBuf arena_;                        // device pointer / index arrays (one block)
+    std::vector<unsigned char> stage_;    // host staging of arena_
     // device arrays
     const u64* const* A_ = nullptr;
     const u64* const* B_ = nullptr;

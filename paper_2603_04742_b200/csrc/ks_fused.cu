@@ -42,7 +42,7 @@ __device__ __forceinline__ int ks_automorph(u32 ginv, int k, int n, bool& neg) {
 template <int LOGN>
 __device__ __forceinline__ void load_col_twiddles(u64* tws, const u64* tw) {
     using G = Ntt2<LOGN>;
-    for (int i = threadIdx.x; i < G::R1; i += 128) {
+    for (int i = threadIdx.x; i < G::R1; i += blockDim.x) {
         const ulonglong2 w = __ldg(reinterpret_cast<const ulonglong2*>(tw) + i);
         tws[2 * i] = w.x;
         tws[2 * i + 1] = w.y;
@@ -53,7 +53,7 @@ __device__ __forceinline__ void load_col_twiddles(u64* tws, const u64* tw) {
 // K1: ModUp + NTT column phase
 // ---------------------------------------------------------------------------
 template <int LOGN, int LT, int KT, int AT>
-__global__ void __launch_bounds__(128) k_ks_modup_cols(const DevConsts* __restrict__ dc, const u64* const* SRC,
+__global__ void __launch_bounds__(Ntt2<LOGN>::TC, 256 / Ntt2<LOGN>::TC * 2) k_ks_modup_cols(const DevConsts* __restrict__ dc, const u64* const* SRC,
                                                        const u64* SRCC, int src_poly, const u32* ginv, u64* DX) {
     using G = Ntt2<LOGN>;
     extern __shared__ u64 smem[];
@@ -75,10 +75,10 @@ __global__ void __launch_bounds__(128) k_ks_modup_cols(const DevConsts* __restri
     const bool own = j >= lo && j < hi;
     const int col0 = tileid * G::LINES;
     load_col_twiddles<LOGN>(tws, dc->tw[j].fwd);
-    constexpr int PER = G::R1 / 8;  // elements per thread (16 lines x R1 / 128)
+    constexpr int PER = G::R1 * 16 / G::TC;  // elements per thread
 #pragma unroll 4
     for (int r = 0; r < PER; ++r) {
-        const int e = threadIdx.x + 128 * r, c = e >> 4, jl = e & 15;
+        const int e = threadIdx.x + G::TC * r, c = e >> 4, jl = e & 15;
         bool neg;
         const int idx = ks_automorph(gi, col0 + jl + G::R2 * c, G::N, neg);
         u64 v;
@@ -108,8 +108,8 @@ __global__ void __launch_bounds__(128) k_ks_modup_cols(const DevConsts* __restri
     line_ntt<G::A, 0, false>(tile, m, addr, twf);
     u64* dst = DX + (((size_t)item * dnum + dg) * LK + j) * G::N;
 #pragma unroll
-    for (int r = 0; r < G::R1 / 16; ++r) {
-        const int i = threadIdx.x + 128 * r, c = i >> 3, h = i & 7;
+    for (int r = 0; r < G::R1 * 8 / G::TC; ++r) {
+        const int i = threadIdx.x + G::TC * r, c = i >> 3, h = i & 7;
         *reinterpret_cast<ulonglong2*>(dst + (size_t)c * G::R2 + col0 + 2 * h) =
             make_ulonglong2(tile[c * 16 + 2 * h], tile[c * 16 + 2 * h + 1]);
     }
@@ -236,7 +236,7 @@ static void ks_fused_t(const DevConsts* dc, const RnsParams& P, const u64* const
         cudaFuncSetAttribute(k_ks_blocks_inner<LOGN, LT, KT, AT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
         configured = true;
     }
-    k_ks_modup_cols<LOGN, LT, KT, AT><<<items * dnum * LK * G::CTAS_C, 128, smem1, st>>>(dc, SRC, SRCC, src_poly,
+    k_ks_modup_cols<LOGN, LT, KT, AT><<<items * dnum * LK * G::CTAS_C, G::TC, smem1, st>>>(dc, SRC, SRCC, src_poly,
                                                                                       ginv, DX);
     KS_CHECK();
     k_ks_blocks_inner<LOGN, LT, KT, AT><<<items * LK * G::CTAS_B, 128, smem2, st>>>(dc, DX, KEY, ACC);

@@ -31,7 +31,8 @@ struct Ntt2 {
     static constexpr int R1 = 1 << A;         // column length
     static constexpr int R2 = 1 << B;         // block length / number of columns
     static constexpr int N = 1 << LOGN;
-    static constexpr int THREADS = 128;
+    static constexpr int THREADS = 128;        // block-phase CTAs
+    static constexpr int TC = R1 >= 256 ? 256 : 128;  // column-phase CTAs: one radix group per thread
     static constexpr int LINES = 16;
     static constexpr int CTAS_C = R2 / LINES;  // column-phase CTAs per limb
     static constexpr int CTAS_B = R1 / LINES;  // block-phase CTAs per limb
@@ -67,7 +68,7 @@ __device__ __forceinline__ void load_block_twiddles(u64* tws, const u64* table, 
     for (int s = 0; s < G::B; ++s) {
         const int cnt = G::LINES << s;
         const int gbase = (1 << (G::A + s)) + (blk0 << s);
-        for (int i = threadIdx.x; i < cnt; i += 128) {
+        for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
             const int l = i >> s, blk = i & ((1 << s) - 1);
             const int e = G::tw_off(s) + l * G::tw_stride(s) + blk;
             cp_async16(tws + 2 * e, t2 + gbase + i);
@@ -92,7 +93,7 @@ __device__ __forceinline__ void line_pass(u64* s, u64 q, Addr addr, Tw tw) {
     constexpr int G = 16 * (1 << (RB - R));
     const u64 two_q = 2 * q;
 #pragma unroll 1
-    for (int gi = threadIdx.x; gi < G; gi += 128) {
+    for (int gi = threadIdx.x; gi < G; gi += blockDim.x) {
         const int l = gi & 15;
         const int g = gi >> 4;
         const int blk = g >> LOG_TL;
