@@ -268,11 +268,19 @@ def measure_config(pk, cfg, args, rank, world, device, full=True):
     hbm_bytes = limbs * 2 * n * 8
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    traffic = None
+    tfile = ROOT / "profiles" / f"r01_ntt_traffic_{limbs}.json"
+    if tfile.exists():  # dram read+write of the same launch shape from one ncu capture
+        tj = json.loads(tfile.read_text())
+        if tj.get("logn") == logn:
+            traffic = int(tj["traffic_bytes_per_launch"])
     out["roofline"] = {
-        "bound": "int", "kernel": "k_ntt (batched negacyclic NTT, one CTA per limb)",
+        "bound": "int", "kernel": "forward NTT launch = k_ntt_cols + k_ntt_blocks (two-phase, all limbs)",
         "achieved": round(bfly / (us * 1e-6) / 1e9, 2), "peak": round(peak / 1e9, 2),
         "unit": "Gbutterfly/s", "frac": round(bfly / (us * 1e-6) / peak, 4),
-        "traffic": None, "launch_us": round(us, 3), "limbs_per_launch": limbs,
+        "traffic": traffic, "traffic_source": str(tfile.relative_to(ROOT)) if traffic else None,
+        "algorithmic_bytes_per_launch": 2 * limbs * n * 8,  # one compulsory read + write per limb
+        "launch_us": round(us, 3), "limbs_per_launch": limbs,
         "hbm_achieved_gbs": round(hbm_bytes / (us * 1e-6) / 1e9, 1), "hbm_peak_gbs": hbm_peak,
         "hbm_frac": round(hbm_bytes / (us * 1e-6) / 1e9 / hbm_peak, 4),
         "peak_source": "register-resident lazy-Shoup radix-16 butterfly probe (this run); HBM: MEASURED_PEAKS.json",

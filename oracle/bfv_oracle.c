@@ -390,7 +390,7 @@ bfvo_ctx* bfvo_create(int logn, int L, int K, int alpha, int qbits, int pbits, u
     u64 twoN = 2 * (u64)n;
     gen_primes(qbits, twoN, L, c->q, NULL, 0);
     gen_primes(pbits, twoN, K, c->q + L, c->q, L);
-    gen_primes(60, twoN, c->nB, c->q + L + K, c->q, L + K);
+    gen_primes(58, twoN, c->nB, c->q + L + K, c->q, L + K);
     c->np = L + K + c->nB + 1;
     c->q[c->np - 1] = t;
     for (int i = 0; i < c->np; i++) ntt_tables(c, i);

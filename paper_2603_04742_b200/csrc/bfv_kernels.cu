@@ -134,46 +134,86 @@ __global__ void __launch_bounds__(Ntt2<LOGN>::TC, 256 / Ntt2<LOGN>::TC * 2) k_nt
 
 // Block phase: 16 contiguous blocks of R2 elements.  Forward: last phase
 // (dst -> dst, canonical output).  Inverse: first phase (src -> dst).
+// The twiddles of a block tile (~2x the tile's bytes) depend only on the
+// prime and the tile, so one CTA handles the same tile of `ipc` items that
+// share limb index j (same prime): twiddles staged once, tiles double-buffered
+// (the next item's cp.async load overlaps the current item's butterflies).
 template <int LOGN, bool INV>
-__global__ void __launch_bounds__(128) k_ntt_blocks(const DevConsts* __restrict__ dc, NttJob job) {
+__global__ void __launch_bounds__(128) k_ntt_blocks(const DevConsts* __restrict__ dc, NttJob job, int items,
+                                                    int ipc) {
     using G = Ntt2<LOGN>;
     extern __shared__ u64 smem[];
-    constexpr int PITCH = G::R2 + 1;
+    constexpr int PITCH = G::PITCH;
+    constexpr int TILE = G::LINES * PITCH;
     const int tileid = blockIdx.x % G::CTAS_B;
-    const int lj = blockIdx.x / G::CTAS_B;
-    const int item = lj / job.limbs, j = lj - item * job.limbs;
+    const int rest = blockIdx.x / G::CTAS_B;
+    const int j = rest % job.limbs, grp = rest / job.limbs;
+    const int it0 = grp * ipc, it1 = min(items, it0 + ipc);
     const int prime = job.pidx[j];
     const u64 q = dc->mod[prime].q;
     const u64* tw = INV ? dc->tw[prime].inv : dc->tw[prime].fwd;
-    const u64* src = INV ? job_src(job, item, j, G::N) : job_dst(job, item, j, G::N);
-    u64* dst = job_dst(job, item, j, G::N);
     const int blk0 = tileid * G::LINES;
     const size_t base = (size_t)blk0 * G::R2;
-    u64* tws = smem + G::LINES * PITCH;
+    u64* tws = smem + 2 * TILE;
+    auto src_of = [&](int it) { return INV ? job_src(job, it, j, G::N) : job_dst(job, it, j, G::N); };
+    auto issue_load = [&](int it, u64* buf) {
+        const u64* src = src_of(it) + base;
 #pragma unroll
-    for (int r = 0; r < G::LINES * G::R2 / 128; ++r) {
-        const int x = threadIdx.x + 128 * r, b = x >> G::B, c = x & (G::R2 - 1);
-        cp_async8(smem + b * PITCH + c, src + base + x);
-    }
+        for (int r = 0; r < G::LINES * G::R2 / 128; ++r) {
+            const int x = threadIdx.x + 128 * r, b = x >> G::B, c = x & (G::R2 - 1);
+            cp_async8(buf + b * PITCH + c, src + x);
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    issue_load(it0, smem);
     load_block_twiddles<LOGN>(tws, tw, blk0);
-    cp_async_wait_all();
-    __syncthreads();
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
     auto addr = [](int l, int pos) { return l * PITCH + pos; };
     auto twf = [&](int sl, int l, int blk) { return block_tw<LOGN>(tws, sl, l, blk); };
-    line_ntt<G::B, 0, INV>(smem, q, addr, twf);
-    const u64 two_q = 2 * q;
-#pragma unroll
-    for (int r = 0; r < G::LINES * G::R2 / 256; ++r) {
-        const int x = 2 * (threadIdx.x + 128 * r), b = x >> G::B, c = x & (G::R2 - 1);
-        u64 a0 = smem[b * PITCH + c], a1 = smem[b * PITCH + c + 1];
-        if (!INV) {
-            a0 = a0 >= two_q ? a0 - two_q : a0;
-            a0 = a0 >= q ? a0 - q : a0;
-            a1 = a1 >= two_q ? a1 - two_q : a1;
-            a1 = a1 >= q ? a1 - q : a1;
+    const u64 mu = dc->mod[prime].mu1;  // floor(2^64 / q)
+#pragma unroll 1
+    for (int it = it0; it < it1; ++it) {
+        u64* cur = smem + ((it - it0) & 1) * TILE;
+        if (it + 1 < it1) {
+            issue_load(it + 1, smem + ((it + 1 - it0) & 1) * TILE);
+            asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        } else {
+            cp_async_wait_all();
         }
-        *reinterpret_cast<ulonglong2*>(dst + base + x) = make_ulonglong2(a0, a1);
+        __syncthreads();
+        line_ntt<G::B, 0, INV>(cur, q, addr, twf);
+        u64* dst = job_dst(job, it, j, G::N) + base;
+#pragma unroll
+        for (int r = 0; r < G::LINES * G::R2 / 256; ++r) {
+            const int x = 2 * (threadIdx.x + 128 * r), b = x >> G::B, c = x & (G::R2 - 1);
+            u64 a0 = cur[b * PITCH + c], a1 = cur[b * PITCH + c + 1];
+            if (!INV) {  // forward output < 31q: one Barrett step to [0, 3q), then canonical
+                a0 -= umulhi(a0, mu) * q;
+                a1 -= umulhi(a1, mu) * q;
+                a0 = a0 >= q ? a0 - q : a0;
+                a0 = a0 >= q ? a0 - q : a0;
+                a1 = a1 >= q ? a1 - q : a1;
+                a1 = a1 >= q ? a1 - q : a1;
+            }
+            *reinterpret_cast<ulonglong2*>(dst + x) = make_ulonglong2(a0, a1);
+        }
+        __syncthreads();  // `cur` is reloaded two items later
     }
+}
+
+// items per block-phase CTA: amortise twiddle staging while keeping >= ~2 waves
+static int blocks_ipc(int items, int limbs_per_item, int ctas_per_limb) {
+    int ipc = 1;
+    while (ipc < 8 && (long)items * limbs_per_item * ctas_per_limb / (2 * ipc) >= 2 * 148 * 4) ipc *= 2;
+    return ipc;
+}
+
+template <int LOGN, bool INV>
+static void launch_blocks(const DevConsts* dc, const NttJob& job, int items, cudaStream_t st) {
+    using G = Ntt2<LOGN>;
+    const int ipc = blocks_ipc(items, job.limbs, G::CTAS_B);
+    const int groups = (items + ipc - 1) / ipc;
+    k_ntt_blocks<LOGN, INV><<<groups * job.limbs * G::CTAS_B, 128, G::SMEM_B, st>>>(dc, job, items, ipc);
 }
 
 size_t ntt_smem_bytes(int logn) { return (size_t)8 << logn; }
@@ -195,9 +235,9 @@ static void launch_ntt_t(const DevConsts* dc, bool inv, const NttJob& job, int i
     if (!inv) {
         k_ntt_cols<LOGN, false><<<limbs * G::CTAS_C, G::TC, G::SMEM_C, st>>>(dc, job);
         CSSC_CHECK_LAUNCH();
-        k_ntt_blocks<LOGN, false><<<limbs * G::CTAS_B, 128, G::SMEM_B, st>>>(dc, job);
+        launch_blocks<LOGN, false>(dc, job, items, st);
     } else {
-        k_ntt_blocks<LOGN, true><<<limbs * G::CTAS_B, 128, G::SMEM_B, st>>>(dc, job);
+        launch_blocks<LOGN, true>(dc, job, items, st);
         CSSC_CHECK_LAUNCH();
         k_ntt_cols<LOGN, true><<<limbs * G::CTAS_C, G::TC, G::SMEM_C, st>>>(dc, job);
     }
@@ -217,9 +257,9 @@ static void launch_phase_t(const DevConsts* dc, bool inv, bool cols, const NttJo
             k_ntt_cols<LOGN, false><<<limbs * G::CTAS_C, G::TC, G::SMEM_C, st>>>(dc, job);
     } else {
         if (inv)
-            k_ntt_blocks<LOGN, true><<<limbs * G::CTAS_B, 128, G::SMEM_B, st>>>(dc, job);
+            launch_blocks<LOGN, true>(dc, job, items, st);
         else
-            k_ntt_blocks<LOGN, false><<<limbs * G::CTAS_B, 128, G::SMEM_B, st>>>(dc, job);
+            launch_blocks<LOGN, false>(dc, job, items, st);
     }
     CSSC_CHECK_LAUNCH();
 }
@@ -995,9 +1035,11 @@ void launch_automorph_ct(const DevConsts* dc, const RnsParams& P, const u64* con
 namespace cssc {
 
 // ---------------------------------------------------------------------------
-// roofline probe: the radix-16 lazy-Shoup butterfly network of fwd_pass, fed
-// from registers only (no memory traffic), to measure the integer peak the
-// NTT can approach.  Each iteration = 4 stages x 8 butterflies.
+// roofline probe: the radix-16 forward butterfly network of line_pass
+// (correction-free lazy Shoup, as the forward NTT runs it), fed from
+// registers only (no memory traffic), to measure the integer peak the NTT can
+// approach.  Each iteration = 4 stages x 8 butterflies.  Values wrap; only the
+// instruction stream matters.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_bfly_peak(u64 q, u64 w0, u64 w0sh, int iters, u64* sink) {
     u64 v[16];
@@ -1012,8 +1054,7 @@ __global__ void __launch_bounds__(256) k_bfly_peak(u64 q, u64 w0, u64 w0sh, int 
 #pragma unroll
             for (int c = 0; c < 16; ++c) {
                 if (c & h) continue;
-                u64 x = v[c];
-                x = x >= two_q ? x - two_q : x;
+                const u64 x = v[c];
                 const u64 y = shoup_lazy(v[c + h], w, wsh, q);
                 v[c] = x + y;
                 v[c + h] = x - y + two_q;

@@ -143,10 +143,10 @@ void spmvgpu_default_params(int logn, spmvgpu_params* p) {
     p->logn = logn;
     if (logn <= 13) {  // N = 8192: Q 3 x 54 bits + P 54 bits = 216 <= 218 (128-bit security)
         p->L = 3, p->K = 1, p->alpha = 1, p->qbits = 54, p->pbits = 54;
-    } else if (logn == 14) {  // N = 16384: 6 x 60 = 360 <= 438
-        p->L = 4, p->K = 2, p->alpha = 2, p->qbits = 60, p->pbits = 60;
-    } else {  // N = 32768: 12 x 60 = 720 <= 881
-        p->L = 8, p->K = 4, p->alpha = 4, p->qbits = 60, p->pbits = 60;
+    } else if (logn == 14) {  // N = 16384: 6 x 58 = 348 <= 438
+        p->L = 4, p->K = 2, p->alpha = 2, p->qbits = 58, p->pbits = 58;
+    } else {  // N = 32768: 12 x 58 = 696 <= 881
+        p->L = 8, p->K = 4, p->alpha = 4, p->qbits = 58, p->pbits = 58;
     }
     p->t = 65537;
     p->seed = 1;

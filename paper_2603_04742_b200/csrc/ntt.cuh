@@ -43,7 +43,7 @@ struct Ntt2 {
     __host__ __device__ static constexpr int tw_off(int s) { return s == 0 ? 0 : LINES * ((1 << s) + s - 2); }
     static constexpr int TWB = LINES * ((1 << B) + B - 2);  // = tw_off(B) entries
     static constexpr int SMEM_C = (LINES * R1 + 2 * R1) * 8;
-    static constexpr int SMEM_B = (LINES * PITCH + 2 * TWB) * 8;
+    static constexpr int SMEM_B = (2 * LINES * PITCH + 2 * TWB) * 8;  // 2 tile buffers + twiddles
 };
 
 // Ampere-style async global->smem copies (LDGSTS): the tile and twiddle loads
@@ -109,9 +109,11 @@ __device__ __forceinline__ void line_pass(u64* s, u64 q, Addr addr, Tw tw) {
 #pragma unroll
                 for (int k = 0; k < E; ++k) {
                     if (k & h) continue;
+                    // no correction: y < 2q, so each stage adds < 2q to the bound;
+                    // a whole forward transform from < q stays < 31q < 2^64 for
+                    // q < 2^58 (enforced by RnsParams) and is reduced once at the end
                     const ulonglong2 w = tw(S0L + u, l, (blk << u) + (k >> (R - u)));
-                    u64 x = v[k];
-                    x = x >= two_q ? x - two_q : x;
+                    const u64 x = v[k];
                     const u64 y = shoup_lazy(v[k + h], w.x, w.y, q);
                     v[k] = x + y;
                     v[k + h] = x - y + two_q;

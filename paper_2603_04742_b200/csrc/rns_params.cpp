@@ -134,8 +134,9 @@ RnsParams::RnsParams(const RnsConfig& c) : cfg(c), host{} {
     if (c.logn < 4 || c.logn > 15) throw std::invalid_argument("logn must be in [4, 15]");
     if (c.L < 1 || c.L > MAXL || c.K < 1 || c.K > MAXL || c.alpha < 1 || c.alpha > c.L)
         throw std::invalid_argument("prime counts out of range");
-    if (c.qbits < 30 || c.qbits > 60 || c.pbits < 30 || c.pbits > 60)
-        throw std::invalid_argument("prime bit sizes must be in [30, 60]");
+    if (c.qbits < 30 || c.qbits > 58 || c.pbits < 30 || c.pbits > 58)
+        // <= 58 bits: 64q headroom lets the forward NTT skip per-butterfly corrections
+        throw std::invalid_argument("prime bit sizes must be in [30, 58]");
     n = 1 << c.logn;
     S = n / 2;
     const u64 two_n = 2 * (u64)n;
@@ -149,7 +150,7 @@ RnsParams::RnsParams(const RnsConfig& c) : cfg(c), host{} {
     }
     pick_primes(c.qbits, two_n, c.L, primes);
     pick_primes(c.pbits, two_n, c.K, primes);
-    pick_primes(60, two_n, nB, primes);
+    pick_primes(58, two_n, nB, primes);
     primes.push_back(c.t);
     np = (int)primes.size();
     if (np > MAXP) throw std::invalid_argument("too many primes");

@@ -14,7 +14,7 @@ pytestmark = pytest.mark.gpu
 # (logn, overrides): small rings for speed plus the real C1/C2 parameter sets
 SETS = [
     (10, {}),
-    (11, dict(L=4, K=2, alpha=2, qbits=60, pbits=60)),
+    (11, dict(L=4, K=2, alpha=2, qbits=58, pbits=58)),
     (12, dict(L=5, K=2, alpha=2, qbits=58, pbits=58)),
     (13, {}),
 ]

@@ -11,7 +11,7 @@ import paper_2603_04742_b200 as pk
 T = 65537
 
 
-@pytest.fixture(scope="module", params=[(5, 3, 1, 1, 54), (6, 4, 2, 2, 60), (4, 8, 4, 4, 60)],
+@pytest.fixture(scope="module", params=[(5, 3, 1, 1, 54), (6, 4, 2, 2, 58), (4, 8, 4, 4, 58)],
                 ids=["n32_L3", "n64_L4", "n16_L8"])
 def orc(request):
     logn, L, K, a, qb = request.param
