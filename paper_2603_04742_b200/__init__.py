@@ -336,6 +336,28 @@ class Context:
         return bps.value
 
 
+def cloud_plan(ctx: Context, r_list, c_list, slice_ids, n_slices: int, a_cts, b_cts, graph: bool = False):
+    """Run the batched cloud phase on raw ciphertext handles (device level):
+    returns one result-ciphertext handle per slice (caller frees them)."""
+    n = len(r_list)
+    r = _u64(r_list)
+    c = _u64(c_list)
+    s = np.ascontiguousarray(np.asarray(slice_ids, dtype=np.uint32))
+    a, b = _u64(a_cts), _u64(b_cts)
+    out = ctx.alloc(n_slices)
+    h = C.c_void_p()
+    check(lib().spmvgpu_plan_create(ctx.h, n, _p(r, u64p), _p(c, u64p), _p(s, u32p), n_slices, _p(a, u64p),
+                                    _p(b, u64p), _p(out, u64p), C.byref(h)))
+    try:
+        if graph:
+            check(lib().spmvgpu_plan_capture(h))
+        check(lib().spmvgpu_plan_run(h))
+        ctx.sync()
+    finally:
+        lib().spmvgpu_plan_destroy(h)
+    return out
+
+
 @dataclass
 class Csr:
     rows: int

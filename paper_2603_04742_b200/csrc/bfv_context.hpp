@@ -115,8 +115,10 @@ public:
     // building blocks reused by the batched cloud plan (pointer arrays on device)
     void mul_relin_dev(const u64* const* A, const u64* const* B, u64* const* OUT, int items,
                        u64* T, u64* Z, u64* D2, u64* DX, u64* ACC, const u64* const* RLK);
+    // OUT = BASE + EXTRA + rot(SRC) (BASE / EXTRA per-item nullable)
     void rotate_dev(const u64* const* SRC, const u32* ginv, const u64* const* KEY,
-                    const u64* const* BASE, u64* const* OUT, int items, u64* DX, u64* ACC);
+                    const u64* const* BASE, u64* const* OUT, int items, u64* DX, u64* ACC,
+                    const u64* const* EXTRA = nullptr);
     void encode_masks(const std::vector<int>& ones_len, u64* MASKS);  // NTT form [m][L][N]
     NttJob job(const u64* src, u64* dst, int limbs, const std::vector<int>& pidx) const;
 

@@ -560,11 +560,12 @@ void launch_ks_inner(const DevConsts* dc, const RnsParams& P, const u64* DX,
     CSSC_CHECK_LAUNCH();
 }
 
-// E4 + fused adds
+// E4 + fused adds: out = BASE[item] + EXTRA[item] + phi_g(RSRC[item].c0) + ModDown(acc);
+// per-item BASE / EXTRA entries may be null
 template <int LT, int KT, int AT>
 __global__ void k_ks_moddown(const DevConsts* __restrict__ dc, const u64* __restrict__ ACC,
                              const u64* const* BASE, const u64* const* RSRC, const u32* ginv,
-                             u64* const* OUT) {
+                             u64* const* OUT, const u64* const* EXTRA) {
     const int n = dc->n, L = LT ? LT : dc->L, K = KT ? KT : dc->K, LK = L + K;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     const int item = blockIdx.y;
@@ -582,7 +583,10 @@ __global__ void k_ks_moddown(const DevConsts* __restrict__ dc, const u64* __rest
             y[kk] = shoup(acc[(size_t)(L + kk) * n + k], dc->phat_inv[kk], dc->phat_inv_sh[kk], pk);
         }
         u64* out = OUT[item] + (size_t)p * L * n;
-        const u64* base = BASE ? BASE[item] + (size_t)p * L * n : nullptr;
+        const u64* base = BASE ? BASE[item] : nullptr;
+        if (base) base += (size_t)p * L * n;
+        const u64* ex = EXTRA ? EXTRA[item] : nullptr;
+        if (ex) ex += (size_t)p * L * n;
         const u64* rs = (RSRC && p == 0) ? RSRC[item] : nullptr;
 #pragma unroll
         for (int j = 0; j < L; ++j) {
@@ -593,6 +597,7 @@ __global__ void k_ks_moddown(const DevConsts* __restrict__ dc, const u64* __rest
                 c = add_mod(c, shoup(y[kk], dc->phat_q[kk][j], dc->phat_q_sh[kk][j], q), q);
             u64 v = shoup(sub_mod(acc[(size_t)j * n + k], c, q), dc->Pinv_q[j], dc->Pinv_q_sh[j], q);
             if (base) v = add_mod(v, base[(size_t)j * n + k], q);
+            if (ex) v = add_mod(v, ex[(size_t)j * n + k], q);
             if (rs) {
                 const u64 r = rs[(size_t)j * n + ridx];
                 v = add_mod(v, neg ? neg_mod(r, q) : r, q);
@@ -604,10 +609,11 @@ __global__ void k_ks_moddown(const DevConsts* __restrict__ dc, const u64* __rest
 
 void launch_ks_moddown(const DevConsts* dc, const RnsParams& P, const u64* ACC,
                        const u64* const* BASE, const u64* const* RSRC, const u32* ginv,
-                       u64* const* OUT, int items, cudaStream_t st) {
+                       u64* const* OUT, int items, cudaStream_t st, const u64* const* EXTRA) {
     if (!items) return;
     dispatch_shape(P, [&](auto l_, auto k_, auto a_) {
-        k_ks_moddown<SHAPE_ARGS><<<ew_grid(P.n, items), EW_THREADS, 0, st>>>(dc, ACC, BASE, RSRC, ginv, OUT);
+        k_ks_moddown<SHAPE_ARGS><<<ew_grid(P.n, items), EW_THREADS, 0, st>>>(dc, ACC, BASE, RSRC, ginv, OUT,
+                                                                             EXTRA);
     });
     CSSC_CHECK_LAUNCH();
 }

@@ -63,7 +63,7 @@ void launch_ks_inner(const DevConsts* dc, const RnsParams& P, const u64* DX,
 //          + ModDown(ACC[p])
 void launch_ks_moddown(const DevConsts* dc, const RnsParams& P, const u64* ACC,
                        const u64* const* BASE, const u64* const* RSRC, const u32* ginv,
-                       u64* const* OUT, int items, cudaStream_t st);
+                       u64* const* OUT, int items, cudaStream_t st, const u64* const* EXTRA = nullptr);
 
 // masks / plaintext products
 void launch_mask_accum(const DevConsts* dc, const RnsParams& P, const u64* MT,
@@ -126,5 +126,6 @@ namespace cssc {
 // contiguous [item][L][N] polynomials at SRCC instead.  DX / ACC are workspaces.
 void launch_ks_fused(const DevConsts* dc, const RnsParams& P, const u64* const* SRC, const u64* SRCC,
                      int src_poly, const u32* ginv, const u64* const* KEY, const u64* const* BASE,
-                     const u64* const* RSRC, u64* const* OUT, u64* DX, u64* ACC, int items, cudaStream_t st);
+                     const u64* const* RSRC, u64* const* OUT, u64* DX, u64* ACC, int items, cudaStream_t st,
+                     const u64* const* EXTRA = nullptr);
 }  // namespace cssc

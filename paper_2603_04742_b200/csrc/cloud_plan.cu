@@ -1,4 +1,17 @@
 // cloud_plan.cu -- see cloud_plan.hpp.
+//
+// Level structure of the rotate-and-add trees.  rotation_schedule(r, c)
+// (aggregate.cpp:19-34) interleaves "doubling" steps D_k (rotate the running
+// accumulator) with "odd" steps O_k (rotate the ORIGINAL product, then add).
+// An odd step's rotation does not depend on the accumulator, so the plan
+// hoists every O_k into level 0, next to D_1, which also rotates the product.
+// Its result RP_k is added where the reference adds it: right after D_k.
+//   * k >= 2: the add is fused into the ModDown of the level computing D_k,
+//     as an extra addend;
+//   * k == 1: one elementwise add after level 0.
+// The tree depth drops from numBits + popcount - 2 launches to numBits - 1.
+// The ciphertexts are identical, because every rotation and addition is an
+// exact function of its inputs, and the op ledger is unchanged.
 #include "cloud_plan.hpp"
 
 #include <algorithm>
@@ -24,6 +37,36 @@ T* CloudPlan::put(const std::vector<T>& v) {
     return reinterpret_cast<T*>(arena_.as<unsigned char>() + off);
 }
 
+namespace {
+
+u32 inverse_galois(u32 g, int n) {
+    const u64 two_n = 2 * (u64)n;
+    u64 inv = 1, b = g;
+    for (u64 e = (u64)n - 1; e; e >>= 1) {  // g^(N-1) = g^-1 in (Z/2N)^*
+        if (e & 1) inv = inv * b % two_n;
+        b = b * b % two_n;
+    }
+    return (u32)inv;
+}
+
+struct Tree {
+    std::vector<u64> dbl;                  // doubling offsets D_1..D_m
+    std::vector<std::pair<int, u64>> odd;  // (k, offset): O_k follows D_k
+};
+
+Tree split_schedule(const std::vector<spmv::RotStep>& steps) {
+    Tree t;
+    for (const spmv::RotStep& s : steps) {
+        if (s.from_accumulator)
+            t.dbl.push_back(s.offset);
+        else
+            t.odd.emplace_back((int)t.dbl.size(), s.offset);
+    }
+    return t;
+}
+
+}  // namespace
+
 CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
                      const std::vector<uint64_t>& c, const std::vector<uint32_t>& slice,
                      int n_slices, const std::vector<const u64*>& a,
@@ -37,36 +80,43 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
     const size_t ctw = ctx.ct_words();
     const int L = P.cfg.L, LK = L + P.cfg.K, M = L + P.nB;
 
-    std::vector<std::vector<spmv::RotStep>> steps(n);
+    std::vector<Tree> trees(n);
+    size_t n_rot = 0, n_odd = 0;
     for (int i = 0; i < n; ++i) {
         if (r[i] * c[i] > (uint64_t)P.S) throw std::length_error("plan: chunk exceeds slot count");
         if (slice[i] >= (uint32_t)ns_) throw std::invalid_argument("plan: slice id out of range");
-        steps[i] = spmv::rotation_schedule(r[i], c[i]);
+        const auto steps = spmv::rotation_schedule(r[i], c[i]);
+        trees[i] = split_schedule(steps);
+        n_rot += steps.size();
+        n_odd += trees[i].odd.size();
     }
+    // chunks with more doubling levels first: level l is a prefix of the items
     std::vector<int> order(n);
     std::iota(order.begin(), order.end(), 0);
     std::stable_sort(order.begin(), order.end(),
-                     [&](int x, int y) { return steps[x].size() > steps[y].size(); });
-    const int depth = n ? (int)steps[order[0]].size() : 0;
-    // upper bound of all plan arrays (8-byte entries) plus 16-byte alignment slack
-    arena_ = DevBuf(&ctx.pool(), 8 * ((size_t)(8 + 5 * depth) * std::max(n, 1) + 2 * (size_t)ns_ + 8) +
-                                     16 * (size_t)(5 * depth + 16));
+                     [&](int x, int y) { return trees[x].dbl.size() > trees[y].dbl.size(); });
+    const int depth = n ? (int)trees[order[0]].dbl.size() : 0;
 
+    arena_ = DevBuf(&ctx.pool(), 8 * ((size_t)(10 + 6 * std::max(depth, 1)) * std::max(n, 1) + 7 * n_odd +
+                                      2 * (size_t)ns_ + 8) +
+                                     16 * (size_t)(6 * depth + 24));
     prod_ = DevBuf(&ctx.pool(), sizeof(u64) * ctw * std::max(n, 1));
     if (depth >= 1) acc0_ = DevBuf(&ctx.pool(), sizeof(u64) * ctw * n);
     if (depth >= 2) acc1_ = DevBuf(&ctx.pool(), sizeof(u64) * ctw * n);
+    if (n_odd) rp_ = DevBuf(&ctx.pool(), sizeof(u64) * ctw * n_odd);
     T_ = DevBuf(&ctx.pool(), sizeof(u64) * std::max<size_t>(1, n) * ctx.mul_T_words());
     Z_ = DevBuf(&ctx.pool(), sizeof(u64) * std::max<size_t>(1, n) * ctx.mul_Z_words());
     D2_ = DevBuf(&ctx.pool(), sizeof(u64) * std::max<size_t>(1, n) * ctx.poly_words());
-    DX_ = DevBuf(&ctx.pool(), sizeof(u64) * std::max<size_t>(1, n) * ctx.dx_words());
-    ACC_ = DevBuf(&ctx.pool(), sizeof(u64) * std::max<size_t>(1, n) * ctx.ksacc_words());
+    const size_t ks_items = std::max<size_t>(1, (size_t)n + n_odd);
+    DX_ = DevBuf(&ctx.pool(), sizeof(u64) * ks_items * ctx.dx_words());
+    ACC_ = DevBuf(&ctx.pool(), sizeof(u64) * ks_items * ctx.ksacc_words());
     MT_ = DevBuf(&ctx.pool(), sizeof(u64) * std::max<size_t>(1, n) * ctw);
 
     auto prod_at = [&](int k) { return prod_.words() + (size_t)k * ctw; };
     auto acc_at = [&](int which, int k) {
         return (which == 0 ? acc0_.words() : acc1_.words()) + (size_t)k * ctw;
     };
-    auto acc_after = [&](int k, int done) -> u64* {  // accumulator after `done` steps
+    auto acc_after = [&](int k, int done) -> u64* {  // accumulator after `done` doubling levels
         if (done == 0) return prod_at(k);
         return acc_at((done - 1) % 2, k);
     };
@@ -83,57 +133,90 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
     PROD_ = put(vp);
     RLK_ = put(rlk);
 
+    const bool fused = ctx.fused_key_switch();
     const u64 C = sizeof(u64) * ctw, KEY = sizeof(u64) * ctx.ksk_words(),
               PT = sizeof(u64) * ctx.poly_words();
     stats_.chunks = n;
     stats_.slices = ns_;
     stats_.levels = depth;
+    stats_.rotations = n_rot;
     stats_.hbm_bytes = n ? (u64)n * 3 * C + KEY : 0;
     stats_.key_bytes = n ? KEY : 0;
-    const bool fused = ctx.fused_key_switch();
     stats_.kernels = n ? (fused ? 11 : 14) : 0;  // each NTT is two kernels (column, block phase)
-    stats_.limb_ntts = (u64)n * (7 * M + P.dnum * LK + 2 * LK);
+    stats_.limb_ntts = (u64)n * (7 * M + P.dnum * LK + 2 * LK) + (u64)n_rot * (P.dnum * LK + 2 * LK);
 
+    // where each hoisted rotation lands: rp slot per (chunk item k, odd step)
+    std::vector<std::map<int, u64*>> rp_after(n);  // k -> (D index -> RP ct)
     std::set<u32> all_keys;
+    auto key_of = [&](u64 offset, std::set<u32>& lvl, u32& gi) {
+        const u32 g = galois_element((int64_t)offset, P.n);
+        lvl.insert(g);
+        all_keys.insert(g);
+        gi = inverse_galois(g, P.n);
+        return ctx.galois_key(g);
+    };
+    std::vector<const u64*> pre_a, pre_b;
+    std::vector<u64*> pre_out;
     for (int l = 0; l < depth; ++l) {
-        int items = 0;
-        while (items < n && (int)steps[order[items]].size() > l) ++items;
-        std::vector<const u64*> src(items), base(items), key(items);
-        std::vector<u64*> o(items);
-        std::vector<u32> gi(items);
+        std::vector<const u64*> src, base, key, extra;
+        std::vector<u64*> o;
+        std::vector<u32> gi;
         std::set<u32> lvl_keys;
-        for (int k = 0; k < items; ++k) {
-            const spmv::RotStep& s = steps[order[k]][l];
+        size_t odd_slot = 0;
+        for (int k = 0; k < n && (int)trees[order[k]].dbl.size() > l; ++k) {
+            const Tree& t = trees[order[k]];
             u64* cur = acc_after(k, l);
-            base[k] = cur;
-            src[k] = s.from_accumulator ? cur : prod_at(k);
-            o[k] = acc_at(l % 2, k);
-            const u32 g = galois_element((int64_t)s.offset, P.n);
-            key[k] = ctx.galois_key(g);
-            // inverse Galois element in (Z/2N)^*: g^(N-1)
-            u64 inv = 1, bb = g;
-            const u64 two_n = 2 * (u64)P.n;
-            for (u64 e = (u64)P.n - 1; e; e >>= 1) {
-                if (e & 1) inv = inv * bb % two_n;
-                bb = bb * bb % two_n;
+            u32 g;
+            key.push_back(key_of(t.dbl[l], lvl_keys, g));
+            gi.push_back(g);
+            src.push_back(cur);
+            base.push_back(cur);
+            o.push_back(acc_at(l % 2, k));
+            extra.push_back(nullptr);
+            if (l >= 1) {  // fuse RP of the odd step that follows D_{l+1}
+                auto it = rp_after[k].find(l + 1);
+                if (it != rp_after[k].end()) extra.back() = it->second;
             }
-            gi[k] = (u32)inv;
-            lvl_keys.insert(g);
-            all_keys.insert(g);
+        }
+        if (l == 0) {  // hoisted odd steps: rot(prod) of every chunk, same launch
+            for (int k = 0; k < n; ++k) {
+                for (const auto& [after, off] : trees[order[k]].odd) {
+                    u64* slot = rp_.words() + (odd_slot++) * ctw;
+                    u32 g;
+                    key.push_back(key_of(off, lvl_keys, g));
+                    gi.push_back(g);
+                    src.push_back(prod_at(k));
+                    base.push_back(nullptr);
+                    extra.push_back(nullptr);
+                    o.push_back(slot);
+                    rp_after[k][after] = slot;
+                    if (after == 1) {  // follows D_1: elementwise add once level 0 is done
+                        pre_a.push_back(acc_after(k, 1));
+                        pre_b.push_back(slot);
+                        pre_out.push_back(acc_after(k, 1));
+                    }
+                }
+            }
         }
         Level lv;
-        lv.items = items;
+        lv.items = (int)o.size();
         lv.src = put(src);
         lv.base = put(base);
         lv.out = put(o);
         lv.key = put(key);
         lv.ginv = put(gi);
+        lv.extra = put(extra);
         levels_.push_back(lv);
-        stats_.rotations += items;
-        stats_.hbm_bytes += (u64)items * 3 * C + lvl_keys.size() * KEY;
+        stats_.hbm_bytes += (u64)lv.items * 3 * C + lvl_keys.size() * KEY;
         stats_.key_bytes += lvl_keys.size() * KEY;
         stats_.kernels += fused ? 4 : 7;
-        stats_.limb_ntts += (u64)items * (P.dnum * LK + 2 * LK);
+        if (l == 0 && !pre_out.empty()) {
+            add_items_ = (int)pre_out.size();
+            ADD_A_ = put(pre_a);
+            ADD_B_ = put(pre_b);
+            ADD_OUT_ = put(pre_out);
+            stats_.kernels += 1;
+        }
     }
     stats_.distinct_keys = all_keys.size();
 
@@ -150,7 +233,7 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
             ones.push_back((int)rr);
         }
         item_mask[k] = it->second;
-        fin[k] = acc_after(k, (int)steps[order[k]].size());
+        fin[k] = acc_after(k, (int)trees[order[k]].dbl.size());
     }
     n_masks_ = (int)ones.size();
     MASKS_ = DevBuf(&ctx.pool(), sizeof(u64) * std::max<size_t>(1, n_masks_) * ctx.poly_words());
@@ -190,9 +273,13 @@ void CloudPlan::record() {
     cudaStream_t st = ctx_.stream();
     ctx_.mul_relin_dev(A_, B_, PROD_, n_, T_.words(), Z_.words(), D2_.words(), DX_.words(),
                        ACC_.words(), RLK_);
-    for (const Level& lv : levels_)
-        ctx_.rotate_dev(lv.src, lv.ginv, lv.key, lv.base, lv.out, lv.items, DX_.words(),
-                        ACC_.words());
+    for (size_t l = 0; l < levels_.size(); ++l) {
+        const Level& lv = levels_[l];
+        ctx_.rotate_dev(lv.src, lv.ginv, lv.key, lv.base, lv.out, lv.items, DX_.words(), ACC_.words(),
+                        lv.extra);
+        if (l == 0 && add_items_)
+            launch_add(ctx_.dconsts(), P, ADD_A_, ADD_B_, ADD_OUT_, add_items_, st);
+    }
     std::vector<int> qidx(L);
     std::iota(qidx.begin(), qidx.end(), 0);
     NttJob fwd = ctx_.job(nullptr, MT_.words(), 2 * L, qidx);

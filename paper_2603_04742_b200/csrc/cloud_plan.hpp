@@ -4,11 +4,13 @@
 // multiply -> intra_chunk_sum -> inter_chunk_sum) over every chunk of every
 // slice (and every matrix of a batch) into a fixed launch sequence:
 //   1. one batched ct x ct multiply + relinearisation over all chunks;
-//   2. level l = 0..depth-1 of the rotate-and-add trees: every chunk whose
-//      rotation_schedule (aggregate.cpp:19-34) has > l steps does
-//      acc <- acc + rot(step.from_accumulator ? acc : product, offset)
-//      in one fused key-switch launch group (chunks are ordered by descending
-//      schedule length so level l is a prefix of the item list);
+//   2. level l = 0..depth-1 of the rotate-and-add trees (rotation_schedule,
+//      aggregate.cpp:19-34): every chunk with more than l doubling steps does
+//      acc <- acc + rot(acc, offset) [+ a hoisted odd-step rotation of the
+//      product] in one fused key-switch launch group; level 0 also rotates the
+//      products for all odd steps (they never depend on the accumulator), so
+//      the depth is numBits(c) - 1 instead of numBits(c) + popcount(c) - 2
+//      (chunks are ordered by descending depth: level l is an item prefix);
 //   3. one masked, segmented accumulation of all folded chunks into one
 //      result ciphertext per slice (inter_chunk_sum, aggregate.cpp:55-74).
 // The sequence is fixed at plan time and can be captured as a CUDA graph.
@@ -47,7 +49,7 @@ private:
     GpuContext& ctx_;
     int n_ = 0, ns_ = 0;
     PlanStats stats_;
-    DevBuf prod_, acc0_, acc1_;
+    DevBuf prod_, acc0_, acc1_, rp_;  // rp_: hoisted odd-step rotations of the products
     DevBuf T_, Z_, D2_, DX_, ACC_, MT_, MASKS_;
     DevBuf arena_;                        // device pointer / index arrays (one block)
     std::vector<unsigned char> stage_;    // host staging of arena_
@@ -63,8 +65,13 @@ private:
         u64* const* out;
         const u64* const* key;
         const u32* ginv;
+        const u64* const* extra;  // fused add of a hoisted odd-step rotation (nullable)
     };
     std::vector<Level> levels_;
+    int add_items_ = 0;  // odd steps right after D_1: added once level 0 is done
+    const u64* const* ADD_A_ = nullptr;
+    const u64* const* ADD_B_ = nullptr;
+    u64* const* ADD_OUT_ = nullptr;
     const u64* const* FINAL_ = nullptr;
     u64* const* OUT_ = nullptr;
     const int* slice_off_ = nullptr;

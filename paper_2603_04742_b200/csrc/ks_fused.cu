@@ -225,7 +225,8 @@ static void ks_dispatch_shape(const RnsParams& P, F&& f) {
 template <int LOGN, int LT, int KT, int AT>
 static void ks_fused_t(const DevConsts* dc, const RnsParams& P, const u64* const* SRC, const u64* SRCC,
                        int src_poly, const u32* ginv, const u64* const* KEY, const u64* const* BASE,
-                       const u64* const* RSRC, u64* const* OUT, u64* DX, u64* ACC, int items, cudaStream_t st) {
+                       const u64* const* RSRC, u64* const* OUT, u64* DX, u64* ACC, int items, cudaStream_t st,
+                       const u64* const* EXTRA) {
     using G = Ntt2<LOGN>;
     const int L = P.cfg.L, K = P.cfg.K, LK = L + K, dnum = P.dnum;
     const int smem1 = G::SMEM_C;
@@ -247,30 +248,32 @@ static void ks_fused_t(const DevConsts* dc, const RnsParams& P, const u64* const
     j.dst = ACC;
     j.limbs = 2 * LK;
     launch_ntt_phase(dc, LOGN, /*inverse=*/true, /*cols=*/true, j, items, st);
-    launch_ks_moddown(dc, P, ACC, BASE, RSRC, ginv, OUT, items, st);
+    launch_ks_moddown(dc, P, ACC, BASE, RSRC, ginv, OUT, items, st, EXTRA);
 }
 
 template <int LOGN>
 static void ks_fused_logn(const DevConsts* dc, const RnsParams& P, const u64* const* SRC, const u64* SRCC,
                           int src_poly, const u32* ginv, const u64* const* KEY, const u64* const* BASE,
-                          const u64* const* RSRC, u64* const* OUT, u64* DX, u64* ACC, int items, cudaStream_t st) {
+                          const u64* const* RSRC, u64* const* OUT, u64* DX, u64* ACC, int items, cudaStream_t st,
+                       const u64* const* EXTRA) {
     ks_dispatch_shape(P, [&](auto l_, auto k_, auto a_) {
         ks_fused_t<LOGN, decltype(l_)::value, decltype(k_)::value, decltype(a_)::value>(
-            dc, P, SRC, SRCC, src_poly, ginv, KEY, BASE, RSRC, OUT, DX, ACC, items, st);
+            dc, P, SRC, SRCC, src_poly, ginv, KEY, BASE, RSRC, OUT, DX, ACC, items, st, EXTRA);
     });
 }
 
 void launch_ks_fused(const DevConsts* dc, const RnsParams& P, const u64* const* SRC, const u64* SRCC,
                      int src_poly, const u32* ginv, const u64* const* KEY, const u64* const* BASE,
-                     const u64* const* RSRC, u64* const* OUT, u64* DX, u64* ACC, int items, cudaStream_t st) {
+                     const u64* const* RSRC, u64* const* OUT, u64* DX, u64* ACC, int items, cudaStream_t st,
+                       const u64* const* EXTRA) {
     if (!items) return;
     switch (P.cfg.logn) {
-        case 10: ks_fused_logn<10>(dc, P, SRC, SRCC, src_poly, ginv, KEY, BASE, RSRC, OUT, DX, ACC, items, st); break;
-        case 11: ks_fused_logn<11>(dc, P, SRC, SRCC, src_poly, ginv, KEY, BASE, RSRC, OUT, DX, ACC, items, st); break;
-        case 12: ks_fused_logn<12>(dc, P, SRC, SRCC, src_poly, ginv, KEY, BASE, RSRC, OUT, DX, ACC, items, st); break;
-        case 13: ks_fused_logn<13>(dc, P, SRC, SRCC, src_poly, ginv, KEY, BASE, RSRC, OUT, DX, ACC, items, st); break;
-        case 14: ks_fused_logn<14>(dc, P, SRC, SRCC, src_poly, ginv, KEY, BASE, RSRC, OUT, DX, ACC, items, st); break;
-        case 15: ks_fused_logn<15>(dc, P, SRC, SRCC, src_poly, ginv, KEY, BASE, RSRC, OUT, DX, ACC, items, st); break;
+        case 10: ks_fused_logn<10>(dc, P, SRC, SRCC, src_poly, ginv, KEY, BASE, RSRC, OUT, DX, ACC, items, st, EXTRA); break;
+        case 11: ks_fused_logn<11>(dc, P, SRC, SRCC, src_poly, ginv, KEY, BASE, RSRC, OUT, DX, ACC, items, st, EXTRA); break;
+        case 12: ks_fused_logn<12>(dc, P, SRC, SRCC, src_poly, ginv, KEY, BASE, RSRC, OUT, DX, ACC, items, st, EXTRA); break;
+        case 13: ks_fused_logn<13>(dc, P, SRC, SRCC, src_poly, ginv, KEY, BASE, RSRC, OUT, DX, ACC, items, st, EXTRA); break;
+        case 14: ks_fused_logn<14>(dc, P, SRC, SRCC, src_poly, ginv, KEY, BASE, RSRC, OUT, DX, ACC, items, st, EXTRA); break;
+        case 15: ks_fused_logn<15>(dc, P, SRC, SRCC, src_poly, ginv, KEY, BASE, RSRC, OUT, DX, ACC, items, st, EXTRA); break;
         default: throw std::invalid_argument("key switch: unsupported logn");
     }
 }

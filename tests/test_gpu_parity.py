@@ -121,3 +121,33 @@ def test_fused_and_unfused_key_switch_agree():
         hr = ctx.rotate_add(hp, hp, [129])
         outs[fused] = (ctx.download(int(hp[0])), ctx.download(int(hr[0])))
     assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+
+
+@pytest.mark.parametrize("graph", [False, True])
+def test_cloud_plan_words_match_oracle(graph):
+    """The whole batched cloud phase (mult+relin, hoisted rotate-and-add trees,
+    masked per-slice accumulation) equals the oracle's op-by-op evaluation of
+    the reference algorithm (protocol.cpp:121-140) word for word (P5)."""
+    ctx = pk.Context(logn=10, seed=9)
+    orc = BfvOracle.like(ctx)
+    S = ctx.slots
+    shapes = [(7, 13), (3, 6), (5, 7), (11, 2), (1, 64), (40, 12), (2, 1), (8, 3)]
+    slices = [0, 0, 1, 1, 1, 0, 2, 2]
+    rng = np.random.default_rng(5)
+    vals_a = [rng.integers(-8, 9, r * c) for r, c in shapes]
+    vals_b = [rng.integers(-8, 9, r * c) for r, c in shapes]
+    sa = [1000 + i for i in range(len(shapes))]
+    sb = [2000 + i for i in range(len(shapes))]
+    ha, hb = ctx.encrypt(vals_a, sa), ctx.encrypt(vals_b, sb)
+    out = pk.cloud_plan(ctx, [r for r, _ in shapes], [c for _, c in shapes], slices, 3, ha, hb, graph=graph)
+    want = [None] * 3
+    for i, (r, c) in enumerate(shapes):
+        prod = orc.mul_relin(orc.encrypt(vals_a[i], sa[i]), orc.encrypt(vals_b[i], sb[i]))
+        acc = prod
+        for off, from_acc in pk.rotation_schedule(r, c):
+            acc = orc.add(acc, orc.rotate(acc if from_acc else prod, off))
+        part = orc.mul_plain(acc, np.ones(r, np.int64))
+        want[slices[i]] = part if want[slices[i]] is None else orc.add(want[slices[i]], part)
+    for s in range(3):
+        assert np.array_equal(ctx.download(int(out[s])), want[s]), s
+    ctx.free(np.concatenate([ha, hb, out]))
