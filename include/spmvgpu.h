@@ -69,7 +69,9 @@ int spmvgpu_ctx_sizes(const spmvgpu_ctx* c, uint64_t* n, uint64_t* slots, uint64
                       uint64_t* ksk_words, int* dnum);
 int spmvgpu_sync(spmvgpu_ctx* c);
 /* tuning switches: "fused_key_switch" (1 = 3-kernel fused key switch, default;
- * 0 = the 7-launch ModUp / NTT / inner product / INTT / ModDown pipeline) */
+ * 0 = the 7-launch ModUp / NTT / inner product / INTT / ModDown pipeline);
+ * "plan_cache" (how many cloud plans, keyed by chunk shapes, cssc_spmv_* and
+ * cssc_job_* keep for reuse with their buffers and CUDA graph; default 4, 0 = off) */
 int spmvgpu_set_option(spmvgpu_ctx* c, const char* name, int64_t value);
 /* opaque CUDA stream the context works on (cudaStream_t) */
 void* spmvgpu_stream(spmvgpu_ctx* c);

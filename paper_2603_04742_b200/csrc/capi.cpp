@@ -3,7 +3,9 @@
 // protocol front door (cssc_*) wraps the host C++ spmv layer, which itself
 // talks to the device only through spmvgpu_*.  No exception crosses the ABI.
 #include <cstring>
+#include <list>
 #include <memory>
+#include <mutex>
 #include <new>
 #include <stdexcept>
 #include <string>
@@ -11,6 +13,7 @@
 #include "bfv_context.hpp"
 #include "cloud_plan.hpp"
 #include "host/batched_spmv.hpp"
+#include "host/plan_cache.hpp"
 #include "spmv/gpu_backend.hpp"
 #include "spmv/synthetic.hpp"
 #include "spmvgpu.h"
@@ -19,6 +22,11 @@ struct spmvgpu_ctx {
     std::unique_ptr<cssc::GpuContext> g;
     spmvgpu_params p;
     spmv::HeParams hp;
+    // plan cache (host/plan_cache.hpp), most recently returned first
+    std::mutex plans_mu;
+    std::list<spmv::detail::PlanLease> plans;
+    std::size_t plan_capacity = 4;
+    ~spmvgpu_ctx();
 };
 
 struct spmvgpu_plan {
@@ -134,6 +142,50 @@ void fill_result(const spmv::SpmvResult& r, int64_t* values, cssc_result* res, c
 
 }  // namespace
 
+namespace spmv::detail {
+
+bool plan_cache_take(spmvgpu_ctx* ctx, const std::vector<std::uint64_t>& key, PlanLease& out) {
+    std::lock_guard<std::mutex> g(ctx->plans_mu);
+    for (auto it = ctx->plans.begin(); it != ctx->plans.end(); ++it)
+        if (it->key == key) {
+            out = std::move(*it);
+            ctx->plans.erase(it);
+            return true;
+        }
+    return false;
+}
+
+void plan_lease_free(spmvgpu_ctx* ctx, PlanLease& l) {
+    if (l.plan) spmvgpu_plan_destroy(l.plan);
+    l.plan = nullptr;
+    for (auto* v : {&l.a, &l.b, &l.out}) {
+        if (!v->empty()) spmvgpu_ct_free(ctx, v->data(), v->size());
+        v->clear();
+    }
+    l.key.clear();
+}
+
+void plan_cache_give(spmvgpu_ctx* ctx, PlanLease&& lease) {
+    std::list<PlanLease> evicted;
+    {
+        std::lock_guard<std::mutex> g(ctx->plans_mu);
+        ctx->plans.push_front(std::move(lease));
+        while (ctx->plans.size() > ctx->plan_capacity) {
+            evicted.splice(evicted.end(), ctx->plans, std::prev(ctx->plans.end()));
+        }
+    }
+    for (auto& l : evicted) plan_lease_free(ctx, l);
+}
+
+}  // namespace spmv::detail
+
+spmvgpu_ctx::~spmvgpu_ctx() {
+    if (g) {
+        for (auto& l : plans) spmv::detail::plan_lease_free(this, l);
+        plans.clear();
+    }
+}
+
 extern "C" {
 
 const char* spmvgpu_last_error(void) { return g_err.c_str(); }
@@ -185,6 +237,7 @@ int spmvgpu_ctx_create(const spmvgpu_params* p, spmvgpu_ctx** out) {
 
 void spmvgpu_ctx_destroy(spmvgpu_ctx* c) { delete c; }
 
+
 int spmvgpu_ctx_primes(const spmvgpu_ctx* c, uint64_t* primes, int cap, int* count) {
     return guard([&] {
         const auto& P = const_cast<spmvgpu_ctx*>(c)->g->params();
@@ -209,8 +262,19 @@ int spmvgpu_sync(spmvgpu_ctx* c) { return guard([&] { G(c).synchronize(); }); }
 int spmvgpu_set_option(spmvgpu_ctx* c, const char* name, int64_t value) {
     return guard([&] {
         const std::string n = name ? name : "";
-        if (n == "fused_key_switch")
+        if (n == "fused_key_switch") {
             G(c).set_fused_key_switch(value != 0);
+        } else if (n == "plan_cache") {
+            if (value < 0) throw std::invalid_argument("plan_cache: capacity must be >= 0");
+            std::list<spmv::detail::PlanLease> evicted;
+            {
+                std::lock_guard<std::mutex> g(c->plans_mu);
+                c->plan_capacity = static_cast<std::size_t>(value);
+                while (c->plans.size() > c->plan_capacity)
+                    evicted.splice(evicted.end(), c->plans, std::prev(c->plans.end()));
+            }
+            for (auto& l : evicted) spmv::detail::plan_lease_free(c, l);
+        }
         else
             throw std::invalid_argument("unknown option: " + n);
     });

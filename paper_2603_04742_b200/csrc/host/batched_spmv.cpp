@@ -50,8 +50,7 @@ BatchedSpmv::BatchedSpmv(spmvgpu_ctx* ctx, const HeParams& hp, std::span<const C
                 c_.push_back(s.cs.c_list[i]);
             }
             if (s.cs.n_ct()) {
-                s.result = static_cast<int>(out_.size());
-                out_.push_back(0);
+                s.result = static_cast<int>(n_out_++);
             }
             for (std::size_t i = 0; i < s.cs.n_ct(); ++i) slice_id_.push_back(static_cast<std::uint32_t>(s.result));
             for (const auto& seg : rv.segments) b_vals.insert(b_vals.end(), seg.begin(), seg.end());
@@ -70,55 +69,71 @@ BatchedSpmv::BatchedSpmv(spmvgpu_ctx* ctx, const HeParams& hp, std::span<const C
                 ++k;
             }
     vals_.insert(vals_.end(), b_vals.begin(), b_vals.end());
-    a_.assign(n, 0);
-    b_.assign(n, 0);
-    if (n) {
-        check_status(spmvgpu_ct_alloc(ctx_, n, a_.data()));
-        check_status(spmvgpu_ct_alloc(ctx_, n, b_.data()));
+    if (!n) return;
+    // the cloud's view of the job: chunk shapes and slice ids (ChunkShapeMeta)
+    std::vector<std::uint64_t> key{n, n_out_};
+    key.insert(key.end(), r_.begin(), r_.end());
+    key.insert(key.end(), c_.begin(), c_.end());
+    key.insert(key.end(), slice_id_.begin(), slice_id_.end());
+    if (plan_cache_take(ctx_, key, lease_)) return;
+    lease_.key = std::move(key);
+    lease_.a.assign(n, 0);
+    lease_.b.assign(n, 0);
+    lease_.out.assign(n_out_, 0);
+    try {
+        check_status(spmvgpu_ct_alloc(ctx_, n, lease_.a.data()));
+        check_status(spmvgpu_ct_alloc(ctx_, n, lease_.b.data()));
+        check_status(spmvgpu_ct_alloc(ctx_, n_out_, lease_.out.data()));
+    } catch (...) {
+        plan_lease_free(ctx_, lease_);
+        throw;
     }
-    if (!out_.empty()) check_status(spmvgpu_ct_alloc(ctx_, out_.size(), out_.data()));
 }
 
 BatchedSpmv::~BatchedSpmv() {
-    if (plan_) spmvgpu_plan_destroy(plan_);
-    if (!a_.empty()) spmvgpu_ct_free(ctx_, a_.data(), a_.size());
-    if (!b_.empty()) spmvgpu_ct_free(ctx_, b_.data(), b_.size());
-    if (!out_.empty()) spmvgpu_ct_free(ctx_, out_.data(), out_.size());
+    if (lease_.key.empty()) return;
+    if (done_)
+        plan_cache_give(ctx_, std::move(lease_));
+    else  // an evaluation that did not complete: do not keep its buffers
+        plan_lease_free(ctx_, lease_);
 }
 
 void BatchedSpmv::encrypt() {
     const std::size_t n = r_.size();
     if (!n) return;
-    std::vector<spmvgpu_ct> all(a_);
-    all.insert(all.end(), b_.begin(), b_.end());
+    std::vector<spmvgpu_ct> all(lease_.a);
+    all.insert(all.end(), lease_.b.begin(), lease_.b.end());
     check_status(spmvgpu_encrypt(ctx_, vals_.data(), offs_.data(), nullptr, all.data(), 2 * n));
     h2d_ = sizeof(std::int64_t) * vals_.size() + sizeof(std::uint64_t) * offs_.size();
 }
 
 void BatchedSpmv::ensure_plan() {
-    if (plan_ || r_.empty()) return;
-    check_status(spmvgpu_plan_create(ctx_, r_.size(), r_.data(), c_.data(), slice_id_.data(), out_.size(),
-                                     a_.data(), b_.data(), out_.data(), &plan_));
+    if (lease_.plan || r_.empty()) return;
+    check_status(spmvgpu_plan_create(ctx_, r_.size(), r_.data(), c_.data(), slice_id_.data(), n_out_,
+                                     lease_.a.data(), lease_.b.data(), lease_.out.data(), &lease_.plan));
 }
 
 void BatchedSpmv::cloud(bool use_graph) {
     if (r_.empty()) return;
     ensure_plan();
-    if (use_graph && !graph_) {
-        check_status(spmvgpu_plan_capture(plan_));
-        graph_ = true;
+    // a plan seen before is worth a graph: capture on its second use
+    if ((use_graph || lease_.uses > 0) && !lease_.captured) {
+        check_status(spmvgpu_plan_capture(lease_.plan));
+        lease_.captured = true;
     }
-    check_status(spmvgpu_plan_run(plan_));
+    check_status(spmvgpu_plan_run(lease_.plan));
+    ++lease_.uses;
 }
 
 std::vector<SpmvResult> BatchedSpmv::finish() {
     const std::size_t S = hp_.slot_count;
-    std::vector<std::uint64_t> slots(out_.size() * S);
-    std::vector<std::int32_t> measured(out_.size(), 0);
-    if (!out_.empty())
-        check_status(spmvgpu_decrypt(ctx_, out_.data(), out_.size(), slots.data(), measured.data()));
+    std::vector<std::uint64_t> slots(n_out_ * S);
+    std::vector<std::int32_t> measured(n_out_, 0);
+    if (n_out_)
+        check_status(spmvgpu_decrypt(ctx_, lease_.out.data(), n_out_, slots.data(), measured.data()));
     else
         check_status(spmvgpu_sync(ctx_));
+    done_ = true;
     d2h_ = sizeof(std::uint64_t) * slots.size();
 
     const NoiseModel& nm = hp_.noise;

@@ -9,6 +9,7 @@
 #include <span>
 #include <vector>
 
+#include "host/plan_cache.hpp"
 #include "spmv/protocol.hpp"
 #include "spmvgpu.h"
 
@@ -27,7 +28,7 @@ public:
     void cloud(bool use_graph);   // enqueue the cloud plan (no host sync)
     std::vector<SpmvResult> finish();  // key holder: decrypt, unpermute, bookkeeping
 
-    spmvgpu_plan* plan() const { return plan_; }
+    spmvgpu_plan* plan() const { return lease_.plan; }
     std::uint64_t h2d_bytes() const { return h2d_; }
     std::uint64_t d2h_bytes() const { return d2h_; }
     std::size_t total_chunks() const { return r_.size(); }
@@ -52,9 +53,9 @@ private:
     std::vector<std::uint64_t> offs_;
     std::vector<std::uint64_t> r_, c_;
     std::vector<std::uint32_t> slice_id_;
-    std::vector<spmvgpu_ct> a_, b_, out_;
-    spmvgpu_plan* plan_ = nullptr;
-    bool graph_ = false;
+    std::size_t n_out_ = 0;
+    PlanLease lease_;
+    bool done_ = false;  // plan + ciphertext buffers, from / back to the context's plan cache
     std::uint64_t h2d_ = 0, d2h_ = 0;
 };
 

@@ -1,0 +1,34 @@
+// plan_cache.hpp -- per-context cache of cloud plans keyed by chunk shapes.
+//
+// A cloud plan (cloud_plan.hpp) depends only on the chunk shapes the cloud
+// receives as ChunkShapeMeta (protocol.cpp:113-116): every chunk's (h, k) and
+// the slice it belongs to.  Repeated evaluations over matrices with the same
+// sparsity structure reuse the plan, its ciphertext buffers and, from the
+// second use on, its captured CUDA graph.  Encryption still runs every call:
+// only the launch sequence and the buffers are reused, never a result.
+// Internal to the library (the C-ABI is unchanged); implemented in capi.cpp.
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+#include "spmvgpu.h"
+
+namespace spmv::detail {
+
+struct PlanLease {
+    std::vector<std::uint64_t> key;
+    std::vector<spmvgpu_ct> a, b, out;
+    spmvgpu_plan* plan = nullptr;
+    bool captured = false;
+    std::uint64_t uses = 0;
+};
+
+// Moves a cached lease for `key` into `out` and returns true, or returns false.
+bool plan_cache_take(spmvgpu_ctx* ctx, const std::vector<std::uint64_t>& key, PlanLease& out);
+// Hands a lease back (the cache owns it from now on and may evict it).
+void plan_cache_give(spmvgpu_ctx* ctx, PlanLease&& lease);
+// Frees a lease's plan and ciphertexts.
+void plan_lease_free(spmvgpu_ctx* ctx, PlanLease& lease);
+
+}  // namespace spmv::detail

@@ -113,6 +113,24 @@ def test_job_graph_replay(ctx10):
     assert st["chunks"] > 0 and st["limb_ntts_per_run"] > 0
 
 
+@pytest.mark.parametrize("capacity", [4, 1, 0])
+def test_plan_cache_reuse_with_new_values(capacity):
+    """Repeated calls over one sparsity structure reuse the cached plan (and its
+    graph from the second use); every call still encrypts its own values."""
+    ctx = pk.Context(logn=10, seed=5)
+    ctx.set_option("plan_cache", capacity)
+    rng = np.random.default_rng(capacity)
+    shapes = [pk.random_sparse_csr(70, 60, 400, 31, -8, 8), pk.random_sparse_csr(50, 90, 200, 32, -8, 8)]
+    for it in range(6):
+        base = shapes[it % 2] if it < 4 else shapes[0]
+        vals = rng.integers(1, 9, base.values.size) * rng.choice([-1, 1], base.values.size)
+        m = pk.Csr(base.rows, base.cols, base.row_ptrs, base.col_indices, vals.astype(np.int64))
+        v = rng.integers(-8, 9, base.cols).astype(np.int64)
+        got = pk.spmv_partitioned(ctx, m, v, ctx.slots)
+        assert_same(got, checker(m, v, ctx.slots, ctx.slots))
+    ctx.close()
+
+
 GOLDEN = __import__("json").loads(
     (__import__("pathlib").Path(__file__).parent / "golden" / "ref_cases.json").read_text())["cases"]
 
