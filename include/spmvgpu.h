@@ -95,6 +95,24 @@ int spmvgpu_ct_download(spmvgpu_ctx* c, spmvgpu_ct ct, uint64_t* words);
  * streams may be NULL) */
 int spmvgpu_encrypt(spmvgpu_ctx* c, const int64_t* vals, const uint64_t* offsets,
                     const uint64_t* streams, const spmvgpu_ct* out, size_t n);
+/* Client A + Client B fused on the device (replaces the host chain of
+ * reference sparse.cpp:79-117 csr_to_cssc, chunk.cpp:10-52 generate_chunks,
+ * reorg.cpp:10-34 reorg_vector and he.cpp encode/encrypt per chunk): scatters
+ * CSR entries straight into the CSSC chunk plaintexts and encrypts them.
+ *   col_indices/values: nnz entries (all matrices back to back);
+ *   vec: vec_len entries (all vectors back to back);
+ *   rows: n_rows x {nz_begin, len, pos, slice}: every non-empty row of every
+ *         slice, pos = its place in the slice's descending-length order;
+ *   slices: n_slices x {col_base, vec_base};
+ *   cols: n_cols x {chunk, k, h, 0}: aligned column j of a slice is record
+ *         col_base + j, slot k*h + pos of chunk `chunk` (height h).
+ * Entry j of a row lands in out[chunk] (value) and out[n_chunks + chunk]
+ * (vec[vec_base + col]); all other slots are 0.  Stream ids as for
+ * spmvgpu_encrypt with streams = NULL.  Every index is validated. */
+int spmvgpu_encrypt_cssc(spmvgpu_ctx* c, const int64_t* col_indices, const int64_t* values, uint64_t nnz,
+                         const int64_t* vec, uint64_t vec_len, const int32_t* rows, uint64_t n_rows,
+                         const int32_t* slices, uint64_t n_slices, const int32_t* cols, uint64_t n_cols,
+                         const spmvgpu_ct* out, size_t n_chunks);
 /* batched decrypt+decode: slots is n x S residues mod t; budgets = measured
  * invariant-noise budget (bits, saturates near 60) */
 int spmvgpu_decrypt(spmvgpu_ctx* c, const spmvgpu_ct* cts, size_t n, uint64_t* slots,

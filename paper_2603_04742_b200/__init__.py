@@ -86,6 +86,8 @@ _SIGS = {
     "spmvgpu_ct_upload": (C.c_int, [C.c_void_p, C.c_uint64, u64p]),
     "spmvgpu_ct_download": (C.c_int, [C.c_void_p, C.c_uint64, u64p]),
     "spmvgpu_encrypt": (C.c_int, [C.c_void_p, i64p, u64p, u64p, u64p, C.c_size_t]),
+    "spmvgpu_encrypt_cssc": (C.c_int, [C.c_void_p, i64p, i64p, C.c_uint64, i64p, C.c_uint64, i32p, C.c_uint64,
+                                       i32p, C.c_uint64, i32p, C.c_uint64, u64p, C.c_size_t]),
     "spmvgpu_decrypt": (C.c_int, [C.c_void_p, u64p, C.c_size_t, u64p, i32p]),
     "spmvgpu_add": (C.c_int, [C.c_void_p, u64p, u64p, u64p, C.c_size_t]),
     "spmvgpu_mul_relin": (C.c_int, [C.c_void_p, u64p, u64p, u64p, C.c_size_t]),
@@ -265,6 +267,21 @@ class Context:
         st = _u64(streams) if streams is not None else None
         check(lib().spmvgpu_encrypt(self.h, _p(flat, i64p), _p(offs, u64p),
                                     _p(st, u64p) if st is not None else None, _p(out, u64p), len(vals)))
+        return out
+
+    def encrypt_cssc(self, col_indices, values, vec, rows, slices, cols, n_chunks: int) -> np.ndarray:
+        """Device pack + encrypt (spmvgpu_encrypt_cssc); returns 2 n_chunks handles
+        (value chunks, then vector chunks)."""
+        ci, va, v = _i64(col_indices), _i64(values), _i64(vec)
+        r, sl, co = (np.ascontiguousarray(x, np.int32).reshape(-1) for x in (rows, slices, cols))
+        out = self.alloc(2 * n_chunks)
+        try:
+            check(lib().spmvgpu_encrypt_cssc(self.h, _p(ci, i64p), _p(va, i64p), ci.size, _p(v, i64p), v.size,
+                                             _p(r, i32p), r.size // 4, _p(sl, i32p), sl.size // 2,
+                                             _p(co, i32p), co.size // 4, _p(out, u64p), n_chunks))
+        except Exception:
+            self.free(out)
+            raise
         return out
 
     def decrypt(self, cts):

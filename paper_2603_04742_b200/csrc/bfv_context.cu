@@ -2,6 +2,8 @@
 #include "bfv_context.hpp"
 
 #include <algorithm>
+#include <climits>
+#include <cstdint>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -103,6 +105,8 @@ GpuContext::GpuContext(const RnsConfig& cfg, int device) : P_(cfg), device_(devi
 
 GpuContext::~GpuContext() {
     if (st_) cudaStreamSynchronize(st_);
+    if (stage_ev_) cudaEventDestroy(stage_ev_);
+    if (stage_) cudaFreeHost(stage_);
     // buffers release into pool_; pool_ destructor frees device memory
     gk_.clear();
     if (dc_) cudaFree(dc_);
@@ -116,6 +120,26 @@ void* GpuContext::upload_bytes(const void* src, size_t bytes, int slot) {
     if (bytes)
         cuda_check(cudaMemcpyAsync(scratch_[slot].as<void>(), src, bytes, cudaMemcpyHostToDevice, st_),
                    "upload");
+    return scratch_[slot].as<void>();
+}
+
+unsigned char* GpuContext::stage_host(size_t bytes) {
+    if (stage_ev_) cuda_check(cudaEventSynchronize(stage_ev_), "staging wait");
+    if (bytes > stage_bytes_) {
+        if (stage_) cuda_check(cudaFreeHost(stage_), "cudaFreeHost");
+        stage_ = nullptr;
+        const size_t cap = std::max<size_t>(bytes + bytes / 2, 1 << 20);
+        cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&stage_), cap, cudaHostAllocDefault), "cudaHostAlloc");
+        stage_bytes_ = cap;
+    }
+    if (!stage_ev_) cuda_check(cudaEventCreateWithFlags(&stage_ev_, cudaEventDisableTiming), "event");
+    return stage_;
+}
+
+void* GpuContext::stage_upload(size_t bytes, int slot) {
+    ensure_ws(scratch_[slot], std::max<size_t>(bytes, 256));
+    cuda_check(cudaMemcpyAsync(scratch_[slot].as<void>(), stage_, bytes, cudaMemcpyHostToDevice, st_), "upload");
+    cuda_check(cudaEventRecord(stage_ev_, st_), "event");
     return scratch_[slot].as<void>();
 }
 
@@ -252,12 +276,54 @@ void GpuContext::encrypt(const int64_t* vals, const u64* offs, const u64* stream
 
 void GpuContext::encrypt_dev(const int64_t* d_vals, const u64* d_offs, const u64* d_streams,
                              u64* const* d_out, int items) {
-    const int n = P_.n, L = P_.cfg.L, logn = P_.cfg.logn;
-    ensure_ws(wsM_, sizeof(u64) * (size_t)items * n);
-    ensure_ws(wsU_, sizeof(u64) * (size_t)items * L * n);
-    ensure_ws(wsC_, sizeof(u64) * (size_t)items * 2 * L * n);
+    ensure_ws(wsM_, sizeof(u64) * (size_t)items * P_.n);
     u64* M = wsM_.words();
     launch_encode_scatter(dc_, P_, d_vals, d_offs, M, items, st_);
+    encrypt_encoded(M, d_streams, d_out, items);
+}
+
+void GpuContext::encrypt_cssc(const int64_t* ci, const int64_t* va, size_t nnz, const int64_t* vec,
+                              size_t vec_len, const int32_t* rows, size_t n_rows, const int32_t* slices,
+                              size_t n_slices, const int32_t* cols, size_t n_cols, const std::vector<u64*>& out) {
+    const int items = (int)out.size();
+    if (!items) return;
+    if (items % 2) throw std::invalid_argument("encrypt_cssc: expects value and vector chunks in pairs");
+    if (nnz > (size_t)INT32_MAX || vec_len > (size_t)INT32_MAX || n_rows > (size_t)INT32_MAX)
+        throw std::length_error("encrypt_cssc: batch too large for 32-bit descriptors");
+    // one pinned staging block -> one upload
+    size_t off = 0;
+    auto place = [&](size_t b) {
+        const size_t o = off;
+        off += (b + 15) & ~size_t(15);
+        return o;
+    };
+    const size_t o_ci = place(8 * nnz), o_va = place(8 * nnz), o_v = place(8 * vec_len);
+    const size_t o_rows = place(16 * n_rows), o_sl = place(8 * n_slices), o_cols = place(16 * n_cols);
+    const size_t o_st = place(8 * (size_t)items), o_out = place(8 * (size_t)items);
+    unsigned char* h = stage_host(off);
+    std::memcpy(h + o_ci, ci, 8 * nnz);
+    std::memcpy(h + o_va, va, 8 * nnz);
+    std::memcpy(h + o_v, vec, 8 * vec_len);
+    std::memcpy(h + o_rows, rows, 16 * n_rows);
+    std::memcpy(h + o_sl, slices, 8 * n_slices);
+    std::memcpy(h + o_cols, cols, 16 * n_cols);
+    auto* hs = reinterpret_cast<u64*>(h + o_st);
+    for (int i = 0; i < items; ++i) hs[i] = next_stream_id();
+    std::memcpy(h + o_out, out.data(), 8 * (size_t)items);
+    auto* d = static_cast<unsigned char*>(stage_upload(off, 0));
+    ensure_ws(wsM_, sizeof(u64) * (size_t)items * P_.n);
+    u64* M = wsM_.words();
+    launch_pack_cssc(dc_, P_, reinterpret_cast<const int64_t*>(d + o_ci), reinterpret_cast<const int64_t*>(d + o_va),
+                     reinterpret_cast<const int64_t*>(d + o_v), reinterpret_cast<const int4*>(d + o_rows),
+                     (int)n_rows, reinterpret_cast<const int2*>(d + o_sl), reinterpret_cast<const int4*>(d + o_cols),
+                     items / 2, M, st_);
+    encrypt_encoded(M, reinterpret_cast<const u64*>(d + o_st), reinterpret_cast<u64* const*>(d + o_out), items);
+}
+
+void GpuContext::encrypt_encoded(u64* M, const u64* d_streams, u64* const* d_out, int items) {
+    const int n = P_.n, L = P_.cfg.L, logn = P_.cfg.logn;
+    ensure_ws(wsU_, sizeof(u64) * (size_t)items * L * n);
+    ensure_ws(wsC_, sizeof(u64) * (size_t)items * 2 * L * n);
     launch_ntt(dc_, logn, true, job(M, M, 1, {P_.t_index()}), items, st_);
     launch_enc_sample_u(dc_, P_, P_.cfg.seed, d_streams, wsU_.words(), items, st_);
     launch_ntt(dc_, logn, false, job(wsU_.words(), wsU_.words(), L, range_idx(0, L)), items, st_);

@@ -97,6 +97,12 @@ public:
     // same with device-resident arrays
     void encrypt_dev(const int64_t* d_vals, const u64* d_offs, const u64* d_streams,
                      u64* const* d_out, int items);
+    // Client A + Client B on the device: scatter CSR rows into the CSSC chunk
+    // plaintexts (value chunks then vector chunks) and encrypt them; host arrays
+    // go up in one pinned upload.  Layout of the descriptors: spmvgpu_encrypt_cssc.
+    void encrypt_cssc(const int64_t* ci, const int64_t* va, size_t nnz, const int64_t* vec, size_t vec_len,
+                      const int32_t* rows, size_t n_rows, const int32_t* slices, size_t n_slices,
+                      const int32_t* cols, size_t n_cols, const std::vector<u64*>& out);
     void decrypt(const std::vector<const u64*>& cts, u64* slots_host, int* budgets);
     void add(const std::vector<const u64*>& a, const std::vector<const u64*>& b,
              const std::vector<u64*>& out);
@@ -136,6 +142,11 @@ public:
 
 private:
     void keygen();
+    // encryption of encoded messages M[item][N] (mod t, slot layout applied)
+    void encrypt_encoded(u64* M, const u64* d_streams, u64* const* d_out, int items);
+    // pinned host staging buffer, reusable once its previous upload completed
+    unsigned char* stage_host(size_t bytes);
+    void* stage_upload(size_t bytes, int slot);
     DevBuf gen_ksk(u64 keyid, const u64* sp_ntt);
     void ensure_ws(DevBuf& b, size_t bytes) { b.ensure(&pool_, bytes); }
 
@@ -154,6 +165,9 @@ private:
     // workspaces for ad-hoc batched calls
     DevBuf wsT_, wsZ_, wsD2_, wsDX_, wsACC_, wsM_, wsX_, wsU_, wsC_, wsPT_;
     DevBuf scratch_[8];
+    unsigned char* stage_ = nullptr;  // pinned
+    size_t stage_bytes_ = 0;
+    cudaEvent_t stage_ev_ = nullptr;
     std::mutex mu_;
 };
 

@@ -705,6 +705,42 @@ void launch_encode_scatter(const DevConsts* dc, const RnsParams& P, const int64_
     CSSC_CHECK_LAUNCH();
 }
 
+// Client A + Client B fused: row record {nz_begin, len, pos, slice}; entry j of
+// the row sits in aligned column j (csr_to_cssc, sparse.cpp:79-117), which
+// chunk cols[col_base + j] = {chunk, k, h} holds at flat slot k h + pos
+// (generate_chunks, chunk.cpp:10-52); the vector chunk takes v[col] at the
+// same slot (reorg_vector, reorg.cpp).  Padding stays 0 (memset).
+__global__ void k_pack_cssc(const DevConsts* __restrict__ dc, const int64_t* __restrict__ CI,
+                            const int64_t* __restrict__ VA, const int64_t* __restrict__ V,
+                            const int4* __restrict__ rows, int n_rows, const int2* __restrict__ slices,
+                            const int4* __restrict__ cols, int n_chunks, u64* __restrict__ M) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n_rows) return;
+    const int4 rec = rows[r];
+    const int2 sl = slices[rec.w];
+    const int64_t t = (int64_t)dc->t;
+    const size_t n = (size_t)dc->n;
+    for (int j = 0; j < rec.y; ++j) {
+        const int4 c = __ldg(cols + sl.x + j);
+        const u32 pos = dc->pos0[c.y * c.z + rec.z];
+        int64_t a = VA[rec.x + j] % t;
+        int64_t b = V[sl.y + CI[rec.x + j]] % t;
+        M[(size_t)c.x * n + pos] = (u64)(a < 0 ? a + t : a);
+        M[(size_t)(n_chunks + c.x) * n + pos] = (u64)(b < 0 ? b + t : b);
+    }
+}
+
+void launch_pack_cssc(const DevConsts* dc, const RnsParams& P, const int64_t* CI, const int64_t* VA,
+                      const int64_t* V, const int4* rows, int n_rows, const int2* slices, const int4* cols,
+                      int n_chunks, u64* M, cudaStream_t st) {
+    if (!n_chunks) return;
+    cudaMemsetAsync(M, 0, sizeof(u64) * (size_t)P.n * 2 * n_chunks, st);
+    if (n_rows)
+        k_pack_cssc<<<(unsigned)((n_rows + 127) / 128), 128, 0, st>>>(dc, CI, VA, V, rows, n_rows, slices, cols,
+                                                                     n_chunks, M);
+    CSSC_CHECK_LAUNCH();
+}
+
 // PT[item][L][N] = centred lift of M[item][N] (mod t) to each q_j (coef form)
 __global__ void k_plain_lift(const DevConsts* __restrict__ dc, const u64* M, u64* PT) {
     const int n = dc->n, L = dc->L;

@@ -36,8 +36,6 @@ struct spmvgpu_plan {
 
 struct cssc_job {
     spmvgpu_ctx* ctx;
-    std::vector<spmv::CsrMatrix> ms;
-    std::vector<std::vector<std::int64_t>> vs;
     std::unique_ptr<spmv::detail::BatchedSpmv> job;
 };
 
@@ -105,6 +103,24 @@ std::vector<u64*> mptrs(const spmvgpu_ct* h, size_t n) {
         v[i] = reinterpret_cast<u64*>(h[i]);
     }
     return v;
+}
+
+// C-ABI CSR -> borrowed view (BatchedSpmv validates row pointers and columns)
+spmv::detail::CsrView view_of(const cssc_csr& m, const int64_t* v) {
+    if (m.rows && (!m.row_ptrs || (m.row_ptrs[m.rows] && (!m.col_indices || !m.values))))
+        throw std::invalid_argument("csr: null array");
+    if (m.cols && !v) throw std::invalid_argument("null vector");
+    if (m.rows && m.row_ptrs[0] != 0) throw std::invalid_argument("csr: row_ptrs[0] must be 0");
+    spmv::detail::CsrView w;
+    w.rows = m.rows;
+    w.cols = m.cols;
+    w.nnz = m.rows ? static_cast<size_t>(m.row_ptrs[m.rows]) : 0;
+    static const std::uint64_t zero = 0;
+    w.row_ptrs = m.rows ? reinterpret_cast<const std::uint64_t*>(m.row_ptrs) : &zero;
+    w.col_indices = reinterpret_cast<const std::uint64_t*>(m.col_indices);
+    w.values = m.values;
+    w.vec = v;
+    return w;
 }
 
 spmv::CsrMatrix to_csr(const cssc_csr& m) {
@@ -332,6 +348,43 @@ int spmvgpu_encrypt(spmvgpu_ctx* c, const int64_t* vals, const uint64_t* offsets
         g.encrypt(vals, offsets, st.data(), mptrs(out, n));
     });
 }
+int spmvgpu_encrypt_cssc(spmvgpu_ctx* c, const int64_t* col_indices, const int64_t* values, uint64_t nnz,
+                         const int64_t* vec, uint64_t vec_len, const int32_t* rows, uint64_t n_rows,
+                         const int32_t* slices, uint64_t n_slices, const int32_t* cols, uint64_t n_cols,
+                         const spmvgpu_ct* out, size_t n_chunks) {
+    return guard([&] {
+        auto& g = G(c);
+        // descriptor validation: the kernel trusts every index it reads
+        const uint64_t S = g.params().S;
+        for (uint64_t k = 0; k < n_cols; ++k) {
+            const int32_t* cr = cols + 4 * k;
+            if (cr[0] < 0 || (uint64_t)cr[0] >= n_chunks || cr[1] < 0 || cr[2] <= 0 ||
+                ((uint64_t)cr[1] + 1) * (uint64_t)cr[2] > S)
+                throw std::invalid_argument("encrypt_cssc: column record out of range");
+        }
+        for (uint64_t s = 0; s < n_slices; ++s)
+            if (slices[2 * s] < 0 || slices[2 * s + 1] < 0 || (uint64_t)slices[2 * s + 1] > vec_len)
+                throw std::invalid_argument("encrypt_cssc: slice record out of range");
+        for (uint64_t r = 0; r < n_rows; ++r) {
+            const int32_t* rec = rows + 4 * r;
+            if (rec[0] < 0 || rec[1] < 0 || (uint64_t)rec[0] + (uint64_t)rec[1] > nnz || rec[2] < 0 ||
+                rec[3] < 0 || (uint64_t)rec[3] >= n_slices)
+                throw std::invalid_argument("encrypt_cssc: row record out of range");
+            const int32_t* sl = slices + 2 * rec[3];
+            if ((uint64_t)sl[0] + (uint64_t)rec[1] > n_cols)
+                throw std::invalid_argument("encrypt_cssc: row longer than its slice's aligned columns");
+            const uint64_t vroom = vec_len - (uint64_t)sl[1];
+            for (int32_t j = 0; j < rec[1]; ++j) {
+                if (rec[2] >= cols[4 * (sl[0] + j) + 2])
+                    throw std::invalid_argument("encrypt_cssc: row position beyond its chunk height");
+                if ((uint64_t)col_indices[rec[0] + j] >= vroom)
+                    throw spmv::IndexOutOfRangeError("encrypt_cssc: column index outside the vector");
+            }
+        }
+        g.encrypt_cssc(col_indices, values, nnz, vec, vec_len, rows, n_rows, slices, n_slices, cols, n_cols,
+                       mptrs(out, 2 * n_chunks));
+    });
+}
 int spmvgpu_decrypt(spmvgpu_ctx* c, const spmvgpu_ct* cts, size_t n, uint64_t* slots, int32_t* budgets) {
     return guard([&] {
         std::vector<int> b(n);
@@ -423,14 +476,13 @@ int cssc_spmv_partitioned(spmvgpu_ctx* c, const cssc_csr* m, const int64_t* v, u
 int cssc_spmv_batch(spmvgpu_ctx* c, const cssc_csr* ms, const int64_t* const* vs, size_t nmat, uint64_t chunk_size,
                     int key_holder, int64_t* const* values, cssc_result* res) {
     return guard([&] {
-        spmv::GpuBfvBackend be(c->hp, c);
-        std::vector<spmv::CsrMatrix> mats;
-        std::vector<std::vector<int64_t>> vecs;
-        for (size_t i = 0; i < nmat; ++i) {
-            mats.push_back(to_csr(ms[i]));
-            vecs.emplace_back(vs[i], vs[i] + ms[i].cols);
-        }
-        const auto r = spmv::spmv_batch(be, mats, vecs, chunk_size, static_cast<spmv::PartyRole>(key_holder));
+        G(c);
+        std::vector<spmv::detail::CsrView> w;
+        for (size_t i = 0; i < nmat; ++i) w.push_back(view_of(ms[i], vs[i]));
+        spmv::detail::BatchedSpmv job(c, c->hp, w, chunk_size, static_cast<spmv::PartyRole>(key_holder));
+        job.encrypt();
+        job.cloud(false);
+        const auto r = job.finish();
         for (size_t i = 0; i < nmat; ++i) fill_result(r[i], values ? values[i] : nullptr, res ? res + i : nullptr, nullptr, 0);
     });
 }
@@ -440,12 +492,10 @@ int cssc_job_create(spmvgpu_ctx* c, const cssc_csr* ms, const int64_t* const* vs
     return guard([&] {
         auto j = std::make_unique<cssc_job>();
         j->ctx = c;
-        for (size_t i = 0; i < nmat; ++i) {
-            j->ms.push_back(to_csr(ms[i]));
-            j->vs.emplace_back(vs[i], vs[i] + ms[i].cols);
-        }
-        j->job = std::make_unique<spmv::detail::BatchedSpmv>(c, c->hp, j->ms, j->vs, chunk_size,
-                                                             spmv::PartyRole::ClientA);
+        G(c);
+        std::vector<spmv::detail::CsrView> w;
+        for (size_t i = 0; i < nmat; ++i) w.push_back(view_of(ms[i], vs[i]));
+        j->job = std::make_unique<spmv::detail::BatchedSpmv>(c, c->hp, w, chunk_size, spmv::PartyRole::ClientA);
         *out = j.release();
     });
 }

@@ -2,6 +2,8 @@
 #include "batched_spmv.hpp"
 
 #include <algorithm>
+#include <climits>
+#include <numeric>
 #include <stdexcept>
 #include <string>
 
@@ -11,9 +13,11 @@ namespace spmv::detail {
 
 namespace {
 
-std::uint64_t column_index_bytes(const ChunkSet& cs) {
-    std::uint64_t b = 4;  // chunk count, then an (h, k) header and 4-byte indices per chunk
-    for (const Chunk& c : cs.chunks) b += 8 + 4 * static_cast<std::uint64_t>(c.colidx_flat.size());
+// reference protocol.cpp:108-111: a 4-byte count, then an (h, k) header and
+// 4-byte indices for every padded slot of every chunk
+std::uint64_t column_index_bytes(const std::uint64_t* r, const std::uint64_t* c, std::size_t n) {
+    std::uint64_t b = 4;
+    for (std::size_t i = 0; i < n; ++i) b += 8 + 4 * r[i] * c[i];
     return b;
 }
 
@@ -21,54 +25,63 @@ int lowered(int b, int c) { return std::max(0, b - c); }
 
 }  // namespace
 
-BatchedSpmv::BatchedSpmv(spmvgpu_ctx* ctx, const HeParams& hp, std::span<const CsrMatrix> ms,
-                         std::span<const std::vector<std::int64_t>> vs, std::size_t chunk_size,
-                         PartyRole key_holder, bool partition)
+CsrView view_of(const CsrMatrix& m, std::span<const std::int64_t> v) {
+    if (m.cols != v.size())
+        throw DimensionMismatchError("spmv_partitioned: vector length does not match columns");
+    if (m.row_ptrs.size() != m.rows + 1 || m.col_indices.size() != m.values.size())
+        throw std::invalid_argument("csr: inconsistent array lengths");
+    CsrView w;
+    w.rows = m.rows;
+    w.cols = m.cols;
+    w.nnz = m.values.size();
+    w.row_ptrs = reinterpret_cast<const std::uint64_t*>(m.row_ptrs.data());
+    w.col_indices = reinterpret_cast<const std::uint64_t*>(m.col_indices.data());
+    w.values = m.values.data();
+    w.vec = v.data();
+    return w;
+}
+
+BatchedSpmv::BatchedSpmv(spmvgpu_ctx* ctx, const HeParams& hp, std::span<const CsrView> ms,
+                         std::size_t chunk_size, PartyRole key_holder, bool partition)
     : ctx_(ctx), hp_(hp), kh_(key_holder), nmat_(ms.size()) {
-    if (ms.size() != vs.size()) throw DimensionMismatchError("spmv_batch: matrices and vectors differ in count");
-    std::vector<std::int64_t> b_vals;
+    std::size_t nnz_total = 0, vec_total = 0;
+    for (const CsrView& m : ms) {
+        nnz_total += m.nnz;
+        vec_total += m.cols;
+    }
+    if (nnz_total > INT32_MAX || vec_total > INT32_MAX)
+        throw std::length_error("spmv_batch: more than 2^31 entries in one batch");
+    ci_.reserve(nnz_total);
+    va_.reserve(nnz_total);
+    vec_.reserve(vec_total);
     for (std::size_t mi = 0; mi < ms.size(); ++mi) {
-        const CsrMatrix& m = ms[mi];
-        const auto& v = vs[mi];
-        if (m.cols != v.size())
-            throw DimensionMismatchError("spmv_partitioned: vector length does not match columns");
+        const CsrView& m = ms[mi];
+        if (m.rows && m.row_ptrs[0] != 0) throw std::invalid_argument("csr: row_ptrs[0] must be 0");
+        for (std::size_t i = 0; i < m.rows; ++i)
+            if (m.row_ptrs[i + 1] < m.row_ptrs[i]) throw std::invalid_argument("csr: row_ptrs must be non-decreasing");
+        if (m.rows && m.row_ptrs[m.rows] != m.nnz) throw std::invalid_argument("csr: row_ptrs end is not nnz");
+        for (std::size_t k = 0; k < m.nnz; ++k)
+            if (m.col_indices[k] >= m.cols)
+                throw IndexOutOfRangeError("csr: column index " + std::to_string(m.col_indices[k]) +
+                                           " out of range for " + std::to_string(m.cols) + " columns");
+        const auto nz_base = static_cast<std::int64_t>(ci_.size());
+        const auto vec_base = static_cast<std::int64_t>(vec_.size());
+        ci_.insert(ci_.end(), reinterpret_cast<const std::int64_t*>(m.col_indices),
+                   reinterpret_cast<const std::int64_t*>(m.col_indices) + m.nnz);
+        va_.insert(va_.end(), m.values, m.values + m.nnz);
+        vec_.insert(vec_.end(), m.vec, m.vec + m.cols);
         rows_of_.push_back(m.rows);
-        // spmv_partitioned slices rows by chunk_size; plain spmv keeps one slice
-        std::vector<CsrMatrix> parts = partition ? partition_rows(m, chunk_size) : std::vector<CsrMatrix>{m};
-        for (CsrMatrix& part : parts) {
-            // per-slice checks in the reference's order (protocol.cpp:80-90)
-            if (chunk_size == 0 || chunk_size > hp_.slot_count)
-                throw std::invalid_argument("spmv: chunk_size must be in [1, slot_count]");
-            Slice s;
-            s.mat = mi;
-            s.rows = part.rows;
-            s.cs = generate_chunks(csr_to_cssc(part), chunk_size);
-            const ReorgVector rv = reorg_vector(v, s.cs);
-            s.first_chunk = r_.size();
-            for (std::size_t i = 0; i < s.cs.n_ct(); ++i) {
-                r_.push_back(s.cs.r_list[i]);
-                c_.push_back(s.cs.c_list[i]);
-            }
-            if (s.cs.n_ct()) {
-                s.result = static_cast<int>(n_out_++);
-            }
-            for (std::size_t i = 0; i < s.cs.n_ct(); ++i) slice_id_.push_back(static_cast<std::uint32_t>(s.result));
-            for (const auto& seg : rv.segments) b_vals.insert(b_vals.end(), seg.begin(), seg.end());
-            slices_.push_back(std::move(s));
+        // spmv_partitioned slices rows by chunk_size (partition_rows, chunk.cpp:55-73);
+        // plain spmv keeps one slice
+        if (partition) {
+            if (chunk_size == 0) throw std::invalid_argument("partition_rows: max_rows must be positive");
+            for (std::size_t r0 = 0; r0 < m.rows; r0 += chunk_size)
+                add_slice(m, mi, r0, std::min(m.rows, r0 + chunk_size), chunk_size, nz_base, vec_base);
+        } else {
+            add_slice(m, mi, 0, m.rows, chunk_size, nz_base, vec_base);
         }
     }
-    // encryption inputs: [A flats of all chunks][B segments of all chunks]
     const std::size_t n = r_.size();
-    offs_.assign(2 * n + 1, 0);
-    std::size_t k = 0;
-    for (int half = 0; half < 2; ++half)
-        for (const Slice& s : slices_)
-            for (const Chunk& ch : s.cs.chunks) {
-                if (half == 0) vals_.insert(vals_.end(), ch.value_flat.begin(), ch.value_flat.end());
-                offs_[k + 1] = offs_[k] + ch.value_flat.size();
-                ++k;
-            }
-    vals_.insert(vals_.end(), b_vals.begin(), b_vals.end());
     if (!n) return;
     // the cloud's view of the job: chunk shapes and slice ids (ChunkShapeMeta)
     std::vector<std::uint64_t> key{n, n_out_};
@@ -90,6 +103,62 @@ BatchedSpmv::BatchedSpmv(spmvgpu_ctx* ctx, const HeParams& hp, std::span<const C
     }
 }
 
+// The shape half of csr_to_cssc + generate_chunks for rows [r0, r1) of m
+// (sparse.cpp:79-117, chunk.cpp:10-52): a stable counting sort of the rows by
+// descending length gives the CSSC row order; aligned column j has height
+// h_j = #rows longer than j; chunks open at a column, fix h, and admit columns
+// while h (k + 1) <= budget.  The entries themselves are scattered on the
+// device (k_pack_cssc) from the row records built here.
+void BatchedSpmv::add_slice(const CsrView& m, std::size_t mat, std::size_t r0, std::size_t r1, std::size_t budget,
+                            std::int64_t nz_base, std::int64_t vec_base) {
+    // per-slice checks in the reference's order (protocol.cpp:80-90)
+    if (budget == 0 || budget > hp_.slot_count)
+        throw std::invalid_argument("spmv: chunk_size must be in [1, slot_count]");
+    Slice s;
+    s.mat = mat;
+    s.rows = r1 - r0;
+    const std::uint64_t* rp = m.row_ptrs + r0;
+    std::size_t max_len = 0;
+    for (std::size_t i = 0; i < s.rows; ++i) max_len = std::max<std::size_t>(max_len, rp[i + 1] - rp[i]);
+    std::vector<std::size_t> bucket(max_len + 2, 0);
+    for (std::size_t i = 0; i < s.rows; ++i) ++bucket[max_len - (rp[i + 1] - rp[i]) + 1];
+    std::partial_sum(bucket.begin(), bucket.end(), bucket.begin());
+    s.row_map.resize(s.rows);
+    for (std::size_t i = 0; i < s.rows; ++i) s.row_map[bucket[max_len - (rp[i + 1] - rp[i])]++] = i;
+    std::vector<std::size_t> height(max_len, 0);
+    for (std::size_t i = 0; i < s.rows; ++i)
+        if (rp[i + 1] > rp[i]) ++height[rp[i + 1] - rp[i] - 1];
+    for (std::size_t j = max_len; j-- > 1;) height[j - 1] += height[j];
+    if (max_len && height[0] > budget)
+        throw ColumnTooTallError("generate_chunks: aligned column 0 has height " + std::to_string(height[0]) +
+                                 " > budget " + std::to_string(budget) + "; partition the rows first");
+    s.first_chunk = r_.size();
+    const auto col_base = static_cast<std::int32_t>(colrec_.size() / 4);
+    for (std::size_t first = 0; first < max_len;) {
+        const std::size_t h = height[first];
+        const std::size_t fit = std::min<std::size_t>(budget / h, max_len - first);
+        const auto chunk = static_cast<std::int32_t>(r_.size());
+        for (std::size_t k = 0; k < fit; ++k)
+            colrec_.insert(colrec_.end(), {chunk, static_cast<std::int32_t>(k), static_cast<std::int32_t>(h), 0});
+        r_.push_back(h);
+        c_.push_back(fit);
+        first += fit;
+    }
+    s.n_ct = r_.size() - s.first_chunk;
+    const auto sidx = static_cast<std::int32_t>(slicerec_.size() / 2);
+    slicerec_.insert(slicerec_.end(), {col_base, static_cast<std::int32_t>(vec_base)});
+    for (std::size_t p = 0; p < s.rows; ++p) {
+        const std::size_t i = s.row_map[p];
+        const std::size_t len = rp[i + 1] - rp[i];
+        if (len)
+            rowrec_.insert(rowrec_.end(), {static_cast<std::int32_t>(nz_base + static_cast<std::int64_t>(rp[i])),
+                                           static_cast<std::int32_t>(len), static_cast<std::int32_t>(p), sidx});
+    }
+    if (s.n_ct) s.result = static_cast<int>(n_out_++);
+    for (std::size_t i = 0; i < s.n_ct; ++i) slice_id_.push_back(static_cast<std::uint32_t>(s.result));
+    slices_.push_back(std::move(s));
+}
+
 BatchedSpmv::~BatchedSpmv() {
     if (lease_.key.empty()) return;
     if (done_)
@@ -103,8 +172,11 @@ void BatchedSpmv::encrypt() {
     if (!n) return;
     std::vector<spmvgpu_ct> all(lease_.a);
     all.insert(all.end(), lease_.b.begin(), lease_.b.end());
-    check_status(spmvgpu_encrypt(ctx_, vals_.data(), offs_.data(), nullptr, all.data(), 2 * n));
-    h2d_ = sizeof(std::int64_t) * vals_.size() + sizeof(std::uint64_t) * offs_.size();
+    check_status(spmvgpu_encrypt_cssc(ctx_, ci_.data(), va_.data(), ci_.size(), vec_.data(), vec_.size(),
+                                      rowrec_.data(), rowrec_.size() / 4, slicerec_.data(), slicerec_.size() / 2,
+                                      colrec_.data(), colrec_.size() / 4, all.data(), n));
+    h2d_ = sizeof(std::int64_t) * (ci_.size() + va_.size() + vec_.size()) +
+           sizeof(std::int32_t) * (rowrec_.size() + slicerec_.size() + colrec_.size());
 }
 
 void BatchedSpmv::ensure_plan() {
@@ -145,14 +217,16 @@ std::vector<SpmvResult> BatchedSpmv::finish() {
     }
     for (const Slice& s : slices_) {
         SpmvResult& R = res[s.mat];
-        const std::size_t n_ct = s.cs.n_ct();
+        const std::size_t n_ct = s.n_ct;
+        const std::uint64_t* rl = r_.data() + s.first_chunk;
+        const std::uint64_t* cl = c_.data() + s.first_chunk;
         // ledger identities of one slice (protocol.cpp:99-136)
         OpLedger led;
         led.n_enc = 2 * n_ct;
         led.n_mult_cc = n_ct;
         led.n_mult_cp = n_ct;
         std::uint64_t rot = 0;
-        for (std::size_t i = 0; i < n_ct; ++i) rot += rotation_schedule(s.cs.r_list[i], s.cs.c_list[i]).size();
+        for (std::size_t i = 0; i < n_ct; ++i) rot += rotation_schedule(rl[i], cl[i]).size();
         led.n_rot = rot;
         led.n_add = rot + n_ct;
         led.n_dec = n_ct ? 1 : 0;
@@ -163,7 +237,7 @@ std::vector<SpmvResult> BatchedSpmv::finish() {
         msgs.push_back({PartyRole::ClientA, PartyRole::Cloud, MessageKind::CiphertextBatch,
                         ciphertext_batch_bytes(hp_, n_ct), n_ct});
         msgs.push_back({PartyRole::ClientA, PartyRole::ClientB, MessageKind::ColumnIndexPlain,
-                        column_index_bytes(s.cs), 0});
+                        column_index_bytes(rl, cl, n_ct), 0});
         msgs.push_back({PartyRole::ClientA, PartyRole::Cloud, MessageKind::ChunkShapeMeta,
                         4 + 8 * static_cast<std::uint64_t>(n_ct), 0});
         msgs.push_back({PartyRole::ClientB, PartyRole::Cloud, MessageKind::CiphertextBatch,
@@ -177,7 +251,7 @@ std::vector<SpmvResult> BatchedSpmv::finish() {
             for (std::size_t i = 0; i < n_ct; ++i) {
                 const int prod_b = lowered(nm.initial_budget_bits, nm.cost_ct_ct_mult_bits);
                 int acc_b = prod_b;
-                for (const RotStep& st : rotation_schedule(s.cs.r_list[i], s.cs.c_list[i])) {
+                for (const RotStep& st : rotation_schedule(rl[i], cl[i])) {
                     const int rot_b = lowered(st.from_accumulator ? acc_b : prod_b, nm.cost_rot_bits);
                     acc_b = lowered(std::min(acc_b, rot_b), nm.cost_add_bits);
                 }
@@ -188,7 +262,7 @@ std::vector<SpmvResult> BatchedSpmv::finish() {
                 throw NoiseExhaustedError("decrypt: noise budget exhausted (slice result)");
             const std::uint64_t* sl = slots.data() + static_cast<std::size_t>(s.result) * S;
             for (std::size_t idx = 0; idx < s.rows; ++idx)
-                vals[s.cs.row_map[idx]] = idx < S ? to_signed(sl[idx], hp_.plaintext_modulus) : 0;
+                vals[s.row_map[idx]] = idx < S ? to_signed(sl[idx], hp_.plaintext_modulus) : 0;
             const int meas = measured[static_cast<std::size_t>(s.result)];
             R.measured_noise_budget_bits =
                 R.measured_noise_budget_bits < 0 ? meas : std::min(R.measured_noise_budget_bits, meas);

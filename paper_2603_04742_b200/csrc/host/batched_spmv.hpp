@@ -1,8 +1,10 @@
 // batched_spmv.hpp -- the GPU evaluation of spmv_partitioned over one or more
-// matrices: every slice's pack (Client A/B, host), one batched encryption,
-// one cloud plan over all chunks (device), one batched decryption, then the
-// reference's per-slice bookkeeping (ledger, transcript, model noise) so each
-// matrix's SpmvResult equals its own reference run (protocol.cpp:74-176).
+// matrices: the CSSC shapes of every slice on the host (row-length counting
+// sort and chunk boundaries only), Client A + B's packing and encryption in
+// one device pass (spmvgpu_encrypt_cssc), one cloud plan over all chunks, one
+// batched decryption, then the reference's per-slice bookkeeping (ledger,
+// transcript, model noise) so each matrix's SpmvResult equals its own
+// reference run (protocol.cpp:74-176).
 #pragma once
 
 #include <cstdint>
@@ -15,16 +17,26 @@
 
 namespace spmv::detail {
 
+// Borrowed CSR arrays (a CsrMatrix or a C-ABI cssc_csr); read only while the
+// BatchedSpmv is constructed.
+struct CsrView {
+    std::size_t rows = 0, cols = 0, nnz = 0;
+    const std::uint64_t* row_ptrs = nullptr;     // rows + 1
+    const std::uint64_t* col_indices = nullptr;  // nnz
+    const std::int64_t* values = nullptr;        // nnz
+    const std::int64_t* vec = nullptr;           // cols
+};
+CsrView view_of(const CsrMatrix& m, std::span<const std::int64_t> v);
+
 class BatchedSpmv {
 public:
-    BatchedSpmv(spmvgpu_ctx* ctx, const HeParams& hp, std::span<const CsrMatrix> ms,
-                std::span<const std::vector<std::int64_t>> vs, std::size_t chunk_size,
+    BatchedSpmv(spmvgpu_ctx* ctx, const HeParams& hp, std::span<const CsrView> ms, std::size_t chunk_size,
                 PartyRole key_holder, bool partition = true);
     ~BatchedSpmv();
     BatchedSpmv(const BatchedSpmv&) = delete;
     BatchedSpmv& operator=(const BatchedSpmv&) = delete;
 
-    void encrypt();               // Client A + Client B: one batched encrypt
+    void encrypt();               // Client A + Client B: pack + encrypt on the device
     void cloud(bool use_graph);   // enqueue the cloud plan (no host sync)
     std::vector<SpmvResult> finish();  // key holder: decrypt, unpermute, bookkeeping
 
@@ -37,10 +49,13 @@ private:
     struct Slice {
         std::size_t mat = 0;
         std::size_t rows = 0;
-        ChunkSet cs;
-        std::size_t first_chunk = 0;  // global chunk index
-        int result = -1;              // result ciphertext index, -1 when no chunks
+        std::vector<std::size_t> row_map;  // CSSC row order (rm, sparse.cpp:79-117)
+        std::size_t first_chunk = 0;       // global chunk index
+        std::size_t n_ct = 0;
+        int result = -1;                   // result ciphertext index, -1 when no chunks
     };
+    void add_slice(const CsrView& m, std::size_t mat, std::size_t r0, std::size_t r1, std::size_t budget,
+                   std::int64_t nz_base, std::int64_t vec_base);
     void ensure_plan();
 
     spmvgpu_ctx* ctx_;
@@ -49,13 +64,14 @@ private:
     std::size_t nmat_;
     std::vector<std::size_t> rows_of_;
     std::vector<Slice> slices_;
-    std::vector<std::int64_t> vals_;   // A flats then B segments
-    std::vector<std::uint64_t> offs_;
+    // device pack image (spmvgpu_encrypt_cssc)
+    std::vector<std::int64_t> ci_, va_, vec_;
+    std::vector<std::int32_t> rowrec_, slicerec_, colrec_;
     std::vector<std::uint64_t> r_, c_;
     std::vector<std::uint32_t> slice_id_;
     std::size_t n_out_ = 0;
-    PlanLease lease_;
-    bool done_ = false;  // plan + ciphertext buffers, from / back to the context's plan cache
+    PlanLease lease_;  // plan + ciphertext buffers, from / back to the context's plan cache
+    bool done_ = false;
     std::uint64_t h2d_ = 0, d2h_ = 0;
 };
 

@@ -104,10 +104,9 @@ SpmvResult spmv(const HeBackend& be, const CsrMatrix& m, std::span<const std::in
         throw std::invalid_argument("spmv: chunk_size must be in [1, slot_count]");
     if (const auto* gpu = dynamic_cast<const GpuBfvBackend*>(&be)) {
         // a single slice of the batched path: no row partitioning here
-        const std::vector<std::int64_t> vv(v.begin(), v.end());
-        detail::BatchedSpmv job(gpu->context(), gpu->params(), std::span<const CsrMatrix>(&m, 1),
-                                std::span<const std::vector<std::int64_t>>(&vv, 1), chunk_size, key_holder,
-                                /*partition=*/false);
+        const detail::CsrView w = detail::view_of(m, v);
+        detail::BatchedSpmv job(gpu->context(), gpu->params(), std::span<const detail::CsrView>(&w, 1), chunk_size,
+                                key_holder, /*partition=*/false);
         job.encrypt();
         job.cloud(false);
         return std::move(job.finish()[0]);
@@ -119,7 +118,10 @@ std::vector<SpmvResult> spmv_batch(const HeBackend& be, std::span<const CsrMatri
                                    std::span<const std::vector<std::int64_t>> vs, std::size_t chunk_size,
                                    PartyRole key_holder) {
     if (const auto* gpu = dynamic_cast<const GpuBfvBackend*>(&be)) {
-        detail::BatchedSpmv job(gpu->context(), gpu->params(), ms, vs, chunk_size, key_holder);
+        if (ms.size() != vs.size()) throw DimensionMismatchError("spmv_batch: matrices and vectors differ in count");
+        std::vector<detail::CsrView> w;
+        for (std::size_t i = 0; i < ms.size(); ++i) w.push_back(detail::view_of(ms[i], vs[i]));
+        detail::BatchedSpmv job(gpu->context(), gpu->params(), w, chunk_size, key_holder);
         job.encrypt();
         job.cloud(false);
         return job.finish();
@@ -132,10 +134,13 @@ std::vector<SpmvResult> spmv_batch(const HeBackend& be, std::span<const CsrMatri
 SpmvResult spmv_partitioned(const HeBackend& be, const CsrMatrix& m, std::span<const std::int64_t> v,
                             std::size_t chunk_size, PartyRole key_holder) {
     if (m.cols != v.size()) throw DimensionMismatchError("spmv_partitioned: vector length does not match columns");
-    if (dynamic_cast<const GpuBfvBackend*>(&be)) {
-        const std::vector<std::int64_t> vv(v.begin(), v.end());
-        return std::move(spmv_batch(be, std::span<const CsrMatrix>(&m, 1),
-                                    std::span<const std::vector<std::int64_t>>(&vv, 1), chunk_size, key_holder)[0]);
+    if (const auto* gpu = dynamic_cast<const GpuBfvBackend*>(&be)) {
+        const detail::CsrView w = detail::view_of(m, v);
+        detail::BatchedSpmv job(gpu->context(), gpu->params(), std::span<const detail::CsrView>(&w, 1), chunk_size,
+                                key_holder);
+        job.encrypt();
+        job.cloud(false);
+        return std::move(job.finish()[0]);
     }
     SpmvResult merged;
     merged.message_ledger.key_holder = key_holder;
