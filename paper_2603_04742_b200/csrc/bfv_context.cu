@@ -276,10 +276,15 @@ void GpuContext::encrypt(const int64_t* vals, const u64* offs, const u64* stream
 
 void GpuContext::encrypt_dev(const int64_t* d_vals, const u64* d_offs, const u64* d_streams,
                              u64* const* d_out, int items) {
-    ensure_ws(wsM_, sizeof(u64) * (size_t)items * P_.n);
-    u64* M = wsM_.words();
-    launch_encode_scatter(dc_, P_, d_vals, d_offs, M, items, st_);
-    encrypt_encoded(M, d_streams, d_out, items);
+    u64* CM = enc_workspace(items);
+    launch_encode_scatter(dc_, P_, d_vals, d_offs, CM + (size_t)2 * P_.cfg.L * P_.n, items, st_, cm_stride());
+    encrypt_encoded(d_streams, d_out, items);
+}
+
+u64* GpuContext::enc_workspace(int items) {
+    ensure_ws(wsU_, sizeof(u64) * (size_t)items * P_.cfg.L * P_.n);
+    ensure_ws(wsC_, sizeof(u64) * (size_t)items * cm_stride());
+    return wsC_.words();
 }
 
 void GpuContext::encrypt_cssc(const int64_t* ci, const int64_t* va, size_t nnz, const int64_t* vec,
@@ -311,25 +316,30 @@ void GpuContext::encrypt_cssc(const int64_t* ci, const int64_t* va, size_t nnz, 
     for (int i = 0; i < items; ++i) hs[i] = next_stream_id();
     std::memcpy(h + o_out, out.data(), 8 * (size_t)items);
     auto* d = static_cast<unsigned char*>(stage_upload(off, 0));
-    ensure_ws(wsM_, sizeof(u64) * (size_t)items * P_.n);
-    u64* M = wsM_.words();
+    int log_tpr = 0;
+    while (log_tpr < 5 && ((size_t)n_rows << log_tpr) < nnz) ++log_tpr;
+    u64* CM = enc_workspace(items);
     launch_pack_cssc(dc_, P_, reinterpret_cast<const int64_t*>(d + o_ci), reinterpret_cast<const int64_t*>(d + o_va),
                      reinterpret_cast<const int64_t*>(d + o_v), reinterpret_cast<const int4*>(d + o_rows),
                      (int)n_rows, reinterpret_cast<const int2*>(d + o_sl), reinterpret_cast<const int4*>(d + o_cols),
-                     items / 2, M, st_);
-    encrypt_encoded(M, reinterpret_cast<const u64*>(d + o_st), reinterpret_cast<u64* const*>(d + o_out), items);
+                     items / 2, log_tpr, CM + (size_t)2 * P_.cfg.L * P_.n, cm_stride(), st_);
+    encrypt_encoded(reinterpret_cast<const u64*>(d + o_st), reinterpret_cast<u64* const*>(d + o_out), items);
 }
 
-void GpuContext::encrypt_encoded(u64* M, const u64* d_streams, u64* const* d_out, int items) {
-    const int n = P_.n, L = P_.cfg.L, logn = P_.cfg.logn;
-    ensure_ws(wsU_, sizeof(u64) * (size_t)items * L * n);
-    ensure_ws(wsC_, sizeof(u64) * (size_t)items * 2 * L * n);
-    launch_ntt(dc_, logn, true, job(M, M, 1, {P_.t_index()}), items, st_);
+// CM = wsC_[item][2L+1][N] holds the encoded messages in limb 2L on entry;
+// the inverse NTT of the message (mod t) rides in the same launch as the
+// inverse NTT of pk * u (limbs 0 .. 2L-1).
+void GpuContext::encrypt_encoded(const u64* d_streams, u64* const* d_out, int items) {
+    const int L = P_.cfg.L, logn = P_.cfg.logn;
+    u64* CM = wsC_.words();
     launch_enc_sample_u(dc_, P_, P_.cfg.seed, d_streams, wsU_.words(), items, st_);
     launch_ntt(dc_, logn, false, job(wsU_.words(), wsU_.words(), L, range_idx(0, L)), items, st_);
-    launch_enc_pk(dc_, P_, pk_.words(), wsU_.words(), wsC_.words(), items, st_);
-    launch_ntt(dc_, logn, true, job(wsC_.words(), wsC_.words(), 2 * L, range_idx(0, L)), items, st_);
-    launch_enc_finish(dc_, P_, P_.cfg.seed, d_streams, wsC_.words(), M, d_out, items, st_);
+    launch_enc_pk(dc_, P_, pk_.words(), wsU_.words(), CM, items, st_);
+    std::vector<int> pidx = range_idx(0, L);
+    pidx.insert(pidx.end(), pidx.begin(), pidx.end());
+    pidx.push_back(P_.t_index());
+    launch_ntt(dc_, logn, true, job(CM, CM, 2 * L + 1, pidx), items, st_);
+    launch_enc_finish(dc_, P_, P_.cfg.seed, d_streams, CM, d_out, items, st_);
     stats_.kernels += 7;
     stats_.limb_ntts += (u64)items * (1 + 3 * L);
 }

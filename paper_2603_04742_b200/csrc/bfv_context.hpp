@@ -142,8 +142,10 @@ public:
 
 private:
     void keygen();
-    // encryption of encoded messages M[item][N] (mod t, slot layout applied)
-    void encrypt_encoded(u64* M, const u64* d_streams, u64* const* d_out, int items);
+    // encryption of the encoded messages staged in limb 2L of the CM workspace
+    void encrypt_encoded(const u64* d_streams, u64* const* d_out, int items);
+    u64* enc_workspace(int items);  // wsU_ + wsC_ (CM layout), returns CM
+    size_t cm_stride() const { return (size_t)(2 * P_.cfg.L + 1) * P_.n; }
     // pinned host staging buffer, reusable once its previous upload completed
     unsigned char* stage_host(size_t bytes);
     void* stage_upload(size_t bytes, int slot);

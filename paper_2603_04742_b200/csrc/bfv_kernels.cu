@@ -63,6 +63,35 @@ __device__ void chacha20_block(u64 seed, u32 ctr, u32 n0, u32 n1, u32 n2, u32 ou
     for (int i = 0; i < 16; ++i) out[i] = x[i] + s[i];
 }
 
+// The same block computed by an aligned group of 4 lanes, one column each
+// (lane i holds x[i], x[4+i], x[8+i], x[12+i]); diagonal rounds rotate rows
+// b, c, d across the group with shuffles.  Lane i stores words i, 4+i, 8+i,
+// 12+i of the output block.
+__device__ __forceinline__ void chacha20_block_x4(u64 seed, u32 ctr, u32 n0, u32 n1, u32 n2, u32* out) {
+    const int i = threadIdx.x & 3;
+    const u32 sa = i == 0 ? 0x61707865u : i == 1 ? 0x3320646eu : i == 2 ? 0x79622d32u : 0x6b206574u;
+    const u32 sb = i == 0 ? (u32)seed : i == 1 ? (u32)(seed >> 32) : i == 2 ? 0x63737363u : 0x2d68652du;
+    const u32 sc = i == 0 ? 0x62323030u : i == 1 ? 0x2d707267u : i == 2 ? 0x6b657973u : 0x00000001u;
+    const u32 sd = i == 0 ? ctr : i == 1 ? n0 : i == 2 ? n1 : n2;
+    u32 a = sa, b = sb, c = sc, d = sd;
+    const unsigned full = 0xffffffffu;
+#pragma unroll 1
+    for (int r = 0; r < 10; ++r) {
+        CSSC_QR(a, b, c, d);
+        b = __shfl_sync(full, b, (i + 1) & 3, 4);
+        c = __shfl_sync(full, c, (i + 2) & 3, 4);
+        d = __shfl_sync(full, d, (i + 3) & 3, 4);
+        CSSC_QR(a, b, c, d);
+        b = __shfl_sync(full, b, (i + 3) & 3, 4);
+        c = __shfl_sync(full, c, (i + 2) & 3, 4);
+        d = __shfl_sync(full, d, (i + 1) & 3, 4);
+    }
+    out[i] = a + sa;
+    out[4 + i] = b + sb;
+    out[8 + i] = c + sc;
+    out[12 + i] = d + sd;
+}
+
 __device__ __forceinline__ u64 word64(const u32* blk, int w) {
     return (u64)blk[2 * w] | ((u64)blk[2 * w + 1] << 32);
 }
@@ -684,7 +713,7 @@ void launch_pointwise_plain(const DevConsts* dc, const RnsParams& P, u64* X, con
 // encoding, encryption, decryption
 // ---------------------------------------------------------------------------
 __global__ void k_encode_scatter(const DevConsts* __restrict__ dc, const int64_t* vals,
-                                 const u64* offs, u64* M) {
+                                 const u64* offs, u64* M, size_t mstride) {
     const int S = dc->n / 2;
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     const int item = blockIdx.y;
@@ -693,15 +722,16 @@ __global__ void k_encode_scatter(const DevConsts* __restrict__ dc, const int64_t
     const int64_t t = (int64_t)dc->t;
     int64_t v = vals[b + j] % t;
     if (v < 0) v += t;
-    M[(size_t)item * dc->n + dc->pos0[j]] = (u64)v;
+    M[(size_t)item * mstride + dc->pos0[j]] = (u64)v;
 }
 
 void launch_encode_scatter(const DevConsts* dc, const RnsParams& P, const int64_t* vals,
-                           const u64* offs, u64* M, int items, cudaStream_t st) {
+                           const u64* offs, u64* M, int items, cudaStream_t st, size_t mstride) {
     if (!items) return;
-    cudaMemsetAsync(M, 0, sizeof(u64) * (size_t)P.n * items, st);
+    if (!mstride) mstride = (size_t)P.n;
+    cudaMemset2DAsync(M, mstride * 8, 0, (size_t)P.n * 8, (size_t)items, st);
     k_encode_scatter<<<dim3((unsigned)(P.S / EW_THREADS + 1), (unsigned)items), EW_THREADS, 0, st>>>(
-        dc, vals, offs, M);
+        dc, vals, offs, M, mstride);
     CSSC_CHECK_LAUNCH();
 }
 
@@ -713,31 +743,35 @@ void launch_encode_scatter(const DevConsts* dc, const RnsParams& P, const int64_
 __global__ void k_pack_cssc(const DevConsts* __restrict__ dc, const int64_t* __restrict__ CI,
                             const int64_t* __restrict__ VA, const int64_t* __restrict__ V,
                             const int4* __restrict__ rows, int n_rows, const int2* __restrict__ slices,
-                            const int4* __restrict__ cols, int n_chunks, u64* __restrict__ M) {
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+                            const int4* __restrict__ cols, int n_chunks, int log_tpr, u64* __restrict__ M,
+                            size_t mstride) {
+    const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+    const int r = gid >> log_tpr;
     if (r >= n_rows) return;
     const int4 rec = rows[r];
     const int2 sl = slices[rec.w];
     const int64_t t = (int64_t)dc->t;
-    const size_t n = (size_t)dc->n;
-    for (int j = 0; j < rec.y; ++j) {
+    for (int j = gid & ((1 << log_tpr) - 1); j < rec.y; j += 1 << log_tpr) {
         const int4 c = __ldg(cols + sl.x + j);
         const u32 pos = dc->pos0[c.y * c.z + rec.z];
         int64_t a = VA[rec.x + j] % t;
         int64_t b = V[sl.y + CI[rec.x + j]] % t;
-        M[(size_t)c.x * n + pos] = (u64)(a < 0 ? a + t : a);
-        M[(size_t)(n_chunks + c.x) * n + pos] = (u64)(b < 0 ? b + t : b);
+        M[(size_t)c.x * mstride + pos] = (u64)(a < 0 ? a + t : a);
+        M[(size_t)(n_chunks + c.x) * mstride + pos] = (u64)(b < 0 ? b + t : b);
     }
 }
 
 void launch_pack_cssc(const DevConsts* dc, const RnsParams& P, const int64_t* CI, const int64_t* VA,
                       const int64_t* V, const int4* rows, int n_rows, const int2* slices, const int4* cols,
-                      int n_chunks, u64* M, cudaStream_t st) {
+                      int n_chunks, int log_tpr, u64* M, size_t mstride, cudaStream_t st) {
     if (!n_chunks) return;
-    cudaMemsetAsync(M, 0, sizeof(u64) * (size_t)P.n * 2 * n_chunks, st);
-    if (n_rows)
-        k_pack_cssc<<<(unsigned)((n_rows + 127) / 128), 128, 0, st>>>(dc, CI, VA, V, rows, n_rows, slices, cols,
-                                                                     n_chunks, M);
+    cudaMemset2DAsync(M, mstride * 8, 0, (size_t)P.n * 8, (size_t)2 * n_chunks, st);
+    if (n_rows) {
+        // lanes per row ~ mean row length (rows are short in the BASELINE shapes)
+        const size_t threads = (size_t)n_rows << log_tpr;
+        k_pack_cssc<<<(unsigned)((threads + 127) / 128), 128, 0, st>>>(dc, CI, VA, V, rows, n_rows, slices, cols,
+                                                                      n_chunks, log_tpr, M, mstride);
+    }
     CSSC_CHECK_LAUNCH();
 }
 
@@ -760,19 +794,22 @@ void launch_plain_lift(const DevConsts* dc, const RnsParams& P, const u64* M, u6
     CSSC_CHECK_LAUNCH();
 }
 
-// one thread per ChaCha block = 8 coefficients of u; U[item][L][N]
-__global__ void k_enc_sample_u(const DevConsts* __restrict__ dc, u64 seed, const u64* streams,
-                               u64* U) {
+// U[item][L][N]: a 128-thread CTA draws 32 ChaCha blocks (4 lanes each) =
+// 256 coefficients of u into smem, then writes them coalesced per limb
+__global__ void __launch_bounds__(128) k_enc_sample_u(const DevConsts* __restrict__ dc, u64 seed,
+                                                      const u64* streams, u64* U) {
+    __shared__ u32 blk[32][16];
     const int n = dc->n, L = dc->L;
-    const int b = blockIdx.x * blockDim.x + threadIdx.x;
     const int item = blockIdx.y;
-    if (b >= n / 8) return;
     const u64 id = streams[item];
-    u32 blk[16];
-    chacha20_block(seed, (u32)b, DOM_ENC_U, (u32)id, (u32)(id >> 32), blk);
-    for (int w = 0; w < 8; ++w) {
-        const int64_t u = ternary_of(word64(blk, w));
-        const int k = 8 * b + w;
+    const int g = threadIdx.x >> 2;
+    chacha20_block_x4(seed, (u32)(blockIdx.x * 32 + g), DOM_ENC_U, (u32)id, (u32)(id >> 32), blk[g]);
+    __syncthreads();
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int kk = threadIdx.x + 128 * h;
+        const int k = blockIdx.x * 256 + kk;
+        const int64_t u = ternary_of(word64(blk[kk >> 3], kk & 7));
         for (int j = 0; j < L; ++j) U[((size_t)item * L + j) * n + k] = lift_signed(u, dc->mod[j].q);
     }
 }
@@ -780,8 +817,7 @@ __global__ void k_enc_sample_u(const DevConsts* __restrict__ dc, u64 seed, const
 void launch_enc_sample_u(const DevConsts* dc, const RnsParams& P, u64 seed, const u64* streams,
                          u64* U, int items, cudaStream_t st) {
     if (!items) return;
-    k_enc_sample_u<<<dim3((unsigned)((P.n / 8 + 63) / 64), (unsigned)items), 64, 0, st>>>(dc, seed,
-                                                                                         streams, U);
+    k_enc_sample_u<<<dim3((unsigned)(P.n / 256), (unsigned)items), 128, 0, st>>>(dc, seed, streams, U);
     CSSC_CHECK_LAUNCH();
 }
 
@@ -794,7 +830,7 @@ __global__ void k_enc_pk(const DevConsts* __restrict__ dc, const u64* PK, const 
         const Modulus md = dc->mod[j];
         const u64 u = U[((size_t)item * L + j) * n + k];
         for (int p = 0; p < 2; ++p)
-            C[(((size_t)item * 2 + p) * L + j) * n + k] =
+            C[((size_t)item * (2 * L + 1) + (size_t)p * L + j) * n + k] =
                 mul_mod(__ldg(PK + ((size_t)p * L + j) * n + k), u, md);
     }
 }
@@ -806,40 +842,40 @@ void launch_enc_pk(const DevConsts* dc, const RnsParams& P, const u64* PK, const
     CSSC_CHECK_LAUNCH();
 }
 
-// OUT = C + (e0 + Delta m, e1), thread per 8 coefficients
-__global__ void k_enc_finish(const DevConsts* __restrict__ dc, u64 seed, const u64* streams,
-                             const u64* C, const u64* M, u64* const* OUT) {
+// OUT = C + (e0 + Delta m, e1): a 128-thread CTA draws the 16 + 16 ChaCha
+// blocks of its 128 coefficients (4 lanes per block), then one thread per
+// coefficient finishes every limb with coalesced loads and stores
+__global__ void __launch_bounds__(128) k_enc_finish(const DevConsts* __restrict__ dc, u64 seed,
+                                                    const u64* streams, const u64* C, u64* const* OUT) {
+    __shared__ u32 blk[32][16];
     const int n = dc->n, L = dc->L;
-    const int b = blockIdx.x * blockDim.x + threadIdx.x;
     const int item = blockIdx.y;
-    if (b >= n / 8) return;
     const u64 id = streams[item];
-    u32 e0b[16], e1b[16];
-    chacha20_block(seed, (u32)b, DOM_ENC_E0, (u32)id, (u32)(id >> 32), e0b);
-    chacha20_block(seed, (u32)b, DOM_ENC_E1, (u32)id, (u32)(id >> 32), e1b);
+    const int g = threadIdx.x >> 2;
+    chacha20_block_x4(seed, (u32)(blockIdx.x * 16 + (g & 15)), g < 16 ? DOM_ENC_E0 : DOM_ENC_E1, (u32)id,
+                      (u32)(id >> 32), blk[g]);
+    __syncthreads();
+    const int kk = threadIdx.x, k = blockIdx.x * 128 + kk;
+    const int64_t e0 = cbd_of(word64(blk[kk >> 3], kk & 7)), e1 = cbd_of(word64(blk[16 + (kk >> 3)], kk & 7));
+    const size_t cm = (size_t)item * (2 * L + 1) * n + k;
+    const u64 m = C[cm + (size_t)2 * L * n];
     u64* out = OUT[item];
-    for (int w = 0; w < 8; ++w) {
-        const int k = 8 * b + w;
-        const int64_t e0 = cbd_of(word64(e0b, w)), e1 = cbd_of(word64(e1b, w));
-        const u64 m = M[(size_t)item * n + k];
-        for (int j = 0; j < L; ++j) {
-            const u64 q = dc->mod[j].q;
-            const size_t o0 = (((size_t)item * 2 + 0) * L + j) * n + k;
-            const size_t o1 = (((size_t)item * 2 + 1) * L + j) * n + k;
-            u64 c0 = add_mod(C[o0], lift_signed(e0, q), q);
-            c0 = add_mod(c0, shoup(m, dc->delta[j], dc->delta_sh[j], q), q);
-            const u64 c1 = add_mod(C[o1], lift_signed(e1, q), q);
-            out[(size_t)j * n + k] = c0;
-            out[((size_t)L + j) * n + k] = c1;
-        }
+    for (int j = 0; j < L; ++j) {
+        const u64 q = dc->mod[j].q;
+        const size_t o0 = cm + (size_t)j * n;
+        const size_t o1 = cm + (size_t)(L + j) * n;
+        u64 c0 = add_mod(C[o0], lift_signed(e0, q), q);
+        c0 = add_mod(c0, shoup(m, dc->delta[j], dc->delta_sh[j], q), q);
+        const u64 c1 = add_mod(C[o1], lift_signed(e1, q), q);
+        out[(size_t)j * n + k] = c0;
+        out[((size_t)L + j) * n + k] = c1;
     }
 }
 
 void launch_enc_finish(const DevConsts* dc, const RnsParams& P, u64 seed, const u64* streams,
-                       const u64* C, const u64* M, u64* const* OUT, int items, cudaStream_t st) {
+                       const u64* CM, u64* const* OUT, int items, cudaStream_t st) {
     if (!items) return;
-    k_enc_finish<<<dim3((unsigned)((P.n / 8 + 63) / 64), (unsigned)items), 64, 0, st>>>(
-        dc, seed, streams, C, M, OUT);
+    k_enc_finish<<<dim3((unsigned)(P.n / 128), (unsigned)items), 128, 0, st>>>(dc, seed, streams, CM, OUT);
     CSSC_CHECK_LAUNCH();
 }
 

@@ -78,17 +78,18 @@ void launch_pointwise_plain(const DevConsts* dc, const RnsParams& P, u64* X, con
 // chunks [n_chunks, 2 n_chunks)), slot layout applied; see spmvgpu_encrypt_cssc
 void launch_pack_cssc(const DevConsts* dc, const RnsParams& P, const int64_t* CI, const int64_t* VA,
                       const int64_t* V, const int4* rows, int n_rows, const int2* slices, const int4* cols,
-                      int n_chunks, u64* M, cudaStream_t st);
+                      int n_chunks, int log_tpr, u64* M, size_t mstride, cudaStream_t st);
 void launch_encode_scatter(const DevConsts* dc, const RnsParams& P, const int64_t* vals,
-                           const u64* offs, u64* M, int items, cudaStream_t st);
+                           const u64* offs, u64* M, int items, cudaStream_t st, size_t mstride = 0);
 void launch_plain_lift(const DevConsts* dc, const RnsParams& P, const u64* M, u64* PT, int items,
                        cudaStream_t st);
 void launch_enc_sample_u(const DevConsts* dc, const RnsParams& P, u64 seed, const u64* streams,
                          u64* U, int items, cudaStream_t st);
 void launch_enc_pk(const DevConsts* dc, const RnsParams& P, const u64* PK, const u64* U, u64* C,
                    int items, cudaStream_t st);
+// CM[item][2L+1][N]: c0 (L limbs), c1 (L limbs), then the message (coef form mod t)
 void launch_enc_finish(const DevConsts* dc, const RnsParams& P, u64 seed, const u64* streams,
-                       const u64* C, const u64* M, u64* const* OUT, int items, cudaStream_t st);
+                       const u64* CM, u64* const* OUT, int items, cudaStream_t st);
 void launch_mul_s(const DevConsts* dc, const RnsParams& P, u64* X, const u64* S_NTT, int items,
                   cudaStream_t st);
 void launch_dec_scale(const DevConsts* dc, const RnsParams& P, const u64* const* CT,

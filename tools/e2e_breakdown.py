@@ -45,6 +45,13 @@ for _ in range(reps):
     t0 = time.perf_counter()
     pk.spmv_batch(ctx, ms, vs)
     whole.append((time.perf_counter() - t0) * 1e3)
+if "--profile" in sys.argv:
+    import torch
+    ctx.sync()
+    torch.cuda.profiler.start()
+    pk.spmv_batch(ctx, ms, vs)
+    ctx.sync()
+    torch.cuda.profiler.stop()
 for k, v in stages.items():
     print(f"{k:18s} median {statistics.median(v):8.4f} ms  min {min(v):8.4f}")
 print(f"{'spmv_batch':18s} median {statistics.median(whole):8.4f} ms  min {min(whole):8.4f}")
