@@ -70,9 +70,25 @@ CSSC_HD u64 mul_mod(u64 a, u64 b, u64 q, u64 mu1, u64 mu0) {
 struct Modulus {
     u64 q;
     u64 mu1, mu0;  // floor(2^128 / q)
+    u64 mub;       // floor(2^(k+63) / q), k = bit length of q (< 2^64 as q is not a power of 2)
+    u32 sh;        // k - 1
 };
 
-CSSC_HD u64 mul_mod(u64 a, u64 b, const Modulus& m) { return mul_mod(a, b, m.q, m.mu1, m.mu0); }
+// Barrett reduction of z = z1 * 2^64 + z0 < 2^(k+63) (HAC 14.42 with the
+// quotient scaled so one high product gives it): x = floor(z / 2^(k-1)) < 2^64,
+// qhat = hi64(x * mub).  With z = x 2^(k-1) + zl and mub = 2^(k+63)/q - e,
+// z/q - x mub/2^64 = zl/q + x e/2^64 < 2, so floor(z/q) - 2 <= qhat <= floor(z/q)
+// and z - qhat q lies in [0, 3q): two conditional subtractions.  Needs k <= 63;
+// covers a * b for any a < 2^63 and b < q (lazy NTT outputs < 31q included).
+CSSC_HD u64 barrett(u64 z1, u64 z0, const Modulus& m) {
+    const u64 x = (z0 >> m.sh) | (z1 << (64 - m.sh));
+    const u64 qh = umulhi(x, m.mub);
+    u64 r = z0 - qh * m.q;
+    r = r >= m.q ? r - m.q : r;
+    return r >= m.q ? r - m.q : r;
+}
+
+CSSC_HD u64 mul_mod(u64 a, u64 b, const Modulus& m) { return barrett(umulhi(a, b), a * b, m); }
 CSSC_HD u64 reduce64(u64 a, const Modulus& m) { return reduce128(0, a, m.q, m.mu1, m.mu0); }
 
 // Fixed-point fraction floor(y * 2^64 / x) ~ y*R1 + hi(y*R0), R = floor(2^128/x):

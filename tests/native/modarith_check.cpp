@@ -1,0 +1,63 @@
+// Host check of the device modular arithmetic (csrc/modarith.cuh is
+// host-compilable): barrett()/mul_mod() against __int128 arithmetic over
+// random and boundary operands for moduli of every bit length the library
+// admits (t = 65537 up to 62-bit), including the lazy a < 2^63 inputs.
+#include <cstdio>
+#include <random>
+
+#include "modarith.cuh"
+
+using namespace cssc;
+
+static Modulus make(u64 q) {
+    Modulus m{};
+    m.q = q;
+    const int k = 64 - __builtin_clzll(q);
+    m.mub = (u64)(((unsigned __int128)1 << (k + 63)) / q);
+    m.sh = (u32)(k - 1);
+    return m;
+}
+
+int main() {
+    std::mt19937_64 rng(12345);
+    const u64 fixed[] = {65537ULL, (1ULL << 30) - 35, (1ULL << 54) - 33, (1ULL << 58) - 27,
+                         (1ULL << 57) + 29, (1ULL << 60) - 93, (1ULL << 62) - 57, 3ULL};
+    long bad = 0, n = 0;
+    for (int trial = 0; trial < 64; ++trial) {
+        u64 q;
+        if (trial < 8) {
+            q = fixed[trial];
+        } else {
+            const int k = 17 + (int)(rng() % 46);  // 17 .. 62 bits
+            q = (rng() >> (64 - k)) | (1ULL << (k - 1)) | 1ULL;
+            if ((q & (q - 1)) == 0) q += 2;
+        }
+        const Modulus m = make(q);
+        auto check = [&](u64 a, u64 b) {
+            const unsigned __int128 z = (unsigned __int128)a * b;
+            const u64 want = (u64)(z % q);
+            const u64 got = mul_mod(a, b, m);
+            ++n;
+            if (got != want) {
+                if (bad < 10) std::printf("q=%llu a=%llu b=%llu got %llu want %llu\n", (unsigned long long)q,
+                                          (unsigned long long)a, (unsigned long long)b, (unsigned long long)got,
+                                          (unsigned long long)want);
+                ++bad;
+            }
+        };
+        const u64 amax = (1ULL << 63) - 1;
+        for (u64 a : {(u64)0, (u64)1, q - 1, q, 2 * q - 1, 4 * q - 1, amax, amax - q})
+            for (u64 b : {(u64)0, (u64)1, q - 1, q / 2})
+                if ((unsigned __int128)a * b < ((unsigned __int128)1 << (64 - __builtin_clzll(q) + 63))) check(a, b);
+        for (int i = 0; i < 200000; ++i) {
+            const u64 b = rng() % q;
+            u64 a = rng();
+            if (i & 1) a %= q;              // canonical
+            else if ((i & 2) && q < (1ULL << 59)) a %= 31 * q;  // lazy NTT outputs
+            else a >>= 1;                    // anything below 2^63
+            if ((unsigned __int128)a * b < ((unsigned __int128)1 << (64 - __builtin_clzll(q) + 63))) check(a, b);
+        }
+    }
+    std::printf("%ld / %ld mismatches\n", bad, n);
+    return bad ? 1 : 0;
+}
