@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(128) k_ntt_blocks(const DevConsts* __restrict_
     asm volatile("cp.async.commit_group;\n" ::: "memory");
     auto addr = [](int l, int pos) { return l * PITCH + pos; };
     auto twf = [&](int sl, int l, int blk) { return block_tw<LOGN>(tws, sl, l, blk); };
-    const u64 mu = dc->mod[prime].mu1;  // floor(2^64 / q)
+    const Modulus md = dc->mod[prime];
 #pragma unroll 1
     for (int it = it0; it < it1; ++it) {
         u64* cur = smem + ((it - it0) & 1) * TILE;
@@ -216,13 +216,9 @@ __global__ void __launch_bounds__(128) k_ntt_blocks(const DevConsts* __restrict_
         for (int r = 0; r < G::LINES * G::R2 / 256; ++r) {
             const int x = 2 * (threadIdx.x + 128 * r), b = x >> G::B, c = x & (G::R2 - 1);
             u64 a0 = cur[b * PITCH + c], a1 = cur[b * PITCH + c + 1];
-            if (!INV) {  // forward output < 31q: one Barrett step to [0, 3q), then canonical
-                a0 -= umulhi(a0, mu) * q;
-                a1 -= umulhi(a1, mu) * q;
-                a0 = a0 >= q ? a0 - q : a0;
-                a0 = a0 >= q ? a0 - q : a0;
-                a1 = a1 >= q ? a1 - q : a1;
-                a1 = a1 >= q ? a1 - q : a1;
+            if (!INV) {  // forward output < 31q -> canonical
+                a0 = reduce_small_quot(a0, md);
+                a1 = reduce_small_quot(a1, md);
             }
             *reinterpret_cast<ulonglong2*>(dst + x) = make_ulonglong2(a0, a1);
         }

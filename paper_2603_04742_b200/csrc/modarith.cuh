@@ -72,6 +72,7 @@ struct Modulus {
     u64 mu1, mu0;  // floor(2^128 / q)
     u64 mub;       // floor(2^(k+63) / q), k = bit length of q (< 2^64 as q is not a power of 2)
     u32 sh;        // k - 1
+    u32 mus;       // floor(2^(k+20) / q) < 2^21
 };
 
 // Barrett reduction of z = z1 * 2^64 + z0 < 2^(k+63) (HAC 14.42 with the
@@ -89,6 +90,18 @@ CSSC_HD u64 barrett(u64 z1, u64 z0, const Modulus& m) {
 }
 
 CSSC_HD u64 mul_mod(u64 a, u64 b, const Modulus& m) { return barrett(umulhi(a, b), a * b, m); }
+
+// a mod q for a < 2^(k+5) (a lazy forward-NTT output < 31q, say), k >= 7: the
+// quotient is < 32, so 11 leading bits of a and a 21-bit scaled inverse give
+// it in one 32-bit multiply.  a = x 2^(k-6) + al with al < 2^(k-6) < q/32 and
+// mus = 2^(k+20)/q - e: a/q - x mus/2^26 = al/q + x e/2^26 < 1/32 + 2^-15, so
+// the estimate is exact or one short -> one conditional subtraction.
+CSSC_HD u64 reduce_small_quot(u64 a, const Modulus& m) {
+    const u32 x = (u32)(a >> (m.sh - 5));
+    const u32 qh = (x * m.mus) >> 26;
+    const u64 r = a - (u64)qh * m.q;
+    return r >= m.q ? r - m.q : r;
+}
 CSSC_HD u64 reduce64(u64 a, const Modulus& m) { return reduce128(0, a, m.q, m.mu1, m.mu0); }
 
 // Fixed-point fraction floor(y * 2^64 / x) ~ y*R1 + hi(y*R0), R = floor(2^128/x):

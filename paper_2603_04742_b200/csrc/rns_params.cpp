@@ -175,9 +175,10 @@ RnsParams::RnsParams(const RnsConfig& c) : cfg(c), host{} {
         d.mod[i].q = q;
         floor_pow128_div(q, d.mod[i].mu1, d.mod[i].mu0, rem);
         const int k = 64 - __builtin_clzll(q);
-        if (k < 2 || k > 62) throw std::invalid_argument("modulus bit length out of range");
+        if (k < 7 || k > 62) throw std::invalid_argument("modulus bit length out of range");
         d.mod[i].mub = (u64)(((unsigned __int128)1 << (k + 63)) / q);
         d.mod[i].sh = (u32)(k - 1);
+        d.mod[i].mus = (u32)(((unsigned __int128)1 << (k + 20)) / q);
         psi[i] = root_of_unity(q, two_n);
         const u64 psi_inv = inv_mod_host(psi[i], q);
         tw_fwd[i].resize(2 * (size_t)n);

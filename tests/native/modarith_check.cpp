@@ -15,13 +15,14 @@ static Modulus make(u64 q) {
     const int k = 64 - __builtin_clzll(q);
     m.mub = (u64)(((unsigned __int128)1 << (k + 63)) / q);
     m.sh = (u32)(k - 1);
+    m.mus = (u32)(((unsigned __int128)1 << (k + 20)) / q);
     return m;
 }
 
 int main() {
     std::mt19937_64 rng(12345);
     const u64 fixed[] = {65537ULL, (1ULL << 30) - 35, (1ULL << 54) - 33, (1ULL << 58) - 27,
-                         (1ULL << 57) + 29, (1ULL << 60) - 93, (1ULL << 62) - 57, 3ULL};
+                         (1ULL << 57) + 29, (1ULL << 60) - 93, (1ULL << 62) - 57, 67ULL};
     long bad = 0, n = 0;
     for (int trial = 0; trial < 64; ++trial) {
         u64 q;
@@ -45,6 +46,24 @@ int main() {
                 ++bad;
             }
         };
+        // reduce_small_quot: every a < 2^(k+5)
+        const int kq = 64 - __builtin_clzll(q);
+        if (kq >= 7 && kq <= 58) {
+            const u64 lim = 1ULL << (kq + 5);
+            for (u64 a : {(u64)0, q - 1, q, 2 * q - 1, 31 * q - 1, lim - 1}) {
+                if (a >= lim) continue;
+                ++n;
+                if (reduce_small_quot(a, m) != a % q) ++bad;
+            }
+            for (int i = 0; i < 100000; ++i) {
+                const u64 a = rng() % lim;
+                ++n;
+                if (reduce_small_quot(a, m) != a % q) {
+                    if (bad < 10) std::printf("small q=%llu a=%llu\n", (unsigned long long)q, (unsigned long long)a);
+                    ++bad;
+                }
+            }
+        }
         const u64 amax = (1ULL << 63) - 1;
         for (u64 a : {(u64)0, (u64)1, q - 1, q, 2 * q - 1, 4 * q - 1, amax, amax - q})
             for (u64 b : {(u64)0, (u64)1, q - 1, q / 2})

@@ -11,6 +11,10 @@ logn = int(sys.argv[1]) if len(sys.argv) > 1 else 14
 limbs = int(sys.argv[2]) if len(sys.argv) > 2 else 1152
 ctx = pk.Context(logn=logn, seed=1)
 print("warm", ctx.probe_ntt_us(limbs, False, 3), ctx.probe_ntt_us(limbs, True, 3))
+n = 1 << logn
+for _ in range(3):
+    f20, i20 = ctx.probe_ntt_us(limbs, False, 20), ctx.probe_ntt_us(limbs, True, 20)
+    print(f"reps20 fwd {f20:.2f} us ({limbs * n // 2 * logn / (f20 * 1e-6) / 1e9:.1f} Gbfly/s) inv {i20:.2f} us")
 torch.cuda.profiler.start()
 f = ctx.probe_ntt_us(limbs, False, 1)
 i = ctx.probe_ntt_us(limbs, True, 1)
