@@ -7,6 +7,7 @@
 // (oracle/bfv_oracle.c) states the same integer formulas.
 #include <cstdio>
 #include <type_traits>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 
@@ -228,8 +229,15 @@ __global__ void __launch_bounds__(128) k_ntt_blocks(const DevConsts* __restrict_
 
 // items per block-phase CTA: amortise twiddle staging while keeping >= ~2 waves
 static int blocks_ipc(int items, int limbs_per_item, int ctas_per_limb) {
+    static const int forced = [] {
+        const char* e = std::getenv("CSSC_BLOCKS_IPC");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (forced > 0) return std::min(forced, std::max(items, 1));
+    // largest power of two <= 8 that still leaves >= 3 CTAs per SM (measured:
+    // 144 limbs of 2^14 run 6% faster at ipc 4 than at 1; 1152 limbs saturate at 8)
     int ipc = 1;
-    while (ipc < 8 && (long)items * limbs_per_item * ctas_per_limb / (2 * ipc) >= 2 * 148 * 4) ipc *= 2;
+    while (ipc < 8 && ipc < items && (long)items * limbs_per_item * ctas_per_limb / (2 * ipc) >= 148 * 3) ipc *= 2;
     return ipc;
 }
 
@@ -357,9 +365,11 @@ __device__ __forceinline__ void extend_exact(const DevConsts* __restrict__ dc,
 #pragma unroll
     for (int j = 0; j < ny; ++j) {
         const u64 p = dc->mod[e.yi[j]].q;
+        // lazy sum: nx <= 16 terms < 2p each stay below 2^(k+5) -> one reduction
         u64 acc = 0;
 #pragma unroll
-        for (int i = 0; i < nx; ++i) acc = add_mod(acc, shoup(y[i], e.xhat_y[i][j], e.xhat_y_sh[i][j], p), p);
+        for (int i = 0; i < nx; ++i) acc += shoup_lazy(y[i], e.xhat_y[i][j], e.xhat_y_sh[i][j], p);
+        acc = reduce_small_quot(acc, dc->mod[e.yi[j]]);
         out[j] = sub_mod(acc, shoup(v, e.X_y[j], e.X_y_sh[j], p), p);
     }
 }
@@ -454,8 +464,8 @@ __global__ void k_mul_scale(const DevConsts* __restrict__ dc, const u64* __restr
             const u64 bj = dc->mod[L + K + j].q;
             u64 acc = 0;
 #pragma unroll
-            for (int i = 0; i < L; ++i)
-                acc = add_mod(acc, shoup(xi[i], dc->QhatB[i][j], dc->QhatB_sh[i][j], bj), bj);
+            for (int i = 0; i < L; ++i) acc += shoup_lazy(xi[i], dc->QhatB[i][j], dc->QhatB_sh[i][j], bj);
+            acc = reduce_small_quot(acc, dc->mod[L + K + j]);
             const u64 alpha = shoup(sub_mod(acc, z[(size_t)(L + j) * n + k], bj), dc->QinvB[j],
                                     dc->QinvB_sh[j], bj);
             w[j] = sub_mod(rr, shoup(alpha, dc->tB[j], dc->tB_sh[j], bj), bj);
@@ -523,8 +533,8 @@ __global__ void k_ks_modup(const DevConsts* __restrict__ dc, const u64* const* S
                 const u64 m = dc->mod[j].q;
                 v = 0;
 #pragma unroll
-                for (int i = lo; i < hi; ++i)
-                    v = add_mod(v, shoup(y[i], dc->dig_hat[i][j], dc->dig_hat_sh[i][j], m), m);
+                for (int i = lo; i < hi; ++i) v += shoup_lazy(y[i], dc->dig_hat[i][j], dc->dig_hat_sh[i][j], m);
+                v = reduce_small_quot(v, dc->mod[j]);
             }
             out[(size_t)j * n + k] = v;
         }
@@ -618,8 +628,8 @@ __global__ void k_ks_moddown(const DevConsts* __restrict__ dc, const u64* __rest
             const u64 q = dc->mod[j].q;
             u64 c = 0;
 #pragma unroll
-            for (int kk = 0; kk < K; ++kk)
-                c = add_mod(c, shoup(y[kk], dc->phat_q[kk][j], dc->phat_q_sh[kk][j], q), q);
+            for (int kk = 0; kk < K; ++kk) c += shoup_lazy(y[kk], dc->phat_q[kk][j], dc->phat_q_sh[kk][j], q);
+            c = reduce_small_quot(c, dc->mod[j]);
             u64 v = shoup(sub_mod(acc[(size_t)j * n + k], c, q), dc->Pinv_q[j], dc->Pinv_q_sh[j], q);
             if (base) v = add_mod(v, base[(size_t)j * n + k], q);
             if (ex) v = add_mod(v, ex[(size_t)j * n + k], q);

@@ -94,8 +94,9 @@ __global__ void __launch_bounds__(Ntt2<LOGN>::TC, 256 / Ntt2<LOGN>::TC * 2) k_ks
                 u64 x = __ldg(src + (size_t)i * G::N + idx);
                 x = neg ? neg_mod(x, qi) : x;
                 const u64 y = shoup(x, dc->dig_hat_inv[i], dc->dig_hat_inv_sh[i], qi);
-                v = add_mod(v, shoup(y, dc->dig_hat[i][j], dc->dig_hat_sh[i][j], m), m);
+                v += shoup_lazy(y, dc->dig_hat[i][j], dc->dig_hat_sh[i][j], m);  // alpha <= 16 terms < 2m
             }
+            v = reduce_small_quot(v, dc->mod[j]);
         }
         tile[c * 16 + jl] = v;
     }

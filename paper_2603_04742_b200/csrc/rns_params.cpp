@@ -132,7 +132,8 @@ void fill_ext(ExtConsts& e, const std::vector<u64>& X, const std::vector<int>& x
 
 RnsParams::RnsParams(const RnsConfig& c) : cfg(c), host{} {
     if (c.logn < 4 || c.logn > 15) throw std::invalid_argument("logn must be in [4, 15]");
-    if (c.L < 1 || c.L > MAXL || c.K < 1 || c.K > MAXL || c.alpha < 1 || c.alpha > c.L)
+    // L + 1 <= 16 auxiliary terms keep the lazy basis-conversion sums below 32 q
+    if (c.L < 1 || c.L > MAXL - 1 || c.K < 1 || c.K > MAXL || c.alpha < 1 || c.alpha > c.L)
         throw std::invalid_argument("prime counts out of range");
     if (c.qbits < 30 || c.qbits > 58 || c.pbits < 30 || c.pbits > 58)
         // <= 58 bits: 64q headroom lets the forward NTT skip per-butterfly corrections
