@@ -597,8 +597,10 @@ void launch_ks_inner(const DevConsts* dc, const RnsParams& P, const u64* DX,
 
 // E4 + fused adds: out = BASE[item] + EXTRA[item] + phi_g(RSRC[item].c0) + ModDown(acc);
 // per-item BASE / EXTRA entries may be null
+// one polynomial per grid z-slice; the output loop is only partly unrolled so
+// the acc/base/extra loads of all limbs are not hoisted into registers at once
 template <int LT, int KT, int AT>
-__global__ void k_ks_moddown(const DevConsts* __restrict__ dc, const u64* __restrict__ ACC,
+__global__ void __launch_bounds__(128, 6) k_ks_moddown(const DevConsts* __restrict__ dc, const u64* __restrict__ ACC,
                              const u64* const* BASE, const u64* const* RSRC, const u32* ginv,
                              u64* const* OUT, const u64* const* EXTRA) {
     const int n = dc->n, L = LT ? LT : dc->L, K = KT ? KT : dc->K, LK = L + K;
@@ -609,8 +611,8 @@ __global__ void k_ks_moddown(const DevConsts* __restrict__ dc, const u64* __rest
     int ridx = k;
     if (RSRC) ridx = automorph_src(ginv ? ginv[item] : 0u, k, n, neg);
     u64 y[MAXL];
-#pragma unroll
-    for (int p = 0; p < 2; ++p) {
+    {
+        const int p = blockIdx.z;
         const u64* acc = ACC + ((size_t)item * 2 + p) * PL;
 #pragma unroll
         for (int kk = 0; kk < K; ++kk) {
@@ -623,7 +625,7 @@ __global__ void k_ks_moddown(const DevConsts* __restrict__ dc, const u64* __rest
         const u64* ex = EXTRA ? EXTRA[item] : nullptr;
         if (ex) ex += (size_t)p * L * n;
         const u64* rs = (RSRC && p == 0) ? RSRC[item] : nullptr;
-#pragma unroll
+#pragma unroll 2
         for (int j = 0; j < L; ++j) {
             const u64 q = dc->mod[j].q;
             u64 c = 0;
@@ -647,8 +649,9 @@ void launch_ks_moddown(const DevConsts* dc, const RnsParams& P, const u64* ACC,
                        u64* const* OUT, int items, cudaStream_t st, const u64* const* EXTRA) {
     if (!items) return;
     dispatch_shape(P, [&](auto l_, auto k_, auto a_) {
-        k_ks_moddown<SHAPE_ARGS><<<ew_grid(P.n, items), EW_THREADS, 0, st>>>(dc, ACC, BASE, RSRC, ginv, OUT,
-                                                                             EXTRA);
+        dim3 g = ew_grid(P.n, items);
+        g.z = 2;
+        k_ks_moddown<SHAPE_ARGS><<<g, EW_THREADS, 0, st>>>(dc, ACC, BASE, RSRC, ginv, OUT, EXTRA);
     });
     CSSC_CHECK_LAUNCH();
 }

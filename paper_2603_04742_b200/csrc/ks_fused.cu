@@ -120,12 +120,14 @@ __global__ void __launch_bounds__(Ntt2<LOGN>::TC, 256 / Ntt2<LOGN>::TC * 2) k_ks
 // K2: NTT block phase + key inner product + INTT block phase
 // ---------------------------------------------------------------------------
 template <int LOGN, int LT, int KT, int AT>
-__global__ void __launch_bounds__(128) k_ks_blocks_inner(const DevConsts* __restrict__ dc, const u64* __restrict__ DX,
+__global__ void __launch_bounds__(256) k_ks_blocks_inner(const DevConsts* __restrict__ dc, const u64* __restrict__ DX,
                                                          const u64* const* KEY, u64* __restrict__ ACC) {
     using G = Ntt2<LOGN>;
     extern __shared__ u64 smem[];
     constexpr int PITCH = G::PITCH;
     constexpr int TW = G::LINES * PITCH;
+    constexpr int T = 256;
+    constexpr int PER = G::LINES * G::R2 / T;  // elements per thread
     u64* work = smem;
     u64* acc0 = smem + TW;
     u64* acc1 = smem + 2 * TW;
@@ -143,22 +145,20 @@ __global__ void __launch_bounds__(128) k_ks_blocks_inner(const DevConsts* __rest
     const size_t base = (size_t)blk0 * G::R2;
     const u64* key = KEY[item];
     const size_t PL = (size_t)LK * G::N;
-    constexpr int PER = G::LINES * G::R2 / 256;  // ulonglong2 per thread
+    // element x = threadIdx.x + T r of the tile (line x >> B, column x & (R2-1)):
+    // consecutive lanes touch consecutive words in HBM and in smem (conflict free)
+    auto saddr = [](int x) { return (x >> G::B) * PITCH + (x & (G::R2 - 1)); };
     auto addr = [](int l, int pos) { return l * PITCH + pos; };
     auto twf = [&](int sl, int l, int blk) { return block_tw<LOGN>(tws, sl, l, blk); };
     load_block_twiddles<LOGN>(tws, dc->tw[j].fwd, blk0);
 #pragma unroll 1
     for (int dg = 0; dg < dnum; ++dg) {
         const u64* d = DX + (((size_t)item * dnum + dg) * LK + j) * G::N + base;
-        ulonglong2 v[PER];
-#pragma unroll
-        for (int r = 0; r < PER; ++r) v[r] = __ldg(reinterpret_cast<const ulonglong2*>(d) + threadIdx.x + 128 * r);
         if (dg) __syncthreads();  // previous digit's accumulate finished reading `work`
 #pragma unroll
         for (int r = 0; r < PER; ++r) {
-            const int x = 2 * (threadIdx.x + 128 * r), b = x >> G::B, c = x & (G::R2 - 1);
-            work[b * PITCH + c] = v[r].x;
-            work[b * PITCH + c + 1] = v[r].y;
+            const int x = threadIdx.x + T * r;
+            cp_async8(work + saddr(x), d + x);
         }
         cp_async_wait_all();
         __syncthreads();
@@ -168,23 +168,15 @@ __global__ void __launch_bounds__(128) k_ks_blocks_inner(const DevConsts* __rest
         const u64* k1 = key + ((size_t)dg * 2 + 1) * PL + (size_t)j * G::N + base;
 #pragma unroll
         for (int r = 0; r < PER; ++r) {
-            const int i = threadIdx.x + 128 * r, x = 2 * i, b = x >> G::B, c = x & (G::R2 - 1);
-            const ulonglong2 a = __ldg(reinterpret_cast<const ulonglong2*>(k0) + i);
-            const ulonglong2 e = __ldg(reinterpret_cast<const ulonglong2*>(k1) + i);
-            const int s0 = b * PITCH + c;
-            const u64 w0 = work[s0], w1 = work[s0 + 1];
-            const u64 p00 = mul_mod(w0, a.x, md), p01 = mul_mod(w1, a.y, md);
-            const u64 p10 = mul_mod(w0, e.x, md), p11 = mul_mod(w1, e.y, md);
+            const int x = threadIdx.x + T * r, s0 = saddr(x);
+            const u64 w = work[s0];
+            const u64 p0 = mul_mod(w, __ldg(k0 + x), md), p1 = mul_mod(w, __ldg(k1 + x), md);
             if (dg == 0) {
-                acc0[s0] = p00;
-                acc0[s0 + 1] = p01;
-                acc1[s0] = p10;
-                acc1[s0 + 1] = p11;
+                acc0[s0] = p0;
+                acc1[s0] = p1;
             } else {
-                acc0[s0] = add_mod(acc0[s0], p00, q);
-                acc0[s0 + 1] = add_mod(acc0[s0 + 1], p01, q);
-                acc1[s0] = add_mod(acc1[s0], p10, q);
-                acc1[s0 + 1] = add_mod(acc1[s0 + 1], p11, q);
+                acc0[s0] = add_mod(acc0[s0], p0, q);
+                acc1[s0] = add_mod(acc1[s0], p1, q);
             }
         }
     }
@@ -200,8 +192,8 @@ __global__ void __launch_bounds__(128) k_ks_blocks_inner(const DevConsts* __rest
         u64* dst = ACC + (((size_t)item * 2 + p) * LK + j) * G::N + base;
 #pragma unroll
         for (int r = 0; r < PER; ++r) {
-            const int i = threadIdx.x + 128 * r, x = 2 * i, b = x >> G::B, c = x & (G::R2 - 1);
-            reinterpret_cast<ulonglong2*>(dst)[i] = make_ulonglong2(a[b * PITCH + c], a[b * PITCH + c + 1]);
+            const int x = threadIdx.x + T * r;
+            dst[x] = a[saddr(x)];
         }
     }
 }
@@ -241,7 +233,7 @@ static void ks_fused_t(const DevConsts* dc, const RnsParams& P, const u64* const
     k_ks_modup_cols<LOGN, LT, KT, AT><<<items * dnum * LK * G::CTAS_C, G::TC, smem1, st>>>(dc, SRC, SRCC, src_poly,
                                                                                       ginv, DX);
     KS_CHECK();
-    k_ks_blocks_inner<LOGN, LT, KT, AT><<<items * LK * G::CTAS_B, 128, smem2, st>>>(dc, DX, KEY, ACC);
+    k_ks_blocks_inner<LOGN, LT, KT, AT><<<items * LK * G::CTAS_B, 256, smem2, st>>>(dc, DX, KEY, ACC);
     KS_CHECK();
     NttJob j;
     for (int i = 0; i < MAX_JOB_LIMBS; ++i) j.pidx[i] = (signed char)(i % LK);
