@@ -187,6 +187,47 @@ def run_reference_arm(args, cfg):
             "e2e": {"value": round(v, 4), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
+def key_switch_roofline(ctx, job, stream, flush):
+    """Per launch group of one eager plan run (CUDA events between groups, L2
+    flushed first): compulsory HBM bytes (fused rotate+add = 3C per
+    item + KEY per distinct key) / device time vs the measured copy bandwidth,
+    and the group's NTT butterflies / time vs the butterfly probe."""
+    import torch
+
+    with torch.cuda.stream(stream):
+        flush.zero_()
+    torch.cuda.synchronize()
+    phases = job.profile()
+    peak = ctx.probe_butterfly_peak()
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    n = ctx.n
+    bfly_per_limb = (n // 2) * (n.bit_length() - 1)
+    rows = []
+    for p in phases:
+        if p["us"] <= 0:
+            continue
+        gbs = p["bytes"] / (p["us"] * 1e-6) / 1e9
+        gbfly = p["limb_ntts"] * bfly_per_limb / (p["us"] * 1e-6) / 1e9
+        rows.append({"group": p["name"], "items": p["items"], "us": round(p["us"], 2), "bytes": p["bytes"],
+                     "hbm_gbs": round(gbs, 1), "hbm_frac": round(gbs / hbm_peak, 4),
+                     "ntt_gbfly": round(gbfly, 1), "int_frac": round(gbfly * 1e9 / peak, 4)})
+    ks = [r for r in rows if r["group"].startswith("rotate level") or r["group"] == "multiply+relin"]
+    rot = [r for r in rows if r["group"].startswith("rotate level")]
+    summ = None
+    if rot:
+        us = sum(r["us"] for r in rot)
+        by = sum(r["bytes"] for r in rot)
+        ntt = sum(r["ntt_gbfly"] * r["us"] for r in rot) / us
+        summ = {"us": round(us, 2), "items": sum(r["items"] for r in rot), "bytes": by,
+                "hbm_gbs": round(by / (us * 1e-6) / 1e9, 1), "hbm_frac": round(by / (us * 1e-6) / 1e9 / hbm_peak, 4),
+                "ntt_gbfly": round(ntt, 1), "int_frac": round(ntt * 1e9 / peak, 4)}
+    return {"rotations": summ, "groups": rows if ks else rows, "hbm_peak_gbs": hbm_peak,
+            "int_peak_gbfly": round(peak / 1e9, 1),
+            "note": "eager run, one launch group at a time; bytes = compulsory (SURVEY 8(d)); "
+                    "int_frac counts NTT butterflies only (ModUp/MAC/ModDown modmuls excluded)"}
+
+
 def measure_config(pk, cfg, args, rank, world, device, full=True):
     import torch
 
@@ -238,6 +279,7 @@ def measure_config(pk, cfg, args, rank, world, device, full=True):
     out = {"name": cfg["name"], "ms_per_step": ms_step, "median_ms": statistics.median(times),
            "min_ms": min(times), "verified": verified, "plan": st, "clocks": clocks,
            "measured_noise_bits": min(r["measured_noise"] for r in res if r["n_ct"] > 0)}
+    out["key_switch"] = key_switch_roofline(ctx, job, stream, flush)
     if not full:
         job.close()
         ctx.close()
@@ -333,7 +375,9 @@ def main():
                                    "chunks": o["plan"]["chunks"], "rotations": o["plan"]["rotations"],
                                    "limb_ntts": o["plan"]["limb_ntts_per_run"],
                                    "whole_plan_hbm_gbs": round(o["plan"]["hbm_bytes_algorithmic"] /
-                                                               (o["ms_per_step"] * 1e-3) / 1e9, 1)}
+                                                               (o["ms_per_step"] * 1e-3) / 1e9, 1),
+                                   "key_switch": o["key_switch"]["rotations"],
+                                   "groups": o["key_switch"]["groups"]}
             except Exception as e:  # a failing side config must not hide the headline
                 others[f"C{c}"] = {"error": str(e)[:200]}
 
@@ -360,7 +404,8 @@ def main():
                        "l2": "flushed (256 MiB write) before every timed step",
                        "parallelism": f"replica per GPU x{world}"},
             "clocks": head["clocks"], "e2e": head["e2e"], "gpu_launches": head["plan"]["kernels_per_run"],
-            "roofline": head["roofline"], "cpu_baseline": cpu, "verified_exact": head["verified"],
+            "roofline": head["roofline"], "key_switch": head["key_switch"],
+            "cpu_baseline": cpu, "verified_exact": head["verified"],
             "measured_noise_bits_min": head["measured_noise_bits"],
             "whole_plan_hbm_gbs": head["whole_plan_hbm_gbs"],
             "limb_ntts_per_step": head["plan"]["limb_ntts_per_run"], "other_configs": others,

@@ -155,6 +155,15 @@ typedef struct {
     uint64_t key_bytes_per_run;
 } spmvgpu_plan_stats;
 int spmvgpu_plan_stats_get(const spmvgpu_plan* p, spmvgpu_plan_stats* out);
+/* one eager run with CUDA events between launch groups (multiply+relin, each
+ * rotate level, the level-0 add, mask accumulate): device time per group, its
+ * compulsory HBM bytes (SURVEY 8(d) op table) and limb NTTs; *count = groups */
+typedef struct {
+    char name[32];
+    double us;
+    uint64_t items, bytes, limb_ntts;
+} spmvgpu_phase;
+int spmvgpu_plan_profile(spmvgpu_plan* p, spmvgpu_phase* phases, int cap, int* count);
 void spmvgpu_plan_destroy(spmvgpu_plan* p);
 
 /* ---- protocol level (host C++ above the device ABI) ---- */
@@ -196,6 +205,7 @@ int cssc_job_encrypt(cssc_job* j);            /* client phase: encode + encrypt 
 int cssc_job_cloud(cssc_job* j, int use_graph); /* cloud phase, enqueued (no sync) */
 int cssc_job_finish(cssc_job* j, int64_t* const* values, cssc_result* res); /* decrypt */
 int cssc_job_plan_stats(const cssc_job* j, spmvgpu_plan_stats* out);
+int cssc_job_profile(cssc_job* j, spmvgpu_phase* phases, int cap, int* count); /* see spmvgpu_plan_profile */
 int cssc_job_input_bytes(const cssc_job* j, uint64_t* h2d, uint64_t* d2h);
 void cssc_job_destroy(cssc_job* j);
 

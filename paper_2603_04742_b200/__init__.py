@@ -54,6 +54,11 @@ class Message(C.Structure):
     _fields_ = [(n, C.c_int64) for n in ("from_", "to", "kind", "payload_bytes", "ciphertext_count")]
 
 
+class PhaseC(C.Structure):
+    _fields_ = [("name", C.c_char * 32), ("us", C.c_double), ("items", C.c_uint64), ("bytes", C.c_uint64),
+                ("limb_ntts", C.c_uint64)]
+
+
 class CsrC(C.Structure):
     _fields_ = [("rows", C.c_uint64), ("cols", C.c_uint64), ("row_ptrs", i64p),
                 ("col_indices", i64p), ("values", i64p)]
@@ -102,6 +107,7 @@ _SIGS = {
     "spmvgpu_plan_run": (C.c_int, [C.c_void_p]),
     "spmvgpu_plan_capture": (C.c_int, [C.c_void_p]),
     "spmvgpu_plan_stats_get": (C.c_int, [C.c_void_p, C.POINTER(PlanStats)]),
+    "spmvgpu_plan_profile": (C.c_int, [C.c_void_p, C.POINTER(PhaseC), C.c_int, C.POINTER(C.c_int)]),
     "spmvgpu_plan_destroy": (None, [C.c_void_p]),
     "cssc_spmv_partitioned": (C.c_int, [C.c_void_p, C.POINTER(CsrC), i64p, C.c_uint64, C.c_uint64,
                                         C.c_int, i64p, C.POINTER(ResultC), C.POINTER(Message),
@@ -114,6 +120,7 @@ _SIGS = {
     "cssc_job_cloud": (C.c_int, [C.c_void_p, C.c_int]),
     "cssc_job_finish": (C.c_int, [C.c_void_p, C.POINTER(i64p), C.POINTER(ResultC)]),
     "cssc_job_plan_stats": (C.c_int, [C.c_void_p, C.POINTER(PlanStats)]),
+    "cssc_job_profile": (C.c_int, [C.c_void_p, C.POINTER(PhaseC), C.c_int, C.POINTER(C.c_int)]),
     "cssc_job_input_bytes": (C.c_int, [C.c_void_p, u64p, u64p]),
     "cssc_job_destroy": (None, [C.c_void_p]),
     "cssc_pack_chunks": (C.c_int64, [C.POINTER(CsrC), C.c_uint64, i64p, i64p, i64p, i64p, i64p, u64p]),
@@ -486,6 +493,15 @@ class Job:
         s = PlanStats()
         check(lib().cssc_job_plan_stats(self.h, C.byref(s)))
         return {k: int(getattr(s, k)) for k, _ in PlanStats._fields_}
+
+    def profile(self) -> list:
+        """Device time, compulsory bytes and limb NTTs per launch group (one eager run)."""
+        cap = 64
+        ph = (PhaseC * cap)()
+        cnt = C.c_int()
+        check(lib().cssc_job_profile(self.h, ph, cap, C.byref(cnt)))
+        return [{"name": p.name.decode(), "us": p.us, "items": int(p.items), "bytes": int(p.bytes),
+                 "limb_ntts": int(p.limb_ntts)} for p in ph[: min(cnt.value, cap)]]
 
     def io_bytes(self):
         a, b = C.c_uint64(), C.c_uint64()

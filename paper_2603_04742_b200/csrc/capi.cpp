@@ -458,6 +458,21 @@ int spmvgpu_plan_stats_get(const spmvgpu_plan* p, spmvgpu_plan_stats* o) {
         o->key_bytes_per_run = s.key_bytes;
     });
 }
+int spmvgpu_plan_profile(spmvgpu_plan* p, spmvgpu_phase* phases, int cap, int* count) {
+    return guard([&] {
+        if (!p || !count) throw std::invalid_argument("null argument");
+        const auto ph = p->plan->profile();
+        *count = (int)ph.size();
+        for (int i = 0; i < (int)ph.size() && i < cap; ++i) {
+            std::memset(&phases[i], 0, sizeof phases[i]);
+            std::strncpy(phases[i].name, ph[i].name.c_str(), sizeof phases[i].name - 1);
+            phases[i].us = ph[i].us;
+            phases[i].items = ph[i].items;
+            phases[i].bytes = ph[i].bytes;
+            phases[i].limb_ntts = ph[i].limb_ntts;
+        }
+    });
+}
 void spmvgpu_plan_destroy(spmvgpu_plan* p) { delete p; }
 
 // ---------------------------------------------------------------- protocol front door
@@ -511,6 +526,13 @@ int cssc_job_plan_stats(const cssc_job* j, spmvgpu_plan_stats* out) {
     return guard([&] {
         std::memset(out, 0, sizeof *out);
         if (j->job->plan()) spmvgpu_plan_stats_get(j->job->plan(), out);
+    });
+}
+int cssc_job_profile(cssc_job* j, spmvgpu_phase* phases, int cap, int* count) {
+    return guard([&] {
+        if (!j || !j->job->plan()) throw std::invalid_argument("job has no plan yet (run cloud first)");
+        const int st = spmvgpu_plan_profile(j->job->plan(), phases, cap, count);
+        if (st != SPMVGPU_OK) throw std::runtime_error(g_err);
     });
 }
 int cssc_job_input_bytes(const cssc_job* j, uint64_t* h2d, uint64_t* d2h) {

@@ -206,6 +206,7 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
         lv.key = put(key);
         lv.ginv = put(gi);
         lv.extra = put(extra);
+        lv.keys = (int)lvl_keys.size();
         levels_.push_back(lv);
         stats_.hbm_bytes += (u64)lv.items * 3 * C + lvl_keys.size() * KEY;
         stats_.key_bytes += lvl_keys.size() * KEY;
@@ -266,19 +267,31 @@ CloudPlan::~CloudPlan() {
     if (graph_) cudaGraphDestroy(graph_);
 }
 
-void CloudPlan::record() {
+void CloudPlan::record(std::vector<cudaEvent_t>* marks) {
     if (n_ == 0) return;
     const RnsParams& P = ctx_.params();
     const int L = P.cfg.L, logn = P.cfg.logn;
     cudaStream_t st = ctx_.stream();
+    auto mark = [&] {
+        if (!marks) return;
+        cudaEvent_t e;
+        cuda_check(cudaEventCreate(&e), "event");
+        cuda_check(cudaEventRecord(e, st), "event record");
+        marks->push_back(e);
+    };
+    mark();
     ctx_.mul_relin_dev(A_, B_, PROD_, n_, T_.words(), Z_.words(), D2_.words(), DX_.words(),
                        ACC_.words(), RLK_);
+    mark();
     for (size_t l = 0; l < levels_.size(); ++l) {
         const Level& lv = levels_[l];
         ctx_.rotate_dev(lv.src, lv.ginv, lv.key, lv.base, lv.out, lv.items, DX_.words(), ACC_.words(),
                         lv.extra);
-        if (l == 0 && add_items_)
+        mark();
+        if (l == 0 && add_items_) {
             launch_add(ctx_.dconsts(), P, ADD_A_, ADD_B_, ADD_OUT_, add_items_, st);
+            mark();
+        }
     }
     std::vector<int> qidx(L);
     std::iota(qidx.begin(), qidx.end(), 0);
@@ -291,6 +304,41 @@ void CloudPlan::record() {
     NttJob inv = ctx_.job(RES, nullptr, 2 * L, qidx);
     inv.dst_items = OUT_;
     launch_ntt(ctx_.dconsts(), logn, true, inv, ns_, st);
+    mark();
+}
+
+std::vector<PhaseTiming> CloudPlan::profile() {
+    std::vector<PhaseTiming> out;
+    if (n_ == 0) return out;
+    const RnsParams& P = ctx_.params();
+    const int L = P.cfg.L, LK = L + P.cfg.K, M = L + P.nB;
+    const u64 C = sizeof(u64) * ctx_.ct_words(), KEY = sizeof(u64) * ctx_.ksk_words(),
+              PT = sizeof(u64) * ctx_.poly_words();
+    const u64 ks_ntts = (u64)P.dnum * LK + 2 * LK;
+    out.push_back({"multiply+relin", 0, (u64)n_, (u64)n_ * 3 * C + KEY, (u64)n_ * (7 * M + ks_ntts)});
+    for (size_t l = 0; l < levels_.size(); ++l) {
+        const Level& lv = levels_[l];
+        out.push_back({"rotate level " + std::to_string(l), 0, (u64)lv.items,
+                       (u64)lv.items * 3 * C + (u64)lv.keys * KEY, (u64)lv.items * ks_ntts});
+        if (l == 0 && add_items_) out.push_back({"add", 0, (u64)add_items_, (u64)add_items_ * 3 * C, 0});
+    }
+    out.push_back({"mask accumulate", 0, (u64)n_, (u64)n_ * 2 * C + (u64)n_masks_ * PT,
+                   (u64)n_ * 2 * L + (u64)ns_ * 2 * L});
+    std::vector<cudaEvent_t> marks;
+    try {
+        record(&marks);
+        cuda_check(cudaStreamSynchronize(ctx_.stream()), "profile");
+    } catch (...) {
+        for (auto e : marks) cudaEventDestroy(e);
+        throw;
+    }
+    for (size_t i = 0; i + 1 < marks.size() && i < out.size(); ++i) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, marks[i], marks[i + 1]);
+        out[i].us = 1e3 * ms;
+    }
+    for (auto e : marks) cudaEventDestroy(e);
+    return out;
 }
 
 void CloudPlan::run() {

@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <string>
 #include <vector>
 
 #include "bfv_context.hpp"
@@ -30,6 +31,13 @@ struct PlanStats {
     uint64_t hbm_bytes = 0, key_bytes = 0;
 };
 
+// one launch group of the plan, timed by profile()
+struct PhaseTiming {
+    std::string name;
+    double us = 0;
+    uint64_t items = 0, bytes = 0, limb_ntts = 0;  // compulsory HBM bytes, limb NTTs
+};
+
 class CloudPlan {
 public:
     // a/b: per-chunk input ciphertexts; out: one result ciphertext per slice
@@ -39,10 +47,13 @@ public:
     ~CloudPlan();
     void run();      // enqueue (graph replay when captured)
     void capture();  // record a CUDA graph of run()
+    // eager run with CUDA events between launch groups (multiply+relin, each
+    // rotate level, the level-0 add, the mask accumulation)
+    std::vector<PhaseTiming> profile();
     const PlanStats& stats() const { return stats_; }
 
 private:
-    void record();
+    void record(std::vector<cudaEvent_t>* marks = nullptr);
     template <class T>
     T* put(const std::vector<T>& v);
 
@@ -66,6 +77,7 @@ private:
         const u64* const* key;
         const u32* ginv;
         const u64* const* extra;  // fused add of a hoisted odd-step rotation (nullable)
+        int keys;                  // distinct switching keys of the level
     };
     std::vector<Level> levels_;
     int add_items_ = 0;  // odd steps right after D_1: added once level 0 is done
