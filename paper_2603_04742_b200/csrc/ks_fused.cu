@@ -119,14 +119,18 @@ __global__ void __launch_bounds__(Ntt2<LOGN>::TC, 256 / Ntt2<LOGN>::TC * 2) k_ks
 // ---------------------------------------------------------------------------
 // K2: NTT block phase + key inner product + INTT block phase
 // ---------------------------------------------------------------------------
+// 256 threads at 2^15 (the tiles + twiddles allow only 2 CTAs per SM), 128 below
+template <int LOGN>
+constexpr int ks_blocks_threads() { return LOGN >= 15 ? 256 : 128; }
+
 template <int LOGN, int LT, int KT, int AT>
-__global__ void __launch_bounds__(256) k_ks_blocks_inner(const DevConsts* __restrict__ dc, const u64* __restrict__ DX,
+__global__ void __launch_bounds__(ks_blocks_threads<LOGN>()) k_ks_blocks_inner(const DevConsts* __restrict__ dc, const u64* __restrict__ DX,
                                                          const u64* const* KEY, u64* __restrict__ ACC) {
     using G = Ntt2<LOGN>;
     extern __shared__ u64 smem[];
     constexpr int PITCH = G::PITCH;
     constexpr int TW = G::LINES * PITCH;
-    constexpr int T = 256;
+    constexpr int T = ks_blocks_threads<LOGN>();
     constexpr int PER = G::LINES * G::R2 / T;  // elements per thread
     u64* work = smem;
     u64* acc0 = smem + TW;
@@ -233,7 +237,7 @@ static void ks_fused_t(const DevConsts* dc, const RnsParams& P, const u64* const
     k_ks_modup_cols<LOGN, LT, KT, AT><<<items * dnum * LK * G::CTAS_C, G::TC, smem1, st>>>(dc, SRC, SRCC, src_poly,
                                                                                       ginv, DX);
     KS_CHECK();
-    k_ks_blocks_inner<LOGN, LT, KT, AT><<<items * LK * G::CTAS_B, 256, smem2, st>>>(dc, DX, KEY, ACC);
+    k_ks_blocks_inner<LOGN, LT, KT, AT><<<items * LK * G::CTAS_B, ks_blocks_threads<LOGN>(), smem2, st>>>(dc, DX, KEY, ACC);
     KS_CHECK();
     NttJob j;
     for (int i = 0; i < MAX_JOB_LIMBS; ++i) j.pidx[i] = (signed char)(i % LK);
