@@ -188,7 +188,7 @@ def run_reference_arm(args, cfg):
 
 
 def key_switch_roofline(ctx, job, stream, flush):
-    """Per launch group of one eager plan run (CUDA events between groups, L2
+    """Per launch group of one plan graph replay (event nodes between groups, L2
     flushed first): compulsory HBM bytes (fused rotate+add = 3C per
     item + KEY per distinct key) / device time vs the measured copy bandwidth,
     and the group's NTT butterflies / time vs the butterfly probe."""
@@ -224,7 +224,8 @@ def key_switch_roofline(ctx, job, stream, flush):
                 "ntt_gbfly": round(ntt, 1), "int_frac": round(ntt * 1e9 / peak, 4)}
     return {"rotations": summ, "groups": rows if ks else rows, "hbm_peak_gbs": hbm_peak,
             "int_peak_gbfly": round(peak / 1e9, 1),
-            "note": "eager run, one launch group at a time; bytes = compulsory (SURVEY 8(d)); "
+            "note": "one graph replay with event nodes between launch groups, L2 flushed before; "
+                    "bytes = compulsory (SURVEY 8(d)); "
                     "int_frac counts NTT butterflies only (ModUp/MAC/ModDown modmuls excluded)"}
 
 

@@ -155,8 +155,9 @@ typedef struct {
     uint64_t key_bytes_per_run;
 } spmvgpu_plan_stats;
 int spmvgpu_plan_stats_get(const spmvgpu_plan* p, spmvgpu_plan_stats* out);
-/* one eager run with CUDA events between launch groups (multiply+relin, each
- * rotate level, the level-0 add, mask accumulate): device time per group, its
+/* one CUDA-graph replay of the plan with event nodes between launch groups
+ * (multiply+relin, each rotate level, the level-0 add, mask accumulate; the
+ * L2 is left as the caller left it): device time per group, its
  * compulsory HBM bytes (SURVEY 8(d) op table) and limb NTTs; *count = groups */
 typedef struct {
     char name[32];

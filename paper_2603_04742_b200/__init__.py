@@ -495,7 +495,7 @@ class Job:
         return {k: int(getattr(s, k)) for k, _ in PlanStats._fields_}
 
     def profile(self) -> list:
-        """Device time, compulsory bytes and limb NTTs per launch group (one eager run)."""
+        """Device time, compulsory bytes and limb NTTs per launch group (one graph replay)."""
         cap = 64
         ph = (PhaseC * cap)()
         cnt = C.c_int()

@@ -393,14 +393,20 @@ void GpuContext::mul_relin_dev(const u64* const* A, const u64* const* B, u64* co
     std::vector<int> pm;
     for (int j = 0; j < M; ++j) pm.push_back(j < L ? j : K + j);
     launch_mul_extend(dc_, P_, A, B, T, items, st_);
-    launch_ntt(dc_, logn, false, job(T, T, 4 * M, pm), items, st_);
-    launch_mul_tensor(dc_, P_, T, Z, items, st_);
-    launch_ntt(dc_, logn, true, job(Z, Z, 3 * M, pm), items, st_);
+    if (fused_ks_) {  // column phase, fused blocks + tensor + inverse blocks, column phase
+        launch_ntt_phase(dc_, logn, false, true, job(T, T, 4 * M, pm), items, st_);
+        launch_mul_blocks_tensor(dc_, P_, T, Z, items, st_);
+        launch_ntt_phase(dc_, logn, true, true, job(Z, Z, 3 * M, pm), items, st_);
+    } else {
+        launch_ntt(dc_, logn, false, job(T, T, 4 * M, pm), items, st_);
+        launch_mul_tensor(dc_, P_, T, Z, items, st_);
+        launch_ntt(dc_, logn, true, job(Z, Z, 3 * M, pm), items, st_);
+    }
     launch_mul_scale(dc_, P_, Z, OUT, D2, items, st_);
     if (fused_ks_) {
         launch_ks_fused(dc_, P_, nullptr, D2, 0, nullptr, RLK, reinterpret_cast<const u64* const*>(OUT),
                         nullptr, OUT, DX, ACC, items, st_);
-        stats_.kernels += 11;
+        stats_.kernels += 9;
     } else {
         launch_ks_modup_contig(dc_, P_, D2, DX, items, st_);
         launch_ntt(dc_, logn, false, job(DX, DX, P_.dnum * LK, range_idx(0, LK)), items, st_);

@@ -47,6 +47,14 @@ size_t ntt_smem_bytes(int logn);
 // ct x ct
 void launch_mul_extend(const DevConsts* dc, const RnsParams& P, const u64* const* A,
                        const u64* const* B, u64* T, int items, cudaStream_t st);
+// fused forward block phase + mask multiply-accumulate + inverse block phase
+// (mul_fused.cu); OUT[s] receives the slice sums before the inverse column phase
+void launch_mask_blocks(const DevConsts* dc, const RnsParams& P, const u64* MT, const int* slice_off,
+                        const int* slice_items, const int* item_mask, const u64* MASKS, u64* const* OUT,
+                        int slices, cudaStream_t st);
+// fused forward block phase + tensor + inverse block phase (mul_fused.cu)
+void launch_mul_blocks_tensor(const DevConsts* dc, const RnsParams& P, const u64* T, u64* Z, int items,
+                              cudaStream_t st);
 void launch_mul_tensor(const DevConsts* dc, const RnsParams& P, const u64* T, u64* Z, int items,
                        cudaStream_t st);
 void launch_mul_scale(const DevConsts* dc, const RnsParams& P, const u64* Z, u64* const* OUT,

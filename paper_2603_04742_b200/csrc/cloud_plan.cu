@@ -142,7 +142,9 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
     stats_.rotations = n_rot;
     stats_.hbm_bytes = n ? (u64)n * 3 * C + KEY : 0;
     stats_.key_bytes = n ? KEY : 0;
-    stats_.kernels = n ? (fused ? 11 : 14) : 0;  // each NTT is two kernels (column, block phase)
+    // each NTT is two kernels (column, block phase); fused: extend, cols, blocks+tensor+iblocks,
+    // icols, scale + the 4-kernel relinearisation key switch
+    stats_.kernels = n ? (fused ? 9 : 14) : 0;
     stats_.limb_ntts = (u64)n * (7 * M + P.dnum * LK + 2 * LK) + (u64)n_rot * (P.dnum * LK + 2 * LK);
 
     // where each hoisted rotation lands: rp slot per (chunk item k, odd step)
@@ -253,7 +255,7 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
     slice_items_ = put(items_by_slice);
     item_mask_ = put(item_mask);
     stats_.hbm_bytes += (u64)n * 2 * C + (u64)n_masks_ * PT;
-    stats_.kernels += n ? 5 : 0;
+    stats_.kernels += n ? (fused ? 3 : 5) : 0;
     stats_.limb_ntts += (u64)n * 2 * L + (u64)ns_ * 2 * L;
     if (!stage_.empty())
         cuda_check(cudaMemcpyAsync(arena_.as<void>(), stage_.data(), stage_.size(), cudaMemcpyHostToDevice,
@@ -276,7 +278,8 @@ void CloudPlan::record(std::vector<cudaEvent_t>* marks) {
         if (!marks) return;
         cudaEvent_t e;
         cuda_check(cudaEventCreate(&e), "event");
-        cuda_check(cudaEventRecord(e, st), "event record");
+        // External: under stream capture this becomes an event-record node
+        cuda_check(cudaEventRecordWithFlags(e, st, cudaEventRecordExternal), "event record");
         marks->push_back(e);
     };
     mark();
@@ -297,13 +300,21 @@ void CloudPlan::record(std::vector<cudaEvent_t>* marks) {
     std::iota(qidx.begin(), qidx.end(), 0);
     NttJob fwd = ctx_.job(nullptr, MT_.words(), 2 * L, qidx);
     fwd.src_items = FINAL_;
-    launch_ntt(ctx_.dconsts(), logn, false, fwd, n_, st);
-    u64* RES = T_.words();  // ns <= n results fit the multiply workspace
-    launch_mask_accum(ctx_.dconsts(), P, MT_.words(), slice_off_, slice_items_, item_mask_,
-                      MASKS_.words(), RES, ns_, st);
-    NttJob inv = ctx_.job(RES, nullptr, 2 * L, qidx);
+    NttJob inv = ctx_.job(nullptr, nullptr, 2 * L, qidx);
     inv.dst_items = OUT_;
-    launch_ntt(ctx_.dconsts(), logn, true, inv, ns_, st);
+    if (ctx_.fused_key_switch()) {  // column phase, fused blocks + mask MAC + inverse blocks, column phase
+        launch_ntt_phase(ctx_.dconsts(), logn, false, true, fwd, n_, st);
+        launch_mask_blocks(ctx_.dconsts(), P, MT_.words(), slice_off_, slice_items_, item_mask_, MASKS_.words(),
+                           OUT_, ns_, st);
+        launch_ntt_phase(ctx_.dconsts(), logn, true, true, inv, ns_, st);
+    } else {
+        launch_ntt(ctx_.dconsts(), logn, false, fwd, n_, st);
+        u64* RES = T_.words();  // ns <= n results fit the multiply workspace
+        launch_mask_accum(ctx_.dconsts(), P, MT_.words(), slice_off_, slice_items_, item_mask_,
+                          MASKS_.words(), RES, ns_, st);
+        inv.src = RES;
+        launch_ntt(ctx_.dconsts(), logn, true, inv, ns_, st);
+    }
     mark();
 }
 
@@ -324,17 +335,42 @@ std::vector<PhaseTiming> CloudPlan::profile() {
     }
     out.push_back({"mask accumulate", 0, (u64)n_, (u64)n_ * 2 * C + (u64)n_masks_ * PT,
                    (u64)n_ * 2 * L + (u64)ns_ * 2 * L});
+    // captured like run(), with event-record nodes between the groups, so the
+    // timings include the graph's (small) inter-kernel gaps and nothing else
     std::vector<cudaEvent_t> marks;
+    cudaStream_t st = ctx_.stream();
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t ex = nullptr;
     try {
-        record(&marks);
-        cuda_check(cudaStreamSynchronize(ctx_.stream()), "profile");
+        cuda_check(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "begin capture");
+        try {
+            record(&marks);
+        } catch (...) {
+            cudaGraph_t tmp = nullptr;
+            cudaStreamEndCapture(st, &tmp);
+            if (tmp) cudaGraphDestroy(tmp);
+            throw;
+        }
+        cuda_check(cudaStreamEndCapture(st, &g), "end capture");
+        cuda_check(cudaGraphInstantiate(&ex, g, 0), "graph instantiate");
+        cuda_check(cudaGraphUpload(ex, st), "graph upload");
+        cuda_check(cudaGraphLaunch(ex, st), "graph launch");
+        cuda_check(cudaStreamSynchronize(st), "profile");
     } catch (...) {
+        if (ex) cudaGraphExecDestroy(ex);
+        if (g) cudaGraphDestroy(g);
         for (auto e : marks) cudaEventDestroy(e);
         throw;
     }
+    cudaGraphExecDestroy(ex);
+    cudaGraphDestroy(g);
     for (size_t i = 0; i + 1 < marks.size() && i < out.size(); ++i) {
         float ms = 0;
-        cudaEventElapsedTime(&ms, marks[i], marks[i + 1]);
+        const cudaError_t e = cudaEventElapsedTime(&ms, marks[i], marks[i + 1]);
+        if (e != cudaSuccess) {
+            for (auto m : marks) cudaEventDestroy(m);
+            cuda_check(e, "profile event timing");
+        }
         out[i].us = 1e3 * ms;
     }
     for (auto e : marks) cudaEventDestroy(e);

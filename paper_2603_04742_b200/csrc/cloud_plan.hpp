@@ -47,8 +47,8 @@ public:
     ~CloudPlan();
     void run();      // enqueue (graph replay when captured)
     void capture();  // record a CUDA graph of run()
-    // eager run with CUDA events between launch groups (multiply+relin, each
-    // rotate level, the level-0 add, the mask accumulation)
+    // one graph replay with event nodes between launch groups (multiply+relin,
+    // each rotate level, the level-0 add, the mask accumulation)
     std::vector<PhaseTiming> profile();
     const PlanStats& stats() const { return stats_; }
 

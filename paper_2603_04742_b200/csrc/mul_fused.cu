@@ -1,0 +1,239 @@
+// mul_fused.cu -- the ct x ct multiply and the masked accumulation fused
+// around the NTT block phase.
+//
+//   k_mul_blocks_tensor : for one limb j of Q u B and one tile of 16 blocks of
+//                         one item: the NTT block phase of the four extended
+//                         inputs (a0 a1 b0 b1), the tensor product
+//                           z0 = a0 b0,  z1 = a0 b1 + a1 b0,  z2 = a1 b1,
+//                         and the INTT block phase of z0 .. z2.
+// It replaces the forward block phase, k_mul_tensor and the inverse block
+// phase (three launches and two round trips of seven polynomials through
+// HBM).  The column phases before and after stay standard NTT launches.  The
+// arithmetic is the same as the separate kernels (modular products of the same
+// residues), so the words are identical.
+#include <stdexcept>
+#include <string>
+
+#include "bfv_kernels.cuh"
+#include "ntt.cuh"
+
+namespace cssc {
+
+template <int LOGN>
+constexpr int mulb_threads() { return LOGN >= 15 ? 256 : 128; }
+
+template <int LOGN, int LT, int KT>
+__global__ void __launch_bounds__(mulb_threads<LOGN>()) k_mul_blocks_tensor(const DevConsts* __restrict__ dc,
+                                                                            const u64* __restrict__ T,
+                                                                            u64* __restrict__ Z) {
+    using G = Ntt2<LOGN>;
+    extern __shared__ u64 smem[];
+    constexpr int PITCH = G::PITCH;
+    constexpr int TW = G::LINES * PITCH;
+    constexpr int NT = mulb_threads<LOGN>();
+    constexpr int PER = G::LINES * G::R2 / NT;
+    u64* tile = smem;            // 4 tiles: a0 a1 b0 b1, then z0 z1 z2 in the first three
+    u64* tws = smem + 4 * TW;
+    const int L = LT ? LT : dc->L, K = KT ? KT : dc->K, M = 2 * L + 1;
+    int bid = blockIdx.x;
+    const int tileid = bid % G::CTAS_B;
+    bid /= G::CTAS_B;
+    const int j = bid % M;
+    const int item = bid / M;
+    const int prime = j < L ? j : K + j;  // B primes follow P in the prime table
+    const Modulus md = dc->mod[prime];
+    const u64 q = md.q;
+    const int blk0 = tileid * G::LINES;
+    const size_t base = (size_t)blk0 * G::R2;
+    const size_t PM = (size_t)M * G::N;
+    auto saddr = [](int x) { return (x >> G::B) * PITCH + (x & (G::R2 - 1)); };
+    auto addr = [](int l, int pos) { return l * PITCH + pos; };
+    auto twf = [&](int sl, int l, int blk) { return block_tw<LOGN>(tws, sl, l, blk); };
+    const u64* src = T + (size_t)item * 4 * PM + (size_t)j * G::N + base;
+    load_block_twiddles<LOGN>(tws, dc->tw[prime].fwd, blk0);
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+#pragma unroll
+        for (int r = 0; r < PER; ++r) {
+            const int x = threadIdx.x + NT * r;
+            cp_async8(tile + p * TW + saddr(x), src + p * PM + x);
+        }
+    cp_async_wait_all();
+    __syncthreads();
+#pragma unroll 1
+    for (int p = 0; p < 4; ++p) line_ntt<G::B, 0, false>(tile + p * TW, q, addr, twf);
+    // tensor: a* lazy (< 31q), b* canonicalised, so every product is < 31 q^2 (barrett range)
+#pragma unroll
+    for (int r = 0; r < PER; ++r) {
+        const int s0 = saddr(threadIdx.x + NT * r);
+        const u64 a0 = tile[s0], a1 = tile[TW + s0];
+        const u64 b0 = reduce_small_quot(tile[2 * TW + s0], md), b1 = reduce_small_quot(tile[3 * TW + s0], md);
+        tile[s0] = mul_mod(a0, b0, md);
+        tile[TW + s0] = add_mod(mul_mod(a0, b1, md), mul_mod(a1, b0, md), q);
+        tile[2 * TW + s0] = mul_mod(a1, b1, md);
+    }
+    __syncthreads();
+    load_block_twiddles<LOGN>(tws, dc->tw[prime].inv, blk0);
+    cp_async_wait_all();
+    __syncthreads();
+#pragma unroll 1
+    for (int p = 0; p < 3; ++p) line_ntt<G::B, 0, true>(tile + p * TW, q, addr, twf);
+    u64* dst = Z + (size_t)item * 3 * PM + (size_t)j * G::N + base;
+#pragma unroll
+    for (int p = 0; p < 3; ++p)
+#pragma unroll
+        for (int r = 0; r < PER; ++r) {
+            const int x = threadIdx.x + NT * r;
+            dst[p * PM + x] = tile[p * TW + saddr(x)];
+        }
+}
+
+// Masked inter-chunk accumulation around the block phase: for one slice s,
+// one limb j2 of [c0 | c1] (prime j2 mod L) and one tile of 16 blocks: for each
+// chunk of the slice, the NTT block phase of its folded ciphertext (after the
+// forward column phase, MT), times the chunk's mask tile (NTT form), summed
+// (inter_chunk_sum, aggregate.cpp:55-74); then the INTT block phase of the sum,
+// written to the slice's result ciphertext for the inverse column phase.
+// Replaces the forward block phase, k_mask_accum and the inverse block phase.
+template <int LOGN>
+__global__ void __launch_bounds__(mulb_threads<LOGN>()) k_mask_blocks(const DevConsts* __restrict__ dc,
+                                                                      const u64* __restrict__ MT,
+                                                                      const int* __restrict__ slice_off,
+                                                                      const int* __restrict__ slice_items,
+                                                                      const int* __restrict__ item_mask,
+                                                                      const u64* __restrict__ MASKS,
+                                                                      u64* const* OUT) {
+    using G = Ntt2<LOGN>;
+    extern __shared__ u64 smem[];
+    constexpr int PITCH = G::PITCH;
+    constexpr int TW = G::LINES * PITCH;
+    constexpr int NT = mulb_threads<LOGN>();
+    constexpr int PER = G::LINES * G::R2 / NT;
+    u64* work = smem;
+    u64* acc = smem + TW;
+    u64* tws = smem + 2 * TW;
+    const int L = dc->L;
+    int bid = blockIdx.x;
+    const int tileid = bid % G::CTAS_B;
+    bid /= G::CTAS_B;
+    const int j2 = bid % (2 * L);
+    const int sl = bid / (2 * L);
+    const int j = j2 % L;
+    const Modulus md = dc->mod[j];
+    const u64 q = md.q;
+    const int blk0 = tileid * G::LINES;
+    const size_t base = (size_t)blk0 * G::R2;
+    auto saddr = [](int x) { return (x >> G::B) * PITCH + (x & (G::R2 - 1)); };
+    auto addr = [](int l, int pos) { return l * PITCH + pos; };
+    auto twf = [&](int sl_, int l, int blk) { return block_tw<LOGN>(tws, sl_, l, blk); };
+    load_block_twiddles<LOGN>(tws, dc->tw[j].fwd, blk0);
+    const int b = slice_off[sl], e = slice_off[sl + 1];
+#pragma unroll 1
+    for (int x = b; x < e; ++x) {
+        const int it = slice_items[x];
+        const u64* src = MT + ((size_t)it * 2 * L + j2) * G::N + base;
+        if (x > b) __syncthreads();  // previous chunk finished reading `work`
+#pragma unroll
+        for (int r = 0; r < PER; ++r) {
+            const int y = threadIdx.x + NT * r;
+            cp_async8(work + saddr(y), src + y);
+        }
+        cp_async_wait_all();
+        __syncthreads();
+        line_ntt<G::B, 0, false>(work, q, addr, twf);
+        const u64* mk = MASKS + ((size_t)item_mask[it] * L + j) * G::N + base;
+#pragma unroll
+        for (int r = 0; r < PER; ++r) {
+            const int y = threadIdx.x + NT * r, s0 = saddr(y);
+            const u64 p = mul_mod(work[s0], __ldg(mk + y), md);  // lazy (< 31q) x canonical mask
+            acc[s0] = x == b ? p : add_mod(acc[s0], p, q);
+        }
+    }
+    __syncthreads();
+    load_block_twiddles<LOGN>(tws, dc->tw[j].inv, blk0);
+    cp_async_wait_all();
+    __syncthreads();
+    line_ntt<G::B, 0, true>(acc, q, addr, twf);
+    u64* dst = OUT[sl] + (size_t)j2 * G::N + base;
+#pragma unroll
+    for (int r = 0; r < PER; ++r) {
+        const int y = threadIdx.x + NT * r;
+        dst[y] = acc[saddr(y)];
+    }
+}
+
+template <int LOGN>
+static void maskb_t(const DevConsts* dc, const RnsParams& P, const u64* MT, const int* slice_off,
+                    const int* slice_items, const int* item_mask, const u64* MASKS, u64* const* OUT, int slices,
+                    cudaStream_t st) {
+    using G = Ntt2<LOGN>;
+    const int smem = (2 * G::LINES * G::PITCH + 2 * G::TWB) * 8;
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(k_mask_blocks<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        configured = true;
+    }
+    k_mask_blocks<LOGN><<<slices * 2 * P.cfg.L * G::CTAS_B, mulb_threads<LOGN>(), smem, st>>>(
+        dc, MT, slice_off, slice_items, item_mask, MASKS, OUT);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw std::runtime_error(std::string("mask blocks launch: ") + cudaGetErrorString(e));
+}
+
+void launch_mask_blocks(const DevConsts* dc, const RnsParams& P, const u64* MT, const int* slice_off,
+                        const int* slice_items, const int* item_mask, const u64* MASKS, u64* const* OUT,
+                        int slices, cudaStream_t st) {
+    if (!slices) return;
+    switch (P.cfg.logn) {
+        case 10: maskb_t<10>(dc, P, MT, slice_off, slice_items, item_mask, MASKS, OUT, slices, st); break;
+        case 11: maskb_t<11>(dc, P, MT, slice_off, slice_items, item_mask, MASKS, OUT, slices, st); break;
+        case 12: maskb_t<12>(dc, P, MT, slice_off, slice_items, item_mask, MASKS, OUT, slices, st); break;
+        case 13: maskb_t<13>(dc, P, MT, slice_off, slice_items, item_mask, MASKS, OUT, slices, st); break;
+        case 14: maskb_t<14>(dc, P, MT, slice_off, slice_items, item_mask, MASKS, OUT, slices, st); break;
+        case 15: maskb_t<15>(dc, P, MT, slice_off, slice_items, item_mask, MASKS, OUT, slices, st); break;
+        default: throw std::invalid_argument("mask: unsupported logn");
+    }
+}
+
+template <int LOGN, int LT, int KT>
+static void mulb_t(const DevConsts* dc, const RnsParams& P, const u64* T, u64* Z, int items, cudaStream_t st) {
+    using G = Ntt2<LOGN>;
+    const int M = P.cfg.L + P.nB;
+    const int smem = (4 * G::LINES * G::PITCH + 2 * G::TWB) * 8;
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(k_mul_blocks_tensor<LOGN, LT, KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        configured = true;
+    }
+    k_mul_blocks_tensor<LOGN, LT, KT><<<items * M * G::CTAS_B, mulb_threads<LOGN>(), smem, st>>>(dc, T, Z);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw std::runtime_error(std::string("mul blocks launch: ") + cudaGetErrorString(e));
+}
+
+template <int LOGN>
+static void mulb_logn(const DevConsts* dc, const RnsParams& P, const u64* T, u64* Z, int items, cudaStream_t st) {
+    const auto& c = P.cfg;
+    if (c.L == 3 && c.K == 1)
+        mulb_t<LOGN, 3, 1>(dc, P, T, Z, items, st);
+    else if (c.L == 4 && c.K == 2)
+        mulb_t<LOGN, 4, 2>(dc, P, T, Z, items, st);
+    else if (c.L == 8 && c.K == 4)
+        mulb_t<LOGN, 8, 4>(dc, P, T, Z, items, st);
+    else
+        mulb_t<LOGN, 0, 0>(dc, P, T, Z, items, st);
+}
+
+void launch_mul_blocks_tensor(const DevConsts* dc, const RnsParams& P, const u64* T, u64* Z, int items,
+                              cudaStream_t st) {
+    if (!items) return;
+    switch (P.cfg.logn) {
+        case 10: mulb_logn<10>(dc, P, T, Z, items, st); break;
+        case 11: mulb_logn<11>(dc, P, T, Z, items, st); break;
+        case 12: mulb_logn<12>(dc, P, T, Z, items, st); break;
+        case 13: mulb_logn<13>(dc, P, T, Z, items, st); break;
+        case 14: mulb_logn<14>(dc, P, T, Z, items, st); break;
+        case 15: mulb_logn<15>(dc, P, T, Z, items, st); break;
+        default: throw std::invalid_argument("multiply: unsupported logn");
+    }
+}
+
+}  // namespace cssc

@@ -115,7 +115,7 @@ def test_job_graph_replay(ctx10):
     assert ph[0]["name"] == "multiply+relin" and ph[-1]["name"] == "mask accumulate"
     assert len([p for p in ph if p["name"].startswith("rotate level")]) == st["levels"]
     assert all(p["us"] > 0 and p["bytes"] > 0 for p in ph)
-    # the eager profiled run leaves the same result behind
+    # the profiled replay leaves the same result behind
     res = job.finish()
     for m, v, r in zip(ms, vs, res):
         assert np.array_equal(r["values"], checker(m, v, ctx10.slots, ctx10.slots)["values"])
