@@ -37,7 +37,8 @@ enum {
     SPMVGPU_ERR_INDEX_RANGE = -6,       /* IndexOutOfRangeError */
     SPMVGPU_ERR_DUPLICATE = -7,         /* DuplicateEntryError */
     SPMVGPU_ERR_CUDA = -8,
-    SPMVGPU_ERR_INTERNAL = -9
+    SPMVGPU_ERR_INTERNAL = -9,
+    SPMVGPU_ERR_NON_SQUARE = -10        /* NonSquareError (diagonal method) */
 };
 
 typedef struct spmvgpu_ctx spmvgpu_ctx;
@@ -121,6 +122,8 @@ int spmvgpu_add(spmvgpu_ctx* c, const spmvgpu_ct* a, const spmvgpu_ct* b, const 
                 size_t n);
 int spmvgpu_mul_relin(spmvgpu_ctx* c, const spmvgpu_ct* a, const spmvgpu_ct* b,
                       const spmvgpu_ct* out, size_t n);
+/* out = cts[0] + ... + cts[n-1] in one launch (n = 0: the zero ciphertext) */
+int spmvgpu_sum(spmvgpu_ctx* c, const spmvgpu_ct* cts, size_t n, spmvgpu_ct out);
 /* out_i = rot(src_i, steps_i) (cyclic left over S slots, negative = right) */
 int spmvgpu_rotate(spmvgpu_ctx* c, const spmvgpu_ct* src, const int64_t* steps,
                    const spmvgpu_ct* out, size_t n);
@@ -192,6 +195,10 @@ typedef struct {
 int cssc_spmv_partitioned(spmvgpu_ctx* c, const cssc_csr* m, const int64_t* v, uint64_t vlen,
                           uint64_t chunk_size, int key_holder, int64_t* values,
                           cssc_result* res, cssc_message* msgs, uint64_t msg_cap);
+/* the diagonal-method baseline (reference diagonal.cpp:56-104) on the GPU
+ * backend: square matrices, n <= slots/2 (or n == slots); values has n rows */
+int cssc_diag_spmv(spmvgpu_ctx* c, const cssc_csr* m, const int64_t* v, uint64_t vlen, int key_holder,
+                   int64_t* values, cssc_result* res, cssc_message* msgs, uint64_t msg_cap);
 /* several independent matrices in shared launches (BASELINE config 5) */
 int cssc_spmv_batch(spmvgpu_ctx* c, const cssc_csr* ms, const int64_t* const* vs, size_t nmat,
                     uint64_t chunk_size, int key_holder, int64_t* const* values,

@@ -13,6 +13,7 @@
 //   rotation_schedule     proj/src/aggregate.cpp:19-34
 //   csr_to_cssc           proj/src/sparse.cpp:79-117
 //   generate_chunks       proj/src/chunk.cpp:10-50
+//   diag_spmv             proj/src/diagonal.cpp:44-104
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -22,6 +23,7 @@
 
 #include "spmv/aggregate.hpp"
 #include "spmv/chunk.hpp"
+#include "spmv/diagonal.hpp"
 #include "spmv/he.hpp"
 #include "spmv/protocol.hpp"
 #include "spmv/sparse.hpp"
@@ -91,6 +93,46 @@ int64_t ref_spmv_partitioned(uint64_t slot_count, uint64_t t, double ct_mb, cons
         *noise_out = r.noise_budget_remaining_bits;
         return static_cast<int64_t>(r.n_ct);
     } catch (const std::exception& e) {
+        return classify(e);
+    }
+}
+
+// The diagonal-method baseline on the reference SimBackend; same outputs as
+// ref_spmv_partitioned (returns the number of diagonal ciphertexts).
+int64_t ref_diag_spmv(uint64_t slot_count, uint64_t t, double ct_mb, const int* noise5, uint64_t rows,
+                      uint64_t cols, const int64_t* rp, const int64_t* ci, const int64_t* va, const int64_t* v,
+                      uint64_t vlen, int key_holder, int64_t* out_vals, uint64_t* ledger6, int64_t* msgs,
+                      uint64_t* nmsgs, uint64_t msg_cap, int* noise_out) {
+    try {
+        spmv::HeParams p;
+        p.slot_count = slot_count;
+        p.plaintext_modulus = t;
+        p.ciphertext_size_mb = ct_mb;
+        p.noise = {noise5[0], noise5[1], noise5[2], noise5[3], noise5[4]};
+        spmv::SimBackend be(p);
+        const spmv::CsrMatrix m = make_csr(rows, cols, rp, ci, va);
+        const std::vector<int64_t> vv(v, v + vlen);
+        spmv::SpmvResult r = spmv::diag_spmv(be, m, vv, static_cast<spmv::PartyRole>(key_holder));
+        std::memcpy(out_vals, r.values.data(), sizeof(int64_t) * r.values.size());
+        const auto& L = r.op_ledger;
+        const uint64_t led[6] = {L.n_mult_cc, L.n_mult_cp, L.n_rot, L.n_add, L.n_enc, L.n_dec};
+        std::memcpy(ledger6, led, sizeof led);
+        const auto& ms = r.message_ledger.messages;
+        *nmsgs = ms.size();
+        for (size_t i = 0; i < ms.size() && i < msg_cap; ++i) {
+            msgs[5 * i + 0] = static_cast<int64_t>(ms[i].from);
+            msgs[5 * i + 1] = static_cast<int64_t>(ms[i].to);
+            msgs[5 * i + 2] = static_cast<int64_t>(ms[i].kind);
+            msgs[5 * i + 3] = static_cast<int64_t>(ms[i].payload_bytes);
+            msgs[5 * i + 4] = static_cast<int64_t>(ms[i].ciphertext_count);
+        }
+        *noise_out = r.noise_budget_remaining_bits;
+        return static_cast<int64_t>(r.n_ct);
+    } catch (const std::exception& e) {
+        if (dynamic_cast<const spmv::NonSquareError*>(&e)) {
+            g_err = e.what();
+            return -5;
+        }
         return classify(e);
     }
 }

@@ -112,6 +112,9 @@ _SIGS = {
     "cssc_spmv_partitioned": (C.c_int, [C.c_void_p, C.POINTER(CsrC), i64p, C.c_uint64, C.c_uint64,
                                         C.c_int, i64p, C.POINTER(ResultC), C.POINTER(Message),
                                         C.c_uint64]),
+    "cssc_diag_spmv": (C.c_int, [C.c_void_p, C.POINTER(CsrC), i64p, C.c_uint64, C.c_int, i64p,
+                                 C.POINTER(ResultC), C.POINTER(Message), C.c_uint64]),
+    "spmvgpu_sum": (C.c_int, [C.c_void_p, u64p, C.c_size_t, C.c_uint64]),
     "cssc_spmv_batch": (C.c_int, [C.c_void_p, C.POINTER(CsrC), C.POINTER(i64p), C.c_size_t,
                                   C.c_uint64, C.c_int, C.POINTER(i64p), C.POINTER(ResultC)]),
     "cssc_job_create": (C.c_int, [C.c_void_p, C.POINTER(CsrC), C.POINTER(i64p), C.c_size_t,
@@ -155,7 +158,7 @@ def lib() -> C.CDLL:
 
 STATUS = {-1: ValueError, -2: "OverLengthError", -3: "NoiseExhaustedError", -4: "DimensionMismatchError",
           -5: "ColumnTooTallError", -6: "IndexOutOfRangeError", -7: "DuplicateEntryError",
-          -8: RuntimeError, -9: RuntimeError}
+          -8: RuntimeError, -9: RuntimeError, -10: "NonSquareError"}
 
 
 class SpmvError(RuntimeError):
@@ -297,6 +300,13 @@ class Context:
         b = np.zeros(cts.size, np.int32)
         check(lib().spmvgpu_decrypt(self.h, _p(cts, u64p), cts.size, _p(slots, u64p), _p(b, i32p)))
         return slots, b
+
+    def sum(self, cts) -> int:
+        """One ciphertext = the sum of `cts` (one launch); caller frees it."""
+        cts = _u64(cts)
+        out = self.alloc(1)
+        check(lib().spmvgpu_sum(self.h, _p(cts, u64p) if cts.size else None, cts.size, int(out[0])))
+        return int(out[0])
 
     def add(self, a, b) -> np.ndarray:
         a, b = _u64(a), _u64(b)
@@ -445,6 +455,19 @@ def spmv_partitioned(ctx: Context, m: Csr, v, chunk_size: int | None = None, key
     vp = vv if vv.size else np.zeros(1, np.int64)
     check(lib().cssc_spmv_partitioned(ctx.h, C.byref(csr), _p(vp, i64p), vv.size, chunk, key_holder,
                                       _p(vals, i64p), C.byref(res), msgs, cap))
+    return _result(res, vals[: m.rows], msgs)
+
+
+def diag_spmv(ctx: Context, m: Csr, v, key_holder: int = 0) -> dict:
+    """The diagonal-method baseline (reference diagonal.cpp) batched on the GPU backend."""
+    vv = _i64(v)
+    vals = np.zeros(max(m.rows, 1), np.int64)
+    res = ResultC()
+    msgs = (Message * 8)()
+    csr = m.c()
+    vp = vv if vv.size else np.zeros(1, np.int64)
+    check(lib().cssc_diag_spmv(ctx.h, C.byref(csr), _p(vp, i64p), vv.size, key_holder, _p(vals, i64p),
+                               C.byref(res), msgs, 8))
     return _result(res, vals[: m.rows], msgs)
 
 

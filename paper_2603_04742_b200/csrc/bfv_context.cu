@@ -333,14 +333,22 @@ void GpuContext::encrypt_encoded(const u64* d_streams, u64* const* d_out, int it
     const int L = P_.cfg.L, logn = P_.cfg.logn;
     u64* CM = wsC_.words();
     launch_enc_sample_u(dc_, P_, P_.cfg.seed, d_streams, wsU_.words(), items, st_);
-    launch_ntt(dc_, logn, false, job(wsU_.words(), wsU_.words(), L, range_idx(0, L)), items, st_);
-    launch_enc_pk(dc_, P_, pk_.words(), wsU_.words(), CM, items, st_);
     std::vector<int> pidx = range_idx(0, L);
     pidx.insert(pidx.end(), pidx.begin(), pidx.end());
     pidx.push_back(P_.t_index());
-    launch_ntt(dc_, logn, true, job(CM, CM, 2 * L + 1, pidx), items, st_);
+    if (fused_ks_) {  // NTT(u) column phase; block phase x pk + inverse block phase (+ message); columns
+        launch_ntt_phase(dc_, logn, false, true, job(wsU_.words(), wsU_.words(), L, range_idx(0, L)), items, st_);
+        launch_blocks_mul_inv(dc_, P_, wsU_.words(), pk_.words(), 2, CM, cm_stride(), CM, 2 * L, P_.t_index(),
+                              items, st_);
+        launch_ntt_phase(dc_, logn, true, true, job(CM, CM, 2 * L + 1, pidx), items, st_);
+        stats_.kernels += 5;
+    } else {
+        launch_ntt(dc_, logn, false, job(wsU_.words(), wsU_.words(), L, range_idx(0, L)), items, st_);
+        launch_enc_pk(dc_, P_, pk_.words(), wsU_.words(), CM, items, st_);
+        launch_ntt(dc_, logn, true, job(CM, CM, 2 * L + 1, pidx), items, st_);
+        stats_.kernels += 7;
+    }
     launch_enc_finish(dc_, P_, P_.cfg.seed, d_streams, CM, d_out, items, st_);
-    stats_.kernels += 7;
     stats_.limb_ntts += (u64)items * (1 + 3 * L);
 }
 
@@ -355,9 +363,16 @@ void GpuContext::decrypt(const std::vector<const u64*>& cts, u64* slots_host, in
     NttJob j = job(nullptr, wsX_.words(), L, range_idx(0, L));
     j.src_items = dct;
     j.src_limb_offset = L;
-    launch_ntt(dc_, logn, false, j, items, st_);
-    launch_mul_s(dc_, P_, wsX_.words(), s_ntt_.words(), items, st_);
-    launch_ntt(dc_, logn, true, job(wsX_.words(), wsX_.words(), L, range_idx(0, L)), items, st_);
+    if (fused_ks_) {  // column phase of c1; block phase x s + inverse block phase; inverse columns
+        launch_ntt_phase(dc_, logn, false, true, j, items, st_);
+        launch_blocks_mul_inv(dc_, P_, wsX_.words(), s_ntt_.words(), 1, wsX_.words(), (size_t)L * n, nullptr,
+                              0, 0, items, st_);
+        launch_ntt_phase(dc_, logn, true, true, job(wsX_.words(), wsX_.words(), L, range_idx(0, L)), items, st_);
+    } else {
+        launch_ntt(dc_, logn, false, j, items, st_);
+        launch_mul_s(dc_, P_, wsX_.words(), s_ntt_.words(), items, st_);
+        launch_ntt(dc_, logn, true, job(wsX_.words(), wsX_.words(), L, range_idx(0, L)), items, st_);
+    }
     u64* slots_dev = wsU_.words();
     auto* maxdev = reinterpret_cast<unsigned long long*>(wsU_.words() + (size_t)items * (n / 2));
     launch_dec_scale(dc_, P_, dct, wsX_.words(), wsM_.words(), maxdev, items, st_);
@@ -378,6 +393,17 @@ void GpuContext::decrypt(const std::vector<const u64*>& cts, u64* slots_host, in
 }
 
 // ------------------------------------------------------------------ ct ops
+void GpuContext::sum(const std::vector<const u64*>& a, u64* out) {
+    if (a.empty()) {
+        cuda_check(cudaMemsetAsync(out, 0, sizeof(u64) * ct_words(), st_), "zero");
+        return;
+    }
+    for (const u64* p : a)
+        if (p == out) throw std::invalid_argument("sum: output aliases an input");
+    launch_sum_items(dc_, P_, upload_ptrs(a, 0), (int)a.size(), out, st_);
+    stats_.kernels += 1;
+}
+
 void GpuContext::add(const std::vector<const u64*>& a, const std::vector<const u64*>& b,
                      const std::vector<u64*>& out) {
     const int items = (int)out.size();

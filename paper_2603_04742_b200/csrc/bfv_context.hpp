@@ -108,6 +108,8 @@ public:
              const std::vector<u64*>& out);
     void mul_relin(const std::vector<const u64*>& a, const std::vector<const u64*>& b,
                    const std::vector<u64*>& out);
+    // out = a_0 + a_1 + ... (out may not alias an input)
+    void sum(const std::vector<const u64*>& a, u64* out);
     // out_i = (base_i ? base_i : 0) + rot(src_i, k_i)
     void rotate(const std::vector<const u64*>& src, const std::vector<int64_t>& k,
                 const std::vector<const u64*>& base, const std::vector<u64*>& out);

@@ -1096,6 +1096,34 @@ void launch_add(const DevConsts* dc, const RnsParams& P, const u64* const* A,
     CSSC_CHECK_LAUNCH();
 }
 
+// OUT = sum of `count` ciphertexts (the diagonal method's accumulation):
+// one thread per (coefficient, limb); lazy sums of < 31 canonical terms,
+// reduced by the 32-bit quotient estimate
+__global__ void k_sum_items(const DevConsts* __restrict__ dc, const u64* const* A, int count, u64* OUT) {
+    const int n = dc->n, L = dc->L;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int x = blockIdx.y;  // limb of [c0 | c1]
+    const Modulus md = dc->mod[x % L];
+    const size_t o = (size_t)x * n + k;
+    u64 acc = 0;
+    int lazy = 0;
+    for (int i = 0; i < count; ++i) {
+        acc += A[i][o];
+        if (++lazy == 30) {
+            acc = reduce_small_quot(acc, md);
+            lazy = 1;
+        }
+    }
+    OUT[o] = reduce_small_quot(acc, md);
+}
+
+void launch_sum_items(const DevConsts* dc, const RnsParams& P, const u64* const* A, int count, u64* OUT,
+                      cudaStream_t st) {
+    k_sum_items<<<dim3((unsigned)(P.n / EW_THREADS), (unsigned)(2 * P.cfg.L)), EW_THREADS, 0, st>>>(dc, A, count,
+                                                                                                 OUT);
+    CSSC_CHECK_LAUNCH();
+}
+
 __global__ void k_automorph_ct(const DevConsts* __restrict__ dc, const u64* const* A,
                                const u32* ginv, u64* const* OUT) {
     const int n = dc->n, L = dc->L;

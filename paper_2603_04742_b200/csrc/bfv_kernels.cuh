@@ -52,6 +52,12 @@ void launch_mul_extend(const DevConsts* dc, const RnsParams& P, const u64* const
 void launch_mask_blocks(const DevConsts* dc, const RnsParams& P, const u64* MT, const int* slice_off,
                         const int* slice_items, const int* item_mask, const u64* MASKS, u64* const* OUT,
                         int slices, cudaStream_t st);
+// block phase x NTT-form multipliers (pk or s) + inverse block phase, limb-wise
+// (mul_fused.cu); OUT limb p*L+j of item i at OUT + i*out_stride; XTRA: an extra
+// limb run through the inverse block phase in place (prime index xprime)
+void launch_blocks_mul_inv(const DevConsts* dc, const RnsParams& P, const u64* IN, const u64* MUL, int nmul,
+                           u64* OUT, size_t out_stride, u64* XTRA, int xlimb, int xprime, int items,
+                           cudaStream_t st);
 // fused forward block phase + tensor + inverse block phase (mul_fused.cu)
 void launch_mul_blocks_tensor(const DevConsts* dc, const RnsParams& P, const u64* T, u64* Z, int items,
                               cudaStream_t st);
@@ -122,6 +128,8 @@ void launch_square(const DevConsts* dc, int logn, int limbs, const u64* S, u64* 
                    cudaStream_t st);
 
 // generic ct ops
+void launch_sum_items(const DevConsts* dc, const RnsParams& P, const u64* const* A, int count, u64* OUT,
+                      cudaStream_t st);
 void launch_add(const DevConsts* dc, const RnsParams& P, const u64* const* A,
                 const u64* const* B, u64* const* OUT, int items, cudaStream_t st);
 void launch_automorph_ct(const DevConsts* dc, const RnsParams& P, const u64* const* A,

@@ -14,6 +14,7 @@
 #include "cloud_plan.hpp"
 #include "host/batched_spmv.hpp"
 #include "host/plan_cache.hpp"
+#include "spmv/diagonal.hpp"
 #include "spmv/gpu_backend.hpp"
 #include "spmv/synthetic.hpp"
 #include "spmvgpu.h"
@@ -67,6 +68,8 @@ int guard(F&& f) {
         return fail(SPMVGPU_ERR_INDEX_RANGE, e.what());
     } catch (const spmv::DuplicateEntryError& e) {
         return fail(SPMVGPU_ERR_DUPLICATE, e.what());
+    } catch (const spmv::NonSquareError& e) {
+        return fail(SPMVGPU_ERR_NON_SQUARE, e.what());
     } catch (const std::invalid_argument& e) {
         return fail(SPMVGPU_ERR_INVALID_ARGUMENT, e.what());
     } catch (const std::bad_alloc&) {
@@ -396,6 +399,12 @@ int spmvgpu_decrypt(spmvgpu_ctx* c, const spmvgpu_ct* cts, size_t n, uint64_t* s
 int spmvgpu_add(spmvgpu_ctx* c, const spmvgpu_ct* a, const spmvgpu_ct* b, const spmvgpu_ct* out, size_t n) {
     return guard([&] { G(c).add(cptrs(a, n), cptrs(b, n), mptrs(out, n)); });
 }
+int spmvgpu_sum(spmvgpu_ctx* c, const spmvgpu_ct* cts, size_t n, spmvgpu_ct out) {
+    return guard([&] {
+        if (!out) throw std::invalid_argument("null output ciphertext");
+        G(c).sum(cptrs(cts, n), reinterpret_cast<u64*>(out));
+    });
+}
 int spmvgpu_mul_relin(spmvgpu_ctx* c, const spmvgpu_ct* a, const spmvgpu_ct* b, const spmvgpu_ct* out,
                       size_t n) {
     return guard([&] { G(c).mul_relin(cptrs(a, n), cptrs(b, n), mptrs(out, n)); });
@@ -484,6 +493,17 @@ int cssc_spmv_partitioned(spmvgpu_ctx* c, const cssc_csr* m, const int64_t* v, u
         const spmv::CsrMatrix mm = to_csr(*m);
         const std::vector<int64_t> vv(v, v + vlen);
         const auto r = spmv::spmv_partitioned(be, mm, vv, chunk_size, static_cast<spmv::PartyRole>(key_holder));
+        fill_result(r, values, res, msgs, msg_cap);
+    });
+}
+
+int cssc_diag_spmv(spmvgpu_ctx* c, const cssc_csr* m, const int64_t* v, uint64_t vlen, int key_holder,
+                   int64_t* values, cssc_result* res, cssc_message* msgs, uint64_t msg_cap) {
+    return guard([&] {
+        spmv::GpuBfvBackend be(c->hp, c);
+        const spmv::CsrMatrix mm = to_csr(*m);
+        const std::vector<int64_t> vv(v, v + vlen);
+        const auto r = spmv::diag_spmv(be, mm, vv, static_cast<spmv::PartyRole>(key_holder));
         fill_result(r, values, res, msgs, msg_cap);
     });
 }

@@ -29,6 +29,7 @@ struct DeviceCiphertext {
         case SPMVGPU_ERR_COLUMN_TOO_TALL: throw ColumnTooTallError(msg);
         case SPMVGPU_ERR_INDEX_RANGE: throw IndexOutOfRangeError(msg);
         case SPMVGPU_ERR_DUPLICATE: throw DuplicateEntryError(msg);
+        case SPMVGPU_ERR_NON_SQUARE: throw NonSquareError(msg);
         default: throw std::runtime_error("spmvgpu: " + msg);
     }
 }

@@ -194,6 +194,138 @@ void launch_mask_blocks(const DevConsts* dc, const RnsParams& P, const u64* MT, 
     }
 }
 
+// Client-side polynomial product around the block phase (encryption: u x pk,
+// decryption: c1 x s): for one limb j < L and one tile of one item, the block
+// phase of IN (after the forward column phase), times each of the NMUL
+// NTT-form multipliers, and the inverse block phase of each product, written
+// to OUT limb p*L + j.  CTAs with j == L (only when XTRA is set) run the
+// inverse block phase of limb `xlimb` of XTRA in place with prime `xprime`:
+// the encoded message riding in the encryption's inverse NTT.
+template <int LOGN, int NMUL>
+__global__ void __launch_bounds__(mulb_threads<LOGN>()) k_blocks_mul_inv(const DevConsts* __restrict__ dc,
+                                                                         const u64* __restrict__ IN,
+                                                                         const u64* __restrict__ MUL,
+                                                                         u64* __restrict__ OUT, size_t out_stride,
+                                                                         u64* __restrict__ XTRA, int xlimb,
+                                                                         int xprime) {
+    using G = Ntt2<LOGN>;
+    extern __shared__ u64 smem[];
+    constexpr int PITCH = G::PITCH;
+    constexpr int TW = G::LINES * PITCH;
+    constexpr int NT = mulb_threads<LOGN>();
+    constexpr int PER = G::LINES * G::R2 / NT;
+    u64* tile = smem;  // input, then NMUL products
+    u64* tws = smem + (NMUL + 1) * TW;
+    const int L = dc->L, J = XTRA ? L + 1 : L;
+    int bid = blockIdx.x;
+    const int tileid = bid % G::CTAS_B;
+    bid /= G::CTAS_B;
+    const int j = bid % J;
+    const int item = bid / J;
+    const int blk0 = tileid * G::LINES;
+    const size_t base = (size_t)blk0 * G::R2;
+    auto saddr = [](int x) { return (x >> G::B) * PITCH + (x & (G::R2 - 1)); };
+    auto addr = [](int l, int pos) { return l * PITCH + pos; };
+    auto twf = [&](int sl, int l, int blk) { return block_tw<LOGN>(tws, sl, l, blk); };
+    if (j == L) {  // the extra limb: inverse block phase only, in place
+        const Modulus mx = dc->mod[xprime];
+        u64* x = XTRA + (size_t)item * out_stride + (size_t)xlimb * G::N + base;
+        load_block_twiddles<LOGN>(tws, dc->tw[xprime].inv, blk0);
+#pragma unroll
+        for (int r = 0; r < PER; ++r) {
+            const int y = threadIdx.x + NT * r;
+            cp_async8(tile + saddr(y), x + y);
+        }
+        cp_async_wait_all();
+        __syncthreads();
+        line_ntt<G::B, 0, true>(tile, mx.q, addr, twf);
+#pragma unroll
+        for (int r = 0; r < PER; ++r) {
+            const int y = threadIdx.x + NT * r;
+            x[y] = tile[saddr(y)];
+        }
+        return;
+    }
+    const Modulus md = dc->mod[j];
+    const u64 q = md.q;
+    const u64* in = IN + ((size_t)item * L + j) * G::N + base;
+    load_block_twiddles<LOGN>(tws, dc->tw[j].fwd, blk0);
+#pragma unroll
+    for (int r = 0; r < PER; ++r) {
+        const int y = threadIdx.x + NT * r;
+        cp_async8(tile + saddr(y), in + y);
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    line_ntt<G::B, 0, false>(tile, q, addr, twf);
+#pragma unroll
+    for (int r = 0; r < PER; ++r) {
+        const int y = threadIdx.x + NT * r, s0 = saddr(y);
+        const u64 w = tile[s0];  // lazy (< 31q) x canonical multiplier
+#pragma unroll
+        for (int p = 0; p < NMUL; ++p)
+            tile[(p + 1) * TW + s0] = mul_mod(w, __ldg(MUL + ((size_t)p * L + j) * G::N + base + y), md);
+    }
+    __syncthreads();
+    load_block_twiddles<LOGN>(tws, dc->tw[j].inv, blk0);
+    cp_async_wait_all();
+    __syncthreads();
+#pragma unroll 1
+    for (int p = 0; p < NMUL; ++p) line_ntt<G::B, 0, true>(tile + (p + 1) * TW, q, addr, twf);
+#pragma unroll
+    for (int p = 0; p < NMUL; ++p) {
+        u64* dst = OUT + (size_t)item * out_stride + ((size_t)p * L + j) * G::N + base;
+#pragma unroll
+        for (int r = 0; r < PER; ++r) {
+            const int y = threadIdx.x + NT * r;
+            dst[y] = tile[(p + 1) * TW + saddr(y)];
+        }
+    }
+}
+
+template <int LOGN, int NMUL>
+static void bmi_t(const DevConsts* dc, const RnsParams& P, const u64* IN, const u64* MUL, u64* OUT,
+                  size_t out_stride, u64* XTRA, int xlimb, int xprime, int items, cudaStream_t st) {
+    using G = Ntt2<LOGN>;
+    const int smem = ((NMUL + 1) * G::LINES * G::PITCH + 2 * G::TWB) * 8;
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(k_blocks_mul_inv<LOGN, NMUL>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        configured = true;
+    }
+    const int J = P.cfg.L + (XTRA ? 1 : 0);
+    k_blocks_mul_inv<LOGN, NMUL><<<items * J * G::CTAS_B, mulb_threads<LOGN>(), smem, st>>>(
+        dc, IN, MUL, OUT, out_stride, XTRA, xlimb, xprime);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw std::runtime_error(std::string("blocks-mul launch: ") + cudaGetErrorString(e));
+}
+
+template <int LOGN>
+static void bmi_logn(const DevConsts* dc, const RnsParams& P, const u64* IN, const u64* MUL, int nmul, u64* OUT,
+                     size_t out_stride, u64* XTRA, int xlimb, int xprime, int items, cudaStream_t st) {
+    if (nmul == 1)
+        bmi_t<LOGN, 1>(dc, P, IN, MUL, OUT, out_stride, XTRA, xlimb, xprime, items, st);
+    else if (nmul == 2)
+        bmi_t<LOGN, 2>(dc, P, IN, MUL, OUT, out_stride, XTRA, xlimb, xprime, items, st);
+    else
+        throw std::invalid_argument("blocks-mul: 1 or 2 multipliers");
+}
+
+void launch_blocks_mul_inv(const DevConsts* dc, const RnsParams& P, const u64* IN, const u64* MUL, int nmul,
+                           u64* OUT, size_t out_stride, u64* XTRA, int xlimb, int xprime, int items,
+                           cudaStream_t st) {
+    if (!items) return;
+    switch (P.cfg.logn) {
+        case 10: bmi_logn<10>(dc, P, IN, MUL, nmul, OUT, out_stride, XTRA, xlimb, xprime, items, st); break;
+        case 11: bmi_logn<11>(dc, P, IN, MUL, nmul, OUT, out_stride, XTRA, xlimb, xprime, items, st); break;
+        case 12: bmi_logn<12>(dc, P, IN, MUL, nmul, OUT, out_stride, XTRA, xlimb, xprime, items, st); break;
+        case 13: bmi_logn<13>(dc, P, IN, MUL, nmul, OUT, out_stride, XTRA, xlimb, xprime, items, st); break;
+        case 14: bmi_logn<14>(dc, P, IN, MUL, nmul, OUT, out_stride, XTRA, xlimb, xprime, items, st); break;
+        case 15: bmi_logn<15>(dc, P, IN, MUL, nmul, OUT, out_stride, XTRA, xlimb, xprime, items, st); break;
+        default: throw std::invalid_argument("blocks-mul: unsupported logn");
+    }
+}
+
 template <int LOGN, int LT, int KT>
 static void mulb_t(const DevConsts* dc, const RnsParams& P, const u64* T, u64* Z, int items, cudaStream_t st) {
     using G = Ntt2<LOGN>;

@@ -222,6 +222,9 @@ def ref_lib():
         L.ref_spmv_partitioned.argtypes = [C.c_uint64, C.c_uint64, C.c_double, ip, C.c_uint64, C.c_uint64,
                                            i64p, i64p, i64p, i64p, C.c_uint64, C.c_uint64, C.c_int, i64p,
                                            u64p, i64p, u64p, C.c_uint64, ip]
+        L.ref_diag_spmv.restype = C.c_int64
+        L.ref_diag_spmv.argtypes = [C.c_uint64, C.c_uint64, C.c_double, ip, C.c_uint64, C.c_uint64, i64p, i64p,
+                                    i64p, i64p, C.c_uint64, C.c_int, i64p, u64p, i64p, u64p, C.c_uint64, ip]
         L.ref_time_spmv_partitioned.restype = C.c_double
         L.ref_time_spmv_partitioned.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, i64p, i64p,
                                                 i64p, i64p, C.c_uint64, C.c_int]
@@ -234,3 +237,46 @@ def ref_lib():
                                  i64p, u64p]
         _rlib = L
     return _rlib
+
+
+def diag_reference(m, v, slot_count, t=65537, ct_mb=0.52, noise=(146, 33, 26, 0, 0), key_holder=0):
+    """The reference's diag_spmv (oracle/_ref) or, when absent, a restatement of
+    diagonal.cpp:44-104 on exact integers (values, ledger, transcript, model noise)."""
+    L = ref_lib()
+    if L is not None:
+        rp, ci, va, vv = _i64(m.row_ptrs), _i64(m.col_indices), _i64(m.values), _i64(v)
+        if va.size == 0:
+            ci = va = np.zeros(1, np.int64)
+        vv_p = vv if vv.size else np.zeros(1, np.int64)
+        out = np.zeros(max(m.rows, 1), np.int64)
+        led = np.zeros(6, np.uint64)
+        msgs = np.zeros(5 * 8, np.int64)
+        nm, nz = C.c_uint64(), C.c_int()
+        r = L.ref_diag_spmv(slot_count, t, ct_mb, (C.c_int * 5)(*noise), m.rows, m.cols, _p(rp, i64p),
+                            _p(ci, i64p), _p(va, i64p), _p(vv_p, i64p), vv.size, key_holder, _p(out, i64p),
+                            _p(led, u64p), _p(msgs, i64p), C.byref(nm), 8, C.byref(nz))
+        if r < 0:
+            return {"error": int(r)}
+        keys = ("n_mult_cc", "n_mult_cp", "n_rot", "n_add", "n_enc", "n_dec")
+        return {"values": out[: m.rows], "n_ct": int(r), "noise": nz.value,
+                "ledger": {k: int(x) for k, x in zip(keys, led)},
+                "messages": [tuple(int(x) for x in msgs[5 * i: 5 * i + 5]) for i in range(nm.value)]}
+    n = m.rows
+    rows = np.repeat(np.arange(n), np.diff(m.row_ptrs))
+    nd = len(set(((np.asarray(m.col_indices) + n - rows) % n).tolist())) if n else 0
+    acc = np.zeros(n, np.int64)
+    np.add.at(acc, rows, np.asarray(m.values) * np.asarray(v)[m.col_indices])
+    r = np.mod(acc, t)
+    vals = np.where(r > t // 2, r - t, r)
+    price = lambda c: int(round(c * ct_mb * 1048576))  # noqa: E731
+    msgs = [(0, 2, 0, price(nd), nd), (1, 2, 0, price(1), 1)]
+    if nd:
+        msgs.append((2, key_holder, 3, price(1), 1))
+    prod = max(0, min(noise[0], max(0, noise[0] - noise[4])) - noise[1])
+    noise_v = noise[0]
+    for _ in range(nd):
+        noise_v = max(0, min(noise_v, prod) - noise[3])
+    return {"values": vals, "n_ct": nd, "noise": noise_v,
+            "ledger": {"n_mult_cc": nd, "n_mult_cp": 0, "n_rot": nd, "n_add": nd, "n_enc": nd + 1,
+                       "n_dec": 1 if nd else 0},
+            "messages": msgs}
