@@ -187,6 +187,19 @@ def run_reference_arm(args, cfg):
             "e2e": {"value": round(v, 4), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
+# the reference's per-op cost table (cost.hpp: single-thread BFV, N = 8192)
+PAPER_COSTS = {"n_enc": 5.501, "n_dec": 2.570, "n_add": 0.550, "n_mult_cc": 20.874, "n_mult_cp": 4.138,
+               "n_rot": 5.350}
+
+
+def paper_cloud_ms(led):
+    return sum(led[k] * PAPER_COSTS[k] for k in ("n_add", "n_mult_cc", "n_mult_cp", "n_rot"))
+
+
+def paper_total_ms(led):
+    return sum(led[k] * c for k, c in PAPER_COSTS.items())
+
+
 def key_switch_roofline(ctx, job, stream, flush):
     """Per launch group of one plan graph replay (event nodes between groups, L2
     flushed first): compulsory HBM bytes (fused rotate+add = 3C per
@@ -299,6 +312,21 @@ def measure_config(pk, cfg, args, rank, world, device, full=True):
     e2e = e2e[1:]
     out["e2e"] = {"value": round(statistics.mean(e2e), 4), "unit": "ms", "h2d_bytes_per_step": int(h2d),
                   "d2h_bytes_per_step": int(d2h)}
+    out["wire_bytes_per_ct"] = ctx.wire_size  # real serialized ciphertext (vs the reference's 545 260 B price)
+    # paper-calibrated CPU estimate of the same ledger (cost.hpp: N=8192, 1 thread)
+    led = {k: sum(x["ledger"][k] for x in r) for k in r[0]["ledger"]}
+    out["paper_cost_model"] = {"cloud_ms": round(paper_cloud_ms(led), 1), "total_ms": round(paper_total_ms(led), 1),
+                               "ledger": led}
+    # the diagonal-method baseline on the same GPU backend (square inputs that fit)
+    if len(ms) == 1 and ms[0].rows == ms[0].cols and 2 * ms[0].rows <= ctx.slots:
+        pk.diag_spmv(ctx, ms[0], vs[0])
+        torch.cuda.synchronize(device)
+        t0 = time.perf_counter()
+        dr = pk.diag_spmv(ctx, ms[0], vs[0])
+        dms = (time.perf_counter() - t0) * 1e3
+        out["diagonal_baseline"] = {"e2e_ms": round(dms, 3), "diagonals": dr["n_ct"], "ledger": dr["ledger"],
+                                    "verified": bool(np.array_equal(dr["values"], exact_values(ms[0], vs[0]))),
+                                    "paper_cost_model_ms": round(paper_total_ms(dr["ledger"]), 1)}
     out["verified"] = verified
     # roofline of the dominant kernel: the batched NTT (largest launch of the plan)
     L, nB = ctx.params.L, ctx.params.L + 1
@@ -406,6 +434,8 @@ def main():
                        "parallelism": f"replica per GPU x{world}"},
             "clocks": head["clocks"], "e2e": head["e2e"], "gpu_launches": head["plan"]["kernels_per_run"],
             "roofline": head["roofline"], "key_switch": head["key_switch"],
+            "paper_cost_model": head["paper_cost_model"], "diagonal_baseline": head.get("diagonal_baseline"),
+            "transcript": {"priced_bytes_per_ct": 545260, "wire_bytes_per_ct": head["wire_bytes_per_ct"]},
             "cpu_baseline": cpu, "verified_exact": head["verified"],
             "measured_noise_bits_min": head["measured_noise_bits"],
             "whole_plan_hbm_gbs": head["whole_plan_hbm_gbs"],

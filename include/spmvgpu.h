@@ -90,6 +90,12 @@ int spmvgpu_ct_alloc(spmvgpu_ctx* c, size_t count, spmvgpu_ct* out);
 int spmvgpu_ct_free(spmvgpu_ctx* c, const spmvgpu_ct* cts, size_t count);
 int spmvgpu_ct_upload(spmvgpu_ctx* c, spmvgpu_ct ct, const uint64_t* words);
 int spmvgpu_ct_download(spmvgpu_ctx* c, spmvgpu_ct ct, uint64_t* words);
+/* wire format (in place of protocol.cpp:51-54's 0.52 MB price):
+ * 16-byte header (magic, logn, L, fingerprint of Q) + every residue of q_j at
+ * bitlen(q_j) bits.  Deserialisation rejects foreign headers and residues >= q_j. */
+int spmvgpu_ct_wire_size(spmvgpu_ctx* c, size_t* bytes);
+int spmvgpu_ct_serialize(spmvgpu_ctx* c, spmvgpu_ct ct, uint8_t* buf, size_t cap, size_t* written);
+int spmvgpu_ct_deserialize(spmvgpu_ctx* c, const uint8_t* buf, size_t len, spmvgpu_ct ct);
 
 /* batched encode+encrypt: item i encodes vals[offsets[i] .. offsets[i+1]) into
  * row 0 of the slots with encryption stream streams[i] (0 = next fresh id;

@@ -90,6 +90,10 @@ _SIGS = {
     "spmvgpu_ct_free": (C.c_int, [C.c_void_p, u64p, C.c_size_t]),
     "spmvgpu_ct_upload": (C.c_int, [C.c_void_p, C.c_uint64, u64p]),
     "spmvgpu_ct_download": (C.c_int, [C.c_void_p, C.c_uint64, u64p]),
+    "spmvgpu_ct_wire_size": (C.c_int, [C.c_void_p, C.POINTER(C.c_size_t)]),
+    "spmvgpu_ct_serialize": (C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(C.c_uint8), C.c_size_t,
+                                       C.POINTER(C.c_size_t)]),
+    "spmvgpu_ct_deserialize": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint8), C.c_size_t, C.c_uint64]),
     "spmvgpu_encrypt": (C.c_int, [C.c_void_p, i64p, u64p, u64p, u64p, C.c_size_t]),
     "spmvgpu_encrypt_cssc": (C.c_int, [C.c_void_p, i64p, i64p, C.c_uint64, i64p, C.c_uint64, i32p, C.c_uint64,
                                        i32p, C.c_uint64, i32p, C.c_uint64, u64p, C.c_size_t]),
@@ -247,6 +251,31 @@ class Context:
         w = np.zeros(self.ct_words, np.uint64)
         check(lib().spmvgpu_ct_download(self.h, int(ct), _p(w, u64p)))
         return w
+
+    # ---- wire format
+    @property
+    def wire_size(self) -> int:
+        b = C.c_size_t()
+        check(lib().spmvgpu_ct_wire_size(self.h, C.byref(b)))
+        return b.value
+
+    def serialize(self, ct: int) -> bytes:
+        buf = np.zeros(self.wire_size, np.uint8)
+        w = C.c_size_t()
+        check(lib().spmvgpu_ct_serialize(self.h, int(ct), buf.ctypes.data_as(C.POINTER(C.c_uint8)), buf.size,
+                                         C.byref(w)))
+        return buf[: w.value].tobytes()
+
+    def deserialize(self, data: bytes) -> int:
+        buf = np.frombuffer(data, np.uint8).copy()
+        out = self.alloc(1)
+        try:
+            check(lib().spmvgpu_ct_deserialize(self.h, buf.ctypes.data_as(C.POINTER(C.c_uint8)), buf.size,
+                                               int(out[0])))
+        except Exception:
+            self.free(out)
+            raise
+        return int(out[0])
 
     # ---- keys
     def download_sk(self) -> np.ndarray:

@@ -2,6 +2,7 @@
 // Device-side entry points (spmvgpu_*) wrap GpuContext / CloudPlan; the
 // protocol front door (cssc_*) wraps the host C++ spmv layer, which itself
 // talks to the device only through spmvgpu_*.  No exception crosses the ABI.
+#include <algorithm>
 #include <cstring>
 #include <list>
 #include <memory>
@@ -338,6 +339,112 @@ int spmvgpu_ct_download(spmvgpu_ctx* c, spmvgpu_ct ct, uint64_t* words) {
         auto& g = G(c);
         cssc::cuda_check(cudaMemcpyAsync(words, reinterpret_cast<void*>(ct), sizeof(u64) * g.ct_words(),
                                          cudaMemcpyDeviceToHost, g.stream()), "ct download");
+        g.synchronize();
+    });
+}
+
+// ---------------------------------------------------------------- wire format
+// [magic "CSW1"][logn u8][L u8][0 u16][FNV-1a of the Q primes, u64] then, for
+// poly 0..1 and limb j < L, the N residues of q_j at bitlen(q_j) bits each,
+// one little-endian bit stream (a real serialized size in place
+// of the reference's 0.52 MB pricing, protocol.cpp:51-54).
+namespace {
+constexpr size_t kWireHeader = 16;
+
+uint64_t q_fingerprint(const cssc::RnsParams& P) {
+    uint64_t h = 1469598103934665603ULL;
+    for (int j = 0; j < P.cfg.L; ++j)
+        for (int b = 0; b < 8; ++b) {
+            h ^= (P.primes[j] >> (8 * b)) & 0xff;
+            h *= 1099511628211ULL;
+        }
+    return h;
+}
+int bitlen(uint64_t q) { return 64 - __builtin_clzll(q); }
+size_t wire_bytes(const cssc::RnsParams& P) {
+    uint64_t bits = 0;
+    for (int j = 0; j < P.cfg.L; ++j) bits += (uint64_t)bitlen(P.primes[j]);
+    return kWireHeader + (size_t)((2 * (uint64_t)P.n * bits + 7) / 8);
+}
+}  // namespace
+
+int spmvgpu_ct_wire_size(spmvgpu_ctx* c, size_t* bytes) {
+    return guard([&] {
+        if (!bytes) throw std::invalid_argument("null argument");
+        *bytes = wire_bytes(G(c).params());
+    });
+}
+
+int spmvgpu_ct_serialize(spmvgpu_ctx* c, spmvgpu_ct ct, uint8_t* buf, size_t cap, size_t* written) {
+    return guard([&] {
+        auto& g = G(c);
+        const auto& P = g.params();
+        const size_t need = wire_bytes(P);
+        if (!buf || cap < need) throw std::length_error("serialize: buffer smaller than the wire size");
+        if (!ct) throw std::invalid_argument("null ciphertext handle");
+        std::vector<u64> w(g.ct_words());
+        cssc::cuda_check(cudaMemcpyAsync(w.data(), reinterpret_cast<void*>(ct), sizeof(u64) * w.size(),
+                                         cudaMemcpyDeviceToHost, g.stream()), "ct download");
+        g.synchronize();
+        std::memset(buf, 0, need);
+        std::memcpy(buf, "CSW1", 4);
+        buf[4] = (uint8_t)P.cfg.logn;
+        buf[5] = (uint8_t)P.cfg.L;
+        const uint64_t fp = q_fingerprint(P);
+        std::memcpy(buf + 8, &fp, 8);
+        uint64_t bitpos = 0;
+        uint8_t* out = buf + kWireHeader;
+        for (int p = 0; p < 2; ++p)
+            for (int j = 0; j < P.cfg.L; ++j) {
+                const int nb = bitlen(P.primes[j]);
+                const u64* src = w.data() + ((size_t)p * P.cfg.L + j) * P.n;
+                for (int k = 0; k < P.n; ++k) {
+                    u64 v = src[k];
+                    if (v >= P.primes[j]) throw std::runtime_error("serialize: non-canonical residue");
+                    for (int b = 0; b < nb;) {  // write nb bits, byte-aligned chunks
+                        const int off = (int)(bitpos & 7), take = std::min(8 - off, nb - b);
+                        out[bitpos >> 3] |= (uint8_t)((v & ((1u << take) - 1)) << off);
+                        v >>= take;
+                        b += take;
+                        bitpos += (uint64_t)take;
+                    }
+                }
+            }
+        if (written) *written = need;
+    });
+}
+
+int spmvgpu_ct_deserialize(spmvgpu_ctx* c, const uint8_t* buf, size_t len, spmvgpu_ct ct) {
+    return guard([&] {
+        auto& g = G(c);
+        const auto& P = g.params();
+        if (!buf || !ct) throw std::invalid_argument("null argument");
+        if (len != wire_bytes(P)) throw std::invalid_argument("deserialize: wrong length for these parameters");
+        uint64_t fp = 0;
+        std::memcpy(&fp, buf + 8, 8);
+        if (std::memcmp(buf, "CSW1", 4) != 0 || buf[4] != P.cfg.logn || buf[5] != P.cfg.L || fp != q_fingerprint(P))
+            throw std::invalid_argument("deserialize: header does not match this context");
+        std::vector<u64> w(g.ct_words());
+        uint64_t bitpos = 0;
+        const uint8_t* in = buf + kWireHeader;
+        for (int p = 0; p < 2; ++p)
+            for (int j = 0; j < P.cfg.L; ++j) {
+                const int nb = bitlen(P.primes[j]);
+                u64* dst = w.data() + ((size_t)p * P.cfg.L + j) * P.n;
+                for (int k = 0; k < P.n; ++k) {
+                    u64 v = 0;
+                    for (int b = 0; b < nb;) {
+                        const int off = (int)(bitpos & 7), take = std::min(8 - off, nb - b);
+                        v |= (u64)((in[bitpos >> 3] >> off) & ((1u << take) - 1)) << b;
+                        b += take;
+                        bitpos += (uint64_t)take;
+                    }
+                    if (v >= P.primes[j]) throw std::invalid_argument("deserialize: residue out of range");
+                    dst[k] = v;
+                }
+            }
+        cssc::cuda_check(cudaMemcpyAsync(reinterpret_cast<void*>(ct), w.data(), sizeof(u64) * w.size(),
+                                         cudaMemcpyHostToDevice, g.stream()), "ct upload");
         g.synchronize();
     });
 }
