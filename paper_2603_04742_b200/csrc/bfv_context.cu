@@ -107,6 +107,7 @@ GpuContext::~GpuContext() {
     if (st_) cudaStreamSynchronize(st_);
     if (stage_ev_) cudaEventDestroy(stage_ev_);
     if (stage_) cudaFreeHost(stage_);
+    for (auto& kv : pinned_free_) cudaFreeHost(kv.second);
     // buffers release into pool_; pool_ destructor frees device memory
     gk_.clear();
     if (dc_) cudaFree(dc_);
@@ -287,6 +288,56 @@ u64* GpuContext::enc_workspace(int items) {
     return wsC_.words();
 }
 
+CsscLayout CsscLayout::make(size_t nnz, size_t vec_len, size_t n_rows, size_t n_slices, size_t n_cols, int items) {
+    CsscLayout l;
+    size_t off = 0;
+    auto place = [&](size_t b) {
+        const size_t o = off;
+        off += (b + 15) & ~size_t(15);
+        return o;
+    };
+    l.o_ci = place(8 * nnz);
+    l.o_va = place(8 * nnz);
+    l.o_v = place(8 * vec_len);
+    l.o_rows = place(16 * n_rows);
+    l.o_sl = place(8 * n_slices);
+    l.o_cols = place(16 * n_cols);
+    l.o_st = place(8 * (size_t)items);
+    l.o_out = place(8 * (size_t)items);
+    l.bytes = off;
+    l.nnz = nnz;
+    l.vec_len = vec_len;
+    l.n_rows = n_rows;
+    l.n_slices = n_slices;
+    l.n_cols = n_cols;
+    l.items = items;
+    return l;
+}
+
+unsigned char* GpuContext::pinned_take(size_t bytes, size_t* cap) {
+    {
+        std::lock_guard<std::mutex> g(mu_);
+        auto it = pinned_free_.lower_bound(bytes);
+        if (it != pinned_free_.end() && it->first <= 2 * bytes + (1 << 20)) {
+            unsigned char* p = it->second;
+            *cap = it->first;
+            pinned_free_.erase(it);
+            return p;
+        }
+    }
+    const size_t c = std::max<size_t>(bytes, 1 << 16);
+    unsigned char* p = nullptr;
+    cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&p), c, cudaHostAllocDefault), "cudaHostAlloc");
+    *cap = c;
+    return p;
+}
+
+void GpuContext::pinned_give(unsigned char* p, size_t cap) {
+    if (!p) return;
+    std::lock_guard<std::mutex> g(mu_);
+    pinned_free_.emplace(cap, p);
+}
+
 void GpuContext::encrypt_cssc(const int64_t* ci, const int64_t* va, size_t nnz, const int64_t* vec,
                               size_t vec_len, const int32_t* rows, size_t n_rows, const int32_t* slices,
                               size_t n_slices, const int32_t* cols, size_t n_cols, const std::vector<u64*>& out) {
@@ -295,35 +346,36 @@ void GpuContext::encrypt_cssc(const int64_t* ci, const int64_t* va, size_t nnz, 
     if (items % 2) throw std::invalid_argument("encrypt_cssc: expects value and vector chunks in pairs");
     if (nnz > (size_t)INT32_MAX || vec_len > (size_t)INT32_MAX || n_rows > (size_t)INT32_MAX)
         throw std::length_error("encrypt_cssc: batch too large for 32-bit descriptors");
-    // one pinned staging block -> one upload
-    size_t off = 0;
-    auto place = [&](size_t b) {
-        const size_t o = off;
-        off += (b + 15) & ~size_t(15);
-        return o;
-    };
-    const size_t o_ci = place(8 * nnz), o_va = place(8 * nnz), o_v = place(8 * vec_len);
-    const size_t o_rows = place(16 * n_rows), o_sl = place(8 * n_slices), o_cols = place(16 * n_cols);
-    const size_t o_st = place(8 * (size_t)items), o_out = place(8 * (size_t)items);
-    unsigned char* h = stage_host(off);
-    std::memcpy(h + o_ci, ci, 8 * nnz);
-    std::memcpy(h + o_va, va, 8 * nnz);
-    std::memcpy(h + o_v, vec, 8 * vec_len);
-    std::memcpy(h + o_rows, rows, 16 * n_rows);
-    std::memcpy(h + o_sl, slices, 8 * n_slices);
-    std::memcpy(h + o_cols, cols, 16 * n_cols);
-    auto* hs = reinterpret_cast<u64*>(h + o_st);
+    const CsscLayout lay = CsscLayout::make(nnz, vec_len, n_rows, n_slices, n_cols, items);
+    unsigned char* h = stage_host(lay.bytes);
+    std::memcpy(h + lay.o_ci, ci, 8 * nnz);
+    std::memcpy(h + lay.o_va, va, 8 * nnz);
+    std::memcpy(h + lay.o_v, vec, 8 * vec_len);
+    std::memcpy(h + lay.o_rows, rows, 16 * n_rows);
+    std::memcpy(h + lay.o_sl, slices, 8 * n_slices);
+    std::memcpy(h + lay.o_cols, cols, 16 * n_cols);
+    auto* hs = reinterpret_cast<u64*>(h + lay.o_st);
     for (int i = 0; i < items; ++i) hs[i] = next_stream_id();
-    std::memcpy(h + o_out, out.data(), 8 * (size_t)items);
-    auto* d = static_cast<unsigned char*>(stage_upload(off, 0));
+    std::memcpy(h + lay.o_out, out.data(), 8 * (size_t)items);
+    encrypt_cssc_image(h, lay);
+}
+
+void GpuContext::encrypt_cssc_image(const unsigned char* img, const CsscLayout& lay) {
+    const int items = lay.items;
+    if (!items) return;
+    ensure_ws(scratch_[0], std::max<size_t>(lay.bytes, 256));
+    auto* d = scratch_[0].as<unsigned char>();
+    cuda_check(cudaMemcpyAsync(d, img, lay.bytes, cudaMemcpyHostToDevice, st_), "upload");
+    if (img == stage_) cuda_check(cudaEventRecord(stage_ev_, st_), "event");  // staging reusable after this
     int log_tpr = 0;
-    while (log_tpr < 5 && ((size_t)n_rows << log_tpr) < nnz) ++log_tpr;
+    while (log_tpr < 5 && (lay.n_rows << log_tpr) < lay.nnz) ++log_tpr;
     u64* CM = enc_workspace(items);
-    launch_pack_cssc(dc_, P_, reinterpret_cast<const int64_t*>(d + o_ci), reinterpret_cast<const int64_t*>(d + o_va),
-                     reinterpret_cast<const int64_t*>(d + o_v), reinterpret_cast<const int4*>(d + o_rows),
-                     (int)n_rows, reinterpret_cast<const int2*>(d + o_sl), reinterpret_cast<const int4*>(d + o_cols),
+    launch_pack_cssc(dc_, P_, reinterpret_cast<const int64_t*>(d + lay.o_ci),
+                     reinterpret_cast<const int64_t*>(d + lay.o_va), reinterpret_cast<const int64_t*>(d + lay.o_v),
+                     reinterpret_cast<const int4*>(d + lay.o_rows), (int)lay.n_rows,
+                     reinterpret_cast<const int2*>(d + lay.o_sl), reinterpret_cast<const int4*>(d + lay.o_cols),
                      items / 2, log_tpr, CM + (size_t)2 * P_.cfg.L * P_.n, cm_stride(), st_);
-    encrypt_encoded(reinterpret_cast<const u64*>(d + o_st), reinterpret_cast<u64* const*>(d + o_out), items);
+    encrypt_encoded(reinterpret_cast<const u64*>(d + lay.o_st), reinterpret_cast<u64* const*>(d + lay.o_out), items);
 }
 
 // CM = wsC_[item][2L+1][N] holds the encoded messages in limb 2L on entry;

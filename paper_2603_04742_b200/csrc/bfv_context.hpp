@@ -60,6 +60,14 @@ struct LaunchStats {
     uint64_t limb_ntts = 0;
 };
 
+// Byte offsets of the arrays in one client upload image (see encrypt_cssc).
+struct CsscLayout {
+    size_t o_ci = 0, o_va = 0, o_v = 0, o_rows = 0, o_sl = 0, o_cols = 0, o_st = 0, o_out = 0, bytes = 0;
+    size_t nnz = 0, vec_len = 0, n_rows = 0, n_slices = 0, n_cols = 0;
+    int items = 0;  // 2 * chunks
+    static CsscLayout make(size_t nnz, size_t vec_len, size_t n_rows, size_t n_slices, size_t n_cols, int items);
+};
+
 class GpuContext {
 public:
     explicit GpuContext(const RnsConfig& cfg, int device = 0);
@@ -103,6 +111,13 @@ public:
     void encrypt_cssc(const int64_t* ci, const int64_t* va, size_t nnz, const int64_t* vec, size_t vec_len,
                       const int32_t* rows, size_t n_rows, const int32_t* slices, size_t n_slices,
                       const int32_t* cols, size_t n_cols, const std::vector<u64*>& out);
+    // the same from an image already laid out in pinned host memory (trusted
+    // descriptors: the caller built them); the image must stay alive until the
+    // stream has consumed it
+    void encrypt_cssc_image(const unsigned char* img, const CsscLayout& lay);
+    // pinned host buffers, pooled by capacity
+    unsigned char* pinned_take(size_t bytes, size_t* cap);
+    void pinned_give(unsigned char* p, size_t cap);
     void decrypt(const std::vector<const u64*>& cts, u64* slots_host, int* budgets);
     void add(const std::vector<const u64*>& a, const std::vector<const u64*>& b,
              const std::vector<u64*>& out);
@@ -169,6 +184,7 @@ private:
     // workspaces for ad-hoc batched calls
     DevBuf wsT_, wsZ_, wsD2_, wsDX_, wsACC_, wsM_, wsX_, wsU_, wsC_, wsPT_;
     DevBuf scratch_[8];
+    std::multimap<size_t, unsigned char*> pinned_free_;
     unsigned char* stage_ = nullptr;  // pinned
     size_t stage_bytes_ = 0;
     cudaEvent_t stage_ev_ = nullptr;

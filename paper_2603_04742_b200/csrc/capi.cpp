@@ -199,6 +199,62 @@ void plan_cache_give(spmvgpu_ctx* ctx, PlanLease&& lease) {
 
 }  // namespace spmv::detail
 
+namespace spmv::detail {
+
+ClientImage client_image_take(spmvgpu_ctx* ctx, std::size_t nnz, std::size_t vec_len, std::size_t n_rows,
+                              std::size_t n_slices, std::size_t n_cols, int items) {
+    const cssc::CsscLayout l = cssc::CsscLayout::make(nnz, vec_len, n_rows, n_slices, n_cols, items);
+    ClientImage img;
+    img.p = ctx->g->pinned_take(l.bytes, &img.cap);
+    img.o_ci = l.o_ci;
+    img.o_va = l.o_va;
+    img.o_v = l.o_v;
+    img.o_rows = l.o_rows;
+    img.o_sl = l.o_sl;
+    img.o_cols = l.o_cols;
+    img.o_st = l.o_st;
+    img.o_out = l.o_out;
+    img.bytes = l.bytes;
+    img.nnz = nnz;
+    img.vec_len = vec_len;
+    img.n_rows = n_rows;
+    img.n_slices = n_slices;
+    img.n_cols = n_cols;
+    img.items = items;
+    return img;
+}
+
+void client_image_give(spmvgpu_ctx* ctx, ClientImage& img) {
+    if (img.p) ctx->g->pinned_give(img.p, img.cap);
+    img.p = nullptr;
+}
+
+void client_image_encrypt(spmvgpu_ctx* ctx, ClientImage& img, const spmvgpu_ct* out) {
+    auto& g = *ctx->g;
+    auto* st = reinterpret_cast<std::uint64_t*>(img.p + img.o_st);
+    for (int i = 0; i < img.items; ++i) st[i] = g.next_stream_id();
+    std::memcpy(img.p + img.o_out, out, sizeof(spmvgpu_ct) * (std::size_t)img.items);
+    cssc::CsscLayout l;
+    l.o_ci = img.o_ci;
+    l.o_va = img.o_va;
+    l.o_v = img.o_v;
+    l.o_rows = img.o_rows;
+    l.o_sl = img.o_sl;
+    l.o_cols = img.o_cols;
+    l.o_st = img.o_st;
+    l.o_out = img.o_out;
+    l.bytes = img.bytes;
+    l.nnz = img.nnz;
+    l.vec_len = img.vec_len;
+    l.n_rows = img.n_rows;
+    l.n_slices = img.n_slices;
+    l.n_cols = img.n_cols;
+    l.items = img.items;
+    g.encrypt_cssc_image(img.p, l);
+}
+
+}  // namespace spmv::detail
+
 spmvgpu_ctx::~spmvgpu_ctx() {
     if (g) {
         for (auto& l : plans) spmv::detail::plan_lease_free(this, l);

@@ -2,6 +2,7 @@
 #include "batched_spmv.hpp"
 
 #include <algorithm>
+#include <cstring>
 #include <climits>
 #include <numeric>
 #include <stdexcept>
@@ -51,9 +52,7 @@ BatchedSpmv::BatchedSpmv(spmvgpu_ctx* ctx, const HeParams& hp, std::span<const C
     }
     if (nnz_total > INT32_MAX || vec_total > INT32_MAX)
         throw std::length_error("spmv_batch: more than 2^31 entries in one batch");
-    ci_.reserve(nnz_total);
-    va_.reserve(nnz_total);
-    vec_.reserve(vec_total);
+    std::int64_t nz_next = 0, vec_next = 0;
     for (std::size_t mi = 0; mi < ms.size(); ++mi) {
         const CsrView& m = ms[mi];
         if (m.rows && m.row_ptrs[0] != 0) throw std::invalid_argument("csr: row_ptrs[0] must be 0");
@@ -64,12 +63,9 @@ BatchedSpmv::BatchedSpmv(spmvgpu_ctx* ctx, const HeParams& hp, std::span<const C
             if (m.col_indices[k] >= m.cols)
                 throw IndexOutOfRangeError("csr: column index " + std::to_string(m.col_indices[k]) +
                                            " out of range for " + std::to_string(m.cols) + " columns");
-        const auto nz_base = static_cast<std::int64_t>(ci_.size());
-        const auto vec_base = static_cast<std::int64_t>(vec_.size());
-        ci_.insert(ci_.end(), reinterpret_cast<const std::int64_t*>(m.col_indices),
-                   reinterpret_cast<const std::int64_t*>(m.col_indices) + m.nnz);
-        va_.insert(va_.end(), m.values, m.values + m.nnz);
-        vec_.insert(vec_.end(), m.vec, m.vec + m.cols);
+        const std::int64_t nz_base = nz_next, vec_base = vec_next;
+        nz_next += static_cast<std::int64_t>(m.nnz);
+        vec_next += static_cast<std::int64_t>(m.cols);
         rows_of_.push_back(m.rows);
         // spmv_partitioned slices rows by chunk_size (partition_rows, chunk.cpp:55-73);
         // plain spmv keeps one slice
@@ -83,6 +79,25 @@ BatchedSpmv::BatchedSpmv(spmvgpu_ctx* ctx, const HeParams& hp, std::span<const C
     }
     const std::size_t n = r_.size();
     if (!n) return;
+    // the client upload image, written once straight from the callers' arrays
+    img_ = client_image_take(ctx_, nnz_total, vec_total, rowrec_.size() / 4, slicerec_.size() / 2,
+                             colrec_.size() / 4, static_cast<int>(2 * n));
+    {
+        std::size_t nz = 0, vo = 0;
+        for (const CsrView& m : ms) {
+            std::memcpy(img_.p + img_.o_ci + 8 * nz, m.col_indices, 8 * m.nnz);
+            std::memcpy(img_.p + img_.o_va + 8 * nz, m.values, 8 * m.nnz);
+            std::memcpy(img_.p + img_.o_v + 8 * vo, m.vec, 8 * m.cols);
+            nz += m.nnz;
+            vo += m.cols;
+        }
+        std::memcpy(img_.p + img_.o_rows, rowrec_.data(), 4 * rowrec_.size());
+        std::memcpy(img_.p + img_.o_sl, slicerec_.data(), 4 * slicerec_.size());
+        std::memcpy(img_.p + img_.o_cols, colrec_.data(), 4 * colrec_.size());
+        std::vector<std::int32_t>().swap(rowrec_);
+        std::vector<std::int32_t>().swap(slicerec_);
+        std::vector<std::int32_t>().swap(colrec_);
+    }
     // the cloud's view of the job: chunk shapes and slice ids (ChunkShapeMeta)
     std::vector<std::uint64_t> key{n, n_out_};
     key.insert(key.end(), r_.begin(), r_.end());
@@ -99,6 +114,7 @@ BatchedSpmv::BatchedSpmv(spmvgpu_ctx* ctx, const HeParams& hp, std::span<const C
         check_status(spmvgpu_ct_alloc(ctx_, n_out_, lease_.out.data()));
     } catch (...) {
         plan_lease_free(ctx_, lease_);
+        client_image_give(ctx_, img_);
         throw;
     }
 }
@@ -160,6 +176,10 @@ void BatchedSpmv::add_slice(const CsrView& m, std::size_t mat, std::size_t r0, s
 }
 
 BatchedSpmv::~BatchedSpmv() {
+    if (img_.p) {
+        if (encrypted_ && !done_) spmvgpu_sync(ctx_);  // the upload may still read the image
+        client_image_give(ctx_, img_);
+    }
     if (lease_.key.empty()) return;
     if (done_)
         plan_cache_give(ctx_, std::move(lease_));
@@ -172,11 +192,10 @@ void BatchedSpmv::encrypt() {
     if (!n) return;
     std::vector<spmvgpu_ct> all(lease_.a);
     all.insert(all.end(), lease_.b.begin(), lease_.b.end());
-    check_status(spmvgpu_encrypt_cssc(ctx_, ci_.data(), va_.data(), ci_.size(), vec_.data(), vec_.size(),
-                                      rowrec_.data(), rowrec_.size() / 4, slicerec_.data(), slicerec_.size() / 2,
-                                      colrec_.data(), colrec_.size() / 4, all.data(), n));
-    h2d_ = sizeof(std::int64_t) * (ci_.size() + va_.size() + vec_.size()) +
-           sizeof(std::int32_t) * (rowrec_.size() + slicerec_.size() + colrec_.size());
+    if (encrypted_) spmvgpu_sync(ctx_);  // re-encryption rewrites the image's stream ids
+    client_image_encrypt(ctx_, img_, all.data());
+    encrypted_ = true;
+    h2d_ = img_.bytes;
 }
 
 void BatchedSpmv::ensure_plan() {

@@ -64,9 +64,10 @@ private:
     std::size_t nmat_;
     std::vector<std::size_t> rows_of_;
     std::vector<Slice> slices_;
-    // device pack image (spmvgpu_encrypt_cssc)
-    std::vector<std::int64_t> ci_, va_, vec_;
+    // device pack descriptors (spmvgpu_encrypt_cssc layout), then the pinned upload image
     std::vector<std::int32_t> rowrec_, slicerec_, colrec_;
+    ClientImage img_;
+    bool encrypted_ = false;
     std::vector<std::uint64_t> r_, c_;
     std::vector<std::uint32_t> slice_id_;
     std::size_t n_out_ = 0;

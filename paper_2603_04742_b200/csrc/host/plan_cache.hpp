@@ -31,4 +31,20 @@ void plan_cache_give(spmvgpu_ctx* ctx, PlanLease&& lease);
 // Frees a lease's plan and ciphertexts.
 void plan_lease_free(spmvgpu_ctx* ctx, PlanLease& lease);
 
+// Client upload image in pinned host memory, laid out like spmvgpu_encrypt_cssc's
+// arrays (BatchedSpmv writes it directly; the descriptors are correct by
+// construction, so this internal path skips the C-ABI's validation).
+struct ClientImage {
+    unsigned char* p = nullptr;
+    std::size_t cap = 0;
+    std::size_t o_ci = 0, o_va = 0, o_v = 0, o_rows = 0, o_sl = 0, o_cols = 0, o_st = 0, o_out = 0, bytes = 0;
+    std::size_t nnz = 0, vec_len = 0, n_rows = 0, n_slices = 0, n_cols = 0;
+    int items = 0;
+};
+ClientImage client_image_take(spmvgpu_ctx* ctx, std::size_t nnz, std::size_t vec_len, std::size_t n_rows,
+                              std::size_t n_slices, std::size_t n_cols, int items);
+void client_image_give(spmvgpu_ctx* ctx, ClientImage& img);
+// fills the stream ids and output handles, uploads, packs and encrypts
+void client_image_encrypt(spmvgpu_ctx* ctx, ClientImage& img, const spmvgpu_ct* out);
+
 }  // namespace spmv::detail
