@@ -411,7 +411,15 @@ void GpuContext::decrypt(const std::vector<const u64*>& cts, u64* slots_host, in
     ensure_ws(wsX_, sizeof(u64) * (size_t)items * L * n);
     ensure_ws(wsM_, sizeof(u64) * (size_t)items * n);
     ensure_ws(wsU_, sizeof(u64) * (size_t)items * (n / 2) + 8 * (size_t)items + 64);
-    auto* dct = upload_ptrs(cts, 0);
+    // one pinned block: ct pointers up, slots + noise deviations down (async copies)
+    const size_t down = sizeof(u64) * (size_t)items * (n / 2) + 8 * (size_t)items;
+    size_t pcap = 0;
+    unsigned char* pin = pinned_take(8 * (size_t)items + down, &pcap);
+    std::memcpy(pin, cts.data(), 8 * (size_t)items);
+    ensure_ws(scratch_[0], std::max<size_t>(8 * (size_t)items, 256));
+    auto* dct = scratch_[0].as<const u64*>();
+    cuda_check(cudaMemcpyAsync(scratch_[0].as<void>(), pin, 8 * (size_t)items, cudaMemcpyHostToDevice, st_),
+               "upload");
     NttJob j = job(nullptr, wsX_.words(), L, range_idx(0, L));
     j.src_items = dct;
     j.src_limb_offset = L;
@@ -430,16 +438,21 @@ void GpuContext::decrypt(const std::vector<const u64*>& cts, u64* slots_host, in
     launch_dec_scale(dc_, P_, dct, wsX_.words(), wsM_.words(), maxdev, items, st_);
     launch_ntt(dc_, logn, false, job(wsM_.words(), wsM_.words(), 1, {P_.t_index()}), items, st_);
     launch_decode_gather(dc_, P_, wsM_.words(), slots_dev, items, st_);
-    std::vector<unsigned long long> md(items);
-    cuda_check(cudaMemcpyAsync(slots_host, slots_dev, sizeof(u64) * (size_t)items * (n / 2),
-                               cudaMemcpyDeviceToHost, st_), "slots");
-    cuda_check(cudaMemcpyAsync(md.data(), maxdev, sizeof(unsigned long long) * items,
-                               cudaMemcpyDeviceToHost, st_), "dev");
-    synchronize();
+    unsigned char* back = pin + 8 * (size_t)items;
+    cuda_check(cudaMemcpyAsync(back, slots_dev, down, cudaMemcpyDeviceToHost, st_), "slots");
+    try {
+        synchronize();
+    } catch (...) {
+        pinned_give(pin, pcap);
+        throw;
+    }
+    std::memcpy(slots_host, back, sizeof(u64) * (size_t)items * (n / 2));
+    const auto* md = reinterpret_cast<const unsigned long long*>(back + sizeof(u64) * (size_t)items * (n / 2));
     for (int i = 0; i < items; ++i) {
         const int bl = md[i] ? 64 - __builtin_clzll(md[i]) : 0;
         if (budgets) budgets[i] = std::max(0, 63 - bl);
     }
+    pinned_give(pin, pcap);
     stats_.kernels += 7;
     stats_.limb_ntts += (u64)items * (2 * L + 1);
 }
