@@ -119,25 +119,26 @@ __global__ void __launch_bounds__(Ntt2<LOGN>::TC, 256 / Ntt2<LOGN>::TC * 2) k_ks
 // ---------------------------------------------------------------------------
 // K2: NTT block phase + key inner product + INTT block phase
 // ---------------------------------------------------------------------------
-// 256 threads at 2^15 (the tiles + twiddles allow only 2 CTAs per SM), 128 below
-template <int LOGN>
-constexpr int ks_blocks_threads() { return LOGN >= 15 ? 256 : 128; }
+// Two 128-thread groups with named barriers: the dnum digit tiles are
+// transformed two at a time, and the two accumulators' inverse transforms run
+// concurrently, so a CTA's serial chain is ceil(dnum/2) + 1 tile transforms.
+constexpr int kKsGroups = 2, kKsGroupThreads = 128;
 
 template <int LOGN, int LT, int KT, int AT>
-__global__ void __launch_bounds__(ks_blocks_threads<LOGN>()) k_ks_blocks_inner(const DevConsts* __restrict__ dc, const u64* __restrict__ DX,
-                                                         const u64* const* KEY, u64* __restrict__ ACC) {
+__global__ void __launch_bounds__(kKsGroups * kKsGroupThreads) k_ks_blocks_inner(const DevConsts* __restrict__ dc,
+                                                                               const u64* __restrict__ DX,
+                                                                               const u64* const* KEY,
+                                                                               u64* __restrict__ ACC) {
     using G = Ntt2<LOGN>;
     extern __shared__ u64 smem[];
     constexpr int PITCH = G::PITCH;
     constexpr int TW = G::LINES * PITCH;
-    constexpr int T = ks_blocks_threads<LOGN>();
+    constexpr int T = kKsGroups * kKsGroupThreads;
     constexpr int PER = G::LINES * G::R2 / T;  // elements per thread
-    u64* work = smem;
-    u64* acc0 = smem + TW;
-    u64* acc1 = smem + 2 * TW;
-    u64* tws = smem + 3 * TW;
     const int L = LT ? LT : dc->L, K = KT ? KT : dc->K, LK = L + K;
     const int alpha = AT ? AT : dc->alpha, dnum = (L + alpha - 1) / alpha;
+    u64* work = smem;               // dnum digit tiles; then acc0 in tile 0, acc1 in tile 1
+    u64* tws = smem + (dnum < 2 ? 2 : dnum) * TW;
     int bid = blockIdx.x;
     const int tileid = bid % G::CTAS_B;
     bid /= G::CTAS_B;
@@ -149,55 +150,56 @@ __global__ void __launch_bounds__(ks_blocks_threads<LOGN>()) k_ks_blocks_inner(c
     const size_t base = (size_t)blk0 * G::R2;
     const u64* key = KEY[item];
     const size_t PL = (size_t)LK * G::N;
+    const int grp = threadIdx.x / kKsGroupThreads;
+    const ThreadGroup tg = cta_slice(grp, kKsGroups);
     // element x = threadIdx.x + T r of the tile (line x >> B, column x & (R2-1)):
     // consecutive lanes touch consecutive words in HBM and in smem (conflict free)
     auto saddr = [](int x) { return (x >> G::B) * PITCH + (x & (G::R2 - 1)); };
     auto addr = [](int l, int pos) { return l * PITCH + pos; };
     auto twf = [&](int sl, int l, int blk) { return block_tw<LOGN>(tws, sl, l, blk); };
     load_block_twiddles<LOGN>(tws, dc->tw[j].fwd, blk0);
-#pragma unroll 1
     for (int dg = 0; dg < dnum; ++dg) {
         const u64* d = DX + (((size_t)item * dnum + dg) * LK + j) * G::N + base;
-        if (dg) __syncthreads();  // previous digit's accumulate finished reading `work`
 #pragma unroll
         for (int r = 0; r < PER; ++r) {
             const int x = threadIdx.x + T * r;
-            cp_async8(work + saddr(x), d + x);
+            cp_async8(work + dg * TW + saddr(x), d + x);
         }
-        cp_async_wait_all();
-        __syncthreads();
-        line_ntt<G::B, 0, false>(work, q, addr, twf);
-        // accumulate work (.) key into acc0/acc1, key tiles streamed coalesced
-        const u64* k0 = key + ((size_t)dg * 2 + 0) * PL + (size_t)j * G::N + base;
-        const u64* k1 = key + ((size_t)dg * 2 + 1) * PL + (size_t)j * G::N + base;
+    }
+    cp_async_wait_all();
+    __syncthreads();
+#pragma unroll 1
+    for (int dg = grp; dg < dnum; dg += kKsGroups) line_ntt<G::B, 0, false>(work + dg * TW, q, addr, twf, tg);
+    __syncthreads();
+    // inner product with both key polynomials, key tiles streamed coalesced;
+    // every position is read (all digits) and then overwritten by one thread
 #pragma unroll
-        for (int r = 0; r < PER; ++r) {
-            const int x = threadIdx.x + T * r, s0 = saddr(x);
-            const u64 w = work[s0];
-            const u64 p0 = mul_mod(w, __ldg(k0 + x), md), p1 = mul_mod(w, __ldg(k1 + x), md);
-            if (dg == 0) {
-                acc0[s0] = p0;
-                acc1[s0] = p1;
-            } else {
-                acc0[s0] = add_mod(acc0[s0], p0, q);
-                acc1[s0] = add_mod(acc1[s0], p1, q);
-            }
+    for (int r = 0; r < PER; ++r) {
+        const int x = threadIdx.x + T * r, s0 = saddr(x);
+        u64 a0 = 0, a1 = 0;
+        for (int dg = 0; dg < dnum; ++dg) {
+            const u64 w = work[dg * TW + s0];
+            const u64* k0 = key + ((size_t)dg * 2 + 0) * PL + (size_t)j * G::N + base;
+            const u64* k1 = key + ((size_t)dg * 2 + 1) * PL + (size_t)j * G::N + base;
+            a0 = add_mod(a0, mul_mod(w, __ldg(k0 + x), md), q);
+            a1 = add_mod(a1, mul_mod(w, __ldg(k1 + x), md), q);
         }
+        work[s0] = a0;
+        work[TW + s0] = a1;
     }
     __syncthreads();
     load_block_twiddles<LOGN>(tws, dc->tw[j].inv, blk0);
     cp_async_wait_all();
     __syncthreads();
-    line_ntt<G::B, 0, true>(acc0, q, addr, twf);
-    line_ntt<G::B, 0, true>(acc1, q, addr, twf);
+    line_ntt<G::B, 0, true>(work + grp * TW, q, addr, twf, tg);  // group p: accumulator p
+    __syncthreads();
 #pragma unroll
     for (int p = 0; p < 2; ++p) {
-        const u64* a = p ? acc1 : acc0;
         u64* dst = ACC + (((size_t)item * 2 + p) * LK + j) * G::N + base;
 #pragma unroll
         for (int r = 0; r < PER; ++r) {
             const int x = threadIdx.x + T * r;
-            dst[x] = a[saddr(x)];
+            dst[x] = work[p * TW + saddr(x)];
         }
     }
 }
@@ -227,17 +229,19 @@ static void ks_fused_t(const DevConsts* dc, const RnsParams& P, const u64* const
     using G = Ntt2<LOGN>;
     const int L = P.cfg.L, K = P.cfg.K, LK = L + K, dnum = P.dnum;
     const int smem1 = G::SMEM_C;
-    const int smem2 = (3 * G::LINES * G::PITCH + 2 * G::TWB) * 8;
-    static bool configured = false;
-    if (!configured) {
+    const int smem2 = ((dnum < 2 ? 2 : dnum) * G::LINES * G::PITCH + 2 * G::TWB) * 8;
+    if (smem2 > 200 * 1024)
+        throw std::invalid_argument("key switch: too many digits for the fused kernel; set fused_key_switch 0");
+    static int configured = 0;  // largest K2 smem set so far (the generic shape's dnum varies)
+    if (smem2 > configured) {
         cudaFuncSetAttribute(k_ks_modup_cols<LOGN, LT, KT, AT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem1);
         cudaFuncSetAttribute(k_ks_blocks_inner<LOGN, LT, KT, AT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
-        configured = true;
+        configured = smem2;
     }
     k_ks_modup_cols<LOGN, LT, KT, AT><<<items * dnum * LK * G::CTAS_C, G::TC, smem1, st>>>(dc, SRC, SRCC, src_poly,
                                                                                       ginv, DX);
     KS_CHECK();
-    k_ks_blocks_inner<LOGN, LT, KT, AT><<<items * LK * G::CTAS_B, ks_blocks_threads<LOGN>(), smem2, st>>>(dc, DX, KEY, ACC);
+    k_ks_blocks_inner<LOGN, LT, KT, AT><<<items * LK * G::CTAS_B, kKsGroups * kKsGroupThreads, smem2, st>>>(dc, DX, KEY, ACC);
     KS_CHECK();
     NttJob j;
     for (int i = 0; i < MAX_JOB_LIMBS; ++i) j.pidx[i] = (signed char)(i % LK);

@@ -22,16 +22,21 @@ namespace cssc {
 template <int LOGN>
 constexpr int mulb_threads() { return LOGN >= 15 ? 256 : 128; }
 
+// k_mul_blocks_tensor runs its four forward and three inverse tile transforms
+// concurrently: four 128-thread groups with named barriers, one tile each.
+constexpr int kMulGroups = 4, kGroupThreads = 128;
+
 template <int LOGN, int LT, int KT>
-__global__ void __launch_bounds__(mulb_threads<LOGN>()) k_mul_blocks_tensor(const DevConsts* __restrict__ dc,
-                                                                            const u64* __restrict__ T,
-                                                                            u64* __restrict__ Z) {
+__global__ void __launch_bounds__(kMulGroups * kGroupThreads) k_mul_blocks_tensor(const DevConsts* __restrict__ dc,
+                                                                                  const u64* __restrict__ T,
+                                                                                  u64* __restrict__ Z) {
     using G = Ntt2<LOGN>;
     extern __shared__ u64 smem[];
     constexpr int PITCH = G::PITCH;
     constexpr int TW = G::LINES * PITCH;
-    constexpr int NT = mulb_threads<LOGN>();
+    constexpr int NT = kMulGroups * kGroupThreads;
     constexpr int PER = G::LINES * G::R2 / NT;
+    static_assert(PER >= 1, "tile smaller than the CTA");
     u64* tile = smem;            // 4 tiles: a0 a1 b0 b1, then z0 z1 z2 in the first three
     u64* tws = smem + 4 * TW;
     const int L = LT ? LT : dc->L, K = KT ? KT : dc->K, M = 2 * L + 1;
@@ -46,6 +51,8 @@ __global__ void __launch_bounds__(mulb_threads<LOGN>()) k_mul_blocks_tensor(cons
     const int blk0 = tileid * G::LINES;
     const size_t base = (size_t)blk0 * G::R2;
     const size_t PM = (size_t)M * G::N;
+    const int grp = threadIdx.x / kGroupThreads;
+    const ThreadGroup tg = cta_slice(grp, kMulGroups);
     auto saddr = [](int x) { return (x >> G::B) * PITCH + (x & (G::R2 - 1)); };
     auto addr = [](int l, int pos) { return l * PITCH + pos; };
     auto twf = [&](int sl, int l, int blk) { return block_tw<LOGN>(tws, sl, l, blk); };
@@ -60,8 +67,8 @@ __global__ void __launch_bounds__(mulb_threads<LOGN>()) k_mul_blocks_tensor(cons
         }
     cp_async_wait_all();
     __syncthreads();
-#pragma unroll 1
-    for (int p = 0; p < 4; ++p) line_ntt<G::B, 0, false>(tile + p * TW, q, addr, twf);
+    line_ntt<G::B, 0, false>(tile + grp * TW, q, addr, twf, tg);  // group g: input g
+    __syncthreads();
     // tensor: a* lazy (< 31q), b* canonicalised, so every product is < 31 q^2 (barrett range)
 #pragma unroll
     for (int r = 0; r < PER; ++r) {
@@ -76,8 +83,8 @@ __global__ void __launch_bounds__(mulb_threads<LOGN>()) k_mul_blocks_tensor(cons
     load_block_twiddles<LOGN>(tws, dc->tw[prime].inv, blk0);
     cp_async_wait_all();
     __syncthreads();
-#pragma unroll 1
-    for (int p = 0; p < 3; ++p) line_ntt<G::B, 0, true>(tile + p * TW, q, addr, twf);
+    if (grp < 3) line_ntt<G::B, 0, true>(tile + grp * TW, q, addr, twf, tg);
+    __syncthreads();
     u64* dst = Z + (size_t)item * 3 * PM + (size_t)j * G::N + base;
 #pragma unroll
     for (int p = 0; p < 3; ++p)
@@ -96,22 +103,24 @@ __global__ void __launch_bounds__(mulb_threads<LOGN>()) k_mul_blocks_tensor(cons
 // written to the slice's result ciphertext for the inverse column phase.
 // Replaces the forward block phase, k_mask_accum and the inverse block phase.
 template <int LOGN>
-__global__ void __launch_bounds__(mulb_threads<LOGN>()) k_mask_blocks(const DevConsts* __restrict__ dc,
-                                                                      const u64* __restrict__ MT,
-                                                                      const int* __restrict__ slice_off,
-                                                                      const int* __restrict__ slice_items,
-                                                                      const int* __restrict__ item_mask,
-                                                                      const u64* __restrict__ MASKS,
-                                                                      u64* const* OUT) {
+__global__ void __launch_bounds__(2 * kGroupThreads) k_mask_blocks(const DevConsts* __restrict__ dc,
+                                                                   const u64* __restrict__ MT,
+                                                                   const int* __restrict__ slice_off,
+                                                                   const int* __restrict__ slice_items,
+                                                                   const int* __restrict__ item_mask,
+                                                                   const u64* __restrict__ MASKS,
+                                                                   u64* const* OUT) {
     using G = Ntt2<LOGN>;
     extern __shared__ u64 smem[];
     constexpr int PITCH = G::PITCH;
     constexpr int TW = G::LINES * PITCH;
-    constexpr int NT = mulb_threads<LOGN>();
+    constexpr int NG = 2;  // groups: chunks x = b + g, b + g + 2, ... each into its own partial sum
+    constexpr int NT = NG * kGroupThreads;
+    constexpr int PERG = G::LINES * G::R2 / kGroupThreads;  // elements per thread within a group
     constexpr int PER = G::LINES * G::R2 / NT;
-    u64* work = smem;
-    u64* acc = smem + TW;
-    u64* tws = smem + 2 * TW;
+    u64* work = smem;             // NG work tiles
+    u64* acc = smem + NG * TW;    // NG partial sums
+    u64* tws = smem + 2 * NG * TW;
     const int L = dc->L;
     int bid = blockIdx.x;
     const int tileid = bid % G::CTAS_B;
@@ -123,31 +132,48 @@ __global__ void __launch_bounds__(mulb_threads<LOGN>()) k_mask_blocks(const DevC
     const u64 q = md.q;
     const int blk0 = tileid * G::LINES;
     const size_t base = (size_t)blk0 * G::R2;
+    const int grp = threadIdx.x / kGroupThreads;
+    const ThreadGroup tg = cta_slice(grp, NG);
+    u64* wk = work + grp * TW;
+    u64* ac = acc + grp * TW;
     auto saddr = [](int x) { return (x >> G::B) * PITCH + (x & (G::R2 - 1)); };
     auto addr = [](int l, int pos) { return l * PITCH + pos; };
     auto twf = [&](int sl_, int l, int blk) { return block_tw<LOGN>(tws, sl_, l, blk); };
     load_block_twiddles<LOGN>(tws, dc->tw[j].fwd, blk0);
+    cp_async_wait_all();
+    __syncthreads();
     const int b = slice_off[sl], e = slice_off[sl + 1];
+    bool any = false;
 #pragma unroll 1
-    for (int x = b; x < e; ++x) {
+    for (int x = b + grp; x < e; x += NG) {
         const int it = slice_items[x];
         const u64* src = MT + ((size_t)it * 2 * L + j2) * G::N + base;
-        if (x > b) __syncthreads();  // previous chunk finished reading `work`
 #pragma unroll
-        for (int r = 0; r < PER; ++r) {
-            const int y = threadIdx.x + NT * r;
-            cp_async8(work + saddr(y), src + y);
+        for (int r = 0; r < PERG; ++r) {
+            const int y = tg.tid + kGroupThreads * r;
+            cp_async8(wk + saddr(y), src + y);
         }
         cp_async_wait_all();
-        __syncthreads();
-        line_ntt<G::B, 0, false>(work, q, addr, twf);
+        tg.sync();
+        line_ntt<G::B, 0, false>(wk, q, addr, twf, tg);
         const u64* mk = MASKS + ((size_t)item_mask[it] * L + j) * G::N + base;
 #pragma unroll
-        for (int r = 0; r < PER; ++r) {
-            const int y = threadIdx.x + NT * r, s0 = saddr(y);
-            const u64 p = mul_mod(work[s0], __ldg(mk + y), md);  // lazy (< 31q) x canonical mask
-            acc[s0] = x == b ? p : add_mod(acc[s0], p, q);
+        for (int r = 0; r < PERG; ++r) {
+            const int y = tg.tid + kGroupThreads * r, s0 = saddr(y);
+            const u64 p = mul_mod(wk[s0], __ldg(mk + y), md);  // lazy (< 31q) x canonical mask
+            ac[s0] = any ? add_mod(ac[s0], p, q) : p;
         }
+        any = true;
+        tg.sync();  // work tile reloaded next round
+    }
+    if (!any)
+#pragma unroll
+        for (int r = 0; r < PERG; ++r) ac[saddr(tg.tid + kGroupThreads * r)] = 0;
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < PER; ++r) {
+        const int s0 = saddr(threadIdx.x + NT * r);
+        acc[s0] = add_mod(acc[s0], acc[TW + s0], q);
     }
     __syncthreads();
     load_block_twiddles<LOGN>(tws, dc->tw[j].inv, blk0);
@@ -167,13 +193,13 @@ static void maskb_t(const DevConsts* dc, const RnsParams& P, const u64* MT, cons
                     const int* slice_items, const int* item_mask, const u64* MASKS, u64* const* OUT, int slices,
                     cudaStream_t st) {
     using G = Ntt2<LOGN>;
-    const int smem = (2 * G::LINES * G::PITCH + 2 * G::TWB) * 8;
+    const int smem = (4 * G::LINES * G::PITCH + 2 * G::TWB) * 8;
     static bool configured = false;
     if (!configured) {
         cudaFuncSetAttribute(k_mask_blocks<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         configured = true;
     }
-    k_mask_blocks<LOGN><<<slices * 2 * P.cfg.L * G::CTAS_B, mulb_threads<LOGN>(), smem, st>>>(
+    k_mask_blocks<LOGN><<<slices * 2 * P.cfg.L * G::CTAS_B, 2 * kGroupThreads, smem, st>>>(
         dc, MT, slice_off, slice_items, item_mask, MASKS, OUT);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) throw std::runtime_error(std::string("mask blocks launch: ") + cudaGetErrorString(e));
@@ -336,7 +362,7 @@ static void mulb_t(const DevConsts* dc, const RnsParams& P, const u64* T, u64* Z
         cudaFuncSetAttribute(k_mul_blocks_tensor<LOGN, LT, KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         configured = true;
     }
-    k_mul_blocks_tensor<LOGN, LT, KT><<<items * M * G::CTAS_B, mulb_threads<LOGN>(), smem, st>>>(dc, T, Z);
+    k_mul_blocks_tensor<LOGN, LT, KT><<<items * M * G::CTAS_B, kMulGroups * kGroupThreads, smem, st>>>(dc, T, Z);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) throw std::runtime_error(std::string("mul blocks launch: ") + cudaGetErrorString(e));
 }

@@ -82,18 +82,38 @@ __device__ __forceinline__ ulonglong2 block_tw(const u64* tws, int s, int l, int
     return *reinterpret_cast<const ulonglong2*>(tws + 2 * (G::tw_off(s) + l * G::tw_stride(s) + blk));
 }
 
+// A set of threads working on one tile: the whole CTA (__syncthreads) or a
+// warp-aligned group of it with its own named barrier, so that several tiles
+// of one CTA are transformed concurrently (fused kernels with many tiles per
+// CTA would otherwise run them one after another).
+struct ThreadGroup {
+    int tid, nthreads, bar;  // bar < 0: the whole CTA
+    __device__ __forceinline__ void sync() const {
+        if (bar < 0)
+            __syncthreads();
+        else
+            asm volatile("bar.sync %0, %1;\n" ::"r"(bar), "r"(nthreads) : "memory");
+    }
+};
+__device__ __forceinline__ ThreadGroup whole_cta() { return ThreadGroup{(int)threadIdx.x, (int)blockDim.x, -1}; }
+// group g of `groups` equal warp-aligned slices of the CTA (named barrier g + 1)
+__device__ __forceinline__ ThreadGroup cta_slice(int g, int groups) {
+    const int n = (int)blockDim.x / groups;
+    return ThreadGroup{(int)threadIdx.x - g * n, n, g + 1};
+}
+
 // One radix-2^R pass over local stages [S0L, S0L+R) of 16 lines of length 2^RB.
 // addr(l, pos): smem word of element pos of line l.  tw(sl, l, blk): twiddle
 // (w, w_shoup) of local stage sl for line l and line-local butterfly block blk.
 template <int RB, int S0L, int R, bool INV, class Addr, class Tw>
-__device__ __forceinline__ void line_pass(u64* s, u64 q, Addr addr, Tw tw) {
+__device__ __forceinline__ void line_pass(u64* s, u64 q, Addr addr, Tw tw, const ThreadGroup& tg) {
     constexpr int E = 1 << R;
     constexpr int TL = 1 << (RB - S0L - R);
     constexpr int LOG_TL = RB - S0L - R;
     constexpr int G = 16 * (1 << (RB - R));
     const u64 two_q = 2 * q;
 #pragma unroll 1
-    for (int gi = threadIdx.x; gi < G; gi += blockDim.x) {
+    for (int gi = tg.tid; gi < G; gi += tg.nthreads) {
         const int l = gi & 15;
         const int g = gi >> 4;
         const int blk = g >> LOG_TL;
@@ -143,21 +163,26 @@ __device__ __forceinline__ void line_pass(u64* s, u64 q, Addr addr, Tw tw) {
 // all passes of a line transform (radix-16 passes, remainder last); inverse
 // runs the passes in reverse order.
 template <int RB, int S0L, bool INV, class Addr, class Tw>
-__device__ __forceinline__ void line_ntt(u64* s, u64 q, Addr addr, Tw tw) {
+__device__ __forceinline__ void line_ntt(u64* s, u64 q, Addr addr, Tw tw, const ThreadGroup& tg) {
     if constexpr (S0L < RB) {
         // pass radix: 6 -> 3+3, 9 -> 3+3+3, 5 -> 3+2, otherwise 4s then the rest
         constexpr int REM = RB - S0L;
         constexpr int R = (REM == 6 || REM == 9 || REM == 5) ? 3 : (REM >= 4 ? 4 : REM);
         if (!INV) {
-            line_pass<RB, S0L, R, false>(s, q, addr, tw);
-            __syncthreads();
-            line_ntt<RB, S0L + R, false>(s, q, addr, tw);
+            line_pass<RB, S0L, R, false>(s, q, addr, tw, tg);
+            tg.sync();
+            line_ntt<RB, S0L + R, false>(s, q, addr, tw, tg);
         } else {
-            line_ntt<RB, S0L + R, true>(s, q, addr, tw);
-            line_pass<RB, S0L, R, true>(s, q, addr, tw);
-            __syncthreads();
+            line_ntt<RB, S0L + R, true>(s, q, addr, tw, tg);
+            line_pass<RB, S0L, R, true>(s, q, addr, tw, tg);
+            tg.sync();
         }
     }
+}
+// the whole CTA on one tile
+template <int RB, int S0L, bool INV, class Addr, class Tw>
+__device__ __forceinline__ void line_ntt(u64* s, u64 q, Addr addr, Tw tw) {
+    line_ntt<RB, S0L, INV>(s, q, addr, tw, whole_cta());
 }
 
 }  // namespace cssc
