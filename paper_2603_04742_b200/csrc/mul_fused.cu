@@ -23,8 +23,10 @@ template <int LOGN>
 constexpr int mulb_threads() { return LOGN >= 15 ? 256 : 128; }
 
 // k_mul_blocks_tensor runs its four forward and three inverse tile transforms
-// concurrently: four 128-thread groups with named barriers, one tile each.
-constexpr int kMulGroups = 4, kGroupThreads = 128;
+// on two 128-thread groups with named barriers (tiles g, g+2): a serial chain
+// of 2 + 2 transforms instead of 7, at the occupancy of a 256-thread CTA
+// (four groups measured no faster: the register file then halves the CTAs).
+constexpr int kMulGroups = 2, kGroupThreads = 128;
 
 template <int LOGN, int LT, int KT>
 __global__ void __launch_bounds__(kMulGroups * kGroupThreads) k_mul_blocks_tensor(const DevConsts* __restrict__ dc,
@@ -67,7 +69,8 @@ __global__ void __launch_bounds__(kMulGroups * kGroupThreads) k_mul_blocks_tenso
         }
     cp_async_wait_all();
     __syncthreads();
-    line_ntt<G::B, 0, false>(tile + grp * TW, q, addr, twf, tg);  // group g: input g
+#pragma unroll 1
+    for (int p = grp; p < 4; p += kMulGroups) line_ntt<G::B, 0, false>(tile + p * TW, q, addr, twf, tg);
     __syncthreads();
     // tensor: a* lazy (< 31q), b* canonicalised, so every product is < 31 q^2 (barrett range)
 #pragma unroll
@@ -83,7 +86,8 @@ __global__ void __launch_bounds__(kMulGroups * kGroupThreads) k_mul_blocks_tenso
     load_block_twiddles<LOGN>(tws, dc->tw[prime].inv, blk0);
     cp_async_wait_all();
     __syncthreads();
-    if (grp < 3) line_ntt<G::B, 0, true>(tile + grp * TW, q, addr, twf, tg);
+#pragma unroll 1
+    for (int p = grp; p < 3; p += kMulGroups) line_ntt<G::B, 0, true>(tile + p * TW, q, addr, twf, tg);
     __syncthreads();
     u64* dst = Z + (size_t)item * 3 * PM + (size_t)j * G::N + base;
 #pragma unroll
