@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(Ntt2<LOGN>::TC, 256 / Ntt2<LOGN>::TC * 2) k_ks
     const int col0 = tileid * G::LINES;
     load_col_twiddles<LOGN>(tws, dc->tw[j].fwd);
     constexpr int PER = G::R1 * 16 / G::TC;  // elements per thread
-#pragma unroll 4
+#pragma unroll 8
     for (int r = 0; r < PER; ++r) {
         const int e = threadIdx.x + G::TC * r, c = e >> 4, jl = e & 15;
         bool neg;
