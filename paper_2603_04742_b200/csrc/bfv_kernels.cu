@@ -118,7 +118,7 @@ __device__ __forceinline__ u64* job_dst(const NttJob& job, int item, int j, int 
 // Column phase: 16 strided columns of R1 elements.  Forward: first phase
 // (src -> dst).  Inverse: last phase (dst -> dst), applies N^-1, canonical.
 template <int LOGN, bool INV>
-__global__ void __launch_bounds__(Ntt2<LOGN>::TC, 256 / Ntt2<LOGN>::TC * 2) k_ntt_cols(const DevConsts* __restrict__ dc, NttJob job) {
+__global__ void __launch_bounds__(Ntt2<LOGN>::TC, 256 / Ntt2<LOGN>::TC * 3) k_ntt_cols(const DevConsts* __restrict__ dc, NttJob job) {
     using G = Ntt2<LOGN>;
     constexpr int T = G::TC;
     extern __shared__ u64 smem[];
@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(Ntt2<LOGN>::TC, 256 / Ntt2<LOGN>::TC * 2) k_nt
         const int k = (1 << sl) + blk;
         return make_ulonglong2(tws[2 * k], tws[2 * k + 1]);
     };
-    line_ntt<G::A, 0, INV>(tile, q, addr, twf);
+    line_ntt<G::A, 0, INV, 3>(tile, q, addr, twf);  // radix-8 passes: 3 CTAs per SM
     const u64 ni = dc->ninv[prime], nish = dc->ninv_sh[prime];
 #pragma unroll
     for (int r = 0; r < G::R1 * 8 / T; ++r) {

@@ -162,27 +162,29 @@ __device__ __forceinline__ void line_pass(u64* s, u64 q, Addr addr, Tw tw, const
 
 // all passes of a line transform (radix-16 passes, remainder last); inverse
 // runs the passes in reverse order.
-template <int RB, int S0L, bool INV, class Addr, class Tw>
+// MAXR caps the pass radix (3: radix-8 passes, fewer live registers).
+template <int RB, int S0L, bool INV, int MAXR = 4, class Addr, class Tw>
 __device__ __forceinline__ void line_ntt(u64* s, u64 q, Addr addr, Tw tw, const ThreadGroup& tg) {
     if constexpr (S0L < RB) {
         // pass radix: 6 -> 3+3, 9 -> 3+3+3, 5 -> 3+2, otherwise 4s then the rest
         constexpr int REM = RB - S0L;
-        constexpr int R = (REM == 6 || REM == 9 || REM == 5) ? 3 : (REM >= 4 ? 4 : REM);
+        constexpr int R0 = (REM == 6 || REM == 9 || REM == 5) ? 3 : (REM >= 4 ? 4 : REM);
+        constexpr int R = R0 < MAXR ? R0 : MAXR;
         if (!INV) {
             line_pass<RB, S0L, R, false>(s, q, addr, tw, tg);
             tg.sync();
-            line_ntt<RB, S0L + R, false>(s, q, addr, tw, tg);
+            line_ntt<RB, S0L + R, false, MAXR>(s, q, addr, tw, tg);
         } else {
-            line_ntt<RB, S0L + R, true>(s, q, addr, tw, tg);
+            line_ntt<RB, S0L + R, true, MAXR>(s, q, addr, tw, tg);
             line_pass<RB, S0L, R, true>(s, q, addr, tw, tg);
             tg.sync();
         }
     }
 }
 // the whole CTA on one tile
-template <int RB, int S0L, bool INV, class Addr, class Tw>
+template <int RB, int S0L, bool INV, int MAXR = 4, class Addr, class Tw>
 __device__ __forceinline__ void line_ntt(u64* s, u64 q, Addr addr, Tw tw) {
-    line_ntt<RB, S0L, INV>(s, q, addr, tw, whole_cta());
+    line_ntt<RB, S0L, INV, MAXR>(s, q, addr, tw, whole_cta());
 }
 
 }  // namespace cssc
