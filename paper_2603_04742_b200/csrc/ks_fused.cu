@@ -53,7 +53,7 @@ __device__ __forceinline__ void load_col_twiddles(u64* tws, const u64* tw) {
 // K1: ModUp + NTT column phase
 // ---------------------------------------------------------------------------
 template <int LOGN, int LT, int KT, int AT>
-__global__ void __launch_bounds__(Ntt2<LOGN>::TC, 256 / Ntt2<LOGN>::TC * 2) k_ks_modup_cols(const DevConsts* __restrict__ dc, const u64* const* SRC,
+__global__ void __launch_bounds__(Ntt2<LOGN>::TC, 256 / Ntt2<LOGN>::TC * 3) k_ks_modup_cols(const DevConsts* __restrict__ dc, const u64* const* SRC,
                                                        const u64* SRCC, int src_poly, const u32* ginv, u64* DX) {
     using G = Ntt2<LOGN>;
     extern __shared__ u64 smem[];
@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(Ntt2<LOGN>::TC, 256 / Ntt2<LOGN>::TC * 2) k_ks
         const int k = (1 << sl) + blk;
         return make_ulonglong2(tws[2 * k], tws[2 * k + 1]);
     };
-    line_ntt<G::A, 0, false>(tile, m, addr, twf);
+    line_ntt<G::A, 0, false, 3>(tile, m, addr, twf);  // radix-8 passes: 3 CTAs per SM
     u64* dst = DX + (((size_t)item * dnum + dg) * LK + j) * G::N;
 #pragma unroll
     for (int r = 0; r < G::R1 * 8 / G::TC; ++r) {
