@@ -102,20 +102,28 @@ __device__ __forceinline__ ThreadGroup cta_slice(int g, int groups) {
     return ThreadGroup{(int)threadIdx.x - g * n, n, g + 1};
 }
 
-// One radix-2^R pass over local stages [S0L, S0L+R) of 16 lines of length 2^RB.
+// the modulus of every line of a tile (one prime per tile)
+struct ConstQ {
+    u64 q;
+    __device__ __forceinline__ u64 operator()(int) const { return q; }
+};
+
+// One radix-2^R pass over local stages [S0L, S0L+R) of VL lines of length 2^RB.
 // addr(l, pos): smem word of element pos of line l.  tw(sl, l, blk): twiddle
 // (w, w_shoup) of local stage sl for line l and line-local butterfly block blk.
-template <int RB, int S0L, int R, bool INV, class Addr, class Tw>
-__device__ __forceinline__ void line_pass(u64* s, u64 q, Addr addr, Tw tw, const ThreadGroup& tg) {
+// qf(l): the modulus of line l (lines of several limbs in one tile).
+template <int RB, int S0L, int R, bool INV, int VL, class QF, class Addr, class Tw>
+__device__ __forceinline__ void line_pass(u64* s, QF qf, Addr addr, Tw tw, const ThreadGroup& tg) {
     constexpr int E = 1 << R;
     constexpr int TL = 1 << (RB - S0L - R);
     constexpr int LOG_TL = RB - S0L - R;
-    constexpr int G = 16 * (1 << (RB - R));
-    const u64 two_q = 2 * q;
+    constexpr int G = VL * (1 << (RB - R));
 #pragma unroll 1
     for (int gi = tg.tid; gi < G; gi += tg.nthreads) {
-        const int l = gi & 15;
-        const int g = gi >> 4;
+        const int l = gi % VL;
+        const int g = gi / VL;
+        const u64 q = qf(l);
+        const u64 two_q = 2 * q;
         const int blk = g >> LOG_TL;
         const int off = g & (TL - 1);
         const int base = (blk << (RB - S0L)) + off;
@@ -163,23 +171,28 @@ __device__ __forceinline__ void line_pass(u64* s, u64 q, Addr addr, Tw tw, const
 // all passes of a line transform (radix-16 passes, remainder last); inverse
 // runs the passes in reverse order.
 // MAXR caps the pass radix (3: radix-8 passes, fewer live registers).
-template <int RB, int S0L, bool INV, int MAXR = 4, class Addr, class Tw>
-__device__ __forceinline__ void line_ntt(u64* s, u64 q, Addr addr, Tw tw, const ThreadGroup& tg) {
+template <int RB, int S0L, bool INV, int MAXR, int VL, class QF, class Addr, class Tw>
+__device__ __forceinline__ void line_ntt_v(u64* s, QF qf, Addr addr, Tw tw, const ThreadGroup& tg) {
     if constexpr (S0L < RB) {
         // pass radix: 6 -> 3+3, 9 -> 3+3+3, 5 -> 3+2, otherwise 4s then the rest
         constexpr int REM = RB - S0L;
         constexpr int R0 = (REM == 6 || REM == 9 || REM == 5) ? 3 : (REM >= 4 ? 4 : REM);
         constexpr int R = R0 < MAXR ? R0 : MAXR;
         if (!INV) {
-            line_pass<RB, S0L, R, false>(s, q, addr, tw, tg);
+            line_pass<RB, S0L, R, false, VL>(s, qf, addr, tw, tg);
             tg.sync();
-            line_ntt<RB, S0L + R, false, MAXR>(s, q, addr, tw, tg);
+            line_ntt_v<RB, S0L + R, false, MAXR, VL>(s, qf, addr, tw, tg);
         } else {
-            line_ntt<RB, S0L + R, true, MAXR>(s, q, addr, tw, tg);
-            line_pass<RB, S0L, R, true>(s, q, addr, tw, tg);
+            line_ntt_v<RB, S0L + R, true, MAXR, VL>(s, qf, addr, tw, tg);
+            line_pass<RB, S0L, R, true, VL>(s, qf, addr, tw, tg);
             tg.sync();
         }
     }
+}
+// 16 lines of one prime
+template <int RB, int S0L, bool INV, int MAXR = 4, class Addr, class Tw>
+__device__ __forceinline__ void line_ntt(u64* s, u64 q, Addr addr, Tw tw, const ThreadGroup& tg) {
+    line_ntt_v<RB, S0L, INV, MAXR, 16>(s, ConstQ{q}, addr, tw, tg);
 }
 // the whole CTA on one tile
 template <int RB, int S0L, bool INV, int MAXR = 4, class Addr, class Tw>
