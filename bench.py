@@ -21,6 +21,7 @@ value = ms_per_step / world_size (amortised latency per workload).
 from __future__ import annotations
 
 import argparse
+from concurrent.futures import ThreadPoolExecutor
 import json
 import os
 import statistics
@@ -162,22 +163,25 @@ def run_reference_arm(args, cfg):
             L.ref_time_spmv_partitioned(S, 65537, m.rows, m.cols, _p(rp, i64p), _p(ci, i64p), _p(va, i64p),
                                         _p(vv, i64p), S, 1)
 
+    parts = [list(range(k, len(ms), threads)) for k in range(threads)]
+    pool = ThreadPoolExecutor(max_workers=threads) if threads > 1 else None  # persistent workers
+
     def step():
-        parts = [list(range(k, len(ms), threads)) for k in range(threads)]
-        ts = [threading.Thread(target=work, args=(p,)) for p in parts]
         t0 = time.perf_counter()
-        for t in ts:
-            t.start()
-        for t in ts:
-            t.join()
+        if pool is None:
+            work(parts[0])
+        else:
+            list(pool.map(work, parts))
         return (time.perf_counter() - t0) * 1e3
 
     for _ in range(args.warmup):
         step()
     times = [step() for _ in range(args.steps)]
+    if pool is not None:
+        pool.shutdown()
     v = statistics.mean(times)
     sample = f"{cfg['name']}: full workload per step ({len(ms)} matrix/matrices), SimBackend slot_count={S}"
-    return {"metric": METRIC, "value": round(v, 4), "unit": "ms", "n_gpus": 0, "steps": args.steps,
+    return {"metric": METRIC, "value": round(v, 4), "unit": "ms", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(v, 4), "higher_is_better": False, "scaling": "weak",
             "vs_baseline": None, "dtype": "u64", "data": "synthetic (seeded, BASELINE.json shapes)",
             "impl": "reference",
