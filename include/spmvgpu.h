@@ -112,7 +112,8 @@ int spmvgpu_encrypt(spmvgpu_ctx* c, const int64_t* vals, const uint64_t* offsets
  *         slice, pos = its place in the slice's descending-length order;
  *   slices: n_slices x {col_base, vec_base};
  *   cols: n_cols x {chunk, k, h, 0}: aligned column j of a slice is record
- *         col_base + j, slot k*h + pos of chunk `chunk` (height h).
+ *         col_base + j, slot k*h + pos of chunk `chunk` (height h); chunk -1
+ *         drops the column's entries (a chunk another GPU evaluates).
  * Entry j of a row lands in out[chunk] (value) and out[n_chunks + chunk]
  * (vec[vec_base + col]); all other slots are 0.  Stream ids as for
  * spmvgpu_encrypt with streams = NULL.  Every index is validated. */
@@ -215,6 +216,14 @@ int cssc_spmv_batch(spmvgpu_ctx* c, const cssc_csr* ms, const int64_t* const* vs
 typedef struct cssc_job cssc_job;
 int cssc_job_create(spmvgpu_ctx* c, const cssc_csr* ms, const int64_t* const* vs, size_t nmat,
                     uint64_t chunk_size, cssc_job** out);
+/* SURVEY 8(e) chunk split: this GPU evaluates the chunks g with g % world == rank;
+ * cssc_job_result_words gives its per-slice partial results ([results][ct words],
+ * zeros where it holds no chunk of a slice; words = NULL: count only), the caller
+ * sums them across GPUs (mod q_j per limb), and cssc_job_finish_words decrypts */
+int cssc_job_create_shard(spmvgpu_ctx* c, const cssc_csr* ms, const int64_t* const* vs, size_t nmat,
+                          uint64_t chunk_size, int rank, int world, cssc_job** out);
+int cssc_job_result_words(cssc_job* j, uint64_t* words, uint64_t cap_words, uint64_t* n_results);
+int cssc_job_finish_words(cssc_job* j, const uint64_t* words, int64_t* const* values, cssc_result* res);
 int cssc_job_encrypt(cssc_job* j);            /* client phase: encode + encrypt on device */
 int cssc_job_cloud(cssc_job* j, int use_graph); /* cloud phase, enqueued (no sync) */
 int cssc_job_finish(cssc_job* j, int64_t* const* values, cssc_result* res); /* decrypt */

@@ -123,6 +123,10 @@ _SIGS = {
                                   C.c_uint64, C.c_int, C.POINTER(i64p), C.POINTER(ResultC)]),
     "cssc_job_create": (C.c_int, [C.c_void_p, C.POINTER(CsrC), C.POINTER(i64p), C.c_size_t,
                                   C.c_uint64, C.POINTER(C.c_void_p)]),
+    "cssc_job_create_shard": (C.c_int, [C.c_void_p, C.POINTER(CsrC), C.POINTER(i64p), C.c_size_t, C.c_uint64,
+                                        C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
+    "cssc_job_result_words": (C.c_int, [C.c_void_p, u64p, C.c_uint64, u64p]),
+    "cssc_job_finish_words": (C.c_int, [C.c_void_p, u64p, C.POINTER(i64p), C.POINTER(ResultC)]),
     "cssc_job_encrypt": (C.c_int, [C.c_void_p]),
     "cssc_job_cloud": (C.c_int, [C.c_void_p, C.c_int]),
     "cssc_job_finish": (C.c_int, [C.c_void_p, C.POINTER(i64p), C.POINTER(ResultC)]),
@@ -516,7 +520,7 @@ def spmv_batch(ctx: Context, ms, vs, chunk_size: int | None = None, key_holder: 
 class Job:
     """Staged evaluation: pack (host) -> encrypt (device) -> cloud (device, repeatable) -> finish."""
 
-    def __init__(self, ctx: Context, ms, vs, chunk_size: int | None = None):
+    def __init__(self, ctx: Context, ms, vs, chunk_size: int | None = None, rank: int = 0, world: int = 1):
         self.ctx, self.ms = ctx, list(ms)
         chunk = ctx.slots if chunk_size is None else chunk_size
         n = len(self.ms)
@@ -524,8 +528,27 @@ class Job:
         self._vv = [_i64(v) for v in vs]
         vptr = (i64p * n)(*[_p(v, i64p) for v in self._vv])
         h = C.c_void_p()
-        check(lib().cssc_job_create(ctx.h, self._csrs, vptr, n, chunk, C.byref(h)))
+        check(lib().cssc_job_create_shard(ctx.h, self._csrs, vptr, n, chunk, rank, world, C.byref(h)))
         self.h = h
+
+    def result_words(self) -> np.ndarray:
+        """This shard's per-slice partial result ciphertexts, [results][ct words]."""
+        cnt = C.c_uint64()
+        check(lib().cssc_job_result_words(self.h, None, 0, C.byref(cnt)))
+        w = np.zeros((cnt.value, self.ctx.ct_words), np.uint64)
+        if cnt.value:
+            check(lib().cssc_job_result_words(self.h, _p(w, u64p), w.size, C.byref(cnt)))
+        return w
+
+    def finish_words(self, words: np.ndarray) -> list:
+        """Decrypt summed partial results (see result_words) and do the bookkeeping."""
+        w = _u64(words)
+        n = len(self.ms)
+        outs = [np.zeros(max(m.rows, 1), np.int64) for m in self.ms]
+        optr = (i64p * n)(*[_p(o, i64p) for o in outs])
+        res = (ResultC * n)()
+        check(lib().cssc_job_finish_words(self.h, _p(w, u64p) if w.size else None, optr, res))
+        return [_result(res[i], outs[i][: self.ms[i].rows]) for i in range(n)]
 
     def encrypt(self):
         check(lib().cssc_job_encrypt(self.h))

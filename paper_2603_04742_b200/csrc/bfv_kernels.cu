@@ -762,6 +762,7 @@ __global__ void k_pack_cssc(const DevConsts* __restrict__ dc, const int64_t* __r
     const int64_t t = (int64_t)dc->t;
     for (int j = gid & ((1 << log_tpr) - 1); j < rec.y; j += 1 << log_tpr) {
         const int4 c = __ldg(cols + sl.x + j);
+        if (c.x < 0) continue;  // a chunk another rank evaluates (sharded jobs)
         const u32 pos = dc->pos0[c.y * c.z + rec.z];
         int64_t a = VA[rec.x + j] % t;
         int64_t b = V[sl.y + CI[rec.x + j]] % t;

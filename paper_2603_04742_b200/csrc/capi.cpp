@@ -524,7 +524,7 @@ int spmvgpu_encrypt_cssc(spmvgpu_ctx* c, const int64_t* col_indices, const int64
         const uint64_t S = g.params().S;
         for (uint64_t k = 0; k < n_cols; ++k) {
             const int32_t* cr = cols + 4 * k;
-            if (cr[0] < 0 || (uint64_t)cr[0] >= n_chunks || cr[1] < 0 || cr[2] <= 0 ||
+            if (cr[0] < -1 || cr[0] >= (int64_t)n_chunks || cr[1] < 0 || cr[2] <= 0 ||
                 ((uint64_t)cr[1] + 1) * (uint64_t)cr[2] > S)
                 throw std::invalid_argument("encrypt_cssc: column record out of range");
         }
@@ -685,16 +685,38 @@ int cssc_spmv_batch(spmvgpu_ctx* c, const cssc_csr* ms, const int64_t* const* vs
     });
 }
 
-int cssc_job_create(spmvgpu_ctx* c, const cssc_csr* ms, const int64_t* const* vs, size_t nmat,
-                    uint64_t chunk_size, cssc_job** out) {
+int cssc_job_create_shard(spmvgpu_ctx* c, const cssc_csr* ms, const int64_t* const* vs, size_t nmat,
+                          uint64_t chunk_size, int rank, int world, cssc_job** out) {
     return guard([&] {
         auto j = std::make_unique<cssc_job>();
         j->ctx = c;
         G(c);
         std::vector<spmv::detail::CsrView> w;
         for (size_t i = 0; i < nmat; ++i) w.push_back(view_of(ms[i], vs[i]));
-        j->job = std::make_unique<spmv::detail::BatchedSpmv>(c, c->hp, w, chunk_size, spmv::PartyRole::ClientA);
+        j->job = std::make_unique<spmv::detail::BatchedSpmv>(c, c->hp, w, chunk_size, spmv::PartyRole::ClientA,
+                                                             true, rank, world);
         *out = j.release();
+    });
+}
+int cssc_job_create(spmvgpu_ctx* c, const cssc_csr* ms, const int64_t* const* vs, size_t nmat,
+                    uint64_t chunk_size, cssc_job** out) {
+    return cssc_job_create_shard(c, ms, vs, nmat, chunk_size, 0, 1, out);
+}
+int cssc_job_result_words(cssc_job* j, uint64_t* words, uint64_t cap_words, uint64_t* n_results) {
+    return guard([&] {
+        if (!j || !n_results) throw std::invalid_argument("null argument");
+        *n_results = j->job->result_count();
+        if (!words) return;
+        const auto w = j->job->result_words();
+        if (cap_words < w.size()) throw std::length_error("result_words: buffer too small");
+        std::memcpy(words, w.data(), sizeof(uint64_t) * w.size());
+    });
+}
+int cssc_job_finish_words(cssc_job* j, const uint64_t* words, int64_t* const* values, cssc_result* res) {
+    return guard([&] {
+        if (!j || (!words && j->job->result_count())) throw std::invalid_argument("null argument");
+        const auto r = j->job->finish_words(words);
+        for (size_t i = 0; i < r.size(); ++i) fill_result(r[i], values ? values[i] : nullptr, res ? res + i : nullptr, nullptr, 0);
     });
 }
 int cssc_job_encrypt(cssc_job* j) { return guard([&] { j->job->encrypt(); }); }

@@ -43,8 +43,9 @@ CsrView view_of(const CsrMatrix& m, std::span<const std::int64_t> v) {
 }
 
 BatchedSpmv::BatchedSpmv(spmvgpu_ctx* ctx, const HeParams& hp, std::span<const CsrView> ms,
-                         std::size_t chunk_size, PartyRole key_holder, bool partition)
-    : ctx_(ctx), hp_(hp), kh_(key_holder), nmat_(ms.size()) {
+                         std::size_t chunk_size, PartyRole key_holder, bool partition, int rank, int world)
+    : ctx_(ctx), hp_(hp), kh_(key_holder), nmat_(ms.size()), rank_(rank), world_(world) {
+    if (world < 1 || rank < 0 || rank >= world) throw std::invalid_argument("shard: rank must be in [0, world)");
     std::size_t nnz_total = 0, vec_total = 0;
     for (const CsrView& m : ms) {
         nnz_total += m.nnz;
@@ -77,7 +78,21 @@ BatchedSpmv::BatchedSpmv(spmvgpu_ctx* ctx, const HeParams& hp, std::span<const C
             add_slice(m, mi, 0, m.rows, chunk_size, nz_base, vec_base);
         }
     }
-    const std::size_t n = r_.size();
+    // this rank's chunks (round-robin over global chunk indices);
+    // world == 1 keeps every chunk
+    std::vector<std::int32_t> local_of(r_.size(), -1);
+    res_local_.assign(n_out_, -1);
+    for (std::size_t g = 0; g < r_.size(); ++g) {
+        if ((int)(g % (std::size_t)world_) != rank_) continue;
+        local_of[g] = static_cast<std::int32_t>(dr_.size());
+        dr_.push_back(r_[g]);
+        dc_.push_back(c_[g]);
+        const std::uint32_t res = slice_id_[g];
+        if (res_local_[res] < 0) res_local_[res] = static_cast<int>(n_dout_++);
+        dslice_.push_back(static_cast<std::uint32_t>(res_local_[res]));
+    }
+    for (std::size_t i = 0; i < colrec_.size(); i += 4) colrec_[i] = local_of[static_cast<std::size_t>(colrec_[i])];
+    const std::size_t n = dr_.size();
     if (!n) return;
     // the client upload image, written once straight from the callers' arrays
     img_ = client_image_take(ctx_, nnz_total, vec_total, rowrec_.size() / 4, slicerec_.size() / 2,
@@ -99,19 +114,19 @@ BatchedSpmv::BatchedSpmv(spmvgpu_ctx* ctx, const HeParams& hp, std::span<const C
         std::vector<std::int32_t>().swap(colrec_);
     }
     // the cloud's view of the job: chunk shapes and slice ids (ChunkShapeMeta)
-    std::vector<std::uint64_t> key{n, n_out_};
-    key.insert(key.end(), r_.begin(), r_.end());
-    key.insert(key.end(), c_.begin(), c_.end());
-    key.insert(key.end(), slice_id_.begin(), slice_id_.end());
+    std::vector<std::uint64_t> key{n, n_dout_};
+    key.insert(key.end(), dr_.begin(), dr_.end());
+    key.insert(key.end(), dc_.begin(), dc_.end());
+    key.insert(key.end(), dslice_.begin(), dslice_.end());
     if (plan_cache_take(ctx_, key, lease_)) return;
     lease_.key = std::move(key);
     lease_.a.assign(n, 0);
     lease_.b.assign(n, 0);
-    lease_.out.assign(n_out_, 0);
+    lease_.out.assign(n_dout_, 0);
     try {
         check_status(spmvgpu_ct_alloc(ctx_, n, lease_.a.data()));
         check_status(spmvgpu_ct_alloc(ctx_, n, lease_.b.data()));
-        check_status(spmvgpu_ct_alloc(ctx_, n_out_, lease_.out.data()));
+        check_status(spmvgpu_ct_alloc(ctx_, n_dout_, lease_.out.data()));
     } catch (...) {
         plan_lease_free(ctx_, lease_);
         client_image_give(ctx_, img_);
@@ -188,7 +203,7 @@ BatchedSpmv::~BatchedSpmv() {
 }
 
 void BatchedSpmv::encrypt() {
-    const std::size_t n = r_.size();
+    const std::size_t n = dr_.size();
     if (!n) return;
     std::vector<spmvgpu_ct> all(lease_.a);
     all.insert(all.end(), lease_.b.begin(), lease_.b.end());
@@ -199,13 +214,13 @@ void BatchedSpmv::encrypt() {
 }
 
 void BatchedSpmv::ensure_plan() {
-    if (lease_.plan || r_.empty()) return;
-    check_status(spmvgpu_plan_create(ctx_, r_.size(), r_.data(), c_.data(), slice_id_.data(), n_out_,
+    if (lease_.plan || dr_.empty()) return;
+    check_status(spmvgpu_plan_create(ctx_, dr_.size(), dr_.data(), dc_.data(), dslice_.data(), n_dout_,
                                      lease_.a.data(), lease_.b.data(), lease_.out.data(), &lease_.plan));
 }
 
 void BatchedSpmv::cloud(bool use_graph) {
-    if (r_.empty()) return;
+    if (dr_.empty()) return;
     ensure_plan();
     // a plan seen before is worth a graph: capture on its second use
     if ((use_graph || lease_.uses > 0) && !lease_.captured) {
@@ -216,12 +231,51 @@ void BatchedSpmv::cloud(bool use_graph) {
     ++lease_.uses;
 }
 
+std::vector<std::uint64_t> BatchedSpmv::result_words() {
+    std::uint64_t n = 0, slots = 0, ctw = 0, kw = 0;
+    int dnum = 0;
+    check_status(spmvgpu_ctx_sizes(ctx_, &n, &slots, &ctw, &kw, &dnum));
+    std::vector<std::uint64_t> w(n_out_ * ctw, 0);
+    for (std::size_t r = 0; r < n_out_; ++r)
+        if (res_local_[r] >= 0)
+            check_status(spmvgpu_ct_download(ctx_, lease_.out[static_cast<std::size_t>(res_local_[r])],
+                                             w.data() + r * ctw));
+    if (!n_out_) check_status(spmvgpu_sync(ctx_));
+    return w;
+}
+
 std::vector<SpmvResult> BatchedSpmv::finish() {
+    if (world_ > 1)
+        throw std::invalid_argument("finish: a sharded job holds partial results; sum result_words() across "
+                                    "ranks and call finish_words()");
+    std::vector<spmvgpu_ct> outs(n_out_);
+    for (std::size_t r = 0; r < n_out_; ++r) outs[r] = lease_.out[static_cast<std::size_t>(res_local_[r])];
+    return decrypt_and_report(outs);
+}
+
+std::vector<SpmvResult> BatchedSpmv::finish_words(const std::uint64_t* words) {
+    std::uint64_t n = 0, slots = 0, ctw = 0, kw = 0;
+    int dnum = 0;
+    check_status(spmvgpu_ctx_sizes(ctx_, &n, &slots, &ctw, &kw, &dnum));
+    std::vector<spmvgpu_ct> tmp(n_out_, 0);
+    if (n_out_) check_status(spmvgpu_ct_alloc(ctx_, n_out_, tmp.data()));
+    try {
+        for (std::size_t r = 0; r < n_out_; ++r) check_status(spmvgpu_ct_upload(ctx_, tmp[r], words + r * ctw));
+        auto res = decrypt_and_report(tmp);
+        if (n_out_) spmvgpu_ct_free(ctx_, tmp.data(), tmp.size());
+        return res;
+    } catch (...) {
+        if (n_out_) spmvgpu_ct_free(ctx_, tmp.data(), tmp.size());
+        throw;
+    }
+}
+
+std::vector<SpmvResult> BatchedSpmv::decrypt_and_report(const std::vector<spmvgpu_ct>& outs) {
     const std::size_t S = hp_.slot_count;
     std::vector<std::uint64_t> slots(n_out_ * S);
     std::vector<std::int32_t> measured(n_out_, 0);
     if (n_out_)
-        check_status(spmvgpu_decrypt(ctx_, lease_.out.data(), n_out_, slots.data(), measured.data()));
+        check_status(spmvgpu_decrypt(ctx_, outs.data(), n_out_, slots.data(), measured.data()));
     else
         check_status(spmvgpu_sync(ctx_));
     done_ = true;

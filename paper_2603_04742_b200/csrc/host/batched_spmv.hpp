@@ -30,8 +30,11 @@ CsrView view_of(const CsrMatrix& m, std::span<const std::int64_t> v);
 
 class BatchedSpmv {
 public:
+    // rank/world: evaluate only the chunks g with g % world == rank (SURVEY 8(e):
+    // chunks split across GPUs); the per-slice partial results are summed
+    // across ranks from result_words() and decrypted with finish_words()
     BatchedSpmv(spmvgpu_ctx* ctx, const HeParams& hp, std::span<const CsrView> ms, std::size_t chunk_size,
-                PartyRole key_holder, bool partition = true);
+                PartyRole key_holder, bool partition = true, int rank = 0, int world = 1);
     ~BatchedSpmv();
     BatchedSpmv(const BatchedSpmv&) = delete;
     BatchedSpmv& operator=(const BatchedSpmv&) = delete;
@@ -39,11 +42,17 @@ public:
     void encrypt();               // Client A + Client B: pack + encrypt on the device
     void cloud(bool use_graph);   // enqueue the cloud plan (no host sync)
     std::vector<SpmvResult> finish();  // key holder: decrypt, unpermute, bookkeeping
+    // this rank's per-slice result ciphertext words (zeros for slices it holds
+    // no chunk of), [results][ct words]; and the decryption of summed words
+    std::vector<std::uint64_t> result_words();
+    std::vector<SpmvResult> finish_words(const std::uint64_t* words);
+    std::size_t result_count() const { return n_out_; }
 
     spmvgpu_plan* plan() const { return lease_.plan; }
     std::uint64_t h2d_bytes() const { return h2d_; }
     std::uint64_t d2h_bytes() const { return d2h_; }
     std::size_t total_chunks() const { return r_.size(); }
+    std::size_t local_chunks() const { return dr_.size(); }
 
 private:
     struct Slice {
@@ -57,6 +66,7 @@ private:
     void add_slice(const CsrView& m, std::size_t mat, std::size_t r0, std::size_t r1, std::size_t budget,
                    std::int64_t nz_base, std::int64_t vec_base);
     void ensure_plan();
+    std::vector<SpmvResult> decrypt_and_report(const std::vector<spmvgpu_ct>& outs);
 
     spmvgpu_ctx* ctx_;
     HeParams hp_;
@@ -71,6 +81,12 @@ private:
     std::vector<std::uint64_t> r_, c_;
     std::vector<std::uint32_t> slice_id_;
     std::size_t n_out_ = 0;
+    // this rank's share: local chunk shapes, local result ids, global -> local result
+    int rank_ = 0, world_ = 1;
+    std::vector<std::uint64_t> dr_, dc_;
+    std::vector<std::uint32_t> dslice_;
+    std::vector<int> res_local_;
+    std::size_t n_dout_ = 0;
     PlanLease lease_;  // plan + ciphertext buffers, from / back to the context's plan cache
     bool done_ = false;
     std::uint64_t h2d_ = 0, d2h_ = 0;

@@ -1,9 +1,16 @@
-"""Multi-GPU sharding of independent SpMV units.
+"""Multi-GPU sharding.
 
-Row slices of one matrix and the matrices of a batch are independent until
-their outputs are concatenated (reference protocol.cpp:164-174), so N GPUs
-take units round-robin with no data-path collective; the only communication
-is gathering the decrypted result rows to the key holder (rank 0).
+* run_sharded: row slices of one matrix and the matrices of a batch are
+  independent until their outputs are concatenated (reference
+  protocol.cpp:164-174), so N GPUs take units round-robin with no data-path
+  collective; only the decrypted rows are gathered at the key holder (rank 0).
+* run_chunk_split: one large matrix (C3/C4) splits its chunks round-robin over
+  the GPUs; each GPU runs multiply, rotate-and-add and the masked
+  accumulation of its chunks, giving per-slice partial result ciphertexts;
+  one all-reduce (sum of uint64 words, NCCL) per job adds them, a mod-q_j
+  fold per limb restores residues (exact: world * q_j < 2^63 for q_j < 2^58,
+  world <= 16), and rank 0 decrypts.  inter_chunk_sum is a plain sum
+  (aggregate.cpp:64-72), so the result equals the single-GPU evaluation.
 """
 from __future__ import annotations
 
@@ -41,3 +48,49 @@ def run_sharded(ctx, ms, vs, chunk_size=None):
     res = spmv_batch(ctx, [ms[i] for i in mine], [vs[i] for i in mine], chunk_size) if mine else []
     local = {i: r["values"] for i, r in zip(mine, res)}
     return gather_values(local, len(ms), [m.rows for m in ms])
+
+
+def fold_mod(words: np.ndarray, primes, L: int, n: int) -> np.ndarray:
+    """Sums of partial ciphertext words -> residues: [results][2][L][N] mod q_j."""
+    w = np.asarray(words, dtype=np.uint64).reshape(-1, 2, L, n)
+    q = np.asarray(primes[:L], dtype=np.uint64).reshape(1, 1, L, 1)
+    return (w % q).reshape(w.shape[0], -1)
+
+
+def reduce_partials(words: np.ndarray, primes, L: int, n: int, device=None) -> np.ndarray | None:
+    """All-reduce this rank's partial result words (torch.distributed) and fold
+    them mod q; returns the folded words on rank 0, None elsewhere."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size()
+    if world > 16:
+        raise ValueError("chunk split: the uint64 sum is exact for at most 16 ranks")
+    t = torch.from_numpy(np.ascontiguousarray(words).view(np.int64).copy())
+    if device is not None:
+        t = t.to(device)
+    dist.all_reduce(t)
+    if dist.get_rank() != 0:
+        return None
+    q = torch.tensor([int(x) for x in primes[:L]], dtype=torch.int64, device=t.device).view(1, 1, L, 1)
+    folded = torch.remainder(t.view(-1, 2, L, n), q)
+    return folded.view(t.shape).cpu().numpy().view(np.uint64)
+
+
+def run_chunk_split(ctx, ms, vs, chunk_size=None, device=None):
+    """Evaluate this rank's chunks of every slice, sum the partial results across
+    ranks, decrypt at rank 0 (returns the results there, None elsewhere)."""
+    import torch.distributed as dist
+
+    from . import Job
+
+    rank, world = dist.get_rank(), dist.get_world_size()
+    job = Job(ctx, ms, vs, chunk_size, rank=rank, world=world)
+    try:
+        job.encrypt()
+        job.cloud(graph=True)
+        words = job.result_words()
+        summed = reduce_partials(words, ctx.primes, ctx.L, ctx.n, device)
+        return job.finish_words(summed) if summed is not None else None
+    finally:
+        job.close()

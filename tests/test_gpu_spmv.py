@@ -154,3 +154,33 @@ def test_matches_reference_fixtures(ctx10, ctx13, case):
     assert [int(x) for x in got["values"]] == case["values"]
     assert got["ledger"] == case["ledger"] and got["n_ct"] == case["n_ct"] and got["noise"] == case["noise"]
     assert [list(x) for x in got["messages"]] == case["messages"]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_chunk_split_shards_sum_to_the_full_result(world):
+    """the chunks of one matrix split over `world` shards (evaluated
+    here one after another on one GPU); the summed partial results, folded mod
+    q, decrypt to the reference's values, ledger, transcript and noise."""
+    ctx = pk.Context(logn=10, seed=8)
+    m = pk.random_sparse_csr(1300, 700, 6000, 77, -8, 8)  # 3 slices of 512 rows, several chunks each
+    v = pk.random_vector(700, 77, -8, 8, nonzero=True)
+    from paper_2603_04742_b200 import shard
+    total = None
+    jobs = []
+    for r in range(world):
+        job = pk.Job(ctx, [m], [v], rank=r, world=world)
+        job.encrypt()
+        job.cloud(graph=r == 0)
+        w = job.result_words()
+        total = w if total is None else total + w
+        jobs.append(job)
+    folded = shard.fold_mod(total, ctx.primes, ctx.L, ctx.n)
+    got = jobs[0].finish_words(folded)[0]
+    want = checker(m, v, ctx.slots, ctx.slots)
+    assert np.array_equal(got["values"], want["values"])
+    assert got["ledger"] == want["ledger"] and got["n_ct"] == want["n_ct"] and got["noise"] == want["noise"]
+    with pytest.raises(pk.SpmvError):  # a shard alone cannot decrypt its partial slices
+        jobs[1].finish()
+    for j in jobs:
+        j.close()
+    ctx.close()
