@@ -360,43 +360,53 @@ void GpuContext::encrypt_cssc(const int64_t* ci, const int64_t* va, size_t nnz, 
     encrypt_cssc_image(h, lay);
 }
 
-void GpuContext::encrypt_cssc_image(const unsigned char* img, const CsscLayout& lay) {
+void GpuContext::encrypt_cssc_image(const unsigned char* img, const CsscLayout& lay, const ClientWs* ws) {
     const int items = lay.items;
     if (!items) return;
-    ensure_ws(scratch_[0], std::max<size_t>(lay.bytes, 256));
-    auto* d = scratch_[0].as<unsigned char>();
+    unsigned char* d;
+    u64 *U, *CM;
+    if (ws) {
+        d = ws->up;
+        U = ws->U;
+        CM = ws->CM;
+    } else {
+        ensure_ws(scratch_[0], std::max<size_t>(lay.bytes, 256));
+        d = scratch_[0].as<unsigned char>();
+        CM = enc_workspace(items);
+        U = wsU_.words();
+    }
     cuda_check(cudaMemcpyAsync(d, img, lay.bytes, cudaMemcpyHostToDevice, st_), "upload");
     if (img == stage_) cuda_check(cudaEventRecord(stage_ev_, st_), "event");  // staging reusable after this
     int log_tpr = 0;
     while (log_tpr < 5 && (lay.n_rows << log_tpr) < lay.nnz) ++log_tpr;
-    u64* CM = enc_workspace(items);
     launch_pack_cssc(dc_, P_, reinterpret_cast<const int64_t*>(d + lay.o_ci),
                      reinterpret_cast<const int64_t*>(d + lay.o_va), reinterpret_cast<const int64_t*>(d + lay.o_v),
                      reinterpret_cast<const int4*>(d + lay.o_rows), (int)lay.n_rows,
                      reinterpret_cast<const int2*>(d + lay.o_sl), reinterpret_cast<const int4*>(d + lay.o_cols),
                      items / 2, log_tpr, CM + (size_t)2 * P_.cfg.L * P_.n, cm_stride(), st_);
-    encrypt_encoded(reinterpret_cast<const u64*>(d + lay.o_st), reinterpret_cast<u64* const*>(d + lay.o_out), items);
+    encrypt_encoded(reinterpret_cast<const u64*>(d + lay.o_st), reinterpret_cast<u64* const*>(d + lay.o_out), items,
+                    U, CM);
 }
 
 // CM = wsC_[item][2L+1][N] holds the encoded messages in limb 2L on entry;
 // the inverse NTT of the message (mod t) rides in the same launch as the
 // inverse NTT of pk * u (limbs 0 .. 2L-1).
-void GpuContext::encrypt_encoded(const u64* d_streams, u64* const* d_out, int items) {
+void GpuContext::encrypt_encoded(const u64* d_streams, u64* const* d_out, int items, u64* U, u64* CM) {
     const int L = P_.cfg.L, logn = P_.cfg.logn;
-    u64* CM = wsC_.words();
-    launch_enc_sample_u(dc_, P_, P_.cfg.seed, d_streams, wsU_.words(), items, st_);
+    if (!U) U = wsU_.words();
+    if (!CM) CM = wsC_.words();
+    launch_enc_sample_u(dc_, P_, P_.cfg.seed, d_streams, U, items, st_);
     std::vector<int> pidx = range_idx(0, L);
     pidx.insert(pidx.end(), pidx.begin(), pidx.end());
     pidx.push_back(P_.t_index());
     if (fused_ks_) {  // NTT(u) column phase; block phase x pk + inverse block phase (+ message); columns
-        launch_ntt_phase(dc_, logn, false, true, job(wsU_.words(), wsU_.words(), L, range_idx(0, L)), items, st_);
-        launch_blocks_mul_inv(dc_, P_, wsU_.words(), pk_.words(), 2, CM, cm_stride(), CM, 2 * L, P_.t_index(),
-                              items, st_);
+        launch_ntt_phase(dc_, logn, false, true, job(U, U, L, range_idx(0, L)), items, st_);
+        launch_blocks_mul_inv(dc_, P_, U, pk_.words(), 2, CM, cm_stride(), CM, 2 * L, P_.t_index(), items, st_);
         launch_ntt_phase(dc_, logn, true, true, job(CM, CM, 2 * L + 1, pidx), items, st_);
         stats_.kernels += 5;
     } else {
-        launch_ntt(dc_, logn, false, job(wsU_.words(), wsU_.words(), L, range_idx(0, L)), items, st_);
-        launch_enc_pk(dc_, P_, pk_.words(), wsU_.words(), CM, items, st_);
+        launch_ntt(dc_, logn, false, job(U, U, L, range_idx(0, L)), items, st_);
+        launch_enc_pk(dc_, P_, pk_.words(), U, CM, items, st_);
         launch_ntt(dc_, logn, true, job(CM, CM, 2 * L + 1, pidx), items, st_);
         stats_.kernels += 7;
     }
@@ -420,24 +430,9 @@ void GpuContext::decrypt(const std::vector<const u64*>& cts, u64* slots_host, in
     auto* dct = scratch_[0].as<const u64*>();
     cuda_check(cudaMemcpyAsync(scratch_[0].as<void>(), pin, 8 * (size_t)items, cudaMemcpyHostToDevice, st_),
                "upload");
-    NttJob j = job(nullptr, wsX_.words(), L, range_idx(0, L));
-    j.src_items = dct;
-    j.src_limb_offset = L;
-    if (fused_ks_) {  // column phase of c1; block phase x s + inverse block phase; inverse columns
-        launch_ntt_phase(dc_, logn, false, true, j, items, st_);
-        launch_blocks_mul_inv(dc_, P_, wsX_.words(), s_ntt_.words(), 1, wsX_.words(), (size_t)L * n, nullptr,
-                              0, 0, items, st_);
-        launch_ntt_phase(dc_, logn, true, true, job(wsX_.words(), wsX_.words(), L, range_idx(0, L)), items, st_);
-    } else {
-        launch_ntt(dc_, logn, false, j, items, st_);
-        launch_mul_s(dc_, P_, wsX_.words(), s_ntt_.words(), items, st_);
-        launch_ntt(dc_, logn, true, job(wsX_.words(), wsX_.words(), L, range_idx(0, L)), items, st_);
-    }
     u64* slots_dev = wsU_.words();
     auto* maxdev = reinterpret_cast<unsigned long long*>(wsU_.words() + (size_t)items * (n / 2));
-    launch_dec_scale(dc_, P_, dct, wsX_.words(), wsM_.words(), maxdev, items, st_);
-    launch_ntt(dc_, logn, false, job(wsM_.words(), wsM_.words(), 1, {P_.t_index()}), items, st_);
-    launch_decode_gather(dc_, P_, wsM_.words(), slots_dev, items, st_);
+    decrypt_dev(dct, items, wsX_.words(), wsM_.words(), slots_dev, maxdev);
     unsigned char* back = pin + 8 * (size_t)items;
     cuda_check(cudaMemcpyAsync(back, slots_dev, down, cudaMemcpyDeviceToHost, st_), "slots");
     try {
@@ -453,6 +448,26 @@ void GpuContext::decrypt(const std::vector<const u64*>& cts, u64* slots_host, in
         if (budgets) budgets[i] = std::max(0, 63 - bl);
     }
     pinned_give(pin, pcap);
+}
+
+void GpuContext::decrypt_dev(const u64* const* dct, int items, u64* X, u64* M, u64* slots_dev,
+                             unsigned long long* maxdev) {
+    const int n = P_.n, L = P_.cfg.L, logn = P_.cfg.logn;
+    NttJob j = job(nullptr, X, L, range_idx(0, L));
+    j.src_items = dct;
+    j.src_limb_offset = L;
+    if (fused_ks_) {  // column phase of c1; block phase x s + inverse block phase; inverse columns
+        launch_ntt_phase(dc_, logn, false, true, j, items, st_);
+        launch_blocks_mul_inv(dc_, P_, X, s_ntt_.words(), 1, X, (size_t)L * n, nullptr, 0, 0, items, st_);
+        launch_ntt_phase(dc_, logn, true, true, job(X, X, L, range_idx(0, L)), items, st_);
+    } else {
+        launch_ntt(dc_, logn, false, j, items, st_);
+        launch_mul_s(dc_, P_, X, s_ntt_.words(), items, st_);
+        launch_ntt(dc_, logn, true, job(X, X, L, range_idx(0, L)), items, st_);
+    }
+    launch_dec_scale(dc_, P_, dct, X, M, maxdev, items, st_);
+    launch_ntt(dc_, logn, false, job(M, M, 1, {P_.t_index()}), items, st_);
+    launch_decode_gather(dc_, P_, M, slots_dev, items, st_);
     stats_.kernels += 7;
     stats_.limb_ntts += (u64)items * (2 * L + 1);
 }

@@ -68,6 +68,17 @@ struct CsscLayout {
     static CsscLayout make(size_t nnz, size_t vec_len, size_t n_rows, size_t n_slices, size_t n_cols, int items);
 };
 
+// Device buffers of a client pass owned by its caller (a cached pipeline), so
+// that a captured graph never points into the context's growable workspaces.
+struct ClientWs {
+    unsigned char* up = nullptr;  // upload image
+    u64* U = nullptr;             // [items][L][N] encryption u
+    u64* CM = nullptr;            // [items][2L+1][N] encryption accumulators + message
+    u64* X = nullptr;             // [results][L][N] decryption c1*s
+    u64* M = nullptr;             // [results][N] decoded message
+    u64* slots = nullptr;         // [results][S] slots, then [results] noise deviations
+};
+
 class GpuContext {
 public:
     explicit GpuContext(const RnsConfig& cfg, int device = 0);
@@ -114,11 +125,14 @@ public:
     // the same from an image already laid out in pinned host memory (trusted
     // descriptors: the caller built them); the image must stay alive until the
     // stream has consumed it
-    void encrypt_cssc_image(const unsigned char* img, const CsscLayout& lay);
+    void encrypt_cssc_image(const unsigned char* img, const CsscLayout& lay, const ClientWs* ws = nullptr);
     // pinned host buffers, pooled by capacity
     unsigned char* pinned_take(size_t bytes, size_t* cap);
     void pinned_give(unsigned char* p, size_t cap);
     void decrypt(const std::vector<const u64*>& cts, u64* slots_host, int* budgets);
+    // capture-safe device part of decrypt: slots_dev[items][S], maxdev[items]
+    // (zeroed here) from the device pointer array dct
+    void decrypt_dev(const u64* const* dct, int items, u64* X, u64* M, u64* slots_dev, unsigned long long* maxdev);
     void add(const std::vector<const u64*>& a, const std::vector<const u64*>& b,
              const std::vector<u64*>& out);
     void mul_relin(const std::vector<const u64*>& a, const std::vector<const u64*>& b,
@@ -151,6 +165,7 @@ public:
     size_t dx_words() const { return (size_t)P_.dnum * (P_.cfg.L + P_.cfg.K) * P_.n; }
     size_t ksacc_words() const { return (size_t)2 * (P_.cfg.L + P_.cfg.K) * P_.n; }
     size_t poly_words() const { return (size_t)P_.cfg.L * P_.n; }
+    size_t cm_stride() const { return (size_t)(2 * P_.cfg.L + 1) * P_.n; }  // encryption CM item stride
 
     // scratch pointer arrays (stream-ordered reuse)
     template <class T>
@@ -160,9 +175,8 @@ public:
 private:
     void keygen();
     // encryption of the encoded messages staged in limb 2L of the CM workspace
-    void encrypt_encoded(const u64* d_streams, u64* const* d_out, int items);
+    void encrypt_encoded(const u64* d_streams, u64* const* d_out, int items, u64* U = nullptr, u64* CM = nullptr);
     u64* enc_workspace(int items);  // wsU_ + wsC_ (CM layout), returns CM
-    size_t cm_stride() const { return (size_t)(2 * P_.cfg.L + 1) * P_.n; }
     // pinned host staging buffer, reusable once its previous upload completed
     unsigned char* stage_host(size_t bytes);
     void* stage_upload(size_t bytes, int slot);

@@ -178,6 +178,12 @@ bool plan_cache_take(spmvgpu_ctx* ctx, const std::vector<std::uint64_t>& key, Pl
 void plan_lease_free(spmvgpu_ctx* ctx, PlanLease& l) {
     if (l.plan) spmvgpu_plan_destroy(l.plan);
     l.plan = nullptr;
+    if (ctx->g) {
+        if (l.pimg) ctx->g->pinned_give(l.pimg, l.pimg_cap);
+        if (l.pout) ctx->g->pinned_give(l.pout, l.pout_cap);
+    }
+    l.pimg = l.pout = nullptr;
+    l.pkey.clear();
     for (auto* v : {&l.a, &l.b, &l.out}) {
         if (!v->empty()) spmvgpu_ct_free(ctx, v->data(), v->size());
         v->clear();
@@ -201,11 +207,10 @@ void plan_cache_give(spmvgpu_ctx* ctx, PlanLease&& lease) {
 
 namespace spmv::detail {
 
-ClientImage client_image_take(spmvgpu_ctx* ctx, std::size_t nnz, std::size_t vec_len, std::size_t n_rows,
-                              std::size_t n_slices, std::size_t n_cols, int items) {
+ClientImage client_image_layout(std::size_t nnz, std::size_t vec_len, std::size_t n_rows, std::size_t n_slices,
+                                std::size_t n_cols, int items) {
     const cssc::CsscLayout l = cssc::CsscLayout::make(nnz, vec_len, n_rows, n_slices, n_cols, items);
     ClientImage img;
-    img.p = ctx->g->pinned_take(l.bytes, &img.cap);
     img.o_ci = l.o_ci;
     img.o_va = l.o_va;
     img.o_v = l.o_v;
@@ -224,16 +229,81 @@ ClientImage client_image_take(spmvgpu_ctx* ctx, std::size_t nnz, std::size_t vec
     return img;
 }
 
+ClientImage client_image_take(spmvgpu_ctx* ctx, std::size_t nnz, std::size_t vec_len, std::size_t n_rows,
+                              std::size_t n_slices, std::size_t n_cols, int items) {
+    ClientImage img = client_image_layout(nnz, vec_len, n_rows, n_slices, n_cols, items);
+    img.p = ctx->g->pinned_take(img.bytes, &img.cap);
+    return img;
+}
+
 void client_image_give(spmvgpu_ctx* ctx, ClientImage& img) {
     if (img.p) ctx->g->pinned_give(img.p, img.cap);
     img.p = nullptr;
 }
 
+void client_image_fill(spmvgpu_ctx* ctx, unsigned char* p, const ClientImage& img, const spmvgpu_ct* out) {
+    auto& g = *ctx->g;
+    auto* st = reinterpret_cast<std::uint64_t*>(p + img.o_st);
+    for (int i = 0; i < img.items; ++i) st[i] = g.next_stream_id();
+    std::memcpy(p + img.o_out, out, sizeof(spmvgpu_ct) * (std::size_t)img.items);
+}
+
+std::vector<std::size_t> client_image_key(const ClientImage& img) {
+    return {img.bytes, img.nnz, img.vec_len, img.n_rows, img.n_slices, img.n_cols, (std::size_t)img.items};
+}
+
+static cssc::CsscLayout layout_of(const ClientImage& img) {
+    cssc::CsscLayout l;
+    l.o_ci = img.o_ci;
+    l.o_va = img.o_va;
+    l.o_v = img.o_v;
+    l.o_rows = img.o_rows;
+    l.o_sl = img.o_sl;
+    l.o_cols = img.o_cols;
+    l.o_st = img.o_st;
+    l.o_out = img.o_out;
+    l.bytes = img.bytes;
+    l.nnz = img.nnz;
+    l.vec_len = img.vec_len;
+    l.n_rows = img.n_rows;
+    l.n_slices = img.n_slices;
+    l.n_cols = img.n_cols;
+    l.items = img.items;
+    return l;
+}
+
+bool pipeline_ready(const PlanLease& lease, const ClientImage& img) {
+    return lease.plan && lease.plan->plan->has_pipeline() && lease.pimg && lease.pkey == client_image_key(img);
+}
+
+void pipeline_prepare(spmvgpu_ctx* ctx, PlanLease& lease, const ClientImage& img) {
+    auto& g = *ctx->g;
+    if (!lease.plan) throw std::logic_error("pipeline: no plan");
+    const int ns = lease.plan->plan->results();
+    const std::size_t out_bytes = sizeof(std::uint64_t) * (std::size_t)ns * (g.n() / 2) + 8 * (std::size_t)ns;
+    if (!lease.pimg || lease.pimg_cap < img.bytes) {
+        if (lease.pimg) g.pinned_give(lease.pimg, lease.pimg_cap);
+        lease.pimg = nullptr;
+        lease.pimg = g.pinned_take(img.bytes, &lease.pimg_cap);
+    }
+    if (!lease.pout || lease.pout_cap < out_bytes) {
+        if (lease.pout) g.pinned_give(lease.pout, lease.pout_cap);
+        lease.pout = nullptr;
+        lease.pout = g.pinned_take(out_bytes, &lease.pout_cap);
+    }
+    lease.pkey.clear();
+    lease.plan->plan->capture_pipeline(lease.pimg, layout_of(img), lease.pout);
+    lease.pkey = client_image_key(img);
+}
+
+void pipeline_run(spmvgpu_ctx* ctx, PlanLease& lease) {
+    lease.plan->plan->run_pipeline();
+    ctx->g->synchronize();
+}
+
 void client_image_encrypt(spmvgpu_ctx* ctx, ClientImage& img, const spmvgpu_ct* out) {
     auto& g = *ctx->g;
-    auto* st = reinterpret_cast<std::uint64_t*>(img.p + img.o_st);
-    for (int i = 0; i < img.items; ++i) st[i] = g.next_stream_id();
-    std::memcpy(img.p + img.o_out, out, sizeof(spmvgpu_ct) * (std::size_t)img.items);
+    client_image_fill(ctx, img.p, img, out);
     cssc::CsscLayout l;
     l.o_ci = img.o_ci;
     l.o_va = img.o_va;
@@ -678,9 +748,7 @@ int cssc_spmv_batch(spmvgpu_ctx* c, const cssc_csr* ms, const int64_t* const* vs
         std::vector<spmv::detail::CsrView> w;
         for (size_t i = 0; i < nmat; ++i) w.push_back(view_of(ms[i], vs[i]));
         spmv::detail::BatchedSpmv job(c, c->hp, w, chunk_size, static_cast<spmv::PartyRole>(key_holder));
-        job.encrypt();
-        job.cloud(false);
-        const auto r = job.finish();
+        const auto r = job.run_all();
         for (size_t i = 0; i < nmat; ++i) fill_result(r[i], values ? values[i] : nullptr, res ? res + i : nullptr, nullptr, 0);
     });
 }

@@ -265,6 +265,7 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
 }
 
 CloudPlan::~CloudPlan() {
+    if (pexec_) cudaGraphExecDestroy(pexec_);
     if (exec_) cudaGraphExecDestroy(exec_);
     if (graph_) cudaGraphDestroy(graph_);
 }
@@ -399,6 +400,61 @@ void CloudPlan::capture() {
     }
     cuda_check(cudaStreamEndCapture(st, &graph_), "end capture");
     cuda_check(cudaGraphInstantiate(&exec_, graph_, 0), "graph instantiate");
+}
+
+}  // namespace cssc
+
+namespace cssc {
+
+void CloudPlan::capture_pipeline(const unsigned char* img, const CsscLayout& lay, unsigned char* out) {
+    if (n_ == 0) throw std::invalid_argument("pipeline: empty plan");
+    if (lay.items != 2 * n_) throw std::invalid_argument("pipeline: image does not match the plan's chunks");
+    if (pexec_) {
+        cudaGraphExecDestroy(pexec_);
+        pexec_ = nullptr;
+    }
+    const RnsParams& P = ctx_.params();
+    const size_t n = (size_t)P.n, L = (size_t)P.cfg.L;
+    DevicePool* pool = &ctx_.pool();
+    pup_.ensure(pool, std::max<size_t>(lay.bytes, 256));
+    pU_.ensure(pool, sizeof(u64) * (size_t)lay.items * L * n);
+    pCM_.ensure(pool, sizeof(u64) * (size_t)lay.items * ctx_.cm_stride());
+    pX_.ensure(pool, sizeof(u64) * (size_t)ns_ * L * n);
+    pM_.ensure(pool, sizeof(u64) * (size_t)ns_ * n);
+    pslots_.ensure(pool, sizeof(u64) * (size_t)ns_ * (n / 2) + 8 * (size_t)ns_ + 64);
+    ClientWs ws;
+    ws.up = pup_.as<unsigned char>();
+    ws.U = pU_.words();
+    ws.CM = pCM_.words();
+    ws.X = pX_.words();
+    ws.M = pM_.words();
+    ws.slots = pslots_.words();
+    auto* maxdev = reinterpret_cast<unsigned long long*>(ws.slots + (size_t)ns_ * (n / 2));
+    cudaStream_t st = ctx_.stream();
+    cudaGraph_t g = nullptr;
+    cuda_check(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "begin capture");
+    try {
+        ctx_.encrypt_cssc_image(img, lay, &ws);
+        record();
+        ctx_.decrypt_dev(OUT_, ns_, ws.X, ws.M, ws.slots, maxdev);
+        cuda_check(cudaMemcpyAsync(out, ws.slots, sizeof(u64) * (size_t)ns_ * (n / 2) + 8 * (size_t)ns_,
+                                   cudaMemcpyDeviceToHost, st),
+                   "download");
+    } catch (...) {
+        cudaGraph_t tmp = nullptr;
+        cudaStreamEndCapture(st, &tmp);
+        if (tmp) cudaGraphDestroy(tmp);
+        throw;
+    }
+    cuda_check(cudaStreamEndCapture(st, &g), "end capture");
+    const cudaError_t e = cudaGraphInstantiate(&pexec_, g, 0);
+    cudaGraphDestroy(g);
+    cuda_check(e, "graph instantiate");
+}
+
+void CloudPlan::run_pipeline() {
+    if (!pexec_) throw std::logic_error("pipeline not captured");
+    cuda_check(cudaGraphLaunch(pexec_, ctx_.stream()), "graph launch");
 }
 
 }  // namespace cssc

@@ -50,6 +50,14 @@ public:
     // one graph replay with event nodes between launch groups (multiply+relin,
     // each rotate level, the level-0 add, the mask accumulation)
     std::vector<PhaseTiming> profile();
+    // The whole evaluation as one graph: upload of the client image `img`
+    // (pinned, fixed address), device pack + encryption into the plan's input
+    // ciphertexts, the cloud plan, decryption of the results and the download
+    // of slots + noise deviations into `out` (pinned).  Plan-owned workspaces.
+    void capture_pipeline(const unsigned char* img, const CsscLayout& lay, unsigned char* out);
+    void run_pipeline();  // enqueue (no sync)
+    bool has_pipeline() const { return pexec_ != nullptr; }
+    int results() const { return ns_; }
     const PlanStats& stats() const { return stats_; }
 
 private:
@@ -92,6 +100,8 @@ private:
     int n_masks_ = 0;
     cudaGraph_t graph_ = nullptr;
     cudaGraphExec_t exec_ = nullptr;
+    DevBuf pup_, pU_, pCM_, pX_, pM_, pslots_;  // pipeline workspaces
+    cudaGraphExec_t pexec_ = nullptr;
 };
 
 }  // namespace cssc

@@ -42,6 +42,8 @@ public:
     void encrypt();               // Client A + Client B: pack + encrypt on the device
     void cloud(bool use_graph);   // enqueue the cloud plan (no host sync)
     std::vector<SpmvResult> finish();  // key holder: decrypt, unpermute, bookkeeping
+    // encrypt + cloud + finish; from a plan's second use on, one graph launch
+    std::vector<SpmvResult> run_all();
     // this rank's per-slice result ciphertext words (zeros for slices it holds
     // no chunk of), [results][ct words]; and the decryption of summed words
     std::vector<std::uint64_t> result_words();
@@ -67,6 +69,7 @@ private:
                    std::int64_t nz_base, std::int64_t vec_base);
     void ensure_plan();
     std::vector<SpmvResult> decrypt_and_report(const std::vector<spmvgpu_ct>& outs);
+    std::vector<SpmvResult> report(const std::vector<std::uint64_t>& slots, const std::vector<std::int32_t>& measured);
 
     spmvgpu_ctx* ctx_;
     HeParams hp_;
@@ -77,6 +80,7 @@ private:
     // device pack descriptors (spmvgpu_encrypt_cssc layout), then the pinned upload image
     std::vector<std::int32_t> rowrec_, slicerec_, colrec_;
     ClientImage img_;
+    bool img_borrowed_ = false;  // img_.p is the cached pipeline's pinned buffer
     bool encrypted_ = false;
     std::vector<std::uint64_t> r_, c_;
     std::vector<std::uint32_t> slice_id_;

@@ -22,6 +22,13 @@ struct PlanLease {
     spmvgpu_plan* plan = nullptr;
     bool captured = false;
     std::uint64_t uses = 0;
+    // whole-evaluation pipeline (CloudPlan::capture_pipeline): pinned image and
+    // result buffers at fixed addresses, and the image layout it was captured for
+    unsigned char* pimg = nullptr;
+    std::size_t pimg_cap = 0;
+    unsigned char* pout = nullptr;
+    std::size_t pout_cap = 0;
+    std::vector<std::size_t> pkey;
 };
 
 // Moves a cached lease for `key` into `out` and returns true, or returns false.
@@ -41,10 +48,21 @@ struct ClientImage {
     std::size_t nnz = 0, vec_len = 0, n_rows = 0, n_slices = 0, n_cols = 0;
     int items = 0;
 };
+ClientImage client_image_layout(std::size_t nnz, std::size_t vec_len, std::size_t n_rows, std::size_t n_slices,
+                                std::size_t n_cols, int items);  // offsets only, p = nullptr
 ClientImage client_image_take(spmvgpu_ctx* ctx, std::size_t nnz, std::size_t vec_len, std::size_t n_rows,
                               std::size_t n_slices, std::size_t n_cols, int items);
 void client_image_give(spmvgpu_ctx* ctx, ClientImage& img);
 // fills the stream ids and output handles, uploads, packs and encrypts
 void client_image_encrypt(spmvgpu_ctx* ctx, ClientImage& img, const spmvgpu_ct* out);
+// writes fresh stream ids and the output handles into an image at `p` laid out as `img`
+void client_image_fill(spmvgpu_ctx* ctx, unsigned char* p, const ClientImage& img, const spmvgpu_ct* out);
+// the image layout a pipeline depends on
+std::vector<std::size_t> client_image_key(const ClientImage& img);
+// (re)captures the lease's whole-evaluation graph for images laid out as `img`
+// (allocates the lease's pinned image/result buffers); then runs it and waits
+void pipeline_prepare(spmvgpu_ctx* ctx, PlanLease& lease, const ClientImage& img);
+void pipeline_run(spmvgpu_ctx* ctx, PlanLease& lease);
+bool pipeline_ready(const PlanLease& lease, const ClientImage& img);
 
 }  // namespace spmv::detail

@@ -107,9 +107,7 @@ SpmvResult spmv(const HeBackend& be, const CsrMatrix& m, std::span<const std::in
         const detail::CsrView w = detail::view_of(m, v);
         detail::BatchedSpmv job(gpu->context(), gpu->params(), std::span<const detail::CsrView>(&w, 1), chunk_size,
                                 key_holder, /*partition=*/false);
-        job.encrypt();
-        job.cloud(false);
-        return std::move(job.finish()[0]);
+        return std::move(job.run_all()[0]);
     }
     return spmv_generic(be, m, v, chunk_size, key_holder);
 }
@@ -122,9 +120,7 @@ std::vector<SpmvResult> spmv_batch(const HeBackend& be, std::span<const CsrMatri
         std::vector<detail::CsrView> w;
         for (std::size_t i = 0; i < ms.size(); ++i) w.push_back(detail::view_of(ms[i], vs[i]));
         detail::BatchedSpmv job(gpu->context(), gpu->params(), w, chunk_size, key_holder);
-        job.encrypt();
-        job.cloud(false);
-        return job.finish();
+        return job.run_all();
     }
     std::vector<SpmvResult> out;
     for (std::size_t i = 0; i < ms.size(); ++i) out.push_back(spmv_partitioned(be, ms[i], vs[i], chunk_size, key_holder));
@@ -138,9 +134,7 @@ SpmvResult spmv_partitioned(const HeBackend& be, const CsrMatrix& m, std::span<c
         const detail::CsrView w = detail::view_of(m, v);
         detail::BatchedSpmv job(gpu->context(), gpu->params(), std::span<const detail::CsrView>(&w, 1), chunk_size,
                                 key_holder);
-        job.encrypt();
-        job.cloud(false);
-        return std::move(job.finish()[0]);
+        return std::move(job.run_all()[0]);
     }
     SpmvResult merged;
     merged.message_ledger.key_holder = key_holder;
