@@ -115,50 +115,66 @@ __device__ __forceinline__ u64* job_dst(const NttJob& job, int item, int j, int 
     return job.dst_items ? job.dst_items[item] + (size_t)j * n : job.dst + ((size_t)item * job.limbs + j) * n;
 }
 
-// Column phase: 16 strided columns of R1 elements.  Forward: first phase
-// (src -> dst).  Inverse: last phase (dst -> dst), applies N^-1, canonical.
-template <int LOGN, bool INV>
+// Column phase: LN strided columns of R1 elements per CTA (LN = 16, or 8 for
+// launches too small to fill the GPU: twice the CTAs, half the serial work
+// each).  Forward: first phase (src -> dst).  Inverse: last phase (dst ->
+// dst), applies N^-1, canonical.
+template <int LOGN, bool INV, int LN = 16>
 __global__ void __launch_bounds__(Ntt2<LOGN>::TC, 256 / Ntt2<LOGN>::TC * 3) k_ntt_cols(const DevConsts* __restrict__ dc, NttJob job) {
     using G = Ntt2<LOGN>;
     constexpr int T = G::TC;
+    constexpr int CTAS = G::R2 / LN;     // column tiles per limb
+    constexpr int SEG = LN / 2;          // 16-byte copies per row
     extern __shared__ u64 smem[];
-    u64* tile = smem;                       // [R1][16]
-    u64* tws = smem + G::LINES * G::R1;     // [R1] pairs
-    const int tileid = blockIdx.x % G::CTAS_C;
-    const int lj = blockIdx.x / G::CTAS_C;
+    u64* tile = smem;                    // [R1][LN]
+    u64* tws = smem + LN * G::R1;        // [R1] pairs
+    const int tileid = blockIdx.x % CTAS;
+    const int lj = blockIdx.x / CTAS;
     const int item = lj / job.limbs, j = lj - item * job.limbs;
     const int prime = job.pidx[j];
     const u64 q = dc->mod[prime].q;
     const u64* tw = INV ? dc->tw[prime].inv : dc->tw[prime].fwd;
     const u64* src = INV ? job_dst(job, item, j, G::N) : job_src(job, item, j, G::N);
     u64* dst = job_dst(job, item, j, G::N);
-    const int col0 = tileid * G::LINES;
-    // twiddles W[0 .. R1) and the tile (rows of 16 consecutive words, 8 threads
-    // x 16 B per row) via async copies: every load of the CTA in flight at once
+    const int col0 = tileid * LN;
+    // twiddles W[0 .. R1) and the tile (rows of LN consecutive words, SEG
+    // threads x 16 B per row) via async copies: every load in flight at once
     for (int i = threadIdx.x; i < G::R1; i += T) cp_async16(tws + 2 * i, tw + 2 * i);
 #pragma unroll
-    for (int r = 0; r < G::R1 * 8 / T; ++r) {
-        const int i = threadIdx.x + T * r, c = i >> 3, h = i & 7;
-        cp_async16(tile + c * 16 + 2 * h, src + (size_t)c * G::R2 + col0 + 2 * h);
+    for (int r = 0; r < G::R1 * SEG / T; ++r) {
+        const int i = threadIdx.x + T * r, c = i / SEG, h = i % SEG;
+        cp_async16(tile + c * LN + 2 * h, src + (size_t)c * G::R2 + col0 + 2 * h);
     }
     cp_async_wait_all();
     __syncthreads();
-    auto addr = [](int l, int pos) { return pos * 16 + l; };
+    auto addr = [](int l, int pos) { return pos * LN + l; };
     auto twf = [&](int sl, int, int blk) {
         const int k = (1 << sl) + blk;
         return make_ulonglong2(tws[2 * k], tws[2 * k + 1]);
     };
-    line_ntt<G::A, 0, INV, 3>(tile, q, addr, twf);  // radix-8 passes: 3 CTAs per SM
+    line_ntt_v<G::A, 0, INV, 3, LN>(tile, ConstQ{q}, addr, twf, whole_cta());  // radix-8 passes: 3 CTAs per SM
     const u64 ni = dc->ninv[prime], nish = dc->ninv_sh[prime];
 #pragma unroll
-    for (int r = 0; r < G::R1 * 8 / T; ++r) {
-        const int i = threadIdx.x + T * r, c = i >> 3, h = i & 7;
-        u64 a0 = tile[c * 16 + 2 * h], a1 = tile[c * 16 + 2 * h + 1];
+    for (int r = 0; r < G::R1 * SEG / T; ++r) {
+        const int i = threadIdx.x + T * r, c = i / SEG, h = i % SEG;
+        u64 a0 = tile[c * LN + 2 * h], a1 = tile[c * LN + 2 * h + 1];
         if (INV) {
             a0 = shoup(a0, ni, nish, q);
             a1 = shoup(a1, ni, nish, q);
         }
         *reinterpret_cast<ulonglong2*>(dst + (size_t)c * G::R2 + col0 + 2 * h) = make_ulonglong2(a0, a1);
+    }
+}
+
+// 8-column tiles when 16-column tiles would leave SMs idle
+template <int LOGN, bool INV>
+static void launch_cols(const DevConsts* dc, const NttJob& job, int limbs, cudaStream_t st) {
+    using G = Ntt2<LOGN>;
+    if (limbs * G::CTAS_C < 2 * 148 && G::R2 >= 16 && G::R1 * 4 >= G::TC) {
+        constexpr int LN = 8;
+        k_ntt_cols<LOGN, INV, LN><<<limbs * (G::R2 / LN), G::TC, (LN * G::R1 + 2 * G::R1) * 8, st>>>(dc, job);
+    } else {
+        k_ntt_cols<LOGN, INV><<<limbs * G::CTAS_C, G::TC, G::SMEM_C, st>>>(dc, job);
     }
 }
 
@@ -266,13 +282,13 @@ static void launch_ntt_t(const DevConsts* dc, bool inv, const NttJob& job, int i
     const int limbs = items * job.limbs;
     if (limbs == 0) return;
     if (!inv) {
-        k_ntt_cols<LOGN, false><<<limbs * G::CTAS_C, G::TC, G::SMEM_C, st>>>(dc, job);
+        launch_cols<LOGN, false>(dc, job, limbs, st);
         CSSC_CHECK_LAUNCH();
         launch_blocks<LOGN, false>(dc, job, items, st);
     } else {
         launch_blocks<LOGN, true>(dc, job, items, st);
         CSSC_CHECK_LAUNCH();
-        k_ntt_cols<LOGN, true><<<limbs * G::CTAS_C, G::TC, G::SMEM_C, st>>>(dc, job);
+        launch_cols<LOGN, true>(dc, job, limbs, st);
     }
     CSSC_CHECK_LAUNCH();
 }
@@ -285,9 +301,9 @@ static void launch_phase_t(const DevConsts* dc, bool inv, bool cols, const NttJo
     if (limbs == 0) return;
     if (cols) {
         if (inv)
-            k_ntt_cols<LOGN, true><<<limbs * G::CTAS_C, G::TC, G::SMEM_C, st>>>(dc, job);
+            launch_cols<LOGN, true>(dc, job, limbs, st);
         else
-            k_ntt_cols<LOGN, false><<<limbs * G::CTAS_C, G::TC, G::SMEM_C, st>>>(dc, job);
+            launch_cols<LOGN, false>(dc, job, limbs, st);
     } else {
         if (inv)
             launch_blocks<LOGN, true>(dc, job, items, st);

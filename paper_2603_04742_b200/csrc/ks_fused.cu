@@ -52,18 +52,20 @@ __device__ __forceinline__ void load_col_twiddles(u64* tws, const u64* tw) {
 // ---------------------------------------------------------------------------
 // K1: ModUp + NTT column phase
 // ---------------------------------------------------------------------------
-template <int LOGN, int LT, int KT, int AT>
+// LN columns per CTA: 16, or 8 when the launch would not fill the GPU
+template <int LOGN, int LT, int KT, int AT, int LN = 16>
 __global__ void __launch_bounds__(Ntt2<LOGN>::TC, 256 / Ntt2<LOGN>::TC * 3) k_ks_modup_cols(const DevConsts* __restrict__ dc, const u64* const* SRC,
                                                        const u64* SRCC, int src_poly, const u32* ginv, u64* DX) {
     using G = Ntt2<LOGN>;
+    constexpr int CTAS = G::R2 / LN;
     extern __shared__ u64 smem[];
     u64* tile = smem;
-    u64* tws = smem + G::LINES * G::R1;
+    u64* tws = smem + LN * G::R1;
     const int L = LT ? LT : dc->L, K = KT ? KT : dc->K, LK = L + K;
     const int alpha = AT ? AT : dc->alpha, dnum = (L + alpha - 1) / alpha;
     int bid = blockIdx.x;
-    const int tileid = bid % G::CTAS_C;
-    bid /= G::CTAS_C;
+    const int tileid = bid % CTAS;
+    bid /= CTAS;
     const int j = bid % LK;
     bid /= LK;
     const int dg = bid % dnum;
@@ -73,12 +75,12 @@ __global__ void __launch_bounds__(Ntt2<LOGN>::TC, 256 / Ntt2<LOGN>::TC * 3) k_ks
     const u32 gi = ginv ? ginv[item] : 0u;
     const u64 m = dc->mod[j].q;
     const bool own = j >= lo && j < hi;
-    const int col0 = tileid * G::LINES;
+    const int col0 = tileid * LN;
     load_col_twiddles<LOGN>(tws, dc->tw[j].fwd);
-    constexpr int PER = G::R1 * 16 / G::TC;  // elements per thread
+    constexpr int PER = G::R1 * LN / G::TC;  // elements per thread
 #pragma unroll 8
     for (int r = 0; r < PER; ++r) {
-        const int e = threadIdx.x + G::TC * r, c = e >> 4, jl = e & 15;
+        const int e = threadIdx.x + G::TC * r, c = e / LN, jl = e % LN;
         bool neg;
         const int idx = ks_automorph(gi, col0 + jl + G::R2 * c, G::N, neg);
         u64 v;
@@ -98,21 +100,22 @@ __global__ void __launch_bounds__(Ntt2<LOGN>::TC, 256 / Ntt2<LOGN>::TC * 3) k_ks
             }
             v = reduce_small_quot(v, dc->mod[j]);
         }
-        tile[c * 16 + jl] = v;
+        tile[c * LN + jl] = v;
     }
     __syncthreads();
-    auto addr = [](int l, int pos) { return pos * 16 + l; };
+    auto addr = [](int l, int pos) { return pos * LN + l; };
     auto twf = [&](int sl, int, int blk) {
         const int k = (1 << sl) + blk;
         return make_ulonglong2(tws[2 * k], tws[2 * k + 1]);
     };
-    line_ntt<G::A, 0, false, 3>(tile, m, addr, twf);  // radix-8 passes: 3 CTAs per SM
+    line_ntt_v<G::A, 0, false, 3, LN>(tile, ConstQ{m}, addr, twf, whole_cta());  // radix-8: 3 CTAs per SM
     u64* dst = DX + (((size_t)item * dnum + dg) * LK + j) * G::N;
+    constexpr int SEG = LN / 2;
 #pragma unroll
-    for (int r = 0; r < G::R1 * 8 / G::TC; ++r) {
-        const int i = threadIdx.x + G::TC * r, c = i >> 3, h = i & 7;
+    for (int r = 0; r < G::R1 * SEG / G::TC; ++r) {
+        const int i = threadIdx.x + G::TC * r, c = i / SEG, h = i % SEG;
         *reinterpret_cast<ulonglong2*>(dst + (size_t)c * G::R2 + col0 + 2 * h) =
-            make_ulonglong2(tile[c * 16 + 2 * h], tile[c * 16 + 2 * h + 1]);
+            make_ulonglong2(tile[c * LN + 2 * h], tile[c * LN + 2 * h + 1]);
     }
 }
 
@@ -238,8 +241,14 @@ static void ks_fused_t(const DevConsts* dc, const RnsParams& P, const u64* const
         cudaFuncSetAttribute(k_ks_blocks_inner<LOGN, LT, KT, AT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
         configured = smem2;
     }
-    k_ks_modup_cols<LOGN, LT, KT, AT><<<items * dnum * LK * G::CTAS_C, G::TC, smem1, st>>>(dc, SRC, SRCC, src_poly,
-                                                                                      ginv, DX);
+    if (items * dnum * LK * G::CTAS_C < 2 * 148 && G::R1 * 4 >= G::TC) {  // small launch: 8-column tiles
+        constexpr int LN = 8;
+        k_ks_modup_cols<LOGN, LT, KT, AT, LN><<<items * dnum * LK * (G::R2 / LN), G::TC,
+                                                (LN * G::R1 + 2 * G::R1) * 8, st>>>(dc, SRC, SRCC, src_poly, ginv, DX);
+    } else {
+        k_ks_modup_cols<LOGN, LT, KT, AT><<<items * dnum * LK * G::CTAS_C, G::TC, smem1, st>>>(dc, SRC, SRCC,
+                                                                                          src_poly, ginv, DX);
+    }
     KS_CHECK();
     k_ks_blocks_inner<LOGN, LT, KT, AT><<<items * LK * G::CTAS_B, kKsGroups * kKsGroupThreads, smem2, st>>>(dc, DX, KEY, ACC);
     KS_CHECK();
