@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(Ntt2<LOGN>::TC, 256 / Ntt2<LOGN>::TC * 3) k_ks
 // concurrently, so a CTA's serial chain is ceil(dnum/2) + 1 tile transforms.
 constexpr int kKsGroups = 2, kKsGroupThreads = 128;
 
-template <int LOGN, int LT, int KT, int AT>
+template <int LOGN, int LT, int KT, int AT, int LN = 16>
 __global__ void __launch_bounds__(kKsGroups * kKsGroupThreads) k_ks_blocks_inner(const DevConsts* __restrict__ dc,
                                                                                const u64* __restrict__ DX,
                                                                                const u64* const* KEY,
@@ -135,21 +135,23 @@ __global__ void __launch_bounds__(kKsGroups * kKsGroupThreads) k_ks_blocks_inner
     using G = Ntt2<LOGN>;
     extern __shared__ u64 smem[];
     constexpr int PITCH = G::PITCH;
-    constexpr int TW = G::LINES * PITCH;
+    constexpr int TW = LN * PITCH;
     constexpr int T = kKsGroups * kKsGroupThreads;
-    constexpr int PER = G::LINES * G::R2 / T;  // elements per thread
+    constexpr int PER = LN * G::R2 / T;  // elements per thread
+    constexpr int CTAS = G::R1 / LN;
+    static_assert(PER >= 1, "tile smaller than the CTA");
     const int L = LT ? LT : dc->L, K = KT ? KT : dc->K, LK = L + K;
     const int alpha = AT ? AT : dc->alpha, dnum = (L + alpha - 1) / alpha;
     u64* work = smem;               // dnum digit tiles; then acc0 in tile 0, acc1 in tile 1
     u64* tws = smem + (dnum < 2 ? 2 : dnum) * TW;
     int bid = blockIdx.x;
-    const int tileid = bid % G::CTAS_B;
-    bid /= G::CTAS_B;
+    const int tileid = bid % CTAS;
+    bid /= CTAS;
     const int j = bid % LK;
     const int item = bid / LK;
     const Modulus md = dc->mod[j];
     const u64 q = md.q;
-    const int blk0 = tileid * G::LINES;
+    const int blk0 = tileid * LN;
     const size_t base = (size_t)blk0 * G::R2;
     const u64* key = KEY[item];
     const size_t PL = (size_t)LK * G::N;
@@ -159,8 +161,8 @@ __global__ void __launch_bounds__(kKsGroups * kKsGroupThreads) k_ks_blocks_inner
     // consecutive lanes touch consecutive words in HBM and in smem (conflict free)
     auto saddr = [](int x) { return (x >> G::B) * PITCH + (x & (G::R2 - 1)); };
     auto addr = [](int l, int pos) { return l * PITCH + pos; };
-    auto twf = [&](int sl, int l, int blk) { return block_tw<LOGN>(tws, sl, l, blk); };
-    load_block_twiddles<LOGN>(tws, dc->tw[j].fwd, blk0);
+    auto twf = [&](int sl, int l, int blk) { return block_tw<LOGN, LN>(tws, sl, l, blk); };
+    load_block_twiddles<LOGN, LN>(tws, dc->tw[j].fwd, blk0);
     for (int dg = 0; dg < dnum; ++dg) {
         const u64* d = DX + (((size_t)item * dnum + dg) * LK + j) * G::N + base;
 #pragma unroll
@@ -172,7 +174,8 @@ __global__ void __launch_bounds__(kKsGroups * kKsGroupThreads) k_ks_blocks_inner
     cp_async_wait_all();
     __syncthreads();
 #pragma unroll 1
-    for (int dg = grp; dg < dnum; dg += kKsGroups) line_ntt<G::B, 0, false>(work + dg * TW, q, addr, twf, tg);
+    for (int dg = grp; dg < dnum; dg += kKsGroups)
+        line_ntt_v<G::B, 0, false, 4, LN>(work + dg * TW, ConstQ{q}, addr, twf, tg);
     __syncthreads();
     // inner product with both key polynomials, key tiles streamed coalesced;
     // every position is read (all digits) and then overwritten by one thread
@@ -191,10 +194,10 @@ __global__ void __launch_bounds__(kKsGroups * kKsGroupThreads) k_ks_blocks_inner
         work[TW + s0] = a1;
     }
     __syncthreads();
-    load_block_twiddles<LOGN>(tws, dc->tw[j].inv, blk0);
+    load_block_twiddles<LOGN, LN>(tws, dc->tw[j].inv, blk0);
     cp_async_wait_all();
     __syncthreads();
-    line_ntt<G::B, 0, true>(work + grp * TW, q, addr, twf, tg);  // group p: accumulator p
+    line_ntt_v<G::B, 0, true, 4, LN>(work + grp * TW, ConstQ{q}, addr, twf, tg);  // group p: accumulator p
     __syncthreads();
 #pragma unroll
     for (int p = 0; p < 2; ++p) {
@@ -233,12 +236,15 @@ static void ks_fused_t(const DevConsts* dc, const RnsParams& P, const u64* const
     const int L = P.cfg.L, K = P.cfg.K, LK = L + K, dnum = P.dnum;
     const int smem1 = G::SMEM_C;
     const int smem2 = ((dnum < 2 ? 2 : dnum) * G::LINES * G::PITCH + 2 * G::TWB) * 8;
+    const int smem2h = ((dnum < 2 ? 2 : dnum) * 8 * G::PITCH + 2 * btw_entries<LOGN, 8>()) * 8;
     if (smem2 > 200 * 1024)
         throw std::invalid_argument("key switch: too many digits for the fused kernel; set fused_key_switch 0");
     static int configured = 0;  // largest K2 smem set so far (the generic shape's dnum varies)
     if (smem2 > configured) {
         cudaFuncSetAttribute(k_ks_modup_cols<LOGN, LT, KT, AT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem1);
         cudaFuncSetAttribute(k_ks_blocks_inner<LOGN, LT, KT, AT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
+        cudaFuncSetAttribute(k_ks_blocks_inner<LOGN, LT, KT, AT, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             smem2h);
         configured = smem2;
     }
     if (items * dnum * LK * G::CTAS_C < 2 * 148 && G::R1 * 4 >= G::TC) {  // small launch: 8-column tiles
@@ -250,7 +256,11 @@ static void ks_fused_t(const DevConsts* dc, const RnsParams& P, const u64* const
                                                                                           src_poly, ginv, DX);
     }
     KS_CHECK();
-    k_ks_blocks_inner<LOGN, LT, KT, AT><<<items * LK * G::CTAS_B, kKsGroups * kKsGroupThreads, smem2, st>>>(dc, DX, KEY, ACC);
+    constexpr int T2 = kKsGroups * kKsGroupThreads;
+    if (items * LK * G::CTAS_B < 2 * 148 && 8 * G::R2 >= T2)  // small launch: 8-block tiles
+        k_ks_blocks_inner<LOGN, LT, KT, AT, 8><<<items * LK * (G::R1 / 8), T2, smem2h, st>>>(dc, DX, KEY, ACC);
+    else
+        k_ks_blocks_inner<LOGN, LT, KT, AT><<<items * LK * G::CTAS_B, T2, smem2, st>>>(dc, DX, KEY, ACC);
     KS_CHECK();
     NttJob j;
     for (int i = 0; i < MAX_JOB_LIMBS; ++i) j.pidx[i] = (signed char)(i % LK);

@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(kMulGroups * kGroupThreads) k_mul_blocks_tenso
 // (inter_chunk_sum, aggregate.cpp:55-74); then the INTT block phase of the sum,
 // written to the slice's result ciphertext for the inverse column phase.
 // Replaces the forward block phase, k_mask_accum and the inverse block phase.
-template <int LOGN>
+template <int LOGN, int LN = 16>
 __global__ void __launch_bounds__(2 * kGroupThreads) k_mask_blocks(const DevConsts* __restrict__ dc,
                                                                    const u64* __restrict__ MT,
                                                                    const int* __restrict__ slice_off,
@@ -117,24 +117,26 @@ __global__ void __launch_bounds__(2 * kGroupThreads) k_mask_blocks(const DevCons
     using G = Ntt2<LOGN>;
     extern __shared__ u64 smem[];
     constexpr int PITCH = G::PITCH;
-    constexpr int TW = G::LINES * PITCH;
+    constexpr int TW = LN * PITCH;
     constexpr int NG = 2;  // groups: chunks x = b + g, b + g + 2, ... each into its own partial sum
     constexpr int NT = NG * kGroupThreads;
-    constexpr int PERG = G::LINES * G::R2 / kGroupThreads;  // elements per thread within a group
-    constexpr int PER = G::LINES * G::R2 / NT;
+    constexpr int PERG = LN * G::R2 / kGroupThreads;  // elements per thread within a group
+    constexpr int PER = LN * G::R2 / NT;
+    constexpr int CTAS = G::R1 / LN;
+    static_assert(PER >= 1, "tile smaller than the CTA");
     u64* work = smem;             // NG work tiles
     u64* acc = smem + NG * TW;    // NG partial sums
     u64* tws = smem + 2 * NG * TW;
     const int L = dc->L;
     int bid = blockIdx.x;
-    const int tileid = bid % G::CTAS_B;
-    bid /= G::CTAS_B;
+    const int tileid = bid % CTAS;
+    bid /= CTAS;
     const int j2 = bid % (2 * L);
     const int sl = bid / (2 * L);
     const int j = j2 % L;
     const Modulus md = dc->mod[j];
     const u64 q = md.q;
-    const int blk0 = tileid * G::LINES;
+    const int blk0 = tileid * LN;
     const size_t base = (size_t)blk0 * G::R2;
     const int grp = threadIdx.x / kGroupThreads;
     const ThreadGroup tg = cta_slice(grp, NG);
@@ -142,8 +144,8 @@ __global__ void __launch_bounds__(2 * kGroupThreads) k_mask_blocks(const DevCons
     u64* ac = acc + grp * TW;
     auto saddr = [](int x) { return (x >> G::B) * PITCH + (x & (G::R2 - 1)); };
     auto addr = [](int l, int pos) { return l * PITCH + pos; };
-    auto twf = [&](int sl_, int l, int blk) { return block_tw<LOGN>(tws, sl_, l, blk); };
-    load_block_twiddles<LOGN>(tws, dc->tw[j].fwd, blk0);
+    auto twf = [&](int sl_, int l, int blk) { return block_tw<LOGN, LN>(tws, sl_, l, blk); };
+    load_block_twiddles<LOGN, LN>(tws, dc->tw[j].fwd, blk0);
     cp_async_wait_all();
     __syncthreads();
     const int b = slice_off[sl], e = slice_off[sl + 1];
@@ -159,7 +161,7 @@ __global__ void __launch_bounds__(2 * kGroupThreads) k_mask_blocks(const DevCons
         }
         cp_async_wait_all();
         tg.sync();
-        line_ntt<G::B, 0, false>(wk, q, addr, twf, tg);
+        line_ntt_v<G::B, 0, false, 4, LN>(wk, ConstQ{q}, addr, twf, tg);
         const u64* mk = MASKS + ((size_t)item_mask[it] * L + j) * G::N + base;
 #pragma unroll
         for (int r = 0; r < PERG; ++r) {
@@ -180,10 +182,10 @@ __global__ void __launch_bounds__(2 * kGroupThreads) k_mask_blocks(const DevCons
         acc[s0] = add_mod(acc[s0], acc[TW + s0], q);
     }
     __syncthreads();
-    load_block_twiddles<LOGN>(tws, dc->tw[j].inv, blk0);
+    load_block_twiddles<LOGN, LN>(tws, dc->tw[j].inv, blk0);
     cp_async_wait_all();
     __syncthreads();
-    line_ntt<G::B, 0, true>(acc, q, addr, twf);
+    line_ntt_v<G::B, 0, true, 4, LN>(acc, ConstQ{q}, addr, twf, whole_cta());
     u64* dst = OUT[sl] + (size_t)j2 * G::N + base;
 #pragma unroll
     for (int r = 0; r < PER; ++r) {
@@ -198,13 +200,19 @@ static void maskb_t(const DevConsts* dc, const RnsParams& P, const u64* MT, cons
                     cudaStream_t st) {
     using G = Ntt2<LOGN>;
     const int smem = (4 * G::LINES * G::PITCH + 2 * G::TWB) * 8;
+    const int smemh = (4 * 8 * G::PITCH + 2 * btw_entries<LOGN, 8>()) * 8;
     static bool configured = false;
     if (!configured) {
         cudaFuncSetAttribute(k_mask_blocks<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(k_mask_blocks<LOGN, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smemh);
         configured = true;
     }
-    k_mask_blocks<LOGN><<<slices * 2 * P.cfg.L * G::CTAS_B, 2 * kGroupThreads, smem, st>>>(
-        dc, MT, slice_off, slice_items, item_mask, MASKS, OUT);
+    if (slices * 2 * P.cfg.L * G::CTAS_B < 2 * 148 && 8 * G::R2 >= 2 * kGroupThreads)  // small: 8-block tiles
+        k_mask_blocks<LOGN, 8><<<slices * 2 * P.cfg.L * (G::R1 / 8), 2 * kGroupThreads, smemh, st>>>(
+            dc, MT, slice_off, slice_items, item_mask, MASKS, OUT);
+    else
+        k_mask_blocks<LOGN><<<slices * 2 * P.cfg.L * G::CTAS_B, 2 * kGroupThreads, smem, st>>>(
+            dc, MT, slice_off, slice_items, item_mask, MASKS, OUT);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) throw std::runtime_error(std::string("mask blocks launch: ") + cudaGetErrorString(e));
 }

@@ -58,28 +58,35 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
-// Stage the block-phase twiddles of blocks [blk0, blk0 + 16) into smem:
+// Block-phase twiddle layout for tiles of LN blocks: stage s holds LN lines x
+// 2^s entries with an odd line stride (conflict-free LDS.128).
+template <int LN>
+__host__ __device__ constexpr int btw_off(int s) { return s == 0 ? 0 : LN * ((1 << s) + s - 2); }
+template <int LOGN, int LN>
+constexpr int btw_entries() { return LN * ((1 << Ntt2<LOGN>::B) + Ntt2<LOGN>::B - 2); }
+
+// Stage the block-phase twiddles of blocks [blk0, blk0 + LN) into smem:
 // stage s needs W[2^(A+s) + (blk0 + l) * 2^s + blk], contiguous over (l, blk).
-template <int LOGN>
+template <int LOGN, int LN = 16>
 __device__ __forceinline__ void load_block_twiddles(u64* tws, const u64* table, int blk0) {
     using G = Ntt2<LOGN>;
     const ulonglong2* t2 = reinterpret_cast<const ulonglong2*>(table);
 #pragma unroll
     for (int s = 0; s < G::B; ++s) {
-        const int cnt = G::LINES << s;
+        const int cnt = LN << s;
         const int gbase = (1 << (G::A + s)) + (blk0 << s);
         for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
             const int l = i >> s, blk = i & ((1 << s) - 1);
-            const int e = G::tw_off(s) + l * G::tw_stride(s) + blk;
+            const int e = btw_off<LN>(s) + l * G::tw_stride(s) + blk;
             cp_async16(tws + 2 * e, t2 + gbase + i);
         }
     }
 }
 
-template <int LOGN>
+template <int LOGN, int LN = 16>
 __device__ __forceinline__ ulonglong2 block_tw(const u64* tws, int s, int l, int blk) {
     using G = Ntt2<LOGN>;
-    return *reinterpret_cast<const ulonglong2*>(tws + 2 * (G::tw_off(s) + l * G::tw_stride(s) + blk));
+    return *reinterpret_cast<const ulonglong2*>(tws + 2 * (btw_off<LN>(s) + l * G::tw_stride(s) + blk));
 }
 
 // A set of threads working on one tile: the whole CTA (__syncthreads) or a
