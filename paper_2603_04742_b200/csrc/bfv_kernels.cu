@@ -170,7 +170,8 @@ __global__ void __launch_bounds__(Ntt2<LOGN>::TC, 256 / Ntt2<LOGN>::TC * 3) k_nt
 template <int LOGN, bool INV>
 static void launch_cols(const DevConsts* dc, const NttJob& job, int limbs, cudaStream_t st) {
     using G = Ntt2<LOGN>;
-    if (limbs * G::CTAS_C < 2 * 148 && G::R2 >= 16 && G::R1 * 4 >= G::TC) {
+    // 8-column tiles when twice the CTAs still fit one wave (3 CTAs per SM)
+    if (2 * limbs * G::CTAS_C <= 3 * 148 && G::R2 >= 16 && G::R1 * 4 >= G::TC) {
         constexpr int LN = 8;
         k_ntt_cols<LOGN, INV, LN><<<limbs * (G::R2 / LN), G::TC, (LN * G::R1 + 2 * G::R1) * 8, st>>>(dc, job);
     } else {
