@@ -1142,26 +1142,6 @@ void launch_sum_items(const DevConsts* dc, const RnsParams& P, const u64* const*
     CSSC_CHECK_LAUNCH();
 }
 
-__global__ void k_automorph_ct(const DevConsts* __restrict__ dc, const u64* const* A,
-                               const u32* ginv, u64* const* OUT) {
-    const int n = dc->n, L = dc->L;
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    const int item = blockIdx.y;
-    bool neg;
-    const int idx = automorph_src(ginv[item], k, n, neg);
-    for (int p = 0; p < 2; ++p)
-        for (int j = 0; j < L; ++j) {
-            const u64 v = A[item][((size_t)p * L + j) * n + idx];
-            OUT[item][((size_t)p * L + j) * n + k] = neg ? neg_mod(v, dc->mod[j].q) : v;
-        }
-}
-
-void launch_automorph_ct(const DevConsts* dc, const RnsParams& P, const u64* const* A,
-                         const u32* ginv, u64* const* OUT, int items, cudaStream_t st) {
-    if (!items) return;
-    k_automorph_ct<<<ew_grid(P.n, items), EW_THREADS, 0, st>>>(dc, A, ginv, OUT);
-    CSSC_CHECK_LAUNCH();
-}
 
 }  // namespace cssc
 

@@ -132,8 +132,7 @@ void launch_sum_items(const DevConsts* dc, const RnsParams& P, const u64* const*
                       cudaStream_t st);
 void launch_add(const DevConsts* dc, const RnsParams& P, const u64* const* A,
                 const u64* const* B, u64* const* OUT, int items, cudaStream_t st);
-void launch_automorph_ct(const DevConsts* dc, const RnsParams& P, const u64* const* A,
-                         const u32* ginv, u64* const* OUT, int items, cudaStream_t st);
+
 
 }  // namespace cssc
 
