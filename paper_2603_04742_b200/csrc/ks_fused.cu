@@ -126,6 +126,8 @@ __global__ void __launch_bounds__(Ntt2<LOGN>::TC, 256 / Ntt2<LOGN>::TC * 3) k_ks
 // transformed two at a time, and the two accumulators' inverse transforms run
 // concurrently, so a CTA's serial chain is ceil(dnum/2) + 1 tile transforms.
 constexpr int kKsGroups = 2, kKsGroupThreads = 128;
+template <int LOGN>
+constexpr bool ks_keys_tma() { return LOGN <= 14; }
 
 template <int LOGN, int LT, int KT, int AT, int LN = 16>
 __global__ void __launch_bounds__(kKsGroups * kKsGroupThreads) k_ks_blocks_inner(const DevConsts* __restrict__ dc,
@@ -144,6 +146,12 @@ __global__ void __launch_bounds__(kKsGroups * kKsGroupThreads) k_ks_blocks_inner
     const int alpha = AT ? AT : dc->alpha, dnum = (L + alpha - 1) / alpha;
     u64* work = smem;               // dnum digit tiles; then acc0 in tile 0, acc1 in tile 1
     u64* tws = smem + (dnum < 2 ? 2 : dnum) * TW;
+    constexpr int KT_W = LN * G::R2;  // words of one key tile (contiguous in HBM)
+    // key tiles by TMA into smem at 2^14 and below; at 2^15 they would cost the
+    // second CTA per SM, so the MAC reads them straight from HBM there
+    constexpr bool KTMA = ks_keys_tma<LOGN>();
+    u64* keys = tws + 2 * btw_entries<LOGN, LN>();  // [dnum][2][KT_W]
+    auto* bar = reinterpret_cast<unsigned long long*>(keys + (KTMA ? (size_t)dnum * 2 * KT_W : 0));
     int bid = blockIdx.x;
     const int tileid = bid % CTAS;
     bid /= CTAS;
@@ -162,6 +170,16 @@ __global__ void __launch_bounds__(kKsGroups * kKsGroupThreads) k_ks_blocks_inner
     auto saddr = [](int x) { return (x >> G::B) * PITCH + (x & (G::R2 - 1)); };
     auto addr = [](int l, int pos) { return l * PITCH + pos; };
     auto twf = [&](int sl, int l, int blk) { return block_tw<LOGN, LN>(tws, sl, l, blk); };
+    // the key tiles of every digit and both polynomials: TMA bulk copies issued
+    // first, landing while the digits are transformed
+    if (KTMA && threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        mbar_expect_tx(bar, (unsigned)(dnum * 2 * KT_W * 8));
+        for (int dg = 0; dg < dnum; ++dg)
+            for (int p = 0; p < 2; ++p)
+                bulk_g2s(keys + (size_t)(dg * 2 + p) * KT_W, key + ((size_t)dg * 2 + p) * PL + (size_t)j * G::N + base,
+                         KT_W * 8, bar);
+    }
     load_block_twiddles<LOGN, LN>(tws, dc->tw[j].fwd, blk0);
     for (int dg = 0; dg < dnum; ++dg) {
         const u64* d = DX + (((size_t)item * dnum + dg) * LK + j) * G::N + base;
@@ -177,18 +195,26 @@ __global__ void __launch_bounds__(kKsGroups * kKsGroupThreads) k_ks_blocks_inner
     for (int dg = grp; dg < dnum; dg += kKsGroups)
         line_ntt_v<G::B, 0, false, 4, LN>(work + dg * TW, ConstQ{q}, addr, twf, tg);
     __syncthreads();
-    // inner product with both key polynomials, key tiles streamed coalesced;
-    // every position is read (all digits) and then overwritten by one thread
+    // inner product with both key polynomials (tiles in smem once the TMA
+    // transaction completes); every position is read (all digits) and then
+    // overwritten by one thread
+    if (KTMA) mbar_wait(bar, 0);
 #pragma unroll
     for (int r = 0; r < PER; ++r) {
         const int x = threadIdx.x + T * r, s0 = saddr(x);
         u64 a0 = 0, a1 = 0;
         for (int dg = 0; dg < dnum; ++dg) {
             const u64 w = work[dg * TW + s0];
-            const u64* k0 = key + ((size_t)dg * 2 + 0) * PL + (size_t)j * G::N + base;
-            const u64* k1 = key + ((size_t)dg * 2 + 1) * PL + (size_t)j * G::N + base;
-            a0 = add_mod(a0, mul_mod(w, __ldg(k0 + x), md), q);
-            a1 = add_mod(a1, mul_mod(w, __ldg(k1 + x), md), q);
+            u64 k0, k1;
+            if (KTMA) {
+                k0 = keys[(size_t)(dg * 2) * KT_W + x];
+                k1 = keys[(size_t)(dg * 2 + 1) * KT_W + x];
+            } else {
+                k0 = __ldg(key + ((size_t)dg * 2 + 0) * PL + (size_t)j * G::N + base + x);
+                k1 = __ldg(key + ((size_t)dg * 2 + 1) * PL + (size_t)j * G::N + base + x);
+            }
+            a0 = add_mod(a0, mul_mod(w, k0, md), q);
+            a1 = add_mod(a1, mul_mod(w, k1, md), q);
         }
         work[s0] = a0;
         work[TW + s0] = a1;
@@ -235,8 +261,11 @@ static void ks_fused_t(const DevConsts* dc, const RnsParams& P, const u64* const
     using G = Ntt2<LOGN>;
     const int L = P.cfg.L, K = P.cfg.K, LK = L + K, dnum = P.dnum;
     const int smem1 = G::SMEM_C;
-    const int smem2 = ((dnum < 2 ? 2 : dnum) * G::LINES * G::PITCH + 2 * G::TWB) * 8;
-    const int smem2h = ((dnum < 2 ? 2 : dnum) * 8 * G::PITCH + 2 * btw_entries<LOGN, 8>()) * 8;
+    constexpr int KTM = ks_keys_tma<LOGN>() ? 1 : 0;
+    const int smem2 =
+        ((dnum < 2 ? 2 : dnum) * G::LINES * G::PITCH + 2 * G::TWB + KTM * dnum * 2 * G::LINES * G::R2) * 8 + 16;
+    const int smem2h =
+        ((dnum < 2 ? 2 : dnum) * 8 * G::PITCH + 2 * btw_entries<LOGN, 8>() + KTM * dnum * 2 * 8 * G::R2) * 8 + 16;
     if (smem2 > 200 * 1024)
         throw std::invalid_argument("key switch: too many digits for the fused kernel; set fused_key_switch 0");
     static int configured = 0;  // largest K2 smem set so far (the generic shape's dnum varies)
