@@ -28,6 +28,10 @@ struct spmvgpu_ctx {
     std::mutex plans_mu;
     std::list<spmv::detail::PlanLease> plans;
     std::size_t plan_capacity = 4;
+    // one host thread at a time per context (the reference's backends may be
+    // shared across threads); recursive: the protocol layer calls
+    // back into the C-ABI
+    std::recursive_mutex api_mu;
     ~spmvgpu_ctx();
 };
 
@@ -83,6 +87,11 @@ int guard(F&& f) {
                         : SPMVGPU_ERR_INTERNAL,
                     w);
     }
+}
+
+std::unique_lock<std::recursive_mutex> api_lock(const spmvgpu_ctx* c) {
+    if (!c) throw std::invalid_argument("null context");
+    return std::unique_lock<std::recursive_mutex>(const_cast<spmvgpu_ctx*>(c)->api_mu);
 }
 
 cssc::GpuContext& G(spmvgpu_ctx* c) {
@@ -385,7 +394,7 @@ void spmvgpu_ctx_destroy(spmvgpu_ctx* c) { delete c; }
 
 
 int spmvgpu_ctx_primes(const spmvgpu_ctx* c, uint64_t* primes, int cap, int* count) {
-    return guard([&] {
+    return guard([&] { auto lk_ = api_lock(c);
         const auto& P = const_cast<spmvgpu_ctx*>(c)->g->params();
         *count = P.np;
         for (int i = 0; i < P.np && i < cap; ++i) primes[i] = P.primes[i];
@@ -394,7 +403,7 @@ int spmvgpu_ctx_primes(const spmvgpu_ctx* c, uint64_t* primes, int cap, int* cou
 
 int spmvgpu_ctx_sizes(const spmvgpu_ctx* c, uint64_t* n, uint64_t* slots, uint64_t* ct_words,
                       uint64_t* ksk_words, int* dnum) {
-    return guard([&] {
+    return guard([&] { auto lk_ = api_lock(c);
         auto& g = G(const_cast<spmvgpu_ctx*>(c));
         if (n) *n = g.n();
         if (slots) *slots = g.params().S;
@@ -404,9 +413,9 @@ int spmvgpu_ctx_sizes(const spmvgpu_ctx* c, uint64_t* n, uint64_t* slots, uint64
     });
 }
 
-int spmvgpu_sync(spmvgpu_ctx* c) { return guard([&] { G(c).synchronize(); }); }
+int spmvgpu_sync(spmvgpu_ctx* c) { return guard([&] { auto lk_ = api_lock(c); G(c).synchronize(); }); }
 int spmvgpu_set_option(spmvgpu_ctx* c, const char* name, int64_t value) {
-    return guard([&] {
+    return guard([&] { auto lk_ = api_lock(c);
         const std::string n = name ? name : "";
         if (n == "fused_key_switch") {
             G(c).set_fused_key_switch(value != 0);
@@ -428,32 +437,32 @@ int spmvgpu_set_option(spmvgpu_ctx* c, const char* name, int64_t value) {
 void* spmvgpu_stream(spmvgpu_ctx* c) { return c && c->g ? (void*)c->g->stream() : nullptr; }
 
 int spmvgpu_galois_keys(spmvgpu_ctx* c, const int64_t* steps, size_t n) {
-    return guard([&] { G(c).ensure_galois_keys(std::vector<int64_t>(steps, steps + n)); });
+    return guard([&] { auto lk_ = api_lock(c); G(c).ensure_galois_keys(std::vector<int64_t>(steps, steps + n)); });
 }
 uint32_t spmvgpu_galois_element(const spmvgpu_ctx* c, int64_t step) {
     return cssc::galois_element(step, const_cast<spmvgpu_ctx*>(c)->g->n());
 }
-int spmvgpu_download_sk(spmvgpu_ctx* c, int64_t* out) { return guard([&] { G(c).download_sk(out); }); }
-int spmvgpu_download_pk(spmvgpu_ctx* c, uint64_t* out) { return guard([&] { G(c).download_pk_coef(out); }); }
+int spmvgpu_download_sk(spmvgpu_ctx* c, int64_t* out) { return guard([&] { auto lk_ = api_lock(c); G(c).download_sk(out); }); }
+int spmvgpu_download_pk(spmvgpu_ctx* c, uint64_t* out) { return guard([&] { auto lk_ = api_lock(c); G(c).download_pk_coef(out); }); }
 int spmvgpu_download_ksk(spmvgpu_ctx* c, uint32_t which, uint64_t* out) {
-    return guard([&] { G(c).download_key_coef(which, out); });
+    return guard([&] { auto lk_ = api_lock(c); G(c).download_key_coef(which, out); });
 }
 
 int spmvgpu_ct_alloc(spmvgpu_ctx* c, size_t count, spmvgpu_ct* out) {
-    return guard([&] {
+    return guard([&] { auto lk_ = api_lock(c);
         auto& g = G(c);
         for (size_t i = 0; i < count; ++i) out[i] = reinterpret_cast<spmvgpu_ct>(g.pool().alloc(sizeof(u64) * g.ct_words()));
     });
 }
 int spmvgpu_ct_free(spmvgpu_ctx* c, const spmvgpu_ct* cts, size_t count) {
-    return guard([&] {
+    return guard([&] { auto lk_ = api_lock(c);
         auto& g = G(c);
         for (size_t i = 0; i < count; ++i)
             if (cts[i]) g.pool().release(reinterpret_cast<void*>(cts[i]), sizeof(u64) * g.ct_words());
     });
 }
 int spmvgpu_ct_upload(spmvgpu_ctx* c, spmvgpu_ct ct, const uint64_t* words) {
-    return guard([&] {
+    return guard([&] { auto lk_ = api_lock(c);
         auto& g = G(c);
         cssc::cuda_check(cudaMemcpyAsync(reinterpret_cast<void*>(ct), words, sizeof(u64) * g.ct_words(),
                                          cudaMemcpyHostToDevice, g.stream()), "ct upload");
@@ -461,7 +470,7 @@ int spmvgpu_ct_upload(spmvgpu_ctx* c, spmvgpu_ct ct, const uint64_t* words) {
     });
 }
 int spmvgpu_ct_download(spmvgpu_ctx* c, spmvgpu_ct ct, uint64_t* words) {
-    return guard([&] {
+    return guard([&] { auto lk_ = api_lock(c);
         auto& g = G(c);
         cssc::cuda_check(cudaMemcpyAsync(words, reinterpret_cast<void*>(ct), sizeof(u64) * g.ct_words(),
                                          cudaMemcpyDeviceToHost, g.stream()), "ct download");
@@ -495,14 +504,14 @@ size_t wire_bytes(const cssc::RnsParams& P) {
 }  // namespace
 
 int spmvgpu_ct_wire_size(spmvgpu_ctx* c, size_t* bytes) {
-    return guard([&] {
+    return guard([&] { auto lk_ = api_lock(c);
         if (!bytes) throw std::invalid_argument("null argument");
         *bytes = wire_bytes(G(c).params());
     });
 }
 
 int spmvgpu_ct_serialize(spmvgpu_ctx* c, spmvgpu_ct ct, uint8_t* buf, size_t cap, size_t* written) {
-    return guard([&] {
+    return guard([&] { auto lk_ = api_lock(c);
         auto& g = G(c);
         const auto& P = g.params();
         const size_t need = wire_bytes(P);
@@ -541,7 +550,7 @@ int spmvgpu_ct_serialize(spmvgpu_ctx* c, spmvgpu_ct ct, uint8_t* buf, size_t cap
 }
 
 int spmvgpu_ct_deserialize(spmvgpu_ctx* c, const uint8_t* buf, size_t len, spmvgpu_ct ct) {
-    return guard([&] {
+    return guard([&] { auto lk_ = api_lock(c);
         auto& g = G(c);
         const auto& P = g.params();
         if (!buf || !ct) throw std::invalid_argument("null argument");
@@ -577,7 +586,7 @@ int spmvgpu_ct_deserialize(spmvgpu_ctx* c, const uint8_t* buf, size_t len, spmvg
 
 int spmvgpu_encrypt(spmvgpu_ctx* c, const int64_t* vals, const uint64_t* offsets, const uint64_t* streams,
                     const spmvgpu_ct* out, size_t n) {
-    return guard([&] {
+    return guard([&] { auto lk_ = api_lock(c);
         auto& g = G(c);
         std::vector<u64> st(n);
         for (size_t i = 0; i < n; ++i) st[i] = streams && streams[i] ? streams[i] : g.next_stream_id();
@@ -588,7 +597,7 @@ int spmvgpu_encrypt_cssc(spmvgpu_ctx* c, const int64_t* col_indices, const int64
                          const int64_t* vec, uint64_t vec_len, const int32_t* rows, uint64_t n_rows,
                          const int32_t* slices, uint64_t n_slices, const int32_t* cols, uint64_t n_cols,
                          const spmvgpu_ct* out, size_t n_chunks) {
-    return guard([&] {
+    return guard([&] { auto lk_ = api_lock(c);
         auto& g = G(c);
         // descriptor validation: the kernel trusts every index it reads
         const uint64_t S = g.params().S;
@@ -622,7 +631,7 @@ int spmvgpu_encrypt_cssc(spmvgpu_ctx* c, const int64_t* col_indices, const int64
     });
 }
 int spmvgpu_decrypt(spmvgpu_ctx* c, const spmvgpu_ct* cts, size_t n, uint64_t* slots, int32_t* budgets) {
-    return guard([&] {
+    return guard([&] { auto lk_ = api_lock(c);
         std::vector<int> b(n);
         G(c).decrypt(cptrs(cts, n), slots, b.data());
         if (budgets)
@@ -630,28 +639,28 @@ int spmvgpu_decrypt(spmvgpu_ctx* c, const spmvgpu_ct* cts, size_t n, uint64_t* s
     });
 }
 int spmvgpu_add(spmvgpu_ctx* c, const spmvgpu_ct* a, const spmvgpu_ct* b, const spmvgpu_ct* out, size_t n) {
-    return guard([&] { G(c).add(cptrs(a, n), cptrs(b, n), mptrs(out, n)); });
+    return guard([&] { auto lk_ = api_lock(c); G(c).add(cptrs(a, n), cptrs(b, n), mptrs(out, n)); });
 }
 int spmvgpu_sum(spmvgpu_ctx* c, const spmvgpu_ct* cts, size_t n, spmvgpu_ct out) {
-    return guard([&] {
+    return guard([&] { auto lk_ = api_lock(c);
         if (!out) throw std::invalid_argument("null output ciphertext");
         G(c).sum(cptrs(cts, n), reinterpret_cast<u64*>(out));
     });
 }
 int spmvgpu_mul_relin(spmvgpu_ctx* c, const spmvgpu_ct* a, const spmvgpu_ct* b, const spmvgpu_ct* out,
                       size_t n) {
-    return guard([&] { G(c).mul_relin(cptrs(a, n), cptrs(b, n), mptrs(out, n)); });
+    return guard([&] { auto lk_ = api_lock(c); G(c).mul_relin(cptrs(a, n), cptrs(b, n), mptrs(out, n)); });
 }
 int spmvgpu_rotate(spmvgpu_ctx* c, const spmvgpu_ct* src, const int64_t* steps, const spmvgpu_ct* out,
                    size_t n) {
-    return guard([&] {
+    return guard([&] { auto lk_ = api_lock(c);
         G(c).rotate(cptrs(src, n), std::vector<int64_t>(steps, steps + n), std::vector<const u64*>(n, nullptr),
                     mptrs(out, n));
     });
 }
 int spmvgpu_rotate_add(spmvgpu_ctx* c, const spmvgpu_ct* acc, const spmvgpu_ct* src, const int64_t* steps,
                        const spmvgpu_ct* out, size_t n) {
-    return guard([&] {
+    return guard([&] { auto lk_ = api_lock(c);
         auto o = mptrs(out, n);
         auto s = cptrs(src, n);
         for (size_t i = 0; i < n; ++i)
@@ -661,10 +670,10 @@ int spmvgpu_rotate_add(spmvgpu_ctx* c, const spmvgpu_ct* acc, const spmvgpu_ct* 
 }
 int spmvgpu_mul_plain(spmvgpu_ctx* c, const spmvgpu_ct* a, const int64_t* vals, const uint64_t* offsets,
                       const spmvgpu_ct* out, size_t n) {
-    return guard([&] { G(c).mul_plain(cptrs(a, n), vals, offsets, mptrs(out, n)); });
+    return guard([&] { auto lk_ = api_lock(c); G(c).mul_plain(cptrs(a, n), vals, offsets, mptrs(out, n)); });
 }
 int spmvgpu_ntt(spmvgpu_ctx* c, int prime_index, uint64_t* data, size_t limbs, int inverse) {
-    return guard([&] {
+    return guard([&] { auto lk_ = api_lock(c);
         auto& g = G(c);
         if (prime_index < 0 || prime_index >= g.params().np) throw std::invalid_argument("prime index");
         g.ntt_host(prime_index, data, (int)limbs, inverse != 0);
@@ -674,7 +683,7 @@ int spmvgpu_ntt(spmvgpu_ctx* c, int prime_index, uint64_t* data, size_t limbs, i
 int spmvgpu_plan_create(spmvgpu_ctx* c, size_t n_chunks, const uint64_t* r, const uint64_t* cols,
                         const uint32_t* slice, size_t n_slices, const spmvgpu_ct* a_cts, const spmvgpu_ct* b_cts,
                         const spmvgpu_ct* out_cts, spmvgpu_plan** out) {
-    return guard([&] {
+    return guard([&] { auto lk_ = api_lock(c);
         auto p = std::make_unique<spmvgpu_plan>();
         p->ctx = c;
         p->plan = std::make_unique<cssc::CloudPlan>(
@@ -684,10 +693,10 @@ int spmvgpu_plan_create(spmvgpu_ctx* c, size_t n_chunks, const uint64_t* r, cons
         *out = p.release();
     });
 }
-int spmvgpu_plan_run(spmvgpu_plan* p) { return guard([&] { p->plan->run(); }); }
-int spmvgpu_plan_capture(spmvgpu_plan* p) { return guard([&] { p->plan->capture(); }); }
+int spmvgpu_plan_run(spmvgpu_plan* p) { return guard([&] { auto lk_ = api_lock(p ? p->ctx : nullptr); p->plan->run(); }); }
+int spmvgpu_plan_capture(spmvgpu_plan* p) { return guard([&] { auto lk_ = api_lock(p ? p->ctx : nullptr); p->plan->capture(); }); }
 int spmvgpu_plan_stats_get(const spmvgpu_plan* p, spmvgpu_plan_stats* o) {
-    return guard([&] {
+    return guard([&] { auto lk_ = api_lock(p ? p->ctx : nullptr);
         const auto& s = p->plan->stats();
         o->chunks = s.chunks;
         o->slices = s.slices;
@@ -701,7 +710,7 @@ int spmvgpu_plan_stats_get(const spmvgpu_plan* p, spmvgpu_plan_stats* o) {
     });
 }
 int spmvgpu_plan_profile(spmvgpu_plan* p, spmvgpu_phase* phases, int cap, int* count) {
-    return guard([&] {
+    return guard([&] { auto lk_ = api_lock(p ? p->ctx : nullptr);
         if (!p || !count) throw std::invalid_argument("null argument");
         const auto ph = p->plan->profile();
         *count = (int)ph.size();
@@ -721,7 +730,7 @@ void spmvgpu_plan_destroy(spmvgpu_plan* p) { delete p; }
 int cssc_spmv_partitioned(spmvgpu_ctx* c, const cssc_csr* m, const int64_t* v, uint64_t vlen,
                           uint64_t chunk_size, int key_holder, int64_t* values, cssc_result* res,
                           cssc_message* msgs, uint64_t msg_cap) {
-    return guard([&] {
+    return guard([&] { auto lk_ = api_lock(c);
         spmv::GpuBfvBackend be(c->hp, c);
         const spmv::CsrMatrix mm = to_csr(*m);
         const std::vector<int64_t> vv(v, v + vlen);
@@ -732,7 +741,7 @@ int cssc_spmv_partitioned(spmvgpu_ctx* c, const cssc_csr* m, const int64_t* v, u
 
 int cssc_diag_spmv(spmvgpu_ctx* c, const cssc_csr* m, const int64_t* v, uint64_t vlen, int key_holder,
                    int64_t* values, cssc_result* res, cssc_message* msgs, uint64_t msg_cap) {
-    return guard([&] {
+    return guard([&] { auto lk_ = api_lock(c);
         spmv::GpuBfvBackend be(c->hp, c);
         const spmv::CsrMatrix mm = to_csr(*m);
         const std::vector<int64_t> vv(v, v + vlen);
@@ -743,7 +752,7 @@ int cssc_diag_spmv(spmvgpu_ctx* c, const cssc_csr* m, const int64_t* v, uint64_t
 
 int cssc_spmv_batch(spmvgpu_ctx* c, const cssc_csr* ms, const int64_t* const* vs, size_t nmat, uint64_t chunk_size,
                     int key_holder, int64_t* const* values, cssc_result* res) {
-    return guard([&] {
+    return guard([&] { auto lk_ = api_lock(c);
         G(c);
         std::vector<spmv::detail::CsrView> w;
         for (size_t i = 0; i < nmat; ++i) w.push_back(view_of(ms[i], vs[i]));
@@ -755,7 +764,7 @@ int cssc_spmv_batch(spmvgpu_ctx* c, const cssc_csr* ms, const int64_t* const* vs
 
 int cssc_job_create_shard(spmvgpu_ctx* c, const cssc_csr* ms, const int64_t* const* vs, size_t nmat,
                           uint64_t chunk_size, int rank, int world, cssc_job** out) {
-    return guard([&] {
+    return guard([&] { auto lk_ = api_lock(c);
         auto j = std::make_unique<cssc_job>();
         j->ctx = c;
         G(c);
@@ -771,7 +780,7 @@ int cssc_job_create(spmvgpu_ctx* c, const cssc_csr* ms, const int64_t* const* vs
     return cssc_job_create_shard(c, ms, vs, nmat, chunk_size, 0, 1, out);
 }
 int cssc_job_result_words(cssc_job* j, uint64_t* words, uint64_t cap_words, uint64_t* n_results) {
-    return guard([&] {
+    return guard([&] { auto lk_ = api_lock(j ? j->ctx : nullptr);
         if (!j || !n_results) throw std::invalid_argument("null argument");
         *n_results = j->job->result_count();
         if (!words) return;
@@ -781,35 +790,35 @@ int cssc_job_result_words(cssc_job* j, uint64_t* words, uint64_t cap_words, uint
     });
 }
 int cssc_job_finish_words(cssc_job* j, const uint64_t* words, int64_t* const* values, cssc_result* res) {
-    return guard([&] {
+    return guard([&] { auto lk_ = api_lock(j ? j->ctx : nullptr);
         if (!j || (!words && j->job->result_count())) throw std::invalid_argument("null argument");
         const auto r = j->job->finish_words(words);
         for (size_t i = 0; i < r.size(); ++i) fill_result(r[i], values ? values[i] : nullptr, res ? res + i : nullptr, nullptr, 0);
     });
 }
-int cssc_job_encrypt(cssc_job* j) { return guard([&] { j->job->encrypt(); }); }
-int cssc_job_cloud(cssc_job* j, int use_graph) { return guard([&] { j->job->cloud(use_graph != 0); }); }
+int cssc_job_encrypt(cssc_job* j) { return guard([&] { auto lk_ = api_lock(j ? j->ctx : nullptr); j->job->encrypt(); }); }
+int cssc_job_cloud(cssc_job* j, int use_graph) { return guard([&] { auto lk_ = api_lock(j ? j->ctx : nullptr); j->job->cloud(use_graph != 0); }); }
 int cssc_job_finish(cssc_job* j, int64_t* const* values, cssc_result* res) {
-    return guard([&] {
+    return guard([&] { auto lk_ = api_lock(j ? j->ctx : nullptr);
         const auto r = j->job->finish();
         for (size_t i = 0; i < r.size(); ++i) fill_result(r[i], values ? values[i] : nullptr, res ? res + i : nullptr, nullptr, 0);
     });
 }
 int cssc_job_plan_stats(const cssc_job* j, spmvgpu_plan_stats* out) {
-    return guard([&] {
+    return guard([&] { auto lk_ = api_lock(j ? j->ctx : nullptr);
         std::memset(out, 0, sizeof *out);
         if (j->job->plan()) spmvgpu_plan_stats_get(j->job->plan(), out);
     });
 }
 int cssc_job_profile(cssc_job* j, spmvgpu_phase* phases, int cap, int* count) {
-    return guard([&] {
+    return guard([&] { auto lk_ = api_lock(j ? j->ctx : nullptr);
         if (!j || !j->job->plan()) throw std::invalid_argument("job has no plan yet (run cloud first)");
         const int st = spmvgpu_plan_profile(j->job->plan(), phases, cap, count);
         if (st != SPMVGPU_OK) throw std::runtime_error(g_err);
     });
 }
 int cssc_job_input_bytes(const cssc_job* j, uint64_t* h2d, uint64_t* d2h) {
-    return guard([&] {
+    return guard([&] { auto lk_ = api_lock(j ? j->ctx : nullptr);
         *h2d = j->job->h2d_bytes();
         *d2h = j->job->d2h_bytes();
     });
@@ -895,7 +904,7 @@ int64_t cssc_stencil27_csr(uint64_t side, uint64_t seed, int64_t lo, int64_t hi,
 extern "C" {
 
 int spmvgpu_probe_ntt(spmvgpu_ctx* c, size_t limbs, int inverse, int reps, double* us_per_launch) {
-    return guard([&] {
+    return guard([&] { auto lk_ = api_lock(c);
         auto& g = G(c);
         const auto& P = g.params();
         cssc::DevBuf buf(&g.pool(), sizeof(u64) * limbs * P.n);
@@ -923,7 +932,7 @@ int spmvgpu_probe_ntt(spmvgpu_ctx* c, size_t limbs, int inverse, int reps, doubl
 }
 
 int spmvgpu_probe_butterfly_peak(spmvgpu_ctx* c, double* bps) {
-    return guard([&] {
+    return guard([&] { auto lk_ = api_lock(c);
         auto& g = G(c);
         const auto& P = g.params();
         const u64 q = P.primes[0], w = P.tw_fwd[0][2], wsh = P.tw_fwd[0][3];

@@ -184,3 +184,24 @@ def test_chunk_split_shards_sum_to_the_full_result(world):
     for j in jobs:
         j.close()
     ctx.close()
+
+
+def test_context_shared_across_host_threads():
+    """a backend may be shared by host threads; calls on one
+    context serialise and every result stays the reference's."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    ctx = pk.Context(logn=10, seed=12)
+    cases = [(pk.random_sparse_csr(90, 70, 500, s, -8, 8), pk.random_vector(70, s, -8, 8, nonzero=True))
+             for s in range(40, 52)]
+
+    def run(i):
+        m, v = cases[i % len(cases)]
+        return i, pk.spmv_partitioned(ctx, m, v, ctx.slots)
+
+    with ThreadPoolExecutor(max_workers=6) as ex:
+        results = list(ex.map(run, range(36)))
+    for i, got in results:
+        m, v = cases[i % len(cases)]
+        assert_same(got, checker(m, v, ctx.slots, ctx.slots))
+    ctx.close()
