@@ -142,6 +142,69 @@ def cpu_reference_time(ms, vs, slot_count, budget_s=3.0):
     return best, reps
 
 
+def cpu_bfv_time(pk, ctx, cfg, max_chunks=64):
+    """SURVEY 8(d) CPU baseline 3: the cloud phase of the workload in real
+    RNS-BFV on the host, through the C restatement (oracle/bfv_oracle.c, same
+    parameters and keys as the device), op by op like the reference algorithm:
+    multiply+relinearise, the rotation_schedule rotate-and-add, mask, sum.
+    Timed on 1 thread and on all host threads (chunks in parallel; ctypes
+    drops the GIL).  Bounded sample: the first max_chunks chunks."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    from oracle_bindings import BfvOracle
+
+    orc = BfvOracle.like(ctx)
+    S = ctx.slots
+    chunks = []
+    for m, v in zip(cfg["ms"], cfg["vs"]):
+        pc = pk.pack_chunks(m, S) if m.rows <= S else None
+        if pc is None:
+            continue
+        off = 0
+        for r, c in zip(pc["r"], pc["c"]):
+            size = int(r * c)
+            vf, cf = pc["vflat"][off:off + size], pc["cflat"][off:off + size]
+            off += size
+            chunks.append((int(r), int(c), vf, np.where(cf >= 0, np.asarray(v)[np.maximum(cf, 0)], 0)))
+        if len(chunks) >= max_chunks:
+            break
+    chunks = chunks[:max_chunks]
+    if not chunks:
+        return None
+    scheds = [pk.rotation_schedule(r, c) for r, c, _, _ in chunks]
+    for g in sorted({orc.galois_elt(off) for sc in scheds for off, _ in sc}):
+        if g != 1:
+            orc.lib.bfvo_add_galois_key(orc.h, g)  # keys are setup, not timed
+    cts = [(orc.encrypt(a, 100 + i), orc.encrypt(b, 200 + i)) for i, (_, _, a, b) in enumerate(chunks)]
+
+    def chain(i):
+        r = chunks[i][0]
+        prod = orc.mul_relin(*cts[i])
+        acc = prod
+        for off, from_acc in scheds[i]:
+            acc = orc.add(acc, orc.rotate(acc if from_acc else prod, off))
+        return orc.mul_plain(acc, np.ones(r, np.int64))
+
+    def run(threads):
+        t0 = time.perf_counter()
+        if threads == 1:
+            parts = [chain(i) for i in range(len(chunks))]
+        else:
+            with ThreadPoolExecutor(max_workers=threads) as ex:
+                parts = list(ex.map(chain, range(len(chunks))))
+        acc = parts[0]
+        for p in parts[1:]:
+            acc = orc.add(acc, p)
+        return (time.perf_counter() - t0) * 1e3
+
+    threads = os.cpu_count() or 1
+    one = run(1)
+    many = run(threads)
+    return {"ms_1_thread": round(one, 2), "ms_all_threads": round(many, 2), "threads": threads,
+            "chunks": len(chunks), "kind": "port",
+            "sample": f"{cfg['name']}: cloud phase of {len(chunks)} chunk(s) in RNS-BFV on the CPU oracle "
+                      "(oracle/bfv_oracle.c), same parameters, keys excluded"}
+
+
 def run_reference_arm(args, cfg):
     """--impl reference: the reference's own CPU path on all host cores it can use
     (independent matrices in parallel threads; the library itself is single-threaded)."""
@@ -418,7 +481,14 @@ def main():
                 others[f"C{c}"] = {"error": str(e)[:200]}
 
     cpu = None
+    cpu_bfv = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            bctx = pk.Context(logn=cfg["logn"], seed=1)
+            cpu_bfv = cpu_bfv_time(pk, bctx, cfg)
+            bctx.close()
+        except Exception as e:  # the baseline must not hide the headline
+            cpu_bfv = {"error": str(e)[:200]}
         r = cpu_reference_time(cfg["ms"], cfg["vs"], 1 << (cfg["logn"] - 1))
         if r is not None:
             best, reps = r
@@ -440,7 +510,7 @@ def main():
                        "l2": "flushed (256 MiB write) before every timed step",
                        "parallelism": f"replica per GPU x{world}"},
             "clocks": head["clocks"], "e2e": head["e2e"], "gpu_launches": head["plan"]["kernels_per_run"],
-            "roofline": head["roofline"], "key_switch": head["key_switch"],
+            "roofline": head["roofline"], "key_switch": head["key_switch"], "cpu_bfv_baseline": cpu_bfv,
             "paper_cost_model": head["paper_cost_model"], "diagonal_baseline": head.get("diagonal_baseline"),
             "transcript": {"priced_bytes_per_ct": 545260, "wire_bytes_per_ct": head["wire_bytes_per_ct"]},
             "cpu_baseline": cpu, "verified_exact": head["verified"],
