@@ -10,13 +10,16 @@
 //   phase C: stages 0..A-1 act on the R2 strided columns {j + R2*c}; their
 //            twiddles are W[1 .. R1), shared by every column -> staged in smem;
 //   phase B: stages A..logN-1 act on the R1 contiguous blocks {b*R2 + c}.
-// A CTA owns 16 lines (16 columns or 16 blocks): a small tile (16-32 KB), so
-// several CTAs share an SM and one limb is spread over R/16 CTAs -- this keeps
-// the machine busy even for a single ciphertext.  Inside a tile each thread
-// runs radix-16 (then radix-2^r) butterfly groups in registers; lane%16 picks
-// the line, which makes every pass bank-conflict free (column tiles have
-// stride 1 across lines, block tiles an odd stride R2+1).  Harvey lazy
-// reduction: [0, 4q) forward, [0, 2q) inverse, canonical at the end.
+// A CTA owns LN lines (16 columns or blocks; 8 when a launch is too small to
+// fill the GPU): a small tile (8-32 KB), so several CTAs share an SM and one
+// limb is spread over R/LN CTAs -- the machine stays busy even for a single
+// ciphertext.  Inside a tile each thread runs radix-2^r butterfly groups in
+// registers (radix-8 in the column phase, to stay at 80 registers and 3 CTAs
+// per SM); lane % LN picks the line, which keeps the passes bank-conflict free
+// (column tiles have stride 1 across lines, block tiles an odd stride R2+1).
+// Lazy reduction: the forward transform needs no correction at all for
+// q < 2^58 (values stay < 31q, reduced once at the end), the inverse keeps
+// [0, 2q) with one conditional subtraction per butterfly.
 #pragma once
 #include "modarith.cuh"
 #include "rns_params.hpp"
