@@ -151,3 +151,25 @@ def test_cloud_plan_words_match_oracle(graph):
     for s in range(3):
         assert np.array_equal(ctx.download(int(out[s])), want[s]), s
     ctx.free(np.concatenate([ha, hb, out]))
+
+
+def test_cloud_plan_fused_and_unfused_agree():
+    """The fused plan (fused multiply, K1/K2 key switch, block-phase mask
+    accumulation, small-launch tiles) and the launch-per-op pipeline give the
+    same result words."""
+    shapes = [(7, 13), (3, 6), (5, 7), (11, 2), (1, 64), (2, 1)]
+    slices = [0, 0, 1, 1, 1, 0]
+    rng = np.random.default_rng(9)
+    va = [rng.integers(-8, 9, r * c) for r, c in shapes]
+    vb = [rng.integers(-8, 9, r * c) for r, c in shapes]
+    outs = {}
+    for fused in (1, 0):
+        ctx = pk.Context(logn=11, seed=4)
+        ctx.set_option("fused_key_switch", fused)
+        ha = ctx.encrypt(va, [300 + i for i in range(len(shapes))])
+        hb = ctx.encrypt(vb, [400 + i for i in range(len(shapes))])
+        out = pk.cloud_plan(ctx, [r for r, _ in shapes], [c for _, c in shapes], slices, 2, ha, hb, graph=True)
+        outs[fused] = [ctx.download(int(h)) for h in out]
+        ctx.close()
+    for a, b in zip(outs[0], outs[1]):
+        assert np.array_equal(a, b)
