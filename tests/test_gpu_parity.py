@@ -123,12 +123,14 @@ def test_fused_and_unfused_key_switch_agree():
     assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
 
 
-@pytest.mark.parametrize("graph", [False, True])
-def test_cloud_plan_words_match_oracle(graph):
+@pytest.mark.parametrize("graph,shape", [(False, 0), (True, 0), (True, 1)])
+def test_cloud_plan_words_match_oracle(graph, shape):
     """The whole batched cloud phase (mult+relin, hoisted rotate-and-add trees,
     masked per-slice accumulation) equals the oracle's op-by-op evaluation of
-    the reference algorithm (protocol.cpp:121-140) word for word (P5)."""
-    ctx = pk.Context(logn=10, seed=9)
+    the reference algorithm (protocol.cpp:121-140) word for word (P5); shape 1
+    is a parameter set without a compile-time specialisation (L=5, K=2, 3 digits)."""
+    ctx = pk.Context(logn=10, seed=9) if shape == 0 else pk.Context(logn=12, seed=9, L=5, K=2, alpha=2,
+                                                                     qbits=58, pbits=58)
     orc = BfvOracle.like(ctx)
     S = ctx.slots
     shapes = [(7, 13), (3, 6), (5, 7), (11, 2), (1, 64), (40, 12), (2, 1), (8, 3)]
