@@ -198,6 +198,10 @@ typedef struct {
     uint64_t n_messages;
 } cssc_result;
 
+/* spmv on the GPU backend (reference protocol.cpp:74-153): one slice, every row
+ * in one chunk set (rows <= slot budget, else ColumnTooTallError) */
+int cssc_spmv(spmvgpu_ctx* c, const cssc_csr* m, const int64_t* v, uint64_t vlen, uint64_t chunk_size,
+              int key_holder, int64_t* values, cssc_result* res, cssc_message* msgs, uint64_t msg_cap);
 /* spmv_partitioned on the GPU backend: values (rows) in original row order */
 int cssc_spmv_partitioned(spmvgpu_ctx* c, const cssc_csr* m, const int64_t* v, uint64_t vlen,
                           uint64_t chunk_size, int key_holder, int64_t* values,

@@ -116,6 +116,8 @@ _SIGS = {
     "cssc_spmv_partitioned": (C.c_int, [C.c_void_p, C.POINTER(CsrC), i64p, C.c_uint64, C.c_uint64,
                                         C.c_int, i64p, C.POINTER(ResultC), C.POINTER(Message),
                                         C.c_uint64]),
+    "cssc_spmv": (C.c_int, [C.c_void_p, C.POINTER(CsrC), i64p, C.c_uint64, C.c_uint64, C.c_int, i64p,
+                            C.POINTER(ResultC), C.POINTER(Message), C.c_uint64]),
     "cssc_diag_spmv": (C.c_int, [C.c_void_p, C.POINTER(CsrC), i64p, C.c_uint64, C.c_int, i64p,
                                  C.POINTER(ResultC), C.POINTER(Message), C.c_uint64]),
     "spmvgpu_sum": (C.c_int, [C.c_void_p, u64p, C.c_size_t, C.c_uint64]),
@@ -488,6 +490,20 @@ def spmv_partitioned(ctx: Context, m: Csr, v, chunk_size: int | None = None, key
     vp = vv if vv.size else np.zeros(1, np.int64)
     check(lib().cssc_spmv_partitioned(ctx.h, C.byref(csr), _p(vp, i64p), vv.size, chunk, key_holder,
                                       _p(vals, i64p), C.byref(res), msgs, cap))
+    return _result(res, vals[: m.rows], msgs)
+
+
+def spmv(ctx: Context, m: Csr, v, chunk_size: int | None = None, key_holder: int = 0) -> dict:
+    """The reference's spmv (no row partitioning) on the GPU backend."""
+    vv = _i64(v)
+    chunk = ctx.slots if chunk_size is None else chunk_size
+    vals = np.zeros(max(m.rows, 1), np.int64)
+    res = ResultC()
+    msgs = (Message * 8)()
+    csr = m.c()
+    vp = vv if vv.size else np.zeros(1, np.int64)
+    check(lib().cssc_spmv(ctx.h, C.byref(csr), _p(vp, i64p), vv.size, chunk, key_holder, _p(vals, i64p),
+                          C.byref(res), msgs, 8))
     return _result(res, vals[: m.rows], msgs)
 
 

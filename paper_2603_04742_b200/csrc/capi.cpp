@@ -739,6 +739,17 @@ int cssc_spmv_partitioned(spmvgpu_ctx* c, const cssc_csr* m, const int64_t* v, u
     });
 }
 
+int cssc_spmv(spmvgpu_ctx* c, const cssc_csr* m, const int64_t* v, uint64_t vlen, uint64_t chunk_size,
+              int key_holder, int64_t* values, cssc_result* res, cssc_message* msgs, uint64_t msg_cap) {
+    return guard([&] { auto lk_ = api_lock(c);
+        spmv::GpuBfvBackend be(c->hp, c);
+        const spmv::CsrMatrix mm = to_csr(*m);
+        const std::vector<int64_t> vv(v, v + vlen);
+        const auto r = spmv::spmv(be, mm, vv, chunk_size, static_cast<spmv::PartyRole>(key_holder));
+        fill_result(r, values, res, msgs, msg_cap);
+    });
+}
+
 int cssc_diag_spmv(spmvgpu_ctx* c, const cssc_csr* m, const int64_t* v, uint64_t vlen, int key_holder,
                    int64_t* values, cssc_result* res, cssc_message* msgs, uint64_t msg_cap) {
     return guard([&] { auto lk_ = api_lock(c);

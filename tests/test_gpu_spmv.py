@@ -205,3 +205,15 @@ def test_context_shared_across_host_threads():
         m, v = cases[i % len(cases)]
         assert_same(got, checker(m, v, ctx.slots, ctx.slots))
     ctx.close()
+
+
+def test_plain_spmv_is_one_slice(ctx10):
+    """spmv (protocol.cpp:74-153): one slice; equals spmv_partitioned when the
+    rows fit one chunk budget, ColumnTooTallError when a column does not."""
+    m = pk.random_sparse_csr(300, 80, 900, 61, -8, 8)
+    v = pk.random_vector(80, 61, -8, 8, nonzero=True)
+    got = pk.spmv(ctx10, m, v)
+    assert_same(got, checker(m, v, ctx10.slots, ctx10.slots))
+    with pytest.raises(pk.SpmvError) as e:
+        pk.spmv(ctx10, m, v, 16)  # 300 rows: aligned column 0 is taller than 16
+    assert e.value.kind == "ColumnTooTallError"
