@@ -13,6 +13,9 @@
  * scale-and-round; hybrid key switching with digit decomposition) and pinned
  * by the known-answer tests in tests/test_oracle_bfv.py.  Decryptions are
  * pinned to the reference simulator (oracle/_ref) slot for slot.
+ * At the ciphertext-word level parity is therefore UNPINNED by the reference
+ * (SURVEY 8(c)): the words are self-consistent with these KATs, not with a
+ * reference output.
  *
  * Every integer formula that is not a canonical modular identity (the
  * fixed-point rounding terms of the exact basis extension and of the t/Q
