@@ -145,6 +145,10 @@ namespace cssc {
 // Fused hybrid key switch (ks_fused.cu): OUT[p] = BASE[p] + (p==0 ? phi_g(RSRC.c0) : 0)
 // + KeySwitch(phi_g(SRC poly src_poly)) with per-item keys; SRC == nullptr reads the
 // contiguous [item][L][N] polynomials at SRCC instead.  DX / ACC are workspaces.
+// ModUp + NTT + key product + INTT of a key switch as one cluster kernel
+// (ks_cluster.cu); false when the shape has no cluster specialisation
+bool launch_ks_cluster(const DevConsts* dc, const RnsParams& P, const u64* const* SRC, const u64* SRCC,
+                       int src_poly, const u32* ginv, const u64* const* KEY, u64* ACC, int items, cudaStream_t st);
 void launch_ks_fused(const DevConsts* dc, const RnsParams& P, const u64* const* SRC, const u64* SRCC,
                      int src_poly, const u32* ginv, const u64* const* KEY, const u64* const* BASE,
                      const u64* const* RSRC, u64* const* OUT, u64* DX, u64* ACC, int items, cudaStream_t st,

@@ -259,6 +259,10 @@ static void ks_fused_t(const DevConsts* dc, const RnsParams& P, const u64* const
                        const u64* const* RSRC, u64* const* OUT, u64* DX, u64* ACC, int items, cudaStream_t st,
                        const u64* const* EXTRA) {
     using G = Ntt2<LOGN>;
+    if (launch_ks_cluster(dc, P, SRC, SRCC, src_poly, ginv, KEY, ACC, items, st)) {
+        launch_ks_moddown(dc, P, ACC, BASE, RSRC, ginv, OUT, items, st, EXTRA);
+        return;
+    }
     const int L = P.cfg.L, K = P.cfg.K, LK = L + K, dnum = P.dnum;
     const int smem1 = G::SMEM_C;
     constexpr int KTM = ks_keys_tma<LOGN>() ? 1 : 0;

@@ -88,3 +88,15 @@ def test_config_result_words_match_oracle(cfgno):
         assert np.array_equal(ctx.download(int(out[s])), want[s]), (cfgno, s)
     ctx.free(np.concatenate([ha, hb, out]))
     ctx.close()
+
+
+@pytest.mark.parametrize("cfgno", [1, 2])
+def test_cluster_key_switch_words_match_oracle(cfgno):
+    """The opt-in thread-block-cluster key switch (ks_cluster.cu, CSSC_KS_CLUSTER=1)
+    produces the same words; run in a child so the env switch is read fresh."""
+    import subprocess
+    env = dict(os.environ, CSSC_KS_CLUSTER="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider",
+                        f"{__file__}::test_config_result_words_match_oracle[{cfgno}]"],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
