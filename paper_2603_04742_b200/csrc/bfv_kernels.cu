@@ -391,6 +391,172 @@ __device__ __forceinline__ void extend_exact(const DevConsts* __restrict__ dc,
     }
 }
 
+// ---------------------------------------------------------------------------
+// Kernel-parameter copies of the RNS constants (fixed shapes).  A
+// __grid_constant__ parameter lives in the constant bank, so the modmul IMADs
+// take the constants as operands: no LDG per constant and no load latency
+// on the E1/E2/E4 chains (k_mul_scale issued ~180 constant LDGs per
+// coefficient when it read them through the DevConsts pointer).
+// ---------------------------------------------------------------------------
+template <int NX, int NY>
+struct ExtK {
+    u64 xq[NX];
+    Modulus ym[NY];
+    u64 xhat_inv[NX], xhat_inv_sh[NX], R1[NX], R0[NX];
+    u64 xhat_y[NX][NY], xhat_y_sh[NX][NY];
+    u64 X_y[NY], X_y_sh[NY];
+};
+
+template <int NX, int NY>
+static void fill_extk(ExtK<NX, NY>& k, const DevConsts& h, const ExtConsts& e) {
+    for (int i = 0; i < NX; ++i) {
+        k.xq[i] = h.mod[e.xi[i]].q;
+        k.xhat_inv[i] = e.xhat_inv[i];
+        k.xhat_inv_sh[i] = e.xhat_inv_sh[i];
+        k.R1[i] = e.R1[i];
+        k.R0[i] = e.R0[i];
+        for (int j = 0; j < NY; ++j) {
+            k.xhat_y[i][j] = e.xhat_y[i][j];
+            k.xhat_y_sh[i][j] = e.xhat_y_sh[i][j];
+        }
+    }
+    for (int j = 0; j < NY; ++j) {
+        k.ym[j] = h.mod[e.yi[j]];
+        k.X_y[j] = e.X_y[j];
+        k.X_y_sh[j] = e.X_y_sh[j];
+    }
+}
+
+// extend_exact with the constants from a parameter block (same formulas)
+template <int NX, int NY>
+__device__ __forceinline__ void extend_k(const ExtK<NX, NY>& e, const u64* x, u64* out) {
+    u64 y[NX];
+    u64 shi = 0, slo = 0;
+#pragma unroll
+    for (int i = 0; i < NX; ++i) {
+        y[i] = shoup(x[i], e.xhat_inv[i], e.xhat_inv_sh[i], e.xq[i]);
+        add128(shi, slo, 0, frac64(y[i], e.R1[i], e.R0[i]));
+    }
+    const u64 v = shi + (slo >> 63);
+#pragma unroll
+    for (int j = 0; j < NY; ++j) {
+        const u64 p = e.ym[j].q;
+        u64 acc = 0;
+#pragma unroll
+        for (int i = 0; i < NX; ++i) acc += shoup_lazy(y[i], e.xhat_y[i][j], e.xhat_y_sh[i][j], p);
+        acc = reduce_small_quot(acc, e.ym[j]);
+        out[j] = sub_mod(acc, shoup(v, e.X_y[j], e.X_y_sh[j], p), p);
+    }
+}
+
+template <int L>
+struct ExtendK {
+    int n;
+    ExtK<L, L + 1> qb;
+};
+
+template <int L>
+__global__ void k_mul_extend_k(const __grid_constant__ ExtendK<L> c, const u64* const* A, const u64* const* B,
+                               u64* T) {
+    constexpr int nB = L + 1, M = L + nB;
+    const int n = c.n;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int item = blockIdx.y;
+    const int p = blockIdx.z;
+    const u64* src = (p < 2 ? A[item] : B[item]) + (size_t)(p & 1) * L * n;
+    u64* dst = T + ((size_t)item * 4 + p) * M * n;
+    u64 x[L], o[nB];
+#pragma unroll
+    for (int i = 0; i < L; ++i) {
+        x[i] = src[(size_t)i * n + k];
+        dst[(size_t)i * n + k] = x[i];
+    }
+    extend_k(c.qb, x, o);
+#pragma unroll
+    for (int j = 0; j < nB; ++j) dst[(size_t)(L + j) * n + k] = o[j];
+}
+
+template <int L>
+struct ScaleK {
+    int n;
+    u64 q[L], QhatInv[L], QhatInv_sh[L], T1[L], T0[L];
+    Modulus bm[L + 1];
+    u64 QhatB[L][L + 1], QhatB_sh[L][L + 1];
+    u64 QinvB[L + 1], QinvB_sh[L + 1], tB[L + 1], tB_sh[L + 1];
+    ExtK<L + 1, L> bq;
+};
+
+// E2 + E1 as k_mul_scale, constants from the parameter block
+template <int L>
+__global__ void k_mul_scale_k(const __grid_constant__ ScaleK<L> c, const u64* __restrict__ Z, u64* const* OUT,
+                              u64* __restrict__ D2) {
+    constexpr int nB = L + 1, M = L + nB;
+    const int n = c.n;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int item = blockIdx.y;
+    const int r = blockIdx.z;
+    const size_t P = (size_t)M * n;
+    const u64* z = Z + ((size_t)item * 3 + r) * P;
+    u64 xi[L], w[nB], o[L];
+    u64 shi = 0, slo = 0;
+#pragma unroll
+    for (int i = 0; i < L; ++i) {
+        xi[i] = shoup(z[(size_t)i * n + k], c.QhatInv[i], c.QhatInv_sh[i], c.q[i]);
+        add128(shi, slo, umulhi(xi[i], c.T1[i]), xi[i] * c.T1[i]);
+        add128(shi, slo, 0, umulhi(xi[i], c.T0[i]));
+    }
+    const u64 rr = shi + (slo >> 63);
+#pragma unroll
+    for (int j = 0; j < nB; ++j) {
+        const u64 bj = c.bm[j].q;
+        u64 acc = 0;
+#pragma unroll
+        for (int i = 0; i < L; ++i) acc += shoup_lazy(xi[i], c.QhatB[i][j], c.QhatB_sh[i][j], bj);
+        acc = reduce_small_quot(acc, c.bm[j]);
+        const u64 alpha = shoup(sub_mod(acc, z[(size_t)(L + j) * n + k], bj), c.QinvB[j], c.QinvB_sh[j], bj);
+        w[j] = sub_mod(rr, shoup(alpha, c.tB[j], c.tB_sh[j], bj), bj);
+    }
+    extend_k(c.bq, w, o);
+    u64* dst = r < 2 ? OUT[item] + (size_t)r * L * n : D2 + (size_t)item * L * n;
+#pragma unroll
+    for (int i = 0; i < L; ++i) dst[(size_t)i * n + k] = o[i];
+}
+
+template <int L>
+static ExtendK<L> make_extend_k(const RnsParams& P) {
+    ExtendK<L> c{};
+    c.n = P.n;
+    fill_extk(c.qb, P.host, P.host.extQB);
+    return c;
+}
+
+template <int L>
+static ScaleK<L> make_scale_k(const RnsParams& P) {
+    const DevConsts& h = P.host;
+    ScaleK<L> c{};
+    c.n = P.n;
+    for (int i = 0; i < L; ++i) {
+        c.q[i] = h.mod[i].q;
+        c.QhatInv[i] = h.QhatInv[i];
+        c.QhatInv_sh[i] = h.QhatInv_sh[i];
+        c.T1[i] = h.T1[i];
+        c.T0[i] = h.T0[i];
+        for (int j = 0; j <= L; ++j) {
+            c.QhatB[i][j] = h.QhatB[i][j];
+            c.QhatB_sh[i][j] = h.QhatB_sh[i][j];
+        }
+    }
+    for (int j = 0; j <= L; ++j) {
+        c.bm[j] = h.mod[L + P.cfg.K + j];
+        c.QinvB[j] = h.QinvB[j];
+        c.QinvB_sh[j] = h.QinvB_sh[j];
+        c.tB[j] = h.tB[j];
+        c.tB_sh[j] = h.tB_sh[j];
+    }
+    fill_extk(c.bq, h, h.extBQ);
+    return c;
+}
+
 // T[item][poly 0..3][M][N]: Q limbs copied, B limbs by E1.  polys: a0 a1 b0 b1
 template <int LT, int KT, int AT>
 __global__ void k_mul_extend(const DevConsts* __restrict__ dc, const u64* const* A,
@@ -418,9 +584,13 @@ void launch_mul_extend(const DevConsts* dc, const RnsParams& P, const u64* const
                        const u64* const* B, u64* T, int items, cudaStream_t st) {
     if (!items) return;
     dispatch_shape(P, [&](auto l_, auto k_, auto a_) {
+        constexpr int LT = decltype(l_)::value;
         dim3 g = ew_grid(P.n, items);
         g.z = 4;
-        k_mul_extend<SHAPE_ARGS><<<g, EW_THREADS, 0, st>>>(dc, A, B, T);
+        if constexpr (LT > 0)
+            k_mul_extend_k<LT><<<g, EW_THREADS, 0, st>>>(make_extend_k<LT>(P), A, B, T);
+        else
+            k_mul_extend<SHAPE_ARGS><<<g, EW_THREADS, 0, st>>>(dc, A, B, T);
     });
     CSSC_CHECK_LAUNCH();
 }
@@ -500,7 +670,11 @@ void launch_mul_scale(const DevConsts* dc, const RnsParams& P, const u64* Z, u64
     dispatch_shape(P, [&](auto l_, auto k_, auto a_) {
         dim3 g = ew_grid(P.n, items);
         g.z = 3;
-        k_mul_scale<SHAPE_ARGS><<<g, EW_THREADS, 0, st>>>(dc, Z, OUT, D2);
+        constexpr int LT = decltype(l_)::value;
+        if constexpr (LT > 0)
+            k_mul_scale_k<LT><<<g, EW_THREADS, 0, st>>>(make_scale_k<LT>(P), Z, OUT, D2);
+        else
+            k_mul_scale<SHAPE_ARGS><<<g, EW_THREADS, 0, st>>>(dc, Z, OUT, D2);
     });
     CSSC_CHECK_LAUNCH();
 }
@@ -661,6 +835,80 @@ __global__ void __launch_bounds__(128, 6) k_ks_moddown(const DevConsts* __restri
     }
 }
 
+template <int L, int K>
+struct ModDownK {
+    int n;
+    u64 pk[K], phat_inv[K], phat_inv_sh[K];
+    Modulus qm[L];
+    u64 phat_q[K][L], phat_q_sh[K][L];
+    u64 Pinv_q[L], Pinv_q_sh[L];
+};
+
+// k_ks_moddown with the constants from a parameter block (same formulas)
+template <int L, int K>
+__global__ void __launch_bounds__(128, 6) k_ks_moddown_k(const __grid_constant__ ModDownK<L, K> c,
+                                                         const u64* __restrict__ ACC, const u64* const* BASE,
+                                                         const u64* const* RSRC, const u32* ginv, u64* const* OUT,
+                                                         const u64* const* EXTRA) {
+    constexpr int LK = L + K;
+    const int n = c.n;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int item = blockIdx.y;
+    const int p = blockIdx.z;
+    bool neg = false;
+    int ridx = k;
+    if (RSRC) ridx = automorph_src(ginv ? ginv[item] : 0u, k, n, neg);
+    const u64* acc = ACC + ((size_t)item * 2 + p) * LK * n;
+    u64 y[K];
+#pragma unroll
+    for (int kk = 0; kk < K; ++kk)
+        y[kk] = shoup(acc[(size_t)(L + kk) * n + k], c.phat_inv[kk], c.phat_inv_sh[kk], c.pk[kk]);
+    u64* out = OUT[item] + (size_t)p * L * n;
+    const u64* base = BASE ? BASE[item] : nullptr;
+    if (base) base += (size_t)p * L * n;
+    const u64* ex = EXTRA ? EXTRA[item] : nullptr;
+    if (ex) ex += (size_t)p * L * n;
+    const u64* rs = (RSRC && p == 0) ? RSRC[item] : nullptr;
+#pragma unroll 2
+    for (int j = 0; j < L; ++j) {
+        const u64 q = c.qm[j].q;
+        u64 v = 0;
+#pragma unroll
+        for (int kk = 0; kk < K; ++kk) v += shoup_lazy(y[kk], c.phat_q[kk][j], c.phat_q_sh[kk][j], q);
+        v = reduce_small_quot(v, c.qm[j]);
+        v = shoup(sub_mod(acc[(size_t)j * n + k], v, q), c.Pinv_q[j], c.Pinv_q_sh[j], q);
+        if (base) v = add_mod(v, base[(size_t)j * n + k], q);
+        if (ex) v = add_mod(v, ex[(size_t)j * n + k], q);
+        if (rs) {
+            const u64 r = rs[(size_t)j * n + ridx];
+            v = add_mod(v, neg ? neg_mod(r, q) : r, q);
+        }
+        out[(size_t)j * n + k] = v;
+    }
+}
+
+template <int L, int K>
+static ModDownK<L, K> make_moddown_k(const RnsParams& P) {
+    const DevConsts& h = P.host;
+    ModDownK<L, K> c{};
+    c.n = P.n;
+    for (int kk = 0; kk < K; ++kk) {
+        c.pk[kk] = h.mod[L + kk].q;
+        c.phat_inv[kk] = h.phat_inv[kk];
+        c.phat_inv_sh[kk] = h.phat_inv_sh[kk];
+        for (int j = 0; j < L; ++j) {
+            c.phat_q[kk][j] = h.phat_q[kk][j];
+            c.phat_q_sh[kk][j] = h.phat_q_sh[kk][j];
+        }
+    }
+    for (int j = 0; j < L; ++j) {
+        c.qm[j] = h.mod[j];
+        c.Pinv_q[j] = h.Pinv_q[j];
+        c.Pinv_q_sh[j] = h.Pinv_q_sh[j];
+    }
+    return c;
+}
+
 void launch_ks_moddown(const DevConsts* dc, const RnsParams& P, const u64* ACC,
                        const u64* const* BASE, const u64* const* RSRC, const u32* ginv,
                        u64* const* OUT, int items, cudaStream_t st, const u64* const* EXTRA) {
@@ -668,7 +916,12 @@ void launch_ks_moddown(const DevConsts* dc, const RnsParams& P, const u64* ACC,
     dispatch_shape(P, [&](auto l_, auto k_, auto a_) {
         dim3 g = ew_grid(P.n, items);
         g.z = 2;
-        k_ks_moddown<SHAPE_ARGS><<<g, EW_THREADS, 0, st>>>(dc, ACC, BASE, RSRC, ginv, OUT, EXTRA);
+        constexpr int LT = decltype(l_)::value, KT = decltype(k_)::value;
+        if constexpr (LT > 0)
+            k_ks_moddown_k<LT, KT><<<g, EW_THREADS, 0, st>>>(make_moddown_k<LT, KT>(P), ACC, BASE, RSRC, ginv, OUT,
+                                                            EXTRA);
+        else
+            k_ks_moddown<SHAPE_ARGS><<<g, EW_THREADS, 0, st>>>(dc, ACC, BASE, RSRC, ginv, OUT, EXTRA);
     });
     CSSC_CHECK_LAUNCH();
 }
