@@ -72,7 +72,10 @@ int spmvgpu_sync(spmvgpu_ctx* c);
 /* tuning switches: "fused_key_switch" (1 = 3-kernel fused key switch, default;
  * 0 = the 7-launch ModUp / NTT / inner product / INTT / ModDown pipeline);
  * "plan_cache" (how many cloud plans, keyed by chunk shapes, cssc_spmv_* and
- * cssc_job_* keep for reuse with their buffers and CUDA graph; default 4, 0 = off) */
+ * cssc_job_* keep for reuse with their buffers and CUDA graph; default 4, 0 = off);
+ * "forked_encrypt" (spmvgpu_encrypt_cssc as two concurrent branches, upload +
+ * pack beside the message-independent encryption, as the cached whole-
+ * evaluation graph always does; same words; default 0) */
 int spmvgpu_set_option(spmvgpu_ctx* c, const char* name, int64_t value);
 /* opaque CUDA stream the context works on (cudaStream_t) */
 void* spmvgpu_stream(spmvgpu_ctx* c);

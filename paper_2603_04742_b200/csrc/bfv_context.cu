@@ -82,6 +82,9 @@ void DevBuf::ensure(DevicePool* pool, size_t bytes) {
 GpuContext::GpuContext(const RnsConfig& cfg, int device) : P_(cfg), device_(device) {
     cuda_check(cudaSetDevice(device), "cudaSetDevice");
     cuda_check(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking), "stream");
+    cuda_check(cudaStreamCreateWithFlags(&st2_, cudaStreamNonBlocking), "stream");
+    cuda_check(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming), "event");
+    cuda_check(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming), "event");
     DevConsts host = P_.host;
     const size_t tw_bytes = sizeof(u64) * 2 * (size_t)P_.n;
     for (int i = 0; i < P_.np; ++i) {
@@ -111,6 +114,9 @@ GpuContext::~GpuContext() {
     // buffers release into pool_; pool_ destructor frees device memory
     gk_.clear();
     if (dc_) cudaFree(dc_);
+    if (ev_fork_) cudaEventDestroy(ev_fork_);
+    if (ev_join_) cudaEventDestroy(ev_join_);
+    if (st2_) cudaStreamDestroy(st2_);
     if (st_) cudaStreamDestroy(st_);
 }
 
@@ -366,9 +372,17 @@ void GpuContext::encrypt_cssc_image(const unsigned char* img, const CsscLayout& 
     unsigned char* d;
     u64 *U, *CM;
     if (ws) {
-        d = ws->up;
-        U = ws->U;
-        CM = ws->CM;
+        encrypt_cssc_forked(img, lay, *ws);
+        return;
+    } else if (forked_enc_) {
+        ensure_ws(scratch_[0], std::max<size_t>(lay.bytes, 256));
+        ClientWs w;
+        w.up = scratch_[0].as<unsigned char>();
+        w.CM = enc_workspace(items);
+        w.U = wsU_.words();
+        encrypt_cssc_forked(img, lay, w);
+        if (img == stage_) cuda_check(cudaEventRecord(stage_ev_, st_), "event");
+        return;
     } else {
         ensure_ws(scratch_[0], std::max<size_t>(lay.bytes, 256));
         d = scratch_[0].as<unsigned char>();
@@ -386,6 +400,50 @@ void GpuContext::encrypt_cssc_image(const unsigned char* img, const CsscLayout& 
                      items / 2, log_tpr, CM + (size_t)2 * P_.cfg.L * P_.n, cm_stride(), st_);
     encrypt_encoded(reinterpret_cast<const u64*>(d + lay.o_st), reinterpret_cast<u64* const*>(d + lay.o_out), items,
                     U, CM);
+}
+
+// The pipeline's encryption as two graph branches (captured from st_ and
+// st2_): the ciphertext randomness depends only on (seed, stream id), so
+//   st_ : stream ids + output pointers (16 B per item) -> sample u -> NTT(u)
+//         -> x pk + inverse block phase -> inverse columns      (c0', c1')
+//   st2_: CSR image -> device CSSC pack -> inverse NTT of the messages mod t
+// run side by side, joined by the finishing kernel (+ e0 + Delta m, + e1).
+// CM is [item][2L][N] followed by the messages [item][N]; same words as the
+// staged path.
+void GpuContext::encrypt_cssc_forked(const unsigned char* img, const CsscLayout& lay, const ClientWs& ws) {
+    const int items = lay.items, L = P_.cfg.L, logn = P_.cfg.logn;
+    const size_t n = (size_t)P_.n;
+    unsigned char* d = ws.up;
+    u64* CM = ws.CM;
+    u64* MSG = CM + (size_t)items * 2 * L * n;
+    cuda_check(cudaEventRecord(ev_fork_, st_), "fork");
+    cuda_check(cudaStreamWaitEvent(st2_, ev_fork_, 0), "fork");
+    // branch B: the CSR image, packing, message INTT
+    cuda_check(cudaMemcpyAsync(d, img, lay.o_st, cudaMemcpyHostToDevice, st2_), "upload");
+    int log_tpr = 0;
+    while (log_tpr < 5 && (lay.n_rows << log_tpr) < lay.nnz) ++log_tpr;
+    launch_pack_cssc(dc_, P_, reinterpret_cast<const int64_t*>(d + lay.o_ci),
+                     reinterpret_cast<const int64_t*>(d + lay.o_va), reinterpret_cast<const int64_t*>(d + lay.o_v),
+                     reinterpret_cast<const int4*>(d + lay.o_rows), (int)lay.n_rows,
+                     reinterpret_cast<const int2*>(d + lay.o_sl), reinterpret_cast<const int4*>(d + lay.o_cols),
+                     items / 2, log_tpr, MSG, n, st2_);
+    launch_ntt(dc_, logn, true, job(MSG, MSG, 1, {P_.t_index()}), items, st2_);
+    cuda_check(cudaEventRecord(ev_join_, st2_), "join");
+    // branch A: stream ids and output pointers, then the message-independent encryption
+    cuda_check(cudaMemcpyAsync(d + lay.o_st, img + lay.o_st, lay.bytes - lay.o_st, cudaMemcpyHostToDevice, st_),
+               "upload");
+    const auto* streams = reinterpret_cast<const u64*>(d + lay.o_st);
+    launch_enc_sample_u(dc_, P_, P_.cfg.seed, streams, ws.U, items, st_);
+    launch_ntt_phase(dc_, logn, false, true, job(ws.U, ws.U, L, range_idx(0, L)), items, st_);
+    launch_blocks_mul_inv(dc_, P_, ws.U, pk_.words(), 2, CM, (size_t)2 * L * n, nullptr, 0, 0, items, st_);
+    std::vector<int> pidx = range_idx(0, L);
+    pidx.insert(pidx.end(), pidx.begin(), pidx.end());
+    launch_ntt_phase(dc_, logn, true, true, job(CM, CM, 2 * L, pidx), items, st_);
+    cuda_check(cudaStreamWaitEvent(st_, ev_join_, 0), "join");
+    launch_enc_finish(dc_, P_, P_.cfg.seed, streams, CM, reinterpret_cast<u64* const*>(d + lay.o_out), items, st_,
+                      MSG, (size_t)2 * L * n, n);
+    stats_.kernels += 8;
+    stats_.limb_ntts += (u64)items * (1 + 3 * L);
 }
 
 // CM = wsC_[item][2L+1][N] holds the encoded messages in limb 2L on entry;

@@ -97,6 +97,7 @@ public:
     // fused 3-kernel key switch (default) or the 7-launch reference pipeline
     void set_fused_key_switch(bool on) { fused_ks_ = on; }
     bool fused_key_switch() const { return fused_ks_; }
+    void set_forked_encrypt(bool on) { forked_enc_ = on; }
 
     // keys (NTT form on device)
     const u64* relin_key() const { return rlk_.words(); }
@@ -181,6 +182,7 @@ private:
     unsigned char* stage_host(size_t bytes);
     void* stage_upload(size_t bytes, int slot);
     DevBuf gen_ksk(u64 keyid, const u64* sp_ntt);
+    void encrypt_cssc_forked(const unsigned char* img, const CsscLayout& lay, const ClientWs& ws);
     void ensure_ws(DevBuf& b, size_t bytes) { b.ensure(&pool_, bytes); }
 
     RnsParams P_;
@@ -195,6 +197,7 @@ private:
     std::atomic<uint64_t> stream_counter_{1};
     LaunchStats stats_;
     bool fused_ks_ = true;
+    bool forked_enc_ = false;
     // workspaces for ad-hoc batched calls
     DevBuf wsT_, wsZ_, wsD2_, wsDX_, wsACC_, wsM_, wsX_, wsU_, wsC_, wsPT_;
     DevBuf scratch_[8];
@@ -202,6 +205,10 @@ private:
     unsigned char* stage_ = nullptr;  // pinned
     size_t stage_bytes_ = 0;
     cudaEvent_t stage_ev_ = nullptr;
+    // side stream + fork/join events: the pipeline's encryption runs its
+    // message-independent part beside the upload and packing
+    cudaStream_t st2_ = nullptr;
+    cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
     std::mutex mu_;
 };
 

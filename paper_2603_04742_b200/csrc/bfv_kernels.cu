@@ -1126,7 +1126,8 @@ void launch_enc_pk(const DevConsts* dc, const RnsParams& P, const u64* PK, const
 // blocks of its 128 coefficients (4 lanes per block), then one thread per
 // coefficient finishes every limb with coalesced loads and stores
 __global__ void __launch_bounds__(128) k_enc_finish(const DevConsts* __restrict__ dc, u64 seed,
-                                                    const u64* streams, const u64* C, u64* const* OUT) {
+                                                    const u64* streams, const u64* C, size_t cstride,
+                                                    const u64* MSG, size_t mstride, u64* const* OUT) {
     __shared__ u32 blk[32][16];
     const int n = dc->n, L = dc->L;
     const int item = blockIdx.y;
@@ -1137,8 +1138,8 @@ __global__ void __launch_bounds__(128) k_enc_finish(const DevConsts* __restrict_
     __syncthreads();
     const int kk = threadIdx.x, k = blockIdx.x * 128 + kk;
     const int64_t e0 = cbd_of(word64(blk[kk >> 3], kk & 7)), e1 = cbd_of(word64(blk[16 + (kk >> 3)], kk & 7));
-    const size_t cm = (size_t)item * (2 * L + 1) * n + k;
-    const u64 m = C[cm + (size_t)2 * L * n];
+    const size_t cm = (size_t)item * cstride + k;
+    const u64 m = MSG[(size_t)item * mstride + k];
     u64* out = OUT[item];
     for (int j = 0; j < L; ++j) {
         const u64 q = dc->mod[j].q;
@@ -1153,9 +1154,16 @@ __global__ void __launch_bounds__(128) k_enc_finish(const DevConsts* __restrict_
 }
 
 void launch_enc_finish(const DevConsts* dc, const RnsParams& P, u64 seed, const u64* streams,
-                       const u64* CM, u64* const* OUT, int items, cudaStream_t st) {
+                       const u64* CM, u64* const* OUT, int items, cudaStream_t st, const u64* MSG, size_t cstride,
+                       size_t mstride) {
     if (!items) return;
-    k_enc_finish<<<dim3((unsigned)(P.n / 128), (unsigned)items), 128, 0, st>>>(dc, seed, streams, CM, OUT);
+    if (!cstride) cstride = (size_t)(2 * P.cfg.L + 1) * P.n;
+    if (!MSG) {
+        MSG = CM + (size_t)2 * P.cfg.L * P.n;
+        mstride = cstride;
+    }
+    k_enc_finish<<<dim3((unsigned)(P.n / 128), (unsigned)items), 128, 0, st>>>(dc, seed, streams, CM, cstride, MSG,
+                                                                               mstride, OUT);
     CSSC_CHECK_LAUNCH();
 }
 

@@ -101,9 +101,12 @@ void launch_enc_sample_u(const DevConsts* dc, const RnsParams& P, u64 seed, cons
                          u64* U, int items, cudaStream_t st);
 void launch_enc_pk(const DevConsts* dc, const RnsParams& P, const u64* PK, const u64* U, u64* C,
                    int items, cudaStream_t st);
-// CM[item][2L+1][N]: c0 (L limbs), c1 (L limbs), then the message (coef form mod t)
+// CM[item][2L+1][N]: c0 (L limbs), c1 (L limbs), then the message (coef form mod t);
+// or, with MSG set, CM items cstride words apart and the messages in MSG
+// (mstride words apart)
 void launch_enc_finish(const DevConsts* dc, const RnsParams& P, u64 seed, const u64* streams,
-                       const u64* CM, u64* const* OUT, int items, cudaStream_t st);
+                       const u64* CM, u64* const* OUT, int items, cudaStream_t st, const u64* MSG = nullptr,
+                       size_t cstride = 0, size_t mstride = 0);
 void launch_mul_s(const DevConsts* dc, const RnsParams& P, u64* X, const u64* S_NTT, int items,
                   cudaStream_t st);
 void launch_dec_scale(const DevConsts* dc, const RnsParams& P, const u64* const* CT,

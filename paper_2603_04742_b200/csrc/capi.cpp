@@ -3,6 +3,8 @@
 // protocol front door (cssc_*) wraps the host C++ spmv layer, which itself
 // talks to the device only through spmvgpu_*.  No exception crosses the ABI.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstring>
 #include <list>
 #include <memory>
@@ -419,6 +421,8 @@ int spmvgpu_set_option(spmvgpu_ctx* c, const char* name, int64_t value) {
         const std::string n = name ? name : "";
         if (n == "fused_key_switch") {
             G(c).set_fused_key_switch(value != 0);
+        } else if (n == "forked_encrypt") {
+            G(c).set_forked_encrypt(value != 0);
         } else if (n == "plan_cache") {
             if (value < 0) throw std::invalid_argument("plan_cache: capacity must be >= 0");
             std::list<spmv::detail::PlanLease> evicted;
@@ -765,11 +769,20 @@ int cssc_spmv_batch(spmvgpu_ctx* c, const cssc_csr* ms, const int64_t* const* vs
                     int key_holder, int64_t* const* values, cssc_result* res) {
     return guard([&] { auto lk_ = api_lock(c);
         G(c);
+        static const bool trace = std::getenv("CSSC_TRACE_E2E") != nullptr;
+        const auto t0 = std::chrono::steady_clock::now();
         std::vector<spmv::detail::CsrView> w;
         for (size_t i = 0; i < nmat; ++i) w.push_back(view_of(ms[i], vs[i]));
         spmv::detail::BatchedSpmv job(c, c->hp, w, chunk_size, static_cast<spmv::PartyRole>(key_holder));
+        const auto t1 = std::chrono::steady_clock::now();
         const auto r = job.run_all();
+        const auto t2 = std::chrono::steady_clock::now();
         for (size_t i = 0; i < nmat; ++i) fill_result(r[i], values ? values[i] : nullptr, res ? res + i : nullptr, nullptr, 0);
+        if (trace) {
+            const auto t3 = std::chrono::steady_clock::now();
+            auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+            std::fprintf(stderr, "e2e-trace pack %.1f run %.1f fill %.1f us\n", us(t0, t1), us(t1, t2), us(t2, t3));
+        }
     });
 }
 

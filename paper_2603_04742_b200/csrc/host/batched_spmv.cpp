@@ -1,6 +1,9 @@
 // batched_spmv.cpp -- see batched_spmv.hpp.
 #include "batched_spmv.hpp"
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <algorithm>
 #include <cstring>
 #include <climits>
@@ -289,6 +292,8 @@ std::vector<SpmvResult> BatchedSpmv::run_all() {
         cloud(false);
         return finish();
     }
+    static const bool trace = std::getenv("CSSC_TRACE_E2E") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
     ensure_plan();
     if (!pipeline_ready(lease_, img_)) pipeline_prepare(ctx_, lease_, img_);
     if (img_.p != lease_.pimg) std::memcpy(lease_.pimg, img_.p, img_.bytes);
@@ -297,8 +302,14 @@ std::vector<SpmvResult> BatchedSpmv::run_all() {
     client_image_fill(ctx_, lease_.pimg, img_, all.data());
     encrypted_ = true;
     h2d_ = img_.bytes;
+    const auto t1 = std::chrono::steady_clock::now();
     pipeline_run(ctx_, lease_);
+    const auto t2 = std::chrono::steady_clock::now();
     ++lease_.uses;
+    if (trace) {
+        auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+        std::fprintf(stderr, "e2e-trace prepare %.1f graph+sync %.1f us\n", us(t0, t1), us(t1, t2));
+    }
     const std::size_t S = hp_.slot_count;
     std::vector<std::uint64_t> slots(n_out_ * S);
     std::vector<std::int32_t> measured(n_out_, 0);

@@ -86,3 +86,23 @@ def test_device_pack_rejects_bad_descriptors(ctx):
         ctx.encrypt_cssc(ci, m.values, v, rows_d, slices_d, cols_d, n)
     with pytest.raises(pk.SpmvError):
         ctx.encrypt_cssc(m.col_indices, m.values, v, rows_d, slices_d, cols_d, 0)
+
+
+@pytest.mark.parametrize("logn,seed", [(11, 1), (14, 2)])
+def test_forked_encryption_gives_the_staged_words(logn, seed):
+    """The two-branch encryption of the cached whole-evaluation graph (upload +
+    pack beside the message-independent part, bfv_context.cu
+    encrypt_cssc_forked) produces the staged path's ciphertext words: two
+    contexts with the same seed hand out the same stream ids."""
+    a, b = pk.Context(logn=logn, seed=4), pk.Context(logn=logn, seed=4)
+    b.set_option("forked_encrypt", 1)
+    m = pk.random_sparse_csr(200, 150, 900, seed, -8, 8)
+    v = pk.random_vector(150, seed, -8, 8)
+    rows_d, slices_d, cols_d, r_list, _ = descriptors(m, a.slots)
+    n = len(r_list)
+    ca = a.encrypt_cssc(m.col_indices, m.values, v, rows_d, slices_d, cols_d, n)
+    cb = b.encrypt_cssc(m.col_indices, m.values, v, rows_d, slices_d, cols_d, n)
+    for x, y in zip(ca, cb):
+        assert np.array_equal(a.download(int(x)), b.download(int(y)))
+    a.close()
+    b.close()
