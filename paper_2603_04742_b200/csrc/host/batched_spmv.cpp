@@ -49,6 +49,8 @@ BatchedSpmv::BatchedSpmv(spmvgpu_ctx* ctx, const HeParams& hp, std::span<const C
                          std::size_t chunk_size, PartyRole key_holder, bool partition, int rank, int world)
     : ctx_(ctx), hp_(hp), kh_(key_holder), nmat_(ms.size()), rank_(rank), world_(world) {
     if (world < 1 || rank < 0 || rank >= world) throw std::invalid_argument("shard: rank must be in [0, world)");
+    static const bool trace = std::getenv("CSSC_TRACE_E2E") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
     std::size_t nnz_total = 0, vec_total = 0;
     for (const CsrView& m : ms) {
         nnz_total += m.nnz;
@@ -60,13 +62,24 @@ BatchedSpmv::BatchedSpmv(spmvgpu_ctx* ctx, const HeParams& hp, std::span<const C
     for (std::size_t mi = 0; mi < ms.size(); ++mi) {
         const CsrView& m = ms[mi];
         if (m.rows && m.row_ptrs[0] != 0) throw std::invalid_argument("csr: row_ptrs[0] must be 0");
-        for (std::size_t i = 0; i < m.rows; ++i)
-            if (m.row_ptrs[i + 1] < m.row_ptrs[i]) throw std::invalid_argument("csr: row_ptrs must be non-decreasing");
+        {  // branch-free scans (vectorised); the offending entry is located only on failure
+            bool dec = false;
+            for (std::size_t i = 0; i < m.rows; ++i) dec |= m.row_ptrs[i + 1] < m.row_ptrs[i];
+            if (dec) throw std::invalid_argument("csr: row_ptrs must be non-decreasing");
+        }
         if (m.rows && m.row_ptrs[m.rows] != m.nnz) throw std::invalid_argument("csr: row_ptrs end is not nnz");
-        for (std::size_t k = 0; k < m.nnz; ++k)
-            if (m.col_indices[k] >= m.cols)
-                throw IndexOutOfRangeError("csr: column index " + std::to_string(m.col_indices[k]) +
-                                           " out of range for " + std::to_string(m.cols) + " columns");
+        {  // all col < cols: every col - cols is negative (and no col has bit 63 set)
+            std::uint64_t all_neg = ~std::uint64_t{0}, any_top = 0;
+            for (std::size_t k = 0; k < m.nnz; ++k) {
+                all_neg &= m.col_indices[k] - m.cols;
+                any_top |= m.col_indices[k];
+            }
+            if (m.nnz && (!(all_neg >> 63) || (any_top >> 63)))
+                for (std::size_t k = 0; k < m.nnz; ++k)
+                    if (m.col_indices[k] >= m.cols)
+                        throw IndexOutOfRangeError("csr: column index " + std::to_string(m.col_indices[k]) +
+                                                   " out of range for " + std::to_string(m.cols) + " columns");
+        }
         const std::int64_t nz_base = nz_next, vec_base = vec_next;
         nz_next += static_cast<std::int64_t>(m.nnz);
         vec_next += static_cast<std::int64_t>(m.cols);
@@ -102,6 +115,7 @@ BatchedSpmv::BatchedSpmv(spmvgpu_ctx* ctx, const HeParams& hp, std::span<const C
     key.insert(key.end(), dr_.begin(), dr_.end());
     key.insert(key.end(), dc_.begin(), dc_.end());
     key.insert(key.end(), dslice_.begin(), dslice_.end());
+    const auto t1 = std::chrono::steady_clock::now();
     const bool hit = plan_cache_take(ctx_, key, lease_);
     // the client upload image, written once straight from the callers' arrays:
     // into the cached pipeline's own pinned buffer when its layout matches
@@ -131,6 +145,11 @@ BatchedSpmv::BatchedSpmv(spmvgpu_ctx* ctx, const HeParams& hp, std::span<const C
         std::vector<std::int32_t>().swap(rowrec_);
         std::vector<std::int32_t>().swap(slicerec_);
         std::vector<std::int32_t>().swap(colrec_);
+    }
+    if (trace) {
+        const auto t2 = std::chrono::steady_clock::now();
+        auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+        std::fprintf(stderr, "e2e-trace shapes %.1f image %.1f us\n", us(t0, t1), us(t1, t2));
     }
     if (hit) return;
     lease_.key = std::move(key);
@@ -165,40 +184,62 @@ void BatchedSpmv::add_slice(const CsrView& m, std::size_t mat, std::size_t r0, s
     const std::uint64_t* rp = m.row_ptrs + r0;
     std::size_t max_len = 0;
     for (std::size_t i = 0; i < s.rows; ++i) max_len = std::max<std::size_t>(max_len, rp[i + 1] - rp[i]);
-    std::vector<std::size_t> bucket(max_len + 2, 0);
+    // histogram of the lengths, slot max_len - len + 1 (descending order);
+    // height[j] = #rows longer than j is its suffix sum
+    std::vector<std::uint32_t> bucket(max_len + 2, 0);
     for (std::size_t i = 0; i < s.rows; ++i) ++bucket[max_len - (rp[i + 1] - rp[i]) + 1];
-    std::partial_sum(bucket.begin(), bucket.end(), bucket.begin());
-    s.row_map.resize(s.rows);
-    for (std::size_t i = 0; i < s.rows; ++i) s.row_map[bucket[max_len - (rp[i + 1] - rp[i])]++] = i;
     std::vector<std::size_t> height(max_len, 0);
-    for (std::size_t i = 0; i < s.rows; ++i)
-        if (rp[i + 1] > rp[i]) ++height[rp[i + 1] - rp[i] - 1];
-    for (std::size_t j = max_len; j-- > 1;) height[j - 1] += height[j];
+    for (std::size_t acc = 0, len = max_len; len >= 1; --len) {
+        acc += bucket[max_len - len + 1];
+        height[len - 1] = acc;
+    }
     if (max_len && height[0] > budget)
         throw ColumnTooTallError("generate_chunks: aligned column 0 has height " + std::to_string(height[0]) +
                                  " > budget " + std::to_string(budget) + "; partition the rows first");
+    std::partial_sum(bucket.begin(), bucket.end(), bucket.begin());
+    // stable counting sort (the CSSC row order) and, in the same pass, the
+    // device row records {nz_begin, len, pos, slice} of the non-empty rows,
+    // which take the first height[0] positions
+    const std::size_t nonempty = max_len ? height[0] : 0;
+    const auto sidx = static_cast<std::int32_t>(slicerec_.size() / 2);
+    const std::size_t rw0 = rowrec_.size();
+    rowrec_.resize(rw0 + 4 * nonempty);
+    std::int32_t* rr = rowrec_.data() + rw0;
+    s.row_map.resize(s.rows);
+    for (std::size_t i = 0; i < s.rows; ++i) {
+        const std::size_t len = rp[i + 1] - rp[i];
+        const std::uint32_t p = bucket[max_len - len]++;
+        s.row_map[p] = i;
+        if (len) {
+            rr[4 * p] = static_cast<std::int32_t>(nz_base + static_cast<std::int64_t>(rp[i]));
+            rr[4 * p + 1] = static_cast<std::int32_t>(len);
+            rr[4 * p + 2] = static_cast<std::int32_t>(p);
+            rr[4 * p + 3] = sidx;
+        }
+    }
     s.first_chunk = r_.size();
     const auto col_base = static_cast<std::int32_t>(colrec_.size() / 4);
-    for (std::size_t first = 0; first < max_len;) {
-        const std::size_t h = height[first];
-        const std::size_t fit = std::min<std::size_t>(budget / h, max_len - first);
-        const auto chunk = static_cast<std::int32_t>(r_.size());
-        for (std::size_t k = 0; k < fit; ++k)
-            colrec_.insert(colrec_.end(), {chunk, static_cast<std::int32_t>(k), static_cast<std::int32_t>(h), 0});
-        r_.push_back(h);
-        c_.push_back(fit);
-        first += fit;
+    {
+        std::size_t cw = colrec_.size();
+        colrec_.resize(cw + 4 * max_len);
+        std::int32_t* cr = colrec_.data();
+        for (std::size_t first = 0; first < max_len;) {
+            const std::size_t h = height[first];
+            const std::size_t fit = std::min<std::size_t>(budget / h, max_len - first);
+            const auto chunk = static_cast<std::int32_t>(r_.size());
+            for (std::size_t k = 0; k < fit; ++k, cw += 4) {
+                cr[cw] = chunk;
+                cr[cw + 1] = static_cast<std::int32_t>(k);
+                cr[cw + 2] = static_cast<std::int32_t>(h);
+                cr[cw + 3] = 0;
+            }
+            r_.push_back(h);
+            c_.push_back(fit);
+            first += fit;
+        }
     }
     s.n_ct = r_.size() - s.first_chunk;
-    const auto sidx = static_cast<std::int32_t>(slicerec_.size() / 2);
     slicerec_.insert(slicerec_.end(), {col_base, static_cast<std::int32_t>(vec_base)});
-    for (std::size_t p = 0; p < s.rows; ++p) {
-        const std::size_t i = s.row_map[p];
-        const std::size_t len = rp[i + 1] - rp[i];
-        if (len)
-            rowrec_.insert(rowrec_.end(), {static_cast<std::int32_t>(nz_base + static_cast<std::int64_t>(rp[i])),
-                                           static_cast<std::int32_t>(len), static_cast<std::int32_t>(p), sidx});
-    }
     if (s.n_ct) s.result = static_cast<int>(n_out_++);
     for (std::size_t i = 0; i < s.n_ct; ++i) slice_id_.push_back(static_cast<std::uint32_t>(s.result));
     slices_.push_back(std::move(s));
