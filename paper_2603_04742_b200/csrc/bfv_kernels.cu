@@ -1219,6 +1219,116 @@ void launch_dec_scale(const DevConsts* dc, const RnsParams& P, const u64* const*
     CSSC_CHECK_LAUNCH();
 }
 
+// Decryption's t/Q scaling fused into the column phase of the forward NTT
+// mod t (the decode): one CTA per (slice, column tile) reads the L residues of
+// d = c0 + c1 s (coefficient form, D[slice][L][N]) at each of its tile's
+// coefficients, computes m = round(t d / Q) mod t (E5, as k_dec_scale) and the
+// largest rounding distance, then runs the column phase mod t and stores the
+// tile like k_ntt_cols; k_ntt_blocks finishes the transform.
+template <int LOGN, int LN>
+__global__ void __launch_bounds__(Ntt2<LOGN>::TC) k_dec_cols(const DevConsts* __restrict__ dc, const u64* __restrict__ D,
+                                                             u64* __restrict__ M, unsigned long long* maxdev) {
+    using G = Ntt2<LOGN>;
+    constexpr int T = G::TC;
+    constexpr int CTAS = G::R2 / LN;
+    constexpr int SEG = LN / 2;
+    extern __shared__ u64 smem[];
+    u64* tile = smem;
+    u64* tws = smem + LN * G::R1;
+    const int tileid = blockIdx.x % CTAS;
+    const int item = blockIdx.x / CTAS;
+    const int L = dc->L;
+    const int tp = dc->np - 1;
+    const u64 t = dc->t;
+    const int col0 = tileid * LN;
+    const u64* tw = dc->tw[tp].fwd;
+    for (int i = threadIdx.x; i < G::R1; i += T) cp_async16(tws + 2 * i, tw + 2 * i);
+    const u64* d = D + (size_t)item * L * G::N;
+    unsigned long long ad_max = 0;
+    constexpr int PER = G::R1 * LN / T;
+#pragma unroll 4
+    for (int r = 0; r < PER; ++r) {
+        const int e = threadIdx.x + T * r, c = e / LN, jl = e % LN;
+        const int k = c * G::R2 + col0 + jl;
+        u64 shi = 0, slo = 0;
+        for (int i = 0; i < L; ++i) {
+            const u64 q = dc->mod[i].q;
+            const u64 xi = shoup(__ldg(d + (size_t)i * G::N + k), dc->QhatInv[i], dc->QhatInv_sh[i], q);
+            add128(shi, slo, umulhi(xi, dc->T1[i]), xi * dc->T1[i]);
+            add128(shi, slo, 0, umulhi(xi, dc->T0[i]));
+        }
+        tile[c * LN + jl] = (shi + (slo >> 63)) % t;
+        const int64_t dv = (int64_t)slo;
+        const unsigned long long ad = dv < 0 ? (unsigned long long)0 - (unsigned long long)dv : (unsigned long long)dv;
+        ad_max = ad > ad_max ? ad : ad_max;
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+        const unsigned long long o = __shfl_xor_sync(0xffffffffu, ad_max, off);
+        ad_max = o > ad_max ? o : ad_max;
+    }
+    if ((threadIdx.x & 31) == 0) atomicMax(maxdev + item, ad_max);
+    cp_async_wait_all();
+    __syncthreads();
+    auto addr = [](int l, int pos) { return pos * LN + l; };
+    auto twf = [&](int sl, int, int blk) {
+        const int kk = (1 << sl) + blk;
+        return make_ulonglong2(tws[2 * kk], tws[2 * kk + 1]);
+    };
+    line_ntt_v<G::A, 0, false, 3, LN>(tile, ConstQ{dc->mod[tp].q}, addr, twf, whole_cta());
+    u64* dst = M + (size_t)item * G::N;
+#pragma unroll
+    for (int r = 0; r < G::R1 * SEG / T; ++r) {
+        const int i = threadIdx.x + T * r, c = i / SEG, h = i % SEG;
+        *reinterpret_cast<ulonglong2*>(dst + (size_t)c * G::R2 + col0 + 2 * h) =
+            make_ulonglong2(tile[c * LN + 2 * h], tile[c * LN + 2 * h + 1]);
+    }
+}
+
+template <int LOGN>
+static void dec_ntt_t(const DevConsts* dc, const RnsParams& P, u64* D, u64* M, u64* slots,
+                      unsigned long long* maxdev, int items, cudaStream_t st) {
+    using G = Ntt2<LOGN>;
+    const int L = P.cfg.L;
+    NttJob jd;
+    jd.src = D;
+    jd.dst = D;
+    jd.limbs = L;
+    for (int i = 0; i < L; ++i) jd.pidx[i] = (signed char)i;
+    launch_ntt_phase(dc, LOGN, true, true, jd, items, st);  // inverse column phase of d
+    cudaMemsetAsync(maxdev, 0, sizeof(unsigned long long) * items, st);
+    constexpr int LN = 8;
+    const int smem = (LN * G::R1 + 2 * G::R1) * 8;
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(k_dec_cols<LOGN, LN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        configured = true;
+    }
+    k_dec_cols<LOGN, LN><<<items * (G::R2 / LN), G::TC, smem, st>>>(dc, D, M, maxdev);
+    CSSC_CHECK_LAUNCH();
+    NttJob jm;
+    jm.src = M;
+    jm.dst = M;
+    jm.limbs = 1;
+    jm.pidx[0] = (signed char)P.t_index();
+    launch_ntt_phase(dc, LOGN, false, false, jm, items, st);  // forward block phase mod t
+    launch_decode_gather(dc, P, M, slots, items, st);
+}
+
+// D (d = c0 + c1 s after the inverse block phase) -> slots, see k_dec_cols
+void launch_decrypt_ntt(const DevConsts* dc, const RnsParams& P, u64* D, u64* M, u64* slots,
+                        unsigned long long* maxdev, int items, cudaStream_t st) {
+    if (!items) return;
+    switch (P.cfg.logn) {
+        case 10: dec_ntt_t<10>(dc, P, D, M, slots, maxdev, items, st); break;
+        case 11: dec_ntt_t<11>(dc, P, D, M, slots, maxdev, items, st); break;
+        case 12: dec_ntt_t<12>(dc, P, D, M, slots, maxdev, items, st); break;
+        case 13: dec_ntt_t<13>(dc, P, D, M, slots, maxdev, items, st); break;
+        case 14: dec_ntt_t<14>(dc, P, D, M, slots, maxdev, items, st); break;
+        case 15: dec_ntt_t<15>(dc, P, D, M, slots, maxdev, items, st); break;
+        default: throw std::invalid_argument("decrypt: unsupported logn");
+    }
+}
+
 __global__ void k_decode_gather(const DevConsts* __restrict__ dc, const u64* M, u64* slots) {
     const int S = dc->n / 2;
     const int j = blockIdx.x * blockDim.x + threadIdx.x;

@@ -49,6 +49,13 @@ void launch_mul_extend(const DevConsts* dc, const RnsParams& P, const u64* const
                        const u64* const* B, u64* T, int items, cudaStream_t st);
 // fused forward block phase + mask multiply-accumulate + inverse block phase
 // (mul_fused.cu); OUT[s] receives the slice sums before the inverse column phase
+// the pipeline's decrypting mask step: D[slice][L][N] = c0 + c1 s (see mul_fused.cu)
+void launch_mask_dec_blocks(const DevConsts* dc, const RnsParams& P, const u64* MT, const int* slice_off,
+                            const int* slice_items, const int* item_mask, const u64* MASKS, const u64* S_NTT,
+                            u64* D, int slices, cudaStream_t st);
+// D -> inverse column phase -> t/Q scale + decode NTT mod t -> slots (maxdev per item)
+void launch_decrypt_ntt(const DevConsts* dc, const RnsParams& P, u64* D, u64* M, u64* slots,
+                        unsigned long long* maxdev, int items, cudaStream_t st);
 void launch_mask_blocks(const DevConsts* dc, const RnsParams& P, const u64* MT, const int* slice_off,
                         const int* slice_items, const int* item_mask, const u64* MASKS, u64* const* OUT,
                         int slices, cudaStream_t st);

@@ -270,7 +270,7 @@ CloudPlan::~CloudPlan() {
     if (graph_) cudaGraphDestroy(graph_);
 }
 
-void CloudPlan::record(std::vector<cudaEvent_t>* marks) {
+void CloudPlan::record(std::vector<cudaEvent_t>* marks, u64* dec_d) {
     if (n_ == 0) return;
     const RnsParams& P = ctx_.params();
     const int L = P.cfg.L, logn = P.cfg.logn;
@@ -303,7 +303,11 @@ void CloudPlan::record(std::vector<cudaEvent_t>* marks) {
     fwd.src_items = FINAL_;
     NttJob inv = ctx_.job(nullptr, nullptr, 2 * L, qidx);
     inv.dst_items = OUT_;
-    if (ctx_.fused_key_switch()) {  // column phase, fused blocks + mask MAC + inverse blocks, column phase
+    if (dec_d) {  // column phase, fused blocks + mask MAC + (c0 + c1 s) + inverse blocks
+        launch_ntt_phase(ctx_.dconsts(), logn, false, true, fwd, n_, st);
+        launch_mask_dec_blocks(ctx_.dconsts(), P, MT_.words(), slice_off_, slice_items_, item_mask_,
+                               MASKS_.words(), ctx_.s_ntt(), dec_d, ns_, st);
+    } else if (ctx_.fused_key_switch()) {  // column phase, fused blocks + mask MAC + inverse blocks, column phase
         launch_ntt_phase(ctx_.dconsts(), logn, false, true, fwd, n_, st);
         launch_mask_blocks(ctx_.dconsts(), P, MT_.words(), slice_off_, slice_items_, item_mask_, MASKS_.words(),
                            OUT_, ns_, st);
@@ -435,8 +439,13 @@ void CloudPlan::capture_pipeline(const unsigned char* img, const CsscLayout& lay
     cuda_check(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "begin capture");
     try {
         ctx_.encrypt_cssc_image(img, lay, &ws);
-        record();
-        ctx_.decrypt_dev(OUT_, ns_, ws.X, ws.M, ws.slots, maxdev);
+        if (ctx_.fused_key_switch()) {  // decryption fused into the mask step (k_mask_dec_blocks)
+            record(nullptr, ws.X);
+            launch_decrypt_ntt(ctx_.dconsts(), P, ws.X, ws.M, ws.slots, maxdev, ns_, st);
+        } else {
+            record();
+            ctx_.decrypt_dev(OUT_, ns_, ws.X, ws.M, ws.slots, maxdev);
+        }
         cuda_check(cudaMemcpyAsync(out, ws.slots, sizeof(u64) * (size_t)ns_ * (n / 2) + 8 * (size_t)ns_,
                                    cudaMemcpyDeviceToHost, st),
                    "download");

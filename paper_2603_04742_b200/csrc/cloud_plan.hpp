@@ -61,7 +61,9 @@ public:
     const PlanStats& stats() const { return stats_; }
 
 private:
-    void record(std::vector<cudaEvent_t>* marks = nullptr);
+    // dec_d: the pipeline's decrypting tail (fused path): the mask step writes
+    // d = c0 + c1 s per slice into dec_d ([ns][L][N]) instead of the result cts
+    void record(std::vector<cudaEvent_t>* marks = nullptr, u64* dec_d = nullptr);
     template <class T>
     T* put(const std::vector<T>& v);
 

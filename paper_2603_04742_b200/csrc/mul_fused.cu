@@ -194,6 +194,142 @@ __global__ void __launch_bounds__(2 * kGroupThreads) k_mask_blocks(const DevCons
     }
 }
 
+// The pipeline's decrypting variant of k_mask_blocks: for one slice, one
+// prime j < L and one tile, group 0 sums the c0 limb and group 1 the c1 limb
+// of every chunk (block phase x mask), then d = c0 + c1 s (s in NTT form,
+// the key holder's decryption product, done where c1 already is in the NTT
+// domain) goes through the inverse block phase into D[slice][j].  The
+// inverse column phase of D and the t/Q scaling follow (k_dec_cols).  The
+// slice's result ciphertext is never materialised: the pipeline returns only
+// its decryption, and d mod q_j is the same residue c0 + INTT(NTT(c1) s)
+// gives, so the slots are unchanged.
+template <int LOGN, int LN = 16>
+__global__ void __launch_bounds__(2 * kGroupThreads) k_mask_dec_blocks(const DevConsts* __restrict__ dc,
+                                                                       const u64* __restrict__ MT,
+                                                                       const int* __restrict__ slice_off,
+                                                                       const int* __restrict__ slice_items,
+                                                                       const int* __restrict__ item_mask,
+                                                                       const u64* __restrict__ MASKS,
+                                                                       const u64* __restrict__ S_NTT,
+                                                                       u64* __restrict__ D) {
+    using G = Ntt2<LOGN>;
+    extern __shared__ u64 smem[];
+    constexpr int PITCH = G::PITCH;
+    constexpr int TW = LN * PITCH;
+    constexpr int NG = 2;  // group 0: c0, group 1: c1
+    constexpr int NT = NG * kGroupThreads;
+    constexpr int PERG = LN * G::R2 / kGroupThreads;
+    constexpr int PER = LN * G::R2 / NT;
+    constexpr int CTAS = G::R1 / LN;
+    u64* work = smem;
+    u64* acc = smem + NG * TW;
+    u64* tws = smem + 2 * NG * TW;
+    const int L = dc->L;
+    int bid = blockIdx.x;
+    const int tileid = bid % CTAS;
+    bid /= CTAS;
+    const int j = bid % L;
+    const int sl = bid / L;
+    const Modulus md = dc->mod[j];
+    const u64 q = md.q;
+    const int blk0 = tileid * LN;
+    const size_t base = (size_t)blk0 * G::R2;
+    const int grp = threadIdx.x / kGroupThreads;
+    const ThreadGroup tg = cta_slice(grp, NG);
+    const int j2 = grp * L + j;
+    u64* wk = work + grp * TW;
+    u64* ac = acc + grp * TW;
+    auto saddr = [](int x) { return (x >> G::B) * PITCH + (x & (G::R2 - 1)); };
+    auto addr = [](int l, int pos) { return l * PITCH + pos; };
+    auto twf = [&](int sl_, int l, int blk) { return block_tw<LOGN, LN>(tws, sl_, l, blk); };
+    load_block_twiddles<LOGN, LN>(tws, dc->tw[j].fwd, blk0);
+    cp_async_wait_all();
+    __syncthreads();
+    const int b = slice_off[sl], e = slice_off[sl + 1];
+    bool any = false;
+#pragma unroll 1
+    for (int x = b; x < e; ++x) {
+        const int it = slice_items[x];
+        const u64* src = MT + ((size_t)it * 2 * L + j2) * G::N + base;
+#pragma unroll
+        for (int r = 0; r < PERG; ++r) {
+            const int y = tg.tid + kGroupThreads * r;
+            cp_async8(wk + saddr(y), src + y);
+        }
+        cp_async_wait_all();
+        tg.sync();
+        line_ntt_v<G::B, 0, false, 4, LN>(wk, ConstQ{q}, addr, twf, tg);
+        const u64* mk = MASKS + ((size_t)item_mask[it] * L + j) * G::N + base;
+#pragma unroll
+        for (int r = 0; r < PERG; ++r) {
+            const int y = tg.tid + kGroupThreads * r, s0 = saddr(y);
+            const u64 p = mul_mod(wk[s0], __ldg(mk + y), md);
+            ac[s0] = any ? add_mod(ac[s0], p, q) : p;
+        }
+        any = true;
+        tg.sync();
+    }
+    if (!any)
+#pragma unroll
+        for (int r = 0; r < PERG; ++r) ac[saddr(tg.tid + kGroupThreads * r)] = 0;
+    __syncthreads();
+    const u64* sk = S_NTT + (size_t)j * G::N + base;
+#pragma unroll
+    for (int r = 0; r < PER; ++r) {
+        const int y = threadIdx.x + NT * r, s0 = saddr(y);
+        acc[s0] = add_mod(acc[s0], mul_mod(acc[TW + s0], __ldg(sk + y), md), q);
+    }
+    __syncthreads();
+    load_block_twiddles<LOGN, LN>(tws, dc->tw[j].inv, blk0);
+    cp_async_wait_all();
+    __syncthreads();
+    line_ntt_v<G::B, 0, true, 4, LN>(acc, ConstQ{q}, addr, twf, whole_cta());
+    u64* dst = D + ((size_t)sl * L + j) * G::N + base;
+#pragma unroll
+    for (int r = 0; r < PER; ++r) {
+        const int y = threadIdx.x + NT * r;
+        dst[y] = acc[saddr(y)];
+    }
+}
+
+template <int LOGN>
+static void maskdec_t(const DevConsts* dc, const RnsParams& P, const u64* MT, const int* slice_off,
+                      const int* slice_items, const int* item_mask, const u64* MASKS, const u64* S_NTT, u64* D,
+                      int slices, cudaStream_t st) {
+    using G = Ntt2<LOGN>;
+    const int smem = (4 * G::LINES * G::PITCH + 2 * G::TWB) * 8;
+    const int smemh = (4 * 8 * G::PITCH + 2 * btw_entries<LOGN, 8>()) * 8;
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(k_mask_dec_blocks<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(k_mask_dec_blocks<LOGN, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smemh);
+        configured = true;
+    }
+    if (slices * P.cfg.L * G::CTAS_B < 2 * 148 && 8 * G::R2 >= 2 * kGroupThreads)  // small: 8-block tiles
+        k_mask_dec_blocks<LOGN, 8><<<slices * P.cfg.L * (G::R1 / 8), 2 * kGroupThreads, smemh, st>>>(
+            dc, MT, slice_off, slice_items, item_mask, MASKS, S_NTT, D);
+    else
+        k_mask_dec_blocks<LOGN><<<slices * P.cfg.L * G::CTAS_B, 2 * kGroupThreads, smem, st>>>(
+            dc, MT, slice_off, slice_items, item_mask, MASKS, S_NTT, D);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw std::runtime_error(std::string("mask-decrypt launch: ") + cudaGetErrorString(e));
+}
+
+void launch_mask_dec_blocks(const DevConsts* dc, const RnsParams& P, const u64* MT, const int* slice_off,
+                            const int* slice_items, const int* item_mask, const u64* MASKS, const u64* S_NTT,
+                            u64* D, int slices, cudaStream_t st) {
+    if (!slices) return;
+    switch (P.cfg.logn) {
+        case 10: maskdec_t<10>(dc, P, MT, slice_off, slice_items, item_mask, MASKS, S_NTT, D, slices, st); break;
+        case 11: maskdec_t<11>(dc, P, MT, slice_off, slice_items, item_mask, MASKS, S_NTT, D, slices, st); break;
+        case 12: maskdec_t<12>(dc, P, MT, slice_off, slice_items, item_mask, MASKS, S_NTT, D, slices, st); break;
+        case 13: maskdec_t<13>(dc, P, MT, slice_off, slice_items, item_mask, MASKS, S_NTT, D, slices, st); break;
+        case 14: maskdec_t<14>(dc, P, MT, slice_off, slice_items, item_mask, MASKS, S_NTT, D, slices, st); break;
+        case 15: maskdec_t<15>(dc, P, MT, slice_off, slice_items, item_mask, MASKS, S_NTT, D, slices, st); break;
+        default: throw std::invalid_argument("mask-decrypt: unsupported logn");
+    }
+}
+
 template <int LOGN>
 static void maskb_t(const DevConsts* dc, const RnsParams& P, const u64* MT, const int* slice_off,
                     const int* slice_items, const int* item_mask, const u64* MASKS, u64* const* OUT, int slices,
