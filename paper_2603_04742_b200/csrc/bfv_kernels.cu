@@ -1245,10 +1245,8 @@ __global__ void __launch_bounds__(Ntt2<LOGN>::TC) k_dec_cols(const DevConsts* __
     for (int i = threadIdx.x; i < G::R1; i += T) cp_async16(tws + 2 * i, tw + 2 * i);
     const u64* d = D + (size_t)item * L * G::N;
     unsigned long long ad_max = 0;
-    constexpr int PER = G::R1 * LN / T;
-#pragma unroll 4
-    for (int r = 0; r < PER; ++r) {
-        const int e = threadIdx.x + T * r, c = e / LN, jl = e % LN;
+    for (int e = threadIdx.x; e < G::R1 * LN; e += T) {
+        const int c = e / LN, jl = e % LN;
         const int k = c * G::R2 + col0 + jl;
         u64 shi = 0, slo = 0;
         for (int i = 0; i < L; ++i) {
@@ -1276,9 +1274,8 @@ __global__ void __launch_bounds__(Ntt2<LOGN>::TC) k_dec_cols(const DevConsts* __
     };
     line_ntt_v<G::A, 0, false, 3, LN>(tile, ConstQ{dc->mod[tp].q}, addr, twf, whole_cta());
     u64* dst = M + (size_t)item * G::N;
-#pragma unroll
-    for (int r = 0; r < G::R1 * SEG / T; ++r) {
-        const int i = threadIdx.x + T * r, c = i / SEG, h = i % SEG;
+    for (int i = threadIdx.x; i < G::R1 * SEG; i += T) {
+        const int c = i / SEG, h = i % SEG;
         *reinterpret_cast<ulonglong2*>(dst + (size_t)c * G::R2 + col0 + 2 * h) =
             make_ulonglong2(tile[c * LN + 2 * h], tile[c * LN + 2 * h + 1]);
     }
@@ -1296,14 +1293,21 @@ static void dec_ntt_t(const DevConsts* dc, const RnsParams& P, u64* D, u64* M, u
     for (int i = 0; i < L; ++i) jd.pidx[i] = (signed char)i;
     launch_ntt_phase(dc, LOGN, true, true, jd, items, st);  // inverse column phase of d
     cudaMemsetAsync(maxdev, 0, sizeof(unsigned long long) * items, st);
-    constexpr int LN = 8;
-    const int smem = (LN * G::R1 + 2 * G::R1) * 8;
+    // 2-column tiles unless 8-column tiles already give one CTA per SM: the
+    // per-coefficient scaling dominates, and a single result has only R2
+    // columns
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(k_dec_cols<LOGN, LN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(k_dec_cols<LOGN, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (8 * G::R1 + 2 * G::R1) * 8);
+        cudaFuncSetAttribute(k_dec_cols<LOGN, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (2 * G::R1 + 2 * G::R1) * 8);
         configured = true;
     }
-    k_dec_cols<LOGN, LN><<<items * (G::R2 / LN), G::TC, smem, st>>>(dc, D, M, maxdev);
+    if ((long)items * (G::R2 / 8) >= 148)
+        k_dec_cols<LOGN, 8><<<items * (G::R2 / 8), G::TC, (8 * G::R1 + 2 * G::R1) * 8, st>>>(dc, D, M, maxdev);
+    else
+        k_dec_cols<LOGN, 2><<<items * (G::R2 / 2), G::TC, (2 * G::R1 + 2 * G::R1) * 8, st>>>(dc, D, M, maxdev);
     CSSC_CHECK_LAUNCH();
     NttJob jm;
     jm.src = M;

@@ -195,8 +195,8 @@ __global__ void __launch_bounds__(2 * kGroupThreads) k_mask_blocks(const DevCons
 }
 
 // The pipeline's decrypting variant of k_mask_blocks: for one slice, one
-// prime j < L and one tile, group 0 sums the c0 limb and group 1 the c1 limb
-// of every chunk (block phase x mask), then d = c0 + c1 s (s in NTT form,
+// prime j < L and one tile, groups 0-1 sum the c0 limb and groups 2-3 the c1
+// limb of the slice's chunks (block phase x mask; even / odd chunks), then d = c0 + c1 s (s in NTT form,
 // the key holder's decryption product, done where c1 already is in the NTT
 // domain) goes through the inverse block phase into D[slice][j].  The
 // inverse column phase of D and the t/Q scaling follow (k_dec_cols).  The
@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(2 * kGroupThreads) k_mask_blocks(const DevCons
 // its decryption, and d mod q_j is the same residue c0 + INTT(NTT(c1) s)
 // gives, so the slots are unchanged.
 template <int LOGN, int LN = 16>
-__global__ void __launch_bounds__(2 * kGroupThreads) k_mask_dec_blocks(const DevConsts* __restrict__ dc,
+__global__ void __launch_bounds__(4 * kGroupThreads) k_mask_dec_blocks(const DevConsts* __restrict__ dc,
                                                                        const u64* __restrict__ MT,
                                                                        const int* __restrict__ slice_off,
                                                                        const int* __restrict__ slice_items,
@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(2 * kGroupThreads) k_mask_dec_blocks(const Dev
     extern __shared__ u64 smem[];
     constexpr int PITCH = G::PITCH;
     constexpr int TW = LN * PITCH;
-    constexpr int NG = 2;  // group 0: c0, group 1: c1
+    constexpr int NG = 4;  // groups 0, 1: c0 (even / odd chunks), groups 2, 3: c1
     constexpr int NT = NG * kGroupThreads;
     constexpr int PERG = LN * G::R2 / kGroupThreads;
     constexpr int PER = LN * G::R2 / NT;
@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(2 * kGroupThreads) k_mask_dec_blocks(const Dev
     const size_t base = (size_t)blk0 * G::R2;
     const int grp = threadIdx.x / kGroupThreads;
     const ThreadGroup tg = cta_slice(grp, NG);
-    const int j2 = grp * L + j;
+    const int j2 = (grp >> 1) * L + j;
     u64* wk = work + grp * TW;
     u64* ac = acc + grp * TW;
     auto saddr = [](int x) { return (x >> G::B) * PITCH + (x & (G::R2 - 1)); };
@@ -248,7 +248,7 @@ __global__ void __launch_bounds__(2 * kGroupThreads) k_mask_dec_blocks(const Dev
     const int b = slice_off[sl], e = slice_off[sl + 1];
     bool any = false;
 #pragma unroll 1
-    for (int x = b; x < e; ++x) {
+    for (int x = b + (grp & 1); x < e; x += 2) {
         const int it = slice_items[x];
         const u64* src = MT + ((size_t)it * 2 * L + j2) * G::N + base;
 #pragma unroll
@@ -277,7 +277,8 @@ __global__ void __launch_bounds__(2 * kGroupThreads) k_mask_dec_blocks(const Dev
 #pragma unroll
     for (int r = 0; r < PER; ++r) {
         const int y = threadIdx.x + NT * r, s0 = saddr(y);
-        acc[s0] = add_mod(acc[s0], mul_mod(acc[TW + s0], __ldg(sk + y), md), q);
+        const u64 c0 = add_mod(acc[s0], acc[TW + s0], q), c1 = add_mod(acc[2 * TW + s0], acc[3 * TW + s0], q);
+        acc[s0] = add_mod(c0, mul_mod(c1, __ldg(sk + y), md), q);
     }
     __syncthreads();
     load_block_twiddles<LOGN, LN>(tws, dc->tw[j].inv, blk0);
@@ -297,19 +298,19 @@ static void maskdec_t(const DevConsts* dc, const RnsParams& P, const u64* MT, co
                       const int* slice_items, const int* item_mask, const u64* MASKS, const u64* S_NTT, u64* D,
                       int slices, cudaStream_t st) {
     using G = Ntt2<LOGN>;
-    const int smem = (4 * G::LINES * G::PITCH + 2 * G::TWB) * 8;
-    const int smemh = (4 * 8 * G::PITCH + 2 * btw_entries<LOGN, 8>()) * 8;
+    const int smem = (8 * G::LINES * G::PITCH + 2 * G::TWB) * 8;
+    const int smemh = (8 * 8 * G::PITCH + 2 * btw_entries<LOGN, 8>()) * 8;
     static bool configured = false;
     if (!configured) {
         cudaFuncSetAttribute(k_mask_dec_blocks<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         cudaFuncSetAttribute(k_mask_dec_blocks<LOGN, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smemh);
         configured = true;
     }
-    if (slices * P.cfg.L * G::CTAS_B < 2 * 148 && 8 * G::R2 >= 2 * kGroupThreads)  // small: 8-block tiles
-        k_mask_dec_blocks<LOGN, 8><<<slices * P.cfg.L * (G::R1 / 8), 2 * kGroupThreads, smemh, st>>>(
+    if (slices * P.cfg.L * G::CTAS_B < 2 * 148 && 8 * G::R2 >= 4 * kGroupThreads)  // small: 8-block tiles
+        k_mask_dec_blocks<LOGN, 8><<<slices * P.cfg.L * (G::R1 / 8), 4 * kGroupThreads, smemh, st>>>(
             dc, MT, slice_off, slice_items, item_mask, MASKS, S_NTT, D);
     else
-        k_mask_dec_blocks<LOGN><<<slices * P.cfg.L * G::CTAS_B, 2 * kGroupThreads, smem, st>>>(
+        k_mask_dec_blocks<LOGN><<<slices * P.cfg.L * G::CTAS_B, 4 * kGroupThreads, smem, st>>>(
             dc, MT, slice_off, slice_items, item_mask, MASKS, S_NTT, D);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) throw std::runtime_error(std::string("mask-decrypt launch: ") + cudaGetErrorString(e));
