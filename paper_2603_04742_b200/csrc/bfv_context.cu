@@ -366,13 +366,14 @@ void GpuContext::encrypt_cssc(const int64_t* ci, const int64_t* va, size_t nnz, 
     encrypt_cssc_image(h, lay);
 }
 
-void GpuContext::encrypt_cssc_image(const unsigned char* img, const CsscLayout& lay, const ClientWs* ws) {
+void GpuContext::encrypt_cssc_image(const unsigned char* img, const CsscLayout& lay, const ClientWs* ws,
+                                    EncIn* defer) {
     const int items = lay.items;
     if (!items) return;
     unsigned char* d;
     u64 *U, *CM;
     if (ws) {
-        encrypt_cssc_forked(img, lay, *ws);
+        encrypt_cssc_forked(img, lay, *ws, defer);
         return;
     } else if (forked_enc_) {
         ensure_ws(scratch_[0], std::max<size_t>(lay.bytes, 256));
@@ -410,7 +411,8 @@ void GpuContext::encrypt_cssc_image(const unsigned char* img, const CsscLayout& 
 // run side by side, joined by the finishing kernel (+ e0 + Delta m, + e1).
 // CM is [item][2L][N] followed by the messages [item][N]; same words as the
 // staged path.
-void GpuContext::encrypt_cssc_forked(const unsigned char* img, const CsscLayout& lay, const ClientWs& ws) {
+void GpuContext::encrypt_cssc_forked(const unsigned char* img, const CsscLayout& lay, const ClientWs& ws,
+                                     EncIn* defer) {
     const int items = lay.items, L = P_.cfg.L, logn = P_.cfg.logn;
     const size_t n = (size_t)P_.n;
     unsigned char* d = ws.up;
@@ -440,9 +442,15 @@ void GpuContext::encrypt_cssc_forked(const unsigned char* img, const CsscLayout&
     pidx.insert(pidx.end(), pidx.begin(), pidx.end());
     launch_ntt_phase(dc_, logn, true, true, job(CM, CM, 2 * L, pidx), items, st_);
     cuda_check(cudaStreamWaitEvent(st_, ev_join_, 0), "join");
-    launch_enc_finish(dc_, P_, P_.cfg.seed, streams, CM, reinterpret_cast<u64* const*>(d + lay.o_out), items, st_,
-                      MSG, (size_t)2 * L * n, n);
-    stats_.kernels += 8;
+    if (defer) {
+        *defer = EncIn{P_.cfg.seed, streams, CM, (size_t)2 * L * n, MSG, n,
+                       reinterpret_cast<u64* const*>(d + lay.o_out), items / 2};
+        stats_.kernels += 7;
+    } else {
+        launch_enc_finish(dc_, P_, P_.cfg.seed, streams, CM, reinterpret_cast<u64* const*>(d + lay.o_out), items,
+                          st_, MSG, (size_t)2 * L * n, n);
+        stats_.kernels += 8;
+    }
     stats_.limb_ntts += (u64)items * (1 + 3 * L);
 }
 
@@ -552,11 +560,14 @@ void GpuContext::add(const std::vector<const u64*>& a, const std::vector<const u
 
 void GpuContext::mul_relin_dev(const u64* const* A, const u64* const* B, u64* const* OUT,
                                int items, u64* T, u64* Z, u64* D2, u64* DX, u64* ACC,
-                               const u64* const* RLK) {
+                               const u64* const* RLK, const EncIn* enc) {
     const int L = P_.cfg.L, K = P_.cfg.K, LK = L + K, M = L + P_.nB, logn = P_.cfg.logn;
     std::vector<int> pm;
     for (int j = 0; j < M; ++j) pm.push_back(j < L ? j : K + j);
-    launch_mul_extend(dc_, P_, A, B, T, items, st_);
+    if (enc)
+        launch_mul_extend_enc(dc_, P_, *enc, T, items, st_);
+    else
+        launch_mul_extend(dc_, P_, A, B, T, items, st_);
     if (fused_ks_) {  // column phase, fused blocks + tensor + inverse blocks, column phase
         launch_ntt_phase(dc_, logn, false, true, job(T, T, 4 * M, pm), items, st_);
         launch_mul_blocks_tensor(dc_, P_, T, Z, items, st_);

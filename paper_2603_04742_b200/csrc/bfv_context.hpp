@@ -126,7 +126,10 @@ public:
     // the same from an image already laid out in pinned host memory (trusted
     // descriptors: the caller built them); the image must stay alive until the
     // stream has consumed it
-    void encrypt_cssc_image(const unsigned char* img, const CsscLayout& lay, const ClientWs* ws = nullptr);
+    // defer (pipeline, fused path): skip the finishing kernel and describe its
+    // inputs instead; the multiply's extension (launch_mul_extend_enc) finishes
+    void encrypt_cssc_image(const unsigned char* img, const CsscLayout& lay, const ClientWs* ws = nullptr,
+                            EncIn* defer = nullptr);
     // pinned host buffers, pooled by capacity
     unsigned char* pinned_take(size_t bytes, size_t* cap);
     void pinned_give(unsigned char* p, size_t cap);
@@ -151,8 +154,10 @@ public:
     void synchronize();
 
     // building blocks reused by the batched cloud plan (pointer arrays on device)
+    // enc: A and B are still to be finished from a deferred encryption (EncIn)
     void mul_relin_dev(const u64* const* A, const u64* const* B, u64* const* OUT, int items,
-                       u64* T, u64* Z, u64* D2, u64* DX, u64* ACC, const u64* const* RLK);
+                       u64* T, u64* Z, u64* D2, u64* DX, u64* ACC, const u64* const* RLK,
+                       const EncIn* enc = nullptr);
     // OUT = BASE + EXTRA + rot(SRC) (BASE / EXTRA per-item nullable)
     void rotate_dev(const u64* const* SRC, const u32* ginv, const u64* const* KEY,
                     const u64* const* BASE, u64* const* OUT, int items, u64* DX, u64* ACC,
@@ -182,7 +187,8 @@ private:
     unsigned char* stage_host(size_t bytes);
     void* stage_upload(size_t bytes, int slot);
     DevBuf gen_ksk(u64 keyid, const u64* sp_ntt);
-    void encrypt_cssc_forked(const unsigned char* img, const CsscLayout& lay, const ClientWs& ws);
+    void encrypt_cssc_forked(const unsigned char* img, const CsscLayout& lay, const ClientWs& ws,
+                             EncIn* defer = nullptr);
     void ensure_ws(DevBuf& b, size_t bytes) { b.ensure(&pool_, bytes); }
 
     RnsParams P_;

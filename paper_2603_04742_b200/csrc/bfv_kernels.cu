@@ -476,6 +476,53 @@ __global__ void k_mul_extend_k(const __grid_constant__ ExtendK<L> c, const u64* 
     for (int j = 0; j < nB; ++j) dst[(size_t)(L + j) * n + k] = o[j];
 }
 
+// The pipeline's encryption finish fused into the multiply's base
+// extension: for one (chunk, polynomial of a or b) and 128 coefficients, the
+// ChaCha e draw of k_enc_finish, c = (pk u) + e (+ Delta m for c0) per Q
+// limb (the ciphertext words, also stored to the ciphertext), then E1 of
+// those words into T.  Same words as k_enc_finish followed by k_mul_extend.
+
+template <int L>
+struct ExtendEncK {
+    ExtendK<L> x;
+    u64 delta[L], delta_sh[L];
+};
+
+template <int L>
+__global__ void __launch_bounds__(128) k_mul_extend_enc(const __grid_constant__ ExtendEncK<L> c, const EncIn in,
+                                                        u64* T) {
+    constexpr int nB = L + 1, M = L + nB;
+    __shared__ u32 blk[16][16];
+    const int n = c.x.n;
+    const int item = blockIdx.y, p = blockIdx.z, poly = p & 1;
+    const int eitem = (p < 2 ? 0 : in.n_chunks) + item;
+    const u64 id = in.streams[eitem];
+    const int g = threadIdx.x >> 2;
+    if (g < 16)
+        chacha20_block_x4(in.seed, (u32)(blockIdx.x * 16 + g), poly ? DOM_ENC_E1 : DOM_ENC_E0, (u32)id,
+                          (u32)(id >> 32), blk[g]);
+    __syncthreads();
+    const int kk = threadIdx.x, k = blockIdx.x * 128 + kk;
+    const int64_t e = cbd_of(word64(blk[kk >> 3], kk & 7));
+    const u64* cm = in.CM + (size_t)eitem * in.cstride + (size_t)poly * L * n + k;
+    const u64 m = poly ? 0 : in.MSG[(size_t)eitem * in.mstride + k];
+    u64* ct = in.OUT[eitem] + (size_t)poly * L * n + k;
+    u64* dst = T + ((size_t)item * 4 + p) * M * n + k;
+    u64 x[L], o[nB];
+#pragma unroll
+    for (int i = 0; i < L; ++i) {
+        const u64 q = c.x.qb.xq[i];
+        u64 v = add_mod(cm[(size_t)i * n], lift_signed(e, q), q);
+        if (!poly) v = add_mod(v, shoup(m, c.delta[i], c.delta_sh[i], q), q);
+        x[i] = v;
+        ct[(size_t)i * n] = v;
+        dst[(size_t)i * n] = v;
+    }
+    extend_k(c.x.qb, x, o);
+#pragma unroll
+    for (int j = 0; j < nB; ++j) dst[(size_t)(L + j) * n] = o[j];
+}
+
 template <int L>
 struct ScaleK {
     int n;
@@ -578,6 +625,34 @@ __global__ void k_mul_extend(const DevConsts* __restrict__ dc, const u64* const*
 #pragma unroll
         for (int j = 0; j < nB; ++j) dst[(size_t)(L + j) * n + k] = o[j];
     }
+}
+
+bool fixed_rns_shape(const RnsParams& P) {
+    bool fixed = false;
+    dispatch_shape(P, [&](auto l_, auto, auto) { fixed = decltype(l_)::value > 0; });
+    return fixed;
+}
+
+void launch_mul_extend_enc(const DevConsts* dc, const RnsParams& P, const EncIn& in, u64* T, int items,
+                           cudaStream_t st) {
+    if (!items) return;
+    dispatch_shape(P, [&](auto l_, auto k_, auto a_) {
+        constexpr int LT = decltype(l_)::value;
+        if constexpr (LT > 0) {
+            ExtendEncK<LT> c{};
+            c.x = make_extend_k<LT>(P);
+            for (int i = 0; i < LT; ++i) {
+                c.delta[i] = P.host.delta[i];
+                c.delta_sh[i] = P.host.delta_sh[i];
+            }
+            dim3 g = ew_grid(P.n, items);
+            g.z = 4;
+            k_mul_extend_enc<LT><<<g, 128, 0, st>>>(c, in, T);
+        } else {
+            throw std::invalid_argument("fused encryption + extension needs a fixed RNS shape");
+        }
+    });
+    CSSC_CHECK_LAUNCH();
 }
 
 void launch_mul_extend(const DevConsts* dc, const RnsParams& P, const u64* const* A,

@@ -45,6 +45,20 @@ void launch_ntt_phase(const DevConsts* dc, int logn, bool inverse, bool cols, co
 size_t ntt_smem_bytes(int logn);
 
 // ct x ct
+// pipeline: the encryption's finish (e, Delta m) fused into the base extension
+struct EncIn {
+    u64 seed;
+    const u64* streams;  // per encryption item (a chunks, then b chunks)
+    const u64* CM;       // pk u after the inverse NTT, [item][2L][N] (cstride words apart)
+    size_t cstride;
+    const u64* MSG;      // encoded messages mod t, mstride words apart
+    size_t mstride;
+    u64* const* OUT;     // ciphertext of each encryption item
+    int n_chunks;
+};
+bool fixed_rns_shape(const RnsParams& P);  // one of the compiled (L, K, alpha) shapes
+void launch_mul_extend_enc(const DevConsts* dc, const RnsParams& P, const EncIn& in, u64* T, int items,
+                           cudaStream_t st);
 void launch_mul_extend(const DevConsts* dc, const RnsParams& P, const u64* const* A,
                        const u64* const* B, u64* T, int items, cudaStream_t st);
 // fused forward block phase + mask multiply-accumulate + inverse block phase

@@ -270,7 +270,7 @@ CloudPlan::~CloudPlan() {
     if (graph_) cudaGraphDestroy(graph_);
 }
 
-void CloudPlan::record(std::vector<cudaEvent_t>* marks, u64* dec_d) {
+void CloudPlan::record(std::vector<cudaEvent_t>* marks, u64* dec_d, const EncIn* enc) {
     if (n_ == 0) return;
     const RnsParams& P = ctx_.params();
     const int L = P.cfg.L, logn = P.cfg.logn;
@@ -285,7 +285,7 @@ void CloudPlan::record(std::vector<cudaEvent_t>* marks, u64* dec_d) {
     };
     mark();
     ctx_.mul_relin_dev(A_, B_, PROD_, n_, T_.words(), Z_.words(), D2_.words(), DX_.words(),
-                       ACC_.words(), RLK_);
+                       ACC_.words(), RLK_, enc);
     mark();
     for (size_t l = 0; l < levels_.size(); ++l) {
         const Level& lv = levels_[l];
@@ -438,9 +438,13 @@ void CloudPlan::capture_pipeline(const unsigned char* img, const CsscLayout& lay
     cudaGraph_t g = nullptr;
     cuda_check(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "begin capture");
     try {
-        ctx_.encrypt_cssc_image(img, lay, &ws);
-        if (ctx_.fused_key_switch()) {  // decryption fused into the mask step (k_mask_dec_blocks)
-            record(nullptr, ws.X);
+        // fused path: the encryption's finish rides in the multiply's base
+        // extension, the decryption in the mask step (k_mask_dec_blocks)
+        const bool fused = ctx_.fused_key_switch() && fixed_rns_shape(P);
+        EncIn enc{};
+        ctx_.encrypt_cssc_image(img, lay, &ws, fused ? &enc : nullptr);
+        if (fused) {
+            record(nullptr, ws.X, &enc);
             launch_decrypt_ntt(ctx_.dconsts(), P, ws.X, ws.M, ws.slots, maxdev, ns_, st);
         } else {
             record();

@@ -63,7 +63,8 @@ public:
 private:
     // dec_d: the pipeline's decrypting tail (fused path): the mask step writes
     // d = c0 + c1 s per slice into dec_d ([ns][L][N]) instead of the result cts
-    void record(std::vector<cudaEvent_t>* marks = nullptr, u64* dec_d = nullptr);
+    // enc: the inputs still need the encryption's finishing step (pipeline)
+    void record(std::vector<cudaEvent_t>* marks = nullptr, u64* dec_d = nullptr, const EncIn* enc = nullptr);
     template <class T>
     T* put(const std::vector<T>& v);
 
