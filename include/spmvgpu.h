@@ -234,6 +234,9 @@ int cssc_job_finish_words(cssc_job* j, const uint64_t* words, int64_t* const* va
 int cssc_job_encrypt(cssc_job* j);            /* client phase: encode + encrypt on device */
 int cssc_job_cloud(cssc_job* j, int use_graph); /* cloud phase, enqueued (no sync) */
 int cssc_job_finish(cssc_job* j, int64_t* const* values, cssc_result* res); /* decrypt */
+/* encrypt + cloud + decrypt in one call (what cssc_spmv_batch runs): from the
+ * second job over a chunk-shape structure, one cached graph launch */
+int cssc_job_run(cssc_job* j, int64_t* const* values, cssc_result* res);
 int cssc_job_plan_stats(const cssc_job* j, spmvgpu_plan_stats* out);
 int cssc_job_profile(cssc_job* j, spmvgpu_phase* phases, int cap, int* count); /* see spmvgpu_plan_profile */
 int cssc_job_input_bytes(const cssc_job* j, uint64_t* h2d, uint64_t* d2h);

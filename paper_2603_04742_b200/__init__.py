@@ -132,6 +132,7 @@ _SIGS = {
     "cssc_job_encrypt": (C.c_int, [C.c_void_p]),
     "cssc_job_cloud": (C.c_int, [C.c_void_p, C.c_int]),
     "cssc_job_finish": (C.c_int, [C.c_void_p, C.POINTER(i64p), C.POINTER(ResultC)]),
+    "cssc_job_run": (C.c_int, [C.c_void_p, C.POINTER(i64p), C.POINTER(ResultC)]),
     "cssc_job_plan_stats": (C.c_int, [C.c_void_p, C.POINTER(PlanStats)]),
     "cssc_job_profile": (C.c_int, [C.c_void_p, C.POINTER(PhaseC), C.c_int, C.POINTER(C.c_int)]),
     "cssc_job_input_bytes": (C.c_int, [C.c_void_p, u64p, u64p]),
@@ -584,6 +585,16 @@ class Job:
         optr = (i64p * n)(*[_p(o, i64p) for o in outs])
         res = (ResultC * n)()
         check(lib().cssc_job_finish(self.h, optr, res))
+        return [_result(res[i], outs[i][: self.ms[i].rows]) for i in range(n)]
+
+    def run(self) -> list:
+        """encrypt + cloud + finish in one call (spmv_batch's path: one cached
+        graph launch from the second job over the same chunk shapes)."""
+        n = len(self.ms)
+        outs = [np.zeros(max(m.rows, 1), np.int64) for m in self.ms]
+        optr = (i64p * n)(*[_p(o, i64p) for o in outs])
+        res = (ResultC * n)()
+        check(lib().cssc_job_run(self.h, optr, res))
         return [_result(res[i], outs[i][: self.ms[i].rows]) for i in range(n)]
 
     def stats(self) -> dict:

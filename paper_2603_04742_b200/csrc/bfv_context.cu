@@ -444,7 +444,7 @@ void GpuContext::encrypt_cssc_forked(const unsigned char* img, const CsscLayout&
     cuda_check(cudaStreamWaitEvent(st_, ev_join_, 0), "join");
     if (defer) {
         *defer = EncIn{P_.cfg.seed, streams, CM, (size_t)2 * L * n, MSG, n,
-                       reinterpret_cast<u64* const*>(d + lay.o_out), items / 2};
+                       reinterpret_cast<u64* const*>(d + lay.o_out), items / 2, nullptr};
         stats_.kernels += 7;
     } else {
         launch_enc_finish(dc_, P_, P_.cfg.seed, streams, CM, reinterpret_cast<u64* const*>(d + lay.o_out), items,
@@ -533,7 +533,7 @@ void GpuContext::decrypt_dev(const u64* const* dct, int items, u64* X, u64* M, u
     }
     launch_dec_scale(dc_, P_, dct, X, M, maxdev, items, st_);
     launch_ntt(dc_, logn, false, job(M, M, 1, {P_.t_index()}), items, st_);
-    launch_decode_gather(dc_, P_, M, slots_dev, items, st_);
+    if (slots_dev) launch_decode_gather(dc_, P_, M, slots_dev, items, st_);
     stats_.kernels += 7;
     stats_.limb_ntts += (u64)items * (2 * L + 1);
 }

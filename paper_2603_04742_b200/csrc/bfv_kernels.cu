@@ -495,7 +495,7 @@ __global__ void __launch_bounds__(128) k_mul_extend_enc(const __grid_constant__ 
     __shared__ u32 blk[16][16];
     const int n = c.x.n;
     const int item = blockIdx.y, p = blockIdx.z, poly = p & 1;
-    const int eitem = (p < 2 ? 0 : in.n_chunks) + item;
+    const int eitem = (p < 2 ? 0 : in.n_chunks) + (in.order ? in.order[item] : item);
     const u64 id = in.streams[eitem];
     const int g = threadIdx.x >> 2;
     if (g < 16)
@@ -1390,7 +1390,7 @@ static void dec_ntt_t(const DevConsts* dc, const RnsParams& P, u64* D, u64* M, u
     jm.limbs = 1;
     jm.pidx[0] = (signed char)P.t_index();
     launch_ntt_phase(dc, LOGN, false, false, jm, items, st);  // forward block phase mod t
-    launch_decode_gather(dc, P, M, slots, items, st);
+    if (slots) launch_decode_gather(dc, P, M, slots, items, st);
 }
 
 // D (d = c0 + c1 s after the inverse block phase) -> slots, see k_dec_cols
@@ -1414,6 +1414,23 @@ __global__ void k_decode_gather(const DevConsts* __restrict__ dc, const u64* M, 
     const int item = blockIdx.y;
     if (j >= S) return;
     slots[(size_t)item * S + j] = M[(size_t)item * dc->n + dc->pos0[j]];
+}
+
+// pipeline download: result r's first rows[r] slots as u32 at out + off[r]
+__global__ void k_decode_rows(const DevConsts* __restrict__ dc, const u64* M, u32* out, const int* rows,
+                              const int* off) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const int item = blockIdx.y;
+    if (j >= rows[item]) return;
+    out[off[item] + j] = (u32)M[(size_t)item * dc->n + dc->pos0[j]];
+}
+
+void launch_decode_rows(const DevConsts* dc, const RnsParams& P, const u64* M, u32* out, const int* rows,
+                        const int* off, int max_rows, int items, cudaStream_t st) {
+    if (!items || max_rows <= 0) return;
+    k_decode_rows<<<dim3((unsigned)((max_rows + EW_THREADS - 1) / EW_THREADS), (unsigned)items), EW_THREADS, 0,
+                    st>>>(dc, M, out, rows, off);
+    CSSC_CHECK_LAUNCH();
 }
 
 void launch_decode_gather(const DevConsts* dc, const RnsParams& P, const u64* M, u64* slots,

@@ -55,6 +55,7 @@ struct EncIn {
     size_t mstride;
     u64* const* OUT;     // ciphertext of each encryption item
     int n_chunks;
+    const int* order;    // multiply item -> chunk (the plan's depth order); null = identity
 };
 bool fixed_rns_shape(const RnsParams& P);  // one of the compiled (L, K, alpha) shapes
 void launch_mul_extend_enc(const DevConsts* dc, const RnsParams& P, const EncIn& in, u64* T, int items,
@@ -133,6 +134,9 @@ void launch_mul_s(const DevConsts* dc, const RnsParams& P, u64* X, const u64* S_
 void launch_dec_scale(const DevConsts* dc, const RnsParams& P, const u64* const* CT,
                       const u64* X, u64* M, unsigned long long* maxdev, int items,
                       cudaStream_t st);
+// slots [0, rows[r]) of result r as u32 at out + off[r] (the pipeline's compact download)
+void launch_decode_rows(const DevConsts* dc, const RnsParams& P, const u64* M, u32* out, const int* rows,
+                        const int* off, int max_rows, int items, cudaStream_t st);
 void launch_decode_gather(const DevConsts* dc, const RnsParams& P, const u64* M, u64* slots,
                           int items, cudaStream_t st);
 

@@ -290,8 +290,7 @@ bool pipeline_ready(const PlanLease& lease, const ClientImage& img) {
 void pipeline_prepare(spmvgpu_ctx* ctx, PlanLease& lease, const ClientImage& img) {
     auto& g = *ctx->g;
     if (!lease.plan) throw std::logic_error("pipeline: no plan");
-    const int ns = lease.plan->plan->results();
-    const std::size_t out_bytes = sizeof(std::uint64_t) * (std::size_t)ns * (g.n() / 2) + 8 * (std::size_t)ns;
+    const std::size_t out_bytes = lease.plan->plan->pipeline_out_bytes();
     if (!lease.pimg || lease.pimg_cap < img.bytes) {
         if (lease.pimg) g.pinned_give(lease.pimg, lease.pimg_cap);
         lease.pimg = nullptr;
@@ -305,6 +304,14 @@ void pipeline_prepare(spmvgpu_ctx* ctx, PlanLease& lease, const ClientImage& img
     lease.pkey.clear();
     lease.plan->plan->capture_pipeline(lease.pimg, layout_of(img), lease.pout);
     lease.pkey = client_image_key(img);
+}
+
+std::size_t pipeline_out_bytes(const PlanLease& lease) { return lease.plan->plan->pipeline_out_bytes(); }
+
+PipelineResult pipeline_result(const PlanLease& lease, int r) {
+    const auto& pl = *lease.plan->plan;
+    const auto* md = reinterpret_cast<const unsigned long long*>(lease.pout + pl.maxdev_off());
+    return {reinterpret_cast<const std::uint32_t*>(lease.pout) + pl.out_off()[r], pl.out_rows()[r], md[r]};
 }
 
 void pipeline_run(spmvgpu_ctx* ctx, PlanLease& lease) {
@@ -825,6 +832,12 @@ int cssc_job_cloud(cssc_job* j, int use_graph) { return guard([&] { auto lk_ = a
 int cssc_job_finish(cssc_job* j, int64_t* const* values, cssc_result* res) {
     return guard([&] { auto lk_ = api_lock(j ? j->ctx : nullptr);
         const auto r = j->job->finish();
+        for (size_t i = 0; i < r.size(); ++i) fill_result(r[i], values ? values[i] : nullptr, res ? res + i : nullptr, nullptr, 0);
+    });
+}
+int cssc_job_run(cssc_job* j, int64_t* const* values, cssc_result* res) {
+    return guard([&] { auto lk_ = api_lock(j ? j->ctx : nullptr);
+        const auto r = j->job->run_all();
         for (size_t i = 0; i < r.size(); ++i) fill_result(r[i], values ? values[i] : nullptr, res ? res + i : nullptr, nullptr, 0);
     });
 }

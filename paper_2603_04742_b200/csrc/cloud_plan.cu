@@ -15,6 +15,8 @@
 #include "cloud_plan.hpp"
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <numeric>
@@ -80,6 +82,18 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
     const size_t ctw = ctx.ct_words();
     const int L = P.cfg.L, LK = L + P.cfg.K, M = L + P.nB;
 
+    rows_.assign(ns_, 0);
+    for (int i = 0; i < n; ++i)
+        if (slice[i] < (uint32_t)ns_) rows_[slice[i]] = std::max<int>(rows_[slice[i]], (int)r[i]);
+    out_off_.assign(ns_, 0);
+    {
+        size_t o = 0;
+        for (int s2 = 0; s2 < ns_; ++s2) {
+            out_off_[s2] = o;
+            o += (size_t)rows_[s2];
+        }
+        maxdev_off_ = (4 * o + 15) & ~size_t(15);
+    }
     std::vector<Tree> trees(n);
     size_t n_rot = 0, n_odd = 0;
     for (int i = 0; i < n; ++i) {
@@ -97,7 +111,7 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
                      [&](int x, int y) { return trees[x].dbl.size() > trees[y].dbl.size(); });
     const int depth = n ? (int)trees[order[0]].dbl.size() : 0;
 
-    arena_ = DevBuf(&ctx.pool(), 8 * ((size_t)(10 + 6 * std::max(depth, 1)) * std::max(n, 1) + 7 * n_odd +
+    arena_ = DevBuf(&ctx.pool(), 8 * ((size_t)(11 + 6 * std::max(depth, 1)) * std::max(n, 1) + 7 * n_odd +
                                       2 * (size_t)ns_ + 8) +
                                      16 * (size_t)(6 * depth + 24));
     prod_ = DevBuf(&ctx.pool(), sizeof(u64) * ctw * std::max(n, 1));
@@ -130,6 +144,7 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
     }
     A_ = put(va);
     B_ = put(vb);
+    ORDER_ = put(order);
     PROD_ = put(vp);
     RLK_ = put(rlk);
 
@@ -425,7 +440,17 @@ void CloudPlan::capture_pipeline(const unsigned char* img, const CsscLayout& lay
     pCM_.ensure(pool, sizeof(u64) * (size_t)lay.items * ctx_.cm_stride());
     pX_.ensure(pool, sizeof(u64) * (size_t)ns_ * L * n);
     pM_.ensure(pool, sizeof(u64) * (size_t)ns_ * n);
-    pslots_.ensure(pool, sizeof(u64) * (size_t)ns_ * (n / 2) + 8 * (size_t)ns_ + 64);
+    pslots_.ensure(pool, pipeline_out_bytes() + 64);
+    {
+        std::vector<int> g(2 * (size_t)ns_);
+        for (int s2 = 0; s2 < ns_; ++s2) {
+            g[s2] = rows_[s2];
+            g[ns_ + s2] = (int)out_off_[s2];
+        }
+        pgather_.ensure(pool, sizeof(int) * std::max<size_t>(g.size(), 1));
+        cuda_check(cudaMemcpy(pgather_.as<int>(), g.data(), sizeof(int) * g.size(), cudaMemcpyHostToDevice),
+                   "gather table");
+    }
     ClientWs ws;
     ws.up = pup_.as<unsigned char>();
     ws.U = pU_.words();
@@ -433,26 +458,49 @@ void CloudPlan::capture_pipeline(const unsigned char* img, const CsscLayout& lay
     ws.X = pX_.words();
     ws.M = pM_.words();
     ws.slots = pslots_.words();
-    auto* maxdev = reinterpret_cast<unsigned long long*>(ws.slots + (size_t)ns_ * (n / 2));
+    auto* maxdev = reinterpret_cast<unsigned long long*>(pslots_.as<unsigned char>() + maxdev_off_);
     cudaStream_t st = ctx_.stream();
     cudaGraph_t g = nullptr;
+    static const bool prof = std::getenv("CSSC_PIPE_PROFILE") != nullptr;
+    for (cudaEvent_t ev : pmarks_) cudaEventDestroy(ev);
+    pmarks_.clear();
+    std::vector<cudaEvent_t>* mk = prof ? &pmarks_ : nullptr;
+    auto mark = [&] {
+        if (!mk) return;
+        cudaEvent_t ev;
+        cuda_check(cudaEventCreate(&ev), "event");
+        cuda_check(cudaEventRecordWithFlags(ev, st, cudaEventRecordExternal), "event record");
+        mk->push_back(ev);
+    };
     cuda_check(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "begin capture");
     try {
+        mark();
         // fused path: the encryption's finish rides in the multiply's base
         // extension, the decryption in the mask step (k_mask_dec_blocks)
+        static const int fuse_mask = [] {  // debugging aid: bit 0 encryption finish, bit 1 decryption
+            const char* e = std::getenv("CSSC_PIPE_FUSE");
+            return e ? std::atoi(e) : 3;
+        }();
         const bool fused = ctx_.fused_key_switch() && fixed_rns_shape(P);
+        const bool fenc = fused && (fuse_mask & 1), fdec = fused && (fuse_mask & 2);
         EncIn enc{};
-        ctx_.encrypt_cssc_image(img, lay, &ws, fused ? &enc : nullptr);
-        if (fused) {
-            record(nullptr, ws.X, &enc);
-            launch_decrypt_ntt(ctx_.dconsts(), P, ws.X, ws.M, ws.slots, maxdev, ns_, st);
+        ctx_.encrypt_cssc_image(img, lay, &ws, fenc ? &enc : nullptr);
+        enc.order = ORDER_;  // the multiply's items are the chunks in depth order
+        const int* grows = pgather_.as<int>();
+        if (fdec) {
+            record(mk, ws.X, fenc ? &enc : nullptr);
+            launch_decrypt_ntt(ctx_.dconsts(), P, ws.X, ws.M, nullptr, maxdev, ns_, st);
         } else {
-            record();
-            ctx_.decrypt_dev(OUT_, ns_, ws.X, ws.M, ws.slots, maxdev);
+            record(mk, nullptr, fenc ? &enc : nullptr);
+            ctx_.decrypt_dev(OUT_, ns_, ws.X, ws.M, nullptr, maxdev);
         }
-        cuda_check(cudaMemcpyAsync(out, ws.slots, sizeof(u64) * (size_t)ns_ * (n / 2) + 8 * (size_t)ns_,
-                                   cudaMemcpyDeviceToHost, st),
-                   "download");
+        int rmax = 0;
+        for (int v : rows_) rmax = std::max(rmax, v);
+        launch_decode_rows(ctx_.dconsts(), P, ws.M, reinterpret_cast<u32*>(ws.slots), grows, grows + ns_, rmax,
+                           ns_, st);
+        mark();
+        cuda_check(cudaMemcpyAsync(out, ws.slots, pipeline_out_bytes(), cudaMemcpyDeviceToHost, st), "download");
+        mark();
     } catch (...) {
         cudaGraph_t tmp = nullptr;
         cudaStreamEndCapture(st, &tmp);
@@ -468,6 +516,16 @@ void CloudPlan::capture_pipeline(const unsigned char* img, const CsscLayout& lay
 void CloudPlan::run_pipeline() {
     if (!pexec_) throw std::logic_error("pipeline not captured");
     cuda_check(cudaGraphLaunch(pexec_, ctx_.stream()), "graph launch");
+    if (!pmarks_.empty()) {  // CSSC_PIPE_PROFILE: encrypt | multiply | levels.. | mask | decrypt | download
+        cuda_check(cudaStreamSynchronize(ctx_.stream()), "sync");
+        std::fprintf(stderr, "pipe-profile us:");
+        for (size_t i = 1; i < pmarks_.size(); ++i) {
+            float ms = 0;
+            cudaEventElapsedTime(&ms, pmarks_[i - 1], pmarks_[i]);
+            std::fprintf(stderr, " %.1f", 1e3 * ms);
+        }
+        std::fprintf(stderr, "\n");
+    }
 }
 
 }  // namespace cssc

@@ -58,6 +58,14 @@ public:
     void run_pipeline();  // enqueue (no sync)
     bool has_pipeline() const { return pexec_ != nullptr; }
     int results() const { return ns_; }
+    // pipeline download layout: result s's first rows_[s] slots as u32 at
+    // out_off()[s] (in u32 units), then one u64 rounding deviation per result
+    // at byte offset maxdev_off(); slots past the tallest chunk of a slice are
+    // masked to zero and not downloaded
+    const std::vector<size_t>& out_off() const { return out_off_; }
+    const std::vector<int>& out_rows() const { return rows_; }
+    size_t maxdev_off() const { return maxdev_off_; }
+    size_t pipeline_out_bytes() const { return maxdev_off_ + 8 * (size_t)ns_; }
     const PlanStats& stats() const { return stats_; }
 
 private:
@@ -70,6 +78,11 @@ private:
 
     GpuContext& ctx_;
     int n_ = 0, ns_ = 0;
+    std::vector<int> rows_;        // per result: tallest chunk height
+    std::vector<size_t> out_off_;  // per result: u32 offset in the download
+    size_t maxdev_off_ = 0;
+    DevBuf pgather_;               // device copy of {rows, out_off}
+    const int* ORDER_ = nullptr;   // multiply item k -> chunk (depth order), device
     PlanStats stats_;
     DevBuf prod_, acc0_, acc1_, rp_;  // rp_: hoisted odd-step rotations of the products
     DevBuf T_, Z_, D2_, DX_, ACC_, MT_, MASKS_;
@@ -105,6 +118,7 @@ private:
     cudaGraphExec_t exec_ = nullptr;
     DevBuf pup_, pU_, pCM_, pX_, pM_, pslots_;  // pipeline workspaces
     cudaGraphExec_t pexec_ = nullptr;
+    std::vector<cudaEvent_t> pmarks_;  // CSSC_PIPE_PROFILE=1: phase marks inside the pipeline graph
 };
 
 }  // namespace cssc

@@ -354,15 +354,16 @@ std::vector<SpmvResult> BatchedSpmv::run_all() {
     const std::size_t S = hp_.slot_count;
     std::vector<std::uint64_t> slots(n_out_ * S);
     std::vector<std::int32_t> measured(n_out_, 0);
-    const auto* pslots = reinterpret_cast<const std::uint64_t*>(lease_.pout);
-    const auto* md = reinterpret_cast<const unsigned long long*>(lease_.pout + 8 * n_dout_ * S);
     for (std::size_t r = 0; r < n_out_; ++r) {  // world == 1: every result is local
-        const auto lr = static_cast<std::size_t>(res_local_[r]);
-        std::memcpy(slots.data() + r * S, pslots + lr * S, 8 * S);
-        const int bl = md[lr] ? 64 - __builtin_clzll(md[lr]) : 0;
+        const PipelineResult pr = pipeline_result(lease_, res_local_[r]);
+        std::uint64_t* dst = slots.data() + r * S;
+        for (int i = 0; i < pr.rows; ++i) dst[i] = pr.slots[i];
+        const int bl = pr.maxdev ? 64 - __builtin_clzll(pr.maxdev) : 0;
         measured[r] = std::max(0, 63 - bl);
     }
-    return report(slots, measured);
+    auto res = report(slots, measured);
+    d2h_ = pipeline_out_bytes(lease_);
+    return res;
 }
 
 std::vector<SpmvResult> BatchedSpmv::decrypt_and_report(const std::vector<spmvgpu_ct>& outs) {

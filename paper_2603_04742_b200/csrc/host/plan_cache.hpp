@@ -64,5 +64,14 @@ std::vector<std::size_t> client_image_key(const ClientImage& img);
 void pipeline_prepare(spmvgpu_ctx* ctx, PlanLease& lease, const ClientImage& img);
 void pipeline_run(spmvgpu_ctx* ctx, PlanLease& lease);
 bool pipeline_ready(const PlanLease& lease, const ClientImage& img);
+// after pipeline_run: result r's decrypted slots [0, rows) as u32 (slots past
+// rows are zero) and its rounding deviation
+struct PipelineResult {
+    const std::uint32_t* slots;
+    int rows;
+    unsigned long long maxdev;
+};
+PipelineResult pipeline_result(const PlanLease& lease, int r);
+std::size_t pipeline_out_bytes(const PlanLease& lease);  // bytes one pipeline run downloads
 
 }  // namespace spmv::detail

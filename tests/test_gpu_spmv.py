@@ -217,3 +217,45 @@ def test_plain_spmv_is_one_slice(ctx10):
     with pytest.raises(pk.SpmvError) as e:
         pk.spmv(ctx10, m, v, 16)  # 300 rows: aligned column 0 is taller than 16
     assert e.value.kind == "ColumnTooTallError"
+
+
+def test_job_run_uses_the_pipeline_and_compact_download():
+    """Job.run (cssc_job_run) = encrypt + cloud + decrypt; from the second job
+    over one chunk-shape structure it is the cached graph, whose download holds
+    only each slice's first max-height slots (u32) and the deviations."""
+    ctx = pk.Context(logn=12, seed=8)
+    base = pk.random_sparse_csr(300, 250, 1800, 77, -8, 8)
+    rng = np.random.default_rng(3)
+    for it in range(3):
+        vals = (rng.integers(1, 9, base.values.size) * rng.choice([-1, 1], base.values.size)).astype(np.int64)
+        m = pk.Csr(base.rows, base.cols, base.row_ptrs, base.col_indices, vals)
+        v = rng.integers(-8, 9, base.cols).astype(np.int64)
+        j = pk.Job(ctx, [m], [v])
+        got = j.run()[0]
+        h2d, d2h = j.io_bytes()
+        j.close()
+        assert_same(got, checker(m, v, ctx.slots, ctx.slots))
+        if it:  # pipeline: rows of the tallest chunk as u32, padded to 16 B, + one u64
+            tallest = int((np.diff(base.row_ptrs) > 0).sum())
+            assert d2h == ((4 * tallest + 15) // 16) * 16 + 8
+    ctx.close()
+
+
+@pytest.mark.parametrize("logn", [10, 11, 12, 13])
+@pytest.mark.parametrize("fused", [1, 0])
+def test_pipeline_over_ring_sizes_and_chunk_depths(logn, fused):
+    """Repeated spmv_batch calls (the cached whole-evaluation graph from the
+    second one: fused encryption finish, depth-ordered multiply items, fused
+    decryption, compact download) equal the reference semantics; chunks of
+    different tree depths make the plan reorder its items."""
+    ctx = pk.Context(logn=logn, seed=8)
+    ctx.set_option("fused_key_switch", fused)
+    base = pk.random_sparse_csr(300, 250, 1800, 77, -8, 8)
+    rng = np.random.default_rng(3)
+    for _ in range(3):
+        vals = (rng.integers(1, 9, base.values.size) * rng.choice([-1, 1], base.values.size)).astype(np.int64)
+        m = pk.Csr(base.rows, base.cols, base.row_ptrs, base.col_indices, vals)
+        v = rng.integers(-8, 9, base.cols).astype(np.int64)
+        got = pk.spmv_batch(ctx, [m], [v])[0]
+        assert_same(got, checker(m, v, ctx.slots, ctx.slots))
+    ctx.close()
