@@ -166,12 +166,26 @@ __global__ void __launch_bounds__(Ntt2<LOGN>::TC, 256 / Ntt2<LOGN>::TC * 3) k_nt
     }
 }
 
-// 8-column tiles when 16-column tiles would leave SMs idle
+// Column-tile width: 8 columns only when twice the CTAs still fit one wave
+// (3 CTAs per SM, register-bound).  A wave-quantisation model that also
+// picked 8 columns for 1-2 waves (C2's 144-limb launch) measured 6 % slower:
+// an 8-column CTA costs well over half a 16-column one.  CSSC_COLS_LN=8|16
+// forces a width.
+bool cols_use_ln8(long ctas16, bool allowed) {
+    if (!allowed) return false;
+    static const int forced = [] {
+        const char* e = std::getenv("CSSC_COLS_LN");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (forced == 8) return true;
+    if (forced == 16) return false;
+    return 2 * ctas16 <= 3L * 148;
+}
+
 template <int LOGN, bool INV>
 static void launch_cols(const DevConsts* dc, const NttJob& job, int limbs, cudaStream_t st) {
     using G = Ntt2<LOGN>;
-    // 8-column tiles when twice the CTAs still fit one wave (3 CTAs per SM)
-    if (2 * limbs * G::CTAS_C <= 3 * 148 && G::R2 >= 16 && G::R1 * 4 >= G::TC) {
+    if (cols_use_ln8((long)limbs * G::CTAS_C, G::R2 >= 16 && G::R1 * 4 >= G::TC)) {
         constexpr int LN = 8;
         k_ntt_cols<LOGN, INV, LN><<<limbs * (G::R2 / LN), G::TC, (LN * G::R1 + 2 * G::R1) * 8, st>>>(dc, job);
     } else {

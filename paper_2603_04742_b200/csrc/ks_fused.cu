@@ -280,7 +280,7 @@ static void ks_fused_t(const DevConsts* dc, const RnsParams& P, const u64* const
                              smem2h);
         configured = smem2;
     }
-    if (2 * items * dnum * LK * G::CTAS_C <= 3 * 148 && G::R1 * 4 >= G::TC) {  // 8-column tiles fit one wave
+    if (cols_use_ln8((long)items * dnum * LK * G::CTAS_C, G::R1 * 4 >= G::TC)) {  // 8-column tiles
         constexpr int LN = 8;
         k_ks_modup_cols<LOGN, LT, KT, AT, LN><<<items * dnum * LK * (G::R2 / LN), G::TC,
                                                 (LN * G::R1 + 2 * G::R1) * 8, st>>>(dc, SRC, SRCC, src_poly, ginv, DX);
