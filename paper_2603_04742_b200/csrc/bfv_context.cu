@@ -306,12 +306,14 @@ CsscLayout CsscLayout::make(size_t nnz, size_t vec_len, size_t n_rows, size_t n_
     l.o_va = place(8 * nnz);
     l.o_v = place(8 * vec_len);
     l.o_rows = place(16 * n_rows);
+    l.o_rpre = place(4 * (n_rows + 1));  // exclusive prefix of the row lengths (+ total)
     l.o_sl = place(8 * n_slices);
     l.o_cols = place(16 * n_cols);
     l.o_st = place(8 * (size_t)items);
     l.o_out = place(8 * (size_t)items);
     l.bytes = off;
     l.nnz = nnz;
+    l.entries = nnz;
     l.vec_len = vec_len;
     l.n_rows = n_rows;
     l.n_slices = n_slices;
@@ -352,8 +354,19 @@ void GpuContext::encrypt_cssc(const int64_t* ci, const int64_t* va, size_t nnz, 
     if (items % 2) throw std::invalid_argument("encrypt_cssc: expects value and vector chunks in pairs");
     if (nnz > (size_t)INT32_MAX || vec_len > (size_t)INT32_MAX || n_rows > (size_t)INT32_MAX)
         throw std::length_error("encrypt_cssc: batch too large for 32-bit descriptors");
-    const CsscLayout lay = CsscLayout::make(nnz, vec_len, n_rows, n_slices, n_cols, items);
+    CsscLayout lay = CsscLayout::make(nnz, vec_len, n_rows, n_slices, n_cols, items);
     unsigned char* h = stage_host(lay.bytes);
+    {
+        auto* pre = reinterpret_cast<int32_t*>(h + lay.o_rpre);
+        int64_t acc = 0;
+        for (size_t r = 0; r < n_rows; ++r) {
+            pre[r] = (int32_t)acc;
+            acc += rows[4 * r + 1];
+            if (acc > INT32_MAX) throw std::length_error("encrypt_cssc: row entries exceed 2^31");
+        }
+        pre[n_rows] = (int32_t)acc;
+        lay.entries = (size_t)acc;
+    }
     std::memcpy(h + lay.o_ci, ci, 8 * nnz);
     std::memcpy(h + lay.o_va, va, 8 * nnz);
     std::memcpy(h + lay.o_v, vec, 8 * vec_len);
@@ -392,13 +405,12 @@ void GpuContext::encrypt_cssc_image(const unsigned char* img, const CsscLayout& 
     }
     cuda_check(cudaMemcpyAsync(d, img, lay.bytes, cudaMemcpyHostToDevice, st_), "upload");
     if (img == stage_) cuda_check(cudaEventRecord(stage_ev_, st_), "event");  // staging reusable after this
-    int log_tpr = 0;
-    while (log_tpr < 5 && (lay.n_rows << log_tpr) < lay.nnz) ++log_tpr;
     launch_pack_cssc(dc_, P_, reinterpret_cast<const int64_t*>(d + lay.o_ci),
                      reinterpret_cast<const int64_t*>(d + lay.o_va), reinterpret_cast<const int64_t*>(d + lay.o_v),
-                     reinterpret_cast<const int4*>(d + lay.o_rows), (int)lay.n_rows,
+                     reinterpret_cast<const int4*>(d + lay.o_rows), reinterpret_cast<const int*>(d + lay.o_rpre),
+                     (int)lay.n_rows, (long)lay.entries,
                      reinterpret_cast<const int2*>(d + lay.o_sl), reinterpret_cast<const int4*>(d + lay.o_cols),
-                     items / 2, log_tpr, CM + (size_t)2 * P_.cfg.L * P_.n, cm_stride(), st_);
+                     items / 2, CM + (size_t)2 * P_.cfg.L * P_.n, cm_stride(), st_);
     encrypt_encoded(reinterpret_cast<const u64*>(d + lay.o_st), reinterpret_cast<u64* const*>(d + lay.o_out), items,
                     U, CM);
 }
@@ -422,13 +434,12 @@ void GpuContext::encrypt_cssc_forked(const unsigned char* img, const CsscLayout&
     cuda_check(cudaStreamWaitEvent(st2_, ev_fork_, 0), "fork");
     // branch B: the CSR image, packing, message INTT
     cuda_check(cudaMemcpyAsync(d, img, lay.o_st, cudaMemcpyHostToDevice, st2_), "upload");
-    int log_tpr = 0;
-    while (log_tpr < 5 && (lay.n_rows << log_tpr) < lay.nnz) ++log_tpr;
     launch_pack_cssc(dc_, P_, reinterpret_cast<const int64_t*>(d + lay.o_ci),
                      reinterpret_cast<const int64_t*>(d + lay.o_va), reinterpret_cast<const int64_t*>(d + lay.o_v),
-                     reinterpret_cast<const int4*>(d + lay.o_rows), (int)lay.n_rows,
+                     reinterpret_cast<const int4*>(d + lay.o_rows), reinterpret_cast<const int*>(d + lay.o_rpre),
+                     (int)lay.n_rows, (long)lay.entries,
                      reinterpret_cast<const int2*>(d + lay.o_sl), reinterpret_cast<const int4*>(d + lay.o_cols),
-                     items / 2, log_tpr, MSG, n, st2_);
+                     items / 2, MSG, n, st2_);
     launch_ntt(dc_, logn, true, job(MSG, MSG, 1, {P_.t_index()}), items, st2_);
     cuda_check(cudaEventRecord(ev_join_, st2_), "join");
     // branch A: stream ids and output pointers, then the message-independent encryption

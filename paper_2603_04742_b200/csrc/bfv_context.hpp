@@ -62,8 +62,9 @@ struct LaunchStats {
 
 // Byte offsets of the arrays in one client upload image (see encrypt_cssc).
 struct CsscLayout {
-    size_t o_ci = 0, o_va = 0, o_v = 0, o_rows = 0, o_sl = 0, o_cols = 0, o_st = 0, o_out = 0, bytes = 0;
+    size_t o_ci = 0, o_va = 0, o_v = 0, o_rows = 0, o_rpre = 0, o_sl = 0, o_cols = 0, o_st = 0, o_out = 0, bytes = 0;
     size_t nnz = 0, vec_len = 0, n_rows = 0, n_slices = 0, n_cols = 0;
+    size_t entries = 0;  // sum of the row lengths (= nnz for CSR-derived rows): one pack thread each
     int items = 0;  // 2 * chunks
     static CsscLayout make(size_t nnz, size_t vec_len, size_t n_rows, size_t n_slices, size_t n_cols, int items);
 };

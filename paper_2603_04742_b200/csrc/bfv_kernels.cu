@@ -1108,39 +1108,44 @@ void launch_encode_scatter(const DevConsts* dc, const RnsParams& P, const int64_
 // chunk cols[col_base + j] = {chunk, k, h} holds at flat slot k h + pos
 // (generate_chunks, chunk.cpp:10-52); the vector chunk takes v[col] at the
 // same slot (reorg_vector, reorg.cpp).  Padding stays 0 (memset).
+// One thread per row entry (load-balanced for power-law rows: a hub row of
+// thousands of entries no longer serialises on a few lanes): entry e belongs
+// to row record r with rpre[r] <= e < rpre[r + 1] (binary search over the
+// exclusive prefix of the row lengths), at aligned column j = e - rpre[r].
 __global__ void k_pack_cssc(const DevConsts* __restrict__ dc, const int64_t* __restrict__ CI,
                             const int64_t* __restrict__ VA, const int64_t* __restrict__ V,
-                            const int4* __restrict__ rows, int n_rows, const int2* __restrict__ slices,
-                            const int4* __restrict__ cols, int n_chunks, int log_tpr, u64* __restrict__ M,
-                            size_t mstride) {
-    const int gid = blockIdx.x * blockDim.x + threadIdx.x;
-    const int r = gid >> log_tpr;
-    if (r >= n_rows) return;
-    const int4 rec = rows[r];
+                            const int4* __restrict__ rows, const int* __restrict__ rpre, int n_rows,
+                            const int2* __restrict__ slices, const int4* __restrict__ cols, int n_chunks,
+                            u64* __restrict__ M, size_t mstride) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (n_rows <= 0 || e >= __ldg(rpre + n_rows)) return;
+    int lo = 0, hi = n_rows - 1;  // last r with rpre[r] <= e
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (__ldg(rpre + mid) <= e) lo = mid;
+        else hi = mid - 1;
+    }
+    const int4 rec = rows[lo];
+    const int j = e - __ldg(rpre + lo);
     const int2 sl = slices[rec.w];
     const int64_t t = (int64_t)dc->t;
-    for (int j = gid & ((1 << log_tpr) - 1); j < rec.y; j += 1 << log_tpr) {
-        const int4 c = __ldg(cols + sl.x + j);
-        if (c.x < 0) continue;  // a chunk another rank evaluates (sharded jobs)
-        const u32 pos = dc->pos0[c.y * c.z + rec.z];
-        int64_t a = VA[rec.x + j] % t;
-        int64_t b = V[sl.y + CI[rec.x + j]] % t;
-        M[(size_t)c.x * mstride + pos] = (u64)(a < 0 ? a + t : a);
-        M[(size_t)(n_chunks + c.x) * mstride + pos] = (u64)(b < 0 ? b + t : b);
-    }
+    const int4 c = __ldg(cols + sl.x + j);
+    if (c.x < 0) return;  // a chunk another rank evaluates (sharded jobs)
+    const u32 pos = dc->pos0[c.y * c.z + rec.z];
+    int64_t a = VA[rec.x + j] % t;
+    int64_t b = V[sl.y + CI[rec.x + j]] % t;
+    M[(size_t)c.x * mstride + pos] = (u64)(a < 0 ? a + t : a);
+    M[(size_t)(n_chunks + c.x) * mstride + pos] = (u64)(b < 0 ? b + t : b);
 }
 
 void launch_pack_cssc(const DevConsts* dc, const RnsParams& P, const int64_t* CI, const int64_t* VA,
-                      const int64_t* V, const int4* rows, int n_rows, const int2* slices, const int4* cols,
-                      int n_chunks, int log_tpr, u64* M, size_t mstride, cudaStream_t st) {
+                      const int64_t* V, const int4* rows, const int* rpre, int n_rows, long entries,
+                      const int2* slices, const int4* cols, int n_chunks, u64* M, size_t mstride, cudaStream_t st) {
     if (!n_chunks) return;
     cudaMemset2DAsync(M, mstride * 8, 0, (size_t)P.n * 8, (size_t)2 * n_chunks, st);
-    if (n_rows) {
-        // lanes per row ~ mean row length (rows are short in the BASELINE shapes)
-        const size_t threads = (size_t)n_rows << log_tpr;
-        k_pack_cssc<<<(unsigned)((threads + 127) / 128), 128, 0, st>>>(dc, CI, VA, V, rows, n_rows, slices, cols,
-                                                                      n_chunks, log_tpr, M, mstride);
-    }
+    if (n_rows && entries > 0)
+        k_pack_cssc<<<(unsigned)((entries + 127) / 128), 128, 0, st>>>(dc, CI, VA, V, rows, rpre, n_rows, slices,
+                                                                      cols, n_chunks, M, mstride);
     CSSC_CHECK_LAUNCH();
 }
 

@@ -115,8 +115,8 @@ void launch_pointwise_plain(const DevConsts* dc, const RnsParams& P, u64* X, con
 // CSR rows -> CSSC chunk plaintexts (value chunks [0, n_chunks), vector
 // chunks [n_chunks, 2 n_chunks)), slot layout applied; see spmvgpu_encrypt_cssc
 void launch_pack_cssc(const DevConsts* dc, const RnsParams& P, const int64_t* CI, const int64_t* VA,
-                      const int64_t* V, const int4* rows, int n_rows, const int2* slices, const int4* cols,
-                      int n_chunks, int log_tpr, u64* M, size_t mstride, cudaStream_t st);
+                      const int64_t* V, const int4* rows, const int* rpre, int n_rows, long entries,
+                      const int2* slices, const int4* cols, int n_chunks, u64* M, size_t mstride, cudaStream_t st);
 void launch_encode_scatter(const DevConsts* dc, const RnsParams& P, const int64_t* vals,
                            const u64* offs, u64* M, int items, cudaStream_t st, size_t mstride = 0);
 void launch_plain_lift(const DevConsts* dc, const RnsParams& P, const u64* M, u64* PT, int items,

@@ -226,6 +226,7 @@ ClientImage client_image_layout(std::size_t nnz, std::size_t vec_len, std::size_
     img.o_va = l.o_va;
     img.o_v = l.o_v;
     img.o_rows = l.o_rows;
+    img.o_rpre = l.o_rpre;
     img.o_sl = l.o_sl;
     img.o_cols = l.o_cols;
     img.o_st = l.o_st;
@@ -269,12 +270,14 @@ static cssc::CsscLayout layout_of(const ClientImage& img) {
     l.o_va = img.o_va;
     l.o_v = img.o_v;
     l.o_rows = img.o_rows;
+    l.o_rpre = img.o_rpre;
     l.o_sl = img.o_sl;
     l.o_cols = img.o_cols;
     l.o_st = img.o_st;
     l.o_out = img.o_out;
     l.bytes = img.bytes;
     l.nnz = img.nnz;
+    l.entries = img.nnz;  // BatchedSpmv's rows partition the nonzeros
     l.vec_len = img.vec_len;
     l.n_rows = img.n_rows;
     l.n_slices = img.n_slices;
@@ -327,12 +330,14 @@ void client_image_encrypt(spmvgpu_ctx* ctx, ClientImage& img, const spmvgpu_ct* 
     l.o_va = img.o_va;
     l.o_v = img.o_v;
     l.o_rows = img.o_rows;
+    l.o_rpre = img.o_rpre;
     l.o_sl = img.o_sl;
     l.o_cols = img.o_cols;
     l.o_st = img.o_st;
     l.o_out = img.o_out;
     l.bytes = img.bytes;
     l.nnz = img.nnz;
+    l.entries = img.nnz;  // BatchedSpmv's rows partition the nonzeros
     l.vec_len = img.vec_len;
     l.n_rows = img.n_rows;
     l.n_slices = img.n_slices;

@@ -10,7 +10,10 @@
 #include <numeric>
 #include <stdexcept>
 #include <string>
+#include <tuple>
+#include <utility>
 
+#include "host/host_pool.hpp"
 #include "spmv/gpu_backend.hpp"
 
 namespace spmv::detail {
@@ -26,6 +29,10 @@ std::uint64_t column_index_bytes(const std::uint64_t* r, const std::uint64_t* c,
 }
 
 int lowered(int b, int c) { return std::max(0, b - c); }
+
+// batches with at least this many nonzeros use the host pool for the CSR
+// scans and the pinned image (C2's 16 777 stay single-threaded)
+constexpr std::size_t kParallelEntries = 1 << 18;
 
 }  // namespace
 
@@ -58,17 +65,42 @@ BatchedSpmv::BatchedSpmv(spmvgpu_ctx* ctx, const HeParams& hp, std::span<const C
     }
     if (nnz_total > INT32_MAX || vec_total > INT32_MAX)
         throw std::length_error("spmv_batch: more than 2^31 entries in one batch");
+    // large batches: the branch-free CSR scans below run on the host pool
+    // first; the sequential checks then only locate the failure, in order
+    const bool big = nnz_total >= kParallelEntries;
+    bool scanned_ok = false;
+    if (big) {
+        constexpr std::size_t kBlock = 1 << 16;
+        std::vector<std::pair<std::size_t, std::size_t>> tasks;  // (matrix, block)
+        for (std::size_t mi = 0; mi < ms.size(); ++mi)
+            for (std::size_t b0 = 0; b0 * kBlock < std::max(ms[mi].nnz, ms[mi].rows + 1); ++b0) tasks.push_back({mi, b0});
+        std::vector<unsigned char> bad(tasks.size(), 0);
+        HostPool::get().run(tasks.size(), [&](std::size_t t) {
+            const CsrView& m = ms[tasks[t].first];
+            const std::size_t b0 = tasks[t].second * kBlock;
+            bool dec = false;
+            for (std::size_t i = b0; i < std::min(m.rows, b0 + kBlock); ++i) dec |= m.row_ptrs[i + 1] < m.row_ptrs[i];
+            std::uint64_t all_neg = ~std::uint64_t{0}, any_top = 0;
+            for (std::size_t k = b0; k < std::min(m.nnz, b0 + kBlock); ++k) {
+                all_neg &= m.col_indices[k] - m.cols;
+                any_top |= m.col_indices[k];
+            }
+            const bool cols_bad = b0 < m.nnz && (!(all_neg >> 63) || (any_top >> 63));
+            bad[t] = dec || cols_bad;
+        });
+        scanned_ok = std::none_of(bad.begin(), bad.end(), [](unsigned char x) { return x != 0; });
+    }
     std::int64_t nz_next = 0, vec_next = 0;
     for (std::size_t mi = 0; mi < ms.size(); ++mi) {
         const CsrView& m = ms[mi];
         if (m.rows && m.row_ptrs[0] != 0) throw std::invalid_argument("csr: row_ptrs[0] must be 0");
-        {  // branch-free scans (vectorised); the offending entry is located only on failure
+        if (!scanned_ok) {  // branch-free scans (vectorised); the offending entry is located only on failure
             bool dec = false;
             for (std::size_t i = 0; i < m.rows; ++i) dec |= m.row_ptrs[i + 1] < m.row_ptrs[i];
             if (dec) throw std::invalid_argument("csr: row_ptrs must be non-decreasing");
         }
         if (m.rows && m.row_ptrs[m.rows] != m.nnz) throw std::invalid_argument("csr: row_ptrs end is not nnz");
-        {  // all col < cols: every col - cols is negative (and no col has bit 63 set)
+        if (!scanned_ok) {  // all col < cols: every col - cols is negative (and no col has bit 63 set)
             std::uint64_t all_neg = ~std::uint64_t{0}, any_top = 0;
             for (std::size_t k = 0; k < m.nnz; ++k) {
                 all_neg &= m.col_indices[k] - m.cols;
@@ -131,17 +163,43 @@ BatchedSpmv::BatchedSpmv(spmvgpu_ctx* ctx, const HeParams& hp, std::span<const C
                                  colrec_.size() / 4, static_cast<int>(2 * n));
     }
     {
+        // (dst, src, bytes) pieces of the image; large batches copy them on the host pool
+        std::vector<std::tuple<unsigned char*, const void*, std::size_t>> cp;
         std::size_t nz = 0, vo = 0;
         for (const CsrView& m : ms) {
-            std::memcpy(img_.p + img_.o_ci + 8 * nz, m.col_indices, 8 * m.nnz);
-            std::memcpy(img_.p + img_.o_va + 8 * nz, m.values, 8 * m.nnz);
-            std::memcpy(img_.p + img_.o_v + 8 * vo, m.vec, 8 * m.cols);
+            cp.emplace_back(img_.p + img_.o_ci + 8 * nz, m.col_indices, 8 * m.nnz);
+            cp.emplace_back(img_.p + img_.o_va + 8 * nz, m.values, 8 * m.nnz);
+            cp.emplace_back(img_.p + img_.o_v + 8 * vo, m.vec, 8 * m.cols);
             nz += m.nnz;
             vo += m.cols;
         }
-        std::memcpy(img_.p + img_.o_rows, rowrec_.data(), 4 * rowrec_.size());
-        std::memcpy(img_.p + img_.o_sl, slicerec_.data(), 4 * slicerec_.size());
-        std::memcpy(img_.p + img_.o_cols, colrec_.data(), 4 * colrec_.size());
+        cp.emplace_back(img_.p + img_.o_rows, rowrec_.data(), 4 * rowrec_.size());
+        {  // exclusive prefix of the row lengths: the device pack's entry -> row map
+            auto* pre = reinterpret_cast<std::int32_t*>(img_.p + img_.o_rpre);
+            const std::size_t nr = rowrec_.size() / 4;
+            std::int32_t acc = 0;
+            for (std::size_t r = 0; r < nr; ++r) {
+                pre[r] = acc;
+                acc += rowrec_[4 * r + 1];
+            }
+            pre[nr] = acc;
+        }
+        cp.emplace_back(img_.p + img_.o_sl, slicerec_.data(), 4 * slicerec_.size());
+        cp.emplace_back(img_.p + img_.o_cols, colrec_.data(), 4 * colrec_.size());
+        if (big) {
+            constexpr std::size_t kPiece = 1 << 18;
+            std::vector<std::tuple<unsigned char*, const unsigned char*, std::size_t>> pieces;
+            for (auto& [d, src, bytes] : cp)
+                for (std::size_t o = 0; o < bytes; o += kPiece)
+                    pieces.emplace_back(d + o, static_cast<const unsigned char*>(src) + o, std::min(kPiece, bytes - o));
+            HostPool::get().run(pieces.size(), [&](std::size_t i) {
+                const auto& [d, src, bytes] = pieces[i];
+                std::memcpy(d, src, bytes);
+            });
+        } else {
+            for (auto& [d, src, bytes] : cp)
+                if (bytes) std::memcpy(d, src, bytes);
+        }
         std::vector<std::int32_t>().swap(rowrec_);
         std::vector<std::int32_t>().swap(slicerec_);
         std::vector<std::int32_t>().swap(colrec_);

@@ -44,7 +44,8 @@ void plan_lease_free(spmvgpu_ctx* ctx, PlanLease& lease);
 struct ClientImage {
     unsigned char* p = nullptr;
     std::size_t cap = 0;
-    std::size_t o_ci = 0, o_va = 0, o_v = 0, o_rows = 0, o_sl = 0, o_cols = 0, o_st = 0, o_out = 0, bytes = 0;
+    std::size_t o_ci = 0, o_va = 0, o_v = 0, o_rows = 0, o_rpre = 0, o_sl = 0, o_cols = 0, o_st = 0, o_out = 0,
+                bytes = 0;
     std::size_t nnz = 0, vec_len = 0, n_rows = 0, n_slices = 0, n_cols = 0;
     int items = 0;
 };

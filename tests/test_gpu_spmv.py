@@ -259,3 +259,24 @@ def test_pipeline_over_ring_sizes_and_chunk_depths(logn, fused):
         got = pk.spmv_batch(ctx, [m], [v])[0]
         assert_same(got, checker(m, v, ctx.slots, ctx.slots))
     ctx.close()
+
+
+@pytest.mark.parametrize("where", ["first", "middle", "last"])
+def test_large_batch_validation_on_the_host_pool(where):
+    """Batches of >= 2^18 nonzeros scan the CSR arrays on the host pool; a bad
+    column index anywhere is still reported as the sequential check reports it,
+    and a valid large batch evaluates exactly."""
+    ctx = pk.Context(logn=13, seed=2)
+    ms = [pk.random_sparse_csr(2048, 2048, 70000, 100 + i, -8, 8) for i in range(4)]
+    vs = [pk.random_vector(2048, 100 + i, -8, 8, nonzero=True) for i in range(4)]
+    k = {"first": 0, "middle": 35000, "last": 69999}[where]
+    bad = ms[2].col_indices.copy()
+    bad[k] = 2048 + 5
+    mbad = pk.Csr(2048, 2048, ms[2].row_ptrs, bad, ms[2].values)
+    with pytest.raises(pk.SpmvError) as e:
+        pk.spmv_batch(ctx, [ms[0], ms[1], mbad, ms[3]], vs, chunk_size=ctx.slots)
+    assert e.value.kind == "IndexOutOfRangeError" and "2053" in str(e.value)
+    got = pk.spmv_batch(ctx, ms, vs, chunk_size=ctx.slots)
+    for m, v, g in zip(ms, vs, got):
+        assert np.array_equal(g["values"], checker(m, v, ctx.slots, ctx.slots)["values"])
+    ctx.close()
