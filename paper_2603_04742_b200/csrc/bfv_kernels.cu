@@ -1117,14 +1117,24 @@ __global__ void k_pack_cssc(const DevConsts* __restrict__ dc, const int64_t* __r
                             const int4* __restrict__ rows, const int* __restrict__ rpre, int n_rows,
                             const int2* __restrict__ slices, const int4* __restrict__ cols, int n_chunks,
                             u64* __restrict__ M, size_t mstride) {
-    const int e = blockIdx.x * blockDim.x + threadIdx.x;
-    if (n_rows <= 0 || e >= __ldg(rpre + n_rows)) return;
-    int lo = 0, hi = n_rows - 1;  // last r with rpre[r] <= e
-    while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (__ldg(rpre + mid) <= e) lo = mid;
-        else hi = mid - 1;
-    }
+    __shared__ int range[2];
+    const int e0 = blockIdx.x * blockDim.x;
+    const int e = e0 + threadIdx.x;
+    const int total = __ldg(rpre + n_rows);
+    auto row_of = [&](int x, int lo, int hi) {  // last r in [lo, hi] with rpre[r] <= x
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (__ldg(rpre + mid) <= x) lo = mid;
+            else hi = mid - 1;
+        }
+        return lo;
+    };
+    // the CTA's first and last entries bound every thread's search
+    if (threadIdx.x < 2 && e0 < total)
+        range[threadIdx.x] = row_of(threadIdx.x ? min(e0 + (int)blockDim.x, total) - 1 : e0, 0, n_rows - 1);
+    __syncthreads();
+    if (e >= total) return;
+    const int lo = row_of(e, range[0], range[1]);
     const int4 rec = rows[lo];
     const int j = e - __ldg(rpre + lo);
     const int2 sl = slices[rec.w];
