@@ -417,31 +417,32 @@ struct ExtK {
     u64 xq[NX];
     Modulus ym[NY];
     u64 xhat_inv[NX], xhat_inv_sh[NX], R1[NX], R0[NX];
-    u64 xhat_y[NX][NY], xhat_y_sh[NX][NY];
-    u64 X_y[NY], X_y_sh[NY];
+    u32 w0[NX][NY], w1[NX][NY];  // [X/x_i]_{y_j} in 29-bit halves (Dot29)
+    u32 nX0[NY], nX1[NY];        // [-X]_{y_j} in 29-bit halves
 };
+
+static inline u64 host_mulmod(u64 a, u64 b, u64 p) { return (u64)((unsigned __int128)a * b % p); }
 
 template <int NX, int NY>
 static void fill_extk(ExtK<NX, NY>& k, const DevConsts& h, const ExtConsts& e) {
+    static_assert(NX + 1 <= 15, "Dot29 bound: at most 15 terms");
     for (int i = 0; i < NX; ++i) {
         k.xq[i] = h.mod[e.xi[i]].q;
         k.xhat_inv[i] = e.xhat_inv[i];
         k.xhat_inv_sh[i] = e.xhat_inv_sh[i];
         k.R1[i] = e.R1[i];
         k.R0[i] = e.R0[i];
-        for (int j = 0; j < NY; ++j) {
-            k.xhat_y[i][j] = e.xhat_y[i][j];
-            k.xhat_y_sh[i][j] = e.xhat_y_sh[i][j];
-        }
+        for (int j = 0; j < NY; ++j) split29(e.xhat_y[i][j], k.w0[i][j], k.w1[i][j]);
     }
     for (int j = 0; j < NY; ++j) {
         k.ym[j] = h.mod[e.yi[j]];
-        k.X_y[j] = e.X_y[j];
-        k.X_y_sh[j] = e.X_y_sh[j];
+        const u64 p = k.ym[j].q;
+        split29((p - e.X_y[j] % p) % p, k.nX0[j], k.nX1[j]);
     }
 }
 
-// extend_exact with the constants from a parameter block (same formulas)
+// extend_exact with the constants from a parameter block: the same value,
+// sum_i y_i [X/x_i]_p - v [X]_p mod p, as one Dot29 per target prime
 template <int NX, int NY>
 __device__ __forceinline__ void extend_k(const ExtK<NX, NY>& e, const u64* x, u64* out) {
     u64 y[NX];
@@ -451,15 +452,14 @@ __device__ __forceinline__ void extend_k(const ExtK<NX, NY>& e, const u64* x, u6
         y[i] = shoup(x[i], e.xhat_inv[i], e.xhat_inv_sh[i], e.xq[i]);
         add128(shi, slo, 0, frac64(y[i], e.R1[i], e.R0[i]));
     }
-    const u64 v = shi + (slo >> 63);
+    const u32 v = (u32)(shi + (slo >> 63));  // <= NX
 #pragma unroll
     for (int j = 0; j < NY; ++j) {
-        const u64 p = e.ym[j].q;
-        u64 acc = 0;
+        Dot29 d;
 #pragma unroll
-        for (int i = 0; i < NX; ++i) acc += shoup_lazy(y[i], e.xhat_y[i][j], e.xhat_y_sh[i][j], p);
-        acc = reduce_small_quot(acc, e.ym[j]);
-        out[j] = sub_mod(acc, shoup(v, e.X_y[j], e.X_y_sh[j], p), p);
+        for (int i = 0; i < NX; ++i) dot29_mac(d, y[i], e.w0[i][j], e.w1[i][j]);
+        dot29_mac_small(d, v, e.nX0[j], e.nX1[j]);
+        out[j] = dot29_reduce(d, e.ym[j]);
     }
 }
 
@@ -542,8 +542,10 @@ struct ScaleK {
     int n;
     u64 q[L], QhatInv[L], QhatInv_sh[L], T1[L], T0[L];
     Modulus bm[L + 1];
-    u64 QhatB[L][L + 1], QhatB_sh[L][L + 1];
-    u64 QinvB[L + 1], QinvB_sh[L + 1], tB[L + 1], tB_sh[L + 1];
+    // w_j = rr - t [ (sum_i x_i [Q/q_i]_{b_j} - z_j) Q^-1 ]_{b_j}
+    //     = rr + sum_i x_i C_ij + z_j D_j  mod b_j  (one Dot29 per b_j)
+    u32 C0[L][L + 1], C1[L][L + 1];  // [-[Q/q_i]_{b_j} Q^-1 t]_{b_j}
+    u32 D0[L + 1], D1[L + 1];        // [Q^-1 t]_{b_j}
     ExtK<L + 1, L> bq;
 };
 
@@ -566,16 +568,15 @@ __global__ void k_mul_scale_k(const __grid_constant__ ScaleK<L> c, const u64* __
         add128(shi, slo, umulhi(xi[i], c.T1[i]), xi[i] * c.T1[i]);
         add128(shi, slo, 0, umulhi(xi[i], c.T0[i]));
     }
-    const u64 rr = shi + (slo >> 63);
+    const u64 rr = shi + (slo >> 63);  // < L t + 1
 #pragma unroll
     for (int j = 0; j < nB; ++j) {
-        const u64 bj = c.bm[j].q;
-        u64 acc = 0;
+        Dot29 d;
+        d.a0 = rr;
 #pragma unroll
-        for (int i = 0; i < L; ++i) acc += shoup_lazy(xi[i], c.QhatB[i][j], c.QhatB_sh[i][j], bj);
-        acc = reduce_small_quot(acc, c.bm[j]);
-        const u64 alpha = shoup(sub_mod(acc, z[(size_t)(L + j) * n + k], bj), c.QinvB[j], c.QinvB_sh[j], bj);
-        w[j] = sub_mod(rr, shoup(alpha, c.tB[j], c.tB_sh[j], bj), bj);
+        for (int i = 0; i < L; ++i) dot29_mac(d, xi[i], c.C0[i][j], c.C1[i][j]);
+        dot29_mac(d, z[(size_t)(L + j) * n + k], c.D0[j], c.D1[j]);
+        w[j] = dot29_reduce(d, c.bm[j]);
     }
     extend_k(c.bq, w, o);
     u64* dst = r < 2 ? OUT[item] + (size_t)r * L * n : D2 + (size_t)item * L * n;
@@ -602,17 +603,12 @@ static ScaleK<L> make_scale_k(const RnsParams& P) {
         c.QhatInv_sh[i] = h.QhatInv_sh[i];
         c.T1[i] = h.T1[i];
         c.T0[i] = h.T0[i];
-        for (int j = 0; j <= L; ++j) {
-            c.QhatB[i][j] = h.QhatB[i][j];
-            c.QhatB_sh[i][j] = h.QhatB_sh[i][j];
-        }
     }
     for (int j = 0; j <= L; ++j) {
         c.bm[j] = h.mod[L + P.cfg.K + j];
-        c.QinvB[j] = h.QinvB[j];
-        c.QinvB_sh[j] = h.QinvB_sh[j];
-        c.tB[j] = h.tB[j];
-        c.tB_sh[j] = h.tB_sh[j];
+        const u64 b = c.bm[j].q, D = host_mulmod(h.QinvB[j], h.tB[j], b);
+        split29(D, c.D0[j], c.D1[j]);
+        for (int i = 0; i < L; ++i) split29((b - host_mulmod(h.QhatB[i][j], D, b)) % b, c.C0[i][j], c.C1[i][j]);
     }
     fill_extk(c.bq, h, h.extBQ);
     return c;
@@ -929,17 +925,20 @@ struct ModDownK {
     int n;
     u64 pk[K], phat_inv[K], phat_inv_sh[K];
     Modulus qm[L];
-    u64 phat_q[K][L], phat_q_sh[K][L];
-    u64 Pinv_q[L], Pinv_q_sh[L];
+    // out_j = (acc_j - sum_k y_k [P/p_k]_{q_j}) P^-1 = acc_j Pinv + sum_k y_k E_kj
+    u32 E0[K][L], E1[K][L];  // [-[P/p_k]_{q_j} P^-1]_{q_j} in 29-bit halves
+    u32 F0[L], F1[L];        // [P^-1]_{q_j}
 };
 
-// k_ks_moddown with the constants from a parameter block (same formulas)
+// k_ks_moddown with the constants from a parameter block (same values; the
+// ModDown of each target limb is one Dot29 of K + 1 terms)
 template <int L, int K>
 __global__ void __launch_bounds__(128, 6) k_ks_moddown_k(const __grid_constant__ ModDownK<L, K> c,
                                                          const u64* __restrict__ ACC, const u64* const* BASE,
                                                          const u64* const* RSRC, const u32* ginv, u64* const* OUT,
                                                          const u64* const* EXTRA) {
     constexpr int LK = L + K;
+    static_assert(K + 1 <= 15, "Dot29 bound");
     const int n = c.n;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     const int item = blockIdx.y;
@@ -961,11 +960,11 @@ __global__ void __launch_bounds__(128, 6) k_ks_moddown_k(const __grid_constant__
 #pragma unroll 2
     for (int j = 0; j < L; ++j) {
         const u64 q = c.qm[j].q;
-        u64 v = 0;
+        Dot29 d;
+        dot29_mac(d, acc[(size_t)j * n + k], c.F0[j], c.F1[j]);  // canonical inverse-NTT output
 #pragma unroll
-        for (int kk = 0; kk < K; ++kk) v += shoup_lazy(y[kk], c.phat_q[kk][j], c.phat_q_sh[kk][j], q);
-        v = reduce_small_quot(v, c.qm[j]);
-        v = shoup(sub_mod(acc[(size_t)j * n + k], v, q), c.Pinv_q[j], c.Pinv_q_sh[j], q);
+        for (int kk = 0; kk < K; ++kk) dot29_mac(d, y[kk], c.E0[kk][j], c.E1[kk][j]);
+        u64 v = dot29_reduce(d, c.qm[j]);
         if (base) v = add_mod(v, base[(size_t)j * n + k], q);
         if (ex) v = add_mod(v, ex[(size_t)j * n + k], q);
         if (rs) {
@@ -985,15 +984,13 @@ static ModDownK<L, K> make_moddown_k(const RnsParams& P) {
         c.pk[kk] = h.mod[L + kk].q;
         c.phat_inv[kk] = h.phat_inv[kk];
         c.phat_inv_sh[kk] = h.phat_inv_sh[kk];
-        for (int j = 0; j < L; ++j) {
-            c.phat_q[kk][j] = h.phat_q[kk][j];
-            c.phat_q_sh[kk][j] = h.phat_q_sh[kk][j];
-        }
     }
     for (int j = 0; j < L; ++j) {
         c.qm[j] = h.mod[j];
-        c.Pinv_q[j] = h.Pinv_q[j];
-        c.Pinv_q_sh[j] = h.Pinv_q_sh[j];
+        const u64 q = h.mod[j].q;
+        split29(h.Pinv_q[j], c.F0[j], c.F1[j]);
+        for (int kk = 0; kk < K; ++kk)
+            split29((q - host_mulmod(h.phat_q[kk][j], h.Pinv_q[j], q)) % q, c.E0[kk][j], c.E1[kk][j]);
     }
     return c;
 }
