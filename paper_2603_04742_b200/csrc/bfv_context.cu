@@ -621,17 +621,17 @@ void GpuContext::mul_relin(const std::vector<const u64*>& a, const std::vector<c
 
 void GpuContext::rotate_dev(const u64* const* SRC, const u32* ginv, const u64* const* KEY,
                             const u64* const* BASE, u64* const* OUT, int items, u64* DX, u64* ACC,
-                            const u64* const* EXTRA) {
+                            const u64* const* EXTRA, const int* PAIR) {
     const int LK = P_.cfg.L + P_.cfg.K, logn = P_.cfg.logn;
     if (fused_ks_) {
-        launch_ks_fused(dc_, P_, SRC, nullptr, 1, ginv, KEY, BASE, SRC, OUT, DX, ACC, items, st_, EXTRA);
+        launch_ks_fused(dc_, P_, SRC, nullptr, 1, ginv, KEY, BASE, SRC, OUT, DX, ACC, items, st_, EXTRA, PAIR);
         stats_.kernels += 4;
     } else {
         launch_ks_modup(dc_, P_, SRC, 1, ginv, DX, items, st_);
         launch_ntt(dc_, logn, false, job(DX, DX, P_.dnum * LK, range_idx(0, LK)), items, st_);
         launch_ks_inner(dc_, P_, DX, KEY, ACC, items, st_);
         launch_ntt(dc_, logn, true, job(ACC, ACC, 2 * LK, range_idx(0, LK)), items, st_);
-        launch_ks_moddown(dc_, P_, ACC, BASE, SRC, ginv, OUT, items, st_, EXTRA);
+        launch_ks_moddown(dc_, P_, ACC, BASE, SRC, ginv, OUT, items, st_, EXTRA, PAIR);
         stats_.kernels += 7;
     }
     stats_.limb_ntts += (u64)items * (P_.dnum * LK + 2 * LK);

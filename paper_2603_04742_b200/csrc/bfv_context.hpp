@@ -159,10 +159,11 @@ public:
     void mul_relin_dev(const u64* const* A, const u64* const* B, u64* const* OUT, int items,
                        u64* T, u64* Z, u64* D2, u64* DX, u64* ACC, const u64* const* RLK,
                        const EncIn* enc = nullptr);
-    // OUT = BASE + EXTRA + rot(SRC) (BASE / EXTRA per-item nullable)
+    // OUT = BASE + EXTRA + rot(SRC) (BASE / EXTRA per-item nullable); PAIR (nullable):
+    // PAIR[i] = j >= 0 also adds item j's rotation into OUT[i], -2 skips item i
     void rotate_dev(const u64* const* SRC, const u32* ginv, const u64* const* KEY,
                     const u64* const* BASE, u64* const* OUT, int items, u64* DX, u64* ACC,
-                    const u64* const* EXTRA = nullptr);
+                    const u64* const* EXTRA = nullptr, const int* PAIR = nullptr);
     void encode_masks(const std::vector<int>& ones_len, u64* MASKS);  // NTT form [m][L][N]
     NttJob job(const u64* src, u64* dst, int limbs, const std::vector<int>& pidx) const;
 

@@ -872,35 +872,43 @@ void launch_ks_inner(const DevConsts* dc, const RnsParams& P, const u64* DX,
 }
 
 // E4 + fused adds: out = BASE[item] + EXTRA[item] + phi_g(RSRC[item].c0) + ModDown(acc);
-// per-item BASE / EXTRA entries may be null
+// per-item BASE / EXTRA entries may be null.  PAIR (nullable): PAIR[item] = j >= 0
+// also adds item j's rotation phi_gj(RSRC[j].c0) + ModDown(acc_j) (item j has no
+// BASE / EXTRA of its own), and PAIR[item] = -2 skips the item (merged elsewhere).
+// Every sum is exact mod q, so merging two rotations' adds into one pass gives
+// the words of the separate rotate and add.
 // one polynomial per grid z-slice; the output loop is only partly unrolled so
 // the acc/base/extra loads of all limbs are not hoisted into registers at once
 template <int LT, int KT, int AT>
 __global__ void __launch_bounds__(128, 6) k_ks_moddown(const DevConsts* __restrict__ dc, const u64* __restrict__ ACC,
                              const u64* const* BASE, const u64* const* RSRC, const u32* ginv,
-                             u64* const* OUT, const u64* const* EXTRA) {
+                             u64* const* OUT, const u64* const* EXTRA, const int* PAIR) {
     const int n = dc->n, L = LT ? LT : dc->L, K = KT ? KT : dc->K, LK = L + K;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     const int item = blockIdx.y;
+    const int pair = PAIR ? PAIR[item] : -1;
+    if (pair == -2) return;
+    const int nsrc = pair >= 0 ? 2 : 1;
     const size_t PL = (size_t)LK * n;
-    bool neg = false;
-    int ridx = k;
-    if (RSRC) ridx = automorph_src(ginv ? ginv[item] : 0u, k, n, neg);
-    u64 y[MAXL];
-    {
-        const int p = blockIdx.z;
-        const u64* acc = ACC + ((size_t)item * 2 + p) * PL;
+    const int p = blockIdx.z;
+    u64* out = OUT[item] + (size_t)p * L * n;
+    const u64* base = BASE ? BASE[item] : nullptr;
+    if (base) base += (size_t)p * L * n;
+    const u64* ex = EXTRA ? EXTRA[item] : nullptr;
+    if (ex) ex += (size_t)p * L * n;
+    for (int s = 0; s < nsrc; ++s) {
+        const int it = s ? pair : item;
+        bool neg = false;
+        int ridx = k;
+        if (RSRC) ridx = automorph_src(ginv ? ginv[it] : 0u, k, n, neg);
+        u64 y[MAXL];
+        const u64* acc = ACC + ((size_t)it * 2 + p) * PL;
 #pragma unroll
         for (int kk = 0; kk < K; ++kk) {
             const u64 pk = dc->mod[L + kk].q;
             y[kk] = shoup(acc[(size_t)(L + kk) * n + k], dc->phat_inv[kk], dc->phat_inv_sh[kk], pk);
         }
-        u64* out = OUT[item] + (size_t)p * L * n;
-        const u64* base = BASE ? BASE[item] : nullptr;
-        if (base) base += (size_t)p * L * n;
-        const u64* ex = EXTRA ? EXTRA[item] : nullptr;
-        if (ex) ex += (size_t)p * L * n;
-        const u64* rs = (RSRC && p == 0) ? RSRC[item] : nullptr;
+        const u64* rs = (RSRC && p == 0) ? RSRC[it] : nullptr;
 #pragma unroll 2
         for (int j = 0; j < L; ++j) {
             const u64 q = dc->mod[j].q;
@@ -909,8 +917,12 @@ __global__ void __launch_bounds__(128, 6) k_ks_moddown(const DevConsts* __restri
             for (int kk = 0; kk < K; ++kk) c += shoup_lazy(y[kk], dc->phat_q[kk][j], dc->phat_q_sh[kk][j], q);
             c = reduce_small_quot(c, dc->mod[j]);
             u64 v = shoup(sub_mod(acc[(size_t)j * n + k], c, q), dc->Pinv_q[j], dc->Pinv_q_sh[j], q);
-            if (base) v = add_mod(v, base[(size_t)j * n + k], q);
-            if (ex) v = add_mod(v, ex[(size_t)j * n + k], q);
+            if (s) {
+                v = add_mod(v, out[(size_t)j * n + k], q);  // this thread's own first-pass word
+            } else {
+                if (base) v = add_mod(v, base[(size_t)j * n + k], q);
+                if (ex) v = add_mod(v, ex[(size_t)j * n + k], q);
+            }
             if (rs) {
                 const u64 r = rs[(size_t)j * n + ridx];
                 v = add_mod(v, neg ? neg_mod(r, q) : r, q);
@@ -931,47 +943,76 @@ struct ModDownK {
 };
 
 // k_ks_moddown with the constants from a parameter block (same values; the
-// ModDown of each target limb is one Dot29 of K + 1 terms)
+// ModDown of each target limb is one Dot29 of K + 1 terms; same PAIR merge)
 template <int L, int K>
 __global__ void __launch_bounds__(128, 6) k_ks_moddown_k(const __grid_constant__ ModDownK<L, K> c,
                                                          const u64* __restrict__ ACC, const u64* const* BASE,
                                                          const u64* const* RSRC, const u32* ginv, u64* const* OUT,
-                                                         const u64* const* EXTRA) {
+                                                         const u64* const* EXTRA, const int* PAIR) {
     constexpr int LK = L + K;
     static_assert(K + 1 <= 15, "Dot29 bound");
     const int n = c.n;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     const int item = blockIdx.y;
+    const int pair = PAIR ? PAIR[item] : -1;
+    if (pair == -2) return;
     const int p = blockIdx.z;
-    bool neg = false;
-    int ridx = k;
-    if (RSRC) ridx = automorph_src(ginv ? ginv[item] : 0u, k, n, neg);
-    const u64* acc = ACC + ((size_t)item * 2 + p) * LK * n;
-    u64 y[K];
-#pragma unroll
-    for (int kk = 0; kk < K; ++kk)
-        y[kk] = shoup(acc[(size_t)(L + kk) * n + k], c.phat_inv[kk], c.phat_inv_sh[kk], c.pk[kk]);
     u64* out = OUT[item] + (size_t)p * L * n;
     const u64* base = BASE ? BASE[item] : nullptr;
     if (base) base += (size_t)p * L * n;
     const u64* ex = EXTRA ? EXTRA[item] : nullptr;
     if (ex) ex += (size_t)p * L * n;
-    const u64* rs = (RSRC && p == 0) ? RSRC[item] : nullptr;
-#pragma unroll 2
-    for (int j = 0; j < L; ++j) {
+    auto setup = [&](int it, u64* y, const u64*& acc, const u64*& rs, int& ridx, bool& neg) {
+        neg = false;
+        ridx = k;
+        if (RSRC) ridx = automorph_src(ginv ? ginv[it] : 0u, k, n, neg);
+        acc = ACC + ((size_t)it * 2 + p) * LK * n;
+#pragma unroll
+        for (int kk = 0; kk < K; ++kk)
+            y[kk] = shoup(acc[(size_t)(L + kk) * n + k], c.phat_inv[kk], c.phat_inv_sh[kk], c.pk[kk]);
+        rs = (RSRC && p == 0) ? RSRC[it] : nullptr;
+    };
+    auto term = [&](int j, const u64* y, const u64* acc, const u64* rs, int ridx, bool neg) {
         const u64 q = c.qm[j].q;
         Dot29 d;
         dot29_mac(d, acc[(size_t)j * n + k], c.F0[j], c.F1[j]);  // canonical inverse-NTT output
 #pragma unroll
         for (int kk = 0; kk < K; ++kk) dot29_mac(d, y[kk], c.E0[kk][j], c.E1[kk][j]);
         u64 v = dot29_reduce(d, c.qm[j]);
-        if (base) v = add_mod(v, base[(size_t)j * n + k], q);
-        if (ex) v = add_mod(v, ex[(size_t)j * n + k], q);
         if (rs) {
             const u64 r = rs[(size_t)j * n + ridx];
             v = add_mod(v, neg ? neg_mod(r, q) : r, q);
         }
-        out[(size_t)j * n + k] = v;
+        return v;
+    };
+    u64 y[K];
+    const u64 *acc, *rs;
+    int ridx;
+    bool neg;
+    setup(item, y, acc, rs, ridx, neg);
+    if (pair < 0) {
+#pragma unroll 2
+        for (int j = 0; j < L; ++j) {
+            const u64 q = c.qm[j].q;
+            u64 v = term(j, y, acc, rs, ridx, neg);
+            if (base) v = add_mod(v, base[(size_t)j * n + k], q);
+            if (ex) v = add_mod(v, ex[(size_t)j * n + k], q);
+            out[(size_t)j * n + k] = v;
+        }
+    } else {  // merged rotation of item `pair`
+        u64 y2[K];
+        const u64 *acc2, *rs2;
+        int ridx2;
+        bool neg2;
+        setup(pair, y2, acc2, rs2, ridx2, neg2);
+#pragma unroll 1
+        for (int j = 0; j < L; ++j) {
+            const u64 q = c.qm[j].q;
+            u64 v = add_mod(term(j, y, acc, rs, ridx, neg), term(j, y2, acc2, rs2, ridx2, neg2), q);
+            if (base) v = add_mod(v, base[(size_t)j * n + k], q);
+            if (ex) v = add_mod(v, ex[(size_t)j * n + k], q);
+            out[(size_t)j * n + k] = v;
+        }
     }
 }
 
@@ -997,7 +1038,7 @@ static ModDownK<L, K> make_moddown_k(const RnsParams& P) {
 
 void launch_ks_moddown(const DevConsts* dc, const RnsParams& P, const u64* ACC,
                        const u64* const* BASE, const u64* const* RSRC, const u32* ginv,
-                       u64* const* OUT, int items, cudaStream_t st, const u64* const* EXTRA) {
+                       u64* const* OUT, int items, cudaStream_t st, const u64* const* EXTRA, const int* PAIR) {
     if (!items) return;
     dispatch_shape(P, [&](auto l_, auto k_, auto a_) {
         dim3 g = ew_grid(P.n, items);
@@ -1005,9 +1046,9 @@ void launch_ks_moddown(const DevConsts* dc, const RnsParams& P, const u64* ACC,
         constexpr int LT = decltype(l_)::value, KT = decltype(k_)::value;
         if constexpr (LT > 0)
             k_ks_moddown_k<LT, KT><<<g, EW_THREADS, 0, st>>>(make_moddown_k<LT, KT>(P), ACC, BASE, RSRC, ginv, OUT,
-                                                            EXTRA);
+                                                            EXTRA, PAIR);
         else
-            k_ks_moddown<SHAPE_ARGS><<<g, EW_THREADS, 0, st>>>(dc, ACC, BASE, RSRC, ginv, OUT, EXTRA);
+            k_ks_moddown<SHAPE_ARGS><<<g, EW_THREADS, 0, st>>>(dc, ACC, BASE, RSRC, ginv, OUT, EXTRA, PAIR);
     });
     CSSC_CHECK_LAUNCH();
 }

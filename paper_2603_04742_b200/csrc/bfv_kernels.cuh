@@ -101,7 +101,8 @@ void launch_ks_inner(const DevConsts* dc, const RnsParams& P, const u64* DX,
 //          + ModDown(ACC[p])
 void launch_ks_moddown(const DevConsts* dc, const RnsParams& P, const u64* ACC,
                        const u64* const* BASE, const u64* const* RSRC, const u32* ginv,
-                       u64* const* OUT, int items, cudaStream_t st, const u64* const* EXTRA = nullptr);
+                       u64* const* OUT, int items, cudaStream_t st, const u64* const* EXTRA = nullptr,
+                       const int* PAIR = nullptr);
 
 // masks / plaintext products
 void launch_mask_accum(const DevConsts* dc, const RnsParams& P, const u64* MT,
@@ -182,5 +183,5 @@ bool launch_ks_cluster(const DevConsts* dc, const RnsParams& P, const u64* const
 void launch_ks_fused(const DevConsts* dc, const RnsParams& P, const u64* const* SRC, const u64* SRCC,
                      int src_poly, const u32* ginv, const u64* const* KEY, const u64* const* BASE,
                      const u64* const* RSRC, u64* const* OUT, u64* DX, u64* ACC, int items, cudaStream_t st,
-                     const u64* const* EXTRA = nullptr);
+                     const u64* const* EXTRA = nullptr, const int* PAIR = nullptr);
 }  // namespace cssc

@@ -172,12 +172,11 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
         gi = inverse_galois(g, P.n);
         return ctx.galois_key(g);
     };
-    std::vector<const u64*> pre_a, pre_b;
-    std::vector<u64*> pre_out;
     for (int l = 0; l < depth; ++l) {
         std::vector<const u64*> src, base, key, extra;
         std::vector<u64*> o;
         std::vector<u32> gi;
+        std::vector<int> pair;  // -1 plain, j merge item j, -2 merged elsewhere
         std::set<u32> lvl_keys;
         size_t odd_slot = 0;
         for (int k = 0; k < n && (int)trees[order[k]].dbl.size() > l; ++k) {
@@ -198,6 +197,11 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
         if (l == 0) {  // hoisted odd steps: rot(prod) of every chunk, same launch
             for (int k = 0; k < n; ++k) {
                 for (const auto& [after, off] : trees[order[k]].odd) {
+                    if (after == 1) {  // follows D_1: merged into D_1's ModDown (PAIR)
+                        pair.resize(o.size() + 1, -1);
+                        pair[k] = (int)o.size();
+                        pair[o.size()] = -2;
+                    }
                     u64* slot = rp_.words() + (odd_slot++) * ctw;
                     u32 g;
                     key.push_back(key_of(off, lvl_keys, g));
@@ -207,11 +211,6 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
                     extra.push_back(nullptr);
                     o.push_back(slot);
                     rp_after[k][after] = slot;
-                    if (after == 1) {  // follows D_1: elementwise add once level 0 is done
-                        pre_a.push_back(acc_after(k, 1));
-                        pre_b.push_back(slot);
-                        pre_out.push_back(acc_after(k, 1));
-                    }
                 }
             }
         }
@@ -223,18 +222,13 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
         lv.key = put(key);
         lv.ginv = put(gi);
         lv.extra = put(extra);
+        pair.resize(o.size(), -1);
+        lv.pair = std::count(pair.begin(), pair.end(), -2) ? put(pair) : nullptr;
         lv.keys = (int)lvl_keys.size();
         levels_.push_back(lv);
         stats_.hbm_bytes += (u64)lv.items * 3 * C + lvl_keys.size() * KEY;
         stats_.key_bytes += lvl_keys.size() * KEY;
         stats_.kernels += fused ? 4 : 7;
-        if (l == 0 && !pre_out.empty()) {
-            add_items_ = (int)pre_out.size();
-            ADD_A_ = put(pre_a);
-            ADD_B_ = put(pre_b);
-            ADD_OUT_ = put(pre_out);
-            stats_.kernels += 1;
-        }
     }
     stats_.distinct_keys = all_keys.size();
 
@@ -305,12 +299,8 @@ void CloudPlan::record(std::vector<cudaEvent_t>* marks, u64* dec_d, const EncIn*
     for (size_t l = 0; l < levels_.size(); ++l) {
         const Level& lv = levels_[l];
         ctx_.rotate_dev(lv.src, lv.ginv, lv.key, lv.base, lv.out, lv.items, DX_.words(), ACC_.words(),
-                        lv.extra);
+                        lv.extra, lv.pair);
         mark();
-        if (l == 0 && add_items_) {
-            launch_add(ctx_.dconsts(), P, ADD_A_, ADD_B_, ADD_OUT_, add_items_, st);
-            mark();
-        }
     }
     std::vector<int> qidx(L);
     std::iota(qidx.begin(), qidx.end(), 0);
@@ -351,7 +341,6 @@ std::vector<PhaseTiming> CloudPlan::profile() {
         const Level& lv = levels_[l];
         out.push_back({"rotate level " + std::to_string(l), 0, (u64)lv.items,
                        (u64)lv.items * 3 * C + (u64)lv.keys * KEY, (u64)lv.items * ks_ntts});
-        if (l == 0 && add_items_) out.push_back({"add", 0, (u64)add_items_, (u64)add_items_ * 3 * C, 0});
     }
     out.push_back({"mask accumulate", 0, (u64)n_, (u64)n_ * 2 * C + (u64)n_masks_ * PT,
                    (u64)n_ * 2 * L + (u64)ns_ * 2 * L});

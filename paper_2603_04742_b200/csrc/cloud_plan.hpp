@@ -101,13 +101,10 @@ private:
         const u64* const* key;
         const u32* ginv;
         const u64* const* extra;  // fused add of a hoisted odd-step rotation (nullable)
+        const int* pair;          // level 0: D_1 items merging their O_1 rotation (nullable)
         int keys;                  // distinct switching keys of the level
     };
     std::vector<Level> levels_;
-    int add_items_ = 0;  // odd steps right after D_1: added once level 0 is done
-    const u64* const* ADD_A_ = nullptr;
-    const u64* const* ADD_B_ = nullptr;
-    u64* const* ADD_OUT_ = nullptr;
     const u64* const* FINAL_ = nullptr;
     u64* const* OUT_ = nullptr;
     const int* slice_off_ = nullptr;

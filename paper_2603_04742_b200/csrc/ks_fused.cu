@@ -257,10 +257,10 @@ template <int LOGN, int LT, int KT, int AT>
 static void ks_fused_t(const DevConsts* dc, const RnsParams& P, const u64* const* SRC, const u64* SRCC,
                        int src_poly, const u32* ginv, const u64* const* KEY, const u64* const* BASE,
                        const u64* const* RSRC, u64* const* OUT, u64* DX, u64* ACC, int items, cudaStream_t st,
-                       const u64* const* EXTRA) {
+                       const u64* const* EXTRA, const int* PAIR) {
     using G = Ntt2<LOGN>;
     if (launch_ks_cluster(dc, P, SRC, SRCC, src_poly, ginv, KEY, ACC, items, st)) {
-        launch_ks_moddown(dc, P, ACC, BASE, RSRC, ginv, OUT, items, st, EXTRA);
+        launch_ks_moddown(dc, P, ACC, BASE, RSRC, ginv, OUT, items, st, EXTRA, PAIR);
         return;
     }
     const int L = P.cfg.L, K = P.cfg.K, LK = L + K, dnum = P.dnum;
@@ -301,32 +301,32 @@ static void ks_fused_t(const DevConsts* dc, const RnsParams& P, const u64* const
     j.dst = ACC;
     j.limbs = 2 * LK;
     launch_ntt_phase(dc, LOGN, /*inverse=*/true, /*cols=*/true, j, items, st);
-    launch_ks_moddown(dc, P, ACC, BASE, RSRC, ginv, OUT, items, st, EXTRA);
+    launch_ks_moddown(dc, P, ACC, BASE, RSRC, ginv, OUT, items, st, EXTRA, PAIR);
 }
 
 template <int LOGN>
 static void ks_fused_logn(const DevConsts* dc, const RnsParams& P, const u64* const* SRC, const u64* SRCC,
                           int src_poly, const u32* ginv, const u64* const* KEY, const u64* const* BASE,
                           const u64* const* RSRC, u64* const* OUT, u64* DX, u64* ACC, int items, cudaStream_t st,
-                       const u64* const* EXTRA) {
+                       const u64* const* EXTRA, const int* PAIR) {
     ks_dispatch_shape(P, [&](auto l_, auto k_, auto a_) {
         ks_fused_t<LOGN, decltype(l_)::value, decltype(k_)::value, decltype(a_)::value>(
-            dc, P, SRC, SRCC, src_poly, ginv, KEY, BASE, RSRC, OUT, DX, ACC, items, st, EXTRA);
+            dc, P, SRC, SRCC, src_poly, ginv, KEY, BASE, RSRC, OUT, DX, ACC, items, st, EXTRA, PAIR);
     });
 }
 
 void launch_ks_fused(const DevConsts* dc, const RnsParams& P, const u64* const* SRC, const u64* SRCC,
                      int src_poly, const u32* ginv, const u64* const* KEY, const u64* const* BASE,
                      const u64* const* RSRC, u64* const* OUT, u64* DX, u64* ACC, int items, cudaStream_t st,
-                       const u64* const* EXTRA) {
+                       const u64* const* EXTRA, const int* PAIR) {
     if (!items) return;
     switch (P.cfg.logn) {
-        case 10: ks_fused_logn<10>(dc, P, SRC, SRCC, src_poly, ginv, KEY, BASE, RSRC, OUT, DX, ACC, items, st, EXTRA); break;
-        case 11: ks_fused_logn<11>(dc, P, SRC, SRCC, src_poly, ginv, KEY, BASE, RSRC, OUT, DX, ACC, items, st, EXTRA); break;
-        case 12: ks_fused_logn<12>(dc, P, SRC, SRCC, src_poly, ginv, KEY, BASE, RSRC, OUT, DX, ACC, items, st, EXTRA); break;
-        case 13: ks_fused_logn<13>(dc, P, SRC, SRCC, src_poly, ginv, KEY, BASE, RSRC, OUT, DX, ACC, items, st, EXTRA); break;
-        case 14: ks_fused_logn<14>(dc, P, SRC, SRCC, src_poly, ginv, KEY, BASE, RSRC, OUT, DX, ACC, items, st, EXTRA); break;
-        case 15: ks_fused_logn<15>(dc, P, SRC, SRCC, src_poly, ginv, KEY, BASE, RSRC, OUT, DX, ACC, items, st, EXTRA); break;
+        case 10: ks_fused_logn<10>(dc, P, SRC, SRCC, src_poly, ginv, KEY, BASE, RSRC, OUT, DX, ACC, items, st, EXTRA, PAIR); break;
+        case 11: ks_fused_logn<11>(dc, P, SRC, SRCC, src_poly, ginv, KEY, BASE, RSRC, OUT, DX, ACC, items, st, EXTRA, PAIR); break;
+        case 12: ks_fused_logn<12>(dc, P, SRC, SRCC, src_poly, ginv, KEY, BASE, RSRC, OUT, DX, ACC, items, st, EXTRA, PAIR); break;
+        case 13: ks_fused_logn<13>(dc, P, SRC, SRCC, src_poly, ginv, KEY, BASE, RSRC, OUT, DX, ACC, items, st, EXTRA, PAIR); break;
+        case 14: ks_fused_logn<14>(dc, P, SRC, SRCC, src_poly, ginv, KEY, BASE, RSRC, OUT, DX, ACC, items, st, EXTRA, PAIR); break;
+        case 15: ks_fused_logn<15>(dc, P, SRC, SRCC, src_poly, ginv, KEY, BASE, RSRC, OUT, DX, ACC, items, st, EXTRA, PAIR); break;
         default: throw std::invalid_argument("key switch: unsupported logn");
     }
 }
