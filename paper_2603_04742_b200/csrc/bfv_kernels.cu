@@ -417,8 +417,8 @@ struct ExtK {
     u64 xq[NX];
     Modulus ym[NY];
     u64 xhat_inv[NX], xhat_inv_sh[NX], R1[NX], R0[NX];
-    u32 w0[NX][NY], w1[NX][NY];  // [X/x_i]_{y_j} in 29-bit halves (Dot29)
-    u32 nX0[NY], nX1[NY];        // [-X]_{y_j} in 29-bit halves
+    W29 w[NX][NY];  // [X/x_i]_{y_j} in 29-bit halves (Dot29)
+    W29 nX[NY];     // [-X]_{y_j}
 };
 
 static inline u64 host_mulmod(u64 a, u64 b, u64 p) { return (u64)((unsigned __int128)a * b % p); }
@@ -432,12 +432,12 @@ static void fill_extk(ExtK<NX, NY>& k, const DevConsts& h, const ExtConsts& e) {
         k.xhat_inv_sh[i] = e.xhat_inv_sh[i];
         k.R1[i] = e.R1[i];
         k.R0[i] = e.R0[i];
-        for (int j = 0; j < NY; ++j) split29(e.xhat_y[i][j], k.w0[i][j], k.w1[i][j]);
+        for (int j = 0; j < NY; ++j) k.w[i][j] = split29(e.xhat_y[i][j]);
     }
     for (int j = 0; j < NY; ++j) {
         k.ym[j] = h.mod[e.yi[j]];
         const u64 p = k.ym[j].q;
-        split29((p - e.X_y[j] % p) % p, k.nX0[j], k.nX1[j]);
+        k.nX[j] = split29((p - e.X_y[j] % p) % p);
     }
 }
 
@@ -457,8 +457,8 @@ __device__ __forceinline__ void extend_k(const ExtK<NX, NY>& e, const u64* x, u6
     for (int j = 0; j < NY; ++j) {
         Dot29 d;
 #pragma unroll
-        for (int i = 0; i < NX; ++i) dot29_mac(d, y[i], e.w0[i][j], e.w1[i][j]);
-        dot29_mac_small(d, v, e.nX0[j], e.nX1[j]);
+        for (int i = 0; i < NX; ++i) dot29_mac(d, y[i], e.w[i][j]);
+        dot29_mac_small(d, v, e.nX[j]);
         out[j] = dot29_reduce(d, e.ym[j]);
     }
 }
@@ -544,8 +544,8 @@ struct ScaleK {
     Modulus bm[L + 1];
     // w_j = rr - t [ (sum_i x_i [Q/q_i]_{b_j} - z_j) Q^-1 ]_{b_j}
     //     = rr + sum_i x_i C_ij + z_j D_j  mod b_j  (one Dot29 per b_j)
-    u32 C0[L][L + 1], C1[L][L + 1];  // [-[Q/q_i]_{b_j} Q^-1 t]_{b_j}
-    u32 D0[L + 1], D1[L + 1];        // [Q^-1 t]_{b_j}
+    W29 C[L][L + 1];  // [-[Q/q_i]_{b_j} Q^-1 t]_{b_j}
+    W29 D[L + 1];     // [Q^-1 t]_{b_j}
     ExtK<L + 1, L> bq;
 };
 
@@ -572,10 +572,10 @@ __global__ void k_mul_scale_k(const __grid_constant__ ScaleK<L> c, const u64* __
 #pragma unroll
     for (int j = 0; j < nB; ++j) {
         Dot29 d;
-        d.a0 = rr;
+        d.a0 = d.am = rr;  // rr * (1 in 29-bit halves): leaves the middle column sum alone
 #pragma unroll
-        for (int i = 0; i < L; ++i) dot29_mac(d, xi[i], c.C0[i][j], c.C1[i][j]);
-        dot29_mac(d, z[(size_t)(L + j) * n + k], c.D0[j], c.D1[j]);
+        for (int i = 0; i < L; ++i) dot29_mac(d, xi[i], c.C[i][j]);
+        dot29_mac(d, z[(size_t)(L + j) * n + k], c.D[j]);
         w[j] = dot29_reduce(d, c.bm[j]);
     }
     extend_k(c.bq, w, o);
@@ -607,8 +607,8 @@ static ScaleK<L> make_scale_k(const RnsParams& P) {
     for (int j = 0; j <= L; ++j) {
         c.bm[j] = h.mod[L + P.cfg.K + j];
         const u64 b = c.bm[j].q, D = host_mulmod(h.QinvB[j], h.tB[j], b);
-        split29(D, c.D0[j], c.D1[j]);
-        for (int i = 0; i < L; ++i) split29((b - host_mulmod(h.QhatB[i][j], D, b)) % b, c.C0[i][j], c.C1[i][j]);
+        c.D[j] = split29(D);
+        for (int i = 0; i < L; ++i) c.C[i][j] = split29((b - host_mulmod(h.QhatB[i][j], D, b)) % b);
     }
     fill_extk(c.bq, h, h.extBQ);
     return c;
@@ -938,8 +938,8 @@ struct ModDownK {
     u64 pk[K], phat_inv[K], phat_inv_sh[K];
     Modulus qm[L];
     // out_j = (acc_j - sum_k y_k [P/p_k]_{q_j}) P^-1 = acc_j Pinv + sum_k y_k E_kj
-    u32 E0[K][L], E1[K][L];  // [-[P/p_k]_{q_j} P^-1]_{q_j} in 29-bit halves
-    u32 F0[L], F1[L];        // [P^-1]_{q_j}
+    W29 E[K][L];  // [-[P/p_k]_{q_j} P^-1]_{q_j} in 29-bit halves
+    W29 F[L];     // [P^-1]_{q_j}
 };
 
 // k_ks_moddown with the constants from a parameter block (same values; the
@@ -975,9 +975,9 @@ __global__ void __launch_bounds__(128, 6) k_ks_moddown_k(const __grid_constant__
     auto term = [&](int j, const u64* y, const u64* acc, const u64* rs, int ridx, bool neg) {
         const u64 q = c.qm[j].q;
         Dot29 d;
-        dot29_mac(d, acc[(size_t)j * n + k], c.F0[j], c.F1[j]);  // canonical inverse-NTT output
+        dot29_mac(d, acc[(size_t)j * n + k], c.F[j]);  // canonical inverse-NTT output
 #pragma unroll
-        for (int kk = 0; kk < K; ++kk) dot29_mac(d, y[kk], c.E0[kk][j], c.E1[kk][j]);
+        for (int kk = 0; kk < K; ++kk) dot29_mac(d, y[kk], c.E[kk][j]);
         u64 v = dot29_reduce(d, c.qm[j]);
         if (rs) {
             const u64 r = rs[(size_t)j * n + ridx];
@@ -1029,9 +1029,9 @@ static ModDownK<L, K> make_moddown_k(const RnsParams& P) {
     for (int j = 0; j < L; ++j) {
         c.qm[j] = h.mod[j];
         const u64 q = h.mod[j].q;
-        split29(h.Pinv_q[j], c.F0[j], c.F1[j]);
+        c.F[j] = split29(h.Pinv_q[j]);
         for (int kk = 0; kk < K; ++kk)
-            split29((q - host_mulmod(h.phat_q[kk][j], h.Pinv_q[j], q)) % q, c.E0[kk][j], c.E1[kk][j]);
+            c.E[kk][j] = split29((q - host_mulmod(h.phat_q[kk][j], h.Pinv_q[j], q)) % q);
     }
     return c;
 }

@@ -92,40 +92,45 @@ CSSC_HD u64 barrett(u64 z1, u64 z0, const Modulus& m) {
 CSSC_HD u64 mul_mod(u64 a, u64 b, const Modulus& m) { return barrett(umulhi(a, b), a * b, m); }
 
 // Exact dot products for the basis conversions: sum_i y_i * w_i mod p with
-// every y_i < 2^59 and constant w_i < p.  Both factors are split into 29-bit
-// halves, so each term is four 32x32->64 multiply-adds (IMAD.WIDE.U32 with the
-// 64-bit addend) into three u64 column sums instead of a Shoup product
-// (~10 IMADs); the sum S = a0 + am 2^29 + ah 2^58 is reduced once by the
-// Barrett step above.  Bounds for up to 15 terms: a0 < 2^62, am < 2^64,
-// ah < 2^63, S < 15 * 2^(59+k) < 2^(k+63) with k = bit length of p >= 30.
-// The result is canonical, hence identical to any other exact reduction.
+// every y_i < 2^58 (canonical residues) and constant w_i < p <= 2^58.  Both
+// factors are split into 29-bit halves and each term is three 32x32->64
+// multiply-adds (IMAD.WIDE.U32 with the 64-bit addend, Karatsuba middle term
+// (y0 + y1)(w0 + w1)) into three u64 column sums, instead of a Shoup product
+// (six IMAD.WIDE + four IMAD); the sum S = a0 + mid 2^29 + ah 2^58, mid =
+// am - a0 - ah, is reduced once by the Barrett step above.  Bounds for up to
+// 15 terms: a0, ah < 2^62, am < 15 * 2^60 < 2^64, S < 2^(k+62) < 2^(k+63),
+// k = bit length of p >= 30.  The result is canonical, hence identical to any
+// other exact reduction.
 struct Dot29 {
     u64 a0 = 0, am = 0, ah = 0;
 };
+struct W29 {
+    u32 lo, hi, sum;  // w = hi 2^29 + lo, sum = lo + hi
+};
 constexpr u32 kMask29 = (1u << 29) - 1;
-CSSC_HD void dot29_mac(Dot29& d, u64 y, u32 w0, u32 w1) {
+CSSC_HD void dot29_mac(Dot29& d, u64 y, const W29& w) {
     const u32 y0 = (u32)y & kMask29, y1 = (u32)(y >> 29);
-    d.a0 += (u64)y0 * w0;
-    d.am += (u64)y0 * w1;
-    d.am += (u64)y1 * w0;
-    d.ah += (u64)y1 * w1;
+    d.a0 += (u64)y0 * w.lo;
+    d.ah += (u64)y1 * w.hi;
+    d.am += (u64)(y0 + y1) * w.sum;
 }
 // a small multiplier (y < 2^29) times w
-CSSC_HD void dot29_mac_small(Dot29& d, u32 y, u32 w0, u32 w1) {
-    d.a0 += (u64)y * w0;
-    d.am += (u64)y * w1;
+CSSC_HD void dot29_mac_small(Dot29& d, u32 y, const W29& w) {
+    d.a0 += (u64)y * w.lo;
+    d.am += (u64)y * w.sum;
 }
 CSSC_HD u64 dot29_reduce(const Dot29& d, const Modulus& m) {
-    const u64 t = d.am << 29, u = d.ah << 58;
+    const u64 mid = d.am - d.a0 - d.ah;
+    const u64 t = mid << 29, u = d.ah << 58;
     const u64 lo = d.a0 + t;
-    u64 hi = (d.am >> 35) + (d.ah >> 6) + (lo < t);
+    u64 hi = (mid >> 35) + (d.ah >> 6) + (lo < t);
     const u64 lo2 = lo + u;
     hi += lo2 < u;
     return barrett(hi, lo2, m);
 }
-inline void split29(u64 w, u32& w0, u32& w1) {
-    w0 = (u32)(w & kMask29);
-    w1 = (u32)(w >> 29);
+inline W29 split29(u64 w) {
+    const u32 lo = (u32)(w & kMask29), hi = (u32)(w >> 29);
+    return W29{lo, hi, lo + hi};
 }
 
 // a mod q for a < 2^(k+5) (a lazy forward-NTT output < 31q, say), k >= 7: the
