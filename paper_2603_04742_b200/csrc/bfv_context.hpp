@@ -160,7 +160,8 @@ public:
                        u64* T, u64* Z, u64* D2, u64* DX, u64* ACC, const u64* const* RLK,
                        const EncIn* enc = nullptr);
     // OUT = BASE + EXTRA + rot(SRC) (BASE / EXTRA per-item nullable); PAIR (nullable):
-    // PAIR[i] = j >= 0 also adds item j's rotation into OUT[i], -2 skips item i
+    // PAIR[i] = j >= 0 also adds item j's rotation into OUT[i] (PAIR[j] = -3 - i;
+    // the two items' CTAs split the limbs)
     void rotate_dev(const u64* const* SRC, const u32* ginv, const u64* const* KEY,
                     const u64* const* BASE, u64* const* OUT, int items, u64* DX, u64* ACC,
                     const u64* const* EXTRA = nullptr, const int* PAIR = nullptr);

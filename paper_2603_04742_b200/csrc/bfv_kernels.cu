@@ -874,7 +874,8 @@ void launch_ks_inner(const DevConsts* dc, const RnsParams& P, const u64* DX,
 // E4 + fused adds: out = BASE[item] + EXTRA[item] + phi_g(RSRC[item].c0) + ModDown(acc);
 // per-item BASE / EXTRA entries may be null.  PAIR (nullable): PAIR[item] = j >= 0
 // also adds item j's rotation phi_gj(RSRC[j].c0) + ModDown(acc_j) (item j has no
-// BASE / EXTRA of its own), and PAIR[item] = -2 skips the item (merged elsewhere).
+// BASE / EXTRA of its own) and PAIR[j] = -3 - item: item's CTAs write limbs
+// [0, L/2) of the merged sum, j's CTAs limbs [L/2, L), both into OUT[item].
 // Every sum is exact mod q, so merging two rotations' adds into one pass gives
 // the words of the separate rotate and add.
 // one polynomial per grid z-slice; the output loop is only partly unrolled so
@@ -885,10 +886,11 @@ __global__ void __launch_bounds__(128, 6) k_ks_moddown(const DevConsts* __restri
                              u64* const* OUT, const u64* const* EXTRA, const int* PAIR) {
     const int n = dc->n, L = LT ? LT : dc->L, K = KT ? KT : dc->K, LK = L + K;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    const int item = blockIdx.y;
-    const int pair = PAIR ? PAIR[item] : -1;
-    if (pair == -2) return;
+    const int pv = PAIR ? PAIR[blockIdx.y] : -1;  // see k_ks_moddown_k
+    const int item = pv <= -3 ? -3 - pv : blockIdx.y;
+    const int pair = pv <= -3 ? blockIdx.y : pv;
     const int nsrc = pair >= 0 ? 2 : 1;
+    const int jlo = pv <= -3 ? L / 2 : 0, jhi = pv >= 0 ? L / 2 : L;
     const size_t PL = (size_t)LK * n;
     const int p = blockIdx.z;
     u64* out = OUT[item] + (size_t)p * L * n;
@@ -910,7 +912,7 @@ __global__ void __launch_bounds__(128, 6) k_ks_moddown(const DevConsts* __restri
         }
         const u64* rs = (RSRC && p == 0) ? RSRC[it] : nullptr;
 #pragma unroll 2
-        for (int j = 0; j < L; ++j) {
+        for (int j = jlo; j < jhi; ++j) {
             const u64 q = dc->mod[j].q;
             u64 c = 0;
 #pragma unroll
@@ -953,9 +955,12 @@ __global__ void __launch_bounds__(128, 6) k_ks_moddown_k(const __grid_constant__
     static_assert(K + 1 <= 15, "Dot29 bound");
     const int n = c.n;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    const int item = blockIdx.y;
-    const int pair = PAIR ? PAIR[item] : -1;
-    if (pair == -2) return;
+    // PAIR: a merged pair (D, O) shares its 2 x L limb outputs: D's CTAs
+    // write limbs [0, L/2) of rot_D + rot_O, O's CTAs limbs [L/2, L), both
+    // into D's output with D's BASE / EXTRA
+    const int pv = PAIR ? PAIR[blockIdx.y] : -1;
+    const int item = pv <= -3 ? -3 - pv : blockIdx.y;
+    const int pair = pv <= -3 ? blockIdx.y : pv;
     const int p = blockIdx.z;
     u64* out = OUT[item] + (size_t)p * L * n;
     const u64* base = BASE ? BASE[item] : nullptr;
@@ -990,7 +995,29 @@ __global__ void __launch_bounds__(128, 6) k_ks_moddown_k(const __grid_constant__
     int ridx;
     bool neg;
     setup(item, y, acc, rs, ridx, neg);
-    if (pair < 0) {
+    if (pair < 0 && L <= 4) {
+        // small L: every load of the coefficient is issued before any product
+        // (the launches are latency-bound: long-scoreboard stalls dominate)
+        u64 av[L], bv[L], rv[L];
+#pragma unroll
+        for (int j = 0; j < L; ++j) {
+            av[j] = acc[(size_t)j * n + k];
+            bv[j] = base ? base[(size_t)j * n + k] : 0;
+            if (ex) bv[j] = add_mod(bv[j], ex[(size_t)j * n + k], c.qm[j].q);
+            rv[j] = rs ? rs[(size_t)j * n + ridx] : 0;
+        }
+#pragma unroll
+        for (int j = 0; j < L; ++j) {
+            const u64 q = c.qm[j].q;
+            Dot29 d;
+            dot29_mac(d, av[j], c.F[j]);
+#pragma unroll
+            for (int kk = 0; kk < K; ++kk) dot29_mac(d, y[kk], c.E[kk][j]);
+            u64 v = dot29_reduce(d, c.qm[j]);
+            if (rs) v = add_mod(v, neg ? neg_mod(rv[j], q) : rv[j], q);
+            out[(size_t)j * n + k] = add_mod(v, bv[j], q);
+        }
+    } else if (pair < 0) {
 #pragma unroll 2
         for (int j = 0; j < L; ++j) {
             const u64 q = c.qm[j].q;
@@ -999,14 +1026,15 @@ __global__ void __launch_bounds__(128, 6) k_ks_moddown_k(const __grid_constant__
             if (ex) v = add_mod(v, ex[(size_t)j * n + k], q);
             out[(size_t)j * n + k] = v;
         }
-    } else {  // merged rotation of item `pair`
+    } else {  // merged rotation of item `pair`, half of the limbs
         u64 y2[K];
         const u64 *acc2, *rs2;
         int ridx2;
         bool neg2;
         setup(pair, y2, acc2, rs2, ridx2, neg2);
+        const int jlo = pv <= -3 ? L / 2 : 0, jhi = pv <= -3 ? L : L / 2;
 #pragma unroll 1
-        for (int j = 0; j < L; ++j) {
+        for (int j = jlo; j < jhi; ++j) {
             const u64 q = c.qm[j].q;
             u64 v = add_mod(term(j, y, acc, rs, ridx, neg), term(j, y2, acc2, rs2, ridx2, neg2), q);
             if (base) v = add_mod(v, base[(size_t)j * n + k], q);

@@ -176,7 +176,7 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
         std::vector<const u64*> src, base, key, extra;
         std::vector<u64*> o;
         std::vector<u32> gi;
-        std::vector<int> pair;  // -1 plain, j merge item j, -2 merged elsewhere
+        std::vector<int> pair;  // -1 plain; D_1 k: its O_1 item j; that O_1 item: -3 - k
         std::set<u32> lvl_keys;
         size_t odd_slot = 0;
         for (int k = 0; k < n && (int)trees[order[k]].dbl.size() > l; ++k) {
@@ -200,7 +200,7 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
                     if (after == 1) {  // follows D_1: merged into D_1's ModDown (PAIR)
                         pair.resize(o.size() + 1, -1);
                         pair[k] = (int)o.size();
-                        pair[o.size()] = -2;
+                        pair[o.size()] = -3 - k;
                     }
                     u64* slot = rp_.words() + (odd_slot++) * ctw;
                     u32 g;
@@ -223,7 +223,7 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
         lv.ginv = put(gi);
         lv.extra = put(extra);
         pair.resize(o.size(), -1);
-        lv.pair = std::count(pair.begin(), pair.end(), -2) ? put(pair) : nullptr;
+        lv.pair = std::any_of(pair.begin(), pair.end(), [](int v) { return v != -1; }) ? put(pair) : nullptr;
         lv.keys = (int)lvl_keys.size();
         levels_.push_back(lv);
         stats_.hbm_bytes += (u64)lv.items * 3 * C + lvl_keys.size() * KEY;
