@@ -380,13 +380,13 @@ void GpuContext::encrypt_cssc(const int64_t* ci, const int64_t* va, size_t nnz, 
 }
 
 void GpuContext::encrypt_cssc_image(const unsigned char* img, const CsscLayout& lay, const ClientWs* ws,
-                                    EncIn* defer) {
+                                    EncIn* defer, int part) {
     const int items = lay.items;
     if (!items) return;
     unsigned char* d;
     u64 *U, *CM;
     if (ws) {
-        encrypt_cssc_forked(img, lay, *ws, defer);
+        encrypt_cssc_forked(img, lay, *ws, defer, part);
         return;
     } else if (forked_enc_) {
         ensure_ws(scratch_[0], std::max<size_t>(lay.bytes, 256));
@@ -424,35 +424,47 @@ void GpuContext::encrypt_cssc_image(const unsigned char* img, const CsscLayout& 
 // CM is [item][2L][N] followed by the messages [item][N]; same words as the
 // staged path.
 void GpuContext::encrypt_cssc_forked(const unsigned char* img, const CsscLayout& lay, const ClientWs& ws,
-                                     EncIn* defer) {
+                                     EncIn* defer, int part) {
     const int items = lay.items, L = P_.cfg.L, logn = P_.cfg.logn;
     const size_t n = (size_t)P_.n;
     unsigned char* d = ws.up;
     u64* CM = ws.CM;
     u64* MSG = CM + (size_t)items * 2 * L * n;
-    cuda_check(cudaEventRecord(ev_fork_, st_), "fork");
-    cuda_check(cudaStreamWaitEvent(st2_, ev_fork_, 0), "fork");
+    const auto* streams = reinterpret_cast<const u64*>(d + lay.o_st);
+    // branch A: stream ids and output pointers, then the message-independent encryption
+    auto branch_a = [&] {
+        cuda_check(cudaMemcpyAsync(d + lay.o_st, img + lay.o_st, lay.bytes - lay.o_st, cudaMemcpyHostToDevice, st_),
+                   "upload");
+        launch_enc_sample_u(dc_, P_, P_.cfg.seed, streams, ws.U, items, st_);
+        launch_ntt_phase(dc_, logn, false, true, job(ws.U, ws.U, L, range_idx(0, L)), items, st_);
+        launch_blocks_mul_inv(dc_, P_, ws.U, pk_.words(), 2, CM, (size_t)2 * L * n, nullptr, 0, 0, items, st_);
+        std::vector<int> pidx = range_idx(0, L);
+        pidx.insert(pidx.end(), pidx.begin(), pidx.end());
+        launch_ntt_phase(dc_, logn, true, true, job(CM, CM, 2 * L, pidx), items, st_);
+    };
+    if (part == 1) {  // branch A alone (the pipeline's early graph)
+        branch_a();
+        return;
+    }
+    cudaStream_t sb = part == 2 ? st_ : st2_;
+    if (part != 2) {
+        cuda_check(cudaEventRecord(ev_fork_, st_), "fork");
+        cuda_check(cudaStreamWaitEvent(st2_, ev_fork_, 0), "fork");
+    }
     // branch B: the CSR image, packing, message INTT
-    cuda_check(cudaMemcpyAsync(d, img, lay.o_st, cudaMemcpyHostToDevice, st2_), "upload");
+    cuda_check(cudaMemcpyAsync(d, img, lay.o_st, cudaMemcpyHostToDevice, sb), "upload");
     launch_pack_cssc(dc_, P_, reinterpret_cast<const int64_t*>(d + lay.o_ci),
                      reinterpret_cast<const int64_t*>(d + lay.o_va), reinterpret_cast<const int64_t*>(d + lay.o_v),
                      reinterpret_cast<const int4*>(d + lay.o_rows), reinterpret_cast<const int*>(d + lay.o_rpre),
                      (int)lay.n_rows, (long)lay.entries,
                      reinterpret_cast<const int2*>(d + lay.o_sl), reinterpret_cast<const int4*>(d + lay.o_cols),
-                     items / 2, MSG, n, st2_);
-    launch_ntt(dc_, logn, true, job(MSG, MSG, 1, {P_.t_index()}), items, st2_);
-    cuda_check(cudaEventRecord(ev_join_, st2_), "join");
-    // branch A: stream ids and output pointers, then the message-independent encryption
-    cuda_check(cudaMemcpyAsync(d + lay.o_st, img + lay.o_st, lay.bytes - lay.o_st, cudaMemcpyHostToDevice, st_),
-               "upload");
-    const auto* streams = reinterpret_cast<const u64*>(d + lay.o_st);
-    launch_enc_sample_u(dc_, P_, P_.cfg.seed, streams, ws.U, items, st_);
-    launch_ntt_phase(dc_, logn, false, true, job(ws.U, ws.U, L, range_idx(0, L)), items, st_);
-    launch_blocks_mul_inv(dc_, P_, ws.U, pk_.words(), 2, CM, (size_t)2 * L * n, nullptr, 0, 0, items, st_);
-    std::vector<int> pidx = range_idx(0, L);
-    pidx.insert(pidx.end(), pidx.begin(), pidx.end());
-    launch_ntt_phase(dc_, logn, true, true, job(CM, CM, 2 * L, pidx), items, st_);
-    cuda_check(cudaStreamWaitEvent(st_, ev_join_, 0), "join");
+                     items / 2, MSG, n, sb);
+    launch_ntt(dc_, logn, true, job(MSG, MSG, 1, {P_.t_index()}), items, sb);
+    if (part != 2) {
+        cuda_check(cudaEventRecord(ev_join_, st2_), "join");
+        branch_a();
+        cuda_check(cudaStreamWaitEvent(st_, ev_join_, 0), "join");
+    }
     if (defer) {
         *defer = EncIn{P_.cfg.seed, streams, CM, (size_t)2 * L * n, MSG, n,
                        reinterpret_cast<u64* const*>(d + lay.o_out), items / 2, nullptr};

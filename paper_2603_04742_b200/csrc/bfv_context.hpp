@@ -129,8 +129,12 @@ public:
     // stream has consumed it
     // defer (pipeline, fused path): skip the finishing kernel and describe its
     // inputs instead; the multiply's extension (launch_mul_extend_enc) finishes
+    // part (pipeline capture): 0 both branches, 1 only the message-independent
+    // branch (ids + output handles upload, u, pk u), 2 only the image branch
+    // and the join (part 1 must have run before on the same stream)
     void encrypt_cssc_image(const unsigned char* img, const CsscLayout& lay, const ClientWs* ws = nullptr,
-                            EncIn* defer = nullptr);
+                            EncIn* defer = nullptr, int part = 0);
+    uint64_t peek_stream_id() const { return stream_counter_.load(); }
     // pinned host buffers, pooled by capacity
     unsigned char* pinned_take(size_t bytes, size_t* cap);
     void pinned_give(unsigned char* p, size_t cap);
@@ -191,7 +195,7 @@ private:
     void* stage_upload(size_t bytes, int slot);
     DevBuf gen_ksk(u64 keyid, const u64* sp_ntt);
     void encrypt_cssc_forked(const unsigned char* img, const CsscLayout& lay, const ClientWs& ws,
-                             EncIn* defer = nullptr);
+                             EncIn* defer = nullptr, int part = 0);
     void ensure_ws(DevBuf& b, size_t bytes) { b.ensure(&pool_, bytes); }
 
     RnsParams P_;

@@ -34,6 +34,12 @@ struct spmvgpu_ctx {
     // shared across threads); recursive: the protocol layer calls
     // back into the C-ABI
     std::recursive_mutex api_mu;
+    // early encryption (pipeline_speculate): the chunk-shape key of the last
+    // pipeline run, and within one call the plan whose early graph was
+    // enqueued with stream ids from spec_id0
+    std::vector<std::uint64_t> spec_key;
+    spmvgpu_plan* spec_plan = nullptr;
+    std::uint64_t spec_id0 = 0;
     ~spmvgpu_ctx();
 };
 
@@ -290,8 +296,36 @@ bool pipeline_ready(const PlanLease& lease, const ClientImage& img) {
     return lease.plan && lease.plan->plan->has_pipeline() && lease.pimg && lease.pkey == client_image_key(img);
 }
 
+static ClientImage layout_of_key(const std::vector<std::size_t>& k) {
+    return client_image_layout(k[1], k[2], k[3], k[4], k[5], static_cast<int>(k[6]));
+}
+
+void pipeline_speculate(spmvgpu_ctx* ctx) {
+    ctx->spec_plan = nullptr;
+    if (ctx->spec_key.empty() || !ctx->g) return;
+    std::lock_guard<std::mutex> lk(ctx->plans_mu);
+    for (PlanLease& l : ctx->plans) {
+        if (l.key != ctx->spec_key) continue;
+        if (!l.plan || !l.plan->plan->has_pipeline() || !l.pimg || l.pkey.size() != 7) return;
+        const ClientImage lay = layout_of_key(l.pkey);
+        if (l.a.size() + l.b.size() != static_cast<std::size_t>(lay.items)) return;
+        // the ids and output handles exactly as client_image_fill will write them
+        const std::uint64_t id0 = ctx->g->peek_stream_id();
+        auto* st = reinterpret_cast<std::uint64_t*>(l.pimg + lay.o_st);
+        for (int i = 0; i < lay.items; ++i) st[i] = id0 + static_cast<std::uint64_t>(i);
+        unsigned char* o = l.pimg + lay.o_out;
+        std::memcpy(o, l.a.data(), sizeof(spmvgpu_ct) * l.a.size());
+        std::memcpy(o + sizeof(spmvgpu_ct) * l.a.size(), l.b.data(), sizeof(spmvgpu_ct) * l.b.size());
+        l.plan->plan->run_early();
+        ctx->spec_plan = l.plan;
+        ctx->spec_id0 = id0;
+        return;
+    }
+}
+
 void pipeline_prepare(spmvgpu_ctx* ctx, PlanLease& lease, const ClientImage& img) {
     auto& g = *ctx->g;
+    ctx->spec_plan = nullptr;  // a re-capture invalidates an early graph already enqueued
     if (!lease.plan) throw std::logic_error("pipeline: no plan");
     const std::size_t out_bytes = lease.plan->plan->pipeline_out_bytes();
     if (!lease.pimg || lease.pimg_cap < img.bytes) {
@@ -318,8 +352,15 @@ PipelineResult pipeline_result(const PlanLease& lease, int r) {
 }
 
 void pipeline_run(spmvgpu_ctx* ctx, PlanLease& lease) {
-    lease.plan->plan->run_pipeline();
+    // the early graph already ran iff pipeline_speculate enqueued it for this
+    // plan with the ids client_image_fill has just written
+    const ClientImage lay = layout_of_key(lease.pkey);
+    const auto id0 = *reinterpret_cast<const std::uint64_t*>(lease.pimg + lay.o_st);
+    const bool early = ctx->spec_plan == lease.plan && ctx->spec_id0 == id0;
+    ctx->spec_plan = nullptr;
+    lease.plan->plan->run_pipeline(early);
     ctx->g->synchronize();
+    ctx->spec_key = lease.key;
 }
 
 void client_image_encrypt(spmvgpu_ctx* ctx, ClientImage& img, const spmvgpu_ct* out) {
@@ -783,6 +824,10 @@ int cssc_spmv_batch(spmvgpu_ctx* c, const cssc_csr* ms, const int64_t* const* vs
         G(c);
         static const bool trace = std::getenv("CSSC_TRACE_E2E") != nullptr;
         const auto t0 = std::chrono::steady_clock::now();
+        // the previous call's plan: its early encryption graph runs while the
+        // host packs (used only if this call's chunk shapes select that plan)
+        static const bool spec = std::getenv("CSSC_NO_EARLY_ENC") == nullptr;
+        if (spec) spmv::detail::pipeline_speculate(c);
         std::vector<spmv::detail::CsrView> w;
         for (size_t i = 0; i < nmat; ++i) w.push_back(view_of(ms[i], vs[i]));
         spmv::detail::BatchedSpmv job(c, c->hp, w, chunk_size, static_cast<spmv::PartyRole>(key_holder));

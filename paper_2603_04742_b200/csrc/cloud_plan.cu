@@ -275,6 +275,7 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
 
 CloudPlan::~CloudPlan() {
     if (pexec_) cudaGraphExecDestroy(pexec_);
+    if (eexec_) cudaGraphExecDestroy(eexec_);
     if (exec_) cudaGraphExecDestroy(exec_);
     if (graph_) cudaGraphDestroy(graph_);
 }
@@ -421,6 +422,10 @@ void CloudPlan::capture_pipeline(const unsigned char* img, const CsscLayout& lay
         cudaGraphExecDestroy(pexec_);
         pexec_ = nullptr;
     }
+    if (eexec_) {
+        cudaGraphExecDestroy(eexec_);
+        eexec_ = nullptr;
+    }
     const RnsParams& P = ctx_.params();
     const size_t n = (size_t)P.n, L = (size_t)P.cfg.L;
     DevicePool* pool = &ctx_.pool();
@@ -461,6 +466,22 @@ void CloudPlan::capture_pipeline(const unsigned char* img, const CsscLayout& lay
         cuda_check(cudaEventRecordWithFlags(ev, st, cudaEventRecordExternal), "event record");
         mk->push_back(ev);
     };
+    {  // early graph: the encryption's message-independent branch
+        cudaGraph_t ge = nullptr;
+        cuda_check(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "begin capture");
+        try {
+            ctx_.encrypt_cssc_image(img, lay, &ws, nullptr, 1);
+        } catch (...) {
+            cudaGraph_t tmp = nullptr;
+            cudaStreamEndCapture(st, &tmp);
+            if (tmp) cudaGraphDestroy(tmp);
+            throw;
+        }
+        cuda_check(cudaStreamEndCapture(st, &ge), "end capture");
+        const cudaError_t e = cudaGraphInstantiate(&eexec_, ge, 0);
+        cudaGraphDestroy(ge);
+        cuda_check(e, "graph instantiate");
+    }
     cuda_check(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "begin capture");
     try {
         mark();
@@ -473,7 +494,7 @@ void CloudPlan::capture_pipeline(const unsigned char* img, const CsscLayout& lay
         const bool fused = ctx_.fused_key_switch() && fixed_rns_shape(P);
         const bool fenc = fused && (fuse_mask & 1), fdec = fused && (fuse_mask & 2);
         EncIn enc{};
-        ctx_.encrypt_cssc_image(img, lay, &ws, fenc ? &enc : nullptr);
+        ctx_.encrypt_cssc_image(img, lay, &ws, fenc ? &enc : nullptr, 2);
         enc.order = ORDER_;  // the multiply's items are the chunks in depth order
         const int* grows = pgather_.as<int>();
         if (fdec) {
@@ -502,8 +523,14 @@ void CloudPlan::capture_pipeline(const unsigned char* img, const CsscLayout& lay
     cuda_check(e, "graph instantiate");
 }
 
-void CloudPlan::run_pipeline() {
+void CloudPlan::run_early() {
+    if (!eexec_) throw std::logic_error("pipeline not captured");
+    cuda_check(cudaGraphLaunch(eexec_, ctx_.stream()), "graph launch");
+}
+
+void CloudPlan::run_pipeline(bool early_done) {
     if (!pexec_) throw std::logic_error("pipeline not captured");
+    if (!early_done) run_early();
     cuda_check(cudaGraphLaunch(pexec_, ctx_.stream()), "graph launch");
     if (!pmarks_.empty()) {  // CSSC_PIPE_PROFILE: encrypt | multiply | levels.. | mask | decrypt | download
         cuda_check(cudaStreamSynchronize(ctx_.stream()), "sync");

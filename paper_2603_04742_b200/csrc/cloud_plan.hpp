@@ -54,8 +54,14 @@ public:
     // (pinned, fixed address), device pack + encryption into the plan's input
     // ciphertexts, the cloud plan, decryption of the results and the download
     // of slots + noise deviations into `out` (pinned).  Plan-owned workspaces.
+    // Two graphs: the early one is the encryption's message-independent branch
+    // (upload of the image's stream ids and output handles, u, pk u), the main
+    // one everything else.  run_early() may be enqueued before the host has
+    // built the image's CSR part (the ids must already be in place);
+    // run_pipeline(early_done) enqueues the early graph too unless it ran.
     void capture_pipeline(const unsigned char* img, const CsscLayout& lay, unsigned char* out);
-    void run_pipeline();  // enqueue (no sync)
+    void run_early();
+    void run_pipeline(bool early_done = false);  // enqueue (no sync)
     bool has_pipeline() const { return pexec_ != nullptr; }
     int results() const { return ns_; }
     // pipeline download layout: result s's first rows_[s] slots as u32 at
@@ -114,7 +120,7 @@ private:
     cudaGraph_t graph_ = nullptr;
     cudaGraphExec_t exec_ = nullptr;
     DevBuf pup_, pU_, pCM_, pX_, pM_, pslots_;  // pipeline workspaces
-    cudaGraphExec_t pexec_ = nullptr;
+    cudaGraphExec_t pexec_ = nullptr, eexec_ = nullptr;
     std::vector<cudaEvent_t> pmarks_;  // CSSC_PIPE_PROFILE=1: phase marks inside the pipeline graph
 };
 

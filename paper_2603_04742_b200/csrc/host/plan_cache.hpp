@@ -63,6 +63,11 @@ std::vector<std::size_t> client_image_key(const ClientImage& img);
 // (re)captures the lease's whole-evaluation graph for images laid out as `img`
 // (allocates the lease's pinned image/result buffers); then runs it and waits
 void pipeline_prepare(spmvgpu_ctx* ctx, PlanLease& lease, const ClientImage& img);
+// at the start of a batch call: enqueue the early encryption graph of the
+// last pipeline run's plan with the stream ids the call will assign next, so
+// it overlaps the host's packing; pipeline_run skips it if the call uses that
+// plan and those ids, and runs it otherwise
+void pipeline_speculate(spmvgpu_ctx* ctx);
 void pipeline_run(spmvgpu_ctx* ctx, PlanLease& lease);
 bool pipeline_ready(const PlanLease& lease, const ClientImage& img);
 // after pipeline_run: result r's decrypted slots [0, rows) as u32 (slots past
