@@ -327,9 +327,9 @@ def measure_config(pk, cfg, args, rank, world, device, full=True):
         with torch.cuda.stream(stream):
             flush.zero_()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        job.cloud(graph=True)
+        a.record(stream)  # creates the events; re-recorded inside the C call around the launch
         b.record(stream)
+        job.cloud_timed(a, b, graph=True)
         return a, b
 
     for _ in range(args.warmup):

@@ -233,6 +233,9 @@ int cssc_job_result_words(cssc_job* j, uint64_t* words, uint64_t cap_words, uint
 int cssc_job_finish_words(cssc_job* j, const uint64_t* words, int64_t* const* values, cssc_result* res);
 int cssc_job_encrypt(cssc_job* j);            /* client phase: encode + encrypt on device */
 int cssc_job_cloud(cssc_job* j, int use_graph); /* cloud phase, enqueued (no sync) */
+/* the same between two caller-created cudaEvent_t records on the context
+ * stream, both issued inside this call (no host gap inside the bracket) */
+int cssc_job_cloud_timed(cssc_job* j, int use_graph, void* ev_start, void* ev_stop);
 int cssc_job_finish(cssc_job* j, int64_t* const* values, cssc_result* res); /* decrypt */
 /* encrypt + cloud + decrypt in one call (what cssc_spmv_batch runs): from the
  * second job over a chunk-shape structure, one cached graph launch */

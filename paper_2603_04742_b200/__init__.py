@@ -131,6 +131,7 @@ _SIGS = {
     "cssc_job_finish_words": (C.c_int, [C.c_void_p, u64p, C.POINTER(i64p), C.POINTER(ResultC)]),
     "cssc_job_encrypt": (C.c_int, [C.c_void_p]),
     "cssc_job_cloud": (C.c_int, [C.c_void_p, C.c_int]),
+    "cssc_job_cloud_timed": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]),
     "cssc_job_finish": (C.c_int, [C.c_void_p, C.POINTER(i64p), C.POINTER(ResultC)]),
     "cssc_job_run": (C.c_int, [C.c_void_p, C.POINTER(i64p), C.POINTER(ResultC)]),
     "cssc_job_plan_stats": (C.c_int, [C.c_void_p, C.POINTER(PlanStats)]),
@@ -578,6 +579,11 @@ class Job:
 
     def cloud(self, graph: bool = True):
         check(lib().cssc_job_cloud(self.h, int(graph)))
+
+    def cloud_timed(self, start, stop, graph: bool = True):
+        """cloud() bracketed by two torch.cuda.Event (timing) records issued in the same C call."""
+        check(lib().cssc_job_cloud_timed(self.h, int(graph), C.c_void_p(start.cuda_event),
+                                         C.c_void_p(stop.cuda_event)))
 
     def finish(self) -> list:
         n = len(self.ms)

@@ -380,13 +380,13 @@ void GpuContext::encrypt_cssc(const int64_t* ci, const int64_t* va, size_t nnz, 
 }
 
 void GpuContext::encrypt_cssc_image(const unsigned char* img, const CsscLayout& lay, const ClientWs* ws,
-                                    EncIn* defer, int part) {
+                                    EncIn* defer, int part, cudaEvent_t early_ev) {
     const int items = lay.items;
     if (!items) return;
     unsigned char* d;
     u64 *U, *CM;
     if (ws) {
-        encrypt_cssc_forked(img, lay, *ws, defer, part);
+        encrypt_cssc_forked(img, lay, *ws, defer, part, early_ev);
         return;
     } else if (forked_enc_) {
         ensure_ws(scratch_[0], std::max<size_t>(lay.bytes, 256));
@@ -424,7 +424,7 @@ void GpuContext::encrypt_cssc_image(const unsigned char* img, const CsscLayout& 
 // CM is [item][2L][N] followed by the messages [item][N]; same words as the
 // staged path.
 void GpuContext::encrypt_cssc_forked(const unsigned char* img, const CsscLayout& lay, const ClientWs& ws,
-                                     EncIn* defer, int part) {
+                                     EncIn* defer, int part, cudaEvent_t early_ev) {
     const int items = lay.items, L = P_.cfg.L, logn = P_.cfg.logn;
     const size_t n = (size_t)P_.n;
     unsigned char* d = ws.up;
@@ -464,6 +464,8 @@ void GpuContext::encrypt_cssc_forked(const unsigned char* img, const CsscLayout&
         cuda_check(cudaEventRecord(ev_join_, st2_), "join");
         branch_a();
         cuda_check(cudaStreamWaitEvent(st_, ev_join_, 0), "join");
+    } else if (early_ev) {  // branch A ran as the early graph on the side stream
+        cuda_check(cudaStreamWaitEvent(st_, early_ev, cudaEventWaitExternal), "join early");
     }
     if (defer) {
         *defer = EncIn{P_.cfg.seed, streams, CM, (size_t)2 * L * n, MSG, n,

@@ -132,8 +132,11 @@ public:
     // part (pipeline capture): 0 both branches, 1 only the message-independent
     // branch (ids + output handles upload, u, pk u), 2 only the image branch
     // and the join (part 1 must have run before on the same stream)
+    // early_ev (part 2): the early graph's completion event, waited on
+    // (external event wait) before the join
     void encrypt_cssc_image(const unsigned char* img, const CsscLayout& lay, const ClientWs* ws = nullptr,
-                            EncIn* defer = nullptr, int part = 0);
+                            EncIn* defer = nullptr, int part = 0, cudaEvent_t early_ev = nullptr);
+    cudaStream_t side_stream() const { return st2_; }
     uint64_t peek_stream_id() const { return stream_counter_.load(); }
     // pinned host buffers, pooled by capacity
     unsigned char* pinned_take(size_t bytes, size_t* cap);
@@ -195,7 +198,7 @@ private:
     void* stage_upload(size_t bytes, int slot);
     DevBuf gen_ksk(u64 keyid, const u64* sp_ntt);
     void encrypt_cssc_forked(const unsigned char* img, const CsscLayout& lay, const ClientWs& ws,
-                             EncIn* defer = nullptr, int part = 0);
+                             EncIn* defer = nullptr, int part = 0, cudaEvent_t early_ev = nullptr);
     void ensure_ws(DevBuf& b, size_t bytes) { b.ensure(&pool_, bytes); }
 
     RnsParams P_;

@@ -1195,9 +1195,33 @@ __global__ void k_pack_cssc(const DevConsts* __restrict__ dc, const int64_t* __r
         }
         return lo;
     };
-    // the CTA's first and last entries bound every thread's search
-    if (threadIdx.x < 2 && e0 < total)
-        range[threadIdx.x] = row_of(threadIdx.x ? min(e0 + (int)blockDim.x, total) - 1 : e0, 0, n_rows - 1);
+    // the CTA's first and last entries bound every thread's search; both are
+    // located cooperatively (each round: every thread samples one row prefix,
+    // __syncthreads_count narrows [lo, hi] by the CTA width), so two rounds
+    // of loads replace a ~log2(rows)-deep dependent chain
+    if (e0 >= total) return;  // uniform per CTA
+    const int x0 = e0, x1 = min(e0 + (int)blockDim.x, total) - 1;
+    int lo0 = 0, hi0 = n_rows - 1, lo1 = 0, hi1 = n_rows - 1;
+    const int nt = blockDim.x;
+    for (int round = 0; round < 2 && (hi0 > lo0 || hi1 > lo1); ++round) {
+        // sample r_t = lo + ceil(t * span / nt): the last r with rpre[r] <= x lies
+        // in [r_(c-1), r_c - 1], c = #samples <= x (rpre is non-decreasing)
+        const int s0 = hi0 - lo0 + 1, s1 = hi1 - lo1 + 1;
+        const int r0 = lo0 + (int)(((long)threadIdx.x * s0 + nt - 1) / nt);
+        const int r1 = lo1 + (int)(((long)threadIdx.x * s1 + nt - 1) / nt);
+        const bool p0 = r0 <= hi0 && __ldg(rpre + r0) <= x0;
+        const bool p1 = r1 <= hi1 && __ldg(rpre + r1) <= x1;
+        const int c0 = __syncthreads_count(p0), c1 = __syncthreads_count(p1);
+        auto narrow = [&](int c, int& lo, int& hi, int span) {
+            const int a = lo + (int)(((long)(c - 1) * span + nt - 1) / nt);      // sample c-1 (c >= 1: rpre[lo] <= x)
+            const int b = c < nt ? lo + (int)(((long)c * span + nt - 1) / nt) - 1 : hi;
+            lo = a;
+            hi = min(b, hi);
+        };
+        narrow(c0, lo0, hi0, s0);
+        narrow(c1, lo1, hi1, s1);
+    }
+    if (threadIdx.x < 2) range[threadIdx.x] = threadIdx.x ? row_of(x1, lo1, hi1) : row_of(x0, lo0, hi0);
     __syncthreads();
     if (e >= total) return;
     const int lo = row_of(e, range[0], range[1]);

@@ -879,6 +879,15 @@ int cssc_job_finish_words(cssc_job* j, const uint64_t* words, int64_t* const* va
 }
 int cssc_job_encrypt(cssc_job* j) { return guard([&] { auto lk_ = api_lock(j ? j->ctx : nullptr); j->job->encrypt(); }); }
 int cssc_job_cloud(cssc_job* j, int use_graph) { return guard([&] { auto lk_ = api_lock(j ? j->ctx : nullptr); j->job->cloud(use_graph != 0); }); }
+int cssc_job_cloud_timed(cssc_job* j, int use_graph, void* ev_start, void* ev_stop) {
+    return guard([&] { auto lk_ = api_lock(j ? j->ctx : nullptr);
+        if (!j || !ev_start || !ev_stop) throw std::invalid_argument("null argument");
+        cudaStream_t st = j->ctx->g->stream();
+        cssc::cuda_check(cudaEventRecord(static_cast<cudaEvent_t>(ev_start), st), "event record");
+        j->job->cloud(use_graph != 0);
+        cssc::cuda_check(cudaEventRecord(static_cast<cudaEvent_t>(ev_stop), st), "event record");
+    });
+}
 int cssc_job_finish(cssc_job* j, int64_t* const* values, cssc_result* res) {
     return guard([&] { auto lk_ = api_lock(j ? j->ctx : nullptr);
         const auto r = j->job->finish();

@@ -276,6 +276,8 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
 CloudPlan::~CloudPlan() {
     if (pexec_) cudaGraphExecDestroy(pexec_);
     if (eexec_) cudaGraphExecDestroy(eexec_);
+    if (ev_early_) cudaEventDestroy(ev_early_);
+    if (ev_fork_) cudaEventDestroy(ev_fork_);
     if (exec_) cudaGraphExecDestroy(exec_);
     if (graph_) cudaGraphDestroy(graph_);
 }
@@ -466,6 +468,8 @@ void CloudPlan::capture_pipeline(const unsigned char* img, const CsscLayout& lay
         cuda_check(cudaEventRecordWithFlags(ev, st, cudaEventRecordExternal), "event record");
         mk->push_back(ev);
     };
+    if (!ev_early_) cuda_check(cudaEventCreateWithFlags(&ev_early_, cudaEventDisableTiming), "event");
+    if (!ev_fork_) cuda_check(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming), "event");
     {  // early graph: the encryption's message-independent branch
         cudaGraph_t ge = nullptr;
         cuda_check(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "begin capture");
@@ -494,7 +498,7 @@ void CloudPlan::capture_pipeline(const unsigned char* img, const CsscLayout& lay
         const bool fused = ctx_.fused_key_switch() && fixed_rns_shape(P);
         const bool fenc = fused && (fuse_mask & 1), fdec = fused && (fuse_mask & 2);
         EncIn enc{};
-        ctx_.encrypt_cssc_image(img, lay, &ws, fenc ? &enc : nullptr, 2);
+        ctx_.encrypt_cssc_image(img, lay, &ws, fenc ? &enc : nullptr, 2, ev_early_);
         enc.order = ORDER_;  // the multiply's items are the chunks in depth order
         const int* grows = pgather_.as<int>();
         if (fdec) {
@@ -523,9 +527,16 @@ void CloudPlan::capture_pipeline(const unsigned char* img, const CsscLayout& lay
     cuda_check(e, "graph instantiate");
 }
 
+// The early graph runs on the side stream (after everything already on the
+// context stream); the main graph's image branch starts beside it and its
+// join waits for ev_early_ (an external event-wait node).
 void CloudPlan::run_early() {
     if (!eexec_) throw std::logic_error("pipeline not captured");
-    cuda_check(cudaGraphLaunch(eexec_, ctx_.stream()), "graph launch");
+    cudaStream_t side = ctx_.side_stream();
+    cuda_check(cudaEventRecord(ev_fork_, ctx_.stream()), "fork");
+    cuda_check(cudaStreamWaitEvent(side, ev_fork_, 0), "fork");
+    cuda_check(cudaGraphLaunch(eexec_, side), "graph launch");
+    cuda_check(cudaEventRecord(ev_early_, side), "event record");
 }
 
 void CloudPlan::run_pipeline(bool early_done) {
