@@ -85,6 +85,7 @@ GpuContext::GpuContext(const RnsConfig& cfg, int device) : P_(cfg), device_(devi
     cuda_check(cudaStreamCreateWithFlags(&st2_, cudaStreamNonBlocking), "stream");
     cuda_check(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming), "event");
     cuda_check(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming), "event");
+    cuda_check(cudaEventCreateWithFlags(&ev_upload_, cudaEventDisableTiming), "event");
     DevConsts host = P_.host;
     const size_t tw_bytes = sizeof(u64) * 2 * (size_t)P_.n;
     for (int i = 0; i < P_.np; ++i) {
@@ -116,6 +117,7 @@ GpuContext::~GpuContext() {
     if (dc_) cudaFree(dc_);
     if (ev_fork_) cudaEventDestroy(ev_fork_);
     if (ev_join_) cudaEventDestroy(ev_join_);
+    if (ev_upload_) cudaEventDestroy(ev_upload_);
     if (st2_) cudaStreamDestroy(st2_);
     if (st_) cudaStreamDestroy(st_);
 }
@@ -435,6 +437,7 @@ void GpuContext::encrypt_cssc_forked(const unsigned char* img, const CsscLayout&
     auto branch_a = [&] {
         cuda_check(cudaMemcpyAsync(d + lay.o_st, img + lay.o_st, lay.bytes - lay.o_st, cudaMemcpyHostToDevice, st_),
                    "upload");
+        if (part == 1 && ws.E) cuda_check(cudaEventRecord(ev_upload_, st_), "ids uploaded");
         launch_enc_sample_u(dc_, P_, P_.cfg.seed, streams, ws.U, items, st_);
         launch_ntt_phase(dc_, logn, false, true, job(ws.U, ws.U, L, range_idx(0, L)), items, st_);
         launch_blocks_mul_inv(dc_, P_, ws.U, pk_.words(), 2, CM, (size_t)2 * L * n, nullptr, 0, 0, items, st_);
@@ -442,8 +445,14 @@ void GpuContext::encrypt_cssc_forked(const unsigned char* img, const CsscLayout&
         pidx.insert(pidx.end(), pidx.begin(), pidx.end());
         launch_ntt_phase(dc_, logn, true, true, job(CM, CM, 2 * L, pidx), items, st_);
     };
-    if (part == 1) {  // branch A alone (the pipeline's early graph)
+    if (part == 1) {  // branch A alone (the pipeline's early graph), the e draws beside it
         branch_a();
+        if (ws.E) {
+            cuda_check(cudaStreamWaitEvent(st2_, ev_upload_, 0), "ids");
+            launch_enc_sample_e(dc_, P_, P_.cfg.seed, streams, ws.E, items, st2_);
+            cuda_check(cudaEventRecord(ev_join_, st2_), "join");
+            cuda_check(cudaStreamWaitEvent(st_, ev_join_, 0), "join");
+        }
         return;
     }
     cudaStream_t sb = part == 2 ? st_ : st2_;
@@ -469,7 +478,8 @@ void GpuContext::encrypt_cssc_forked(const unsigned char* img, const CsscLayout&
     }
     if (defer) {
         *defer = EncIn{P_.cfg.seed, streams, CM, (size_t)2 * L * n, MSG, n,
-                       reinterpret_cast<u64* const*>(d + lay.o_out), items / 2, nullptr};
+                       reinterpret_cast<u64* const*>(d + lay.o_out), items / 2, nullptr,
+                       part == 2 ? ws.E : nullptr};
         stats_.kernels += 7;
     } else {
         launch_enc_finish(dc_, P_, P_.cfg.seed, streams, CM, reinterpret_cast<u64* const*>(d + lay.o_out), items,

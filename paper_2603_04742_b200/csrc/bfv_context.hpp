@@ -78,6 +78,7 @@ struct ClientWs {
     u64* X = nullptr;             // [results][L][N] decryption c1*s
     u64* M = nullptr;             // [results][N] decoded message
     u64* slots = nullptr;         // [results][S] slots, then [results] noise deviations
+    int8_t* E = nullptr;          // [items][2][N] pre-drawn e (early graph; null: drawn in the finish)
 };
 
 class GpuContext {
@@ -224,7 +225,7 @@ private:
     // side stream + fork/join events: the pipeline's encryption runs its
     // message-independent part beside the upload and packing
     cudaStream_t st2_ = nullptr;
-    cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
+    cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr, ev_upload_ = nullptr;
     std::mutex mu_;
 };
 

@@ -510,14 +510,19 @@ __global__ void __launch_bounds__(128) k_mul_extend_enc(const __grid_constant__ 
     const int n = c.x.n;
     const int item = blockIdx.y, p = blockIdx.z, poly = p & 1;
     const int eitem = (p < 2 ? 0 : in.n_chunks) + (in.order ? in.order[item] : item);
-    const u64 id = in.streams[eitem];
-    const int g = threadIdx.x >> 2;
-    if (g < 16)
-        chacha20_block_x4(in.seed, (u32)(blockIdx.x * 16 + g), poly ? DOM_ENC_E1 : DOM_ENC_E0, (u32)id,
-                          (u32)(id >> 32), blk[g]);
-    __syncthreads();
     const int kk = threadIdx.x, k = blockIdx.x * 128 + kk;
-    const int64_t e = cbd_of(word64(blk[kk >> 3], kk & 7));
+    int64_t e;
+    if (in.E) {  // drawn ahead by k_enc_sample_e (the early graph)
+        e = in.E[((size_t)eitem * 2 + poly) * n + k];
+    } else {
+        const u64 id = in.streams[eitem];
+        const int g = threadIdx.x >> 2;
+        if (g < 16)
+            chacha20_block_x4(in.seed, (u32)(blockIdx.x * 16 + g), poly ? DOM_ENC_E1 : DOM_ENC_E0, (u32)id,
+                              (u32)(id >> 32), blk[g]);
+        __syncthreads();
+        e = cbd_of(word64(blk[kk >> 3], kk & 7));
+    }
     const u64* cm = in.CM + (size_t)eitem * in.cstride + (size_t)poly * L * n + k;
     const u64 m = poly ? 0 : in.MSG[(size_t)eitem * in.mstride + k];
     u64* ct = in.OUT[eitem] + (size_t)poly * L * n + k;
@@ -1345,6 +1350,29 @@ __global__ void __launch_bounds__(128) k_enc_finish(const DevConsts* __restrict_
         out[(size_t)j * n + k] = c0;
         out[((size_t)L + j) * n + k] = c1;
     }
+}
+
+// the e draws of k_enc_finish / k_mul_extend_enc, ahead of time: one CTA per
+// 128 coefficients of one polynomial of one item
+__global__ void __launch_bounds__(128) k_enc_sample_e(u64 seed, const u64* streams, int8_t* E, int n) {
+    __shared__ u32 blk[16][16];
+    const int item = blockIdx.y, poly = blockIdx.z;
+    const u64 id = streams[item];
+    const int g = threadIdx.x >> 2;
+    if (g < 16)
+        chacha20_block_x4(seed, (u32)(blockIdx.x * 16 + g), poly ? DOM_ENC_E1 : DOM_ENC_E0, (u32)id, (u32)(id >> 32),
+                          blk[g]);
+    __syncthreads();
+    const int kk = threadIdx.x, k = blockIdx.x * 128 + kk;
+    E[((size_t)item * 2 + poly) * n + k] = (int8_t)cbd_of(word64(blk[kk >> 3], kk & 7));
+}
+
+void launch_enc_sample_e(const DevConsts* dc, const RnsParams& P, u64 seed, const u64* streams, int8_t* E,
+                         int items, cudaStream_t st) {
+    (void)dc;
+    if (!items) return;
+    k_enc_sample_e<<<dim3((unsigned)(P.n / 128), (unsigned)items, 2), 128, 0, st>>>(seed, streams, E, P.n);
+    CSSC_CHECK_LAUNCH();
 }
 
 void launch_enc_finish(const DevConsts* dc, const RnsParams& P, u64 seed, const u64* streams,

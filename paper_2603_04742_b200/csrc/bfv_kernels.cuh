@@ -58,6 +58,7 @@ struct EncIn {
     u64* const* OUT;     // ciphertext of each encryption item
     int n_chunks;
     const int* order;    // multiply item -> chunk (the plan's depth order); null = identity
+    const int8_t* E;     // pre-drawn e: [item][2][N] (k_enc_sample_e); null = draw in place
 };
 bool fixed_rns_shape(const RnsParams& P);  // one of the compiled (L, K, alpha) shapes
 void launch_mul_extend_enc(const DevConsts* dc, const RnsParams& P, const EncIn& in, u64* T, int items,
@@ -122,6 +123,9 @@ void launch_encode_scatter(const DevConsts* dc, const RnsParams& P, const int64_
                            const u64* offs, u64* M, int items, cudaStream_t st, size_t mstride = 0);
 void launch_plain_lift(const DevConsts* dc, const RnsParams& P, const u64* M, u64* PT, int items,
                        cudaStream_t st);
+// E[item][poly][N] = the CBD e draws of k_enc_finish (|e| <= 21, as int8)
+void launch_enc_sample_e(const DevConsts* dc, const RnsParams& P, u64 seed, const u64* streams, int8_t* E,
+                         int items, cudaStream_t st);
 void launch_enc_sample_u(const DevConsts* dc, const RnsParams& P, u64 seed, const u64* streams,
                          u64* U, int items, cudaStream_t st);
 void launch_enc_pk(const DevConsts* dc, const RnsParams& P, const u64* PK, const u64* U, u64* C,

@@ -437,6 +437,7 @@ void CloudPlan::capture_pipeline(const unsigned char* img, const CsscLayout& lay
     pX_.ensure(pool, sizeof(u64) * (size_t)ns_ * L * n);
     pM_.ensure(pool, sizeof(u64) * (size_t)ns_ * n);
     pslots_.ensure(pool, pipeline_out_bytes() + 64);
+    pE_.ensure(pool, (size_t)lay.items * 2 * n);
     {
         std::vector<int> g(2 * (size_t)ns_);
         for (int s2 = 0; s2 < ns_; ++s2) {
@@ -454,6 +455,7 @@ void CloudPlan::capture_pipeline(const unsigned char* img, const CsscLayout& lay
     ws.X = pX_.words();
     ws.M = pM_.words();
     ws.slots = pslots_.words();
+    ws.E = pE_.as<int8_t>();
     auto* maxdev = reinterpret_cast<unsigned long long*>(pslots_.as<unsigned char>() + maxdev_off_);
     cudaStream_t st = ctx_.stream();
     cudaGraph_t g = nullptr;

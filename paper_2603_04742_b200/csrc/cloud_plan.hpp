@@ -119,7 +119,7 @@ private:
     int n_masks_ = 0;
     cudaGraph_t graph_ = nullptr;
     cudaGraphExec_t exec_ = nullptr;
-    DevBuf pup_, pU_, pCM_, pX_, pM_, pslots_;  // pipeline workspaces
+    DevBuf pup_, pU_, pCM_, pX_, pM_, pslots_, pE_;  // pipeline workspaces
     cudaGraphExec_t pexec_ = nullptr, eexec_ = nullptr;
     cudaEvent_t ev_early_ = nullptr, ev_fork_ = nullptr;  // early graph on the side stream
     std::vector<cudaEvent_t> pmarks_;  // CSSC_PIPE_PROFILE=1: phase marks inside the pipeline graph
