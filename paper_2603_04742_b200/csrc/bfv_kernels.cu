@@ -152,7 +152,8 @@ __global__ void __launch_bounds__(Ntt2<LOGN>::TC, 256 / Ntt2<LOGN>::TC * 3) k_nt
         const int k = (1 << sl) + blk;
         return make_ulonglong2(tws[2 * k], tws[2 * k + 1]);
     };
-    line_ntt_v<G::A, 0, INV, 3, LN>(tile, ConstQ{q}, addr, twf, whole_cta());  // radix-8 passes: 3 CTAs per SM
+    // radix-8 passes (3 CTAs per SM); 4-column tiles: radix-4, one group per thread
+    line_ntt_v<G::A, 0, INV, (LN >= 8 ? 3 : 2), LN>(tile, ConstQ{q}, addr, twf, whole_cta());
     const u64 ni = dc->ninv[prime], nish = dc->ninv_sh[prime];
 #pragma unroll
     for (int r = 0; r < G::R1 * SEG / T; ++r) {
@@ -171,21 +172,41 @@ __global__ void __launch_bounds__(Ntt2<LOGN>::TC, 256 / Ntt2<LOGN>::TC * 3) k_nt
 // picked 8 columns for 1-2 waves (C2's 144-limb launch) measured 6 % slower:
 // an 8-column CTA costs well over half a 16-column one.  CSSC_COLS_LN=8|16
 // forces a width.
-bool cols_use_ln8(long ctas16, bool allowed) {
-    if (!allowed) return false;
+static int cols_forced() {
     static const int forced = [] {
         const char* e = std::getenv("CSSC_COLS_LN");
         return e ? std::atoi(e) : 0;
     }();
-    if (forced == 8) return true;
+    return forced;
+}
+
+bool cols_use_ln8(long ctas16, bool allowed) {
+    if (!allowed) return false;
+    const int forced = cols_forced();
+    if (forced == 8 || forced == 4) return true;
     if (forced == 16) return false;
     return 2 * ctas16 <= 3L * 148;
+}
+
+// 4-column tiles (radix-4 passes, 4 words per thread) for launches whose
+// 8-column CTAs fill less than half a wave (a lone rotation's key switch):
+// the CTA's serial chain halves, the CTA count doubles.
+bool cols_use_ln4(long ctas16, bool allowed) {
+    if (!allowed) return false;
+    const int forced = cols_forced();
+    if (forced) return forced == 4;
+    return 4 * ctas16 <= 3L * 148;
 }
 
 template <int LOGN, bool INV>
 static void launch_cols(const DevConsts* dc, const NttJob& job, int limbs, cudaStream_t st) {
     using G = Ntt2<LOGN>;
-    if (cols_use_ln8((long)limbs * G::CTAS_C, G::R2 >= 16 && G::R1 * 4 >= G::TC)) {
+    // (4-column tiles measured slower here than in K1, whose ModUp gather
+    // dominates its chain: 8.1 vs 7.7 us for a lone rotation's inverse columns)
+    if (cols_forced() == 4 && G::R2 >= 16 && G::R1 >= G::TC) {
+        constexpr int LN = 4;
+        k_ntt_cols<LOGN, INV, LN><<<limbs * (G::R2 / LN), G::TC, (LN * G::R1 + 2 * G::R1) * 8, st>>>(dc, job);
+    } else if (cols_use_ln8((long)limbs * G::CTAS_C, G::R2 >= 16 && G::R1 * 4 >= G::TC)) {
         constexpr int LN = 8;
         k_ntt_cols<LOGN, INV, LN><<<limbs * (G::R2 / LN), G::TC, (LN * G::R1 + 2 * G::R1) * 8, st>>>(dc, job);
     } else {

@@ -39,6 +39,7 @@ enum SampleDomain : u32 {
 
 // column-tile width policy shared by the column-phase kernels (ctas16 = CTAs at 16 columns)
 bool cols_use_ln8(long ctas16, bool allowed);
+bool cols_use_ln4(long ctas16, bool allowed);
 void launch_ntt(const DevConsts* dc, int logn, bool inverse, const NttJob& job, int items,
                 cudaStream_t st);
 // a single phase of the two-phase NTT (cols = column phase, else block phase)

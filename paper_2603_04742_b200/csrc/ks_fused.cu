@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(Ntt2<LOGN>::TC, 256 / Ntt2<LOGN>::TC * 3) k_ks
         const int k = (1 << sl) + blk;
         return make_ulonglong2(tws[2 * k], tws[2 * k + 1]);
     };
-    line_ntt_v<G::A, 0, false, 3, LN>(tile, ConstQ{m}, addr, twf, whole_cta());  // radix-8: 3 CTAs per SM
+    line_ntt_v<G::A, 0, false, (LN >= 8 ? 3 : 2), LN>(tile, ConstQ{m}, addr, twf, whole_cta());  // radix-8: 3 CTAs/SM
     u64* dst = DX + (((size_t)item * dnum + dg) * LK + j) * G::N;
     constexpr int SEG = LN / 2;
 #pragma unroll
@@ -280,7 +280,11 @@ static void ks_fused_t(const DevConsts* dc, const RnsParams& P, const u64* const
                              smem2h);
         configured = smem2;
     }
-    if (cols_use_ln8((long)items * dnum * LK * G::CTAS_C, G::R1 * 4 >= G::TC)) {  // 8-column tiles
+    if (cols_use_ln4((long)items * dnum * LK * G::CTAS_C, G::R1 >= G::TC)) {  // 4-column tiles
+        constexpr int LN = 4;
+        k_ks_modup_cols<LOGN, LT, KT, AT, LN><<<items * dnum * LK * (G::R2 / LN), G::TC,
+                                                (LN * G::R1 + 2 * G::R1) * 8, st>>>(dc, SRC, SRCC, src_poly, ginv, DX);
+    } else if (cols_use_ln8((long)items * dnum * LK * G::CTAS_C, G::R1 * 4 >= G::TC)) {  // 8-column tiles
         constexpr int LN = 8;
         k_ks_modup_cols<LOGN, LT, KT, AT, LN><<<items * dnum * LK * (G::R2 / LN), G::TC,
                                                 (LN * G::R1 + 2 * G::R1) * 8, st>>>(dc, SRC, SRCC, src_poly, ginv, DX);
