@@ -140,6 +140,9 @@ __global__ void __launch_bounds__(kKsGroups * kKsGroupThreads) k_ks_blocks_inner
     constexpr int TW = LN * PITCH;
     constexpr int T = kKsGroups * kKsGroupThreads;
     constexpr int PER = LN * G::R2 / T;  // elements per thread
+    // 8-block tiles (small launches): radix-4 passes keep all 128 threads of a
+    // group busy (radix-8 would leave half idle) and halve each thread's chain
+    constexpr int KMR = LN >= 16 ? 4 : 2;
     constexpr int CTAS = G::R1 / LN;
     static_assert(PER >= 1, "tile smaller than the CTA");
     const int L = LT ? LT : dc->L, K = KT ? KT : dc->K, LK = L + K;
@@ -193,7 +196,7 @@ __global__ void __launch_bounds__(kKsGroups * kKsGroupThreads) k_ks_blocks_inner
     __syncthreads();
 #pragma unroll 1
     for (int dg = grp; dg < dnum; dg += kKsGroups)
-        line_ntt_v<G::B, 0, false, 4, LN>(work + dg * TW, ConstQ{q}, addr, twf, tg);
+        line_ntt_v<G::B, 0, false, KMR, LN>(work + dg * TW, ConstQ{q}, addr, twf, tg);
     __syncthreads();
     // inner product with both key polynomials (tiles in smem once the TMA
     // transaction completes); every position is read (all digits) and then
@@ -223,7 +226,7 @@ __global__ void __launch_bounds__(kKsGroups * kKsGroupThreads) k_ks_blocks_inner
     load_block_twiddles<LOGN, LN>(tws, dc->tw[j].inv, blk0);
     cp_async_wait_all();
     __syncthreads();
-    line_ntt_v<G::B, 0, true, 4, LN>(work + grp * TW, ConstQ{q}, addr, twf, tg);  // group p: accumulator p
+    line_ntt_v<G::B, 0, true, KMR, LN>(work + grp * TW, ConstQ{q}, addr, twf, tg);  // group p: accumulator p
     __syncthreads();
 #pragma unroll
     for (int p = 0; p < 2; ++p) {
