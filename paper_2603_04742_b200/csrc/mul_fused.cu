@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(2 * kGroupThreads) k_mask_blocks(const DevCons
         }
         cp_async_wait_all();
         tg.sync();
-        line_ntt_v<G::B, 0, false, 4, LN>(wk, ConstQ{q}, addr, twf, tg);
+        line_ntt_v<G::B, 0, false, (LN >= 16 ? 4 : 2), LN>(wk, ConstQ{q}, addr, twf, tg);
         const u64* mk = MASKS + ((size_t)item_mask[it] * L + j) * G::N + base;
 #pragma unroll
         for (int r = 0; r < PERG; ++r) {
@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(2 * kGroupThreads) k_mask_blocks(const DevCons
     load_block_twiddles<LOGN, LN>(tws, dc->tw[j].inv, blk0);
     cp_async_wait_all();
     __syncthreads();
-    line_ntt_v<G::B, 0, true, 4, LN>(acc, ConstQ{q}, addr, twf, whole_cta());
+    line_ntt_v<G::B, 0, true, 2, LN>(acc, ConstQ{q}, addr, twf, whole_cta());  // radix-4: more threads busy
     u64* dst = OUT[sl] + (size_t)j2 * G::N + base;
 #pragma unroll
     for (int r = 0; r < PER; ++r) {
@@ -258,7 +258,7 @@ __global__ void __launch_bounds__(4 * kGroupThreads) k_mask_dec_blocks(const Dev
         }
         cp_async_wait_all();
         tg.sync();
-        line_ntt_v<G::B, 0, false, 4, LN>(wk, ConstQ{q}, addr, twf, tg);
+        line_ntt_v<G::B, 0, false, (LN >= 16 ? 4 : 2), LN>(wk, ConstQ{q}, addr, twf, tg);
         const u64* mk = MASKS + ((size_t)item_mask[it] * L + j) * G::N + base;
 #pragma unroll
         for (int r = 0; r < PERG; ++r) {
@@ -284,7 +284,7 @@ __global__ void __launch_bounds__(4 * kGroupThreads) k_mask_dec_blocks(const Dev
     load_block_twiddles<LOGN, LN>(tws, dc->tw[j].inv, blk0);
     cp_async_wait_all();
     __syncthreads();
-    line_ntt_v<G::B, 0, true, 4, LN>(acc, ConstQ{q}, addr, twf, whole_cta());
+    line_ntt_v<G::B, 0, true, 2, LN>(acc, ConstQ{q}, addr, twf, whole_cta());  // radix-4: more threads busy
     u64* dst = D + ((size_t)sl * L + j) * G::N + base;
 #pragma unroll
     for (int r = 0; r < PER; ++r) {
