@@ -595,7 +595,7 @@ void GpuContext::add(const std::vector<const u64*>& a, const std::vector<const u
 
 void GpuContext::mul_relin_dev(const u64* const* A, const u64* const* B, u64* const* OUT,
                                int items, u64* T, u64* Z, u64* D2, u64* DX, u64* ACC,
-                               const u64* const* RLK, const EncIn* enc) {
+                               const u64* const* RLK, const EncIn* enc, u64* D2Y, u64* const* YOUT) {
     const int L = P_.cfg.L, K = P_.cfg.K, LK = L + K, M = L + P_.nB, logn = P_.cfg.logn;
     std::vector<int> pm;
     for (int j = 0; j < M; ++j) pm.push_back(j < L ? j : K + j);
@@ -612,10 +612,13 @@ void GpuContext::mul_relin_dev(const u64* const* A, const u64* const* B, u64* co
         launch_mul_tensor(dc_, P_, T, Z, items, st_);
         launch_ntt(dc_, logn, true, job(Z, Z, 3 * M, pm), items, st_);
     }
-    launch_mul_scale(dc_, P_, Z, OUT, D2, items, st_);
+    launch_mul_scale(dc_, P_, Z, OUT, D2, items, st_, fused_ks_ ? D2Y : nullptr);
     if (fused_ks_) {
+        KsY ky;
+        ky.srcc = D2Y;
+        ky.out = YOUT;
         launch_ks_fused(dc_, P_, nullptr, D2, 0, nullptr, RLK, reinterpret_cast<const u64* const*>(OUT),
-                        nullptr, OUT, DX, ACC, items, st_);
+                        nullptr, OUT, DX, ACC, items, st_, nullptr, nullptr, ky);
         stats_.kernels += 9;
     } else {
         launch_ks_modup_contig(dc_, P_, D2, DX, items, st_);
@@ -645,10 +648,10 @@ void GpuContext::mul_relin(const std::vector<const u64*>& a, const std::vector<c
 
 void GpuContext::rotate_dev(const u64* const* SRC, const u32* ginv, const u64* const* KEY,
                             const u64* const* BASE, u64* const* OUT, int items, u64* DX, u64* ACC,
-                            const u64* const* EXTRA, const int* PAIR) {
+                            const u64* const* EXTRA, const int* PAIR, const KsY& ky) {
     const int LK = P_.cfg.L + P_.cfg.K, logn = P_.cfg.logn;
     if (fused_ks_) {
-        launch_ks_fused(dc_, P_, SRC, nullptr, 1, ginv, KEY, BASE, SRC, OUT, DX, ACC, items, st_, EXTRA, PAIR);
+        launch_ks_fused(dc_, P_, SRC, nullptr, 1, ginv, KEY, BASE, SRC, OUT, DX, ACC, items, st_, EXTRA, PAIR, ky);
         stats_.kernels += 4;
     } else {
         launch_ks_modup(dc_, P_, SRC, 1, ginv, DX, items, st_);

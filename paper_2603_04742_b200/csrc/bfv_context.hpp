@@ -164,15 +164,17 @@ public:
 
     // building blocks reused by the batched cloud plan (pointer arrays on device)
     // enc: A and B are still to be finished from a deferred encryption (EncIn)
+    // D2Y / YOUT (fused key switch, fixed shapes): the ModUp factors of c2 and
+    // of the products' c1 (KsY)
     void mul_relin_dev(const u64* const* A, const u64* const* B, u64* const* OUT, int items,
                        u64* T, u64* Z, u64* D2, u64* DX, u64* ACC, const u64* const* RLK,
-                       const EncIn* enc = nullptr);
+                       const EncIn* enc = nullptr, u64* D2Y = nullptr, u64* const* YOUT = nullptr);
     // OUT = BASE + EXTRA + rot(SRC) (BASE / EXTRA per-item nullable); PAIR (nullable):
     // PAIR[i] = j >= 0 also adds item j's rotation into OUT[i] (PAIR[j] = -3 - i;
     // the two items' CTAs split the limbs)
     void rotate_dev(const u64* const* SRC, const u32* ginv, const u64* const* KEY,
                     const u64* const* BASE, u64* const* OUT, int items, u64* DX, u64* ACC,
-                    const u64* const* EXTRA = nullptr, const int* PAIR = nullptr);
+                    const u64* const* EXTRA = nullptr, const int* PAIR = nullptr, const KsY& ky = KsY{});
     void encode_masks(const std::vector<int>& ones_len, u64* MASKS);  // NTT form [m][L][N]
     NttJob job(const u64* src, u64* dst, int limbs, const std::vector<int>& pidx) const;
 

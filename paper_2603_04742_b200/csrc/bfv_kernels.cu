@@ -573,12 +573,13 @@ struct ScaleK {
     W29 C[L][L + 1];  // [-[Q/q_i]_{b_j} Q^-1 t]_{b_j}
     W29 D[L + 1];     // [Q^-1 t]_{b_j}
     ExtK<L + 1, L> bq;
+    u64 dhi[L], dhi_sh[L];  // ModUp factors [(Q_d / q_i)^-1]_{q_i} (KsY)
 };
 
 // E2 + E1 as k_mul_scale, constants from the parameter block
 template <int L>
 __global__ void k_mul_scale_k(const __grid_constant__ ScaleK<L> c, const u64* __restrict__ Z, u64* const* OUT,
-                              u64* __restrict__ D2) {
+                              u64* __restrict__ D2, u64* __restrict__ D2Y) {
     constexpr int nB = L + 1, M = L + nB;
     const int n = c.n;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
@@ -608,6 +609,11 @@ __global__ void k_mul_scale_k(const __grid_constant__ ScaleK<L> c, const u64* __
     u64* dst = r < 2 ? OUT[item] + (size_t)r * L * n : D2 + (size_t)item * L * n;
 #pragma unroll
     for (int i = 0; i < L; ++i) dst[(size_t)i * n + k] = o[i];
+    if (r == 2 && D2Y) {  // the relinearisation's ModUp factors of c2
+        u64* y = D2Y + (size_t)item * L * n;
+#pragma unroll
+        for (int i = 0; i < L; ++i) y[(size_t)i * n + k] = shoup(o[i], c.dhi[i], c.dhi_sh[i], c.q[i]);
+    }
 }
 
 template <int L>
@@ -637,6 +643,10 @@ static ScaleK<L> make_scale_k(const RnsParams& P) {
         for (int i = 0; i < L; ++i) c.C[i][j] = split29((b - host_mulmod(h.QhatB[i][j], D, b)) % b);
     }
     fill_extk(c.bq, h, h.extBQ);
+    for (int i = 0; i < L; ++i) {
+        c.dhi[i] = h.dig_hat_inv[i];
+        c.dhi_sh[i] = h.dig_hat_inv_sh[i];
+    }
     return c;
 }
 
@@ -776,14 +786,16 @@ __global__ void k_mul_scale(const DevConsts* __restrict__ dc, const u64* __restr
 }
 
 void launch_mul_scale(const DevConsts* dc, const RnsParams& P, const u64* Z, u64* const* OUT,
-                      u64* D2, int items, cudaStream_t st) {
+                      u64* D2, int items, cudaStream_t st, u64* D2Y) {
     if (!items) return;
     dispatch_shape(P, [&](auto l_, auto k_, auto a_) {
         dim3 g = ew_grid(P.n, items);
         g.z = 3;
         constexpr int LT = decltype(l_)::value;
         if constexpr (LT > 0)
-            k_mul_scale_k<LT><<<g, EW_THREADS, 0, st>>>(make_scale_k<LT>(P), Z, OUT, D2);
+            k_mul_scale_k<LT><<<g, EW_THREADS, 0, st>>>(make_scale_k<LT>(P), Z, OUT, D2, D2Y);
+        else if (D2Y)
+            throw std::invalid_argument("hoisted ModUp factors need a fixed RNS shape");
         else
             k_mul_scale<SHAPE_ARGS><<<g, EW_THREADS, 0, st>>>(dc, Z, OUT, D2);
     });
@@ -968,6 +980,7 @@ struct ModDownK {
     // out_j = (acc_j - sum_k y_k [P/p_k]_{q_j}) P^-1 = acc_j Pinv + sum_k y_k E_kj
     W29 E[K][L];  // [-[P/p_k]_{q_j} P^-1]_{q_j} in 29-bit halves
     W29 F[L];     // [P^-1]_{q_j}
+    u64 dhi[L], dhi_sh[L];  // ModUp factors of the output's c1 (KsY)
 };
 
 // k_ks_moddown with the constants from a parameter block (same values; the
@@ -976,7 +989,8 @@ template <int L, int K>
 __global__ void __launch_bounds__(128, 6) k_ks_moddown_k(const __grid_constant__ ModDownK<L, K> c,
                                                          const u64* __restrict__ ACC, const u64* const* BASE,
                                                          const u64* const* RSRC, const u32* ginv, u64* const* OUT,
-                                                         const u64* const* EXTRA, const int* PAIR) {
+                                                         const u64* const* EXTRA, const int* PAIR,
+                                                         u64* const* YOUT) {
     constexpr int LK = L + K;
     static_assert(K + 1 <= 15, "Dot29 bound");
     const int n = c.n;
@@ -989,6 +1003,7 @@ __global__ void __launch_bounds__(128, 6) k_ks_moddown_k(const __grid_constant__
     const int pair = pv <= -3 ? blockIdx.y : pv;
     const int p = blockIdx.z;
     u64* out = OUT[item] + (size_t)p * L * n;
+    u64* yo = (p == 1 && YOUT) ? YOUT[item] : nullptr;  // ModUp factors of c1 for the next key switch
     const u64* base = BASE ? BASE[item] : nullptr;
     if (base) base += (size_t)p * L * n;
     const u64* ex = EXTRA ? EXTRA[item] : nullptr;
@@ -1041,7 +1056,9 @@ __global__ void __launch_bounds__(128, 6) k_ks_moddown_k(const __grid_constant__
             for (int kk = 0; kk < K; ++kk) dot29_mac(d, y[kk], c.E[kk][j]);
             u64 v = dot29_reduce(d, c.qm[j]);
             if (rs) v = add_mod(v, neg ? neg_mod(rv[j], q) : rv[j], q);
-            out[(size_t)j * n + k] = add_mod(v, bv[j], q);
+            v = add_mod(v, bv[j], q);
+            out[(size_t)j * n + k] = v;
+            if (yo) yo[(size_t)j * n + k] = shoup(v, c.dhi[j], c.dhi_sh[j], q);
         }
     } else if (pair < 0) {
 #pragma unroll 2
@@ -1051,6 +1068,7 @@ __global__ void __launch_bounds__(128, 6) k_ks_moddown_k(const __grid_constant__
             if (base) v = add_mod(v, base[(size_t)j * n + k], q);
             if (ex) v = add_mod(v, ex[(size_t)j * n + k], q);
             out[(size_t)j * n + k] = v;
+            if (yo) yo[(size_t)j * n + k] = shoup(v, c.dhi[j], c.dhi_sh[j], q);
         }
     } else {  // merged rotation of item `pair`, half of the limbs
         u64 y2[K];
@@ -1066,6 +1084,7 @@ __global__ void __launch_bounds__(128, 6) k_ks_moddown_k(const __grid_constant__
             if (base) v = add_mod(v, base[(size_t)j * n + k], q);
             if (ex) v = add_mod(v, ex[(size_t)j * n + k], q);
             out[(size_t)j * n + k] = v;
+            if (yo) yo[(size_t)j * n + k] = shoup(v, c.dhi[j], c.dhi_sh[j], q);
         }
     }
 }
@@ -1082,6 +1101,8 @@ static ModDownK<L, K> make_moddown_k(const RnsParams& P) {
     }
     for (int j = 0; j < L; ++j) {
         c.qm[j] = h.mod[j];
+        c.dhi[j] = h.dig_hat_inv[j];
+        c.dhi_sh[j] = h.dig_hat_inv_sh[j];
         const u64 q = h.mod[j].q;
         c.F[j] = split29(h.Pinv_q[j]);
         for (int kk = 0; kk < K; ++kk)
@@ -1092,7 +1113,8 @@ static ModDownK<L, K> make_moddown_k(const RnsParams& P) {
 
 void launch_ks_moddown(const DevConsts* dc, const RnsParams& P, const u64* ACC,
                        const u64* const* BASE, const u64* const* RSRC, const u32* ginv,
-                       u64* const* OUT, int items, cudaStream_t st, const u64* const* EXTRA, const int* PAIR) {
+                       u64* const* OUT, int items, cudaStream_t st, const u64* const* EXTRA, const int* PAIR,
+                       u64* const* YOUT) {
     if (!items) return;
     dispatch_shape(P, [&](auto l_, auto k_, auto a_) {
         dim3 g = ew_grid(P.n, items);
@@ -1100,7 +1122,9 @@ void launch_ks_moddown(const DevConsts* dc, const RnsParams& P, const u64* ACC,
         constexpr int LT = decltype(l_)::value, KT = decltype(k_)::value;
         if constexpr (LT > 0)
             k_ks_moddown_k<LT, KT><<<g, EW_THREADS, 0, st>>>(make_moddown_k<LT, KT>(P), ACC, BASE, RSRC, ginv, OUT,
-                                                            EXTRA, PAIR);
+                                                            EXTRA, PAIR, YOUT);
+        else if (YOUT)
+            throw std::invalid_argument("hoisted ModUp factors need a fixed RNS shape");
         else
             k_ks_moddown<SHAPE_ARGS><<<g, EW_THREADS, 0, st>>>(dc, ACC, BASE, RSRC, ginv, OUT, EXTRA, PAIR);
     });

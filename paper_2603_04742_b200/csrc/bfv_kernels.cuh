@@ -49,6 +49,15 @@ size_t ntt_smem_bytes(int logn);
 
 // ct x ct
 // pipeline: the encryption's finish (e, Delta m) fused into the base extension
+// Hoisted ModUp factors: y_i = [x_i (Q_d / q_i)^-1]_{q_i} of a ciphertext's c1
+// (the key switch's source), written by the kernel that produces c1 (ModDown,
+// the multiply's scale) so K1 reads y instead of recomputing it per target.
+struct KsY {
+    const u64* const* src = nullptr;  // per item: y of the source's c1 [L][N] (null: compute from x)
+    const u64* srcc = nullptr;        // contiguous variant ([item][L][N])
+    u64* const* out = nullptr;        // per item (nullable entries): y of the output's c1
+};
+
 struct EncIn {
     u64 seed;
     const u64* streams;  // per encryption item (a chunks, then b chunks)
@@ -90,7 +99,7 @@ void launch_mul_blocks_tensor(const DevConsts* dc, const RnsParams& P, const u64
 void launch_mul_tensor(const DevConsts* dc, const RnsParams& P, const u64* T, u64* Z, int items,
                        cudaStream_t st);
 void launch_mul_scale(const DevConsts* dc, const RnsParams& P, const u64* Z, u64* const* OUT,
-                      u64* D2, int items, cudaStream_t st);
+                      u64* D2, int items, cudaStream_t st, u64* D2Y = nullptr);
 
 // hybrid key switching
 void launch_ks_modup(const DevConsts* dc, const RnsParams& P, const u64* const* SRC, int src_poly,
@@ -104,7 +113,7 @@ void launch_ks_inner(const DevConsts* dc, const RnsParams& P, const u64* DX,
 void launch_ks_moddown(const DevConsts* dc, const RnsParams& P, const u64* ACC,
                        const u64* const* BASE, const u64* const* RSRC, const u32* ginv,
                        u64* const* OUT, int items, cudaStream_t st, const u64* const* EXTRA = nullptr,
-                       const int* PAIR = nullptr);
+                       const int* PAIR = nullptr, u64* const* YOUT = nullptr);
 
 // masks / plaintext products
 void launch_mask_accum(const DevConsts* dc, const RnsParams& P, const u64* MT,
@@ -188,5 +197,5 @@ bool launch_ks_cluster(const DevConsts* dc, const RnsParams& P, const u64* const
 void launch_ks_fused(const DevConsts* dc, const RnsParams& P, const u64* const* SRC, const u64* SRCC,
                      int src_poly, const u32* ginv, const u64* const* KEY, const u64* const* BASE,
                      const u64* const* RSRC, u64* const* OUT, u64* DX, u64* ACC, int items, cudaStream_t st,
-                     const u64* const* EXTRA = nullptr, const int* PAIR = nullptr);
+                     const u64* const* EXTRA = nullptr, const int* PAIR = nullptr, const KsY& ky = KsY{});
 }  // namespace cssc

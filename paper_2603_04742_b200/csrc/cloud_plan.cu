@@ -111,7 +111,7 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
                      [&](int x, int y) { return trees[x].dbl.size() > trees[y].dbl.size(); });
     const int depth = n ? (int)trees[order[0]].dbl.size() : 0;
 
-    arena_ = DevBuf(&ctx.pool(), 8 * ((size_t)(11 + 6 * std::max(depth, 1)) * std::max(n, 1) + 7 * n_odd +
+    arena_ = DevBuf(&ctx.pool(), 8 * ((size_t)(12 + 8 * std::max(depth, 1)) * std::max(n, 1) + 9 * n_odd +
                                       2 * (size_t)ns_ + 8) +
                                      16 * (size_t)(6 * depth + 24));
     prod_ = DevBuf(&ctx.pool(), sizeof(u64) * ctw * std::max(n, 1));
@@ -125,6 +125,21 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
     DX_ = DevBuf(&ctx.pool(), sizeof(u64) * ks_items * ctx.dx_words());
     ACC_ = DevBuf(&ctx.pool(), sizeof(u64) * ks_items * ctx.ksacc_words());
     MT_ = DevBuf(&ctx.pool(), sizeof(u64) * std::max<size_t>(1, n) * ctw);
+    // hoisted ModUp factors (KsY) of every ciphertext a key switch reads: the
+    // products, both accumulator arrays and the relinearisation's c2
+    const bool hoist = ctx.fused_key_switch() && fixed_rns_shape(P) && std::getenv("CSSC_NO_KSY") == nullptr;
+    const size_t pw = ctx.poly_words();
+    if (hoist) {
+        prodY_ = DevBuf(&ctx.pool(), sizeof(u64) * pw * std::max(n, 1));
+        if (depth >= 1) accY0_ = DevBuf(&ctx.pool(), sizeof(u64) * pw * n);
+        if (depth >= 2) accY1_ = DevBuf(&ctx.pool(), sizeof(u64) * pw * n);
+        D2Y_ = DevBuf(&ctx.pool(), sizeof(u64) * pw * std::max(n, 1));
+    }
+    auto prodY_at = [&](int k) -> u64* { return hoist ? prodY_.words() + (size_t)k * pw : nullptr; };
+    auto accY_at = [&](int which, int k) -> u64* {
+        return hoist ? (which == 0 ? accY0_.words() : accY1_.words()) + (size_t)k * pw : nullptr;
+    };
+    auto yafter = [&](int k, int done) -> u64* { return done == 0 ? prodY_at(k) : accY_at((done - 1) % 2, k); };
 
     auto prod_at = [&](int k) { return prod_.words() + (size_t)k * ctw; };
     auto acc_at = [&](int which, int k) {
@@ -147,6 +162,12 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
     ORDER_ = put(order);
     PROD_ = put(vp);
     RLK_ = put(rlk);
+    if (hoist) {
+        std::vector<u64*> py(n);
+        for (int k = 0; k < n; ++k)
+            py[k] = (trees[order[k]].dbl.empty() && trees[order[k]].odd.empty()) ? nullptr : prodY_at(k);
+        PRODY_ = put(py);
+    }
 
     const bool fused = ctx.fused_key_switch();
     const u64 C = sizeof(u64) * ctw, KEY = sizeof(u64) * ctx.ksk_words(),
@@ -173,7 +194,8 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
         return ctx.galois_key(g);
     };
     for (int l = 0; l < depth; ++l) {
-        std::vector<const u64*> src, base, key, extra;
+        std::vector<const u64*> src, base, key, extra, ysrc;
+        std::vector<u64*> yout;
         std::vector<u64*> o;
         std::vector<u32> gi;
         std::vector<int> pair;  // -1 plain; D_1 k: its O_1 item j; that O_1 item: -3 - k
@@ -188,6 +210,8 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
             src.push_back(cur);
             base.push_back(cur);
             o.push_back(acc_at(l % 2, k));
+            ysrc.push_back(yafter(k, l));
+            yout.push_back((int)t.dbl.size() > l + 1 ? accY_at(l % 2, k) : nullptr);
             extra.push_back(nullptr);
             if (l >= 1) {  // fuse RP of the odd step that follows D_{l+1}
                 auto it = rp_after[k].find(l + 1);
@@ -207,6 +231,8 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
                     key.push_back(key_of(off, lvl_keys, g));
                     gi.push_back(g);
                     src.push_back(prod_at(k));
+                    ysrc.push_back(prodY_at(k));
+                    yout.push_back(nullptr);
                     base.push_back(nullptr);
                     extra.push_back(nullptr);
                     o.push_back(slot);
@@ -222,6 +248,8 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
         lv.key = put(key);
         lv.ginv = put(gi);
         lv.extra = put(extra);
+        lv.ysrc = hoist ? put(ysrc) : nullptr;
+        lv.yout = hoist ? put(yout) : nullptr;
         pair.resize(o.size(), -1);
         lv.pair = std::any_of(pair.begin(), pair.end(), [](int v) { return v != -1; }) ? put(pair) : nullptr;
         lv.keys = (int)lvl_keys.size();
@@ -297,12 +325,15 @@ void CloudPlan::record(std::vector<cudaEvent_t>* marks, u64* dec_d, const EncIn*
     };
     mark();
     ctx_.mul_relin_dev(A_, B_, PROD_, n_, T_.words(), Z_.words(), D2_.words(), DX_.words(),
-                       ACC_.words(), RLK_, enc);
+                       ACC_.words(), RLK_, enc, PRODY_ ? D2Y_.words() : nullptr, PRODY_);
     mark();
     for (size_t l = 0; l < levels_.size(); ++l) {
         const Level& lv = levels_[l];
+        KsY ky;
+        ky.src = lv.ysrc;
+        ky.out = lv.yout;
         ctx_.rotate_dev(lv.src, lv.ginv, lv.key, lv.base, lv.out, lv.items, DX_.words(), ACC_.words(),
-                        lv.extra, lv.pair);
+                        lv.extra, lv.pair, ky);
         mark();
     }
     std::vector<int> qidx(L);

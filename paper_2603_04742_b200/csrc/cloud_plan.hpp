@@ -108,6 +108,8 @@ private:
         const u32* ginv;
         const u64* const* extra;  // fused add of a hoisted odd-step rotation (nullable)
         const int* pair;          // level 0: D_1 items merging their O_1 rotation (nullable)
+        const u64* const* ysrc;   // hoisted ModUp factors of each source's c1 (KsY; nullable)
+        u64* const* yout;         // ... of each output's c1 when a later level rotates it
         int keys;                  // distinct switching keys of the level
     };
     std::vector<Level> levels_;
@@ -120,6 +122,8 @@ private:
     cudaGraph_t graph_ = nullptr;
     cudaGraphExec_t exec_ = nullptr;
     DevBuf pup_, pU_, pCM_, pX_, pM_, pslots_, pE_;  // pipeline workspaces
+    DevBuf prodY_, accY0_, accY1_, D2Y_;            // hoisted ModUp factors (KsY)
+    u64* const* PRODY_ = nullptr;
     cudaGraphExec_t pexec_ = nullptr, eexec_ = nullptr;
     cudaEvent_t ev_early_ = nullptr, ev_fork_ = nullptr;  // early graph on the side stream
     std::vector<cudaEvent_t> pmarks_;  // CSSC_PIPE_PROFILE=1: phase marks inside the pipeline graph

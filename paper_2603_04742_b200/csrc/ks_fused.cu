@@ -55,7 +55,8 @@ __device__ __forceinline__ void load_col_twiddles(u64* tws, const u64* tw) {
 // LN columns per CTA: 16, or 8 when the launch would not fill the GPU
 template <int LOGN, int LT, int KT, int AT, int LN = 16>
 __global__ void __launch_bounds__(Ntt2<LOGN>::TC, 256 / Ntt2<LOGN>::TC * 3) k_ks_modup_cols(const DevConsts* __restrict__ dc, const u64* const* SRC,
-                                                       const u64* SRCC, int src_poly, const u32* ginv, u64* DX) {
+                                                       const u64* SRCC, int src_poly, const u32* ginv, u64* DX,
+                                                       const u64* const* YS, const u64* YSC) {
     using G = Ntt2<LOGN>;
     constexpr int CTAS = G::R2 / LN;
     extern __shared__ u64 smem[];
@@ -72,6 +73,8 @@ __global__ void __launch_bounds__(Ntt2<LOGN>::TC, 256 / Ntt2<LOGN>::TC * 3) k_ks
     const int item = bid / dnum;
     const int lo = dg * alpha, hi = min(lo + alpha, L);
     const u64* src = SRC ? SRC[item] + (size_t)src_poly * L * G::N : SRCC + (size_t)item * L * G::N;
+    // hoisted ModUp factors y_i of the source (KsY), when its producer wrote them
+    const u64* ysrc = YS ? YS[item] : (YSC ? YSC + (size_t)item * L * G::N : nullptr);
     const u32 gi = ginv ? ginv[item] : 0u;
     const u64 m = dc->mod[j].q;
     const bool own = j >= lo && j < hi;
@@ -93,9 +96,15 @@ __global__ void __launch_bounds__(Ntt2<LOGN>::TC, 256 / Ntt2<LOGN>::TC * 3) k_ks
             for (int i = lo; i < (AT ? lo + AT : hi); ++i) {
                 if (AT && i >= hi) break;
                 const u64 qi = dc->mod[i].q;
-                u64 x = __ldg(src + (size_t)i * G::N + idx);
-                x = neg ? neg_mod(x, qi) : x;
-                const u64 y = shoup(x, dc->dig_hat_inv[i], dc->dig_hat_inv_sh[i], qi);
+                u64 y;
+                if (ysrc) {  // y of phi_g(x) is phi_g(y): the same gather and negation
+                    y = __ldg(ysrc + (size_t)i * G::N + idx);
+                    y = neg ? neg_mod(y, qi) : y;
+                } else {
+                    u64 x = __ldg(src + (size_t)i * G::N + idx);
+                    x = neg ? neg_mod(x, qi) : x;
+                    y = shoup(x, dc->dig_hat_inv[i], dc->dig_hat_inv_sh[i], qi);
+                }
                 v += shoup_lazy(y, dc->dig_hat[i][j], dc->dig_hat_sh[i][j], m);  // alpha <= 16 terms < 2m
             }
             v = reduce_small_quot(v, dc->mod[j]);
@@ -260,10 +269,10 @@ template <int LOGN, int LT, int KT, int AT>
 static void ks_fused_t(const DevConsts* dc, const RnsParams& P, const u64* const* SRC, const u64* SRCC,
                        int src_poly, const u32* ginv, const u64* const* KEY, const u64* const* BASE,
                        const u64* const* RSRC, u64* const* OUT, u64* DX, u64* ACC, int items, cudaStream_t st,
-                       const u64* const* EXTRA, const int* PAIR) {
+                       const u64* const* EXTRA, const int* PAIR, const KsY& ky) {
     using G = Ntt2<LOGN>;
     if (launch_ks_cluster(dc, P, SRC, SRCC, src_poly, ginv, KEY, ACC, items, st)) {
-        launch_ks_moddown(dc, P, ACC, BASE, RSRC, ginv, OUT, items, st, EXTRA, PAIR);
+        launch_ks_moddown(dc, P, ACC, BASE, RSRC, ginv, OUT, items, st, EXTRA, PAIR, ky.out);
         return;
     }
     const int L = P.cfg.L, K = P.cfg.K, LK = L + K, dnum = P.dnum;
@@ -286,14 +295,15 @@ static void ks_fused_t(const DevConsts* dc, const RnsParams& P, const u64* const
     if (cols_use_ln4((long)items * dnum * LK * G::CTAS_C, G::R1 >= G::TC)) {  // 4-column tiles
         constexpr int LN = 4;
         k_ks_modup_cols<LOGN, LT, KT, AT, LN><<<items * dnum * LK * (G::R2 / LN), G::TC,
-                                                (LN * G::R1 + 2 * G::R1) * 8, st>>>(dc, SRC, SRCC, src_poly, ginv, DX);
+                                                (LN * G::R1 + 2 * G::R1) * 8, st>>>(dc, SRC, SRCC, src_poly, ginv, DX, ky.src, ky.srcc);
     } else if (cols_use_ln8((long)items * dnum * LK * G::CTAS_C, G::R1 * 4 >= G::TC)) {  // 8-column tiles
         constexpr int LN = 8;
         k_ks_modup_cols<LOGN, LT, KT, AT, LN><<<items * dnum * LK * (G::R2 / LN), G::TC,
-                                                (LN * G::R1 + 2 * G::R1) * 8, st>>>(dc, SRC, SRCC, src_poly, ginv, DX);
+                                                (LN * G::R1 + 2 * G::R1) * 8, st>>>(dc, SRC, SRCC, src_poly, ginv, DX, ky.src, ky.srcc);
     } else {
         k_ks_modup_cols<LOGN, LT, KT, AT><<<items * dnum * LK * G::CTAS_C, G::TC, smem1, st>>>(dc, SRC, SRCC,
-                                                                                          src_poly, ginv, DX);
+                                                                                          src_poly, ginv, DX, ky.src,
+                                                                                          ky.srcc);
     }
     KS_CHECK();
     constexpr int T2 = kKsGroups * kKsGroupThreads;
@@ -308,32 +318,32 @@ static void ks_fused_t(const DevConsts* dc, const RnsParams& P, const u64* const
     j.dst = ACC;
     j.limbs = 2 * LK;
     launch_ntt_phase(dc, LOGN, /*inverse=*/true, /*cols=*/true, j, items, st);
-    launch_ks_moddown(dc, P, ACC, BASE, RSRC, ginv, OUT, items, st, EXTRA, PAIR);
+    launch_ks_moddown(dc, P, ACC, BASE, RSRC, ginv, OUT, items, st, EXTRA, PAIR, ky.out);
 }
 
 template <int LOGN>
 static void ks_fused_logn(const DevConsts* dc, const RnsParams& P, const u64* const* SRC, const u64* SRCC,
                           int src_poly, const u32* ginv, const u64* const* KEY, const u64* const* BASE,
                           const u64* const* RSRC, u64* const* OUT, u64* DX, u64* ACC, int items, cudaStream_t st,
-                       const u64* const* EXTRA, const int* PAIR) {
+                       const u64* const* EXTRA, const int* PAIR, const KsY& ky) {
     ks_dispatch_shape(P, [&](auto l_, auto k_, auto a_) {
         ks_fused_t<LOGN, decltype(l_)::value, decltype(k_)::value, decltype(a_)::value>(
-            dc, P, SRC, SRCC, src_poly, ginv, KEY, BASE, RSRC, OUT, DX, ACC, items, st, EXTRA, PAIR);
+            dc, P, SRC, SRCC, src_poly, ginv, KEY, BASE, RSRC, OUT, DX, ACC, items, st, EXTRA, PAIR, ky);
     });
 }
 
 void launch_ks_fused(const DevConsts* dc, const RnsParams& P, const u64* const* SRC, const u64* SRCC,
                      int src_poly, const u32* ginv, const u64* const* KEY, const u64* const* BASE,
                      const u64* const* RSRC, u64* const* OUT, u64* DX, u64* ACC, int items, cudaStream_t st,
-                       const u64* const* EXTRA, const int* PAIR) {
+                       const u64* const* EXTRA, const int* PAIR, const KsY& ky) {
     if (!items) return;
     switch (P.cfg.logn) {
-        case 10: ks_fused_logn<10>(dc, P, SRC, SRCC, src_poly, ginv, KEY, BASE, RSRC, OUT, DX, ACC, items, st, EXTRA, PAIR); break;
-        case 11: ks_fused_logn<11>(dc, P, SRC, SRCC, src_poly, ginv, KEY, BASE, RSRC, OUT, DX, ACC, items, st, EXTRA, PAIR); break;
-        case 12: ks_fused_logn<12>(dc, P, SRC, SRCC, src_poly, ginv, KEY, BASE, RSRC, OUT, DX, ACC, items, st, EXTRA, PAIR); break;
-        case 13: ks_fused_logn<13>(dc, P, SRC, SRCC, src_poly, ginv, KEY, BASE, RSRC, OUT, DX, ACC, items, st, EXTRA, PAIR); break;
-        case 14: ks_fused_logn<14>(dc, P, SRC, SRCC, src_poly, ginv, KEY, BASE, RSRC, OUT, DX, ACC, items, st, EXTRA, PAIR); break;
-        case 15: ks_fused_logn<15>(dc, P, SRC, SRCC, src_poly, ginv, KEY, BASE, RSRC, OUT, DX, ACC, items, st, EXTRA, PAIR); break;
+        case 10: ks_fused_logn<10>(dc, P, SRC, SRCC, src_poly, ginv, KEY, BASE, RSRC, OUT, DX, ACC, items, st, EXTRA, PAIR, ky); break;
+        case 11: ks_fused_logn<11>(dc, P, SRC, SRCC, src_poly, ginv, KEY, BASE, RSRC, OUT, DX, ACC, items, st, EXTRA, PAIR, ky); break;
+        case 12: ks_fused_logn<12>(dc, P, SRC, SRCC, src_poly, ginv, KEY, BASE, RSRC, OUT, DX, ACC, items, st, EXTRA, PAIR, ky); break;
+        case 13: ks_fused_logn<13>(dc, P, SRC, SRCC, src_poly, ginv, KEY, BASE, RSRC, OUT, DX, ACC, items, st, EXTRA, PAIR, ky); break;
+        case 14: ks_fused_logn<14>(dc, P, SRC, SRCC, src_poly, ginv, KEY, BASE, RSRC, OUT, DX, ACC, items, st, EXTRA, PAIR, ky); break;
+        case 15: ks_fused_logn<15>(dc, P, SRC, SRCC, src_poly, ginv, KEY, BASE, RSRC, OUT, DX, ACC, items, st, EXTRA, PAIR, ky); break;
         default: throw std::invalid_argument("key switch: unsupported logn");
     }
 }
