@@ -201,9 +201,12 @@ bool cols_use_ln4(long ctas16, bool allowed) {
 template <int LOGN, bool INV>
 static void launch_cols(const DevConsts* dc, const NttJob& job, int limbs, cudaStream_t st) {
     using G = Ntt2<LOGN>;
-    // (4-column tiles measured slower here than in K1, whose ModUp gather
-    // dominates its chain: 8.1 vs 7.7 us for a lone rotation's inverse columns)
-    if (cols_forced() == 4 && G::R2 >= 16 && G::R1 >= G::TC) {
+    // 4-column tiles for launches under a quarter wave (CSSC_COLS_SMALL4=0 keeps 8)
+    static const bool small4 = [] {
+        const char* e = std::getenv("CSSC_COLS_SMALL4");
+        return !e || std::atoi(e) != 0;
+    }();
+    if ((small4 || cols_forced() == 4) && cols_use_ln4((long)limbs * G::CTAS_C, G::R2 >= 16 && G::R1 >= G::TC)) {
         constexpr int LN = 4;
         k_ntt_cols<LOGN, INV, LN><<<limbs * (G::R2 / LN), G::TC, (LN * G::R1 + 2 * G::R1) * 8, st>>>(dc, job);
     } else if (cols_use_ln8((long)limbs * G::CTAS_C, G::R2 >= 16 && G::R1 * 4 >= G::TC)) {
