@@ -188,6 +188,19 @@ bool cols_use_ln8(long ctas16, bool allowed) {
     return 2 * ctas16 <= 3L * 148;
 }
 
+bool blocks_use_ln8(long ctas16) {
+    static const long lim = [] {
+        const char* e = std::getenv("CSSC_BLOCKS_LN8_MAX");
+        return e ? std::atol(e) : 2L * 148;
+    }();
+    static const int forced = [] {
+        const char* e = std::getenv("CSSC_BLOCKS_LN");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (forced) return forced == 8;
+    return ctas16 < lim;
+}
+
 // 4-column tiles (radix-4 passes, 4 words per thread) for launches whose
 // 8-column CTAs fill less than half a wave (a lone rotation's key switch):
 // the CTA's serial chain halves, the CTA count doubles.

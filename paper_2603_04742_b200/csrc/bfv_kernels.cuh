@@ -40,6 +40,9 @@ enum SampleDomain : u32 {
 // column-tile width policy shared by the column-phase kernels (ctas16 = CTAs at 16 columns)
 bool cols_use_ln8(long ctas16, bool allowed);
 bool cols_use_ln4(long ctas16, bool allowed);
+// block-phase kernels (K2, mask): 8-block tiles when the 16-block launch has
+// fewer than CSSC_BLOCKS_LN8_MAX CTAs (default 2 x 148); CSSC_BLOCKS_LN=8|16 forces
+bool blocks_use_ln8(long ctas16);
 void launch_ntt(const DevConsts* dc, int logn, bool inverse, const NttJob& job, int items,
                 cudaStream_t st);
 // a single phase of the two-phase NTT (cols = column phase, else block phase)

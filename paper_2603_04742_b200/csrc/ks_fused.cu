@@ -307,7 +307,7 @@ static void ks_fused_t(const DevConsts* dc, const RnsParams& P, const u64* const
     }
     KS_CHECK();
     constexpr int T2 = kKsGroups * kKsGroupThreads;
-    if (items * LK * G::CTAS_B < 2 * 148 && 8 * G::R2 >= T2)  // small launch: 8-block tiles
+    if (blocks_use_ln8((long)items * LK * G::CTAS_B) && 8 * G::R2 >= T2)  // small launch: 8-block tiles
         k_ks_blocks_inner<LOGN, LT, KT, AT, 8><<<items * LK * (G::R1 / 8), T2, smem2h, st>>>(dc, DX, KEY, ACC);
     else
         k_ks_blocks_inner<LOGN, LT, KT, AT><<<items * LK * G::CTAS_B, T2, smem2, st>>>(dc, DX, KEY, ACC);

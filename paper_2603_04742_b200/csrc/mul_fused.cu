@@ -306,7 +306,7 @@ static void maskdec_t(const DevConsts* dc, const RnsParams& P, const u64* MT, co
         cudaFuncSetAttribute(k_mask_dec_blocks<LOGN, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smemh);
         configured = true;
     }
-    if (slices * P.cfg.L * G::CTAS_B < 2 * 148 && 8 * G::R2 >= 4 * kGroupThreads)  // small: 8-block tiles
+    if (blocks_use_ln8((long)slices * P.cfg.L * G::CTAS_B) && 8 * G::R2 >= 4 * kGroupThreads)  // small: 8-block tiles
         k_mask_dec_blocks<LOGN, 8><<<slices * P.cfg.L * (G::R1 / 8), 4 * kGroupThreads, smemh, st>>>(
             dc, MT, slice_off, slice_items, item_mask, MASKS, S_NTT, D);
     else
@@ -344,7 +344,7 @@ static void maskb_t(const DevConsts* dc, const RnsParams& P, const u64* MT, cons
         cudaFuncSetAttribute(k_mask_blocks<LOGN, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smemh);
         configured = true;
     }
-    if (slices * 2 * P.cfg.L * G::CTAS_B < 2 * 148 && 8 * G::R2 >= 2 * kGroupThreads)  // small: 8-block tiles
+    if (blocks_use_ln8((long)slices * 2 * P.cfg.L * G::CTAS_B) && 8 * G::R2 >= 2 * kGroupThreads)  // small: 8-block tiles
         k_mask_blocks<LOGN, 8><<<slices * 2 * P.cfg.L * (G::R1 / 8), 2 * kGroupThreads, smemh, st>>>(
             dc, MT, slice_off, slice_items, item_mask, MASKS, OUT);
     else
