@@ -161,6 +161,8 @@ public:
     // KAT helpers
     void ntt_host(int prime_index, u64* data, int limbs, bool inverse);
     void synchronize();
+    // the side stream (an early encryption graph may run there, pipeline_speculate)
+    void synchronize_side() { cuda_check(cudaStreamSynchronize(st2_), "side stream sync"); }
 
     // building blocks reused by the batched cloud plan (pointer arrays on device)
     // enc: A and B are still to be finished from a deferred encryption (EncIn)

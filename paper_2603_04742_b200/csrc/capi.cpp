@@ -193,6 +193,8 @@ bool plan_cache_take(spmvgpu_ctx* ctx, const std::vector<std::uint64_t>& key, Pl
 }
 
 void plan_lease_free(spmvgpu_ctx* ctx, PlanLease& l) {
+    // a speculative early graph of this plan may still run on the side stream
+    if (l.plan && ctx->g) ctx->g->synchronize_side();
     if (l.plan) spmvgpu_plan_destroy(l.plan);
     l.plan = nullptr;
     if (ctx->g) {
@@ -326,6 +328,7 @@ void pipeline_speculate(spmvgpu_ctx* ctx) {
 void pipeline_prepare(spmvgpu_ctx* ctx, PlanLease& lease, const ClientImage& img) {
     auto& g = *ctx->g;
     ctx->spec_plan = nullptr;  // a re-capture invalidates an early graph already enqueued
+    g.synchronize_side();      // ... which must not run while its workspaces are replaced
     if (!lease.plan) throw std::logic_error("pipeline: no plan");
     const std::size_t out_bytes = lease.plan->plan->pipeline_out_bytes();
     if (!lease.pimg || lease.pimg_cap < img.bytes) {
@@ -360,6 +363,7 @@ void pipeline_run(spmvgpu_ctx* ctx, PlanLease& lease) {
     ctx->spec_plan = nullptr;
     lease.plan->plan->run_pipeline(early);
     ctx->g->synchronize();
+    ctx->g->synchronize_side();  // done already unless another plan's speculative graph is still running
     ctx->spec_key = lease.key;
 }
 

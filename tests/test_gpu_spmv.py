@@ -280,3 +280,23 @@ def test_large_batch_validation_on_the_host_pool(where):
     for m, v, g in zip(ms, vs, got):
         assert np.array_equal(g["values"], checker(m, v, ctx.slots, ctx.slots)["values"])
     ctx.close()
+
+
+@pytest.mark.parametrize("capacity", [1, 4])
+def test_alternating_plans_with_speculative_early_encryption(capacity):
+    """Each spmv_batch call enqueues the previous call's early encryption graph
+    before packing (pipeline_speculate).  Alternating sparsity structures makes
+    every guess wrong (the graph is re-run for the selected plan), a cache of
+    one plan evicts the guessed plan while its early graph may still run, and
+    repeats of one structure make the guess right; every result must equal the
+    reference semantics."""
+    ctx = pk.Context(logn=10, seed=5)
+    ctx.set_option("plan_cache", capacity)
+    a = pk.random_sparse_csr(200, 180, 900, 11, -8, 8)
+    b = pk.random_sparse_csr(120, 260, 700, 12, -8, 8)
+    rng = np.random.default_rng(9)
+    for m in [a, b, a, b, a, a, a, b, b, a]:
+        v = rng.integers(-8, 9, m.cols).astype(np.int64)
+        got = pk.spmv_batch(ctx, [m], [v])[0]
+        assert_same(got, checker(m, v, ctx.slots, ctx.slots))
+    ctx.close()
