@@ -40,29 +40,11 @@ METRIC = "encrypted SpMV latency (ms) & key-switch/NTT GB/s vs HBM roofline, 1xB
 
 
 def make_config(cfg: int):
-    import paper_2603_04742_b200 as pk
+    """Seeded inputs of BASELINE config `cfg` (synth.py: numpy only, so the
+    reference arm never loads the product library)."""
+    import synth
 
-    if cfg == 1:
-        ms = [pk.random_sparse_csr(256, 256, 655, 1, -8, 8)]
-        vs = [pk.random_vector(256, 1, -8, 8, nonzero=True)]
-        return dict(name="C1 256x256 uniform 1% (655 nnz)", logn=13, ms=ms, vs=vs)
-    if cfg == 2:
-        ms = [pk.random_sparse_csr(4096, 4096, 16777, 2, -8, 8)]
-        vs = [pk.random_vector(4096, 2, -8, 8, nonzero=True)]
-        return dict(name="C2 4096x4096 uniform 0.1% (16777 nnz)", logn=14, ms=ms, vs=vs)
-    if cfg == 3:
-        ms = [pk.power_law_csr(16384, 12.0, 2.0, 3, -8, 8)]
-        vs = [pk.random_vector(16384, 3, -8, 8, nonzero=True)]
-        return dict(name="C3 16384x16384 power-law Zipf(2) mean 12", logn=14, ms=ms, vs=vs)
-    if cfg == 4:
-        ms = [pk.stencil27_csr(32, 4, -8, 8)]
-        vs = [pk.random_vector(32768, 4, -8, 8, nonzero=True)]
-        return dict(name="C4 32^3 grid 27-point stencil (830584 nnz)", logn=15, ms=ms, vs=vs)
-    if cfg == 5:
-        ms = [pk.random_sparse_csr(2048, 2048, 20972, 500 + k, -8, 8) for k in range(64)]
-        vs = [pk.random_vector(2048, 500 + k, -8, 8, nonzero=True) for k in range(64)]
-        return dict(name="C5 64 x 2048x2048 uniform 0.5% (20972 nnz each)", logn=14, ms=ms, vs=vs)
-    raise ValueError(cfg)
+    return synth.config(cfg)
 
 
 def exact_values(m, v, t=65537):

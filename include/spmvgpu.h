@@ -214,20 +214,21 @@ int cssc_spmv_partitioned(spmvgpu_ctx* c, const cssc_csr* m, const int64_t* v, u
 int cssc_diag_spmv(spmvgpu_ctx* c, const cssc_csr* m, const int64_t* v, uint64_t vlen, int key_holder,
                    int64_t* values, cssc_result* res, cssc_message* msgs, uint64_t msg_cap);
 /* several independent matrices in shared launches (BASELINE config 5) */
-int cssc_spmv_batch(spmvgpu_ctx* c, const cssc_csr* ms, const int64_t* const* vs, size_t nmat,
+/* vlens[i] = length of vs[i]; != ms[i].cols raises DimensionMismatchError */
+int cssc_spmv_batch(spmvgpu_ctx* c, const cssc_csr* ms, const int64_t* const* vs, const uint64_t* vlens, size_t nmat,
                     uint64_t chunk_size, int key_holder, int64_t* const* values,
                     cssc_result* res);
 
 /* staged form for benchmarking: pack + encrypt once, run the cloud phase many
  * times from device-resident ciphertexts, then decrypt */
 typedef struct cssc_job cssc_job;
-int cssc_job_create(spmvgpu_ctx* c, const cssc_csr* ms, const int64_t* const* vs, size_t nmat,
+int cssc_job_create(spmvgpu_ctx* c, const cssc_csr* ms, const int64_t* const* vs, const uint64_t* vlens, size_t nmat,
                     uint64_t chunk_size, cssc_job** out);
 /* SURVEY 8(e) chunk split: this GPU evaluates the chunks g with g % world == rank;
  * cssc_job_result_words gives its per-slice partial results ([results][ct words],
  * zeros where it holds no chunk of a slice; words = NULL: count only), the caller
  * sums them across GPUs (mod q_j per limb), and cssc_job_finish_words decrypts */
-int cssc_job_create_shard(spmvgpu_ctx* c, const cssc_csr* ms, const int64_t* const* vs, size_t nmat,
+int cssc_job_create_shard(spmvgpu_ctx* c, const cssc_csr* ms, const int64_t* const* vs, const uint64_t* vlens, size_t nmat,
                           uint64_t chunk_size, int rank, int world, cssc_job** out);
 int cssc_job_result_words(cssc_job* j, uint64_t* words, uint64_t cap_words, uint64_t* n_results);
 int cssc_job_finish_words(cssc_job* j, const uint64_t* words, int64_t* const* values, cssc_result* res);
@@ -249,17 +250,6 @@ void cssc_job_destroy(cssc_job* j);
 int64_t cssc_pack_chunks(const cssc_csr* m, uint64_t budget, int64_t* r_list, int64_t* c_list,
                          int64_t* vflat, int64_t* cflat, int64_t* row_map, uint64_t* flat_total);
 int cssc_rotation_schedule(uint64_t rows, uint64_t cols, uint64_t* offsets, int32_t* from_acc);
-/* synthetic generators matching the reference's (synthetic.cpp:32-86) plus the
- * BASELINE config shapes */
-int64_t cssc_random_sparse_csr(uint64_t rows, uint64_t cols, uint64_t nnz, uint64_t seed,
-                               int64_t lo, int64_t hi, int64_t* rp, int64_t* ci, int64_t* va);
-void cssc_random_vector(uint64_t len, uint64_t seed, int64_t lo, int64_t hi, int64_t* out);
-void cssc_random_nonzero_vector(uint64_t len, uint64_t seed, int64_t lo, int64_t hi, int64_t* out);
-int64_t cssc_power_law_csr(uint64_t n, double mean_degree, double exponent, uint64_t seed,
-                           int64_t lo, int64_t hi, int64_t* rp, int64_t* ci, int64_t* va,
-                           uint64_t cap);
-int64_t cssc_stencil27_csr(uint64_t side, uint64_t seed, int64_t lo, int64_t hi, int64_t* rp,
-                           int64_t* ci, int64_t* va, uint64_t cap);
 
 #ifdef __cplusplus
 }

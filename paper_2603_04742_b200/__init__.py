@@ -121,11 +121,11 @@ _SIGS = {
     "cssc_diag_spmv": (C.c_int, [C.c_void_p, C.POINTER(CsrC), i64p, C.c_uint64, C.c_int, i64p,
                                  C.POINTER(ResultC), C.POINTER(Message), C.c_uint64]),
     "spmvgpu_sum": (C.c_int, [C.c_void_p, u64p, C.c_size_t, C.c_uint64]),
-    "cssc_spmv_batch": (C.c_int, [C.c_void_p, C.POINTER(CsrC), C.POINTER(i64p), C.c_size_t,
+    "cssc_spmv_batch": (C.c_int, [C.c_void_p, C.POINTER(CsrC), C.POINTER(i64p), u64p, C.c_size_t,
                                   C.c_uint64, C.c_int, C.POINTER(i64p), C.POINTER(ResultC)]),
-    "cssc_job_create": (C.c_int, [C.c_void_p, C.POINTER(CsrC), C.POINTER(i64p), C.c_size_t,
+    "cssc_job_create": (C.c_int, [C.c_void_p, C.POINTER(CsrC), C.POINTER(i64p), u64p, C.c_size_t,
                                   C.c_uint64, C.POINTER(C.c_void_p)]),
-    "cssc_job_create_shard": (C.c_int, [C.c_void_p, C.POINTER(CsrC), C.POINTER(i64p), C.c_size_t, C.c_uint64,
+    "cssc_job_create_shard": (C.c_int, [C.c_void_p, C.POINTER(CsrC), C.POINTER(i64p), u64p, C.c_size_t, C.c_uint64,
                                         C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
     "cssc_job_result_words": (C.c_int, [C.c_void_p, u64p, C.c_uint64, u64p]),
     "cssc_job_finish_words": (C.c_int, [C.c_void_p, u64p, C.POINTER(i64p), C.POINTER(ResultC)]),
@@ -140,14 +140,6 @@ _SIGS = {
     "cssc_job_destroy": (None, [C.c_void_p]),
     "cssc_pack_chunks": (C.c_int64, [C.POINTER(CsrC), C.c_uint64, i64p, i64p, i64p, i64p, i64p, u64p]),
     "cssc_rotation_schedule": (C.c_int, [C.c_uint64, C.c_uint64, u64p, i32p]),
-    "cssc_random_sparse_csr": (C.c_int64, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int64,
-                                           C.c_int64, i64p, i64p, i64p]),
-    "cssc_random_vector": (None, [C.c_uint64, C.c_uint64, C.c_int64, C.c_int64, i64p]),
-    "cssc_random_nonzero_vector": (None, [C.c_uint64, C.c_uint64, C.c_int64, C.c_int64, i64p]),
-    "cssc_power_law_csr": (C.c_int64, [C.c_uint64, C.c_double, C.c_double, C.c_uint64, C.c_int64,
-                                       C.c_int64, i64p, i64p, i64p, C.c_uint64]),
-    "cssc_stencil27_csr": (C.c_int64, [C.c_uint64, C.c_uint64, C.c_int64, C.c_int64, i64p, i64p,
-                                       i64p, C.c_uint64]),
 }
 
 _lib = None
@@ -437,29 +429,22 @@ def cloud_plan(ctx: Context, r_list, c_list, slice_ids, n_slices: int, a_cts, b_
 
 @dataclass
 class Csr:
+    """CSR matrix (reference CsrMatrix, sparse.hpp).  Every entry point also
+    accepts any object with these five attributes."""
     rows: int
     cols: int
     row_ptrs: np.ndarray
     col_indices: np.ndarray
     values: np.ndarray
-    _keep: list = field(default_factory=list, repr=False)
 
     @property
     def nnz(self) -> int:
         return int(self.row_ptrs[-1]) if self.rows else 0
 
-    def c(self) -> CsrC:
-        rp, ci, va = _i64(self.row_ptrs), _i64(self.col_indices), _i64(self.values)
-        if va.size == 0:
-            ci = va = np.zeros(1, np.int64)
-        self._keep = [rp, ci, va]
-        return CsrC(self.rows, self.cols, _p(rp, i64p), _p(ci, i64p), _p(va, i64p))
-
     def dense(self) -> np.ndarray:
         d = np.zeros((self.rows, self.cols), np.int64)
-        for i in range(self.rows):
-            for k in range(int(self.row_ptrs[i]), int(self.row_ptrs[i + 1])):
-                d[i, int(self.col_indices[k])] = int(self.values[k])
+        rows = np.repeat(np.arange(self.rows), np.diff(_i64(self.row_ptrs)))
+        d[rows, _i64(self.col_indices)[: rows.size]] = _i64(self.values)[: rows.size]
         return d
 
     @staticmethod
@@ -474,6 +459,32 @@ class Csr:
                     va.append(int(d[i, j]))
             rp.append(len(va))
         return Csr(rows, cols, _i64(rp), _i64(ci), _i64(va))
+
+
+def _csr_c(m, keep: list) -> CsrC:
+    """C view of a CSR matrix; the converted arrays are appended to `keep`,
+    which the caller holds until the C call returns."""
+    rp, ci, va = _i64(m.row_ptrs), _i64(m.col_indices), _i64(m.values)
+    if va.size == 0:
+        ci = va = np.zeros(1, np.int64)
+    keep += [rp, ci, va]
+    return CsrC(int(m.rows), int(m.cols), _p(rp, i64p), _p(ci, i64p), _p(va, i64p))
+
+
+def _vectors(ms, vs, keep: list):
+    """int64 copies of the vectors, their pointer array and lengths (the C-ABI
+    raises DimensionMismatchError on a length != cols, reference protocol.cpp:77-81)."""
+    ms, vs = list(ms), list(vs)
+    if len(ms) != len(vs):
+        raise SpmvError(-4, "DimensionMismatchError",
+                        f"spmv_batch: {len(ms)} matrices but {len(vs)} vectors")
+    vv = [_i64(v) for v in vs]
+    vv = [v if v.size else np.zeros(1, np.int64) for v in vv]
+    keep += vv
+    n = len(vv)
+    lens = np.array([np.asarray(v).size for v in vs], dtype=np.uint64)
+    keep.append(lens)
+    return (i64p * max(n, 1))(*[_p(v, i64p) for v in vv]), _p(lens, u64p) if n else None
 
 
 def _result(r: ResultC, values: np.ndarray, msgs=None) -> dict:
@@ -494,7 +505,8 @@ def spmv_partitioned(ctx: Context, m: Csr, v, chunk_size: int | None = None, key
     res = ResultC()
     cap = 5 * (m.rows // max(chunk, 1) + 2)
     msgs = (Message * cap)()
-    csr = m.c()
+    keep: list = []
+    csr = _csr_c(m, keep)
     vp = vv if vv.size else np.zeros(1, np.int64)
     check(lib().cssc_spmv_partitioned(ctx.h, C.byref(csr), _p(vp, i64p), vv.size, chunk, key_holder,
                                       _p(vals, i64p), C.byref(res), msgs, cap))
@@ -508,7 +520,8 @@ def spmv(ctx: Context, m: Csr, v, chunk_size: int | None = None, key_holder: int
     vals = np.zeros(max(m.rows, 1), np.int64)
     res = ResultC()
     msgs = (Message * 8)()
-    csr = m.c()
+    keep: list = []
+    csr = _csr_c(m, keep)
     vp = vv if vv.size else np.zeros(1, np.int64)
     check(lib().cssc_spmv(ctx.h, C.byref(csr), _p(vp, i64p), vv.size, chunk, key_holder, _p(vals, i64p),
                           C.byref(res), msgs, 8))
@@ -521,7 +534,8 @@ def diag_spmv(ctx: Context, m: Csr, v, key_holder: int = 0) -> dict:
     vals = np.zeros(max(m.rows, 1), np.int64)
     res = ResultC()
     msgs = (Message * 8)()
-    csr = m.c()
+    keep: list = []
+    csr = _csr_c(m, keep)
     vp = vv if vv.size else np.zeros(1, np.int64)
     check(lib().cssc_diag_spmv(ctx.h, C.byref(csr), _p(vp, i64p), vv.size, key_holder, _p(vals, i64p),
                                C.byref(res), msgs, 8))
@@ -531,13 +545,13 @@ def diag_spmv(ctx: Context, m: Csr, v, key_holder: int = 0) -> dict:
 def spmv_batch(ctx: Context, ms, vs, chunk_size: int | None = None, key_holder: int = 0) -> list:
     chunk = ctx.slots if chunk_size is None else chunk_size
     n = len(ms)
-    csrs = (CsrC * n)(*[m.c() for m in ms])
-    vv = [_i64(v) for v in vs]
-    vptr = (i64p * n)(*[_p(v, i64p) for v in vv])
+    keep: list = []
+    csrs = (CsrC * max(n, 1))(*[_csr_c(m, keep) for m in ms])
+    vptr, vlens = _vectors(ms, vs, keep)
     outs = [np.zeros(max(m.rows, 1), np.int64) for m in ms]
     optr = (i64p * n)(*[_p(o, i64p) for o in outs])
     res = (ResultC * n)()
-    check(lib().cssc_spmv_batch(ctx.h, csrs, vptr, n, chunk, key_holder, optr, res))
+    check(lib().cssc_spmv_batch(ctx.h, csrs, vptr, vlens, n, chunk, key_holder, optr, res))
     return [_result(res[i], outs[i][: ms[i].rows]) for i in range(n)]
 
 
@@ -548,11 +562,11 @@ class Job:
         self.ctx, self.ms = ctx, list(ms)
         chunk = ctx.slots if chunk_size is None else chunk_size
         n = len(self.ms)
-        self._csrs = (CsrC * n)(*[m.c() for m in self.ms])
-        self._vv = [_i64(v) for v in vs]
-        vptr = (i64p * n)(*[_p(v, i64p) for v in self._vv])
+        self._keep: list = []  # the job borrows these arrays until it is destroyed
+        self._csrs = (CsrC * max(n, 1))(*[_csr_c(m, self._keep) for m in self.ms])
+        vptr, vlens = _vectors(self.ms, vs, self._keep)
         h = C.c_void_p()
-        check(lib().cssc_job_create_shard(ctx.h, self._csrs, vptr, n, chunk, rank, world, C.byref(h)))
+        check(lib().cssc_job_create_shard(ctx.h, self._csrs, vptr, vlens, n, chunk, rank, world, C.byref(h)))
         self.h = h
 
     def result_words(self) -> np.ndarray:
@@ -634,52 +648,6 @@ class Job:
             pass
 
 
-# ---- generators (native, reference-identical streams) ----
-def random_sparse_csr(rows, cols, nnz, seed, lo=-100, hi=100) -> Csr:
-    rp = np.zeros(rows + 1, np.int64)
-    ci = np.zeros(max(nnz, 1), np.int64)
-    va = np.zeros(max(nnz, 1), np.int64)
-    r = lib().cssc_random_sparse_csr(rows, cols, nnz, seed, lo, hi, _p(rp, i64p), _p(ci, i64p), _p(va, i64p))
-    if r < 0:
-        check(int(r))
-    return Csr(rows, cols, rp, ci[:r], va[:r])
-
-
-def random_vector(n, seed, lo=-100, hi=100, nonzero=False) -> np.ndarray:
-    out = np.zeros(max(n, 1), np.int64)
-    f = lib().cssc_random_nonzero_vector if nonzero else lib().cssc_random_vector
-    f(n, seed, lo, hi, _p(out, i64p))
-    return out[:n]
-
-
-def _grow(call, rows):
-    cap = 1 << 16
-    while True:
-        rp = np.zeros(rows + 1, np.int64)
-        ci = np.zeros(cap, np.int64)
-        va = np.zeros(cap, np.int64)
-        r = call(rp, ci, va, cap)
-        if r >= 0:
-            return rp, ci[:r], va[:r]
-        if r <= -100:
-            cap = int(-r - 100) + 1
-            continue
-        check(int(r))
-
-
-def power_law_csr(n, mean_degree=12.0, exponent=2.0, seed=3, lo=-8, hi=8) -> Csr:
-    rp, ci, va = _grow(lambda rp, ci, va, cap: lib().cssc_power_law_csr(
-        n, mean_degree, exponent, seed, lo, hi, _p(rp, i64p), _p(ci, i64p), _p(va, i64p), cap), n)
-    return Csr(n, n, rp, ci, va)
-
-
-def stencil27_csr(side=32, seed=4, lo=-8, hi=8) -> Csr:
-    n = side ** 3
-    rp, ci, va = _grow(lambda rp, ci, va, cap: lib().cssc_stencil27_csr(
-        side, seed, lo, hi, _p(rp, i64p), _p(ci, i64p), _p(va, i64p), cap), n)
-    return Csr(n, n, rp, ci, va)
-
-
 def rotation_schedule(rows: int, cols: int):
     off = np.zeros(128, np.uint64)
     fa = np.zeros(128, np.int32)
@@ -690,7 +658,8 @@ def rotation_schedule(rows: int, cols: int):
 
 
 def pack_chunks(m: Csr, budget: int) -> dict:
-    csr = m.c()
+    keep: list = []
+    csr = _csr_c(m, keep)
     tot = C.c_uint64()
     n = lib().cssc_pack_chunks(C.byref(csr), budget, None, None, None, None, None, C.byref(tot))
     if n < 0:

@@ -19,7 +19,6 @@
 #include "host/plan_cache.hpp"
 #include "spmv/diagonal.hpp"
 #include "spmv/gpu_backend.hpp"
-#include "spmv/synthetic.hpp"
 #include "spmvgpu.h"
 
 struct spmvgpu_ctx {
@@ -127,7 +126,10 @@ std::vector<u64*> mptrs(const spmvgpu_ct* h, size_t n) {
 }
 
 // C-ABI CSR -> borrowed view (BatchedSpmv validates row pointers and columns)
-spmv::detail::CsrView view_of(const cssc_csr& m, const int64_t* v) {
+spmv::detail::CsrView view_of(const cssc_csr& m, const int64_t* v, uint64_t vlen) {
+    if (vlen != m.cols)  // reference protocol.cpp:77-81
+        throw spmv::DimensionMismatchError("spmv: vector length " + std::to_string(vlen) +
+                                           " does not match matrix column count " + std::to_string(m.cols));
     if (m.rows && (!m.row_ptrs || (m.row_ptrs[m.rows] && (!m.col_indices || !m.values))))
         throw std::invalid_argument("csr: null array");
     if (m.cols && !v) throw std::invalid_argument("null vector");
@@ -822,8 +824,8 @@ int cssc_diag_spmv(spmvgpu_ctx* c, const cssc_csr* m, const int64_t* v, uint64_t
     });
 }
 
-int cssc_spmv_batch(spmvgpu_ctx* c, const cssc_csr* ms, const int64_t* const* vs, size_t nmat, uint64_t chunk_size,
-                    int key_holder, int64_t* const* values, cssc_result* res) {
+int cssc_spmv_batch(spmvgpu_ctx* c, const cssc_csr* ms, const int64_t* const* vs, const uint64_t* vlens, size_t nmat,
+                    uint64_t chunk_size, int key_holder, int64_t* const* values, cssc_result* res) {
     return guard([&] { auto lk_ = api_lock(c);
         G(c);
         static const bool trace = std::getenv("CSSC_TRACE_E2E") != nullptr;
@@ -832,8 +834,9 @@ int cssc_spmv_batch(spmvgpu_ctx* c, const cssc_csr* ms, const int64_t* const* vs
         // host packs (used only if this call's chunk shapes select that plan)
         static const bool spec = std::getenv("CSSC_NO_EARLY_ENC") == nullptr;
         if (spec) spmv::detail::pipeline_speculate(c);
+        if (nmat && (!ms || !vs || !vlens)) throw std::invalid_argument("null argument");
         std::vector<spmv::detail::CsrView> w;
-        for (size_t i = 0; i < nmat; ++i) w.push_back(view_of(ms[i], vs[i]));
+        for (size_t i = 0; i < nmat; ++i) w.push_back(view_of(ms[i], vs[i], vlens[i]));
         spmv::detail::BatchedSpmv job(c, c->hp, w, chunk_size, static_cast<spmv::PartyRole>(key_holder));
         const auto t1 = std::chrono::steady_clock::now();
         const auto r = job.run_all();
@@ -847,22 +850,23 @@ int cssc_spmv_batch(spmvgpu_ctx* c, const cssc_csr* ms, const int64_t* const* vs
     });
 }
 
-int cssc_job_create_shard(spmvgpu_ctx* c, const cssc_csr* ms, const int64_t* const* vs, size_t nmat,
-                          uint64_t chunk_size, int rank, int world, cssc_job** out) {
+int cssc_job_create_shard(spmvgpu_ctx* c, const cssc_csr* ms, const int64_t* const* vs, const uint64_t* vlens,
+                          size_t nmat, uint64_t chunk_size, int rank, int world, cssc_job** out) {
     return guard([&] { auto lk_ = api_lock(c);
         auto j = std::make_unique<cssc_job>();
         j->ctx = c;
         G(c);
+        if (nmat && (!ms || !vs || !vlens)) throw std::invalid_argument("null argument");
         std::vector<spmv::detail::CsrView> w;
-        for (size_t i = 0; i < nmat; ++i) w.push_back(view_of(ms[i], vs[i]));
+        for (size_t i = 0; i < nmat; ++i) w.push_back(view_of(ms[i], vs[i], vlens[i]));
         j->job = std::make_unique<spmv::detail::BatchedSpmv>(c, c->hp, w, chunk_size, spmv::PartyRole::ClientA,
                                                              true, rank, world);
         *out = j.release();
     });
 }
-int cssc_job_create(spmvgpu_ctx* c, const cssc_csr* ms, const int64_t* const* vs, size_t nmat,
+int cssc_job_create(spmvgpu_ctx* c, const cssc_csr* ms, const int64_t* const* vs, const uint64_t* vlens, size_t nmat,
                     uint64_t chunk_size, cssc_job** out) {
-    return cssc_job_create_shard(c, ms, vs, nmat, chunk_size, 0, 1, out);
+    return cssc_job_create_shard(c, ms, vs, vlens, nmat, chunk_size, 0, 1, out);
 }
 int cssc_job_result_words(cssc_job* j, uint64_t* words, uint64_t cap_words, uint64_t* n_results) {
     return guard([&] { auto lk_ = api_lock(j ? j->ctx : nullptr);
@@ -960,43 +964,6 @@ int cssc_rotation_schedule(uint64_t rows, uint64_t cols, uint64_t* offsets, int3
         n = (int)s.size();
     });
     return st == SPMVGPU_OK ? n : st;
-}
-
-static int64_t export_csr(const spmv::CsrMatrix& m, int64_t* rp, int64_t* ci, int64_t* va, uint64_t cap) {
-    if (m.nnz() > cap) return -(int64_t)m.nnz() - 100;  // caller retries with a larger buffer
-    for (size_t i = 0; i <= m.rows; ++i) rp[i] = (int64_t)m.row_ptrs[i];
-    for (size_t k = 0; k < m.nnz(); ++k) {
-        ci[k] = (int64_t)m.col_indices[k];
-        va[k] = m.values[k];
-    }
-    return (int64_t)m.nnz();
-}
-
-int64_t cssc_random_sparse_csr(uint64_t rows, uint64_t cols, uint64_t nnz, uint64_t seed, int64_t lo, int64_t hi,
-                               int64_t* rp, int64_t* ci, int64_t* va) {
-    int64_t r = 0;
-    const int st = guard([&] { r = export_csr(spmv::random_sparse_csr(rows, cols, nnz, seed, lo, hi), rp, ci, va, nnz); });
-    return st == SPMVGPU_OK ? r : st;
-}
-void cssc_random_vector(uint64_t len, uint64_t seed, int64_t lo, int64_t hi, int64_t* out) {
-    const auto v = spmv::random_vector(len, seed, lo, hi);
-    std::memcpy(out, v.data(), sizeof(int64_t) * len);
-}
-void cssc_random_nonzero_vector(uint64_t len, uint64_t seed, int64_t lo, int64_t hi, int64_t* out) {
-    const auto v = spmv::random_nonzero_vector(len, seed, lo, hi);
-    std::memcpy(out, v.data(), sizeof(int64_t) * len);
-}
-int64_t cssc_power_law_csr(uint64_t n, double mean_degree, double exponent, uint64_t seed, int64_t lo, int64_t hi,
-                           int64_t* rp, int64_t* ci, int64_t* va, uint64_t cap) {
-    int64_t r = 0;
-    const int st = guard([&] { r = export_csr(spmv::power_law_csr(n, mean_degree, exponent, seed, lo, hi), rp, ci, va, cap); });
-    return st == SPMVGPU_OK ? r : st;
-}
-int64_t cssc_stencil27_csr(uint64_t side, uint64_t seed, int64_t lo, int64_t hi, int64_t* rp, int64_t* ci,
-                           int64_t* va, uint64_t cap) {
-    int64_t r = 0;
-    const int st = guard([&] { r = export_csr(spmv::stencil27_csr(side, seed, lo, hi), rp, ci, va, cap); });
-    return st == SPMVGPU_OK ? r : st;
 }
 
 }  // extern "C"

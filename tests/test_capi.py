@@ -10,6 +10,7 @@ import numpy as np
 import pytest
 
 import paper_2603_04742_b200 as pk
+import synth
 from oracle_bindings import BfvOracle, _i64, _p, i64p, ip, ref_lib, sim_spmv_partitioned, u64p
 
 ROOT = Path(__file__).resolve().parent.parent
@@ -52,23 +53,41 @@ def test_default_params_and_security_budget():
 @pytest.mark.skipif(ref_lib() is None, reason="reference library not built")
 def test_generators_match_reference():
     L = ref_lib()
-    for rows, cols, nnz, seed in ((256, 256, 655, 1), (4096, 4096, 16777, 2), (30, 40, 700, 9), (5, 5, 20, 3)):
-        m = pk.random_sparse_csr(rows, cols, nnz, seed, -8, 8)
+    for rows, cols, nnz, seed in ((256, 256, 655, 1), (4096, 4096, 16777, 2), (2048, 2048, 20972, 500),
+                                  (2048, 2048, 20972, 563), (30, 40, 700, 9), (5, 5, 20, 3), (7, 9, 0, 4)):
+        m = synth.random_sparse_csr(rows, cols, nnz, seed, -8, 8)
         rp = np.zeros(rows + 1, np.int64)
-        ci = np.zeros(nnz, np.int64)
-        va = np.zeros(nnz, np.int64)
+        ci = np.zeros(max(nnz, 1), np.int64)
+        va = np.zeros(max(nnz, 1), np.int64)
         assert L.ref_random_sparse_csr(rows, cols, nnz, seed, -8, 8, _p(rp, i64p), _p(ci, i64p), _p(va, i64p)) == nnz
-        assert np.array_equal(m.row_ptrs, rp) and np.array_equal(m.col_indices, ci) and np.array_equal(m.values, va)
+        assert np.array_equal(m.row_ptrs, rp) and np.array_equal(m.col_indices, ci[:nnz])
+        assert np.array_equal(m.values, va[:nnz])
     out = np.zeros(100, np.int64)
     L.ref_random_vector(100, 5, -8, 8, _p(out, i64p))
-    assert np.array_equal(pk.random_vector(100, 5, -8, 8), out)
+    assert np.array_equal(synth.random_vector(100, 5, -8, 8), out)
+
+
+def test_product_carries_no_generator():
+    """Input generation is bench/test data (synth.py), not part of the library."""
+    nm = __import__("subprocess").run(["nm", "-D", "--defined-only", str(pk.LIB_PATH)], capture_output=True,
+                                      text=True).stdout
+    for bad in ("random_sparse_csr", "random_vector", "power_law", "stencil27", "mt19937"):
+        assert bad not in nm, bad
+    assert "import synth" not in (ROOT / "paper_2603_04742_b200" / "__init__.py").read_text()
+
+
+def test_batch_vector_count_mismatch_raises():
+    m = synth.random_sparse_csr(6, 5, 10, 1, -8, 8)
+    with pytest.raises(pk.SpmvError) as e:
+        pk._vectors([m, m], [np.ones(5)], [])
+    assert e.value.kind == "DimensionMismatchError"
 
 
 def test_config_generators_shapes():
-    assert pk.stencil27_csr(32, 4).nnz == 830584  # 94^3, boundary-truncated 27-point stencil
-    p = pk.power_law_csr(16384, 12.0, 2.0, 3)
+    assert synth.stencil27_csr(32, 4).nnz == 830584  # 94^3, boundary-truncated 27-point stencil
+    p = synth.power_law_csr(16384, 12.0, 2.0, 3)
     assert 150_000 < p.nnz < 250_000
-    v = pk.random_vector(1000, 3, -8, 8, nonzero=True)
+    v = synth.random_vector(1000, 3, -8, 8, nonzero=True)
     assert (v != 0).all() and v.min() >= -8 and v.max() <= 8
 
 
@@ -98,7 +117,7 @@ def ref_chunks(m, budget):
                                    (8, 8, 64, 4, 8), (100, 3, 150, 5, 128)])
 def test_pack_matches_reference(shape):
     rows, cols, nnz, seed, budget = shape
-    m = pk.random_sparse_csr(rows, cols, nnz, seed, -8, 8)
+    m = synth.random_sparse_csr(rows, cols, nnz, seed, -8, 8)
     got = pk.pack_chunks(m, budget)
     want = ref_chunks(m, budget)
     for k in ("r", "c", "vflat", "cflat", "row_map"):
@@ -107,7 +126,7 @@ def test_pack_matches_reference(shape):
 
 def test_pack_large_configs_consistent():
     """C3 (power law, 2 slices) and C4 (stencil) pack invariants at full size."""
-    for m, S in ((pk.power_law_csr(16384, 12.0, 2.0, 3), 8192), (pk.stencil27_csr(32, 4), 16384)):
+    for m, S in ((synth.power_law_csr(16384, 12.0, 2.0, 3), 8192), (synth.stencil27_csr(32, 4), 16384)):
         for r0 in range(0, m.rows, S):
             r1 = min(m.rows, r0 + S)
             b, e = int(m.row_ptrs[r0]), int(m.row_ptrs[r1])

@@ -9,6 +9,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 import paper_2603_04742_b200 as pk
+import synth
 from paper_2603_04742_b200 import shard
 
 
@@ -19,8 +20,8 @@ def _worker(rank, world, port, q):
     sys.path.insert(0, os.path.dirname(__file__))
     from oracle_bindings import sim_spmv_partitioned
 
-    ms = [pk.random_sparse_csr(64, 64, 200, s, -8, 8) for s in range(500, 507)]
-    vs = [pk.random_vector(64, s, -8, 8, nonzero=True) for s in range(500, 507)]
+    ms = [synth.random_sparse_csr(64, 64, 200, s, -8, 8) for s in range(500, 507)]
+    vs = [synth.random_vector(64, s, -8, 8, nonzero=True) for s in range(500, 507)]
     mine = shard.units_for_rank(len(ms), rank, world)
     local = {i: sim_spmv_partitioned(ms[i], vs[i], 64, 64)["values"] for i in mine}
     full = shard.gather_values(local, len(ms), [m.rows for m in ms])
@@ -44,8 +45,8 @@ def test_sharded_batch_gathers_in_order():
     sys.path.insert(0, os.path.dirname(__file__))
     from oracle_bindings import sim_spmv_partitioned
     for i, s in enumerate(range(500, 507)):
-        m = pk.random_sparse_csr(64, 64, 200, s, -8, 8)
-        v = pk.random_vector(64, s, -8, 8, nonzero=True)
+        m = synth.random_sparse_csr(64, 64, 200, s, -8, 8)
+        v = synth.random_vector(64, s, -8, 8, nonzero=True)
         assert got[i] == sim_spmv_partitioned(m, v, 64, 64)["values"].tolist()
 
 

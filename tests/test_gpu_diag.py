@@ -5,6 +5,7 @@ import numpy as np
 import pytest
 
 import paper_2603_04742_b200 as pk
+import synth
 from oracle_bindings import diag_reference
 
 pytestmark = pytest.mark.gpu
@@ -23,8 +24,8 @@ def exact(m, v, t=65537):
 
 @pytest.mark.parametrize("n,nnz,seed", [(8, 20, 1), (64, 300, 2), (512, 2000, 3), (1024, 1500, 4), (500, 9000, 5)])
 def test_diag_matches_reference(ctx11, n, nnz, seed):
-    m = pk.random_sparse_csr(n, n, nnz, seed, -8, 8)
-    v = pk.random_vector(n, seed, -8, 8, nonzero=True)
+    m = synth.random_sparse_csr(n, n, nnz, seed, -8, 8)
+    v = synth.random_vector(n, seed, -8, 8, nonzero=True)
     got = pk.diag_spmv(ctx11, m, v)
     want = diag_reference(m, v, ctx11.slots)
     assert np.array_equal(got["values"], want["values"])
@@ -39,13 +40,13 @@ def test_diag_edge_cases(ctx11):
     z = pk.Csr.from_dense([[0, 0], [0, 0]])
     r = pk.diag_spmv(ctx11, z, [1, 2])
     assert list(r["values"]) == [0, 0] and r["n_ct"] == 0 and r["noise"] == 146
-    full = pk.random_sparse_csr(S, S, 3 * S, 9, -8, 8)  # n == slot_count: natural wrap
-    v = pk.random_vector(S, 9, -8, 8, nonzero=True)
+    full = synth.random_sparse_csr(S, S, 3 * S, 9, -8, 8)  # n == slot_count: natural wrap
+    v = synth.random_vector(S, 9, -8, 8, nonzero=True)
     assert np.array_equal(pk.diag_spmv(ctx11, full, v)["values"], exact(full, v))
     with pytest.raises(pk.SpmvError) as e:  # non-square
         pk.diag_spmv(ctx11, pk.Csr.from_dense([[1, 2, 3], [4, 5, 6]]), [1, 2, 3])
     assert e.value.kind == "NonSquareError"
-    m = pk.random_sparse_csr(S // 2 + 1, S // 2 + 1, 10, 1, -8, 8)
+    m = synth.random_sparse_csr(S // 2 + 1, S // 2 + 1, 10, 1, -8, 8)
     with pytest.raises(pk.SpmvError) as e:  # S/2 < n < S
         pk.diag_spmv(ctx11, m, np.ones(S // 2 + 1, np.int64))
     assert e.value.kind == "OverLengthError"

@@ -6,6 +6,7 @@ import numpy as np
 import pytest
 
 import paper_2603_04742_b200 as pk
+import synth
 
 pytestmark = pytest.mark.gpu
 T = 65537
@@ -43,8 +44,8 @@ def test_device_pack_equals_reference_chunks(ctx, seed):
     rng = np.random.default_rng(seed)
     rows, ncols = int(rng.integers(20, 300)), int(rng.integers(20, 300))
     nnz = int(rng.integers(1, rows * 4))
-    m = pk.random_sparse_csr(rows, ncols, min(nnz, rows * ncols), seed, -9, 9)
-    v = pk.random_vector(ncols, seed, -9, 9)
+    m = synth.random_sparse_csr(rows, ncols, min(nnz, rows * ncols), seed, -9, 9)
+    v = synth.random_vector(ncols, seed, -9, 9)
     budget = ctx.slots if seed % 2 else max(int(np.diff(m.row_ptrs).astype(bool).sum()), 64)
     ref = pk.pack_chunks(m, budget)
     rows_d, slices_d, cols_d, r_list, c_list = descriptors(m, budget)
@@ -68,8 +69,8 @@ def test_device_pack_equals_reference_chunks(ctx, seed):
 
 
 def test_device_pack_rejects_bad_descriptors(ctx):
-    m = pk.random_sparse_csr(30, 30, 90, 5, -9, 9)
-    v = pk.random_vector(30, 5, -9, 9)
+    m = synth.random_sparse_csr(30, 30, 90, 5, -9, 9)
+    v = synth.random_vector(30, 5, -9, 9)
     rows_d, slices_d, cols_d, r_list, _ = descriptors(m, ctx.slots)
     n = len(r_list)
     bad = rows_d.copy()
@@ -96,8 +97,8 @@ def test_forked_encryption_gives_the_staged_words(logn, seed):
     contexts with the same seed hand out the same stream ids."""
     a, b = pk.Context(logn=logn, seed=4), pk.Context(logn=logn, seed=4)
     b.set_option("forked_encrypt", 1)
-    m = pk.random_sparse_csr(200, 150, 900, seed, -8, 8)
-    v = pk.random_vector(150, seed, -8, 8)
+    m = synth.random_sparse_csr(200, 150, 900, seed, -8, 8)
+    v = synth.random_vector(150, seed, -8, 8)
     rows_d, slices_d, cols_d, r_list, _ = descriptors(m, a.slots)
     n = len(r_list)
     ca = a.encrypt_cssc(m.col_indices, m.values, v, rows_d, slices_d, cols_d, n)

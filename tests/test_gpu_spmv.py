@@ -7,6 +7,7 @@ import numpy as np
 import pytest
 
 import paper_2603_04742_b200 as pk
+import synth
 from oracle_bindings import ref_lib, sim_spmv_partitioned
 
 pytestmark = pytest.mark.gpu
@@ -40,8 +41,8 @@ def assert_same(got, want):
 def test_random_small_instances(ctx10, seed):
     rows, cols = 1 + seed % 17, 1 + (seed * 3) % 19
     nnz = (rows * cols) // (1 + seed % 3)
-    m = pk.random_sparse_csr(rows, cols, nnz, seed)
-    v = pk.random_vector(cols, seed)
+    m = synth.random_sparse_csr(rows, cols, nnz, seed)
+    v = synth.random_vector(cols, seed)
     got = pk.spmv_partitioned(ctx10, m, v, ctx10.slots)
     assert_same(got, checker(m, v, ctx10.slots, ctx10.slots))
     assert got["measured_noise"] > 0 or got["n_ct"] == 0
@@ -50,8 +51,8 @@ def test_random_small_instances(ctx10, seed):
 @pytest.mark.parametrize("seed", range(1200, 1206))
 def test_partitioned_small_budget(ctx10, seed):
     rows, cols = 8 + seed % 70, 1 + (seed * 3) % 12
-    m = pk.random_sparse_csr(rows, cols, rows * cols // 4, seed)
-    v = pk.random_vector(cols, seed)
+    m = synth.random_sparse_csr(rows, cols, rows * cols // 4, seed)
+    v = synth.random_vector(cols, seed)
     got = pk.spmv_partitioned(ctx10, m, v, 8)
     assert_same(got, checker(m, v, ctx10.slots, 8))
 
@@ -78,8 +79,8 @@ def test_edge_cases(ctx10):
 
 def test_config1_matches_reference(ctx13):
     """BASELINE config 1: 256x256, 1% density, values in [-8,8]\\{0}, N=8192."""
-    m = pk.random_sparse_csr(256, 256, 655, 1, -8, 8)
-    v = pk.random_vector(256, 1, -8, 8, nonzero=True)
+    m = synth.random_sparse_csr(256, 256, 655, 1, -8, 8)
+    v = synth.random_vector(256, 1, -8, 8, nonzero=True)
     got = pk.spmv_partitioned(ctx13, m, v)
     want = checker(m, v, ctx13.slots, ctx13.slots)
     assert_same(got, want)
@@ -90,8 +91,8 @@ def test_config1_matches_reference(ctx13):
 
 
 def test_batch_equals_individual_runs(ctx10):
-    ms = [pk.random_sparse_csr(40, 40, 120, s, -8, 8) for s in range(500, 506)]
-    vs = [pk.random_vector(40, s, -8, 8, nonzero=True) for s in range(500, 506)]
+    ms = [synth.random_sparse_csr(40, 40, 120, s, -8, 8) for s in range(500, 506)]
+    vs = [synth.random_vector(40, s, -8, 8, nonzero=True) for s in range(500, 506)]
     batch = pk.spmv_batch(ctx10, ms, vs, 32)
     for m, v, b in zip(ms, vs, batch):
         want = checker(m, v, ctx10.slots, 32)
@@ -100,8 +101,8 @@ def test_batch_equals_individual_runs(ctx10):
 
 
 def test_job_graph_replay(ctx10):
-    ms = [pk.random_sparse_csr(60, 50, 300, s, -8, 8) for s in range(7, 10)]
-    vs = [pk.random_vector(50, s, -8, 8, nonzero=True) for s in range(7, 10)]
+    ms = [synth.random_sparse_csr(60, 50, 300, s, -8, 8) for s in range(7, 10)]
+    vs = [synth.random_vector(50, s, -8, 8, nonzero=True) for s in range(7, 10)]
     job = pk.Job(ctx10, ms, vs)
     job.encrypt()
     for _ in range(3):
@@ -128,7 +129,7 @@ def test_plan_cache_reuse_with_new_values(capacity):
     ctx = pk.Context(logn=10, seed=5)
     ctx.set_option("plan_cache", capacity)
     rng = np.random.default_rng(capacity)
-    shapes = [pk.random_sparse_csr(70, 60, 400, 31, -8, 8), pk.random_sparse_csr(50, 90, 200, 32, -8, 8)]
+    shapes = [synth.random_sparse_csr(70, 60, 400, 31, -8, 8), synth.random_sparse_csr(50, 90, 200, 32, -8, 8)]
     for it in range(6):
         base = shapes[it % 2] if it < 4 else shapes[0]
         vals = rng.integers(1, 9, base.values.size) * rng.choice([-1, 1], base.values.size)
@@ -162,8 +163,8 @@ def test_chunk_split_shards_sum_to_the_full_result(world):
     here one after another on one GPU); the summed partial results, folded mod
     q, decrypt to the reference's values, ledger, transcript and noise."""
     ctx = pk.Context(logn=10, seed=8)
-    m = pk.random_sparse_csr(1300, 700, 6000, 77, -8, 8)  # 3 slices of 512 rows, several chunks each
-    v = pk.random_vector(700, 77, -8, 8, nonzero=True)
+    m = synth.random_sparse_csr(1300, 700, 6000, 77, -8, 8)  # 3 slices of 512 rows, several chunks each
+    v = synth.random_vector(700, 77, -8, 8, nonzero=True)
     from paper_2603_04742_b200 import shard
     total = None
     jobs = []
@@ -192,7 +193,7 @@ def test_context_shared_across_host_threads():
     from concurrent.futures import ThreadPoolExecutor
 
     ctx = pk.Context(logn=10, seed=12)
-    cases = [(pk.random_sparse_csr(90, 70, 500, s, -8, 8), pk.random_vector(70, s, -8, 8, nonzero=True))
+    cases = [(synth.random_sparse_csr(90, 70, 500, s, -8, 8), synth.random_vector(70, s, -8, 8, nonzero=True))
              for s in range(40, 52)]
 
     def run(i):
@@ -210,8 +211,8 @@ def test_context_shared_across_host_threads():
 def test_plain_spmv_is_one_slice(ctx10):
     """spmv (protocol.cpp:74-153): one slice; equals spmv_partitioned when the
     rows fit one chunk budget, ColumnTooTallError when a column does not."""
-    m = pk.random_sparse_csr(300, 80, 900, 61, -8, 8)
-    v = pk.random_vector(80, 61, -8, 8, nonzero=True)
+    m = synth.random_sparse_csr(300, 80, 900, 61, -8, 8)
+    v = synth.random_vector(80, 61, -8, 8, nonzero=True)
     got = pk.spmv(ctx10, m, v)
     assert_same(got, checker(m, v, ctx10.slots, ctx10.slots))
     with pytest.raises(pk.SpmvError) as e:
@@ -224,7 +225,7 @@ def test_job_run_uses_the_pipeline_and_compact_download():
     over one chunk-shape structure it is the cached graph, whose download holds
     only each slice's first max-height slots (u32) and the deviations."""
     ctx = pk.Context(logn=12, seed=8)
-    base = pk.random_sparse_csr(300, 250, 1800, 77, -8, 8)
+    base = synth.random_sparse_csr(300, 250, 1800, 77, -8, 8)
     rng = np.random.default_rng(3)
     for it in range(3):
         vals = (rng.integers(1, 9, base.values.size) * rng.choice([-1, 1], base.values.size)).astype(np.int64)
@@ -250,7 +251,7 @@ def test_pipeline_over_ring_sizes_and_chunk_depths(logn, fused):
     different tree depths make the plan reorder its items."""
     ctx = pk.Context(logn=logn, seed=8)
     ctx.set_option("fused_key_switch", fused)
-    base = pk.random_sparse_csr(300, 250, 1800, 77, -8, 8)
+    base = synth.random_sparse_csr(300, 250, 1800, 77, -8, 8)
     rng = np.random.default_rng(3)
     for _ in range(3):
         vals = (rng.integers(1, 9, base.values.size) * rng.choice([-1, 1], base.values.size)).astype(np.int64)
@@ -267,8 +268,8 @@ def test_large_batch_validation_on_the_host_pool(where):
     column index anywhere is still reported as the sequential check reports it,
     and a valid large batch evaluates exactly."""
     ctx = pk.Context(logn=13, seed=2)
-    ms = [pk.random_sparse_csr(2048, 2048, 70000, 100 + i, -8, 8) for i in range(4)]
-    vs = [pk.random_vector(2048, 100 + i, -8, 8, nonzero=True) for i in range(4)]
+    ms = [synth.random_sparse_csr(2048, 2048, 70000, 100 + i, -8, 8) for i in range(4)]
+    vs = [synth.random_vector(2048, 100 + i, -8, 8, nonzero=True) for i in range(4)]
     k = {"first": 0, "middle": 35000, "last": 69999}[where]
     bad = ms[2].col_indices.copy()
     bad[k] = 2048 + 5
@@ -292,8 +293,8 @@ def test_alternating_plans_with_speculative_early_encryption(capacity):
     reference semantics."""
     ctx = pk.Context(logn=10, seed=5)
     ctx.set_option("plan_cache", capacity)
-    a = pk.random_sparse_csr(200, 180, 900, 11, -8, 8)
-    b = pk.random_sparse_csr(120, 260, 700, 12, -8, 8)
+    a = synth.random_sparse_csr(200, 180, 900, 11, -8, 8)
+    b = synth.random_sparse_csr(120, 260, 700, 12, -8, 8)
     rng = np.random.default_rng(9)
     for m in [a, b, a, b, a, a, a, b, b, a]:
         v = rng.integers(-8, 9, m.cols).astype(np.int64)

@@ -7,6 +7,7 @@ import pytest
 
 from oracle_bindings import BfvOracle, oracle_lib, sim_spmv_partitioned, _u64, _i64
 import paper_2603_04742_b200 as pk
+import synth
 
 T = 65537
 
@@ -107,8 +108,8 @@ def test_bfv_protocol_decrypts_to_reference():
     orc = BfvOracle(7, 3, 1, 1, 54, 54, T, 5)
     S = 64
     for seed in (11, 12):
-        m = pk.random_sparse_csr(20, 24, 90, seed, -8, 8)
-        v = pk.random_vector(24, seed, -8, 8)
+        m = synth.random_sparse_csr(20, 24, 90, seed, -8, 8)
+        v = synth.random_vector(24, seed, -8, 8)
         want = sim_spmv_partitioned(m, v, S, S)
         pc = pk.pack_chunks(m, S)
         res = None

@@ -9,6 +9,7 @@ import numpy as np
 import pytest
 
 import paper_2603_04742_b200 as pk
+import synth
 from oracle_bindings import _i64, _p, _u64, i64p, ip, oracle_lib, sim_spmv_partitioned, u64p
 
 GOLDEN = json.loads((Path(__file__).parent / "golden" / "ref_cases.json").read_text())["cases"]
@@ -126,8 +127,8 @@ def test_protocol_golden_small():  # test_protocol.cpp:28-70, 138-167
     assert list(r["values"]) == [0, 21, 0]
     z = sim_spmv_partitioned(pk.Csr.from_dense([[0, 0], [0, 0]]), [3, 9], 32)
     assert list(z["values"]) == [0, 0] and z["n_ct"] == 0 and z["noise"] == 146
-    m = pk.random_sparse_csr(6, 7, 20, 77)
-    r = sim_spmv_partitioned(m, pk.random_vector(7, 77), 64, 16)
+    m = synth.random_sparse_csr(6, 7, 20, 77)
+    r = sim_spmv_partitioned(m, synth.random_vector(7, 77), 64, 16)
     kinds = [x[2] for x in r["messages"]]
     assert kinds == [0, 1, 2, 0, 3]
     assert r["messages"][0][3] == round(r["n_ct"] * 0.52 * 1048576)  # protocol.cpp:51-54
