@@ -1,22 +1,35 @@
 #!/usr/bin/env python
 """Encrypted CSSC SpMV benchmark (B200, sm_100a RNS-BFV).
 
-One "step" = the cloud phase of one encrypted SpMV workload (BASELINE.json
-config; default config 2 = configs[1], 4096x4096 at 0.1%): batched ct x ct
-multiply + relinearisation, the rotate-and-add trees, and the masked per-slice
-accumulation, from device-resident input ciphertexts to result ciphertexts.
-  value  : ms per step on the device (CUDA events, L2 flushed before every step)
-  e2e    : the same workload through the public API (spmv_batch: host CSR +
-           vector in, decrypted values out; pack, H2D, encrypt, cloud,
-           decrypt, D2H all inside the timed region)
-  roofline: the dominant kernel (batched NTT) against the measured integer
-           butterfly peak, plus its HBM fraction of MEASURED_PEAKS.json
-  cpu_baseline: the unmodified reference (oracle/_ref, SimBackend) on 1 host core
+One "step" = the cloud phase of one encrypted SpMV workload of a BASELINE.json
+config (default config 5 = configs[4], the largest single-GPU workload: 64
+independent 2048x2048 matrices, 256 chunks, 712 rotations): batched ct x ct
+multiply + relinearisation, the rotate-and-add trees and the masked per-slice
+accumulation, from device-resident input ciphertexts to result ciphertexts
+(reference protocol.cpp:121-134 for every row slice).
+  value   : ms per step on the device (CUDA events on the context stream, L2
+            flushed before every step by a 256 MiB write)
+  e2e     : the same workload through the public API, party-separated
+            (spmv_batch: host CSR + vectors in, decrypted values out; client
+            pack + encryption write real input ciphertexts, the cloud writes
+            the result ciphertexts, the key holder decrypts them; host->device
+            and device->host copies inside the timed region)
+  roofline: the dominant kernel launch of the step (per-kernel CUDA-event
+            profile of the plan graph) against the register-resident butterfly
+            peak measured in the same run; its DRAM traffic from the committed
+            ncu capture of the same launch
+  configs : C1..C5 each with cloud / e2e times, per-kernel table, key-switch
+            groups, the reference CPU path (cloud section and whole
+            spmv_partitioned, 1 core) and the CPU RNS-BFV oracle (bounded
+            sample, 1 thread and all threads)
 
-Multi-GPU (torchrun): every rank runs its own replica of the workload (weak
-scaling, no data-path collective); ms_per_step is the max over ranks and
-value = ms_per_step / world_size (amortised latency per workload).
-`--impl reference` times the reference's own CPU path instead.
+Multi-GPU (torchrun): config 5's matrices go round-robin to the ranks (no
+data-path collective, `scaling` strong: the 64-matrix workload is fixed); a
+single-matrix config splits its chunks over the ranks and sums the partial
+result ciphertexts with one NCCL all-reduce on the device.
+`--impl reference` times the reference's own CPU path (oracle/_ref, the
+unmodified reference library) on all host threads; it never loads the
+product library.
 """
 from __future__ import annotations
 
@@ -36,7 +49,8 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-METRIC = "encrypted SpMV latency (ms) & key-switch/NTT GB/s vs HBM roofline, 1xB200"
+METRIC = "encrypted SpMV latency (ms) & key-switch/NTT GB/s vs HBM roofline, 1×B200"
+T_MOD = 65537
 
 
 def make_config(cfg: int):
@@ -47,14 +61,19 @@ def make_config(cfg: int):
     return synth.config(cfg)
 
 
-def exact_values(m, v, t=65537):
+def exact_values(m, v, t=T_MOD):
     """Plain matvec reduced to the centred residues the decryptor reports."""
-    rp, ci, va = m.row_ptrs, m.col_indices, m.values
+    rp, ci, va = np.asarray(m.row_ptrs), np.asarray(m.col_indices), np.asarray(m.values)
     rows = np.repeat(np.arange(m.rows), np.diff(rp))
     acc = np.zeros(m.rows, np.int64)
-    np.add.at(acc, rows, va * v[ci])
+    np.add.at(acc, rows, va * np.asarray(v)[ci])
     r = np.mod(acc, t)
     return np.where(r > t // 2, r - t, r)
+
+
+def peaks():
+    f = ROOT / "MEASURED_PEAKS.json"
+    return json.loads(f.read_text()) if f.exists() else {}
 
 
 class ClockSampler:
@@ -98,142 +117,478 @@ class ClockSampler:
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
 
 
-def cpu_reference_time(ms, vs, slot_count, budget_s=3.0):
-    """The unmodified reference SimBackend spmv_partitioned on 1 host core
-    (oracle/_ref); best-of-reps wall time of one whole workload, ms."""
+# ----------------------------------------------------------------------------
+# CPU baselines (test-side checkers under oracle/, never the thing measured)
+# ----------------------------------------------------------------------------
+def _oracle():
     sys.path.insert(0, str(ROOT / "tests"))
-    from oracle_bindings import ref_lib, _i64, _p, i64p
+    import oracle_bindings
 
-    L = ref_lib()
-    if L is None:
-        return None
-    keep = []
+    return oracle_bindings
 
-    def one():
-        tot = 0.0
-        for m, v in zip(ms, vs):
-            rp, ci, va, vv = _i64(m.row_ptrs), _i64(m.col_indices), _i64(m.values), _i64(v)
-            keep.append((rp, ci, va, vv))
-            tot += L.ref_time_spmv_partitioned(slot_count, 65537, m.rows, m.cols, _p(rp, i64p), _p(ci, i64p),
-                                               _p(va, i64p), _p(vv, i64p), slot_count, 1)
+
+class RefWorkload:
+    """The unmodified reference (oracle/_ref) on one config: the cloud section
+    (protocol.cpp:121-134 on the prepared client ciphertexts of every slice) and
+    the whole spmv_partitioned (protocol.cpp:155-176), SimBackend with
+    slot_count = chunk_size = S = N/2."""
+
+    def __init__(self, cfg):
+        ob = _oracle()
+        self.L = ob.ref_lib()
+        if self.L is None:
+            raise RuntimeError("oracle/_ref/libspmv_ref.so not built")
+        self.S = 1 << (cfg["logn"] - 1)
+        self.ms = cfg["ms"]
+        self.arrays = []
+        for m, v in zip(cfg["ms"], cfg["vs"]):
+            rp, ci, va, vv = (ob._i64(x) for x in (m.row_ptrs, m.col_indices, m.values, v))
+            if va.size == 0:
+                ci = va = np.zeros(1, np.int64)
+            self.arrays.append((rp, ci, va, vv))
+        self.ob = ob
+        self.handles = None
+
+    def prepare_cloud(self):
+        ob, L = self.ob, self.L
+        self.handles = []
+        for m, (rp, ci, va, vv) in zip(self.ms, self.arrays):
+            h = L.ref_cloud_prepare(self.S, T_MOD, m.rows, m.cols, ob._p(rp, ob.i64p), ob._p(ci, ob.i64p),
+                                    ob._p(va, ob.i64p), ob._p(vv, ob.i64p), self.S)
+            if not h:
+                raise RuntimeError("ref_cloud_prepare: " + L.ref_last_error().decode())
+            self.handles.append(h)
+
+    def cloud(self, idx) -> float:
+        return sum(self.L.ref_cloud_run(self.handles[i]) for i in idx)
+
+    def full(self, idx) -> float:
+        ob, tot = self.ob, 0.0
+        for i in idx:
+            m, (rp, ci, va, vv) = self.ms[i], self.arrays[i]
+            tot += self.L.ref_time_spmv_partitioned(self.S, T_MOD, m.rows, m.cols, ob._p(rp, ob.i64p),
+                                                    ob._p(ci, ob.i64p), ob._p(va, ob.i64p), ob._p(vv, ob.i64p),
+                                                    self.S, 1)
         return tot
 
-    first = one()
+    def close(self):
+        for h in self.handles or []:
+            self.L.ref_cloud_free(h)
+        self.handles = None
+
+
+def _best_of(fn, budget_s):
+    first = fn()
     reps = max(1, min(200, int(budget_s * 1e3 / max(first, 1e-3))))
-    best = min([first] + [one() for _ in range(reps - 1)])
-    return best, reps
+    return min([first] + [fn() for _ in range(reps - 1)]), reps
 
 
-def cpu_bfv_time(pk, ctx, cfg, max_chunks=64):
-    """SURVEY 8(d) CPU baseline 3: the cloud phase of the workload in real
-    RNS-BFV on the host, through the C restatement (oracle/bfv_oracle.c, same
-    parameters and keys as the device), op by op like the reference algorithm:
-    multiply+relinearise, the rotation_schedule rotate-and-add, mask, sum.
-    Timed on 1 thread and on all host threads (chunks in parallel; ctypes
-    drops the GIL).  Bounded sample: the first max_chunks chunks."""
-    sys.path.insert(0, str(ROOT / "tests"))
-    from oracle_bindings import BfvOracle
+def cpu_reference_baseline(cfg, budget_s=2.0):
+    """B1: the reference CPU path on 1 core, cloud section and
+    whole spmv_partitioned, best of a bounded number of runs of the workload."""
+    rw = RefWorkload(cfg)
+    try:
+        rw.prepare_cloud()
+        allm = list(range(len(cfg["ms"])))
+        cloud, rc = _best_of(lambda: rw.cloud(allm), budget_s)
+        full, rf = _best_of(lambda: rw.full(allm), budget_s)
+    finally:
+        rw.close()
+    return {"value": round(cloud, 4), "unit": "ms", "cores": 1, "kind": "reference",
+            "e2e_value": round(full, 4),
+            "sample": f"{cfg['name']}: whole workload, unmodified reference SimBackend (plaintext slot "
+                      f"simulator, oracle/_ref), slot_count = chunk_size = {rw.S}; value = cloud section "
+                      f"(multiply + intra_chunk_sum + inter_chunk_sum, protocol.cpp:121-134) best of {rc}; "
+                      f"e2e_value = whole spmv_partitioned best of {rf}"}
 
-    orc = BfvOracle.like(ctx)
-    S = ctx.slots
+
+def cpu_bfv_baseline(pk, cfg, budget_s=3.0):
+    """B3: the cloud phase in real RNS-BFV on the host through the
+    C restatement (oracle/bfv_oracle.c; same parameters and keys as the device),
+    op by op like the reference algorithm: multiply + relinearise, the
+    rotation_schedule rotate-and-add, mask, sum.  Bounded sample: chunks in plan
+    order until ~budget_s of 1-thread work; the same sample on all host threads
+    (chunks in parallel; ctypes drops the GIL); extrapolated to the whole
+    workload by its key-switch count (multiplies + rotations)."""
+    ob = _oracle()
+    p = pk.default_params(cfg["logn"])
+    orc = ob.BfvOracle(p.logn, p.L, p.K, p.alpha, p.qbits, p.pbits, T_MOD, 1)
+    S = 1 << (cfg["logn"] - 1)
     chunks = []
     for m, v in zip(cfg["ms"], cfg["vs"]):
-        pc = pk.pack_chunks(m, S) if m.rows <= S else None
-        if pc is None:
-            continue
-        off = 0
-        for r, c in zip(pc["r"], pc["c"]):
-            size = int(r * c)
-            vf, cf = pc["vflat"][off:off + size], pc["cflat"][off:off + size]
-            off += size
-            chunks.append((int(r), int(c), vf, np.where(cf >= 0, np.asarray(v)[np.maximum(cf, 0)], 0)))
-        if len(chunks) >= max_chunks:
-            break
-    chunks = chunks[:max_chunks]
+        rp = np.asarray(m.row_ptrs)
+        for r0 in range(0, max(m.rows, 1), S):  # row slices like partition_rows
+            r1 = min(m.rows, r0 + S)
+            sl = pk.Csr(r1 - r0, m.cols, rp[r0:r1 + 1] - rp[r0], np.asarray(m.col_indices)[rp[r0]:rp[r1]],
+                        np.asarray(m.values)[rp[r0]:rp[r1]])
+            pc = pk.pack_chunks(sl, S)
+            off = 0
+            for r, c in zip(pc["r"], pc["c"]):
+                size = int(r * c)
+                vf, cf = pc["vflat"][off:off + size], pc["cflat"][off:off + size]
+                off += size
+                chunks.append((int(r), int(c), vf, np.where(cf >= 0, np.asarray(v)[np.maximum(cf, 0)], 0)))
     if not chunks:
         return None
     scheds = [pk.rotation_schedule(r, c) for r, c, _, _ in chunks]
-    for g in sorted({orc.galois_elt(off) for sc in scheds for off, _ in sc}):
-        if g != 1:
-            orc.lib.bfvo_add_galois_key(orc.h, g)  # keys are setup, not timed
-    cts = [(orc.encrypt(a, 100 + i), orc.encrypt(b, 200 + i)) for i, (_, _, a, b) in enumerate(chunks)]
+    total_ks = sum(1 + len(s) for s in scheds)
+    keys = set()
 
     def chain(i):
         r = chunks[i][0]
-        prod = orc.mul_relin(*cts[i])
+        a = orc.encrypt(chunks[i][2], 100 + i)
+        b = orc.encrypt(chunks[i][3], 200 + i)
+        t0 = time.perf_counter()
+        prod = orc.mul_relin(a, b)
         acc = prod
         for off, from_acc in scheds[i]:
             acc = orc.add(acc, orc.rotate(acc if from_acc else prod, off))
-        return orc.mul_plain(acc, np.ones(r, np.int64))
+        out = orc.mul_plain(acc, np.ones(r, np.int64))
+        return out, (time.perf_counter() - t0) * 1e3
 
-    def run(threads):
-        t0 = time.perf_counter()
-        if threads == 1:
-            parts = [chain(i) for i in range(len(chunks))]
-        else:
-            with ThreadPoolExecutor(max_workers=threads) as ex:
-                parts = list(ex.map(chain, range(len(chunks))))
-        acc = parts[0]
-        for p in parts[1:]:
-            acc = orc.add(acc, p)
-        return (time.perf_counter() - t0) * 1e3
-
+    # 1 thread: chunk after chunk until the budget is spent (keys are setup, not timed)
+    parts, one, n = [], 0.0, 0
+    while n < len(chunks) and (one < budget_s * 1e3 or n == 0):
+        for off, _ in scheds[n]:
+            g = orc.galois_elt(off)
+            if g != 1 and g not in keys:
+                orc.lib.bfvo_add_galois_key(orc.h, g)
+                keys.add(g)
+        out, ms = chain(n)
+        parts.append(out)
+        one += ms
+        n += 1
+    t0 = time.perf_counter()
+    acc = parts[0]
+    for q in parts[1:]:
+        acc = orc.add(acc, q)
+    one += (time.perf_counter() - t0) * 1e3
     threads = os.cpu_count() or 1
-    one = run(1)
-    many = run(threads)
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        outs = list(ex.map(lambda i: chain(i)[0], range(n)))
+    acc = outs[0]
+    for q in outs[1:]:
+        acc = orc.add(acc, q)
+    many = (time.perf_counter() - t0) * 1e3
+    sample_ks = sum(1 + len(s) for s in scheds[:n])
+    scale = total_ks / sample_ks
     return {"ms_1_thread": round(one, 2), "ms_all_threads": round(many, 2), "threads": threads,
-            "chunks": len(chunks), "kind": "port",
-            "sample": f"{cfg['name']}: cloud phase of {len(chunks)} chunk(s) in RNS-BFV on the CPU oracle "
-                      "(oracle/bfv_oracle.c), same parameters, keys excluded"}
+            "sample_chunks": n, "chunks": len(chunks), "sample_key_switches": sample_ks,
+            "key_switches": total_ks,
+            "extrapolated_ms_1_thread": round(one * scale, 1), "extrapolated_ms_all_threads": round(many * scale, 1),
+            "kind": "port",
+            "sample": f"{cfg['name']}: cloud phase of {n} of {len(chunks)} chunk(s) in RNS-BFV on the CPU oracle "
+                      "(oracle/bfv_oracle.c), same parameters, keys excluded; the all-threads run includes the "
+                      "sample's encryptions; extrapolated by key-switch count"}
 
 
 def run_reference_arm(args, cfg):
-    """--impl reference: the reference's own CPU path on all host cores it can use
-    (independent matrices in parallel threads; the library itself is single-threaded)."""
-    sys.path.insert(0, str(ROOT / "tests"))
-    from oracle_bindings import ref_lib, _i64, _p, i64p
-
-    L = ref_lib()
-    if L is None:
-        return {"impl": "reference", "unavailable": "oracle/_ref/libspmv_ref.so not built"}
-    S = 1 << (cfg["logn"] - 1)
-    ms, vs = cfg["ms"], cfg["vs"]
-    arrays = [(_i64(m.row_ptrs), _i64(m.col_indices), _i64(m.values), _i64(v)) for m, v in zip(ms, vs)]
-    threads = max(1, min(len(ms), os.cpu_count() or 1))
-
-    def work(idx):
-        for i in idx:
-            rp, ci, va, vv = arrays[i]
-            m = ms[i]
-            L.ref_time_spmv_partitioned(S, 65537, m.rows, m.cols, _p(rp, i64p), _p(ci, i64p), _p(va, i64p),
-                                        _p(vv, i64p), S, 1)
-
-    parts = [list(range(k, len(ms), threads)) for k in range(threads)]
+    """--impl reference: the reference's own CPU path on all host threads it can
+    use (independent matrices in parallel threads; the library itself is
+    single-threaded).  value = the cloud section per step, e2e = the whole
+    spmv_partitioned per step (same workload, same seeds)."""
+    try:
+        rw = RefWorkload(cfg)
+    except RuntimeError as e:
+        return {"impl": "reference", "unavailable": str(e)}
+    rw.prepare_cloud()
+    nm = len(cfg["ms"])
+    threads = max(1, min(nm, os.cpu_count() or 1))
+    parts = [list(range(k, nm, threads)) for k in range(threads)]
     pool = ThreadPoolExecutor(max_workers=threads) if threads > 1 else None  # persistent workers
 
-    def step():
+    def step(fn):
         t0 = time.perf_counter()
         if pool is None:
-            work(parts[0])
+            fn(parts[0])
         else:
-            list(pool.map(work, parts))
+            list(pool.map(fn, parts))
         return (time.perf_counter() - t0) * 1e3
 
     for _ in range(args.warmup):
-        step()
-    times = [step() for _ in range(args.steps)]
+        step(rw.cloud)
+    cloud = [step(rw.cloud) for _ in range(args.steps)]
+    for _ in range(min(args.warmup, 3)):
+        step(rw.full)
+    full = [step(rw.full) for _ in range(args.steps)]
     if pool is not None:
         pool.shutdown()
-    v = statistics.mean(times)
-    sample = f"{cfg['name']}: full workload per step ({len(ms)} matrix/matrices), SimBackend slot_count={S}"
+    rw.close()
+    v, e = statistics.mean(cloud), statistics.mean(full)
+    sample = (f"{cfg['name']}: the whole workload per step ({nm} matrix/matrices), unmodified reference "
+              f"SimBackend (oracle/_ref), slot_count = chunk_size = {rw.S}, {threads} host threads over matrices")
     return {"metric": METRIC, "value": round(v, 4), "unit": "ms", "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(v, 4), "higher_is_better": False, "scaling": "weak",
-            "vs_baseline": None, "dtype": "u64", "data": "synthetic (seeded, BASELINE.json shapes)",
-            "impl": "reference",
-            "config": {"workload": cfg["name"], "parallelism": f"{threads} host threads"},
+            "warmup": args.warmup, "ms_per_step": round(v, 4), "higher_is_better": False, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u64 (slot simulator mod t)",
+            "data": "synthetic (synth.py, BASELINE.json shapes)", "impl": "reference",
+            "config": {"workload": cfg["name"], "parallelism": f"{threads} host threads",
+                       "value_scope": "cloud section: multiply + intra_chunk_sum + inter_chunk_sum "
+                                      "(protocol.cpp:121-134) of every slice",
+                       "e2e_scope": "whole spmv_partitioned (pack, encode/encrypt, cloud, decrypt)"},
             "cpu_baseline": {"value": round(v, 4), "unit": "ms", "cores": threads, "kind": "reference",
                              "sample": sample},
-            "e2e": {"value": round(v, 4), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "e2e": {"value": round(e, 4), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+# ----------------------------------------------------------------------------
+# integer work model of the plan's kernels (modmul-equivalents per launch)
+# ----------------------------------------------------------------------------
+# One unit = one lazy Shoup butterfly (1 modmul + 2 modadd: the op k_bfly_peak
+# measures).  A Shoup or Barrett product counts 1; a Dot29 basis-conversion
+# term counts 0.375 (12 of the 32 fmaheavy-pipe cycles of a Shoup product,
+# DESIGN.md 4).
+DOT = 0.375
+
+
+def kernel_units(name: str, items: int, slices: int, logn: int, L: int, K: int, dnum: int, alpha: int) -> float:
+    n, h = 1 << logn, 1 << (logn - 1)
+    Bs = 7 if logn >= 15 else (6 if logn >= 12 else logn // 2)
+    As = logn - Bs
+    M, LK, nB = 2 * L + 1, L + K, L + 1
+    e1_q2b = L + L + nB * (L + 1) * DOT          # E1 Q -> B per coefficient of one poly
+    e1_b2q = nB + nB + L * (nB + 1) * DOT        # E1 B -> Q
+    e2 = L + L + nB * (L + 1) * DOT              # E2 scale-and-round into B
+    if name.startswith("k_mul_extend"):
+        return items * 4 * n * e1_q2b
+    if name.startswith("k_ntt_cols fwd (multiply)"):
+        return items * 4 * M * h * As
+    if name.startswith("k_mul_blocks_tensor"):
+        return items * M * (7 * h * Bs + 4 * n)
+    if name.startswith("k_ntt_cols inv (multiply)"):
+        return items * 3 * M * h * As
+    if name.startswith("k_mul_scale"):
+        return items * 3 * n * (e2 + e1_b2q)
+    if name.startswith("k_ks_modup_cols"):
+        return items * dnum * LK * (n * alpha + h * As)
+    if name.startswith("k_ks_blocks_inner"):
+        return items * LK * (dnum * h * Bs + 2 * dnum * n + 2 * h * Bs)
+    if name.startswith("k_ntt_cols inv (key switch)"):
+        return items * 2 * LK * h * As
+    if name.startswith("k_ks_moddown"):
+        return items * 2 * n * (K + L * (K + 1) * DOT)
+    if name.startswith("k_ntt_cols fwd (mask)"):
+        return items * 2 * L * h * As
+    if name.startswith("k_mask_blocks"):
+        return items * 2 * L * (h * Bs + n) + slices * 2 * L * h * Bs
+    if name.startswith("k_ntt_cols inv (mask)"):
+        return slices * 2 * L * h * As
+    return 0.0
+
+
+def kernel_table(job, groups, st, logn, p, bfly_peak, reps=3):
+    """Per-launch CUDA-event profile of the plan graph (L2 flushed before each
+    replay) with the work model above: units / launch time vs the probe peak."""
+    ks = job.profile_kernels(reps=reps)
+    rows = []
+    for k in ks:
+        g = groups[k["group"]] if k["group"] < len(groups) else {"items": 0, "name": "?"}
+        units = kernel_units(k["name"], g["items"], st["slices"], logn, p.L, p.K,
+                             (p.L + p.alpha - 1) // p.alpha, p.alpha)
+        rate = units / (k["us"] * 1e-6) if k["us"] > 0 else 0.0
+        rows.append({"kernel": k["name"], "group": g["name"], "items": g["items"], "us": round(k["us"], 2),
+                     "units": int(units), "g_units_s": round(rate / 1e9, 1),
+                     "int_frac": round(rate / bfly_peak, 4) if bfly_peak else None})
+    return rows
+
+
+def traffic_of(cfgno: int, launch_index: int):
+    """DRAM read+write bytes of the same launch from the committed ncu capture
+    (profiles/r02_traffic_c<cfg>.json, made by tools/ncu_traffic.py)."""
+    f = ROOT / "profiles" / f"r02_traffic_c{cfgno}.json"
+    if not f.exists():
+        return None, None
+    d = json.loads(f.read_text())
+    ls = d.get("launches", [])
+    if launch_index < len(ls):
+        return int(ls[launch_index]["dram_bytes"]), str(f.relative_to(ROOT))
+    return None, None
+
+
+# ----------------------------------------------------------------------------
+# our arm
+# ----------------------------------------------------------------------------
+def time_cloud(job, stream, flush, steps, warmup, sampler_s=0.0, world=1, device=0):
+    import torch
+
+    def step_timed():
+        with torch.cuda.stream(stream):
+            flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)  # creates the events; re-recorded inside the C call around the launch
+        b.record(stream)
+        job.cloud_timed(a, b, graph=True)
+        return a, b
+
+    for _ in range(warmup):
+        step_timed()
+    torch.cuda.synchronize(device)
+    sampler = None
+    if sampler_s > 0:
+        sampler = ClockSampler(device)
+        sampler.start()
+        t_end = time.time() + sampler_s  # let the sampler see the loaded state
+        while time.time() < t_end:
+            for _ in range(4):
+                job.cloud(graph=True)
+            torch.cuda.synchronize(device)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize(device)
+    evs = [step_timed() for _ in range(steps)]
+    torch.cuda.synchronize(device)
+    if world > 1:
+        torch.distributed.barrier()
+    clocks = sampler.stop() if sampler else None
+    times = [a.elapsed_time(b) for a, b in evs]
+    return times, clocks
+
+
+def time_e2e(pk, ctx, ms, vs, warmup, steps, device):
+    """spmv_batch through the public API (host in, host out), mean wall ms."""
+    import torch
+
+    for _ in range(warmup):
+        r = pk.spmv_batch(ctx, ms, vs)
+    ok = all(np.array_equal(x["values"], exact_values(m, v)) for m, v, x in zip(ms, vs, r))
+    out = []
+    for _ in range(steps):
+        torch.cuda.synchronize(device)
+        t0 = time.perf_counter()
+        r = pk.spmv_batch(ctx, ms, vs)
+        out.append((time.perf_counter() - t0) * 1e3)
+    ok = ok and all(np.array_equal(x["values"], exact_values(m, v)) for m, v, x in zip(ms, vs, r))
+    return out, ok, r
+
+
+def measure_config(pk, cfgno, cfg, args, rank, world, device, headline):
+    import torch
+
+    ms, vs = cfg["ms"], cfg["vs"]
+    split = world > 1 and len(ms) == 1  # one matrix: chunk split over the GPUs
+    if split:  # the ranks share one key (rank 0 decrypts the summed partials)
+        from paper_2603_04742_b200 import shard
+
+        ctx = pk.Context(logn=cfg["logn"], seed=shard.shared_seed(), device=device)
+        shard.disjoint_streams(ctx, rank)
+    else:
+        ctx = pk.Context(logn=cfg["logn"], device=device)
+    p = ctx.params
+    if world > 1 and len(ms) > 1:  # independent matrices round-robin (no collective)
+        from paper_2603_04742_b200 import shard
+
+        mine = shard.units_for_rank(len(ms), rank, world)
+        ms, vs = [ms[i] for i in mine], [vs[i] for i in mine]
+    job = pk.Job(ctx, ms, vs, rank=rank if split else 0, world=world if split else 1)
+    job.encrypt()
+    job.cloud(graph=True)
+    if split:
+        from paper_2603_04742_b200 import shard
+
+        res = shard.finish_chunk_split(ctx, job, device)
+        verified = res is None or all(np.array_equal(r["values"], exact_values(m, v))
+                                      for m, v, r in zip(ms, vs, res))
+    else:
+        res = job.finish()
+        verified = all(np.array_equal(r["values"], exact_values(m, v)) for m, v, r in zip(ms, vs, res))
+    st = job.stats()
+    stream = torch.cuda.ExternalStream(ctx.stream_ptr(), device=device)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
+    steps = args.steps if headline else max(5, min(args.steps, 10))
+    times, clocks = time_cloud(job, stream, flush, steps, args.warmup, 1.0 if headline else 0.0, world, device)
+    ms_step = statistics.mean(times)
+    if world > 1:
+        t = torch.tensor([ms_step], device=device)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms_step = float(t.item())
+    out = {"name": cfg["name"], "ms": round(ms_step, 4), "median_ms": round(statistics.median(times), 4),
+           "min_ms": round(min(times), 4), "verified": verified, "plan": st, "clocks": clocks,
+           "measured_noise_bits": min((r["measured_noise"] for r in (res or []) if r["n_ct"] > 0), default=None)}
+    bfly_peak = ctx.probe_butterfly_peak()
+    hbm_peak = peaks().get("hbm_gbs", 6650.0)
+    n = ctx.n
+    # launch groups (multiply+relin, rotate levels, mask): compulsory bytes vs HBM, NTT work vs the probe
+    with torch.cuda.stream(stream):
+        flush.zero_()
+    torch.cuda.synchronize(device)
+    groups = job.profile()
+    bfly_per_limb = (n // 2) * (n.bit_length() - 1)
+    gro = []
+    for g in groups:
+        gbs = g["bytes"] / (g["us"] * 1e-6) / 1e9 if g["us"] > 0 else 0.0
+        gbfly = g["limb_ntts"] * bfly_per_limb / (g["us"] * 1e-6) / 1e9 if g["us"] > 0 else 0.0
+        gro.append({"group": g["name"], "items": g["items"], "us": round(g["us"], 2), "bytes": g["bytes"],
+                    "hbm_gbs": round(gbs, 1), "hbm_frac": round(gbs / hbm_peak, 4),
+                    "ntt_gbfly": round(gbfly, 1), "ntt_frac": round(gbfly * 1e9 / bfly_peak, 4)})
+    kt = kernel_table(job, groups, st, cfg["logn"], p, bfly_peak)
+    # integer fraction per launch group with every kernel's modmul work (not butterflies only)
+    for g in gro:
+        k_in = [k for k in kt if k["group"] == g["group"]]
+        us = sum(k["us"] for k in k_in)
+        units = sum(k["units"] for k in k_in)
+        g["int_units"] = units
+        g["int_frac"] = round(units / (us * 1e-6) / bfly_peak, 4) if us > 0 else None
+    rot = [g for g in gro if g["group"].startswith("rotate level")]
+    ks_summary = None
+    if rot:
+        us = sum(g["us"] for g in rot)
+        by = sum(g["bytes"] for g in rot)
+        un = sum(g["int_units"] for g in rot)
+        ks_summary = {"us": round(us, 2), "items": sum(g["items"] for g in rot), "bytes": by,
+                      "hbm_gbs": round(by / (us * 1e-6) / 1e9, 1),
+                      "hbm_frac": round(by / (us * 1e-6) / 1e9 / hbm_peak, 4),
+                      "int_frac": round(un / (us * 1e-6) / bfly_peak, 4)}
+    if kt:  # dominant kernel launch of the step
+        top_i = max(range(len(kt)), key=lambda i: kt[i]["us"])
+        top = kt[top_i]
+        traffic, tsrc = traffic_of(cfgno, top_i)
+        grp = next((g for g in gro if g["group"] == top["group"]), None)
+        out["roofline"] = {
+            "bound": "int", "kernel": top["kernel"], "launch_index": top_i, "group": top["group"],
+            "achieved": top["g_units_s"], "peak": round(bfly_peak / 1e9, 2), "unit": "G modmul-equiv/s",
+            "frac": top["int_frac"], "traffic": traffic, "traffic_source": tsrc,
+            "launch_us": top["us"], "units_per_launch": top["units"],
+            "share_of_step": round(top["us"] / (ms_step * 1e3), 4),
+            "timing": "CUDA events on the context stream around this launch inside a replay of the plan graph, "
+                      "mean of 3 replays, L2 flushed before each",
+            "peak_source": "k_bfly_peak: register-resident lazy-Shoup radix-16 butterfly sequence (this run)",
+            "work_model": "bench.py kernel_units(): butterfly = 1, Shoup/Barrett product = 1, Dot29 term = 0.375",
+            "group_int_frac": grp["int_frac"] if grp else None,
+            "hbm_peak_gbs": hbm_peak, "hbm_peak_source": "MEASURED_PEAKS.json" if peaks() else "fallback",
+        }
+    out["groups"] = gro
+    out["kernels"] = kt
+    out["key_switch"] = ks_summary
+    out["whole_plan_hbm_gbs"] = round(st["hbm_bytes_algorithmic"] / (ms_step * 1e-3) / 1e9, 1)
+    out["whole_step_int_frac"] = round(sum(k["units"] for k in kt) / (ms_step * 1e-3) / bfly_peak, 4)
+    # e2e through the public API: party-separated (default), then the fused variant
+    if world == 1:
+        e2e_n = args.steps if headline else 5
+        t_sep, ok_sep, r = time_e2e(pk, ctx, ms, vs, max(2, min(args.warmup, 3)), e2e_n, device)
+        jr = pk.Job(ctx, ms, vs)
+        jr.run()
+        h2d, d2h = jr.io_bytes()
+        jr.close()
+        out["e2e"] = {"value": round(statistics.mean(t_sep), 4), "unit": "ms", "h2d_bytes_per_step": int(h2d),
+                      "d2h_bytes_per_step": int(d2h), "verified": ok_sep,
+                      "scope": "spmv_batch, party-separated: clients write input ciphertexts, the cloud writes "
+                               "result ciphertexts, the key holder decrypts them"}
+        ctx.set_option("pipeline_fuse", 3)
+        t_f, ok_f, _ = time_e2e(pk, ctx, ms, vs, 2, e2e_n, device)
+        ctx.set_option("pipeline_fuse", 0)
+        out["e2e_fused"] = {"value": round(statistics.mean(t_f), 4), "unit": "ms", "verified": ok_f,
+                            "scope": "pipeline_fuse=3: encryption finish inside the cloud's multiply "
+                                     "extension, decryption inside the cloud's mask step (crosses the "
+                                     "party boundary; reported separately)"}
+        out["verified"] = out["verified"] and ok_sep and ok_f
+        led = {k: sum(x["ledger"][k] for x in r) for k in r[0]["ledger"]}
+        out["ledger"] = led
+        out["paper_cost_model"] = {"cloud_ms": round(paper_cloud_ms(led), 1),
+                                   "total_ms": round(paper_total_ms(led), 1)}
+        out["wire_bytes_per_ct"] = ctx.wire_size
+    job.close()
+    ctx.close()
+    return out
 
 
 # the reference's per-op cost table (cost.hpp: single-thread BFV, N = 8192)
@@ -249,188 +604,9 @@ def paper_total_ms(led):
     return sum(led[k] * c for k, c in PAPER_COSTS.items())
 
 
-def key_switch_roofline(ctx, job, stream, flush):
-    """Per launch group of one plan graph replay (event nodes between groups, L2
-    flushed first): compulsory HBM bytes (fused rotate+add = 3C per
-    item + KEY per distinct key) / device time vs the measured copy bandwidth,
-    and the group's NTT butterflies / time vs the butterfly probe."""
-    import torch
-
-    with torch.cuda.stream(stream):
-        flush.zero_()
-    torch.cuda.synchronize()
-    phases = job.profile()
-    peak = ctx.probe_butterfly_peak()
-    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
-    hbm_peak = peaks.get("hbm_gbs", 6650.0)
-    n = ctx.n
-    bfly_per_limb = (n // 2) * (n.bit_length() - 1)
-    rows = []
-    for p in phases:
-        if p["us"] <= 0:
-            continue
-        gbs = p["bytes"] / (p["us"] * 1e-6) / 1e9
-        gbfly = p["limb_ntts"] * bfly_per_limb / (p["us"] * 1e-6) / 1e9
-        rows.append({"group": p["name"], "items": p["items"], "us": round(p["us"], 2), "bytes": p["bytes"],
-                     "hbm_gbs": round(gbs, 1), "hbm_frac": round(gbs / hbm_peak, 4),
-                     "ntt_gbfly": round(gbfly, 1), "int_frac": round(gbfly * 1e9 / peak, 4)})
-    ks = [r for r in rows if r["group"].startswith("rotate level") or r["group"] == "multiply+relin"]
-    rot = [r for r in rows if r["group"].startswith("rotate level")]
-    summ = None
-    if rot:
-        us = sum(r["us"] for r in rot)
-        by = sum(r["bytes"] for r in rot)
-        ntt = sum(r["ntt_gbfly"] * r["us"] for r in rot) / us
-        summ = {"us": round(us, 2), "items": sum(r["items"] for r in rot), "bytes": by,
-                "hbm_gbs": round(by / (us * 1e-6) / 1e9, 1), "hbm_frac": round(by / (us * 1e-6) / 1e9 / hbm_peak, 4),
-                "ntt_gbfly": round(ntt, 1), "int_frac": round(ntt * 1e9 / peak, 4)}
-    return {"rotations": summ, "groups": rows if ks else rows, "hbm_peak_gbs": hbm_peak,
-            "int_peak_gbfly": round(peak / 1e9, 1),
-            "note": "one graph replay with event nodes between launch groups, L2 flushed before; "
-                    "bytes = compulsory (SURVEY 8(d)); "
-                    "int_frac counts NTT butterflies only (ModUp/MAC/ModDown modmuls excluded)"}
-
-
-def measure_config(pk, cfg, args, rank, world, device, full=True):
-    import torch
-
-    ctx = pk.Context(logn=cfg["logn"], seed=1, device=device)
-    ms, vs = cfg["ms"], cfg["vs"]
-    job = pk.Job(ctx, ms, vs)
-    job.encrypt()
-    job.cloud(graph=True)
-    res = job.finish()
-    verified = all(np.array_equal(r["values"], exact_values(m, v)) for m, v, r in zip(ms, vs, res))
-    st = job.stats()
-    stream = torch.cuda.ExternalStream(ctx.stream_ptr(), device=device)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
-
-    def step_timed():
-        with torch.cuda.stream(stream):
-            flush.zero_()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)  # creates the events; re-recorded inside the C call around the launch
-        b.record(stream)
-        job.cloud_timed(a, b, graph=True)
-        return a, b
-
-    for _ in range(args.warmup):
-        step_timed()
-    torch.cuda.synchronize(device)
-    sampler = ClockSampler(device)
-    sampler.start()
-    # keep the GPU busy long enough for the clock sampler to see the loaded state
-    t_end = time.time() + (1.0 if full else 0.3)
-    while time.time() < t_end:
-        for _ in range(4):
-            job.cloud(graph=True)
-        torch.cuda.synchronize(device)
-    if world > 1:
-        torch.distributed.barrier()
-    torch.cuda.synchronize(device)
-    evs = [step_timed() for _ in range(args.steps)]
-    torch.cuda.synchronize(device)
-    if world > 1:
-        torch.distributed.barrier()
-    clocks = sampler.stop()
-    times = [a.elapsed_time(b) for a, b in evs]
-    ms_step = statistics.mean(times)
-    if world > 1:
-        t = torch.tensor([ms_step], device=device)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms_step = float(t.item())
-    out = {"name": cfg["name"], "ms_per_step": ms_step, "median_ms": statistics.median(times),
-           "min_ms": min(times), "verified": verified, "plan": st, "clocks": clocks,
-           "measured_noise_bits": min(r["measured_noise"] for r in res if r["n_ct"] > 0)}
-    out["key_switch"] = key_switch_roofline(ctx, job, stream, flush)
-    if not full:
-        # e2e through the public API, as for the headline (fewer calls)
-        for _ in range(3):
-            pk.spmv_batch(ctx, ms, vs)
-        e2e = []
-        for _ in range(5):
-            torch.cuda.synchronize(device)
-            t0 = time.perf_counter()
-            r = pk.spmv_batch(ctx, ms, vs)
-            e2e.append((time.perf_counter() - t0) * 1e3)
-        out["verified"] = verified and all(np.array_equal(x["values"], exact_values(m, v))
-                                           for m, v, x in zip(ms, vs, r))
-        out["e2e_ms"] = round(statistics.mean(e2e), 4)
-        job.close()
-        ctx.close()
-        return out
-
-    # e2e through the public API (host in, host out)
-    e2e = []
-    # warm-up like the device step: the first calls build the plan, the second
-    # captures the whole-evaluation graph (cached per chunk-shape structure)
-    for _ in range(args.warmup):
-        r = pk.spmv_batch(ctx, ms, vs)
-        verified = verified and all(np.array_equal(x["values"], exact_values(m, v)) for m, v, x in zip(ms, vs, r))
-    for i in range(max(2, min(args.steps, 20))):
-        torch.cuda.synchronize(device)
-        t0 = time.perf_counter()
-        r = pk.spmv_batch(ctx, ms, vs)
-        e2e.append((time.perf_counter() - t0) * 1e3)
-    verified = verified and all(np.array_equal(x["values"], exact_values(m, v)) for m, v, x in zip(ms, vs, r))
-    # bytes one spmv_batch call moves (the cached pipeline's upload image and
-    # compact result download), from a job run the same way
-    jr = pk.Job(ctx, ms, vs)
-    jr.run()
-    h2d, d2h = jr.io_bytes()
-    jr.close()
-    out["e2e"] = {"value": round(statistics.mean(e2e), 4), "unit": "ms", "h2d_bytes_per_step": int(h2d),
-                  "d2h_bytes_per_step": int(d2h)}
-    out["wire_bytes_per_ct"] = ctx.wire_size  # real serialized ciphertext (vs the reference's 545 260 B price)
-    # paper-calibrated CPU estimate of the same ledger (cost.hpp: N=8192, 1 thread)
-    led = {k: sum(x["ledger"][k] for x in r) for k in r[0]["ledger"]}
-    out["paper_cost_model"] = {"cloud_ms": round(paper_cloud_ms(led), 1), "total_ms": round(paper_total_ms(led), 1),
-                               "ledger": led}
-    # the diagonal-method baseline on the same GPU backend (square inputs that fit)
-    if len(ms) == 1 and ms[0].rows == ms[0].cols and 2 * ms[0].rows <= ctx.slots:
-        pk.diag_spmv(ctx, ms[0], vs[0])
-        torch.cuda.synchronize(device)
-        t0 = time.perf_counter()
-        dr = pk.diag_spmv(ctx, ms[0], vs[0])
-        dms = (time.perf_counter() - t0) * 1e3
-        out["diagonal_baseline"] = {"e2e_ms": round(dms, 3), "diagonals": dr["n_ct"], "ledger": dr["ledger"],
-                                    "verified": bool(np.array_equal(dr["values"], exact_values(ms[0], vs[0]))),
-                                    "paper_cost_model_ms": round(paper_total_ms(dr["ledger"]), 1)}
-    out["verified"] = verified
-    # roofline of the dominant kernel: the batched NTT (largest launch of the plan)
-    L, nB = ctx.params.L, ctx.params.L + 1
-    limbs = max(1, st["chunks"]) * 4 * (L + nB)
-    # mean of 20 back-to-back launches, best of 3 trials (clock / neighbour noise)
-    us = min(ctx.probe_ntt_us(limbs, inverse=False, reps=20) for _ in range(3))
-    n = ctx.n
-    logn = cfg["logn"]
-    bfly = limbs * (n // 2) * logn
-    peak = ctx.probe_butterfly_peak()
-    hbm_bytes = limbs * 2 * n * 8
-    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
-    hbm_peak = peaks.get("hbm_gbs", 6650.0)
-    traffic = None
-    tfile = ROOT / "profiles" / f"r01_ntt_traffic_{limbs}.json"
-    if tfile.exists():  # dram read+write of the same launch shape from one ncu capture
-        tj = json.loads(tfile.read_text())
-        if tj.get("logn") == logn:
-            traffic = int(tj["traffic_bytes_per_launch"])
-    out["roofline"] = {
-        "bound": "int", "kernel": "forward NTT launch = k_ntt_cols + k_ntt_blocks (two-phase, all limbs)",
-        "achieved": round(bfly / (us * 1e-6) / 1e9, 2), "peak": round(peak / 1e9, 2),
-        "unit": "Gbutterfly/s", "frac": round(bfly / (us * 1e-6) / peak, 4),
-        "traffic": traffic, "traffic_source": str(tfile.relative_to(ROOT)) if traffic else None,
-        "algorithmic_bytes_per_launch": 2 * limbs * n * 8,  # one compulsory read + write per limb
-        "launch_us": round(us, 3), "limbs_per_launch": limbs,
-        "timing": "CUDA events on the context stream: mean of 20 back-to-back launches, best of 3 trials",
-        "hbm_achieved_gbs": round(hbm_bytes / (us * 1e-6) / 1e9, 1), "hbm_peak_gbs": hbm_peak,
-        "hbm_frac": round(hbm_bytes / (us * 1e-6) / 1e9 / hbm_peak, 4),
-        "peak_source": "register-resident lazy-Shoup radix-16 butterfly probe (this run); HBM: MEASURED_PEAKS.json",
-    }
-    out["whole_plan_hbm_gbs"] = round(st["hbm_bytes_algorithmic"] / (ms_step * 1e-3) / 1e9, 1)
-    job.close()
-    ctx.close()
-    return out
+def ctx_desc(pk, logn):
+    p = pk.default_params(logn)
+    return f"N=2^{logn}, L={p.L}x{p.qbits}b, K={p.K}x{p.pbits}b, alpha={p.alpha}, t={T_MOD}"
 
 
 def main():
@@ -439,9 +615,9 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=2)
-    ap.add_argument("--all-configs", dest="all_configs", action="store_true", default=True)
-    ap.add_argument("--only", dest="all_configs", action="store_false")
+    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--only", dest="all_configs", action="store_false", default=True,
+                    help="headline config only (no side configs)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -452,8 +628,7 @@ def main():
 
     if args.impl == "reference":
         if rank == 0:
-            cfg = make_config(args.config)
-            print(json.dumps(run_reference_arm(args, cfg)), flush=True)
+            print(json.dumps(run_reference_arm(args, make_config(args.config))), flush=True)
         return
 
     import torch
@@ -462,74 +637,58 @@ def main():
     if world > 1:
         torch.cuda.set_device(local)
         torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
-    cfg = make_config(args.config)
-    head = measure_config(pk, cfg, args, rank, world, local, full=True)
-    others = {}
-    if args.all_configs:
-        for c in (1, 2, 3, 4, 5):
-            if c == args.config:
-                continue
-            try:
-                o = measure_config(pk, make_config(c), args, rank, world, local, full=False)
-                others[f"C{c}"] = {"ms": round(o["ms_per_step"], 4), "e2e_ms": o["e2e_ms"],
-                                   "verified": o["verified"],
-                                   "chunks": o["plan"]["chunks"], "rotations": o["plan"]["rotations"],
-                                   "limb_ntts": o["plan"]["limb_ntts_per_run"],
-                                   "whole_plan_hbm_gbs": round(o["plan"]["hbm_bytes_algorithmic"] /
-                                                               (o["ms_per_step"] * 1e-3) / 1e9, 1),
-                                   "key_switch": o["key_switch"]["rotations"],
-                                   "groups": o["key_switch"]["groups"]}
-            except Exception as e:  # a failing side config must not hide the headline
-                others[f"C{c}"] = {"error": str(e)[:200]}
-
-    cpu = None
-    cpu_bfv = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    order = [args.config] + ([c for c in (1, 2, 3, 4, 5) if c != args.config] if args.all_configs and world == 1
+                             else [])
+    results = {}
+    for c in order:
+        cfg = make_config(c)
         try:
-            bctx = pk.Context(logn=cfg["logn"], seed=1)
-            cpu_bfv = cpu_bfv_time(pk, bctx, cfg)
-            bctx.close()
-        except Exception as e:  # the baseline must not hide the headline
-            cpu_bfv = {"error": str(e)[:200]}
-        r = cpu_reference_time(cfg["ms"], cfg["vs"], 1 << (cfg["logn"] - 1))
-        if r is not None:
-            best, reps = r
-            cpu = {"value": round(best, 4), "unit": "ms", "cores": 1, "kind": "reference",
-                   "sample": f"{cfg['name']}: whole workload, reference SimBackend spmv_partitioned "
-                             f"(plaintext slot simulator), best of {reps} runs, slot_count={1 << (cfg['logn'] - 1)}"}
+            r = measure_config(pk, c, cfg, args, rank, world, local, headline=(c == args.config))
+        except Exception as e:  # a failing side config must not hide the headline
+            if c == args.config:
+                raise
+            r = {"error": str(e)[:300]}
+        if rank == 0 and world == 1 and not args.no_cpu_baseline and "error" not in r:
+            try:
+                r["cpu_baseline"] = cpu_reference_baseline(cfg)
+            except Exception as e:
+                r["cpu_baseline"] = {"error": str(e)[:200]}
+            try:
+                r["cpu_bfv_baseline"] = cpu_bfv_baseline(pk, cfg)
+            except Exception as e:
+                r["cpu_bfv_baseline"] = {"error": str(e)[:200]}
+        r["rns"] = ctx_desc(pk, cfg["logn"])
+        results[c] = r
     if world > 1:
         torch.distributed.barrier()
     if rank == 0:
-        ms_step = head["ms_per_step"]
+        head = results[args.config]
+        nmat = len(make_config(args.config)["ms"])
         line = {
-            "metric": METRIC, "value": round(ms_step / world, 4), "unit": "ms", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
-            "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
-            "data": "synthetic (seeded generators with BASELINE.json shapes; values in [-8,8]\\{0})",
-            "config": {"workload": head["name"], "ring_degree": 1 << cfg["logn"],
-                       "rns": f"L={ctx_desc(cfg['logn'])}", "chunks": head["plan"]["chunks"],
+            "metric": METRIC, "value": head["ms"], "unit": "ms", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": head["ms"],
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+            "dtype": "u64", "data": "synthetic (synth.py: seeded generators with BASELINE.json shapes; values in "
+                                    "[-8,8]\\{0}; C1/C2/C5 bit-identical to the reference's random_sparse_csr)",
+            "config": {"workload": head["name"], "rns": head["rns"], "chunks": head["plan"]["chunks"],
                        "rotations": head["plan"]["rotations"], "levels": head["plan"]["levels"],
                        "l2": "flushed (256 MiB write) before every timed step",
-                       "parallelism": f"replica per GPU x{world}"},
-            "clocks": head["clocks"], "e2e": head["e2e"], "gpu_launches": head["plan"]["kernels_per_run"],
-            "roofline": head["roofline"], "key_switch": head["key_switch"], "cpu_bfv_baseline": cpu_bfv,
-            "paper_cost_model": head["paper_cost_model"], "diagonal_baseline": head.get("diagonal_baseline"),
-            "transcript": {"priced_bytes_per_ct": 545260, "wire_bytes_per_ct": head["wire_bytes_per_ct"]},
-            "cpu_baseline": cpu, "verified_exact": head["verified"],
-            "measured_noise_bits_min": head["measured_noise_bits"],
-            "whole_plan_hbm_gbs": head["whole_plan_hbm_gbs"],
-            "limb_ntts_per_step": head["plan"]["limb_ntts_per_run"], "other_configs": others,
+                       "parallelism": (f"{world} GPUs: " + ("matrices round-robin, no collective" if nmat > 1
+                                                            else "chunk split + NCCL all-reduce of partial results"))
+                       if world > 1 else "1 GPU"},
+            "clocks": head["clocks"], "e2e": head.get("e2e"), "e2e_fused": head.get("e2e_fused"),
+            "gpu_launches": head["plan"]["kernels_per_run"],
+            "roofline": head.get("roofline"), "cpu_baseline": head.get("cpu_baseline"),
+            "cpu_bfv_baseline": head.get("cpu_bfv_baseline"), "key_switch": head.get("key_switch"),
+            "verified_exact": head["verified"], "measured_noise_bits_min": head["measured_noise_bits"],
+            "whole_plan_hbm_gbs": head["whole_plan_hbm_gbs"], "whole_step_int_frac": head["whole_step_int_frac"],
+            "paper_cost_model": head.get("paper_cost_model"),
+            "transcript": {"priced_bytes_per_ct": 545260, "wire_bytes_per_ct": head.get("wire_bytes_per_ct")},
+            "configs": {f"C{c}": results[c] for c in order},
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
-
-
-def ctx_desc(logn):
-    import paper_2603_04742_b200 as pk
-
-    p = pk.default_params(logn)
-    return f"{p.L}x{p.qbits}b,K={p.K}x{p.pbits}b,alpha={p.alpha}"
 
 
 if __name__ == "__main__":

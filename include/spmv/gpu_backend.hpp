@@ -19,7 +19,7 @@ namespace spmv {
 struct GpuBfvOptions {
     int logn = 0;        // 0: derive from slot_count (N = 2 * slot_count)
     int L = 0, K = 0, alpha = 0, qbits = 0, pbits = 0;  // 0: defaults for N
-    std::uint64_t seed = 1;
+    std::uint64_t seed = 0;  // 0: 256-bit key from OS entropy; nonzero: deterministic (tests)
     int device = 0;
 };
 

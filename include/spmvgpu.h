@@ -52,7 +52,9 @@ typedef struct {
     int alpha;       /* primes per key-switching digit */
     int qbits, pbits;
     uint64_t t;      /* plaintext modulus, prime, t = 1 mod 2N */
-    uint64_t seed;   /* seeds every sampled polynomial (keys, encryptions) */
+    uint64_t seed;   /* 0 (default): a 256-bit ChaCha20 key and a random stream-id base
+                      * from OS entropy; nonzero: the deterministic key (seed_lo, seed_hi,
+                      * 6 fixed words) and stream ids from 1 (tests / known answers) */
     int device;
     /* reference HeParams fields kept for API parity (he.hpp:24-43) */
     double ciphertext_size_mb;
@@ -75,7 +77,16 @@ int spmvgpu_sync(spmvgpu_ctx* c);
  * cssc_job_* keep for reuse with their buffers and CUDA graph; default 4, 0 = off);
  * "forked_encrypt" (spmvgpu_encrypt_cssc as two concurrent branches, upload +
  * pack beside the message-independent encryption, as the cached whole-
- * evaluation graph always does; same words; default 0) */
+ * evaluation graph always does; same words; default 0);
+ * "pipeline_fuse" (the cached whole-evaluation graph of cssc_spmv_batch /
+ * cssc_job_run: 0 = party-separated, default: the clients' encryption writes
+ * the input ciphertexts, the cloud writes the result ciphertexts, the key
+ * holder decrypts them; bit 0 fuses the encryption's finish into the cloud's
+ * multiply, bit 1 the decryption into the cloud's mask step; evicts cached
+ * plans);
+ * "stream_base" (the next stream id spmvgpu_encrypt / the pipeline hand out
+ * when streams = NULL; contexts sharing a key -- the ranks of a chunk split --
+ * must use disjoint ranges) */
 int spmvgpu_set_option(spmvgpu_ctx* c, const char* name, int64_t value);
 /* opaque CUDA stream the context works on (cudaStream_t) */
 void* spmvgpu_stream(spmvgpu_ctx* c);
@@ -178,6 +189,17 @@ typedef struct {
     uint64_t items, bytes, limb_ntts;
 } spmvgpu_phase;
 int spmvgpu_plan_profile(spmvgpu_plan* p, spmvgpu_phase* phases, int cap, int* count);
+/* per kernel launch of the plan: `reps` graph replays, each after an L2 flush
+ * (a memset of flush_bytes), with an event node after every launch; mean us
+ * per launch, its kernel name and the launch group it belongs to (the index
+ * into spmvgpu_plan_profile's groups); *count = launches */
+typedef struct {
+    char name[48];
+    int32_t group;
+    double us;
+} spmvgpu_kernel_timing;
+int spmvgpu_plan_profile_kernels(spmvgpu_plan* p, int reps, uint64_t flush_bytes, spmvgpu_kernel_timing* out,
+                                 int cap, int* count);
 void spmvgpu_plan_destroy(spmvgpu_plan* p);
 
 /* ---- protocol level (host C++ above the device ABI) ---- */
@@ -243,6 +265,8 @@ int cssc_job_finish(cssc_job* j, int64_t* const* values, cssc_result* res); /* d
 int cssc_job_run(cssc_job* j, int64_t* const* values, cssc_result* res);
 int cssc_job_plan_stats(const cssc_job* j, spmvgpu_plan_stats* out);
 int cssc_job_profile(cssc_job* j, spmvgpu_phase* phases, int cap, int* count); /* see spmvgpu_plan_profile */
+int cssc_job_profile_kernels(cssc_job* j, int reps, uint64_t flush_bytes, spmvgpu_kernel_timing* out, int cap,
+                             int* count); /* see spmvgpu_plan_profile_kernels */
 int cssc_job_input_bytes(const cssc_job* j, uint64_t* h2d, uint64_t* d2h);
 void cssc_job_destroy(cssc_job* j);
 

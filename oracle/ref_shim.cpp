@@ -14,10 +14,14 @@
 //   csr_to_cssc           proj/src/sparse.cpp:79-117
 //   generate_chunks       proj/src/chunk.cpp:10-50
 //   diag_spmv             proj/src/diagonal.cpp:44-104
+//   cloud section         proj/src/protocol.cpp:121-134 (multiply,
+//                         intra_chunk_sum, inter_chunk_sum on the prepared
+//                         client ciphertexts of every row slice)
 #include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -26,6 +30,7 @@
 #include "spmv/diagonal.hpp"
 #include "spmv/he.hpp"
 #include "spmv/protocol.hpp"
+#include "spmv/reorg.hpp"
 #include "spmv/sparse.hpp"
 #include "spmv/synthetic.hpp"
 
@@ -224,5 +229,69 @@ int64_t ref_chunks(uint64_t rows, uint64_t cols, const int64_t* rp, const int64_
         return classify(e);
     }
 }
+
+// ---- cloud-section probe (bench.py --impl reference `value`) ----
+// ref_cloud_prepare runs the client phases of spmv() for every row slice
+// (partition_rows, csr_to_cssc, generate_chunks, reorg_vector, encode +
+// encrypt; protocol.cpp:94-119, :164) once; ref_cloud_run then replays only
+// the cloud section (protocol.cpp:121-134) with the reference's own
+// functions and returns its wall time in ms.
+struct RefCloud {
+    spmv::SimBackend be;
+    struct Slice {
+        std::vector<spmv::Ciphertext> a, b;
+        std::vector<std::size_t> r, c;
+    };
+    std::vector<Slice> slices;
+    explicit RefCloud(const spmv::HeParams& p) : be(p) {}
+};
+
+void* ref_cloud_prepare(uint64_t slot_count, uint64_t t, uint64_t rows, uint64_t cols, const int64_t* rp,
+                        const int64_t* ci, const int64_t* va, const int64_t* v, uint64_t chunk) {
+    try {
+        spmv::HeParams p;
+        p.slot_count = slot_count;
+        p.plaintext_modulus = t;
+        auto h = std::make_unique<RefCloud>(p);
+        const spmv::CsrMatrix m = make_csr(rows, cols, rp, ci, va);
+        const std::vector<int64_t> vv(v, v + cols);
+        spmv::OpLedger ops;
+        for (const spmv::CsrMatrix& slice : spmv::partition_rows(m, chunk)) {
+            const spmv::ChunkSet cs = spmv::generate_chunks(spmv::csr_to_cssc(slice), chunk);
+            const spmv::ReorgVector rv = spmv::reorg_vector(vv, cs);
+            RefCloud::Slice s;
+            for (const auto& c : cs.chunks) s.a.push_back(h->be.encrypt(h->be.encode(c.value_flat), ops));
+            for (const auto& seg : rv.segments) s.b.push_back(h->be.encrypt(h->be.encode(seg), ops));
+            s.r = cs.r_list;
+            s.c = cs.c_list;
+            h->slices.push_back(std::move(s));
+        }
+        return h.release();
+    } catch (const std::exception& e) {
+        classify(e);
+        return nullptr;
+    }
+}
+
+double ref_cloud_run(void* handle) {
+    auto* h = static_cast<RefCloud*>(handle);
+    spmv::OpLedger ops;
+    const auto t0 = std::chrono::steady_clock::now();
+    for (const auto& s : h->slices) {
+        if (s.a.empty()) continue;
+        std::vector<spmv::Ciphertext> parts;
+        parts.reserve(s.a.size());
+        for (std::size_t i = 0; i < s.a.size(); ++i) {
+            spmv::Ciphertext product = h->be.multiply(s.a[i], s.b[i], ops);
+            parts.push_back(spmv::intra_chunk_sum(h->be, product, s.r[i], s.c[i], ops));
+        }
+        spmv::Ciphertext res = spmv::inter_chunk_sum(h->be, parts, s.r, ops);
+        (void)res;
+    }
+    const auto t1 = std::chrono::steady_clock::now();
+    return std::chrono::duration<double, std::milli>(t1 - t0).count();
+}
+
+void ref_cloud_free(void* handle) { delete static_cast<RefCloud*>(handle); }
 
 }  // extern "C"

@@ -59,6 +59,10 @@ class PhaseC(C.Structure):
                 ("limb_ntts", C.c_uint64)]
 
 
+class KernelTimingC(C.Structure):
+    _fields_ = [("name", C.c_char * 48), ("group", C.c_int32), ("us", C.c_double)]
+
+
 class CsrC(C.Structure):
     _fields_ = [("rows", C.c_uint64), ("cols", C.c_uint64), ("row_ptrs", i64p),
                 ("col_indices", i64p), ("values", i64p)]
@@ -112,6 +116,8 @@ _SIGS = {
     "spmvgpu_plan_capture": (C.c_int, [C.c_void_p]),
     "spmvgpu_plan_stats_get": (C.c_int, [C.c_void_p, C.POINTER(PlanStats)]),
     "spmvgpu_plan_profile": (C.c_int, [C.c_void_p, C.POINTER(PhaseC), C.c_int, C.POINTER(C.c_int)]),
+    "spmvgpu_plan_profile_kernels": (C.c_int, [C.c_void_p, C.c_int, C.c_uint64, C.POINTER(KernelTimingC), C.c_int,
+                                               C.POINTER(C.c_int)]),
     "spmvgpu_plan_destroy": (None, [C.c_void_p]),
     "cssc_spmv_partitioned": (C.c_int, [C.c_void_p, C.POINTER(CsrC), i64p, C.c_uint64, C.c_uint64,
                                         C.c_int, i64p, C.POINTER(ResultC), C.POINTER(Message),
@@ -136,6 +142,8 @@ _SIGS = {
     "cssc_job_run": (C.c_int, [C.c_void_p, C.POINTER(i64p), C.POINTER(ResultC)]),
     "cssc_job_plan_stats": (C.c_int, [C.c_void_p, C.POINTER(PlanStats)]),
     "cssc_job_profile": (C.c_int, [C.c_void_p, C.POINTER(PhaseC), C.c_int, C.POINTER(C.c_int)]),
+    "cssc_job_profile_kernels": (C.c_int, [C.c_void_p, C.c_int, C.c_uint64, C.POINTER(KernelTimingC), C.c_int,
+                                           C.POINTER(C.c_int)]),
     "cssc_job_input_bytes": (C.c_int, [C.c_void_p, u64p, u64p]),
     "cssc_job_destroy": (None, [C.c_void_p]),
     "cssc_pack_chunks": (C.c_int64, [C.POINTER(CsrC), C.c_uint64, i64p, i64p, i64p, i64p, i64p, u64p]),
@@ -203,11 +211,15 @@ def default_params(logn: int) -> SpmvgpuParams:
 
 
 class Context:
-    """Device-resident RNS-BFV context (keys generated on the GPU from `seed`)."""
+    """Device-resident RNS-BFV context (keys generated on the GPU).  seed=None
+    (default) draws a 256-bit key from OS entropy; an integer seed gives the
+    deterministic key the CPU oracle restates (tests, known answers)."""
 
-    def __init__(self, logn: int = 14, seed: int = 1, device: int = 0, **overrides):
+    def __init__(self, logn: int = 14, seed: int | None = None, device: int = 0, **overrides):
         p = default_params(logn)
-        p.seed = seed
+        p.seed = 0 if seed is None else int(seed)
+        if seed is not None and p.seed == 0:
+            raise ValueError("seed must be nonzero (None draws the key from OS entropy)")
         p.device = device
         for k, v in overrides.items():
             setattr(p, k, v)
@@ -630,6 +642,15 @@ class Job:
         check(lib().cssc_job_profile(self.h, ph, cap, C.byref(cnt)))
         return [{"name": p.name.decode(), "us": p.us, "items": int(p.items), "bytes": int(p.bytes),
                  "limb_ntts": int(p.limb_ntts)} for p in ph[: min(cnt.value, cap)]]
+
+    def profile_kernels(self, reps: int = 5, flush_bytes: int = 256 << 20) -> list:
+        """Mean device time of every kernel launch of the cloud phase over `reps`
+        graph replays (L2 flushed before each), with its launch group index."""
+        cap = 1024
+        kt = (KernelTimingC * cap)()
+        cnt = C.c_int()
+        check(lib().cssc_job_profile_kernels(self.h, reps, flush_bytes, kt, cap, C.byref(cnt)))
+        return [{"name": k.name.decode(), "group": int(k.group), "us": k.us} for k in kt[: min(cnt.value, cap)]]
 
     def io_bytes(self):
         a, b = C.c_uint64(), C.c_uint64()

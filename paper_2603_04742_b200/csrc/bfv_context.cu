@@ -179,7 +179,7 @@ static std::vector<int> range_idx(int lo, int hi) {
 // ------------------------------------------------------------------ keys
 void GpuContext::keygen() {
     const int n = P_.n, L = P_.cfg.L, LK = L + P_.cfg.K, logn = P_.cfg.logn;
-    const u64 seed = P_.cfg.seed;
+    const SeedKey seed = P_.cfg.key;
     s_small_ = DevBuf(&pool_, sizeof(int64_t) * n);
     launch_sample_small(logn, seed, DOM_SK, 0, 0, s_small_.as<int64_t>(), st_);
     s_ntt_ = DevBuf(&pool_, sizeof(u64) * (size_t)LK * n);
@@ -207,7 +207,7 @@ void GpuContext::keygen() {
 
 DevBuf GpuContext::gen_ksk(u64 keyid, const u64* sp_ntt) {
     const int n = P_.n, L = P_.cfg.L, LK = L + P_.cfg.K, logn = P_.cfg.logn;
-    const u64 seed = P_.cfg.seed;
+    const SeedKey seed = P_.cfg.key;
     DevBuf key(&pool_, sizeof(u64) * ksk_words());
     DevBuf e_small(&pool_, sizeof(int64_t) * n), E(&pool_, sizeof(u64) * (size_t)LK * n);
     for (int d = 0; d < P_.dnum; ++d) {
@@ -438,7 +438,7 @@ void GpuContext::encrypt_cssc_forked(const unsigned char* img, const CsscLayout&
         cuda_check(cudaMemcpyAsync(d + lay.o_st, img + lay.o_st, lay.bytes - lay.o_st, cudaMemcpyHostToDevice, st_),
                    "upload");
         if (part == 1 && ws.E) cuda_check(cudaEventRecord(ev_upload_, st_), "ids uploaded");
-        launch_enc_sample_u(dc_, P_, P_.cfg.seed, streams, ws.U, items, st_);
+        launch_enc_sample_u(dc_, P_, P_.cfg.key, streams, ws.U, items, st_);
         launch_ntt_phase(dc_, logn, false, true, job(ws.U, ws.U, L, range_idx(0, L)), items, st_);
         launch_blocks_mul_inv(dc_, P_, ws.U, pk_.words(), 2, CM, (size_t)2 * L * n, nullptr, 0, 0, items, st_);
         std::vector<int> pidx = range_idx(0, L);
@@ -449,7 +449,7 @@ void GpuContext::encrypt_cssc_forked(const unsigned char* img, const CsscLayout&
         branch_a();
         if (ws.E) {
             cuda_check(cudaStreamWaitEvent(st2_, ev_upload_, 0), "ids");
-            launch_enc_sample_e(dc_, P_, P_.cfg.seed, streams, ws.E, items, st2_);
+            launch_enc_sample_e(dc_, P_, P_.cfg.key, streams, ws.E, items, st2_);
             cuda_check(cudaEventRecord(ev_join_, st2_), "join");
             cuda_check(cudaStreamWaitEvent(st_, ev_join_, 0), "join");
         }
@@ -477,12 +477,12 @@ void GpuContext::encrypt_cssc_forked(const unsigned char* img, const CsscLayout&
         cuda_check(cudaStreamWaitEvent(st_, early_ev, cudaEventWaitExternal), "join early");
     }
     if (defer) {
-        *defer = EncIn{P_.cfg.seed, streams, CM, (size_t)2 * L * n, MSG, n,
+        *defer = EncIn{P_.cfg.key, streams, CM, (size_t)2 * L * n, MSG, n,
                        reinterpret_cast<u64* const*>(d + lay.o_out), items / 2, nullptr,
                        part == 2 ? ws.E : nullptr};
         stats_.kernels += 7;
     } else {
-        launch_enc_finish(dc_, P_, P_.cfg.seed, streams, CM, reinterpret_cast<u64* const*>(d + lay.o_out), items,
+        launch_enc_finish(dc_, P_, P_.cfg.key, streams, CM, reinterpret_cast<u64* const*>(d + lay.o_out), items,
                           st_, MSG, (size_t)2 * L * n, n);
         stats_.kernels += 8;
     }
@@ -496,7 +496,7 @@ void GpuContext::encrypt_encoded(const u64* d_streams, u64* const* d_out, int it
     const int L = P_.cfg.L, logn = P_.cfg.logn;
     if (!U) U = wsU_.words();
     if (!CM) CM = wsC_.words();
-    launch_enc_sample_u(dc_, P_, P_.cfg.seed, d_streams, U, items, st_);
+    launch_enc_sample_u(dc_, P_, P_.cfg.key, d_streams, U, items, st_);
     std::vector<int> pidx = range_idx(0, L);
     pidx.insert(pidx.end(), pidx.begin(), pidx.end());
     pidx.push_back(P_.t_index());
@@ -511,7 +511,7 @@ void GpuContext::encrypt_encoded(const u64* d_streams, u64* const* d_out, int it
         launch_ntt(dc_, logn, true, job(CM, CM, 2 * L + 1, pidx), items, st_);
         stats_.kernels += 7;
     }
-    launch_enc_finish(dc_, P_, P_.cfg.seed, d_streams, CM, d_out, items, st_);
+    launch_enc_finish(dc_, P_, P_.cfg.key, d_streams, CM, d_out, items, st_);
     stats_.limb_ntts += (u64)items * (1 + 3 * L);
 }
 
@@ -603,16 +603,21 @@ void GpuContext::mul_relin_dev(const u64* const* A, const u64* const* B, u64* co
         launch_mul_extend_enc(dc_, P_, *enc, T, items, st_);
     else
         launch_mul_extend(dc_, P_, A, B, T, items, st_);
+    kmark(enc ? "k_mul_extend_enc" : "k_mul_extend_k", st_);
     if (fused_ks_) {  // column phase, fused blocks + tensor + inverse blocks, column phase
         launch_ntt_phase(dc_, logn, false, true, job(T, T, 4 * M, pm), items, st_);
+        kmark("k_ntt_cols fwd (multiply)", st_);
         launch_mul_blocks_tensor(dc_, P_, T, Z, items, st_);
+        kmark("k_mul_blocks_tensor", st_);
         launch_ntt_phase(dc_, logn, true, true, job(Z, Z, 3 * M, pm), items, st_);
+        kmark("k_ntt_cols inv (multiply)", st_);
     } else {
         launch_ntt(dc_, logn, false, job(T, T, 4 * M, pm), items, st_);
         launch_mul_tensor(dc_, P_, T, Z, items, st_);
         launch_ntt(dc_, logn, true, job(Z, Z, 3 * M, pm), items, st_);
     }
     launch_mul_scale(dc_, P_, Z, OUT, D2, items, st_, fused_ks_ ? D2Y : nullptr);
+    kmark("k_mul_scale_k", st_);
     if (fused_ks_) {
         KsY ky;
         ky.srcc = D2Y;

@@ -95,11 +95,20 @@ public:
     size_t ct_words() const { return (size_t)2 * P_.cfg.L * P_.n; }
     size_t ksk_words() const { return (size_t)P_.dnum * 2 * (P_.cfg.L + P_.cfg.K) * P_.n; }
     uint64_t next_stream_id() { return stream_counter_.fetch_add(1); }
+    // first stream id the counter hands out (ids name the encryption
+    // randomness under the context key: two contexts sharing a key must use
+    // disjoint id ranges)
+    void set_stream_base(uint64_t b) { stream_counter_.store(b); }
     LaunchStats& stats() { return stats_; }
     // fused 3-kernel key switch (default) or the 7-launch reference pipeline
     void set_fused_key_switch(bool on) { fused_ks_ = on; }
     bool fused_key_switch() const { return fused_ks_; }
     void set_forked_encrypt(bool on) { forked_enc_ = on; }
+    // whole-evaluation graph fusions across the party boundary (bit 0: the
+    // encryption's finish inside the multiply's extension, bit 1: the
+    // decryption inside the mask step); 0 = party-separated (default)
+    void set_pipe_fuse(int mask) { pipe_fuse_ = mask & 3; }
+    int pipe_fuse() const { return pipe_fuse_; }
 
     // keys (NTT form on device)
     const u64* relin_key() const { return rlk_.words(); }
@@ -219,6 +228,7 @@ private:
     LaunchStats stats_;
     bool fused_ks_ = true;
     bool forked_enc_ = false;
+    int pipe_fuse_ = 0;
     // workspaces for ad-hoc batched calls
     DevBuf wsT_, wsZ_, wsD2_, wsDX_, wsACC_, wsM_, wsX_, wsU_, wsC_, wsPT_;
     DevBuf scratch_[8];

@@ -6,6 +6,8 @@
 // Formulas E1..E5 refer to DESIGN.md "Arithmetic spec"; the CPU oracle
 // (oracle/bfv_oracle.c) states the same integer formulas.
 #include <cstdio>
+#include <map>
+#include <mutex>
 #include <type_traits>
 #include <cstdlib>
 #include <stdexcept>
@@ -31,7 +33,7 @@ __device__ __forceinline__ void add128(u64& hi, u64& lo, u64 xhi, u64 xlo) {
 }
 
 // ---------------------------------------------------------------------------
-// ChaCha20 block (RFC 8439 2.3); key = (seed_lo, seed_hi, fixed words)
+// ChaCha20 block (RFC 8439 2.3); key = the context's SeedKey (rns_params.hpp)
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ u32 rotl32(u32 v, int n) { return __funnelshift_l(v, v, n); }
 
@@ -41,10 +43,10 @@ __device__ __forceinline__ u32 rotl32(u32 v, int n) { return __funnelshift_l(v, 
     a += b; d ^= a; d = rotl32(d, 8);               \
     c += d; b ^= c; b = rotl32(b, 7);
 
-__device__ void chacha20_block(u64 seed, u32 ctr, u32 n0, u32 n1, u32 n2, u32 out[16]) {
+__device__ void chacha20_block(const SeedKey& seed, u32 ctr, u32 n0, u32 n1, u32 n2, u32 out[16]) {
     const u32 s[16] = {0x61707865u, 0x3320646eu, 0x79622d32u, 0x6b206574u,
-                       (u32)seed,   (u32)(seed >> 32), 0x63737363u, 0x2d68652du,
-                       0x62323030u, 0x2d707267u, 0x6b657973u, 0x00000001u,
+                       seed.w[0],   seed.w[1],   seed.w[2],   seed.w[3],
+                       seed.w[4],   seed.w[5],   seed.w[6],   seed.w[7],
                        ctr,         n0,          n1,          n2};
     u32 x[16];
 #pragma unroll
@@ -68,11 +70,11 @@ __device__ void chacha20_block(u64 seed, u32 ctr, u32 n0, u32 n1, u32 n2, u32 ou
 // (lane i holds x[i], x[4+i], x[8+i], x[12+i]); diagonal rounds rotate rows
 // b, c, d across the group with shuffles.  Lane i stores words i, 4+i, 8+i,
 // 12+i of the output block.
-__device__ __forceinline__ void chacha20_block_x4(u64 seed, u32 ctr, u32 n0, u32 n1, u32 n2, u32* out) {
+__device__ __forceinline__ void chacha20_block_x4(const SeedKey& seed, u32 ctr, u32 n0, u32 n1, u32 n2, u32* out) {
     const int i = threadIdx.x & 3;
     const u32 sa = i == 0 ? 0x61707865u : i == 1 ? 0x3320646eu : i == 2 ? 0x79622d32u : 0x6b206574u;
-    const u32 sb = i == 0 ? (u32)seed : i == 1 ? (u32)(seed >> 32) : i == 2 ? 0x63737363u : 0x2d68652du;
-    const u32 sc = i == 0 ? 0x62323030u : i == 1 ? 0x2d707267u : i == 2 ? 0x6b657973u : 0x00000001u;
+    const u32 sb = i == 0 ? seed.w[0] : i == 1 ? seed.w[1] : i == 2 ? seed.w[2] : seed.w[3];
+    const u32 sc = i == 0 ? seed.w[4] : i == 1 ? seed.w[5] : i == 2 ? seed.w[6] : seed.w[7];
     const u32 sd = i == 0 ? ctr : i == 1 ? n0 : i == 2 ? n1 : n2;
     u32 a = sa, b = sb, c = sc, d = sd;
     const unsigned full = 0xffffffffu;
@@ -319,18 +321,36 @@ static void launch_blocks(const DevConsts* dc, const NttJob& job, int items, cud
 
 size_t ntt_smem_bytes(int logn) { return (size_t)8 << logn; }
 
+void smem_optin(const void* fn, int bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, int> done;  // (kernel, device) -> bytes opted in
+    int dev = 0;
+    cuda_check(cudaGetDevice(&dev), "get device");
+    std::lock_guard<std::mutex> lk(mu);
+    int& have = done[{fn, dev}];
+    if (bytes <= have) return;
+    cuda_check(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes), "smem opt-in");
+    have = bytes;
+}
+
+static thread_local std::vector<KernelMark>* g_kmarks = nullptr;
+void kmarks_install(std::vector<KernelMark>* marks) { g_kmarks = marks; }
+void kmark(const char* name, cudaStream_t st) {
+    if (!g_kmarks) return;
+    cudaEvent_t e;
+    cuda_check(cudaEventCreate(&e), "event");
+    cuda_check(cudaEventRecordWithFlags(e, st, cudaEventRecordExternal), "event record");
+    g_kmarks->push_back({name, e});
+}
+
 template <int LOGN>
 static void launch_ntt_t(const DevConsts* dc, bool inv, const NttJob& job, int items,
                          cudaStream_t st) {
     using G = Ntt2<LOGN>;
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(k_ntt_cols<LOGN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM_C);
-        cudaFuncSetAttribute(k_ntt_cols<LOGN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM_C);
-        cudaFuncSetAttribute(k_ntt_blocks<LOGN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM_B);
-        cudaFuncSetAttribute(k_ntt_blocks<LOGN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM_B);
-        configured = true;
-    }
+    smem_optin_k(k_ntt_cols<LOGN, false>, G::SMEM_C);
+    smem_optin_k(k_ntt_cols<LOGN, true>, G::SMEM_C);
+    smem_optin_k(k_ntt_blocks<LOGN, false>, G::SMEM_B);
+    smem_optin_k(k_ntt_blocks<LOGN, true>, G::SMEM_B);
     const int limbs = items * job.limbs;
     if (limbs == 0) return;
     if (!inv) {
@@ -1336,7 +1356,7 @@ void launch_plain_lift(const DevConsts* dc, const RnsParams& P, const u64* M, u6
 
 // U[item][L][N]: a 128-thread CTA draws 32 ChaCha blocks (4 lanes each) =
 // 256 coefficients of u into smem, then writes them coalesced per limb
-__global__ void __launch_bounds__(128) k_enc_sample_u(const DevConsts* __restrict__ dc, u64 seed,
+__global__ void __launch_bounds__(128) k_enc_sample_u(const DevConsts* __restrict__ dc, SeedKey seed,
                                                       const u64* streams, u64* U) {
     __shared__ u32 blk[32][16];
     const int n = dc->n, L = dc->L;
@@ -1354,7 +1374,7 @@ __global__ void __launch_bounds__(128) k_enc_sample_u(const DevConsts* __restric
     }
 }
 
-void launch_enc_sample_u(const DevConsts* dc, const RnsParams& P, u64 seed, const u64* streams,
+void launch_enc_sample_u(const DevConsts* dc, const RnsParams& P, SeedKey seed, const u64* streams,
                          u64* U, int items, cudaStream_t st) {
     if (!items) return;
     k_enc_sample_u<<<dim3((unsigned)(P.n / 256), (unsigned)items), 128, 0, st>>>(dc, seed, streams, U);
@@ -1385,7 +1405,7 @@ void launch_enc_pk(const DevConsts* dc, const RnsParams& P, const u64* PK, const
 // OUT = C + (e0 + Delta m, e1): a 128-thread CTA draws the 16 + 16 ChaCha
 // blocks of its 128 coefficients (4 lanes per block), then one thread per
 // coefficient finishes every limb with coalesced loads and stores
-__global__ void __launch_bounds__(128) k_enc_finish(const DevConsts* __restrict__ dc, u64 seed,
+__global__ void __launch_bounds__(128) k_enc_finish(const DevConsts* __restrict__ dc, SeedKey seed,
                                                     const u64* streams, const u64* C, size_t cstride,
                                                     const u64* MSG, size_t mstride, u64* const* OUT) {
     __shared__ u32 blk[32][16];
@@ -1415,7 +1435,7 @@ __global__ void __launch_bounds__(128) k_enc_finish(const DevConsts* __restrict_
 
 // the e draws of k_enc_finish / k_mul_extend_enc, ahead of time: one CTA per
 // 128 coefficients of one polynomial of one item
-__global__ void __launch_bounds__(128) k_enc_sample_e(u64 seed, const u64* streams, int8_t* E, int n) {
+__global__ void __launch_bounds__(128) k_enc_sample_e(SeedKey seed, const u64* streams, int8_t* E, int n) {
     __shared__ u32 blk[16][16];
     const int item = blockIdx.y, poly = blockIdx.z;
     const u64 id = streams[item];
@@ -1428,7 +1448,7 @@ __global__ void __launch_bounds__(128) k_enc_sample_e(u64 seed, const u64* strea
     E[((size_t)item * 2 + poly) * n + k] = (int8_t)cbd_of(word64(blk[kk >> 3], kk & 7));
 }
 
-void launch_enc_sample_e(const DevConsts* dc, const RnsParams& P, u64 seed, const u64* streams, int8_t* E,
+void launch_enc_sample_e(const DevConsts* dc, const RnsParams& P, SeedKey seed, const u64* streams, int8_t* E,
                          int items, cudaStream_t st) {
     (void)dc;
     if (!items) return;
@@ -1436,7 +1456,7 @@ void launch_enc_sample_e(const DevConsts* dc, const RnsParams& P, u64 seed, cons
     CSSC_CHECK_LAUNCH();
 }
 
-void launch_enc_finish(const DevConsts* dc, const RnsParams& P, u64 seed, const u64* streams,
+void launch_enc_finish(const DevConsts* dc, const RnsParams& P, SeedKey seed, const u64* streams,
                        const u64* CM, u64* const* OUT, int items, cudaStream_t st, const u64* MSG, size_t cstride,
                        size_t mstride) {
     if (!items) return;
@@ -1579,14 +1599,8 @@ static void dec_ntt_t(const DevConsts* dc, const RnsParams& P, u64* D, u64* M, u
     // 2-column tiles unless 8-column tiles already give one CTA per SM: the
     // per-coefficient scaling dominates, and a single result has only R2
     // columns
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(k_dec_cols<LOGN, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (8 * G::R1 + 2 * G::R1) * 8);
-        cudaFuncSetAttribute(k_dec_cols<LOGN, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (2 * G::R1 + 2 * G::R1) * 8);
-        configured = true;
-    }
+    smem_optin_k(k_dec_cols<LOGN, 8>, (8 * G::R1 + 2 * G::R1) * 8);
+    smem_optin_k(k_dec_cols<LOGN, 2>, (2 * G::R1 + 2 * G::R1) * 8);
     if ((long)items * (G::R2 / 8) >= 148)
         k_dec_cols<LOGN, 8><<<items * (G::R2 / 8), G::TC, (8 * G::R1 + 2 * G::R1) * 8, st>>>(dc, D, M, maxdev);
     else
@@ -1652,7 +1666,7 @@ void launch_decode_gather(const DevConsts* dc, const RnsParams& P, const u64* M,
 // ---------------------------------------------------------------------------
 // key generation helpers
 // ---------------------------------------------------------------------------
-__global__ void k_sample_small(int n, u64 seed, u32 n0, u64 id, int kind, int64_t* out) {
+__global__ void k_sample_small(int n, SeedKey seed, u32 n0, u64 id, int kind, int64_t* out) {
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= n / 8) return;
     u32 blk[16];
@@ -1663,7 +1677,7 @@ __global__ void k_sample_small(int n, u64 seed, u32 n0, u64 id, int kind, int64_
     }
 }
 
-void launch_sample_small(int logn, u64 seed, u32 dom, u64 id, int kind, int64_t* out,
+void launch_sample_small(int logn, SeedKey seed, u32 dom, u64 id, int kind, int64_t* out,
                          cudaStream_t st) {
     const int n = 1 << logn;
     k_sample_small<<<(n / 8 + 63) / 64, 64, 0, st>>>(n, seed, dom, id, kind, out);
@@ -1671,7 +1685,7 @@ void launch_sample_small(int logn, u64 seed, u32 dom, u64 id, int kind, int64_t*
 }
 
 // uniform residues for limbs [limb0, limb0+limbs): coefficient k uses words 2k, 2k+1
-__global__ void k_sample_uniform(const DevConsts* __restrict__ dc, u64 seed, u32 dom, int digit,
+__global__ void k_sample_uniform(const DevConsts* __restrict__ dc, SeedKey seed, u32 dom, int digit,
                                  u64 id, int limb0, u64* out) {
     const int n = dc->n;
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1688,7 +1702,7 @@ __global__ void k_sample_uniform(const DevConsts* __restrict__ dc, u64 seed, u32
     }
 }
 
-void launch_sample_uniform(const DevConsts* dc, int logn, u64 seed, u32 dom, int digit, u64 id,
+void launch_sample_uniform(const DevConsts* dc, int logn, SeedKey seed, u32 dom, int digit, u64 id,
                            int limbs, int limb0, u64* out, cudaStream_t st) {
     const int n = 1 << logn;
     k_sample_uniform<<<dim3((unsigned)((n / 4 + 63) / 64), (unsigned)limbs), 64, 0, st>>>(

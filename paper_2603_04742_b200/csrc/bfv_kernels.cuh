@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <vector>
 
 #include "rns_params.hpp"
 
@@ -37,6 +38,27 @@ enum SampleDomain : u32 {
     DOM_ENC_E1 = 8,
 };
 
+void cuda_check(cudaError_t e, const char* what);
+
+// Opt kernel `fn` into `bytes` of dynamic shared memory on the CURRENT device.
+// The attribute is per device, so the record is keyed by (kernel, device) and
+// guarded by a mutex (several contexts / devices / threads in one process).
+void smem_optin(const void* fn, int bytes);
+template <class F>
+inline void smem_optin_k(F* fn, int bytes) {
+    smem_optin(reinterpret_cast<const void*>(fn), bytes);
+}
+
+// Kernel-level timing marks (bench.py's per-kernel profile): when a mark list
+// is installed for this thread, every launch site records an external event
+// labelled with its kernel after the launch (an event node under capture).
+struct KernelMark {
+    const char* name;
+    cudaEvent_t ev;
+};
+void kmarks_install(std::vector<KernelMark>* marks);  // nullptr: off
+void kmark(const char* name, cudaStream_t st);
+
 // column-tile width policy shared by the column-phase kernels (ctas16 = CTAs at 16 columns)
 bool cols_use_ln8(long ctas16, bool allowed);
 bool cols_use_ln4(long ctas16, bool allowed);
@@ -62,7 +84,7 @@ struct KsY {
 };
 
 struct EncIn {
-    u64 seed;
+    SeedKey seed;
     const u64* streams;  // per encryption item (a chunks, then b chunks)
     const u64* CM;       // pk u after the inverse NTT, [item][2L][N] (cstride words apart)
     size_t cstride;
@@ -137,16 +159,16 @@ void launch_encode_scatter(const DevConsts* dc, const RnsParams& P, const int64_
 void launch_plain_lift(const DevConsts* dc, const RnsParams& P, const u64* M, u64* PT, int items,
                        cudaStream_t st);
 // E[item][poly][N] = the CBD e draws of k_enc_finish (|e| <= 21, as int8)
-void launch_enc_sample_e(const DevConsts* dc, const RnsParams& P, u64 seed, const u64* streams, int8_t* E,
+void launch_enc_sample_e(const DevConsts* dc, const RnsParams& P, SeedKey seed, const u64* streams, int8_t* E,
                          int items, cudaStream_t st);
-void launch_enc_sample_u(const DevConsts* dc, const RnsParams& P, u64 seed, const u64* streams,
+void launch_enc_sample_u(const DevConsts* dc, const RnsParams& P, SeedKey seed, const u64* streams,
                          u64* U, int items, cudaStream_t st);
 void launch_enc_pk(const DevConsts* dc, const RnsParams& P, const u64* PK, const u64* U, u64* C,
                    int items, cudaStream_t st);
 // CM[item][2L+1][N]: c0 (L limbs), c1 (L limbs), then the message (coef form mod t);
 // or, with MSG set, CM items cstride words apart and the messages in MSG
 // (mstride words apart)
-void launch_enc_finish(const DevConsts* dc, const RnsParams& P, u64 seed, const u64* streams,
+void launch_enc_finish(const DevConsts* dc, const RnsParams& P, SeedKey seed, const u64* streams,
                        const u64* CM, u64* const* OUT, int items, cudaStream_t st, const u64* MSG = nullptr,
                        size_t cstride = 0, size_t mstride = 0);
 void launch_mul_s(const DevConsts* dc, const RnsParams& P, u64* X, const u64* S_NTT, int items,
@@ -161,9 +183,9 @@ void launch_decode_gather(const DevConsts* dc, const RnsParams& P, const u64* M,
                           int items, cudaStream_t st);
 
 // keys
-void launch_sample_small(int logn, u64 seed, u32 dom, u64 id, int kind /*0 ternary,1 cbd*/,
+void launch_sample_small(int logn, SeedKey seed, u32 dom, u64 id, int kind /*0 ternary,1 cbd*/,
                          int64_t* out, cudaStream_t st);
-void launch_sample_uniform(const DevConsts* dc, int logn, u64 seed, u32 dom, int digit, u64 id,
+void launch_sample_uniform(const DevConsts* dc, int logn, SeedKey seed, u32 dom, int digit, u64 id,
                            int limbs, int limb0, u64* out, cudaStream_t st);
 void launch_lift_small(const DevConsts* dc, int logn, const int64_t* s, int limbs, int limb0,
                        u64* out, cudaStream_t st);

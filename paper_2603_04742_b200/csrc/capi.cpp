@@ -13,6 +13,8 @@
 #include <stdexcept>
 #include <string>
 
+#include <sys/random.h>
+
 #include "bfv_context.hpp"
 #include "cloud_plan.hpp"
 #include "host/batched_spmv.hpp"
@@ -417,7 +419,7 @@ void spmvgpu_default_params(int logn, spmvgpu_params* p) {
         p->L = 8, p->K = 4, p->alpha = 4, p->qbits = 58, p->pbits = 58;
     }
     p->t = 65537;
-    p->seed = 1;
+    p->seed = 0;  // 0: 256-bit ChaCha key + stream-id base from OS entropy
     p->device = 0;
     p->ciphertext_size_mb = 0.52;
     p->noise_initial = 146;
@@ -439,6 +441,21 @@ int spmvgpu_ctx_create(const spmvgpu_params* p, spmvgpu_ctx** out) {
         cfg.pbits = p->pbits;
         cfg.t = p->t;
         cfg.seed = p->seed;
+        uint64_t stream_base = 1;
+        if (p->seed) {  // deterministic key (tests, KATs; oracle/bfv_oracle.c restates it)
+            cfg.key = cssc::seed_key(p->seed);
+        } else {  // production default: 256-bit key and a random stream-id base
+            unsigned char rnd[40];
+            size_t got = 0;
+            while (got < sizeof rnd) {
+                const ssize_t r = getrandom(rnd + got, sizeof rnd - got, 0);
+                if (r <= 0) throw std::runtime_error("getrandom failed: no OS entropy for the key");
+                got += static_cast<size_t>(r);
+            }
+            std::memcpy(cfg.key.w, rnd, 32);
+            std::memcpy(&stream_base, rnd + 32, 8);
+            stream_base = (stream_base >> 2) | 1;  // leave headroom below 2^64
+        }
         auto c = std::make_unique<spmvgpu_ctx>();
         c->p = *p;
         c->hp.slot_count = (size_t)1 << (p->logn - 1);
@@ -447,6 +464,7 @@ int spmvgpu_ctx_create(const spmvgpu_params* p, spmvgpu_ctx** out) {
         c->hp.noise = {p->noise_initial, p->noise_ct_ct, p->noise_ct_pt, p->noise_add, p->noise_rot};
         c->hp.validate();
         c->g = std::make_unique<cssc::GpuContext>(cfg, p->device);
+        c->g->set_stream_base(stream_base);
         *out = c.release();
     });
 }
@@ -482,6 +500,18 @@ int spmvgpu_set_option(spmvgpu_ctx* c, const char* name, int64_t value) {
             G(c).set_fused_key_switch(value != 0);
         } else if (n == "forked_encrypt") {
             G(c).set_forked_encrypt(value != 0);
+        } else if (n == "pipeline_fuse") {
+            if (value < 0 || value > 3) throw std::invalid_argument("pipeline_fuse: 0..3");
+            G(c).set_pipe_fuse(static_cast<int>(value));
+            std::list<spmv::detail::PlanLease> evicted;  // cached graphs bake the old choice in
+            {
+                std::lock_guard<std::mutex> g(c->plans_mu);
+                evicted.splice(evicted.end(), c->plans);
+            }
+            for (auto& l : evicted) spmv::detail::plan_lease_free(c, l);
+        } else if (n == "stream_base") {
+            if (value <= 0) throw std::invalid_argument("stream_base: must be positive");
+            G(c).set_stream_base(static_cast<uint64_t>(value));
         } else if (n == "plan_cache") {
             if (value < 0) throw std::invalid_argument("plan_cache: capacity must be >= 0");
             std::list<spmv::detail::PlanLease> evicted;
@@ -787,6 +817,20 @@ int spmvgpu_plan_profile(spmvgpu_plan* p, spmvgpu_phase* phases, int cap, int* c
         }
     });
 }
+int spmvgpu_plan_profile_kernels(spmvgpu_plan* p, int reps, uint64_t flush_bytes, spmvgpu_kernel_timing* out,
+                                 int cap, int* count) {
+    return guard([&] { auto lk_ = api_lock(p ? p->ctx : nullptr);
+        if (!p || !count) throw std::invalid_argument("null argument");
+        const auto kt = p->plan->profile_kernels(reps, flush_bytes);
+        *count = (int)kt.size();
+        for (int i = 0; i < (int)kt.size() && i < cap; ++i) {
+            std::memset(&out[i], 0, sizeof out[i]);
+            std::strncpy(out[i].name, kt[i].name.c_str(), sizeof out[i].name - 1);
+            out[i].group = kt[i].group;
+            out[i].us = kt[i].us;
+        }
+    });
+}
 void spmvgpu_plan_destroy(spmvgpu_plan* p) { delete p; }
 
 // ---------------------------------------------------------------- protocol front door
@@ -918,6 +962,14 @@ int cssc_job_profile(cssc_job* j, spmvgpu_phase* phases, int cap, int* count) {
     return guard([&] { auto lk_ = api_lock(j ? j->ctx : nullptr);
         if (!j || !j->job->plan()) throw std::invalid_argument("job has no plan yet (run cloud first)");
         const int st = spmvgpu_plan_profile(j->job->plan(), phases, cap, count);
+        if (st != SPMVGPU_OK) throw std::runtime_error(g_err);
+    });
+}
+int cssc_job_profile_kernels(cssc_job* j, int reps, uint64_t flush_bytes, spmvgpu_kernel_timing* out, int cap,
+                             int* count) {
+    return guard([&] { auto lk_ = api_lock(j ? j->ctx : nullptr);
+        if (!j || !j->job->plan()) throw std::invalid_argument("job has no plan yet (run cloud first)");
+        const int st = spmvgpu_plan_profile_kernels(j->job->plan(), reps, flush_bytes, out, cap, count);
         if (st != SPMVGPU_OK) throw std::runtime_error(g_err);
     });
 }

@@ -316,6 +316,7 @@ void CloudPlan::record(std::vector<cudaEvent_t>* marks, u64* dec_d, const EncIn*
     const int L = P.cfg.L, logn = P.cfg.logn;
     cudaStream_t st = ctx_.stream();
     auto mark = [&] {
+        kmark("@group", st);
         if (!marks) return;
         cudaEvent_t e;
         cuda_check(cudaEventCreate(&e), "event");
@@ -348,9 +349,12 @@ void CloudPlan::record(std::vector<cudaEvent_t>* marks, u64* dec_d, const EncIn*
                                MASKS_.words(), ctx_.s_ntt(), dec_d, ns_, st);
     } else if (ctx_.fused_key_switch()) {  // column phase, fused blocks + mask MAC + inverse blocks, column phase
         launch_ntt_phase(ctx_.dconsts(), logn, false, true, fwd, n_, st);
+        kmark("k_ntt_cols fwd (mask)", st);
         launch_mask_blocks(ctx_.dconsts(), P, MT_.words(), slice_off_, slice_items_, item_mask_, MASKS_.words(),
                            OUT_, ns_, st);
+        kmark("k_mask_blocks", st);
         launch_ntt_phase(ctx_.dconsts(), logn, true, true, inv, ns_, st);
+        kmark("k_ntt_cols inv (mask)", st);
     } else {
         launch_ntt(ctx_.dconsts(), logn, false, fwd, n_, st);
         u64* RES = T_.words();  // ns <= n results fit the multiply workspace
@@ -417,6 +421,61 @@ std::vector<PhaseTiming> CloudPlan::profile() {
         out[i].us = 1e3 * ms;
     }
     for (auto e : marks) cudaEventDestroy(e);
+    return out;
+}
+
+std::vector<KernelTiming> CloudPlan::profile_kernels(int reps, size_t flush_bytes) {
+    std::vector<KernelTiming> out;
+    if (n_ == 0 || reps < 1) return out;
+    cudaStream_t st = ctx_.stream();
+    std::vector<KernelMark> km;
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t ex = nullptr;
+    auto cleanup = [&] {
+        kmarks_install(nullptr);
+        if (ex) cudaGraphExecDestroy(ex);
+        if (g) cudaGraphDestroy(g);
+        for (auto& m : km) cudaEventDestroy(m.ev);
+    };
+    try {
+        DevBuf flush(&ctx_.pool(), flush_bytes ? flush_bytes : 8);
+        kmarks_install(&km);
+        cuda_check(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "begin capture");
+        try {
+            record();
+        } catch (...) {
+            cudaGraph_t tmp = nullptr;
+            cudaStreamEndCapture(st, &tmp);
+            if (tmp) cudaGraphDestroy(tmp);
+            throw;
+        }
+        kmarks_install(nullptr);
+        cuda_check(cudaStreamEndCapture(st, &g), "end capture");
+        cuda_check(cudaGraphInstantiate(&ex, g, 0), "graph instantiate");
+        cuda_check(cudaGraphUpload(ex, st), "graph upload");
+        int group = 0;
+        for (size_t i = 1; i < km.size(); ++i) {
+            if (std::strcmp(km[i].name, "@group") == 0)
+                ++group;
+            else
+                out.push_back({km[i].name, group, 0.0});
+        }
+        for (int r = 0; r < reps; ++r) {
+            if (flush_bytes) cuda_check(cudaMemsetAsync(flush.words(), r & 0xff, flush_bytes, st), "flush");
+            cuda_check(cudaGraphLaunch(ex, st), "graph launch");
+            cuda_check(cudaStreamSynchronize(st), "profile kernels");
+            size_t k = 0;
+            for (size_t i = 1; i < km.size(); ++i) {
+                float ms = 0;
+                cuda_check(cudaEventElapsedTime(&ms, km[i - 1].ev, km[i].ev), "profile event timing");
+                if (std::strcmp(km[i].name, "@group") != 0) out[k++].us += 1e3 * ms / reps;
+            }
+        }
+    } catch (...) {
+        cleanup();
+        throw;
+    }
+    cleanup();
     return out;
 }
 
@@ -524,10 +583,7 @@ void CloudPlan::capture_pipeline(const unsigned char* img, const CsscLayout& lay
         mark();
         // fused path: the encryption's finish rides in the multiply's base
         // extension, the decryption in the mask step (k_mask_dec_blocks)
-        static const int fuse_mask = [] {  // debugging aid: bit 0 encryption finish, bit 1 decryption
-            const char* e = std::getenv("CSSC_PIPE_FUSE");
-            return e ? std::atoi(e) : 3;
-        }();
+        const int fuse_mask = ctx_.pipe_fuse();  // bit 0 encryption finish, bit 1 decryption
         const bool fused = ctx_.fused_key_switch() && fixed_rns_shape(P);
         const bool fenc = fused && (fuse_mask & 1), fdec = fused && (fuse_mask & 2);
         EncIn enc{};

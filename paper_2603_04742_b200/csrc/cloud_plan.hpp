@@ -38,6 +38,13 @@ struct PhaseTiming {
     uint64_t items = 0, bytes = 0, limb_ntts = 0;  // compulsory HBM bytes, limb NTTs
 };
 
+// one kernel launch of the plan, timed by profile_kernels()
+struct KernelTiming {
+    std::string name;
+    int group = 0;  // index into profile()'s launch groups
+    double us = 0;  // mean over the replays
+};
+
 class CloudPlan {
 public:
     // a/b: per-chunk input ciphertexts; out: one result ciphertext per slice
@@ -50,6 +57,9 @@ public:
     // one graph replay with event nodes between launch groups (multiply+relin,
     // each rotate level, the level-0 add, the mask accumulation)
     std::vector<PhaseTiming> profile();
+    // `reps` graph replays with an event node after every kernel launch; L2 is
+    // flushed (a `flush_bytes` device memset) before each replay
+    std::vector<KernelTiming> profile_kernels(int reps, size_t flush_bytes);
     // The whole evaluation as one graph: upload of the client image `img`
     // (pinned, fixed address), device pack + encryption into the plan's input
     // ciphertexts, the cloud plan, decryption of the results and the download

@@ -203,14 +203,11 @@ static bool ks_cluster_t(const DevConsts* dc, const u64* const* SRC, const u64* 
     if constexpr (LT == 0 || C::CL < 2 || C::CL > 8 || (C::RB * Ntt2<LOGN>::R2) % C::T != 0) {
         return false;
     } else {
-        static bool configured = false;
-        if (!configured) {
-            if (cudaFuncSetAttribute(k_ks_cluster<LOGN, LT, KT, AT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     C::SMEM) != cudaSuccess) {
-                cudaGetLastError();
-                return false;
-            }
-            configured = true;
+        try {
+            smem_optin_k(k_ks_cluster<LOGN, LT, KT, AT>, C::SMEM);
+        } catch (const std::exception&) {
+            cudaGetLastError();
+            return false;
         }
         const int LK = LT + KT;
         k_ks_cluster<LOGN, LT, KT, AT><<<items * LK * C::CL, C::T, C::SMEM, st>>>(dc, SRC, SRCC, src_poly, ginv, KEY,

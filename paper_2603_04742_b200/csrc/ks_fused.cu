@@ -284,14 +284,9 @@ static void ks_fused_t(const DevConsts* dc, const RnsParams& P, const u64* const
         ((dnum < 2 ? 2 : dnum) * 8 * G::PITCH + 2 * btw_entries<LOGN, 8>() + KTM * dnum * 2 * 8 * G::R2) * 8 + 16;
     if (smem2 > 200 * 1024)
         throw std::invalid_argument("key switch: too many digits for the fused kernel; set fused_key_switch 0");
-    static int configured = 0;  // largest K2 smem set so far (the generic shape's dnum varies)
-    if (smem2 > configured) {
-        cudaFuncSetAttribute(k_ks_modup_cols<LOGN, LT, KT, AT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem1);
-        cudaFuncSetAttribute(k_ks_blocks_inner<LOGN, LT, KT, AT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
-        cudaFuncSetAttribute(k_ks_blocks_inner<LOGN, LT, KT, AT, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             smem2h);
-        configured = smem2;
-    }
+    smem_optin_k(k_ks_modup_cols<LOGN, LT, KT, AT>, smem1);
+    smem_optin_k(k_ks_blocks_inner<LOGN, LT, KT, AT>, smem2);
+    smem_optin_k(k_ks_blocks_inner<LOGN, LT, KT, AT, 8>, smem2h);
     if (cols_use_ln4((long)items * dnum * LK * G::CTAS_C, G::R1 >= G::TC)) {  // 4-column tiles
         constexpr int LN = 4;
         k_ks_modup_cols<LOGN, LT, KT, AT, LN><<<items * dnum * LK * (G::R2 / LN), G::TC,
@@ -306,19 +301,23 @@ static void ks_fused_t(const DevConsts* dc, const RnsParams& P, const u64* const
                                                                                           ky.srcc);
     }
     KS_CHECK();
+    kmark("k_ks_modup_cols (K1)", st);
     constexpr int T2 = kKsGroups * kKsGroupThreads;
     if (blocks_use_ln8((long)items * LK * G::CTAS_B) && 8 * G::R2 >= T2)  // small launch: 8-block tiles
         k_ks_blocks_inner<LOGN, LT, KT, AT, 8><<<items * LK * (G::R1 / 8), T2, smem2h, st>>>(dc, DX, KEY, ACC);
     else
         k_ks_blocks_inner<LOGN, LT, KT, AT><<<items * LK * G::CTAS_B, T2, smem2, st>>>(dc, DX, KEY, ACC);
     KS_CHECK();
+    kmark("k_ks_blocks_inner (K2)", st);
     NttJob j;
     for (int i = 0; i < MAX_JOB_LIMBS; ++i) j.pidx[i] = (signed char)(i % LK);
     j.src = ACC;
     j.dst = ACC;
     j.limbs = 2 * LK;
     launch_ntt_phase(dc, LOGN, /*inverse=*/true, /*cols=*/true, j, items, st);
+    kmark("k_ntt_cols inv (key switch)", st);
     launch_ks_moddown(dc, P, ACC, BASE, RSRC, ginv, OUT, items, st, EXTRA, PAIR, ky.out);
+    kmark("k_ks_moddown_k", st);
 }
 
 template <int LOGN>

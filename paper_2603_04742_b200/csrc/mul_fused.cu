@@ -300,12 +300,8 @@ static void maskdec_t(const DevConsts* dc, const RnsParams& P, const u64* MT, co
     using G = Ntt2<LOGN>;
     const int smem = (8 * G::LINES * G::PITCH + 2 * G::TWB) * 8;
     const int smemh = (8 * 8 * G::PITCH + 2 * btw_entries<LOGN, 8>()) * 8;
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(k_mask_dec_blocks<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        cudaFuncSetAttribute(k_mask_dec_blocks<LOGN, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smemh);
-        configured = true;
-    }
+    smem_optin_k(k_mask_dec_blocks<LOGN>, smem);
+    smem_optin_k(k_mask_dec_blocks<LOGN, 8>, smemh);
     if (blocks_use_ln8((long)slices * P.cfg.L * G::CTAS_B) && 8 * G::R2 >= 4 * kGroupThreads)  // small: 8-block tiles
         k_mask_dec_blocks<LOGN, 8><<<slices * P.cfg.L * (G::R1 / 8), 4 * kGroupThreads, smemh, st>>>(
             dc, MT, slice_off, slice_items, item_mask, MASKS, S_NTT, D);
@@ -338,12 +334,8 @@ static void maskb_t(const DevConsts* dc, const RnsParams& P, const u64* MT, cons
     using G = Ntt2<LOGN>;
     const int smem = (4 * G::LINES * G::PITCH + 2 * G::TWB) * 8;
     const int smemh = (4 * 8 * G::PITCH + 2 * btw_entries<LOGN, 8>()) * 8;
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(k_mask_blocks<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        cudaFuncSetAttribute(k_mask_blocks<LOGN, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smemh);
-        configured = true;
-    }
+    smem_optin_k(k_mask_blocks<LOGN>, smem);
+    smem_optin_k(k_mask_blocks<LOGN, 8>, smemh);
     if (blocks_use_ln8((long)slices * 2 * P.cfg.L * G::CTAS_B) && 8 * G::R2 >= 2 * kGroupThreads)  // small: 8-block tiles
         k_mask_blocks<LOGN, 8><<<slices * 2 * P.cfg.L * (G::R1 / 8), 2 * kGroupThreads, smemh, st>>>(
             dc, MT, slice_off, slice_items, item_mask, MASKS, OUT);
@@ -463,11 +455,7 @@ static void bmi_t(const DevConsts* dc, const RnsParams& P, const u64* IN, const 
                   size_t out_stride, u64* XTRA, int xlimb, int xprime, int items, cudaStream_t st) {
     using G = Ntt2<LOGN>;
     const int smem = ((NMUL + 1) * G::LINES * G::PITCH + 2 * G::TWB) * 8;
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(k_blocks_mul_inv<LOGN, NMUL>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        configured = true;
-    }
+    smem_optin_k(k_blocks_mul_inv<LOGN, NMUL>, smem);
     const int J = P.cfg.L + (XTRA ? 1 : 0);
     k_blocks_mul_inv<LOGN, NMUL><<<items * J * G::CTAS_B, mulb_threads<LOGN>(), smem, st>>>(
         dc, IN, MUL, OUT, out_stride, XTRA, xlimb, xprime);
@@ -506,11 +494,7 @@ static void mulb_t(const DevConsts* dc, const RnsParams& P, const u64* T, u64* Z
     using G = Ntt2<LOGN>;
     const int M = P.cfg.L + P.nB;
     const int smem = (4 * G::LINES * G::PITCH + 2 * G::TWB) * 8;
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(k_mul_blocks_tensor<LOGN, LT, KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        configured = true;
-    }
+    smem_optin_k(k_mul_blocks_tensor<LOGN, LT, KT>, smem);
     k_mul_blocks_tensor<LOGN, LT, KT><<<items * M * G::CTAS_B, kMulGroups * kGroupThreads, smem, st>>>(dc, T, Z);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) throw std::runtime_error(std::string("mul blocks launch: ") + cudaGetErrorString(e));

@@ -18,6 +18,18 @@ constexpr int MAXL = 16;  // max data / special primes
 constexpr int MAXB = MAXL + 1;
 constexpr int MAXP = 56;  // Q + P + B + t
 
+// ChaCha20 key of every sampled polynomial (keys, encryptions).  A nonzero
+// 64-bit seed gives the deterministic key (seed_lo, seed_hi, 6 fixed words)
+// that oracle/bfv_oracle.c restates (tests, KATs); seed 0 asks the context for
+// 256 bits of OS entropy (getrandom) instead.
+struct SeedKey {
+    uint32_t w[8];
+};
+inline SeedKey seed_key(u64 seed) {
+    return SeedKey{{(uint32_t)seed, (uint32_t)(seed >> 32), 0x63737363u, 0x2d68652du, 0x62323030u, 0x2d707267u,
+                    0x6b657973u, 0x00000001u}};
+}
+
 struct RnsConfig {
     int logn = 14;
     int L = 4;       // data primes (ciphertext modulus Q)
@@ -27,6 +39,7 @@ struct RnsConfig {
     int pbits = 60;
     u64 t = 65537;
     u64 seed = 1;
+    SeedKey key = seed_key(1);
 };
 
 // exact centred basis extension X -> Y (E1), all constants in Shoup form

@@ -77,20 +77,47 @@ def reduce_partials(words: np.ndarray, primes, L: int, n: int, device=None) -> n
     return folded.view(t.shape).cpu().numpy().view(np.uint64)
 
 
+def shared_seed() -> int:
+    """A nonzero 63-bit key seed drawn at rank 0 and broadcast: the ranks of a
+    chunk split must share the secret key so rank 0 can decrypt the summed
+    partial results."""
+    import os
+
+    import torch.distributed as dist
+
+    obj = [int.from_bytes(os.urandom(8), "little") >> 1 | 1] if dist.get_rank() == 0 else [None]
+    dist.broadcast_object_list(obj, src=0)
+    return int(obj[0])
+
+
+def disjoint_streams(ctx, rank: int) -> None:
+    """Contexts sharing a key draw encryption randomness from disjoint stream-id
+    ranges (rank << 56), so no two ranks encrypt with the same (u, e)."""
+    ctx.set_option("stream_base", (rank << 56) | 1)
+
+
+def finish_chunk_split(ctx, job, device=None):
+    """Sum this rank's partial result ciphertexts with every other rank's (one
+    all-reduce), fold mod q and decrypt at rank 0 (returns results there)."""
+    words = job.result_words()
+    summed = reduce_partials(words, ctx.primes, ctx.L, ctx.n, device)
+    return job.finish_words(summed) if summed is not None else None
+
+
 def run_chunk_split(ctx, ms, vs, chunk_size=None, device=None):
     """Evaluate this rank's chunks of every slice, sum the partial results across
-    ranks, decrypt at rank 0 (returns the results there, None elsewhere)."""
+    ranks, decrypt at rank 0 (returns the results there, None elsewhere).  Every
+    rank's ctx must hold the same key (created with shared_seed())."""
     import torch.distributed as dist
 
     from . import Job
 
     rank, world = dist.get_rank(), dist.get_world_size()
+    disjoint_streams(ctx, rank)
     job = Job(ctx, ms, vs, chunk_size, rank=rank, world=world)
     try:
         job.encrypt()
         job.cloud(graph=True)
-        words = job.result_words()
-        summed = reduce_partials(words, ctx.primes, ctx.L, ctx.n, device)
-        return job.finish_words(summed) if summed is not None else None
+        return finish_chunk_split(ctx, job, device)
     finally:
         job.close()

@@ -232,6 +232,11 @@ def ref_lib():
         L.ref_random_sparse_csr.argtypes = [C.c_uint64] * 4 + [C.c_int64] * 2 + [i64p] * 3
         L.ref_random_vector.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, C.c_int64, i64p]
         L.ref_rotation_schedule.argtypes = [C.c_uint64, C.c_uint64, u64p, ip]
+        L.ref_cloud_prepare.restype = C.c_void_p
+        L.ref_cloud_prepare.argtypes = [C.c_uint64] * 4 + [i64p] * 4 + [C.c_uint64]
+        L.ref_cloud_run.restype = C.c_double
+        L.ref_cloud_run.argtypes = [C.c_void_p]
+        L.ref_cloud_free.argtypes = [C.c_void_p]
         L.ref_chunks.restype = C.c_int64
         L.ref_chunks.argtypes = [C.c_uint64, C.c_uint64, i64p, i64p, i64p, C.c_uint64, i64p, i64p, i64p, i64p,
                                  i64p, u64p]

@@ -243,14 +243,16 @@ def test_job_run_uses_the_pipeline_and_compact_download():
 
 
 @pytest.mark.parametrize("logn", [10, 11, 12, 13])
-@pytest.mark.parametrize("fused", [1, 0])
-def test_pipeline_over_ring_sizes_and_chunk_depths(logn, fused):
+@pytest.mark.parametrize("fused,pipe", [(1, 0), (1, 1), (1, 2), (1, 3), (0, 0)])
+def test_pipeline_over_ring_sizes_and_chunk_depths(logn, fused, pipe):
     """Repeated spmv_batch calls (the cached whole-evaluation graph from the
-    second one: fused encryption finish, depth-ordered multiply items, fused
-    decryption, compact download) equal the reference semantics; chunks of
-    different tree depths make the plan reorder its items."""
+    second one: depth-ordered multiply items, compact download; party-separated
+    by default, pipe = 1/2/3 fuses the encryption finish / the decryption into
+    the cloud kernels) equal the reference semantics; chunks of different tree
+    depths make the plan reorder its items."""
     ctx = pk.Context(logn=logn, seed=8)
     ctx.set_option("fused_key_switch", fused)
+    ctx.set_option("pipeline_fuse", pipe)
     base = synth.random_sparse_csr(300, 250, 1800, 77, -8, 8)
     rng = np.random.default_rng(3)
     for _ in range(3):
