@@ -423,12 +423,10 @@ template <class F>
 static void dispatch_shape(const RnsParams& P, F&& f) {
     const auto& c = P.cfg;
     using std::integral_constant;
-    if (c.L == 3 && c.K == 1 && c.alpha == 1)
-        f(integral_constant<int, 3>{}, integral_constant<int, 1>{}, integral_constant<int, 1>{});
-    else if (c.L == 4 && c.K == 2 && c.alpha == 2)
-        f(integral_constant<int, 4>{}, integral_constant<int, 2>{}, integral_constant<int, 2>{});
-    else if (c.L == 8 && c.K == 4 && c.alpha == 4)
-        f(integral_constant<int, 8>{}, integral_constant<int, 4>{}, integral_constant<int, 4>{});
+    if (c.L == 2 && c.K == 2 && c.alpha == 2)
+        f(integral_constant<int, 2>{}, integral_constant<int, 2>{}, integral_constant<int, 2>{});
+    else if (c.L == 4 && c.K == 4 && c.alpha == 4)
+        f(integral_constant<int, 4>{}, integral_constant<int, 4>{}, integral_constant<int, 4>{});
     else
         f(integral_constant<int, 0>{}, integral_constant<int, 0>{}, integral_constant<int, 0>{});
 }

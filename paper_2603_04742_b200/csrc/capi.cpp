@@ -411,12 +411,18 @@ const char* spmvgpu_last_error(void) { return g_err.c_str(); }
 void spmvgpu_default_params(int logn, spmvgpu_params* p) {
     std::memset(p, 0, sizeof *p);
     p->logn = logn;
-    if (logn <= 13) {  // N = 8192: Q 3 x 54 bits + P 54 bits = 216 <= 218 (128-bit security)
-        p->L = 3, p->K = 1, p->alpha = 1, p->qbits = 54, p->pbits = 54;
-    } else if (logn == 14) {  // N = 16384: 6 x 58 = 348 <= 438
-        p->L = 4, p->K = 2, p->alpha = 2, p->qbits = 58, p->pbits = 58;
-    } else {  // N = 32768: 12 x 58 = 696 <= 881
-        p->L = 8, p->K = 4, p->alpha = 4, p->qbits = 58, p->pbits = 58;
+    // Q just large enough for the path's depth (1 ct x ct + 1 ct x pt + a
+    // rotate-and-add tree of up to 14 doublings) with a wide margin: the
+    // invariant-noise budget left after the deepest tree (1 x S chunk) is ~30
+    // bits at N = 2^13 / 2^14 and ~140 bits at 2^15.  One
+    // key-switching digit (alpha = L, K = L: P >= Q), so a key switch is one
+    // ModUp of c1 and L + K limb NTTs each way.
+    if (logn <= 13) {  // N = 8192: 4 x 54 = 216 <= 218 (128-bit security), 4 primes
+        p->L = 2, p->K = 2, p->alpha = 2, p->qbits = 54, p->pbits = 54;
+    } else if (logn == 14) {  // N = 16384: 4 x 58 = 232 <= 438, 4 primes
+        p->L = 2, p->K = 2, p->alpha = 2, p->qbits = 58, p->pbits = 58;
+    } else {  // N = 32768: 8 x 58 = 464 <= 881, 8 primes
+        p->L = 4, p->K = 4, p->alpha = 4, p->qbits = 58, p->pbits = 58;
     }
     p->t = 65537;
     p->seed = 0;  // 0: 256-bit ChaCha key + stream-id base from OS entropy

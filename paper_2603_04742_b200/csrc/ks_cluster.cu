@@ -229,9 +229,9 @@ bool launch_ks_cluster(const DevConsts* dc, const RnsParams& P, const u64* const
 #define CSSC_KSC(LG, L_, K_, A_) \
     if (c.logn == LG && c.L == L_ && c.K == K_ && c.alpha == A_) \
         return ks_cluster_t<LG, L_, K_, A_>(dc, SRC, SRCC, src_poly, ginv, KEY, ACC, items, st);
-    CSSC_KSC(13, 3, 1, 1)
-    CSSC_KSC(14, 4, 2, 2)
-    CSSC_KSC(15, 8, 4, 4)
+    CSSC_KSC(13, 2, 2, 2)
+    CSSC_KSC(14, 2, 2, 2)
+    CSSC_KSC(15, 4, 4, 4)
 #undef CSSC_KSC
     return false;
 }

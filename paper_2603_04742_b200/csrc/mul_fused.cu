@@ -503,12 +503,10 @@ static void mulb_t(const DevConsts* dc, const RnsParams& P, const u64* T, u64* Z
 template <int LOGN>
 static void mulb_logn(const DevConsts* dc, const RnsParams& P, const u64* T, u64* Z, int items, cudaStream_t st) {
     const auto& c = P.cfg;
-    if (c.L == 3 && c.K == 1)
-        mulb_t<LOGN, 3, 1>(dc, P, T, Z, items, st);
-    else if (c.L == 4 && c.K == 2)
-        mulb_t<LOGN, 4, 2>(dc, P, T, Z, items, st);
-    else if (c.L == 8 && c.K == 4)
-        mulb_t<LOGN, 8, 4>(dc, P, T, Z, items, st);
+    if (c.L == 2 && c.K == 2)
+        mulb_t<LOGN, 2, 2>(dc, P, T, Z, items, st);
+    else if (c.L == 4 && c.K == 4)
+        mulb_t<LOGN, 4, 4>(dc, P, T, Z, items, st);
     else
         mulb_t<LOGN, 0, 0>(dc, P, T, Z, items, st);
 }
