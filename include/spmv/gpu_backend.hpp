@@ -43,15 +43,18 @@ public:
 
     // measured invariant-noise budget of a ciphertext (decrypts it)
     int measured_noise_budget(const Ciphertext& ct) const;
-    spmvgpu_ctx* context() const { return ctx_; }
+    spmvgpu_ctx* context() const { return ctx_.get(); }
     spmvgpu_ct handle(const Ciphertext& ct) const;
 
 private:
-    Ciphertext wrap(spmvgpu_ct h, int budget) const;
-    spmvgpu_ct fresh() const;
+    // a fresh device ciphertext, owned (freed on every exit path) before the
+    // operation that fills it runs
+    std::shared_ptr<DeviceCiphertext> fresh() const;
+    Ciphertext wrap(std::shared_ptr<DeviceCiphertext> d, int budget) const;
     HeParams params_;
-    spmvgpu_ctx* ctx_ = nullptr;
-    bool owns_ = false;
+    // shared with every DeviceCiphertext this backend creates: an owned
+    // context lives until the backend and its last ciphertext are gone
+    std::shared_ptr<spmvgpu_ctx> ctx_;
 };
 
 // map a C-ABI status to the reference exception types

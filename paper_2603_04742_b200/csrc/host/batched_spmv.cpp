@@ -493,10 +493,14 @@ std::vector<SpmvResult> BatchedSpmv::report(const std::vector<std::uint64_t>& sl
             slice_noise = res_b;
             if (res_b <= 0)
                 throw NoiseExhaustedError("decrypt: noise budget exhausted (slice result)");
+            // the real BFV check: a result whose measured invariant-noise
+            // budget is gone would decrypt to wrong values (he.cpp:84-91 semantics)
+            const int meas = measured[static_cast<std::size_t>(s.result)];
+            if (meas <= 0)
+                throw NoiseExhaustedError("decrypt: measured invariant-noise budget exhausted (slice result)");
             const std::uint64_t* sl = slots.data() + static_cast<std::size_t>(s.result) * S;
             for (std::size_t idx = 0; idx < s.rows; ++idx)
                 vals[s.row_map[idx]] = idx < S ? to_signed(sl[idx], hp_.plaintext_modulus) : 0;
-            const int meas = measured[static_cast<std::size_t>(s.result)];
             R.measured_noise_budget_bits =
                 R.measured_noise_budget_bits < 0 ? meas : std::min(R.measured_noise_budget_bits, meas);
         }

@@ -168,6 +168,8 @@ SpmvResult diag_spmv(const HeBackend& be, const CsrMatrix& m, std::span<const st
         if (acc_b <= 0) throw NoiseExhaustedError("decrypt: noise budget exhausted");
         int measured = -1;
         const SlotVector slots = diag_cloud_gpu(*gpu, plan, packed, &measured);
+        if (measured <= 0)  // the real BFV check: the result would decrypt to wrong values
+            throw NoiseExhaustedError("decrypt: measured invariant-noise budget exhausted");
         ops.n_dec += 1;
         res.noise_budget_remaining_bits = acc_b;
         res.measured_noise_budget_bits = measured;

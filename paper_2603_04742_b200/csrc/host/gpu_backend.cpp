@@ -12,10 +12,10 @@
 namespace spmv {
 
 struct DeviceCiphertext {
-    spmvgpu_ctx* ctx = nullptr;
+    std::shared_ptr<spmvgpu_ctx> ctx;  // keeps the context alive while this ciphertext exists
     spmvgpu_ct h = 0;
     ~DeviceCiphertext() {
-        if (ctx && h) spmvgpu_ct_free(ctx, &h, 1);
+        if (ctx && h) spmvgpu_ct_free(ctx.get(), &h, 1);
     }
 };
 
@@ -38,7 +38,7 @@ namespace {
 int lowered(int b, int c) { return b - c > 0 ? b - c : 0; }
 }  // namespace
 
-GpuBfvBackend::GpuBfvBackend(HeParams params, GpuBfvOptions opt) : params_(params), owns_(true) {
+GpuBfvBackend::GpuBfvBackend(HeParams params, GpuBfvOptions opt) : params_(params) {
     params_.validate();
     int logn = opt.logn;
     if (logn == 0) {
@@ -64,28 +64,28 @@ GpuBfvBackend::GpuBfvBackend(HeParams params, GpuBfvOptions opt) : params_(param
     p.noise_rot = params_.noise.cost_rot_bits;
     if ((std::size_t{1} << (logn - 1)) != params_.slot_count)
         throw std::invalid_argument("GpuBfvBackend: slot_count must equal N/2");
-    check_status(spmvgpu_ctx_create(&p, &ctx_));
+    spmvgpu_ctx* raw = nullptr;
+    check_status(spmvgpu_ctx_create(&p, &raw));
+    ctx_ = std::shared_ptr<spmvgpu_ctx>(raw, [](spmvgpu_ctx* c) { spmvgpu_ctx_destroy(c); });
 }
 
-GpuBfvBackend::GpuBfvBackend(HeParams params, spmvgpu_ctx* ctx) : params_(params), ctx_(ctx), owns_(false) {
+// a view: the caller owns the context and keeps it alive
+GpuBfvBackend::GpuBfvBackend(HeParams params, spmvgpu_ctx* ctx)
+    : params_(params), ctx_(ctx, [](spmvgpu_ctx*) {}) {
     params_.validate();
 }
 
-GpuBfvBackend::~GpuBfvBackend() {
-    if (owns_ && ctx_) spmvgpu_ctx_destroy(ctx_);
-}
+GpuBfvBackend::~GpuBfvBackend() = default;
 
-spmvgpu_ct GpuBfvBackend::fresh() const {
-    spmvgpu_ct h = 0;
-    check_status(spmvgpu_ct_alloc(ctx_, 1, &h));
-    return h;
-}
-
-Ciphertext GpuBfvBackend::wrap(spmvgpu_ct h, int budget) const {
-    static std::atomic<std::uint64_t> next_id{1};
+std::shared_ptr<DeviceCiphertext> GpuBfvBackend::fresh() const {
     auto d = std::make_shared<DeviceCiphertext>();
+    check_status(spmvgpu_ct_alloc(ctx_.get(), 1, &d->h));
     d->ctx = ctx_;
-    d->h = h;
+    return d;
+}
+
+Ciphertext GpuBfvBackend::wrap(std::shared_ptr<DeviceCiphertext> d, int budget) const {
+    static std::atomic<std::uint64_t> next_id{1};
     return Ciphertext{std::move(d), budget, next_id.fetch_add(1)};
 }
 
@@ -109,10 +109,10 @@ Ciphertext GpuBfvBackend::encrypt(const Plaintext& pt, OpLedger& ledger) const {
         throw DimensionMismatchError("encrypt: plaintext slot count does not match parameters");
     std::vector<std::int64_t> vals(pt.slots.begin(), pt.slots.end());
     const std::uint64_t offs[2] = {0, vals.size()};
-    const spmvgpu_ct h = fresh();
-    check_status(spmvgpu_encrypt(ctx_, vals.data(), offs, nullptr, &h, 1));
+    auto out = fresh();
+    check_status(spmvgpu_encrypt(ctx_.get(), vals.data(), offs, nullptr, &out->h, 1));
     ledger.n_enc += 1;
-    return wrap(h, params_.noise.initial_budget_bits);
+    return wrap(std::move(out), params_.noise.initial_budget_bits);
 }
 
 SlotVector GpuBfvBackend::decrypt(const Ciphertext& ct, OpLedger& ledger) const {
@@ -121,7 +121,12 @@ SlotVector GpuBfvBackend::decrypt(const Ciphertext& ct, OpLedger& ledger) const 
     SlotVector slots(params_.slot_count);
     const spmvgpu_ct h = handle(ct);
     std::int32_t measured = 0;
-    check_status(spmvgpu_decrypt(ctx_, &h, 1, slots.data(), &measured));
+    check_status(spmvgpu_decrypt(ctx_.get(), &h, 1, slots.data(), &measured));
+    // the real BFV check behind the model counter: no invariant-noise
+    // budget left means the slots below are not the plaintext
+    if (measured <= 0)
+        throw NoiseExhaustedError("decrypt: measured invariant-noise budget exhausted (ciphertext id " +
+                                  std::to_string(ct.id) + ")");
     ledger.n_dec += 1;
     return slots;
 }
@@ -130,49 +135,53 @@ int GpuBfvBackend::measured_noise_budget(const Ciphertext& ct) const {
     SlotVector slots(params_.slot_count);
     const spmvgpu_ct h = handle(ct);
     std::int32_t measured = 0;
-    check_status(spmvgpu_decrypt(ctx_, &h, 1, slots.data(), &measured));
+    check_status(spmvgpu_decrypt(ctx_.get(), &h, 1, slots.data(), &measured));
     return measured;
 }
 
 Ciphertext GpuBfvBackend::add(const Ciphertext& a, const Ciphertext& b, OpLedger& ledger) const {
-    const spmvgpu_ct x = handle(a), y = handle(b), o = fresh();
-    check_status(spmvgpu_add(ctx_, &x, &y, &o, 1));
+    const spmvgpu_ct x = handle(a), y = handle(b);
+    auto o = fresh();
+    check_status(spmvgpu_add(ctx_.get(), &x, &y, &o->h, 1));
     ledger.n_add += 1;
-    return wrap(o, lowered(std::min(a.noise_budget_bits, b.noise_budget_bits), params_.noise.cost_add_bits));
+    return wrap(std::move(o), lowered(std::min(a.noise_budget_bits, b.noise_budget_bits), params_.noise.cost_add_bits));
 }
 
 Ciphertext GpuBfvBackend::multiply(const Ciphertext& a, const Ciphertext& b, OpLedger& ledger) const {
-    const spmvgpu_ct x = handle(a), y = handle(b), o = fresh();
-    check_status(spmvgpu_mul_relin(ctx_, &x, &y, &o, 1));
+    const spmvgpu_ct x = handle(a), y = handle(b);
+    auto o = fresh();
+    check_status(spmvgpu_mul_relin(ctx_.get(), &x, &y, &o->h, 1));
     ledger.n_mult_cc += 1;
-    return wrap(o, lowered(std::min(a.noise_budget_bits, b.noise_budget_bits), params_.noise.cost_ct_ct_mult_bits));
+    return wrap(std::move(o), lowered(std::min(a.noise_budget_bits, b.noise_budget_bits), params_.noise.cost_ct_ct_mult_bits));
 }
 
 Ciphertext GpuBfvBackend::multiply_plain(const Ciphertext& a, const Plaintext& b, OpLedger& ledger) const {
     if (b.slots.size() != params_.slot_count) throw DimensionMismatchError("multiply_plain: slot counts differ");
     std::vector<std::int64_t> vals(b.slots.begin(), b.slots.end());
     const std::uint64_t offs[2] = {0, vals.size()};
-    const spmvgpu_ct x = handle(a), o = fresh();
-    check_status(spmvgpu_mul_plain(ctx_, &x, vals.data(), offs, &o, 1));
+    const spmvgpu_ct x = handle(a);
+    auto o = fresh();
+    check_status(spmvgpu_mul_plain(ctx_.get(), &x, vals.data(), offs, &o->h, 1));
     ledger.n_mult_cp += 1;
-    return wrap(o, lowered(a.noise_budget_bits, params_.noise.cost_ct_pt_mult_bits));
+    return wrap(std::move(o), lowered(a.noise_budget_bits, params_.noise.cost_ct_pt_mult_bits));
 }
 
 Ciphertext GpuBfvBackend::rotate(const Ciphertext& a, std::int64_t k, OpLedger& ledger) const {
-    const spmvgpu_ct x = handle(a), o = fresh();
-    check_status(spmvgpu_rotate(ctx_, &x, &k, &o, 1));
+    const spmvgpu_ct x = handle(a);
+    auto o = fresh();
+    check_status(spmvgpu_rotate(ctx_.get(), &x, &k, &o->h, 1));
     ledger.n_rot += 1;
-    return wrap(o, lowered(a.noise_budget_bits, params_.noise.cost_rot_bits));
+    return wrap(std::move(o), lowered(a.noise_budget_bits, params_.noise.cost_rot_bits));
 }
 
 Ciphertext GpuBfvBackend::zero_ciphertext() const {
     std::uint64_t n = 0, slots = 0, ctw = 0, kw = 0;
     int dnum = 0;
-    check_status(spmvgpu_ctx_sizes(ctx_, &n, &slots, &ctw, &kw, &dnum));
+    check_status(spmvgpu_ctx_sizes(ctx_.get(), &n, &slots, &ctw, &kw, &dnum));
     const std::vector<std::uint64_t> zeros(ctw, 0);
-    const spmvgpu_ct o = fresh();
-    check_status(spmvgpu_ct_upload(ctx_, o, zeros.data()));
-    return wrap(o, params_.noise.initial_budget_bits);
+    auto o = fresh();
+    check_status(spmvgpu_ct_upload(ctx_.get(), o->h, zeros.data()));
+    return wrap(std::move(o), params_.noise.initial_budget_bits);
 }
 
 }  // namespace spmv

@@ -303,3 +303,36 @@ def test_alternating_plans_with_speculative_early_encryption(capacity):
         got = pk.spmv_batch(ctx, [m], [v])[0]
         assert_same(got, checker(m, v, ctx.slots, ctx.slots))
     ctx.close()
+
+
+def test_batch_vector_length_checked_at_the_c_abi():
+    """cssc_spmv_batch takes each vector's length and raises DimensionMismatchError
+    (reference protocol.cpp:77-81) instead of reading past a short vector."""
+    ctx = pk.Context(logn=10, seed=3)
+    m = synth.random_sparse_csr(20, 30, 50, 1, -8, 8)
+    keep = []
+    csrs = (pk.CsrC * 1)(pk._csr_c(m, keep))
+    vptr, vlens = pk._vectors([m], [np.ones(29, np.int64)], keep)  # one entry short
+    outs = np.zeros(20, np.int64)
+    optr = (pk.i64p * 1)(pk._p(outs, pk.i64p))
+    res = (pk.ResultC * 1)()
+    assert pk.lib().cssc_spmv_batch(ctx.h, csrs, vptr, vlens, 1, ctx.slots, 0, optr, res) == -4
+    assert b"does not match" in pk.lib().spmvgpu_last_error()
+    with pytest.raises(pk.SpmvError) as e:
+        pk.spmv_batch(ctx, [m], [np.ones(31, np.int64)])
+    assert e.value.kind == "DimensionMismatchError"
+    ctx.close()
+
+
+def test_exhausted_noise_budget_raises():
+    """A modulus too small for the path's depth (Q = one 54-bit prime): the
+    product's measured invariant-noise budget is gone, so the batched path
+    raises NoiseExhaustedError (reference he.cpp:84-91 semantics) instead of
+    returning wrong values; the model counter alone (87 bits) would pass it."""
+    ctx = pk.Context(logn=12, seed=3, L=1, K=1, alpha=1, qbits=54, pbits=54)
+    m = synth.random_sparse_csr(64, 64, 300, 5, -8, 8)
+    v = synth.random_vector(64, 5, -8, 8, nonzero=True)
+    with pytest.raises(pk.SpmvError) as e:
+        pk.spmv_partitioned(ctx, m, v)
+    assert e.value.kind == "NoiseExhaustedError"
+    ctx.close()
