@@ -254,6 +254,15 @@ int cssc_job_create_shard(spmvgpu_ctx* c, const cssc_csr* ms, const int64_t* con
                           uint64_t chunk_size, int rank, int world, cssc_job** out);
 int cssc_job_result_words(cssc_job* j, uint64_t* words, uint64_t cap_words, uint64_t* n_results);
 int cssc_job_finish_words(cssc_job* j, const uint64_t* words, int64_t* const* values, cssc_result* res);
+/* the same with the words in DEVICE memory of the context's GPU, for an
+ * all-reduce that stays on the device (NCCL over NVLink): result_words_dev
+ * copies this rank's partials into dev_words ([results][ct words]) and waits;
+ * finish_words_dev folds the summed words mod q_j in place (spmvgpu_fold_mod)
+ * and decrypts */
+int cssc_job_result_words_dev(cssc_job* j, uint64_t* dev_words, uint64_t cap_words, uint64_t* n_results);
+int cssc_job_finish_words_dev(cssc_job* j, uint64_t* dev_words, int64_t* const* values, cssc_result* res);
+/* device words [n_cts][2][L][N], each a sum of <= 16 residues < q_j: reduce mod q_j in place */
+int spmvgpu_fold_mod(spmvgpu_ctx* c, uint64_t* dev_words, uint64_t n_cts);
 int cssc_job_encrypt(cssc_job* j);            /* client phase: encode + encrypt on device */
 int cssc_job_cloud(cssc_job* j, int use_graph); /* cloud phase, enqueued (no sync) */
 /* the same between two caller-created cudaEvent_t records on the context

@@ -127,19 +127,22 @@ _SIGS = {
     "cssc_diag_spmv": (C.c_int, [C.c_void_p, C.POINTER(CsrC), i64p, C.c_uint64, C.c_int, i64p,
                                  C.POINTER(ResultC), C.POINTER(Message), C.c_uint64]),
     "spmvgpu_sum": (C.c_int, [C.c_void_p, u64p, C.c_size_t, C.c_uint64]),
-    "cssc_spmv_batch": (C.c_int, [C.c_void_p, C.POINTER(CsrC), C.POINTER(i64p), u64p, C.c_size_t,
-                                  C.c_uint64, C.c_int, C.POINTER(i64p), C.POINTER(ResultC)]),
-    "cssc_job_create": (C.c_int, [C.c_void_p, C.POINTER(CsrC), C.POINTER(i64p), u64p, C.c_size_t,
+    "cssc_spmv_batch": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t,
+                                  C.c_uint64, C.c_int, C.c_void_p, C.c_void_p]),
+    "cssc_job_create": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t,
                                   C.c_uint64, C.POINTER(C.c_void_p)]),
-    "cssc_job_create_shard": (C.c_int, [C.c_void_p, C.POINTER(CsrC), C.POINTER(i64p), u64p, C.c_size_t, C.c_uint64,
+    "cssc_job_create_shard": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_uint64,
                                         C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
     "cssc_job_result_words": (C.c_int, [C.c_void_p, u64p, C.c_uint64, u64p]),
-    "cssc_job_finish_words": (C.c_int, [C.c_void_p, u64p, C.POINTER(i64p), C.POINTER(ResultC)]),
+    "cssc_job_finish_words": (C.c_int, [C.c_void_p, u64p, C.c_void_p, C.c_void_p]),
+    "cssc_job_result_words_dev": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, u64p]),
+    "cssc_job_finish_words_dev": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "spmvgpu_fold_mod": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64]),
     "cssc_job_encrypt": (C.c_int, [C.c_void_p]),
     "cssc_job_cloud": (C.c_int, [C.c_void_p, C.c_int]),
     "cssc_job_cloud_timed": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]),
-    "cssc_job_finish": (C.c_int, [C.c_void_p, C.POINTER(i64p), C.POINTER(ResultC)]),
-    "cssc_job_run": (C.c_int, [C.c_void_p, C.POINTER(i64p), C.POINTER(ResultC)]),
+    "cssc_job_finish": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "cssc_job_run": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "cssc_job_plan_stats": (C.c_int, [C.c_void_p, C.POINTER(PlanStats)]),
     "cssc_job_profile": (C.c_int, [C.c_void_p, C.POINTER(PhaseC), C.c_int, C.POINTER(C.c_int)]),
     "cssc_job_profile_kernels": (C.c_int, [C.c_void_p, C.c_int, C.c_uint64, C.POINTER(KernelTimingC), C.c_int,
@@ -483,20 +486,72 @@ def _csr_c(m, keep: list) -> CsrC:
     return CsrC(int(m.rows), int(m.cols), _p(rp, i64p), _p(ci, i64p), _p(va, i64p))
 
 
+def _addr(a: np.ndarray) -> int:
+    """Data address of a C-contiguous array (from_buffer is ~3x cheaper than
+    __array_interface__; read-only arrays take the slow path)."""
+    try:
+        return C.addressof(C.c_char.from_buffer(a))
+    except (TypeError, ValueError, BufferError):
+        return a.__array_interface__["data"][0]
+
+
+_ONE0 = np.zeros(1, np.int64)
+_CSR_DT = np.dtype([("rows", "<u8"), ("cols", "<u8"), ("rp", "<u8"), ("ci", "<u8"), ("va", "<u8")])
+_RES_DT = np.dtype([("led", "<u8", 6), ("n_ct", "<u8"), ("model", "<i4"), ("measured", "<i4"), ("nmsg", "<u8")])
+assert _CSR_DT.itemsize == C.sizeof(CsrC) and _RES_DT.itemsize == C.sizeof(ResultC)
+_LEDGER_KEYS = tuple(k for k, _ in Ledger._fields_)
+
+
+def _csr_table(ms, keep: list) -> np.ndarray:
+    """cssc_csr[] for a batch as one numpy record array (addresses of int64
+    copies kept alive in `keep`); a few us per matrix instead of ctypes objects."""
+    rows = []
+    for m in ms:
+        rp, ci, va = _i64(m.row_ptrs), _i64(m.col_indices), _i64(m.values)
+        if va.size == 0:
+            ci = va = _ONE0
+        keep += (rp, ci, va)
+        rows.append((int(m.rows), int(m.cols), _addr(rp), _addr(ci), _addr(va)))
+    t = np.array(rows, dtype=_CSR_DT) if rows else np.zeros(1, _CSR_DT)
+    keep.append(t)
+    return t
+
+
 def _vectors(ms, vs, keep: list):
-    """int64 copies of the vectors, their pointer array and lengths (the C-ABI
+    """Addresses of int64 copies of the vectors and their lengths (the C-ABI
     raises DimensionMismatchError on a length != cols, reference protocol.cpp:77-81)."""
     ms, vs = list(ms), list(vs)
     if len(ms) != len(vs):
         raise SpmvError(-4, "DimensionMismatchError",
                         f"spmv_batch: {len(ms)} matrices but {len(vs)} vectors")
     vv = [_i64(v) for v in vs]
-    vv = [v if v.size else np.zeros(1, np.int64) for v in vv]
+    lens = np.array([v.size for v in vv] or [0], dtype=np.uint64)
+    vv = [v if v.size else _ONE0 for v in vv]
+    ptrs = np.array([_addr(v) for v in vv] or [0], dtype=np.uint64)
     keep += vv
-    n = len(vv)
-    lens = np.array([np.asarray(v).size for v in vs], dtype=np.uint64)
-    keep.append(lens)
-    return (i64p * max(n, 1))(*[_p(v, i64p) for v in vv]), _p(lens, u64p) if n else None
+    keep += (ptrs, lens)
+    return _addr(ptrs), _addr(lens)
+
+
+def _outputs(ms, keep: list):
+    """One int64 buffer for every matrix's rows, the per-matrix address table
+    and a cssc_result[] record array."""
+    rows = [int(m.rows) for m in ms]
+    off = np.zeros(len(rows) + 1, np.int64)
+    off[1:] = np.cumsum([max(r, 1) for r in rows])
+    buf = np.zeros(int(off[-1]) or 1, np.int64)
+    ptrs = (off[:-1] * 8 + _addr(buf)).astype(np.uint64) if rows else np.zeros(1, np.uint64)
+    res = np.zeros(max(len(rows), 1), _RES_DT)
+    keep += (buf, ptrs, res)
+    return buf, off, rows, _addr(ptrs), res
+
+
+def _results(buf, off, rows, res) -> list:
+    n = len(rows)
+    led, nct = res["led"][:n].tolist(), res["n_ct"][:n].tolist()
+    model, meas, offs = res["model"][:n].tolist(), res["measured"][:n].tolist(), off.tolist()
+    return [{"values": buf[offs[i]: offs[i] + rows[i]], "n_ct": nct[i], "noise": model[i],
+             "measured_noise": meas[i], "ledger": dict(zip(_LEDGER_KEYS, led[i]))} for i in range(n)]
 
 
 def _result(r: ResultC, values: np.ndarray, msgs=None) -> dict:
@@ -555,16 +610,17 @@ def diag_spmv(ctx: Context, m: Csr, v, key_holder: int = 0) -> dict:
 
 
 def spmv_batch(ctx: Context, ms, vs, chunk_size: int | None = None, key_holder: int = 0) -> list:
+    """Several independent spmv_partitioned runs in shared launches (each result
+    equals its own run); party-separated unless the context's pipeline_fuse
+    option says otherwise."""
     chunk = ctx.slots if chunk_size is None else chunk_size
-    n = len(ms)
+    ms = list(ms)
     keep: list = []
-    csrs = (CsrC * max(n, 1))(*[_csr_c(m, keep) for m in ms])
+    csrs = _csr_table(ms, keep)
     vptr, vlens = _vectors(ms, vs, keep)
-    outs = [np.zeros(max(m.rows, 1), np.int64) for m in ms]
-    optr = (i64p * n)(*[_p(o, i64p) for o in outs])
-    res = (ResultC * n)()
-    check(lib().cssc_spmv_batch(ctx.h, csrs, vptr, vlens, n, chunk, key_holder, optr, res))
-    return [_result(res[i], outs[i][: ms[i].rows]) for i in range(n)]
+    buf, off, rows, optr, res = _outputs(ms, keep)
+    check(lib().cssc_spmv_batch(ctx.h, _addr(csrs), vptr, vlens, len(ms), chunk, key_holder, optr, _addr(res)))
+    return _results(buf, off, rows, res)
 
 
 class Job:
@@ -575,10 +631,10 @@ class Job:
         chunk = ctx.slots if chunk_size is None else chunk_size
         n = len(self.ms)
         self._keep: list = []  # the job borrows these arrays until it is destroyed
-        self._csrs = (CsrC * max(n, 1))(*[_csr_c(m, self._keep) for m in self.ms])
+        csrs = _csr_table(self.ms, self._keep)
         vptr, vlens = _vectors(self.ms, vs, self._keep)
         h = C.c_void_p()
-        check(lib().cssc_job_create_shard(ctx.h, self._csrs, vptr, vlens, n, chunk, rank, world, C.byref(h)))
+        check(lib().cssc_job_create_shard(ctx.h, _addr(csrs), vptr, vlens, n, chunk, rank, world, C.byref(h)))
         self.h = h
 
     def result_words(self) -> np.ndarray:
@@ -593,12 +649,32 @@ class Job:
     def finish_words(self, words: np.ndarray) -> list:
         """Decrypt summed partial results (see result_words) and do the bookkeeping."""
         w = _u64(words)
-        n = len(self.ms)
-        outs = [np.zeros(max(m.rows, 1), np.int64) for m in self.ms]
-        optr = (i64p * n)(*[_p(o, i64p) for o in outs])
-        res = (ResultC * n)()
-        check(lib().cssc_job_finish_words(self.h, _p(w, u64p) if w.size else None, optr, res))
-        return [_result(res[i], outs[i][: self.ms[i].rows]) for i in range(n)]
+        keep: list = []
+        buf, off, rows, optr, res = _outputs(self.ms, keep)
+        check(lib().cssc_job_finish_words(self.h, _p(w, u64p) if w.size else None, optr, _addr(res)))
+        return _results(buf, off, rows, res)
+
+    def result_words_dev(self, out=None):
+        """This shard's partial result ciphertexts copied into a device tensor
+        (torch.int64 [results * ct_words] on the context's GPU; allocated when
+        `out` is None) -- the buffer an NCCL all-reduce sums across ranks."""
+        import torch
+
+        cnt = C.c_uint64()
+        check(lib().cssc_job_result_words_dev(self.h, None, 0, C.byref(cnt)))
+        if out is None:
+            out = torch.empty(max(cnt.value, 1) * self.ctx.ct_words, dtype=torch.int64,
+                              device=torch.device("cuda", self.ctx.params.device))
+        if cnt.value:
+            check(lib().cssc_job_result_words_dev(self.h, out.data_ptr(), out.numel(), C.byref(cnt)))
+        return out
+
+    def finish_words_dev(self, dev) -> list:
+        """Fold the summed device words mod q (in place, on the GPU) and decrypt."""
+        keep: list = []
+        buf, off, rows, optr, res = _outputs(self.ms, keep)
+        check(lib().cssc_job_finish_words_dev(self.h, dev.data_ptr(), optr, _addr(res)))
+        return _results(buf, off, rows, res)
 
     def encrypt(self):
         check(lib().cssc_job_encrypt(self.h))
@@ -612,22 +688,18 @@ class Job:
                                          C.c_void_p(stop.cuda_event)))
 
     def finish(self) -> list:
-        n = len(self.ms)
-        outs = [np.zeros(max(m.rows, 1), np.int64) for m in self.ms]
-        optr = (i64p * n)(*[_p(o, i64p) for o in outs])
-        res = (ResultC * n)()
-        check(lib().cssc_job_finish(self.h, optr, res))
-        return [_result(res[i], outs[i][: self.ms[i].rows]) for i in range(n)]
+        keep: list = []
+        buf, off, rows, optr, res = _outputs(self.ms, keep)
+        check(lib().cssc_job_finish(self.h, optr, _addr(res)))
+        return _results(buf, off, rows, res)
 
     def run(self) -> list:
         """encrypt + cloud + finish in one call (spmv_batch's path: one cached
         graph launch from the second job over the same chunk shapes)."""
-        n = len(self.ms)
-        outs = [np.zeros(max(m.rows, 1), np.int64) for m in self.ms]
-        optr = (i64p * n)(*[_p(o, i64p) for o in outs])
-        res = (ResultC * n)()
-        check(lib().cssc_job_run(self.h, optr, res))
-        return [_result(res[i], outs[i][: self.ms[i].rows]) for i in range(n)]
+        keep: list = []
+        buf, off, rows, optr, res = _outputs(self.ms, keep)
+        check(lib().cssc_job_run(self.h, optr, _addr(res)))
+        return _results(buf, off, rows, res)
 
     def stats(self) -> dict:
         s = PlanStats()

@@ -483,7 +483,7 @@ void GpuContext::encrypt_cssc_forked(const unsigned char* img, const CsscLayout&
         stats_.kernels += 7;
     } else {
         launch_enc_finish(dc_, P_, P_.cfg.key, streams, CM, reinterpret_cast<u64* const*>(d + lay.o_out), items,
-                          st_, MSG, (size_t)2 * L * n, n);
+                          st_, MSG, (size_t)2 * L * n, n, part == 2 ? ws.E : nullptr);
         stats_.kernels += 8;
     }
     stats_.limb_ntts += (u64)items * (1 + 3 * L);

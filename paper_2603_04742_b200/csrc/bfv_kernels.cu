@@ -1403,19 +1403,30 @@ void launch_enc_pk(const DevConsts* dc, const RnsParams& P, const u64* PK, const
 // OUT = C + (e0 + Delta m, e1): a 128-thread CTA draws the 16 + 16 ChaCha
 // blocks of its 128 coefficients (4 lanes per block), then one thread per
 // coefficient finishes every limb with coalesced loads and stores
+// E (int8 [item][2][N], drawn ahead by k_enc_sample_e): read the e draws
+// instead of running ChaCha again (same words)
+template <bool FROM_E>
 __global__ void __launch_bounds__(128) k_enc_finish(const DevConsts* __restrict__ dc, SeedKey seed,
                                                     const u64* streams, const u64* C, size_t cstride,
-                                                    const u64* MSG, size_t mstride, u64* const* OUT) {
-    __shared__ u32 blk[32][16];
+                                                    const u64* MSG, size_t mstride, u64* const* OUT,
+                                                    const int8_t* __restrict__ E) {
     const int n = dc->n, L = dc->L;
     const int item = blockIdx.y;
-    const u64 id = streams[item];
-    const int g = threadIdx.x >> 2;
-    chacha20_block_x4(seed, (u32)(blockIdx.x * 16 + (g & 15)), g < 16 ? DOM_ENC_E0 : DOM_ENC_E1, (u32)id,
-                      (u32)(id >> 32), blk[g]);
-    __syncthreads();
     const int kk = threadIdx.x, k = blockIdx.x * 128 + kk;
-    const int64_t e0 = cbd_of(word64(blk[kk >> 3], kk & 7)), e1 = cbd_of(word64(blk[16 + (kk >> 3)], kk & 7));
+    int64_t e0, e1;
+    if constexpr (FROM_E) {
+        e0 = E[((size_t)item * 2) * n + k];
+        e1 = E[((size_t)item * 2 + 1) * n + k];
+    } else {
+        __shared__ u32 blk[32][16];
+        const u64 id = streams[item];
+        const int g = threadIdx.x >> 2;
+        chacha20_block_x4(seed, (u32)(blockIdx.x * 16 + (g & 15)), g < 16 ? DOM_ENC_E0 : DOM_ENC_E1, (u32)id,
+                          (u32)(id >> 32), blk[g]);
+        __syncthreads();
+        e0 = cbd_of(word64(blk[kk >> 3], kk & 7));
+        e1 = cbd_of(word64(blk[16 + (kk >> 3)], kk & 7));
+    }
     const size_t cm = (size_t)item * cstride + k;
     const u64 m = MSG[(size_t)item * mstride + k];
     u64* out = OUT[item];
@@ -1456,15 +1467,18 @@ void launch_enc_sample_e(const DevConsts* dc, const RnsParams& P, SeedKey seed, 
 
 void launch_enc_finish(const DevConsts* dc, const RnsParams& P, SeedKey seed, const u64* streams,
                        const u64* CM, u64* const* OUT, int items, cudaStream_t st, const u64* MSG, size_t cstride,
-                       size_t mstride) {
+                       size_t mstride, const int8_t* E) {
     if (!items) return;
     if (!cstride) cstride = (size_t)(2 * P.cfg.L + 1) * P.n;
     if (!MSG) {
         MSG = CM + (size_t)2 * P.cfg.L * P.n;
         mstride = cstride;
     }
-    k_enc_finish<<<dim3((unsigned)(P.n / 128), (unsigned)items), 128, 0, st>>>(dc, seed, streams, CM, cstride, MSG,
-                                                                               mstride, OUT);
+    const dim3 g((unsigned)(P.n / 128), (unsigned)items);
+    if (E)
+        k_enc_finish<true><<<g, 128, 0, st>>>(dc, seed, streams, CM, cstride, MSG, mstride, OUT, E);
+    else
+        k_enc_finish<false><<<g, 128, 0, st>>>(dc, seed, streams, CM, cstride, MSG, mstride, OUT, nullptr);
     CSSC_CHECK_LAUNCH();
 }
 
@@ -1798,6 +1812,20 @@ void launch_add(const DevConsts* dc, const RnsParams& P, const u64* const* A,
                 const u64* const* B, u64* const* OUT, int items, cudaStream_t st) {
     if (!items) return;
     k_add<<<ew_grid(P.n, items), EW_THREADS, 0, st>>>(dc, A, B, OUT);
+    CSSC_CHECK_LAUNCH();
+}
+
+__global__ void k_fold_mod(const DevConsts* __restrict__ dc, u64* W) {
+    const int n = dc->n, L = dc->L;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = blockIdx.y % L;  // limb of row blockIdx.y = (result, poly, limb)
+    u64* w = W + (size_t)blockIdx.y * n + k;
+    *w = reduce64(*w, dc->mod[j]);
+}
+
+void launch_fold_mod(const DevConsts* dc, const RnsParams& P, u64* W, int results, cudaStream_t st) {
+    if (!results) return;
+    k_fold_mod<<<dim3((unsigned)(P.n / EW_THREADS), (unsigned)(results * 2 * P.cfg.L)), EW_THREADS, 0, st>>>(dc, W);
     CSSC_CHECK_LAUNCH();
 }
 

@@ -170,7 +170,7 @@ void launch_enc_pk(const DevConsts* dc, const RnsParams& P, const u64* PK, const
 // (mstride words apart)
 void launch_enc_finish(const DevConsts* dc, const RnsParams& P, SeedKey seed, const u64* streams,
                        const u64* CM, u64* const* OUT, int items, cudaStream_t st, const u64* MSG = nullptr,
-                       size_t cstride = 0, size_t mstride = 0);
+                       size_t cstride = 0, size_t mstride = 0, const int8_t* E = nullptr);
 void launch_mul_s(const DevConsts* dc, const RnsParams& P, u64* X, const u64* S_NTT, int items,
                   cudaStream_t st);
 void launch_dec_scale(const DevConsts* dc, const RnsParams& P, const u64* const* CT,
@@ -202,6 +202,9 @@ void launch_sum_items(const DevConsts* dc, const RnsParams& P, const u64* const*
                       cudaStream_t st);
 void launch_add(const DevConsts* dc, const RnsParams& P, const u64* const* A,
                 const u64* const* B, u64* const* OUT, int items, cudaStream_t st);
+// SURVEY 8(e) chunk split: W = [results][2][L][N] sums of the ranks' partial
+// result words (each < q_j, at most 16 ranks: < 2^62) -> residues mod q_j, in place
+void launch_fold_mod(const DevConsts* dc, const RnsParams& P, u64* W, int results, cudaStream_t st);
 
 
 }  // namespace cssc

@@ -884,6 +884,7 @@ int cssc_spmv_batch(spmvgpu_ctx* c, const cssc_csr* ms, const int64_t* const* vs
         // host packs (used only if this call's chunk shapes select that plan)
         static const bool spec = std::getenv("CSSC_NO_EARLY_ENC") == nullptr;
         if (spec) spmv::detail::pipeline_speculate(c);
+        const auto t0s = std::chrono::steady_clock::now();
         if (nmat && (!ms || !vs || !vlens)) throw std::invalid_argument("null argument");
         std::vector<spmv::detail::CsrView> w;
         for (size_t i = 0; i < nmat; ++i) w.push_back(view_of(ms[i], vs[i], vlens[i]));
@@ -895,7 +896,8 @@ int cssc_spmv_batch(spmvgpu_ctx* c, const cssc_csr* ms, const int64_t* const* vs
         if (trace) {
             const auto t3 = std::chrono::steady_clock::now();
             auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
-            std::fprintf(stderr, "e2e-trace pack %.1f run %.1f fill %.1f us\n", us(t0, t1), us(t1, t2), us(t2, t3));
+            std::fprintf(stderr, "e2e-trace speculate %.1f pack %.1f run %.1f fill %.1f us\n", us(t0, t0s),
+                         us(t0s, t1), us(t1, t2), us(t2, t3));
         }
     });
 }
@@ -933,6 +935,29 @@ int cssc_job_finish_words(cssc_job* j, const uint64_t* words, int64_t* const* va
         if (!j || (!words && j->job->result_count())) throw std::invalid_argument("null argument");
         const auto r = j->job->finish_words(words);
         for (size_t i = 0; i < r.size(); ++i) fill_result(r[i], values ? values[i] : nullptr, res ? res + i : nullptr, nullptr, 0);
+    });
+}
+int cssc_job_result_words_dev(cssc_job* j, uint64_t* dev_words, uint64_t cap_words, uint64_t* n_results) {
+    return guard([&] { auto lk_ = api_lock(j ? j->ctx : nullptr);
+        if (!j || !n_results) throw std::invalid_argument("null argument");
+        *n_results = j->job->result_count();
+        if (!dev_words) return;
+        if (cap_words < *n_results * G(j->ctx).ct_words()) throw std::length_error("result_words_dev: buffer too small");
+        j->job->result_words_dev(dev_words);
+    });
+}
+int cssc_job_finish_words_dev(cssc_job* j, uint64_t* dev_words, int64_t* const* values, cssc_result* res) {
+    return guard([&] { auto lk_ = api_lock(j ? j->ctx : nullptr);
+        if (!j || (!dev_words && j->job->result_count())) throw std::invalid_argument("null argument");
+        const auto r = j->job->finish_words_dev(dev_words);
+        for (size_t i = 0; i < r.size(); ++i) fill_result(r[i], values ? values[i] : nullptr, res ? res + i : nullptr, nullptr, 0);
+    });
+}
+int spmvgpu_fold_mod(spmvgpu_ctx* c, uint64_t* dev_words, uint64_t n_cts) {
+    return guard([&] { auto lk_ = api_lock(c);
+        auto& g = G(c);
+        cssc::launch_fold_mod(g.dconsts(), g.params(), dev_words, (int)n_cts, g.stream());
+        g.synchronize();
     });
 }
 int cssc_job_encrypt(cssc_job* j) { return guard([&] { auto lk_ = api_lock(j ? j->ctx : nullptr); j->job->encrypt(); }); }

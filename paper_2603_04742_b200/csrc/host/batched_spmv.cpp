@@ -1,11 +1,14 @@
 // batched_spmv.cpp -- see batched_spmv.hpp.
 #include "batched_spmv.hpp"
 
+#include <cuda_runtime.h>
+
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <algorithm>
 #include <cstring>
+#include <exception>
 #include <climits>
 #include <numeric>
 #include <stdexcept>
@@ -90,8 +93,14 @@ BatchedSpmv::BatchedSpmv(spmvgpu_ctx* ctx, const HeParams& hp, std::span<const C
         });
         scanned_ok = std::none_of(bad.begin(), bad.end(), [](unsigned char x) { return x != 0; });
     }
+    // validation in matrix order; the slices to shape are collected and shaped
+    // afterwards (on the host pool for large batches), errors still surface in
+    // the order the sequential evaluation would raise them
+    const auto tv = std::chrono::steady_clock::now();
+    std::vector<SliceJob> jobs;
+    std::exception_ptr pending;
     std::int64_t nz_next = 0, vec_next = 0;
-    for (std::size_t mi = 0; mi < ms.size(); ++mi) {
+    for (std::size_t mi = 0; mi < ms.size() && !pending; ++mi) try {
         const CsrView& m = ms[mi];
         if (m.rows && m.row_ptrs[0] != 0) throw std::invalid_argument("csr: row_ptrs[0] must be 0");
         if (!scanned_ok) {  // branch-free scans (vectorised); the offending entry is located only on failure
@@ -121,10 +130,70 @@ BatchedSpmv::BatchedSpmv(spmvgpu_ctx* ctx, const HeParams& hp, std::span<const C
         if (partition) {
             if (chunk_size == 0) throw std::invalid_argument("partition_rows: max_rows must be positive");
             for (std::size_t r0 = 0; r0 < m.rows; r0 += chunk_size)
-                add_slice(m, mi, r0, std::min(m.rows, r0 + chunk_size), chunk_size, nz_base, vec_base);
+                jobs.push_back({mi, r0, std::min(m.rows, r0 + chunk_size), nz_base, vec_base});
         } else {
-            add_slice(m, mi, 0, m.rows, chunk_size, nz_base, vec_base);
+            jobs.push_back({mi, 0, m.rows, nz_base, vec_base});
         }
+    } catch (...) {
+        pending = std::current_exception();
+    }
+    {
+        std::vector<SliceShape> shapes(jobs.size());
+        auto shape_one = [&](std::size_t j) {
+            try {
+                shape_slice(ms[jobs[j].mat], jobs[j], chunk_size, shapes[j]);
+            } catch (...) {
+                shapes[j].err = std::current_exception();
+            }
+        };
+        const auto tj = std::chrono::steady_clock::now();
+        if (big && jobs.size() > 1)
+            HostPool::get().run(jobs.size(), shape_one);
+        else
+            for (std::size_t j = 0; j < jobs.size(); ++j) shape_one(j);
+        const auto ts = std::chrono::steady_clock::now();
+        if (trace) {
+            auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+            std::fprintf(stderr, "e2e-trace scan %.1f validate %.1f shape %.1f us\n", us(t0, tv), us(tv, tj),
+                         us(tj, ts));
+        }
+        for (std::size_t j = 0; j < jobs.size(); ++j)
+            if (shapes[j].err) std::rethrow_exception(shapes[j].err);
+        // slice metadata in order, then the row / column records copied into
+        // place with their slice ids and chunk indices fixed up
+        std::vector<std::size_t> row_at(jobs.size() + 1, rowrec_.size()), col_at(jobs.size() + 1, colrec_.size());
+        std::vector<std::int32_t> chunk0(jobs.size()), sidx(jobs.size());
+        for (std::size_t j = 0; j < jobs.size(); ++j) {
+            row_at[j + 1] = row_at[j] + shapes[j].rowrec.size();
+            col_at[j + 1] = col_at[j] + shapes[j].colrec.size();
+            chunk0[j] = static_cast<std::int32_t>(r_.size());
+            sidx[j] = static_cast<std::int32_t>(slicerec_.size() / 2);
+            append_slice(std::move(shapes[j]), col_at[j] / 4);
+        }
+        rowrec_.resize(row_at.back());
+        colrec_.resize(col_at.back());
+        auto place = [&](std::size_t j) {
+            const auto& sh = shapes[j];
+            std::int32_t* rr = rowrec_.data() + row_at[j];
+            for (std::size_t i = 0; i < sh.rowrec.size(); i += 4) {
+                rr[i] = sh.rowrec[i];
+                rr[i + 1] = sh.rowrec[i + 1];
+                rr[i + 2] = sh.rowrec[i + 2];
+                rr[i + 3] = sidx[j];
+            }
+            std::int32_t* cr = colrec_.data() + col_at[j];
+            for (std::size_t i = 0; i < sh.colrec.size(); i += 4) {
+                cr[i] = sh.colrec[i] + chunk0[j];
+                cr[i + 1] = sh.colrec[i + 1];
+                cr[i + 2] = sh.colrec[i + 2];
+                cr[i + 3] = sh.colrec[i + 3];
+            }
+        };
+        if (big && jobs.size() > 1)
+            HostPool::get().run(jobs.size(), place);
+        else
+            for (std::size_t j = 0; j < jobs.size(); ++j) place(j);
+        if (pending) std::rethrow_exception(pending);
     }
     // this rank's chunks (round-robin over global chunk indices);
     // world == 1 keeps every chunk
@@ -162,6 +231,7 @@ BatchedSpmv::BatchedSpmv(spmvgpu_ctx* ctx, const HeParams& hp, std::span<const C
         img_ = client_image_take(ctx_, nnz_total, vec_total, rowrec_.size() / 4, slicerec_.size() / 2,
                                  colrec_.size() / 4, static_cast<int>(2 * n));
     }
+    const auto t1b = std::chrono::steady_clock::now();
     {
         // (dst, src, bytes) pieces of the image; large batches copy them on the host pool
         std::vector<std::tuple<unsigned char*, const void*, std::size_t>> cp;
@@ -207,7 +277,8 @@ BatchedSpmv::BatchedSpmv(spmvgpu_ctx* ctx, const HeParams& hp, std::span<const C
     if (trace) {
         const auto t2 = std::chrono::steady_clock::now();
         auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
-        std::fprintf(stderr, "e2e-trace shapes %.1f image %.1f us\n", us(t0, t1), us(t1, t2));
+        std::fprintf(stderr, "e2e-trace shapes %.1f image %.1f (take %.1f) us\n", us(t0, t1), us(t1, t2),
+                     us(t1, t1b));
     }
     if (hit) return;
     lease_.key = std::move(key);
@@ -230,16 +301,16 @@ BatchedSpmv::BatchedSpmv(spmvgpu_ctx* ctx, const HeParams& hp, std::span<const C
 // descending length gives the CSSC row order; aligned column j has height
 // h_j = #rows longer than j; chunks open at a column, fix h, and admit columns
 // while h (k + 1) <= budget.  The entries themselves are scattered on the
-// device (k_pack_cssc) from the row records built here.
-void BatchedSpmv::add_slice(const CsrView& m, std::size_t mat, std::size_t r0, std::size_t r1, std::size_t budget,
-                            std::int64_t nz_base, std::int64_t vec_base) {
+// device (k_pack_cssc) from the row records built here.  Independent per
+// slice (chunk indices and the slice id are local, fixed up by append_slice).
+void BatchedSpmv::shape_slice(const CsrView& m, const SliceJob& job, std::size_t budget, SliceShape& s) const {
     // per-slice checks in the reference's order (protocol.cpp:80-90)
     if (budget == 0 || budget > hp_.slot_count)
         throw std::invalid_argument("spmv: chunk_size must be in [1, slot_count]");
-    Slice s;
-    s.mat = mat;
-    s.rows = r1 - r0;
-    const std::uint64_t* rp = m.row_ptrs + r0;
+    s.mat = job.mat;
+    s.rows = job.r1 - job.r0;
+    s.vec_base = static_cast<std::int32_t>(job.vec_base);
+    const std::uint64_t* rp = m.row_ptrs + job.r0;
     std::size_t max_len = 0;
     for (std::size_t i = 0; i < s.rows; ++i) max_len = std::max<std::size_t>(max_len, rp[i + 1] - rp[i]);
     // histogram of the lengths, slot max_len - len + 1 (descending order);
@@ -259,45 +330,49 @@ void BatchedSpmv::add_slice(const CsrView& m, std::size_t mat, std::size_t r0, s
     // device row records {nz_begin, len, pos, slice} of the non-empty rows,
     // which take the first height[0] positions
     const std::size_t nonempty = max_len ? height[0] : 0;
-    const auto sidx = static_cast<std::int32_t>(slicerec_.size() / 2);
-    const std::size_t rw0 = rowrec_.size();
-    rowrec_.resize(rw0 + 4 * nonempty);
-    std::int32_t* rr = rowrec_.data() + rw0;
+    s.rowrec.resize(4 * nonempty);
+    std::int32_t* rr = s.rowrec.data();
     s.row_map.resize(s.rows);
     for (std::size_t i = 0; i < s.rows; ++i) {
         const std::size_t len = rp[i + 1] - rp[i];
         const std::uint32_t p = bucket[max_len - len]++;
         s.row_map[p] = i;
         if (len) {
-            rr[4 * p] = static_cast<std::int32_t>(nz_base + static_cast<std::int64_t>(rp[i]));
+            rr[4 * p] = static_cast<std::int32_t>(job.nz_base + static_cast<std::int64_t>(rp[i]));
             rr[4 * p + 1] = static_cast<std::int32_t>(len);
             rr[4 * p + 2] = static_cast<std::int32_t>(p);
-            rr[4 * p + 3] = sidx;
+            rr[4 * p + 3] = 0;  // slice id, set by append_slice
         }
     }
+    s.colrec.resize(4 * max_len);
+    std::int32_t* cr = s.colrec.data();
+    std::size_t cw = 0;
+    for (std::size_t first = 0; first < max_len;) {
+        const std::size_t h = height[first];
+        const std::size_t fit = std::min<std::size_t>(budget / h, max_len - first);
+        const auto chunk = static_cast<std::int32_t>(s.r.size());  // local; append_slice offsets it
+        for (std::size_t k = 0; k < fit; ++k, cw += 4) {
+            cr[cw] = chunk;
+            cr[cw + 1] = static_cast<std::int32_t>(k);
+            cr[cw + 2] = static_cast<std::int32_t>(h);
+            cr[cw + 3] = 0;
+        }
+        s.r.push_back(h);
+        s.c.push_back(fit);
+        first += fit;
+    }
+}
+
+void BatchedSpmv::append_slice(SliceShape&& sh, std::size_t col_base) {
+    Slice s;
+    s.mat = sh.mat;
+    s.rows = sh.rows;
+    s.row_map = std::move(sh.row_map);
     s.first_chunk = r_.size();
-    const auto col_base = static_cast<std::int32_t>(colrec_.size() / 4);
-    {
-        std::size_t cw = colrec_.size();
-        colrec_.resize(cw + 4 * max_len);
-        std::int32_t* cr = colrec_.data();
-        for (std::size_t first = 0; first < max_len;) {
-            const std::size_t h = height[first];
-            const std::size_t fit = std::min<std::size_t>(budget / h, max_len - first);
-            const auto chunk = static_cast<std::int32_t>(r_.size());
-            for (std::size_t k = 0; k < fit; ++k, cw += 4) {
-                cr[cw] = chunk;
-                cr[cw + 1] = static_cast<std::int32_t>(k);
-                cr[cw + 2] = static_cast<std::int32_t>(h);
-                cr[cw + 3] = 0;
-            }
-            r_.push_back(h);
-            c_.push_back(fit);
-            first += fit;
-        }
-    }
+    r_.insert(r_.end(), sh.r.begin(), sh.r.end());
+    c_.insert(c_.end(), sh.c.begin(), sh.c.end());
     s.n_ct = r_.size() - s.first_chunk;
-    slicerec_.insert(slicerec_.end(), {col_base, static_cast<std::int32_t>(vec_base)});
+    slicerec_.insert(slicerec_.end(), {static_cast<std::int32_t>(col_base), sh.vec_base});
     if (s.n_ct) s.result = static_cast<int>(n_out_++);
     for (std::size_t i = 0; i < s.n_ct; ++i) slice_id_.push_back(static_cast<std::uint32_t>(s.result));
     slices_.push_back(std::move(s));
@@ -374,6 +449,47 @@ std::vector<SpmvResult> BatchedSpmv::finish_words(const std::uint64_t* words) {
     if (n_out_) check_status(spmvgpu_ct_alloc(ctx_, n_out_, tmp.data()));
     try {
         for (std::size_t r = 0; r < n_out_; ++r) check_status(spmvgpu_ct_upload(ctx_, tmp[r], words + r * ctw));
+        auto res = decrypt_and_report(tmp);
+        if (n_out_) spmvgpu_ct_free(ctx_, tmp.data(), tmp.size());
+        return res;
+    } catch (...) {
+        if (n_out_) spmvgpu_ct_free(ctx_, tmp.data(), tmp.size());
+        throw;
+    }
+}
+
+void BatchedSpmv::result_words_dev(std::uint64_t* dev) {
+    std::uint64_t n = 0, slots = 0, ctw = 0, kw = 0;
+    int dnum = 0;
+    check_status(spmvgpu_ctx_sizes(ctx_, &n, &slots, &ctw, &kw, &dnum));
+    auto* st = static_cast<cudaStream_t>(spmvgpu_stream(ctx_));
+    for (std::size_t r = 0; r < n_out_; ++r) {
+        std::uint64_t* dst = dev + r * ctw;
+        cudaError_t e;
+        if (res_local_[r] >= 0)
+            e = cudaMemcpyAsync(dst, reinterpret_cast<const void*>(lease_.out[static_cast<std::size_t>(res_local_[r])]),
+                                8 * ctw, cudaMemcpyDeviceToDevice, st);
+        else
+            e = cudaMemsetAsync(dst, 0, 8 * ctw, st);
+        if (e != cudaSuccess) throw std::runtime_error(std::string("result_words_dev: ") + cudaGetErrorString(e));
+    }
+    check_status(spmvgpu_sync(ctx_));  // the caller's collective runs on another stream
+}
+
+std::vector<SpmvResult> BatchedSpmv::finish_words_dev(std::uint64_t* dev) {
+    std::uint64_t n = 0, slots = 0, ctw = 0, kw = 0;
+    int dnum = 0;
+    check_status(spmvgpu_ctx_sizes(ctx_, &n, &slots, &ctw, &kw, &dnum));
+    check_status(spmvgpu_fold_mod(ctx_, dev, n_out_));
+    std::vector<spmvgpu_ct> tmp(n_out_, 0);
+    if (n_out_) check_status(spmvgpu_ct_alloc(ctx_, n_out_, tmp.data()));
+    try {
+        auto* st = static_cast<cudaStream_t>(spmvgpu_stream(ctx_));
+        for (std::size_t r = 0; r < n_out_; ++r) {
+            const cudaError_t e = cudaMemcpyAsync(reinterpret_cast<void*>(tmp[r]), dev + r * ctw, 8 * ctw,
+                                                  cudaMemcpyDeviceToDevice, st);
+            if (e != cudaSuccess) throw std::runtime_error(std::string("finish_words_dev: ") + cudaGetErrorString(e));
+        }
         auto res = decrypt_and_report(tmp);
         if (n_out_) spmvgpu_ct_free(ctx_, tmp.data(), tmp.size());
         return res;

@@ -8,6 +8,7 @@
 #pragma once
 
 #include <cstdint>
+#include <exception>
 #include <span>
 #include <vector>
 
@@ -48,6 +49,12 @@ public:
     // no chunk of), [results][ct words]; and the decryption of summed words
     std::vector<std::uint64_t> result_words();
     std::vector<SpmvResult> finish_words(const std::uint64_t* words);
+    // the same with the words in device memory (the ranks' buffers summed by an
+    // NCCL all-reduce): result_words_dev copies this rank's partial results
+    // into `dev` (zeros for slices it holds none of) and waits; finish_words_dev
+    // folds `dev` mod q_j in place on the device, then decrypts
+    void result_words_dev(std::uint64_t* dev);
+    std::vector<SpmvResult> finish_words_dev(std::uint64_t* dev);
     std::size_t result_count() const { return n_out_; }
 
     spmvgpu_plan* plan() const { return lease_.plan; }
@@ -65,8 +72,22 @@ private:
         std::size_t n_ct = 0;
         int result = -1;                   // result ciphertext index, -1 when no chunks
     };
-    void add_slice(const CsrView& m, std::size_t mat, std::size_t r0, std::size_t r1, std::size_t budget,
-                   std::int64_t nz_base, std::int64_t vec_base);
+    struct SliceJob {  // rows [r0, r1) of matrix `mat`
+        std::size_t mat = 0, r0 = 0, r1 = 0;
+        std::int64_t nz_base = 0, vec_base = 0;
+    };
+    struct SliceShape {  // one slice's CSSC shapes, chunk indices and slice id local
+        std::size_t mat = 0, rows = 0;
+        std::int32_t vec_base = 0;
+        std::vector<std::size_t> row_map;
+        std::vector<std::int32_t> rowrec, colrec;
+        std::vector<std::uint64_t> r, c;
+        std::exception_ptr err;
+    };
+    void shape_slice(const CsrView& m, const SliceJob& job, std::size_t budget, SliceShape& out) const;
+    // slice metadata, chunk shapes and slice record; the row / column records
+    // are placed by the caller (col_base = the slice's first column record)
+    void append_slice(SliceShape&& s, std::size_t col_base);
     void ensure_plan();
     std::vector<SpmvResult> decrypt_and_report(const std::vector<spmvgpu_ct>& outs);
     std::vector<SpmvResult> report(const std::vector<std::uint64_t>& slots, const std::vector<std::int32_t>& measured);

@@ -97,8 +97,22 @@ def disjoint_streams(ctx, rank: int) -> None:
 
 
 def finish_chunk_split(ctx, job, device=None):
-    """Sum this rank's partial result ciphertexts with every other rank's (one
-    all-reduce), fold mod q and decrypt at rank 0 (returns results there)."""
+    """Sum this rank's partial result ciphertexts with every other rank's and
+    decrypt at rank 0 (returns results there).  On a GPU the partial words stay
+    in device memory: one NCCL all-reduce (int64 sum) over the job's result
+    buffer, then the library's mod-q fold kernel and the decryption; the host
+    path (reduce_partials) serves gloo / CPU runs."""
+    import torch
+    import torch.distributed as dist
+
+    if dist.get_backend() == "nccl":
+        if dist.get_world_size() > 16:
+            raise ValueError("chunk split: the uint64 sum is exact for at most 16 ranks")
+        dev = job.result_words_dev()
+        torch.cuda.synchronize(dev.device)
+        dist.all_reduce(dev)  # residues < 2^58, <= 16 ranks: no int64 overflow
+        torch.cuda.synchronize(dev.device)
+        return job.finish_words_dev(dev) if dist.get_rank() == 0 else None
     words = job.result_words()
     summed = reduce_partials(words, ctx.primes, ctx.L, ctx.n, device)
     return job.finish_words(summed) if summed is not None else None

@@ -187,6 +187,41 @@ def test_chunk_split_shards_sum_to_the_full_result(world):
     ctx.close()
 
 
+@pytest.mark.parametrize("world", [2, 3])
+def test_chunk_split_device_reduction(world):
+    """The device path of the chunk split: each shard copies its partial result
+    ciphertexts into a device buffer (what NCCL all-reduces across GPUs), the
+    buffers are summed on the device, and the library folds mod q on the GPU and
+    decrypts; equals the reference, and the fold equals the host fold."""
+    import torch
+
+    ctx = pk.Context(logn=10, seed=8)
+    m = synth.random_sparse_csr(1300, 700, 6000, 78, -8, 8)
+    v = synth.random_vector(700, 78, -8, 8, nonzero=True)
+    from paper_2603_04742_b200 import shard
+    total, host_total, jobs = None, None, []
+    for r in range(world):
+        job = pk.Job(ctx, [m], [v], rank=r, world=world)
+        job.encrypt()
+        job.cloud(graph=False)
+        d = job.result_words_dev()
+        total = d if total is None else total + d  # the all-reduce's int64 sum
+        w = job.result_words()
+        host_total = w if host_total is None else host_total + w
+        jobs.append(job)
+    torch.cuda.synchronize()
+    assert np.array_equal(total.cpu().numpy().view(np.uint64).reshape(host_total.shape), host_total)
+    got = jobs[0].finish_words_dev(total)[0]
+    folded = shard.fold_mod(host_total, ctx.primes, ctx.L, ctx.n)
+    assert np.array_equal(total.cpu().numpy().view(np.uint64).reshape(folded.shape), folded)
+    want = checker(m, v, ctx.slots, ctx.slots)
+    assert np.array_equal(got["values"], want["values"])
+    assert got["ledger"] == want["ledger"] and got["noise"] == want["noise"]
+    for j in jobs:
+        j.close()
+    ctx.close()
+
+
 def test_context_shared_across_host_threads():
     """a backend may be shared by host threads; calls on one
     context serialise and every result stays the reference's."""
@@ -311,12 +346,10 @@ def test_batch_vector_length_checked_at_the_c_abi():
     ctx = pk.Context(logn=10, seed=3)
     m = synth.random_sparse_csr(20, 30, 50, 1, -8, 8)
     keep = []
-    csrs = (pk.CsrC * 1)(pk._csr_c(m, keep))
+    csrs = pk._csr_table([m], keep)
     vptr, vlens = pk._vectors([m], [np.ones(29, np.int64)], keep)  # one entry short
-    outs = np.zeros(20, np.int64)
-    optr = (pk.i64p * 1)(pk._p(outs, pk.i64p))
-    res = (pk.ResultC * 1)()
-    assert pk.lib().cssc_spmv_batch(ctx.h, csrs, vptr, vlens, 1, ctx.slots, 0, optr, res) == -4
+    _, _, _, optr, res = pk._outputs([m], keep)
+    assert pk.lib().cssc_spmv_batch(ctx.h, pk._addr(csrs), vptr, vlens, 1, ctx.slots, 0, optr, pk._addr(res)) == -4
     assert b"does not match" in pk.lib().spmvgpu_last_error()
     with pytest.raises(pk.SpmvError) as e:
         pk.spmv_batch(ctx, [m], [np.ones(31, np.int64)])
