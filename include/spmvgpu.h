@@ -38,7 +38,8 @@ enum {
     SPMVGPU_ERR_DUPLICATE = -7,         /* DuplicateEntryError */
     SPMVGPU_ERR_CUDA = -8,
     SPMVGPU_ERR_INTERNAL = -9,
-    SPMVGPU_ERR_NON_SQUARE = -10        /* NonSquareError (diagonal method) */
+    SPMVGPU_ERR_NON_SQUARE = -10,       /* NonSquareError (diagonal method) */
+    SPMVGPU_ERR_PARSE = -11             /* ParseError (malformed CSSC buffer) */
 };
 
 typedef struct spmvgpu_ctx spmvgpu_ctx;
@@ -283,6 +284,16 @@ void cssc_job_destroy(cssc_job* j);
 int64_t cssc_pack_chunks(const cssc_csr* m, uint64_t budget, int64_t* r_list, int64_t* c_list,
                          int64_t* vflat, int64_t* cflat, int64_t* row_map, uint64_t* flat_total);
 int cssc_rotation_schedule(uint64_t rows, uint64_t cols, uint64_t* offsets, int32_t* from_acc);
+/* CSSC persistence, in place of `spmv convert` (reference
+ * tools/spmv_main.cpp:39-58): csr_to_cssc + validate_cssc, then the compact
+ * binary form (buf NULL: size only) or the reference's JSON text (same bytes
+ * as its ordered_json dump(2)); cssc_load_binary returns the CSSC arrays
+ * (va, ci, rm, cp; NULL arrays: sizes only) and raises ParseError on a
+ * malformed buffer */
+int cssc_convert_binary(const cssc_csr* m, uint8_t* buf, uint64_t cap, uint64_t* written);
+int cssc_convert_json(const cssc_csr* m, char* buf, uint64_t cap, uint64_t* written);
+int cssc_load_binary(const uint8_t* buf, uint64_t len, uint64_t* rows, uint64_t* cols, uint64_t* nnz,
+                     uint64_t* aligned_cols, int64_t* va, uint64_t* ci, uint64_t* rm, uint64_t* cp);
 
 #ifdef __cplusplus
 }

@@ -14,6 +14,9 @@
 //   csr_to_cssc           proj/src/sparse.cpp:79-117
 //   generate_chunks       proj/src/chunk.cpp:10-50
 //   diag_spmv             proj/src/diagonal.cpp:44-104
+//   spmv convert JSON     proj/tools/spmv_main.cpp:39-58 (csr_to_cssc,
+//                         validate_cssc, ordered_json dump(2); needs the
+//                         nlohmann/json header the CLI uses)
 //   cloud section         proj/src/protocol.cpp:121-134 (multiply,
 //                         intra_chunk_sum, inter_chunk_sum on the prepared
 //                         client ciphertexts of every row slice)
@@ -33,6 +36,11 @@
 #include "spmv/reorg.hpp"
 #include "spmv/sparse.hpp"
 #include "spmv/synthetic.hpp"
+
+#if __has_include(<nlohmann/json.hpp>)
+#include <nlohmann/json.hpp>
+#define REF_HAVE_JSON 1
+#endif
 
 namespace {
 thread_local std::string g_err;
@@ -228,6 +236,47 @@ int64_t ref_chunks(uint64_t rows, uint64_t cols, const int64_t* rp, const int64_
     } catch (const std::exception& e) {
         return classify(e);
     }
+}
+
+// csr_to_cssc of the reference: sizes first (null arrays), then va/ci/rm/cp
+int64_t ref_csr_to_cssc(uint64_t rows, uint64_t cols, const int64_t* rp, const int64_t* ci, const int64_t* va,
+                        int64_t* out_va, int64_t* out_ci, int64_t* out_rm, int64_t* out_cp, uint64_t* aligned) {
+    try {
+        const spmv::CsscMatrix c = spmv::csr_to_cssc(make_csr(rows, cols, rp, ci, va));
+        *aligned = c.aligned_cols();
+        if (out_va) {
+            for (size_t k = 0; k < c.va.size(); ++k) out_va[k] = c.va[k], out_ci[k] = static_cast<int64_t>(c.ci[k]);
+            for (size_t k = 0; k < c.rm.size(); ++k) out_rm[k] = static_cast<int64_t>(c.rm[k]);
+            for (size_t k = 0; k < c.cp.size(); ++k) out_cp[k] = static_cast<int64_t>(c.cp[k]);
+        }
+        return static_cast<int64_t>(c.nnz());
+    } catch (const std::exception& e) {
+        return classify(e);
+    }
+}
+
+// the text `spmv convert` writes (tools/spmv_main.cpp:50-54): length, then bytes
+int64_t ref_cssc_json(uint64_t rows, uint64_t cols, const int64_t* rp, const int64_t* ci, const int64_t* va,
+                      char* out, uint64_t cap) {
+#ifdef REF_HAVE_JSON
+    try {
+        const spmv::CsscMatrix cssc = spmv::csr_to_cssc(make_csr(rows, cols, rp, ci, va));
+        using ordered_json = nlohmann::ordered_json;
+        ordered_json j{
+            {"rows", cssc.rows}, {"cols", cssc.cols}, {"va", cssc.va},
+            {"ci", cssc.ci},     {"rm", cssc.rm},     {"cp", cssc.cp},
+        };
+        const std::string text = j.dump(2) + "\n";
+        if (out && cap >= text.size()) std::memcpy(out, text.data(), text.size());
+        return static_cast<int64_t>(text.size());
+    } catch (const std::exception& e) {
+        return classify(e);
+    }
+#else
+    (void)rows, (void)cols, (void)rp, (void)ci, (void)va, (void)out, (void)cap;
+    g_err = "built without nlohmann/json";
+    return -8;
+#endif
 }
 
 // ---- cloud-section probe (bench.py --impl reference `value`) ----

@@ -151,6 +151,10 @@ _SIGS = {
     "cssc_job_destroy": (None, [C.c_void_p]),
     "cssc_pack_chunks": (C.c_int64, [C.POINTER(CsrC), C.c_uint64, i64p, i64p, i64p, i64p, i64p, u64p]),
     "cssc_rotation_schedule": (C.c_int, [C.c_uint64, C.c_uint64, u64p, i32p]),
+    "cssc_convert_binary": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, u64p]),
+    "cssc_convert_json": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, u64p]),
+    "cssc_load_binary": (C.c_int, [C.c_void_p, C.c_uint64, u64p, u64p, u64p, u64p, C.c_void_p, C.c_void_p,
+                                   C.c_void_p, C.c_void_p]),
 }
 
 _lib = None
@@ -173,7 +177,7 @@ def lib() -> C.CDLL:
 
 STATUS = {-1: ValueError, -2: "OverLengthError", -3: "NoiseExhaustedError", -4: "DimensionMismatchError",
           -5: "ColumnTooTallError", -6: "IndexOutOfRangeError", -7: "DuplicateEntryError",
-          -8: RuntimeError, -9: RuntimeError, -10: "NonSquareError"}
+          -8: RuntimeError, -9: RuntimeError, -10: "NonSquareError", -11: "ParseError"}
 
 
 class SpmvError(RuntimeError):
@@ -766,3 +770,42 @@ def pack_chunks(m: Csr, budget: int) -> dict:
                            _p(rm, i64p), C.byref(tot))
     return {"n_ct": int(n), "r": r[:n], "c": c[:n], "vflat": vf[: tot.value], "cflat": cf[: tot.value],
             "row_map": rm[: m.rows]}
+
+
+# ---- CSSC persistence (the reference's `spmv convert`) ----
+def cssc_to_bytes(m) -> bytes:
+    """csr_to_cssc + validate_cssc, then the compact binary CSSC form."""
+    keep: list = []
+    t = _csr_table([m], keep)
+    n = C.c_uint64()
+    check(lib().cssc_convert_binary(_addr(t), None, 0, C.byref(n)))
+    buf = np.zeros(max(n.value, 1), np.uint8)
+    check(lib().cssc_convert_binary(_addr(t), _addr(buf), buf.size, C.byref(n)))
+    return buf[: n.value].tobytes()
+
+
+def cssc_to_json(m) -> str:
+    """The JSON text `spmv convert` writes for the same matrix (byte for byte)."""
+    keep: list = []
+    t = _csr_table([m], keep)
+    n = C.c_uint64()
+    check(lib().cssc_convert_json(_addr(t), None, 0, C.byref(n)))
+    buf = np.zeros(max(n.value, 1), np.uint8)
+    check(lib().cssc_convert_json(_addr(t), _addr(buf), buf.size, C.byref(n)))
+    return buf[: n.value].tobytes().decode()
+
+
+def cssc_from_bytes(data: bytes) -> dict:
+    """The CSSC arrays {rows, cols, va, ci, rm, cp} of a binary buffer."""
+    b = np.frombuffer(data, np.uint8).copy() if data else np.zeros(1, np.uint8)
+    r, c, nz, L = (C.c_uint64() for _ in range(4))
+    check(lib().cssc_load_binary(_addr(b), len(data), C.byref(r), C.byref(c), C.byref(nz), C.byref(L),
+                                 None, None, None, None))
+    va = np.zeros(max(nz.value, 1), np.int64)
+    ci = np.zeros(max(nz.value, 1), np.uint64)
+    rm = np.zeros(max(r.value, 1), np.uint64)
+    cp = np.zeros(L.value + 1, np.uint64)
+    check(lib().cssc_load_binary(_addr(b), len(data), C.byref(r), C.byref(c), C.byref(nz), C.byref(L),
+                                 _addr(va), _addr(ci), _addr(rm), _addr(cp)))
+    return {"rows": r.value, "cols": c.value, "va": va[: nz.value], "ci": ci[: nz.value].astype(np.int64),
+            "rm": rm[: r.value].astype(np.int64), "cp": cp.astype(np.int64)}

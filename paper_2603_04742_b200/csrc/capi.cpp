@@ -84,6 +84,8 @@ int guard(F&& f) {
         return fail(SPMVGPU_ERR_DUPLICATE, e.what());
     } catch (const spmv::NonSquareError& e) {
         return fail(SPMVGPU_ERR_NON_SQUARE, e.what());
+    } catch (const spmv::ParseError& e) {
+        return fail(SPMVGPU_ERR_PARSE, e.what());
     } catch (const std::invalid_argument& e) {
         return fail(SPMVGPU_ERR_INVALID_ARGUMENT, e.what());
     } catch (const std::bad_alloc&) {
@@ -1047,6 +1049,49 @@ int cssc_rotation_schedule(uint64_t rows, uint64_t cols, uint64_t* offsets, int3
         n = (int)s.size();
     });
     return st == SPMVGPU_OK ? n : st;
+}
+
+static spmv::CsscMatrix converted(const cssc_csr* m) {
+    if (!m) throw std::invalid_argument("null matrix");
+    spmv::CsscMatrix c = spmv::csr_to_cssc(to_csr(*m));
+    const auto bad = spmv::validate_cssc(c);
+    if (!bad.empty()) throw std::runtime_error("conversion produced an invalid structure: " + bad.front());
+    return c;
+}
+int cssc_convert_binary(const cssc_csr* m, uint8_t* buf, uint64_t cap, uint64_t* written) {
+    return guard([&] {
+        if (!written) throw std::invalid_argument("null argument");
+        const auto bytes = spmv::cssc_to_bytes(converted(m));
+        *written = bytes.size();
+        if (!buf) return;
+        if (cap < bytes.size()) throw std::length_error("convert: buffer too small");
+        std::memcpy(buf, bytes.data(), bytes.size());
+    });
+}
+int cssc_convert_json(const cssc_csr* m, char* buf, uint64_t cap, uint64_t* written) {
+    return guard([&] {
+        if (!written) throw std::invalid_argument("null argument");
+        const std::string j = spmv::cssc_to_json(converted(m));
+        *written = j.size();
+        if (!buf) return;
+        if (cap < j.size()) throw std::length_error("convert: buffer too small");
+        std::memcpy(buf, j.data(), j.size());
+    });
+}
+int cssc_load_binary(const uint8_t* buf, uint64_t len, uint64_t* rows, uint64_t* cols, uint64_t* nnz,
+                     uint64_t* aligned_cols, int64_t* va, uint64_t* ci, uint64_t* rm, uint64_t* cp) {
+    return guard([&] {
+        if (!buf || !rows || !cols || !nnz || !aligned_cols) throw std::invalid_argument("null argument");
+        const spmv::CsscMatrix c = spmv::cssc_from_bytes(std::span<const uint8_t>(buf, len));
+        *rows = c.rows;
+        *cols = c.cols;
+        *nnz = c.nnz();
+        *aligned_cols = c.aligned_cols();
+        if (va) std::memcpy(va, c.va.data(), 8 * c.va.size());
+        if (ci) for (size_t k = 0; k < c.ci.size(); ++k) ci[k] = c.ci[k];
+        if (rm) for (size_t k = 0; k < c.rm.size(); ++k) rm[k] = c.rm[k];
+        if (cp) for (size_t k = 0; k < c.cp.size(); ++k) cp[k] = c.cp[k];
+    });
 }
 
 }  // extern "C"
