@@ -24,7 +24,9 @@ from pathlib import Path
 import numpy as np
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "lib" / "libcssc_he.so"
+# CSSC_LIB selects another build of the same library (the sanitizer build of
+# tools/asan_check.sh); the default is the in-tree product build
+LIB_PATH = Path(os.environ["CSSC_LIB"]) if os.environ.get("CSSC_LIB") else _PKG / "lib" / "libcssc_he.so"
 
 u64p = C.POINTER(C.c_uint64)
 i64p = C.POINTER(C.c_int64)

@@ -86,6 +86,40 @@ def build(verbose: bool = False, jobs: int | None = None) -> Path:
     return LIB
 
 
+def build_sanitized(out: Path, verbose: bool = False) -> Path:
+    """The same library with AddressSanitizer + UBSan on every host code path
+    (the .cpp files and the host side of the .cu files), for the CPU-side
+    checks of tools/asan_check.sh (compute-sanitizer is closed on this GPU
+    pool).  Objects and the .so go to `out`, never next to the product."""
+    out = Path(out)
+    out.mkdir(parents=True, exist_ok=True)
+    san = ["-fsanitize=address", "-fsanitize=undefined", "-fno-omit-frame-pointer", "-g"]  # nvcc splits on ","
+    cu, cpp = _sources()
+
+    def run(src):
+        o = out / (str(src.relative_to(CSRC)).replace("/", "__") + ".o")
+        if src.suffix == ".cu":
+            cmd = [NVCC, "-std=c++20", "-O1", *ARCH, "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr", *INCLUDES,
+                   *[x for f in san for x in ("-Xcompiler", f)], "-c", str(src), "-o", str(o)]
+        else:
+            cmd = ["g++", "-std=c++20", "-O1", "-fPIC", *san, *INCLUDES, "-c", str(src), "-o", str(o)]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"compile failed: {src}\n{r.stdout}\n{r.stderr}")
+        return str(o)
+
+    with cf.ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
+        objs = list(ex.map(run, cu + cpp))
+    lib = out / "libcssc_he.so"
+    r = subprocess.run([NVCC, "-shared", *ARCH, "-o", str(lib), *objs, "-Xcompiler",
+                        "-fsanitize=address", "-Xcompiler", "-fsanitize=undefined"], capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"link failed\n{r.stdout}\n{r.stderr}")
+    return lib
+
+
 def build_oracle(verbose: bool = False) -> None:
     """Test-side checkers (oracle/build, oracle/_ref); not part of the product."""
     r = subprocess.run(["make", "-C", str(ROOT / "oracle"), "all"], capture_output=True, text=True)

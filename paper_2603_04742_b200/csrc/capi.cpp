@@ -1087,7 +1087,7 @@ int cssc_load_binary(const uint8_t* buf, uint64_t len, uint64_t* rows, uint64_t*
         *cols = c.cols;
         *nnz = c.nnz();
         *aligned_cols = c.aligned_cols();
-        if (va) std::memcpy(va, c.va.data(), 8 * c.va.size());
+        if (va && !c.va.empty()) std::memcpy(va, c.va.data(), 8 * c.va.size());
         if (ci) for (size_t k = 0; k < c.ci.size(); ++k) ci[k] = c.ci[k];
         if (rm) for (size_t k = 0; k < c.rm.size(); ++k) rm[k] = c.rm[k];
         if (cp) for (size_t k = 0; k < c.cp.size(); ++k) cp[k] = c.cp[k];

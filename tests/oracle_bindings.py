@@ -12,7 +12,10 @@ from pathlib import Path
 import numpy as np
 
 ROOT = Path(__file__).resolve().parent.parent
-ORACLE_SO = ROOT / "oracle" / "build" / "liboracle.so"
+import os  # noqa: E402
+
+# CSSC_ORACLE_SO: the sanitizer build of tools/asan_check.sh
+ORACLE_SO = Path(os.environ.get("CSSC_ORACLE_SO") or ROOT / "oracle" / "build" / "liboracle.so")
 REF_SO = ROOT / "oracle" / "_ref" / "libspmv_ref.so"
 
 u64p = C.POINTER(C.c_uint64)
