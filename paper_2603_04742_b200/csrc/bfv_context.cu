@@ -599,6 +599,7 @@ void GpuContext::mul_relin_dev(const u64* const* A, const u64* const* B, u64* co
     const int L = P_.cfg.L, K = P_.cfg.K, LK = L + K, M = L + P_.nB, logn = P_.cfg.logn;
     std::vector<int> pm;
     for (int j = 0; j < M; ++j) pm.push_back(j < L ? j : K + j);
+    bool lazy_z = false;
     if (enc)
         launch_mul_extend_enc(dc_, P_, *enc, T, items, st_);
     else
@@ -609,14 +610,17 @@ void GpuContext::mul_relin_dev(const u64* const* A, const u64* const* B, u64* co
         kmark("k_ntt_cols fwd (multiply)", st_);
         launch_mul_blocks_tensor(dc_, P_, T, Z, items, st_);
         kmark("k_mul_blocks_tensor", st_);
-        launch_ntt_phase(dc_, logn, true, true, job(Z, Z, 3 * M, pm), items, st_);
+        NttJob jz = job(Z, Z, 3 * M, pm);
+        jz.lazy_out = fixed_rns_shape(P_) ? 1 : 0;  // the fixed-shape scale folds N^-1 into its constants
+        launch_ntt_phase(dc_, logn, true, true, jz, items, st_);
+        lazy_z = jz.lazy_out != 0;
         kmark("k_ntt_cols inv (multiply)", st_);
     } else {
         launch_ntt(dc_, logn, false, job(T, T, 4 * M, pm), items, st_);
         launch_mul_tensor(dc_, P_, T, Z, items, st_);
         launch_ntt(dc_, logn, true, job(Z, Z, 3 * M, pm), items, st_);
     }
-    launch_mul_scale(dc_, P_, Z, OUT, D2, items, st_, fused_ks_ ? D2Y : nullptr);
+    launch_mul_scale(dc_, P_, Z, OUT, D2, items, st_, fused_ks_ ? D2Y : nullptr, lazy_z);
     kmark("k_mul_scale_k", st_);
     if (fused_ks_) {
         KsY ky;

@@ -157,11 +157,12 @@ __global__ void __launch_bounds__(Ntt2<LOGN>::TC, 256 / Ntt2<LOGN>::TC * 3) k_nt
     // radix-8 passes (3 CTAs per SM); 4-column tiles: radix-4, one group per thread
     line_ntt_v<G::A, 0, INV, (LN >= 8 ? 3 : 2), LN>(tile, ConstQ{q}, addr, twf, whole_cta());
     const u64 ni = dc->ninv[prime], nish = dc->ninv_sh[prime];
+    const bool scale = INV && !job.lazy_out;
 #pragma unroll
     for (int r = 0; r < G::R1 * SEG / T; ++r) {
         const int i = threadIdx.x + T * r, c = i / SEG, h = i % SEG;
         u64 a0 = tile[c * LN + 2 * h], a1 = tile[c * LN + 2 * h + 1];
-        if (INV) {
+        if (scale) {
             a0 = shoup(a0, ni, nish, q);
             a1 = shoup(a1, ni, nish, q);
         }
@@ -636,7 +637,9 @@ __global__ void k_mul_scale_k(const __grid_constant__ ScaleK<L> c, const u64* __
         d.a0 = d.am = rr;  // rr * (1 in 29-bit halves): leaves the middle column sum alone
 #pragma unroll
         for (int i = 0; i < L; ++i) dot29_mac(d, xi[i], c.C[i][j]);
-        dot29_mac(d, z[(size_t)(L + j) * n + k], c.D[j]);
+        u64 zb = z[(size_t)(L + j) * n + k];  // lazy (< 2b) when the inverse NTT left N^-1 to D
+        zb = zb >= c.bm[j].q ? zb - c.bm[j].q : zb;
+        dot29_mac(d, zb, c.D[j]);
         w[j] = dot29_reduce(d, c.bm[j]);
     }
     extend_k(c.bq, w, o);
@@ -658,22 +661,26 @@ static ExtendK<L> make_extend_k(const RnsParams& P) {
     return c;
 }
 
+// lazy: Z is the inverse NTT without its final x N^-1 (NttJob::lazy_out); N^-1
+// rides in the constants that multiply z (Qhat_i^-1 for the Q limbs, D_j for
+// the B limbs), so x_i and w_j -- hence the output words -- are unchanged
 template <int L>
-static ScaleK<L> make_scale_k(const RnsParams& P) {
+static ScaleK<L> make_scale_k(const RnsParams& P, bool lazy = false) {
     const DevConsts& h = P.host;
     ScaleK<L> c{};
     c.n = P.n;
     for (int i = 0; i < L; ++i) {
         c.q[i] = h.mod[i].q;
-        c.QhatInv[i] = h.QhatInv[i];
-        c.QhatInv_sh[i] = h.QhatInv_sh[i];
+        c.QhatInv[i] = lazy ? host_mulmod(h.QhatInv[i], h.ninv[i], c.q[i]) : h.QhatInv[i];
+        c.QhatInv_sh[i] = lazy ? shoup_factor(c.QhatInv[i], c.q[i]) : h.QhatInv_sh[i];
         c.T1[i] = h.T1[i];
         c.T0[i] = h.T0[i];
     }
     for (int j = 0; j <= L; ++j) {
-        c.bm[j] = h.mod[L + P.cfg.K + j];
+        const int bj = L + P.cfg.K + j;  // global prime index of b_j
+        c.bm[j] = h.mod[bj];
         const u64 b = c.bm[j].q, D = host_mulmod(h.QinvB[j], h.tB[j], b);
-        c.D[j] = split29(D);
+        c.D[j] = split29(lazy ? host_mulmod(D, h.ninv[bj], b) : D);
         for (int i = 0; i < L; ++i) c.C[i][j] = split29((b - host_mulmod(h.QhatB[i][j], D, b)) % b);
     }
     fill_extk(c.bq, h, h.extBQ);
@@ -820,14 +827,16 @@ __global__ void k_mul_scale(const DevConsts* __restrict__ dc, const u64* __restr
 }
 
 void launch_mul_scale(const DevConsts* dc, const RnsParams& P, const u64* Z, u64* const* OUT,
-                      u64* D2, int items, cudaStream_t st, u64* D2Y) {
+                      u64* D2, int items, cudaStream_t st, u64* D2Y, bool lazy_in) {
     if (!items) return;
     dispatch_shape(P, [&](auto l_, auto k_, auto a_) {
         dim3 g = ew_grid(P.n, items);
         g.z = 3;
         constexpr int LT = decltype(l_)::value;
         if constexpr (LT > 0)
-            k_mul_scale_k<LT><<<g, EW_THREADS, 0, st>>>(make_scale_k<LT>(P), Z, OUT, D2, D2Y);
+            k_mul_scale_k<LT><<<g, EW_THREADS, 0, st>>>(make_scale_k<LT>(P, lazy_in), Z, OUT, D2, D2Y);
+        else if (lazy_in)
+            throw std::invalid_argument("unscaled inverse-NTT input needs a fixed RNS shape");
         else if (D2Y)
             throw std::invalid_argument("hoisted ModUp factors need a fixed RNS shape");
         else
@@ -1055,7 +1064,9 @@ __global__ void __launch_bounds__(128, 6) k_ks_moddown_k(const __grid_constant__
     auto term = [&](int j, const u64* y, const u64* acc, const u64* rs, int ridx, bool neg) {
         const u64 q = c.qm[j].q;
         Dot29 d;
-        dot29_mac(d, acc[(size_t)j * n + k], c.F[j]);  // canonical inverse-NTT output
+        u64 a = acc[(size_t)j * n + k];  // lazy (< 2q) when the inverse NTT left N^-1 to F
+        a = a >= q ? a - q : a;
+        dot29_mac(d, a, c.F[j]);
 #pragma unroll
         for (int kk = 0; kk < K; ++kk) dot29_mac(d, y[kk], c.E[kk][j]);
         u64 v = dot29_reduce(d, c.qm[j]);
@@ -1077,6 +1088,7 @@ __global__ void __launch_bounds__(128, 6) k_ks_moddown_k(const __grid_constant__
 #pragma unroll
         for (int j = 0; j < L; ++j) {
             av[j] = acc[(size_t)j * n + k];
+            av[j] = av[j] >= c.qm[j].q ? av[j] - c.qm[j].q : av[j];
             bv[j] = base ? base[(size_t)j * n + k] : 0;
             if (ex) bv[j] = add_mod(bv[j], ex[(size_t)j * n + k], c.qm[j].q);
             rv[j] = rs ? rs[(size_t)j * n + ridx] : 0;
@@ -1123,22 +1135,24 @@ __global__ void __launch_bounds__(128, 6) k_ks_moddown_k(const __grid_constant__
     }
 }
 
+// lazy: ACC is the inverse NTT without its final x N^-1 (NttJob::lazy_out);
+// N^-1 rides in (P/p_k)^-1 (the y_k) and in P^-1 (the acc_j term)
 template <int L, int K>
-static ModDownK<L, K> make_moddown_k(const RnsParams& P) {
+static ModDownK<L, K> make_moddown_k(const RnsParams& P, bool lazy = false) {
     const DevConsts& h = P.host;
     ModDownK<L, K> c{};
     c.n = P.n;
     for (int kk = 0; kk < K; ++kk) {
         c.pk[kk] = h.mod[L + kk].q;
-        c.phat_inv[kk] = h.phat_inv[kk];
-        c.phat_inv_sh[kk] = h.phat_inv_sh[kk];
+        c.phat_inv[kk] = lazy ? host_mulmod(h.phat_inv[kk], h.ninv[L + kk], c.pk[kk]) : h.phat_inv[kk];
+        c.phat_inv_sh[kk] = lazy ? shoup_factor(c.phat_inv[kk], c.pk[kk]) : h.phat_inv_sh[kk];
     }
     for (int j = 0; j < L; ++j) {
         c.qm[j] = h.mod[j];
         c.dhi[j] = h.dig_hat_inv[j];
         c.dhi_sh[j] = h.dig_hat_inv_sh[j];
         const u64 q = h.mod[j].q;
-        c.F[j] = split29(h.Pinv_q[j]);
+        c.F[j] = split29(lazy ? host_mulmod(h.Pinv_q[j], h.ninv[j], q) : h.Pinv_q[j]);
         for (int kk = 0; kk < K; ++kk)
             c.E[kk][j] = split29((q - host_mulmod(h.phat_q[kk][j], h.Pinv_q[j], q)) % q);
     }
@@ -1148,15 +1162,17 @@ static ModDownK<L, K> make_moddown_k(const RnsParams& P) {
 void launch_ks_moddown(const DevConsts* dc, const RnsParams& P, const u64* ACC,
                        const u64* const* BASE, const u64* const* RSRC, const u32* ginv,
                        u64* const* OUT, int items, cudaStream_t st, const u64* const* EXTRA, const int* PAIR,
-                       u64* const* YOUT) {
+                       u64* const* YOUT, bool lazy_in) {
     if (!items) return;
     dispatch_shape(P, [&](auto l_, auto k_, auto a_) {
         dim3 g = ew_grid(P.n, items);
         g.z = 2;
         constexpr int LT = decltype(l_)::value, KT = decltype(k_)::value;
         if constexpr (LT > 0)
-            k_ks_moddown_k<LT, KT><<<g, EW_THREADS, 0, st>>>(make_moddown_k<LT, KT>(P), ACC, BASE, RSRC, ginv, OUT,
-                                                            EXTRA, PAIR, YOUT);
+            k_ks_moddown_k<LT, KT><<<g, EW_THREADS, 0, st>>>(make_moddown_k<LT, KT>(P, lazy_in), ACC, BASE, RSRC,
+                                                            ginv, OUT, EXTRA, PAIR, YOUT);
+        else if (lazy_in)
+            throw std::invalid_argument("unscaled inverse-NTT input needs a fixed RNS shape");
         else if (YOUT)
             throw std::invalid_argument("hoisted ModUp factors need a fixed RNS shape");
         else

@@ -24,6 +24,10 @@ struct NttJob {
     u64* const* dst_items = nullptr;        // per-item base pointers, each [limbs][N]
     int limbs = 0;                          // limbs per item
     signed char pidx[MAX_JOB_LIMBS];        // global prime index of limb j
+    // inverse column phase only: skip the final x N^-1, outputs lazy in [0, 2q);
+    // set when the consumer (k_mul_scale_k, k_ks_moddown_k) folds N^-1 into its
+    // constants (same canonical results, one Shoup product less per coefficient)
+    int lazy_out = 0;
 };
 
 // sampler domains (nonce word 0 = dom | limb << 8 | digit << 16)
@@ -123,8 +127,9 @@ void launch_mul_blocks_tensor(const DevConsts* dc, const RnsParams& P, const u64
                               cudaStream_t st);
 void launch_mul_tensor(const DevConsts* dc, const RnsParams& P, const u64* T, u64* Z, int items,
                        cudaStream_t st);
+// lazy_in: Z is the unscaled, lazy inverse column output (NttJob::lazy_out)
 void launch_mul_scale(const DevConsts* dc, const RnsParams& P, const u64* Z, u64* const* OUT,
-                      u64* D2, int items, cudaStream_t st, u64* D2Y = nullptr);
+                      u64* D2, int items, cudaStream_t st, u64* D2Y = nullptr, bool lazy_in = false);
 
 // hybrid key switching
 void launch_ks_modup(const DevConsts* dc, const RnsParams& P, const u64* const* SRC, int src_poly,
@@ -138,7 +143,7 @@ void launch_ks_inner(const DevConsts* dc, const RnsParams& P, const u64* DX,
 void launch_ks_moddown(const DevConsts* dc, const RnsParams& P, const u64* ACC,
                        const u64* const* BASE, const u64* const* RSRC, const u32* ginv,
                        u64* const* OUT, int items, cudaStream_t st, const u64* const* EXTRA = nullptr,
-                       const int* PAIR = nullptr, u64* const* YOUT = nullptr);
+                       const int* PAIR = nullptr, u64* const* YOUT = nullptr, bool lazy_in = false);
 
 // masks / plaintext products
 void launch_mask_accum(const DevConsts* dc, const RnsParams& P, const u64* MT,

@@ -312,9 +312,10 @@ static void ks_fused_t(const DevConsts* dc, const RnsParams& P, const u64* const
     j.src = ACC;
     j.dst = ACC;
     j.limbs = 2 * LK;
+    j.lazy_out = LT > 0 ? 1 : 0;  // the fixed-shape ModDown folds N^-1 into its constants
     launch_ntt_phase(dc, LOGN, /*inverse=*/true, /*cols=*/true, j, items, st);
     kmark("k_ntt_cols inv (key switch)", st);
-    launch_ks_moddown(dc, P, ACC, BASE, RSRC, ginv, OUT, items, st, EXTRA, PAIR, ky.out);
+    launch_ks_moddown(dc, P, ACC, BASE, RSRC, ginv, OUT, items, st, EXTRA, PAIR, ky.out, j.lazy_out != 0);
     kmark("k_ks_moddown_k", st);
 }
 
