@@ -296,17 +296,23 @@ u64* GpuContext::enc_workspace(int items) {
     return wsC_.words();
 }
 
-CsscLayout CsscLayout::make(size_t nnz, size_t vec_len, size_t n_rows, size_t n_slices, size_t n_cols, int items) {
+CsscLayout CsscLayout::make(size_t nnz, size_t vec_len, size_t n_rows, size_t n_slices, size_t n_cols, int items,
+                            int ci_w, int va_w, int v_w) {
+    if ((ci_w != 2 && ci_w != 4 && ci_w != 8) || (va_w != 1 && va_w != 8) || (v_w != 1 && v_w != 8))
+        throw std::invalid_argument("client image: unsupported element width");
     CsscLayout l;
+    l.ci_w = ci_w;
+    l.va_w = va_w;
+    l.v_w = v_w;
     size_t off = 0;
     auto place = [&](size_t b) {
         const size_t o = off;
         off += (b + 15) & ~size_t(15);
         return o;
     };
-    l.o_ci = place(8 * nnz);
-    l.o_va = place(8 * nnz);
-    l.o_v = place(8 * vec_len);
+    l.o_ci = place((size_t)ci_w * nnz);
+    l.o_va = place((size_t)va_w * nnz);
+    l.o_v = place((size_t)v_w * vec_len);
     l.o_rows = place(16 * n_rows);
     l.o_rpre = place(4 * (n_rows + 1));  // exclusive prefix of the row lengths (+ total)
     l.o_sl = place(8 * n_slices);
@@ -407,8 +413,7 @@ void GpuContext::encrypt_cssc_image(const unsigned char* img, const CsscLayout& 
     }
     cuda_check(cudaMemcpyAsync(d, img, lay.bytes, cudaMemcpyHostToDevice, st_), "upload");
     if (img == stage_) cuda_check(cudaEventRecord(stage_ev_, st_), "event");  // staging reusable after this
-    launch_pack_cssc(dc_, P_, reinterpret_cast<const int64_t*>(d + lay.o_ci),
-                     reinterpret_cast<const int64_t*>(d + lay.o_va), reinterpret_cast<const int64_t*>(d + lay.o_v),
+    launch_pack_cssc(dc_, P_, d + lay.o_ci, d + lay.o_va, d + lay.o_v, lay.ci_w, lay.va_w, lay.v_w,
                      reinterpret_cast<const int4*>(d + lay.o_rows), reinterpret_cast<const int*>(d + lay.o_rpre),
                      (int)lay.n_rows, (long)lay.entries,
                      reinterpret_cast<const int2*>(d + lay.o_sl), reinterpret_cast<const int4*>(d + lay.o_cols),
@@ -462,8 +467,7 @@ void GpuContext::encrypt_cssc_forked(const unsigned char* img, const CsscLayout&
     }
     // branch B: the CSR image, packing, message INTT
     cuda_check(cudaMemcpyAsync(d, img, lay.o_st, cudaMemcpyHostToDevice, sb), "upload");
-    launch_pack_cssc(dc_, P_, reinterpret_cast<const int64_t*>(d + lay.o_ci),
-                     reinterpret_cast<const int64_t*>(d + lay.o_va), reinterpret_cast<const int64_t*>(d + lay.o_v),
+    launch_pack_cssc(dc_, P_, d + lay.o_ci, d + lay.o_va, d + lay.o_v, lay.ci_w, lay.va_w, lay.v_w,
                      reinterpret_cast<const int4*>(d + lay.o_rows), reinterpret_cast<const int*>(d + lay.o_rpre),
                      (int)lay.n_rows, (long)lay.entries,
                      reinterpret_cast<const int2*>(d + lay.o_sl), reinterpret_cast<const int4*>(d + lay.o_cols),

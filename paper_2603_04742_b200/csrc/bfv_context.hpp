@@ -66,7 +66,11 @@ struct CsscLayout {
     size_t nnz = 0, vec_len = 0, n_rows = 0, n_slices = 0, n_cols = 0;
     size_t entries = 0;  // sum of the row lengths (= nnz for CSR-derived rows): one pack thread each
     int items = 0;  // 2 * chunks
-    static CsscLayout make(size_t nnz, size_t vec_len, size_t n_rows, size_t n_slices, size_t n_cols, int items);
+    // element widths in bytes: column indices 2 / 4 / 8 (unsigned), values and
+    // vector entries 1 / 8 (signed) -- the compact forms when every entry fits
+    int ci_w = 8, va_w = 8, v_w = 8;
+    static CsscLayout make(size_t nnz, size_t vec_len, size_t n_rows, size_t n_slices, size_t n_cols, int items,
+                           int ci_w = 8, int va_w = 8, int v_w = 8);
 };
 
 // Device buffers of a client pass owned by its caller (a cached pipeline), so

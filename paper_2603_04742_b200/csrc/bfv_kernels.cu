@@ -1278,8 +1278,9 @@ void launch_encode_scatter(const DevConsts* dc, const RnsParams& P, const int64_
 // thousands of entries no longer serialises on a few lanes): entry e belongs
 // to row record r with rpre[r] <= e < rpre[r + 1] (binary search over the
 // exclusive prefix of the row lengths), at aligned column j = e - rpre[r].
-__global__ void k_pack_cssc(const DevConsts* __restrict__ dc, const int64_t* __restrict__ CI,
-                            const int64_t* __restrict__ VA, const int64_t* __restrict__ V,
+template <class CIT, class VAT, class VT>
+__global__ void k_pack_cssc(const DevConsts* __restrict__ dc, const CIT* __restrict__ CI,
+                            const VAT* __restrict__ VA, const VT* __restrict__ V,
                             const int4* __restrict__ rows, const int* __restrict__ rpre, int n_rows,
                             const int2* __restrict__ slices, const int4* __restrict__ cols, int n_chunks,
                             u64* __restrict__ M, size_t mstride) {
@@ -1332,20 +1333,52 @@ __global__ void k_pack_cssc(const DevConsts* __restrict__ dc, const int64_t* __r
     const int4 c = __ldg(cols + sl.x + j);
     if (c.x < 0) return;  // a chunk another rank evaluates (sharded jobs)
     const u32 pos = dc->pos0[c.y * c.z + rec.z];
-    int64_t a = VA[rec.x + j] % t;
-    int64_t b = V[sl.y + CI[rec.x + j]] % t;
+    int64_t a = (int64_t)VA[rec.x + j] % t;
+    int64_t b = (int64_t)V[(int64_t)sl.y + (int64_t)CI[rec.x + j]] % t;
     M[(size_t)c.x * mstride + pos] = (u64)(a < 0 ? a + t : a);
     M[(size_t)(n_chunks + c.x) * mstride + pos] = (u64)(b < 0 ? b + t : b);
 }
 
-void launch_pack_cssc(const DevConsts* dc, const RnsParams& P, const int64_t* CI, const int64_t* VA,
-                      const int64_t* V, const int4* rows, const int* rpre, int n_rows, long entries,
+template <class CIT, class VAT, class VT>
+static void pack_t(const DevConsts* dc, const void* CI, const void* VA, const void* V, const int4* rows,
+                   const int* rpre, int n_rows, long entries, const int2* slices, const int4* cols, int n_chunks,
+                   u64* M, size_t mstride, cudaStream_t st) {
+    k_pack_cssc<CIT, VAT, VT><<<(unsigned)((entries + 127) / 128), 128, 0, st>>>(
+        dc, static_cast<const CIT*>(CI), static_cast<const VAT*>(VA), static_cast<const VT*>(V), rows, rpre, n_rows,
+        slices, cols, n_chunks, M, mstride);
+}
+
+template <class CIT>
+static void pack_ci(int va_w, int v_w, const DevConsts* dc, const void* CI, const void* VA, const void* V,
+                    const int4* rows, const int* rpre, int n_rows, long entries, const int2* slices, const int4* cols,
+                    int n_chunks, u64* M, size_t mstride, cudaStream_t st) {
+    if (va_w == 1 && v_w == 1)
+        pack_t<CIT, int8_t, int8_t>(dc, CI, VA, V, rows, rpre, n_rows, entries, slices, cols, n_chunks, M, mstride, st);
+    else if (va_w == 1)
+        pack_t<CIT, int8_t, int64_t>(dc, CI, VA, V, rows, rpre, n_rows, entries, slices, cols, n_chunks, M, mstride, st);
+    else if (v_w == 1)
+        pack_t<CIT, int64_t, int8_t>(dc, CI, VA, V, rows, rpre, n_rows, entries, slices, cols, n_chunks, M, mstride, st);
+    else
+        pack_t<CIT, int64_t, int64_t>(dc, CI, VA, V, rows, rpre, n_rows, entries, slices, cols, n_chunks, M, mstride,
+                                      st);
+}
+
+void launch_pack_cssc(const DevConsts* dc, const RnsParams& P, const void* CI, const void* VA, const void* V,
+                      int ci_w, int va_w, int v_w, const int4* rows, const int* rpre, int n_rows, long entries,
                       const int2* slices, const int4* cols, int n_chunks, u64* M, size_t mstride, cudaStream_t st) {
     if (!n_chunks) return;
     cudaMemset2DAsync(M, mstride * 8, 0, (size_t)P.n * 8, (size_t)2 * n_chunks, st);
-    if (n_rows && entries > 0)
-        k_pack_cssc<<<(unsigned)((entries + 127) / 128), 128, 0, st>>>(dc, CI, VA, V, rows, rpre, n_rows, slices,
-                                                                      cols, n_chunks, M, mstride);
+    if (n_rows && entries > 0) {
+        if (ci_w == 2)
+            pack_ci<uint16_t>(va_w, v_w, dc, CI, VA, V, rows, rpre, n_rows, entries, slices, cols, n_chunks, M, mstride,
+                              st);
+        else if (ci_w == 4)
+            pack_ci<uint32_t>(va_w, v_w, dc, CI, VA, V, rows, rpre, n_rows, entries, slices, cols, n_chunks, M, mstride,
+                              st);
+        else
+            pack_ci<uint64_t>(va_w, v_w, dc, CI, VA, V, rows, rpre, n_rows, entries, slices, cols, n_chunks, M, mstride,
+                              st);
+    }
     CSSC_CHECK_LAUNCH();
 }
 

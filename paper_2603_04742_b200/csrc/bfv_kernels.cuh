@@ -156,8 +156,10 @@ void launch_pointwise_plain(const DevConsts* dc, const RnsParams& P, u64* X, con
 // item i encodes vals[offs[i] .. offs[i+1]) (at most S values)
 // CSR rows -> CSSC chunk plaintexts (value chunks [0, n_chunks), vector
 // chunks [n_chunks, 2 n_chunks)), slot layout applied; see spmvgpu_encrypt_cssc
-void launch_pack_cssc(const DevConsts* dc, const RnsParams& P, const int64_t* CI, const int64_t* VA,
-                      const int64_t* V, const int4* rows, const int* rpre, int n_rows, long entries,
+// CI / VA / V: column indices (unsigned, ci_w = 2 / 4 / 8 bytes), values and
+// vector entries (signed, va_w / v_w = 1 / 8 bytes) of the client image
+void launch_pack_cssc(const DevConsts* dc, const RnsParams& P, const void* CI, const void* VA, const void* V,
+                      int ci_w, int va_w, int v_w, const int4* rows, const int* rpre, int n_rows, long entries,
                       const int2* slices, const int4* cols, int n_chunks, u64* M, size_t mstride, cudaStream_t st);
 void launch_encode_scatter(const DevConsts* dc, const RnsParams& P, const int64_t* vals,
                            const u64* offs, u64* M, int items, cudaStream_t st, size_t mstride = 0);

@@ -233,9 +233,12 @@ void plan_cache_give(spmvgpu_ctx* ctx, PlanLease&& lease) {
 namespace spmv::detail {
 
 ClientImage client_image_layout(std::size_t nnz, std::size_t vec_len, std::size_t n_rows, std::size_t n_slices,
-                                std::size_t n_cols, int items) {
-    const cssc::CsscLayout l = cssc::CsscLayout::make(nnz, vec_len, n_rows, n_slices, n_cols, items);
+                                std::size_t n_cols, int items, int ci_w, int va_w, int v_w) {
+    const cssc::CsscLayout l = cssc::CsscLayout::make(nnz, vec_len, n_rows, n_slices, n_cols, items, ci_w, va_w, v_w);
     ClientImage img;
+    img.ci_w = ci_w;
+    img.va_w = va_w;
+    img.v_w = v_w;
     img.o_ci = l.o_ci;
     img.o_va = l.o_va;
     img.o_v = l.o_v;
@@ -256,8 +259,8 @@ ClientImage client_image_layout(std::size_t nnz, std::size_t vec_len, std::size_
 }
 
 ClientImage client_image_take(spmvgpu_ctx* ctx, std::size_t nnz, std::size_t vec_len, std::size_t n_rows,
-                              std::size_t n_slices, std::size_t n_cols, int items) {
-    ClientImage img = client_image_layout(nnz, vec_len, n_rows, n_slices, n_cols, items);
+                              std::size_t n_slices, std::size_t n_cols, int items, int ci_w, int va_w, int v_w) {
+    ClientImage img = client_image_layout(nnz, vec_len, n_rows, n_slices, n_cols, items, ci_w, va_w, v_w);
     img.p = ctx->g->pinned_take(img.bytes, &img.cap);
     return img;
 }
@@ -275,7 +278,8 @@ void client_image_fill(spmvgpu_ctx* ctx, unsigned char* p, const ClientImage& im
 }
 
 std::vector<std::size_t> client_image_key(const ClientImage& img) {
-    return {img.bytes, img.nnz, img.vec_len, img.n_rows, img.n_slices, img.n_cols, (std::size_t)img.items};
+    return {img.bytes, img.nnz, img.vec_len, img.n_rows, img.n_slices, img.n_cols, (std::size_t)img.items,
+            (std::size_t)img.ci_w, (std::size_t)img.va_w, (std::size_t)img.v_w};
 }
 
 static cssc::CsscLayout layout_of(const ClientImage& img) {
@@ -297,6 +301,9 @@ static cssc::CsscLayout layout_of(const ClientImage& img) {
     l.n_slices = img.n_slices;
     l.n_cols = img.n_cols;
     l.items = img.items;
+    l.ci_w = img.ci_w;
+    l.va_w = img.va_w;
+    l.v_w = img.v_w;
     return l;
 }
 
@@ -305,7 +312,8 @@ bool pipeline_ready(const PlanLease& lease, const ClientImage& img) {
 }
 
 static ClientImage layout_of_key(const std::vector<std::size_t>& k) {
-    return client_image_layout(k[1], k[2], k[3], k[4], k[5], static_cast<int>(k[6]));
+    return client_image_layout(k[1], k[2], k[3], k[4], k[5], static_cast<int>(k[6]), static_cast<int>(k[7]),
+                               static_cast<int>(k[8]), static_cast<int>(k[9]));
 }
 
 void pipeline_speculate(spmvgpu_ctx* ctx) {
@@ -314,7 +322,7 @@ void pipeline_speculate(spmvgpu_ctx* ctx) {
     std::lock_guard<std::mutex> lk(ctx->plans_mu);
     for (PlanLease& l : ctx->plans) {
         if (l.key != ctx->spec_key) continue;
-        if (!l.plan || !l.plan->plan->has_pipeline() || !l.pimg || l.pkey.size() != 7) return;
+        if (!l.plan || !l.plan->plan->has_pipeline() || !l.pimg || l.pkey.size() != 10) return;
         const ClientImage lay = layout_of_key(l.pkey);
         if (l.a.size() + l.b.size() != static_cast<std::size_t>(lay.items)) return;
         // the ids and output handles exactly as client_image_fill will write them
@@ -394,6 +402,9 @@ void client_image_encrypt(spmvgpu_ctx* ctx, ClientImage& img, const spmvgpu_ct* 
     l.n_slices = img.n_slices;
     l.n_cols = img.n_cols;
     l.items = img.items;
+    l.ci_w = img.ci_w;
+    l.va_w = img.va_w;
+    l.v_w = img.v_w;
     g.encrypt_cssc_image(img.p, l);
 }
 

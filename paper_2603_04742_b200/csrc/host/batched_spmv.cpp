@@ -72,26 +72,45 @@ BatchedSpmv::BatchedSpmv(spmvgpu_ctx* ctx, const HeParams& hp, std::span<const C
     // first; the sequential checks then only locate the failure, in order
     const bool big = nnz_total >= kParallelEntries;
     bool scanned_ok = false;
+    // the compact client image: int8 values / vector entries when all fit,
+    // 16-bit column indices when every matrix has at most 2^16 columns
+    bool va_narrow = true, v_narrow = true;
     if (big) {
         constexpr std::size_t kBlock = 1 << 16;
         std::vector<std::pair<std::size_t, std::size_t>> tasks;  // (matrix, block)
         for (std::size_t mi = 0; mi < ms.size(); ++mi)
             for (std::size_t b0 = 0; b0 * kBlock < std::max(ms[mi].nnz, ms[mi].rows + 1); ++b0) tasks.push_back({mi, b0});
-        std::vector<unsigned char> bad(tasks.size(), 0);
+        std::vector<unsigned char> bad(tasks.size(), 0), wide(tasks.size(), 0);
         HostPool::get().run(tasks.size(), [&](std::size_t t) {
             const CsrView& m = ms[tasks[t].first];
             const std::size_t b0 = tasks[t].second * kBlock;
             bool dec = false;
             for (std::size_t i = b0; i < std::min(m.rows, b0 + kBlock); ++i) dec |= m.row_ptrs[i + 1] < m.row_ptrs[i];
-            std::uint64_t all_neg = ~std::uint64_t{0}, any_top = 0;
+            std::uint64_t all_neg = ~std::uint64_t{0}, any_top = 0, outside8 = 0;
             for (std::size_t k = b0; k < std::min(m.nnz, b0 + kBlock); ++k) {
                 all_neg &= m.col_indices[k] - m.cols;
                 any_top |= m.col_indices[k];
+                outside8 |= (static_cast<std::uint64_t>(m.values[k]) + 128) >> 8;  // value outside [-128, 127]
             }
             const bool cols_bad = b0 < m.nnz && (!(all_neg >> 63) || (any_top >> 63));
             bad[t] = dec || cols_bad;
+            wide[t] = outside8 != 0;
         });
         scanned_ok = std::none_of(bad.begin(), bad.end(), [](unsigned char x) { return x != 0; });
+        va_narrow = std::none_of(wide.begin(), wide.end(), [](unsigned char x) { return x != 0; });
+    } else {
+        for (const CsrView& m : ms) {
+            std::uint64_t outside8 = 0;
+            for (std::size_t k = 0; k < m.nnz; ++k) outside8 |= (static_cast<std::uint64_t>(m.values[k]) + 128) >> 8;
+            va_narrow = va_narrow && outside8 == 0;
+        }
+    }
+    std::size_t max_cols = 0;
+    for (const CsrView& m : ms) {
+        max_cols = std::max(max_cols, m.cols);
+        std::uint64_t outside8 = 0;
+        for (std::size_t k = 0; k < m.cols; ++k) outside8 |= (static_cast<std::uint64_t>(m.vec[k]) + 128) >> 8;
+        v_narrow = v_narrow && outside8 == 0;
     }
     // validation in matrix order; the slices to shape are collected and shaped
     // afterwards (on the host pool for large batches), errors still surface in
@@ -220,8 +239,9 @@ BatchedSpmv::BatchedSpmv(spmvgpu_ctx* ctx, const HeParams& hp, std::span<const C
     const bool hit = plan_cache_take(ctx_, key, lease_);
     // the client upload image, written once straight from the callers' arrays:
     // into the cached pipeline's own pinned buffer when its layout matches
+    const int ci_w = max_cols <= (std::size_t{1} << 16) ? 2 : 4, va_w = va_narrow ? 1 : 8, v_w = v_narrow ? 1 : 8;
     ClientImage lay = client_image_layout(nnz_total, vec_total, rowrec_.size() / 4, slicerec_.size() / 2,
-                                          colrec_.size() / 4, static_cast<int>(2 * n));
+                                          colrec_.size() / 4, static_cast<int>(2 * n), ci_w, va_w, v_w);
     if (hit && lease_.pimg && lease_.pkey == client_image_key(lay)) {
         img_ = lay;
         img_.p = lease_.pimg;
@@ -229,20 +249,49 @@ BatchedSpmv::BatchedSpmv(spmvgpu_ctx* ctx, const HeParams& hp, std::span<const C
         img_borrowed_ = true;
     } else {
         img_ = client_image_take(ctx_, nnz_total, vec_total, rowrec_.size() / 4, slicerec_.size() / 2,
-                                 colrec_.size() / 4, static_cast<int>(2 * n));
+                                 colrec_.size() / 4, static_cast<int>(2 * n), ci_w, va_w, v_w);
     }
     const auto t1b = std::chrono::steady_clock::now();
     {
         // (dst, src, bytes) pieces of the image; large batches copy them on the host pool
         std::vector<std::tuple<unsigned char*, const void*, std::size_t>> cp;
+        // narrowing copies of the column indices, values and vectors: (dst, src, count, kind)
+        enum Narrow { CI16, CI32, I8, I64 };
+        std::vector<std::tuple<unsigned char*, const void*, std::size_t, Narrow>> nc;
         std::size_t nz = 0, vo = 0;
         for (const CsrView& m : ms) {
-            cp.emplace_back(img_.p + img_.o_ci + 8 * nz, m.col_indices, 8 * m.nnz);
-            cp.emplace_back(img_.p + img_.o_va + 8 * nz, m.values, 8 * m.nnz);
-            cp.emplace_back(img_.p + img_.o_v + 8 * vo, m.vec, 8 * m.cols);
+            nc.emplace_back(img_.p + img_.o_ci + (std::size_t)img_.ci_w * nz, m.col_indices, m.nnz,
+                            img_.ci_w == 2 ? CI16 : CI32);
+            nc.emplace_back(img_.p + img_.o_va + (std::size_t)img_.va_w * nz, m.values, m.nnz, img_.va_w == 1 ? I8 : I64);
+            nc.emplace_back(img_.p + img_.o_v + (std::size_t)img_.v_w * vo, m.vec, m.cols, img_.v_w == 1 ? I8 : I64);
             nz += m.nnz;
             vo += m.cols;
         }
+        auto narrow = [](unsigned char* d, const void* src, std::size_t cnt, Narrow kind) {
+            switch (kind) {
+                case CI16: {
+                    auto* o = reinterpret_cast<std::uint16_t*>(d);
+                    const auto* x = static_cast<const std::uint64_t*>(src);
+                    for (std::size_t i = 0; i < cnt; ++i) o[i] = static_cast<std::uint16_t>(x[i]);
+                    break;
+                }
+                case CI32: {
+                    auto* o = reinterpret_cast<std::uint32_t*>(d);
+                    const auto* x = static_cast<const std::uint64_t*>(src);
+                    for (std::size_t i = 0; i < cnt; ++i) o[i] = static_cast<std::uint32_t>(x[i]);
+                    break;
+                }
+                case I8: {
+                    auto* o = reinterpret_cast<std::int8_t*>(d);
+                    const auto* x = static_cast<const std::int64_t*>(src);
+                    for (std::size_t i = 0; i < cnt; ++i) o[i] = static_cast<std::int8_t>(x[i]);
+                    break;
+                }
+                case I64:
+                    if (cnt) std::memcpy(d, src, 8 * cnt);
+                    break;
+            }
+        };
         cp.emplace_back(img_.p + img_.o_rows, rowrec_.data(), 4 * rowrec_.size());
         {  // exclusive prefix of the row lengths: the device pack's entry -> row map
             auto* pre = reinterpret_cast<std::int32_t*>(img_.p + img_.o_rpre);
@@ -262,13 +311,27 @@ BatchedSpmv::BatchedSpmv(spmvgpu_ctx* ctx, const HeParams& hp, std::span<const C
             for (auto& [d, src, bytes] : cp)
                 for (std::size_t o = 0; o < bytes; o += kPiece)
                     pieces.emplace_back(d + o, static_cast<const unsigned char*>(src) + o, std::min(kPiece, bytes - o));
-            HostPool::get().run(pieces.size(), [&](std::size_t i) {
-                const auto& [d, src, bytes] = pieces[i];
-                std::memcpy(d, src, bytes);
+            constexpr std::size_t kElems = 1 << 16;
+            std::vector<std::tuple<unsigned char*, const void*, std::size_t, Narrow>> npieces;
+            for (auto& [d, src, cnt, kind] : nc) {
+                const std::size_t dw = kind == CI16 ? 2 : kind == CI32 ? 4 : kind == I8 ? 1 : 8;
+                for (std::size_t o = 0; o < cnt; o += kElems)
+                    npieces.emplace_back(d + dw * o, static_cast<const std::uint64_t*>(src) + o, std::min(kElems, cnt - o),
+                                         kind);
+            }
+            HostPool::get().run(pieces.size() + npieces.size(), [&](std::size_t i) {
+                if (i < pieces.size()) {
+                    const auto& [d, src, bytes] = pieces[i];
+                    std::memcpy(d, src, bytes);
+                } else {
+                    const auto& [d, src, cnt, kind] = npieces[i - pieces.size()];
+                    narrow(d, src, cnt, kind);
+                }
             });
         } else {
             for (auto& [d, src, bytes] : cp)
                 if (bytes) std::memcpy(d, src, bytes);
+            for (auto& [d, src, cnt, kind] : nc) narrow(d, src, cnt, kind);
         }
         std::vector<std::int32_t>().swap(rowrec_);
         std::vector<std::int32_t>().swap(slicerec_);

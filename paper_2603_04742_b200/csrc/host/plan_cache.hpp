@@ -48,11 +48,14 @@ struct ClientImage {
                 bytes = 0;
     std::size_t nnz = 0, vec_len = 0, n_rows = 0, n_slices = 0, n_cols = 0;
     int items = 0;
+    int ci_w = 8, va_w = 8, v_w = 8;  // element widths (cssc::CsscLayout)
 };
 ClientImage client_image_layout(std::size_t nnz, std::size_t vec_len, std::size_t n_rows, std::size_t n_slices,
-                                std::size_t n_cols, int items);  // offsets only, p = nullptr
+                                std::size_t n_cols, int items, int ci_w = 8, int va_w = 8,
+                                int v_w = 8);  // offsets only, p = nullptr
 ClientImage client_image_take(spmvgpu_ctx* ctx, std::size_t nnz, std::size_t vec_len, std::size_t n_rows,
-                              std::size_t n_slices, std::size_t n_cols, int items);
+                              std::size_t n_slices, std::size_t n_cols, int items, int ci_w = 8, int va_w = 8,
+                              int v_w = 8);
 void client_image_give(spmvgpu_ctx* ctx, ClientImage& img);
 // fills the stream ids and output handles, uploads, packs and encrypts
 void client_image_encrypt(spmvgpu_ctx* ctx, ClientImage& img, const spmvgpu_ct* out);

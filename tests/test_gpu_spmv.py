@@ -369,3 +369,27 @@ def test_exhausted_noise_budget_raises():
         pk.spmv_partitioned(ctx, m, v)
     assert e.value.kind == "NoiseExhaustedError"
     ctx.close()
+
+
+@pytest.mark.parametrize("vals,vec,cols,big", [(8, 8, 300, False), (1000, 8, 300, False), (8, 1 << 40, 300, False),
+                                               (200, 300, 70000, False), (8, 8, 300, True), (1 << 40, 8, 300, True)])
+def test_compact_client_image_widths(vals, vec, cols, big):
+    """The client upload image narrows column indices to 16 bits (<= 2^16
+    columns, else 32) and values / vector entries to int8 when every one fits,
+    int64 otherwise; every combination, small batches and host-pool batches
+    (>= 2^18 nonzeros), evaluates exactly."""
+    ctx = pk.Context(logn=11, seed=4)
+    rng = np.random.default_rng(vals % 97 + cols)
+    n_m = 8 if big else 1
+    ms, vs = [], []
+    for i in range(n_m):
+        nnz = 40000 if big else 900
+        base = synth.random_sparse_csr(600, cols, nnz, 300 + i, -8, 8)
+        va = rng.integers(-vals, vals + 1, base.values.size)
+        va[va == 0] = 1
+        ms.append(pk.Csr(base.rows, cols, base.row_ptrs, base.col_indices, va.astype(np.int64)))
+        vs.append(rng.integers(-vec, vec + 1, cols).astype(np.int64))
+    got = pk.spmv_batch(ctx, ms, vs, chunk_size=ctx.slots)
+    for m, v, g in zip(ms, vs, got):
+        assert np.array_equal(g["values"], checker(m, v, ctx.slots, ctx.slots)["values"])
+    ctx.close()
