@@ -903,7 +903,7 @@ int cssc_spmv_batch(spmvgpu_ctx* c, const cssc_csr* ms, const int64_t* const* vs
         for (size_t i = 0; i < nmat; ++i) w.push_back(view_of(ms[i], vs[i], vlens[i]));
         spmv::detail::BatchedSpmv job(c, c->hp, w, chunk_size, static_cast<spmv::PartyRole>(key_holder));
         const auto t1 = std::chrono::steady_clock::now();
-        const auto r = job.run_all();
+        const auto r = job.run_all(values);
         const auto t2 = std::chrono::steady_clock::now();
         for (size_t i = 0; i < nmat; ++i) fill_result(r[i], values ? values[i] : nullptr, res ? res + i : nullptr, nullptr, 0);
         if (trace) {
@@ -992,7 +992,7 @@ int cssc_job_finish(cssc_job* j, int64_t* const* values, cssc_result* res) {
 }
 int cssc_job_run(cssc_job* j, int64_t* const* values, cssc_result* res) {
     return guard([&] { auto lk_ = api_lock(j ? j->ctx : nullptr);
-        const auto r = j->job->run_all();
+        const auto r = j->job->run_all(values);
         for (size_t i = 0; i < r.size(); ++i) fill_result(r[i], values ? values[i] : nullptr, res ? res + i : nullptr, nullptr, 0);
     });
 }

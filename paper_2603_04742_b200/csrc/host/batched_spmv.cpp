@@ -562,7 +562,7 @@ std::vector<SpmvResult> BatchedSpmv::finish_words_dev(std::uint64_t* dev) {
     }
 }
 
-std::vector<SpmvResult> BatchedSpmv::run_all() {
+std::vector<SpmvResult> BatchedSpmv::run_all(std::int64_t* const* out_values) {
     // first use of a plan, sharded jobs: the staged calls; a plan seen before:
     // pack, encryption, cloud, decryption and download as one graph launch
     if (dr_.empty() || world_ > 1 || lease_.uses == 0) {
@@ -588,18 +588,24 @@ std::vector<SpmvResult> BatchedSpmv::run_all() {
         auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
         std::fprintf(stderr, "e2e-trace prepare %.1f graph+sync %.1f us\n", us(t0, t1), us(t1, t2));
     }
-    const std::size_t S = hp_.slot_count;
-    std::vector<std::uint64_t> slots(n_out_ * S);
+    // the pinned download holds each result's slots [0, rows) as u32 (the rest
+    // are zero): read in place, no S-slot copy per result
+    std::vector<SlotSource> src(n_out_);
     std::vector<std::int32_t> measured(n_out_, 0);
     for (std::size_t r = 0; r < n_out_; ++r) {  // world == 1: every result is local
         const PipelineResult pr = pipeline_result(lease_, res_local_[r]);
-        std::uint64_t* dst = slots.data() + r * S;
-        for (int i = 0; i < pr.rows; ++i) dst[i] = pr.slots[i];
+        src[r] = SlotSource{nullptr, pr.slots, static_cast<std::size_t>(pr.rows)};
         const int bl = pr.maxdev ? 64 - __builtin_clzll(pr.maxdev) : 0;
         measured[r] = std::max(0, 63 - bl);
     }
-    auto res = report(slots, measured);
+    const auto t3 = std::chrono::steady_clock::now();
+    auto res = report(src, measured, out_values);
     d2h_ = pipeline_out_bytes(lease_);
+    if (trace) {
+        auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+        std::fprintf(stderr, "e2e-trace results %.1f report %.1f us\n", us(t2, t3),
+                     us(t3, std::chrono::steady_clock::now()));
+    }
     return res;
 }
 
@@ -611,21 +617,37 @@ std::vector<SpmvResult> BatchedSpmv::decrypt_and_report(const std::vector<spmvgp
         check_status(spmvgpu_decrypt(ctx_, outs.data(), n_out_, slots.data(), measured.data()));
     else
         check_status(spmvgpu_sync(ctx_));
-    return report(slots, measured);
+    std::vector<SlotSource> src(n_out_);
+    for (std::size_t r = 0; r < n_out_; ++r) src[r] = SlotSource{slots.data() + r * S, nullptr, S};
+    auto res = report(src, measured);
+    d2h_ = sizeof(std::uint64_t) * slots.size();
+    return res;
 }
 
-std::vector<SpmvResult> BatchedSpmv::report(const std::vector<std::uint64_t>& slots,
-                                            const std::vector<std::int32_t>& measured) {
+std::vector<SpmvResult> BatchedSpmv::report(const std::vector<SlotSource>& slots,
+                                            const std::vector<std::int32_t>& measured,
+                                            std::int64_t* const* out_values) {
     const std::size_t S = hp_.slot_count;
     done_ = true;
-    d2h_ = sizeof(std::uint64_t) * slots.size();
 
+    static const bool trace = std::getenv("CSSC_TRACE_E2E") != nullptr;
+    double t_sched = 0, t_msgs = 0, t_noise = 0, t_rows = 0;
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto dus = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+    const auto tr0 = now();
     const NoiseModel& nm = hp_.noise;
     std::vector<SpmvResult> res(nmat_);
+    struct Unpermute {  // one slice's decrypted rows -> original row order (rm, protocol.cpp:142-151)
+        const Slice* s;
+        std::int64_t* vals;
+        const SlotSource* sl;
+    };
+    std::vector<Unpermute> unpermute;
+    std::vector<std::size_t> row0(nmat_, 0);  // next row of each matrix
     for (std::size_t mi = 0; mi < nmat_; ++mi) {
         res[mi].message_ledger.key_holder = kh_;
         res[mi].noise_budget_remaining_bits = nm.initial_budget_bits;
-        res[mi].values.reserve(rows_of_[mi]);
+        if (!out_values) res[mi].values.assign(rows_of_[mi], 0);
     }
     for (const Slice& s : slices_) {
         SpmvResult& R = res[s.mat];
@@ -637,13 +659,20 @@ std::vector<SpmvResult> BatchedSpmv::report(const std::vector<std::uint64_t>& sl
         led.n_enc = 2 * n_ct;
         led.n_mult_cc = n_ct;
         led.n_mult_cp = n_ct;
+        const auto ta = now();
         std::uint64_t rot = 0;
-        for (std::size_t i = 0; i < n_ct; ++i) rot += rotation_schedule(rl[i], cl[i]).size();
+        std::vector<std::vector<RotStep>> sched(n_ct);
+        for (std::size_t i = 0; i < n_ct; ++i) {
+            sched[i] = rotation_schedule(rl[i], cl[i]);
+            rot += sched[i].size();
+        }
         led.n_rot = rot;
         led.n_add = rot + n_ct;
         led.n_dec = n_ct ? 1 : 0;
         R.op_ledger += led;
         R.n_ct += n_ct;
+        const auto tb = now();
+        t_sched += dus(ta, tb);
         // transcript (protocol.cpp:104-134)
         auto& msgs = R.message_ledger.messages;
         msgs.push_back({PartyRole::ClientA, PartyRole::Cloud, MessageKind::CiphertextBatch,
@@ -654,16 +683,21 @@ std::vector<SpmvResult> BatchedSpmv::report(const std::vector<std::uint64_t>& sl
                         4 + 8 * static_cast<std::uint64_t>(n_ct), 0});
         msgs.push_back({PartyRole::ClientB, PartyRole::Cloud, MessageKind::CiphertextBatch,
                         ciphertext_batch_bytes(hp_, n_ct), n_ct});
+        const auto tc = now();
+        t_msgs += dus(tb, tc);
         // model noise, replaying the backend's budget arithmetic
         int slice_noise = nm.initial_budget_bits;
-        std::vector<std::int64_t> vals(s.rows, 0);
+        // this slice's rows (rows past the tallest chunk are 0)
+        std::int64_t* vals = (out_values ? out_values[s.mat] : R.values.data()) + row0[s.mat];
+        row0[s.mat] += s.rows;
+        if (!n_ct && out_values) std::fill(vals, vals + s.rows, 0);
         if (n_ct) {
             msgs.push_back({PartyRole::Cloud, kh_, MessageKind::ResultCiphertext, ciphertext_batch_bytes(hp_, 1), 1});
             int res_b = nm.initial_budget_bits;
             for (std::size_t i = 0; i < n_ct; ++i) {
                 const int prod_b = lowered(nm.initial_budget_bits, nm.cost_ct_ct_mult_bits);
                 int acc_b = prod_b;
-                for (const RotStep& st : rotation_schedule(rl[i], cl[i])) {
+                for (const RotStep& st : sched[i]) {
                     const int rot_b = lowered(st.from_accumulator ? acc_b : prod_b, nm.cost_rot_bits);
                     acc_b = lowered(std::min(acc_b, rot_b), nm.cost_add_bits);
                 }
@@ -677,15 +711,40 @@ std::vector<SpmvResult> BatchedSpmv::report(const std::vector<std::uint64_t>& sl
             const int meas = measured[static_cast<std::size_t>(s.result)];
             if (meas <= 0)
                 throw NoiseExhaustedError("decrypt: measured invariant-noise budget exhausted (slice result)");
-            const std::uint64_t* sl = slots.data() + static_cast<std::size_t>(s.result) * S;
-            for (std::size_t idx = 0; idx < s.rows; ++idx)
-                vals[s.row_map[idx]] = idx < S ? to_signed(sl[idx], hp_.plaintext_modulus) : 0;
+            const auto td = now();
+            t_noise += dus(tc, td);
+            unpermute.push_back({&s, vals, &slots[static_cast<std::size_t>(s.result)]});
             R.measured_noise_budget_bits =
                 R.measured_noise_budget_bits < 0 ? meas : std::min(R.measured_noise_budget_bits, meas);
+            t_noise += dus(td, now());
         }
-        R.values.insert(R.values.end(), vals.begin(), vals.end());
         R.noise_budget_remaining_bits = std::min(R.noise_budget_remaining_bits, slice_noise);
     }
+    const auto tu = now();
+    const std::uint64_t t = hp_.plaintext_modulus, half = t / 2;  // to_signed: centred residue
+    auto one = [&](std::size_t i) {
+        const Unpermute& u = unpermute[i];
+        const std::size_t avail = std::min({u.s->rows, S, u.sl->count});
+        const std::size_t* rm = u.s->row_map.data();
+        auto centred = [t, half](std::uint64_t r) {
+            return static_cast<std::int64_t>(r) - (r > half ? static_cast<std::int64_t>(t) : 0);
+        };
+        if (u.sl->u64)
+            for (std::size_t idx = 0; idx < avail; ++idx) u.vals[rm[idx]] = centred(u.sl->u64[idx]);
+        else
+            for (std::size_t idx = 0; idx < avail; ++idx) u.vals[rm[idx]] = centred(u.sl->u32[idx]);
+        for (std::size_t idx = avail; idx < u.s->rows; ++idx) u.vals[rm[idx]] = 0;  // past the tallest chunk
+    };
+    std::size_t total_rows = 0;
+    for (const auto& u : unpermute) total_rows += u.s->rows;
+    if (total_rows >= (std::size_t{1} << 15) && unpermute.size() > 1)
+        HostPool::get().run(unpermute.size(), one);
+    else
+        for (std::size_t i = 0; i < unpermute.size(); ++i) one(i);
+    t_rows += dus(tu, now());
+    if (trace)
+        std::fprintf(stderr, "e2e-trace report: init+loop %.1f sched %.1f msgs %.1f noise %.1f rows %.1f us\n",
+                     dus(tr0, now()), t_sched, t_msgs, t_noise, t_rows);
     return res;
 }
 

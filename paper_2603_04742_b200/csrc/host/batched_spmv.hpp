@@ -44,7 +44,10 @@ public:
     void cloud(bool use_graph);   // enqueue the cloud plan (no host sync)
     std::vector<SpmvResult> finish();  // key holder: decrypt, unpermute, bookkeeping
     // encrypt + cloud + finish; from a plan's second use on, one graph launch
-    std::vector<SpmvResult> run_all();
+    // out_values (optional, one caller buffer of rows_i entries per matrix):
+    // the decrypted rows are written there directly and the results' `values`
+    // stay empty (the C-ABI batch path; saves a copy of every row)
+    std::vector<SpmvResult> run_all(std::int64_t* const* out_values = nullptr);
     // this rank's per-slice result ciphertext words (zeros for slices it holds
     // no chunk of), [results][ct words]; and the decryption of summed words
     std::vector<std::uint64_t> result_words();
@@ -90,7 +93,15 @@ private:
     void append_slice(SliceShape&& s, std::size_t col_base);
     void ensure_plan();
     std::vector<SpmvResult> decrypt_and_report(const std::vector<spmvgpu_ct>& outs);
-    std::vector<SpmvResult> report(const std::vector<std::uint64_t>& slots, const std::vector<std::int32_t>& measured);
+    // one result's decrypted slots: u64 (decrypt) or u32 (pipeline download);
+    // slots at and past `count` are zero
+    struct SlotSource {
+        const std::uint64_t* u64 = nullptr;
+        const std::uint32_t* u32 = nullptr;
+        std::size_t count = 0;
+    };
+    std::vector<SpmvResult> report(const std::vector<SlotSource>& slots, const std::vector<std::int32_t>& measured,
+                                   std::int64_t* const* out_values = nullptr);
 
     spmvgpu_ctx* ctx_;
     HeParams hp_;
