@@ -18,6 +18,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import weakref
 from dataclasses import dataclass, field
 from pathlib import Path
 
@@ -508,19 +509,62 @@ assert _CSR_DT.itemsize == C.sizeof(CsrC) and _RES_DT.itemsize == C.sizeof(Resul
 _LEDGER_KEYS = tuple(k for k, _ in Ledger._fields_)
 
 
+# Marshalling cache: (matrix row, addresses) per CSR object, valid while the
+# object still holds the very same arrays (identity-checked on every call;
+# the cache entry keeps them alive, so their addresses cannot be reused).
+# In-place edits of the arrays need no invalidation: the C side reads the
+# contents at call time.
+_CSR_CACHE: dict = {}  # id(matrix) -> (weakref, row_ptrs, col_indices, values, row, arrays)
+_VEC_CACHE: dict = {}  # id(vector) -> (weakref, entry)
+
+
+def _cache_put(cache: dict, obj, value) -> None:
+    key = id(obj)
+    try:
+        ref = weakref.ref(obj, lambda _r, k=key: cache.pop(k, None))
+    except TypeError:  # not weak-referenceable: no caching
+        return
+    cache[key] = (ref,) + value
+
+
+def _csr_row(m):
+    hit = _CSR_CACHE.get(id(m))
+    if hit is not None and hit[0]() is m and hit[1] is m.row_ptrs and hit[2] is m.col_indices \
+            and hit[3] is m.values and hit[4][0] == m.rows and hit[4][1] == m.cols:
+        return hit[4], hit[5]
+    rp, ci, va = _i64(m.row_ptrs), _i64(m.col_indices), _i64(m.values)
+    if va.size == 0:
+        ci = va = _ONE0
+    row = (int(m.rows), int(m.cols), _addr(rp), _addr(ci), _addr(va))
+    arrays = (rp, ci, va)
+    if rp is m.row_ptrs and (va is _ONE0 or (ci is m.col_indices and va is m.values)):
+        # only when no conversion copy was made (a copy would go stale on in-place edits)
+        _cache_put(_CSR_CACHE, m, (m.row_ptrs, m.col_indices, m.values, row, arrays))
+    return row, arrays
+
+
 def _csr_table(ms, keep: list) -> np.ndarray:
     """cssc_csr[] for a batch as one numpy record array (addresses of int64
     copies kept alive in `keep`); a few us per matrix instead of ctypes objects."""
     rows = []
     for m in ms:
-        rp, ci, va = _i64(m.row_ptrs), _i64(m.col_indices), _i64(m.values)
-        if va.size == 0:
-            ci = va = _ONE0
-        keep += (rp, ci, va)
-        rows.append((int(m.rows), int(m.cols), _addr(rp), _addr(ci), _addr(va)))
+        row, arrays = _csr_row(m)
+        keep.append(arrays)
+        rows.append(row)
     t = np.array(rows, dtype=_CSR_DT) if rows else np.zeros(1, _CSR_DT)
     keep.append(t)
     return t
+
+
+def _vec_entry(v):
+    hit = _VEC_CACHE.get(id(v))
+    if hit is not None and hit[0]() is v:
+        return hit[1]
+    a = _i64(v)
+    ent = (a.size, _addr(a if a.size else _ONE0), a if a.size else _ONE0)
+    if a is v:  # no conversion copy (a copy would go stale on in-place edits)
+        _cache_put(_VEC_CACHE, v, (ent,))
+    return ent
 
 
 def _vectors(ms, vs, keep: list):
@@ -530,11 +574,10 @@ def _vectors(ms, vs, keep: list):
     if len(ms) != len(vs):
         raise SpmvError(-4, "DimensionMismatchError",
                         f"spmv_batch: {len(ms)} matrices but {len(vs)} vectors")
-    vv = [_i64(v) for v in vs]
-    lens = np.array([v.size for v in vv] or [0], dtype=np.uint64)
-    vv = [v if v.size else _ONE0 for v in vv]
-    ptrs = np.array([_addr(v) for v in vv] or [0], dtype=np.uint64)
-    keep += vv
+    ents = [_vec_entry(v) for v in vs]
+    lens = np.array([e[0] for e in ents] or [0], dtype=np.uint64)
+    ptrs = np.array([e[1] for e in ents] or [0], dtype=np.uint64)
+    keep.append(ents)
     keep += (ptrs, lens)
     return _addr(ptrs), _addr(lens)
 
