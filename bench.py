@@ -365,6 +365,8 @@ def kernel_units(name: str, items: int, slices: int, logn: int, L: int, K: int, 
         return items * LK * (dnum * h * Bs + 2 * dnum * n + 2 * h * Bs)
     if name.startswith("k_ntt_cols inv (key switch)"):
         return items * 2 * LK * h * As
+    if name.startswith("k_ks_cols_moddown"):  # inverse column phase + ModDown in one launch
+        return items * 2 * LK * h * As + items * 2 * n * (K + L * (K + 1) * DOT)
     if name.startswith("k_ks_moddown"):
         return items * 2 * n * (K + L * (K + 1) * DOT)
     if name.startswith("k_ntt_cols fwd (mask)"):

@@ -1159,6 +1159,186 @@ static ModDownK<L, K> make_moddown_k(const RnsParams& P, bool lazy = false) {
     return c;
 }
 
+// The key switch's inverse column phase fused with ModDown (E4) for the
+// fixed shapes: one CTA = one (item, polynomial, LN-column tile).  The L+K
+// limb tiles of ACC (block phase already inverted by K2) are loaded once,
+// inverse-transformed in shared memory (lazy: N^-1 rides in the ModDown
+// constants, make_moddown_k(P, true)), and ModDown + base + extra + the
+// rotated c0 of the source run on the tile; the accumulators cross HBM once
+// (written by K2, read here) instead of three times, and one launch goes.
+// PAIR (level 0): the CTAs of a D_1 item also transform their O_1 partner's
+// tiles and add both ModDowns (same sums as k_ks_moddown_k's split pair);
+// the partner's CTAs exit.  Same words as k_ntt_cols + k_ks_moddown_k.
+template <int LOGN, int L, int K, int LN>
+__global__ void __launch_bounds__(Ntt2<LOGN>::TC) k_ks_cols_moddown(
+    const __grid_constant__ ModDownK<L, K> c, const DevConsts* __restrict__ dc, const u64* __restrict__ ACC,
+    const u64* const* BASE, const u64* const* RSRC, const u32* ginv, u64* const* OUT, const u64* const* EXTRA,
+    const int* PAIR, u64* const* YOUT) {
+    using G = Ntt2<LOGN>;
+    constexpr int LK = L + K, T = G::TC, CTAS = G::R2 / LN, SEG = LN / 2;
+    constexpr int TILE = LN * G::R1, PER = TILE / T;  // elements per thread
+    static_assert(PER >= 1 && TILE % T == 0, "tile smaller than the CTA");
+    extern __shared__ u64 smem[];
+    u64* tiles = smem;              // [LK][R1][LN]
+    u64* tws = smem + LK * TILE;    // [LK][R1] (w, w_shoup) pairs
+    const int n = c.n;
+    const int tileid = blockIdx.x % CTAS;
+    const int rest = blockIdx.x / CTAS;
+    const int p = rest & 1;
+    const int item = rest >> 1;
+    const int pv = PAIR ? PAIR[item] : -1;
+    if (pv <= -3) return;  // an O_1 partner: evaluated by its D_1's CTAs
+    const int col0 = tileid * LN;
+    for (int j = 0; j < LK; ++j)
+        for (int i = threadIdx.x; i < G::R1; i += T) cp_async16(tws + 2 * ((size_t)j * G::R1 + i), dc->tw[j].inv + 2 * i);
+    auto addr = [](int l, int pos) { return pos * LN + l; };
+    // inverse column phase of item `it`'s LK tiles of polynomial p, in smem
+    auto transform = [&](int it) {
+        const u64* acc = ACC + ((size_t)it * 2 + p) * LK * n;
+#pragma unroll
+        for (int j = 0; j < LK; ++j) {
+#pragma unroll
+            for (int r = 0; r < G::R1 * SEG / T; ++r) {
+                const int i = threadIdx.x + T * r, cc = i / SEG, h = i % SEG;
+                cp_async16(tiles + (size_t)j * TILE + cc * LN + 2 * h, acc + (size_t)j * n + (size_t)cc * G::R2 + col0 + 2 * h);
+            }
+        }
+        cp_async_wait_all();
+        __syncthreads();
+#pragma unroll 1
+        for (int j = 0; j < LK; ++j) {
+            const u64* tw = tws + 2 * (size_t)j * G::R1;
+            auto twf = [&](int sl, int, int blk) {
+                const int k = (1 << sl) + blk;
+                return make_ulonglong2(tw[2 * k], tw[2 * k + 1]);
+            };
+            line_ntt_v<G::A, 0, true, (LN >= 8 ? 3 : 2), LN>(tiles + (size_t)j * TILE, ConstQ{dc->mod[j].q}, addr, twf,
+                                                            whole_cta());
+        }
+    };
+    // ModDown of element e of the transformed tiles of item `it` (+ its rotated c0)
+    auto moddown = [&](int it, int e, u64 out[L]) {
+        const int k = (e / LN) * G::R2 + col0 + (e % LN);
+        u64 y[K];
+#pragma unroll
+        for (int kk = 0; kk < K; ++kk)
+            y[kk] = shoup(tiles[(size_t)(L + kk) * TILE + e], c.phat_inv[kk], c.phat_inv_sh[kk], c.pk[kk]);
+        const u64* rs = (RSRC && p == 0) ? RSRC[it] : nullptr;
+        bool neg = false;
+        const int ridx = rs ? automorph_src(ginv ? ginv[it] : 0u, k, n, neg) : k;
+#pragma unroll
+        for (int j = 0; j < L; ++j) {
+            const u64 q = c.qm[j].q;
+            u64 a = tiles[(size_t)j * TILE + e];
+            a = a >= q ? a - q : a;
+            Dot29 d;
+            dot29_mac(d, a, c.F[j]);
+#pragma unroll
+            for (int kk = 0; kk < K; ++kk) dot29_mac(d, y[kk], c.E[kk][j]);
+            u64 v = dot29_reduce(d, c.qm[j]);
+            if (rs) {
+                const u64 r = rs[(size_t)j * n + ridx];
+                v = add_mod(v, neg ? neg_mod(r, q) : r, q);
+            }
+            out[j] = v;
+        }
+    };
+    transform(item);
+    u64 v[PER][L];
+#pragma unroll
+    for (int r = 0; r < PER; ++r) moddown(item, threadIdx.x + T * r, v[r]);
+    if (pv >= 0) {  // D_1 of a merged pair: add the rotation of its O_1 partner
+        __syncthreads();
+        transform(pv);
+#pragma unroll
+        for (int r = 0; r < PER; ++r) {
+            u64 w[L];
+            moddown(pv, threadIdx.x + T * r, w);
+#pragma unroll
+            for (int j = 0; j < L; ++j) v[r][j] = add_mod(v[r][j], w[j], c.qm[j].q);
+        }
+    }
+    u64* out = OUT[item] + (size_t)p * L * n;
+    u64* yo = (p == 1 && YOUT) ? YOUT[item] : nullptr;
+    const u64* base = BASE ? BASE[item] : nullptr;  // per-item entries may be null (hoisted odd steps)
+    if (base) base += (size_t)p * L * n;
+    const u64* ex = EXTRA ? EXTRA[item] : nullptr;
+    if (ex) ex += (size_t)p * L * n;
+#pragma unroll
+    for (int r = 0; r < PER; ++r) {
+        const int e = threadIdx.x + T * r;
+        const size_t k = (size_t)(e / LN) * G::R2 + col0 + (e % LN);
+#pragma unroll
+        for (int j = 0; j < L; ++j) {
+            const u64 q = c.qm[j].q;
+            u64 x = v[r][j];
+            if (base) x = add_mod(x, base[(size_t)j * n + k], q);
+            if (ex) x = add_mod(x, ex[(size_t)j * n + k], q);
+            out[(size_t)j * n + k] = x;
+            if (yo) yo[(size_t)j * n + k] = shoup(x, c.dhi[j], c.dhi_sh[j], q);
+        }
+    }
+}
+
+template <int LOGN, int L, int K, int LN>
+static bool cols_moddown_ln(const DevConsts* dc, const RnsParams& P, const u64* ACC, const u64* const* BASE,
+                            const u64* const* RSRC, const u32* ginv, u64* const* OUT, int items, cudaStream_t st,
+                            const u64* const* EXTRA, const int* PAIR, u64* const* YOUT);
+
+template <int LOGN, int L, int K>
+static bool cols_moddown_t(const DevConsts* dc, const RnsParams& P, const u64* ACC, const u64* const* BASE,
+                           const u64* const* RSRC, const u32* ginv, u64* const* OUT, int items, cudaStream_t st,
+                           const u64* const* EXTRA, const int* PAIR, u64* const* YOUT) {
+    using G = Ntt2<LOGN>;
+    static const int ln = [] {
+        const char* e = std::getenv("CSSC_COLS_MODDOWN_LN");
+        return e ? std::atoi(e) : 4;
+    }();
+    // 4-column tiles (radix-4 passes, 40 KB smem, 3 CTAs per SM) measured faster
+    // than 8 (80 KB, 2 CTAs per SM): C5 6.08 vs 6.19 ms
+    if (ln == 8) return cols_moddown_ln<LOGN, L, K, 8>(dc, P, ACC, BASE, RSRC, ginv, OUT, items, st, EXTRA, PAIR, YOUT);
+    return cols_moddown_ln<LOGN, L, K, 4>(dc, P, ACC, BASE, RSRC, ginv, OUT, items, st, EXTRA, PAIR, YOUT);
+}
+
+template <int LOGN, int L, int K, int LN>
+static bool cols_moddown_ln(const DevConsts* dc, const RnsParams& P, const u64* ACC, const u64* const* BASE,
+                            const u64* const* RSRC, const u32* ginv, u64* const* OUT, int items, cudaStream_t st,
+                            const u64* const* EXTRA, const int* PAIR, u64* const* YOUT) {
+    using G = Ntt2<LOGN>;
+    if constexpr (G::R2 < 16 || G::R1 * LN < G::TC) {
+        return false;
+    } else {
+        constexpr int smem = ((L + K) * LN * G::R1 + 2 * (L + K) * G::R1) * 8;
+        smem_optin_k(k_ks_cols_moddown<LOGN, L, K, LN>, smem);
+        const unsigned grid = (unsigned)items * 2 * (G::R2 / LN);
+        k_ks_cols_moddown<LOGN, L, K, LN><<<grid, G::TC, smem, st>>>(make_moddown_k<L, K>(P, true), dc, ACC, BASE,
+                                                                     RSRC, ginv, OUT, EXTRA, PAIR, YOUT);
+        CSSC_CHECK_LAUNCH();
+        return true;
+    }
+}
+
+bool ks_cols_moddown_applies(const RnsParams& P) {
+    static const bool off = std::getenv("CSSC_NO_COLS_MODDOWN") != nullptr;
+    const auto& cf = P.cfg;
+    return !off && cf.L == 2 && cf.K == 2 && cf.alpha == 2 && (cf.logn == 13 || cf.logn == 14);
+}
+
+bool launch_ks_cols_moddown(const DevConsts* dc, const RnsParams& P, const u64* ACC, const u64* const* BASE,
+                            const u64* const* RSRC, const u32* ginv, u64* const* OUT, int items, cudaStream_t st,
+                            const u64* const* EXTRA, const int* PAIR, u64* const* YOUT) {
+    if (!items || !ks_cols_moddown_applies(P)) return false;
+    const auto& cf = P.cfg;
+    {
+        switch (cf.logn) {
+            case 13: return cols_moddown_t<13, 2, 2>(dc, P, ACC, BASE, RSRC, ginv, OUT, items, st, EXTRA, PAIR, YOUT);
+            case 14: return cols_moddown_t<14, 2, 2>(dc, P, ACC, BASE, RSRC, ginv, OUT, items, st, EXTRA, PAIR, YOUT);
+            default: return false;
+        }
+    }
+    return false;
+}
+
 void launch_ks_moddown(const DevConsts* dc, const RnsParams& P, const u64* ACC,
                        const u64* const* BASE, const u64* const* RSRC, const u32* ginv,
                        u64* const* OUT, int items, cudaStream_t st, const u64* const* EXTRA, const int* PAIR,

@@ -140,6 +140,12 @@ void launch_ks_inner(const DevConsts* dc, const RnsParams& P, const u64* DX,
                      const u64* const* KEY, u64* ACC, int items, cudaStream_t st);
 // OUT[p] = BASE[p] (same index, optional) + (p==0 ? phi_g(RSRC[0]) : 0) (optional)
 //          + ModDown(ACC[p])
+// the key switch's inverse column phase + ModDown in one launch (fixed shapes
+// L = K = 2 at N = 2^13 / 2^14); false: not applicable, use the two kernels
+bool ks_cols_moddown_applies(const RnsParams& P);
+bool launch_ks_cols_moddown(const DevConsts* dc, const RnsParams& P, const u64* ACC, const u64* const* BASE,
+                            const u64* const* RSRC, const u32* ginv, u64* const* OUT, int items, cudaStream_t st,
+                            const u64* const* EXTRA, const int* PAIR, u64* const* YOUT);
 void launch_ks_moddown(const DevConsts* dc, const RnsParams& P, const u64* ACC,
                        const u64* const* BASE, const u64* const* RSRC, const u32* ginv,
                        u64* const* OUT, int items, cudaStream_t st, const u64* const* EXTRA = nullptr,

@@ -312,6 +312,10 @@ static void ks_fused_t(const DevConsts* dc, const RnsParams& P, const u64* const
     j.src = ACC;
     j.dst = ACC;
     j.limbs = 2 * LK;
+    if (launch_ks_cols_moddown(dc, P, ACC, BASE, RSRC, ginv, OUT, items, st, EXTRA, PAIR, ky.out)) {
+        kmark("k_ks_cols_moddown (inv cols + ModDown)", st);
+        return;
+    }
     j.lazy_out = LT > 0 ? 1 : 0;  // the fixed-shape ModDown folds N^-1 into its constants
     launch_ntt_phase(dc, LOGN, /*inverse=*/true, /*cols=*/true, j, items, st);
     kmark("k_ntt_cols inv (key switch)", st);
