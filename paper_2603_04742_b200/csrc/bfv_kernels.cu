@@ -1318,16 +1318,22 @@ static bool cols_moddown_ln(const DevConsts* dc, const RnsParams& P, const u64* 
     }
 }
 
-bool ks_cols_moddown_applies(const RnsParams& P) {
+// The fused kernel gives each CTA a whole (item, polynomial) column tile of
+// all L+K limbs: launches of fewer than one wave of such CTAs (a lone
+// rotation, C1/C2's small levels) keep the two-kernel path, whose separate
+// launches spread the same work over more CTAs.
+bool ks_cols_moddown_applies(const RnsParams& P, int items) {
     static const bool off = std::getenv("CSSC_NO_COLS_MODDOWN") != nullptr;
     const auto& cf = P.cfg;
-    return !off && cf.L == 2 && cf.K == 2 && cf.alpha == 2 && (cf.logn == 13 || cf.logn == 14);
+    if (off || cf.L != 2 || cf.K != 2 || cf.alpha != 2 || (cf.logn != 13 && cf.logn != 14)) return false;
+    const long ctas = (long)items * 2 * (64 / 4);  // R2 / LN: R2 = 64 at 2^13 and 2^14, LN = 4
+    return ctas >= 3L * 148;
 }
 
 bool launch_ks_cols_moddown(const DevConsts* dc, const RnsParams& P, const u64* ACC, const u64* const* BASE,
                             const u64* const* RSRC, const u32* ginv, u64* const* OUT, int items, cudaStream_t st,
                             const u64* const* EXTRA, const int* PAIR, u64* const* YOUT) {
-    if (!items || !ks_cols_moddown_applies(P)) return false;
+    if (!items || !ks_cols_moddown_applies(P, items)) return false;
     const auto& cf = P.cfg;
     {
         switch (cf.logn) {

@@ -142,7 +142,7 @@ void launch_ks_inner(const DevConsts* dc, const RnsParams& P, const u64* DX,
 //          + ModDown(ACC[p])
 // the key switch's inverse column phase + ModDown in one launch (fixed shapes
 // L = K = 2 at N = 2^13 / 2^14); false: not applicable, use the two kernels
-bool ks_cols_moddown_applies(const RnsParams& P);
+bool ks_cols_moddown_applies(const RnsParams& P, int items);
 bool launch_ks_cols_moddown(const DevConsts* dc, const RnsParams& P, const u64* ACC, const u64* const* BASE,
                             const u64* const* RSRC, const u32* ginv, u64* const* OUT, int items, cudaStream_t st,
                             const u64* const* EXTRA, const int* PAIR, u64* const* YOUT);

@@ -180,8 +180,9 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
     stats_.key_bytes = n ? KEY : 0;
     // each NTT is two kernels (column, block phase); fused: extend, cols, blocks+tensor+iblocks,
     // icols, scale + the 4-kernel relinearisation key switch
-    const int kfuse = fused && ks_cols_moddown_applies(P) && !std::getenv("CSSC_KS_CLUSTER") ? 1 : 0;
-    stats_.kernels = n ? (fused ? 9 - kfuse : 14) : 0;
+    const bool ksc = std::getenv("CSSC_KS_CLUSTER") != nullptr;
+    auto kfuse = [&](int items) { return fused && !ksc && ks_cols_moddown_applies(P, items) ? 1 : 0; };
+    stats_.kernels = n ? (fused ? 9 - kfuse(n) : 14) : 0;
     stats_.limb_ntts = (u64)n * (7 * M + P.dnum * LK + 2 * LK) + (u64)n_rot * (P.dnum * LK + 2 * LK);
 
     // where each hoisted rotation lands: rp slot per (chunk item k, odd step)
@@ -257,7 +258,7 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
         levels_.push_back(lv);
         stats_.hbm_bytes += (u64)lv.items * 3 * C + lvl_keys.size() * KEY;
         stats_.key_bytes += lvl_keys.size() * KEY;
-        stats_.kernels += fused ? 4 - kfuse : 7;
+        stats_.kernels += fused ? 4 - kfuse(lv.items) : 7;
     }
     stats_.distinct_keys = all_keys.size();
 

@@ -72,14 +72,21 @@ __global__ void __launch_bounds__(kMulGroups * kGroupThreads) k_mul_blocks_tenso
 #pragma unroll 1
     for (int p = grp; p < 4; p += kMulGroups) line_ntt<G::B, 0, false>(tile + p * TW, q, addr, twf, tg);
     __syncthreads();
-    // tensor: a* lazy (< 31q), b* canonicalised, so every product is < 31 q^2 (barrett range)
+    // tensor: all four inputs canonicalised (cheap 32-bit quotient estimate),
+    // so z1 = a0 b1 + a1 b0 < 2 q^2 < 2^117 is one 128-bit sum under a single
+    // Barrett reduction (range < 2^(k+63)) instead of two reductions and an add
 #pragma unroll
     for (int r = 0; r < PER; ++r) {
         const int s0 = saddr(threadIdx.x + NT * r);
-        const u64 a0 = tile[s0], a1 = tile[TW + s0];
+        const u64 a0 = reduce_small_quot(tile[s0], md), a1 = reduce_small_quot(tile[TW + s0], md);
         const u64 b0 = reduce_small_quot(tile[2 * TW + s0], md), b1 = reduce_small_quot(tile[3 * TW + s0], md);
         tile[s0] = mul_mod(a0, b0, md);
-        tile[TW + s0] = add_mod(mul_mod(a0, b1, md), mul_mod(a1, b0, md), q);
+        u64 hi = umulhi(a0, b1), lo = a0 * b1;
+        const u64 lo2 = a1 * b0;
+        hi += umulhi(a1, b0);
+        lo += lo2;
+        hi += lo < lo2;
+        tile[TW + s0] = barrett(hi, lo, md);
         tile[2 * TW + s0] = mul_mod(a1, b1, md);
     }
     __syncthreads();
