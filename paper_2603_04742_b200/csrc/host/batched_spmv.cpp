@@ -80,24 +80,22 @@ BatchedSpmv::BatchedSpmv(spmvgpu_ctx* ctx, const HeParams& hp, std::span<const C
         std::vector<std::pair<std::size_t, std::size_t>> tasks;  // (matrix, block)
         for (std::size_t mi = 0; mi < ms.size(); ++mi)
             for (std::size_t b0 = 0; b0 * kBlock < std::max(ms[mi].nnz, ms[mi].rows + 1); ++b0) tasks.push_back({mi, b0});
-        std::vector<unsigned char> bad(tasks.size(), 0), wide(tasks.size(), 0);
+        std::vector<unsigned char> bad(tasks.size(), 0);
         HostPool::get().run(tasks.size(), [&](std::size_t t) {
             const CsrView& m = ms[tasks[t].first];
             const std::size_t b0 = tasks[t].second * kBlock;
             bool dec = false;
             for (std::size_t i = b0; i < std::min(m.rows, b0 + kBlock); ++i) dec |= m.row_ptrs[i + 1] < m.row_ptrs[i];
-            std::uint64_t all_neg = ~std::uint64_t{0}, any_top = 0, outside8 = 0;
+            std::uint64_t all_neg = ~std::uint64_t{0}, any_top = 0;
             for (std::size_t k = b0; k < std::min(m.nnz, b0 + kBlock); ++k) {
                 all_neg &= m.col_indices[k] - m.cols;
                 any_top |= m.col_indices[k];
-                outside8 |= (static_cast<std::uint64_t>(m.values[k]) + 128) >> 8;  // value outside [-128, 127]
             }
             const bool cols_bad = b0 < m.nnz && (!(all_neg >> 63) || (any_top >> 63));
             bad[t] = dec || cols_bad;
-            wide[t] = outside8 != 0;
         });
         scanned_ok = std::none_of(bad.begin(), bad.end(), [](unsigned char x) { return x != 0; });
-        va_narrow = std::none_of(wide.begin(), wide.end(), [](unsigned char x) { return x != 0; });
+        // values: int8 assumed, checked while the image is written (one pass over them)
     } else {
         for (const CsrView& m : ms) {
             std::uint64_t outside8 = 0;
@@ -189,6 +187,7 @@ BatchedSpmv::BatchedSpmv(spmvgpu_ctx* ctx, const HeParams& hp, std::span<const C
             sidx[j] = static_cast<std::int32_t>(slicerec_.size() / 2);
             append_slice(std::move(shapes[j]), col_at[j] / 4);
         }
+        const auto tap = std::chrono::steady_clock::now();
         rowrec_.resize(row_at.back());
         colrec_.resize(col_at.back());
         auto place = [&](std::size_t j) {
@@ -208,10 +207,16 @@ BatchedSpmv::BatchedSpmv(spmvgpu_ctx* ctx, const HeParams& hp, std::span<const C
                 cr[i + 3] = sh.colrec[i + 3];
             }
         };
+        const auto trs = std::chrono::steady_clock::now();
         if (big && jobs.size() > 1)
             HostPool::get().run(jobs.size(), place);
         else
             for (std::size_t j = 0; j < jobs.size(); ++j) place(j);
+        if (trace) {
+            auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+            std::fprintf(stderr, "e2e-trace append %.1f resize %.1f place %.1f us\n", us(ts, tap), us(tap, trs),
+                         us(trs, std::chrono::steady_clock::now()));
+        }
         if (pending) std::rethrow_exception(pending);
     }
     // this rank's chunks (round-robin over global chunk indices);
@@ -239,58 +244,69 @@ BatchedSpmv::BatchedSpmv(spmvgpu_ctx* ctx, const HeParams& hp, std::span<const C
     const bool hit = plan_cache_take(ctx_, key, lease_);
     // the client upload image, written once straight from the callers' arrays:
     // into the cached pipeline's own pinned buffer when its layout matches
-    const int ci_w = max_cols <= (std::size_t{1} << 16) ? 2 : 4, va_w = va_narrow ? 1 : 8, v_w = v_narrow ? 1 : 8;
-    ClientImage lay = client_image_layout(nnz_total, vec_total, rowrec_.size() / 4, slicerec_.size() / 2,
-                                          colrec_.size() / 4, static_cast<int>(2 * n), ci_w, va_w, v_w);
-    if (hit && lease_.pimg && lease_.pkey == client_image_key(lay)) {
-        img_ = lay;
-        img_.p = lease_.pimg;
-        img_.cap = lease_.pimg_cap;
-        img_borrowed_ = true;
-    } else {
-        img_ = client_image_take(ctx_, nnz_total, vec_total, rowrec_.size() / 4, slicerec_.size() / 2,
-                                 colrec_.size() / 4, static_cast<int>(2 * n), ci_w, va_w, v_w);
-    }
+    const int ci_w = max_cols <= (std::size_t{1} << 16) ? 2 : 4, v_w = v_narrow ? 1 : 8;
     const auto t1b = std::chrono::steady_clock::now();
-    {
+    // the image with int8 values when every value fits (checked while writing
+    // it: on a miss it is rebuilt with int64 values)
+    auto build_image = [&](int va_w) -> bool {
+        ClientImage lay = client_image_layout(nnz_total, vec_total, rowrec_.size() / 4, slicerec_.size() / 2,
+                                              colrec_.size() / 4, static_cast<int>(2 * n), ci_w, va_w, v_w);
+        if (hit && lease_.pimg && lease_.pkey == client_image_key(lay)) {
+            img_ = lay;
+            img_.p = lease_.pimg;
+            img_.cap = lease_.pimg_cap;
+            img_borrowed_ = true;
+        } else {
+            img_ = client_image_take(ctx_, nnz_total, vec_total, rowrec_.size() / 4, slicerec_.size() / 2,
+                                     colrec_.size() / 4, static_cast<int>(2 * n), ci_w, va_w, v_w);
+            img_borrowed_ = false;
+        }
         // (dst, src, bytes) pieces of the image; large batches copy them on the host pool
         std::vector<std::tuple<unsigned char*, const void*, std::size_t>> cp;
         // narrowing copies of the column indices, values and vectors: (dst, src, count, kind)
-        enum Narrow { CI16, CI32, I8, I64 };
+        enum Narrow { CI16, CI32, I8, I8V, I64 };
         std::vector<std::tuple<unsigned char*, const void*, std::size_t, Narrow>> nc;
         std::size_t nz = 0, vo = 0;
         for (const CsrView& m : ms) {
             nc.emplace_back(img_.p + img_.o_ci + (std::size_t)img_.ci_w * nz, m.col_indices, m.nnz,
                             img_.ci_w == 2 ? CI16 : CI32);
-            nc.emplace_back(img_.p + img_.o_va + (std::size_t)img_.va_w * nz, m.values, m.nnz, img_.va_w == 1 ? I8 : I64);
+            nc.emplace_back(img_.p + img_.o_va + (std::size_t)img_.va_w * nz, m.values, m.nnz,
+                            img_.va_w == 1 ? I8V : I64);
             nc.emplace_back(img_.p + img_.o_v + (std::size_t)img_.v_w * vo, m.vec, m.cols, img_.v_w == 1 ? I8 : I64);
             nz += m.nnz;
             vo += m.cols;
         }
-        auto narrow = [](unsigned char* d, const void* src, std::size_t cnt, Narrow kind) {
+        // returns false when an int8-narrowed value did not fit
+        auto narrow = [](unsigned char* d, const void* src, std::size_t cnt, Narrow kind) -> bool {
             switch (kind) {
                 case CI16: {
                     auto* o = reinterpret_cast<std::uint16_t*>(d);
                     const auto* x = static_cast<const std::uint64_t*>(src);
                     for (std::size_t i = 0; i < cnt; ++i) o[i] = static_cast<std::uint16_t>(x[i]);
-                    break;
+                    return true;
                 }
                 case CI32: {
                     auto* o = reinterpret_cast<std::uint32_t*>(d);
                     const auto* x = static_cast<const std::uint64_t*>(src);
                     for (std::size_t i = 0; i < cnt; ++i) o[i] = static_cast<std::uint32_t>(x[i]);
-                    break;
+                    return true;
                 }
-                case I8: {
+                case I8:
+                case I8V: {
                     auto* o = reinterpret_cast<std::int8_t*>(d);
                     const auto* x = static_cast<const std::int64_t*>(src);
-                    for (std::size_t i = 0; i < cnt; ++i) o[i] = static_cast<std::int8_t>(x[i]);
-                    break;
+                    std::uint64_t outside8 = 0;
+                    for (std::size_t i = 0; i < cnt; ++i) {
+                        o[i] = static_cast<std::int8_t>(x[i]);
+                        outside8 |= (static_cast<std::uint64_t>(x[i]) + 128) >> 8;  // outside [-128, 127]
+                    }
+                    return outside8 == 0;
                 }
                 case I64:
                     if (cnt) std::memcpy(d, src, 8 * cnt);
-                    break;
+                    return true;
             }
+            return true;
         };
         cp.emplace_back(img_.p + img_.o_rows, rowrec_.data(), 4 * rowrec_.size());
         {  // exclusive prefix of the row lengths: the device pack's entry -> row map
@@ -305,6 +321,7 @@ BatchedSpmv::BatchedSpmv(spmvgpu_ctx* ctx, const HeParams& hp, std::span<const C
         }
         cp.emplace_back(img_.p + img_.o_sl, slicerec_.data(), 4 * slicerec_.size());
         cp.emplace_back(img_.p + img_.o_cols, colrec_.data(), 4 * colrec_.size());
+        bool fits = true;
         if (big) {
             constexpr std::size_t kPiece = 1 << 18;
             std::vector<std::tuple<unsigned char*, const unsigned char*, std::size_t>> pieces;
@@ -314,29 +331,36 @@ BatchedSpmv::BatchedSpmv(spmvgpu_ctx* ctx, const HeParams& hp, std::span<const C
             constexpr std::size_t kElems = 1 << 16;
             std::vector<std::tuple<unsigned char*, const void*, std::size_t, Narrow>> npieces;
             for (auto& [d, src, cnt, kind] : nc) {
-                const std::size_t dw = kind == CI16 ? 2 : kind == CI32 ? 4 : kind == I8 ? 1 : 8;
+                const std::size_t dw = kind == CI16 ? 2 : kind == CI32 ? 4 : (kind == I8 || kind == I8V) ? 1 : 8;
                 for (std::size_t o = 0; o < cnt; o += kElems)
                     npieces.emplace_back(d + dw * o, static_cast<const std::uint64_t*>(src) + o, std::min(kElems, cnt - o),
                                          kind);
             }
+            std::vector<unsigned char> miss(npieces.size(), 0);
             HostPool::get().run(pieces.size() + npieces.size(), [&](std::size_t i) {
                 if (i < pieces.size()) {
                     const auto& [d, src, bytes] = pieces[i];
                     std::memcpy(d, src, bytes);
                 } else {
                     const auto& [d, src, cnt, kind] = npieces[i - pieces.size()];
-                    narrow(d, src, cnt, kind);
+                    miss[i - pieces.size()] = !narrow(d, src, cnt, kind);
                 }
             });
+            fits = std::none_of(miss.begin(), miss.end(), [](unsigned char x) { return x != 0; });
         } else {
             for (auto& [d, src, bytes] : cp)
                 if (bytes) std::memcpy(d, src, bytes);
-            for (auto& [d, src, cnt, kind] : nc) narrow(d, src, cnt, kind);
+            for (auto& [d, src, cnt, kind] : nc) fits = narrow(d, src, cnt, kind) && fits;
         }
-        std::vector<std::int32_t>().swap(rowrec_);
-        std::vector<std::int32_t>().swap(slicerec_);
-        std::vector<std::int32_t>().swap(colrec_);
+        return fits;
+    };
+    if (!build_image(va_narrow ? 1 : 8)) {  // a value outside int8: int64 values
+        if (!img_borrowed_) client_image_give(ctx_, img_);
+        build_image(8);
     }
+    decltype(rowrec_)().swap(rowrec_);
+    std::vector<std::int32_t>().swap(slicerec_);
+    decltype(colrec_)().swap(colrec_);
     if (trace) {
         const auto t2 = std::chrono::steady_clock::now();
         auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
