@@ -241,6 +241,12 @@ int cssc_diag_spmv(spmvgpu_ctx* c, const cssc_csr* m, const int64_t* v, uint64_t
 int cssc_spmv_batch(spmvgpu_ctx* c, const cssc_csr* ms, const int64_t* const* vs, const uint64_t* vlens, size_t nmat,
                     uint64_t chunk_size, int key_holder, int64_t* const* values,
                     cssc_result* res);
+/* optional, before marshalling a cssc_spmv_batch call: enqueue the early
+ * (message-independent) encryption graph of the previous call's plan with the
+ * stream ids the next call will assign, so the device starts while the host
+ * still prepares the call; cssc_spmv_batch does it itself otherwise, and
+ * re-runs it when the next call selects another plan */
+int cssc_speculate(spmvgpu_ctx* c);
 
 /* staged form for benchmarking: pack + encrypt once, run the cloud phase many
  * times from device-resident ciphertexts, then decrypt */

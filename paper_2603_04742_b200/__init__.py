@@ -130,6 +130,7 @@ _SIGS = {
     "cssc_diag_spmv": (C.c_int, [C.c_void_p, C.POINTER(CsrC), i64p, C.c_uint64, C.c_int, i64p,
                                  C.POINTER(ResultC), C.POINTER(Message), C.c_uint64]),
     "spmvgpu_sum": (C.c_int, [C.c_void_p, u64p, C.c_size_t, C.c_uint64]),
+    "cssc_speculate": (C.c_int, [C.c_void_p]),
     "cssc_spmv_batch": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t,
                                   C.c_uint64, C.c_int, C.c_void_p, C.c_void_p]),
     "cssc_job_create": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t,
@@ -662,6 +663,7 @@ def spmv_batch(ctx: Context, ms, vs, chunk_size: int | None = None, key_holder: 
     """Several independent spmv_partitioned runs in shared launches (each result
     equals its own run); party-separated unless the context's pipeline_fuse
     option says otherwise."""
+    lib().cssc_speculate(ctx.h)  # the device starts on the previous plan's encryption while this marshals
     chunk = ctx.slots if chunk_size is None else chunk_size
     ms = list(ms)
     keep: list = []

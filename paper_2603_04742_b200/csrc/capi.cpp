@@ -896,7 +896,7 @@ int cssc_spmv_batch(spmvgpu_ctx* c, const cssc_csr* ms, const int64_t* const* vs
         // the previous call's plan: its early encryption graph runs while the
         // host packs (used only if this call's chunk shapes select that plan)
         static const bool spec = std::getenv("CSSC_NO_EARLY_ENC") == nullptr;
-        if (spec) spmv::detail::pipeline_speculate(c);
+        if (spec && !c->spec_plan) spmv::detail::pipeline_speculate(c);  // unless cssc_speculate did
         const auto t0s = std::chrono::steady_clock::now();
         if (nmat && (!ms || !vs || !vlens)) throw std::invalid_argument("null argument");
         std::vector<spmv::detail::CsrView> w;
@@ -912,6 +912,14 @@ int cssc_spmv_batch(spmvgpu_ctx* c, const cssc_csr* ms, const int64_t* const* vs
             std::fprintf(stderr, "e2e-trace speculate %.1f pack %.1f run %.1f fill %.1f us\n", us(t0, t0s),
                          us(t0s, t1), us(t1, t2), us(t2, t3));
         }
+    });
+}
+
+int cssc_speculate(spmvgpu_ctx* c) {
+    return guard([&] { auto lk_ = api_lock(c);
+        G(c);
+        static const bool spec = std::getenv("CSSC_NO_EARLY_ENC") == nullptr;
+        if (spec) spmv::detail::pipeline_speculate(c);
     });
 }
 

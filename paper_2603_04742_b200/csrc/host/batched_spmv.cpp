@@ -68,33 +68,28 @@ BatchedSpmv::BatchedSpmv(spmvgpu_ctx* ctx, const HeParams& hp, std::span<const C
     }
     if (nnz_total > INT32_MAX || vec_total > INT32_MAX)
         throw std::length_error("spmv_batch: more than 2^31 entries in one batch");
-    // large batches: the branch-free CSR scans below run on the host pool
-    // first; the sequential checks then only locate the failure, in order
+    // large batches: the row_ptrs scan runs on the host pool; the column-range
+    // check rides in the image pass below (one read of the column indices).
+    // Any failure re-runs the checks in the reference's order (raise_first).
     const bool big = nnz_total >= kParallelEntries;
-    bool scanned_ok = false;
+    bool rows_ok = false;
     // the compact client image: int8 values / vector entries when all fit,
     // 16-bit column indices when every matrix has at most 2^16 columns
     bool va_narrow = true, v_narrow = true;
     if (big) {
         constexpr std::size_t kBlock = 1 << 16;
-        std::vector<std::pair<std::size_t, std::size_t>> tasks;  // (matrix, block)
+        std::vector<std::pair<std::size_t, std::size_t>> tasks;  // (matrix, block of rows)
         for (std::size_t mi = 0; mi < ms.size(); ++mi)
-            for (std::size_t b0 = 0; b0 * kBlock < std::max(ms[mi].nnz, ms[mi].rows + 1); ++b0) tasks.push_back({mi, b0});
+            for (std::size_t b0 = 0; b0 * kBlock < ms[mi].rows; ++b0) tasks.push_back({mi, b0});
         std::vector<unsigned char> bad(tasks.size(), 0);
         HostPool::get().run(tasks.size(), [&](std::size_t t) {
             const CsrView& m = ms[tasks[t].first];
             const std::size_t b0 = tasks[t].second * kBlock;
             bool dec = false;
             for (std::size_t i = b0; i < std::min(m.rows, b0 + kBlock); ++i) dec |= m.row_ptrs[i + 1] < m.row_ptrs[i];
-            std::uint64_t all_neg = ~std::uint64_t{0}, any_top = 0;
-            for (std::size_t k = b0; k < std::min(m.nnz, b0 + kBlock); ++k) {
-                all_neg &= m.col_indices[k] - m.cols;
-                any_top |= m.col_indices[k];
-            }
-            const bool cols_bad = b0 < m.nnz && (!(all_neg >> 63) || (any_top >> 63));
-            bad[t] = dec || cols_bad;
+            bad[t] = dec;
         });
-        scanned_ok = std::none_of(bad.begin(), bad.end(), [](unsigned char x) { return x != 0; });
+        rows_ok = std::none_of(bad.begin(), bad.end(), [](unsigned char x) { return x != 0; });
         // values: int8 assumed, checked while the image is written (one pass over them)
     } else {
         for (const CsrView& m : ms) {
@@ -110,52 +105,65 @@ BatchedSpmv::BatchedSpmv(spmvgpu_ctx* ctx, const HeParams& hp, std::span<const C
         for (std::size_t k = 0; k < m.cols; ++k) outside8 |= (static_cast<std::uint64_t>(m.vec[k]) + 128) >> 8;
         v_narrow = v_narrow && outside8 == 0;
     }
+    // all col < cols: every col - cols is negative (and no col has bit 63 set)
+    auto cols_in_range = [](const CsrView& m, std::size_t k0, std::size_t k1) {
+        std::uint64_t all_neg = ~std::uint64_t{0}, any_top = 0;
+        for (std::size_t k = k0; k < k1; ++k) {
+            all_neg &= m.col_indices[k] - m.cols;
+            any_top |= m.col_indices[k];
+        }
+        return k0 >= k1 || ((all_neg >> 63) && !(any_top >> 63));
+    };
+    auto col_check = [&](const CsrView& m) {  // branch-free scan; the offending entry is located only on failure
+        if (cols_in_range(m, 0, m.nnz)) return;
+        for (std::size_t k = 0; k < m.nnz; ++k)
+            if (m.col_indices[k] >= m.cols)
+                throw IndexOutOfRangeError("csr: column index " + std::to_string(m.col_indices[k]) +
+                                           " out of range for " + std::to_string(m.cols) + " columns");
+    };
     // validation in matrix order; the slices to shape are collected and shaped
     // afterwards (on the host pool for large batches), errors still surface in
     // the order the sequential evaluation would raise them
     const auto tv = std::chrono::steady_clock::now();
     std::vector<SliceJob> jobs;
     std::exception_ptr pending;
+    std::size_t fail_mat = ms.size();
+    bool pending_after_cols = false;  // the failed check comes after the matrix's column check
     std::int64_t nz_next = 0, vec_next = 0;
-    for (std::size_t mi = 0; mi < ms.size() && !pending; ++mi) try {
-        const CsrView& m = ms[mi];
-        if (m.rows && m.row_ptrs[0] != 0) throw std::invalid_argument("csr: row_ptrs[0] must be 0");
-        if (!scanned_ok) {  // branch-free scans (vectorised); the offending entry is located only on failure
-            bool dec = false;
-            for (std::size_t i = 0; i < m.rows; ++i) dec |= m.row_ptrs[i + 1] < m.row_ptrs[i];
-            if (dec) throw std::invalid_argument("csr: row_ptrs must be non-decreasing");
-        }
-        if (m.rows && m.row_ptrs[m.rows] != m.nnz) throw std::invalid_argument("csr: row_ptrs end is not nnz");
-        if (!scanned_ok) {  // all col < cols: every col - cols is negative (and no col has bit 63 set)
-            std::uint64_t all_neg = ~std::uint64_t{0}, any_top = 0;
-            for (std::size_t k = 0; k < m.nnz; ++k) {
-                all_neg &= m.col_indices[k] - m.cols;
-                any_top |= m.col_indices[k];
+    for (std::size_t mi = 0; mi < ms.size() && !pending; ++mi) {
+        bool past_cols = false;
+        try {
+            const CsrView& m = ms[mi];
+            if (m.rows && m.row_ptrs[0] != 0) throw std::invalid_argument("csr: row_ptrs[0] must be 0");
+            if (!rows_ok) {
+                bool dec = false;
+                for (std::size_t i = 0; i < m.rows; ++i) dec |= m.row_ptrs[i + 1] < m.row_ptrs[i];
+                if (dec) throw std::invalid_argument("csr: row_ptrs must be non-decreasing");
             }
-            if (m.nnz && (!(all_neg >> 63) || (any_top >> 63)))
-                for (std::size_t k = 0; k < m.nnz; ++k)
-                    if (m.col_indices[k] >= m.cols)
-                        throw IndexOutOfRangeError("csr: column index " + std::to_string(m.col_indices[k]) +
-                                                   " out of range for " + std::to_string(m.cols) + " columns");
+            if (m.rows && m.row_ptrs[m.rows] != m.nnz) throw std::invalid_argument("csr: row_ptrs end is not nnz");
+            if (!big) col_check(m);
+            past_cols = true;
+            const std::int64_t nz_base = nz_next, vec_base = vec_next;
+            nz_next += static_cast<std::int64_t>(m.nnz);
+            vec_next += static_cast<std::int64_t>(m.cols);
+            rows_of_.push_back(m.rows);
+            // spmv_partitioned slices rows by chunk_size (partition_rows, chunk.cpp:55-73);
+            // plain spmv keeps one slice
+            if (partition) {
+                if (chunk_size == 0) throw std::invalid_argument("partition_rows: max_rows must be positive");
+                for (std::size_t r0 = 0; r0 < m.rows; r0 += chunk_size)
+                    jobs.push_back({mi, r0, std::min(m.rows, r0 + chunk_size), nz_base, vec_base});
+            } else {
+                jobs.push_back({mi, 0, m.rows, nz_base, vec_base});
+            }
+        } catch (...) {
+            pending = std::current_exception();
+            fail_mat = mi;
+            pending_after_cols = past_cols;
         }
-        const std::int64_t nz_base = nz_next, vec_base = vec_next;
-        nz_next += static_cast<std::int64_t>(m.nnz);
-        vec_next += static_cast<std::int64_t>(m.cols);
-        rows_of_.push_back(m.rows);
-        // spmv_partitioned slices rows by chunk_size (partition_rows, chunk.cpp:55-73);
-        // plain spmv keeps one slice
-        if (partition) {
-            if (chunk_size == 0) throw std::invalid_argument("partition_rows: max_rows must be positive");
-            for (std::size_t r0 = 0; r0 < m.rows; r0 += chunk_size)
-                jobs.push_back({mi, r0, std::min(m.rows, r0 + chunk_size), nz_base, vec_base});
-        } else {
-            jobs.push_back({mi, 0, m.rows, nz_base, vec_base});
-        }
-    } catch (...) {
-        pending = std::current_exception();
     }
+    std::vector<SliceShape> shapes(jobs.size());
     {
-        std::vector<SliceShape> shapes(jobs.size());
         auto shape_one = [&](std::size_t j) {
             try {
                 shape_slice(ms[jobs[j].mat], jobs[j], chunk_size, shapes[j]);
@@ -168,56 +176,43 @@ BatchedSpmv::BatchedSpmv(spmvgpu_ctx* ctx, const HeParams& hp, std::span<const C
             HostPool::get().run(jobs.size(), shape_one);
         else
             for (std::size_t j = 0; j < jobs.size(); ++j) shape_one(j);
-        const auto ts = std::chrono::steady_clock::now();
         if (trace) {
             auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
             std::fprintf(stderr, "e2e-trace scan %.1f validate %.1f shape %.1f us\n", us(t0, tv), us(tv, tj),
-                         us(tj, ts));
+                         us(tj, std::chrono::steady_clock::now()));
         }
-        for (std::size_t j = 0; j < jobs.size(); ++j)
-            if (shapes[j].err) std::rethrow_exception(shapes[j].err);
-        // slice metadata in order, then the row / column records copied into
-        // place with their slice ids and chunk indices fixed up
-        std::vector<std::size_t> row_at(jobs.size() + 1, rowrec_.size()), col_at(jobs.size() + 1, colrec_.size());
-        std::vector<std::int32_t> chunk0(jobs.size()), sidx(jobs.size());
-        for (std::size_t j = 0; j < jobs.size(); ++j) {
-            row_at[j + 1] = row_at[j] + shapes[j].rowrec.size();
-            col_at[j + 1] = col_at[j] + shapes[j].colrec.size();
-            chunk0[j] = static_cast<std::int32_t>(r_.size());
-            sidx[j] = static_cast<std::int32_t>(slicerec_.size() / 2);
-            append_slice(std::move(shapes[j]), col_at[j] / 4);
+    }
+    // the first error in the reference's order: per matrix its CSR checks (the
+    // column check deferred for large batches), then its slices' shape errors;
+    // with no earlier error, the failed matrix's own checks
+    auto raise_first = [&] {
+        std::size_t j = 0;
+        for (std::size_t mi = 0; mi < fail_mat; ++mi) {
+            if (big) col_check(ms[mi]);
+            for (; j < jobs.size() && jobs[j].mat == mi; ++j)
+                if (shapes[j].err) std::rethrow_exception(shapes[j].err);
         }
-        const auto tap = std::chrono::steady_clock::now();
-        rowrec_.resize(row_at.back());
-        colrec_.resize(col_at.back());
-        auto place = [&](std::size_t j) {
-            const auto& sh = shapes[j];
-            std::int32_t* rr = rowrec_.data() + row_at[j];
-            for (std::size_t i = 0; i < sh.rowrec.size(); i += 4) {
-                rr[i] = sh.rowrec[i];
-                rr[i + 1] = sh.rowrec[i + 1];
-                rr[i + 2] = sh.rowrec[i + 2];
-                rr[i + 3] = sidx[j];
-            }
-            std::int32_t* cr = colrec_.data() + col_at[j];
-            for (std::size_t i = 0; i < sh.colrec.size(); i += 4) {
-                cr[i] = sh.colrec[i] + chunk0[j];
-                cr[i + 1] = sh.colrec[i + 1];
-                cr[i + 2] = sh.colrec[i + 2];
-                cr[i + 3] = sh.colrec[i + 3];
-            }
-        };
-        const auto trs = std::chrono::steady_clock::now();
-        if (big && jobs.size() > 1)
-            HostPool::get().run(jobs.size(), place);
-        else
-            for (std::size_t j = 0; j < jobs.size(); ++j) place(j);
-        if (trace) {
-            auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
-            std::fprintf(stderr, "e2e-trace append %.1f resize %.1f place %.1f us\n", us(ts, tap), us(tap, trs),
-                         us(trs, std::chrono::steady_clock::now()));
+        if (pending) {
+            if (big && pending_after_cols) col_check(ms[fail_mat]);
+            std::rethrow_exception(pending);
         }
-        if (pending) std::rethrow_exception(pending);
+    };
+    if (pending || std::any_of(shapes.begin(), shapes.end(), [](const SliceShape& s) { return bool(s.err); }))
+        raise_first();
+    const auto ts = std::chrono::steady_clock::now();
+    // slice metadata in order; the row / column records are written straight
+    // into the image below, each slice's at its offsets computed here
+    std::vector<std::size_t> row_at(jobs.size() + 1, 0), col_at(jobs.size() + 1, 0);
+    std::vector<std::int64_t> nz_at(jobs.size() + 1, 0);  // rpre base: entries of the earlier slices
+    std::vector<std::int32_t> chunk0(jobs.size()), sidx(jobs.size());
+    for (std::size_t j = 0; j < jobs.size(); ++j) {
+        const CsrView& m = ms[jobs[j].mat];
+        row_at[j + 1] = row_at[j] + shapes[j].rowrec.size() / 4;
+        col_at[j + 1] = col_at[j] + shapes[j].colrec.size() / 4;
+        nz_at[j + 1] = nz_at[j] + static_cast<std::int64_t>(m.row_ptrs[jobs[j].r1] - m.row_ptrs[jobs[j].r0]);
+        chunk0[j] = static_cast<std::int32_t>(r_.size());
+        sidx[j] = static_cast<std::int32_t>(slicerec_.size() / 2);
+        append_slice(shapes[j], col_at[j]);
     }
     // this rank's chunks (round-robin over global chunk indices);
     // world == 1 keeps every chunk
@@ -232,9 +227,12 @@ BatchedSpmv::BatchedSpmv(spmvgpu_ctx* ctx, const HeParams& hp, std::span<const C
         if (res_local_[res] < 0) res_local_[res] = static_cast<int>(n_dout_++);
         dslice_.push_back(static_cast<std::uint32_t>(res_local_[res]));
     }
-    for (std::size_t i = 0; i < colrec_.size(); i += 4) colrec_[i] = local_of[static_cast<std::size_t>(colrec_[i])];
     const std::size_t n = dr_.size();
-    if (!n) return;
+    if (!n) {  // no image: the deferred column checks on their own
+        if (big)
+            for (const CsrView& m : ms) col_check(m);
+        return;
+    }
     // the cloud's view of the job: chunk shapes and slice ids (ChunkShapeMeta)
     std::vector<std::uint64_t> key{n, n_dout_};
     key.insert(key.end(), dr_.begin(), dr_.end());
@@ -242,130 +240,163 @@ BatchedSpmv::BatchedSpmv(spmvgpu_ctx* ctx, const HeParams& hp, std::span<const C
     key.insert(key.end(), dslice_.begin(), dslice_.end());
     const auto t1 = std::chrono::steady_clock::now();
     const bool hit = plan_cache_take(ctx_, key, lease_);
-    // the client upload image, written once straight from the callers' arrays:
-    // into the cached pipeline's own pinned buffer when its layout matches
+    // the client upload image, written once straight from the callers' arrays
+    // and the slice shapes: into the cached pipeline's own pinned buffer when
+    // its layout matches
     const int ci_w = max_cols <= (std::size_t{1} << 16) ? 2 : 4, v_w = v_narrow ? 1 : 8;
     const auto t1b = std::chrono::steady_clock::now();
-    // the image with int8 values when every value fits (checked while writing
-    // it: on a miss it is rebuilt with int64 values)
-    auto build_image = [&](int va_w) -> bool {
-        ClientImage lay = client_image_layout(nnz_total, vec_total, rowrec_.size() / 4, slicerec_.size() / 2,
-                                              colrec_.size() / 4, static_cast<int>(2 * n), ci_w, va_w, v_w);
+    // narrowing copies of the column indices (range-checked for large batches),
+    // values (int8 checked) and vectors
+    enum Narrow { CI16, CI32, I8, I8V, I64 };
+    struct Piece {
+        unsigned char* d;
+        const void* src;
+        std::size_t cnt;
+        Narrow kind;
+        const CsrView* m;  // column pieces of large batches: the matrix to range-check against
+    };
+    // false when a value did not fit (I8V) or a column was out of range
+    auto narrow = [&](const Piece& p) -> bool {
+        switch (p.kind) {
+            case CI16:
+            case CI32: {
+                const auto* x = static_cast<const std::uint64_t*>(p.src);
+                std::uint64_t all_neg = ~std::uint64_t{0}, any_top = 0;
+                const std::uint64_t cols = p.m ? p.m->cols : 0;
+                if (p.kind == CI16) {
+                    auto* o = reinterpret_cast<std::uint16_t*>(p.d);
+                    for (std::size_t i = 0; i < p.cnt; ++i) {
+                        o[i] = static_cast<std::uint16_t>(x[i]);
+                        all_neg &= x[i] - cols;
+                        any_top |= x[i];
+                    }
+                } else {
+                    auto* o = reinterpret_cast<std::uint32_t*>(p.d);
+                    for (std::size_t i = 0; i < p.cnt; ++i) {
+                        o[i] = static_cast<std::uint32_t>(x[i]);
+                        all_neg &= x[i] - cols;
+                        any_top |= x[i];
+                    }
+                }
+                return !p.m || p.cnt == 0 || ((all_neg >> 63) && !(any_top >> 63));
+            }
+            case I8:
+            case I8V: {
+                auto* o = reinterpret_cast<std::int8_t*>(p.d);
+                const auto* x = static_cast<const std::int64_t*>(p.src);
+                std::uint64_t outside8 = 0;
+                for (std::size_t i = 0; i < p.cnt; ++i) {
+                    o[i] = static_cast<std::int8_t>(x[i]);
+                    outside8 |= (static_cast<std::uint64_t>(x[i]) + 128) >> 8;  // outside [-128, 127]
+                }
+                return outside8 == 0;
+            }
+            case I64:
+                if (p.cnt) std::memcpy(p.d, p.src, 8 * p.cnt);
+                return true;
+        }
+        return true;
+    };
+    double t_place = 0;
+    // returns {values fit the image's width, columns in range}
+    auto build_image = [&](int va_w) -> std::pair<bool, bool> {
+        ClientImage lay = client_image_layout(nnz_total, vec_total, row_at.back(), slicerec_.size() / 2,
+                                              col_at.back(), static_cast<int>(2 * n), ci_w, va_w, v_w);
         if (hit && lease_.pimg && lease_.pkey == client_image_key(lay)) {
             img_ = lay;
             img_.p = lease_.pimg;
             img_.cap = lease_.pimg_cap;
             img_borrowed_ = true;
         } else {
-            img_ = client_image_take(ctx_, nnz_total, vec_total, rowrec_.size() / 4, slicerec_.size() / 2,
-                                     colrec_.size() / 4, static_cast<int>(2 * n), ci_w, va_w, v_w);
+            img_ = client_image_take(ctx_, nnz_total, vec_total, row_at.back(), slicerec_.size() / 2,
+                                     col_at.back(), static_cast<int>(2 * n), ci_w, va_w, v_w);
             img_borrowed_ = false;
         }
-        // (dst, src, bytes) pieces of the image; large batches copy them on the host pool
-        std::vector<std::tuple<unsigned char*, const void*, std::size_t>> cp;
-        // narrowing copies of the column indices, values and vectors: (dst, src, count, kind)
-        enum Narrow { CI16, CI32, I8, I8V, I64 };
-        std::vector<std::tuple<unsigned char*, const void*, std::size_t, Narrow>> nc;
+        const auto tp = std::chrono::steady_clock::now();
+        std::vector<Piece> pieces;
+        constexpr std::size_t kElems = 1 << 16;
+        auto add = [&](unsigned char* d, std::size_t dw, const void* src, std::size_t cnt, Narrow kind,
+                       const CsrView* m) {
+            for (std::size_t o = 0; o < cnt; o += kElems)
+                pieces.push_back({d + dw * o, static_cast<const std::uint64_t*>(src) + o, std::min(kElems, cnt - o),
+                                  kind, m});
+        };
         std::size_t nz = 0, vo = 0;
         for (const CsrView& m : ms) {
-            nc.emplace_back(img_.p + img_.o_ci + (std::size_t)img_.ci_w * nz, m.col_indices, m.nnz,
-                            img_.ci_w == 2 ? CI16 : CI32);
-            nc.emplace_back(img_.p + img_.o_va + (std::size_t)img_.va_w * nz, m.values, m.nnz,
-                            img_.va_w == 1 ? I8V : I64);
-            nc.emplace_back(img_.p + img_.o_v + (std::size_t)img_.v_w * vo, m.vec, m.cols, img_.v_w == 1 ? I8 : I64);
+            add(img_.p + img_.o_ci + (std::size_t)img_.ci_w * nz, img_.ci_w, m.col_indices, m.nnz,
+                img_.ci_w == 2 ? CI16 : CI32, big ? &m : nullptr);
+            add(img_.p + img_.o_va + (std::size_t)img_.va_w * nz, img_.va_w, m.values, m.nnz,
+                img_.va_w == 1 ? I8V : I64, nullptr);
+            add(img_.p + img_.o_v + (std::size_t)img_.v_w * vo, img_.v_w, m.vec, m.cols, img_.v_w == 1 ? I8 : I64,
+                nullptr);
             nz += m.nnz;
             vo += m.cols;
         }
-        // returns false when an int8-narrowed value did not fit
-        auto narrow = [](unsigned char* d, const void* src, std::size_t cnt, Narrow kind) -> bool {
-            switch (kind) {
-                case CI16: {
-                    auto* o = reinterpret_cast<std::uint16_t*>(d);
-                    const auto* x = static_cast<const std::uint64_t*>(src);
-                    for (std::size_t i = 0; i < cnt; ++i) o[i] = static_cast<std::uint16_t>(x[i]);
-                    return true;
-                }
-                case CI32: {
-                    auto* o = reinterpret_cast<std::uint32_t*>(d);
-                    const auto* x = static_cast<const std::uint64_t*>(src);
-                    for (std::size_t i = 0; i < cnt; ++i) o[i] = static_cast<std::uint32_t>(x[i]);
-                    return true;
-                }
-                case I8:
-                case I8V: {
-                    auto* o = reinterpret_cast<std::int8_t*>(d);
-                    const auto* x = static_cast<const std::int64_t*>(src);
-                    std::uint64_t outside8 = 0;
-                    for (std::size_t i = 0; i < cnt; ++i) {
-                        o[i] = static_cast<std::int8_t>(x[i]);
-                        outside8 |= (static_cast<std::uint64_t>(x[i]) + 128) >> 8;  // outside [-128, 127]
-                    }
-                    return outside8 == 0;
-                }
-                case I64:
-                    if (cnt) std::memcpy(d, src, 8 * cnt);
-                    return true;
+        if (!slicerec_.empty()) std::memcpy(img_.p + img_.o_sl, slicerec_.data(), 4 * slicerec_.size());
+        auto* rows = reinterpret_cast<std::int32_t*>(img_.p + img_.o_rows);
+        auto* pre = reinterpret_cast<std::int32_t*>(img_.p + img_.o_rpre);
+        auto* cols = reinterpret_cast<std::int32_t*>(img_.p + img_.o_cols);
+        pre[row_at.back()] = static_cast<std::int32_t>(nz_at.back());
+        // slice j's device records {nz_begin, len, pos, slice} and the exclusive
+        // prefix of the row lengths (the device pack's entry -> row map), and its
+        // column records {local chunk, k, h, 0}
+        auto place = [&](std::size_t j) {
+            const SliceShape& sh = shapes[j];
+            std::int32_t* rr = rows + 4 * row_at[j];
+            std::int32_t* rp = pre + row_at[j];
+            std::int32_t acc = static_cast<std::int32_t>(nz_at[j]);
+            for (std::size_t i = 0, r = 0; i < sh.rowrec.size(); i += 4, ++r) {
+                rr[i] = sh.rowrec[i];
+                rr[i + 1] = sh.rowrec[i + 1];
+                rr[i + 2] = sh.rowrec[i + 2];
+                rr[i + 3] = sidx[j];
+                rp[r] = acc;
+                acc += sh.rowrec[i + 1];
             }
-            return true;
+            std::int32_t* cr = cols + 4 * col_at[j];
+            for (std::size_t i = 0; i < sh.colrec.size(); i += 4) {
+                cr[i] = local_of[static_cast<std::size_t>(sh.colrec[i] + chunk0[j])];
+                cr[i + 1] = sh.colrec[i + 1];
+                cr[i + 2] = sh.colrec[i + 2];
+                cr[i + 3] = sh.colrec[i + 3];
+            }
         };
-        cp.emplace_back(img_.p + img_.o_rows, rowrec_.data(), 4 * rowrec_.size());
-        {  // exclusive prefix of the row lengths: the device pack's entry -> row map
-            auto* pre = reinterpret_cast<std::int32_t*>(img_.p + img_.o_rpre);
-            const std::size_t nr = rowrec_.size() / 4;
-            std::int32_t acc = 0;
-            for (std::size_t r = 0; r < nr; ++r) {
-                pre[r] = acc;
-                acc += rowrec_[4 * r + 1];
-            }
-            pre[nr] = acc;
-        }
-        cp.emplace_back(img_.p + img_.o_sl, slicerec_.data(), 4 * slicerec_.size());
-        cp.emplace_back(img_.p + img_.o_cols, colrec_.data(), 4 * colrec_.size());
-        bool fits = true;
-        if (big) {
-            constexpr std::size_t kPiece = 1 << 18;
-            std::vector<std::tuple<unsigned char*, const unsigned char*, std::size_t>> pieces;
-            for (auto& [d, src, bytes] : cp)
-                for (std::size_t o = 0; o < bytes; o += kPiece)
-                    pieces.emplace_back(d + o, static_cast<const unsigned char*>(src) + o, std::min(kPiece, bytes - o));
-            constexpr std::size_t kElems = 1 << 16;
-            std::vector<std::tuple<unsigned char*, const void*, std::size_t, Narrow>> npieces;
-            for (auto& [d, src, cnt, kind] : nc) {
-                const std::size_t dw = kind == CI16 ? 2 : kind == CI32 ? 4 : (kind == I8 || kind == I8V) ? 1 : 8;
-                for (std::size_t o = 0; o < cnt; o += kElems)
-                    npieces.emplace_back(d + dw * o, static_cast<const std::uint64_t*>(src) + o, std::min(kElems, cnt - o),
-                                         kind);
-            }
-            std::vector<unsigned char> miss(npieces.size(), 0);
-            HostPool::get().run(pieces.size() + npieces.size(), [&](std::size_t i) {
-                if (i < pieces.size()) {
-                    const auto& [d, src, bytes] = pieces[i];
-                    std::memcpy(d, src, bytes);
-                } else {
-                    const auto& [d, src, cnt, kind] = npieces[i - pieces.size()];
-                    miss[i - pieces.size()] = !narrow(d, src, cnt, kind);
-                }
-            });
-            fits = std::none_of(miss.begin(), miss.end(), [](unsigned char x) { return x != 0; });
-        } else {
-            for (auto& [d, src, bytes] : cp)
-                if (bytes) std::memcpy(d, src, bytes);
-            for (auto& [d, src, cnt, kind] : nc) fits = narrow(d, src, cnt, kind) && fits;
-        }
-        return fits;
+        const std::size_t ns = slices_.size(), np = pieces.size();
+        std::vector<unsigned char> miss(np, 0);
+        auto task = [&](std::size_t i) {
+            if (i < ns)
+                place(i);
+            else
+                miss[i - ns] = !narrow(pieces[i - ns]);
+        };
+        if (big)
+            HostPool::get().run(ns + np, task);
+        else
+            for (std::size_t i = 0; i < ns + np; ++i) task(i);
+        bool fits = true, cols_ok = true;
+        for (std::size_t i = 0; i < np; ++i)
+            if (miss[i]) (pieces[i].kind == I8V ? fits : cols_ok) = false;
+        t_place += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - tp).count();
+        return {fits, cols_ok};
     };
-    if (!build_image(va_narrow ? 1 : 8)) {  // a value outside int8: int64 values
+    auto [fits, cols_ok] = build_image(va_narrow ? 1 : 8);
+    if (cols_ok && !fits) {  // a value outside int8: int64 values
         if (!img_borrowed_) client_image_give(ctx_, img_);
-        build_image(8);
+        std::tie(fits, cols_ok) = build_image(8);
     }
-    decltype(rowrec_)().swap(rowrec_);
-    std::vector<std::int32_t>().swap(slicerec_);
-    decltype(colrec_)().swap(colrec_);
+    if (!cols_ok) {  // the constructor throws: hand back what it holds, then raise in order
+        if (!img_borrowed_) client_image_give(ctx_, img_);
+        img_ = ClientImage{};
+        if (hit) plan_cache_give(ctx_, std::move(lease_));
+        lease_ = PlanLease{};
+        for (const CsrView& m : ms) col_check(m);
+        throw std::logic_error("spmv: column check disagreement");
+    }
     if (trace) {
         const auto t2 = std::chrono::steady_clock::now();
         auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
-        std::fprintf(stderr, "e2e-trace shapes %.1f image %.1f (take %.1f) us\n", us(t0, t1), us(t1, t2),
-                     us(t1, t1b));
+        std::fprintf(stderr, "e2e-trace append %.1f image %.1f (take %.1f place+narrow %.1f) us\n", us(ts, t1),
+                     us(t1, t2), us(t1, t1b), t_place);
     }
     if (hit) return;
     lease_.key = std::move(key);
@@ -389,7 +420,8 @@ BatchedSpmv::BatchedSpmv(spmvgpu_ctx* ctx, const HeParams& hp, std::span<const C
 // h_j = #rows longer than j; chunks open at a column, fix h, and admit columns
 // while h (k + 1) <= budget.  The entries themselves are scattered on the
 // device (k_pack_cssc) from the row records built here.  Independent per
-// slice (chunk indices and the slice id are local, fixed up by append_slice).
+// slice (chunk indices and the slice id are local, fixed up when the records
+// are placed into the client image).
 void BatchedSpmv::shape_slice(const CsrView& m, const SliceJob& job, std::size_t budget, SliceShape& s) const {
     // per-slice checks in the reference's order (protocol.cpp:80-90)
     if (budget == 0 || budget > hp_.slot_count)
@@ -428,7 +460,7 @@ void BatchedSpmv::shape_slice(const CsrView& m, const SliceJob& job, std::size_t
             rr[4 * p] = static_cast<std::int32_t>(job.nz_base + static_cast<std::int64_t>(rp[i]));
             rr[4 * p + 1] = static_cast<std::int32_t>(len);
             rr[4 * p + 2] = static_cast<std::int32_t>(p);
-            rr[4 * p + 3] = 0;  // slice id, set by append_slice
+            rr[4 * p + 3] = 0;  // slice id, set when placed
         }
     }
     s.colrec.resize(4 * max_len);
@@ -437,7 +469,7 @@ void BatchedSpmv::shape_slice(const CsrView& m, const SliceJob& job, std::size_t
     for (std::size_t first = 0; first < max_len;) {
         const std::size_t h = height[first];
         const std::size_t fit = std::min<std::size_t>(budget / h, max_len - first);
-        const auto chunk = static_cast<std::int32_t>(s.r.size());  // local; append_slice offsets it
+        const auto chunk = static_cast<std::int32_t>(s.r.size());  // local; offset when placed
         for (std::size_t k = 0; k < fit; ++k, cw += 4) {
             cr[cw] = chunk;
             cr[cw + 1] = static_cast<std::int32_t>(k);
@@ -450,7 +482,7 @@ void BatchedSpmv::shape_slice(const CsrView& m, const SliceJob& job, std::size_t
     }
 }
 
-void BatchedSpmv::append_slice(SliceShape&& sh, std::size_t col_base) {
+void BatchedSpmv::append_slice(SliceShape& sh, std::size_t col_base) {
     Slice s;
     s.mat = sh.mat;
     s.rows = sh.rows;

@@ -90,9 +90,10 @@ private:
         std::exception_ptr err;
     };
     void shape_slice(const CsrView& m, const SliceJob& job, std::size_t budget, SliceShape& out) const;
-    // slice metadata, chunk shapes and slice record; the row / column records
-    // are placed by the caller (col_base = the slice's first column record)
-    void append_slice(SliceShape&& s, std::size_t col_base);
+    // slice metadata (takes the shape's row map), chunk shapes and slice
+    // record; the row / column records are placed into the image by the
+    // caller (col_base = the slice's first column record)
+    void append_slice(SliceShape& s, std::size_t col_base);
     void ensure_plan();
     std::vector<SpmvResult> decrypt_and_report(const std::vector<spmvgpu_ct>& outs);
     // one result's decrypted slots: u64 (decrypt) or u32 (pipeline download);
@@ -111,26 +112,7 @@ private:
     std::size_t nmat_;
     std::vector<std::size_t> rows_of_;
     std::vector<Slice> slices_;
-    // device pack descriptors (spmvgpu_encrypt_cssc layout), then the pinned upload image
-    // resize() leaves new elements uninitialised: every record is written by
-    // place() right after (2 MB of rows at C5; zero-filling them cost 0.1 ms)
-    template <class T>
-    struct UninitAlloc : std::allocator<T> {
-        template <class U>
-        struct rebind {
-            using other = UninitAlloc<U>;
-        };
-        UninitAlloc() = default;
-        template <class U>
-        UninitAlloc(const UninitAlloc<U>&) noexcept {}
-        template <class U>
-        void construct(U*) noexcept {}  // value-initialisation: skipped
-        template <class U, class... A>
-        void construct(U* p, A&&... a) {
-            ::new (static_cast<void*>(p)) U(std::forward<A>(a)...);
-        }
-    };
-    std::vector<std::int32_t, UninitAlloc<std::int32_t>> rowrec_, colrec_;
+    // slice records {first column record, vector base} (the image's slice table)
     std::vector<std::int32_t> slicerec_;
     ClientImage img_;
     bool img_borrowed_ = false;  // img_.p is the cached pipeline's pinned buffer

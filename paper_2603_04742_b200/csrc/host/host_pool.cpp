@@ -2,12 +2,17 @@
 #include "host/host_pool.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace spmv::detail {
 
 HostPool& HostPool::get() {
     // never destroyed: idle workers simply end with the process
-    static HostPool* pool = new HostPool(std::min(7u, std::max(1u, std::thread::hardware_concurrency()) - 1));
+    static HostPool* pool = [] {
+        unsigned w = std::min(15u, std::max(1u, std::thread::hardware_concurrency()) - 1);
+        if (const char* e = std::getenv("CSSC_HOST_THREADS")) w = static_cast<unsigned>(std::max(1, std::atoi(e)) - 1);
+        return new HostPool(w);
+    }();
     return *pool;
 }
 

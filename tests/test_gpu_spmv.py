@@ -320,6 +320,48 @@ def test_large_batch_validation_on_the_host_pool(where):
     ctx.close()
 
 
+def test_large_batch_error_order():
+    """Large batches check column ranges inside the image pass; when several
+    matrices are bad, the error raised is still the one the sequential
+    evaluation meets first (per matrix: row_ptrs, columns, then chunking), and
+    a failed call leaves the cached plan usable."""
+    ctx = pk.Context(logn=13, seed=2)
+    ms = [synth.random_sparse_csr(2048, 2048, 70000, 100 + i, -8, 8) for i in range(4)]
+    vs = [synth.random_vector(2048, 100 + i, -8, 8, nonzero=True) for i in range(4)]
+
+    def badcol(i):
+        c = ms[i].col_indices.copy()
+        c[123] = 2048 + 7
+        return pk.Csr(2048, 2048, ms[i].row_ptrs, c, ms[i].values)
+
+    def badrows(i):
+        rp = ms[i].row_ptrs.copy()
+        rp[10] = rp[11] + 1
+        return pk.Csr(2048, 2048, rp, ms[i].col_indices, ms[i].values)
+
+    def run(batch, chunk=None):
+        with pytest.raises(pk.SpmvError) as e:
+            pk.spmv_batch(ctx, batch, vs, chunk_size=chunk or ctx.slots)
+        return e.value
+
+    good = pk.spmv_batch(ctx, ms, vs, chunk_size=ctx.slots)  # caches the plan
+    e = run([ms[0], badcol(1), ms[2], badrows(3)])
+    assert e.kind == "IndexOutOfRangeError" and "2055" in str(e)
+    e = run([ms[0], badrows(1), badcol(2), ms[3]])
+    assert "non-decreasing" in str(e)
+    e = run([badcol(0), ms[1], ms[2], ms[3]], ctx.slots + 1)
+    assert e.kind == "IndexOutOfRangeError"
+    e = run([ms[0], ms[1], badcol(2), ms[3]], ctx.slots + 1)
+    assert "chunk_size" in str(e)
+    e = run([ms[0], ms[1], ms[2], badcol(3)])  # same shapes as the cached plan
+    assert e.kind == "IndexOutOfRangeError"
+    again = pk.spmv_batch(ctx, ms, vs, chunk_size=ctx.slots)
+    for m, v, g, h in zip(ms, vs, good, again):
+        want = checker(m, v, ctx.slots, ctx.slots)["values"]
+        assert np.array_equal(g["values"], want) and np.array_equal(h["values"], want)
+    ctx.close()
+
+
 @pytest.mark.parametrize("capacity", [1, 4])
 def test_alternating_plans_with_speculative_early_encryption(capacity):
     """Each spmv_batch call enqueues the previous call's early encryption graph
