@@ -128,6 +128,119 @@ __global__ void __launch_bounds__(Ntt2<LOGN>::TC, 256 / Ntt2<LOGN>::TC * 3) k_ks
     }
 }
 
+// K1 over all target limbs of a digit (fixed RNS shapes): one CTA per (item,
+// digit, tile of LC columns) holds the LC columns of every one of the L+K
+// target limbs (16 lines = (L+K) x LC).  Each coefficient of phi_g(source)
+// is gathered once per digit prime -- the alpha hoisted factors y_i -- and
+// feeds every target limb: the digit's own limbs x_i = y_i [Q_d/q_i]_{q_i}
+// (one Shoup product, the same canonical word as gathering x_i), the others
+// the ModUp sum.  The per-limb kernel above gathers each coefficient once
+// per target limb (x_i for own limbs, all y_i for each other limb: 6 loads
+// per coefficient at L = K = 2 instead of 2); K1 stalls on those gathers
+// (long scoreboard, profiles/r02_ncu_c5_*).
+template <int LOGN, int LT, int KT, int AT, int LC>
+__global__ void __launch_bounds__(Ntt2<LOGN>::TC, 256 / Ntt2<LOGN>::TC * 3)
+    k_ks_modup_all(const DevConsts* __restrict__ dc, const u64* const* SRC, const u64* SRCC, int src_poly,
+                   const u32* ginv, u64* DX, const u64* const* YS, const u64* YSC) {
+    using G = Ntt2<LOGN>;
+    constexpr int LK = LT + KT, VL = LK * LC, DN = (LT + AT - 1) / AT;
+    static_assert(LT > 0 && VL <= 16 && G::TC % VL == 0, "fixed shapes with at most 16 lines");
+    constexpr int CT = G::R2 / LC;
+    constexpr int TWS = 2 * G::R1 + 2;  // per-limb twiddle stride (16 B pad: limbs on distinct banks)
+    extern __shared__ u64 smem[];
+    u64* tile = smem;                   // [R1][VL], line = limb * LC + column
+    u64* tws = smem + VL * G::R1;       // [LK][TWS]
+    int bid = blockIdx.x;
+    const int tileid = bid % CT;
+    bid /= CT;
+    const int dg = bid % DN;
+    const int item = bid / DN;
+    const int lo = dg * AT, hi = lo + AT < LT ? lo + AT : LT;
+    const u64* src = SRC ? SRC[item] + (size_t)src_poly * LT * G::N : SRCC + (size_t)item * LT * G::N;
+    const u64* ysrc = YS ? YS[item] : (YSC ? YSC + (size_t)item * LT * G::N : nullptr);
+    const u32 gi = ginv ? ginv[item] : 0u;
+    const int col0 = tileid * LC;
+    for (int i = threadIdx.x; i < LK * G::R1; i += G::TC) {
+        const int jj = i / G::R1, k = i % G::R1;
+        const ulonglong2 w = __ldg(reinterpret_cast<const ulonglong2*>(dc->tw[jj].fwd) + k);
+        *reinterpret_cast<ulonglong2*>(tws + jj * TWS + 2 * k) = w;
+    }
+    constexpr int PER = G::R1 * LC / G::TC;
+    static_assert(PER >= 1, "column tile smaller than the CTA");
+#pragma unroll
+    for (int r = 0; r < PER; ++r) {
+        const int e = threadIdx.x + G::TC * r, c = e / LC, jl = e % LC;
+        bool neg;
+        const int idx = ks_automorph(gi, col0 + jl + G::R2 * c, G::N, neg);
+        u64 x[AT], y[AT];
+#pragma unroll
+        for (int a = 0; a < AT; ++a) {
+            const int i = lo + a;
+            if (i >= hi) break;
+            const u64 qi = dc->mod[i].q;
+            if (ysrc) {  // y of phi_g(x) is phi_g(y); x_i = y_i [Q_d/q_i]_{q_i}
+                u64 v = __ldg(ysrc + (size_t)i * G::N + idx);
+                y[a] = neg ? neg_mod(v, qi) : v;
+                x[a] = shoup(y[a], dc->dig_hat[i][i], dc->dig_hat_sh[i][i], qi);
+            } else {
+                u64 v = __ldg(src + (size_t)i * G::N + idx);
+                x[a] = neg ? neg_mod(v, qi) : v;
+                y[a] = shoup(x[a], dc->dig_hat_inv[i], dc->dig_hat_inv_sh[i], qi);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < LK; ++j) {
+            u64 v;
+            if (j >= lo && j < hi) {
+                v = x[j - lo];
+            } else {
+                v = 0;
+#pragma unroll
+                for (int a = 0; a < AT; ++a) {
+                    const int i = lo + a;
+                    if (i >= hi) break;
+                    v += shoup_lazy(y[a], dc->dig_hat[i][j], dc->dig_hat_sh[i][j], dc->mod[j].q);
+                }
+                v = reduce_small_quot(v, dc->mod[j]);
+            }
+            tile[c * VL + j * LC + jl] = v;
+        }
+    }
+    __syncthreads();
+    // every thread keeps one line (tid % VL) in every pass: its modulus and
+    // twiddle row are per-thread constants
+    const int myl = threadIdx.x % VL;
+    const u64 myq = dc->mod[myl / LC].q;
+    const u64* mytw = tws + (myl / LC) * TWS;
+    auto addr = [](int l, int pos) { return pos * VL + l; };
+    auto twf = [&](int sl, int, int blk) {
+        const int k = (1 << sl) + blk;
+        return *reinterpret_cast<const ulonglong2*>(mytw + 2 * k);
+    };
+    line_ntt_v<G::A, 0, false, 3, VL>(tile, ConstQ{myq}, addr, twf, whole_cta());
+    u64* dst = DX + ((size_t)item * DN + dg) * LK * G::N;
+    constexpr int SEG = LC / 2;
+    static_assert(LC % 2 == 0, "pairs of columns per store");
+#pragma unroll
+    for (int r = 0; r < G::R1 * LK * SEG / G::TC; ++r) {
+        const int i = threadIdx.x + G::TC * r, h = i % SEG, j = (i / SEG) % LK, c = i / (SEG * LK);
+        *reinterpret_cast<ulonglong2*>(dst + (size_t)j * G::N + (size_t)c * G::R2 + col0 + 2 * h) =
+            make_ulonglong2(tile[c * VL + j * LC + 2 * h], tile[c * VL + j * LC + 2 * h + 1]);
+    }
+}
+
+template <int LT, int KT>
+constexpr int modup_all_lc() { return 16 / (LT + KT) >= 2 ? 16 / (LT + KT) : 0; }
+
+// CSSC_K1_ALL=0 keeps the per-limb K1
+static bool k1_all_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("CSSC_K1_ALL");
+        return !e || std::atoi(e) != 0;
+    }();
+    return on;
+}
+
 // ---------------------------------------------------------------------------
 // K2: NTT block phase + key inner product + INTT block phase
 // ---------------------------------------------------------------------------
@@ -285,7 +398,20 @@ static void ks_fused_t(const DevConsts* dc, const RnsParams& P, const u64* const
     smem_optin_k(k_ks_modup_cols<LOGN, LT, KT, AT>, smem1);
     smem_optin_k(k_ks_blocks_inner<LOGN, LT, KT, AT>, smem2);
     smem_optin_k(k_ks_blocks_inner<LOGN, LT, KT, AT, 8>, smem2h);
-    if (cols_use_ln4((long)items * dnum * LK * G::CTAS_C, G::R1 >= G::TC)) {  // 4-column tiles
+    bool k1_done = false;
+    constexpr int LCA = LT ? modup_all_lc<LT, KT>() : 0;
+    if constexpr (LCA > 0 && G::R1 * LCA >= G::TC && (G::R1 * LCA / 2 * (LT + KT)) % G::TC == 0) {
+        if (k1_all_enabled() && !cols_use_ln8((long)items * dnum * LK * G::CTAS_C, G::R1 * 4 >= G::TC)) {
+            constexpr int VL = (LT + KT) * LCA;
+            const int smemA = (VL * G::R1 + (LT + KT) * (2 * G::R1 + 2)) * 8;
+            smem_optin_k(k_ks_modup_all<LOGN, LT, KT, AT, LCA>, smemA);
+            k_ks_modup_all<LOGN, LT, KT, AT, LCA><<<items * dnum * (G::R2 / LCA), G::TC, smemA, st>>>(
+                dc, SRC, SRCC, src_poly, ginv, DX, ky.src, ky.srcc);
+            k1_done = true;
+        }
+    }
+    if (k1_done) {
+    } else if (cols_use_ln4((long)items * dnum * LK * G::CTAS_C, G::R1 >= G::TC)) {  // 4-column tiles
         constexpr int LN = 4;
         k_ks_modup_cols<LOGN, LT, KT, AT, LN><<<items * dnum * LK * (G::R2 / LN), G::TC,
                                                 (LN * G::R1 + 2 * G::R1) * 8, st>>>(dc, SRC, SRCC, src_poly, ginv, DX, ky.src, ky.srcc);
