@@ -232,13 +232,15 @@ __global__ void __launch_bounds__(Ntt2<LOGN>::TC, 256 / Ntt2<LOGN>::TC * 3)
 template <int LT, int KT>
 constexpr int modup_all_lc() { return 16 / (LT + KT) >= 2 ? 16 / (LT + KT) : 0; }
 
-// CSSC_K1_ALL=0 keeps the per-limb K1
-static bool k1_all_enabled() {
-    static const bool on = [] {
+// Used for launches whose 16-column CTAs fill a wave (default, =2); =1 also
+// below that with 8 lines per CTA (measured 1-2 % slower at C1-C3 than the
+// per-limb 4/8-column tiles there); =0 keeps the per-limb K1 everywhere.
+static int k1_all_mode() {
+    static const int mode = [] {
         const char* e = std::getenv("CSSC_K1_ALL");
-        return !e || std::atoi(e) != 0;
+        return e ? std::atoi(e) : 2;
     }();
-    return on;
+    return mode;
 }
 
 // ---------------------------------------------------------------------------
@@ -400,13 +402,26 @@ static void ks_fused_t(const DevConsts* dc, const RnsParams& P, const u64* const
     smem_optin_k(k_ks_blocks_inner<LOGN, LT, KT, AT, 8>, smem2h);
     bool k1_done = false;
     constexpr int LCA = LT ? modup_all_lc<LT, KT>() : 0;
-    if constexpr (LCA > 0 && G::R1 * LCA >= G::TC && (G::R1 * LCA / 2 * (LT + KT)) % G::TC == 0) {
-        if (k1_all_enabled() && !cols_use_ln8((long)items * dnum * LK * G::CTAS_C, G::R1 * 4 >= G::TC)) {
+    constexpr bool HALF = LCA >= 4 && G::R1 * LCA / 2 >= G::TC && (G::R1 * LCA / 4 * (LT + KT)) % G::TC == 0;
+    if constexpr (LCA >= 2 && G::R1 * LCA >= G::TC && (G::R1 * LCA / 2 * (LT + KT)) % G::TC == 0) {
+        const bool small = cols_use_ln8((long)items * dnum * LK * G::CTAS_C, G::R1 * 4 >= G::TC);
+        if (k1_all_mode() != 0 && (!small || (HALF && k1_all_mode() == 1))) {
+            // 16 lines, or 8 (half the columns per CTA) when the launch would not fill the GPU
             constexpr int VL = (LT + KT) * LCA;
-            const int smemA = (VL * G::R1 + (LT + KT) * (2 * G::R1 + 2)) * 8;
-            smem_optin_k(k_ks_modup_all<LOGN, LT, KT, AT, LCA>, smemA);
-            k_ks_modup_all<LOGN, LT, KT, AT, LCA><<<items * dnum * (G::R2 / LCA), G::TC, smemA, st>>>(
-                dc, SRC, SRCC, src_poly, ginv, DX, ky.src, ky.srcc);
+            auto go = [&](auto lc_) {
+                constexpr int LC = decltype(lc_)::value;
+                const int smemA = (VL / (LCA / LC) * G::R1 + (LT + KT) * (2 * G::R1 + 2)) * 8;
+                smem_optin_k(k_ks_modup_all<LOGN, LT, KT, AT, LC>, smemA);
+                k_ks_modup_all<LOGN, LT, KT, AT, LC><<<items * dnum * (G::R2 / LC), G::TC, smemA, st>>>(
+                    dc, SRC, SRCC, src_poly, ginv, DX, ky.src, ky.srcc);
+            };
+            if constexpr (HALF)
+                if (small) {
+                    go(std::integral_constant<int, LCA / 2>{});
+                    k1_done = true;
+                }
+            if (!k1_done)
+                go(std::integral_constant<int, LCA>{});
             k1_done = true;
         }
     }
