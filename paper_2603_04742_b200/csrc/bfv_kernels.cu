@@ -1169,18 +1169,20 @@ static ModDownK<L, K> make_moddown_k(const RnsParams& P, bool lazy = false) {
 // PAIR (level 0): the CTAs of a D_1 item also transform their O_1 partner's
 // tiles and add both ModDowns (same sums as k_ks_moddown_k's split pair);
 // the partner's CTAs exit.  Same words as k_ntt_cols + k_ks_moddown_k.
-template <int LOGN, int L, int K, int LN>
-__global__ void __launch_bounds__(Ntt2<LOGN>::TC) k_ks_cols_moddown(
+template <int LOGN, int L, int K, int LN, int RADIX = 3>
+__global__ void __launch_bounds__(Ntt2<LOGN>::TC, 256 / Ntt2<LOGN>::TC * (RADIX == 3 ? 3 : 4)) k_ks_cols_moddown(
     const __grid_constant__ ModDownK<L, K> c, const DevConsts* __restrict__ dc, const u64* __restrict__ ACC,
     const u64* const* BASE, const u64* const* RSRC, const u32* ginv, u64* const* OUT, const u64* const* EXTRA,
     const int* PAIR, u64* const* YOUT) {
     using G = Ntt2<LOGN>;
     constexpr int LK = L + K, T = G::TC, CTAS = G::R2 / LN, SEG = LN / 2;
-    constexpr int TILE = LN * G::R1, PER = TILE / T;  // elements per thread
-    static_assert(PER >= 1 && TILE % T == 0, "tile smaller than the CTA");
+    constexpr int VL = LK * LN;                 // lines: (limb, column)
+    constexpr int TILE = LN * G::R1, PER = TILE / T;  // elements per thread and limb
+    constexpr int TWS = 2 * G::R1 + 2;          // per-limb twiddle stride (16 B pad: limbs on distinct banks)
+    static_assert(PER >= 1 && TILE % T == 0 && T % VL == 0, "tile smaller than the CTA");
     extern __shared__ u64 smem[];
-    u64* tiles = smem;              // [LK][R1][LN]
-    u64* tws = smem + LK * TILE;    // [LK][R1] (w, w_shoup) pairs
+    u64* tiles = smem;              // [R1][VL], line = limb * LN + column
+    u64* tws = smem + LK * TILE;    // [LK][TWS] (w, w_shoup) pairs
     const int n = c.n;
     const int tileid = blockIdx.x % CTAS;
     const int rest = blockIdx.x / CTAS;
@@ -1190,9 +1192,16 @@ __global__ void __launch_bounds__(Ntt2<LOGN>::TC) k_ks_cols_moddown(
     if (pv <= -3) return;  // an O_1 partner: evaluated by its D_1's CTAs
     const int col0 = tileid * LN;
     for (int j = 0; j < LK; ++j)
-        for (int i = threadIdx.x; i < G::R1; i += T) cp_async16(tws + 2 * ((size_t)j * G::R1 + i), dc->tw[j].inv + 2 * i);
-    auto addr = [](int l, int pos) { return pos * LN + l; };
-    // inverse column phase of item `it`'s LK tiles of polynomial p, in smem
+        for (int i = threadIdx.x; i < G::R1; i += T) cp_async16(tws + (size_t)j * TWS + 2 * i, dc->tw[j].inv + 2 * i);
+    auto addr = [](int l, int pos) { return pos * VL + l; };
+    auto at = [](int j, int e) { return (e / LN) * VL + j * LN + (e % LN); };  // element e of limb j's tile
+    // every thread keeps one line (tid % VL) in every pass: its modulus and
+    // twiddle row are per-thread constants
+    const int myl = threadIdx.x % VL;
+    const u64 myq = dc->mod[myl / LN].q;
+    const u64* mytw = tws + (size_t)(myl / LN) * TWS;
+    // inverse column phase of item `it`'s LK tiles of polynomial p, in smem:
+    // all limbs in the same passes (radix-8, 16 lines)
     auto transform = [&](int it) {
         const u64* acc = ACC + ((size_t)it * 2 + p) * LK * n;
 #pragma unroll
@@ -1200,21 +1209,16 @@ __global__ void __launch_bounds__(Ntt2<LOGN>::TC) k_ks_cols_moddown(
 #pragma unroll
             for (int r = 0; r < G::R1 * SEG / T; ++r) {
                 const int i = threadIdx.x + T * r, cc = i / SEG, h = i % SEG;
-                cp_async16(tiles + (size_t)j * TILE + cc * LN + 2 * h, acc + (size_t)j * n + (size_t)cc * G::R2 + col0 + 2 * h);
+                cp_async16(tiles + (size_t)cc * VL + j * LN + 2 * h, acc + (size_t)j * n + (size_t)cc * G::R2 + col0 + 2 * h);
             }
         }
         cp_async_wait_all();
         __syncthreads();
-#pragma unroll 1
-        for (int j = 0; j < LK; ++j) {
-            const u64* tw = tws + 2 * (size_t)j * G::R1;
-            auto twf = [&](int sl, int, int blk) {
-                const int k = (1 << sl) + blk;
-                return make_ulonglong2(tw[2 * k], tw[2 * k + 1]);
-            };
-            line_ntt_v<G::A, 0, true, (LN >= 8 ? 3 : 2), LN>(tiles + (size_t)j * TILE, ConstQ{dc->mod[j].q}, addr, twf,
-                                                            whole_cta());
-        }
+        auto twf = [&](int sl, int, int blk) {
+            const int k = (1 << sl) + blk;
+            return *reinterpret_cast<const ulonglong2*>(mytw + 2 * k);
+        };
+        line_ntt_v<G::A, 0, true, RADIX, VL>(tiles, ConstQ{myq}, addr, twf, whole_cta());
     };
     // ModDown of element e of the transformed tiles of item `it` (+ its rotated c0)
     auto moddown = [&](int it, int e, u64 out[L]) {
@@ -1222,14 +1226,14 @@ __global__ void __launch_bounds__(Ntt2<LOGN>::TC) k_ks_cols_moddown(
         u64 y[K];
 #pragma unroll
         for (int kk = 0; kk < K; ++kk)
-            y[kk] = shoup(tiles[(size_t)(L + kk) * TILE + e], c.phat_inv[kk], c.phat_inv_sh[kk], c.pk[kk]);
+            y[kk] = shoup(tiles[at(L + kk, e)], c.phat_inv[kk], c.phat_inv_sh[kk], c.pk[kk]);
         const u64* rs = (RSRC && p == 0) ? RSRC[it] : nullptr;
         bool neg = false;
         const int ridx = rs ? automorph_src(ginv ? ginv[it] : 0u, k, n, neg) : k;
 #pragma unroll
         for (int j = 0; j < L; ++j) {
             const u64 q = c.qm[j].q;
-            u64 a = tiles[(size_t)j * TILE + e];
+            u64 a = tiles[at(j, e)];
             a = a >= q ? a - q : a;
             Dot29 d;
             dot29_mac(d, a, c.F[j]);
@@ -1308,11 +1312,21 @@ static bool cols_moddown_ln(const DevConsts* dc, const RnsParams& P, const u64* 
     if constexpr (G::R2 < 16 || G::R1 * LN < G::TC) {
         return false;
     } else {
-        constexpr int smem = ((L + K) * LN * G::R1 + 2 * (L + K) * G::R1) * 8;
-        smem_optin_k(k_ks_cols_moddown<LOGN, L, K, LN>, smem);
+        constexpr int smem = ((L + K) * LN * G::R1 + (L + K) * (2 * G::R1 + 2)) * 8;
         const unsigned grid = (unsigned)items * 2 * (G::R2 / LN);
-        k_ks_cols_moddown<LOGN, L, K, LN><<<grid, G::TC, smem, st>>>(make_moddown_k<L, K>(P, true), dc, ACC, BASE,
-                                                                     RSRC, ginv, OUT, EXTRA, PAIR, YOUT);
+        static const int radix = [] {
+            const char* e = std::getenv("CSSC_CMD_RADIX");  // radix-4 passes (64 regs, 4 CTAs/SM) measured 0.2 % faster at C5
+            return e ? std::atoi(e) : 2;
+        }();
+        if (radix == 2) {
+            smem_optin_k(k_ks_cols_moddown<LOGN, L, K, LN, 2>, smem);
+            k_ks_cols_moddown<LOGN, L, K, LN, 2><<<grid, G::TC, smem, st>>>(make_moddown_k<L, K>(P, true), dc, ACC,
+                                                                            BASE, RSRC, ginv, OUT, EXTRA, PAIR, YOUT);
+        } else {
+            smem_optin_k(k_ks_cols_moddown<LOGN, L, K, LN>, smem);
+            k_ks_cols_moddown<LOGN, L, K, LN><<<grid, G::TC, smem, st>>>(make_moddown_k<L, K>(P, true), dc, ACC, BASE,
+                                                                         RSRC, ginv, OUT, EXTRA, PAIR, YOUT);
+        }
         CSSC_CHECK_LAUNCH();
         return true;
     }
