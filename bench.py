@@ -345,11 +345,19 @@ def kernel_units(name: str, items: int, slices: int, logn: int, L: int, K: int, 
     n, h = 1 << logn, 1 << (logn - 1)
     Bs = 7 if logn >= 15 else (6 if logn >= 12 else logn // 2)
     As = logn - Bs
-    M, LK, nB = 2 * L + 1, L + K, L + 1
+    # the shapes with specialised kernels multiply over Q u R (2L limbs, E6-E8),
+    # the others over Q u B (HPS, 2L + 1)
+    overq = (L, K, alpha) in ((2, 2, 2), (4, 4, 4))
+    M, LK, nB = (2 * L if overq else 2 * L + 1), L + K, L + 1
     e1_q2b = L + L + nB * (L + 1) * DOT          # E1 Q -> B per coefficient of one poly
     e1_b2q = nB + nB + L * (nB + 1) * DOT        # E1 B -> Q
     e2 = L + L + nB * (L + 1) * DOT              # E2 scale-and-round into B
+    e1_qr = L + L + L * (L + 1) * DOT            # E1 Q -> R (or R -> Q)
+    e6 = L + L + L * L * DOT                     # E6 b -> round(R b / Q) in R
+    e8 = L + 2 * L + L * (L + 1) * DOT           # E8 round(t z / R) into Q
     if name.startswith("k_mul_extend"):
+        if overq:
+            return items * 2 * n * (e1_qr + e6 + e1_qr)
         return items * 4 * n * e1_q2b
     if name.startswith("k_ntt_cols fwd (multiply)"):
         return items * 4 * M * h * As
@@ -358,7 +366,7 @@ def kernel_units(name: str, items: int, slices: int, logn: int, L: int, K: int, 
     if name.startswith("k_ntt_cols inv (multiply)"):
         return items * 3 * M * h * As
     if name.startswith("k_mul_scale"):
-        return items * 3 * n * (e2 + e1_b2q)
+        return items * 3 * n * (e8 if overq else e2 + e1_b2q)
     if name.startswith("k_ks_modup_cols"):
         return items * dnum * LK * (n * alpha + h * As)
     if name.startswith("k_ks_blocks_inner"):

@@ -195,6 +195,14 @@ struct bfvo_ctx {
     u64 Pinv_q[MAXP];           /* [P^-1]_{q_j} */
     u64 phat_inv[MAXP];         /* [(P/p_k)^-1]_{p_k} */
     u64 phat_q[MAXP][MAXP];     /* [P/p_k]_{q_j} */
+    /* the over-Q multiply (fixed shapes, E6-E8): R = first L primes of B */
+    int overq;
+    ext_t extQR, extRQ;
+    u64 QR_theta[MAXP];         /* floor(2^64 [R]_{q_i} / q_i) */
+    u64 QR_omega[MAXP][MAXP];   /* [floor(R / q_i)]_{r_k} */
+    u64 TR1[MAXP], TR0[MAXP];   /* floor(t 2^128 / r_k) */
+    u64 tRinv_q[MAXP];          /* [t R^-1]_{q_j} */
+    u64 tRinvRhat_q[MAXP][MAXP];/* [-t R^-1 (R / r_k)]_{q_j} */
 };
 
 static void floor_2_128_div(u64 q, u64* hi, u64* lo, u64* rem) {
@@ -457,6 +465,40 @@ bfvo_ctx* bfvo_create(int logn, int L, int K, int alpha, int qbits, int pbits, u
             u64 hq = 1;
             for (int m = 0; m < K; m++) if (m != k) hq = mulm(hq, c->q[L + m] % Q[j], Q[j]);
             c->phat_q[k][j] = hq;
+        }
+    }
+
+    /* over-Q multiply: the shapes with specialised GPU kernels use it (E6-E8) */
+    c->overq = (L == 2 && K == 2 && alpha == 2) || (L == 4 && K == 4 && alpha == 4);
+    {
+        const u64* R = B; /* r_k = b_k, k < L */
+        setup_ext(&c->extQR, Q, L, R, L);
+        setup_ext(&c->extRQ, R, L, Q, L);
+        for (int i = 0; i < L; i++) {
+            u64 Rq = 1;
+            for (int k = 0; k < L; k++) Rq = mulm(Rq, R[k] % Q[i], Q[i]);
+            c->QR_theta[i] = (u64)(((u128)Rq << 64) / Q[i]);
+            for (int k = 0; k < L; k++) /* floor(R/q_i) = (R - [R]_{q_i}) / q_i, R = 0 mod r_k */
+                c->QR_omega[i][k] = mulm(subm(0, Rq % R[k], R[k]), invm(Q[i] % R[k], R[k]), R[k]);
+        }
+        for (int k = 0; k < L; k++) {
+            u64 R1, R0, rem;
+            floor_2_128_div(R[k], &R1, &R0, &rem);
+            u128 Rr = ((u128)R1 << 64) | R0;
+            u128 T = Rr * t + ((u128)rem * t) / R[k];
+            c->TR1[k] = (u64)(T >> 64);
+            c->TR0[k] = (u64)T;
+        }
+        for (int j = 0; j < L; j++) {
+            u64 Rq = 1;
+            for (int k = 0; k < L; k++) Rq = mulm(Rq, R[k] % Q[j], Q[j]);
+            u64 tRinv = mulm(t % Q[j], invm(Rq, Q[j]), Q[j]);
+            c->tRinv_q[j] = tRinv;
+            for (int k = 0; k < L; k++) {
+                u64 hk = 1;
+                for (int m = 0; m < L; m++) if (m != k) hk = mulm(hk, R[m] % Q[j], Q[j]);
+                c->tRinvRhat_q[k][j] = subm(0, mulm(tRinv, hk, Q[j]), Q[j]);
+            }
         }
     }
 
@@ -759,7 +801,116 @@ int bfvo_key_switch(bfvo_ctx* c, uint32_t which, const u64* d, u64* ks0, u64* ks
     return 0;
 }
 
+/* E6: b'' = round(R b / Q) mod r_k for one coefficient (b by its Q residues):
+ * R b / Q = sum_i y_i R / q_i - v R with y_i = [b_i (Q/q_i)^-1]_{q_i}; mod r_k the
+ * v R term vanishes and R/q_i = floor(R/q_i) + [R]_{q_i}/q_i, so
+ * b''_k = sum_i y_i [floor(R/q_i)]_{r_k} + round(sum_i y_i theta_i), the
+ * rounding term in 64-bit fixed point (theta_i = floor(2^64 [R]_{q_i} / q_i)). */
+static void scale_q_to_r(const bfvo_ctx* c, const u64* x, u64* out) {
+    const u64* R = c->q + c->L + c->K;
+    u64 y[MAXP];
+    u128 S = 0;
+    for (int i = 0; i < c->L; i++) {
+        y[i] = mulm(x[i], c->extQR.xhat_inv[i], c->q[i]);
+        S += (u128)y[i] * c->QR_theta[i];
+    }
+    u64 rnd = (u64)((S + ((u128)1 << 63)) >> 64);
+    for (int k = 0; k < c->L; k++) {
+        u64 acc = rnd % R[k];
+        for (int i = 0; i < c->L; i++) acc = addm(acc, mulm(y[i] % R[k], c->QR_omega[i][k], R[k]), R[k]);
+        out[k] = acc;
+    }
+}
+
+/* E8: round(t z / R) mod q_j from the Q u R residues of z (any representative
+ * mod QR: t z / R is then fixed mod tQ, so mod Q the wrap is harmless).  With
+ * z_R = sum_k y_k R/r_k - v R (y_k = [z_k (R/r_k)^-1]_{r_k}) and z = z_R + R u,
+ * round(t z / R) = t u + round(sum_k t y_k / r_k) - t v, and mod q_j the v terms
+ * cancel: [t R^-1] z_j + sum_k y_k [-t R^-1 R/r_k] + round(sum_k t y_k / r_k),
+ * the rounding term in the fixed point of E2 (floor(t 2^128 / r_k)). */
+static void scale_r_to_q(const bfvo_ctx* c, const u64* zq, const u64* zr, u64* out) {
+    const u64* R = c->q + c->L + c->K;
+    u64 y[MAXP];
+    u128 S = 0;
+    for (int k = 0; k < c->L; k++) {
+        y[k] = mulm(zr[k], c->extRQ.xhat_inv[k], R[k]);
+        S += (u128)y[k] * c->TR1[k] + mulhi(y[k], c->TR0[k]);
+    }
+    u64 rnd = (u64)((S + ((u128)1 << 63)) >> 64);
+    for (int j = 0; j < c->L; j++) {
+        u64 q = c->q[j];
+        u64 acc = addm(mulm(zq[j], c->tRinv_q[j], q), rnd % q, q);
+        for (int k = 0; k < c->L; k++) acc = addm(acc, mulm(y[k] % q, c->tRinvRhat_q[k][j], q), q);
+        out[j] = acc;
+    }
+}
+
+/* the over-Q multiply (Kim-Polyakov-Zucca's HPS-over-Q): a extended Q -> R
+ * (E1), b scaled to R (E6) and extended R -> Q (E1), tensor over Q u R
+ * (2L limbs instead of 2L+1), round(t z / R) to Q (E8) */
+static void mul_tensor_overq(const bfvo_ctx* c, const u64* a, const u64* b, u64* out3) {
+    int n = c->n, L = c->L, M = 2 * L;
+    int pidx[MAXP];
+    for (int j = 0; j < L; j++) pidx[j] = j;
+    for (int j = 0; j < L; j++) pidx[L + j] = L + c->K + j;
+    u64* ext[4];
+    const u64* src[4] = {a, a + (size_t)L * n, b, b + (size_t)L * n};
+    u64 col[MAXP], o[MAXP], br[MAXP];
+    for (int p = 0; p < 4; p++) {
+        ext[p] = (u64*)malloc(sizeof(u64) * (size_t)M * n);
+        for (int k = 0; k < n; k++) {
+            for (int j = 0; j < L; j++) col[j] = src[p][(size_t)j * n + k];
+            if (p < 2) {
+                ext_coeff(&c->extQR, col, o);
+                for (int j = 0; j < L; j++) {
+                    ext[p][(size_t)j * n + k] = col[j];
+                    ext[p][(size_t)(L + j) * n + k] = o[j];
+                }
+            } else {
+                scale_q_to_r(c, col, br);
+                ext_coeff(&c->extRQ, br, o);
+                for (int j = 0; j < L; j++) {
+                    ext[p][(size_t)j * n + k] = o[j];
+                    ext[p][(size_t)(L + j) * n + k] = br[j];
+                }
+            }
+        }
+        for (int j = 0; j < M; j++) bfvo_ntt(c, pidx[j], ext[p] + (size_t)j * n);
+    }
+    u64* z[3];
+    for (int r = 0; r < 3; r++) z[r] = (u64*)malloc(sizeof(u64) * (size_t)M * n);
+    for (int j = 0; j < M; j++) {
+        u64 q = c->q[pidx[j]];
+        for (int k = 0; k < n; k++) {
+            size_t x = (size_t)j * n + k;
+            z[0][x] = mulm(ext[0][x], ext[2][x], q);
+            z[1][x] = addm(mulm(ext[0][x], ext[3][x], q), mulm(ext[1][x], ext[2][x], q), q);
+            z[2][x] = mulm(ext[1][x], ext[3][x], q);
+        }
+    }
+    for (int r = 0; r < 3; r++)
+        for (int j = 0; j < M; j++) bfvo_intt(c, pidx[j], z[r] + (size_t)j * n);
+    u64 zq[MAXP], zr[MAXP];
+    for (int r = 0; r < 3; r++)
+        for (int k = 0; k < n; k++) {
+            for (int j = 0; j < L; j++) {
+                zq[j] = z[r][(size_t)j * n + k];
+                zr[j] = z[r][(size_t)(L + j) * n + k];
+            }
+            scale_r_to_q(c, zq, zr, o);
+            for (int j = 0; j < L; j++) out3[((size_t)r * L + j) * n + k] = o[j];
+        }
+    for (int p = 0; p < 4; p++) free(ext[p]);
+    for (int r = 0; r < 3; r++) free(z[r]);
+}
+
+int bfvo_mul_overq(const bfvo_ctx* c) { return c->overq; }
+
 void bfvo_mul_tensor(const bfvo_ctx* c, const u64* a, const u64* b, u64* out3) {
+    if (c->overq) {
+        mul_tensor_overq(c, a, b, out3);
+        return;
+    }
     int n = c->n, L = c->L, nB = c->nB, M = L + nB;
     /* basis Q u B: limb index 0..L-1 -> q[0..L-1]; L..L+nB-1 -> q[L+K ..] */
     int pidx[MAXP];

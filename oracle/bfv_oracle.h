@@ -77,6 +77,8 @@ void bfvo_add(const bfvo_ctx* c, const uint64_t* a, const uint64_t* b, uint64_t*
 void bfvo_mul_relin(bfvo_ctx* c, const uint64_t* a, const uint64_t* b, uint64_t* out);
 /* multiply without relinearisation: out is [3][L][N] */
 void bfvo_mul_tensor(const bfvo_ctx* c, const uint64_t* a, const uint64_t* b, uint64_t* out3);
+/* 1: the context multiplies over Q u R (2L limbs, E6-E8), 0: over Q u B (HPS, 2L+1) */
+int bfvo_mul_overq(const bfvo_ctx* c);
 void bfvo_rotate(bfvo_ctx* c, const uint64_t* a, int64_t k, uint64_t* out);
 /* plaintext multiply by a coefficient-form plaintext m (mod t) */
 void bfvo_mul_plain(const bfvo_ctx* c, const uint64_t* a, const uint64_t* m, uint64_t* out);

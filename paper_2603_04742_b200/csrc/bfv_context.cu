@@ -600,7 +600,7 @@ void GpuContext::add(const std::vector<const u64*>& a, const std::vector<const u
 void GpuContext::mul_relin_dev(const u64* const* A, const u64* const* B, u64* const* OUT,
                                int items, u64* T, u64* Z, u64* D2, u64* DX, u64* ACC,
                                const u64* const* RLK, const EncIn* enc, u64* D2Y, u64* const* YOUT) {
-    const int L = P_.cfg.L, K = P_.cfg.K, LK = L + K, M = L + P_.nB, logn = P_.cfg.logn;
+    const int L = P_.cfg.L, K = P_.cfg.K, LK = L + K, M = P_.mul_limbs(), logn = P_.cfg.logn;
     std::vector<int> pm;
     for (int j = 0; j < M; ++j) pm.push_back(j < L ? j : K + j);
     bool lazy_z = false;

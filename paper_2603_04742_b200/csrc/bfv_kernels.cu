@@ -519,31 +519,66 @@ __device__ __forceinline__ void extend_k(const ExtK<NX, NY>& e, const u64* x, u6
     }
 }
 
+// The over-Q multiply's input conversions (fixed shapes; E6-E8,
+// oracle mul_tensor_overq): a's Q limbs are copied and extended Q -> R (E1);
+// b is scaled to R, b''_k = sum_i y_i [floor(R/q_i)]_{r_k} + round(sum_i y_i
+// theta_i) (E6, y_i = [b_i (Q/q_i)^-1]_{q_i}, theta_i in 64-bit fixed point),
+// and b'' extended R -> Q (E1): the Q limbs of b's slot hold ext(b''), not b.
 template <int L>
 struct ExtendK {
     int n;
-    ExtK<L, L + 1> qb;
+    ExtK<L, L> qr;     // Q -> R (its x-side constants give y_i for E6 too)
+    ExtK<L, L> rq;     // R -> Q
+    u64 theta[L];      // floor(2^64 [R]_{q_i} / q_i)
+    W29 omega[L][L];   // [floor(R / q_i)]_{r_k}
 };
+
+template <int L>
+__device__ __forceinline__ void mul_extend_overq(const ExtendK<L>& c, bool is_b, const u64* x, u64* qo, u64* ro) {
+    if (!is_b) {
+#pragma unroll
+        for (int i = 0; i < L; ++i) qo[i] = x[i];
+        extend_k(c.qr, x, ro);
+        return;
+    }
+    u64 y[L];
+    u64 shi = 0, slo = 0;
+#pragma unroll
+    for (int i = 0; i < L; ++i) {
+        y[i] = shoup(x[i], c.qr.xhat_inv[i], c.qr.xhat_inv_sh[i], c.qr.xq[i]);
+        add128(shi, slo, umulhi(y[i], c.theta[i]), y[i] * c.theta[i]);
+    }
+    const u64 rnd = shi + (slo >> 63);  // < L 2^58: rides in both Dot29 column sums (x 1)
+#pragma unroll
+    for (int k = 0; k < L; ++k) {
+        Dot29 d;
+        d.a0 = d.am = rnd;
+#pragma unroll
+        for (int i = 0; i < L; ++i) dot29_mac(d, y[i], c.omega[i][k]);
+        ro[k] = dot29_reduce(d, c.qr.ym[k]);
+    }
+    extend_k(c.rq, ro, qo);
+}
 
 template <int L>
 __global__ void k_mul_extend_k(const __grid_constant__ ExtendK<L> c, const u64* const* A, const u64* const* B,
                                u64* T) {
-    constexpr int nB = L + 1, M = L + nB;
+    constexpr int M = 2 * L;
     const int n = c.n;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     const int item = blockIdx.y;
     const int p = blockIdx.z;
     const u64* src = (p < 2 ? A[item] : B[item]) + (size_t)(p & 1) * L * n;
     u64* dst = T + ((size_t)item * 4 + p) * M * n;
-    u64 x[L], o[nB];
+    u64 x[L], qo[L], ro[L];
+#pragma unroll
+    for (int i = 0; i < L; ++i) x[i] = src[(size_t)i * n + k];
+    mul_extend_overq(c, p >= 2, x, qo, ro);
 #pragma unroll
     for (int i = 0; i < L; ++i) {
-        x[i] = src[(size_t)i * n + k];
-        dst[(size_t)i * n + k] = x[i];
+        dst[(size_t)i * n + k] = qo[i];
+        dst[(size_t)(L + i) * n + k] = ro[i];
     }
-    extend_k(c.qb, x, o);
-#pragma unroll
-    for (int j = 0; j < nB; ++j) dst[(size_t)(L + j) * n + k] = o[j];
 }
 
 // The pipeline's encryption finish fused into the multiply's base
@@ -561,7 +596,7 @@ struct ExtendEncK {
 template <int L>
 __global__ void __launch_bounds__(128) k_mul_extend_enc(const __grid_constant__ ExtendEncK<L> c, const EncIn in,
                                                         u64* T) {
-    constexpr int nB = L + 1, M = L + nB;
+    constexpr int M = 2 * L;
     __shared__ u32 blk[16][16];
     const int n = c.x.n;
     const int item = blockIdx.y, p = blockIdx.z, poly = p & 1;
@@ -583,110 +618,140 @@ __global__ void __launch_bounds__(128) k_mul_extend_enc(const __grid_constant__ 
     const u64 m = poly ? 0 : in.MSG[(size_t)eitem * in.mstride + k];
     u64* ct = in.OUT[eitem] + (size_t)poly * L * n + k;
     u64* dst = T + ((size_t)item * 4 + p) * M * n + k;
-    u64 x[L], o[nB];
+    u64 x[L], qo[L], ro[L];
 #pragma unroll
     for (int i = 0; i < L; ++i) {
-        const u64 q = c.x.qb.xq[i];
+        const u64 q = c.x.qr.xq[i];
         u64 v = add_mod(cm[(size_t)i * n], lift_signed(e, q), q);
         if (!poly) v = add_mod(v, shoup(m, c.delta[i], c.delta_sh[i], q), q);
         x[i] = v;
         ct[(size_t)i * n] = v;
-        dst[(size_t)i * n] = v;
     }
-    extend_k(c.x.qb, x, o);
+    mul_extend_overq(c.x, p >= 2, x, qo, ro);
 #pragma unroll
-    for (int j = 0; j < nB; ++j) dst[(size_t)(L + j) * n] = o[j];
+    for (int i = 0; i < L; ++i) {
+        dst[(size_t)i * n] = qo[i];
+        dst[(size_t)(L + i) * n] = ro[i];
+    }
 }
 
+// E8, round(t z / R) mod q_j from z's Q u R residues (the over-Q multiply's
+// scale; oracle scale_r_to_q): y_k = [z_k (R/r_k)^-1]_{r_k},
+//   out_j = [t R^-1]_{q_j} z_j + sum_k y_k [-t R^-1 R/r_k]_{q_j} + round(sum_k t y_k / r_k)
+// as one Dot29 per q_j; the rounding term in E2's fixed point.
 template <int L>
 struct ScaleK {
     int n;
-    u64 q[L], QhatInv[L], QhatInv_sh[L], T1[L], T0[L];
-    Modulus bm[L + 1];
-    // w_j = rr - t [ (sum_i x_i [Q/q_i]_{b_j} - z_j) Q^-1 ]_{b_j}
-    //     = rr + sum_i x_i C_ij + z_j D_j  mod b_j  (one Dot29 per b_j)
-    W29 C[L][L + 1];  // [-[Q/q_i]_{b_j} Q^-1 t]_{b_j}
-    W29 D[L + 1];     // [Q^-1 t]_{b_j}
-    ExtK<L + 1, L> bq;
+    u64 r[L], RhatInv[L], RhatInv_sh[L], T1[L], T0[L];  // T = floor(t 2^128 / r_k)
+    Modulus qm[L];
+    W29 A[L];         // [t R^-1]_{q_j}
+    W29 C[L][L];      // [-t R^-1 R/r_k]_{q_j}
     u64 dhi[L], dhi_sh[L];  // ModUp factors [(Q_d / q_i)^-1]_{q_i} (KsY)
 };
 
-// E2 + E1 as k_mul_scale, constants from the parameter block
 template <int L>
 __global__ void k_mul_scale_k(const __grid_constant__ ScaleK<L> c, const u64* __restrict__ Z, u64* const* OUT,
                               u64* __restrict__ D2, u64* __restrict__ D2Y) {
-    constexpr int nB = L + 1, M = L + nB;
+    constexpr int M = 2 * L;
     const int n = c.n;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     const int item = blockIdx.y;
     const int r = blockIdx.z;
     const size_t P = (size_t)M * n;
     const u64* z = Z + ((size_t)item * 3 + r) * P;
-    u64 xi[L], w[nB], o[L];
+    u64 y[L], o[L];
     u64 shi = 0, slo = 0;
 #pragma unroll
-    for (int i = 0; i < L; ++i) {
-        xi[i] = shoup(z[(size_t)i * n + k], c.QhatInv[i], c.QhatInv_sh[i], c.q[i]);
-        add128(shi, slo, umulhi(xi[i], c.T1[i]), xi[i] * c.T1[i]);
-        add128(shi, slo, 0, umulhi(xi[i], c.T0[i]));
+    for (int kk = 0; kk < L; ++kk) {
+        y[kk] = shoup(z[(size_t)(L + kk) * n + k], c.RhatInv[kk], c.RhatInv_sh[kk], c.r[kk]);
+        add128(shi, slo, umulhi(y[kk], c.T1[kk]), y[kk] * c.T1[kk]);
+        add128(shi, slo, 0, umulhi(y[kk], c.T0[kk]));
     }
-    const u64 rr = shi + (slo >> 63);  // < L t + 1
+    const u64 rnd = shi + (slo >> 63);  // < L t + 1
 #pragma unroll
-    for (int j = 0; j < nB; ++j) {
+    for (int j = 0; j < L; ++j) {
         Dot29 d;
-        d.a0 = d.am = rr;  // rr * (1 in 29-bit halves): leaves the middle column sum alone
+        d.a0 = d.am = rnd;
+        u64 zq = z[(size_t)j * n + k];  // lazy (< 2q) when the inverse NTT left N^-1 to A
+        zq = zq >= c.qm[j].q ? zq - c.qm[j].q : zq;
+        dot29_mac(d, zq, c.A[j]);
 #pragma unroll
-        for (int i = 0; i < L; ++i) dot29_mac(d, xi[i], c.C[i][j]);
-        u64 zb = z[(size_t)(L + j) * n + k];  // lazy (< 2b) when the inverse NTT left N^-1 to D
-        zb = zb >= c.bm[j].q ? zb - c.bm[j].q : zb;
-        dot29_mac(d, zb, c.D[j]);
-        w[j] = dot29_reduce(d, c.bm[j]);
+        for (int kk = 0; kk < L; ++kk) dot29_mac(d, y[kk], c.C[kk][j]);
+        o[j] = dot29_reduce(d, c.qm[j]);
     }
-    extend_k(c.bq, w, o);
     u64* dst = r < 2 ? OUT[item] + (size_t)r * L * n : D2 + (size_t)item * L * n;
 #pragma unroll
     for (int i = 0; i < L; ++i) dst[(size_t)i * n + k] = o[i];
     if (r == 2 && D2Y) {  // the relinearisation's ModUp factors of c2
-        u64* y = D2Y + (size_t)item * L * n;
+        u64* yy = D2Y + (size_t)item * L * n;
 #pragma unroll
-        for (int i = 0; i < L; ++i) y[(size_t)i * n + k] = shoup(o[i], c.dhi[i], c.dhi_sh[i], c.q[i]);
+        for (int i = 0; i < L; ++i) yy[(size_t)i * n + k] = shoup(o[i], c.dhi[i], c.dhi_sh[i], c.qm[i].q);
     }
 }
 
+static u64 host_inv(u64 a, u64 q) { return inv_mod_host(a % q, q); }
+
 template <int L>
 static ExtendK<L> make_extend_k(const RnsParams& P) {
+    const DevConsts& h = P.host;
     ExtendK<L> c{};
     c.n = P.n;
-    fill_extk(c.qb, P.host, P.host.extQB);
+    fill_extk(c.qr, h, h.extQR);
+    fill_extk(c.rq, h, h.extRQ);
+    for (int i = 0; i < L; ++i) {
+        const u64 q = h.mod[i].q;
+        u64 Rq = 1;
+        for (int kk = 0; kk < L; ++kk) Rq = host_mulmod(Rq, h.mod[h.extQR.yi[kk]].q % q, q);
+        c.theta[i] = (u64)(((unsigned __int128)Rq << 64) / q);
+        for (int kk = 0; kk < L; ++kk) {  // floor(R/q_i) = (R - [R]_{q_i}) / q_i, R = 0 mod r_k
+            const u64 rk = h.mod[h.extQR.yi[kk]].q;
+            c.omega[i][kk] = split29(host_mulmod((rk - Rq % rk) % rk, host_inv(q, rk), rk));
+        }
+    }
     return c;
 }
 
 // lazy: Z is the inverse NTT without its final x N^-1 (NttJob::lazy_out); N^-1
-// rides in the constants that multiply z (Qhat_i^-1 for the Q limbs, D_j for
-// the B limbs), so x_i and w_j -- hence the output words -- are unchanged
+// rides in the constants that multiply z ((R/r_k)^-1 for the R limbs, A_j for
+// the Q limbs), so y_k and the output words are unchanged
 template <int L>
 static ScaleK<L> make_scale_k(const RnsParams& P, bool lazy = false) {
     const DevConsts& h = P.host;
+    const u64 t = P.cfg.t;
     ScaleK<L> c{};
     c.n = P.n;
-    for (int i = 0; i < L; ++i) {
-        c.q[i] = h.mod[i].q;
-        c.QhatInv[i] = lazy ? host_mulmod(h.QhatInv[i], h.ninv[i], c.q[i]) : h.QhatInv[i];
-        c.QhatInv_sh[i] = lazy ? shoup_factor(c.QhatInv[i], c.q[i]) : h.QhatInv_sh[i];
-        c.T1[i] = h.T1[i];
-        c.T0[i] = h.T0[i];
+    for (int kk = 0; kk < L; ++kk) {
+        const int ri = h.extRQ.xi[kk];
+        const u64 rk = h.mod[ri].q;
+        c.r[kk] = rk;
+        c.RhatInv[kk] = lazy ? host_mulmod(h.extRQ.xhat_inv[kk], h.ninv[ri], rk) : h.extRQ.xhat_inv[kk];
+        c.RhatInv_sh[kk] = shoup_factor(c.RhatInv[kk], rk);
+        // T = floor(t 2^128 / r_k) = t floor(2^128 / r_k) + floor(t [2^128]_{r_k} / r_k)
+        using u128 = unsigned __int128;
+        u128 Rf = (~(u128)0) / rk, rem = (~(u128)0) % rk + 1;
+        if (rem == rk) {
+            Rf += 1;
+            rem = 0;
+        }
+        const u128 T = Rf * t + rem * t / rk;
+        c.T1[kk] = (u64)(T >> 64);
+        c.T0[kk] = (u64)T;
     }
-    for (int j = 0; j <= L; ++j) {
-        const int bj = L + P.cfg.K + j;  // global prime index of b_j
-        c.bm[j] = h.mod[bj];
-        const u64 b = c.bm[j].q, D = host_mulmod(h.QinvB[j], h.tB[j], b);
-        c.D[j] = split29(lazy ? host_mulmod(D, h.ninv[bj], b) : D);
-        for (int i = 0; i < L; ++i) c.C[i][j] = split29((b - host_mulmod(h.QhatB[i][j], D, b)) % b);
-    }
-    fill_extk(c.bq, h, h.extBQ);
-    for (int i = 0; i < L; ++i) {
-        c.dhi[i] = h.dig_hat_inv[i];
-        c.dhi_sh[i] = h.dig_hat_inv_sh[i];
+    for (int j = 0; j < L; ++j) {
+        c.qm[j] = h.mod[j];
+        const u64 q = h.mod[j].q;
+        u64 Rq = 1;
+        for (int kk = 0; kk < L; ++kk) Rq = host_mulmod(Rq, c.r[kk] % q, q);
+        const u64 tRinv = host_mulmod(t % q, host_inv(Rq, q), q);
+        c.A[j] = split29(lazy ? host_mulmod(tRinv, h.ninv[j], q) : tRinv);
+        for (int kk = 0; kk < L; ++kk) {
+            u64 hk = 1;
+            for (int m = 0; m < L; ++m)
+                if (m != kk) hk = host_mulmod(hk, c.r[m] % q, q);
+            c.C[kk][j] = split29((q - host_mulmod(tRinv, hk, q)) % q);
+        }
+        c.dhi[j] = h.dig_hat_inv[j];
+        c.dhi_sh[j] = h.dig_hat_inv_sh[j];
     }
     return c;
 }
@@ -760,7 +825,8 @@ void launch_mul_extend(const DevConsts* dc, const RnsParams& P, const u64* const
 template <int LT, int KT, int AT>
 __global__ void k_mul_tensor(const DevConsts* __restrict__ dc, const u64* __restrict__ T,
                              u64* __restrict__ Z) {
-    const int n = dc->n, L = LT ? LT : dc->L, K = KT ? KT : dc->K, M = 2 * L + 1;
+    // fixed shapes multiply over Q u R (2L limbs), the others over Q u B (2L + 1)
+    const int n = dc->n, L = LT ? LT : dc->L, K = KT ? KT : dc->K, M = LT ? 2 * L : 2 * L + 1;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     const int item = blockIdx.y;
     const size_t P = (size_t)M * n;

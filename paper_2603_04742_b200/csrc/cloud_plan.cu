@@ -80,7 +80,7 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
         (int)out.size() != ns_)
         throw std::invalid_argument("plan: inconsistent sizes");
     const size_t ctw = ctx.ct_words();
-    const int L = P.cfg.L, LK = L + P.cfg.K, M = L + P.nB;
+    const int L = P.cfg.L, LK = L + P.cfg.K, M = P.mul_limbs();
 
     rows_.assign(ns_, 0);
     for (int i = 0; i < n; ++i)
@@ -372,7 +372,7 @@ std::vector<PhaseTiming> CloudPlan::profile() {
     std::vector<PhaseTiming> out;
     if (n_ == 0) return out;
     const RnsParams& P = ctx_.params();
-    const int L = P.cfg.L, LK = L + P.cfg.K, M = L + P.nB;
+    const int L = P.cfg.L, LK = L + P.cfg.K, M = P.mul_limbs();
     const u64 C = sizeof(u64) * ctx_.ct_words(), KEY = sizeof(u64) * ctx_.ksk_words(),
               PT = sizeof(u64) * ctx_.poly_words();
     const u64 ks_ntts = (u64)P.dnum * LK + 2 * LK;

@@ -31,7 +31,7 @@ constexpr int kMulGroups = 2, kGroupThreads = 128;
 template <int LOGN, int LT, int KT>
 __global__ void __launch_bounds__(kMulGroups * kGroupThreads) k_mul_blocks_tensor(const DevConsts* __restrict__ dc,
                                                                                   const u64* __restrict__ T,
-                                                                                  u64* __restrict__ Z) {
+                                                                                  u64* __restrict__ Z, int M) {
     using G = Ntt2<LOGN>;
     extern __shared__ u64 smem[];
     constexpr int PITCH = G::PITCH;
@@ -41,7 +41,7 @@ __global__ void __launch_bounds__(kMulGroups * kGroupThreads) k_mul_blocks_tenso
     static_assert(PER >= 1, "tile smaller than the CTA");
     u64* tile = smem;            // 4 tiles: a0 a1 b0 b1, then z0 z1 z2 in the first three
     u64* tws = smem + 4 * TW;
-    const int L = LT ? LT : dc->L, K = KT ? KT : dc->K, M = 2 * L + 1;
+    const int L = LT ? LT : dc->L, K = KT ? KT : dc->K;  // M: 2L over Q u R, 2L + 1 over Q u B
     int bid = blockIdx.x;
     const int tileid = bid % G::CTAS_B;
     bid /= G::CTAS_B;
@@ -499,10 +499,10 @@ void launch_blocks_mul_inv(const DevConsts* dc, const RnsParams& P, const u64* I
 template <int LOGN, int LT, int KT>
 static void mulb_t(const DevConsts* dc, const RnsParams& P, const u64* T, u64* Z, int items, cudaStream_t st) {
     using G = Ntt2<LOGN>;
-    const int M = P.cfg.L + P.nB;
+    const int M = P.mul_limbs();
     const int smem = (4 * G::LINES * G::PITCH + 2 * G::TWB) * 8;
     smem_optin_k(k_mul_blocks_tensor<LOGN, LT, KT>, smem);
-    k_mul_blocks_tensor<LOGN, LT, KT><<<items * M * G::CTAS_B, kMulGroups * kGroupThreads, smem, st>>>(dc, T, Z);
+    k_mul_blocks_tensor<LOGN, LT, KT><<<items * M * G::CTAS_B, kMulGroups * kGroupThreads, smem, st>>>(dc, T, Z, M);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) throw std::runtime_error(std::string("mul blocks launch: ") + cudaGetErrorString(e));
 }

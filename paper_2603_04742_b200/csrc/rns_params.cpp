@@ -219,6 +219,13 @@ RnsParams::RnsParams(const RnsConfig& c) : cfg(c), host{} {
     for (int j = 0; j < nB; ++j) bi[j] = L + K + j;
     fill_ext(d.extQB, Q, qi, B, bi);
     fill_ext(d.extBQ, B, bi, Q, qi);
+    overq = (L == 2 && K == 2 && c.alpha == 2) || (L == 4 && K == 4 && c.alpha == 4);
+    {
+        std::vector<u64> R(B.begin(), B.begin() + L);
+        std::vector<int> ri(bi.begin(), bi.begin() + L);
+        fill_ext(d.extQR, Q, qi, R, ri);
+        fill_ext(d.extRQ, R, ri, Q, qi);
+    }
 
     const u64 t = c.t;
     for (int i = 0; i < L; ++i) {

@@ -66,6 +66,7 @@ struct DevConsts {
     TwiddlePtrs tw[MAXP];
     u64 ninv[MAXP], ninv_sh[MAXP];
     ExtConsts extQB, extBQ;
+    ExtConsts extQR, extRQ;  // over-Q multiply: R = b_0 .. b_{L-1} (E1 both ways)
     // t/Q scale-and-round (E2 / E5)
     u64 QhatInv[MAXL], QhatInv_sh[MAXL];
     u64 T1[MAXL], T0[MAXL];
@@ -91,6 +92,12 @@ struct RnsParams {
     std::vector<std::vector<u64>> tw_fwd, tw_inv;  // interleaved (w, wsh)
     std::vector<u32> pos0;
     DevConsts host;  // filled except device pointers
+
+    // The multiply runs over Q u R (R = the first L primes of B; E6-E8,
+    // 2L limbs) for the shapes with specialised kernels, over Q u B (HPS,
+    // 2L + 1 limbs) otherwise; oracle/bfv_oracle.c applies the same rule.
+    bool overq = false;
+    int mul_limbs() const { return overq ? 2 * cfg.L : cfg.L + nB; }
 
     explicit RnsParams(const RnsConfig& c);
     int q_index(int j) const { return j; }

@@ -55,6 +55,8 @@ def oracle_lib():
         L.bfvo_chacha_word.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64]
         L.bfvo_add_galois_key.argtypes = [C.c_void_p, C.c_uint32]
         L.bfvo_galois_elt.restype = C.c_uint32
+        L.bfvo_mul_overq.restype = C.c_int
+        L.bfvo_mul_overq.argtypes = [C.c_void_p]
         L.bfvo_galois_elt.argtypes = [C.c_void_p, C.c_int64]
         L.bfvo_get_sk.argtypes = [C.c_void_p, i64p]
         L.bfvo_get_pk.argtypes = [C.c_void_p, u64p]

@@ -12,8 +12,9 @@ import synth
 T = 65537
 
 
-@pytest.fixture(scope="module", params=[(5, 3, 1, 1, 54), (6, 4, 2, 2, 58), (4, 8, 4, 4, 58)],
-                ids=["n32_L3", "n64_L4", "n16_L8"])
+@pytest.fixture(scope="module", params=[(5, 3, 1, 1, 54), (6, 4, 2, 2, 58), (4, 8, 4, 4, 58), (6, 2, 2, 2, 58),
+                                        (5, 4, 4, 4, 58)],
+                ids=["n32_L3", "n64_L4", "n16_L8", "n64_L2_overq", "n32_L4_overq"])
 def orc(request):
     logn, L, K, a, qb = request.param
     return BfvOracle(logn, L, K, a, qb, qb, T, 1234)
@@ -133,3 +134,26 @@ def test_bfv_protocol_decrypts_to_reference():
             s = int(slots[p])
             vals[int(pc["row_map"][p])] = s - T if s > T // 2 else s
         assert np.array_equal(vals, want["values"])
+
+
+def test_multiply_method_follows_the_shape():
+    """The shapes with specialised GPU kernels multiply over Q u R (E6-E8),
+    every other shape over Q u B (HPS)."""
+    lib = oracle_lib()
+    for (L, K, a), want in (((2, 2, 2), 1), ((4, 4, 4), 1), ((3, 1, 1), 0), ((4, 2, 2), 0), ((2, 2, 1), 0)):
+        o = BfvOracle(5, L, K, a, 58, 58, T, 7)
+        assert lib.bfvo_mul_overq(o.h) == want
+
+
+@pytest.mark.parametrize("logn,L", [(13, 2), (14, 2), (15, 4)])
+def test_overq_multiply_noise_at_full_size(logn, L):
+    """At the default parameters the over-Q product decrypts exactly with a
+    wide noise margin (a rotation and a mask still to come)."""
+    orc = BfvOracle(logn, L, L, L, 58, 58, T, 99)
+    rng = np.random.default_rng(logn)
+    S = orc.n // 2
+    a, b = rng.integers(-8, 9, S), rng.integers(-8, 9, S)
+    cp = orc.mul_relin(orc.encrypt(a, 1), orc.encrypt(b, 2))
+    vals, budget = orc.decrypt(cp)
+    assert np.array_equal(vals.astype(np.int64), np.mod(a * b, T))
+    assert budget >= 40
