@@ -208,7 +208,8 @@ void GpuContext::keygen() {
 DevBuf GpuContext::gen_ksk(u64 keyid, const u64* sp_ntt) {
     const int n = P_.n, L = P_.cfg.L, LK = L + P_.cfg.K, logn = P_.cfg.logn;
     const SeedKey seed = P_.cfg.key;
-    DevBuf key(&pool_, sizeof(u64) * ksk_words());
+    // [dnum][2][L+K][N] key words, then their Shoup companions (the fused MAC)
+    DevBuf key(&pool_, sizeof(u64) * 2 * ksk_words());
     DevBuf e_small(&pool_, sizeof(int64_t) * n), E(&pool_, sizeof(u64) * (size_t)LK * n);
     for (int d = 0; d < P_.dnum; ++d) {
         u64* k0 = key.words() + ((size_t)d * 2 + 0) * LK * n;
@@ -221,6 +222,7 @@ DevBuf GpuContext::gen_ksk(u64 keyid, const u64* sp_ntt) {
         const int lo = d * P_.cfg.alpha, hi = std::min(lo + P_.cfg.alpha, L);
         launch_key_combine(dc_, logn, LK, k1, E.words(), s_ntt_.words(), sp_ntt, lo, hi, k0, st_);
     }
+    launch_shoup_companions(dc_, key.words(), key.words() + ksk_words(), LK, n, 2 * P_.dnum, st_);
     return key;
 }
 

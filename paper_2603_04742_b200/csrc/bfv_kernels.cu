@@ -2086,6 +2086,31 @@ __global__ void k_key_combine(const DevConsts* __restrict__ dc, const u64* A, co
     out[o] = v;
 }
 
+// floor(w 2^64 / q) by restoring division (key generation only)
+__global__ void k_shoup_companions(const DevConsts* __restrict__ dc, const u64* W, u64* WS, int LK, int n,
+                                   size_t count) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const u64 q = dc->mod[(int)((i / n) % LK)].q;
+    u64 r = W[i], quo = 0;  // r < q < 2^62: r << 1 never overflows
+    for (int b = 0; b < 64; ++b) {
+        r <<= 1;
+        quo <<= 1;
+        if (r >= q) {
+            r -= q;
+            quo |= 1;
+        }
+    }
+    WS[i] = quo;
+}
+
+void launch_shoup_companions(const DevConsts* dc, const u64* W, u64* WS, int LK, int n, int polys,
+                             cudaStream_t st) {
+    const size_t count = (size_t)polys * LK * n;
+    k_shoup_companions<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(dc, W, WS, LK, n, count);
+    CSSC_CHECK_LAUNCH();
+}
+
 void launch_key_combine(const DevConsts* dc, int logn, int limbs, const u64* A, const u64* E,
                         const u64* S, const u64* SP, int digit_lo, int digit_hi, u64* out,
                         cudaStream_t st) {

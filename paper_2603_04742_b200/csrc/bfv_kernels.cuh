@@ -204,6 +204,9 @@ void launch_lift_small(const DevConsts* dc, int logn, const int64_t* s, int limb
                        u64* out, cudaStream_t st);
 void launch_automorph_small(int logn, u32 g, const int64_t* in, int64_t* out, cudaStream_t st);
 // out = -(A*S + E) [+ P_q * SP on the digit's limbs]; all NTT form over limbs [0, limbs)
+// Shoup companions floor(w 2^64 / q_j) of `polys` polynomials over the L+K key primes
+void launch_shoup_companions(const DevConsts* dc, const u64* W, u64* WS, int LK, int n, int polys,
+                             cudaStream_t st);
 void launch_key_combine(const DevConsts* dc, int logn, int limbs, const u64* A, const u64* E,
                         const u64* S, const u64* SP, int digit_lo, int digit_hi, u64* out,
                         cudaStream_t st);

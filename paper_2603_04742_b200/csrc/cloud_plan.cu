@@ -170,7 +170,8 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
     }
 
     const bool fused = ctx.fused_key_switch();
-    const u64 C = sizeof(u64) * ctw, KEY = sizeof(u64) * ctx.ksk_words(),
+    // the fused MAC also streams the key's Shoup companions
+    const u64 C = sizeof(u64) * ctw, KEY = sizeof(u64) * ctx.ksk_words() * (fused ? 2 : 1),
               PT = sizeof(u64) * ctx.poly_words();
     stats_.chunks = n;
     stats_.slices = ns_;
@@ -373,7 +374,8 @@ std::vector<PhaseTiming> CloudPlan::profile() {
     if (n_ == 0) return out;
     const RnsParams& P = ctx_.params();
     const int L = P.cfg.L, LK = L + P.cfg.K, M = P.mul_limbs();
-    const u64 C = sizeof(u64) * ctx_.ct_words(), KEY = sizeof(u64) * ctx_.ksk_words(),
+    const u64 C = sizeof(u64) * ctx_.ct_words(),
+              KEY = sizeof(u64) * ctx_.ksk_words() * (ctx_.fused_key_switch() ? 2 : 1),
               PT = sizeof(u64) * ctx_.poly_words();
     const u64 ks_ntts = (u64)P.dnum * LK + 2 * LK;
     out.push_back({"multiply+relin", 0, (u64)n_, (u64)n_ * 3 * C + KEY, (u64)n_ * (7 * M + ks_ntts)});

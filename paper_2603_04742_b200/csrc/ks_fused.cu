@@ -290,6 +290,7 @@ __global__ void __launch_bounds__(kKsGroups * kKsGroupThreads) k_ks_blocks_inner
     const size_t base = (size_t)blk0 * G::R2;
     const u64* key = KEY[item];
     const size_t PL = (size_t)LK * G::N;
+    const size_t KW = (size_t)dnum * 2 * PL;  // key words; their Shoup companions follow
     const int grp = threadIdx.x / kKsGroupThreads;
     const ThreadGroup tg = cta_slice(grp, kKsGroups);
     // element x = threadIdx.x + T r of the tile (line x >> B, column x & (R2-1)):
@@ -333,15 +334,19 @@ __global__ void __launch_bounds__(kKsGroups * kKsGroupThreads) k_ks_blocks_inner
         for (int dg = 0; dg < dnum; ++dg) {
             const u64 w = work[dg * TW + s0];
             u64 k0, k1;
+            const size_t ko = ((size_t)dg * 2) * PL + (size_t)j * G::N + base + x;
             if (KTMA) {
                 k0 = keys[(size_t)(dg * 2) * KT_W + x];
                 k1 = keys[(size_t)(dg * 2 + 1) * KT_W + x];
             } else {
-                k0 = __ldg(key + ((size_t)dg * 2 + 0) * PL + (size_t)j * G::N + base + x);
-                k1 = __ldg(key + ((size_t)dg * 2 + 1) * PL + (size_t)j * G::N + base + x);
+                k0 = __ldg(key + ko);
+                k1 = __ldg(key + ko + PL);
             }
-            a0 = add_mod(a0, mul_mod(w, k0, md), q);
-            a1 = add_mod(a1, mul_mod(w, k1, md), q);
+            // the key's Shoup companions (stored after the key words, KW apart):
+            // a constant-operand product instead of a Barrett reduction
+            const u64 s0 = __ldg(key + KW + ko), s1 = __ldg(key + KW + ko + PL);
+            a0 = add_mod(a0, shoup(w, k0, s0, q), q);
+            a1 = add_mod(a1, shoup(w, k1, s1, q), q);
         }
         work[s0] = a0;
         work[TW + s0] = a1;

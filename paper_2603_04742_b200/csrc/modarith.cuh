@@ -119,6 +119,15 @@ CSSC_HD void dot29_mac_small(Dot29& d, u32 y, const W29& w) {
     d.a0 += (u64)y * w.lo;
     d.am += (u64)y * w.sum;
 }
+// a variable product a * b (both canonical, < 2^58) into the same column sums:
+// three IMAD.WIDE.U32 instead of the 64 x 64 -> 128 product of mul_mod
+CSSC_HD void dot29_mac_var(Dot29& d, u64 a, u64 b) {
+    const u32 a0 = (u32)a & kMask29, a1 = (u32)(a >> 29);
+    const u32 b0 = (u32)b & kMask29, b1 = (u32)(b >> 29);
+    d.a0 += (u64)a0 * b0;
+    d.ah += (u64)a1 * b1;
+    d.am += (u64)(a0 + a1) * (b0 + b1);
+}
 CSSC_HD u64 dot29_reduce(const Dot29& d, const Modulus& m) {
     const u64 mid = d.am - d.a0 - d.ah;
     const u64 t = mid << 29, u = d.ah << 58;

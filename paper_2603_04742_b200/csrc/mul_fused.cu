@@ -80,14 +80,16 @@ __global__ void __launch_bounds__(kMulGroups * kGroupThreads) k_mul_blocks_tenso
         const int s0 = saddr(threadIdx.x + NT * r);
         const u64 a0 = reduce_small_quot(tile[s0], md), a1 = reduce_small_quot(tile[TW + s0], md);
         const u64 b0 = reduce_small_quot(tile[2 * TW + s0], md), b1 = reduce_small_quot(tile[3 * TW + s0], md);
-        tile[s0] = mul_mod(a0, b0, md);
-        u64 hi = umulhi(a0, b1), lo = a0 * b1;
-        const u64 lo2 = a1 * b0;
-        hi += umulhi(a1, b0);
-        lo += lo2;
-        hi += lo < lo2;
-        tile[TW + s0] = barrett(hi, lo, md);
-        tile[2 * TW + s0] = mul_mod(a1, b1, md);
+        // products as 29-bit Karatsuba column sums (three IMAD.WIDE.U32 each),
+        // one Barrett reduction per output: the canonical words of mul_mod
+        Dot29 d0, d1, d2;
+        dot29_mac_var(d0, a0, b0);
+        dot29_mac_var(d1, a0, b1);
+        dot29_mac_var(d1, a1, b0);
+        dot29_mac_var(d2, a1, b1);
+        tile[s0] = dot29_reduce(d0, md);
+        tile[TW + s0] = dot29_reduce(d1, md);
+        tile[2 * TW + s0] = dot29_reduce(d2, md);
     }
     __syncthreads();
     load_block_twiddles<LOGN>(tws, dc->tw[prime].inv, blk0);
