@@ -18,9 +18,13 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
-BUILD = PKG / "build"
+# CSSC_BUILD_TAG / CSSC_NVCC_DEFINES: a variant build (A/B experiments) into
+# build_<tag>/ and lib/libcssc_he_<tag>.so, loaded with CSSC_LIB
+_TAG = os.environ.get("CSSC_BUILD_TAG", "")
+_DEFS = os.environ.get("CSSC_NVCC_DEFINES", "").split()
+BUILD = PKG / ("build_" + _TAG if _TAG else "build")
 LIBDIR = PKG / "lib"
-LIB = LIBDIR / "libcssc_he.so"
+LIB = LIBDIR / ("libcssc_he_" + _TAG + ".so" if _TAG else "libcssc_he.so")
 CUDA_HOME = Path(os.environ.get("CUDA_HOME", "/usr/local/cuda"))
 NVCC = str(CUDA_HOME / "bin" / "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -48,7 +52,7 @@ def _cmd(src: Path) -> list[str]:
     out = str(_obj(src))
     if src.suffix == ".cu":
         return [NVCC, "-std=c++20", "-O3", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC",
-                "--expt-relaxed-constexpr", *INCLUDES, "-c", str(src), "-o", out]
+                "--expt-relaxed-constexpr", *_DEFS, *INCLUDES, "-c", str(src), "-o", out]
     return ["g++", "-std=c++20", "-O3", "-fPIC", "-Wall", "-Wextra", "-Wno-unused-parameter",
             *INCLUDES, "-c", str(src), "-o", out]
 

@@ -28,6 +28,32 @@ CSSC_HD u64 umulhi(u64 a, u64 b) {
 #endif
 }
 
+// 64-bit add / a - b + c through explicit 32-bit carry chains (PTX add.cc /
+// addc): keeps the high halves on the ALU pipe (IADD3.X) where ptxas would
+// otherwise pick IMAD.X, which competes with the products for the FMA pipe
+CSSC_HD u64 add64(u64 a, u64 b) {
+#ifdef __CUDA_ARCH__
+    unsigned lo, hi;
+    asm("add.cc.u32 %0, %2, %3;\n\taddc.u32 %1, %4, %5;"
+        : "=r"(lo), "=r"(hi)
+        : "r"((unsigned)a), "r"((unsigned)b), "r"((unsigned)(a >> 32)), "r"((unsigned)(b >> 32)));
+    return ((u64)hi << 32) | lo;
+#else
+    return a + b;
+#endif
+}
+CSSC_HD u64 sub_add64(u64 a, u64 b, u64 c) {  // a - b + c
+#ifdef __CUDA_ARCH__
+    unsigned lo, hi;
+    asm("sub.cc.u32 %0, %2, %3;\n\tsubc.u32 %1, %4, %5;"
+        : "=r"(lo), "=r"(hi)
+        : "r"((unsigned)a), "r"((unsigned)b), "r"((unsigned)(a >> 32)), "r"((unsigned)(b >> 32)));
+    return add64(((u64)hi << 32) | lo, c);
+#else
+    return a - b + c;
+#endif
+}
+
 CSSC_HD u64 add_mod(u64 a, u64 b, u64 q) {
     u64 s = a + b;
     return s >= q ? s - q : s;
@@ -36,9 +62,50 @@ CSSC_HD u64 sub_mod(u64 a, u64 b, u64 q) { return a >= b ? a - b : a + q - b; }
 CSSC_HD u64 neg_mod(u64 a, u64 q) { return a ? q - a : 0; }
 
 // a * w mod q in [0, 2q) for any a < 2^64, w < q, wsh = floor(w * 2^64 / q)
+// -q mod 2^64, opaque to the optimiser: a*w + qh*(-q) then compiles to
+// multiply-adds (IMAD.WIDE.U32 with a 64-bit addend) instead of a negated
+// product and a separate 64-bit subtraction (two IMAD.X on the FMA pipe)
+CSSC_HD u64 neg_opaque(u64 q) {
+    u64 nq = 0 - q;
+#ifdef __CUDA_ARCH__
+    asm("" : "+l"(nq));
+#endif
+    return nq;
+}
+#ifndef CSSC_SHOUP_VARIANT
+#define CSSC_SHOUP_VARIANT 2
+#endif
 CSSC_HD u64 shoup_lazy(u64 a, u64 w, u64 wsh, u64 q) {
-    u64 qh = umulhi(a, wsh);
+    const u64 qh = umulhi(a, wsh);
+#if CSSC_SHOUP_VARIANT == 0
     return a * w - qh * q;
+#elif CSSC_SHOUP_VARIANT == 1
+    return a * w + qh * neg_opaque(q);
+#elif defined(__CUDA_ARCH__)
+    // low 64 bits of a*w + qh*(-q) as explicit 32-bit multiply-add chains:
+    // two IMAD.WIDE.U32 (the second taking the first as its 64-bit addend)
+    // and four IMAD into the high word, no separate 64-bit adds
+    const u64 nq = 0 - q;
+    u64 r;
+    asm("{\n\t.reg .u32 a0, a1, w0, w1, h0, h1, n0, n1, th;\n\t.reg .u64 t;\n\t"
+        "mov.b64 {a0, a1}, %1;\n\tmov.b64 {w0, w1}, %2;\n\t"
+        "mov.b64 {h0, h1}, %3;\n\tmov.b64 {n0, n1}, %4;\n\t"
+        "mul.wide.u32 t, a0, w0;\n\t"
+        "mov.b64 {w0, th}, t;\n\t"
+        "mad.lo.u32 th, a0, w1, th;\n\t"
+        "mad.lo.u32 th, a1, %5, th;\n\t"
+        "mov.b64 t, {w0, th};\n\t"
+        "mad.wide.u32 %0, h0, n0, t;\n\t"
+        "mov.b64 {w0, th}, %0;\n\t"
+        "mad.lo.u32 th, h0, n1, th;\n\t"
+        "mad.lo.u32 th, h1, n0, th;\n\t"
+        "mov.b64 %0, {w0, th};\n\t}"
+        : "=l"(r)
+        : "l"(a), "l"(w), "l"(qh), "l"(nq), "r"((unsigned)w));
+    return r;
+#else
+    return a * w - qh * q;
+#endif
 }
 CSSC_HD u64 shoup(u64 a, u64 w, u64 wsh, u64 q) {
     u64 r = shoup_lazy(a, w, wsh, q);

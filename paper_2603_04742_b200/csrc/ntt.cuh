@@ -26,6 +26,17 @@
 
 namespace cssc {
 
+#ifndef CSSC_PTX_ADD
+#define CSSC_PTX_ADD 1
+#endif
+#if CSSC_PTX_ADD
+#define NTT_ADD(a, b) add64(a, b)
+#define NTT_SUBADD(a, b, c) sub_add64(a, b, c)
+#else
+#define NTT_ADD(a, b) ((a) + (b))
+#define NTT_SUBADD(a, b, c) ((a) - (b) + (c))
+#endif
+
 template <int LOGN>
 struct Ntt2 {
     // block phase: 6 stages (7 at 2^15) so its twiddles fit next to the tile
@@ -177,8 +188,8 @@ __device__ __forceinline__ void line_pass(u64* s, QF qf, Addr addr, Tw tw, const
                     const ulonglong2 w = tw(S0L + u, l, (blk << u) + (k >> (R - u)));
                     const u64 x = v[k];
                     const u64 y = shoup_lazy(v[k + h], w.x, w.y, q);
-                    v[k] = x + y;
-                    v[k + h] = x - y + two_q;
+                    v[k] = NTT_ADD(x, y);
+                    v[k + h] = NTT_SUBADD(x, y, two_q);
                 }
             }
         } else {
@@ -190,10 +201,10 @@ __device__ __forceinline__ void line_pass(u64* s, QF qf, Addr addr, Tw tw, const
                     if (k & h) continue;
                     const ulonglong2 w = tw(S0L + u, l, (blk << u) + (k >> (R - u)));
                     const u64 x = v[k], y = v[k + h];
-                    u64 sm = x + y;
+                    u64 sm = NTT_ADD(x, y);
                     sm = sm >= two_q ? sm - two_q : sm;
                     v[k] = sm;
-                    v[k + h] = shoup_lazy(x - y + two_q, w.x, w.y, q);
+                    v[k + h] = shoup_lazy(NTT_SUBADD(x, y, two_q), w.x, w.y, q);
                 }
             }
         }
