@@ -43,7 +43,7 @@ __device__ __forceinline__ u32 rotl32(u32 v, int n) { return __funnelshift_l(v, 
     a += b; d ^= a; d = rotl32(d, 8);               \
     c += d; b ^= c; b = rotl32(b, 7);
 
-__device__ void chacha20_block(const SeedKey& seed, u32 ctr, u32 n0, u32 n1, u32 n2, u32 out[16]) {
+__device__ __forceinline__ void chacha20_block(const SeedKey& seed, u32 ctr, u32 n0, u32 n1, u32 n2, u32 out[16]) {
     const u32 s[16] = {0x61707865u, 0x3320646eu, 0x79622d32u, 0x6b206574u,
                        seed.w[0],   seed.w[1],   seed.w[2],   seed.w[3],
                        seed.w[4],   seed.w[5],   seed.w[6],   seed.w[7],
@@ -1667,30 +1667,33 @@ void launch_plain_lift(const DevConsts* dc, const RnsParams& P, const u64* M, u6
     CSSC_CHECK_LAUNCH();
 }
 
-// U[item][L][N]: a 128-thread CTA draws 32 ChaCha blocks (4 lanes each) =
-// 256 coefficients of u into smem, then writes them coalesced per limb
+// U[item][L][N]: one ChaCha block per thread (8 coefficients of u, the block
+// counter = k / 8 as everywhere), all in registers -- no shuffles, no idle
+// lanes; each thread writes its 8 words per limb as four 16-byte stores
 __global__ void __launch_bounds__(128) k_enc_sample_u(const DevConsts* __restrict__ dc, SeedKey seed,
                                                       const u64* streams, u64* U) {
-    __shared__ u32 blk[32][16];
     const int n = dc->n, L = dc->L;
     const int item = blockIdx.y;
     const u64 id = streams[item];
-    const int g = threadIdx.x >> 2;
-    chacha20_block_x4(seed, (u32)(blockIdx.x * 32 + g), DOM_ENC_U, (u32)id, (u32)(id >> 32), blk[g]);
-    __syncthreads();
+    const int b = blockIdx.x * 128 + threadIdx.x;  // ChaCha block = coefficients 8b .. 8b+7
+    if (8 * b >= n) return;
+    u32 blk[16];
+    chacha20_block(seed, (u32)b, DOM_ENC_U, (u32)id, (u32)(id >> 32), blk);
+    int64_t u[8];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        const int kk = threadIdx.x + 128 * h;
-        const int k = blockIdx.x * 256 + kk;
-        const int64_t u = ternary_of(word64(blk[kk >> 3], kk & 7));
-        for (int j = 0; j < L; ++j) U[((size_t)item * L + j) * n + k] = lift_signed(u, dc->mod[j].q);
+    for (int w = 0; w < 8; ++w) u[w] = ternary_of(word64(blk, w));
+    for (int j = 0; j < L; ++j) {
+        const u64 q = dc->mod[j].q;
+        ulonglong2* dst = reinterpret_cast<ulonglong2*>(U + ((size_t)item * L + j) * n + 8 * (size_t)b);
+#pragma unroll
+        for (int w = 0; w < 4; ++w) dst[w] = make_ulonglong2(lift_signed(u[2 * w], q), lift_signed(u[2 * w + 1], q));
     }
 }
 
 void launch_enc_sample_u(const DevConsts* dc, const RnsParams& P, SeedKey seed, const u64* streams,
                          u64* U, int items, cudaStream_t st) {
     if (!items) return;
-    k_enc_sample_u<<<dim3((unsigned)(P.n / 256), (unsigned)items), 128, 0, st>>>(dc, seed, streams, U);
+    k_enc_sample_u<<<dim3((unsigned)((P.n / 8 + 127) / 128), (unsigned)items), 128, 0, st>>>(dc, seed, streams, U);
     CSSC_CHECK_LAUNCH();
 }
 
@@ -1757,26 +1760,28 @@ __global__ void __launch_bounds__(128) k_enc_finish(const DevConsts* __restrict_
     }
 }
 
-// the e draws of k_enc_finish / k_mul_extend_enc, ahead of time: one CTA per
-// 128 coefficients of one polynomial of one item
+// the e draws of k_enc_finish / k_mul_extend_enc, ahead of time: one ChaCha
+// block per thread (8 coefficients, block counter = k / 8), in registers, one
+// 8-byte store of the 8 int8 draws
 __global__ void __launch_bounds__(128) k_enc_sample_e(SeedKey seed, const u64* streams, int8_t* E, int n) {
-    __shared__ u32 blk[16][16];
     const int item = blockIdx.y, poly = blockIdx.z;
     const u64 id = streams[item];
-    const int g = threadIdx.x >> 2;
-    if (g < 16)
-        chacha20_block_x4(seed, (u32)(blockIdx.x * 16 + g), poly ? DOM_ENC_E1 : DOM_ENC_E0, (u32)id, (u32)(id >> 32),
-                          blk[g]);
-    __syncthreads();
-    const int kk = threadIdx.x, k = blockIdx.x * 128 + kk;
-    E[((size_t)item * 2 + poly) * n + k] = (int8_t)cbd_of(word64(blk[kk >> 3], kk & 7));
+    const int b = blockIdx.x * 128 + threadIdx.x;
+    if (8 * b >= n) return;
+    u32 blk[16];
+    chacha20_block(seed, (u32)b, poly ? DOM_ENC_E1 : DOM_ENC_E0, (u32)id, (u32)(id >> 32), blk);
+    u64 packed = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) packed |= (u64)(uint8_t)(int8_t)cbd_of(word64(blk, w)) << (8 * w);
+    *reinterpret_cast<u64*>(E + ((size_t)item * 2 + poly) * n + 8 * (size_t)b) = packed;
 }
 
 void launch_enc_sample_e(const DevConsts* dc, const RnsParams& P, SeedKey seed, const u64* streams, int8_t* E,
                          int items, cudaStream_t st) {
     (void)dc;
     if (!items) return;
-    k_enc_sample_e<<<dim3((unsigned)(P.n / 128), (unsigned)items, 2), 128, 0, st>>>(seed, streams, E, P.n);
+    k_enc_sample_e<<<dim3((unsigned)((P.n / 8 + 127) / 128), (unsigned)items, 2), 128, 0, st>>>(seed, streams, E,
+                                                                                                 P.n);
     CSSC_CHECK_LAUNCH();
 }
 
