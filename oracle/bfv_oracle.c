@@ -742,11 +742,16 @@ void bfvo_mul_plain(const bfvo_ctx* c, const u64* a, const u64* m, u64* out) {
 }
 
 /* hybrid key switch of d (coef form over Q) with key (NTT form) */
-static void key_switch(const bfvo_ctx* c, const u64* key, const u64* d, u64* ks0, u64* ks1) {
+/* Hybrid key switch of d (E3/E4).  A rotation passes its Galois element g
+ * and the UN-rotated c1: ModUp runs on d and the automorphism is applied to
+ * every ModUp'd limb afterwards, phi_g(ModUp(d)), so rotations
+ * of one source by several g share one ModUp (and its NTT) word for word. */
+static void key_switch_g(const bfvo_ctx* c, const u64* key, const u64* d, uint32_t g, u64* ks0, u64* ks1) {
     int n = c->n, L = c->L, K = c->K, LK = L + K;
     u64* acc0 = (u64*)calloc((size_t)LK * n, sizeof(u64));
     u64* acc1 = (u64*)calloc((size_t)LK * n, sizeof(u64));
     u64* D = (u64*)malloc(sizeof(u64) * n);
+    u64* Dg = (u64*)malloc(sizeof(u64) * n);
     for (int dg = 0; dg < c->dnum; dg++) {
         int lo = dg * c->alpha, hi = lo + c->alpha < L ? lo + c->alpha : L;
         for (int j = 0; j < LK; j++) {
@@ -762,6 +767,10 @@ static void key_switch(const bfvo_ctx* c, const u64* key, const u64* d, u64* ks0
                     }
                     D[k] = acc;
                 }
+            }
+            if (g != 1) {
+                automorph_limb(n, mj, g, D, Dg);
+                memcpy(D, Dg, sizeof(u64) * n);
             }
             bfvo_ntt(c, j, D);
             const u64* k0 = key + (((size_t)dg * 2 + 0) * LK + j) * n;
@@ -791,7 +800,11 @@ static void key_switch(const bfvo_ctx* c, const u64* key, const u64* d, u64* ks0
             }
         }
     }
-    free(acc0); free(acc1); free(D);
+    free(acc0); free(acc1); free(D); free(Dg);
+}
+
+static void key_switch(const bfvo_ctx* c, const u64* key, const u64* d, u64* ks0, u64* ks1) {
+    key_switch_g(c, key, d, 1, ks0, ks1);
 }
 
 int bfvo_key_switch(bfvo_ctx* c, uint32_t which, const u64* d, u64* ks0, u64* ks1) {
@@ -990,17 +1003,15 @@ void bfvo_rotate(bfvo_ctx* c, const u64* a, int64_t k, u64* out) {
     if (g == 1) { memcpy(out, a, sizeof(u64) * 2 * (size_t)L * n); return; }
     const u64* key = find_key(c, g);
     u64* c0 = (u64*)malloc(sizeof(u64) * (size_t)L * n);
-    u64* c1 = (u64*)malloc(sizeof(u64) * (size_t)L * n);
     bfvo_automorph(c, g, a, c0, L);
-    bfvo_automorph(c, g, a + (size_t)L * n, c1, L);
     u64* ks0 = (u64*)malloc(sizeof(u64) * (size_t)L * n);
-    key_switch(c, key, c1, ks0, out + (size_t)L * n);
+    key_switch_g(c, key, a + (size_t)L * n, g, ks0, out + (size_t)L * n);
     for (int j = 0; j < L; j++)
         for (int x = 0; x < n; x++) {
             size_t i = (size_t)j * n + x;
             out[i] = addm(c0[i], ks0[i], c->q[j]);
         }
-    free(c0); free(c1); free(ks0);
+    free(c0); free(ks0);
 }
 
 /* RFC 8439 section 2.3 block function with an arbitrary key / nonce, for the

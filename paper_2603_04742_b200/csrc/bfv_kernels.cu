@@ -937,10 +937,9 @@ __global__ void k_ks_modup(const DevConsts* __restrict__ dc, const u64* const* S
     const int idx = automorph_src(ginv ? ginv[item] : 0u, k, n, neg);
     u64 x[MAXL], y[MAXL];
 #pragma unroll
-    for (int i = 0; i < L; ++i) {
-        const u64 v = src[(size_t)i * n + idx];
+    for (int i = 0; i < L; ++i) {  // ModUp of the un-rotated source, phi_g's sign after (DESIGN 2.9)
         const u64 q = dc->mod[i].q;
-        x[i] = neg ? neg_mod(v, q) : v;
+        x[i] = src[(size_t)i * n + idx];
         y[i] = shoup(x[i], dc->dig_hat_inv[i], dc->dig_hat_inv_sh[i], q);
     }
 #pragma unroll
@@ -959,7 +958,7 @@ __global__ void k_ks_modup(const DevConsts* __restrict__ dc, const u64* const* S
                 for (int i = lo; i < hi; ++i) v += shoup_lazy(y[i], dc->dig_hat[i][j], dc->dig_hat_sh[i][j], m);
                 v = reduce_small_quot(v, dc->mod[j]);
             }
-            out[(size_t)j * n + k] = v;
+            out[(size_t)j * n + k] = neg ? neg_mod(v, dc->mod[j].q) : v;
         }
     }
 }

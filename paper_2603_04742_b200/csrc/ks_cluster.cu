@@ -126,12 +126,12 @@ __global__ void __cluster_dims__(KsCl<LOGN>::CL, 1, 1) __launch_bounds__(KsCl<LO
                 for (int i = lo; i < lo + alpha; ++i) {
                     if (i >= hi) break;
                     const u64 qi = dc->mod[i].q;
-                    u64 x = __ldg(src + (size_t)i * G::N + idx);
-                    x = neg ? neg_mod(x, qi) : x;
+                    const u64 x = __ldg(src + (size_t)i * G::N + idx);
                     const u64 y = shoup(x, dc->dig_hat_inv[i], dc->dig_hat_inv_sh[i], qi);
                     v += shoup_lazy(y, dc->dig_hat[i][j], dc->dig_hat_sh[i][j], q);
                 }
                 v = reduce_small_quot(v, md);
+                v = neg ? neg_mod(v, q) : v;  // phi_g(ModUp(x)) (DESIGN 2.9)
             }
             ct[c * 16 + jl] = v;
         }

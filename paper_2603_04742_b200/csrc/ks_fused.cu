@@ -97,17 +97,17 @@ __global__ void __launch_bounds__(Ntt2<LOGN>::TC, 256 / Ntt2<LOGN>::TC * 3) k_ks
                 if (AT && i >= hi) break;
                 const u64 qi = dc->mod[i].q;
                 u64 y;
-                if (ysrc) {  // y of phi_g(x) is phi_g(y): the same gather and negation
+                if (ysrc) {  // hoisted factors of the source (un-rotated)
                     y = __ldg(ysrc + (size_t)i * G::N + idx);
-                    y = neg ? neg_mod(y, qi) : y;
                 } else {
-                    u64 x = __ldg(src + (size_t)i * G::N + idx);
-                    x = neg ? neg_mod(x, qi) : x;
+                    const u64 x = __ldg(src + (size_t)i * G::N + idx);
                     y = shoup(x, dc->dig_hat_inv[i], dc->dig_hat_inv_sh[i], qi);
                 }
                 v += shoup_lazy(y, dc->dig_hat[i][j], dc->dig_hat_sh[i][j], m);  // alpha <= 16 terms < 2m
             }
+            // phi_g(ModUp(x)): the automorphism's sign applies to the converted limb (DESIGN 2.9)
             v = reduce_small_quot(v, dc->mod[j]);
+            v = neg ? neg_mod(v, m) : v;
         }
         tile[c * LN + jl] = v;
     }
@@ -178,13 +178,11 @@ __global__ void __launch_bounds__(Ntt2<LOGN>::TC, 256 / Ntt2<LOGN>::TC * 3)
             const int i = lo + a;
             if (i >= hi) break;
             const u64 qi = dc->mod[i].q;
-            if (ysrc) {  // y of phi_g(x) is phi_g(y); x_i = y_i [Q_d/q_i]_{q_i}
-                u64 v = __ldg(ysrc + (size_t)i * G::N + idx);
-                y[a] = neg ? neg_mod(v, qi) : v;
+            if (ysrc) {  // hoisted factors of the un-rotated source; x_i = y_i [Q_d/q_i]_{q_i}
+                y[a] = __ldg(ysrc + (size_t)i * G::N + idx);
                 x[a] = shoup(y[a], dc->dig_hat[i][i], dc->dig_hat_sh[i][i], qi);
             } else {
-                u64 v = __ldg(src + (size_t)i * G::N + idx);
-                x[a] = neg ? neg_mod(v, qi) : v;
+                x[a] = __ldg(src + (size_t)i * G::N + idx);
                 y[a] = shoup(x[a], dc->dig_hat_inv[i], dc->dig_hat_inv_sh[i], qi);
             }
         }
@@ -203,7 +201,8 @@ __global__ void __launch_bounds__(Ntt2<LOGN>::TC, 256 / Ntt2<LOGN>::TC * 3)
                 }
                 v = reduce_small_quot(v, dc->mod[j]);
             }
-            tile[c * VL + j * LC + jl] = v;
+            // phi_g(ModUp(x)): the automorphism's sign on every target limb (DESIGN 2.9)
+            tile[c * VL + j * LC + jl] = neg ? neg_mod(v, dc->mod[j].q) : v;
         }
     }
     __syncthreads();
