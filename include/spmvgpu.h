@@ -188,6 +188,7 @@ typedef struct {
     char name[32];
     double us;
     uint64_t items, bytes, limb_ntts;
+    uint64_t sources; /* distinct key-switch sources (< items when a level's ModUp is hoisted) */
 } spmvgpu_phase;
 int spmvgpu_plan_profile(spmvgpu_plan* p, spmvgpu_phase* phases, int cap, int* count);
 /* per kernel launch of the plan: `reps` graph replays, each after an L2 flush

@@ -238,6 +238,19 @@ namespace cssc {
 // (ks_cluster.cu); false when the shape has no cluster specialisation
 bool launch_ks_cluster(const DevConsts* dc, const RnsParams& P, const u64* const* SRC, const u64* SRCC,
                        int src_poly, const u32* ginv, const u64* const* KEY, u64* ACC, int items, cudaStream_t st);
+// Hoisted rotations of shared sources (level 0): per source its c1 and KsY
+// factors; per rotation item the index of its source and its Galois element
+struct HoistedKs {
+    int nsrc = 0;
+    const u64* const* src = nullptr;   // per source: the ciphertext (c1 = polynomial 1)
+    const u64* const* ysrc = nullptr;  // per source: ModUp factors y of c1 (KsY), nullable
+    const int* hidx = nullptr;         // per item: source index
+    const u32* gel = nullptr;          // per item: Galois element g
+};
+void launch_ks_hoisted(const DevConsts* dc, const RnsParams& P, const HoistedKs& hk, const u32* ginv,
+                       const u64* const* KEY, const u64* const* BASE, const u64* const* RSRC, u64* const* OUT,
+                       u64* DX, u64* ACC, int items, cudaStream_t st, const u64* const* EXTRA, const int* PAIR,
+                       u64* const* YOUT);
 void launch_ks_fused(const DevConsts* dc, const RnsParams& P, const u64* const* SRC, const u64* SRCC,
                      int src_poly, const u32* ginv, const u64* const* KEY, const u64* const* BASE,
                      const u64* const* RSRC, u64* const* OUT, u64* DX, u64* ACC, int items, cudaStream_t st,

@@ -833,6 +833,7 @@ int spmvgpu_plan_profile(spmvgpu_plan* p, spmvgpu_phase* phases, int cap, int* c
             phases[i].items = ph[i].items;
             phases[i].bytes = ph[i].bytes;
             phases[i].limb_ntts = ph[i].limb_ntts;
+            phases[i].sources = ph[i].sources;
         }
     });
 }

@@ -112,8 +112,8 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
     const int depth = n ? (int)trees[order[0]].dbl.size() : 0;
 
     arena_ = DevBuf(&ctx.pool(), 8 * ((size_t)(12 + 8 * std::max(depth, 1)) * std::max(n, 1) + 9 * n_odd +
-                                      2 * (size_t)ns_ + 8) +
-                                     16 * (size_t)(6 * depth + 24));
+                                      2 * (size_t)ns_ + 8 + 4 * (size_t)n + 2 * n_odd) +
+                                     16 * (size_t)(6 * depth + 28));
     prod_ = DevBuf(&ctx.pool(), sizeof(u64) * ctw * std::max(n, 1));
     if (depth >= 1) acc0_ = DevBuf(&ctx.pool(), sizeof(u64) * ctw * n);
     if (depth >= 2) acc1_ = DevBuf(&ctx.pool(), sizeof(u64) * ctw * n);
@@ -189,18 +189,24 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
     // where each hoisted rotation lands: rp slot per (chunk item k, odd step)
     std::vector<std::map<int, u64*>> rp_after(n);  // k -> (D index -> RP ct)
     std::set<u32> all_keys;
+    u32 last_g = 0;
     auto key_of = [&](u64 offset, std::set<u32>& lvl, u32& gi) {
         const u32 g = galois_element((int64_t)offset, P.n);
         lvl.insert(g);
         all_keys.insert(g);
         gi = inverse_galois(g, P.n);
+        last_g = g;
         return ctx.galois_key(g);
     };
+    // level 0 rotates only products; with odd steps, several rotations share a
+    // product: hoist its ModUp + forward NTT (CSSC_NO_HOIST=1 keeps per-item K1/K2)
+    const bool hoist0 = fused && !ksc && hoist && n_odd > 0 && std::getenv("CSSC_NO_HOIST") == nullptr;
     for (int l = 0; l < depth; ++l) {
         std::vector<const u64*> src, base, key, extra, ysrc;
         std::vector<u64*> yout;
         std::vector<u64*> o;
-        std::vector<u32> gi;
+        std::vector<u32> gi, gel;
+        std::vector<int> hidx;
         std::vector<int> pair;  // -1 plain; D_1 k: its O_1 item j; that O_1 item: -3 - k
         std::set<u32> lvl_keys;
         size_t odd_slot = 0;
@@ -210,6 +216,8 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
             u32 g;
             key.push_back(key_of(t.dbl[l], lvl_keys, g));
             gi.push_back(g);
+            gel.push_back(last_g);
+            hidx.push_back(k);
             src.push_back(cur);
             base.push_back(cur);
             o.push_back(acc_at(l % 2, k));
@@ -233,6 +241,8 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
                     u32 g;
                     key.push_back(key_of(off, lvl_keys, g));
                     gi.push_back(g);
+                    gel.push_back(last_g);
+                    hidx.push_back(k);
                     src.push_back(prod_at(k));
                     ysrc.push_back(prodY_at(k));
                     yout.push_back(nullptr);
@@ -256,6 +266,23 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
         pair.resize(o.size(), -1);
         lv.pair = std::any_of(pair.begin(), pair.end(), [](int v) { return v != -1; }) ? put(pair) : nullptr;
         lv.keys = (int)lvl_keys.size();
+        int nd = 0;  // level 0's sources: the products of the doubling items (items 0 .. nd-1 are k = 0 .. nd-1)
+        while (l == 0 && nd < n && !trees[order[nd]].dbl.empty()) ++nd;
+        // hoisting adds a launch: not for a handful of products (C1: +3 %, latency-bound)
+        if (l == 0 && hoist0 && nd >= 4) {
+            std::vector<const u64*> hp(nd), hy(nd);
+            for (int k = 0; k < nd; ++k) {
+                hp[k] = prod_at(k);
+                hy[k] = prodY_at(k);
+            }
+            lv.hsrc = nd;
+            lv.hprod = put(hp);
+            lv.hy = put(hy);
+            lv.hidx = put(hidx);
+            lv.gel = put(gel);
+            stats_.limb_ntts -= (u64)(lv.items - nd) * P.dnum * LK;
+            stats_.kernels += 1;
+        }
         levels_.push_back(lv);
         stats_.hbm_bytes += (u64)lv.items * 3 * C + lvl_keys.size() * KEY;
         stats_.key_bytes += lvl_keys.size() * KEY;
@@ -336,8 +363,19 @@ void CloudPlan::record(std::vector<cudaEvent_t>* marks, u64* dec_d, const EncIn*
         KsY ky;
         ky.src = lv.ysrc;
         ky.out = lv.yout;
-        ctx_.rotate_dev(lv.src, lv.ginv, lv.key, lv.base, lv.out, lv.items, DX_.words(), ACC_.words(),
-                        lv.extra, lv.pair, ky);
+        if (lv.hsrc) {
+            HoistedKs hk;
+            hk.nsrc = lv.hsrc;
+            hk.src = lv.hprod;
+            hk.ysrc = lv.hy;
+            hk.hidx = lv.hidx;
+            hk.gel = lv.gel;
+            launch_ks_hoisted(ctx_.dconsts(), P, hk, lv.ginv, lv.key, lv.base, lv.src, lv.out, DX_.words(),
+                              ACC_.words(), lv.items, st, lv.extra, lv.pair, lv.yout);
+        } else {
+            ctx_.rotate_dev(lv.src, lv.ginv, lv.key, lv.base, lv.out, lv.items, DX_.words(), ACC_.words(),
+                            lv.extra, lv.pair, ky);
+        }
         mark();
     }
     std::vector<int> qidx(L);
@@ -378,14 +416,16 @@ std::vector<PhaseTiming> CloudPlan::profile() {
               KEY = sizeof(u64) * ctx_.ksk_words() * (ctx_.fused_key_switch() ? 2 : 1),
               PT = sizeof(u64) * ctx_.poly_words();
     const u64 ks_ntts = (u64)P.dnum * LK + 2 * LK;
-    out.push_back({"multiply+relin", 0, (u64)n_, (u64)n_ * 3 * C + KEY, (u64)n_ * (7 * M + ks_ntts)});
+    out.push_back({"multiply+relin", 0, (u64)n_, (u64)n_ * 3 * C + KEY, (u64)n_ * (7 * M + ks_ntts), (u64)n_});
     for (size_t l = 0; l < levels_.size(); ++l) {
         const Level& lv = levels_[l];
+        const u64 srcs = lv.hsrc ? (u64)lv.hsrc : (u64)lv.items;
         out.push_back({"rotate level " + std::to_string(l), 0, (u64)lv.items,
-                       (u64)lv.items * 3 * C + (u64)lv.keys * KEY, (u64)lv.items * ks_ntts});
+                       (u64)lv.items * 3 * C + (u64)lv.keys * KEY,
+                       srcs * P.dnum * LK + (u64)lv.items * 2 * LK, srcs});
     }
     out.push_back({"mask accumulate", 0, (u64)n_, (u64)n_ * 2 * C + (u64)n_masks_ * PT,
-                   (u64)n_ * 2 * L + (u64)ns_ * 2 * L});
+                   (u64)n_ * 2 * L + (u64)ns_ * 2 * L, (u64)n_});
     // captured like run(), with event-record nodes between the groups, so the
     // timings include the graph's (small) inter-kernel gaps and nothing else
     std::vector<cudaEvent_t> marks;

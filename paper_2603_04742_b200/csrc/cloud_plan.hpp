@@ -36,6 +36,7 @@ struct PhaseTiming {
     std::string name;
     double us = 0;
     uint64_t items = 0, bytes = 0, limb_ntts = 0;  // compulsory HBM bytes, limb NTTs
+    uint64_t sources = 0;  // distinct key-switch sources (hoisted level 0: the products)
 };
 
 // one kernel launch of the plan, timed by profile_kernels()
@@ -121,6 +122,12 @@ private:
         const u64* const* ysrc;   // hoisted ModUp factors of each source's c1 (KsY; nullable)
         u64* const* yout;         // ... of each output's c1 when a later level rotates it
         int keys;                  // distinct switching keys of the level
+        // level 0 hoisted: every rotation of a product shares its ModUp + NTT
+        int hsrc = 0;                      // products (0: not hoisted)
+        const u64* const* hprod = nullptr;  // per product: its ciphertext
+        const u64* const* hy = nullptr;     // per product: KsY factors of c1
+        const int* hidx = nullptr;          // per item: product index
+        const u32* gel = nullptr;           // per item: Galois element
     };
     std::vector<Level> levels_;
     const u64* const* FINAL_ = nullptr;

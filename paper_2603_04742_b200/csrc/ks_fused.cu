@@ -368,6 +368,93 @@ __global__ void __launch_bounds__(kKsGroups * kKsGroupThreads) k_ks_blocks_inner
 }
 
 // ---------------------------------------------------------------------------
+// K2h: hoisted rotations (level 0).  Every rotation of one source shares
+// H = NTT(ModUp(c1)) (K1 without the automorphism + the forward block phase,
+// once per source); a rotation by g reads H in the NTT domain permuted by g
+// (position p holds a(psi^(2 brv(p) + 1)), so NTT(phi_g a)[p] = NTT(a)[p'] with
+// 2 brv(p') + 1 = g (2 brv(p) + 1) mod 2N), then the key MAC and the inverse
+// block phase of both accumulators as K2.  The words equal the unhoisted key
+// switch (phi_g(ModUp(c1)), DESIGN 2.9); a second rotation of the same source
+// costs no ModUp and no forward transform.
+// ---------------------------------------------------------------------------
+template <int LOGN>
+__device__ __forceinline__ int ntt_perm(u32 g, int p) {
+    constexpr u32 TWO_N_MASK = 2u * (1u << LOGN) - 1u;
+    const u32 e = 2u * (__brev((u32)p) >> (32 - LOGN)) + 1u;
+    const u32 e2 = (g * e) & TWO_N_MASK;
+    return (int)(__brev((e2 - 1u) >> 1) >> (32 - LOGN));
+}
+
+template <int LOGN, int LT, int KT, int AT, int LN = 16>
+__global__ void __launch_bounds__(kKsGroups * kKsGroupThreads) k_ks_blocks_gather(const DevConsts* __restrict__ dc,
+                                                                                const u64* __restrict__ H,
+                                                                                const int* __restrict__ HIDX,
+                                                                                const u32* __restrict__ GEL,
+                                                                                const u64* const* KEY,
+                                                                                u64* __restrict__ ACC) {
+    using G = Ntt2<LOGN>;
+    extern __shared__ u64 smem[];
+    constexpr int PITCH = G::PITCH;
+    constexpr int TW = LN * PITCH;
+    constexpr int T = kKsGroups * kKsGroupThreads;
+    constexpr int PER = LN * G::R2 / T;
+    constexpr int KMR = LN >= 16 ? 4 : 2;
+    constexpr int CTAS = G::R1 / LN;
+    static_assert(PER >= 1, "tile smaller than the CTA");
+    const int L = LT ? LT : dc->L, K = KT ? KT : dc->K, LK = L + K;
+    const int alpha = AT ? AT : dc->alpha, dnum = (L + alpha - 1) / alpha;
+    u64* work = smem;  // acc0 in tile 0, acc1 in tile 1
+    u64* tws = smem + 2 * TW;
+    int bid = blockIdx.x;
+    const int tileid = bid % CTAS;
+    bid /= CTAS;
+    const int j = bid % LK;
+    const int item = bid / LK;
+    const Modulus md = dc->mod[j];
+    const u64 q = md.q;
+    const int blk0 = tileid * LN;
+    const size_t base = (size_t)blk0 * G::R2;
+    const u64* key = KEY[item];
+    const size_t PL = (size_t)LK * G::N;
+    const size_t KW = (size_t)dnum * 2 * PL;  // key words; their Shoup companions follow
+    const u64* h = H + (size_t)HIDX[item] * dnum * PL + (size_t)j * G::N;
+    const u32 g = GEL[item];
+    const int grp = threadIdx.x / kKsGroupThreads;
+    const ThreadGroup tg = cta_slice(grp, kKsGroups);
+    auto saddr = [](int x) { return (x >> G::B) * PITCH + (x & (G::R2 - 1)); };
+    auto addr = [](int l, int pos) { return l * PITCH + pos; };
+    auto twf = [&](int sl, int l, int blk) { return block_tw<LOGN, LN>(tws, sl, l, blk); };
+    load_block_twiddles<LOGN, LN>(tws, dc->tw[j].inv, blk0);
+#pragma unroll
+    for (int r = 0; r < PER; ++r) {
+        const int x = threadIdx.x + T * r, s0 = saddr(x);
+        const int src = ntt_perm<LOGN>(g, (int)base + x);
+        u64 a0 = 0, a1 = 0;
+        for (int dg = 0; dg < dnum; ++dg) {
+            const u64 w = __ldg(h + (size_t)dg * PL + src);
+            const size_t ko = ((size_t)dg * 2) * PL + (size_t)j * G::N + base + x;
+            a0 = add_mod(a0, shoup(w, __ldg(key + ko), __ldg(key + KW + ko), q), q);
+            a1 = add_mod(a1, shoup(w, __ldg(key + ko + PL), __ldg(key + KW + ko + PL), q), q);
+        }
+        work[s0] = a0;
+        work[TW + s0] = a1;
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    line_ntt_v<G::B, 0, true, KMR, LN>(work + grp * TW, ConstQ{q}, addr, twf, tg);  // group p: accumulator p
+    __syncthreads();
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+        u64* dst = ACC + (((size_t)item * 2 + p) * LK + j) * G::N + base;
+#pragma unroll
+        for (int r = 0; r < PER; ++r) {
+            const int x = threadIdx.x + T * r;
+            dst[x] = work[p * TW + saddr(x)];
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // launch
 // ---------------------------------------------------------------------------
 template <class F>
@@ -382,28 +469,15 @@ static void ks_dispatch_shape(const RnsParams& P, F&& f) {
         f(integral_constant<int, 0>{}, integral_constant<int, 0>{}, integral_constant<int, 0>{});
 }
 
+// K1 (ModUp + column phase) of `items` sources into DX: the all-limbs kernel
+// for launches of a wave or more, per-limb 16/8/4-column tiles below
 template <int LOGN, int LT, int KT, int AT>
-static void ks_fused_t(const DevConsts* dc, const RnsParams& P, const u64* const* SRC, const u64* SRCC,
-                       int src_poly, const u32* ginv, const u64* const* KEY, const u64* const* BASE,
-                       const u64* const* RSRC, u64* const* OUT, u64* DX, u64* ACC, int items, cudaStream_t st,
-                       const u64* const* EXTRA, const int* PAIR, const KsY& ky) {
+static void launch_k1(const DevConsts* dc, const RnsParams& P, const u64* const* SRC, const u64* SRCC, int src_poly,
+                      const u32* ginv, u64* DX, int items, cudaStream_t st, const KsY& ky) {
     using G = Ntt2<LOGN>;
-    if (launch_ks_cluster(dc, P, SRC, SRCC, src_poly, ginv, KEY, ACC, items, st)) {
-        launch_ks_moddown(dc, P, ACC, BASE, RSRC, ginv, OUT, items, st, EXTRA, PAIR, ky.out);
-        return;
-    }
-    const int L = P.cfg.L, K = P.cfg.K, LK = L + K, dnum = P.dnum;
+    const int LK = P.cfg.L + P.cfg.K, dnum = P.dnum;
     const int smem1 = G::SMEM_C;
-    constexpr int KTM = ks_keys_tma<LOGN>() ? 1 : 0;
-    const int smem2 =
-        ((dnum < 2 ? 2 : dnum) * G::LINES * G::PITCH + 2 * G::TWB + KTM * dnum * 2 * G::LINES * G::R2) * 8 + 16;
-    const int smem2h =
-        ((dnum < 2 ? 2 : dnum) * 8 * G::PITCH + 2 * btw_entries<LOGN, 8>() + KTM * dnum * 2 * 8 * G::R2) * 8 + 16;
-    if (smem2 > 200 * 1024)
-        throw std::invalid_argument("key switch: too many digits for the fused kernel; set fused_key_switch 0");
     smem_optin_k(k_ks_modup_cols<LOGN, LT, KT, AT>, smem1);
-    smem_optin_k(k_ks_blocks_inner<LOGN, LT, KT, AT>, smem2);
-    smem_optin_k(k_ks_blocks_inner<LOGN, LT, KT, AT, 8>, smem2h);
     bool k1_done = false;
     constexpr int LCA = LT ? modup_all_lc<LT, KT>() : 0;
     constexpr bool HALF = LCA >= 4 && G::R1 * LCA / 2 >= G::TC && (G::R1 * LCA / 4 * (LT + KT)) % G::TC == 0;
@@ -445,6 +519,51 @@ static void ks_fused_t(const DevConsts* dc, const RnsParams& P, const u64* const
     }
     KS_CHECK();
     kmark("k_ks_modup_cols (K1)", st);
+}
+
+// inverse column phase of ACC + ModDown + base + extra + phi_g(rsrc.c0)
+template <int LOGN, int LT>
+static void launch_ks_tail(const DevConsts* dc, const RnsParams& P, const u64* const* BASE, const u64* const* RSRC,
+                           const u32* ginv, u64* const* OUT, u64* ACC, int items, cudaStream_t st,
+                           const u64* const* EXTRA, const int* PAIR, u64* const* YOUT) {
+    const int LK = P.cfg.L + P.cfg.K;
+    NttJob j;
+    for (int i = 0; i < MAX_JOB_LIMBS; ++i) j.pidx[i] = (signed char)(i % LK);
+    j.src = ACC;
+    j.dst = ACC;
+    j.limbs = 2 * LK;
+    if (launch_ks_cols_moddown(dc, P, ACC, BASE, RSRC, ginv, OUT, items, st, EXTRA, PAIR, YOUT)) {
+        kmark("k_ks_cols_moddown (inv cols + ModDown)", st);
+        return;
+    }
+    j.lazy_out = LT > 0 ? 1 : 0;  // the fixed-shape ModDown folds N^-1 into its constants
+    launch_ntt_phase(dc, LOGN, /*inverse=*/true, /*cols=*/true, j, items, st);
+    kmark("k_ntt_cols inv (key switch)", st);
+    launch_ks_moddown(dc, P, ACC, BASE, RSRC, ginv, OUT, items, st, EXTRA, PAIR, YOUT, j.lazy_out != 0);
+    kmark("k_ks_moddown_k", st);
+}
+
+template <int LOGN, int LT, int KT, int AT>
+static void ks_fused_t(const DevConsts* dc, const RnsParams& P, const u64* const* SRC, const u64* SRCC,
+                       int src_poly, const u32* ginv, const u64* const* KEY, const u64* const* BASE,
+                       const u64* const* RSRC, u64* const* OUT, u64* DX, u64* ACC, int items, cudaStream_t st,
+                       const u64* const* EXTRA, const int* PAIR, const KsY& ky) {
+    using G = Ntt2<LOGN>;
+    if (launch_ks_cluster(dc, P, SRC, SRCC, src_poly, ginv, KEY, ACC, items, st)) {
+        launch_ks_moddown(dc, P, ACC, BASE, RSRC, ginv, OUT, items, st, EXTRA, PAIR, ky.out);
+        return;
+    }
+    const int L = P.cfg.L, K = P.cfg.K, LK = L + K, dnum = P.dnum;
+    constexpr int KTM = ks_keys_tma<LOGN>() ? 1 : 0;
+    const int smem2 =
+        ((dnum < 2 ? 2 : dnum) * G::LINES * G::PITCH + 2 * G::TWB + KTM * dnum * 2 * G::LINES * G::R2) * 8 + 16;
+    const int smem2h =
+        ((dnum < 2 ? 2 : dnum) * 8 * G::PITCH + 2 * btw_entries<LOGN, 8>() + KTM * dnum * 2 * 8 * G::R2) * 8 + 16;
+    if (smem2 > 200 * 1024)
+        throw std::invalid_argument("key switch: too many digits for the fused kernel; set fused_key_switch 0");
+    smem_optin_k(k_ks_blocks_inner<LOGN, LT, KT, AT>, smem2);
+    smem_optin_k(k_ks_blocks_inner<LOGN, LT, KT, AT, 8>, smem2h);
+    launch_k1<LOGN, LT, KT, AT>(dc, P, SRC, SRCC, src_poly, ginv, DX, items, st, ky);
     constexpr int T2 = kKsGroups * kKsGroupThreads;
     if (blocks_use_ln8((long)items * LK * G::CTAS_B) && 8 * G::R2 >= T2)  // small launch: 8-block tiles
         k_ks_blocks_inner<LOGN, LT, KT, AT, 8><<<items * LK * (G::R1 / 8), T2, smem2h, st>>>(dc, DX, KEY, ACC);
@@ -452,20 +571,43 @@ static void ks_fused_t(const DevConsts* dc, const RnsParams& P, const u64* const
         k_ks_blocks_inner<LOGN, LT, KT, AT><<<items * LK * G::CTAS_B, T2, smem2, st>>>(dc, DX, KEY, ACC);
     KS_CHECK();
     kmark("k_ks_blocks_inner (K2)", st);
-    NttJob j;
-    for (int i = 0; i < MAX_JOB_LIMBS; ++i) j.pidx[i] = (signed char)(i % LK);
-    j.src = ACC;
-    j.dst = ACC;
-    j.limbs = 2 * LK;
-    if (launch_ks_cols_moddown(dc, P, ACC, BASE, RSRC, ginv, OUT, items, st, EXTRA, PAIR, ky.out)) {
-        kmark("k_ks_cols_moddown (inv cols + ModDown)", st);
-        return;
+    launch_ks_tail<LOGN, LT>(dc, P, BASE, RSRC, ginv, OUT, ACC, items, st, EXTRA, PAIR, ky.out);
+}
+
+// Hoisted level: K1 (no automorphism) + the forward block phase of every
+// source once (H in DX), K2h per rotation, then the usual tail
+template <int LOGN, int LT, int KT, int AT>
+static void ks_hoisted_t(const DevConsts* dc, const RnsParams& P, const HoistedKs& hk, const u32* ginv,
+                         const u64* const* KEY, const u64* const* BASE, const u64* const* RSRC, u64* const* OUT,
+                         u64* DX, u64* ACC, int items, cudaStream_t st, const u64* const* EXTRA, const int* PAIR,
+                         u64* const* YOUT) {
+    using G = Ntt2<LOGN>;
+    const int LK = P.cfg.L + P.cfg.K, dnum = P.dnum;
+    KsY ky;
+    ky.src = hk.ysrc;
+    launch_k1<LOGN, LT, KT, AT>(dc, P, hk.src, nullptr, 1, nullptr, DX, hk.nsrc, st, ky);
+    NttJob jb;
+    for (int i = 0; i < MAX_JOB_LIMBS; ++i) jb.pidx[i] = (signed char)(i % LK);
+    jb.src = DX;
+    jb.dst = DX;
+    jb.limbs = dnum * LK;
+    launch_ntt_phase(dc, LOGN, /*inverse=*/false, /*cols=*/false, jb, hk.nsrc, st);
+    kmark("k_ntt_blocks fwd (hoisted ModUp)", st);
+    constexpr int T2 = kKsGroups * kKsGroupThreads;
+    if (blocks_use_ln8((long)items * LK * G::CTAS_B) && 8 * G::R2 >= T2) {
+        const int sm = (2 * 8 * G::PITCH + 2 * btw_entries<LOGN, 8>()) * 8;
+        smem_optin_k(k_ks_blocks_gather<LOGN, LT, KT, AT, 8>, sm);
+        k_ks_blocks_gather<LOGN, LT, KT, AT, 8><<<items * LK * (G::R1 / 8), T2, sm, st>>>(dc, DX, hk.hidx, hk.gel,
+                                                                                        KEY, ACC);
+    } else {
+        const int sm = (2 * G::LINES * G::PITCH + 2 * G::TWB) * 8;
+        smem_optin_k(k_ks_blocks_gather<LOGN, LT, KT, AT>, sm);
+        k_ks_blocks_gather<LOGN, LT, KT, AT><<<items * LK * G::CTAS_B, T2, sm, st>>>(dc, DX, hk.hidx, hk.gel, KEY,
+                                                                                     ACC);
     }
-    j.lazy_out = LT > 0 ? 1 : 0;  // the fixed-shape ModDown folds N^-1 into its constants
-    launch_ntt_phase(dc, LOGN, /*inverse=*/true, /*cols=*/true, j, items, st);
-    kmark("k_ntt_cols inv (key switch)", st);
-    launch_ks_moddown(dc, P, ACC, BASE, RSRC, ginv, OUT, items, st, EXTRA, PAIR, ky.out, j.lazy_out != 0);
-    kmark("k_ks_moddown_k", st);
+    KS_CHECK();
+    kmark("k_ks_blocks_gather (K2h)", st);
+    launch_ks_tail<LOGN, LT>(dc, P, BASE, RSRC, ginv, OUT, ACC, items, st, EXTRA, PAIR, YOUT);
 }
 
 template <int LOGN>
@@ -477,6 +619,29 @@ static void ks_fused_logn(const DevConsts* dc, const RnsParams& P, const u64* co
         ks_fused_t<LOGN, decltype(l_)::value, decltype(k_)::value, decltype(a_)::value>(
             dc, P, SRC, SRCC, src_poly, ginv, KEY, BASE, RSRC, OUT, DX, ACC, items, st, EXTRA, PAIR, ky);
     });
+}
+
+void launch_ks_hoisted(const DevConsts* dc, const RnsParams& P, const HoistedKs& hk, const u32* ginv,
+                       const u64* const* KEY, const u64* const* BASE, const u64* const* RSRC, u64* const* OUT,
+                       u64* DX, u64* ACC, int items, cudaStream_t st, const u64* const* EXTRA, const int* PAIR,
+                       u64* const* YOUT) {
+    if (!items) return;
+    auto go = [&](auto lg_) {
+        constexpr int LG = decltype(lg_)::value;
+        ks_dispatch_shape(P, [&](auto l_, auto k_, auto a_) {
+            ks_hoisted_t<LG, decltype(l_)::value, decltype(k_)::value, decltype(a_)::value>(
+                dc, P, hk, ginv, KEY, BASE, RSRC, OUT, DX, ACC, items, st, EXTRA, PAIR, YOUT);
+        });
+    };
+    switch (P.cfg.logn) {
+        case 10: go(std::integral_constant<int, 10>{}); break;
+        case 11: go(std::integral_constant<int, 11>{}); break;
+        case 12: go(std::integral_constant<int, 12>{}); break;
+        case 13: go(std::integral_constant<int, 13>{}); break;
+        case 14: go(std::integral_constant<int, 14>{}); break;
+        case 15: go(std::integral_constant<int, 15>{}); break;
+        default: throw std::invalid_argument("key switch: unsupported logn");
+    }
 }
 
 void launch_ks_fused(const DevConsts* dc, const RnsParams& P, const u64* const* SRC, const u64* SRCC,
