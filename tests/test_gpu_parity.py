@@ -175,3 +175,26 @@ def test_cloud_plan_fused_and_unfused_agree():
         ctx.close()
     for a, b in zip(outs[0], outs[1]):
         assert np.array_equal(a, b)
+
+
+def test_hoisted_level0_matches_unhoisted(monkeypatch):
+    """Level 0 with shared ModUp (hoisted rotations of each product, K2h's
+    NTT-domain gather) and the per-rotation K1/K2 give the same words."""
+    shapes = [(7, 13), (3, 6), (5, 7), (11, 2), (1, 64), (40, 12), (8, 3)]
+    slices = [0, 0, 1, 1, 1, 0, 1]
+    rng = np.random.default_rng(17)
+    va = [rng.integers(-8, 9, r * c) for r, c in shapes]
+    vb = [rng.integers(-8, 9, r * c) for r, c in shapes]
+    outs = {}
+    for off in ("", "1"):
+        if off:
+            monkeypatch.setenv("CSSC_NO_HOIST", off)
+        else:
+            monkeypatch.delenv("CSSC_NO_HOIST", raising=False)
+        ctx = pk.Context(logn=12, seed=8)
+        ha = ctx.encrypt(va, [500 + i for i in range(len(shapes))])
+        hb = ctx.encrypt(vb, [600 + i for i in range(len(shapes))])
+        out = pk.cloud_plan(ctx, [r for r, _ in shapes], [c for _, c in shapes], slices, 2, ha, hb, graph=True)
+        outs[off] = [ctx.download(int(h)) for h in out]
+        ctx.close()
+    assert all(np.array_equal(x, y) for x, y in zip(outs[""], outs["1"]))
