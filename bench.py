@@ -342,9 +342,11 @@ DOT = 0.375
 
 
 def kernel_units(name: str, items: int, slices: int, logn: int, L: int, K: int, dnum: int, alpha: int,
-                 sources: int | None = None) -> float:
+                 sources: int | None = None, acc_items: int | None = None) -> float:
     """modmul-equivalents of one launch; `sources` = the distinct key-switch
-    sources of a hoisted level (its K1 and forward block phase run once per source)"""
+    sources of a level (hoisted: its K1 and forward block phase run once per
+    source), `acc_items` = its accumulated key switches (K2 / K2h; the odd steps
+    share their doubling step's INTT + ModDown, which runs `items` times)"""
     n, h = 1 << logn, 1 << (logn - 1)
     Bs = 7 if logn >= 15 else (6 if logn >= 12 else logn // 2)
     As = logn - Bs
@@ -370,15 +372,16 @@ def kernel_units(name: str, items: int, slices: int, logn: int, L: int, K: int, 
         return items * 3 * M * h * As
     if name.startswith("k_mul_scale"):
         return items * 3 * n * (e8 if overq else e2 + e1_b2q)
-    src = items if sources is None else sources
+    acc = items if acc_items is None else acc_items
+    src = acc if sources is None else sources
     if name.startswith("k_ks_modup_cols"):
         return src * dnum * LK * (n * alpha + h * As)
     if name.startswith("k_ks_blocks_inner"):
-        return items * LK * (dnum * h * Bs + 2 * dnum * n + 2 * h * Bs)
+        return acc * LK * (dnum * h * Bs + 2 * dnum * n + 2 * h * Bs)
     if name.startswith("k_ntt_blocks fwd (hoisted"):
         return src * dnum * LK * h * Bs
     if name.startswith("k_ks_blocks_gather"):
-        return items * LK * (2 * dnum * n + 2 * h * Bs)
+        return acc * LK * (2 * dnum * n + 2 * h * Bs)
     if name.startswith("k_ntt_cols inv (key switch)"):
         return items * 2 * LK * h * As
     if name.startswith("k_ks_cols_moddown"):  # inverse column phase + ModDown in one launch
@@ -402,7 +405,7 @@ def kernel_table(job, groups, st, logn, p, bfly_peak, reps=3):
     for k in ks:
         g = groups[k["group"]] if k["group"] < len(groups) else {"items": 0, "name": "?"}
         units = kernel_units(k["name"], g["items"], st["slices"], logn, p.L, p.K,
-                             (p.L + p.alpha - 1) // p.alpha, p.alpha, g.get("sources"))
+                             (p.L + p.alpha - 1) // p.alpha, p.alpha, g.get("sources"), g.get("acc_items"))
         rate = units / (k["us"] * 1e-6) if k["us"] > 0 else 0.0
         rows.append({"kernel": k["name"], "group": g["name"], "items": g["items"], "us": round(k["us"], 2),
                      "units": int(units), "g_units_s": round(rate / 1e9, 1),

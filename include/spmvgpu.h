@@ -188,7 +188,8 @@ typedef struct {
     char name[32];
     double us;
     uint64_t items, bytes, limb_ntts;
-    uint64_t sources; /* distinct key-switch sources (< items when a level's ModUp is hoisted) */
+    uint64_t sources;   /* distinct key-switch sources (< items when a level's ModUp is hoisted) */
+    uint64_t acc_items; /* key switches accumulated (> items: odd steps share their doubling step's ModDown) */
 } spmvgpu_phase;
 int spmvgpu_plan_profile(spmvgpu_plan* p, spmvgpu_phase* phases, int cap, int* count);
 /* per kernel launch of the plan: `reps` graph replays, each after an L2 flush

@@ -746,10 +746,10 @@ void bfvo_mul_plain(const bfvo_ctx* c, const u64* a, const u64* m, u64* out) {
  * and the UN-rotated c1: ModUp runs on d and the automorphism is applied to
  * every ModUp'd limb afterwards, phi_g(ModUp(d)), so rotations
  * of one source by several g share one ModUp (and its NTT) word for word. */
-static void key_switch_g(const bfvo_ctx* c, const u64* key, const u64* d, uint32_t g, u64* ks0, u64* ks1) {
+/* key-switch accumulation: acc0/acc1 (NTT domain over Q u P) += the inner
+ * products of phi_g(ModUp(d)) with the key */
+static void ks_accumulate(const bfvo_ctx* c, const u64* key, const u64* d, uint32_t g, u64* acc0, u64* acc1) {
     int n = c->n, L = c->L, K = c->K, LK = L + K;
-    u64* acc0 = (u64*)calloc((size_t)LK * n, sizeof(u64));
-    u64* acc1 = (u64*)calloc((size_t)LK * n, sizeof(u64));
     u64* D = (u64*)malloc(sizeof(u64) * n);
     u64* Dg = (u64*)malloc(sizeof(u64) * n);
     for (int dg = 0; dg < c->dnum; dg++) {
@@ -781,11 +781,17 @@ static void key_switch_g(const bfvo_ctx* c, const u64* key, const u64* d, uint32
             }
         }
     }
+    free(D); free(Dg);
+    (void)K;
+}
+
+/* INTT of the accumulators and ModDown (E4) into ks0/ks1 over Q */
+static void ks_finish(const bfvo_ctx* c, u64* acc0, u64* acc1, u64* ks0, u64* ks1) {
+    int n = c->n, L = c->L, K = c->K, LK = L + K;
     for (int j = 0; j < LK; j++) {
         bfvo_intt(c, j, acc0 + (size_t)j * n);
         bfvo_intt(c, j, acc1 + (size_t)j * n);
     }
-    /* ModDown (E4) */
     for (int p = 0; p < 2; p++) {
         u64* acc = p ? acc1 : acc0;
         u64* out = p ? ks1 : ks0;
@@ -800,7 +806,15 @@ static void key_switch_g(const bfvo_ctx* c, const u64* key, const u64* d, uint32
             }
         }
     }
-    free(acc0); free(acc1); free(D); free(Dg);
+}
+
+static void key_switch_g(const bfvo_ctx* c, const u64* key, const u64* d, uint32_t g, u64* ks0, u64* ks1) {
+    int n = c->n, LK = c->L + c->K;
+    u64* acc0 = (u64*)calloc((size_t)LK * n, sizeof(u64));
+    u64* acc1 = (u64*)calloc((size_t)LK * n, sizeof(u64));
+    ks_accumulate(c, key, d, g, acc0, acc1);
+    ks_finish(c, acc0, acc1, ks0, ks1);
+    free(acc0); free(acc1);
 }
 
 static void key_switch(const bfvo_ctx* c, const u64* key, const u64* d, u64* ks0, u64* ks1) {
@@ -1012,6 +1026,38 @@ void bfvo_rotate(bfvo_ctx* c, const u64* a, int64_t k, u64* out) {
             out[i] = addm(c0[i], ks0[i], c->q[j]);
         }
     free(c0); free(ks0);
+}
+
+/* acc + rot(acc, k1) + rot(src, k2) with ONE ModDown: the two key switches'
+ * accumulators are summed over Q u P before INTT + ModDown (a doubling step
+ * and the odd step right after it in the batched plan) */
+int bfvo_rotate2_add(bfvo_ctx* c, const u64* acc, const u64* src, int64_t k1, int64_t k2, u64* out) {
+    int n = c->n, L = c->L, LK = L + c->K;
+    uint32_t g1 = bfvo_galois_elt(c, k1), g2 = bfvo_galois_elt(c, k2);
+    if (g1 == 1 || g2 == 1) return -2;
+    const u64* key1 = find_key(c, g1);
+    const u64* key2 = find_key(c, g2);
+    if (!key1 || !key2) return -1;
+    u64* a0 = (u64*)calloc((size_t)LK * n, sizeof(u64));
+    u64* a1 = (u64*)calloc((size_t)LK * n, sizeof(u64));
+    ks_accumulate(c, key1, acc + (size_t)L * n, g1, a0, a1);
+    ks_accumulate(c, key2, src + (size_t)L * n, g2, a0, a1);
+    u64* ks0 = (u64*)malloc(sizeof(u64) * (size_t)L * n);
+    u64* ks1 = (u64*)malloc(sizeof(u64) * (size_t)L * n);
+    ks_finish(c, a0, a1, ks0, ks1);
+    u64* r1 = (u64*)malloc(sizeof(u64) * (size_t)L * n);
+    u64* r2 = (u64*)malloc(sizeof(u64) * (size_t)L * n);
+    bfvo_automorph(c, g1, acc, r1, L);
+    bfvo_automorph(c, g2, src, r2, L);
+    for (int j = 0; j < L; j++)
+        for (int x = 0; x < n; x++) {
+            size_t i = (size_t)j * n + x;
+            u64 q = c->q[j];
+            out[i] = addm(addm(addm(acc[i], r1[i], q), r2[i], q), ks0[i], q);
+            out[(size_t)L * n + i] = addm(acc[(size_t)L * n + i], ks1[i], q);
+        }
+    free(a0); free(a1); free(ks0); free(ks1); free(r1); free(r2);
+    return 0;
 }
 
 /* RFC 8439 section 2.3 block function with an arbitrary key / nonce, for the

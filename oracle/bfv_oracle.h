@@ -80,6 +80,9 @@ void bfvo_mul_tensor(const bfvo_ctx* c, const uint64_t* a, const uint64_t* b, ui
 /* 1: the context multiplies over Q u R (2L limbs, E6-E8), 0: over Q u B (HPS, 2L+1) */
 int bfvo_mul_overq(const bfvo_ctx* c);
 void bfvo_rotate(bfvo_ctx* c, const uint64_t* a, int64_t k, uint64_t* out);
+/* acc + rot(acc, k1) + rot(src, k2), the two key switches sharing one ModDown
+ * (the batched plan's doubling step fused with the odd step after it) */
+int bfvo_rotate2_add(bfvo_ctx* c, const uint64_t* acc, const uint64_t* src, int64_t k1, int64_t k2, uint64_t* out);
 /* plaintext multiply by a coefficient-form plaintext m (mod t) */
 void bfvo_mul_plain(const bfvo_ctx* c, const uint64_t* a, const uint64_t* m, uint64_t* out);
 /* key switch of one Q polynomial d (coef form) with the given key id */

@@ -149,6 +149,22 @@ __global__ void __launch_bounds__(Ntt2<LOGN>::TC, 256 / Ntt2<LOGN>::TC * 3) k_nt
     }
     cp_async_wait_all();
     __syncthreads();
+    if (INV && job.add_items) {
+        const u64* ad = job.add_items[item];
+        if (ad) {
+            ad += (size_t)j * G::N;
+            const u64 q2 = 2 * q;
+#pragma unroll
+            for (int r = 0; r < G::R1 * SEG / T; ++r) {
+                const int i = threadIdx.x + T * r, c = i / SEG, h = i % SEG;
+                const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(ad + (size_t)c * G::R2 + col0 + 2 * h);
+                u64 s0 = tile[c * LN + 2 * h] + x.x, s1 = tile[c * LN + 2 * h + 1] + x.y;
+                tile[c * LN + 2 * h] = s0 >= q2 ? s0 - q2 : s0;
+                tile[c * LN + 2 * h + 1] = s1 >= q2 ? s1 - q2 : s1;
+            }
+            __syncthreads();
+        }
+    }
     auto addr = [](int l, int pos) { return pos * LN + l; };
     auto twf = [&](int sl, int, int blk) {
         const int k = (1 << sl) + blk;
@@ -1238,7 +1254,7 @@ template <int LOGN, int L, int K, int LN, int RADIX = 3>
 __global__ void __launch_bounds__(Ntt2<LOGN>::TC, 256 / Ntt2<LOGN>::TC * (RADIX == 3 ? 3 : 4)) k_ks_cols_moddown(
     const __grid_constant__ ModDownK<L, K> c, const DevConsts* __restrict__ dc, const u64* __restrict__ ACC,
     const u64* const* BASE, const u64* const* RSRC, const u32* ginv, u64* const* OUT, const u64* const* EXTRA,
-    const int* PAIR, u64* const* YOUT) {
+    const int* PAIR, u64* const* YOUT, const u64* const* XACC) {
     using G = Ntt2<LOGN>;
     constexpr int LK = L + K, T = G::TC, CTAS = G::R2 / LN, SEG = LN / 2;
     constexpr int VL = LK * LN;                 // lines: (limb, column)
@@ -1279,6 +1295,19 @@ __global__ void __launch_bounds__(Ntt2<LOGN>::TC, 256 / Ntt2<LOGN>::TC * (RADIX 
         }
         cp_async_wait_all();
         __syncthreads();
+        const u64* xa = XACC ? XACC[it] : nullptr;  // an odd step's accumulators, same shared ModDown
+        if (xa) {
+            xa += (size_t)p * LK * n;
+#pragma unroll
+            for (int r = 0; r < LK * TILE / T; ++r) {
+                const int i = threadIdx.x + T * r, cc = i / VL, l = i % VL, j = l / LN;
+                const u64 q2 = 2 * dc->mod[j].q;
+                u64& t = tiles[(size_t)cc * VL + l];
+                const u64 s = t + xa[(size_t)j * n + (size_t)cc * G::R2 + col0 + (l % LN)];
+                t = s >= q2 ? s - q2 : s;
+            }
+            __syncthreads();
+        }
         auto twf = [&](int sl, int, int blk) {
             const int k = (1 << sl) + blk;
             return *reinterpret_cast<const ulonglong2*>(mytw + 2 * k);
@@ -1352,12 +1381,12 @@ __global__ void __launch_bounds__(Ntt2<LOGN>::TC, 256 / Ntt2<LOGN>::TC * (RADIX 
 template <int LOGN, int L, int K, int LN>
 static bool cols_moddown_ln(const DevConsts* dc, const RnsParams& P, const u64* ACC, const u64* const* BASE,
                             const u64* const* RSRC, const u32* ginv, u64* const* OUT, int items, cudaStream_t st,
-                            const u64* const* EXTRA, const int* PAIR, u64* const* YOUT);
+                            const u64* const* EXTRA, const int* PAIR, u64* const* YOUT, const u64* const* XACC);
 
 template <int LOGN, int L, int K>
 static bool cols_moddown_t(const DevConsts* dc, const RnsParams& P, const u64* ACC, const u64* const* BASE,
                            const u64* const* RSRC, const u32* ginv, u64* const* OUT, int items, cudaStream_t st,
-                           const u64* const* EXTRA, const int* PAIR, u64* const* YOUT) {
+                           const u64* const* EXTRA, const int* PAIR, u64* const* YOUT, const u64* const* XACC) {
     using G = Ntt2<LOGN>;
     static const int ln = [] {
         const char* e = std::getenv("CSSC_COLS_MODDOWN_LN");
@@ -1365,14 +1394,15 @@ static bool cols_moddown_t(const DevConsts* dc, const RnsParams& P, const u64* A
     }();
     // 4-column tiles (radix-4 passes, 40 KB smem, 3 CTAs per SM) measured faster
     // than 8 (80 KB, 2 CTAs per SM): C5 6.08 vs 6.19 ms
-    if (ln == 8) return cols_moddown_ln<LOGN, L, K, 8>(dc, P, ACC, BASE, RSRC, ginv, OUT, items, st, EXTRA, PAIR, YOUT);
-    return cols_moddown_ln<LOGN, L, K, 4>(dc, P, ACC, BASE, RSRC, ginv, OUT, items, st, EXTRA, PAIR, YOUT);
+    if (ln == 8)
+        return cols_moddown_ln<LOGN, L, K, 8>(dc, P, ACC, BASE, RSRC, ginv, OUT, items, st, EXTRA, PAIR, YOUT, XACC);
+    return cols_moddown_ln<LOGN, L, K, 4>(dc, P, ACC, BASE, RSRC, ginv, OUT, items, st, EXTRA, PAIR, YOUT, XACC);
 }
 
 template <int LOGN, int L, int K, int LN>
 static bool cols_moddown_ln(const DevConsts* dc, const RnsParams& P, const u64* ACC, const u64* const* BASE,
                             const u64* const* RSRC, const u32* ginv, u64* const* OUT, int items, cudaStream_t st,
-                            const u64* const* EXTRA, const int* PAIR, u64* const* YOUT) {
+                            const u64* const* EXTRA, const int* PAIR, u64* const* YOUT, const u64* const* XACC) {
     using G = Ntt2<LOGN>;
     if constexpr (G::R2 < 16 || G::R1 * LN < G::TC) {
         return false;
@@ -1386,11 +1416,12 @@ static bool cols_moddown_ln(const DevConsts* dc, const RnsParams& P, const u64* 
         if (radix == 2) {
             smem_optin_k(k_ks_cols_moddown<LOGN, L, K, LN, 2>, smem);
             k_ks_cols_moddown<LOGN, L, K, LN, 2><<<grid, G::TC, smem, st>>>(make_moddown_k<L, K>(P, true), dc, ACC,
-                                                                            BASE, RSRC, ginv, OUT, EXTRA, PAIR, YOUT);
+                                                                            BASE, RSRC, ginv, OUT, EXTRA, PAIR, YOUT,
+                                                                            XACC);
         } else {
             smem_optin_k(k_ks_cols_moddown<LOGN, L, K, LN>, smem);
             k_ks_cols_moddown<LOGN, L, K, LN><<<grid, G::TC, smem, st>>>(make_moddown_k<L, K>(P, true), dc, ACC, BASE,
-                                                                         RSRC, ginv, OUT, EXTRA, PAIR, YOUT);
+                                                                         RSRC, ginv, OUT, EXTRA, PAIR, YOUT, XACC);
         }
         CSSC_CHECK_LAUNCH();
         return true;
@@ -1411,13 +1442,15 @@ bool ks_cols_moddown_applies(const RnsParams& P, int items) {
 
 bool launch_ks_cols_moddown(const DevConsts* dc, const RnsParams& P, const u64* ACC, const u64* const* BASE,
                             const u64* const* RSRC, const u32* ginv, u64* const* OUT, int items, cudaStream_t st,
-                            const u64* const* EXTRA, const int* PAIR, u64* const* YOUT) {
+                            const u64* const* EXTRA, const int* PAIR, u64* const* YOUT, const u64* const* XACC) {
     if (!items || !ks_cols_moddown_applies(P, items)) return false;
     const auto& cf = P.cfg;
     {
         switch (cf.logn) {
-            case 13: return cols_moddown_t<13, 2, 2>(dc, P, ACC, BASE, RSRC, ginv, OUT, items, st, EXTRA, PAIR, YOUT);
-            case 14: return cols_moddown_t<14, 2, 2>(dc, P, ACC, BASE, RSRC, ginv, OUT, items, st, EXTRA, PAIR, YOUT);
+            case 13:
+                return cols_moddown_t<13, 2, 2>(dc, P, ACC, BASE, RSRC, ginv, OUT, items, st, EXTRA, PAIR, YOUT, XACC);
+            case 14:
+                return cols_moddown_t<14, 2, 2>(dc, P, ACC, BASE, RSRC, ginv, OUT, items, st, EXTRA, PAIR, YOUT, XACC);
             default: return false;
         }
     }
@@ -2156,6 +2189,53 @@ void launch_add(const DevConsts* dc, const RnsParams& P, const u64* const* A,
                 const u64* const* B, u64* const* OUT, int items, cudaStream_t st) {
     if (!items) return;
     k_add<<<ew_grid(P.n, items), EW_THREADS, 0, st>>>(dc, A, B, OUT);
+    CSSC_CHECK_LAUNCH();
+}
+
+// ACC[item] (2 (L+K) limbs) += XACC[item] (nullable entries): the key-switch
+// accumulators of an odd step summed into its doubling step's before the one
+// shared INTT + ModDown; lazy-safe (inputs < 2q, output < 2q)
+__global__ void k_acc_add(const DevConsts* __restrict__ dc, u64* ACC, const u64* const* XACC, int LK) {
+    const int n = dc->n;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int item = blockIdx.y;
+    const u64* x = XACC[item];
+    if (!x) return;
+    u64* a = ACC + (size_t)item * 2 * LK * n;
+    for (int j = 0; j < 2 * LK; ++j) {
+        const u64 q2 = 2 * dc->mod[j % LK].q;
+        const size_t o = (size_t)j * n + k;
+        const u64 s = a[o] + x[o];
+        a[o] = s >= q2 ? s - q2 : s;
+    }
+}
+
+void launch_acc_add(const DevConsts* dc, const RnsParams& P, u64* ACC, const u64* const* XACC, int items,
+                    cudaStream_t st) {
+    if (!items || !XACC) return;
+    k_acc_add<<<ew_grid(P.n, items), EW_THREADS, 0, st>>>(dc, ACC, XACC, P.cfg.L + P.cfg.K);
+    CSSC_CHECK_LAUNCH();
+}
+
+// OUT[item] = (phi_g(SRC[item].c0), untouched c1): the c0 term of a rotation
+// whose key switch is folded into another's ModDown
+__global__ void k_automorph_c0(const DevConsts* __restrict__ dc, const u64* const* SRC, const u32* ginv,
+                               u64* const* OUT) {
+    const int n = dc->n, L = dc->L;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int item = blockIdx.y;
+    bool neg;
+    const int idx = automorph_src(ginv[item], k, n, neg);
+    for (int j = 0; j < L; ++j) {
+        const u64 v = SRC[item][(size_t)j * n + idx];
+        OUT[item][(size_t)j * n + k] = neg ? neg_mod(v, dc->mod[j].q) : v;
+    }
+}
+
+void launch_automorph_c0(const DevConsts* dc, const RnsParams& P, const u64* const* SRC, const u32* ginv,
+                         u64* const* OUT, int items, cudaStream_t st) {
+    if (!items) return;
+    k_automorph_c0<<<ew_grid(P.n, items), EW_THREADS, 0, st>>>(dc, SRC, ginv, OUT);
     CSSC_CHECK_LAUNCH();
 }
 

@@ -28,6 +28,11 @@ struct NttJob {
     // set when the consumer (k_mul_scale_k, k_ks_moddown_k) folds N^-1 into its
     // constants (same canonical results, one Shoup product less per coefficient)
     int lazy_out = 0;
+    // inverse column phase only: per item (nullable entries) an addend with the
+    // layout of the input, added to it first (lazy inputs < 2q, sum reduced to
+    // < 2q): the key-switch accumulators of an odd step folded into its
+    // doubling step's INTT + ModDown
+    const u64* const* add_items = nullptr;
 };
 
 // sampler domains (nonce word 0 = dom | limb << 8 | digit << 16)
@@ -143,9 +148,15 @@ void launch_ks_inner(const DevConsts* dc, const RnsParams& P, const u64* DX,
 // the key switch's inverse column phase + ModDown in one launch (fixed shapes
 // L = K = 2 at N = 2^13 / 2^14); false: not applicable, use the two kernels
 bool ks_cols_moddown_applies(const RnsParams& P, int items);
+// XACC (nullable, per item nullable): accumulators added before the shared INTT + ModDown
 bool launch_ks_cols_moddown(const DevConsts* dc, const RnsParams& P, const u64* ACC, const u64* const* BASE,
                             const u64* const* RSRC, const u32* ginv, u64* const* OUT, int items, cudaStream_t st,
-                            const u64* const* EXTRA, const int* PAIR, u64* const* YOUT);
+                            const u64* const* EXTRA, const int* PAIR, u64* const* YOUT,
+                            const u64* const* XACC = nullptr);
+void launch_acc_add(const DevConsts* dc, const RnsParams& P, u64* ACC, const u64* const* XACC, int items,
+                    cudaStream_t st);
+void launch_automorph_c0(const DevConsts* dc, const RnsParams& P, const u64* const* SRC, const u32* ginv,
+                         u64* const* OUT, int items, cudaStream_t st);
 void launch_ks_moddown(const DevConsts* dc, const RnsParams& P, const u64* ACC,
                        const u64* const* BASE, const u64* const* RSRC, const u32* ginv,
                        u64* const* OUT, int items, cudaStream_t st, const u64* const* EXTRA = nullptr,
@@ -247,10 +258,19 @@ struct HoistedKs {
     const int* hidx = nullptr;         // per item: source index
     const u32* gel = nullptr;          // per item: Galois element g
 };
-void launch_ks_hoisted(const DevConsts* dc, const RnsParams& P, const HoistedKs& hk, const u32* ginv,
-                       const u64* const* KEY, const u64* const* BASE, const u64* const* RSRC, u64* const* OUT,
-                       u64* DX, u64* ACC, int items, cudaStream_t st, const u64* const* EXTRA, const int* PAIR,
-                       u64* const* YOUT);
+// A batched key switch in two phases, so that the accumulators of several key
+// switches can be summed before one shared INTT + ModDown (the plan's odd steps):
+// accumulate ACC[item] (phi_g(ModUp(SRC[item].c1)) x KEY[item]; hk: hoisted
+// sources), then finish (XACC[item] added, INTT, ModDown, + BASE + EXTRA +
+// phi_g(RSRC.c0), KsY factors of c1 into YOUT).  The domain of ACC between
+// the two depends on the path.
+enum class KsAccDomain { BlockInv, Coeff, Ntt };
+KsAccDomain launch_ks_accumulate(const DevConsts* dc, const RnsParams& P, bool fused, const u64* const* SRC,
+                                 const u32* ginv, const u64* const* KEY, u64* DX, u64* ACC, int items,
+                                 cudaStream_t st, const KsY& ky, const HoistedKs* hk = nullptr);
+void launch_ks_finish(const DevConsts* dc, const RnsParams& P, KsAccDomain dom, const u64* const* BASE,
+                      const u64* const* RSRC, const u32* ginv, u64* const* OUT, u64* ACC, int items, cudaStream_t st,
+                      const u64* const* EXTRA, u64* const* YOUT, const u64* const* XACC);
 void launch_ks_fused(const DevConsts* dc, const RnsParams& P, const u64* const* SRC, const u64* SRCC,
                      int src_poly, const u32* ginv, const u64* const* KEY, const u64* const* BASE,
                      const u64* const* RSRC, u64* const* OUT, u64* DX, u64* ACC, int items, cudaStream_t st,

@@ -834,6 +834,7 @@ int spmvgpu_plan_profile(spmvgpu_plan* p, spmvgpu_phase* phases, int cap, int* c
             phases[i].bytes = ph[i].bytes;
             phases[i].limb_ntts = ph[i].limb_ntts;
             phases[i].sources = ph[i].sources;
+            phases[i].acc_items = ph[i].acc_items;
         }
     });
 }

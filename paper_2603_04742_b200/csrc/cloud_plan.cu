@@ -111,9 +111,9 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
                      [&](int x, int y) { return trees[x].dbl.size() > trees[y].dbl.size(); });
     const int depth = n ? (int)trees[order[0]].dbl.size() : 0;
 
-    arena_ = DevBuf(&ctx.pool(), 8 * ((size_t)(12 + 8 * std::max(depth, 1)) * std::max(n, 1) + 9 * n_odd +
-                                      2 * (size_t)ns_ + 8 + 4 * (size_t)n + 2 * n_odd) +
-                                     16 * (size_t)(6 * depth + 28));
+    arena_ = DevBuf(&ctx.pool(), 8 * ((size_t)(16 + 10 * std::max(depth, 1)) * std::max(n, 1) + 16 * n_odd +
+                                      2 * (size_t)ns_ + 16) +
+                                     16 * (size_t)(16 * depth + 40));
     prod_ = DevBuf(&ctx.pool(), sizeof(u64) * ctw * std::max(n, 1));
     if (depth >= 1) acc0_ = DevBuf(&ctx.pool(), sizeof(u64) * ctw * n);
     if (depth >= 2) acc1_ = DevBuf(&ctx.pool(), sizeof(u64) * ctw * n);
@@ -184,10 +184,8 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
     const bool ksc = std::getenv("CSSC_KS_CLUSTER") != nullptr;
     auto kfuse = [&](int items) { return fused && !ksc && ks_cols_moddown_applies(P, items) ? 1 : 0; };
     stats_.kernels = n ? (fused ? 9 - kfuse(n) : 14) : 0;
-    stats_.limb_ntts = (u64)n * (7 * M + P.dnum * LK + 2 * LK) + (u64)n_rot * (P.dnum * LK + 2 * LK);
+    stats_.limb_ntts = (u64)n * (7 * M + P.dnum * LK + 2 * LK);  // + the rotate levels below
 
-    // where each hoisted rotation lands: rp slot per (chunk item k, odd step)
-    std::vector<std::map<int, u64*>> rp_after(n);  // k -> (D index -> RP ct)
     std::set<u32> all_keys;
     u32 last_g = 0;
     auto key_of = [&](u64 offset, std::set<u32>& lvl, u32& gi) {
@@ -201,15 +199,27 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
     // level 0 rotates only products; with odd steps, several rotations share a
     // product: hoist its ModUp + forward NTT (CSSC_NO_HOIST=1 keeps per-item K1/K2)
     const bool hoist0 = fused && !ksc && hoist && n_odd > 0 && std::getenv("CSSC_NO_HOIST") == nullptr;
+    // Each odd step's key switch is summed into the doubling step it follows
+    // (D_a, O_a share one INTT + ModDown; DESIGN 2.9, the oracle restates it):
+    // level 0 accumulates every rotation of the products (doubling items
+    // 0 .. nd-1, then the odd items: ACC[nd + o]), the odd items' c0 terms
+    // phi_O(prod.c0) go to rp slot o (its c1 half stays zero) and are added as
+    // EXTRA where their key switch is folded: level a-1 for O_a.
+    int nd = 0;
+    while (nd < n && !trees[order[nd]].dbl.empty()) ++nd;
+    const size_t accw = ctx.ksacc_words();
+    std::vector<std::map<int, int>> odd_after(n);  // k -> (a -> odd slot o)
+    std::vector<const u64*> odd_src;
+    std::vector<u32> odd_gi;
+    std::vector<u64*> odd_out;
     for (int l = 0; l < depth; ++l) {
-        std::vector<const u64*> src, base, key, extra, ysrc;
+        std::vector<const u64*> src, base, key, extra, ysrc, xacc;
         std::vector<u64*> yout;
         std::vector<u64*> o;
         std::vector<u32> gi, gel;
         std::vector<int> hidx;
-        std::vector<int> pair;  // -1 plain; D_1 k: its O_1 item j; that O_1 item: -3 - k
         std::set<u32> lvl_keys;
-        size_t odd_slot = 0;
+        bool any_x = false;
         for (int k = 0; k < n && (int)trees[order[k]].dbl.size() > l; ++k) {
             const Tree& t = trees[order[k]];
             u64* cur = acc_after(k, l);
@@ -224,20 +234,13 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
             ysrc.push_back(yafter(k, l));
             yout.push_back((int)t.dbl.size() > l + 1 ? accY_at(l % 2, k) : nullptr);
             extra.push_back(nullptr);
-            if (l >= 1) {  // fuse RP of the odd step that follows D_{l+1}
-                auto it = rp_after[k].find(l + 1);
-                if (it != rp_after[k].end()) extra.back() = it->second;
-            }
+            xacc.push_back(nullptr);
         }
-        if (l == 0) {  // hoisted odd steps: rot(prod) of every chunk, same launch
+        const int tail = (int)o.size();
+        if (l == 0) {  // the odd steps: rot(prod) of every chunk, accumulated in the same launch
             for (int k = 0; k < n; ++k) {
                 for (const auto& [after, off] : trees[order[k]].odd) {
-                    if (after == 1) {  // follows D_1: merged into D_1's ModDown (PAIR)
-                        pair.resize(o.size() + 1, -1);
-                        pair[k] = (int)o.size();
-                        pair[o.size()] = -3 - k;
-                    }
-                    u64* slot = rp_.words() + (odd_slot++) * ctw;
+                    const int slot = (int)odd_src.size();
                     u32 g;
                     key.push_back(key_of(off, lvl_keys, g));
                     gi.push_back(g);
@@ -245,29 +248,40 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
                     hidx.push_back(k);
                     src.push_back(prod_at(k));
                     ysrc.push_back(prodY_at(k));
-                    yout.push_back(nullptr);
-                    base.push_back(nullptr);
-                    extra.push_back(nullptr);
-                    o.push_back(slot);
-                    rp_after[k][after] = slot;
+                    odd_src.push_back(prod_at(k));
+                    odd_gi.push_back(g);
+                    odd_out.push_back(rp_.words() + (size_t)slot * ctw);
+                    odd_after[k][after] = slot;
                 }
             }
         }
+        for (int k = 0; k < tail; ++k) {  // fold the odd step that follows D_{l+1}
+            auto it = odd_after[k].find(l + 1);
+            if (it == odd_after[k].end()) continue;
+            extra[k] = rp_.words() + (size_t)it->second * ctw;
+            xacc[k] = ACC_.words() + (size_t)(nd + it->second) * accw;
+            any_x = true;
+        }
         Level lv;
-        lv.items = (int)o.size();
+        lv.items = tail;
+        lv.acc_items = (int)src.size();
         lv.src = put(src);
         lv.base = put(base);
         lv.out = put(o);
         lv.key = put(key);
         lv.ginv = put(gi);
-        lv.extra = put(extra);
+        lv.extra = any_x ? put(extra) : nullptr;
+        lv.xacc = any_x ? put(xacc) : nullptr;
         lv.ysrc = hoist ? put(ysrc) : nullptr;
         lv.yout = hoist ? put(yout) : nullptr;
-        pair.resize(o.size(), -1);
-        lv.pair = std::any_of(pair.begin(), pair.end(), [](int v) { return v != -1; }) ? put(pair) : nullptr;
+        lv.pair = nullptr;
         lv.keys = (int)lvl_keys.size();
-        int nd = 0;  // level 0's sources: the products of the doubling items (items 0 .. nd-1 are k = 0 .. nd-1)
-        while (l == 0 && nd < n && !trees[order[nd]].dbl.empty()) ++nd;
+        if (l == 0 && !odd_src.empty()) {
+            lv.odd_n = (int)odd_src.size();
+            lv.odd_src = put(odd_src);
+            lv.odd_ginv = put(odd_gi);
+            lv.odd_out = put(odd_out);
+        }
         // hoisting adds a launch: not for a handful of products (C1: +3 %, latency-bound)
         if (l == 0 && hoist0 && nd >= 4) {
             std::vector<const u64*> hp(nd), hy(nd);
@@ -280,14 +294,17 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
             lv.hy = put(hy);
             lv.hidx = put(hidx);
             lv.gel = put(gel);
-            stats_.limb_ntts -= (u64)(lv.items - nd) * P.dnum * LK;
-            stats_.kernels += 1;
         }
         levels_.push_back(lv);
-        stats_.hbm_bytes += (u64)lv.items * 3 * C + lvl_keys.size() * KEY;
+        const int srcs = lv.hsrc ? lv.hsrc : lv.acc_items;
+        const int kf = fused && !ksc && ks_cols_moddown_applies(P, lv.items) ? 1 : 0;
+        stats_.hbm_bytes += (u64)lv.acc_items * 3 * C + lvl_keys.size() * KEY;
         stats_.key_bytes += lvl_keys.size() * KEY;
-        stats_.kernels += fused ? 4 - kfuse(lv.items) : 7;
+        stats_.kernels += fused ? 2 + (2 - kf) + (any_x && !kf ? 1 : 0) + (lv.hsrc ? 1 : 0) + (lv.odd_n ? 1 : 0)
+                                : 7 + (any_x ? 1 : 0) + (lv.odd_n ? 1 : 0);
+        stats_.limb_ntts += (u64)srcs * P.dnum * LK + (u64)lv.items * 2 * LK;
     }
+    if (n_odd) cuda_check(cudaMemsetAsync(rp_.words(), 0, sizeof(u64) * ctw * n_odd, ctx.stream()), "rp zero");
     stats_.distinct_keys = all_keys.size();
 
     // masked inter-chunk accumulation
@@ -358,24 +375,27 @@ void CloudPlan::record(std::vector<cudaEvent_t>* marks, u64* dec_d, const EncIn*
     ctx_.mul_relin_dev(A_, B_, PROD_, n_, T_.words(), Z_.words(), D2_.words(), DX_.words(),
                        ACC_.words(), RLK_, enc, PRODY_ ? D2Y_.words() : nullptr, PRODY_);
     mark();
+    const bool fused = ctx_.fused_key_switch();
     for (size_t l = 0; l < levels_.size(); ++l) {
         const Level& lv = levels_[l];
         KsY ky;
         ky.src = lv.ysrc;
-        ky.out = lv.yout;
+        HoistedKs hk;
         if (lv.hsrc) {
-            HoistedKs hk;
             hk.nsrc = lv.hsrc;
             hk.src = lv.hprod;
             hk.ysrc = lv.hy;
             hk.hidx = lv.hidx;
             hk.gel = lv.gel;
-            launch_ks_hoisted(ctx_.dconsts(), P, hk, lv.ginv, lv.key, lv.base, lv.src, lv.out, DX_.words(),
-                              ACC_.words(), lv.items, st, lv.extra, lv.pair, lv.yout);
-        } else {
-            ctx_.rotate_dev(lv.src, lv.ginv, lv.key, lv.base, lv.out, lv.items, DX_.words(), ACC_.words(),
-                            lv.extra, lv.pair, ky);
         }
+        const KsAccDomain dom = launch_ks_accumulate(ctx_.dconsts(), P, fused, lv.src, lv.ginv, lv.key, DX_.words(),
+                                                     ACC_.words(), lv.acc_items, st, ky, lv.hsrc ? &hk : nullptr);
+        if (lv.odd_n) {
+            launch_automorph_c0(ctx_.dconsts(), P, lv.odd_src, lv.odd_ginv, lv.odd_out, lv.odd_n, st);
+            kmark("k_automorph_c0", st);
+        }
+        launch_ks_finish(ctx_.dconsts(), P, dom, lv.base, lv.src, lv.ginv, lv.out, ACC_.words(), lv.items, st,
+                         lv.extra, lv.yout, lv.xacc);
         mark();
     }
     std::vector<int> qidx(L);
@@ -416,16 +436,16 @@ std::vector<PhaseTiming> CloudPlan::profile() {
               KEY = sizeof(u64) * ctx_.ksk_words() * (ctx_.fused_key_switch() ? 2 : 1),
               PT = sizeof(u64) * ctx_.poly_words();
     const u64 ks_ntts = (u64)P.dnum * LK + 2 * LK;
-    out.push_back({"multiply+relin", 0, (u64)n_, (u64)n_ * 3 * C + KEY, (u64)n_ * (7 * M + ks_ntts), (u64)n_});
+    out.push_back({"multiply+relin", 0, (u64)n_, (u64)n_ * 3 * C + KEY, (u64)n_ * (7 * M + ks_ntts), (u64)n_, (u64)n_});
     for (size_t l = 0; l < levels_.size(); ++l) {
         const Level& lv = levels_[l];
-        const u64 srcs = lv.hsrc ? (u64)lv.hsrc : (u64)lv.items;
+        const u64 srcs = lv.hsrc ? (u64)lv.hsrc : (u64)lv.acc_items;
         out.push_back({"rotate level " + std::to_string(l), 0, (u64)lv.items,
-                       (u64)lv.items * 3 * C + (u64)lv.keys * KEY,
-                       srcs * P.dnum * LK + (u64)lv.items * 2 * LK, srcs});
+                       (u64)lv.acc_items * 3 * C + (u64)lv.keys * KEY,
+                       srcs * P.dnum * LK + (u64)lv.items * 2 * LK, srcs, (u64)lv.acc_items});
     }
     out.push_back({"mask accumulate", 0, (u64)n_, (u64)n_ * 2 * C + (u64)n_masks_ * PT,
-                   (u64)n_ * 2 * L + (u64)ns_ * 2 * L, (u64)n_});
+                   (u64)n_ * 2 * L + (u64)ns_ * 2 * L, (u64)n_, (u64)n_});
     // captured like run(), with event-record nodes between the groups, so the
     // timings include the graph's (small) inter-kernel gaps and nothing else
     std::vector<cudaEvent_t> marks;

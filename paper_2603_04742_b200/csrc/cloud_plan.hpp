@@ -36,7 +36,8 @@ struct PhaseTiming {
     std::string name;
     double us = 0;
     uint64_t items = 0, bytes = 0, limb_ntts = 0;  // compulsory HBM bytes, limb NTTs
-    uint64_t sources = 0;  // distinct key-switch sources (hoisted level 0: the products)
+    uint64_t sources = 0;    // distinct key-switch sources (hoisted level 0: the products)
+    uint64_t acc_items = 0;  // key switches accumulated (odd steps fold into their doubling step's ModDown)
 };
 
 // one kernel launch of the plan, timed by profile_kernels()
@@ -111,7 +112,8 @@ private:
     u64* const* PROD_ = nullptr;
     const u64* const* RLK_ = nullptr;
     struct Level {
-        int items;
+        int items;      // tail items (one INTT + ModDown each): the doubling steps
+        int acc_items;  // key switches accumulated: + level 0's odd steps
         const u64* const* src;
         const u64* const* base;
         u64* const* out;
@@ -128,6 +130,11 @@ private:
         const u64* const* hy = nullptr;     // per product: KsY factors of c1
         const int* hidx = nullptr;          // per item: product index
         const u32* gel = nullptr;           // per item: Galois element
+        const u64* const* xacc = nullptr;   // per tail item: an odd step's accumulators (nullable)
+        int odd_n = 0;                      // level 0: odd steps whose c0 term goes to rp slots
+        const u64* const* odd_src = nullptr;
+        const u32* odd_ginv = nullptr;
+        u64* const* odd_out = nullptr;
     };
     std::vector<Level> levels_;
     const u64* const* FINAL_ = nullptr;

@@ -521,21 +521,25 @@ static void launch_k1(const DevConsts* dc, const RnsParams& P, const u64* const*
     kmark("k_ks_modup_cols (K1)", st);
 }
 
-// inverse column phase of ACC + ModDown + base + extra + phi_g(rsrc.c0)
+// inverse column phase of ACC + ModDown + base + extra + phi_g(rsrc.c0); XACC
+// (nullable): other key switches' accumulators added before the shared INTT +
+// ModDown (inside the fused inverse-cols + ModDown kernel, else one add pass)
 template <int LOGN, int LT>
 static void launch_ks_tail(const DevConsts* dc, const RnsParams& P, const u64* const* BASE, const u64* const* RSRC,
                            const u32* ginv, u64* const* OUT, u64* ACC, int items, cudaStream_t st,
-                           const u64* const* EXTRA, const int* PAIR, u64* const* YOUT) {
+                           const u64* const* EXTRA, const int* PAIR, u64* const* YOUT,
+                           const u64* const* XACC = nullptr) {
     const int LK = P.cfg.L + P.cfg.K;
     NttJob j;
     for (int i = 0; i < MAX_JOB_LIMBS; ++i) j.pidx[i] = (signed char)(i % LK);
     j.src = ACC;
     j.dst = ACC;
     j.limbs = 2 * LK;
-    if (launch_ks_cols_moddown(dc, P, ACC, BASE, RSRC, ginv, OUT, items, st, EXTRA, PAIR, YOUT)) {
+    if (launch_ks_cols_moddown(dc, P, ACC, BASE, RSRC, ginv, OUT, items, st, EXTRA, PAIR, YOUT, XACC)) {
         kmark("k_ks_cols_moddown (inv cols + ModDown)", st);
         return;
     }
+    j.add_items = XACC;           // folded into the inverse column phase's tile load
     j.lazy_out = LT > 0 ? 1 : 0;  // the fixed-shape ModDown folds N^-1 into its constants
     launch_ntt_phase(dc, LOGN, /*inverse=*/true, /*cols=*/true, j, items, st);
     kmark("k_ntt_cols inv (key switch)", st);
@@ -543,16 +547,15 @@ static void launch_ks_tail(const DevConsts* dc, const RnsParams& P, const u64* c
     kmark("k_ks_moddown_k", st);
 }
 
+// accumulate phase: ACC[item] = the key products of phi_g(ModUp(c1)), in the
+// domain the tail expects; returns true when the cluster kernel produced them
+// (coefficient domain: ModDown only)
 template <int LOGN, int LT, int KT, int AT>
-static void ks_fused_t(const DevConsts* dc, const RnsParams& P, const u64* const* SRC, const u64* SRCC,
-                       int src_poly, const u32* ginv, const u64* const* KEY, const u64* const* BASE,
-                       const u64* const* RSRC, u64* const* OUT, u64* DX, u64* ACC, int items, cudaStream_t st,
-                       const u64* const* EXTRA, const int* PAIR, const KsY& ky) {
+static bool ks_accumulate_t(const DevConsts* dc, const RnsParams& P, const u64* const* SRC, const u64* SRCC,
+                            int src_poly, const u32* ginv, const u64* const* KEY, u64* DX, u64* ACC, int items,
+                            cudaStream_t st, const KsY& ky) {
     using G = Ntt2<LOGN>;
-    if (launch_ks_cluster(dc, P, SRC, SRCC, src_poly, ginv, KEY, ACC, items, st)) {
-        launch_ks_moddown(dc, P, ACC, BASE, RSRC, ginv, OUT, items, st, EXTRA, PAIR, ky.out);
-        return;
-    }
+    if (launch_ks_cluster(dc, P, SRC, SRCC, src_poly, ginv, KEY, ACC, items, st)) return true;
     const int L = P.cfg.L, K = P.cfg.K, LK = L + K, dnum = P.dnum;
     constexpr int KTM = ks_keys_tma<LOGN>() ? 1 : 0;
     const int smem2 =
@@ -571,16 +574,26 @@ static void ks_fused_t(const DevConsts* dc, const RnsParams& P, const u64* const
         k_ks_blocks_inner<LOGN, LT, KT, AT><<<items * LK * G::CTAS_B, T2, smem2, st>>>(dc, DX, KEY, ACC);
     KS_CHECK();
     kmark("k_ks_blocks_inner (K2)", st);
+    return false;
+}
+
+template <int LOGN, int LT, int KT, int AT>
+static void ks_fused_t(const DevConsts* dc, const RnsParams& P, const u64* const* SRC, const u64* SRCC,
+                       int src_poly, const u32* ginv, const u64* const* KEY, const u64* const* BASE,
+                       const u64* const* RSRC, u64* const* OUT, u64* DX, u64* ACC, int items, cudaStream_t st,
+                       const u64* const* EXTRA, const int* PAIR, const KsY& ky) {
+    if (ks_accumulate_t<LOGN, LT, KT, AT>(dc, P, SRC, SRCC, src_poly, ginv, KEY, DX, ACC, items, st, ky)) {
+        launch_ks_moddown(dc, P, ACC, BASE, RSRC, ginv, OUT, items, st, EXTRA, PAIR, ky.out);
+        return;
+    }
     launch_ks_tail<LOGN, LT>(dc, P, BASE, RSRC, ginv, OUT, ACC, items, st, EXTRA, PAIR, ky.out);
 }
 
-// Hoisted level: K1 (no automorphism) + the forward block phase of every
-// source once (H in DX), K2h per rotation, then the usual tail
+// Hoisted accumulate: K1 (no automorphism) + the forward block phase of every
+// source once (H in DX), then K2h per rotation into ACC
 template <int LOGN, int LT, int KT, int AT>
-static void ks_hoisted_t(const DevConsts* dc, const RnsParams& P, const HoistedKs& hk, const u32* ginv,
-                         const u64* const* KEY, const u64* const* BASE, const u64* const* RSRC, u64* const* OUT,
-                         u64* DX, u64* ACC, int items, cudaStream_t st, const u64* const* EXTRA, const int* PAIR,
-                         u64* const* YOUT) {
+static void ks_hoisted_acc_t(const DevConsts* dc, const RnsParams& P, const HoistedKs& hk, const u64* const* KEY,
+                             u64* DX, u64* ACC, int items, cudaStream_t st) {
     using G = Ntt2<LOGN>;
     const int LK = P.cfg.L + P.cfg.K, dnum = P.dnum;
     KsY ky;
@@ -607,7 +620,6 @@ static void ks_hoisted_t(const DevConsts* dc, const RnsParams& P, const HoistedK
     }
     KS_CHECK();
     kmark("k_ks_blocks_gather (K2h)", st);
-    launch_ks_tail<LOGN, LT>(dc, P, BASE, RSRC, ginv, OUT, ACC, items, st, EXTRA, PAIR, YOUT);
 }
 
 template <int LOGN>
@@ -621,27 +633,77 @@ static void ks_fused_logn(const DevConsts* dc, const RnsParams& P, const u64* co
     });
 }
 
-void launch_ks_hoisted(const DevConsts* dc, const RnsParams& P, const HoistedKs& hk, const u32* ginv,
-                       const u64* const* KEY, const u64* const* BASE, const u64* const* RSRC, u64* const* OUT,
-                       u64* DX, u64* ACC, int items, cudaStream_t st, const u64* const* EXTRA, const int* PAIR,
-                       u64* const* YOUT) {
-    if (!items) return;
-    auto go = [&](auto lg_) {
-        constexpr int LG = decltype(lg_)::value;
-        ks_dispatch_shape(P, [&](auto l_, auto k_, auto a_) {
-            ks_hoisted_t<LG, decltype(l_)::value, decltype(k_)::value, decltype(a_)::value>(
-                dc, P, hk, ginv, KEY, BASE, RSRC, OUT, DX, ACC, items, st, EXTRA, PAIR, YOUT);
-        });
-    };
-    switch (P.cfg.logn) {
-        case 10: go(std::integral_constant<int, 10>{}); break;
-        case 11: go(std::integral_constant<int, 11>{}); break;
-        case 12: go(std::integral_constant<int, 12>{}); break;
-        case 13: go(std::integral_constant<int, 13>{}); break;
-        case 14: go(std::integral_constant<int, 14>{}); break;
-        case 15: go(std::integral_constant<int, 15>{}); break;
+template <class F>
+static void logn_dispatch(int logn, F&& f) {
+    switch (logn) {
+        case 10: f(std::integral_constant<int, 10>{}); break;
+        case 11: f(std::integral_constant<int, 11>{}); break;
+        case 12: f(std::integral_constant<int, 12>{}); break;
+        case 13: f(std::integral_constant<int, 13>{}); break;
+        case 14: f(std::integral_constant<int, 14>{}); break;
+        case 15: f(std::integral_constant<int, 15>{}); break;
         default: throw std::invalid_argument("key switch: unsupported logn");
     }
+}
+
+KsAccDomain launch_ks_accumulate(const DevConsts* dc, const RnsParams& P, bool fused, const u64* const* SRC,
+                                 const u32* ginv, const u64* const* KEY, u64* DX, u64* ACC, int items,
+                                 cudaStream_t st, const KsY& ky, const HoistedKs* hk) {
+    if (!items) return KsAccDomain::BlockInv;
+    if (!fused) {  // ModUp, NTT, inner product: the NTT domain
+        const int LK = P.cfg.L + P.cfg.K;
+        launch_ks_modup(dc, P, SRC, 1, ginv, DX, items, st);
+        NttJob j;
+        for (int i = 0; i < MAX_JOB_LIMBS; ++i) j.pidx[i] = (signed char)(i % LK);
+        j.src = DX;
+        j.dst = DX;
+        j.limbs = P.dnum * LK;
+        launch_ntt(dc, P.cfg.logn, false, j, items, st);
+        launch_ks_inner(dc, P, DX, KEY, ACC, items, st);
+        return KsAccDomain::Ntt;
+    }
+    KsAccDomain dom = KsAccDomain::BlockInv;
+    logn_dispatch(P.cfg.logn, [&](auto lg_) {
+        constexpr int LG = decltype(lg_)::value;
+        ks_dispatch_shape(P, [&](auto l_, auto k_, auto a_) {
+            constexpr int LT = decltype(l_)::value, KT = decltype(k_)::value, AT = decltype(a_)::value;
+            if (hk)
+                ks_hoisted_acc_t<LG, LT, KT, AT>(dc, P, *hk, KEY, DX, ACC, items, st);
+            else if (ks_accumulate_t<LG, LT, KT, AT>(dc, P, SRC, nullptr, 1, ginv, KEY, DX, ACC, items, st, ky))
+                dom = KsAccDomain::Coeff;
+        });
+    });
+    return dom;
+}
+
+void launch_ks_finish(const DevConsts* dc, const RnsParams& P, KsAccDomain dom, const u64* const* BASE,
+                      const u64* const* RSRC, const u32* ginv, u64* const* OUT, u64* ACC, int items, cudaStream_t st,
+                      const u64* const* EXTRA, u64* const* YOUT, const u64* const* XACC) {
+    if (!items) return;
+    if (dom == KsAccDomain::Coeff) {
+        launch_acc_add(dc, P, ACC, XACC, items, st);
+        launch_ks_moddown(dc, P, ACC, BASE, RSRC, ginv, OUT, items, st, EXTRA, nullptr, YOUT);
+        return;
+    }
+    if (dom == KsAccDomain::Ntt) {
+        const int LK = P.cfg.L + P.cfg.K;
+        launch_acc_add(dc, P, ACC, XACC, items, st);
+        NttJob j;
+        for (int i = 0; i < MAX_JOB_LIMBS; ++i) j.pidx[i] = (signed char)(i % LK);
+        j.src = ACC;
+        j.dst = ACC;
+        j.limbs = 2 * LK;
+        launch_ntt(dc, P.cfg.logn, true, j, items, st);
+        launch_ks_moddown(dc, P, ACC, BASE, RSRC, ginv, OUT, items, st, EXTRA, nullptr, YOUT);
+        return;
+    }
+    logn_dispatch(P.cfg.logn, [&](auto lg_) {
+        constexpr int LG = decltype(lg_)::value;
+        ks_dispatch_shape(P, [&](auto l_, auto, auto) {
+            launch_ks_tail<LG, decltype(l_)::value>(dc, P, BASE, RSRC, ginv, OUT, ACC, items, st, EXTRA, nullptr, YOUT,
+                                                    XACC);
+        });
+    });
 }
 
 void launch_ks_fused(const DevConsts* dc, const RnsParams& P, const u64* const* SRC, const u64* SRCC,

@@ -68,6 +68,8 @@ def oracle_lib():
         for f in ("bfvo_add", "bfvo_mul_relin", "bfvo_mul_tensor", "bfvo_mul_plain"):
             getattr(L, f).argtypes = [C.c_void_p, u64p, u64p, u64p]
         L.bfvo_rotate.argtypes = [C.c_void_p, u64p, C.c_int64, u64p]
+        L.bfvo_rotate2_add.restype = C.c_int
+        L.bfvo_rotate2_add.argtypes = [C.c_void_p, u64p, u64p, C.c_int64, C.c_int64, u64p]
         L.bfvo_key_switch.argtypes = [C.c_void_p, C.c_uint32, u64p, u64p, u64p]
         L.bfvo_automorph.argtypes = [C.c_void_p, C.c_uint32, u64p, u64p, C.c_int]
         # sim oracle
@@ -175,6 +177,28 @@ class BfvOracle:
         out = np.zeros(2 * self.L * self.n, np.uint64)
         self.lib.bfvo_rotate(self.h, _p(_u64(a), u64p), k, _p(out, u64p))
         return out
+
+    def rotate2_add(self, acc, src, k1, k2):
+        """acc + rot(acc, k1) + rot(src, k2) with one shared ModDown."""
+        out = np.zeros(2 * self.L * self.n, np.uint64)
+        r = self.lib.bfvo_rotate2_add(self.h, _p(_u64(acc), u64p), _p(_u64(src), u64p), k1, k2, _p(out, u64p))
+        assert r == 0, r
+        return out
+
+    def plan_fold(self, prod, sched):
+        """intra_chunk_sum as the batched plan evaluates it (aggregate.cpp:36-50
+        semantics): each doubling step and the odd step right after it share
+        one ModDown (rotate2_add); a doubling step without one is rotate + add."""
+        acc, i = prod, 0
+        while i < len(sched):
+            off, from_acc = sched[i]
+            if from_acc and i + 1 < len(sched) and not sched[i + 1][1]:
+                acc = self.rotate2_add(acc, prod, off, sched[i + 1][0])
+                i += 2
+            else:
+                acc = self.add(acc, self.rotate(acc if from_acc else prod, off))
+                i += 1
+        return acc
 
 
 def sim_spmv_partitioned(m, v, slot_count, chunk_size=None, t=65537, ct_mb=0.52,

@@ -73,9 +73,7 @@ def test_config_result_words_match_oracle(cfgno):
 
     def chain(i):
         prod = orc.mul_relin(orc.encrypt(va[i], sa[i]), orc.encrypt(vb[i], sb[i]))
-        acc = prod
-        for off, from_acc in scheds[i]:
-            acc = orc.add(acc, orc.rotate(acc if from_acc else prod, off))
+        acc = orc.plan_fold(prod, scheds[i])
         return orc.mul_plain(acc, np.ones(r_list[i], np.int64))
 
     with ThreadPoolExecutor(max_workers=os.cpu_count() or 1) as ex:

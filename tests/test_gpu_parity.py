@@ -145,9 +145,7 @@ def test_cloud_plan_words_match_oracle(graph, shape):
     want = [None] * 3
     for i, (r, c) in enumerate(shapes):
         prod = orc.mul_relin(orc.encrypt(vals_a[i], sa[i]), orc.encrypt(vals_b[i], sb[i]))
-        acc = prod
-        for off, from_acc in pk.rotation_schedule(r, c):
-            acc = orc.add(acc, orc.rotate(acc if from_acc else prod, off))
+        acc = orc.plan_fold(prod, pk.rotation_schedule(r, c))
         part = orc.mul_plain(acc, np.ones(r, np.int64))
         want[slices[i]] = part if want[slices[i]] is None else orc.add(want[slices[i]], part)
     for s in range(3):

@@ -157,3 +157,21 @@ def test_overq_multiply_noise_at_full_size(logn, L):
     vals, budget = orc.decrypt(cp)
     assert np.array_equal(vals.astype(np.int64), np.mod(a * b, T))
     assert budget >= 40
+
+
+def test_rotate2_add_decrypts_like_two_rotations(orc):
+    """acc + rot(acc, k1) + rot(src, k2) with one shared ModDown (the batched
+    plan's fused doubling + odd step) decrypts to the same slots as the two
+    separate rotate-and-adds of aggregate.cpp:36-50."""
+    rng = np.random.default_rng(11)
+    S = orc.n // 2
+    a, b = rng.integers(-8, 9, S), rng.integers(-8, 9, S)
+    ca, cb = orc.encrypt(a, 5), orc.encrypt(b, 6)
+    for k1, k2 in ((1, 2), (3, S - 1), (2, 5)):
+        for g in (orc.galois_elt(k1), orc.galois_elt(k2)):
+            orc.lib.bfvo_add_galois_key(orc.h, g)
+        fused = orc.rotate2_add(ca, cb, k1, k2)
+        sep = orc.add(orc.add(ca, orc.rotate(ca, k1)), orc.rotate(cb, k2))
+        want = np.mod(a + np.roll(a, -k1) + np.roll(b, -k2), T)
+        assert np.array_equal(orc.decrypt(fused)[0].astype(np.int64), want)
+        assert np.array_equal(orc.decrypt(sep)[0].astype(np.int64), want)
