@@ -181,6 +181,8 @@ struct bfvo_ctx {
     u64* rlk;            /* NTT [dnum][2][L+K][N] */
     gkey_t* gk;
     int ngk, capgk;
+    gkey_t* gk2;         /* keys for target phi_g(s)^2 (rotations of a 3-component product) */
+    int ngk2, capgk2;
     /* constants */
     ext_t extQB, extBQ;
     u64 QhatInv[MAXP];          /* [(Q/q_i)^-1]_{q_i} */
@@ -548,6 +550,8 @@ void bfvo_destroy(bfvo_ctx* c) {
     free(c->pos0); free(c->pos1); free(c->s); free(c->s_ntt); free(c->pk); free(c->rlk);
     for (int i = 0; i < c->ngk; i++) free(c->gk[i].key);
     free(c->gk);
+    for (int i = 0; i < c->ngk2; i++) free(c->gk2[i].key);
+    free(c->gk2);
     free(c);
 }
 
@@ -576,6 +580,37 @@ void bfvo_add_galois_key(bfvo_ctx* c, uint32_t g) {
     c->ngk++;
     free(sp);
     free(tmp);
+}
+
+/* switching key for target phi_g(s)^2 = phi_g(s^2): rotates the s^2 component
+ * of an unrelinearised product (key id 2^32 | g) */
+static const u64* find_key_sq(bfvo_ctx* c, uint32_t g) {
+    for (int i = 0; i < c->ngk2; i++) if (c->gk2[i].g == g) return c->gk2[i].key;
+    int n = c->n, LK = c->L + c->K;
+    u64* sp = (u64*)malloc(sizeof(u64) * (size_t)LK * n);
+    u64* tmp = (u64*)malloc(sizeof(u64) * n);
+    for (int j = 0; j < LK; j++) {
+        u64* sj = sp + (size_t)j * n;
+        lift_small(c->s, n, c->q[j], tmp);
+        automorph_limb(n, c->q[j], g, tmp, sj);
+        bfvo_ntt(c, j, sj);
+        for (int k = 0; k < n; k++) sj[k] = mulm(sj[k], sj[k], c->q[j]);
+    }
+    if (c->ngk2 == c->capgk2) {
+        c->capgk2 = c->capgk2 ? 2 * c->capgk2 : 8;
+        c->gk2 = (gkey_t*)realloc(c->gk2, sizeof(gkey_t) * c->capgk2);
+    }
+    c->gk2[c->ngk2].g = g;
+    c->gk2[c->ngk2].key = gen_ksk(c, ((u64)1 << 32) | g, sp);
+    free(sp);
+    free(tmp);
+    return c->gk2[c->ngk2++].key;
+}
+
+int bfvo_get_ksk_sq(bfvo_ctx* c, uint32_t g, u64* out) {
+    const u64* key = find_key_sq(c, g);
+    memcpy(out, key, sizeof(u64) * (size_t)c->dnum * 2 * (c->L + c->K) * c->n);
+    return 0;
 }
 
 static const u64* find_key(bfvo_ctx* c, uint32_t which) {
@@ -995,6 +1030,21 @@ void bfvo_mul_tensor(const bfvo_ctx* c, const u64* a, const u64* b, u64* out3) {
     for (int r = 0; r < 3; r++) free(z[r]);
 }
 
+/* relinearisation of a tensor z ([3][L][N]) */
+void bfvo_mul_relin_z(bfvo_ctx* c, const u64* z, u64* out) {
+    int n = c->n, L = c->L;
+    u64* ks0 = (u64*)malloc(sizeof(u64) * (size_t)L * n);
+    u64* ks1 = (u64*)malloc(sizeof(u64) * (size_t)L * n);
+    key_switch(c, c->rlk, z + 2 * (size_t)L * n, ks0, ks1);
+    for (int j = 0; j < L; j++)
+        for (int k = 0; k < n; k++) {
+            size_t x = (size_t)j * n + k;
+            out[x] = addm(z[x], ks0[x], c->q[j]);
+            out[(size_t)L * n + x] = addm(z[(size_t)L * n + x], ks1[x], c->q[j]);
+        }
+    free(ks0); free(ks1);
+}
+
 void bfvo_mul_relin(bfvo_ctx* c, const u64* a, const u64* b, u64* out) {
     int n = c->n, L = c->L;
     u64* z = (u64*)malloc(sizeof(u64) * 3 * (size_t)L * n);
@@ -1057,6 +1107,99 @@ int bfvo_rotate2_add(bfvo_ctx* c, const u64* acc, const u64* src, int64_t k1, in
             out[(size_t)L * n + i] = addm(acc[(size_t)L * n + i], ks1[i], q);
         }
     free(a0); free(a1); free(ks0); free(ks1); free(r1); free(r2);
+    return 0;
+}
+
+/* intra_chunk_sum of one chunk as the batched plan evaluates it (aggregate.cpp
+ * semantics), from the product's tensor z = (z0, z1, z2)
+ * ([3][L][N]) and the rotation schedule:
+ *   fold_relin = 0: p = relin(z); then every doubling step D_a and the odd
+ *     step O_a right after it share one ModDown (rotate2_add), a lone D_a is
+ *     rotate + add;
+ *   fold_relin = 1 (the plan with hoisted level 0): with a schedule, p is never
+ *     relinearised on its own: level 0 sums the relinearisation of z2 and the
+ *     key switches of phi_g(z1) (key for phi_g(s)) and phi_g(z2) (key for
+ *     phi_g(s)^2) of D_1 (and O_1) into one ModDown; a later odd step O_a adds
+ *     its two z key switches and phi_O(z0) into D_a's ModDown.
+ * Without a schedule the result is relin(z). */
+int bfvo_plan_fold(bfvo_ctx* c, const u64* z, int nsteps, const int64_t* offs, const int* from_acc, int fold_relin,
+                   u64* out) {
+    int n = c->n, L = c->L, LK = L + c->K;
+    size_t cw = (size_t)L * n, aw = (size_t)LK * n;
+    const u64 *z0 = z, *z1 = z + cw, *z2 = z + 2 * cw;
+    u64* a0 = (u64*)calloc(aw, sizeof(u64));
+    u64* a1 = (u64*)calloc(aw, sizeof(u64));
+    u64* k0 = (u64*)malloc(sizeof(u64) * cw);
+    u64* k1 = (u64*)malloc(sizeof(u64) * cw);
+    u64* r = (u64*)malloc(sizeof(u64) * cw);
+    u64* acc = (u64*)malloc(sizeof(u64) * 2 * cw);
+    u64* nx = (u64*)malloc(sizeof(u64) * 2 * cw);
+    int i = 0;
+    if (!fold_relin || nsteps == 0) {
+        bfvo_mul_relin_z(c, z, acc);
+    } else {
+        /* level 0: relin + D_1 (+ O_1) of the unrelinearised product */
+        uint32_t gd = bfvo_galois_elt(c, offs[0]);
+        ks_accumulate(c, c->rlk, z2, 1, a0, a1);
+        ks_accumulate(c, find_key(c, gd), z1, gd, a0, a1);
+        ks_accumulate(c, find_key_sq(c, gd), z2, gd, a0, a1);
+        memcpy(acc, z, sizeof(u64) * 2 * cw);
+        bfvo_automorph(c, gd, z0, r, L);
+        for (size_t x = 0; x < cw; x++) acc[x] = addm(acc[x], r[x], c->q[x / n]);
+        i = 1;
+        if (nsteps > 1 && !from_acc[1]) {
+            uint32_t go = bfvo_galois_elt(c, offs[1]);
+            ks_accumulate(c, find_key(c, go), z1, go, a0, a1);
+            ks_accumulate(c, find_key_sq(c, go), z2, go, a0, a1);
+            bfvo_automorph(c, go, z0, r, L);
+            for (size_t x = 0; x < cw; x++) acc[x] = addm(acc[x], r[x], c->q[x / n]);
+            i = 2;
+        }
+        ks_finish(c, a0, a1, k0, k1);
+        for (size_t x = 0; x < cw; x++) {
+            acc[x] = addm(acc[x], k0[x], c->q[x / n]);
+            acc[cw + x] = addm(acc[cw + x], k1[x], c->q[x / n]);
+        }
+    }
+    /* p = relin(z) when the odd steps need it in the unfolded form */
+    u64* p = NULL;
+    if (!fold_relin) {
+        p = (u64*)malloc(sizeof(u64) * 2 * cw);
+        bfvo_mul_relin_z(c, z, p);
+    }
+    while (i < nsteps) {
+        if (!from_acc[i]) { free(a0); free(a1); free(k0); free(k1); free(r); free(acc); free(nx); free(p); return -3; }
+        uint32_t gd = bfvo_galois_elt(c, offs[i]);
+        memset(a0, 0, sizeof(u64) * aw);
+        memset(a1, 0, sizeof(u64) * aw);
+        ks_accumulate(c, find_key(c, gd), acc + cw, gd, a0, a1);
+        memcpy(nx, acc, sizeof(u64) * 2 * cw);
+        bfvo_automorph(c, gd, acc, r, L);
+        for (size_t x = 0; x < cw; x++) nx[x] = addm(nx[x], r[x], c->q[x / n]);
+        if (i + 1 < nsteps && !from_acc[i + 1]) {
+            uint32_t go = bfvo_galois_elt(c, offs[i + 1]);
+            if (fold_relin) {
+                ks_accumulate(c, find_key(c, go), z1, go, a0, a1);
+                ks_accumulate(c, find_key_sq(c, go), z2, go, a0, a1);
+                bfvo_automorph(c, go, z0, r, L);
+            } else {
+                ks_accumulate(c, find_key(c, go), p + cw, go, a0, a1);
+                bfvo_automorph(c, go, p, r, L);
+            }
+            for (size_t x = 0; x < cw; x++) nx[x] = addm(nx[x], r[x], c->q[x / n]);
+            i += 2;
+        } else {
+            i += 1;
+        }
+        ks_finish(c, a0, a1, k0, k1);
+        for (size_t x = 0; x < cw; x++) {
+            nx[x] = addm(nx[x], k0[x], c->q[x / n]);
+            nx[cw + x] = addm(nx[cw + x], k1[x], c->q[x / n]);
+        }
+        memcpy(acc, nx, sizeof(u64) * 2 * cw);
+    }
+    memcpy(out, acc, sizeof(u64) * 2 * cw);
+    free(a0); free(a1); free(k0); free(k1); free(r); free(acc); free(nx); free(p);
     return 0;
 }
 

@@ -82,6 +82,12 @@ int bfvo_mul_overq(const bfvo_ctx* c);
 void bfvo_rotate(bfvo_ctx* c, const uint64_t* a, int64_t k, uint64_t* out);
 /* acc + rot(acc, k1) + rot(src, k2), the two key switches sharing one ModDown
  * (the batched plan's doubling step fused with the odd step after it) */
+void bfvo_mul_relin_z(bfvo_ctx* c, const uint64_t* z, uint64_t* out);
+int bfvo_get_ksk_sq(bfvo_ctx* c, uint32_t g, uint64_t* out);
+/* intra_chunk_sum of one chunk from the product's tensor z ([3][L][N]) as the
+ * batched plan evaluates it; fold_relin: relinearisation folded into level 0 */
+int bfvo_plan_fold(bfvo_ctx* c, const uint64_t* z, int nsteps, const int64_t* offs, const int* from_acc,
+                   int fold_relin, uint64_t* out);
 int bfvo_rotate2_add(bfvo_ctx* c, const uint64_t* acc, const uint64_t* src, int64_t k1, int64_t k2, uint64_t* out);
 /* plaintext multiply by a coefficient-form plaintext m (mod t) */
 void bfvo_mul_plain(const bfvo_ctx* c, const uint64_t* a, const uint64_t* m, uint64_t* out);

@@ -69,6 +69,10 @@ def oracle_lib():
             getattr(L, f).argtypes = [C.c_void_p, u64p, u64p, u64p]
         L.bfvo_rotate.argtypes = [C.c_void_p, u64p, C.c_int64, u64p]
         L.bfvo_rotate2_add.restype = C.c_int
+        L.bfvo_plan_fold.restype = C.c_int
+        L.bfvo_plan_fold.argtypes = [C.c_void_p, u64p, C.c_int, i64p, ip, C.c_int, u64p]
+        L.bfvo_get_ksk_sq.argtypes = [C.c_void_p, C.c_uint32, u64p]
+        L.bfvo_mul_relin_z.argtypes = [C.c_void_p, u64p, u64p]
         L.bfvo_rotate2_add.argtypes = [C.c_void_p, u64p, u64p, C.c_int64, C.c_int64, u64p]
         L.bfvo_key_switch.argtypes = [C.c_void_p, C.c_uint32, u64p, u64p, u64p]
         L.bfvo_automorph.argtypes = [C.c_void_p, C.c_uint32, u64p, u64p, C.c_int]
@@ -184,6 +188,25 @@ class BfvOracle:
         r = self.lib.bfvo_rotate2_add(self.h, _p(_u64(acc), u64p), _p(_u64(src), u64p), k1, k2, _p(out, u64p))
         assert r == 0, r
         return out
+
+    def mul_tensor(self, a, b):
+        return self._bin(self.lib.bfvo_mul_tensor, a, b, 3 * self.L * self.n)
+
+    def plan_fold_z(self, z, sched, fold_relin):
+        """intra_chunk_sum from the product's tensor z as the batched plan evaluates
+        it (bfvo_plan_fold); fold_relin: the relinearisation shares level 0's ModDown."""
+        out = np.zeros(2 * self.L * self.n, np.uint64)
+        offs = np.array([o for o, _ in sched] or [0], np.int64)
+        fa = np.array([int(f) for _, f in sched] or [0], np.int32)
+        r = self.lib.bfvo_plan_fold(self.h, _p(_u64(z), u64p), len(sched), _p(offs, i64p), _p(fa, ip),
+                                    int(fold_relin), _p(out, u64p))
+        assert r == 0, r
+        return out
+
+    def ksk_sq(self, g):
+        w = np.zeros(self.dnum * 2 * (self.L + self.K) * self.n, np.uint64)
+        self.lib.bfvo_get_ksk_sq(self.h, g, _p(w, u64p))
+        return w
 
     def plan_fold(self, prod, sched):
         """intra_chunk_sum as the batched plan evaluates it (aggregate.cpp:36-50

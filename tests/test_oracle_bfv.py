@@ -175,3 +175,31 @@ def test_rotate2_add_decrypts_like_two_rotations(orc):
         want = np.mod(a + np.roll(a, -k1) + np.roll(b, -k2), T)
         assert np.array_equal(orc.decrypt(fused)[0].astype(np.int64), want)
         assert np.array_equal(orc.decrypt(sep)[0].astype(np.int64), want)
+
+
+@pytest.mark.parametrize("r,c", [(1, 7), (3, 5), (2, 13), (4, 2), (1, 1)])
+def test_plan_fold_both_forms_decrypt_to_the_intra_chunk_sum(orc, r, c):
+    """bfvo_plan_fold from the product's tensor: unfolded (relin first) equals the
+    rotate2_add fold of relin(z) word for word; folded (relinearisation inside
+    level 0's ModDown, keys for phi_g(s)^2) decrypts to the same slots."""
+    S = orc.n // 2
+    if r * c > S:
+        pytest.skip("chunk exceeds the ring")
+    rng = np.random.default_rng(r * 100 + c)
+    a, b = rng.integers(-8, 9, S), rng.integers(-8, 9, S)
+    z = orc.mul_tensor(orc.encrypt(a, 3), orc.encrypt(b, 4))
+    sched = pk.rotation_schedule(r, c)
+    p = orc.lib  # noqa: F841
+    relin = np.zeros(2 * orc.L * orc.n, np.uint64)
+    orc.lib.bfvo_mul_relin_z(orc.h, _u64(z).ctypes.data_as(C.POINTER(C.c_uint64)),
+                             relin.ctypes.data_as(C.POINTER(C.c_uint64)))
+    unf = orc.plan_fold_z(z, sched, False)
+    assert np.array_equal(unf, orc.plan_fold(relin, sched))
+    fol = orc.plan_fold_z(z, sched, True)
+    prod = np.mod(a * b, T)
+    want = np.zeros(S, np.int64)
+    for k in range(c):  # blocks of r slots summed: slot i gets sum_k prod[i + k r]
+        want += np.roll(prod, -k * r)
+    want = np.mod(want, T)
+    assert np.array_equal(orc.decrypt(unf)[0].astype(np.int64), want)
+    assert np.array_equal(orc.decrypt(fol)[0].astype(np.int64), want)
