@@ -178,6 +178,7 @@ typedef struct {
     uint64_t rotations, distinct_keys;
     uint64_t hbm_bytes_algorithmic; /* compulsory bytes per run (SURVEY 8(d) formulas) */
     uint64_t key_bytes_per_run;
+    uint64_t relin_folded; /* 1: the rotated chunks' relinearisation shares level 0's ModDown (DESIGN 2.9) */
 } spmvgpu_plan_stats;
 int spmvgpu_plan_stats_get(const spmvgpu_plan* p, spmvgpu_plan_stats* out);
 /* one CUDA-graph replay of the plan with event nodes between launch groups

@@ -607,6 +607,8 @@ static const u64* find_key_sq(bfvo_ctx* c, uint32_t g) {
     return c->gk2[c->ngk2++].key;
 }
 
+void bfvo_add_galois_key_sq(bfvo_ctx* c, uint32_t g) { (void)find_key_sq(c, g); }
+
 int bfvo_get_ksk_sq(bfvo_ctx* c, uint32_t g, u64* out) {
     const u64* key = find_key_sq(c, g);
     memcpy(out, key, sizeof(u64) * (size_t)c->dnum * 2 * (c->L + c->K) * c->n);

@@ -83,6 +83,7 @@ void bfvo_rotate(bfvo_ctx* c, const uint64_t* a, int64_t k, uint64_t* out);
 /* acc + rot(acc, k1) + rot(src, k2), the two key switches sharing one ModDown
  * (the batched plan's doubling step fused with the odd step after it) */
 void bfvo_mul_relin_z(bfvo_ctx* c, const uint64_t* z, uint64_t* out);
+void bfvo_add_galois_key_sq(bfvo_ctx* c, uint32_t g); /* not thread safe: call before parallel use */
 int bfvo_get_ksk_sq(bfvo_ctx* c, uint32_t g, uint64_t* out);
 /* intra_chunk_sum of one chunk from the product's tensor z ([3][L][N]) as the
  * batched plan evaluates it; fold_relin: relinearisation folded into level 0 */

@@ -46,7 +46,7 @@ class SpmvgpuParams(C.Structure):
 class PlanStats(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in (
         "chunks", "slices", "levels", "kernels_per_run", "limb_ntts_per_run", "rotations",
-        "distinct_keys", "hbm_bytes_algorithmic", "key_bytes_per_run")]
+        "distinct_keys", "hbm_bytes_algorithmic", "key_bytes_per_run", "relin_folded")]
 
 
 class Ledger(C.Structure):
@@ -429,9 +429,11 @@ class Context:
         return bps.value
 
 
-def cloud_plan(ctx: Context, r_list, c_list, slice_ids, n_slices: int, a_cts, b_cts, graph: bool = False):
+def cloud_plan(ctx: Context, r_list, c_list, slice_ids, n_slices: int, a_cts, b_cts, graph: bool = False,
+               stats: dict | None = None):
     """Run the batched cloud phase on raw ciphertext handles (device level):
-    returns one result-ciphertext handle per slice (caller frees them)."""
+    returns one result-ciphertext handle per slice (caller frees them); `stats`
+    (optional dict) receives the plan's statistics."""
     n = len(r_list)
     r = _u64(r_list)
     c = _u64(c_list)
@@ -446,6 +448,10 @@ def cloud_plan(ctx: Context, r_list, c_list, slice_ids, n_slices: int, a_cts, b_
             check(lib().spmvgpu_plan_capture(h))
         check(lib().spmvgpu_plan_run(h))
         ctx.sync()
+        if stats is not None:
+            ps = PlanStats()
+            check(lib().spmvgpu_plan_stats_get(h, C.byref(ps)))
+            stats.update({k: int(getattr(ps, k)) for k, _ in PlanStats._fields_})
     finally:
         lib().spmvgpu_plan_destroy(h)
     return out

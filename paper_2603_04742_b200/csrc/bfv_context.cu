@@ -114,6 +114,7 @@ GpuContext::~GpuContext() {
     for (auto& kv : pinned_free_) cudaFreeHost(kv.second);
     // buffers release into pool_; pool_ destructor frees device memory
     gk_.clear();
+    gk2_.clear();
     if (dc_) cudaFree(dc_);
     if (ev_fork_) cudaEventDestroy(ev_fork_);
     if (ev_join_) cudaEventDestroy(ev_join_);
@@ -238,6 +239,23 @@ const u64* GpuContext::galois_key(u32 g) {
     DevBuf key = gen_ksk(g, sp.words());
     const u64* p = key.words();
     gk_.emplace(g, std::move(key));
+    return p;
+}
+
+const u64* GpuContext::galois_key_sq(u32 g) {
+    std::lock_guard<std::mutex> lk(mu_);
+    auto it = gk2_.find(g);
+    if (it != gk2_.end()) return it->second.words();
+    const int n = P_.n, LK = P_.cfg.L + P_.cfg.K, logn = P_.cfg.logn;
+    DevBuf sg(&pool_, sizeof(int64_t) * n), sp(&pool_, sizeof(u64) * (size_t)LK * n),
+        sp2(&pool_, sizeof(u64) * (size_t)LK * n);
+    launch_automorph_small(logn, g, s_small_.as<int64_t>(), sg.as<int64_t>(), st_);
+    launch_lift_small(dc_, logn, sg.as<int64_t>(), LK, 0, sp.words(), st_);
+    launch_ntt(dc_, logn, false, job(sp.words(), sp.words(), LK, range_idx(0, LK)), 1, st_);
+    launch_square(dc_, logn, LK, sp.words(), sp2.words(), st_);
+    DevBuf key = gen_ksk(((u64)1 << 32) | g, sp2.words());
+    const u64* p = key.words();
+    gk2_.emplace(g, std::move(key));
     return p;
 }
 
@@ -601,7 +619,8 @@ void GpuContext::add(const std::vector<const u64*>& a, const std::vector<const u
 
 void GpuContext::mul_relin_dev(const u64* const* A, const u64* const* B, u64* const* OUT,
                                int items, u64* T, u64* Z, u64* D2, u64* DX, u64* ACC,
-                               const u64* const* RLK, const EncIn* enc, u64* D2Y, u64* const* YOUT) {
+                               const u64* const* RLK, const EncIn* enc, u64* D2Y, u64* const* YOUT,
+                               int relin_lo, u64* const* Y1) {
     const int L = P_.cfg.L, K = P_.cfg.K, LK = L + K, M = P_.mul_limbs(), logn = P_.cfg.logn;
     std::vector<int> pm;
     for (int j = 0; j < M; ++j) pm.push_back(j < L ? j : K + j);
@@ -626,16 +645,22 @@ void GpuContext::mul_relin_dev(const u64* const* A, const u64* const* B, u64* co
         launch_mul_tensor(dc_, P_, T, Z, items, st_);
         launch_ntt(dc_, logn, true, job(Z, Z, 3 * M, pm), items, st_);
     }
-    launch_mul_scale(dc_, P_, Z, OUT, D2, items, st_, fused_ks_ ? D2Y : nullptr, lazy_z);
+    launch_mul_scale(dc_, P_, Z, OUT, D2, items, st_, fused_ks_ ? D2Y : nullptr, lazy_z, fused_ks_ ? Y1 : nullptr);
     kmark("k_mul_scale_k", st_);
-    if (fused_ks_) {
+    if (relin_lo < 0 || relin_lo > items) throw std::invalid_argument("mul_relin: relin range");
+    const int nr = items - relin_lo;  // relinearised items, from relin_lo on
+    if (nr == 0) {
+        stats_.kernels += 5;
+    } else if (fused_ks_) {
         KsY ky;
-        ky.srcc = D2Y;
-        ky.out = YOUT;
-        launch_ks_fused(dc_, P_, nullptr, D2, 0, nullptr, RLK, reinterpret_cast<const u64* const*>(OUT),
-                        nullptr, OUT, DX, ACC, items, st_, nullptr, nullptr, ky);
+        ky.srcc = D2Y ? D2Y + (size_t)relin_lo * L * P_.n : nullptr;
+        ky.out = YOUT ? YOUT + relin_lo : nullptr;
+        launch_ks_fused(dc_, P_, nullptr, D2 + (size_t)relin_lo * L * P_.n, 0, nullptr, RLK + relin_lo,
+                        reinterpret_cast<const u64* const*>(OUT + relin_lo), nullptr, OUT + relin_lo, DX, ACC, nr,
+                        st_, nullptr, nullptr, ky);
         stats_.kernels += 9;
     } else {
+        if (relin_lo) throw std::invalid_argument("mul_relin: folded relinearisation needs the fused key switch");
         launch_ks_modup_contig(dc_, P_, D2, DX, items, st_);
         launch_ntt(dc_, logn, false, job(DX, DX, P_.dnum * LK, range_idx(0, LK)), items, st_);
         launch_ks_inner(dc_, P_, DX, RLK, ACC, items, st_);

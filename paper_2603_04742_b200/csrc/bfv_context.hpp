@@ -117,6 +117,9 @@ public:
     // keys (NTT form on device)
     const u64* relin_key() const { return rlk_.words(); }
     const u64* galois_key(u32 g);                 // generated on first use
+    // key for target phi_g(s)^2 (key id 2^32 | g): rotates the s^2 component of
+    // an unrelinearised product (the plan's folded level 0)
+    const u64* galois_key_sq(u32 g);
     void ensure_galois_keys(const std::vector<int64_t>& steps);
     size_t galois_key_count() const { return gk_.size(); }
     const u64* s_ntt() const { return s_ntt_.words(); }
@@ -181,9 +184,13 @@ public:
     // enc: A and B are still to be finished from a deferred encryption (EncIn)
     // D2Y / YOUT (fused key switch, fixed shapes): the ModUp factors of c2 and
     // of the products' c1 (KsY)
+    // relin_lo > 0: items [0, relin_lo) stay unrelinearised (OUT = (z0, z1), D2 =
+    // z2, D2Y its ModUp factors, Y1 those of z1: the plan folds their
+    // relinearisation into level 0); items [relin_lo, items) are relinearised
     void mul_relin_dev(const u64* const* A, const u64* const* B, u64* const* OUT, int items,
                        u64* T, u64* Z, u64* D2, u64* DX, u64* ACC, const u64* const* RLK,
-                       const EncIn* enc = nullptr, u64* D2Y = nullptr, u64* const* YOUT = nullptr);
+                       const EncIn* enc = nullptr, u64* D2Y = nullptr, u64* const* YOUT = nullptr,
+                       int relin_lo = 0, u64* const* Y1 = nullptr);
     // OUT = BASE + EXTRA + rot(SRC) (BASE / EXTRA per-item nullable); PAIR (nullable):
     // PAIR[i] = j >= 0 also adds item j's rotation into OUT[i] (PAIR[j] = -3 - i;
     // the two items' CTAs split the limbs)
@@ -227,7 +234,7 @@ private:
     std::vector<DevBuf> tables_;
     DevBuf pos0_;
     DevBuf s_small_, s_ntt_, pk_, rlk_;
-    std::map<u32, DevBuf> gk_;
+    std::map<u32, DevBuf> gk_, gk2_;
     std::atomic<uint64_t> stream_counter_{1};
     LaunchStats stats_;
     bool fused_ks_ = true;

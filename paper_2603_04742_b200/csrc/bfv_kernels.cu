@@ -667,7 +667,7 @@ struct ScaleK {
 
 template <int L>
 __global__ void k_mul_scale_k(const __grid_constant__ ScaleK<L> c, const u64* __restrict__ Z, u64* const* OUT,
-                              u64* __restrict__ D2, u64* __restrict__ D2Y) {
+                              u64* __restrict__ D2, u64* __restrict__ D2Y, u64* const* Y1) {
     constexpr int M = 2 * L;
     const int n = c.n;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
@@ -698,8 +698,10 @@ __global__ void k_mul_scale_k(const __grid_constant__ ScaleK<L> c, const u64* __
     u64* dst = r < 2 ? OUT[item] + (size_t)r * L * n : D2 + (size_t)item * L * n;
 #pragma unroll
     for (int i = 0; i < L; ++i) dst[(size_t)i * n + k] = o[i];
-    if (r == 2 && D2Y) {  // the relinearisation's ModUp factors of c2
-        u64* yy = D2Y + (size_t)item * L * n;
+    // ModUp factors (KsY) of c2 for the relinearisation, and of z1 when the
+    // product's c1 is key-switched unrelinearised (the folded level 0)
+    u64* yy = r == 2 ? (D2Y ? D2Y + (size_t)item * L * n : nullptr) : (r == 1 && Y1 ? Y1[item] : nullptr);
+    if (yy) {
 #pragma unroll
         for (int i = 0; i < L; ++i) yy[(size_t)i * n + k] = shoup(o[i], c.dhi[i], c.dhi_sh[i], c.qm[i].q);
     }
@@ -909,17 +911,17 @@ __global__ void k_mul_scale(const DevConsts* __restrict__ dc, const u64* __restr
 }
 
 void launch_mul_scale(const DevConsts* dc, const RnsParams& P, const u64* Z, u64* const* OUT,
-                      u64* D2, int items, cudaStream_t st, u64* D2Y, bool lazy_in) {
+                      u64* D2, int items, cudaStream_t st, u64* D2Y, bool lazy_in, u64* const* Y1) {
     if (!items) return;
     dispatch_shape(P, [&](auto l_, auto k_, auto a_) {
         dim3 g = ew_grid(P.n, items);
         g.z = 3;
         constexpr int LT = decltype(l_)::value;
         if constexpr (LT > 0)
-            k_mul_scale_k<LT><<<g, EW_THREADS, 0, st>>>(make_scale_k<LT>(P, lazy_in), Z, OUT, D2, D2Y);
+            k_mul_scale_k<LT><<<g, EW_THREADS, 0, st>>>(make_scale_k<LT>(P, lazy_in), Z, OUT, D2, D2Y, Y1);
         else if (lazy_in)
             throw std::invalid_argument("unscaled inverse-NTT input needs a fixed RNS shape");
-        else if (D2Y)
+        else if (D2Y || Y1)
             throw std::invalid_argument("hoisted ModUp factors need a fixed RNS shape");
         else
             k_mul_scale<SHAPE_ARGS><<<g, EW_THREADS, 0, st>>>(dc, Z, OUT, D2);

@@ -133,8 +133,11 @@ void launch_mul_blocks_tensor(const DevConsts* dc, const RnsParams& P, const u64
 void launch_mul_tensor(const DevConsts* dc, const RnsParams& P, const u64* T, u64* Z, int items,
                        cudaStream_t st);
 // lazy_in: Z is the unscaled, lazy inverse column output (NttJob::lazy_out)
+// Y1 (per item nullable): ModUp factors of z1 (the product's c1 when it is
+// key-switched without relinearisation)
 void launch_mul_scale(const DevConsts* dc, const RnsParams& P, const u64* Z, u64* const* OUT,
-                      u64* D2, int items, cudaStream_t st, u64* D2Y = nullptr, bool lazy_in = false);
+                      u64* D2, int items, cudaStream_t st, u64* D2Y = nullptr, bool lazy_in = false,
+                      u64* const* Y1 = nullptr);
 
 // hybrid key switching
 void launch_ks_modup(const DevConsts* dc, const RnsParams& P, const u64* const* SRC, int src_poly,
@@ -249,15 +252,20 @@ namespace cssc {
 // (ks_cluster.cu); false when the shape has no cluster specialisation
 bool launch_ks_cluster(const DevConsts* dc, const RnsParams& P, const u64* const* SRC, const u64* SRCC,
                        int src_poly, const u32* ginv, const u64* const* KEY, u64* ACC, int items, cudaStream_t st);
-// Hoisted rotations of shared sources (level 0): per source its c1 and KsY
-// factors; per rotation item the index of its source and its Galois element
+// Hoisted key switches of shared sources (level 0): every source polynomial
+// gets one ModUp + forward NTT (H); item i's accumulators are the sum over its
+// `nterm` terms t of H[hidx[i*nterm+t]] permuted by gel[...] (1: identity)
+// times key[i*nterm+t] (hidx < 0: no term)
 struct HoistedKs {
     int nsrc = 0;
-    const u64* const* src = nullptr;   // per source: the ciphertext (c1 = polynomial 1)
-    const u64* const* ysrc = nullptr;  // per source: ModUp factors y of c1 (KsY), nullable
-    const int* hidx = nullptr;         // per item: source index
-    const u32* gel = nullptr;          // per item: Galois element g
+    const u64* const* src = nullptr;   // per source: the ciphertext holding it
+    int src_poly = 1;                  // ... as polynomial src_poly of that ciphertext
+    const u64* const* ysrc = nullptr;  // per source: its ModUp factors y (KsY), nullable
+    int nterm = 1;
+    const int* hidx = nullptr;         // [item][nterm] source index
+    const u32* gel = nullptr;          // [item][nterm] Galois element
 };
+
 // A batched key switch in two phases, so that the accumulators of several key
 // switches can be summed before one shared INTT + ModDown (the plan's odd steps):
 // accumulate ACC[item] (phi_g(ModUp(SRC[item].c1)) x KEY[item]; hk: hoisted

@@ -819,6 +819,7 @@ int spmvgpu_plan_stats_get(const spmvgpu_plan* p, spmvgpu_plan_stats* o) {
         o->distinct_keys = s.distinct_keys;
         o->hbm_bytes_algorithmic = s.hbm_bytes;
         o->key_bytes_per_run = s.key_bytes;
+        o->relin_folded = s.relin_folded;
     });
 }
 int spmvgpu_plan_profile(spmvgpu_plan* p, spmvgpu_phase* phases, int cap, int* count) {

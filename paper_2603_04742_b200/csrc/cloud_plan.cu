@@ -110,10 +110,22 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
     std::stable_sort(order.begin(), order.end(),
                      [&](int x, int y) { return trees[x].dbl.size() > trees[y].dbl.size(); });
     const int depth = n ? (int)trees[order[0]].dbl.size() : 0;
+    int nd = 0;  // chunks with at least one doubling step: items 0 .. nd-1
+    while (nd < n && !trees[order[nd]].dbl.empty()) ++nd;
+    // Folded level 0 (fused fixed-shape key switch, hoisting on): the products
+    // of rotated chunks stay unrelinearised; level 0 hoists the ModUp + NTT of
+    // their z1 and z2 and sums, per doubling item, the relinearisation of z2
+    // and the rotations of z1 (key for phi_g(s)) and z2 (key for phi_g(s)^2)
+    // into one ModDown (the oracle restates it: plan fold with fold_relin = 1)
+    const bool fold = ctx.fused_key_switch() && fixed_rns_shape(P) && std::getenv("CSSC_NO_KSY") == nullptr &&
+                      std::getenv("CSSC_KS_CLUSTER") == nullptr && std::getenv("CSSC_NO_HOIST") == nullptr && nd > 0;
+    fold_ = fold;
+    nd_ = nd;
+    stats_.relin_folded = fold ? 1 : 0;
 
     arena_ = DevBuf(&ctx.pool(), 8 * ((size_t)(16 + 10 * std::max(depth, 1)) * std::max(n, 1) + 16 * n_odd +
                                       2 * (size_t)ns_ + 16) +
-                                     16 * (size_t)(16 * depth + 40));
+                                     16 * (size_t)(16 * depth + 40) + 8 * (6 * (size_t)n + 6 * n_odd));
     prod_ = DevBuf(&ctx.pool(), sizeof(u64) * ctw * std::max(n, 1));
     if (depth >= 1) acc0_ = DevBuf(&ctx.pool(), sizeof(u64) * ctw * n);
     if (depth >= 2) acc1_ = DevBuf(&ctx.pool(), sizeof(u64) * ctw * n);
@@ -122,7 +134,7 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
     Z_ = DevBuf(&ctx.pool(), sizeof(u64) * std::max<size_t>(1, n) * ctx.mul_Z_words());
     D2_ = DevBuf(&ctx.pool(), sizeof(u64) * std::max<size_t>(1, n) * ctx.poly_words());
     const size_t ks_items = std::max<size_t>(1, (size_t)n + n_odd);
-    DX_ = DevBuf(&ctx.pool(), sizeof(u64) * ks_items * ctx.dx_words());
+    DX_ = DevBuf(&ctx.pool(), sizeof(u64) * std::max(ks_items, fold ? 2 * (size_t)nd : 1) * ctx.dx_words());
     ACC_ = DevBuf(&ctx.pool(), sizeof(u64) * ks_items * ctx.ksacc_words());
     MT_ = DevBuf(&ctx.pool(), sizeof(u64) * std::max<size_t>(1, n) * ctw);
     // hoisted ModUp factors (KsY) of every ciphertext a key switch reads: the
@@ -198,15 +210,12 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
     };
     // level 0 rotates only products; with odd steps, several rotations share a
     // product: hoist its ModUp + forward NTT (CSSC_NO_HOIST=1 keeps per-item K1/K2)
-    const bool hoist0 = fused && !ksc && hoist && n_odd > 0 && std::getenv("CSSC_NO_HOIST") == nullptr;
     // Each odd step's key switch is summed into the doubling step it follows
     // (D_a, O_a share one INTT + ModDown; DESIGN 2.9, the oracle restates it):
     // level 0 accumulates every rotation of the products (doubling items
     // 0 .. nd-1, then the odd items: ACC[nd + o]), the odd items' c0 terms
     // phi_O(prod.c0) go to rp slot o (its c1 half stays zero) and are added as
     // EXTRA where their key switch is folded: level a-1 for O_a.
-    int nd = 0;
-    while (nd < n && !trees[order[nd]].dbl.empty()) ++nd;
     const size_t accw = ctx.ksacc_words();
     std::vector<std::map<int, int>> odd_after(n);  // k -> (a -> odd slot o)
     std::vector<const u64*> odd_src;
@@ -282,18 +291,43 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
             lv.odd_ginv = put(odd_gi);
             lv.odd_out = put(odd_out);
         }
-        // hoisting adds a launch: not for a handful of products (C1: +3 %, latency-bound)
-        if (l == 0 && hoist0 && nd >= 4) {
-            std::vector<const u64*> hp(nd), hy(nd);
+        if (l == 0 && fold) {
+            // sources: z1 of product k (c1 of its slot) -> H[k], z2 (D2) -> H[nd + k]
+            const size_t pw2 = ctx.poly_words();
+            std::vector<const u64*> hp(2 * nd), hy(2 * nd);
             for (int k = 0; k < nd; ++k) {
-                hp[k] = prod_at(k);
+                hp[k] = prod_at(k) + pw2;
                 hy[k] = prodY_at(k);
+                hp[nd + k] = D2_.words() + (size_t)k * pw2;
+                hy[nd + k] = D2Y_.words() + (size_t)k * pw2;
             }
-            lv.hsrc = nd;
+            constexpr int NT = 3;
+            std::vector<int> th((size_t)lv.acc_items * NT, -1);
+            std::vector<u32> tg((size_t)lv.acc_items * NT, 1u);
+            std::vector<const u64*> tk((size_t)lv.acc_items * NT, nullptr);
+            for (int i = 0; i < lv.acc_items; ++i) {
+                const int k = hidx[i];
+                const u32 g = gel[i];
+                if (i < tail) {  // doubling item: relinearisation of z2 + rot of z1 and z2
+                    th[i * NT + 0] = nd + k;
+                    tk[i * NT + 0] = ctx.relin_key();
+                }
+                th[i * NT + 1] = k;
+                tg[i * NT + 1] = g;
+                tk[i * NT + 1] = key[i];
+                th[i * NT + 2] = nd + k;
+                tg[i * NT + 2] = g;
+                tk[i * NT + 2] = ctx.galois_key_sq(g);
+            }
+            lv.hsrc = 2 * nd;
             lv.hprod = put(hp);
             lv.hy = put(hy);
-            lv.hidx = put(hidx);
-            lv.gel = put(gel);
+            lv.hterm = NT;
+            lv.hidx = put(th);
+            lv.gel = put(tg);
+            lv.hkey = put(tk);
+            stats_.key_bytes += lvl_keys.size() * KEY;  // the phi_g(s)^2 keys
+            stats_.hbm_bytes += lvl_keys.size() * KEY;
         }
         levels_.push_back(lv);
         const int srcs = lv.hsrc ? lv.hsrc : lv.acc_items;
@@ -373,7 +407,8 @@ void CloudPlan::record(std::vector<cudaEvent_t>* marks, u64* dec_d, const EncIn*
     };
     mark();
     ctx_.mul_relin_dev(A_, B_, PROD_, n_, T_.words(), Z_.words(), D2_.words(), DX_.words(),
-                       ACC_.words(), RLK_, enc, PRODY_ ? D2Y_.words() : nullptr, PRODY_);
+                       ACC_.words(), RLK_, enc, PRODY_ ? D2Y_.words() : nullptr, PRODY_, fold_ ? nd_ : 0,
+                       fold_ ? PRODY_ : nullptr);
     mark();
     const bool fused = ctx_.fused_key_switch();
     for (size_t l = 0; l < levels_.size(); ++l) {
@@ -384,12 +419,15 @@ void CloudPlan::record(std::vector<cudaEvent_t>* marks, u64* dec_d, const EncIn*
         if (lv.hsrc) {
             hk.nsrc = lv.hsrc;
             hk.src = lv.hprod;
+            hk.src_poly = 0;
             hk.ysrc = lv.hy;
+            hk.nterm = lv.hterm;
             hk.hidx = lv.hidx;
             hk.gel = lv.gel;
         }
-        const KsAccDomain dom = launch_ks_accumulate(ctx_.dconsts(), P, fused, lv.src, lv.ginv, lv.key, DX_.words(),
-                                                     ACC_.words(), lv.acc_items, st, ky, lv.hsrc ? &hk : nullptr);
+        const KsAccDomain dom = launch_ks_accumulate(ctx_.dconsts(), P, fused, lv.src, lv.ginv,
+                                                     lv.hsrc ? lv.hkey : lv.key, DX_.words(), ACC_.words(),
+                                                     lv.acc_items, st, ky, lv.hsrc ? &hk : nullptr);
         if (lv.odd_n) {
             launch_automorph_c0(ctx_.dconsts(), P, lv.odd_src, lv.odd_ginv, lv.odd_out, lv.odd_n, st);
             kmark("k_automorph_c0", st);

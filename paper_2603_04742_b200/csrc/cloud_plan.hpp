@@ -29,6 +29,7 @@ struct PlanStats {
     uint64_t chunks = 0, slices = 0, levels = 0, kernels = 0, limb_ntts = 0;
     uint64_t rotations = 0, distinct_keys = 0;
     uint64_t hbm_bytes = 0, key_bytes = 0;
+    uint64_t relin_folded = 0;  // 1: rotated chunks' relinearisation folded into level 0
 };
 
 // one launch group of the plan, timed by profile()
@@ -128,8 +129,10 @@ private:
         int hsrc = 0;                      // products (0: not hoisted)
         const u64* const* hprod = nullptr;  // per product: its ciphertext
         const u64* const* hy = nullptr;     // per product: KsY factors of c1
-        const int* hidx = nullptr;          // per item: product index
-        const u32* gel = nullptr;           // per item: Galois element
+        int hterm = 1;                      // MAC terms per item
+        const int* hidx = nullptr;          // [item][hterm] source index (-1: none)
+        const u32* gel = nullptr;           // [item][hterm] Galois element (1: identity)
+        const u64* const* hkey = nullptr;   // [item][hterm] switching key
         const u64* const* xacc = nullptr;   // per tail item: an odd step's accumulators (nullable)
         int odd_n = 0;                      // level 0: odd steps whose c0 term goes to rp slots
         const u64* const* odd_src = nullptr;
@@ -148,6 +151,8 @@ private:
     DevBuf pup_, pU_, pCM_, pX_, pM_, pslots_, pE_;  // pipeline workspaces
     DevBuf prodY_, accY0_, accY1_, D2Y_;            // hoisted ModUp factors (KsY)
     u64* const* PRODY_ = nullptr;
+    bool fold_ = false;  // relinearisation folded into level 0 (rotated chunks' products stay unrelinearised)
+    int nd_ = 0;         // chunks with at least one doubling step (items 0 .. nd_-1)
     cudaGraphExec_t pexec_ = nullptr, eexec_ = nullptr;
     cudaEvent_t ev_early_ = nullptr, ev_fork_ = nullptr;  // early graph on the side stream
     std::vector<cudaEvent_t> pmarks_;  // CSSC_PIPE_PROFILE=1: phase marks inside the pipeline graph

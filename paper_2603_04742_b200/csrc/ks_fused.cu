@@ -390,7 +390,7 @@ __global__ void __launch_bounds__(kKsGroups * kKsGroupThreads) k_ks_blocks_gathe
                                                                                 const u64* __restrict__ H,
                                                                                 const int* __restrict__ HIDX,
                                                                                 const u32* __restrict__ GEL,
-                                                                                const u64* const* KEY,
+                                                                                const u64* const* KEY, int nterm,
                                                                                 u64* __restrict__ ACC) {
     using G = Ntt2<LOGN>;
     extern __shared__ u64 smem[];
@@ -414,30 +414,40 @@ __global__ void __launch_bounds__(kKsGroups * kKsGroupThreads) k_ks_blocks_gathe
     const u64 q = md.q;
     const int blk0 = tileid * LN;
     const size_t base = (size_t)blk0 * G::R2;
-    const u64* key = KEY[item];
     const size_t PL = (size_t)LK * G::N;
     const size_t KW = (size_t)dnum * 2 * PL;  // key words; their Shoup companions follow
-    const u64* h = H + (size_t)HIDX[item] * dnum * PL + (size_t)j * G::N;
-    const u32 g = GEL[item];
     const int grp = threadIdx.x / kKsGroupThreads;
     const ThreadGroup tg = cta_slice(grp, kKsGroups);
     auto saddr = [](int x) { return (x >> G::B) * PITCH + (x & (G::R2 - 1)); };
     auto addr = [](int l, int pos) { return l * PITCH + pos; };
     auto twf = [&](int sl, int l, int blk) { return block_tw<LOGN, LN>(tws, sl, l, blk); };
     load_block_twiddles<LOGN, LN>(tws, dc->tw[j].inv, blk0);
+    u64 a0[PER], a1[PER];
+#pragma unroll
+    for (int r = 0; r < PER; ++r) a0[r] = a1[r] = 0;
+    for (int t = 0; t < nterm; ++t) {
+        const int hi = HIDX[item * nterm + t];
+        if (hi < 0) continue;
+        const u64* h = H + (size_t)hi * dnum * PL + (size_t)j * G::N;
+        const u32 g = GEL[item * nterm + t];
+        const u64* key = KEY[item * nterm + t];
+#pragma unroll
+        for (int r = 0; r < PER; ++r) {
+            const int x = threadIdx.x + T * r;
+            const int src = ntt_perm<LOGN>(g, (int)base + x);
+            for (int dg = 0; dg < dnum; ++dg) {
+                const u64 w = __ldg(h + (size_t)dg * PL + src);
+                const size_t ko = ((size_t)dg * 2) * PL + (size_t)j * G::N + base + x;
+                a0[r] = add_mod(a0[r], shoup(w, __ldg(key + ko), __ldg(key + KW + ko), q), q);
+                a1[r] = add_mod(a1[r], shoup(w, __ldg(key + ko + PL), __ldg(key + KW + ko + PL), q), q);
+            }
+        }
+    }
 #pragma unroll
     for (int r = 0; r < PER; ++r) {
-        const int x = threadIdx.x + T * r, s0 = saddr(x);
-        const int src = ntt_perm<LOGN>(g, (int)base + x);
-        u64 a0 = 0, a1 = 0;
-        for (int dg = 0; dg < dnum; ++dg) {
-            const u64 w = __ldg(h + (size_t)dg * PL + src);
-            const size_t ko = ((size_t)dg * 2) * PL + (size_t)j * G::N + base + x;
-            a0 = add_mod(a0, shoup(w, __ldg(key + ko), __ldg(key + KW + ko), q), q);
-            a1 = add_mod(a1, shoup(w, __ldg(key + ko + PL), __ldg(key + KW + ko + PL), q), q);
-        }
-        work[s0] = a0;
-        work[TW + s0] = a1;
+        const int s0 = saddr(threadIdx.x + T * r);
+        work[s0] = a0[r];
+        work[TW + s0] = a1[r];
     }
     cp_async_wait_all();
     __syncthreads();
@@ -598,7 +608,7 @@ static void ks_hoisted_acc_t(const DevConsts* dc, const RnsParams& P, const Hois
     const int LK = P.cfg.L + P.cfg.K, dnum = P.dnum;
     KsY ky;
     ky.src = hk.ysrc;
-    launch_k1<LOGN, LT, KT, AT>(dc, P, hk.src, nullptr, 1, nullptr, DX, hk.nsrc, st, ky);
+    launch_k1<LOGN, LT, KT, AT>(dc, P, hk.src, nullptr, hk.src_poly, nullptr, DX, hk.nsrc, st, ky);
     NttJob jb;
     for (int i = 0; i < MAX_JOB_LIMBS; ++i) jb.pidx[i] = (signed char)(i % LK);
     jb.src = DX;
@@ -611,12 +621,12 @@ static void ks_hoisted_acc_t(const DevConsts* dc, const RnsParams& P, const Hois
         const int sm = (2 * 8 * G::PITCH + 2 * btw_entries<LOGN, 8>()) * 8;
         smem_optin_k(k_ks_blocks_gather<LOGN, LT, KT, AT, 8>, sm);
         k_ks_blocks_gather<LOGN, LT, KT, AT, 8><<<items * LK * (G::R1 / 8), T2, sm, st>>>(dc, DX, hk.hidx, hk.gel,
-                                                                                        KEY, ACC);
+                                                                                        KEY, hk.nterm, ACC);
     } else {
         const int sm = (2 * G::LINES * G::PITCH + 2 * G::TWB) * 8;
         smem_optin_k(k_ks_blocks_gather<LOGN, LT, KT, AT>, sm);
         k_ks_blocks_gather<LOGN, LT, KT, AT><<<items * LK * G::CTAS_B, T2, sm, st>>>(dc, DX, hk.hidx, hk.gel, KEY,
-                                                                                     ACC);
+                                                                                     hk.nterm, ACC);
     }
     KS_CHECK();
     kmark("k_ks_blocks_gather (K2h)", st);

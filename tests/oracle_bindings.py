@@ -72,6 +72,7 @@ def oracle_lib():
         L.bfvo_plan_fold.restype = C.c_int
         L.bfvo_plan_fold.argtypes = [C.c_void_p, u64p, C.c_int, i64p, ip, C.c_int, u64p]
         L.bfvo_get_ksk_sq.argtypes = [C.c_void_p, C.c_uint32, u64p]
+        L.bfvo_add_galois_key_sq.argtypes = [C.c_void_p, C.c_uint32]
         L.bfvo_mul_relin_z.argtypes = [C.c_void_p, u64p, u64p]
         L.bfvo_rotate2_add.argtypes = [C.c_void_p, u64p, u64p, C.c_int64, C.c_int64, u64p]
         L.bfvo_key_switch.argtypes = [C.c_void_p, C.c_uint32, u64p, u64p, u64p]

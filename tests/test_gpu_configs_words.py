@@ -63,17 +63,20 @@ def test_config_result_words_match_oracle(cfgno):
     sa = [10_000 + i for i in range(n)]
     sb = [20_000 + i for i in range(n)]
     ha, hb = ctx.encrypt(va, sa), ctx.encrypt(vb, sb)
-    out = pk.cloud_plan(ctx, r_list, c_list, slice_of, n_slices, ha, hb, graph=True)
+    st = {}
+    out = pk.cloud_plan(ctx, r_list, c_list, slice_of, n_slices, ha, hb, graph=True, stats=st)
     # Galois keys first (the only oracle state a rotation mutates), then the
     # independent per-chunk chains on all host cores (ctypes drops the GIL)
     scheds = [pk.rotation_schedule(r_list[i], c_list[i]) for i in range(n)]
     for g in sorted({orc.galois_elt(off) for sc in scheds for off, _ in sc}):
         if g != 1:
             orc.lib.bfvo_add_galois_key(orc.h, g)
+            if st["relin_folded"]:
+                orc.lib.bfvo_add_galois_key_sq(orc.h, g)
 
     def chain(i):
-        prod = orc.mul_relin(orc.encrypt(va[i], sa[i]), orc.encrypt(vb[i], sb[i]))
-        acc = orc.plan_fold(prod, scheds[i])
+        z = orc.mul_tensor(orc.encrypt(va[i], sa[i]), orc.encrypt(vb[i], sb[i]))
+        acc = orc.plan_fold_z(z, scheds[i], st["relin_folded"])
         return orc.mul_plain(acc, np.ones(r_list[i], np.int64))
 
     with ThreadPoolExecutor(max_workers=os.cpu_count() or 1) as ex:

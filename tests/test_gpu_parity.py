@@ -141,11 +141,14 @@ def test_cloud_plan_words_match_oracle(graph, shape):
     sa = [1000 + i for i in range(len(shapes))]
     sb = [2000 + i for i in range(len(shapes))]
     ha, hb = ctx.encrypt(vals_a, sa), ctx.encrypt(vals_b, sb)
-    out = pk.cloud_plan(ctx, [r for r, _ in shapes], [c for _, c in shapes], slices, 3, ha, hb, graph=graph)
+    st = {}
+    out = pk.cloud_plan(ctx, [r for r, _ in shapes], [c for _, c in shapes], slices, 3, ha, hb, graph=graph,
+                        stats=st)
+    assert st["relin_folded"] == (1 if shape == 0 else 0)
     want = [None] * 3
     for i, (r, c) in enumerate(shapes):
-        prod = orc.mul_relin(orc.encrypt(vals_a[i], sa[i]), orc.encrypt(vals_b[i], sb[i]))
-        acc = orc.plan_fold(prod, pk.rotation_schedule(r, c))
+        z = orc.mul_tensor(orc.encrypt(vals_a[i], sa[i]), orc.encrypt(vals_b[i], sb[i]))
+        acc = orc.plan_fold_z(z, pk.rotation_schedule(r, c), st["relin_folded"])
         part = orc.mul_plain(acc, np.ones(r, np.int64))
         want[slices[i]] = part if want[slices[i]] is None else orc.add(want[slices[i]], part)
     for s in range(3):
@@ -155,8 +158,9 @@ def test_cloud_plan_words_match_oracle(graph, shape):
 
 def test_cloud_plan_fused_and_unfused_agree():
     """The fused plan (fused multiply, K1/K2 key switch, block-phase mask
-    accumulation, small-launch tiles) and the launch-per-op pipeline give the
-    same result words."""
+    accumulation, small-launch tiles, folded level 0) and the launch-per-op
+    pipeline (relinearise first) each equal the oracle's plan of their form
+    word for word and decrypt to the same slots."""
     shapes = [(7, 13), (3, 6), (5, 7), (11, 2), (1, 64), (2, 1)]
     slices = [0, 0, 1, 1, 1, 0]
     rng = np.random.default_rng(9)
@@ -165,34 +169,61 @@ def test_cloud_plan_fused_and_unfused_agree():
     outs = {}
     for fused in (1, 0):
         ctx = pk.Context(logn=11, seed=4)
+        orc = BfvOracle.like(ctx)
         ctx.set_option("fused_key_switch", fused)
-        ha = ctx.encrypt(va, [300 + i for i in range(len(shapes))])
-        hb = ctx.encrypt(vb, [400 + i for i in range(len(shapes))])
-        out = pk.cloud_plan(ctx, [r for r, _ in shapes], [c for _, c in shapes], slices, 2, ha, hb, graph=True)
-        outs[fused] = [ctx.download(int(h)) for h in out]
+        sa, sb = [300 + i for i in range(len(shapes))], [400 + i for i in range(len(shapes))]
+        ha, hb = ctx.encrypt(va, sa), ctx.encrypt(vb, sb)
+        st = {}
+        out = pk.cloud_plan(ctx, [r for r, _ in shapes], [c for _, c in shapes], slices, 2, ha, hb, graph=True,
+                            stats=st)
+        assert st["relin_folded"] == fused
+        got = [ctx.download(int(h)) for h in out]
+        want = [None] * 2
+        for i, (r, c) in enumerate(shapes):
+            z = orc.mul_tensor(orc.encrypt(va[i], sa[i]), orc.encrypt(vb[i], sb[i]))
+            part = orc.mul_plain(orc.plan_fold_z(z, pk.rotation_schedule(r, c), fused), np.ones(r, np.int64))
+            want[slices[i]] = part if want[slices[i]] is None else orc.add(want[slices[i]], part)
+        assert all(np.array_equal(g, w) for g, w in zip(got, want))
+        outs[fused] = [orc.decrypt(g)[0] for g in got]
         ctx.close()
     for a, b in zip(outs[0], outs[1]):
         assert np.array_equal(a, b)
 
 
-def test_hoisted_level0_matches_unhoisted(monkeypatch):
-    """Level 0 with shared ModUp (hoisted rotations of each product, K2h's
-    NTT-domain gather) and the per-rotation K1/K2 give the same words."""
-    shapes = [(7, 13), (3, 6), (5, 7), (11, 2), (1, 64), (40, 12), (8, 3)]
-    slices = [0, 0, 1, 1, 1, 0, 1]
+def test_folded_level0_matches_oracle_and_unfolded_values(monkeypatch):
+    """Level 0 folded (products unrelinearised; hoisted ModUp + NTT of z1 and
+    z2; relinearisation, rotations of z1 / z2 and the odd steps in one ModDown
+    per doubling item) equals the oracle's folded plan word for word, and the
+    unfolded plan (CSSC_NO_HOIST=1: relinearise, then per-rotation K1/K2)
+    equals the oracle's unfolded plan; both decrypt to the same slots."""
+    shapes = [(7, 13), (3, 6), (5, 7), (11, 2), (1, 64), (40, 12), (8, 3), (2, 1)]
+    slices = [0, 0, 1, 1, 1, 0, 1, 0]
     rng = np.random.default_rng(17)
     va = [rng.integers(-8, 9, r * c) for r, c in shapes]
     vb = [rng.integers(-8, 9, r * c) for r, c in shapes]
-    outs = {}
+    dec = {}
     for off in ("", "1"):
         if off:
             monkeypatch.setenv("CSSC_NO_HOIST", off)
         else:
             monkeypatch.delenv("CSSC_NO_HOIST", raising=False)
         ctx = pk.Context(logn=12, seed=8)
-        ha = ctx.encrypt(va, [500 + i for i in range(len(shapes))])
-        hb = ctx.encrypt(vb, [600 + i for i in range(len(shapes))])
-        out = pk.cloud_plan(ctx, [r for r, _ in shapes], [c for _, c in shapes], slices, 2, ha, hb, graph=True)
-        outs[off] = [ctx.download(int(h)) for h in out]
+        orc = BfvOracle.like(ctx)
+        sa, sb = [500 + i for i in range(len(shapes))], [600 + i for i in range(len(shapes))]
+        ha, hb = ctx.encrypt(va, sa), ctx.encrypt(vb, sb)
+        st = {}
+        out = pk.cloud_plan(ctx, [r for r, _ in shapes], [c for _, c in shapes], slices, 2, ha, hb, graph=True,
+                            stats=st)
+        assert st["relin_folded"] == (0 if off else 1)
+        want = [None] * 2
+        for i, (r, c) in enumerate(shapes):
+            z = orc.mul_tensor(orc.encrypt(va[i], sa[i]), orc.encrypt(vb[i], sb[i]))
+            part = orc.mul_plain(orc.plan_fold_z(z, pk.rotation_schedule(r, c), st["relin_folded"]),
+                                 np.ones(r, np.int64))
+            want[slices[i]] = part if want[slices[i]] is None else orc.add(want[slices[i]], part)
+        got = [ctx.download(int(h)) for h in out]
+        for s_ in range(2):
+            assert np.array_equal(got[s_], want[s_]), (off, s_)
+        dec[off] = [orc.decrypt(g)[0] for g in got]
         ctx.close()
-    assert all(np.array_equal(x, y) for x, y in zip(outs[""], outs["1"]))
+    assert all(np.array_equal(x, y) for x, y in zip(dec[""], dec["1"]))
