@@ -342,7 +342,7 @@ DOT = 0.375
 
 
 def kernel_units(name: str, items: int, slices: int, logn: int, L: int, K: int, dnum: int, alpha: int,
-                 sources: int | None = None, acc_items: int | None = None) -> float:
+                 sources: int | None = None, acc_items: int | None = None, mac_terms: int | None = None) -> float:
     """modmul-equivalents of one launch; `sources` = the distinct key-switch
     sources of a level (hoisted: its K1 and forward block phase run once per
     source), `acc_items` = its accumulated key switches (K2 / K2h; the odd steps
@@ -374,6 +374,7 @@ def kernel_units(name: str, items: int, slices: int, logn: int, L: int, K: int, 
         return items * 3 * n * (e8 if overq else e2 + e1_b2q)
     acc = items if acc_items is None else acc_items
     src = acc if sources is None else sources
+    tail = min(items, acc)  # INTT + ModDown runs per doubling item (the relinearised products in the multiply group)
     if name.startswith("k_ks_modup_cols"):
         return src * dnum * LK * (n * alpha + h * As)
     if name.startswith("k_ks_blocks_inner"):
@@ -381,13 +382,14 @@ def kernel_units(name: str, items: int, slices: int, logn: int, L: int, K: int, 
     if name.startswith("k_ntt_blocks fwd (hoisted"):
         return src * dnum * LK * h * Bs
     if name.startswith("k_ks_blocks_gather"):
-        return acc * LK * (2 * dnum * n + 2 * h * Bs)
+        terms = acc if mac_terms is None else mac_terms
+        return LK * (terms * 2 * dnum * n + acc * 2 * h * Bs)
     if name.startswith("k_ntt_cols inv (key switch)"):
-        return items * 2 * LK * h * As
+        return tail * 2 * LK * h * As
     if name.startswith("k_ks_cols_moddown"):  # inverse column phase + ModDown in one launch
-        return items * 2 * LK * h * As + items * 2 * n * (K + L * (K + 1) * DOT)
+        return tail * 2 * LK * h * As + tail * 2 * n * (K + L * (K + 1) * DOT)
     if name.startswith("k_ks_moddown"):
-        return items * 2 * n * (K + L * (K + 1) * DOT)
+        return tail * 2 * n * (K + L * (K + 1) * DOT)
     if name.startswith("k_ntt_cols fwd (mask)"):
         return items * 2 * L * h * As
     if name.startswith("k_mask_blocks"):
@@ -405,7 +407,8 @@ def kernel_table(job, groups, st, logn, p, bfly_peak, reps=3):
     for k in ks:
         g = groups[k["group"]] if k["group"] < len(groups) else {"items": 0, "name": "?"}
         units = kernel_units(k["name"], g["items"], st["slices"], logn, p.L, p.K,
-                             (p.L + p.alpha - 1) // p.alpha, p.alpha, g.get("sources"), g.get("acc_items"))
+                             (p.L + p.alpha - 1) // p.alpha, p.alpha, g.get("sources"), g.get("acc_items"),
+                             g.get("mac_terms"))
         rate = units / (k["us"] * 1e-6) if k["us"] > 0 else 0.0
         rows.append({"kernel": k["name"], "group": g["name"], "items": g["items"], "us": round(k["us"], 2),
                      "units": int(units), "g_units_s": round(rate / 1e9, 1),

@@ -191,6 +191,7 @@ typedef struct {
     uint64_t items, bytes, limb_ntts;
     uint64_t sources;   /* distinct key-switch sources (< items when a level's ModUp is hoisted) */
     uint64_t acc_items; /* key switches accumulated (> items: odd steps share their doubling step's ModDown) */
+    uint64_t mac_terms; /* key products summed (folded level 0: relinearisation + rotations of z1 and z2) */
 } spmvgpu_phase;
 int spmvgpu_plan_profile(spmvgpu_plan* p, spmvgpu_phase* phases, int cap, int* count);
 /* per kernel launch of the plan: `reps` graph replays, each after an L2 flush

@@ -60,7 +60,7 @@ class Message(C.Structure):
 class PhaseC(C.Structure):
     _fields_ = [("name", C.c_char * 32), ("us", C.c_double), ("items", C.c_uint64), ("bytes", C.c_uint64),
                 ("limb_ntts", C.c_uint64), ("sources", C.c_uint64),
-                ("acc_items", C.c_uint64)]
+                ("acc_items", C.c_uint64), ("mac_terms", C.c_uint64)]
 
 
 class KernelTimingC(C.Structure):
@@ -772,7 +772,7 @@ class Job:
         check(lib().cssc_job_profile(self.h, ph, cap, C.byref(cnt)))
         return [{"name": p.name.decode(), "us": p.us, "items": int(p.items), "bytes": int(p.bytes),
                  "limb_ntts": int(p.limb_ntts), "sources": int(p.sources),
-                 "acc_items": int(p.acc_items)} for p in ph[: min(cnt.value, cap)]]
+                 "acc_items": int(p.acc_items), "mac_terms": int(p.mac_terms)} for p in ph[: min(cnt.value, cap)]]
 
     def profile_kernels(self, reps: int = 5, flush_bytes: int = 256 << 20) -> list:
         """Mean device time of every kernel launch of the cloud phase over `reps`

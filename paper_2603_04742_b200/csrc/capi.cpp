@@ -836,6 +836,7 @@ int spmvgpu_plan_profile(spmvgpu_plan* p, spmvgpu_phase* phases, int cap, int* c
             phases[i].limb_ntts = ph[i].limb_ntts;
             phases[i].sources = ph[i].sources;
             phases[i].acc_items = ph[i].acc_items;
+            phases[i].mac_terms = ph[i].mac_terms;
         }
     });
 }

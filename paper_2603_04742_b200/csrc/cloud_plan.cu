@@ -274,6 +274,7 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
         Level lv;
         lv.items = tail;
         lv.acc_items = (int)src.size();
+        lv.mac_terms = lv.acc_items;
         lv.src = put(src);
         lv.base = put(base);
         lv.out = put(o);
@@ -319,6 +320,8 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
                 tg[i * NT + 2] = g;
                 tk[i * NT + 2] = ctx.galois_key_sq(g);
             }
+            lv.mac_terms = 0;
+            for (int x : th) lv.mac_terms += x >= 0 ? 1 : 0;
             lv.hsrc = 2 * nd;
             lv.hprod = put(hp);
             lv.hy = put(hy);
@@ -474,16 +477,19 @@ std::vector<PhaseTiming> CloudPlan::profile() {
               KEY = sizeof(u64) * ctx_.ksk_words() * (ctx_.fused_key_switch() ? 2 : 1),
               PT = sizeof(u64) * ctx_.poly_words();
     const u64 ks_ntts = (u64)P.dnum * LK + 2 * LK;
-    out.push_back({"multiply+relin", 0, (u64)n_, (u64)n_ * 3 * C + KEY, (u64)n_ * (7 * M + ks_ntts), (u64)n_, (u64)n_});
+    const u64 nrel = (u64)(n_ - (fold_ ? nd_ : 0));  // relinearised products (the rest fold into level 0)
+    out.push_back({"multiply+relin", 0, (u64)n_, (u64)n_ * 3 * C + (nrel ? KEY : 0), (u64)n_ * 7 * M + nrel * ks_ntts,
+                   nrel, nrel, nrel});
     for (size_t l = 0; l < levels_.size(); ++l) {
         const Level& lv = levels_[l];
         const u64 srcs = lv.hsrc ? (u64)lv.hsrc : (u64)lv.acc_items;
         out.push_back({"rotate level " + std::to_string(l), 0, (u64)lv.items,
                        (u64)lv.acc_items * 3 * C + (u64)lv.keys * KEY,
-                       srcs * P.dnum * LK + (u64)lv.items * 2 * LK, srcs, (u64)lv.acc_items});
+                       srcs * P.dnum * LK + (u64)lv.items * 2 * LK, srcs, (u64)lv.acc_items,
+                       (u64)lv.mac_terms});
     }
     out.push_back({"mask accumulate", 0, (u64)n_, (u64)n_ * 2 * C + (u64)n_masks_ * PT,
-                   (u64)n_ * 2 * L + (u64)ns_ * 2 * L, (u64)n_, (u64)n_});
+                   (u64)n_ * 2 * L + (u64)ns_ * 2 * L, (u64)n_, (u64)n_, 0});
     // captured like run(), with event-record nodes between the groups, so the
     // timings include the graph's (small) inter-kernel gaps and nothing else
     std::vector<cudaEvent_t> marks;

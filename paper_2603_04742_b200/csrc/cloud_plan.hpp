@@ -39,6 +39,7 @@ struct PhaseTiming {
     uint64_t items = 0, bytes = 0, limb_ntts = 0;  // compulsory HBM bytes, limb NTTs
     uint64_t sources = 0;    // distinct key-switch sources (hoisted level 0: the products)
     uint64_t acc_items = 0;  // key switches accumulated (odd steps fold into their doubling step's ModDown)
+    uint64_t mac_terms = 0;  // key products summed (folded level 0: relin + z1 and z2 rotations)
 };
 
 // one kernel launch of the plan, timed by profile_kernels()
@@ -130,6 +131,7 @@ private:
         const u64* const* hprod = nullptr;  // per product: its ciphertext
         const u64* const* hy = nullptr;     // per product: KsY factors of c1
         int hterm = 1;                      // MAC terms per item
+        int mac_terms = 0;                  // key products summed over the level's items
         const int* hidx = nullptr;          // [item][hterm] source index (-1: none)
         const u32* gel = nullptr;           // [item][hterm] Galois element (1: identity)
         const u64* const* hkey = nullptr;   // [item][hterm] switching key
