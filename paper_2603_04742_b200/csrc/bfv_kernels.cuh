@@ -264,6 +264,7 @@ struct HoistedKs {
     int nterm = 1;
     const int* hidx = nullptr;         // [item][nterm] source index
     const u32* gel = nullptr;          // [item][nterm] Galois element
+    const int* order = nullptr;        // launch order of the items (nullable)
 };
 
 // A batched key switch in two phases, so that the accumulators of several key

@@ -322,6 +322,13 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
             }
             lv.mac_terms = 0;
             for (int x : th) lv.mac_terms += x >= 0 ? 1 : 0;
+            // launch order: by the rotation's Galois element, so the items that share
+            // its two keys run back to back and read them from L2
+            std::vector<int> ord(lv.acc_items);
+            std::iota(ord.begin(), ord.end(), 0);
+            if (std::getenv("CSSC_NO_KEY_ORDER") == nullptr)
+                std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return gel[x] < gel[y]; });
+            lv.horder = put(ord);
             lv.hsrc = 2 * nd;
             lv.hprod = put(hp);
             lv.hy = put(hy);
@@ -427,6 +434,7 @@ void CloudPlan::record(std::vector<cudaEvent_t>* marks, u64* dec_d, const EncIn*
             hk.nterm = lv.hterm;
             hk.hidx = lv.hidx;
             hk.gel = lv.gel;
+            hk.order = lv.horder;
         }
         const KsAccDomain dom = launch_ks_accumulate(ctx_.dconsts(), P, fused, lv.src, lv.ginv,
                                                      lv.hsrc ? lv.hkey : lv.key, DX_.words(), ACC_.words(),

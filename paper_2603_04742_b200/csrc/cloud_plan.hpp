@@ -135,6 +135,7 @@ private:
         const int* hidx = nullptr;          // [item][hterm] source index (-1: none)
         const u32* gel = nullptr;           // [item][hterm] Galois element (1: identity)
         const u64* const* hkey = nullptr;   // [item][hterm] switching key
+        const int* horder = nullptr;        // K2h launch order (by Galois element)
         const u64* const* xacc = nullptr;   // per tail item: an odd step's accumulators (nullable)
         int odd_n = 0;                      // level 0: odd steps whose c0 term goes to rp slots
         const u64* const* odd_src = nullptr;

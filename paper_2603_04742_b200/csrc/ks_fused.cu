@@ -391,6 +391,7 @@ __global__ void __launch_bounds__(kKsGroups * kKsGroupThreads) k_ks_blocks_gathe
                                                                                 const int* __restrict__ HIDX,
                                                                                 const u32* __restrict__ GEL,
                                                                                 const u64* const* KEY, int nterm,
+                                                                                const int* __restrict__ ORDER,
                                                                                 u64* __restrict__ ACC) {
     using G = Ntt2<LOGN>;
     extern __shared__ u64 smem[];
@@ -409,7 +410,8 @@ __global__ void __launch_bounds__(kKsGroups * kKsGroupThreads) k_ks_blocks_gathe
     const int tileid = bid % CTAS;
     bid /= CTAS;
     const int j = bid % LK;
-    const int item = bid / LK;
+    // ORDER: items sharing switching keys run back to back (the keys stay in L2)
+    const int item = ORDER ? ORDER[bid / LK] : bid / LK;
     const Modulus md = dc->mod[j];
     const u64 q = md.q;
     const int blk0 = tileid * LN;
@@ -621,12 +623,12 @@ static void ks_hoisted_acc_t(const DevConsts* dc, const RnsParams& P, const Hois
         const int sm = (2 * 8 * G::PITCH + 2 * btw_entries<LOGN, 8>()) * 8;
         smem_optin_k(k_ks_blocks_gather<LOGN, LT, KT, AT, 8>, sm);
         k_ks_blocks_gather<LOGN, LT, KT, AT, 8><<<items * LK * (G::R1 / 8), T2, sm, st>>>(dc, DX, hk.hidx, hk.gel,
-                                                                                        KEY, hk.nterm, ACC);
+                                                                                        KEY, hk.nterm, hk.order, ACC);
     } else {
         const int sm = (2 * G::LINES * G::PITCH + 2 * G::TWB) * 8;
         smem_optin_k(k_ks_blocks_gather<LOGN, LT, KT, AT>, sm);
         k_ks_blocks_gather<LOGN, LT, KT, AT><<<items * LK * G::CTAS_B, T2, sm, st>>>(dc, DX, hk.hidx, hk.gel, KEY,
-                                                                                     hk.nterm, ACC);
+                                                                                     hk.nterm, hk.order, ACC);
     }
     KS_CHECK();
     kmark("k_ks_blocks_gather (K2h)", st);
