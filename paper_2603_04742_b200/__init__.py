@@ -596,7 +596,7 @@ def _outputs(ms, keep: list):
     rows = [int(m.rows) for m in ms]
     off = np.zeros(len(rows) + 1, np.int64)
     off[1:] = np.cumsum([max(r, 1) for r in rows])
-    buf = np.zeros(int(off[-1]) or 1, np.int64)
+    buf = np.empty(int(off[-1]) or 1, np.int64)  # the library writes every row of every matrix
     ptrs = (off[:-1] * 8 + _addr(buf)).astype(np.uint64) if rows else np.zeros(1, np.uint64)
     res = np.zeros(max(len(rows), 1), _RES_DT)
     keep += (buf, ptrs, res)
