@@ -199,6 +199,12 @@ void GpuContext::keygen() {
     launch_ntt(dc_, logn, false, job(E.words(), E.words(), L, range_idx(0, L)), 1, st_);
     launch_key_combine(dc_, logn, L, pk1, E.words(), s_ntt_.words(), nullptr, 0, 0, pk0, st_);
 
+    // Shoup companions of the fixed multipliers of encryption (pk) and decryption (s)
+    pk_sh_ = DevBuf(&pool_, sizeof(u64) * 2 * (size_t)L * n);
+    launch_shoup_companions(dc_, pk_.words(), pk_sh_.words(), L, n, 2, st_);
+    s_sh_ = DevBuf(&pool_, sizeof(u64) * (size_t)L * n);
+    launch_shoup_companions(dc_, s_ntt_.words(), s_sh_.words(), L, n, 1, st_);
+
     // relinearisation key: target s^2
     DevBuf s2(&pool_, sizeof(u64) * (size_t)LK * n);
     launch_square(dc_, logn, LK, s_ntt_.words(), s2.words(), st_);
@@ -465,7 +471,8 @@ void GpuContext::encrypt_cssc_forked(const unsigned char* img, const CsscLayout&
         if (part == 1 && ws.E) cuda_check(cudaEventRecord(ev_upload_, st_), "ids uploaded");
         launch_enc_sample_u(dc_, P_, P_.cfg.key, streams, ws.U, items, st_);
         launch_ntt_phase(dc_, logn, false, true, job(ws.U, ws.U, L, range_idx(0, L)), items, st_);
-        launch_blocks_mul_inv(dc_, P_, ws.U, pk_.words(), 2, CM, (size_t)2 * L * n, nullptr, 0, 0, items, st_);
+        launch_blocks_mul_inv(dc_, P_, ws.U, pk_.words(), 2, CM, (size_t)2 * L * n, nullptr, 0, 0, items, st_,
+                              pk_sh_.words());
         std::vector<int> pidx = range_idx(0, L);
         pidx.insert(pidx.end(), pidx.begin(), pidx.end());
         launch_ntt_phase(dc_, logn, true, true, job(CM, CM, 2 * L, pidx), items, st_);
@@ -526,7 +533,8 @@ void GpuContext::encrypt_encoded(const u64* d_streams, u64* const* d_out, int it
     pidx.push_back(P_.t_index());
     if (fused_ks_) {  // NTT(u) column phase; block phase x pk + inverse block phase (+ message); columns
         launch_ntt_phase(dc_, logn, false, true, job(U, U, L, range_idx(0, L)), items, st_);
-        launch_blocks_mul_inv(dc_, P_, U, pk_.words(), 2, CM, cm_stride(), CM, 2 * L, P_.t_index(), items, st_);
+        launch_blocks_mul_inv(dc_, P_, U, pk_.words(), 2, CM, cm_stride(), CM, 2 * L, P_.t_index(), items, st_,
+                              pk_sh_.words());
         launch_ntt_phase(dc_, logn, true, true, job(CM, CM, 2 * L + 1, pidx), items, st_);
         stats_.kernels += 5;
     } else {
@@ -583,7 +591,8 @@ void GpuContext::decrypt_dev(const u64* const* dct, int items, u64* X, u64* M, u
     j.src_limb_offset = L;
     if (fused_ks_) {  // column phase of c1; block phase x s + inverse block phase; inverse columns
         launch_ntt_phase(dc_, logn, false, true, j, items, st_);
-        launch_blocks_mul_inv(dc_, P_, X, s_ntt_.words(), 1, X, (size_t)L * n, nullptr, 0, 0, items, st_);
+        launch_blocks_mul_inv(dc_, P_, X, s_ntt_.words(), 1, X, (size_t)L * n, nullptr, 0, 0, items, st_,
+                              s_sh_.words());
         launch_ntt_phase(dc_, logn, true, true, job(X, X, L, range_idx(0, L)), items, st_);
     } else {
         launch_ntt(dc_, logn, false, j, items, st_);

@@ -235,6 +235,7 @@ private:
     DevBuf pos0_;
     DevBuf s_small_, s_ntt_, pk_, rlk_;
     std::map<u32, DevBuf> gk_, gk2_;
+    DevBuf pk_sh_, s_sh_;  // Shoup companions of pk and of s's Q limbs
     std::atomic<uint64_t> stream_counter_{1};
     LaunchStats stats_;
     bool fused_ks_ = true;

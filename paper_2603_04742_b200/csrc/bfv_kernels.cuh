@@ -126,7 +126,7 @@ void launch_mask_blocks(const DevConsts* dc, const RnsParams& P, const u64* MT, 
 // limb run through the inverse block phase in place (prime index xprime)
 void launch_blocks_mul_inv(const DevConsts* dc, const RnsParams& P, const u64* IN, const u64* MUL, int nmul,
                            u64* OUT, size_t out_stride, u64* XTRA, int xlimb, int xprime, int items,
-                           cudaStream_t st);
+                           cudaStream_t st, const u64* MULSH = nullptr);
 // fused forward block phase + tensor + inverse block phase (mul_fused.cu)
 void launch_mul_blocks_tensor(const DevConsts* dc, const RnsParams& P, const u64* T, u64* Z, int items,
                               cudaStream_t st);

@@ -383,7 +383,7 @@ __global__ void __launch_bounds__(mulb_threads<LOGN>()) k_blocks_mul_inv(const D
                                                                          const u64* __restrict__ MUL,
                                                                          u64* __restrict__ OUT, size_t out_stride,
                                                                          u64* __restrict__ XTRA, int xlimb,
-                                                                         int xprime) {
+                                                                         int xprime, const u64* __restrict__ MULSH) {
     using G = Ntt2<LOGN>;
     extern __shared__ u64 smem[];
     constexpr int PITCH = G::PITCH;
@@ -439,8 +439,11 @@ __global__ void __launch_bounds__(mulb_threads<LOGN>()) k_blocks_mul_inv(const D
         const int y = threadIdx.x + NT * r, s0 = saddr(y);
         const u64 w = tile[s0];  // lazy (< 31q) x canonical multiplier
 #pragma unroll
-        for (int p = 0; p < NMUL; ++p)
-            tile[(p + 1) * TW + s0] = mul_mod(w, __ldg(MUL + ((size_t)p * L + j) * G::N + base + y), md);
+        for (int p = 0; p < NMUL; ++p) {
+            const size_t o = ((size_t)p * L + j) * G::N + base + y;
+            // fixed multipliers (pk, s) with stored Shoup companions: no Barrett reduction
+            tile[(p + 1) * TW + s0] = MULSH ? shoup(w, __ldg(MUL + o), __ldg(MULSH + o), q) : mul_mod(w, __ldg(MUL + o), md);
+        }
     }
     __syncthreads();
     load_block_twiddles<LOGN>(tws, dc->tw[j].inv, blk0);
@@ -461,39 +464,40 @@ __global__ void __launch_bounds__(mulb_threads<LOGN>()) k_blocks_mul_inv(const D
 
 template <int LOGN, int NMUL>
 static void bmi_t(const DevConsts* dc, const RnsParams& P, const u64* IN, const u64* MUL, u64* OUT,
-                  size_t out_stride, u64* XTRA, int xlimb, int xprime, int items, cudaStream_t st) {
+                  size_t out_stride, u64* XTRA, int xlimb, int xprime, int items, cudaStream_t st, const u64* MULSH) {
     using G = Ntt2<LOGN>;
     const int smem = ((NMUL + 1) * G::LINES * G::PITCH + 2 * G::TWB) * 8;
     smem_optin_k(k_blocks_mul_inv<LOGN, NMUL>, smem);
     const int J = P.cfg.L + (XTRA ? 1 : 0);
     k_blocks_mul_inv<LOGN, NMUL><<<items * J * G::CTAS_B, mulb_threads<LOGN>(), smem, st>>>(
-        dc, IN, MUL, OUT, out_stride, XTRA, xlimb, xprime);
+        dc, IN, MUL, OUT, out_stride, XTRA, xlimb, xprime, MULSH);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) throw std::runtime_error(std::string("blocks-mul launch: ") + cudaGetErrorString(e));
 }
 
 template <int LOGN>
 static void bmi_logn(const DevConsts* dc, const RnsParams& P, const u64* IN, const u64* MUL, int nmul, u64* OUT,
-                     size_t out_stride, u64* XTRA, int xlimb, int xprime, int items, cudaStream_t st) {
+                     size_t out_stride, u64* XTRA, int xlimb, int xprime, int items, cudaStream_t st,
+                     const u64* MULSH) {
     if (nmul == 1)
-        bmi_t<LOGN, 1>(dc, P, IN, MUL, OUT, out_stride, XTRA, xlimb, xprime, items, st);
+        bmi_t<LOGN, 1>(dc, P, IN, MUL, OUT, out_stride, XTRA, xlimb, xprime, items, st, MULSH);
     else if (nmul == 2)
-        bmi_t<LOGN, 2>(dc, P, IN, MUL, OUT, out_stride, XTRA, xlimb, xprime, items, st);
+        bmi_t<LOGN, 2>(dc, P, IN, MUL, OUT, out_stride, XTRA, xlimb, xprime, items, st, MULSH);
     else
         throw std::invalid_argument("blocks-mul: 1 or 2 multipliers");
 }
 
 void launch_blocks_mul_inv(const DevConsts* dc, const RnsParams& P, const u64* IN, const u64* MUL, int nmul,
                            u64* OUT, size_t out_stride, u64* XTRA, int xlimb, int xprime, int items,
-                           cudaStream_t st) {
+                           cudaStream_t st, const u64* MULSH) {
     if (!items) return;
     switch (P.cfg.logn) {
-        case 10: bmi_logn<10>(dc, P, IN, MUL, nmul, OUT, out_stride, XTRA, xlimb, xprime, items, st); break;
-        case 11: bmi_logn<11>(dc, P, IN, MUL, nmul, OUT, out_stride, XTRA, xlimb, xprime, items, st); break;
-        case 12: bmi_logn<12>(dc, P, IN, MUL, nmul, OUT, out_stride, XTRA, xlimb, xprime, items, st); break;
-        case 13: bmi_logn<13>(dc, P, IN, MUL, nmul, OUT, out_stride, XTRA, xlimb, xprime, items, st); break;
-        case 14: bmi_logn<14>(dc, P, IN, MUL, nmul, OUT, out_stride, XTRA, xlimb, xprime, items, st); break;
-        case 15: bmi_logn<15>(dc, P, IN, MUL, nmul, OUT, out_stride, XTRA, xlimb, xprime, items, st); break;
+        case 10: bmi_logn<10>(dc, P, IN, MUL, nmul, OUT, out_stride, XTRA, xlimb, xprime, items, st, MULSH); break;
+        case 11: bmi_logn<11>(dc, P, IN, MUL, nmul, OUT, out_stride, XTRA, xlimb, xprime, items, st, MULSH); break;
+        case 12: bmi_logn<12>(dc, P, IN, MUL, nmul, OUT, out_stride, XTRA, xlimb, xprime, items, st, MULSH); break;
+        case 13: bmi_logn<13>(dc, P, IN, MUL, nmul, OUT, out_stride, XTRA, xlimb, xprime, items, st, MULSH); break;
+        case 14: bmi_logn<14>(dc, P, IN, MUL, nmul, OUT, out_stride, XTRA, xlimb, xprime, items, st, MULSH); break;
+        case 15: bmi_logn<15>(dc, P, IN, MUL, nmul, OUT, out_stride, XTRA, xlimb, xprime, items, st, MULSH); break;
         default: throw std::invalid_argument("blocks-mul: unsupported logn");
     }
 }
