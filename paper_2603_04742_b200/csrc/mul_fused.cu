@@ -28,38 +28,40 @@ constexpr int mulb_threads() { return LOGN >= 15 ? 256 : 128; }
 // (four groups measured no faster: the register file then halves the CTAs).
 constexpr int kMulGroups = 2, kGroupThreads = 128;
 
-template <int LOGN, int LT, int KT>
+template <int LOGN, int LT, int KT, int LN = 16>
 __global__ void __launch_bounds__(kMulGroups * kGroupThreads) k_mul_blocks_tensor(const DevConsts* __restrict__ dc,
                                                                                   const u64* __restrict__ T,
                                                                                   u64* __restrict__ Z, int M) {
     using G = Ntt2<LOGN>;
     extern __shared__ u64 smem[];
     constexpr int PITCH = G::PITCH;
-    constexpr int TW = G::LINES * PITCH;
+    constexpr int TW = LN * PITCH;  // LN blocks per tile (8 at 2^15: half the smem, more CTAs per SM)
     constexpr int NT = kMulGroups * kGroupThreads;
-    constexpr int PER = G::LINES * G::R2 / NT;
+    constexpr int PER = LN * G::R2 / NT;
+    constexpr int CTAS = G::R1 / LN;
+    constexpr int MAXR = LN >= 16 ? 4 : 3;  // radix-8 passes keep all threads of a group busy on 8 lines
     static_assert(PER >= 1, "tile smaller than the CTA");
     u64* tile = smem;            // 4 tiles: a0 a1 b0 b1, then z0 z1 z2 in the first three
     u64* tws = smem + 4 * TW;
     const int L = LT ? LT : dc->L, K = KT ? KT : dc->K;  // M: 2L over Q u R, 2L + 1 over Q u B
     int bid = blockIdx.x;
-    const int tileid = bid % G::CTAS_B;
-    bid /= G::CTAS_B;
+    const int tileid = bid % CTAS;
+    bid /= CTAS;
     const int j = bid % M;
     const int item = bid / M;
     const int prime = j < L ? j : K + j;  // B primes follow P in the prime table
     const Modulus md = dc->mod[prime];
     const u64 q = md.q;
-    const int blk0 = tileid * G::LINES;
+    const int blk0 = tileid * LN;
     const size_t base = (size_t)blk0 * G::R2;
     const size_t PM = (size_t)M * G::N;
     const int grp = threadIdx.x / kGroupThreads;
     const ThreadGroup tg = cta_slice(grp, kMulGroups);
     auto saddr = [](int x) { return (x >> G::B) * PITCH + (x & (G::R2 - 1)); };
     auto addr = [](int l, int pos) { return l * PITCH + pos; };
-    auto twf = [&](int sl, int l, int blk) { return block_tw<LOGN>(tws, sl, l, blk); };
+    auto twf = [&](int sl, int l, int blk) { return block_tw<LOGN, LN>(tws, sl, l, blk); };
     const u64* src = T + (size_t)item * 4 * PM + (size_t)j * G::N + base;
-    load_block_twiddles<LOGN>(tws, dc->tw[prime].fwd, blk0);
+    load_block_twiddles<LOGN, LN>(tws, dc->tw[prime].fwd, blk0);
 #pragma unroll
     for (int p = 0; p < 4; ++p)
 #pragma unroll
@@ -70,7 +72,8 @@ __global__ void __launch_bounds__(kMulGroups * kGroupThreads) k_mul_blocks_tenso
     cp_async_wait_all();
     __syncthreads();
 #pragma unroll 1
-    for (int p = grp; p < 4; p += kMulGroups) line_ntt<G::B, 0, false>(tile + p * TW, q, addr, twf, tg);
+    for (int p = grp; p < 4; p += kMulGroups)
+        line_ntt_v<G::B, 0, false, MAXR, LN>(tile + p * TW, ConstQ{q}, addr, twf, tg);
     __syncthreads();
     // tensor: all four inputs canonicalised (cheap 32-bit quotient estimate),
     // so z1 = a0 b1 + a1 b0 < 2 q^2 < 2^117 is one 128-bit sum under a single
@@ -92,11 +95,12 @@ __global__ void __launch_bounds__(kMulGroups * kGroupThreads) k_mul_blocks_tenso
         tile[2 * TW + s0] = dot29_reduce(d2, md);
     }
     __syncthreads();
-    load_block_twiddles<LOGN>(tws, dc->tw[prime].inv, blk0);
+    load_block_twiddles<LOGN, LN>(tws, dc->tw[prime].inv, blk0);
     cp_async_wait_all();
     __syncthreads();
 #pragma unroll 1
-    for (int p = grp; p < 3; p += kMulGroups) line_ntt<G::B, 0, true>(tile + p * TW, q, addr, twf, tg);
+    for (int p = grp; p < 3; p += kMulGroups)
+        line_ntt_v<G::B, 0, true, MAXR, LN>(tile + p * TW, ConstQ{q}, addr, twf, tg);
     __syncthreads();
     u64* dst = Z + (size_t)item * 3 * PM + (size_t)j * G::N + base;
 #pragma unroll
@@ -506,9 +510,24 @@ template <int LOGN, int LT, int KT>
 static void mulb_t(const DevConsts* dc, const RnsParams& P, const u64* T, u64* Z, int items, cudaStream_t st) {
     using G = Ntt2<LOGN>;
     const int M = P.mul_limbs();
-    const int smem = (4 * G::LINES * G::PITCH + 2 * G::TWB) * 8;
-    smem_optin_k(k_mul_blocks_tensor<LOGN, LT, KT>, smem);
-    k_mul_blocks_tensor<LOGN, LT, KT><<<items * M * G::CTAS_B, kMulGroups * kGroupThreads, smem, st>>>(dc, T, Z, M);
+    // 2^15 (B = 7): 16-block tiles need 100 KB of smem (2 CTAs per SM); 8-block
+    // tiles halve it (CSSC_MULB_LN=16 keeps 16)
+    static const int ln_env = [] {
+        const char* e = std::getenv("CSSC_MULB_LN");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (LOGN >= 15 && ln_env != 16) {
+        constexpr int LN = 8;
+        const int smem = (4 * LN * G::PITCH + 2 * btw_entries<LOGN, LN>()) * 8;
+        smem_optin_k(k_mul_blocks_tensor<LOGN, LT, KT, LN>, smem);
+        k_mul_blocks_tensor<LOGN, LT, KT, LN><<<items * M * (G::R1 / LN), kMulGroups * kGroupThreads, smem, st>>>(
+            dc, T, Z, M);
+    } else {
+        const int smem = (4 * G::LINES * G::PITCH + 2 * G::TWB) * 8;
+        smem_optin_k(k_mul_blocks_tensor<LOGN, LT, KT>, smem);
+        k_mul_blocks_tensor<LOGN, LT, KT><<<items * M * G::CTAS_B, kMulGroups * kGroupThreads, smem, st>>>(dc, T, Z,
+                                                                                                          M);
+    }
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) throw std::runtime_error(std::string("mul blocks launch: ") + cudaGetErrorString(e));
 }
