@@ -433,15 +433,24 @@ __global__ void __launch_bounds__(kKsGroups * kKsGroupThreads) k_ks_blocks_gathe
         const u64* h = H + (size_t)hi * dnum * PL + (size_t)j * G::N;
         const u32 g = GEL[item * nterm + t];
         const u64* key = KEY[item * nterm + t];
+        for (int dg = 0; dg < dnum; ++dg) {
+            // every load of the term first (gathered digit, both key words and
+            // their companions for all PER elements), then the products
+            u64 w[PER], k0[PER], k1[PER], c0[PER], c1[PER];
 #pragma unroll
-        for (int r = 0; r < PER; ++r) {
-            const int x = threadIdx.x + T * r;
-            const int src = ntt_perm<LOGN>(g, (int)base + x);
-            for (int dg = 0; dg < dnum; ++dg) {
-                const u64 w = __ldg(h + (size_t)dg * PL + src);
+            for (int r = 0; r < PER; ++r) {
+                const int x = threadIdx.x + T * r;
                 const size_t ko = ((size_t)dg * 2) * PL + (size_t)j * G::N + base + x;
-                a0[r] = add_mod(a0[r], shoup(w, __ldg(key + ko), __ldg(key + KW + ko), q), q);
-                a1[r] = add_mod(a1[r], shoup(w, __ldg(key + ko + PL), __ldg(key + KW + ko + PL), q), q);
+                w[r] = __ldg(h + (size_t)dg * PL + ntt_perm<LOGN>(g, (int)base + x));
+                k0[r] = __ldg(key + ko);
+                k1[r] = __ldg(key + ko + PL);
+                c0[r] = __ldg(key + KW + ko);
+                c1[r] = __ldg(key + KW + ko + PL);
+            }
+#pragma unroll
+            for (int r = 0; r < PER; ++r) {
+                a0[r] = add_mod(a0[r], shoup(w[r], k0[r], c0[r], q), q);
+                a1[r] = add_mod(a1[r], shoup(w[r], k1[r], c1[r], q), q);
             }
         }
     }
