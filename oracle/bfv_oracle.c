@@ -17,6 +17,7 @@
  */
 #include "bfv_oracle.h"
 
+#include <pthread.h>
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
@@ -584,7 +585,18 @@ void bfvo_add_galois_key(bfvo_ctx* c, uint32_t g) {
 
 /* switching key for target phi_g(s)^2 = phi_g(s^2): rotates the s^2 component
  * of an unrelinearised product (key id 2^32 | g) */
+/* the key caches are shared by the tests' parallel per-chunk evaluations */
+static pthread_mutex_t key_mu = PTHREAD_MUTEX_INITIALIZER;
+
+static const u64* find_key_sq_locked(bfvo_ctx* c, uint32_t g);
 static const u64* find_key_sq(bfvo_ctx* c, uint32_t g) {
+    pthread_mutex_lock(&key_mu);
+    const u64* k = find_key_sq_locked(c, g);
+    pthread_mutex_unlock(&key_mu);
+    return k;
+}
+
+static const u64* find_key_sq_locked(bfvo_ctx* c, uint32_t g) {
     for (int i = 0; i < c->ngk2; i++) if (c->gk2[i].g == g) return c->gk2[i].key;
     int n = c->n, LK = c->L + c->K;
     u64* sp = (u64*)malloc(sizeof(u64) * (size_t)LK * n);
@@ -617,9 +629,12 @@ int bfvo_get_ksk_sq(bfvo_ctx* c, uint32_t g, u64* out) {
 
 static const u64* find_key(bfvo_ctx* c, uint32_t which) {
     if (which == 0) return c->rlk;
+    pthread_mutex_lock(&key_mu);
     bfvo_add_galois_key(c, which);
-    for (int i = 0; i < c->ngk; i++) if (c->gk[i].g == which) return c->gk[i].key;
-    return NULL;
+    const u64* k = NULL;
+    for (int i = 0; i < c->ngk; i++) if (c->gk[i].g == which) k = c->gk[i].key;
+    pthread_mutex_unlock(&key_mu);
+    return k;
 }
 
 void bfvo_get_sk(const bfvo_ctx* c, int64_t* s) { memcpy(s, c->s, sizeof(int64_t) * c->n); }
@@ -1169,8 +1184,53 @@ int bfvo_plan_fold(bfvo_ctx* c, const u64* z, int nsteps, const int64_t* offs, c
         p = (u64*)malloc(sizeof(u64) * 2 * cw);
         bfvo_mul_relin_z(c, z, p);
     }
+    int64_t S = n / 2;
     while (i < nsteps) {
         if (!from_acc[i]) { free(a0); free(a1); free(k0); free(k1); free(r); free(acc); free(nx); free(p); return -3; }
+        /* fold_relin = 2: two doubling steps D_{a+1}, D_{a+2} (with their odd
+         * steps) in one key-switch stage: acc + R(acc, d1) + R(acc, d2) +
+         * R(acc, d1 + d2) + R(p, o1) + R(p, o1 + d2) + R(p, o2), one ModDown;
+         * merged only when no combined offset is 0 mod S (plan_stage_merge) */
+        if (fold_relin == 2) {
+            int i2 = i + 1 + (i + 1 < nsteps && !from_acc[i + 1]);  /* index of D_{a+2} */
+            if (i2 < nsteps && from_acc[i2]) {
+                int64_t d1 = offs[i], d2 = offs[i2];
+                int has_o1 = i2 == i + 2, has_o2 = i2 + 1 < nsteps && !from_acc[i2 + 1];
+                int64_t o1 = has_o1 ? offs[i + 1] : 0, o2 = has_o2 ? offs[i2 + 1] : 0;
+                int ok = (d1 + d2) % S != 0 && (!has_o1 || (o1 + d2) % S != 0);
+                if (ok) {
+                    int64_t aoff[3] = {d1, d2, d1 + d2};
+                    int64_t zoff[3];
+                    int nz = 0;
+                    if (has_o1) { zoff[nz++] = o1; zoff[nz++] = o1 + d2; }
+                    if (has_o2) zoff[nz++] = o2;
+                    memset(a0, 0, sizeof(u64) * aw);
+                    memset(a1, 0, sizeof(u64) * aw);
+                    memcpy(nx, acc, sizeof(u64) * 2 * cw);
+                    for (int t = 0; t < 3; t++) {
+                        uint32_t g = bfvo_galois_elt(c, aoff[t]);
+                        ks_accumulate(c, find_key(c, g), acc + cw, g, a0, a1);
+                        bfvo_automorph(c, g, acc, r, L);
+                        for (size_t x = 0; x < cw; x++) nx[x] = addm(nx[x], r[x], c->q[x / n]);
+                    }
+                    for (int t = 0; t < nz; t++) {
+                        uint32_t g = bfvo_galois_elt(c, zoff[t]);
+                        ks_accumulate(c, find_key(c, g), z1, g, a0, a1);
+                        ks_accumulate(c, find_key_sq(c, g), z2, g, a0, a1);
+                        bfvo_automorph(c, g, z0, r, L);
+                        for (size_t x = 0; x < cw; x++) nx[x] = addm(nx[x], r[x], c->q[x / n]);
+                    }
+                    ks_finish(c, a0, a1, k0, k1);
+                    for (size_t x = 0; x < cw; x++) {
+                        nx[x] = addm(nx[x], k0[x], c->q[x / n]);
+                        nx[cw + x] = addm(nx[cw + x], k1[x], c->q[x / n]);
+                    }
+                    memcpy(acc, nx, sizeof(u64) * 2 * cw);
+                    i = i2 + 1 + has_o2;
+                    continue;
+                }
+            }
+        }
         uint32_t gd = bfvo_galois_elt(c, offs[i]);
         memset(a0, 0, sizeof(u64) * aw);
         memset(a1, 0, sizeof(u64) * aw);

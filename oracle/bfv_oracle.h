@@ -86,7 +86,8 @@ void bfvo_mul_relin_z(bfvo_ctx* c, const uint64_t* z, uint64_t* out);
 void bfvo_add_galois_key_sq(bfvo_ctx* c, uint32_t g); /* not thread safe: call before parallel use */
 int bfvo_get_ksk_sq(bfvo_ctx* c, uint32_t g, uint64_t* out);
 /* intra_chunk_sum of one chunk from the product's tensor z ([3][L][N]) as the
- * batched plan evaluates it; fold_relin: relinearisation folded into level 0 */
+ * batched plan evaluates it; fold_relin: 1 relinearisation folded into level 0,
+ * 2 also two doubling steps per key-switch stage after level 0 */
 int bfvo_plan_fold(bfvo_ctx* c, const uint64_t* z, int nsteps, const int64_t* offs, const int* from_acc,
                    int fold_relin, uint64_t* out);
 int bfvo_rotate2_add(bfvo_ctx* c, const uint64_t* acc, const uint64_t* src, int64_t k1, int64_t k2, uint64_t* out);

@@ -2241,6 +2241,39 @@ void launch_automorph_c0(const DevConsts* dc, const RnsParams& P, const u64* con
     CSSC_CHECK_LAUNCH();
 }
 
+// OUT[item].c0 (=|+=) sum_t phi_t(SRC[item][t].c0), t < 3 (GI[item][t] = 0: no
+// term): the c0 terms of the rotations a stage folds into one ModDown beyond
+// the one its ModDown gathers itself (DESIGN 2.9)
+__global__ void k_automorph_sum(const DevConsts* __restrict__ dc, u64* const* OUT, const u64* const* SRC,
+                                const u32* GI, int accumulate) {
+    const int n = dc->n, L = dc->L;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int item = blockIdx.y;
+    u64* out = OUT[item];
+    int idx[3];
+    bool neg[3];
+#pragma unroll
+    for (int t = 0; t < 3; ++t) idx[t] = GI[item * 3 + t] ? automorph_src(GI[item * 3 + t], k, n, neg[t]) : -1;
+    for (int j = 0; j < L; ++j) {
+        const u64 q = dc->mod[j].q;
+        u64 v = accumulate ? out[(size_t)j * n + k] : 0;
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {
+            if (idx[t] < 0) continue;
+            const u64 x = SRC[item * 3 + t][(size_t)j * n + idx[t]];
+            v = add_mod(v, neg[t] ? neg_mod(x, q) : x, q);
+        }
+        out[(size_t)j * n + k] = v;
+    }
+}
+
+void launch_automorph_sum(const DevConsts* dc, const RnsParams& P, u64* const* OUT, const u64* const* SRC,
+                          const u32* GI, bool accumulate, int items, cudaStream_t st) {
+    if (!items) return;
+    k_automorph_sum<<<ew_grid(P.n, items), EW_THREADS, 0, st>>>(dc, OUT, SRC, GI, accumulate ? 1 : 0);
+    CSSC_CHECK_LAUNCH();
+}
+
 __global__ void k_fold_mod(const DevConsts* __restrict__ dc, u64* W) {
     const int n = dc->n, L = dc->L;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;

@@ -158,6 +158,9 @@ bool launch_ks_cols_moddown(const DevConsts* dc, const RnsParams& P, const u64* 
                             const u64* const* XACC = nullptr);
 void launch_acc_add(const DevConsts* dc, const RnsParams& P, u64* ACC, const u64* const* XACC, int items,
                     cudaStream_t st);
+// OUT[i].c0 (=|+=) sum_t phi(SRC[i*3+t].c0) with inverse Galois elements GI[i*3+t] (0: none)
+void launch_automorph_sum(const DevConsts* dc, const RnsParams& P, u64* const* OUT, const u64* const* SRC,
+                          const u32* GI, bool accumulate, int items, cudaStream_t st);
 void launch_automorph_c0(const DevConsts* dc, const RnsParams& P, const u64* const* SRC, const u32* ginv,
                          u64* const* OUT, int items, cudaStream_t st);
 void launch_ks_moddown(const DevConsts* dc, const RnsParams& P, const u64* ACC,

@@ -56,6 +56,51 @@ struct Tree {
     std::vector<std::pair<int, u64>> odd;  // (k, offset): O_k follows D_k
 };
 
+// One key-switch stage of a chunk's fold (fold mode, DESIGN 2.9): one doubling
+// step D (offset d1) or two merged ones (d1, d2: acc + R(acc, d1) + R(acc, d2) +
+// R(acc, d1 + d2)), plus the rotations of the product p its odd steps add
+// (poff: O_a, O_a + d2 when merged, O_{a+1}); one ModDown per stage.
+struct Stage {
+    bool merged = false;
+    u64 d1 = 0, d2 = 0;
+    std::vector<u64> poff;
+};
+
+// Stage 0 is D_1 (+ O_1); after it, consecutive doubling steps pair greedily
+// when no combined offset is 0 mod S (the oracle's plan fold, fold_relin = 2)
+std::vector<Stage> make_stages(const Tree& t, u64 S, bool merge) {
+    const int m = (int)t.dbl.size();
+    std::vector<std::vector<u64>> odd_of(m + 1);
+    for (const auto& [after, off] : t.odd) odd_of[after].push_back(off);
+    std::vector<Stage> st;
+    int a = 1;  // next doubling step D_a (1-based)
+    while (a <= m) {
+        Stage g;
+        g.d1 = t.dbl[a - 1];
+        const bool o1 = !odd_of[a].empty();
+        if (merge && a >= 2 && a + 1 <= m) {
+            const u64 d2 = t.dbl[a];
+            const u64 o = o1 ? odd_of[a][0] : 0;
+            if ((g.d1 + d2) % S != 0 && (!o1 || (o + d2) % S != 0)) {
+                g.merged = true;
+                g.d2 = d2;
+                if (o1) {
+                    g.poff.push_back(o);
+                    g.poff.push_back(o + d2);
+                }
+                for (u64 x : odd_of[a + 1]) g.poff.push_back(x);
+                st.push_back(g);
+                a += 2;
+                continue;
+            }
+        }
+        for (u64 x : odd_of[a]) g.poff.push_back(x);
+        st.push_back(g);
+        a += 1;
+    }
+    return st;
+}
+
 Tree split_schedule(const std::vector<spmv::RotStep>& steps) {
     Tree t;
     for (const spmv::RotStep& s : steps) {
@@ -104,36 +149,50 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
         n_rot += steps.size();
         n_odd += trees[i].odd.size();
     }
-    // chunks with more doubling levels first: level l is a prefix of the items
-    std::vector<int> order(n);
-    std::iota(order.begin(), order.end(), 0);
-    std::stable_sort(order.begin(), order.end(),
-                     [&](int x, int y) { return trees[x].dbl.size() > trees[y].dbl.size(); });
-    const int depth = n ? (int)trees[order[0]].dbl.size() : 0;
-    int nd = 0;  // chunks with at least one doubling step: items 0 .. nd-1
-    while (nd < n && !trees[order[nd]].dbl.empty()) ++nd;
     // Folded level 0 (fused fixed-shape key switch, hoisting on): the products
     // of rotated chunks stay unrelinearised; level 0 hoists the ModUp + NTT of
     // their z1 and z2 and sums, per doubling item, the relinearisation of z2
     // and the rotations of z1 (key for phi_g(s)) and z2 (key for phi_g(s)^2)
-    // into one ModDown (the oracle restates it: plan fold with fold_relin = 1)
+    // into one ModDown; later levels are key-switch stages of one or two
+    // doubling steps (DESIGN 2.9; the oracle restates it: plan fold, fold_relin
+    // = 2, or 1 with CSSC_NO_MERGE=1)
+    int ndbl = 0;
+    for (int i = 0; i < n; ++i) ndbl += trees[i].dbl.empty() ? 0 : 1;
     const bool fold = ctx.fused_key_switch() && fixed_rns_shape(P) && std::getenv("CSSC_NO_KSY") == nullptr &&
-                      std::getenv("CSSC_KS_CLUSTER") == nullptr && std::getenv("CSSC_NO_HOIST") == nullptr && nd > 0;
+                      std::getenv("CSSC_KS_CLUSTER") == nullptr && std::getenv("CSSC_NO_HOIST") == nullptr &&
+                      ndbl > 0;
+    const bool merge = fold && std::getenv("CSSC_NO_MERGE") == nullptr;
+    std::vector<std::vector<Stage>> stages(n);
+    size_t n_stage = 0;
+    if (fold)
+        for (int i = 0; i < n; ++i) {
+            stages[i] = make_stages(trees[i], (u64)P.S, merge);
+            n_stage += stages[i].size();
+        }
+    auto levels_of = [&](int i) { return fold ? stages[i].size() : trees[i].dbl.size(); };
+    // chunks with more levels first: level l is a prefix of the items
+    std::vector<int> order(n);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return levels_of(x) > levels_of(y); });
+    const int depth = n ? (int)levels_of(order[0]) : 0;
+    int nd = 0;  // chunks with at least one doubling step: items 0 .. nd-1
+    while (nd < n && !trees[order[nd]].dbl.empty()) ++nd;
     fold_ = fold;
     nd_ = nd;
-    stats_.relin_folded = fold ? 1 : 0;
+    stats_.relin_folded = fold ? (merge ? 2 : 1) : 0;
 
     arena_ = DevBuf(&ctx.pool(), 8 * ((size_t)(16 + 10 * std::max(depth, 1)) * std::max(n, 1) + 16 * n_odd +
                                       2 * (size_t)ns_ + 16) +
-                                     16 * (size_t)(16 * depth + 40) + 8 * (6 * (size_t)n + 6 * n_odd));
+                                     16 * (size_t)(24 * depth + 40) + 8 * (6 * (size_t)n + 6 * n_odd) +
+                                     8 * 48 * ((size_t)n * std::max(depth, 1) + 2 * n_stage));
     prod_ = DevBuf(&ctx.pool(), sizeof(u64) * ctw * std::max(n, 1));
     if (depth >= 1) acc0_ = DevBuf(&ctx.pool(), sizeof(u64) * ctw * n);
     if (depth >= 2) acc1_ = DevBuf(&ctx.pool(), sizeof(u64) * ctw * n);
-    if (n_odd) rp_ = DevBuf(&ctx.pool(), sizeof(u64) * ctw * n_odd);
+    if (n_odd || n_stage) rp_ = DevBuf(&ctx.pool(), sizeof(u64) * ctw * std::max(n_odd, n_stage));
     T_ = DevBuf(&ctx.pool(), sizeof(u64) * std::max<size_t>(1, n) * ctx.mul_T_words());
     Z_ = DevBuf(&ctx.pool(), sizeof(u64) * std::max<size_t>(1, n) * ctx.mul_Z_words());
     D2_ = DevBuf(&ctx.pool(), sizeof(u64) * std::max<size_t>(1, n) * ctx.poly_words());
-    const size_t ks_items = std::max<size_t>(1, (size_t)n + n_odd);
+    const size_t ks_items = std::max<size_t>(1, (size_t)n + std::max(n_odd, n_stage));
     DX_ = DevBuf(&ctx.pool(), sizeof(u64) * std::max(ks_items, fold ? 2 * (size_t)nd : 1) * ctx.dx_words());
     ACC_ = DevBuf(&ctx.pool(), sizeof(u64) * ks_items * ctx.ksacc_words());
     MT_ = DevBuf(&ctx.pool(), sizeof(u64) * std::max<size_t>(1, n) * ctw);
@@ -221,6 +280,173 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
     std::vector<const u64*> odd_src;
     std::vector<u32> odd_gi;
     std::vector<u64*> odd_out;
+    if (fold) {
+        // stage slots: EXTRA (c0 terms: rp_ slot, c1 half zero) and bundle
+        // (the stage's rotations of p, accumulated at level 0: ACC[nd + b])
+        std::vector<std::vector<int>> xslot(n), bslot(n);
+        int n_x = 0, n_b = 0;
+        for (int k = 0; k < n; ++k) {
+            const auto& sg = stages[order[k]];
+            xslot[k].assign(sg.size(), -1);
+            bslot[k].assign(sg.size(), -1);
+            for (size_t t = 0; t < sg.size(); ++t) {
+                if (!sg[t].poff.empty()) bslot[k][t] = n_b++;
+                if (!sg[t].poff.empty() || sg[t].merged) xslot[k][t] = n_x++;
+            }
+        }
+        auto xs_at = [&](int id) { return rp_.words() + (size_t)id * ctw; };
+        const size_t pw2 = ctx.poly_words();
+        int nt0 = 3;  // level 0's MAC terms per item: 3 per doubling item, 2 per bundled rotation of p
+        for (int k = 0; k < n; ++k)
+            for (const Stage& st : stages[order[k]]) nt0 = std::max(nt0, 2 * (int)st.poff.size());
+        for (int l = 0; l < depth; ++l) {
+            std::vector<const u64*> src, base, key, extra, ysrc, xacc, hp, hy, tk, asrc;
+            std::vector<u64*> yout, o, aout;
+            std::vector<u32> gi, tg, agi;
+            std::vector<int> th;
+            std::set<u32> lvl_keys;
+            const int NT = l == 0 ? nt0 : 3;
+            bool any_x = false, any_merged = false;
+            auto term = [&](int h, u32 g, const u64* kp) {
+                th.push_back(h);
+                tg.push_back(g);
+                tk.push_back(kp);
+            };
+            auto pad = [&](size_t upto) {
+                while (th.size() < upto) term(-1, 1u, nullptr);
+            };
+            int tail = 0;
+            for (int k = 0; k < n && (int)stages[order[k]].size() > l; ++k, ++tail) {
+                const Stage& sg = stages[order[k]][l];
+                u64* cur = acc_after(k, l);  // level 0: the product slot (z0, z1)
+                u32 g;
+                const u64* kd = key_of(sg.d1, lvl_keys, g);
+                const u32 g1 = last_g;
+                key.push_back(kd);
+                gi.push_back(g);
+                src.push_back(cur);
+                base.push_back(cur);
+                o.push_back(acc_at(l % 2, k));
+                ysrc.push_back(yafter(k, l));
+                yout.push_back((int)stages[order[k]].size() > l + 1 ? accY_at(l % 2, k) : nullptr);
+                extra.push_back(xslot[k][l] >= 0 ? xs_at(xslot[k][l]) : nullptr);
+                xacc.push_back(bslot[k][l] >= 0 ? ACC_.words() + (size_t)(nd + bslot[k][l]) * accw : nullptr);
+                any_x = any_x || extra.back() || xacc.back();
+                const size_t t0 = th.size();
+                if (l == 0) {  // relinearisation of z2 + the rotation of z1 and z2
+                    term(nd + k, 1u, ctx.relin_key());
+                    term(k, g1, kd);
+                    term(nd + k, g1, ctx.galois_key_sq(g1));
+                } else {
+                    term(k, g1, kd);
+                    if (sg.merged) {  // R(acc, d2), R(acc, d1 + d2); their c0 terms into the EXTRA slot
+                        any_merged = true;
+                        aout.push_back(xs_at(xslot[k][l]));
+                        for (u64 off : {sg.d2, sg.d1 + sg.d2}) {
+                            u32 gx;
+                            const u64* kx = key_of(off, lvl_keys, gx);
+                            term(k, last_g, kx);
+                            asrc.push_back(cur);
+                            agi.push_back(gx);
+                        }
+                        asrc.push_back(nullptr);  // third term unused
+                        agi.push_back(0);
+                    }
+                }
+                pad(t0 + NT);
+            }
+            if (l == 0) {
+                // the stages' rotations of p as level-0 bundle items, and every EXTRA
+                // slot's c0 terms phi_o(z0) written (zero for merged-only slots)
+                for (int k = 0; k < n; ++k) {
+                    const auto& sg = stages[order[k]];
+                    for (size_t t = 0; t < sg.size(); ++t) {
+                        if (bslot[k][t] >= 0) {
+                            const size_t t0 = th.size();
+                            for (u64 off : sg[t].poff) {
+                                u32 gx;
+                                const u64* kx = key_of(off, lvl_keys, gx);
+                                term(k, last_g, kx);
+                                term(nd + k, last_g, ctx.galois_key_sq(last_g));
+                            }
+                            pad(t0 + NT);
+                        }
+                        if (xslot[k][t] >= 0) {
+                            aout.push_back(xs_at(xslot[k][t]));
+                            for (int x = 0; x < 3; ++x) {
+                                const bool has = x < (int)sg[t].poff.size();
+                                u32 gx = 0;
+                                if (has) key_of(sg[t].poff[x], lvl_keys, gx);
+                                asrc.push_back(has ? prod_at(k) : nullptr);
+                                agi.push_back(has ? gx : 0u);
+                            }
+                        }
+                    }
+                }
+            }
+            Level lv;
+            lv.items = tail;
+            lv.acc_items = (int)(th.size() / NT);
+            lv.src = put(src);
+            lv.base = put(base);
+            lv.out = put(o);
+            lv.key = put(key);
+            lv.ginv = put(gi);
+            lv.extra = any_x ? put(extra) : nullptr;
+            lv.xacc = any_x ? put(xacc) : nullptr;
+            lv.ysrc = put(ysrc);
+            lv.yout = put(yout);
+            lv.pair = nullptr;
+            lv.mac_terms = 0;
+            for (int x : th) lv.mac_terms += x >= 0 ? 1 : 0;
+            if (!aout.empty()) {
+                lv.asum_n = (int)aout.size();
+                lv.asum_out = put(aout);
+                lv.asum_src = put(asrc);
+                lv.asum_gi = put(agi);
+                lv.asum_acc = l > 0;
+            }
+            if (l == 0 || any_merged) {  // hoisted: one ModUp + NTT per source, multi-term MAC
+                if (l == 0) {  // sources: z1 of product k (c1 of its slot) -> H[k], z2 (D2) -> H[nd + k]
+                    hp.resize(2 * nd);
+                    hy.resize(2 * nd);
+                    for (int k = 0; k < nd; ++k) {
+                        hp[k] = prod_at(k) + pw2;
+                        hy[k] = prodY_at(k);
+                        hp[nd + k] = D2_.words() + (size_t)k * pw2;
+                        hy[nd + k] = D2Y_.words() + (size_t)k * pw2;
+                    }
+                } else {  // sources: the accumulators' c1
+                    hp.assign(src.begin(), src.end());
+                    hy.assign(ysrc.begin(), ysrc.end());
+                    for (auto& x : hp) x += pw2;
+                }
+                std::vector<int> ord(lv.acc_items);
+                std::iota(ord.begin(), ord.end(), 0);
+                if (std::getenv("CSSC_NO_KEY_ORDER") == nullptr)  // items sharing keys back to back (L2)
+                    std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) {
+                        return tg[(size_t)x * NT + (l == 0 ? 1 : 0)] < tg[(size_t)y * NT + (l == 0 ? 1 : 0)];
+                    });
+                lv.horder = put(ord);
+                lv.hsrc = (int)hp.size();
+                lv.hprod = put(hp);
+                lv.hy = put(hy);
+                lv.hterm = NT;
+                lv.hidx = put(th);
+                lv.gel = put(tg);
+                lv.hkey = put(tk);
+            }
+            lv.keys = (int)lvl_keys.size();
+            levels_.push_back(lv);
+            const int srcs = lv.hsrc ? lv.hsrc : lv.acc_items;
+            const int kf = ks_cols_moddown_applies(P, lv.items) ? 1 : 0;
+            stats_.hbm_bytes += (u64)lv.acc_items * 3 * C + lvl_keys.size() * KEY * (l == 0 ? 2 : 1);
+            stats_.key_bytes += lvl_keys.size() * KEY * (l == 0 ? 2 : 1);
+            stats_.kernels += 2 + (2 - kf) + (lv.hsrc ? 1 : 0) + (lv.asum_n ? 1 : 0);
+            stats_.limb_ntts += (u64)srcs * P.dnum * LK + (u64)lv.items * 2 * LK;
+        }
+        if (n_x) cuda_check(cudaMemsetAsync(rp_.words(), 0, sizeof(u64) * ctw * n_x, ctx.stream()), "xs zero");
+    } else {
     for (int l = 0; l < depth; ++l) {
         std::vector<const u64*> src, base, key, extra, ysrc, xacc;
         std::vector<u64*> yout;
@@ -292,53 +518,6 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
             lv.odd_ginv = put(odd_gi);
             lv.odd_out = put(odd_out);
         }
-        if (l == 0 && fold) {
-            // sources: z1 of product k (c1 of its slot) -> H[k], z2 (D2) -> H[nd + k]
-            const size_t pw2 = ctx.poly_words();
-            std::vector<const u64*> hp(2 * nd), hy(2 * nd);
-            for (int k = 0; k < nd; ++k) {
-                hp[k] = prod_at(k) + pw2;
-                hy[k] = prodY_at(k);
-                hp[nd + k] = D2_.words() + (size_t)k * pw2;
-                hy[nd + k] = D2Y_.words() + (size_t)k * pw2;
-            }
-            constexpr int NT = 3;
-            std::vector<int> th((size_t)lv.acc_items * NT, -1);
-            std::vector<u32> tg((size_t)lv.acc_items * NT, 1u);
-            std::vector<const u64*> tk((size_t)lv.acc_items * NT, nullptr);
-            for (int i = 0; i < lv.acc_items; ++i) {
-                const int k = hidx[i];
-                const u32 g = gel[i];
-                if (i < tail) {  // doubling item: relinearisation of z2 + rot of z1 and z2
-                    th[i * NT + 0] = nd + k;
-                    tk[i * NT + 0] = ctx.relin_key();
-                }
-                th[i * NT + 1] = k;
-                tg[i * NT + 1] = g;
-                tk[i * NT + 1] = key[i];
-                th[i * NT + 2] = nd + k;
-                tg[i * NT + 2] = g;
-                tk[i * NT + 2] = ctx.galois_key_sq(g);
-            }
-            lv.mac_terms = 0;
-            for (int x : th) lv.mac_terms += x >= 0 ? 1 : 0;
-            // launch order: by the rotation's Galois element, so the items that share
-            // its two keys run back to back and read them from L2
-            std::vector<int> ord(lv.acc_items);
-            std::iota(ord.begin(), ord.end(), 0);
-            if (std::getenv("CSSC_NO_KEY_ORDER") == nullptr)
-                std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return gel[x] < gel[y]; });
-            lv.horder = put(ord);
-            lv.hsrc = 2 * nd;
-            lv.hprod = put(hp);
-            lv.hy = put(hy);
-            lv.hterm = NT;
-            lv.hidx = put(th);
-            lv.gel = put(tg);
-            lv.hkey = put(tk);
-            stats_.key_bytes += lvl_keys.size() * KEY;  // the phi_g(s)^2 keys
-            stats_.hbm_bytes += lvl_keys.size() * KEY;
-        }
         levels_.push_back(lv);
         const int srcs = lv.hsrc ? lv.hsrc : lv.acc_items;
         const int kf = fused && !ksc && ks_cols_moddown_applies(P, lv.items) ? 1 : 0;
@@ -347,6 +526,7 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
         stats_.kernels += fused ? 2 + (2 - kf) + (any_x && !kf ? 1 : 0) + (lv.hsrc ? 1 : 0) + (lv.odd_n ? 1 : 0)
                                 : 7 + (any_x ? 1 : 0) + (lv.odd_n ? 1 : 0);
         stats_.limb_ntts += (u64)srcs * P.dnum * LK + (u64)lv.items * 2 * LK;
+    }
     }
     if (n_odd) cuda_check(cudaMemsetAsync(rp_.words(), 0, sizeof(u64) * ctw * n_odd, ctx.stream()), "rp zero");
     stats_.distinct_keys = all_keys.size();
@@ -364,7 +544,7 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
             ones.push_back((int)rr);
         }
         item_mask[k] = it->second;
-        fin[k] = acc_after(k, (int)trees[order[k]].dbl.size());
+        fin[k] = acc_after(k, (int)levels_of(order[k]));
     }
     n_masks_ = (int)ones.size();
     MASKS_ = DevBuf(&ctx.pool(), sizeof(u64) * std::max<size_t>(1, n_masks_) * ctx.poly_words());
@@ -442,6 +622,10 @@ void CloudPlan::record(std::vector<cudaEvent_t>* marks, u64* dec_d, const EncIn*
         if (lv.odd_n) {
             launch_automorph_c0(ctx_.dconsts(), P, lv.odd_src, lv.odd_ginv, lv.odd_out, lv.odd_n, st);
             kmark("k_automorph_c0", st);
+        }
+        if (lv.asum_n) {
+            launch_automorph_sum(ctx_.dconsts(), P, lv.asum_out, lv.asum_src, lv.asum_gi, lv.asum_acc, lv.asum_n, st);
+            kmark("k_automorph_sum", st);
         }
         launch_ks_finish(ctx_.dconsts(), P, dom, lv.base, lv.src, lv.ginv, lv.out, ACC_.words(), lv.items, st,
                          lv.extra, lv.yout, lv.xacc);

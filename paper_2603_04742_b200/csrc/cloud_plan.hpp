@@ -141,6 +141,12 @@ private:
         const u64* const* odd_src = nullptr;
         const u32* odd_ginv = nullptr;
         u64* const* odd_out = nullptr;
+        // fold mode: c0 terms summed into EXTRA slots (level 0 writes them, later levels add)
+        int asum_n = 0;
+        u64* const* asum_out = nullptr;
+        const u64* const* asum_src = nullptr;  // [item][3]
+        const u32* asum_gi = nullptr;           // [item][3] inverse Galois elements (0: none)
+        bool asum_acc = false;
     };
     std::vector<Level> levels_;
     const u64* const* FINAL_ = nullptr;

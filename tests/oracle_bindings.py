@@ -200,7 +200,7 @@ class BfvOracle:
         offs = np.array([o for o, _ in sched] or [0], np.int64)
         fa = np.array([int(f) for _, f in sched] or [0], np.int32)
         r = self.lib.bfvo_plan_fold(self.h, _p(_u64(z), u64p), len(sched), _p(offs, i64p), _p(fa, ip),
-                                    int(fold_relin), _p(out, u64p))
+                                    int(fold_relin), _p(out, u64p))  # 0 plain, 1 relin folded, 2 + merged stages
         assert r == 0, r
         return out
 

@@ -144,7 +144,7 @@ def test_cloud_plan_words_match_oracle(graph, shape):
     st = {}
     out = pk.cloud_plan(ctx, [r for r, _ in shapes], [c for _, c in shapes], slices, 3, ha, hb, graph=graph,
                         stats=st)
-    assert st["relin_folded"] == (1 if shape == 0 else 0)
+    assert st["relin_folded"] == (2 if shape == 0 else 0)  # fixed shape: folded level 0 + merged stages
     want = [None] * 3
     for i, (r, c) in enumerate(shapes):
         z = orc.mul_tensor(orc.encrypt(vals_a[i], sa[i]), orc.encrypt(vals_b[i], sb[i]))
@@ -176,12 +176,13 @@ def test_cloud_plan_fused_and_unfused_agree():
         st = {}
         out = pk.cloud_plan(ctx, [r for r, _ in shapes], [c for _, c in shapes], slices, 2, ha, hb, graph=True,
                             stats=st)
-        assert st["relin_folded"] == fused
+        assert st["relin_folded"] == 2 * fused
         got = [ctx.download(int(h)) for h in out]
         want = [None] * 2
         for i, (r, c) in enumerate(shapes):
             z = orc.mul_tensor(orc.encrypt(va[i], sa[i]), orc.encrypt(vb[i], sb[i]))
-            part = orc.mul_plain(orc.plan_fold_z(z, pk.rotation_schedule(r, c), fused), np.ones(r, np.int64))
+            part = orc.mul_plain(orc.plan_fold_z(z, pk.rotation_schedule(r, c), st["relin_folded"]),
+                                 np.ones(r, np.int64))
             want[slices[i]] = part if want[slices[i]] is None else orc.add(want[slices[i]], part)
         assert all(np.array_equal(g, w) for g, w in zip(got, want))
         outs[fused] = [orc.decrypt(g)[0] for g in got]
@@ -214,7 +215,7 @@ def test_folded_level0_matches_oracle_and_unfolded_values(monkeypatch):
         st = {}
         out = pk.cloud_plan(ctx, [r for r, _ in shapes], [c for _, c in shapes], slices, 2, ha, hb, graph=True,
                             stats=st)
-        assert st["relin_folded"] == (0 if off else 1)
+        assert st["relin_folded"] == (0 if off else 2)
         want = [None] * 2
         for i, (r, c) in enumerate(shapes):
             z = orc.mul_tensor(orc.encrypt(va[i], sa[i]), orc.encrypt(vb[i], sb[i]))
@@ -227,3 +228,37 @@ def test_folded_level0_matches_oracle_and_unfolded_values(monkeypatch):
         dec[off] = [orc.decrypt(g)[0] for g in got]
         ctx.close()
     assert all(np.array_equal(x, y) for x, y in zip(dec[""], dec["1"]))
+
+
+@pytest.mark.parametrize("merge", [True, False])
+def test_deep_trees_merged_stages_match_oracle(monkeypatch, merge):
+    """Deep intra-chunk trees (up to 8 doubling steps, odd steps at every
+    level): two doubling steps per key-switch stage after level 0 (default)
+    and one per stage (CSSC_NO_MERGE=1) each equal the oracle's plan fold word
+    for word."""
+    if merge:
+        monkeypatch.delenv("CSSC_NO_MERGE", raising=False)
+    else:
+        monkeypatch.setenv("CSSC_NO_MERGE", "1")
+    ctx = pk.Context(logn=11, seed=21)
+    orc = BfvOracle.like(ctx)
+    shapes = [(1, 255), (1, 170), (2, 100), (3, 77), (1, 64), (4, 31), (1, 9), (5, 3)]
+    slices = [0, 1, 0, 1, 2, 2, 0, 1]
+    rng = np.random.default_rng(33)
+    va = [rng.integers(-8, 9, r * c) for r, c in shapes]
+    vb = [rng.integers(-8, 9, r * c) for r, c in shapes]
+    sa, sb = [700 + i for i in range(len(shapes))], [800 + i for i in range(len(shapes))]
+    ha, hb = ctx.encrypt(va, sa), ctx.encrypt(vb, sb)
+    st = {}
+    out = pk.cloud_plan(ctx, [r for r, _ in shapes], [c for _, c in shapes], slices, 3, ha, hb, graph=True,
+                        stats=st)
+    assert st["relin_folded"] == (2 if merge else 1)
+    want = [None] * 3
+    for i, (r, c) in enumerate(shapes):
+        z = orc.mul_tensor(orc.encrypt(va[i], sa[i]), orc.encrypt(vb[i], sb[i]))
+        part = orc.mul_plain(orc.plan_fold_z(z, pk.rotation_schedule(r, c), st["relin_folded"]),
+                             np.ones(r, np.int64))
+        want[slices[i]] = part if want[slices[i]] is None else orc.add(want[slices[i]], part)
+    for s_ in range(3):
+        assert np.array_equal(ctx.download(int(out[s_])), want[s_]), s_
+    ctx.close()

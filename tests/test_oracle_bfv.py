@@ -177,7 +177,7 @@ def test_rotate2_add_decrypts_like_two_rotations(orc):
         assert np.array_equal(orc.decrypt(sep)[0].astype(np.int64), want)
 
 
-@pytest.mark.parametrize("r,c", [(1, 7), (3, 5), (2, 13), (4, 2), (1, 1)])
+@pytest.mark.parametrize("r,c", [(1, 7), (3, 5), (2, 13), (4, 2), (1, 1), (1, 15), (1, 27), (1, 16)])
 def test_plan_fold_both_forms_decrypt_to_the_intra_chunk_sum(orc, r, c):
     """bfvo_plan_fold from the product's tensor: unfolded (relin first) equals the
     rotate2_add fold of relin(z) word for word; folded (relinearisation inside
@@ -195,7 +195,8 @@ def test_plan_fold_both_forms_decrypt_to_the_intra_chunk_sum(orc, r, c):
                              relin.ctypes.data_as(C.POINTER(C.c_uint64)))
     unf = orc.plan_fold_z(z, sched, False)
     assert np.array_equal(unf, orc.plan_fold(relin, sched))
-    fol = orc.plan_fold_z(z, sched, True)
+    fol = orc.plan_fold_z(z, sched, 1)
+    mrg = orc.plan_fold_z(z, sched, 2)  # two doubling steps per key-switch stage after level 0
     prod = np.mod(a * b, T)
     want = np.zeros(S, np.int64)
     for k in range(c):  # blocks of r slots summed: slot i gets sum_k prod[i + k r]
@@ -203,3 +204,4 @@ def test_plan_fold_both_forms_decrypt_to_the_intra_chunk_sum(orc, r, c):
     want = np.mod(want, T)
     assert np.array_equal(orc.decrypt(unf)[0].astype(np.int64), want)
     assert np.array_equal(orc.decrypt(fol)[0].astype(np.int64), want)
+    assert np.array_equal(orc.decrypt(mrg)[0].astype(np.int64), want)
