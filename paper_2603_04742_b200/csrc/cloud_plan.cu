@@ -254,7 +254,11 @@ CloudPlan::CloudPlan(GpuContext& ctx, const std::vector<uint64_t>& r,
     // icols, scale + the 4-kernel relinearisation key switch
     const bool ksc = std::getenv("CSSC_KS_CLUSTER") != nullptr;
     auto kfuse = [&](int items) { return fused && !ksc && ks_cols_moddown_applies(P, items) ? 1 : 0; };
-    stats_.kernels = n ? (fused ? 9 - kfuse(n) : 14) : 0;
+    // multiply: extend, column phase, blocks + tensor, inverse columns, scale; the
+    // relinearisation's key switch (4 launches, 3 with the fused finish) for the
+    // products it is not folded into level 0 for
+    const int n_relin = fold ? n - nd : n;
+    stats_.kernels = n ? (fused ? 5 + (n_relin ? 4 - kfuse(n_relin) : 0) : 14) : 0;
     stats_.limb_ntts = (u64)n * (7 * M + P.dnum * LK + 2 * LK);  // + the rotate levels below
 
     std::set<u32> all_keys;
