@@ -222,6 +222,8 @@ static void floor_2_128_div(u64 q, u64* hi, u64* lo, u64* rem) {
 
 static void gen_primes(int bits, u64 twoN, int count, u64* out, const u64* used, int nused) {
     u64 top = (bits >= 64) ? ~0ull : ((1ull << bits) - 1);
+    /* the product's rule: primes = 1 mod 2^32, largest first */
+    if (twoN < (1ull << 32)) twoN = 1ull << 32;
     u64 cand = (top - 1) / twoN * twoN + 1;
     int got = 0;
     while (got < count) {

@@ -171,7 +171,11 @@ __global__ void __launch_bounds__(Ntt2<LOGN>::TC, 256 / Ntt2<LOGN>::TC * 3) k_nt
         return make_ulonglong2(tws[2 * k], tws[2 * k + 1]);
     };
     // radix-8 passes (3 CTAs per SM); 4-column tiles: radix-4, one group per thread
-    line_ntt_v<G::A, 0, INV, (LN >= 8 ? 3 : 2), LN>(tile, ConstQ{q}, addr, twf, whole_cta());
+    // ciphertext primes are = 1 mod 2^32 (cheaper product); the plaintext modulus is not
+    if ((u32)q == 1u)
+        line_ntt_v<G::A, 0, INV, (LN >= 8 ? 3 : 2), LN>(tile, SpecQ{q}, addr, twf, whole_cta());
+    else
+        line_ntt_v<G::A, 0, INV, (LN >= 8 ? 3 : 2), LN>(tile, ConstQ{q}, addr, twf, whole_cta());
     const u64 ni = dc->ninv[prime], nish = dc->ninv_sh[prime];
     const bool scale = INV && !job.lazy_out;
 #pragma unroll
@@ -298,7 +302,10 @@ __global__ void __launch_bounds__(128) k_ntt_blocks(const DevConsts* __restrict_
             cp_async_wait_all();
         }
         __syncthreads();
-        line_ntt<G::B, 0, INV>(cur, q, addr, twf);
+        if ((u32)q == 1u)
+            line_ntt_q<G::B, 0, INV>(cur, q, addr, twf);
+        else
+            line_ntt<G::B, 0, INV>(cur, q, addr, twf);
         u64* dst = job_dst(job, it, j, G::N) + base;
 #pragma unroll
         for (int r = 0; r < G::LINES * G::R2 / 256; ++r) {
@@ -461,7 +468,7 @@ __device__ __forceinline__ void extend_exact(const DevConsts* __restrict__ dc,
 #pragma unroll
     for (int i = 0; i < nx; ++i) {
         const u64 qi = dc->mod[e.xi[i]].q;
-        y[i] = shoup(x[i], e.xhat_inv[i], e.xhat_inv_sh[i], qi);
+        y[i] = shoup_q(x[i], e.xhat_inv[i], e.xhat_inv_sh[i], qi);
         add128(shi, slo, 0, frac64(y[i], e.R1[i], e.R0[i]));
     }
     const u64 v = shi + (slo >> 63);
@@ -471,9 +478,9 @@ __device__ __forceinline__ void extend_exact(const DevConsts* __restrict__ dc,
         // lazy sum: nx <= 16 terms < 2p each stay below 2^(k+5) -> one reduction
         u64 acc = 0;
 #pragma unroll
-        for (int i = 0; i < nx; ++i) acc += shoup_lazy(y[i], e.xhat_y[i][j], e.xhat_y_sh[i][j], p);
+        for (int i = 0; i < nx; ++i) acc += shoup_lazy_q(y[i], e.xhat_y[i][j], e.xhat_y_sh[i][j], p);
         acc = reduce_small_quot(acc, dc->mod[e.yi[j]]);
-        out[j] = sub_mod(acc, shoup(v, e.X_y[j], e.X_y_sh[j], p), p);
+        out[j] = sub_mod(acc, shoup_q(v, e.X_y[j], e.X_y_sh[j], p), p);
     }
 }
 
@@ -521,7 +528,7 @@ __device__ __forceinline__ void extend_k(const ExtK<NX, NY>& e, const u64* x, u6
     u64 shi = 0, slo = 0;
 #pragma unroll
     for (int i = 0; i < NX; ++i) {
-        y[i] = shoup(x[i], e.xhat_inv[i], e.xhat_inv_sh[i], e.xq[i]);
+        y[i] = shoup_q(x[i], e.xhat_inv[i], e.xhat_inv_sh[i], e.xq[i]);
         add128(shi, slo, 0, frac64(y[i], e.R1[i], e.R0[i]));
     }
     const u32 v = (u32)(shi + (slo >> 63));  // <= NX
@@ -561,7 +568,7 @@ __device__ __forceinline__ void mul_extend_overq(const ExtendK<L>& c, bool is_b,
     u64 shi = 0, slo = 0;
 #pragma unroll
     for (int i = 0; i < L; ++i) {
-        y[i] = shoup(x[i], c.qr.xhat_inv[i], c.qr.xhat_inv_sh[i], c.qr.xq[i]);
+        y[i] = shoup_q(x[i], c.qr.xhat_inv[i], c.qr.xhat_inv_sh[i], c.qr.xq[i]);
         add128(shi, slo, umulhi(y[i], c.theta[i]), y[i] * c.theta[i]);
     }
     const u64 rnd = shi + (slo >> 63);  // < L 2^58: rides in both Dot29 column sums (x 1)
@@ -639,7 +646,7 @@ __global__ void __launch_bounds__(128) k_mul_extend_enc(const __grid_constant__ 
     for (int i = 0; i < L; ++i) {
         const u64 q = c.x.qr.xq[i];
         u64 v = add_mod(cm[(size_t)i * n], lift_signed(e, q), q);
-        if (!poly) v = add_mod(v, shoup(m, c.delta[i], c.delta_sh[i], q), q);
+        if (!poly) v = add_mod(v, shoup_q(m, c.delta[i], c.delta_sh[i], q), q);
         x[i] = v;
         ct[(size_t)i * n] = v;
     }
@@ -679,7 +686,7 @@ __global__ void k_mul_scale_k(const __grid_constant__ ScaleK<L> c, const u64* __
     u64 shi = 0, slo = 0;
 #pragma unroll
     for (int kk = 0; kk < L; ++kk) {
-        y[kk] = shoup(z[(size_t)(L + kk) * n + k], c.RhatInv[kk], c.RhatInv_sh[kk], c.r[kk]);
+        y[kk] = shoup_q(z[(size_t)(L + kk) * n + k], c.RhatInv[kk], c.RhatInv_sh[kk], c.r[kk]);
         add128(shi, slo, umulhi(y[kk], c.T1[kk]), y[kk] * c.T1[kk]);
         add128(shi, slo, 0, umulhi(y[kk], c.T0[kk]));
     }
@@ -703,7 +710,7 @@ __global__ void k_mul_scale_k(const __grid_constant__ ScaleK<L> c, const u64* __
     u64* yy = r == 2 ? (D2Y ? D2Y + (size_t)item * L * n : nullptr) : (r == 1 && Y1 ? Y1[item] : nullptr);
     if (yy) {
 #pragma unroll
-        for (int i = 0; i < L; ++i) yy[(size_t)i * n + k] = shoup(o[i], c.dhi[i], c.dhi_sh[i], c.qm[i].q);
+        for (int i = 0; i < L; ++i) yy[(size_t)i * n + k] = shoup_q(o[i], c.dhi[i], c.dhi_sh[i], c.qm[i].q);
     }
 }
 
@@ -1072,7 +1079,7 @@ __global__ void __launch_bounds__(128, 6) k_ks_moddown(const DevConsts* __restri
 #pragma unroll
         for (int kk = 0; kk < K; ++kk) {
             const u64 pk = dc->mod[L + kk].q;
-            y[kk] = shoup(acc[(size_t)(L + kk) * n + k], dc->phat_inv[kk], dc->phat_inv_sh[kk], pk);
+            y[kk] = shoup_q(acc[(size_t)(L + kk) * n + k], dc->phat_inv[kk], dc->phat_inv_sh[kk], pk);
         }
         const u64* rs = (RSRC && p == 0) ? RSRC[it] : nullptr;
 #pragma unroll 2
@@ -1080,9 +1087,9 @@ __global__ void __launch_bounds__(128, 6) k_ks_moddown(const DevConsts* __restri
             const u64 q = dc->mod[j].q;
             u64 c = 0;
 #pragma unroll
-            for (int kk = 0; kk < K; ++kk) c += shoup_lazy(y[kk], dc->phat_q[kk][j], dc->phat_q_sh[kk][j], q);
+            for (int kk = 0; kk < K; ++kk) c += shoup_lazy_q(y[kk], dc->phat_q[kk][j], dc->phat_q_sh[kk][j], q);
             c = reduce_small_quot(c, dc->mod[j]);
-            u64 v = shoup(sub_mod(acc[(size_t)j * n + k], c, q), dc->Pinv_q[j], dc->Pinv_q_sh[j], q);
+            u64 v = shoup_q(sub_mod(acc[(size_t)j * n + k], c, q), dc->Pinv_q[j], dc->Pinv_q_sh[j], q);
             if (s) {
                 v = add_mod(v, out[(size_t)j * n + k], q);  // this thread's own first-pass word
             } else {
@@ -1141,7 +1148,7 @@ __global__ void __launch_bounds__(128, 6) k_ks_moddown_k(const __grid_constant__
         acc = ACC + ((size_t)it * 2 + p) * LK * n;
 #pragma unroll
         for (int kk = 0; kk < K; ++kk)
-            y[kk] = shoup(acc[(size_t)(L + kk) * n + k], c.phat_inv[kk], c.phat_inv_sh[kk], c.pk[kk]);
+            y[kk] = shoup_q(acc[(size_t)(L + kk) * n + k], c.phat_inv[kk], c.phat_inv_sh[kk], c.pk[kk]);
         rs = (RSRC && p == 0) ? RSRC[it] : nullptr;
     };
     auto term = [&](int j, const u64* y, const u64* acc, const u64* rs, int ridx, bool neg) {
@@ -1187,7 +1194,7 @@ __global__ void __launch_bounds__(128, 6) k_ks_moddown_k(const __grid_constant__
             if (rs) v = add_mod(v, neg ? neg_mod(rv[j], q) : rv[j], q);
             v = add_mod(v, bv[j], q);
             out[(size_t)j * n + k] = v;
-            if (yo) yo[(size_t)j * n + k] = shoup(v, c.dhi[j], c.dhi_sh[j], q);
+            if (yo) yo[(size_t)j * n + k] = shoup_q(v, c.dhi[j], c.dhi_sh[j], q);
         }
     } else if (pair < 0) {
 #pragma unroll 2
@@ -1197,7 +1204,7 @@ __global__ void __launch_bounds__(128, 6) k_ks_moddown_k(const __grid_constant__
             if (base) v = add_mod(v, base[(size_t)j * n + k], q);
             if (ex) v = add_mod(v, ex[(size_t)j * n + k], q);
             out[(size_t)j * n + k] = v;
-            if (yo) yo[(size_t)j * n + k] = shoup(v, c.dhi[j], c.dhi_sh[j], q);
+            if (yo) yo[(size_t)j * n + k] = shoup_q(v, c.dhi[j], c.dhi_sh[j], q);
         }
     } else {  // merged rotation of item `pair`, half of the limbs
         u64 y2[K];
@@ -1213,7 +1220,7 @@ __global__ void __launch_bounds__(128, 6) k_ks_moddown_k(const __grid_constant__
             if (base) v = add_mod(v, base[(size_t)j * n + k], q);
             if (ex) v = add_mod(v, ex[(size_t)j * n + k], q);
             out[(size_t)j * n + k] = v;
-            if (yo) yo[(size_t)j * n + k] = shoup(v, c.dhi[j], c.dhi_sh[j], q);
+            if (yo) yo[(size_t)j * n + k] = shoup_q(v, c.dhi[j], c.dhi_sh[j], q);
         }
     }
 }
@@ -1314,7 +1321,7 @@ __global__ void __launch_bounds__(Ntt2<LOGN>::TC, 256 / Ntt2<LOGN>::TC * (RADIX 
             const int k = (1 << sl) + blk;
             return *reinterpret_cast<const ulonglong2*>(mytw + 2 * k);
         };
-        line_ntt_v<G::A, 0, true, RADIX, VL>(tiles, ConstQ{myq}, addr, twf, whole_cta());
+        line_ntt_v<G::A, 0, true, RADIX, VL>(tiles, SpecQ{myq}, addr, twf, whole_cta());
     };
     // ModDown of element e of the transformed tiles of item `it` (+ its rotated c0)
     auto moddown = [&](int it, int e, u64 out[L]) {
@@ -1322,7 +1329,7 @@ __global__ void __launch_bounds__(Ntt2<LOGN>::TC, 256 / Ntt2<LOGN>::TC * (RADIX 
         u64 y[K];
 #pragma unroll
         for (int kk = 0; kk < K; ++kk)
-            y[kk] = shoup(tiles[at(L + kk, e)], c.phat_inv[kk], c.phat_inv_sh[kk], c.pk[kk]);
+            y[kk] = shoup_q(tiles[at(L + kk, e)], c.phat_inv[kk], c.phat_inv_sh[kk], c.pk[kk]);
         const u64* rs = (RSRC && p == 0) ? RSRC[it] : nullptr;
         bool neg = false;
         const int ridx = rs ? automorph_src(ginv ? ginv[it] : 0u, k, n, neg) : k;
@@ -1375,7 +1382,7 @@ __global__ void __launch_bounds__(Ntt2<LOGN>::TC, 256 / Ntt2<LOGN>::TC * (RADIX 
             if (base) x = add_mod(x, base[(size_t)j * n + k], q);
             if (ex) x = add_mod(x, ex[(size_t)j * n + k], q);
             out[(size_t)j * n + k] = x;
-            if (yo) yo[(size_t)j * n + k] = shoup(x, c.dhi[j], c.dhi_sh[j], q);
+            if (yo) yo[(size_t)j * n + k] = shoup_q(x, c.dhi[j], c.dhi_sh[j], q);
         }
     }
 }
@@ -2342,7 +2349,7 @@ __global__ void __launch_bounds__(256) k_bfly_peak(u64 q, u64 w0, u64 w0sh, int 
             for (int c = 0; c < 16; ++c) {
                 if (c & h) continue;
                 const u64 x = v[c];
-                const u64 y = shoup_lazy(v[c + h], w, wsh, q);
+                const u64 y = shoup_lazy_q(v[c + h], w, wsh, q);
                 v[c] = x + y;
                 v[c + h] = x - y + two_q;
             }

@@ -101,9 +101,9 @@ __global__ void __launch_bounds__(Ntt2<LOGN>::TC, 256 / Ntt2<LOGN>::TC * 3) k_ks
                     y = __ldg(ysrc + (size_t)i * G::N + idx);
                 } else {
                     const u64 x = __ldg(src + (size_t)i * G::N + idx);
-                    y = shoup(x, dc->dig_hat_inv[i], dc->dig_hat_inv_sh[i], qi);
+                    y = shoup_q(x, dc->dig_hat_inv[i], dc->dig_hat_inv_sh[i], qi);
                 }
-                v += shoup_lazy(y, dc->dig_hat[i][j], dc->dig_hat_sh[i][j], m);  // alpha <= 16 terms < 2m
+                v += shoup_lazy_q(y, dc->dig_hat[i][j], dc->dig_hat_sh[i][j], m);  // alpha <= 16 terms < 2m
             }
             // phi_g(ModUp(x)): the automorphism's sign applies to the converted limb (DESIGN 2.9)
             v = reduce_small_quot(v, dc->mod[j]);
@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(Ntt2<LOGN>::TC, 256 / Ntt2<LOGN>::TC * 3) k_ks
         const int k = (1 << sl) + blk;
         return make_ulonglong2(tws[2 * k], tws[2 * k + 1]);
     };
-    line_ntt_v<G::A, 0, false, (LN >= 8 ? 3 : 2), LN>(tile, ConstQ{m}, addr, twf, whole_cta());  // radix-8: 3 CTAs/SM
+    line_ntt_v<G::A, 0, false, (LN >= 8 ? 3 : 2), LN>(tile, SpecQ{m}, addr, twf, whole_cta());  // radix-8: 3 CTAs/SM
     u64* dst = DX + (((size_t)item * dnum + dg) * LK + j) * G::N;
     constexpr int SEG = LN / 2;
 #pragma unroll
@@ -180,10 +180,10 @@ __global__ void __launch_bounds__(Ntt2<LOGN>::TC, 256 / Ntt2<LOGN>::TC * 3)
             const u64 qi = dc->mod[i].q;
             if (ysrc) {  // hoisted factors of the un-rotated source; x_i = y_i [Q_d/q_i]_{q_i}
                 y[a] = __ldg(ysrc + (size_t)i * G::N + idx);
-                x[a] = shoup(y[a], dc->dig_hat[i][i], dc->dig_hat_sh[i][i], qi);
+                x[a] = shoup_q(y[a], dc->dig_hat[i][i], dc->dig_hat_sh[i][i], qi);
             } else {
                 x[a] = __ldg(src + (size_t)i * G::N + idx);
-                y[a] = shoup(x[a], dc->dig_hat_inv[i], dc->dig_hat_inv_sh[i], qi);
+                y[a] = shoup_q(x[a], dc->dig_hat_inv[i], dc->dig_hat_inv_sh[i], qi);
             }
         }
 #pragma unroll
@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(Ntt2<LOGN>::TC, 256 / Ntt2<LOGN>::TC * 3)
                 for (int a = 0; a < AT; ++a) {
                     const int i = lo + a;
                     if (i >= hi) break;
-                    v += shoup_lazy(y[a], dc->dig_hat[i][j], dc->dig_hat_sh[i][j], dc->mod[j].q);
+                    v += shoup_lazy_q(y[a], dc->dig_hat[i][j], dc->dig_hat_sh[i][j], dc->mod[j].q);
                 }
                 v = reduce_small_quot(v, dc->mod[j]);
             }
@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(Ntt2<LOGN>::TC, 256 / Ntt2<LOGN>::TC * 3)
         const int k = (1 << sl) + blk;
         return *reinterpret_cast<const ulonglong2*>(mytw + 2 * k);
     };
-    line_ntt_v<G::A, 0, false, 3, VL>(tile, ConstQ{myq}, addr, twf, whole_cta());
+    line_ntt_v<G::A, 0, false, 3, VL>(tile, SpecQ{myq}, addr, twf, whole_cta());
     u64* dst = DX + ((size_t)item * DN + dg) * LK * G::N;
     constexpr int SEG = LC / 2;
     static_assert(LC % 2 == 0, "pairs of columns per store");
@@ -320,7 +320,7 @@ __global__ void __launch_bounds__(kKsGroups * kKsGroupThreads) k_ks_blocks_inner
     __syncthreads();
 #pragma unroll 1
     for (int dg = grp; dg < dnum; dg += kKsGroups)
-        line_ntt_v<G::B, 0, false, KMR, LN>(work + dg * TW, ConstQ{q}, addr, twf, tg);
+        line_ntt_v<G::B, 0, false, KMR, LN>(work + dg * TW, SpecQ{q}, addr, twf, tg);
     __syncthreads();
     // inner product with both key polynomials (tiles in smem once the TMA
     // transaction completes); every position is read (all digits) and then
@@ -344,8 +344,8 @@ __global__ void __launch_bounds__(kKsGroups * kKsGroupThreads) k_ks_blocks_inner
             // the key's Shoup companions (stored after the key words, KW apart):
             // a constant-operand product instead of a Barrett reduction
             const u64 s0 = __ldg(key + KW + ko), s1 = __ldg(key + KW + ko + PL);
-            a0 = add_mod(a0, shoup(w, k0, s0, q), q);
-            a1 = add_mod(a1, shoup(w, k1, s1, q), q);
+            a0 = add_mod(a0, shoup_q(w, k0, s0, q), q);
+            a1 = add_mod(a1, shoup_q(w, k1, s1, q), q);
         }
         work[s0] = a0;
         work[TW + s0] = a1;
@@ -354,7 +354,7 @@ __global__ void __launch_bounds__(kKsGroups * kKsGroupThreads) k_ks_blocks_inner
     load_block_twiddles<LOGN, LN>(tws, dc->tw[j].inv, blk0);
     cp_async_wait_all();
     __syncthreads();
-    line_ntt_v<G::B, 0, true, KMR, LN>(work + grp * TW, ConstQ{q}, addr, twf, tg);  // group p: accumulator p
+    line_ntt_v<G::B, 0, true, KMR, LN>(work + grp * TW, SpecQ{q}, addr, twf, tg);  // group p: accumulator p
     __syncthreads();
 #pragma unroll
     for (int p = 0; p < 2; ++p) {
@@ -449,8 +449,8 @@ __global__ void __launch_bounds__(kKsGroups * kKsGroupThreads) k_ks_blocks_gathe
             }
 #pragma unroll
             for (int r = 0; r < PER; ++r) {
-                a0[r] = add_mod(a0[r], shoup(w[r], k0[r], c0[r], q), q);
-                a1[r] = add_mod(a1[r], shoup(w[r], k1[r], c1[r], q), q);
+                a0[r] = add_mod(a0[r], shoup_q(w[r], k0[r], c0[r], q), q);
+                a1[r] = add_mod(a1[r], shoup_q(w[r], k1[r], c1[r], q), q);
             }
         }
     }
@@ -462,7 +462,7 @@ __global__ void __launch_bounds__(kKsGroups * kKsGroupThreads) k_ks_blocks_gathe
     }
     cp_async_wait_all();
     __syncthreads();
-    line_ntt_v<G::B, 0, true, KMR, LN>(work + grp * TW, ConstQ{q}, addr, twf, tg);  // group p: accumulator p
+    line_ntt_v<G::B, 0, true, KMR, LN>(work + grp * TW, SpecQ{q}, addr, twf, tg);  // group p: accumulator p
     __syncthreads();
 #pragma unroll
     for (int p = 0; p < 2; ++p) {

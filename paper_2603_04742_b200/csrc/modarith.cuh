@@ -112,6 +112,45 @@ CSSC_HD u64 shoup(u64 a, u64 w, u64 wsh, u64 q) {
     return r >= q ? r - q : r;
 }
 
+// The same product for the ciphertext primes.  Every prime of Q, P and the
+// multiply's extension base is chosen = 1 mod 2^32 (rns_params.cpp,
+// pick_primes): q = h 2^32 + 1, so qh * q mod 2^64 = qh + ((lo32(qh) * h) << 32)
+// and the low words of a*w - qh*q cost one IMAD.WIDE.U32 + three IMAD and a
+// 64-bit subtraction on the ALU pipe (IADD3 / IADD3.X) instead of two
+// IMAD.WIDE.U32 + four IMAD: 8 instead of 10 FMA-pipe operations per product.
+// Same value as shoup_lazy for such q (both are a*w - qh*q mod 2^64); the
+// plaintext modulus t is not of this form and keeps shoup_lazy.
+#ifndef CSSC_Q32
+#define CSSC_Q32 1
+#endif
+CSSC_HD u64 shoup_lazy_q(u64 a, u64 w, u64 wsh, u64 q) {
+#if CSSC_Q32 && defined(__CUDA_ARCH__)
+    const u64 qh = umulhi(a, wsh);
+    const unsigned nh = 0u - (unsigned)(q >> 32);
+    u64 r;
+    asm("{\n\t.reg .u32 a0, a1, w0, w1, h0, h1, tl, th;\n\t.reg .u64 t;\n\t"
+        "mov.b64 {a0, a1}, %1;\n\tmov.b64 {w0, w1}, %2;\n\t"
+        "mov.b64 {h0, h1}, %3;\n\t"
+        "mul.wide.u32 t, a0, w0;\n\t"
+        "mov.b64 {tl, th}, t;\n\t"
+        "mad.lo.u32 th, a0, w1, th;\n\t"
+        "mad.lo.u32 th, a1, w0, th;\n\t"
+        "mad.lo.u32 th, h0, %4, th;\n\t"
+        "sub.cc.u32 tl, tl, h0;\n\t"
+        "subc.u32 th, th, h1;\n\t"
+        "mov.b64 %0, {tl, th};\n\t}"
+        : "=l"(r)
+        : "l"(a), "l"(w), "l"(qh), "r"(nh));
+    return r;
+#else
+    return shoup_lazy(a, w, wsh, q);
+#endif
+}
+CSSC_HD u64 shoup_q(u64 a, u64 w, u64 wsh, u64 q) {
+    u64 r = shoup_lazy_q(a, w, wsh, q);
+    return r >= q ? r - q : r;
+}
+
 // (z1 * 2^64 + z0) mod q for z1 < q; mu = floor(2^128 / q) = mu1 * 2^64 + mu0.
 // The quotient estimate is at most 2 short, hence two conditional subtractions.
 CSSC_HD u64 reduce128(u64 z1, u64 z0, u64 q, u64 mu1, u64 mu0) {

@@ -73,7 +73,7 @@ __global__ void __launch_bounds__(kMulGroups * kGroupThreads) k_mul_blocks_tenso
     __syncthreads();
 #pragma unroll 1
     for (int p = grp; p < 4; p += kMulGroups)
-        line_ntt_v<G::B, 0, false, MAXR, LN>(tile + p * TW, ConstQ{q}, addr, twf, tg);
+        line_ntt_v<G::B, 0, false, MAXR, LN>(tile + p * TW, SpecQ{q}, addr, twf, tg);
     __syncthreads();
     // tensor: all four inputs canonicalised (cheap 32-bit quotient estimate),
     // so z1 = a0 b1 + a1 b0 < 2 q^2 < 2^117 is one 128-bit sum under a single
@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(kMulGroups * kGroupThreads) k_mul_blocks_tenso
     __syncthreads();
 #pragma unroll 1
     for (int p = grp; p < 3; p += kMulGroups)
-        line_ntt_v<G::B, 0, true, MAXR, LN>(tile + p * TW, ConstQ{q}, addr, twf, tg);
+        line_ntt_v<G::B, 0, true, MAXR, LN>(tile + p * TW, SpecQ{q}, addr, twf, tg);
     __syncthreads();
     u64* dst = Z + (size_t)item * 3 * PM + (size_t)j * G::N + base;
 #pragma unroll
@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(2 * kGroupThreads) k_mask_blocks(const DevCons
         }
         cp_async_wait_all();
         tg.sync();
-        line_ntt_v<G::B, 0, false, (LN >= 16 ? 4 : 2), LN>(wk, ConstQ{q}, addr, twf, tg);
+        line_ntt_v<G::B, 0, false, (LN >= 16 ? 4 : 2), LN>(wk, SpecQ{q}, addr, twf, tg);
         const u64* mk = MASKS + ((size_t)item_mask[it] * L + j) * G::N + base;
 #pragma unroll
         for (int r = 0; r < PERG; ++r) {
@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(2 * kGroupThreads) k_mask_blocks(const DevCons
     load_block_twiddles<LOGN, LN>(tws, dc->tw[j].inv, blk0);
     cp_async_wait_all();
     __syncthreads();
-    line_ntt_v<G::B, 0, true, 2, LN>(acc, ConstQ{q}, addr, twf, whole_cta());  // radix-4: more threads busy
+    line_ntt_v<G::B, 0, true, 2, LN>(acc, SpecQ{q}, addr, twf, whole_cta());  // radix-4: more threads busy
     u64* dst = OUT[sl] + (size_t)j2 * G::N + base;
 #pragma unroll
     for (int r = 0; r < PER; ++r) {
@@ -271,7 +271,7 @@ __global__ void __launch_bounds__(4 * kGroupThreads) k_mask_dec_blocks(const Dev
         }
         cp_async_wait_all();
         tg.sync();
-        line_ntt_v<G::B, 0, false, (LN >= 16 ? 4 : 2), LN>(wk, ConstQ{q}, addr, twf, tg);
+        line_ntt_v<G::B, 0, false, (LN >= 16 ? 4 : 2), LN>(wk, SpecQ{q}, addr, twf, tg);
         const u64* mk = MASKS + ((size_t)item_mask[it] * L + j) * G::N + base;
 #pragma unroll
         for (int r = 0; r < PERG; ++r) {
@@ -297,7 +297,7 @@ __global__ void __launch_bounds__(4 * kGroupThreads) k_mask_dec_blocks(const Dev
     load_block_twiddles<LOGN, LN>(tws, dc->tw[j].inv, blk0);
     cp_async_wait_all();
     __syncthreads();
-    line_ntt_v<G::B, 0, true, 2, LN>(acc, ConstQ{q}, addr, twf, whole_cta());  // radix-4: more threads busy
+    line_ntt_v<G::B, 0, true, 2, LN>(acc, SpecQ{q}, addr, twf, whole_cta());  // radix-4: more threads busy
     u64* dst = D + ((size_t)sl * L + j) * G::N + base;
 #pragma unroll
     for (int r = 0; r < PER; ++r) {
@@ -437,7 +437,7 @@ __global__ void __launch_bounds__(mulb_threads<LOGN>()) k_blocks_mul_inv(const D
     }
     cp_async_wait_all();
     __syncthreads();
-    line_ntt<G::B, 0, false>(tile, q, addr, twf);
+    line_ntt_q<G::B, 0, false>(tile, q, addr, twf);
 #pragma unroll
     for (int r = 0; r < PER; ++r) {
         const int y = threadIdx.x + NT * r, s0 = saddr(y);
@@ -446,7 +446,7 @@ __global__ void __launch_bounds__(mulb_threads<LOGN>()) k_blocks_mul_inv(const D
         for (int p = 0; p < NMUL; ++p) {
             const size_t o = ((size_t)p * L + j) * G::N + base + y;
             // fixed multipliers (pk, s) with stored Shoup companions: no Barrett reduction
-            tile[(p + 1) * TW + s0] = MULSH ? shoup(w, __ldg(MUL + o), __ldg(MULSH + o), q) : mul_mod(w, __ldg(MUL + o), md);
+            tile[(p + 1) * TW + s0] = MULSH ? shoup_q(w, __ldg(MUL + o), __ldg(MULSH + o), q) : mul_mod(w, __ldg(MUL + o), md);
         }
     }
     __syncthreads();
@@ -454,7 +454,7 @@ __global__ void __launch_bounds__(mulb_threads<LOGN>()) k_blocks_mul_inv(const D
     cp_async_wait_all();
     __syncthreads();
 #pragma unroll 1
-    for (int p = 0; p < NMUL; ++p) line_ntt<G::B, 0, true>(tile + (p + 1) * TW, q, addr, twf);
+    for (int p = 0; p < NMUL; ++p) line_ntt_q<G::B, 0, true>(tile + (p + 1) * TW, q, addr, twf);
 #pragma unroll
     for (int p = 0; p < NMUL; ++p) {
         u64* dst = OUT + (size_t)item * out_stride + ((size_t)p * L + j) * G::N + base;

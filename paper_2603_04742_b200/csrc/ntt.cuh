@@ -149,9 +149,23 @@ __device__ __forceinline__ ThreadGroup cta_slice(int g, int groups) {
 
 // the modulus of every line of a tile (one prime per tile)
 struct ConstQ {
+    static constexpr bool kSpecial = false;
     u64 q;
     __device__ __forceinline__ u64 operator()(int) const { return q; }
 };
+// the same for a ciphertext prime (= 1 mod 2^32): butterflies use shoup_lazy_q
+struct SpecQ {
+    static constexpr bool kSpecial = true;
+    u64 q;
+    __device__ __forceinline__ u64 operator()(int) const { return q; }
+};
+template <class QF>
+__device__ __forceinline__ u64 shoup_lazy_of(u64 a, u64 w, u64 wsh, u64 q) {
+    if constexpr (QF::kSpecial)
+        return shoup_lazy_q(a, w, wsh, q);
+    else
+        return shoup_lazy(a, w, wsh, q);
+}
 
 // One radix-2^R pass over local stages [S0L, S0L+R) of VL lines of length 2^RB.
 // addr(l, pos): smem word of element pos of line l.  tw(sl, l, blk): twiddle
@@ -187,7 +201,7 @@ __device__ __forceinline__ void line_pass(u64* s, QF qf, Addr addr, Tw tw, const
                     // q < 2^58 (enforced by RnsParams) and is reduced once at the end
                     const ulonglong2 w = tw(S0L + u, l, (blk << u) + (k >> (R - u)));
                     const u64 x = v[k];
-                    const u64 y = shoup_lazy(v[k + h], w.x, w.y, q);
+                    const u64 y = shoup_lazy_of<QF>(v[k + h], w.x, w.y, q);
                     v[k] = NTT_ADD(x, y);
                     v[k + h] = NTT_SUBADD(x, y, two_q);
                 }
@@ -204,7 +218,7 @@ __device__ __forceinline__ void line_pass(u64* s, QF qf, Addr addr, Tw tw, const
                     u64 sm = NTT_ADD(x, y);
                     sm = sm >= two_q ? sm - two_q : sm;
                     v[k] = sm;
-                    v[k + h] = shoup_lazy(NTT_SUBADD(x, y, two_q), w.x, w.y, q);
+                    v[k + h] = shoup_lazy_of<QF>(NTT_SUBADD(x, y, two_q), w.x, w.y, q);
                 }
             }
         }
@@ -243,6 +257,11 @@ __device__ __forceinline__ void line_ntt(u64* s, u64 q, Addr addr, Tw tw, const 
 template <int RB, int S0L, bool INV, int MAXR = 4, class Addr, class Tw>
 __device__ __forceinline__ void line_ntt(u64* s, u64 q, Addr addr, Tw tw) {
     line_ntt<RB, S0L, INV, MAXR>(s, q, addr, tw, whole_cta());
+}
+// the whole CTA on 16 lines of one ciphertext prime
+template <int RB, int S0L, bool INV, int MAXR = 4, class Addr, class Tw>
+__device__ __forceinline__ void line_ntt_q(u64* s, u64 q, Addr addr, Tw tw) {
+    line_ntt_v<RB, S0L, INV, MAXR, 16>(s, SpecQ{q}, addr, tw, whole_cta());
 }
 
 }  // namespace cssc

@@ -64,9 +64,12 @@ unsigned reverse_bits(unsigned x, int bits) {
     return r;
 }
 
-// Largest primes below 2^bits with p = 1 mod 2N, skipping `taken`.
+// Largest primes below 2^bits with p = 1 mod 2^32 (hence = 1 mod 2N for every
+// ring here), skipping `taken`: q = h 2^32 + 1 makes the quotient correction
+// qh * q of every Shoup product one 32-bit multiply (modarith.cuh, shoup_lazy_q).
 void pick_primes(int bits, u64 two_n, int count, std::vector<u64>& out) {
     const u64 top = (1ull << bits) - 1;
+    two_n = std::max<u64>(two_n, 1ull << 32);
     u64 cand = (top - 1) / two_n * two_n + 1;
     int got = 0;
     while (got < count) {
@@ -135,9 +138,9 @@ RnsParams::RnsParams(const RnsConfig& c) : cfg(c), host{} {
     // L + 1 <= 16 auxiliary terms keep the lazy basis-conversion sums below 32 q
     if (c.L < 1 || c.L > MAXL - 1 || c.K < 1 || c.K > MAXL || c.alpha < 1 || c.alpha > c.L)
         throw std::invalid_argument("prime counts out of range");
-    if (c.qbits < 30 || c.qbits > 58 || c.pbits < 30 || c.pbits > 58)
+    if (c.qbits < 44 || c.qbits > 58 || c.pbits < 44 || c.pbits > 58)
         // <= 58 bits: 64q headroom lets the forward NTT skip per-butterfly corrections
-        throw std::invalid_argument("prime bit sizes must be in [30, 58]");
+        throw std::invalid_argument("prime bit sizes must be in [44, 58]");
     n = 1 << c.logn;
     S = n / 2;
     const u64 two_n = 2 * (u64)n;
