@@ -312,8 +312,8 @@ __global__ void __launch_bounds__(128) k_ntt_blocks(const DevConsts* __restrict_
             const int x = 2 * (threadIdx.x + 128 * r), b = x >> G::B, c = x & (G::R2 - 1);
             u64 a0 = cur[b * PITCH + c], a1 = cur[b * PITCH + c + 1];
             if (!INV) {  // forward output < 31q -> canonical
-                a0 = reduce_small_quot(a0, md);
-                a1 = reduce_small_quot(a1, md);
+                a0 = (u32)q == 1u ? reduce_small_quot_q(a0, md) : reduce_small_quot(a0, md);
+                a1 = (u32)q == 1u ? reduce_small_quot_q(a1, md) : reduce_small_quot(a1, md);
             }
             *reinterpret_cast<ulonglong2*>(dst + x) = make_ulonglong2(a0, a1);
         }
@@ -479,7 +479,7 @@ __device__ __forceinline__ void extend_exact(const DevConsts* __restrict__ dc,
         u64 acc = 0;
 #pragma unroll
         for (int i = 0; i < nx; ++i) acc += shoup_lazy_q(y[i], e.xhat_y[i][j], e.xhat_y_sh[i][j], p);
-        acc = reduce_small_quot(acc, dc->mod[e.yi[j]]);
+        acc = reduce_small_quot_q(acc, dc->mod[e.yi[j]]);
         out[j] = sub_mod(acc, shoup_q(v, e.X_y[j], e.X_y_sh[j], p), p);
     }
 }
@@ -538,7 +538,7 @@ __device__ __forceinline__ void extend_k(const ExtK<NX, NY>& e, const u64* x, u6
 #pragma unroll
         for (int i = 0; i < NX; ++i) dot29_mac(d, y[i], e.w[i][j]);
         dot29_mac_small(d, v, e.nX[j]);
-        out[j] = dot29_reduce(d, e.ym[j]);
+        out[j] = dot29_reduce_q(d, e.ym[j]);
     }
 }
 
@@ -578,7 +578,7 @@ __device__ __forceinline__ void mul_extend_overq(const ExtendK<L>& c, bool is_b,
         d.a0 = d.am = rnd;
 #pragma unroll
         for (int i = 0; i < L; ++i) dot29_mac(d, y[i], c.omega[i][k]);
-        ro[k] = dot29_reduce(d, c.qr.ym[k]);
+        ro[k] = dot29_reduce_q(d, c.qr.ym[k]);
     }
     extend_k(c.rq, ro, qo);
 }
@@ -700,7 +700,7 @@ __global__ void k_mul_scale_k(const __grid_constant__ ScaleK<L> c, const u64* __
         dot29_mac(d, zq, c.A[j]);
 #pragma unroll
         for (int kk = 0; kk < L; ++kk) dot29_mac(d, y[kk], c.C[kk][j]);
-        o[j] = dot29_reduce(d, c.qm[j]);
+        o[j] = dot29_reduce_q(d, c.qm[j]);
     }
     u64* dst = r < 2 ? OUT[item] + (size_t)r * L * n : D2 + (size_t)item * L * n;
 #pragma unroll
@@ -1088,7 +1088,7 @@ __global__ void __launch_bounds__(128, 6) k_ks_moddown(const DevConsts* __restri
             u64 c = 0;
 #pragma unroll
             for (int kk = 0; kk < K; ++kk) c += shoup_lazy_q(y[kk], dc->phat_q[kk][j], dc->phat_q_sh[kk][j], q);
-            c = reduce_small_quot(c, dc->mod[j]);
+            c = reduce_small_quot_q(c, dc->mod[j]);
             u64 v = shoup_q(sub_mod(acc[(size_t)j * n + k], c, q), dc->Pinv_q[j], dc->Pinv_q_sh[j], q);
             if (s) {
                 v = add_mod(v, out[(size_t)j * n + k], q);  // this thread's own first-pass word
@@ -1159,7 +1159,7 @@ __global__ void __launch_bounds__(128, 6) k_ks_moddown_k(const __grid_constant__
         dot29_mac(d, a, c.F[j]);
 #pragma unroll
         for (int kk = 0; kk < K; ++kk) dot29_mac(d, y[kk], c.E[kk][j]);
-        u64 v = dot29_reduce(d, c.qm[j]);
+        u64 v = dot29_reduce_q(d, c.qm[j]);
         if (rs) {
             const u64 r = rs[(size_t)j * n + ridx];
             v = add_mod(v, neg ? neg_mod(r, q) : r, q);
@@ -1190,7 +1190,7 @@ __global__ void __launch_bounds__(128, 6) k_ks_moddown_k(const __grid_constant__
             dot29_mac(d, av[j], c.F[j]);
 #pragma unroll
             for (int kk = 0; kk < K; ++kk) dot29_mac(d, y[kk], c.E[kk][j]);
-            u64 v = dot29_reduce(d, c.qm[j]);
+            u64 v = dot29_reduce_q(d, c.qm[j]);
             if (rs) v = add_mod(v, neg ? neg_mod(rv[j], q) : rv[j], q);
             v = add_mod(v, bv[j], q);
             out[(size_t)j * n + k] = v;
@@ -1342,7 +1342,7 @@ __global__ void __launch_bounds__(Ntt2<LOGN>::TC, 256 / Ntt2<LOGN>::TC * (RADIX 
             dot29_mac(d, a, c.F[j]);
 #pragma unroll
             for (int kk = 0; kk < K; ++kk) dot29_mac(d, y[kk], c.E[kk][j]);
-            u64 v = dot29_reduce(d, c.qm[j]);
+            u64 v = dot29_reduce_q(d, c.qm[j]);
             if (rs) {
                 const u64 r = rs[(size_t)j * n + ridx];
                 v = add_mod(v, neg ? neg_mod(r, q) : r, q);

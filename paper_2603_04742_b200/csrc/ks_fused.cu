@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(Ntt2<LOGN>::TC, 256 / Ntt2<LOGN>::TC * 3) k_ks
                 v += shoup_lazy_q(y, dc->dig_hat[i][j], dc->dig_hat_sh[i][j], m);  // alpha <= 16 terms < 2m
             }
             // phi_g(ModUp(x)): the automorphism's sign applies to the converted limb (DESIGN 2.9)
-            v = reduce_small_quot(v, dc->mod[j]);
+            v = reduce_small_quot_q(v, dc->mod[j]);
             v = neg ? neg_mod(v, m) : v;
         }
         tile[c * LN + jl] = v;
@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(Ntt2<LOGN>::TC, 256 / Ntt2<LOGN>::TC * 3)
                     if (i >= hi) break;
                     v += shoup_lazy_q(y[a], dc->dig_hat[i][j], dc->dig_hat_sh[i][j], dc->mod[j].q);
                 }
-                v = reduce_small_quot(v, dc->mod[j]);
+                v = reduce_small_quot_q(v, dc->mod[j]);
             }
             // phi_g(ModUp(x)): the automorphism's sign on every target limb (DESIGN 2.9)
             tile[c * VL + j * LC + jl] = neg ? neg_mod(v, dc->mod[j].q) : v;

@@ -197,6 +197,35 @@ CSSC_HD u64 barrett(u64 z1, u64 z0, const Modulus& m) {
 
 CSSC_HD u64 mul_mod(u64 a, u64 b, const Modulus& m) { return barrett(umulhi(a, b), a * b, m); }
 
+// z - qh * q mod 2^64 for a ciphertext prime q = h 2^32 + 1 (see shoup_lazy_q):
+// one IMAD into the high word and a 64-bit subtraction on the ALU pipe
+CSSC_HD u64 sub_qh_q(u64 z, u64 qh, u64 q) {
+#if CSSC_Q32 && defined(__CUDA_ARCH__)
+    const unsigned nh = 0u - (unsigned)(q >> 32);
+    u64 r;
+    asm("{\n\t.reg .u32 zl, zh, h0, h1;\n\t"
+        "mov.b64 {zl, zh}, %1;\n\tmov.b64 {h0, h1}, %2;\n\t"
+        "mad.lo.u32 zh, h0, %3, zh;\n\t"
+        "sub.cc.u32 zl, zl, h0;\n\t"
+        "subc.u32 zh, zh, h1;\n\t"
+        "mov.b64 %0, {zl, zh};\n\t}"
+        : "=l"(r)
+        : "l"(z), "l"(qh), "r"(nh));
+    return r;
+#else
+    return z - qh * q;
+#endif
+}
+// barrett / mul_mod for a ciphertext prime (same value)
+CSSC_HD u64 barrett_q(u64 z1, u64 z0, const Modulus& m) {
+    const u64 x = (z0 >> m.sh) | (z1 << (64 - m.sh));
+    const u64 qh = umulhi(x, m.mub);
+    u64 r = sub_qh_q(z0, qh, m.q);
+    r = r >= m.q ? r - m.q : r;
+    return r >= m.q ? r - m.q : r;
+}
+CSSC_HD u64 mul_mod_q(u64 a, u64 b, const Modulus& m) { return barrett_q(umulhi(a, b), a * b, m); }
+
 // Exact dot products for the basis conversions: sum_i y_i * w_i mod p with
 // every y_i < 2^58 (canonical residues) and constant w_i < p <= 2^58.  Both
 // factors are split into 29-bit halves and each term is three 32x32->64
@@ -243,6 +272,15 @@ CSSC_HD u64 dot29_reduce(const Dot29& d, const Modulus& m) {
     hi += lo2 < u;
     return barrett(hi, lo2, m);
 }
+CSSC_HD u64 dot29_reduce_q(const Dot29& d, const Modulus& m) {  // m a ciphertext prime
+    const u64 mid = d.am - d.a0 - d.ah;
+    const u64 t = mid << 29, u = d.ah << 58;
+    const u64 lo = d.a0 + t;
+    u64 hi = (mid >> 35) + (d.ah >> 6) + (lo < t);
+    const u64 lo2 = lo + u;
+    hi += lo2 < u;
+    return barrett_q(hi, lo2, m);
+}
 inline W29 split29(u64 w) {
     const u32 lo = (u32)(w & kMask29), hi = (u32)(w >> 29);
     return W29{lo, hi, lo + hi};
@@ -257,6 +295,12 @@ CSSC_HD u64 reduce_small_quot(u64 a, const Modulus& m) {
     const u32 x = (u32)(a >> (m.sh - 5));
     const u32 qh = (x * m.mus) >> 26;
     const u64 r = a - (u64)qh * m.q;
+    return r >= m.q ? r - m.q : r;
+}
+CSSC_HD u64 reduce_small_quot_q(u64 a, const Modulus& m) {  // m a ciphertext prime
+    const u32 x = (u32)(a >> (m.sh - 5));
+    const u32 qh = (x * m.mus) >> 26;
+    const u64 r = sub_qh_q(a, (u64)qh, m.q);
     return r >= m.q ? r - m.q : r;
 }
 CSSC_HD u64 reduce64(u64 a, const Modulus& m) { return reduce128(0, a, m.q, m.mu1, m.mu0); }

@@ -81,8 +81,8 @@ __global__ void __launch_bounds__(kMulGroups * kGroupThreads) k_mul_blocks_tenso
 #pragma unroll
     for (int r = 0; r < PER; ++r) {
         const int s0 = saddr(threadIdx.x + NT * r);
-        const u64 a0 = reduce_small_quot(tile[s0], md), a1 = reduce_small_quot(tile[TW + s0], md);
-        const u64 b0 = reduce_small_quot(tile[2 * TW + s0], md), b1 = reduce_small_quot(tile[3 * TW + s0], md);
+        const u64 a0 = reduce_small_quot_q(tile[s0], md), a1 = reduce_small_quot_q(tile[TW + s0], md);
+        const u64 b0 = reduce_small_quot_q(tile[2 * TW + s0], md), b1 = reduce_small_quot_q(tile[3 * TW + s0], md);
         // products as 29-bit Karatsuba column sums (three IMAD.WIDE.U32 each),
         // one Barrett reduction per output: the canonical words of mul_mod
         Dot29 d0, d1, d2;
@@ -90,9 +90,9 @@ __global__ void __launch_bounds__(kMulGroups * kGroupThreads) k_mul_blocks_tenso
         dot29_mac_var(d1, a0, b1);
         dot29_mac_var(d1, a1, b0);
         dot29_mac_var(d2, a1, b1);
-        tile[s0] = dot29_reduce(d0, md);
-        tile[TW + s0] = dot29_reduce(d1, md);
-        tile[2 * TW + s0] = dot29_reduce(d2, md);
+        tile[s0] = dot29_reduce_q(d0, md);
+        tile[TW + s0] = dot29_reduce_q(d1, md);
+        tile[2 * TW + s0] = dot29_reduce_q(d2, md);
     }
     __syncthreads();
     load_block_twiddles<LOGN, LN>(tws, dc->tw[prime].inv, blk0);
@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(2 * kGroupThreads) k_mask_blocks(const DevCons
 #pragma unroll
         for (int r = 0; r < PERG; ++r) {
             const int y = tg.tid + kGroupThreads * r, s0 = saddr(y);
-            const u64 p = mul_mod(wk[s0], __ldg(mk + y), md);  // lazy (< 31q) x canonical mask
+            const u64 p = mul_mod_q(wk[s0], __ldg(mk + y), md);  // lazy (< 31q) x canonical mask
             ac[s0] = any ? add_mod(ac[s0], p, q) : p;
         }
         any = true;
@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(4 * kGroupThreads) k_mask_dec_blocks(const Dev
 #pragma unroll
         for (int r = 0; r < PERG; ++r) {
             const int y = tg.tid + kGroupThreads * r, s0 = saddr(y);
-            const u64 p = mul_mod(wk[s0], __ldg(mk + y), md);
+            const u64 p = mul_mod_q(wk[s0], __ldg(mk + y), md);
             ac[s0] = any ? add_mod(ac[s0], p, q) : p;
         }
         any = true;
@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(4 * kGroupThreads) k_mask_dec_blocks(const Dev
     for (int r = 0; r < PER; ++r) {
         const int y = threadIdx.x + NT * r, s0 = saddr(y);
         const u64 c0 = add_mod(acc[s0], acc[TW + s0], q), c1 = add_mod(acc[2 * TW + s0], acc[3 * TW + s0], q);
-        acc[s0] = add_mod(c0, mul_mod(c1, __ldg(sk + y), md), q);
+        acc[s0] = add_mod(c0, mul_mod_q(c1, __ldg(sk + y), md), q);
     }
     __syncthreads();
     load_block_twiddles<LOGN, LN>(tws, dc->tw[j].inv, blk0);
@@ -446,7 +446,7 @@ __global__ void __launch_bounds__(mulb_threads<LOGN>()) k_blocks_mul_inv(const D
         for (int p = 0; p < NMUL; ++p) {
             const size_t o = ((size_t)p * L + j) * G::N + base + y;
             // fixed multipliers (pk, s) with stored Shoup companions: no Barrett reduction
-            tile[(p + 1) * TW + s0] = MULSH ? shoup_q(w, __ldg(MUL + o), __ldg(MULSH + o), q) : mul_mod(w, __ldg(MUL + o), md);
+            tile[(p + 1) * TW + s0] = MULSH ? shoup_q(w, __ldg(MUL + o), __ldg(MULSH + o), q) : mul_mod_q(w, __ldg(MUL + o), md);
         }
     }
     __syncthreads();
