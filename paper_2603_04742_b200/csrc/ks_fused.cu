@@ -249,6 +249,27 @@ static int k1_all_mode() {
 // transformed two at a time, and the two accumulators' inverse transforms run
 // concurrently, so a CTA's serial chain is ceil(dnum/2) + 1 tile transforms.
 constexpr int kKsGroups = 2, kKsGroupThreads = 128;
+// Key MAC: lazy sums.  Every Shoup product is < 2q and q < 2^58, so 15 of them
+// stay below 2^(k+5), reduce_small_quot_q's domain: one reduction per sum
+// instead of two conditional subtractions per term (CSSC_LAZY_MAC=0: the eager form).
+#ifndef CSSC_LAZY_MAC
+#define CSSC_LAZY_MAC 1
+#endif
+constexpr int kLazyMacTerms = 15;
+__device__ __forceinline__ void mac_term(u64& a, u64 w, u64 k, u64 ksh, u64 q) {
+#if CSSC_LAZY_MAC
+    a += shoup_lazy_q(w, k, ksh, q);
+#else
+    a = add_mod(a, shoup_q(w, k, ksh, q), q);
+#endif
+}
+__device__ __forceinline__ u64 mac_reduce(u64 a, const Modulus& md) {
+#if CSSC_LAZY_MAC
+    return reduce_small_quot_q(a, md);
+#else
+    return a;
+#endif
+}
 template <int LOGN>
 constexpr bool ks_keys_tma() { return LOGN <= 14; }
 
@@ -330,7 +351,14 @@ __global__ void __launch_bounds__(kKsGroups * kKsGroupThreads) k_ks_blocks_inner
     for (int r = 0; r < PER; ++r) {
         const int x = threadIdx.x + T * r, s0 = saddr(x);
         u64 a0 = 0, a1 = 0;
+        int pend = 0;
         for (int dg = 0; dg < dnum; ++dg) {
+            if (pend == kLazyMacTerms) {
+                a0 = mac_reduce(a0, md);
+                a1 = mac_reduce(a1, md);
+                pend = 1;
+            }
+            ++pend;
             const u64 w = work[dg * TW + s0];
             u64 k0, k1;
             const size_t ko = ((size_t)dg * 2) * PL + (size_t)j * G::N + base + x;
@@ -344,11 +372,11 @@ __global__ void __launch_bounds__(kKsGroups * kKsGroupThreads) k_ks_blocks_inner
             // the key's Shoup companions (stored after the key words, KW apart):
             // a constant-operand product instead of a Barrett reduction
             const u64 s0 = __ldg(key + KW + ko), s1 = __ldg(key + KW + ko + PL);
-            a0 = add_mod(a0, shoup_q(w, k0, s0, q), q);
-            a1 = add_mod(a1, shoup_q(w, k1, s1, q), q);
+            mac_term(a0, w, k0, s0, q);
+            mac_term(a1, w, k1, s1, q);
         }
-        work[s0] = a0;
-        work[TW + s0] = a1;
+        work[s0] = mac_reduce(a0, md);
+        work[TW + s0] = mac_reduce(a1, md);
     }
     __syncthreads();
     load_block_twiddles<LOGN, LN>(tws, dc->tw[j].inv, blk0);
@@ -427,6 +455,8 @@ __global__ void __launch_bounds__(kKsGroups * kKsGroupThreads) k_ks_blocks_gathe
     u64 a0[PER], a1[PER];
 #pragma unroll
     for (int r = 0; r < PER; ++r) a0[r] = a1[r] = 0;
+    // lazy sums (see K2): at most kLazyMacTerms products < 2q between reductions
+    int pend = 0;
     for (int t = 0; t < nterm; ++t) {
         const int hi = HIDX[item * nterm + t];
         if (hi < 0) continue;
@@ -437,6 +467,15 @@ __global__ void __launch_bounds__(kKsGroups * kKsGroupThreads) k_ks_blocks_gathe
             // every load of the term first (gathered digit, both key words and
             // their companions for all PER elements), then the products
             u64 w[PER], k0[PER], k1[PER], c0[PER], c1[PER];
+            if (pend == kLazyMacTerms) {
+#pragma unroll
+                for (int r = 0; r < PER; ++r) {
+                    a0[r] = mac_reduce(a0[r], md);
+                    a1[r] = mac_reduce(a1[r], md);
+                }
+                pend = 1;
+            }
+            ++pend;
 #pragma unroll
             for (int r = 0; r < PER; ++r) {
                 const int x = threadIdx.x + T * r;
@@ -449,16 +488,16 @@ __global__ void __launch_bounds__(kKsGroups * kKsGroupThreads) k_ks_blocks_gathe
             }
 #pragma unroll
             for (int r = 0; r < PER; ++r) {
-                a0[r] = add_mod(a0[r], shoup_q(w[r], k0[r], c0[r], q), q);
-                a1[r] = add_mod(a1[r], shoup_q(w[r], k1[r], c1[r], q), q);
+                mac_term(a0[r], w[r], k0[r], c0[r], q);
+                mac_term(a1[r], w[r], k1[r], c1[r], q);
             }
         }
     }
 #pragma unroll
     for (int r = 0; r < PER; ++r) {
         const int s0 = saddr(threadIdx.x + T * r);
-        work[s0] = a0[r];
-        work[TW + s0] = a1[r];
+        work[s0] = mac_reduce(a0[r], md);
+        work[TW + s0] = mac_reduce(a1[r], md);
     }
     cp_async_wait_all();
     __syncthreads();
