@@ -77,6 +77,33 @@ int main() {
             if ((unsigned __int128)a * b < ((unsigned __int128)1 << (64 - __builtin_clzll(q) + 63))) check(a, b);
         }
     }
+    // the key MAC's lazy sums (ks_fused.cu mac_term / mac_reduce): 15 lazy Shoup
+    // products (< 2q each, any 64-bit first factor) summed without reduction,
+    // then one reduce_small_quot_q, for ciphertext moduli q = 1 mod 2^32
+    for (int k = 44; k <= 58; ++k) {
+        for (int trial = 0; trial < 4; ++trial) {
+            const u64 q = (((rng() >> (64 - (k - 32))) | (1ULL << (k - 33))) << 32) | 1ULL;
+            const Modulus m = make(q);
+            for (int rep = 0; rep < 2000; ++rep) {
+                u64 acc = 0;
+                unsigned __int128 want = 0;
+                for (int t = 0; t < 15; ++t) {
+                    const u64 key = rep == 0 ? q - 1 : rng() % q;
+                    const u64 w = rep == 0 ? ~0ULL : ((t & 1) ? rng() % q : rng());
+                    const u64 ksh = (u64)((((unsigned __int128)key) << 64) / q);
+                    const u64 term = shoup_lazy_q(w, key, ksh, q);
+                    if (term >= 2 * q) ++bad;
+                    acc += term;
+                    want += (unsigned __int128)w % q * key % q;
+                }
+                ++n;
+                if (acc >= (1ULL << (k + 5)) || reduce_small_quot_q(acc, m) != (u64)(want % q)) {
+                    if (bad < 10) std::printf("lazy mac q=%llu\n", (unsigned long long)q);
+                    ++bad;
+                }
+            }
+        }
+    }
     std::printf("%ld / %ld mismatches\n", bad, n);
     return bad ? 1 : 0;
 }
