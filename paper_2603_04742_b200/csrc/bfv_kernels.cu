@@ -182,9 +182,9 @@ __global__ void __launch_bounds__(Ntt2<LOGN>::TC, 256 / Ntt2<LOGN>::TC * 3) k_nt
     for (int r = 0; r < G::R1 * SEG / T; ++r) {
         const int i = threadIdx.x + T * r, c = i / SEG, h = i % SEG;
         u64 a0 = tile[c * LN + 2 * h], a1 = tile[c * LN + 2 * h + 1];
-        if (scale) {
-            a0 = shoup(a0, ni, nish, q);
-            a1 = shoup(a1, ni, nish, q);
+        if (scale) {  // ciphertext primes (= 1 mod 2^32): the cheaper quotient correction, same words
+            a0 = (u32)q == 1u ? shoup_q(a0, ni, nish, q) : shoup(a0, ni, nish, q);
+            a1 = (u32)q == 1u ? shoup_q(a1, ni, nish, q) : shoup(a1, ni, nish, q);
         }
         *reinterpret_cast<ulonglong2*>(dst + (size_t)c * G::R2 + col0 + 2 * h) = make_ulonglong2(a0, a1);
     }
