@@ -23,6 +23,7 @@
 #include <set>
 #include <stdexcept>
 
+#include "nvtx_range.hpp"
 #include "spmv/aggregate.hpp"
 
 namespace cssc {
@@ -600,12 +601,16 @@ void CloudPlan::record(std::vector<cudaEvent_t>* marks, u64* dec_d, const EncIn*
         marks->push_back(e);
     };
     mark();
-    ctx_.mul_relin_dev(A_, B_, PROD_, n_, T_.words(), Z_.words(), D2_.words(), DX_.words(),
-                       ACC_.words(), RLK_, enc, PRODY_ ? D2Y_.words() : nullptr, PRODY_, fold_ ? nd_ : 0,
-                       fold_ ? PRODY_ : nullptr);
+    {
+        const NvtxRange nv("cssc.cloud.multiply");
+        ctx_.mul_relin_dev(A_, B_, PROD_, n_, T_.words(), Z_.words(), D2_.words(), DX_.words(),
+                           ACC_.words(), RLK_, enc, PRODY_ ? D2Y_.words() : nullptr, PRODY_, fold_ ? nd_ : 0,
+                           fold_ ? PRODY_ : nullptr);
+    }
     mark();
     const bool fused = ctx_.fused_key_switch();
     for (size_t l = 0; l < levels_.size(); ++l) {
+        const NvtxRange nv("cssc.cloud.key_switch_stage");
         const Level& lv = levels_[l];
         KsY ky;
         ky.src = lv.ysrc;
@@ -635,6 +640,7 @@ void CloudPlan::record(std::vector<cudaEvent_t>* marks, u64* dec_d, const EncIn*
                          lv.extra, lv.yout, lv.xacc);
         mark();
     }
+    const NvtxRange nv_mask("cssc.cloud.mask_sum");
     std::vector<int> qidx(L);
     std::iota(qidx.begin(), qidx.end(), 0);
     NttJob fwd = ctx_.job(nullptr, MT_.words(), 2 * L, qidx);

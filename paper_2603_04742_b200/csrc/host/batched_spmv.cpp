@@ -17,6 +17,7 @@
 #include <utility>
 
 #include "host/host_pool.hpp"
+#include "nvtx_range.hpp"
 #include "spmv/gpu_backend.hpp"
 
 namespace spmv::detail {
@@ -59,6 +60,7 @@ BatchedSpmv::BatchedSpmv(spmvgpu_ctx* ctx, const HeParams& hp, std::span<const C
                          std::size_t chunk_size, PartyRole key_holder, bool partition, int rank, int world)
     : ctx_(ctx), hp_(hp), kh_(key_holder), nmat_(ms.size()), rank_(rank), world_(world) {
     if (world < 1 || rank < 0 || rank >= world) throw std::invalid_argument("shard: rank must be in [0, world)");
+    const cssc::NvtxRange nvtx_("cssc.pack");
     static const bool trace = std::getenv("CSSC_TRACE_E2E") != nullptr;
     const auto t0 = std::chrono::steady_clock::now();
     std::size_t nnz_total = 0, vec_total = 0;
@@ -510,6 +512,7 @@ BatchedSpmv::~BatchedSpmv() {
 }
 
 void BatchedSpmv::encrypt() {
+    const cssc::NvtxRange nvtx_("cssc.encrypt");
     const std::size_t n = dr_.size();
     if (!n) return;
     std::vector<spmvgpu_ct> all(lease_.a);
@@ -521,12 +524,14 @@ void BatchedSpmv::encrypt() {
 }
 
 void BatchedSpmv::ensure_plan() {
+    const cssc::NvtxRange nvtx_("cssc.plan");
     if (lease_.plan || dr_.empty()) return;
     check_status(spmvgpu_plan_create(ctx_, dr_.size(), dr_.data(), dc_.data(), dslice_.data(), n_dout_,
                                      lease_.a.data(), lease_.b.data(), lease_.out.data(), &lease_.plan));
 }
 
 void BatchedSpmv::cloud(bool use_graph) {
+    const cssc::NvtxRange nvtx_("cssc.cloud");
     if (dr_.empty()) return;
     ensure_plan();
     // a plan seen before is worth a graph: capture on its second use
@@ -552,6 +557,7 @@ std::vector<std::uint64_t> BatchedSpmv::result_words() {
 }
 
 std::vector<SpmvResult> BatchedSpmv::finish() {
+    const cssc::NvtxRange nvtx_("cssc.decrypt");
     if (world_ > 1)
         throw std::invalid_argument("finish: a sharded job holds partial results; sum result_words() across "
                                     "ranks and call finish_words()");
@@ -619,6 +625,7 @@ std::vector<SpmvResult> BatchedSpmv::finish_words_dev(std::uint64_t* dev) {
 }
 
 std::vector<SpmvResult> BatchedSpmv::run_all(std::int64_t* const* out_values) {
+    const cssc::NvtxRange nvtx_("cssc.spmv_batch");
     // first use of a plan, sharded jobs: the staged calls; a plan seen before:
     // pack, encryption, cloud, decryption and download as one graph launch
     if (dr_.empty() || world_ > 1 || lease_.uses == 0) {
